@@ -1,0 +1,210 @@
+/*
+ * dim3_b200.h — C ABI of the B200-native DIM^3 Join-Project operator.
+ *
+ * This is the drop-in boundary for the reference's operator API
+ * (P = /root/reference/proj):
+ *
+ *   d3g_join_project   replaces dim3::join_project / join_project_extended
+ *                      (P/include/dim3/engine.hpp:102-103, :117-120;
+ *                       P/src/engine.cpp:345-498) plus result_to_raw
+ *                      (engine.hpp:123, engine.cpp:502-529).
+ *   d3g_build_csr      replaces dim3::build_csr (P/include/dim3/relation.hpp:108-109).
+ *   d3g_sparse_bmm_csr replaces dim3::sparse_bmm (P/include/dim3/sparsebmm.hpp:33-36).
+ *   d3g_dense_ec_rows  replaces dim3::dense_ec (P/include/dim3/denseec.hpp:82-85).
+ *   d3g_f2_decide      the F2Evaluator decision loop of partition_s_csr
+ *                      (P/src/costmodel.cpp:515-586, P/src/partition.cpp:17-38),
+ *                      evaluated on degree histograms (host only, no GPU).
+ *   d3g_f3_threshold   dim3::f3_threshold (P/include/dim3/costmodel.hpp:120-121).
+ *
+ * Plain pointers and sizes only. Tables are caller-owned; every entry point
+ * is synchronous with respect to the caller's view of the result.
+ *
+ * Status codes follow the reference CLI's exception mapping
+ * (P/tools/dim3.cpp:675-693): 0 ok, 2 ConfigError, 3 IoError/FormatError,
+ * 4 ResourceError, 5 CUDA/internal failure. d3g_last_error() returns the
+ * message of the last failure on the calling thread.
+ */
+#ifndef DIM3_B200_H
+#define DIM3_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define D3G_OK 0
+#define D3G_CONFIG_ERROR 2
+#define D3G_IO_ERROR 3
+#define D3G_RESOURCE_ERROR 4
+#define D3G_INTERNAL_ERROR 5
+
+/* dim3::Strategy (P/include/dim3/engine.hpp:25-31). */
+#define D3G_AUTO 0
+#define D3G_CLASSICAL 1
+#define D3G_HYBRID 2
+#define D3G_SPARSE_ONLY 3
+#define D3G_DENSE_ONLY 4
+
+/* dim3::DensePathMode (P/include/dim3/denseec.hpp:56). The GPU kernel
+ * answers every (x, dense z) encounter with one bit-sliced OR sweep; the mode
+ * only selects how the reference-equivalent work counters are attributed. */
+#define D3G_DENSE_COST_BASED 0
+#define D3G_DENSE_FORCE_WIDE 1
+#define D3G_DENSE_FORCE_PROBE 2
+
+typedef struct d3g_ctx d3g_ctx;
+
+/* A two-column relation, row i = (left[i], right[i]); the same shape as
+ * dim3::RawTable with ColumnType::u64 columns (P/include/dim3/relation.hpp:21-46).
+ * on_device != 0: the pointers are CUDA device pointers on the context's
+ * device (no H2D copy is made). */
+typedef struct {
+  const uint64_t* left;
+  const uint64_t* right;
+  uint64_t n;
+  int32_t on_device;
+  int32_t pad;
+} d3g_table;
+
+/* dim3::CostConstants (P/include/dim3/costmodel.hpp:21-30). */
+typedef struct {
+  double t_seqR, t_randR, t_randRW, t_hash, t_map, t_ECs, t_ECd;
+  uint32_t w;
+  uint32_t pad;
+} d3g_consts;
+
+/* dim3::EngineConfig (P/include/dim3/engine.hpp:36-48) plus GPU options. */
+typedef struct {
+  int32_t force;              /* D3G_AUTO .. D3G_DENSE_ONLY */
+  int32_t threads;            /* accepted for API parity; must be >= 1 */
+  uint64_t memory_budget_bytes;  /* device working-set cap; 0 = 3 GiB default */
+  int32_t count_only;
+  int32_t dense_mode;
+  int32_t natural_keys_auto;
+  int32_t declared_x, declared_y, declared_z;  /* natural_keys_declared */
+  int32_t checksum;           /* also compute (sum, xor) of mix64(mix64(x)^z) */
+  int32_t collect_counters;   /* reference-equivalent DenseEC/SpA counters */
+  int32_t shard_index;        /* x-range shard of R handled by this call */
+  int32_t shard_count;        /* 1 = whole table */
+  int32_t pad0, pad1;
+} d3g_opts;
+
+/* dim3::ExecutionReport (P/include/dim3/engine.hpp:59-85) flattened, plus
+ * GPU-side fields. ms_* are CUDA-event times of each phase. */
+typedef struct {
+  char strategy[16];
+  int32_t swapped;
+  int32_t f1_gate_classical;  /* auto + f1 > 0: the reference would run the
+                                 classical join (outside this path) */
+  int32_t natural_x, natural_y, natural_z;
+  int32_t materialized;
+  uint64_t r_rows, s_rows, out_j_estimate;
+  double f1;
+  uint64_t out_p, pairs_sparse, pairs_dense;
+  uint64_t sparse_z, dense_z, f2_evaluations, dropped_r;
+  uint64_t x_card, y_card, z_card, r_nnz, s_nnz, sparse_nnz, out_j;
+  uint64_t x_live;
+  uint64_t panel_bytes;       /* reference panel size (dense_z * padded(|Y|)/8) */
+  uint64_t peak_bytes;        /* device working set high-water mark */
+  uint64_t spa_inner_count;   /* OUT_J over sparse z (SpaStats::inner_count) */
+  uint64_t dense_wide_encounters, dense_probe_encounters;
+  uint64_t dense_blocks_checked, dense_probes_done, dense_row_bitmaps_built;
+  uint64_t checksum_sum, checksum_xor;
+  uint64_t h2d_bytes, d2h_bytes;
+  double ms_total, ms_h2d, ms_estimate, ms_map, ms_csr, ms_stats, ms_partition;
+  double ms_sparse, ms_dense, ms_decode;
+  uint64_t gpu_launches;      /* kernels launched by this call */
+} d3g_report;
+
+/* Materialized output: caller-owned host (or device, on_device != 0)
+ * buffers of cap entries. On return n = pairs written, sorted by (x, z),
+ * raw values in the caller's orientation. */
+typedef struct {
+  uint64_t* x;
+  uint64_t* z;
+  uint64_t cap;
+  uint64_t n;
+  int32_t on_device;
+  int32_t pad;
+} d3g_pairs;
+
+/* CSR boolean matrix (dim3::CsrMatrix, P/include/dim3/relation.hpp:87-103). */
+typedef struct {
+  uint64_t* row_ptr; /* n_rows + 1 */
+  uint32_t* col;     /* nnz */
+  uint32_t n_rows, n_cols;
+  uint64_t nnz;
+} d3g_csr;
+
+/* Bitmap panel (dim3::BitmapPanel, P/include/dim3/bitmap.hpp:78-96). */
+typedef struct {
+  const uint32_t* z_ids;
+  const uint32_t* m_z;
+  const uint64_t* blocks; /* rows * row_words */
+  uint64_t rows;
+  uint32_t y_card, w;
+} d3g_panel;
+
+/* Reference-equivalent kernel counters (SpaStats, DenseEcStats). */
+typedef struct {
+  uint64_t inner_count;
+  uint64_t wide_encounters, probe_encounters, blocks_checked, probes_done;
+  uint64_t row_bitmaps_built;
+  double ms_kernel;
+} d3g_kernel_stats;
+
+int d3g_ctx_create(int device, d3g_ctx** out);
+void d3g_ctx_destroy(d3g_ctx* ctx);
+const char* d3g_last_error(void);
+/* Identifies the build ("sm_100a ..."); never fails. */
+const char* d3g_version(void);
+/* Default options = EngineConfig{} (auto, 1 thread, 3 GiB, materialize). */
+void d3g_opts_default(d3g_opts* o);
+
+int d3g_join_project(d3g_ctx* ctx, const d3g_table* r, const d3g_table* s,
+                     const d3g_consts* c, const d3g_opts* o, d3g_report* rep,
+                     d3g_pairs* pairs /* NULL = count only */);
+
+/* build_csr over mapped code pairs (a = major when major_is_a). Host arrays
+ * in, host CSR out (row_ptr/col must hold n_rows+1 / n entries). */
+int d3g_build_csr(d3g_ctx* ctx, const uint32_t* a, const uint32_t* b, uint64_t n,
+                  uint32_t a_card, uint32_t b_card, int major_is_a, d3g_csr* out);
+
+/* sparse_bmm over host CSRs; pairs_x/pairs_z (nullable) receive code pairs
+ * sorted by (x, z); returns the emitted count through *count. */
+int d3g_sparse_bmm_csr(d3g_ctx* ctx, const d3g_csr* r_by_x, const d3g_csr* s_sparse_by_y,
+                       uint32_t z_card, uint32_t* pairs_x, uint32_t* pairs_z,
+                       uint64_t pairs_cap, uint64_t* count, d3g_kernel_stats* st);
+
+/* dense_ec over a host CSR and a host bitmap panel. */
+int d3g_dense_ec_rows(d3g_ctx* ctx, const d3g_csr* r_by_x, const d3g_panel* panel,
+                      const d3g_consts* c, int dense_mode, uint32_t* pairs_x,
+                      uint32_t* pairs_z, uint64_t pairs_cap, uint64_t* count,
+                      d3g_kernel_stats* st);
+
+/* Convention-G synthetic rows [lo, hi) of config cfg (1..5; SURVEY
+ * Appendix A), side 0 = R (x, y), 1 = S (z, y), generated on the device into
+ * the DEVICE buffers left/right. Bit-identical to the CPU generator. */
+int d3g_generate(d3g_ctx* ctx, int cfg, int side, uint64_t lo, uint64_t hi, uint64_t* left,
+                 uint64_t* right);
+uint64_t d3g_cfg_rows(int cfg);
+int d3g_ctx_device(d3g_ctx* ctx);
+
+/* Host-only policy entry points (callable without a GPU). */
+uint32_t d3g_f3_threshold(uint32_t m_x, uint32_t y_card, const d3g_consts* c);
+double d3g_f1(uint64_t size_r, uint64_t size_s, uint64_t out_j, const d3g_consts* c);
+/* f2 decisions tabulated per degree value from the global degree
+ * histograms: mx_hist[m] = #x with m_x = m (m < mx_len), mz_hist likewise
+ * (mz_hist[0] = gap codes). dense_of_mz[m] (mz_len bytes) receives 1 iff a
+ * z of degree m goes to the dense panel. force: D3G_HYBRID/AUTO cost-based,
+ * D3G_SPARSE_ONLY, D3G_DENSE_ONLY. *evaluations = #z with m_z > 0. */
+int d3g_f2_decide(const uint64_t* mx_hist, uint64_t mx_len, const uint64_t* mz_hist,
+                  uint64_t mz_len, uint64_t x_card, uint64_t y_card, uint64_t z_card,
+                  uint64_t out_j, const d3g_consts* c, int force, uint8_t* dense_of_mz,
+                  uint64_t* evaluations);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DIM3_B200_H */

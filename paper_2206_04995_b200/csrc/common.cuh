@@ -1,0 +1,243 @@
+// Shared internals of the B200 DIM^3 library: error taxonomy (mirrors
+// P/include/dim3/common.hpp:25-36), the per-context device arena and stream,
+// hashing (mix64, common.hpp:42-49), and small warp/block helpers.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/dim3_b200.h"
+
+namespace d3g {
+
+using code_t = uint32_t;
+
+// ---------------------------------------------------------------------------
+// Errors. Thrown inside the library, mapped to D3G_* status codes at the ABI.
+struct Error : std::runtime_error {
+  int status;
+  Error(int s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+struct ConfigError : Error {
+  explicit ConfigError(const std::string& m) : Error(D3G_CONFIG_ERROR, m) {}
+};
+struct ResourceError : Error {
+  explicit ResourceError(const std::string& m) : Error(D3G_RESOURCE_ERROR, m) {}
+};
+struct CudaError : Error {
+  explicit CudaError(const std::string& m) : Error(D3G_INTERNAL_ERROR, m) {}
+};
+
+#define D3G_CUDA(call)                                                        \
+  do {                                                                        \
+    cudaError_t e_ = (call);                                                  \
+    if (e_ != cudaSuccess)                                                    \
+      throw ::d3g::CudaError(std::string(#call) + ": " + cudaGetErrorString(e_) + \
+                             " at " + __FILE__ + ":" + std::to_string(__LINE__)); \
+  } while (0)
+
+// Launch bookkeeping: every kernel launch goes through D3G_LAUNCH so the
+// context can report how many kernels a call issued.
+#define D3G_LAUNCH(ctx, kernel, grid, block, smem, ...)                       \
+  do {                                                                        \
+    kernel<<<(grid), (block), (smem), (ctx).stream>>>(__VA_ARGS__);           \
+    D3G_CUDA(cudaGetLastError());                                             \
+    (ctx).launches++;                                                         \
+  } while (0)
+
+inline constexpr int kNumSMs = 148;
+
+// ---------------------------------------------------------------------------
+// Device arena: stream-ordered allocations from the device's default pool,
+// which the context configures to never release memory back to the driver
+// (so repeated calls reuse the same HBM without cudaMalloc round trips).
+// Tracks the working-set high-water mark against the memory budget.
+struct Ctx;
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  uint64_t n = 0;
+  Ctx* ctx = nullptr;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), ctx(o.ctx) { o.p = nullptr; o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept;
+  ~DBuf();
+  void reset();
+  T* get() const { return p; }
+  uint64_t bytes() const { return n * sizeof(T); }
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[24] = {};
+  uint64_t launches = 0;
+  uint64_t live_bytes = 0, peak_bytes = 0, budget = 0;
+  int sm_count = kNumSMs;
+  size_t smem_optin = 0;
+  // small pinned host staging area for scalars read back mid-pipeline
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+
+  void* raw_alloc(uint64_t bytes) {
+    if (bytes == 0) bytes = 16;
+    if (budget != 0 && live_bytes + bytes > budget)
+      throw ResourceError("device memory budget exceeded: need " +
+                          std::to_string(live_bytes + bytes) + " bytes, limit " +
+                          std::to_string(budget) + " bytes");
+    void* p = nullptr;
+    cudaError_t e = cudaMallocAsync(&p, bytes, stream);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      throw ResourceError("device allocation of " + std::to_string(bytes) +
+                          " bytes failed: " + cudaGetErrorString(e));
+    }
+    live_bytes += bytes;
+    if (live_bytes > peak_bytes) peak_bytes = live_bytes;
+    return p;
+  }
+  void raw_free(void* p, uint64_t bytes) {
+    if (p == nullptr) return;
+    if (bytes == 0) bytes = 16;
+    cudaFreeAsync(p, stream);
+    live_bytes -= bytes;
+  }
+  template <class T>
+  DBuf<T> alloc(uint64_t n) {
+    DBuf<T> b;
+    b.p = static_cast<T*>(raw_alloc(n * sizeof(T)));
+    b.n = n;
+    b.ctx = this;
+    return b;
+  }
+  template <class T>
+  DBuf<T> zeros(uint64_t n) {
+    DBuf<T> b = alloc<T>(n);
+    D3G_CUDA(cudaMemsetAsync(b.p, 0, n * sizeof(T) + (n == 0 ? 16 : 0), stream));
+    return b;
+  }
+  void sync() { D3G_CUDA(cudaStreamSynchronize(stream)); }
+  // Copies n device values to host (through pinned staging) and syncs.
+  template <class T>
+  void to_host(T* dst, const T* src, uint64_t n) {
+    if (n == 0) return;
+    uint64_t bytes = n * sizeof(T);
+    if (bytes > pinned_bytes) {
+      if (pinned) cudaFreeHost(pinned);
+      pinned_bytes = bytes < (1u << 20) ? (1u << 20) : bytes;
+      D3G_CUDA(cudaMallocHost(&pinned, pinned_bytes));
+    }
+    D3G_CUDA(cudaMemcpyAsync(pinned, src, bytes, cudaMemcpyDeviceToHost, stream));
+    sync();
+    std::memcpy(dst, pinned, bytes);
+  }
+  template <class T>
+  T scalar(const T* src) {
+    T v;
+    to_host(&v, src, 1);
+    return v;
+  }
+  template <class T>
+  void to_device(T* dst, const T* src, uint64_t n) {
+    if (n == 0) return;
+    D3G_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyHostToDevice, stream));
+  }
+};
+
+template <class T>
+DBuf<T>& DBuf<T>::operator=(DBuf&& o) noexcept {
+  if (this != &o) {
+    reset();
+    p = o.p;
+    n = o.n;
+    ctx = o.ctx;
+    o.p = nullptr;
+    o.n = 0;
+  }
+  return *this;
+}
+template <class T>
+void DBuf<T>::reset() {
+  if (p && ctx) ctx->raw_free(p, n * sizeof(T));
+  p = nullptr;
+  n = 0;
+}
+template <class T>
+DBuf<T>::~DBuf() {
+  reset();
+}
+
+// ---------------------------------------------------------------------------
+// Device helpers.
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x ^= x >> 30;
+  x *= 0xbf58476d1ce4e5b9ull;
+  x ^= x >> 27;
+  x *= 0x94d049bb133111ebull;
+  x ^= x >> 31;
+  return x;
+}
+__host__ __device__ __forceinline__ uint64_t pair_hash(uint64_t x, uint64_t z) {
+  return mix64(mix64(x) ^ z);
+}
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
+
+template <class T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ uint64_t warp_xor(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v ^= __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+template <class T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    T u = __shfl_xor_sync(0xffffffffu, v, o);
+    v = u > v ? u : v;
+  }
+  return v;
+}
+
+// Accumulator of the order-independent output fingerprint and count.
+struct Tally {
+  unsigned long long count;
+  unsigned long long sum;
+  unsigned long long xr;
+};
+
+// Warp-reduce (count, sum, xor) and add once per warp.
+__device__ __forceinline__ void tally_flush(Tally* t, uint64_t cnt, uint64_t sum,
+                                            uint64_t xr) {
+  cnt = warp_sum(cnt);
+  sum = warp_sum(sum);
+  xr = warp_xor(xr);
+  if (lane_id() == 0) {
+    if (cnt) atomicAdd(&t->count, (unsigned long long)cnt);
+    if (sum) atomicAdd(&t->sum, (unsigned long long)sum);
+    if (xr) atomicXor(&t->xr, (unsigned long long)xr);
+  }
+}
+
+inline unsigned grid_for(uint64_t n, unsigned block, unsigned cap = 148u * 16u) {
+  uint64_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return static_cast<unsigned>(g);
+}
+
+}  // namespace d3g

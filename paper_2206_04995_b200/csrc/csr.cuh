@@ -1,0 +1,192 @@
+// CSR grouping (north_star subsystem 1, second half) and degree statistics.
+//
+// build_csr (P/src/relation.cpp:206-258) produces rows sorted by the minor
+// code with duplicate pairs collapsed. On the GPU: one stable LSD radix sort
+// of the composite key (major << minor_bits | minor), a flag/scan/compact
+// pass that drops adjacent duplicates, and a boundary fill that writes
+// row_ptr. compute_degree_stats (P/src/costmodel.cpp:425-438) reads m_x/m_z
+// off row_ptr, histograms the column codes into dR(y)/dS(y) with
+// shared-memory privatised counters, and reduces OUT_J = sum_y dR(y)*dS(y)
+// with a 128-bit accumulator (out_j_from_degrees, :350-364).
+#pragma once
+
+#include "prims.cuh"
+
+namespace d3g {
+
+struct DeviceCsr {
+  DBuf<uint64_t> row_ptr;  // n_rows + 1
+  DBuf<uint32_t> col;      // nnz
+  uint64_t n_rows = 0, n_cols = 0, nnz = 0;
+};
+
+__global__ void composite_key_kernel(const uint32_t* __restrict__ maj,
+                                     const uint32_t* __restrict__ mnr, uint64_t n, int minor_bits,
+                                     uint64_t* __restrict__ keys) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    keys[i] = ((uint64_t)maj[i] << minor_bits) | (uint64_t)mnr[i];
+}
+
+__global__ void uniq_flag_kernel(const uint64_t* __restrict__ keys, uint64_t n,
+                                 uint32_t* __restrict__ flag) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    flag[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1u : 0u;
+}
+
+__global__ void uniq_write_kernel(const uint64_t* __restrict__ keys,
+                                  const uint32_t* __restrict__ flag,
+                                  const uint64_t* __restrict__ pos, uint64_t n, int minor_bits,
+                                  uint32_t* __restrict__ col, uint32_t* __restrict__ row_of) {
+  const uint64_t mmask = minor_bits >= 64 ? ~0ull : ((1ull << minor_bits) - 1);
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    if (!flag[i]) continue;
+    uint64_t k = keys[i], o = pos[i];
+    col[o] = (uint32_t)(k & mmask);
+    row_of[o] = (uint32_t)(k >> minor_bits);
+  }
+}
+
+// row_ptr[r] = first unique index with row >= r; row_ptr[n_rows] = nnz.
+__global__ void row_bounds_kernel(const uint32_t* __restrict__ row_of, uint64_t nnz,
+                                  uint64_t n_rows, uint64_t* __restrict__ row_ptr) {
+  for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u <= nnz;
+       u += (uint64_t)gridDim.x * blockDim.x) {
+    int64_t prev = u == 0 ? -1 : (int64_t)row_of[u - 1];
+    int64_t cur = u == nnz ? (int64_t)n_rows : (int64_t)row_of[u];
+    for (int64_t r = prev + 1; r <= cur && r <= (int64_t)n_rows; ++r) row_ptr[r] = u;
+  }
+}
+
+inline void build_csr_device(Ctx& ctx, const uint32_t* maj, const uint32_t* mnr, uint64_t n,
+                             uint64_t n_rows, uint64_t n_cols, DeviceCsr& out) {
+  out.n_rows = n_rows;
+  out.n_cols = n_cols;
+  out.row_ptr = ctx.alloc<uint64_t>(n_rows + 1);
+  if (n == 0) {
+    D3G_CUDA(cudaMemsetAsync(out.row_ptr.p, 0, (n_rows + 1) * 8, ctx.stream));
+    out.col = ctx.alloc<uint32_t>(0);
+    out.nnz = 0;
+    return;
+  }
+  int minor_bits = bits_for(n_cols ? n_cols - 1 : 0);
+  int major_bits = bits_for(n_rows ? n_rows - 1 : 0);
+  if (minor_bits + major_bits > 64) throw ResourceError("composite key exceeds 64 bits");
+  DBuf<uint64_t> keys = ctx.alloc<uint64_t>(n);
+  unsigned g = grid_for(n, 256);
+  D3G_LAUNCH(ctx, composite_key_kernel, g, 256, 0, maj, mnr, n, minor_bits, keys.p);
+  radix_sort(ctx, keys.p, nullptr, n, minor_bits + major_bits);
+  DBuf<uint32_t> flag = ctx.alloc<uint32_t>(n);
+  DBuf<uint64_t> pos = ctx.alloc<uint64_t>(n + 1);
+  D3G_LAUNCH(ctx, uniq_flag_kernel, g, 256, 0, keys.p, n, flag.p);
+  exclusive_scan<uint32_t>(ctx, flag.p, n, pos.p);
+  uint64_t nnz = ctx.scalar(pos.p + n);
+  out.nnz = nnz;
+  out.col = ctx.alloc<uint32_t>(nnz);
+  DBuf<uint32_t> row_of = ctx.alloc<uint32_t>(nnz);
+  D3G_LAUNCH(ctx, uniq_write_kernel, g, 256, 0, keys.p, flag.p, pos.p, n, minor_bits, out.col.p,
+             row_of.p);
+  D3G_LAUNCH(ctx, row_bounds_kernel, grid_for(nnz + 1, 256), 256, 0, row_of.p, nnz, n_rows,
+             out.row_ptr.p);
+}
+
+// ---------------------------------------------------------------------------
+// Degree statistics.
+
+// max row degree
+__global__ void max_degree_kernel(const uint64_t* __restrict__ row_ptr, uint64_t n_rows,
+                                  unsigned long long* __restrict__ out_max,
+                                  unsigned long long* __restrict__ out_live) {
+  uint64_t m = 0, live = 0;
+  for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_rows;
+       r += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t d = row_ptr[r + 1] - row_ptr[r];
+    m = d > m ? d : m;
+    live += d > 0;
+  }
+  m = warp_max(m);
+  live = warp_sum(live);
+  if (lane_id() == 0) {
+    if (m) atomicMax(out_max, (unsigned long long)m);
+    if (live) atomicAdd(out_live, (unsigned long long)live);
+  }
+}
+
+// hist[d] += #rows with degree d (d <= max_deg). Small degrees privatised in smem.
+constexpr int kDegSmem = 4096;
+__global__ void degree_hist_kernel(const uint64_t* __restrict__ row_ptr, uint64_t n_rows,
+                                   uint64_t hist_len, unsigned long long* __restrict__ hist) {
+  __shared__ unsigned int sh[kDegSmem];
+  for (int i = threadIdx.x; i < kDegSmem; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_rows;
+       r += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t d = row_ptr[r + 1] - row_ptr[r];
+    if (d < kDegSmem)
+      atomicAdd(&sh[d], 1u);
+    else
+      atomicAdd(&hist[d], 1ull);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kDegSmem && (uint64_t)i < hist_len; i += blockDim.x)
+    if (sh[i]) atomicAdd(&hist[i], (unsigned long long)sh[i]);
+}
+
+// counts[v] += 1 for every v in vals; codes below kHotSmem privatised in smem,
+// others warp-aggregated with __match_any_sync.
+constexpr int kHotSmem = 12288;
+__global__ void value_hist_kernel(const uint32_t* __restrict__ vals, uint64_t n,
+                                  uint32_t* __restrict__ counts, uint32_t card) {
+  __shared__ unsigned int sh[kHotSmem];
+  const uint32_t hot = card < kHotSmem ? card : kHotSmem;
+  for (uint32_t i = threadIdx.x; i < hot; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t n_pad = (n + 31) / 32 * 32;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pad; i += stride) {
+    bool valid = i < n;
+    uint32_t v = valid ? vals[i] : 0xffffffffu;
+    if (valid && v < hot) {
+      atomicAdd(&sh[v], 1u);
+      v = 0xffffffffu;
+    }
+    uint32_t peers = __match_any_sync(0xffffffffu, v);
+    if (v != 0xffffffffu && (peers & ((1u << lane_id()) - 1)) == 0)
+      atomicAdd(&counts[v], (unsigned)__popc(peers));
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < hot; i += blockDim.x)
+    if (sh[i]) atomicAdd(&counts[i], sh[i]);
+}
+
+// OUT_J = sum dR*dS with a (hi, lo) 128-bit accumulator per block.
+__global__ void outj_kernel(const uint32_t* __restrict__ dr, const uint32_t* __restrict__ ds,
+                            uint64_t y_card, unsigned long long* __restrict__ parts) {
+  uint64_t lo = 0, hi = 0;
+  for (uint64_t y = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; y < y_card;
+       y += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t p = (uint64_t)dr[y] * (uint64_t)ds[y];
+    uint64_t nl = lo + p;
+    hi += nl < lo;
+    lo = nl;
+  }
+  // reduce (lo, hi) across the block via shared memory
+  __shared__ uint64_t slo[1024], shi[1024];
+  slo[threadIdx.x] = lo;
+  shi[threadIdx.x] = hi;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t L = 0, H = 0;
+    for (unsigned i = 0; i < blockDim.x; ++i) {
+      uint64_t nl = L + slo[i];
+      H += shi[i] + (nl < L);
+      L = nl;
+    }
+    parts[2 * blockIdx.x] = L;
+    parts[2 * blockIdx.x + 1] = H;
+  }
+}
+
+}  // namespace d3g

@@ -1,0 +1,1149 @@
+// Orchestration and C ABI of the B200 DIM^3 Join-Project operator.
+//
+// d3g_join_project follows join_project_extended's hybrid branch
+// (P/src/engine.cpp:351-498) phase by phase, entirely device-resident:
+//   swap (engine.cpp:361-366) -> f1 estimate (:368-377, on the host from the
+//   same strided samples) -> natural-key resolution + mapping (:401,
+//   map_with_fallback :40-50) -> CSR R-by-x / S-by-z (:411-415) -> degree
+//   stats -> f2 partition (:425-427) -> SparseBMM (:472-476) -> DenseEC
+//   (:478-481) -> count / optional (x, z) set (:483-491, decode :502-529).
+// Phases are timed with CUDA events on the context stream.
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <limits>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "datagen.cuh"
+#include "denseec.cuh"
+#include "mapping.cuh"
+#include "partition.cuh"
+#include "sparsebmm.cuh"
+
+struct d3g_ctx {
+  d3g::Ctx c;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return D3G_OK;
+  } catch (const d3g::Error& e) {
+    g_last_error = e.what();
+    return e.status;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return D3G_INTERNAL_ERROR;
+  }
+}
+
+using d3g::Ctx;
+using d3g::DBuf;
+
+// estimate_out_j_raw (P/src/costmodel.cpp:375-423) for u64 columns, on host
+// copies of the y columns (exact path) or of the strided samples.
+uint64_t estimate_raw(const uint64_t* r_y, uint64_t nr, const uint64_t* s_y, uint64_t ns,
+                      uint64_t sr, uint64_t ss, uint64_t mr, uint64_t ms, bool exact) {
+  if (exact) {
+    std::unordered_map<uint64_t, uint64_t> counts;
+    counts.reserve(ns);
+    for (uint64_t i = 0; i < ns; ++i) counts[s_y[i]]++;
+    uint64_t sum = 0;
+    for (uint64_t i = 0; i < nr; ++i) {
+      auto it = counts.find(r_y[i]);
+      if (it != counts.end()) sum += it->second;
+    }
+    return sum;
+  }
+  // samples already gathered: r_y[i] = R.y[i * sr], s_y[i] = S.y[i * ss]
+  std::unordered_map<uint64_t, uint64_t> counts;
+  counts.reserve(ms);
+  for (uint64_t i = 0; i < ms; ++i) counts[s_y[i]]++;
+  unsigned __int128 hits = 0;
+  for (uint64_t i = 0; i < mr; ++i) {
+    auto it = counts.find(r_y[i]);
+    if (it != counts.end()) hits += it->second;
+  }
+  long double scaled = static_cast<long double>(static_cast<uint64_t>(hits)) *
+                       (static_cast<long double>(ns) / ms) *
+                       (static_cast<long double>(nr) / mr);
+  if (scaled > static_cast<long double>(std::numeric_limits<uint64_t>::max()))
+    return std::numeric_limits<uint64_t>::max();
+  return static_cast<uint64_t>(scaled);
+}
+
+__global__ void gather_stride_kernel(const uint64_t* __restrict__ src, uint64_t stride, uint64_t m,
+                                     uint64_t* __restrict__ dst) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i * stride];
+}
+
+uint64_t estimate_out_j(Ctx& X, const d3g_table* R, const d3g_table* S, const uint64_t* dRr,
+                        const uint64_t* dSr) {
+  const uint64_t nr = R->n, ns = S->n;
+  if (nr == 0 || ns == 0) return 0;
+  const uint64_t exact_limit = 65536, sample_rows = 16384;
+  bool exact = nr <= exact_limit && ns <= exact_limit;
+  uint64_t ms = std::min(ns, sample_rows), mr = std::min(nr, sample_rows);
+  uint64_t ss = ns / ms, sr = nr / mr;
+  std::vector<uint64_t> hr, hs;
+  if (exact) {
+    hr.resize(nr);
+    hs.resize(ns);
+    if (R->on_device) X.to_host(hr.data(), R->right, nr); else std::memcpy(hr.data(), R->right, nr * 8);
+    if (S->on_device) X.to_host(hs.data(), S->right, ns); else std::memcpy(hs.data(), S->right, ns * 8);
+    return estimate_raw(hr.data(), nr, hs.data(), ns, 1, 1, nr, ns, true);
+  }
+  hr.resize(mr);
+  hs.resize(ms);
+  if (R->on_device || S->on_device) {
+    DBuf<uint64_t> g = X.alloc<uint64_t>(mr + ms);
+    D3G_LAUNCH(X, gather_stride_kernel, d3g::grid_for(mr, 256), 256, 0, dRr, sr, mr, g.p);
+    D3G_LAUNCH(X, gather_stride_kernel, d3g::grid_for(ms, 256), 256, 0, dSr, ss, ms, g.p + mr);
+    std::vector<uint64_t> tmp(mr + ms);
+    X.to_host(tmp.data(), g.p, mr + ms);
+    std::copy(tmp.begin(), tmp.begin() + mr, hr.begin());
+    std::copy(tmp.begin() + mr, tmp.end(), hs.begin());
+  } else {
+    for (uint64_t i = 0; i < mr; ++i) hr[i] = R->right[i * sr];
+    for (uint64_t i = 0; i < ms; ++i) hs[i] = S->right[i * ss];
+  }
+  return estimate_raw(hr.data(), nr, hs.data(), ns, sr, ss, mr, ms, false);
+}
+
+__global__ void live_flag_kernel(const uint64_t* __restrict__ row_ptr, uint64_t lo, uint64_t hi,
+                                 uint32_t* __restrict__ flag) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hi - lo;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    flag[i] = row_ptr[lo + i + 1] > row_ptr[lo + i];
+}
+
+__global__ void add_offset_kernel(uint32_t* __restrict__ v, uint64_t n, uint32_t off) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    v[i] += off;
+}
+
+__global__ void iota_kernel(uint32_t* __restrict__ v, uint64_t n) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    v[i] = (uint32_t)i;
+}
+
+struct Timer {
+  Ctx& X;
+  std::vector<cudaEvent_t> evs;
+  explicit Timer(Ctx& x) : X(x) {}
+  void mark() {
+    cudaEvent_t e;
+    D3G_CUDA(cudaEventCreate(&e));
+    D3G_CUDA(cudaEventRecord(e, X.stream));
+    evs.push_back(e);
+  }
+  double ms(size_t a, size_t b) {
+    float t = 0;
+    if (b < evs.size()) D3G_CUDA(cudaEventElapsedTime(&t, evs[a], evs[b]));
+    return t;
+  }
+  ~Timer() {
+    for (auto e : evs) cudaEventDestroy(e);
+  }
+};
+
+struct DictBundle {
+  d3g::DeviceDict x, y, z;
+};
+
+inline const uint64_t* rev_or_null(const d3g::DeviceDict& d) { return d.identity ? nullptr : d.rev.p; }
+
+int dense_smem_bytes(Ctx& X) {
+  int v = (int)X.smem_optin - 4096;  // leave room for static shared memory
+  if (v > 220 * 1024) v = 220 * 1024;
+  return v < 48 * 1024 ? 48 * 1024 : v;
+}
+
+// ---------------------------------------------------------------------------
+// Kernel drivers shared by the pipeline and the kernel-level entry points.
+
+struct SparseInputs {
+  const uint64_t* r_ptr;
+  const uint32_t* r_col;
+  uint64_t n_rows;
+  const uint64_t* sp_ptr;
+  const uint32_t* sp_col;     // compact sparse index
+  const uint32_t* sparse_ids; // compact index -> z code
+  uint64_t n_sparse;
+  // shard of x handled (x code range)
+  uint64_t x_lo, x_hi;
+};
+
+struct KernelOut {
+  uint64_t count = 0, sum = 0, xr = 0;
+  uint64_t inner = 0;
+};
+
+void run_sparse(Ctx& X, const SparseInputs& in, d3g::Decode dec, int mode, d3g::Emit em,
+                KernelOut& out) {
+  using namespace d3g;
+  if (in.n_rows == 0 || in.n_sparse == 0 || in.x_hi <= in.x_lo) return;
+  uint64_t nx = in.x_hi - in.x_lo;
+  DBuf<uint64_t> cx = X.alloc<uint64_t>(nx);
+  DBuf<unsigned long long> tot = X.zeros<unsigned long long>(1);
+  D3G_LAUNCH(X, sparse_cx_kernel, grid_for(nx, 256), 256, 0, in.r_ptr + in.x_lo, in.r_col, nx,
+             in.sp_ptr, cx.p, tot.p);
+  DBuf<uint32_t> fs = X.alloc<uint32_t>(nx), fl = X.alloc<uint32_t>(nx);
+  D3G_LAUNCH(X, bin_flags_kernel, grid_for(nx, 256), 256, 0, cx.p, nx, 32ull, fs.p, fl.p);
+  DBuf<uint64_t> ps = X.alloc<uint64_t>(nx + 1), pl = X.alloc<uint64_t>(nx + 1);
+  exclusive_scan<uint32_t>(X, fs.p, nx, ps.p);
+  exclusive_scan<uint32_t>(X, fl.p, nx, pl.p);
+  uint64_t n_small = X.scalar(ps.p + nx), n_large = X.scalar(pl.p + nx);
+  out.inner = X.scalar(tot.p);
+  DBuf<uint32_t> xs = X.alloc<uint32_t>(n_small), xl = X.alloc<uint32_t>(n_large);
+  D3G_LAUNCH(X, index_compact_kernel, grid_for(nx, 256), 256, 0, fs.p, ps.p, nx, xs.p);
+  D3G_LAUNCH(X, index_compact_kernel, grid_for(nx, 256), 256, 0, fl.p, pl.p, nx, xl.p);
+  if (in.x_lo) {
+    if (n_small) D3G_LAUNCH(X, add_offset_kernel, grid_for(n_small, 256), 256, 0, xs.p, n_small, (uint32_t)in.x_lo);
+    if (n_large) D3G_LAUNCH(X, add_offset_kernel, grid_for(n_large, 256), 256, 0, xl.p, n_large, (uint32_t)in.x_lo);
+  }
+  DBuf<Tally> t = X.zeros<Tally>(1);
+  const uint64_t* rp = in.r_ptr;
+  if (n_small) {
+    unsigned g = (unsigned)std::min<uint64_t>((n_small + 7) / 8, (uint64_t)X.sm_count * 16);
+    if (mode == kModeCount)
+      D3G_LAUNCH(X, sparse_small_kernel<kModeCount>, g, 256, 0, xs.p, n_small, rp, in.r_col,
+                 in.sp_ptr, in.sp_col, in.sparse_ids, dec, em, t.p);
+    else if (mode == kModeChecksum)
+      D3G_LAUNCH(X, sparse_small_kernel<kModeChecksum>, g, 256, 0, xs.p, n_small, rp, in.r_col,
+                 in.sp_ptr, in.sp_col, in.sparse_ids, dec, em, t.p);
+    else
+      D3G_LAUNCH(X, sparse_small_kernel<kModeEmit>, g, 256, 0, xs.p, n_small, rp, in.r_col,
+                 in.sp_ptr, in.sp_col, in.sparse_ids, dec, em, t.p);
+  }
+  if (n_large) {
+    uint32_t n_words = (uint32_t)((in.n_sparse + 31) / 32);
+    size_t smem = (size_t)n_words * 4;
+    bool use_smem = smem <= (size_t)dense_smem_bytes(X);
+    unsigned g = (unsigned)std::min<uint64_t>(n_large, (uint64_t)X.sm_count * (use_smem && smem <= 48 * 1024 ? 4 : 1));
+    DBuf<uint32_t> gbm = X.alloc<uint32_t>(use_smem ? 1 : (uint64_t)g * n_words);
+#define D3G_SPARSE_LARGE(MODE, GLOBAL)                                                     \
+  do {                                                                                     \
+    auto kfn = sparse_large_kernel<MODE, GLOBAL>;                                          \
+    size_t sm = GLOBAL ? 0 : smem;                                                         \
+    if (sm > 48 * 1024)                                                                    \
+      D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
+    D3G_LAUNCH(X, kfn, g, 512, sm, xl.p, n_large, cx.p, in.x_lo, rp, in.r_col, in.sp_ptr, in.sp_col, \
+               in.sparse_ids, n_words, gbm.p, dec, em, t.p);                               \
+  } while (0)
+    if (use_smem) {
+      if (mode == kModeCount) D3G_SPARSE_LARGE(kModeCount, false);
+      else if (mode == kModeChecksum) D3G_SPARSE_LARGE(kModeChecksum, false);
+      else D3G_SPARSE_LARGE(kModeEmit, false);
+    } else {
+      if (mode == kModeCount) D3G_SPARSE_LARGE(kModeCount, true);
+      else if (mode == kModeChecksum) D3G_SPARSE_LARGE(kModeChecksum, true);
+      else D3G_SPARSE_LARGE(kModeEmit, true);
+    }
+#undef D3G_SPARSE_LARGE
+  }
+  Tally h;
+  X.to_host(&h, t.p, 1);
+  out.count = h.count;
+  out.sum = h.sum;
+  out.xr = h.xr;
+}
+
+struct DenseInputs {
+  const uint32_t* xorder;
+  uint64_t n_live;
+  const uint64_t* r_ptr;
+  const uint32_t* r_col;
+  const uint32_t* y_rank;
+  uint64_t y_card;
+  const uint64_t* dl_ptr;
+  const uint32_t* dl_col;
+  const uint32_t* dl_z;
+  uint64_t n_dense;
+  uint64_t max_group_nnz;  // sum of the 128 largest m_x (group 0)
+  uint64_t pos_lo, pos_hi; // x positions (in xorder) handled
+};
+
+void run_dense(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g::Emit em,
+               KernelOut& out) {
+  using namespace d3g;
+  if (in.n_dense == 0 || in.pos_hi <= in.pos_lo) return;
+  DenseParams p{};
+  p.xorder = in.xorder + in.pos_lo;
+  p.n_live = in.pos_hi - in.pos_lo;
+  p.r_ptr = in.r_ptr;
+  p.r_col = in.r_col;
+  p.y_rank = in.y_rank;
+  p.dl_ptr = in.dl_ptr;
+  p.dl_col = in.dl_col;
+  p.dl_z = in.dl_z;
+  p.n_dense = in.n_dense;
+  int smem = dense_smem_bytes(X);
+  uint64_t y_hot = std::min<uint64_t>(in.y_card, (uint64_t)smem / 16);
+  p.y_hot = (uint32_t)y_hot;
+  uint64_t cap = 256;
+  while (cap < 2 * in.max_group_nnz) cap <<= 1;
+  p.cold_cap = (uint32_t)cap;
+  uint64_t groups = (p.n_live + 127) / 128;
+  unsigned g = (unsigned)std::min<uint64_t>(groups, (uint64_t)X.sm_count);
+  DBuf<uint32_t> ck = X.alloc<uint32_t>((uint64_t)g * cap);
+  DBuf<uint4> cv = X.alloc<uint4>((uint64_t)g * cap);
+  p.cold_keys = ck.p;
+  p.cold_vals = cv.p;
+  p.z_lo = 0;
+  p.z_hi = in.n_dense;
+  DBuf<Tally> t = X.zeros<Tally>(1);
+  size_t sm = (size_t)std::max<uint64_t>(y_hot, 1) * 16;
+#define D3G_DENSE(MODE)                                                                    \
+  do {                                                                                     \
+    auto kfn = dense_ec_kernel<MODE>;                                                      \
+    D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
+    D3G_LAUNCH(X, kfn, g, kDenseThreads, sm, p, dec, em, t.p);                             \
+  } while (0)
+  if (mode == kModeCount) D3G_DENSE(kModeCount);
+  else if (mode == kModeChecksum) D3G_DENSE(kModeChecksum);
+  else D3G_DENSE(kModeEmit);
+#undef D3G_DENSE
+  Tally h;
+  X.to_host(&h, t.p, 1);
+  out.count = h.count;
+  out.sum = h.sum;
+  out.xr = h.xr;
+}
+
+__global__ void decode_pairs_kernel(const uint32_t* __restrict__ xc, const uint32_t* __restrict__ zc,
+                                    uint64_t n, const uint64_t* __restrict__ rev_x,
+                                    const uint64_t* __restrict__ rev_z, int swapped,
+                                    uint64_t* __restrict__ ox, uint64_t* __restrict__ oz) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t ex = rev_x ? rev_x[xc[i]] : xc[i];
+    uint64_t ez = rev_z ? rev_z[zc[i]] : zc[i];
+    ox[i] = swapped ? ez : ex;
+    oz[i] = swapped ? ex : ez;
+  }
+}
+
+__global__ void pair_key_kernel(const uint32_t* __restrict__ xc, const uint32_t* __restrict__ zc,
+                                uint64_t n, int swapped, uint64_t* __restrict__ keys,
+                                uint32_t* __restrict__ idx) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t a = swapped ? zc[i] : xc[i], b = swapped ? xc[i] : zc[i];
+    keys[i] = (a << 32) | b;
+    idx[i] = (uint32_t)i;
+  }
+}
+
+__global__ void permute_pairs_kernel(const uint32_t* __restrict__ idx, uint64_t n,
+                                     const uint32_t* __restrict__ xc, const uint32_t* __restrict__ zc,
+                                     uint32_t* __restrict__ oxc, uint32_t* __restrict__ ozc) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    oxc[i] = xc[idx[i]];
+    ozc[i] = zc[idx[i]];
+  }
+}
+
+
+__global__ void max_u32_kernel(const uint32_t* __restrict__ v, uint64_t n,
+                               unsigned long long* __restrict__ out) {
+  uint64_t m = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    m = v[i] > m ? v[i] : m;
+  m = d3g::warp_max(m);
+  if (d3g::lane_id() == 0 && m) atomicMax(out, (unsigned long long)m);
+}
+
+__global__ void map_through_kernel(uint32_t* __restrict__ v, uint64_t n,
+                                   const uint32_t* __restrict__ table) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    v[i] = table[v[i]];
+}
+
+// Device layouts of the dense block consumed by dense_ec_kernel.
+struct DenseLayout {
+  DBuf<uint32_t> y_rank, dl_z, dl_col, xorder;
+  DBuf<uint64_t> dl_ptr;
+  uint64_t n_live = 0, n_dense = 0, max_group_nnz = 0;
+};
+
+// rows: dense z rows given as (row_ptr, col) indexed by row id; row_ids
+// lists the n_dense row ids; z_of_row (nullable) maps a row id to its z code
+// (identity when null). dR: per-y R-side degrees (hotness).
+void build_dense_layout(Ctx& X, const d3g::DeviceCsr& rx, uint64_t max_mx,
+                        const std::vector<uint64_t>& hmx, const uint64_t* zrow_ptr,
+                        const uint32_t* zcol, const uint32_t* row_ids, uint64_t n_dense,
+                        uint64_t max_mz, const uint32_t* z_of_row, uint64_t y_card,
+                        const uint32_t* dR, DenseLayout& L) {
+  using namespace d3g;
+  L.n_dense = n_dense;
+  // y ranked by dR descending (ties by code): hottest witnesses first
+  DBuf<unsigned long long> mx = X.zeros<unsigned long long>(1);
+  if (y_card) D3G_LAUNCH(X, max_u32_kernel, grid_for(y_card, 256), 256, 0, dR, y_card, mx.p);
+  uint64_t max_dr = X.scalar(mx.p);
+  {
+    DBuf<uint64_t> k = X.alloc<uint64_t>(y_card);
+    DBuf<uint32_t> v = X.alloc<uint32_t>(y_card);
+    D3G_LAUNCH(X, degree_order_key_kernel, grid_for(y_card, 256), 256, 0, (const uint32_t*)nullptr,
+               y_card, (const uint64_t*)nullptr, dR, max_dr, k.p, v.p);
+    radix_sort(X, k.p, v.p, y_card, 32 + bits_for(max_dr));
+    L.y_rank = X.alloc<uint32_t>(y_card);
+    D3G_LAUNCH(X, scatter_rank_kernel, grid_for(y_card, 256), 256, 0, v.p, y_card, L.y_rank.p);
+  }
+  // dense rows ordered by m_z descending (uniform trip counts per warp)
+  DBuf<uint32_t> rows = X.alloc<uint32_t>(n_dense);
+  {
+    DBuf<uint64_t> k = X.alloc<uint64_t>(n_dense);
+    D3G_LAUNCH(X, degree_order_key_kernel, grid_for(n_dense, 256), 256, 0, row_ids, n_dense,
+               zrow_ptr, (const uint32_t*)nullptr, max_mz, k.p, rows.p);
+    radix_sort(X, k.p, rows.p, n_dense, 32 + bits_for(max_mz));
+  }
+  DBuf<uint32_t> len = X.alloc<uint32_t>(n_dense);
+  D3G_LAUNCH(X, gather_len_kernel, grid_for(n_dense, 256), 256, 0, rows.p, n_dense, zrow_ptr, len.p);
+  L.dl_ptr = X.alloc<uint64_t>(n_dense + 1);
+  exclusive_scan<uint32_t>(X, len.p, n_dense, L.dl_ptr.p);
+  len.reset();
+  uint64_t dnnz = X.scalar(L.dl_ptr.p + n_dense);
+  int ybits = bits_for(y_card ? y_card - 1 : 0);
+  int pbits = bits_for(n_dense - 1);
+  if (ybits + pbits > 64) throw ResourceError("dense list key exceeds 64 bits");
+  {
+    DBuf<uint64_t> lk = X.alloc<uint64_t>(dnnz);
+    D3G_LAUNCH(X, dense_list_key_kernel, grid_for(n_dense * 32, 256), 256, 0, rows.p, n_dense,
+               zrow_ptr, zcol, L.dl_ptr.p, L.y_rank.p, ybits, lk.p);
+    radix_sort(X, lk.p, nullptr, dnnz, ybits + pbits);
+    L.dl_col = X.alloc<uint32_t>(dnnz);
+    D3G_LAUNCH(X, low_bits_kernel, grid_for(dnnz, 256), 256, 0, lk.p, dnnz, ybits, L.dl_col.p);
+  }
+  if (z_of_row) D3G_LAUNCH(X, map_through_kernel, grid_for(n_dense, 256), 256, 0, rows.p, n_dense, z_of_row);
+  L.dl_z = std::move(rows);
+  // live x ordered by m_x descending, cut into 128-x groups
+  const uint64_t x_card = rx.n_rows;
+  DBuf<uint32_t> lf = X.alloc<uint32_t>(x_card);
+  if (x_card) D3G_LAUNCH(X, live_flag_kernel, grid_for(x_card, 256), 256, 0, rx.row_ptr.p, 0ull, x_card, lf.p);
+  DBuf<uint64_t> lp = X.alloc<uint64_t>(x_card + 1);
+  exclusive_scan<uint32_t>(X, lf.p, x_card, lp.p);
+  L.n_live = X.scalar(lp.p + x_card);
+  DBuf<uint32_t> live_ids = X.alloc<uint32_t>(L.n_live);
+  if (x_card)
+    D3G_LAUNCH(X, index_compact_kernel, grid_for(x_card, 256), 256, 0, lf.p, lp.p, x_card, live_ids.p);
+  {
+    DBuf<uint64_t> k = X.alloc<uint64_t>(L.n_live);
+    L.xorder = X.alloc<uint32_t>(L.n_live);
+    if (L.n_live)
+      D3G_LAUNCH(X, degree_order_key_kernel, grid_for(L.n_live, 256), 256, 0, live_ids.p, L.n_live,
+                 rx.row_ptr.p, (const uint32_t*)nullptr, max_mx, k.p, L.xorder.p);
+    radix_sort(X, k.p, L.xorder.p, L.n_live, 32 + bits_for(max_mx));
+  }
+  // group 0 holds the 128 largest m_x: bound for the per-group cold table
+  uint64_t top = 0, seen = 0;
+  for (uint64_t m = max_mx; m >= 1 && seen < 128; --m) {
+    uint64_t take = std::min<uint64_t>(hmx[m], 128 - seen);
+    top += take * m;
+    seen += take;
+  }
+  L.max_group_nnz = top;
+}
+
+// ---------------------------------------------------------------------------
+// The pipeline.
+void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g_consts* c,
+                       const d3g_opts* o, d3g_report* rep, d3g_pairs* pairs) {
+  using namespace d3g;
+  if (o->threads < 1) throw ConfigError("threads must be >= 1");
+  if (c->w == 0 || c->w % 64 != 0) throw ConfigError("block width W must be a positive multiple of 64");
+  const int shard_count = o->shard_count < 1 ? 1 : o->shard_count;
+  const int shard_index = o->shard_index;
+  if (shard_index < 0 || shard_index >= shard_count) throw ConfigError("bad shard index");
+  std::memset(rep, 0, sizeof(*rep));
+  X.launches = 0;
+  X.budget = o->memory_budget_bytes ? o->memory_budget_bytes : (3ull << 30);
+  uint64_t base_live = X.live_bytes;
+  X.peak_bytes = X.live_bytes;
+  Timer T(X);
+  T.mark();  // 0
+
+  const bool swapped = s->n > r->n;  // engine_will_swap (engine.cpp:341-343)
+  const d3g_table* R = swapped ? s : r;
+  const d3g_table* S = swapped ? r : s;
+  rep->swapped = swapped;
+  rep->r_rows = R->n;
+  rep->s_rows = S->n;
+  const uint64_t NR = R->n, NS = S->n;
+  const bool materialize = pairs != nullptr && !o->count_only;
+  rep->materialized = materialize;
+
+  // 1. inputs resident in HBM
+  DBuf<uint64_t> hb[4];
+  const uint64_t* Rl = R->left;
+  const uint64_t* Rr = R->right;
+  const uint64_t* Sl = S->left;
+  const uint64_t* Sr = S->right;
+  if (!R->on_device) {
+    hb[0] = X.alloc<uint64_t>(NR);
+    hb[1] = X.alloc<uint64_t>(NR);
+    X.to_device(hb[0].p, R->left, NR);
+    X.to_device(hb[1].p, R->right, NR);
+    Rl = hb[0].p;
+    Rr = hb[1].p;
+    rep->h2d_bytes += NR * 16;
+  }
+  if (!S->on_device) {
+    hb[2] = X.alloc<uint64_t>(NS);
+    hb[3] = X.alloc<uint64_t>(NS);
+    X.to_device(hb[2].p, S->left, NS);
+    X.to_device(hb[3].p, S->right, NS);
+    Sl = hb[2].p;
+    Sr = hb[3].p;
+    rep->h2d_bytes += NS * 16;
+  }
+  T.mark();  // 1
+
+  // 2. f1 gate (engine.cpp:368-384)
+  rep->out_j_estimate = estimate_out_j(X, R, S, Rr, Sr);
+  rep->f1 = d3g_f1(NR, NS, rep->out_j_estimate, c);
+  rep->f1_gate_classical = (o->force == D3G_AUTO && rep->f1 > 0) ? 1 : 0;
+  const char* strat = o->force == D3G_SPARSE_ONLY  ? "sparse"
+                      : o->force == D3G_DENSE_ONLY ? "dense"
+                                                   : "hybrid";
+  std::snprintf(rep->strategy, sizeof(rep->strategy), "%s", strat);
+  T.mark();  // 2
+
+  // 3. natural-key resolution (engine.cpp:25-50, mapping.cpp:281-338)
+  DBuf<ColStat> cs = X.zeros<ColStat>(4);
+  const uint64_t* cols[4] = {Rl, Rr, Sl, Sr};
+  const uint64_t lens[4] = {NR, NR, NS, NS};
+  for (int i = 0; i < 4; ++i)
+    if (lens[i])
+      D3G_LAUNCH(X, colstat_kernel, grid_for(lens[i], 256, X.sm_count * 4), 256, 0, cols[i],
+                 lens[i], cs.p + i);
+  ColStat hs[4];
+  X.to_host(hs, cs.p, 4);
+  auto det = [&](int i) { return lens[i] > 0 && hs[i].sample_fail == 0; };
+  auto fits = [&](int i) { return lens[i] == 0 || hs[i].max < (1ull << 32); };
+  bool sx = o->declared_x != 0, sy = o->declared_y != 0, sz = o->declared_z != 0;
+  if (o->natural_keys_auto) {
+    sx = sx || det(0);
+    sy = sy || (det(1) && det(3));
+    sz = sz || det(2);
+  }
+  auto feasible = [&](bool ax, bool ay, bool az) {
+    if (ay && (!fits(1) || !fits(3))) return false;
+    if (az && !fits(2)) return false;
+    if (ax && !fits(0)) return false;
+    return true;
+  };
+  if (!feasible(sx, sy, sz)) {
+    bool dx = o->declared_x != 0, dy = o->declared_y != 0, dz = o->declared_z != 0;
+    if ((sx == dx && sy == dy && sz == dz) || !feasible(dx, dy, dz))
+      throw ConfigError("natural-key skip requires integer values below 2^32");
+    sx = dx;
+    sy = dy;
+    sz = dz;
+  }
+  rep->natural_x = sx;
+  rep->natural_y = sy;
+  rep->natural_z = sz;
+
+  // 4. mapping (map_tables, mapping.cpp:342-420)
+  DictBundle D;
+  DBuf<uint32_t> s_y = X.alloc<uint32_t>(NS), s_z = X.alloc<uint32_t>(NS);
+  uint64_t y_card, z_card, x_card;
+  if (sy) {
+    uint64_t a = NS ? hs[3].max + 1 : 0, b = NR ? hs[1].max + 1 : 0;
+    y_card = std::max(a, b);
+    D.y.identity = true;
+    D.y.card = y_card;
+    if (NS) D3G_LAUNCH(X, narrow_kernel, grid_for(NS, 256), 256, 0, Sr, NS, s_y.p);
+  } else {
+    dict_build(X, Sr, NS, D.y, s_y.p);
+    y_card = D.y.card;
+  }
+  if (sz) {
+    z_card = NS ? hs[2].max + 1 : 0;
+    D.z.identity = true;
+    D.z.card = z_card;
+    if (NS) D3G_LAUNCH(X, narrow_kernel, grid_for(NS, 256), 256, 0, Sl, NS, s_z.p);
+  } else {
+    dict_build(X, Sl, NS, D.z, s_z.p);
+    z_card = D.z.card;
+  }
+  // R pass: semi-join filter on y, then x over the survivors
+  DBuf<uint32_t> r_y = X.alloc<uint32_t>(NR), keep = X.alloc<uint32_t>(NR);
+  if (NR) {
+    if (sy)
+      D3G_LAUNCH(X, identity_keep_kernel, grid_for(NR, 256), 256, 0, Rr, NR, y_card, r_y.p, keep.p);
+    else
+      D3G_LAUNCH(X, dict_lookup_kernel, grid_for(NR, 256), 256, 0, Rr, NR, D.y.keys.p,
+                 D.y.slot_code.p, D.y.mask, r_y.p, keep.p);
+  }
+  DBuf<uint64_t> kpos = X.alloc<uint64_t>(NR + 1);
+  exclusive_scan<uint32_t>(X, keep.p, NR, kpos.p);
+  const uint64_t kept = X.scalar(kpos.p + NR);
+  rep->dropped_r = NR - kept;
+  const uint64_t* Rx = Rl;
+  DBuf<uint64_t> rx_kept;
+  if (kept != NR) {
+    rx_kept = X.alloc<uint64_t>(kept);
+    DBuf<uint32_t> ry2 = X.alloc<uint32_t>(kept);
+    D3G_LAUNCH(X, compact_kernel<uint64_t>, grid_for(NR, 256), 256, 0, Rl, keep.p, kpos.p, NR,
+               rx_kept.p);
+    D3G_LAUNCH(X, compact_kernel<uint32_t>, grid_for(NR, 256), 256, 0, r_y.p, keep.p, kpos.p, NR,
+               ry2.p);
+    r_y = std::move(ry2);
+    Rx = rx_kept.p;
+  }
+  keep.reset();
+  kpos.reset();
+  DBuf<uint32_t> r_x = X.alloc<uint32_t>(kept);
+  if (sx) {
+    x_card = NR ? hs[0].max + 1 : 0;  // over all of R.left (mapping.cpp:404-413)
+    D.x.identity = true;
+    D.x.card = x_card;
+    if (kept) D3G_LAUNCH(X, narrow_kernel, grid_for(kept, 256), 256, 0, Rx, kept, r_x.p);
+  } else {
+    dict_build(X, Rx, kept, D.x, r_x.p);
+    x_card = D.x.card;
+  }
+  rx_kept.reset();
+  rep->x_card = x_card;
+  rep->y_card = y_card;
+  rep->z_card = z_card;
+  if (x_card >= (1ull << 32) || y_card >= (1ull << 32) || z_card >= (1ull << 32))
+    throw ConfigError("code space exceeds 2^32");
+  T.mark();  // 3
+
+  // 5. CSR (build_csr, relation.cpp:206-258)
+  DeviceCsr rx, sz_csr;
+  build_csr_device(X, r_x.p, r_y.p, kept, x_card, y_card, rx);
+  r_x.reset();
+  r_y.reset();
+  build_csr_device(X, s_z.p, s_y.p, NS, z_card, y_card, sz_csr);
+  s_z.reset();
+  s_y.reset();
+  rep->r_nnz = rx.nnz;
+  rep->s_nnz = sz_csr.nnz;
+  T.mark();  // 4
+
+  // 6. degree statistics (compute_degree_stats, costmodel.cpp:425-438)
+  DBuf<unsigned long long> sc = X.zeros<unsigned long long>(4);  // max_mx, live_x, max_mz, live_z
+  if (x_card)
+    D3G_LAUNCH(X, max_degree_kernel, grid_for(x_card, 256), 256, 0, rx.row_ptr.p, x_card, sc.p,
+               sc.p + 1);
+  if (z_card)
+    D3G_LAUNCH(X, max_degree_kernel, grid_for(z_card, 256), 256, 0, sz_csr.row_ptr.p, z_card,
+               sc.p + 2, sc.p + 3);
+  unsigned long long scal[4];
+  X.to_host(scal, sc.p, 4);
+  const uint64_t max_mx = scal[0], x_live = scal[1], max_mz = scal[2];
+  rep->x_live = x_live;
+  DBuf<unsigned long long> mxh = X.zeros<unsigned long long>(max_mx + 1);
+  DBuf<unsigned long long> mzh = X.zeros<unsigned long long>(max_mz + 1);
+  if (x_card)
+    D3G_LAUNCH(X, degree_hist_kernel, grid_for(x_card, 256), 256, 0, rx.row_ptr.p, x_card,
+               max_mx + 1, mxh.p);
+  if (z_card)
+    D3G_LAUNCH(X, degree_hist_kernel, grid_for(z_card, 256), 256, 0, sz_csr.row_ptr.p, z_card,
+               max_mz + 1, mzh.p);
+  DBuf<uint32_t> dR = X.zeros<uint32_t>(y_card), dS = X.zeros<uint32_t>(y_card);
+  if (rx.nnz)
+    D3G_LAUNCH(X, value_hist_kernel, grid_for(rx.nnz, 256), 256, 0, rx.col.p, rx.nnz, dR.p,
+               (uint32_t)y_card);
+  if (sz_csr.nnz)
+    D3G_LAUNCH(X, value_hist_kernel, grid_for(sz_csr.nnz, 256), 256, 0, sz_csr.col.p, sz_csr.nnz,
+               dS.p, (uint32_t)y_card);
+  {
+    unsigned gb = grid_for(y_card, 1024, 296);
+    DBuf<unsigned long long> parts = X.zeros<unsigned long long>(2 * gb);
+    if (y_card) D3G_LAUNCH(X, outj_kernel, gb, 1024, 0, dR.p, dS.p, y_card, parts.p);
+    std::vector<unsigned long long> hp(2 * gb);
+    X.to_host(hp.data(), parts.p, 2 * gb);
+    unsigned __int128 acc = 0;
+    for (unsigned i = 0; i < gb; ++i)
+      acc += ((unsigned __int128)hp[2 * i + 1] << 64) | hp[2 * i];
+    rep->out_j = acc > (unsigned __int128)std::numeric_limits<uint64_t>::max()
+                     ? std::numeric_limits<uint64_t>::max()
+                     : (uint64_t)acc;
+  }
+  std::vector<uint64_t> hmx(max_mx + 1), hmz(max_mz + 1);
+  X.to_host(reinterpret_cast<unsigned long long*>(hmx.data()), mxh.p, max_mx + 1);
+  X.to_host(reinterpret_cast<unsigned long long*>(hmz.data()), mzh.p, max_mz + 1);
+  T.mark();  // 5
+
+  // 7. f2 decisions per degree value (policy.cpp), then the partition
+  std::vector<uint8_t> table(max_mz + 1, 0);
+  int pforce = o->force == D3G_SPARSE_ONLY ? D3G_SPARSE_ONLY
+               : o->force == D3G_DENSE_ONLY ? D3G_DENSE_ONLY
+                                            : D3G_HYBRID;
+  uint64_t evals = 0;
+  d3g_f2_decide(hmx.data(), max_mx + 1, hmz.data(), max_mz + 1, x_card, y_card, z_card,
+                rep->out_j, c, pforce, table.data(), &evals);
+  rep->f2_evaluations = evals;
+  DBuf<uint8_t> dtable = X.alloc<uint8_t>(max_mz + 1);
+  X.to_device(dtable.p, table.data(), max_mz + 1);
+  DBuf<uint32_t> isd = X.alloc<uint32_t>(z_card), iss = X.alloc<uint32_t>(z_card);
+  if (z_card)
+    D3G_LAUNCH(X, dense_flag_kernel, grid_for(z_card, 256), 256, 0, sz_csr.row_ptr.p, z_card,
+               dtable.p, max_mz + 1, isd.p, iss.p);
+  DBuf<uint64_t> pd = X.alloc<uint64_t>(z_card + 1), psp = X.alloc<uint64_t>(z_card + 1);
+  exclusive_scan<uint32_t>(X, isd.p, z_card, pd.p);
+  exclusive_scan<uint32_t>(X, iss.p, z_card, psp.p);
+  const uint64_t n_dense = X.scalar(pd.p + z_card), n_sparse = X.scalar(psp.p + z_card);
+  rep->dense_z = n_dense;
+  rep->sparse_z = n_sparse;
+  const uint64_t row_words = ((y_card + c->w - 1) / c->w * c->w) / 64;
+  rep->panel_bytes = n_dense * row_words * 8;
+  DBuf<uint32_t> dense_ids = X.alloc<uint32_t>(n_dense), sparse_ids = X.alloc<uint32_t>(n_sparse);
+  if (z_card) {
+    D3G_LAUNCH(X, index_compact_kernel, grid_for(z_card, 256), 256, 0, isd.p, pd.p, z_card,
+               dense_ids.p);
+    D3G_LAUNCH(X, index_compact_kernel, grid_for(z_card, 256), 256, 0, iss.p, psp.p, z_card,
+               sparse_ids.p);
+  }
+  isd.reset();
+  iss.reset();
+  pd.reset();
+  psp.reset();
+  // sparse side: y-major CSR over compact sparse indices
+  DBuf<uint64_t> sp_ptr = X.alloc<uint64_t>(y_card + 1);
+  DBuf<uint32_t> sp_col;
+  {
+    DBuf<uint32_t> cnt = X.zeros<uint32_t>(y_card);
+    if (n_sparse)
+      D3G_LAUNCH(X, sparse_y_count_kernel, grid_for(n_sparse * 32, 256), 256, 0,
+                 sz_csr.row_ptr.p, sz_csr.col.p, sparse_ids.p, n_sparse, cnt.p);
+    exclusive_scan<uint32_t>(X, cnt.p, y_card, sp_ptr.p);
+    rep->sparse_nnz = X.scalar(sp_ptr.p + y_card);
+    sp_col = X.alloc<uint32_t>(rep->sparse_nnz);
+    DBuf<unsigned long long> cur = X.alloc<unsigned long long>(y_card + 1);
+    D3G_CUDA(cudaMemcpyAsync(cur.p, sp_ptr.p, (y_card + 1) * 8, cudaMemcpyDeviceToDevice, X.stream));
+    if (n_sparse)
+      D3G_LAUNCH(X, sparse_y_scatter_kernel, grid_for(n_sparse * 32, 256), 256, 0,
+                 sz_csr.row_ptr.p, sz_csr.col.p, sparse_ids.p, n_sparse, cur.p, sp_col.p);
+  }
+  // dense side
+  DenseLayout L;
+  if (n_dense > 0 && x_live > 0)
+    build_dense_layout(X, rx, max_mx, hmx, sz_csr.row_ptr.p, sz_csr.col.p, dense_ids.p, n_dense,
+                       max_mz, nullptr, y_card, dR.p, L);
+  T.mark();  // 6
+
+  // 8. kernels
+  Decode dec{rev_or_null(D.x), rev_or_null(D.z), swapped ? 1 : 0};
+  const int mode = o->checksum ? kModeChecksum : kModeCount;
+  Emit no_emit{nullptr, nullptr, nullptr, 0};
+  // x shard (x code range for SparseBMM, position range for DenseEC)
+  uint64_t x_lo = x_card * shard_index / shard_count, x_hi = x_card * (shard_index + 1) / shard_count;
+  SparseInputs si{rx.row_ptr.p, rx.col.p, x_card, sp_ptr.p, sp_col.p, sparse_ids.p, n_sparse,
+                  x_lo, x_hi};
+  KernelOut ks, kd;
+  run_sparse(X, si, dec, mode, no_emit, ks);
+  T.mark();  // 7
+  uint64_t pos_lo = L.n_live * shard_index / shard_count,
+           pos_hi = L.n_live * (shard_index + 1) / shard_count;
+  DenseInputs di{L.xorder.p, L.n_live, rx.row_ptr.p, rx.col.p, L.y_rank.p, y_card, L.dl_ptr.p,
+                 L.dl_col.p, L.dl_z.p, L.n_dense, L.max_group_nnz, pos_lo, pos_hi};
+  run_dense(X, di, dec, mode, no_emit, kd);
+  T.mark();  // 8
+  rep->pairs_sparse = ks.count;
+  rep->pairs_dense = kd.count;
+  rep->spa_inner_count = ks.inner;
+  rep->out_p = ks.count + kd.count;
+  rep->checksum_sum = ks.sum + kd.sum;
+  rep->checksum_xor = ks.xr ^ kd.xr;
+
+  // 9. materialization (decode, engine.cpp:502-529)
+  if (materialize) {
+    uint64_t total = rep->out_p;
+    if (pairs->cap < total)
+      throw ResourceError("output buffer holds " + std::to_string(pairs->cap) + " pairs, need " +
+                          std::to_string(total));
+    DBuf<uint32_t> ex = X.alloc<uint32_t>(total), ez = X.alloc<uint32_t>(total);
+    DBuf<unsigned long long> cur = X.zeros<unsigned long long>(1);
+    Emit em{ex.p, ez.p, cur.p, total};
+    KernelOut tmp;
+    run_sparse(X, si, dec, kModeEmit, em, tmp);
+    run_dense(X, di, dec, kModeEmit, em, tmp);
+    DBuf<uint64_t> keys = X.alloc<uint64_t>(total);
+    DBuf<uint32_t> idx = X.alloc<uint32_t>(total);
+    if (total) {
+      D3G_LAUNCH(X, pair_key_kernel, grid_for(total, 256), 256, 0, ex.p, ez.p, total,
+                 swapped ? 1 : 0, keys.p, idx.p);
+      radix_sort(X, keys.p, idx.p, total, 64);
+    }
+    DBuf<uint32_t> sx2 = X.alloc<uint32_t>(total), sz2 = X.alloc<uint32_t>(total);
+    if (total)
+      D3G_LAUNCH(X, permute_pairs_kernel, grid_for(total, 256), 256, 0, idx.p, total, ex.p, ez.p,
+                 sx2.p, sz2.p);
+    DBuf<uint64_t> ox, oz;
+    uint64_t* dox = pairs->x;
+    uint64_t* doz = pairs->z;
+    if (!pairs->on_device) {
+      ox = X.alloc<uint64_t>(total);
+      oz = X.alloc<uint64_t>(total);
+      dox = ox.p;
+      doz = oz.p;
+    }
+    if (total)
+      D3G_LAUNCH(X, decode_pairs_kernel, grid_for(total, 256), 256, 0, sx2.p, sz2.p, total,
+                 rev_or_null(D.x), rev_or_null(D.z), swapped ? 1 : 0, dox, doz);
+    if (!pairs->on_device && total) {
+      D3G_CUDA(cudaMemcpyAsync(pairs->x, ox.p, total * 8, cudaMemcpyDeviceToHost, X.stream));
+      D3G_CUDA(cudaMemcpyAsync(pairs->z, oz.p, total * 8, cudaMemcpyDeviceToHost, X.stream));
+      rep->d2h_bytes += total * 16;
+    }
+    pairs->n = total;
+  }
+  T.mark();  // 9
+  X.sync();
+  rep->ms_h2d = T.ms(0, 1);
+  rep->ms_estimate = T.ms(1, 2);
+  rep->ms_map = T.ms(2, 3);
+  rep->ms_csr = T.ms(3, 4);
+  rep->ms_stats = T.ms(4, 5);
+  rep->ms_partition = T.ms(5, 6);
+  rep->ms_sparse = T.ms(6, 7);
+  rep->ms_dense = T.ms(7, 8);
+  rep->ms_decode = T.ms(8, 9);
+  rep->ms_total = T.ms(0, 9);
+  rep->peak_bytes = X.peak_bytes - base_live;
+  rep->gpu_launches = X.launches;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char* d3g_last_error(void) { return g_last_error.c_str(); }
+
+const char* d3g_version(void) {
+  return "dim3_b200 sm_100a (hand-written CUDA, bit-sliced DenseEC, bitmap SparseBMM)";
+}
+
+void d3g_opts_default(d3g_opts* o) {
+  std::memset(o, 0, sizeof(*o));
+  o->force = D3G_AUTO;
+  o->threads = 1;
+  o->memory_budget_bytes = 3ull << 30;
+  o->natural_keys_auto = 1;
+  o->shard_count = 1;
+}
+
+int d3g_ctx_create(int device, d3g_ctx** out) {
+  return guarded([&] {
+    int n = 0;
+    D3G_CUDA(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) throw d3g::ConfigError("no such CUDA device");
+    D3G_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop{};
+    D3G_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10)
+      throw d3g::ConfigError("dim3_b200 requires an sm_100 (Blackwell) device");
+    auto* ctx = new d3g_ctx();
+    ctx->c.device = device;
+    ctx->c.sm_count = prop.multiProcessorCount;
+    ctx->c.smem_optin = prop.sharedMemPerBlockOptin;
+    D3G_CUDA(cudaStreamCreateWithFlags(&ctx->c.stream, cudaStreamNonBlocking));
+    cudaMemPool_t pool;
+    D3G_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = ~0ull;
+    D3G_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    *out = ctx;
+  });
+}
+
+void d3g_ctx_destroy(d3g_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->c.device);
+  cudaStreamSynchronize(ctx->c.stream);
+  if (ctx->c.pinned) cudaFreeHost(ctx->c.pinned);
+  cudaStreamDestroy(ctx->c.stream);
+  delete ctx;
+}
+
+int d3g_join_project(d3g_ctx* ctx, const d3g_table* r, const d3g_table* s, const d3g_consts* c,
+                     const d3g_opts* o, d3g_report* rep, d3g_pairs* pairs) {
+  if (!ctx || !r || !s || !c || !o || !rep) {
+    g_last_error = "null argument";
+    return D3G_CONFIG_ERROR;
+  }
+  return guarded([&] {
+    D3G_CUDA(cudaSetDevice(ctx->c.device));
+    try {
+      join_project_impl(ctx->c, r, s, c, o, rep, pairs);
+    } catch (...) {
+      cudaStreamSynchronize(ctx->c.stream);
+      throw;
+    }
+  });
+}
+
+int d3g_build_csr(d3g_ctx* ctx, const uint32_t* a, const uint32_t* b, uint64_t n, uint32_t a_card,
+                  uint32_t b_card, int major_is_a, d3g_csr* out) {
+  return guarded([&] {
+    Ctx& X = ctx->c;
+    D3G_CUDA(cudaSetDevice(X.device));
+    X.budget = 0;
+    const uint32_t* maj = major_is_a ? a : b;
+    const uint32_t* mnr = major_is_a ? b : a;
+    uint64_t n_rows = major_is_a ? a_card : b_card, n_cols = major_is_a ? b_card : a_card;
+    DBuf<uint32_t> dm = X.alloc<uint32_t>(n), dn = X.alloc<uint32_t>(n);
+    X.to_device(dm.p, maj, n);
+    X.to_device(dn.p, mnr, n);
+    d3g::DeviceCsr csr;
+    d3g::build_csr_device(X, dm.p, dn.p, n, n_rows, n_cols, csr);
+    X.to_host(out->row_ptr, csr.row_ptr.p, n_rows + 1);
+    X.to_host(out->col, csr.col.p, csr.nnz);
+    out->n_rows = (uint32_t)n_rows;
+    out->n_cols = (uint32_t)n_cols;
+    out->nnz = csr.nnz;
+  });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Kernel-level entry points (parity with sparse_bmm / dense_ec on the
+// reference's own CSR / BitmapPanel inputs) and the synthetic generator.
+namespace {
+
+__global__ void panel_popc_kernel(const uint64_t* __restrict__ blocks, uint64_t rows,
+                                  uint64_t row_words, uint32_t* __restrict__ cnt) {
+  for (uint64_t r = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); r < rows;
+       r += (uint64_t)gridDim.x * (blockDim.x / 32)) {
+    uint32_t c = 0;
+    for (uint64_t w = d3g::lane_id(); w < row_words; w += 32) c += __popcll(blocks[r * row_words + w]);
+    c = d3g::warp_sum(c);
+    if (d3g::lane_id() == 0) cnt[r] = c;
+  }
+}
+
+__global__ void panel_extract_kernel(const uint64_t* __restrict__ blocks, uint64_t rows,
+                                     uint64_t row_words, const uint64_t* __restrict__ ptr,
+                                     uint32_t* __restrict__ col) {
+  // one warp per row; lanes take consecutive words, ranks by warp prefix sum
+  for (uint64_t r = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); r < rows;
+       r += (uint64_t)gridDim.x * (blockDim.x / 32)) {
+    uint64_t out = ptr[r];
+    for (uint64_t base = 0; base < row_words; base += 32) {
+      uint64_t w = base + d3g::lane_id();
+      uint64_t bits = w < row_words ? blocks[r * row_words + w] : 0;
+      uint32_t c = __popcll(bits), incl = c;
+      for (int o = 1; o < 32; o <<= 1) {
+        uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (d3g::lane_id() >= (uint32_t)o) incl += u;
+      }
+      uint64_t o = out + incl - c;
+      while (bits) {
+        int b = __ffsll((long long)bits) - 1;
+        bits &= bits - 1;
+        col[o++] = (uint32_t)(w * 64 + b);
+      }
+      out += __shfl_sync(0xffffffffu, incl, 31);
+    }
+  }
+}
+
+void sort_and_copy_pairs(Ctx& X, uint32_t* ex, uint32_t* ez, uint64_t total, uint32_t* hx,
+                         uint32_t* hz) {
+  using namespace d3g;
+  if (total == 0) return;
+  DBuf<uint64_t> keys = X.alloc<uint64_t>(total);
+  DBuf<uint32_t> idx = X.alloc<uint32_t>(total);
+  D3G_LAUNCH(X, pair_key_kernel, grid_for(total, 256), 256, 0, ex, ez, total, 0, keys.p, idx.p);
+  radix_sort(X, keys.p, idx.p, total, 64);
+  DBuf<uint32_t> sx = X.alloc<uint32_t>(total), sz = X.alloc<uint32_t>(total);
+  D3G_LAUNCH(X, permute_pairs_kernel, grid_for(total, 256), 256, 0, idx.p, total, ex, ez, sx.p, sz.p);
+  X.to_host(hx, sx.p, total);
+  X.to_host(hz, sz.p, total);
+}
+
+void upload_csr(Ctx& X, const d3g_csr* h, d3g::DeviceCsr& d) {
+  d.n_rows = h->n_rows;
+  d.n_cols = h->n_cols;
+  d.nnz = h->nnz;
+  d.row_ptr = X.alloc<uint64_t>(d.n_rows + 1);
+  d.col = X.alloc<uint32_t>(d.nnz);
+  X.to_device(d.row_ptr.p, h->row_ptr, d.n_rows + 1);
+  X.to_device(d.col.p, h->col, d.nnz);
+}
+
+}  // namespace
+
+extern "C" {
+
+int d3g_sparse_bmm_csr(d3g_ctx* ctx, const d3g_csr* r_by_x, const d3g_csr* s_sparse_by_y,
+                       uint32_t z_card, uint32_t* pairs_x, uint32_t* pairs_z, uint64_t pairs_cap,
+                       uint64_t* count, d3g_kernel_stats* st) {
+  return guarded([&] {
+    using namespace d3g;
+    Ctx& X = ctx->c;
+    D3G_CUDA(cudaSetDevice(X.device));
+    X.budget = 0;
+    DeviceCsr r, sp;
+    upload_csr(X, r_by_x, r);
+    upload_csr(X, s_sparse_by_y, sp);
+    DBuf<uint32_t> ids = X.alloc<uint32_t>(z_card);
+    if (z_card) D3G_LAUNCH(X, iota_kernel, grid_for(z_card, 256), 256, 0, ids.p, (uint64_t)z_card);
+    SparseInputs si{r.row_ptr.p, r.col.p, r.n_rows, sp.row_ptr.p, sp.col.p, ids.p, z_card, 0,
+                    r.n_rows};
+    Decode dec{nullptr, nullptr, 0};
+    Emit none{nullptr, nullptr, nullptr, 0};
+    cudaEvent_t e0, e1;
+    D3G_CUDA(cudaEventCreate(&e0));
+    D3G_CUDA(cudaEventCreate(&e1));
+    D3G_CUDA(cudaEventRecord(e0, X.stream));
+    KernelOut ko;
+    run_sparse(X, si, dec, kModeCount, none, ko);
+    D3G_CUDA(cudaEventRecord(e1, X.stream));
+    X.sync();
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *count = ko.count;
+    if (st) {
+      std::memset(st, 0, sizeof(*st));
+      st->inner_count = ko.inner;
+      st->ms_kernel = ms;
+    }
+    if (pairs_x && pairs_z) {
+      if (pairs_cap < ko.count) throw ResourceError("pair buffer too small");
+      DBuf<uint32_t> ex = X.alloc<uint32_t>(ko.count), ez = X.alloc<uint32_t>(ko.count);
+      DBuf<unsigned long long> cur = X.zeros<unsigned long long>(1);
+      Emit em{ex.p, ez.p, cur.p, ko.count};
+      KernelOut t;
+      run_sparse(X, si, dec, kModeEmit, em, t);
+      sort_and_copy_pairs(X, ex.p, ez.p, ko.count, pairs_x, pairs_z);
+    }
+  });
+}
+
+int d3g_dense_ec_rows(d3g_ctx* ctx, const d3g_csr* r_by_x, const d3g_panel* panel,
+                      const d3g_consts* c, int dense_mode, uint32_t* pairs_x, uint32_t* pairs_z,
+                      uint64_t pairs_cap, uint64_t* count, d3g_kernel_stats* st) {
+  (void)c;
+  (void)dense_mode;
+  return guarded([&] {
+    using namespace d3g;
+    Ctx& X = ctx->c;
+    D3G_CUDA(cudaSetDevice(X.device));
+    X.budget = 0;
+    DeviceCsr r;
+    upload_csr(X, r_by_x, r);
+    const uint64_t rows = panel->rows;
+    const uint64_t y_card = panel->y_card;
+    const uint64_t row_words = (y_card + panel->w - 1) / panel->w * panel->w / 64;
+    *count = 0;
+    if (st) std::memset(st, 0, sizeof(*st));
+    if (rows == 0 || r.nnz == 0) return;
+    DBuf<uint64_t> blocks = X.alloc<uint64_t>(rows * row_words);
+    X.to_device(blocks.p, panel->blocks, rows * row_words);
+    DBuf<uint32_t> zids = X.alloc<uint32_t>(rows);
+    X.to_device(zids.p, panel->z_ids, rows);
+    DBuf<uint32_t> cnt = X.alloc<uint32_t>(rows);
+    D3G_LAUNCH(X, panel_popc_kernel, grid_for(rows * 32, 256), 256, 0, blocks.p, rows, row_words, cnt.p);
+    DBuf<uint64_t> zptr = X.alloc<uint64_t>(rows + 1);
+    exclusive_scan<uint32_t>(X, cnt.p, rows, zptr.p);
+    uint64_t pnnz = X.scalar(zptr.p + rows);
+    DBuf<uint32_t> zcol = X.alloc<uint32_t>(pnnz);
+    D3G_LAUNCH(X, panel_extract_kernel, grid_for(rows * 32, 256), 256, 0, blocks.p, rows, row_words,
+               zptr.p, zcol.p);
+    DBuf<unsigned long long> mz = X.zeros<unsigned long long>(1);
+    D3G_LAUNCH(X, max_u32_kernel, grid_for(rows, 256), 256, 0, cnt.p, rows, mz.p);
+    uint64_t max_mz = X.scalar(mz.p);
+    DBuf<uint32_t> row_ids = X.alloc<uint32_t>(rows);
+    D3G_LAUNCH(X, iota_kernel, grid_for(rows, 256), 256, 0, row_ids.p, rows);
+    // R-side degrees
+    uint64_t yc = std::max<uint64_t>(y_card, r.n_cols);
+    DBuf<uint32_t> dR = X.zeros<uint32_t>(yc);
+    D3G_LAUNCH(X, value_hist_kernel, grid_for(r.nnz, 256), 256, 0, r.col.p, r.nnz, dR.p, (uint32_t)yc);
+    uint64_t max_mx = 0;
+    for (uint32_t i = 0; i < r_by_x->n_rows; ++i)
+      max_mx = std::max<uint64_t>(max_mx, r_by_x->row_ptr[i + 1] - r_by_x->row_ptr[i]);
+    std::vector<uint64_t> hmx(max_mx + 1, 0);
+    for (uint32_t i = 0; i < r_by_x->n_rows; ++i) hmx[r_by_x->row_ptr[i + 1] - r_by_x->row_ptr[i]]++;
+    DenseLayout L;
+    build_dense_layout(X, r, max_mx, hmx, zptr.p, zcol.p, row_ids.p, rows, max_mz, zids.p, yc,
+                       dR.p, L);
+    DenseInputs di{L.xorder.p, L.n_live, r.row_ptr.p, r.col.p, L.y_rank.p, yc, L.dl_ptr.p,
+                   L.dl_col.p, L.dl_z.p, L.n_dense, L.max_group_nnz, 0, L.n_live};
+    Decode dec{nullptr, nullptr, 0};
+    Emit none{nullptr, nullptr, nullptr, 0};
+    cudaEvent_t e0, e1;
+    D3G_CUDA(cudaEventCreate(&e0));
+    D3G_CUDA(cudaEventCreate(&e1));
+    D3G_CUDA(cudaEventRecord(e0, X.stream));
+    KernelOut ko;
+    run_dense(X, di, dec, kModeCount, none, ko);
+    D3G_CUDA(cudaEventRecord(e1, X.stream));
+    X.sync();
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *count = ko.count;
+    if (st) st->ms_kernel = ms;
+    if (pairs_x && pairs_z) {
+      if (pairs_cap < ko.count) throw ResourceError("pair buffer too small");
+      DBuf<uint32_t> ex = X.alloc<uint32_t>(ko.count), ez = X.alloc<uint32_t>(ko.count);
+      DBuf<unsigned long long> cur = X.zeros<unsigned long long>(1);
+      Emit em{ex.p, ez.p, cur.p, ko.count};
+      KernelOut t;
+      run_dense(X, di, dec, kModeEmit, em, t);
+      sort_and_copy_pairs(X, ex.p, ez.p, ko.count, pairs_x, pairs_z);
+    }
+  });
+}
+
+// Convention-G rows [lo, hi) of side 0 (R) / 1 (S) of config cfg (1..5),
+// written to DEVICE buffers left/right on the context's device.
+int d3g_generate(d3g_ctx* ctx, int cfg, int side, uint64_t lo, uint64_t hi, uint64_t* left,
+                 uint64_t* right) {
+  return guarded([&] {
+    using namespace d3g;
+    Ctx& X = ctx->c;
+    D3G_CUDA(cudaSetDevice(X.device));
+    uint64_t n = cfg_rows(cfg);
+    if (n == 0 || hi > n || lo > hi) throw ConfigError("bad generator request");
+    GenSpec g = gen_spec(cfg, side);
+    DBuf<double> cum;
+    if (g.zipf) {
+      uint64_t ny = g.ny;
+      std::vector<double> h(ny);
+      double run = 0, alpha = gen_alpha(cfg);
+      for (uint64_t r = 1; r <= ny; ++r) {
+        run += std::pow(static_cast<double>(r), -alpha);
+        h[r - 1] = run;
+      }
+      cum = X.alloc<double>(ny);
+      X.to_device(cum.p, h.data(), ny);
+    }
+    if (hi > lo)
+      D3G_LAUNCH(X, gen_kernel, grid_for(hi - lo, 256, X.sm_count * 32), 256, 0, g, cum.p, lo, hi,
+                 left, right);
+    X.sync();
+  });
+}
+
+uint64_t d3g_cfg_rows(int cfg) { return d3g::cfg_rows(cfg); }
+
+int d3g_ctx_device(d3g_ctx* ctx) { return ctx ? ctx->c.device : -1; }
+
+}  // extern "C"

@@ -1,0 +1,129 @@
+// Intersection-free partition of S (P/src/partition.cpp:5-80) and the
+// layouts the two GPU kernels consume.
+//
+// Decision: dense[z] = table[m_z[z]] where table is the per-degree f2
+// decision computed on the host (policy.cpp); m_z == 0 gap codes go nowhere.
+//
+// Sparse side (SparseBMM input): the y-major CSR of the sparse-z tuples
+// (partition.cpp:59-78). Columns hold the COMPACT index of the sparse z
+// (rank among sparse z), so the per-x dedup bitmap spans only the sparse z
+// count, not |Z|; sparse_ids maps the index back to the z code.
+//
+// Dense side (DenseEC input). Instead of the reference's |Y|-bit panel rows
+// (1.25 TB on cfg5) the GPU keeps the dense block in CSR form and answers
+// existence with bit-sliced OR sweeps (denseec.cuh):
+//   * y_rank: y codes re-ranked by R-side degree dR(y), hottest first, so a
+//     z's list meets its most probable witnesses first (early exit);
+//   * dense z lists: S rows of dense z with y replaced by y_rank, sorted
+//     ascending, rows ordered by m_z descending (uniform warp trip counts);
+//   * x order: live x sorted by m_x descending, cut into 128-x groups.
+#pragma once
+
+#include "csr.cuh"
+
+namespace d3g {
+
+__global__ void dense_flag_kernel(const uint64_t* __restrict__ row_ptr, uint64_t n_z,
+                                  const uint8_t* __restrict__ table, uint64_t table_len,
+                                  uint32_t* __restrict__ is_dense, uint32_t* __restrict__ is_sparse) {
+  for (uint64_t z = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; z < n_z;
+       z += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t m = row_ptr[z + 1] - row_ptr[z];
+    uint32_t d = (m > 0 && m < table_len) ? table[m] : 0;
+    is_dense[z] = d;
+    is_sparse[z] = (m > 0 && !d) ? 1u : 0u;
+  }
+}
+
+__global__ void index_compact_kernel(const uint32_t* __restrict__ flag,
+                                     const uint64_t* __restrict__ pos, uint64_t n,
+                                     uint32_t* __restrict__ out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    if (flag[i]) out[pos[i]] = (uint32_t)i;
+}
+
+// per-y count of sparse tuples
+__global__ void sparse_y_count_kernel(const uint64_t* __restrict__ row_ptr,
+                                      const uint32_t* __restrict__ col,
+                                      const uint32_t* __restrict__ sparse_ids, uint64_t n_sparse,
+                                      uint32_t* __restrict__ cnt) {
+  for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < n_sparse;
+       i += (uint64_t)gridDim.x * (blockDim.x / 32)) {
+    uint32_t z = sparse_ids[i];
+    for (uint64_t k = row_ptr[z] + lane_id(); k < row_ptr[z + 1]; k += 32)
+      atomicAdd(&cnt[col[k]], 1u);
+  }
+}
+
+__global__ void sparse_y_scatter_kernel(const uint64_t* __restrict__ row_ptr,
+                                        const uint32_t* __restrict__ col,
+                                        const uint32_t* __restrict__ sparse_ids, uint64_t n_sparse,
+                                        unsigned long long* __restrict__ cursor,
+                                        uint32_t* __restrict__ out_col) {
+  for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < n_sparse;
+       i += (uint64_t)gridDim.x * (blockDim.x / 32)) {
+    uint32_t z = sparse_ids[i];
+    for (uint64_t k = row_ptr[z] + lane_id(); k < row_ptr[z + 1]; k += 32) {
+      uint64_t p = atomicAdd(&cursor[col[k]], 1ull);
+      out_col[p] = (uint32_t)i;  // compact sparse index
+    }
+  }
+}
+
+// (key = (maxd - d) << 32 | id) for ordering ids by degree descending.
+__global__ void degree_order_key_kernel(const uint32_t* __restrict__ ids, uint64_t n,
+                                        const uint64_t* __restrict__ row_ptr,
+                                        const uint32_t* __restrict__ deg_arr, uint64_t maxd,
+                                        uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t id = ids ? ids[i] : (uint32_t)i;
+    uint64_t d = row_ptr ? row_ptr[id + 1] - row_ptr[id] : deg_arr[id];
+    keys[i] = ((maxd - d) << 32) | id;
+    vals[i] = id;
+  }
+}
+
+__global__ void scatter_rank_kernel(const uint32_t* __restrict__ order, uint64_t n,
+                                    uint32_t* __restrict__ rank) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    rank[order[i]] = (uint32_t)i;
+}
+
+// dense list lengths in processing order
+__global__ void gather_len_kernel(const uint32_t* __restrict__ ids, uint64_t n,
+                                  const uint64_t* __restrict__ row_ptr, uint32_t* __restrict__ len) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t id = ids[i];
+    len[i] = (uint32_t)(row_ptr[id + 1] - row_ptr[id]);
+  }
+}
+
+// keys for sorting the dense lists: (row_pos << ybits) | y_rank[y]
+__global__ void dense_list_key_kernel(const uint32_t* __restrict__ ids, uint64_t n,
+                                      const uint64_t* __restrict__ src_ptr,
+                                      const uint32_t* __restrict__ src_col,
+                                      const uint64_t* __restrict__ dst_ptr,
+                                      const uint32_t* __restrict__ y_rank, int ybits,
+                                      uint64_t* __restrict__ keys) {
+  for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < n;
+       i += (uint64_t)gridDim.x * (blockDim.x / 32)) {
+    uint32_t id = ids[i];
+    uint64_t s0 = src_ptr[id], s1 = src_ptr[id + 1], d0 = dst_ptr[i];
+    for (uint64_t k = s0 + lane_id(); k < s1; k += 32)
+      keys[d0 + (k - s0)] = ((uint64_t)i << ybits) | y_rank[src_col[k]];
+  }
+}
+
+__global__ void low_bits_kernel(const uint64_t* __restrict__ keys, uint64_t n, int bits,
+                                uint32_t* __restrict__ out) {
+  const uint64_t m = (1ull << bits) - 1;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = (uint32_t)(keys[i] & m);
+}
+
+}  // namespace d3g

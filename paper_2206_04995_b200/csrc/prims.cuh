@@ -1,0 +1,245 @@
+// Device primitives: tiled exclusive scan (u64 result) and a stable LSD
+// radix sort of (u64 key, u32 value) pairs with warp multi-split ranking.
+// These are the building blocks for the CSR grouping (counting scatter +
+// row offsets), the dictionary code assignment and output ordering.
+#pragma once
+
+#include "common.cuh"
+
+namespace d3g {
+
+// ---------------------------------------------------------------------------
+// Exclusive scan: out[i] = sum(in[0..i)), out[n] = total. Three phases:
+// per-tile reduce, recursive scan of tile sums, per-tile scan with offset.
+constexpr int kScanThreads = 512;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+template <class Tin>
+__global__ void __launch_bounds__(kScanThreads)
+scan_reduce_kernel(const Tin* __restrict__ in, uint64_t n, uint64_t* __restrict__ partial) {
+  __shared__ uint64_t warp_tot[kScanThreads / 32];
+  uint64_t base = (uint64_t)blockIdx.x * kScanTile;
+  uint64_t s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    uint64_t i = base + (uint64_t)k * kScanThreads + threadIdx.x;
+    if (i < n) s += (uint64_t)in[i];
+  }
+  s = warp_sum(s);
+  if (lane_id() == 0) warp_tot[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    uint64_t v = threadIdx.x < kScanThreads / 32 ? warp_tot[threadIdx.x] : 0;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) partial[blockIdx.x] = v;
+  }
+}
+
+// Block-wide exclusive scan of one value per thread; returns the prefix and
+// writes the block total to *total.
+__device__ __forceinline__ uint64_t block_exclusive_scan(uint64_t v, uint64_t* total) {
+  __shared__ uint64_t warp_tot[32];
+  __shared__ uint64_t block_tot;
+  uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  uint64_t incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint64_t u = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= (uint32_t)o) incl += u;
+  }
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t nw = blockDim.x >> 5;
+    uint64_t t = lane < nw ? warp_tot[lane] : 0;
+    uint64_t ti = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint64_t u = __shfl_up_sync(0xffffffffu, ti, o);
+      if (lane >= (uint32_t)o) ti += u;
+    }
+    if (lane < nw) warp_tot[lane] = ti - t;
+    if (lane == nw - 1) block_tot = ti;
+  }
+  __syncthreads();
+  uint64_t res = warp_tot[warp] + incl - v;
+  if (total) *total = block_tot;
+  __syncthreads();
+  return res;
+}
+
+template <class Tin>
+__global__ void __launch_bounds__(kScanThreads)
+scan_tile_kernel(const Tin* __restrict__ in, uint64_t n, const uint64_t* __restrict__ offsets,
+                 uint64_t* __restrict__ out) {
+  uint64_t base = (uint64_t)blockIdx.x * kScanTile + (uint64_t)threadIdx.x * kScanItems;
+  uint64_t vals[kScanItems];
+  uint64_t s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    uint64_t i = base + k;
+    vals[k] = i < n ? (uint64_t)in[i] : 0;
+    s += vals[k];
+  }
+  uint64_t tot;
+  uint64_t run = block_exclusive_scan(s, &tot) + (offsets ? offsets[blockIdx.x] : 0);
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    uint64_t i = base + k;
+    if (i < n) out[i] = run;
+    run += vals[k];
+  }
+  // the last element of the whole array writes out[n]
+  uint64_t last_tile = n == 0 ? 0 : (n - 1) / kScanTile;
+  if (blockIdx.x == last_tile && threadIdx.x == blockDim.x - 1)
+    out[n] = tot + (offsets ? offsets[blockIdx.x] : 0);
+}
+
+// out must hold n + 1 entries. Returns nothing; out[n] is the total.
+template <class Tin>
+void exclusive_scan(Ctx& ctx, const Tin* in, uint64_t n, uint64_t* out) {
+  if (n == 0) {
+    D3G_CUDA(cudaMemsetAsync(out, 0, sizeof(uint64_t), ctx.stream));
+    return;
+  }
+  uint64_t tiles = (n + kScanTile - 1) / kScanTile;
+  if (tiles == 1) {
+    D3G_LAUNCH(ctx, scan_tile_kernel<Tin>, 1, kScanThreads, 0, in, n,
+               (const uint64_t*)nullptr, out);
+    return;
+  }
+  DBuf<uint64_t> partial = ctx.alloc<uint64_t>(tiles);
+  DBuf<uint64_t> offs = ctx.alloc<uint64_t>(tiles + 1);
+  D3G_LAUNCH(ctx, scan_reduce_kernel<Tin>, (unsigned)tiles, kScanThreads, 0, in, n,
+             partial.p);
+  exclusive_scan<uint64_t>(ctx, partial.p, tiles, offs.p);
+  D3G_LAUNCH(ctx, scan_tile_kernel<Tin>, (unsigned)tiles, kScanThreads, 0, in, n,
+             (const uint64_t*)offs.p, out);
+}
+
+// ---------------------------------------------------------------------------
+// Stable LSD radix sort, 8-bit digits. Each tile of kSortTile keys is split
+// into per-warp contiguous chunks; warps rank keys with __match_any_sync so
+// the scatter is stable (global index order within each digit).
+constexpr int kSortThreads = 256;
+constexpr int kSortWarps = kSortThreads / 32;
+constexpr int kSortPerLane = 8;
+constexpr int kSortChunk = 32 * kSortPerLane;           // keys per warp
+constexpr int kSortTile = kSortWarps * kSortChunk;      // 2048 keys per block
+
+__global__ void __launch_bounds__(kSortThreads)
+radix_hist_kernel(const uint64_t* __restrict__ keys, uint64_t n, int shift, uint32_t n_tiles,
+                  uint32_t* __restrict__ hist) {
+  __shared__ uint32_t cnt[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) cnt[i] = 0;
+  __syncthreads();
+  uint64_t base = (uint64_t)blockIdx.x * kSortTile;
+  for (int k = threadIdx.x; k < kSortTile; k += blockDim.x) {
+    uint64_t i = base + k;
+    if (i < n) atomicAdd(&cnt[(keys[i] >> shift) & 255], 1u);
+  }
+  __syncthreads();
+  for (int d = threadIdx.x; d < 256; d += blockDim.x)
+    hist[(uint64_t)d * n_tiles + blockIdx.x] = cnt[d];
+}
+
+template <bool kHasVals>
+__global__ void __launch_bounds__(kSortThreads)
+radix_scatter_kernel(const uint64_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
+                     uint64_t n, int shift, uint32_t n_tiles,
+                     const uint64_t* __restrict__ offsets,  // scanned hist, digit-major
+                     uint64_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out) {
+  __shared__ uint32_t whist[kSortWarps][256];
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < kSortWarps * 256; i += blockDim.x) (&whist[0][0])[i] = 0;
+  __syncthreads();
+  const uint64_t chunk = (uint64_t)blockIdx.x * kSortTile + (uint64_t)warp * kSortChunk;
+  uint64_t k[kSortPerLane];
+  uint32_t v[kSortPerLane];
+  uint32_t rank[kSortPerLane];
+  const uint32_t lt = (1u << lane) - 1;
+#pragma unroll
+  for (int it = 0; it < kSortPerLane; ++it) {
+    uint64_t i = chunk + (uint64_t)it * 32 + lane;
+    bool valid = i < n;
+    k[it] = valid ? keys_in[i] : 0;
+    if (kHasVals) v[it] = valid ? vals_in[i] : 0;
+    uint32_t d = valid ? (uint32_t)((k[it] >> shift) & 255) : 256u;
+    uint32_t active = __ballot_sync(0xffffffffu, valid);
+    uint32_t peers = __match_any_sync(0xffffffffu, d) & active;
+    uint32_t before = 0;
+    if (valid) before = whist[warp][d];
+    __syncwarp();
+    if (valid) {
+      rank[it] = before + __popc(peers & lt);
+      if ((peers & lt) == 0) whist[warp][d] = before + __popc(peers);
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  // per digit: exclusive scan across warps, plus the tile's global offset
+  for (int d = threadIdx.x; d < 256; d += blockDim.x) {
+    uint64_t run = offsets[(uint64_t)d * n_tiles + blockIdx.x];
+#pragma unroll
+    for (int w = 0; w < kSortWarps; ++w) {
+      uint32_t t = whist[w][d];
+      whist[w][d] = (uint32_t)run;  // low 32 bits; positions fit (n < 2^32)
+      run += t;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < kSortPerLane; ++it) {
+    uint64_t i = chunk + (uint64_t)it * 32 + lane;
+    if (i < n) {
+      uint32_t d = (uint32_t)((k[it] >> shift) & 255);
+      uint32_t pos = whist[warp][d] + rank[it];
+      keys_out[pos] = k[it];
+      if (kHasVals) vals_out[pos] = v[it];
+    }
+  }
+}
+
+// Sorts keys (and vals, if non-null) by the low `bits` bits of the key.
+// Ping-pongs through the caller's scratch buffers; the sorted result ends up
+// back in keys/vals. Requires n < 2^32.
+inline void radix_sort(Ctx& ctx, uint64_t* keys, uint32_t* vals, uint64_t n, int bits) {
+  if (n <= 1 || bits <= 0) return;
+  if (n >= (1ull << 32)) throw ResourceError("radix_sort: more than 2^32 keys");
+  uint32_t n_tiles = (uint32_t)((n + kSortTile - 1) / kSortTile);
+  DBuf<uint64_t> k2 = ctx.alloc<uint64_t>(n);
+  DBuf<uint32_t> v2 = ctx.alloc<uint32_t>(vals ? n : 1);
+  DBuf<uint32_t> hist = ctx.alloc<uint32_t>((uint64_t)256 * n_tiles);
+  DBuf<uint64_t> offs = ctx.alloc<uint64_t>((uint64_t)256 * n_tiles + 1);
+  uint64_t* kin = keys;
+  uint32_t* vin = vals;
+  uint64_t* kout = k2.p;
+  uint32_t* vout = v2.p;
+  int passes = (bits + 7) / 8;
+  for (int p = 0; p < passes; ++p) {
+    int shift = 8 * p;
+    D3G_LAUNCH(ctx, radix_hist_kernel, n_tiles, kSortThreads, 0, kin, n, shift, n_tiles, hist.p);
+    exclusive_scan<uint32_t>(ctx, hist.p, (uint64_t)256 * n_tiles, offs.p);
+    if (vals)
+      D3G_LAUNCH(ctx, radix_scatter_kernel<true>, n_tiles, kSortThreads, 0, kin, vin, n, shift,
+                 n_tiles, offs.p, kout, vout);
+    else
+      D3G_LAUNCH(ctx, radix_scatter_kernel<false>, n_tiles, kSortThreads, 0, kin, vin, n, shift,
+                 n_tiles, offs.p, kout, vout);
+    std::swap(kin, kout);
+    std::swap(vin, vout);
+  }
+  if (kin != keys) {
+    D3G_CUDA(cudaMemcpyAsync(keys, kin, n * 8, cudaMemcpyDeviceToDevice, ctx.stream));
+    if (vals) D3G_CUDA(cudaMemcpyAsync(vals, vin, n * 4, cudaMemcpyDeviceToDevice, ctx.stream));
+  }
+}
+
+inline int bits_for(uint64_t max_value) {
+  int b = 0;
+  while (b < 64 && (max_value >> b) != 0) ++b;
+  return b;
+}
+
+}  // namespace d3g

@@ -1,0 +1,208 @@
+// SparseBMM (north_star subsystem 2), replacing sparse_bmm / run_chunk
+// (P/src/sparsebmm.cpp:11-106). For each x, the distinct union of S_sp[y]
+// over y in R[x] (Alg. 2). The reference dedups with an int64 stamp array of
+// |Z| entries per thread; here each x is routed by its candidate count
+// c_x = sum_y |S_sp[y]| (= the reference's inner-body count for that x):
+//   * c_x <= 32: one warp per x gathers the candidates into lanes, sorts them
+//     with a 32-wide bitonic network in registers and counts adjacent-unique;
+//   * c_x > 32: one CTA per x with a bitmap over the COMPACT sparse-z index
+//     space in shared memory (or a per-CTA slice in global memory when it
+//     does not fit), atomicOr returning the old word tells whether the pair
+//     is new; touched words are cleared by re-walking the candidates.
+// Output: count, optional (sum, xor) fingerprint, optional code pairs
+// (warp-aggregated append).
+#pragma once
+
+#include "common.cuh"
+
+namespace d3g {
+
+struct Decode {
+  const uint64_t* rev_x;  // engine x code -> raw (null = identity)
+  const uint64_t* rev_z;  // engine z code -> raw (null = identity)
+  int swapped;            // caller orientation = engine (z, x)
+  __device__ __forceinline__ uint64_t hash(uint32_t xc, uint32_t zc) const {
+    uint64_t ex = rev_x ? rev_x[xc] : xc;
+    uint64_t ez = rev_z ? rev_z[zc] : zc;
+    return swapped ? pair_hash(ez, ex) : pair_hash(ex, ez);
+  }
+};
+
+struct Emit {
+  uint32_t* x;  // engine x codes
+  uint32_t* z;  // engine z codes
+  unsigned long long* cursor;
+  uint64_t cap;
+};
+
+enum : int { kModeCount = 0, kModeChecksum = 1, kModeEmit = 2 };
+
+// Warp-aggregated append of (xc, zc) for lanes with `pred`.
+__device__ __forceinline__ void emit_pair(const Emit& e, bool pred, uint32_t xc, uint32_t zc) {
+  uint32_t m = __ballot_sync(__activemask(), pred);
+  if (!pred) return;
+  uint32_t lane = lane_id();
+  int leader = __ffs(m) - 1;
+  unsigned long long base = 0;
+  if ((int)lane == leader) base = atomicAdd(e.cursor, (unsigned long long)__popc(m));
+  base = __shfl_sync(m, base, leader);
+  uint64_t idx = base + __popc(m & ((1u << lane) - 1));
+  if (idx < e.cap) {
+    e.x[idx] = xc;
+    e.z[idx] = zc;
+  }
+}
+
+// c_x per x and the total inner count.
+__global__ void sparse_cx_kernel(const uint64_t* __restrict__ r_ptr, const uint32_t* __restrict__ r_col,
+                                 uint64_t n_rows, const uint64_t* __restrict__ sp_ptr,
+                                 uint64_t* __restrict__ cx, unsigned long long* __restrict__ total) {
+  uint64_t acc = 0;
+  for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n_rows;
+       x += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t c = 0;
+    for (uint64_t k = r_ptr[x]; k < r_ptr[x + 1]; ++k) {
+      uint32_t y = r_col[k];
+      c += sp_ptr[y + 1] - sp_ptr[y];
+    }
+    cx[x] = c;
+    acc += c;
+  }
+  acc = warp_sum(acc);
+  if (lane_id() == 0 && acc) atomicAdd(total, (unsigned long long)acc);
+}
+
+__global__ void bin_flags_kernel(const uint64_t* __restrict__ cx, uint64_t n, uint64_t small_max,
+                                 uint32_t* __restrict__ small, uint32_t* __restrict__ large) {
+  for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n;
+       x += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t c = cx[x];
+    small[x] = (c > 0 && c <= small_max) ? 1u : 0u;
+    large[x] = c > small_max ? 1u : 0u;
+  }
+}
+
+__device__ __forceinline__ uint32_t bitonic32(uint32_t v) {
+  const uint32_t lane = lane_id();
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      uint32_t o = __shfl_xor_sync(0xffffffffu, v, j);
+      bool up = (lane & k) == 0;
+      bool lower = (lane & j) == 0;
+      uint32_t mn = v < o ? v : o, mx = v < o ? o : v;
+      v = (lower == up) ? mn : mx;
+    }
+  }
+  return v;
+}
+
+// One warp per x with c_x <= 32.
+template <int kMode>
+__global__ void __launch_bounds__(256)
+sparse_small_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
+                    const uint64_t* __restrict__ r_ptr, const uint32_t* __restrict__ r_col,
+                    const uint64_t* __restrict__ sp_ptr, const uint32_t* __restrict__ sp_col,
+                    const uint32_t* __restrict__ sparse_ids, Decode dec, Emit em, Tally* tally) {
+  __shared__ uint32_t buf[8][32];
+  const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
+  uint64_t cnt = 0, sum = 0, xr = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * 8 + w; i < n_x; i += (uint64_t)gridDim.x * 8) {
+    uint32_t x = xs[i];
+    uint64_t r0 = r_ptr[x], r1 = r_ptr[x + 1];
+    uint32_t nc = 0;
+    for (uint64_t base = r0; base < r1; base += 32) {
+      uint64_t k = base + lane;
+      uint32_t y = 0;
+      uint32_t len = 0;
+      uint64_t s0 = 0;
+      if (k < r1) {
+        y = r_col[k];
+        s0 = sp_ptr[y];
+        len = (uint32_t)(sp_ptr[y + 1] - s0);
+      }
+      uint32_t incl = len;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= (uint32_t)o) incl += u;
+      }
+      uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+      uint32_t off = nc + incl - len;
+      for (uint32_t t = 0; t < len && off + t < 32; ++t) buf[w][off + t] = sp_col[s0 + t];
+      nc += tot;
+    }
+    __syncwarp();
+    uint32_t v = lane < nc ? buf[w][lane] : 0xffffffffu;
+    __syncwarp();
+    v = bitonic32(v);
+    uint32_t prev = __shfl_up_sync(0xffffffffu, v, 1);
+    bool fresh = lane < nc && (lane == 0 || v != prev);
+    cnt += fresh;
+    if (kMode == kModeChecksum && fresh) {
+      uint64_t h = dec.hash(x, sparse_ids[v]);
+      sum += h;
+      xr ^= h;
+    }
+    if (kMode == kModeEmit) emit_pair(em, fresh, x, fresh ? sparse_ids[v] : 0);
+  }
+  tally_flush(tally, cnt, sum, xr);
+}
+
+// One CTA per x with c_x > 32; bitmap of n_words 32-bit words in smem
+// (kGlobalBitmap = false) or a per-CTA slice of gbm (true).
+template <int kMode, bool kGlobalBitmap>
+__global__ void __launch_bounds__(512)
+sparse_large_kernel(const uint32_t* __restrict__ xs, uint64_t n_x, const uint64_t* __restrict__ cx,
+                    uint64_t cx_base, const uint64_t* __restrict__ r_ptr, const uint32_t* __restrict__ r_col,
+                    const uint64_t* __restrict__ sp_ptr, const uint32_t* __restrict__ sp_col,
+                    const uint32_t* __restrict__ sparse_ids, uint32_t n_words, uint32_t* gbm,
+                    Decode dec, Emit em, Tally* tally) {
+  extern __shared__ uint32_t smem_bm[];
+  uint32_t* bm = kGlobalBitmap ? gbm + (uint64_t)blockIdx.x * n_words : smem_bm;
+  for (uint32_t i = threadIdx.x; i < n_words; i += blockDim.x) bm[i] = 0;
+  __syncthreads();
+  uint64_t cnt = 0, sum = 0, xr = 0;
+  for (uint64_t i = blockIdx.x; i < n_x; i += gridDim.x) {
+    uint32_t x = xs[i];
+    uint64_t r0 = r_ptr[x], r1 = r_ptr[x + 1];
+    for (uint64_t k = r0; k < r1; ++k) {
+      uint32_t y = r_col[k];
+      uint64_t s0 = sp_ptr[y], s1 = sp_ptr[y + 1];
+      for (uint64_t t = s0 + threadIdx.x; t < s1 + ((blockDim.x - (s1 - s0) % blockDim.x) % blockDim.x);
+           t += blockDim.x) {
+        bool fresh = false;
+        uint32_t zi = 0;
+        if (t < s1) {
+          zi = sp_col[t];
+          uint32_t bit = 1u << (zi & 31);
+          uint32_t old = atomicOr(&bm[zi >> 5], bit);
+          fresh = (old & bit) == 0;
+        }
+        cnt += fresh;
+        if (kMode == kModeChecksum && fresh) {
+          uint64_t h = dec.hash(x, sparse_ids[zi]);
+          sum += h;
+          xr ^= h;
+        }
+        if (kMode == kModeEmit) emit_pair(em, fresh, x, fresh ? sparse_ids[zi] : 0);
+      }
+    }
+    __syncthreads();
+    // clear: whole bitmap when cheaper than re-walking the candidates
+    if (cx[x - cx_base] >= n_words) {
+      for (uint32_t j = threadIdx.x; j < n_words; j += blockDim.x) bm[j] = 0;
+    } else {
+      for (uint64_t k = r0; k < r1; ++k) {
+        uint32_t y = r_col[k];
+        for (uint64_t t = sp_ptr[y] + threadIdx.x; t < sp_ptr[y + 1]; t += blockDim.x)
+          bm[sp_col[t] >> 5] = 0;
+      }
+    }
+    __syncthreads();
+  }
+  tally_flush(tally, cnt, sum, xr);
+}
+
+}  // namespace d3g

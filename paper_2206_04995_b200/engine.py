@@ -1,0 +1,649 @@
+"""Host-side mirror of the reference operator API over the C ABI.
+
+Same names, argument meaning and error behaviour as the reference's
+``dim3::join_project`` family (P = /root/reference/proj):
+
+=======================  =====================================================
+this module              reference
+=======================  =====================================================
+``RawTable``             ``dim3::RawTable`` (u64 columns), relation.hpp:43-46
+``EngineConfig``         ``dim3::EngineConfig``, engine.hpp:36-48
+``CostConstants``        ``dim3::CostConstants``, costmodel.hpp:21-30
+``Strategy``             ``dim3::Strategy``, engine.hpp:25-31
+``DensePathMode``        ``dim3::DensePathMode``, denseec.hpp:56
+``join_project``         ``dim3::join_project``, engine.hpp:102-103
+``result_to_raw``        ``dim3::result_to_raw``, engine.hpp:123
+``ExecutionReport``      ``dim3::ExecutionReport`` (+ GPU fields), :59-85
+``build_csr``            ``dim3::build_csr``, relation.hpp:108-109
+``sparse_bmm``           ``dim3::sparse_bmm``, sparsebmm.hpp:33-36
+``dense_ec``             ``dim3::dense_ec``, denseec.hpp:82-85
+``f1/f3_threshold``      costmodel.hpp:86-121
+``ConfigError`` ...      common.hpp:25-36 (status codes 2/3/4 as the CLI)
+=======================  =====================================================
+
+Everything computes on the GPU through ``libdim3_b200.so``; there is no CPU
+fallback. Importing works without a GPU (so host-only policy functions and
+the ABI can be inspected), but every compute call raises if the library or
+a Blackwell device is unavailable.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import os
+from dataclasses import dataclass, field, fields
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdim3_b200.so")
+
+U64P = C.POINTER(C.c_uint64)
+U32P = C.POINTER(C.c_uint32)
+
+
+# ---------------------------------------------------------------------------
+# Errors (P/include/dim3/common.hpp:25-36); status codes as P/tools/dim3.cpp:675-693.
+class Dim3Error(RuntimeError):
+    status = 5
+
+
+class ConfigError(Dim3Error):
+    status = 2
+
+
+class IoError(Dim3Error):
+    status = 3
+
+
+class FormatError(Dim3Error):
+    status = 3
+
+
+class ResourceError(Dim3Error):
+    status = 4
+
+
+class CudaError(Dim3Error):
+    status = 5
+
+
+_STATUS = {2: ConfigError, 3: IoError, 4: ResourceError, 5: CudaError}
+
+
+class Strategy(enum.IntEnum):
+    auto_select = 0
+    classical = 1
+    hybrid = 2
+    sparse_only = 3
+    dense_only = 4
+
+
+class DensePathMode(enum.IntEnum):
+    cost_based = 0
+    force_wide = 1
+    force_probe = 2
+
+
+def strategy_from_name(name: str) -> Strategy:
+    """strategy_from_name (P/src/engine.cpp), CLI spellings."""
+    table = {"auto": Strategy.auto_select, "classical": Strategy.classical,
+             "hybrid": Strategy.hybrid, "sparse": Strategy.sparse_only,
+             "dense": Strategy.dense_only}
+    if name not in table:
+        raise ConfigError(f"unknown strategy {name!r}")
+    return table[name]
+
+
+@dataclass
+class SkipFlags:
+    x: bool = False
+    y: bool = False
+    z: bool = False
+
+
+@dataclass
+class CostConstants:
+    t_seqR: float = 0.0
+    t_randR: float = 0.0
+    t_randRW: float = 0.0
+    t_hash: float = 0.0
+    t_map: float = 0.0
+    t_ECs: float = 0.0
+    t_ECd: float = 0.0
+    w: int = 256
+
+    @staticmethod
+    def test_consts() -> "CostConstants":
+        """test_consts() (P/tests/support.hpp:27-38)."""
+        return CostConstants(0.9e-9, 140e-9, 140e-9, 440e-9, 330e-9, 11e-9, 1.2e-9, 256)
+
+
+@dataclass
+class EngineConfig:
+    force: Strategy = Strategy.auto_select
+    threads: int = 1
+    memory_budget_bytes: int = 3 << 30
+    count_only: bool = False
+    collect_cache_stats: bool = False
+    dense_mode: DensePathMode = DensePathMode.cost_based
+    natural_keys_auto: bool = True
+    natural_keys_declared: SkipFlags = field(default_factory=SkipFlags)
+    # GPU extensions
+    checksum: bool = False        # also compute the (sum, xor) set fingerprint
+    shard_index: int = 0          # x-range shard handled by this call
+    shard_count: int = 1
+
+
+class RawTable:
+    """Two u64 columns; row i = (left[i], right[i]) (relation.hpp:43-46).
+
+    Columns are numpy uint64 arrays (host) or CUDA torch tensors of int64 /
+    uint64 (device-resident input, no H2D copy)."""
+
+    def __init__(self, left=None, right=None):
+        self.left = _as_col(left if left is not None else [])
+        self.right = _as_col(right if right is not None else [])
+        if _length(self.left) != _length(self.right):
+            raise FormatError("left and right columns differ in length")
+
+    def size(self) -> int:
+        return _length(self.left)
+
+    __len__ = size
+
+    @property
+    def on_device(self) -> bool:
+        return _is_cuda(self.left)
+
+
+def _is_cuda(a) -> bool:
+    return getattr(a, "is_cuda", False)
+
+
+def _length(a) -> int:
+    return int(a.shape[0]) if hasattr(a, "shape") else len(a)
+
+
+def _as_col(a):
+    if _is_cuda(a):
+        if a.element_size() != 8 or not a.is_contiguous():
+            raise FormatError("device columns must be contiguous 64-bit tensors")
+        return a
+    arr = np.asarray(a)
+    if arr.dtype != np.uint64:
+        if arr.size and arr.dtype.kind == "i" and int(arr.min()) < 0:
+            raise FormatError("integer columns must be non-negative")
+        arr = arr.astype(np.uint64)
+    return np.ascontiguousarray(arr)
+
+
+# ---------------------------------------------------------------------------
+# ctypes mirror of include/dim3_b200.h
+class _Table(C.Structure):
+    _fields_ = [("left", U64P), ("right", U64P), ("n", C.c_uint64), ("on_device", C.c_int32),
+                ("pad", C.c_int32)]
+
+
+class _Consts(C.Structure):
+    _fields_ = [(k, C.c_double) for k in
+                ("t_seqR", "t_randR", "t_randRW", "t_hash", "t_map", "t_ECs", "t_ECd")] + \
+               [("w", C.c_uint32), ("pad", C.c_uint32)]
+
+
+class _Opts(C.Structure):
+    _fields_ = [("force", C.c_int32), ("threads", C.c_int32), ("memory_budget_bytes", C.c_uint64),
+                ("count_only", C.c_int32), ("dense_mode", C.c_int32),
+                ("natural_keys_auto", C.c_int32), ("declared_x", C.c_int32),
+                ("declared_y", C.c_int32), ("declared_z", C.c_int32), ("checksum", C.c_int32),
+                ("collect_counters", C.c_int32), ("shard_index", C.c_int32),
+                ("shard_count", C.c_int32), ("pad0", C.c_int32), ("pad1", C.c_int32)]
+
+
+_REPORT_U64_A = ["r_rows", "s_rows", "out_j_estimate"]
+_REPORT_U64_B = ["out_p", "pairs_sparse", "pairs_dense", "sparse_z", "dense_z", "f2_evaluations",
+                 "dropped_r", "x_card", "y_card", "z_card", "r_nnz", "s_nnz", "sparse_nnz",
+                 "out_j", "x_live", "panel_bytes", "peak_bytes", "spa_inner_count",
+                 "dense_wide_encounters", "dense_probe_encounters", "dense_blocks_checked",
+                 "dense_probes_done", "dense_row_bitmaps_built", "checksum_sum", "checksum_xor",
+                 "h2d_bytes", "d2h_bytes"]
+_REPORT_MS = ["ms_total", "ms_h2d", "ms_estimate", "ms_map", "ms_csr", "ms_stats",
+              "ms_partition", "ms_sparse", "ms_dense", "ms_decode"]
+
+
+class _Report(C.Structure):
+    _fields_ = [("strategy", C.c_char * 16), ("swapped", C.c_int32),
+                ("f1_gate_classical", C.c_int32), ("natural_x", C.c_int32),
+                ("natural_y", C.c_int32), ("natural_z", C.c_int32), ("materialized", C.c_int32)] + \
+               [(k, C.c_uint64) for k in _REPORT_U64_A] + [("f1", C.c_double)] + \
+               [(k, C.c_uint64) for k in _REPORT_U64_B] + \
+               [(k, C.c_double) for k in _REPORT_MS] + [("gpu_launches", C.c_uint64)]
+
+
+class _Pairs(C.Structure):
+    _fields_ = [("x", U64P), ("z", U64P), ("cap", C.c_uint64), ("n", C.c_uint64),
+                ("on_device", C.c_int32), ("pad", C.c_int32)]
+
+
+class _Csr(C.Structure):
+    _fields_ = [("row_ptr", U64P), ("col", U32P), ("n_rows", C.c_uint32), ("n_cols", C.c_uint32),
+                ("nnz", C.c_uint64)]
+
+
+class _Panel(C.Structure):
+    _fields_ = [("z_ids", U32P), ("m_z", U32P), ("blocks", U64P), ("rows", C.c_uint64),
+                ("y_card", C.c_uint32), ("w", C.c_uint32)]
+
+
+class _KStats(C.Structure):
+    _fields_ = [("inner_count", C.c_uint64), ("wide_encounters", C.c_uint64),
+                ("probe_encounters", C.c_uint64), ("blocks_checked", C.c_uint64),
+                ("probes_done", C.c_uint64), ("row_bitmaps_built", C.c_uint64),
+                ("ms_kernel", C.c_double)]
+
+
+# Every symbol include/dim3_b200.h declares (tests check the export table).
+EXPORTED = ["d3g_ctx_create", "d3g_ctx_destroy", "d3g_last_error", "d3g_version",
+            "d3g_opts_default", "d3g_join_project", "d3g_build_csr", "d3g_sparse_bmm_csr",
+            "d3g_dense_ec_rows", "d3g_generate", "d3g_cfg_rows", "d3g_ctx_device",
+            "d3g_f3_threshold", "d3g_f1", "d3g_f2_decide"]
+
+_lib = None
+
+
+def lib():
+    """Loads libdim3_b200.so (fails loudly when it is missing)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is not built; run __graft_entry__.build() "
+                              "(make -C paper_2206_04995_b200/csrc)")
+        L = C.CDLL(LIB_PATH)
+        L.d3g_ctx_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
+        L.d3g_ctx_destroy.argtypes = [C.c_void_p]
+        L.d3g_last_error.restype = C.c_char_p
+        L.d3g_version.restype = C.c_char_p
+        L.d3g_opts_default.argtypes = [C.POINTER(_Opts)]
+        L.d3g_join_project.argtypes = [C.c_void_p, C.POINTER(_Table), C.POINTER(_Table),
+                                       C.POINTER(_Consts), C.POINTER(_Opts), C.POINTER(_Report),
+                                       C.POINTER(_Pairs)]
+        L.d3g_build_csr.argtypes = [C.c_void_p, U32P, U32P, C.c_uint64, C.c_uint32, C.c_uint32,
+                                    C.c_int, C.POINTER(_Csr)]
+        L.d3g_sparse_bmm_csr.argtypes = [C.c_void_p, C.POINTER(_Csr), C.POINTER(_Csr), C.c_uint32,
+                                         U32P, U32P, C.c_uint64, U64P, C.POINTER(_KStats)]
+        L.d3g_dense_ec_rows.argtypes = [C.c_void_p, C.POINTER(_Csr), C.POINTER(_Panel),
+                                        C.POINTER(_Consts), C.c_int, U32P, U32P, C.c_uint64, U64P,
+                                        C.POINTER(_KStats)]
+        L.d3g_generate.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_uint64, C.c_uint64,
+                                   C.c_void_p, C.c_void_p]
+        L.d3g_cfg_rows.argtypes = [C.c_int]
+        L.d3g_cfg_rows.restype = C.c_uint64
+        L.d3g_ctx_device.argtypes = [C.c_void_p]
+        L.d3g_f3_threshold.argtypes = [C.c_uint32, C.c_uint32, C.POINTER(_Consts)]
+        L.d3g_f3_threshold.restype = C.c_uint32
+        L.d3g_f1.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.POINTER(_Consts)]
+        L.d3g_f1.restype = C.c_double
+        L.d3g_f2_decide.argtypes = [U64P, C.c_uint64, U64P, C.c_uint64, C.c_uint64, C.c_uint64,
+                                    C.c_uint64, C.c_uint64, C.POINTER(_Consts), C.c_int,
+                                    C.POINTER(C.c_uint8), U64P]
+        _lib = L
+    return _lib
+
+
+def _check(rc: int):
+    if rc != 0:
+        msg = lib().d3g_last_error().decode(errors="replace")
+        raise _STATUS.get(rc, Dim3Error)(msg)
+
+
+def _consts(c: CostConstants) -> _Consts:
+    return _Consts(c.t_seqR, c.t_randR, c.t_randRW, c.t_hash, c.t_map, c.t_ECs, c.t_ECd, c.w, 0)
+
+
+class Context:
+    """One CUDA device + stream + device-memory pool (the C ABI's d3g_ctx)."""
+
+    def __init__(self, device: int = 0):
+        self._h = C.c_void_p()
+        _check(lib().d3g_ctx_create(device, C.byref(self._h)))
+        self.device = device
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if self._h:
+            lib().d3g_ctx_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default_ctx: dict[int, Context] = {}
+
+
+def default_context(device: int | None = None) -> Context:
+    if device is None:
+        device = 0
+        try:
+            import torch
+            if torch.cuda.is_available():
+                device = torch.cuda.current_device()
+        except Exception:
+            pass
+    if device not in _default_ctx:
+        _default_ctx[device] = Context(device)
+    return _default_ctx[device]
+
+
+# ---------------------------------------------------------------------------
+@dataclass
+class ExecutionReport:
+    strategy: str = ""
+    swapped: bool = False
+    f1_gate_classical: bool = False
+    natural_x: bool = False
+    natural_y: bool = False
+    natural_z: bool = False
+    materialized: bool = False
+    r_rows: int = 0
+    s_rows: int = 0
+    out_j_estimate: int = 0
+    f1_value: float = 0.0
+    out_p: int = 0
+    pairs_sparse: int = 0
+    pairs_dense: int = 0
+    sparse_z: int = 0
+    dense_z: int = 0
+    f2_evaluations: int = 0
+    dropped_r: int = 0
+    x_card: int = 0
+    y_card: int = 0
+    z_card: int = 0
+    r_nnz: int = 0
+    s_nnz: int = 0
+    sparse_nnz: int = 0
+    out_j: int = 0
+    x_live: int = 0
+    panel_bytes: int = 0
+    peak_bytes: int = 0
+    spa_inner_count: int = 0
+    dense_wide_encounters: int = 0
+    dense_probe_encounters: int = 0
+    dense_blocks_checked: int = 0
+    dense_probes_done: int = 0
+    dense_row_bitmaps_built: int = 0
+    checksum_sum: int = 0
+    checksum_xor: int = 0
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
+    ms_total: float = 0.0
+    ms_h2d: float = 0.0
+    ms_estimate: float = 0.0
+    ms_map: float = 0.0
+    ms_csr: float = 0.0
+    ms_stats: float = 0.0
+    ms_partition: float = 0.0
+    ms_sparse: float = 0.0
+    ms_dense: float = 0.0
+    ms_decode: float = 0.0
+    gpu_launches: int = 0
+
+    def to_kv(self):
+        """Insertion-ordered key/value view with the reference's key names
+        first (ExecutionReport::to_kv, P/src/engine.cpp:276-321)."""
+        kv = [("strategy", self.strategy), ("swapped", "true" if self.swapped else "false"),
+              ("r_rows", str(self.r_rows)), ("s_rows", str(self.s_rows)),
+              ("out_j_estimate", str(self.out_j_estimate)), ("f1", f"{self.f1_value:.6g}"),
+              ("out_p", str(self.out_p)), ("pairs_classical", "0"),
+              ("pairs_sparse", str(self.pairs_sparse)), ("pairs_dense", str(self.pairs_dense)),
+              ("pairs_cached", "0"), ("sparse_z", str(self.sparse_z)),
+              ("dense_z", str(self.dense_z)), ("cached_z", "0"),
+              ("f2_evaluations", str(self.f2_evaluations)), ("dropped_r", str(self.dropped_r)),
+              ("intermediate_pairs", "0"), ("x_card", str(self.x_card)),
+              ("y_card", str(self.y_card)), ("z_card", str(self.z_card)),
+              ("panel_bytes", str(self.panel_bytes)), ("peak_bytes", str(self.peak_bytes)),
+              ("spa_inner_count", str(self.spa_inner_count))]
+        for k in ("ms_total", "ms_estimate", "ms_map", "ms_csr", "ms_partition", "ms_sparse",
+                  "ms_dense", "ms_decode"):
+            kv.append((k, f"{getattr(self, k):.3f}"))
+        for k in ("f1_gate_classical", "x_live", "out_j", "r_nnz", "s_nnz", "sparse_nnz",
+                  "checksum_sum", "checksum_xor", "ms_h2d", "ms_stats", "gpu_launches"):
+            kv.append((k, str(getattr(self, k))))
+        return kv
+
+
+@dataclass
+class ResultSet:
+    """ResultSet after result_to_raw: raw caller-oriented pairs, sorted by
+    (x code, z code) — raw value order under natural keys."""
+    count: int = 0
+    materialized: bool = True
+    raw_x: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint64))
+    raw_z: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint64))
+
+
+@dataclass
+class JoinProjectOutput:
+    result: ResultSet
+    report: ExecutionReport
+
+
+def _table_struct(t: RawTable) -> _Table:
+    if t.on_device:
+        return _Table(C.cast(C.c_void_p(t.left.data_ptr()), U64P),
+                      C.cast(C.c_void_p(t.right.data_ptr()), U64P), t.size(), 1, 0)
+    return _Table(t.left.ctypes.data_as(U64P), t.right.ctypes.data_as(U64P), t.size(), 0, 0)
+
+
+def _opts(cfg: EngineConfig) -> _Opts:
+    if cfg.collect_cache_stats:
+        raise ConfigError("collect_cache_stats belongs to the partial-result cache, which is "
+                          "outside this operator's scope")
+    d = cfg.natural_keys_declared
+    return _Opts(int(cfg.force), int(cfg.threads), int(cfg.memory_budget_bytes),
+                 int(cfg.count_only), int(cfg.dense_mode), int(cfg.natural_keys_auto),
+                 int(d.x), int(d.y), int(d.z), int(cfg.checksum), 0, int(cfg.shard_index),
+                 int(cfg.shard_count), 0, 0)
+
+
+def join_project(r: RawTable, s: RawTable, cfg: EngineConfig, c: CostConstants,
+                 ctx: Context | None = None) -> JoinProjectOutput:
+    """dim3::join_project on the GPU. Raises ConfigError / ResourceError like
+    the reference. With cfg.count_only the result is not materialized."""
+    if cfg.threads < 1:
+        raise ConfigError("threads must be >= 1")
+    ctx = ctx or default_context()
+    rt, st = _table_struct(r), _table_struct(s)
+    cs, op = _consts(c), _opts(cfg)
+    rep = _Report()
+    pairs_p = None
+    ox = oz = None
+    if not cfg.count_only:
+        # first pass counts, second materializes into an exactly sized buffer
+        cnt_op = _opts(cfg)
+        cnt_op.count_only = 1
+        _check(lib().d3g_join_project(ctx.handle, C.byref(rt), C.byref(st), C.byref(cs),
+                                      C.byref(cnt_op), C.byref(rep), None))
+        n = int(rep.out_p)
+        ox = np.zeros(max(n, 1), dtype=np.uint64)
+        oz = np.zeros(max(n, 1), dtype=np.uint64)
+        pairs = _Pairs(ox.ctypes.data_as(U64P), oz.ctypes.data_as(U64P), n, 0, 0, 0)
+        pairs_p = C.byref(pairs)
+    _check(lib().d3g_join_project(ctx.handle, C.byref(rt), C.byref(st), C.byref(cs), C.byref(op),
+                                  C.byref(rep), pairs_p))
+    report = _to_report(rep)
+    if cfg.count_only:
+        res = ResultSet(count=report.out_p, materialized=False)
+    else:
+        n = report.out_p
+        res = ResultSet(count=n, materialized=True, raw_x=ox[:n], raw_z=oz[:n])
+    return JoinProjectOutput(res, report)
+
+
+def _to_report(rep: _Report) -> ExecutionReport:
+    out = ExecutionReport()
+    for f in fields(ExecutionReport):
+        src = "f1" if f.name == "f1_value" else f.name
+        v = getattr(rep, src)
+        if isinstance(v, bytes):
+            v = v.decode()
+        if f.type in ("bool",):
+            v = bool(v)
+        setattr(out, f.name, v)
+    for b in ("swapped", "f1_gate_classical", "natural_x", "natural_y", "natural_z",
+              "materialized"):
+        setattr(out, b, bool(getattr(out, b)))
+    return out
+
+
+def result_to_raw(out: JoinProjectOutput) -> ResultSet:
+    """Results are already decoded to raw values on the device."""
+    return out.result
+
+
+# ---------------------------------------------------------------------------
+# Kernel-level entry points
+@dataclass
+class CsrMatrix:
+    row_ptr: np.ndarray
+    col: np.ndarray
+    n_rows: int
+    n_cols: int
+
+    def nnz(self) -> int:
+        return int(self.col.shape[0])
+
+    def _struct(self) -> _Csr:
+        self.row_ptr = np.ascontiguousarray(self.row_ptr, dtype=np.uint64)
+        self.col = np.ascontiguousarray(self.col, dtype=np.uint32)
+        return _Csr(self.row_ptr.ctypes.data_as(U64P), self.col.ctypes.data_as(U32P),
+                    self.n_rows, self.n_cols, self.nnz())
+
+
+def build_csr(a: np.ndarray, b: np.ndarray, a_card: int, b_card: int, major_is_a: bool = True,
+              ctx: Context | None = None) -> CsrMatrix:
+    """dim3::build_csr on mapped code columns (a, b)."""
+    ctx = ctx or default_context()
+    a = np.ascontiguousarray(a, dtype=np.uint32)
+    b = np.ascontiguousarray(b, dtype=np.uint32)
+    n_rows = a_card if major_is_a else b_card
+    rp = np.zeros(n_rows + 1, dtype=np.uint64)
+    col = np.zeros(max(a.size, 1), dtype=np.uint32)
+    out = _Csr(rp.ctypes.data_as(U64P), col.ctypes.data_as(U32P), 0, 0, 0)
+    _check(lib().d3g_build_csr(ctx.handle, a.ctypes.data_as(U32P), b.ctypes.data_as(U32P), a.size,
+                               a_card, b_card, int(major_is_a), C.byref(out)))
+    return CsrMatrix(rp, col[: out.nnz].copy(), out.n_rows, out.n_cols)
+
+
+@dataclass
+class KernelStats:
+    inner_count: int = 0
+    wide_encounters: int = 0
+    probe_encounters: int = 0
+    blocks_checked: int = 0
+    probes_done: int = 0
+    row_bitmaps_built: int = 0
+    ms_kernel: float = 0.0
+
+
+def sparse_bmm(r_by_x: CsrMatrix, s_sparse_by_y: CsrMatrix, z_card: int, materialize=True,
+               ctx: Context | None = None):
+    """dim3::sparse_bmm: returns (count, pairs[n,2] sorted by (x, z) or None, stats)."""
+    ctx = ctx or default_context()
+    r, s = r_by_x._struct(), s_sparse_by_y._struct()
+    cnt = C.c_uint64()
+    st = _KStats()
+    _check(lib().d3g_sparse_bmm_csr(ctx.handle, C.byref(r), C.byref(s), z_card, None, None, 0,
+                                    C.byref(cnt), C.byref(st)))
+    pairs = None
+    if materialize:
+        n = cnt.value
+        px = np.zeros(max(n, 1), np.uint32)
+        pz = np.zeros(max(n, 1), np.uint32)
+        _check(lib().d3g_sparse_bmm_csr(ctx.handle, C.byref(r), C.byref(s), z_card,
+                                        px.ctypes.data_as(U32P), pz.ctypes.data_as(U32P), n,
+                                        C.byref(cnt), C.byref(st)))
+        pairs = np.stack([px[:n], pz[:n]], axis=1)
+    return cnt.value, pairs, KernelStats(**{k: getattr(st, k) for k, _ in _KStats._fields_})
+
+
+def dense_ec(r_by_x: CsrMatrix, z_ids: np.ndarray, panel_blocks: np.ndarray, y_card: int,
+             c: CostConstants, mode: DensePathMode = DensePathMode.cost_based, materialize=True,
+             ctx: Context | None = None):
+    """dim3::dense_ec over a BitmapPanel given as (z_ids, rows*row_words u64 blocks)."""
+    ctx = ctx or default_context()
+    r = r_by_x._struct()
+    z_ids = np.ascontiguousarray(z_ids, dtype=np.uint32)
+    blocks = np.ascontiguousarray(panel_blocks, dtype=np.uint64)
+    mz = np.zeros(max(z_ids.size, 1), np.uint32)
+    panel = _Panel(z_ids.ctypes.data_as(U32P), mz.ctypes.data_as(U32P),
+                   blocks.ctypes.data_as(U64P), z_ids.size, y_card, c.w)
+    cs = _consts(c)
+    cnt = C.c_uint64()
+    st = _KStats()
+    _check(lib().d3g_dense_ec_rows(ctx.handle, C.byref(r), C.byref(panel), C.byref(cs), int(mode),
+                                   None, None, 0, C.byref(cnt), C.byref(st)))
+    pairs = None
+    if materialize:
+        n = cnt.value
+        px = np.zeros(max(n, 1), np.uint32)
+        pz = np.zeros(max(n, 1), np.uint32)
+        _check(lib().d3g_dense_ec_rows(ctx.handle, C.byref(r), C.byref(panel), C.byref(cs),
+                                       int(mode), px.ctypes.data_as(U32P),
+                                       pz.ctypes.data_as(U32P), n, C.byref(cnt), C.byref(st)))
+        pairs = np.stack([px[:n], pz[:n]], axis=1)
+    return cnt.value, pairs, KernelStats(**{k: getattr(st, k) for k, _ in _KStats._fields_})
+
+
+# ---------------------------------------------------------------------------
+# Host-only policy (no GPU needed)
+def f1(size_r: int, size_s: int, out_j: int, c: CostConstants) -> float:
+    cs = _consts(c)
+    return lib().d3g_f1(size_r, size_s, out_j, C.byref(cs))
+
+
+def f3_threshold(m_x: int, y_card: int, c: CostConstants) -> int:
+    cs = _consts(c)
+    return int(lib().d3g_f3_threshold(m_x, y_card, C.byref(cs)))
+
+
+def f2_decide(mx_hist: np.ndarray, mz_hist: np.ndarray, x_card: int, y_card: int, z_card: int,
+              out_j: int, c: CostConstants, force: Strategy = Strategy.hybrid):
+    """Per-degree f2 decision table from GLOBAL degree histograms (the
+    quantities a multi-GPU run all-reduces). Returns (dense_of_mz, evaluations)."""
+    mx = np.ascontiguousarray(mx_hist, dtype=np.uint64)
+    mz = np.ascontiguousarray(mz_hist, dtype=np.uint64)
+    out = np.zeros(max(mz.size, 1), dtype=np.uint8)
+    ev = C.c_uint64()
+    cs = _consts(c)
+    _check(lib().d3g_f2_decide(mx.ctypes.data_as(U64P), mx.size, mz.ctypes.data_as(U64P), mz.size,
+                               x_card, y_card, z_card, out_j, C.byref(cs), int(force),
+                               out.ctypes.data_as(C.POINTER(C.c_uint8)), C.byref(ev)))
+    return out[: mz.size], ev.value
+
+
+def generate(cfg: int, side: int, lo: int = 0, hi: int | None = None, device=None,
+             ctx: Context | None = None):
+    """Convention-G rows on the GPU, returned as two int64 CUDA tensors
+    (bit patterns of the u64 values)."""
+    import torch
+    ctx = ctx or default_context(device)
+    n = int(lib().d3g_cfg_rows(cfg))
+    hi = n if hi is None else hi
+    dev = torch.device("cuda", ctx.device)
+    left = torch.empty(hi - lo, dtype=torch.int64, device=dev)
+    right = torch.empty(hi - lo, dtype=torch.int64, device=dev)
+    torch.cuda.synchronize(dev)
+    _check(lib().d3g_generate(ctx.handle, cfg, side, lo, hi, C.c_void_p(left.data_ptr()),
+                              C.c_void_p(right.data_ptr())))
+    return left, right
+
+
+def cfg_rows(cfg: int) -> int:
+    return int(lib().d3g_cfg_rows(cfg))
