@@ -1,0 +1,399 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 DIM^3 Join-Project hot path (one JSON line on rank 0).
+
+A step = one full join_project (count-only, force=auto, test_consts()) over
+one batch of convention-G synthetic input: map -> CSR -> degree stats -> f2
+partition -> SparseBMM + DenseEC -> count. Default workload: BASELINE
+configs[1] (cfg2, the self-join whose dense block exercises DenseEC).
+
+  value  = input tuples/s with R, S resident in HBM (CUDA-event time of the
+           pipeline on the library's stream, max over ranks)
+  e2e    = the same metric through the C ABI from pinned HOST buffers
+           (H2D of both tables + pipeline + result read-back, wall clock)
+  --impl reference : the reference's own CPU implementation (oracle/_ref,
+           built from /root/reference) on the box's host cores, on a bounded
+           x-slice sample extrapolated to the full job.
+
+Multi-GPU (torchrun): rank 0 generates the tables and broadcasts them over
+NVLink with NCCL; every rank builds the (replicated) mapping/CSR/partition
+and runs SparseBMM/DenseEC on its own x shard (intersection-free, no dedup
+across GPUs); counts are all-reduced.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    1: "cfg1: R,S 100,000 tuples each, x,z~U[0,10000), y~U[0,1000), seed 1",
+    2: "cfg2: self-join R=S, 5,000,000 tuples, x~U[0,200000), y~Zipf(1.0) over [0,50000), seed 2",
+    3: "cfg3: R,S 20,000,000 tuples each, x,z~U[0,2e6), y~U[0,1e7), seed 3",
+    4: "cfg4: R,S 10,000,000 tuples each, random u64 values from pools of 1e6 x / 1e6 z / "
+       "1e5 y, y~Zipf(0.8), seed 4",
+    5: "cfg5: R,S 200,000,000 tuples each, x,z~U[0,1e7), y~Zipf(1.2) over [0,1e6), seed 5",
+}
+METRIC = "input tuples/sec and distinct (x,z) pairs/sec at 1/2/4/8 B200 vs roofline"
+L2_BYTES = 126 * 1024 * 1024
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "_fallback": True}
+
+
+def _golden():
+    try:
+        return json.load(open(os.path.join(ROOT, "tests", "golden", "golden.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._pump, daemon=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _pump(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
+    ap.add_argument("--cpu-frac", type=float, default=0.02,
+                    help="x-slice fraction timed on the CPU reference")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------------------
+def cpu_reference_sample(cfg: int, frac: float, threads: int, tables=None):
+    """Reference prep on the whole job + reference kernels on an x-slice,
+    extrapolated linearly in x. Returns (seconds_full_job_estimate, detail)."""
+    from oracle import oracle as O
+    if tables is None:
+        r = O.gen(cfg, 0)
+        s = O.gen(cfg, 1)
+    else:
+        r, s = tables
+    x_hi = None
+    # x codes are natural for cfg 1/2/3/5 (identity), dictionary codes for cfg4;
+    # slicing rows of r_by_x is the same either way.
+    probe = O.ref_timed_sample(r, s, threads, 0, 0)
+    x_rows = probe["x_rows"]
+    x_hi = max(1, int(x_rows * frac))
+    t = O.ref_timed_sample(r, s, threads, 0, x_hi)
+    est = t["sec_prep"] + t["sec_kernels"] * (x_rows / x_hi)
+    detail = dict(t, x_slice=[0, x_hi], est_full_s=est)
+    return est, detail
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    cfg = args.config
+    n_tuples = 2 * O.cfg_rows(cfg)
+    threads = os.cpu_count() or 1
+    r, s = O.gen(cfg, 0), O.gen(cfg, 1)
+    for _ in range(args.warmup):
+        cpu_reference_sample(cfg, args.cpu_frac, threads, (r, s))
+    ests = []
+    for _ in range(args.steps):
+        est, detail = cpu_reference_sample(cfg, args.cpu_frac, threads, (r, s))
+        ests.append(est)
+    sec = sum(ests) / len(ests)
+    value = n_tuples / sec
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tuples/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic (convention G)",
+        "config": {"workload": WORKLOADS[cfg], "count_only": True, "force": "auto",
+                   "consts": "test_consts()"},
+        "cpu_baseline": {"value": value, "unit": "tuples/s", "cores": threads, "kind": "reference",
+                         "sample": f"reference prep (map/CSR/stats/partition) on the whole job + "
+                                   f"reference sparse_bmm/dense_ec on x rows {detail['x_slice']} "
+                                   f"of {detail['x_rows']}, kernel time extrapolated linearly in x"},
+        "e2e": {"value": value, "unit": "tuples/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "detail": detail,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    rank, world, local = dist_env()
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2206_04995_b200 as d3
+
+    cfg_id = args.config
+    ctx = d3.Context(local)
+    n_rows = d3.cfg_rows(cfg_id)
+    # inputs: generated on rank 0's GPU, broadcast over NVLink (NCCL)
+    if rank == 0:
+        rl, rr = d3.generate(cfg_id, 0, ctx=ctx)
+        sl, sr = d3.generate(cfg_id, 1, ctx=ctx)
+    else:
+        rl, rr, sl, sr = (torch.empty(n_rows, dtype=torch.int64, device=dev) for _ in range(4))
+    if world > 1:
+        for t in (rl, rr, sl, sr):
+            dist.broadcast(t, src=0)
+    torch.cuda.synchronize(dev)
+    R, S = d3.RawTable(rl, rr), d3.RawTable(sl, sr)
+    n_tuples = 2 * n_rows
+    consts = d3.CostConstants.test_consts()
+    ecfg = d3.EngineConfig(force=d3.Strategy.auto_select, count_only=True,
+                           memory_budget_bytes=150 << 30, shard_index=rank, shard_count=world)
+    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device=dev)
+
+    def one_step():
+        flush.zero_()  # evict L2 between steps (outside the timed device region)
+        torch.cuda.synchronize(dev)
+        return d3.join_project(R, S, ecfg, consts, ctx=ctx)
+
+    for _ in range(max(args.warmup, 1)):
+        rep = one_step().report
+    local_pairs = rep.out_p
+
+    # ---- timed region -----------------------------------------------------
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    sampler = ClockSampler(local)
+    reps = []
+    wall0 = time.perf_counter()
+    with sampler:
+        for _ in range(args.steps):
+            reps.append(one_step().report)
+    torch.cuda.synchronize(dev)
+    wall = time.perf_counter() - wall0
+    if world > 1:
+        dist.barrier()
+    dev_s = sum(r.ms_total for r in reps) * 1e-3
+    phase = {k: sum(getattr(r, k) for r in reps) / len(reps)
+             for k in ("ms_estimate", "ms_map", "ms_csr", "ms_stats", "ms_partition", "ms_sparse",
+                       "ms_dense", "ms_decode", "ms_total")}
+    launches = sum(r.gpu_launches for r in reps)
+    t = torch.tensor([dev_s, float(local_pairs), float(launches)], dtype=torch.float64,
+                     device=dev)
+    if world > 1:
+        mx = t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = t.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        dev_s, total_pairs, launches = mx[0].item(), int(sm[1].item()), int(sm[2].item())
+    else:
+        total_pairs = local_pairs
+    sec_per_step = dev_s / args.steps
+    value = n_tuples / sec_per_step
+    clocks = sampler.summary()
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    r0 = reps[-1]
+    # ---- roofline of the dominant phase -----------------------------------
+    peaks = _peaks()
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    golden = _golden().get(f"cfg{cfg_id}", {})
+    ref_rep = golden.get("ref_hybrid_report", {})
+    alu = d3.alu_peak(ctx)
+    s_in = 8
+    X, Y, Z = r0.x_card, r0.y_card, r0.z_card
+    b_map = 2 * s_in * n_tuples + 4 * r0.r_nnz + 8 * (X + 1) + 4 * r0.s_nnz + 8 * (Z + 1) + \
+        4 * r0.sparse_nnz + 8 * (Y + 1)
+    b_sparse = 4 * r0.r_nnz + 8 * (X + 1) + 16 * r0.r_nnz + 4 * r0.spa_inner_count + 8 * X
+    w_dense = None
+    if ref_rep and world == 1:
+        w_dense = 8 * ref_rep["dense_blocks_checked"] + ref_rep["dense_probes_done"]
+    prep_ms = phase["ms_map"] + phase["ms_csr"] + phase["ms_stats"] + phase["ms_partition"]
+    cand = {"map+csr+partition": prep_ms, "sparse_bmm": phase["ms_sparse"],
+            "dense_ec": phase["ms_dense"]}
+    dom = max(cand, key=cand.get)
+    if dom == "dense_ec" and w_dense:
+        achieved = w_dense / (phase["ms_dense"] * 1e-3)
+        roof = {"kernel": "dense_ec", "bound": "int_alu", "achieved": achieved / 1e12,
+                "peak": alu / 1e12, "unit": "Tops/s", "frac": achieved / alu, "traffic": None,
+                "work": f"W_D = 8*blocks_checked + probes_done of the reference's early-exit "
+                        f"DenseEC on this input = {w_dense:.4g} 32-bit word-ops",
+                "peak_source": "measured LOP3 throughput (d3g_alu_peak) in this run"}
+    elif dom == "sparse_bmm":
+        achieved = b_sparse / (phase["ms_sparse"] * 1e-3) / 1e9
+        roof = {"kernel": "sparse_bmm", "bound": "hbm", "achieved": achieved, "peak": hbm,
+                "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+                "work": f"B_S = {b_sparse:.4g} bytes (SURVEY 8(d))",
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+    else:
+        achieved = b_map / (prep_ms * 1e-3) / 1e9
+        roof = {"kernel": "map+csr+partition", "bound": "hbm", "achieved": achieved, "peak": hbm,
+                "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+                "work": f"B_M = {b_map:.4g} compulsory bytes (SURVEY 8(d))",
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+    phases_roof = {
+        "map+csr+partition": {"ms": prep_ms, "GB/s": b_map / (prep_ms * 1e-3) / 1e9 if prep_ms else None},
+        "sparse_bmm": {"ms": phase["ms_sparse"],
+                       "GB/s": b_sparse / (phase["ms_sparse"] * 1e-3) / 1e9 if phase["ms_sparse"] else None},
+        "dense_ec": {"ms": phase["ms_dense"],
+                     "Tops/s": (w_dense / (phase["ms_dense"] * 1e-3) / 1e12)
+                     if (w_dense and phase["ms_dense"]) else None},
+    }
+
+    # ---- e2e through the C ABI from pinned host buffers -------------------
+    e2e = None
+    if not args.no_e2e and world == 1 and not args.profile:
+        hbuf = [torch.empty(n_rows, dtype=torch.int64, pin_memory=True) for _ in range(4)]
+        for h, d in zip(hbuf, (rl, rr, sl, sr)):
+            h.copy_(d)
+        Rh = d3.RawTable(hbuf[0].numpy().view(np.uint64), hbuf[1].numpy().view(np.uint64))
+        Sh = d3.RawTable(hbuf[2].numpy().view(np.uint64), hbuf[3].numpy().view(np.uint64))
+        for _ in range(max(1, args.warmup)):
+            d3.join_project(Rh, Sh, ecfg, consts, ctx=ctx)
+        ts, h2d, d2h = [], 0, 0
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            o = d3.join_project(Rh, Sh, ecfg, consts, ctx=ctx)
+            ts.append(time.perf_counter() - t0)
+            h2d, d2h = o.report.h2d_bytes, o.report.d2h_bytes
+            assert o.report.out_p == total_pairs
+        e2e = {"value": n_tuples / (sum(ts) / len(ts)), "unit": "tuples/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": 1e3 * sum(ts) / len(ts),
+               "pairs_per_sec": total_pairs / (sum(ts) / len(ts))}
+
+    # ---- CPU baseline (reference on host cores, bounded sample) -----------
+    cpu = None
+    if not args.no_cpu_baseline and world == 1 and not args.profile:
+        try:
+            from oracle import oracle as O
+            if O.ref_available():
+                threads = os.cpu_count() or 1
+                est, detail = cpu_reference_sample(cfg_id, args.cpu_frac, threads)
+                cpu = {"value": n_tuples / est, "unit": "tuples/s", "cores": threads,
+                       "kind": "reference",
+                       "sample": f"reference map/CSR/partition on the whole job + reference "
+                                 f"sparse_bmm/dense_ec on x rows {detail['x_slice']} of "
+                                 f"{detail['x_rows']}, kernels extrapolated linearly in x "
+                                 f"(prep {detail['sec_prep']:.2f}s, slice kernels "
+                                 f"{detail['sec_kernels']:.2f}s)",
+                       "est_full_job_s": est}
+            else:
+                cpu = {"value": None, "unavailable": "oracle/_ref not built"}
+        except Exception as e:  # report, never fail the GPU line
+            cpu = {"value": None, "unavailable": repr(e)[:200]}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "tuples/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec_per_step * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (convention G, generated on device)",
+        "config": {"workload": WORKLOADS[cfg_id], "count_only": True, "force": "auto",
+                   "consts": "test_consts()", "parallelism": f"x-shard x{world}",
+                   "l2": "256 MB buffer zeroed between steps (outside the timed device region); "
+                         f"inputs {n_tuples * 8 / 1e6:.0f} MB"},
+        "pairs_per_sec": total_pairs / sec_per_step, "out_p": total_pairs,
+        "roofline": roof, "phases": phases_roof, "phase_ms": phase,
+        "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+        "clocks": clocks, "wall_s_timed": wall,
+        "report": {k: getattr(r0, k) for k in ("strategy", "f1_gate_classical", "dense_z",
+                                                 "sparse_z", "x_live", "out_j", "spa_inner_count",
+                                                 "peak_bytes")},
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

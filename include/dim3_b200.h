@@ -189,6 +189,9 @@ int d3g_dense_ec_rows(d3g_ctx* ctx, const d3g_csr* r_by_x, const d3g_panel* pane
 int d3g_generate(d3g_ctx* ctx, int cfg, int side, uint64_t lo, uint64_t hi, uint64_t* left,
                  uint64_t* right);
 uint64_t d3g_cfg_rows(int cfg);
+/* Measured 32-bit logic-op throughput of this device (LOP3 chains, ops/s);
+ * the denominator of the DenseEC integer-pipe roofline. */
+int d3g_alu_peak(d3g_ctx* ctx, double* ops_per_sec);
 int d3g_ctx_device(d3g_ctx* ctx);
 
 /* Host-only policy entry points (callable without a GPU). */

@@ -160,6 +160,9 @@ def ref_lib():
                                          U64P, U64P, U64P]
         lib.ref_f3_threshold.argtypes = [C.c_uint32, C.c_uint32, C.POINTER(Consts),
                                          C.POINTER(C.c_uint32)]
+        lib.ref_timed_sample.argtypes = [U64P, U64P, C.c_uint64, U64P, U64P, C.c_uint64,
+                                         C.POINTER(Consts), C.c_int, C.c_uint64, C.c_uint64,
+                                         C.POINTER(C.c_double), C.POINTER(C.c_double), U64P, U64P]
         lib.ref_mx_bucket_key.argtypes = [C.c_uint32]
         lib.ref_mx_bucket_key.restype = C.c_uint32
         lib.ref_mz_bucket_index.argtypes = [C.c_uint32, C.c_uint32]
@@ -303,6 +306,21 @@ def ref_set_checksum(r: Table, s: Table, threads=8, rows_per_slice=1024, block_w
     if n_blocks:
         d.update(blk_count=bc, blk_sum=bs, blk_xor=bx)
     return d
+
+
+def ref_timed_sample(r: Table, s: Table, threads: int, x_lo: int, x_hi: int, consts=None):
+    """Reference prep on the whole tables + reference kernels on x rows [x_lo, x_hi)."""
+    lib = ref_lib()
+    rl, rr, sl, sr = (_u64(a) for a in (r.left, r.right, s.left, s.right))
+    c = make_consts(consts)
+    tp, tk = C.c_double(), C.c_double()
+    xr, pr = C.c_uint64(), C.c_uint64()
+    rc = lib.ref_timed_sample(_p(rl), _p(rr), len(rl), _p(sl), _p(sr), len(sl), C.byref(c),
+                              threads, x_lo, x_hi, C.byref(tp), C.byref(tk), C.byref(xr),
+                              C.byref(pr))
+    if rc:
+        raise ConfigErrorLike(rc, lib.ref_last_error().decode())
+    return dict(sec_prep=tp.value, sec_kernels=tk.value, x_rows=xr.value, pairs=pr.value)
 
 
 def mix64(x: int) -> int:

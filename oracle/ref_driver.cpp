@@ -18,6 +18,7 @@
 // Appendix A).
 
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <cstdint>
 #include <cstring>
@@ -384,3 +385,57 @@ std::uint32_t ref_mz_bucket_index(std::uint32_t m, std::uint32_t y) {
 }
 
 }  // extern "C"
+
+// Bounded CPU sample of the reference's own hybrid path for the bench's
+// reference arm / cpu_baseline: the full preparation (map_tables, build_csr,
+// compute_degree_stats, partition_s_csr — the same calls join_project makes,
+// P/src/engine.cpp:401-427) on the WHOLE tables, then the reference kernels
+// sparse_bmm / dense_ec (count-only, `threads` workers) on rows
+// [x_lo, x_hi) of r_by_x. The caller extrapolates the kernel time linearly
+// in x. Seconds are wall-clock (steady_clock).
+extern "C" int ref_timed_sample(const std::uint64_t* rl, const std::uint64_t* rr,
+                                std::uint64_t nr, const std::uint64_t* sl,
+                                const std::uint64_t* sr, std::uint64_t ns,
+                                const RefConsts* consts, int threads, std::uint64_t x_lo,
+                                std::uint64_t x_hi, double* sec_prep, double* sec_kernels,
+                                std::uint64_t* x_rows, std::uint64_t* pairs_in_slice) {
+  try {
+    using Clk = std::chrono::steady_clock;
+    dim3::RawTable R = to_table(rl, rr, nr);
+    dim3::RawTable S = to_table(sl, sr, ns);
+    dim3::CostConstants c = to_consts(consts);
+    auto t0 = Clk::now();
+    dim3::MappingOutput m = map_like_engine(R, S);
+    dim3::CsrMatrix r_by_x = dim3::build_csr(m.r, true);
+    dim3::CsrMatrix s_by_z = dim3::build_csr(m.s, true);
+    dim3::DegreeStats st = dim3::compute_degree_stats(r_by_x, s_by_z);
+    dim3::PartitionResult part = dim3::partition_s_csr(s_by_z, st, c);
+    auto t1 = Clk::now();
+    std::uint64_t n_rows = r_by_x.n_rows;
+    x_hi = std::min(x_hi, n_rows);
+    x_lo = std::min(x_lo, x_hi);
+    dim3::CsrMatrix sl_m;
+    sl_m.n_rows = static_cast<dim3::Code>(x_hi - x_lo);
+    sl_m.n_cols = r_by_x.n_cols;
+    std::uint64_t b0 = r_by_x.row_ptr[x_lo], b1 = r_by_x.row_ptr[x_hi];
+    sl_m.row_ptr.resize(x_hi - x_lo + 1);
+    for (std::uint64_t i = x_lo; i <= x_hi; ++i) sl_m.row_ptr[i - x_lo] = r_by_x.row_ptr[i] - b0;
+    sl_m.col.assign(r_by_x.col.begin() + b0, r_by_x.col.begin() + b1);
+    auto t2 = Clk::now();
+    dim3::SparseOptions so;
+    so.threads = threads;
+    dim3::DenseOptions dopt;
+    dopt.threads = threads;
+    std::uint64_t a = dim3::sparse_bmm(sl_m, part.s_sparse_by_y, m.s.a_card, so);
+    std::uint64_t b = dim3::dense_ec(sl_m, part.panel, c, dopt);
+    auto t3 = Clk::now();
+    *sec_prep = std::chrono::duration<double>(t1 - t0).count();
+    *sec_kernels = std::chrono::duration<double>(t3 - t2).count();
+    *x_rows = n_rows;
+    *pairs_in_slice = a + b;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return status_of(e);
+  }
+}

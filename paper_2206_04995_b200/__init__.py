@@ -25,6 +25,7 @@ from .engine import (  # noqa: F401
     ResourceError,
     ResultSet,
     SkipFlags,
+    alu_peak,
     Strategy,
     build_csr,
     cfg_rows,

@@ -81,6 +81,7 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[24] = {};
   uint64_t launches = 0;
+  uint64_t d2h_bytes = 0;  // device->host bytes read back by the current call
   uint64_t live_bytes = 0, peak_bytes = 0, budget = 0;
   int sm_count = kNumSMs;
   size_t smem_optin = 0;
@@ -137,6 +138,7 @@ struct Ctx {
       D3G_CUDA(cudaMallocHost(&pinned, pinned_bytes));
     }
     D3G_CUDA(cudaMemcpyAsync(pinned, src, bytes, cudaMemcpyDeviceToHost, stream));
+    d2h_bytes += bytes;
     sync();
     std::memcpy(dst, pinned, bytes);
   }

@@ -1,0 +1,327 @@
+// DenseEC v3: hot bit-sliced existence + cold residual join.
+//
+// Rank the y codes by R-side degree (hottest first) and fix K (a multiple of
+// 64). For a pair (x, dense z):
+//   hit  <=>  R_hot[x] & S_hot[z] != 0   OR   R_cold[x] & S_cold[z] != 0.
+// P1 (this file, dense_hot_kernel) counts the pairs with a common HOT y,
+// bit-sliced over groups of 128 live x: every dense z carries a K-bit mask
+// hz[z] of its hot ranks; every x group carries T[g][r] = {x in g : rank r in
+// R[x]} (uint4, 128 bits) for r < K. For each (z, group):
+//      acc = OR_{r in hz[z]} T[g][r]   (early exit once acc == all-live)
+// and popc(acc) pairs are hit. T for a batch of groups is staged into shared
+// memory with one TMA bulk copy (cp.async.bulk + mbarrier transaction count).
+// P2 (engine.cu, through the SparseBMM tiers with a filter) counts pairs that
+// share only COLD y: the cold join R_cold x S_cold restricted to dense z,
+// dedup'd per x, skipping candidates whose hot masks already intersect. The
+// two parts are disjoint and together equal the reference's dense_ec output
+// (P/src/denseec.cpp:8-86): {(x, z) : R[x] and S[z] share a y}, z dense.
+#pragma once
+
+#include "sparsebmm.cuh"
+
+namespace d3g {
+
+constexpr int kHotThreads = 1024;
+
+struct HotParams {
+  const uint4* T;          // [batch of 32 groups][K][32] (uint4 = 128 member bits)
+  const uint64_t* hz;      // [n_dense][K/64]
+  const uint32_t* xorder;  // live x codes by position
+  const uint32_t* dl_z;    // z code per dense row position
+  uint64_t n_live, n_dense;
+  uint32_t groups, K, kw;  // kw = K / 64
+  uint32_t batch;          // groups per smem batch
+  uint32_t z_chunks;       // z ranges per batch (units = batches * z_chunks)
+  unsigned int* work;
+};
+
+// T, hx from the live x in degree order: warp per x position.
+__global__ void hot_build_x_kernel(const uint32_t* __restrict__ xorder, uint64_t n_live,
+                                   const uint64_t* __restrict__ r_ptr,
+                                   const uint32_t* __restrict__ r_col,
+                                   const uint32_t* __restrict__ y_rank, uint32_t K, uint32_t kw,
+                                   uint32_t* __restrict__ T, unsigned long long* __restrict__ hx) {
+  for (uint64_t p = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); p < n_live;
+       p += (uint64_t)gridDim.x * (blockDim.x / 32)) {
+    uint32_t x = xorder[p];
+    uint64_t g = p >> 7;
+    uint64_t bi = g >> 5, gl = g & 31;
+    uint32_t b = (uint32_t)(p & 127);
+    for (uint64_t k = r_ptr[x] + lane_id(); k < r_ptr[x + 1]; k += 32) {
+      uint32_t r = y_rank[r_col[k]];
+      if (r < K) {
+        atomicOr(&T[((bi * K + r) * 32 + gl) * 4 + (b >> 5)], 1u << (b & 31));
+        atomicOr(&hx[(uint64_t)x * kw + (r >> 6)], 1ull << (r & 63));
+      }
+    }
+  }
+}
+
+// hz from the dense lists (ranks ascending: the hot ranks are a prefix).
+__global__ void hot_build_z_kernel(const uint64_t* __restrict__ dl_ptr,
+                                   const uint32_t* __restrict__ dl_col, uint64_t n_dense,
+                                   uint32_t K, uint32_t kw, unsigned long long* __restrict__ hz,
+                                   uint32_t* __restrict__ cold_len) {
+  for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < n_dense;
+       i += (uint64_t)gridDim.x * (blockDim.x / 32)) {
+    uint32_t ncold = 0;
+    for (uint64_t k = dl_ptr[i] + lane_id(); k < dl_ptr[i + 1]; k += 32) {
+      uint32_t r = dl_col[k];
+      if (r < K)
+        atomicOr(&hz[i * kw + (r >> 6)], 1ull << (r & 63));
+      else
+        ++ncold;
+    }
+    ncold = warp_sum(ncold);
+    if (lane_id() == 0 && cold_len) cold_len[i] = ncold;
+  }
+}
+
+// Cold residual side: per y, dense row positions whose lists hold y at a
+// cold rank (y-major CSR, rows indexed by y code).
+__global__ void cold_count_kernel(const uint64_t* __restrict__ dl_ptr,
+                                  const uint32_t* __restrict__ dl_col, uint64_t n_dense, uint32_t K,
+                                  const uint32_t* __restrict__ y_of_rank, uint32_t* __restrict__ cnt) {
+  for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < n_dense;
+       i += (uint64_t)gridDim.x * (blockDim.x / 32))
+    for (uint64_t k = dl_ptr[i] + lane_id(); k < dl_ptr[i + 1]; k += 32) {
+      uint32_t r = dl_col[k];
+      if (r >= K) atomicAdd(&cnt[y_of_rank[r]], 1u);
+    }
+}
+
+__global__ void cold_scatter_kernel(const uint64_t* __restrict__ dl_ptr,
+                                    const uint32_t* __restrict__ dl_col, uint64_t n_dense,
+                                    uint32_t K, const uint32_t* __restrict__ y_of_rank,
+                                    unsigned long long* __restrict__ cursor,
+                                    uint32_t* __restrict__ out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < n_dense;
+       i += (uint64_t)gridDim.x * (blockDim.x / 32))
+    for (uint64_t k = dl_ptr[i] + lane_id(); k < dl_ptr[i + 1]; k += 32) {
+      uint32_t r = dl_col[k];
+      if (r >= K) out[atomicAdd(&cursor[y_of_rank[r]], 1ull)] = (uint32_t)i;
+    }
+}
+
+// --- TMA bulk copy helpers (sm_90+ PTX, used on sm_100a) -------------------
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                             uint64_t* bar) {
+  uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+  uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
+      "l"(src), "r"(bytes), "r"(b)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(phase)
+      : "memory");
+}
+
+__device__ __forceinline__ uint4 full_mask(uint32_t members) {
+  uint4 f;
+  f.x = members >= 32 ? 0xffffffffu : ((1u << members) - 1);
+  f.y = members >= 64 ? 0xffffffffu : (members <= 32 ? 0u : ((1u << (members - 32)) - 1));
+  f.z = members >= 96 ? 0xffffffffu : (members <= 64 ? 0u : ((1u << (members - 64)) - 1));
+  f.w = members >= 128 ? 0xffffffffu : (members <= 96 ? 0u : ((1u << (members - 96)) - 1));
+  return f;
+}
+
+// P1 kernel. A batch = 32 consecutive 128-x groups; its slice table lives in
+// shared memory r-major, Ts[r][lane] (uint4), so for a fixed hot rank r the
+// 32 lanes read 512 contiguous bytes (conflict-free LDS.128). One warp owns
+// one dense z at a time and walks the hot prefix of z's list (ranks ascending,
+// warp-uniform broadcast loads); lane l accumulates group l's 128-bit hit mask.
+// The batch table (K * 512 B, contiguous in global memory) is staged by one
+// TMA bulk copy per batch change.
+template <int kMode>
+__global__ void __launch_bounds__(kHotThreads, 1)
+dense_hot_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
+                 const uint32_t* __restrict__ dl_col, Decode dec, Emit em, Tally* tally) {
+  extern __shared__ __align__(128) uint4 Ts[];  // [K][32]
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ unsigned int s_unit;
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const uint32_t n_batches = (p.groups + 31) / 32;
+  const unsigned int n_units = n_batches * p.z_chunks;
+  uint64_t cnt = 0, sum = 0, xr = 0;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  uint32_t phase = 0;
+  int cur_batch = -1;
+  for (;;) {
+    if (threadIdx.x == 0) s_unit = atomicAdd(p.work, 1u);
+    __syncthreads();
+    const unsigned int unit = s_unit;
+    if (unit >= n_units) break;
+    const uint32_t bi = unit / p.z_chunks, zc_i = unit % p.z_chunks;
+    if ((int)bi != cur_batch) {
+      if (threadIdx.x == 0) {
+        const uint32_t bytes = p.K * 32u * 16u;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&bar, bytes);
+        tma_bulk_g2s(Ts, p.T + (uint64_t)bi * p.K * 32, bytes, &bar);
+      }
+      mbar_wait(&bar, phase);
+      phase ^= 1;
+      cur_batch = (int)bi;
+    }
+    const uint32_t g = bi * 32 + lane;  // this lane's group
+    const bool lane_live = g < p.groups;
+    const uint64_t gp0 = (uint64_t)g * 128;
+    const uint32_t members =
+        lane_live ? (uint32_t)((p.n_live - gp0) < 128 ? (p.n_live - gp0) : 128) : 0;
+    const uint4 full = full_mask(members);
+    const uint64_t z_lo = p.n_dense * zc_i / p.z_chunks, z_hi = p.n_dense * (zc_i + 1) / p.z_chunks;
+    for (uint64_t i = z_lo + warp; i < z_hi; i += nwarps) {
+      const uint64_t k0 = dl_ptr[i], k1 = dl_ptr[i + 1];
+      uint4 acc = make_uint4(0, 0, 0, 0);
+      // the hot prefix of z's list, 32 entries per coalesced lane-load,
+      // broadcast with shuffles; LDS.128 of successive ranks are independent
+      for (uint64_t base = k0; base < k1; base += 32) {
+        const uint32_t mine = base + lane < k1 ? dl_col[base + lane] : 0xffffffffu;
+        const uint32_t nhot = __popc(__ballot_sync(0xffffffffu, mine < p.K));
+#pragma unroll 4
+        for (uint32_t j = 0; j < nhot; ++j) {
+          const uint32_t r = __shfl_sync(0xffffffffu, mine, j);
+          const uint4 v = Ts[r * 32 + lane];
+          acc.x |= v.x;
+          acc.y |= v.y;
+          acc.z |= v.z;
+          acc.w |= v.w;
+        }
+        if (nhot < 32) break;  // ranks ascend: the hot prefix ended
+      }
+      const uint32_t c = __popc(acc.x) + __popc(acc.y) + __popc(acc.z) + __popc(acc.w);
+      cnt += c;
+      if (kMode != kModeCount && c) {
+        const uint32_t zc = p.dl_z[i];
+        const uint32_t words[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+        for (int wi = 0; wi < 4; ++wi) {
+          uint32_t bits = words[wi];
+          while (bits) {
+            const int b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const uint32_t xc = p.xorder[gp0 + wi * 32 + b];
+            if (kMode == kModeChecksum) {
+              const uint64_t h = dec.hash(xc, zc);
+              sum += h;
+              xr ^= h;
+            } else {
+              const unsigned long long idx = atomicAdd(em.cursor, 1ull);
+              if (idx < em.cap) {
+                em.x[idx] = xc;
+                em.z[idx] = zc;
+              }
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();  // Ts may be overwritten by the next unit's copy
+  }
+  tally_flush(tally, cnt, sum, xr);
+}
+
+
+// P2 kernel: cold residual for a dense block whose row count fits a per-warp
+// shared-memory bitmap. One warp per live x. The cold CSR (y-major, rows =
+// dense row positions holding y at a cold rank) stores each candidate's
+// 256-bit hot signature inline (ch, 2 x uint4 per entry), so the filter
+// "hot masks intersect => already counted by P1" streams coalesced instead of
+// gathering hz[z] at random. Survivors are deduplicated in the warp's bitmap.
+constexpr int kColdWarps = 8;
+
+__global__ void cold_sig_kernel(const uint32_t* __restrict__ ccol, uint64_t n,
+                                const uint4* __restrict__ hz4 /* [D][2] */,
+                                uint4* __restrict__ ch /* [n][2] */) {
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t zi = ccol[t];
+    ch[2 * t] = hz4[2 * (uint64_t)zi];
+    ch[2 * t + 1] = hz4[2 * (uint64_t)zi + 1];
+  }
+}
+
+template <int kMode>
+__global__ void __launch_bounds__(kColdWarps * 32, 1)
+dense_cold_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
+                  const uint64_t* __restrict__ r_ptr, const uint32_t* __restrict__ r_col,
+                  const uint64_t* __restrict__ cptr, const uint32_t* __restrict__ ccol,
+                  const uint4* __restrict__ ch, const uint4* __restrict__ hx4 /* [X][2] */,
+                  uint32_t d_words, const uint32_t* __restrict__ dl_z, Decode dec, Emit em,
+                  unsigned int* __restrict__ next, Tally* tally) {
+  extern __shared__ __align__(16) uint32_t cbm[];  // [kColdWarps][d_words]
+  const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
+  uint32_t* bm = cbm + (uint64_t)w * d_words;
+  for (uint32_t i = lane; i < d_words; i += 32) bm[i] = 0;
+  __syncwarp();
+  uint64_t cnt = 0, sum = 0, xr = 0;
+  for (;;) {
+    uint32_t item = 0;
+    if (lane == 0) item = atomicAdd(next, 1u);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= n_x) break;
+    const uint32_t x = xs[item];
+    const uint4 a0 = hx4[2 * (uint64_t)x], a1 = hx4[2 * (uint64_t)x + 1];
+    bool touched = false;
+    for (uint64_t k = r_ptr[x]; k < r_ptr[x + 1]; ++k) {
+      const uint32_t y = r_col[k];
+      const uint64_t s0 = cptr[y], s1 = cptr[y + 1];
+      for (uint64_t t = s0 + lane; t < s1; t += 32) {
+        const uint4 b0 = ch[2 * t], b1 = ch[2 * t + 1];
+        const bool hot = ((a0.x & b0.x) | (a0.y & b0.y) | (a0.z & b0.z) | (a0.w & b0.w) |
+                          (a1.x & b1.x) | (a1.y & b1.y) | (a1.z & b1.z) | (a1.w & b1.w)) != 0;
+        if (hot) continue;
+        const uint32_t zi = ccol[t];
+        const uint32_t bit = 1u << (zi & 31);
+        const uint32_t old = atomicOr(&bm[zi >> 5], bit);
+        touched = true;
+        if (old & bit) continue;
+        ++cnt;
+        if (kMode == kModeChecksum) {
+          const uint64_t h = dec.hash(x, dl_z[zi]);
+          sum += h;
+          xr ^= h;
+        } else if (kMode == kModeEmit) {
+          const unsigned long long idx = atomicAdd(em.cursor, 1ull);
+          if (idx < em.cap) {
+            em.x[idx] = x;
+            em.z[idx] = dl_z[zi];
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (__any_sync(0xffffffffu, touched))
+      for (uint32_t i = lane; i < d_words; i += 32) bm[i] = 0;
+    __syncwarp();
+  }
+  tally_flush(tally, cnt, sum, xr);
+}
+
+}  // namespace d3g

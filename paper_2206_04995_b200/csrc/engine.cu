@@ -12,13 +12,16 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <limits>
 #include <string>
+#include <type_traits>
 #include <unordered_map>
 #include <vector>
 
 #include "datagen.cuh"
 #include "denseec.cuh"
+#include "denseec_hot.cuh"
 #include "mapping.cuh"
 #include "partition.cuh"
 #include "sparsebmm.cuh"
@@ -182,6 +185,7 @@ struct SparseInputs {
   const uint32_t* sp_col;     // compact sparse index
   const uint32_t* sparse_ids; // compact index -> z code
   uint64_t n_sparse;
+  uint64_t y_card;            // rows of sp_ptr
   // shard of x handled (x code range)
   uint64_t x_lo, x_hi;
 };
@@ -191,68 +195,122 @@ struct KernelOut {
   uint64_t inner = 0;
 };
 
+template <class F>
+void with_mode(int mode, F&& f) {
+  if (mode == d3g::kModeCount) f(std::integral_constant<int, d3g::kModeCount>{});
+  else if (mode == d3g::kModeChecksum) f(std::integral_constant<int, d3g::kModeChecksum>{});
+  else f(std::integral_constant<int, d3g::kModeEmit>{});
+}
+
+__global__ void sparse_bin_kernel(const uint64_t* __restrict__ cx, uint64_t n, uint64_t small_max,
+                                  uint64_t mid_max, uint32_t* __restrict__ f1,
+                                  uint32_t* __restrict__ f2, uint32_t* __restrict__ f3) {
+  for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n;
+       x += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t c = cx[x];
+    f1[x] = (c > 0 && c <= small_max) ? 1u : 0u;
+    f2[x] = (c > small_max && c <= mid_max) ? 1u : 0u;
+    f3[x] = c > mid_max ? 1u : 0u;
+  }
+}
+
+// SparseBMM driver. Tiers per x by candidate count c_x (= its inner count):
+//   c_x <= 32                     warp, register bitonic sort
+//   n_sparse <= 8192, c_x > 32    warp, OR of bitset rows in registers
+//   32 < c_x <= 1024              warp-private shared-memory hash set
+//   c_x > 1024                    CTA bitmap over the sparse index (smem, or
+//                                 a per-CTA global slice when too large)
 void run_sparse(Ctx& X, const SparseInputs& in, d3g::Decode dec, int mode, d3g::Emit em,
-                KernelOut& out) {
+                KernelOut& out, d3g::Filter flt = d3g::Filter{nullptr, nullptr, 0}) {
   using namespace d3g;
   if (in.n_rows == 0 || in.n_sparse == 0 || in.x_hi <= in.x_lo) return;
-  uint64_t nx = in.x_hi - in.x_lo;
+  const uint64_t nx = in.x_hi - in.x_lo;
+  const uint32_t n_words = (uint32_t)((in.n_sparse + 31) / 32);
+  const bool bitset_tier = flt.hz == nullptr && n_words <= 32u * kBitsetMaxWordsPerLane;
+  const uint64_t mid_max = bitset_tier ? ~0ull : (uint64_t)(kHashCap / 2);
   DBuf<uint64_t> cx = X.alloc<uint64_t>(nx);
   DBuf<unsigned long long> tot = X.zeros<unsigned long long>(1);
   D3G_LAUNCH(X, sparse_cx_kernel, grid_for(nx, 256), 256, 0, in.r_ptr + in.x_lo, in.r_col, nx,
              in.sp_ptr, cx.p, tot.p);
-  DBuf<uint32_t> fs = X.alloc<uint32_t>(nx), fl = X.alloc<uint32_t>(nx);
-  D3G_LAUNCH(X, bin_flags_kernel, grid_for(nx, 256), 256, 0, cx.p, nx, 32ull, fs.p, fl.p);
-  DBuf<uint64_t> ps = X.alloc<uint64_t>(nx + 1), pl = X.alloc<uint64_t>(nx + 1);
-  exclusive_scan<uint32_t>(X, fs.p, nx, ps.p);
-  exclusive_scan<uint32_t>(X, fl.p, nx, pl.p);
-  uint64_t n_small = X.scalar(ps.p + nx), n_large = X.scalar(pl.p + nx);
-  out.inner = X.scalar(tot.p);
-  DBuf<uint32_t> xs = X.alloc<uint32_t>(n_small), xl = X.alloc<uint32_t>(n_large);
-  D3G_LAUNCH(X, index_compact_kernel, grid_for(nx, 256), 256, 0, fs.p, ps.p, nx, xs.p);
-  D3G_LAUNCH(X, index_compact_kernel, grid_for(nx, 256), 256, 0, fl.p, pl.p, nx, xl.p);
-  if (in.x_lo) {
-    if (n_small) D3G_LAUNCH(X, add_offset_kernel, grid_for(n_small, 256), 256, 0, xs.p, n_small, (uint32_t)in.x_lo);
-    if (n_large) D3G_LAUNCH(X, add_offset_kernel, grid_for(n_large, 256), 256, 0, xl.p, n_large, (uint32_t)in.x_lo);
+  DBuf<uint32_t> fl[3];
+  DBuf<uint64_t> pos[3];
+  DBuf<uint32_t> lists[3];
+  uint64_t cnt[3];
+  for (int b = 0; b < 3; ++b) {
+    fl[b] = X.alloc<uint32_t>(nx);
+    pos[b] = X.alloc<uint64_t>(nx + 1);
   }
+  D3G_LAUNCH(X, sparse_bin_kernel, grid_for(nx, 256), 256, 0, cx.p, nx, 32ull, mid_max, fl[0].p,
+             fl[1].p, fl[2].p);
+  for (int b = 0; b < 3; ++b) exclusive_scan<uint32_t>(X, fl[b].p, nx, pos[b].p);
+  for (int b = 0; b < 3; ++b) {
+    cnt[b] = X.scalar(pos[b].p + nx);
+    lists[b] = X.alloc<uint32_t>(cnt[b]);
+    if (cnt[b]) {
+      D3G_LAUNCH(X, index_compact_kernel, grid_for(nx, 256), 256, 0, fl[b].p, pos[b].p, nx,
+                 lists[b].p);
+      if (in.x_lo)
+        D3G_LAUNCH(X, add_offset_kernel, grid_for(cnt[b], 256), 256, 0, lists[b].p, cnt[b],
+                   (uint32_t)in.x_lo);
+    }
+  }
+  out.inner = X.scalar(tot.p);
   DBuf<Tally> t = X.zeros<Tally>(1);
   const uint64_t* rp = in.r_ptr;
-  if (n_small) {
-    unsigned g = (unsigned)std::min<uint64_t>((n_small + 7) / 8, (uint64_t)X.sm_count * 16);
-    if (mode == kModeCount)
-      D3G_LAUNCH(X, sparse_small_kernel<kModeCount>, g, 256, 0, xs.p, n_small, rp, in.r_col,
-                 in.sp_ptr, in.sp_col, in.sparse_ids, dec, em, t.p);
-    else if (mode == kModeChecksum)
-      D3G_LAUNCH(X, sparse_small_kernel<kModeChecksum>, g, 256, 0, xs.p, n_small, rp, in.r_col,
-                 in.sp_ptr, in.sp_col, in.sparse_ids, dec, em, t.p);
-    else
-      D3G_LAUNCH(X, sparse_small_kernel<kModeEmit>, g, 256, 0, xs.p, n_small, rp, in.r_col,
-                 in.sp_ptr, in.sp_col, in.sparse_ids, dec, em, t.p);
+  if (cnt[0]) {
+    unsigned g = (unsigned)std::min<uint64_t>((cnt[0] + 7) / 8, (uint64_t)X.sm_count * 16);
+    with_mode(mode, [&](auto M) {
+      D3G_LAUNCH(X, sparse_small_kernel<M()>, g, 256, 0, lists[0].p, cnt[0], rp, in.r_col,
+                 in.sp_ptr, in.sp_col, in.sparse_ids, dec, em, t.p, flt);
+    });
   }
-  if (n_large) {
-    uint32_t n_words = (uint32_t)((in.n_sparse + 31) / 32);
+  if (cnt[1] && bitset_tier) {
+    DBuf<uint32_t> rows = X.zeros<uint32_t>(in.y_card * n_words);
+    D3G_LAUNCH(X, sparse_rowbits_build_kernel, grid_for(in.y_card * 32, 256), 256, 0, in.sp_ptr,
+               in.sp_col, in.y_card, n_words, rows.p);
+    unsigned g = (unsigned)std::min<uint64_t>((cnt[1] + 7) / 8, (uint64_t)X.sm_count * 16);
+    with_mode(mode, [&](auto M) {
+      int wpl = (int)((n_words + 31) / 32);
+      if (wpl <= 1)
+        D3G_LAUNCH(X, (sparse_bitset_kernel<M(), 1>), g, 256, 0, lists[1].p, cnt[1], rp, in.r_col,
+                   in.sp_ptr, rows.p, n_words, in.sparse_ids, dec, em, t.p);
+      else if (wpl <= 2)
+        D3G_LAUNCH(X, (sparse_bitset_kernel<M(), 2>), g, 256, 0, lists[1].p, cnt[1], rp, in.r_col,
+                   in.sp_ptr, rows.p, n_words, in.sparse_ids, dec, em, t.p);
+      else if (wpl <= 4)
+        D3G_LAUNCH(X, (sparse_bitset_kernel<M(), 4>), g, 256, 0, lists[1].p, cnt[1], rp, in.r_col,
+                   in.sp_ptr, rows.p, n_words, in.sparse_ids, dec, em, t.p);
+      else
+        D3G_LAUNCH(X, (sparse_bitset_kernel<M(), 8>), g, 256, 0, lists[1].p, cnt[1], rp, in.r_col,
+                   in.sp_ptr, rows.p, n_words, in.sparse_ids, dec, em, t.p);
+    });
+  } else if (cnt[1]) {
+    unsigned g = (unsigned)std::min<uint64_t>((cnt[1] + kHashWarps - 1) / kHashWarps,
+                                              (uint64_t)X.sm_count * 14);
+    with_mode(mode, [&](auto M) {
+      D3G_LAUNCH(X, sparse_hash_kernel<M()>, g, kHashWarps * 32, 0, lists[1].p, cnt[1], rp,
+                 in.r_col, in.sp_ptr, in.sp_col, in.sparse_ids, dec, em, t.p, flt);
+    });
+  }
+  if (cnt[2]) {
     size_t smem = (size_t)n_words * 4;
     bool use_smem = smem <= (size_t)dense_smem_bytes(X);
-    unsigned g = (unsigned)std::min<uint64_t>(n_large, (uint64_t)X.sm_count * (use_smem && smem <= 48 * 1024 ? 4 : 1));
+    unsigned g = (unsigned)std::min<uint64_t>(cnt[2], (uint64_t)X.sm_count *
+                                                         (use_smem && smem <= 48 * 1024 ? 4 : 1));
     DBuf<uint32_t> gbm = X.alloc<uint32_t>(use_smem ? 1 : (uint64_t)g * n_words);
-#define D3G_SPARSE_LARGE(MODE, GLOBAL)                                                     \
-  do {                                                                                     \
-    auto kfn = sparse_large_kernel<MODE, GLOBAL>;                                          \
-    size_t sm = GLOBAL ? 0 : smem;                                                         \
-    if (sm > 48 * 1024)                                                                    \
-      D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
-    D3G_LAUNCH(X, kfn, g, 512, sm, xl.p, n_large, cx.p, in.x_lo, rp, in.r_col, in.sp_ptr, in.sp_col, \
-               in.sparse_ids, n_words, gbm.p, dec, em, t.p);                               \
-  } while (0)
-    if (use_smem) {
-      if (mode == kModeCount) D3G_SPARSE_LARGE(kModeCount, false);
-      else if (mode == kModeChecksum) D3G_SPARSE_LARGE(kModeChecksum, false);
-      else D3G_SPARSE_LARGE(kModeEmit, false);
-    } else {
-      if (mode == kModeCount) D3G_SPARSE_LARGE(kModeCount, true);
-      else if (mode == kModeChecksum) D3G_SPARSE_LARGE(kModeChecksum, true);
-      else D3G_SPARSE_LARGE(kModeEmit, true);
-    }
-#undef D3G_SPARSE_LARGE
+    with_mode(mode, [&](auto M) {
+      if (use_smem) {
+        auto kfn = sparse_large_kernel<M(), false>;
+        if (smem > 48 * 1024)
+          D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        D3G_LAUNCH(X, kfn, g, 512, smem, lists[2].p, cnt[2], cx.p, in.x_lo, rp, in.r_col,
+                   in.sp_ptr, in.sp_col, in.sparse_ids, n_words, gbm.p, dec, em, t.p, flt);
+      } else {
+        auto kfn = sparse_large_kernel<M(), true>;
+        D3G_LAUNCH(X, kfn, g, 512, 0, lists[2].p, cnt[2], cx.p, in.x_lo, rp, in.r_col, in.sp_ptr,
+                   in.sp_col, in.sparse_ids, n_words, gbm.p, dec, em, t.p, flt);
+      }
+    });
   }
   Tally h;
   X.to_host(&h, t.p, 1);
@@ -274,12 +332,18 @@ struct DenseInputs {
   uint64_t n_dense;
   uint64_t max_group_nnz;  // sum of the 128 largest m_x (group 0)
   uint64_t pos_lo, pos_hi; // x positions (in xorder) handled
+  const uint32_t* y_of_rank;
+  const uint32_t* dR;      // R-side degree per y code
+  uint64_t x_card;
+  uint64_t x_lo, x_hi;     // x code range of the cold residual pass
 };
 
-void run_dense(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g::Emit em,
-               KernelOut& out) {
+// DenseEC driver: the z-tile-resident kernel (dense_ec_tile_kernel) when the
+// group's cold entries and the longest dense list fit in shared memory, the
+// list-streaming kernel (dense_ec_kernel) otherwise.
+void run_dense_streaming(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g::Emit em,
+                         KernelOut& out) {
   using namespace d3g;
-  if (in.n_dense == 0 || in.pos_hi <= in.pos_lo) return;
   DenseParams p{};
   p.xorder = in.xorder + in.pos_lo;
   p.n_live = in.pos_hi - in.pos_lo;
@@ -306,21 +370,273 @@ void run_dense(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g::Em
   p.z_hi = in.n_dense;
   DBuf<Tally> t = X.zeros<Tally>(1);
   size_t sm = (size_t)std::max<uint64_t>(y_hot, 1) * 16;
-#define D3G_DENSE(MODE)                                                                    \
-  do {                                                                                     \
-    auto kfn = dense_ec_kernel<MODE>;                                                      \
-    D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
-    D3G_LAUNCH(X, kfn, g, kDenseThreads, sm, p, dec, em, t.p);                             \
-  } while (0)
-  if (mode == kModeCount) D3G_DENSE(kModeCount);
-  else if (mode == kModeChecksum) D3G_DENSE(kModeChecksum);
-  else D3G_DENSE(kModeEmit);
-#undef D3G_DENSE
+  with_mode(mode, [&](auto M) {
+    auto kfn = dense_ec_kernel<M()>;
+    D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    D3G_LAUNCH(X, kfn, g, kDenseThreads, sm, p, dec, em, t.p);
+  });
   Tally h;
   X.to_host(&h, t.p, 1);
   out.count = h.count;
   out.sum = h.sum;
   out.xr = h.xr;
+}
+
+void run_dense_tiles(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g::Emit em,
+                     KernelOut& out) {
+  using namespace d3g;
+  if (in.n_dense == 0 || in.pos_hi <= in.pos_lo) return;
+  const uint64_t n_live = in.pos_hi - in.pos_lo;
+  const uint32_t groups = (uint32_t)((n_live + 127) / 128);
+  const uint32_t* xorder = in.xorder + in.pos_lo;
+  // cold-entry bound per group for each candidate hot size
+  DBuf<unsigned int> mc = X.zeros<unsigned int>(kHotCandidates);
+  D3G_LAUNCH(X, dense_cold_count_kernel, std::min<uint32_t>(groups, X.sm_count * 16), 128, 0,
+             xorder, n_live, in.r_ptr, in.r_col, in.y_rank, mc.p);
+  unsigned int maxcold[kHotCandidates];
+  X.to_host(maxcold, mc.p, kHotCandidates);
+  std::vector<uint64_t> hp(in.n_dense + 1);
+  X.to_host(hp.data(), in.dl_ptr, in.n_dense + 1);
+  uint64_t max_len = 0;
+  for (uint64_t i = 0; i < in.n_dense; ++i) max_len = std::max(max_len, hp[i + 1] - hp[i]);
+  const uint64_t budget = (uint64_t)dense_smem_bytes(X);
+  static const uint32_t cand[kHotCandidates] = {16384, 8192, 4096, 2048, 1024, 512};
+  int pick = -1;
+  uint32_t hot = 0, ccap = 0, list_cap = 0, row_cap = 0;
+  for (int j = 0; j < kHotCandidates; ++j) {
+    uint32_t h = (uint32_t)std::min<uint64_t>(cand[j], in.y_card);
+    uint64_t cold = h < in.y_card ? maxcold[j] : 0;
+    uint64_t cc = 64;
+    while (cc < 2 * cold) cc <<= 1;
+    uint64_t fixed = (uint64_t)h * 16 + cc * 20;
+    if (fixed + 64 * 1024 > budget) continue;
+    uint64_t rest = budget - fixed;
+    // 3/4 of the rest for list entries, 1/4 for row pointers
+    uint64_t lc = (rest * 3 / 4) / 4, rc = (rest / 4) / 4 - 1;
+    if (lc < max_len) continue;
+    pick = j;
+    hot = h;
+    ccap = (uint32_t)cc;
+    list_cap = (uint32_t)lc;
+    row_cap = (uint32_t)rc;
+    break;
+  }
+  if (pick < 0) {
+    run_dense_streaming(X, in, dec, mode, em, out);
+    return;
+  }
+  // greedy z tiles: <= row_cap rows and <= list_cap entries each
+  std::vector<uint32_t> tb{0};
+  {
+    uint64_t r = 0;
+    while (r < in.n_dense) {
+      uint64_t e = r;
+      while (e < in.n_dense && e - r < row_cap && hp[e + 1] - hp[r] <= list_cap) ++e;
+      tb.push_back((uint32_t)e);
+      r = e;
+    }
+  }
+  const uint32_t n_tiles = (uint32_t)(tb.size() - 1);
+  const uint32_t want_units = (uint32_t)X.sm_count * 6;
+  uint32_t x_splits = std::max<uint32_t>(1, std::min<uint32_t>(groups, (want_units + n_tiles - 1) / n_tiles));
+  DBuf<uint32_t> dtb = X.alloc<uint32_t>(tb.size());
+  X.to_device(dtb.p, tb.data(), tb.size());
+  DBuf<unsigned int> work = X.zeros<unsigned int>(1);
+  DenseTileParams p{};
+  p.xorder = xorder;
+  p.n_live = n_live;
+  p.r_ptr = in.r_ptr;
+  p.r_col = in.r_col;
+  p.y_rank = in.y_rank;
+  p.dl_ptr = in.dl_ptr;
+  p.dl_col = in.dl_col;
+  p.dl_z = in.dl_z;
+  p.tile_begin = dtb.p;
+  p.n_tiles = n_tiles;
+  p.x_splits = x_splits;
+  p.groups = groups;
+  p.hot = hot;
+  p.cold_cap = ccap;
+  p.list_cap = list_cap;
+  p.row_cap = row_cap;
+  p.work = work.p;
+  size_t sm = (size_t)hot * 16 + (size_t)ccap * 20 + (size_t)(row_cap + 1) * 4 + (size_t)list_cap * 4;
+  DBuf<Tally> t = X.zeros<Tally>(1);
+  unsigned g = (unsigned)std::min<uint64_t>((uint64_t)n_tiles * x_splits, (uint64_t)X.sm_count);
+  with_mode(mode, [&](auto M) {
+    auto kfn = dense_ec_tile_kernel<M()>;
+    D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    D3G_LAUNCH(X, kfn, g, kD2Threads, sm, p, dec, em, t.p);
+  });
+  Tally h;
+  X.to_host(&h, t.p, 1);
+  out.count = h.count;
+  out.sum = h.sum;
+  out.xr = h.xr;
+}
+
+// ---------------------------------------------------------------------------
+// DenseEC v3 driver (denseec_hot.cuh): hot bit-sliced pass + cold residual
+// join. K is chosen from the measured rank histogram so that the cold join
+// stays small relative to the pair tests.
+constexpr int kKCand = 5;
+__constant__ uint32_t kKValues[kKCand] = {64, 128, 256, 512, 1024};
+
+__global__ void k_estimate_kernel(const uint32_t* __restrict__ y_of_rank,
+                                  const uint32_t* __restrict__ dR,
+                                  const uint32_t* __restrict__ cnt_rank, uint64_t y_card,
+                                  unsigned long long* __restrict__ out /* [2][kKCand] */) {
+  uint64_t cold[kKCand] = {}, hot[kKCand] = {};
+  for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < y_card;
+       r += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t c = cnt_rank[r];
+    if (!c) continue;
+    uint64_t prod = (uint64_t)dR[y_of_rank[r]] * c;
+#pragma unroll
+    for (int j = 0; j < kKCand; ++j) {
+      if (r >= kKValues[j]) cold[j] += prod;
+      else hot[j] += c;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kKCand; ++j) {
+    uint64_t a = d3g::warp_sum(cold[j]), b = d3g::warp_sum(hot[j]);
+    if (d3g::lane_id() == 0) {
+      if (a) atomicAdd(&out[j], (unsigned long long)a);
+      if (b) atomicAdd(&out[kKCand + j], (unsigned long long)b);
+    }
+  }
+}
+
+void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g::Emit em,
+                   KernelOut& out) {
+  using namespace d3g;
+  if (in.n_dense == 0 || in.pos_hi <= in.pos_lo) return;
+  const uint64_t n_live = in.pos_hi - in.pos_lo;
+  const uint32_t* xorder = in.xorder + in.pos_lo;
+  const uint32_t groups = (uint32_t)((n_live + 127) / 128);
+  const uint64_t D = in.n_dense, Y = in.y_card;
+  const uint64_t dnnz = X.scalar(in.dl_ptr + D);
+  // choose K
+  DBuf<uint32_t> cnt_rank = X.zeros<uint32_t>(Y);
+  if (dnnz) D3G_LAUNCH(X, value_hist_kernel, grid_for(dnnz, 256), 256, 0, in.dl_col, dnnz, cnt_rank.p, (uint32_t)Y);
+  DBuf<unsigned long long> est = X.zeros<unsigned long long>(2 * kKCand);
+  D3G_LAUNCH(X, k_estimate_kernel, grid_for(Y, 256), 256, 0, in.y_of_rank, in.dR, cnt_rank.p, Y, est.p);
+  unsigned long long e[2 * kKCand];
+  X.to_host(e, est.p, 2 * kKCand);
+  static const uint32_t kv[kKCand] = {64, 128, 256, 512, 1024};
+  // K is bounded by the shared-memory slice of a 32-group batch (K * 512 B)
+  const uint64_t budget = (uint64_t)dense_smem_bytes(X) - 1024;
+  const uint32_t k_cap = (uint32_t)std::min<uint64_t>(1024, budget / 512 / 64 * 64);
+  const double units = (double)D * (double)((groups + 31) / 32);
+  int best = 0;
+  double best_cost = 1e300;
+  for (int j = 0; j < kKCand; ++j) {
+    if (kv[j] > k_cap) break;
+    double hot_per_z = (double)e[kKCand + j] / (double)D;
+    double cost = units * hot_per_z * 8.0 + 12.0 * (double)e[j] * ((double)n_live / std::max<uint64_t>(in.x_card, 1));
+    if (cost < best_cost) { best_cost = cost; best = j; }
+  }
+  uint32_t K = kv[best];
+  if (K * 2 <= k_cap && K == 256 && k_cap >= 384) K = 384;  // use the slack of the batch slice
+  // the warp-bitmap cold kernel carries 256-bit hot signatures: K = 256
+  const uint32_t d_words = (uint32_t)((D + 31) / 32);
+  const bool cold_kernel_ok = (uint64_t)d_words * 4 * kColdWarps <= budget && k_cap >= 256;
+  if (cold_kernel_ok) K = 256;
+  const uint32_t kw = (K + 63) / 64;
+  const uint32_t n_batches = (groups + 31) / 32;
+  // hot structures
+  DBuf<uint4> T = X.zeros<uint4>((uint64_t)n_batches * K * 32);
+  DBuf<unsigned long long> hx = X.zeros<unsigned long long>(in.x_card * kw);
+  DBuf<unsigned long long> hz = X.zeros<unsigned long long>(D * kw);
+  D3G_LAUNCH(X, hot_build_x_kernel, grid_for(n_live * 32, 256), 256, 0, xorder, n_live, in.r_ptr,
+             in.r_col, in.y_rank, K, kw, reinterpret_cast<uint32_t*>(T.p), hx.p);
+  D3G_LAUNCH(X, hot_build_z_kernel, grid_for(D * 32, 256), 256, 0, in.dl_ptr, in.dl_col, D, K, kw,
+             hz.p, (uint32_t*)nullptr);
+  // P1: hot bit-sliced pass
+  HotParams hp{};
+  hp.T = T.p;
+  hp.hz = reinterpret_cast<const uint64_t*>(hz.p);
+  hp.xorder = xorder;
+  hp.dl_z = in.dl_z;
+  hp.n_live = n_live;
+  hp.n_dense = D;
+  hp.groups = groups;
+  hp.K = K;
+  hp.kw = kw;
+  hp.batch = 32;
+  hp.z_chunks = std::max<uint32_t>(1, (uint32_t)std::min<uint64_t>(
+      (D + 255) / 256, ((uint64_t)X.sm_count * 8 + n_batches - 1) / n_batches));
+  DBuf<unsigned int> work = X.zeros<unsigned int>(1);
+  hp.work = work.p;
+  DBuf<Tally> t = X.zeros<Tally>(1);
+  size_t sm = (size_t)K * 32 * 16;
+  unsigned g = (unsigned)std::min<uint64_t>((uint64_t)n_batches * hp.z_chunks, (uint64_t)X.sm_count);
+  with_mode(mode, [&](auto M) {
+    auto kfn = dense_hot_kernel<decltype(M)::value>;
+    D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    D3G_LAUNCH(X, kfn, g, kHotThreads, sm, hp, in.dl_ptr, in.dl_col, dec, em, t.p);
+  });
+  Tally h;
+  X.to_host(&h, t.p, 1);
+  // P2: cold residual join (SparseBMM tiers, hot-hit candidates filtered)
+  KernelOut cold;
+  if (e[best] > 0) {
+    DBuf<uint32_t> cc = X.zeros<uint32_t>(Y);
+    D3G_LAUNCH(X, cold_count_kernel, grid_for(D * 32, 256), 256, 0, in.dl_ptr, in.dl_col, D, K,
+               in.y_of_rank, cc.p);
+    DBuf<uint64_t> cptr = X.alloc<uint64_t>(Y + 1);
+    exclusive_scan<uint32_t>(X, cc.p, Y, cptr.p);
+    const uint64_t cnnz = X.scalar(cptr.p + Y);
+    DBuf<uint32_t> ccol = X.alloc<uint32_t>(cnnz);
+    DBuf<unsigned long long> cur = X.alloc<unsigned long long>(Y + 1);
+    D3G_CUDA(cudaMemcpyAsync(cur.p, cptr.p, (Y + 1) * 8, cudaMemcpyDeviceToDevice, X.stream));
+    D3G_LAUNCH(X, cold_scatter_kernel, grid_for(D * 32, 256), 256, 0, in.dl_ptr, in.dl_col, D, K,
+               in.y_of_rank, cur.p, ccol.p);
+    if (cold_kernel_ok) {
+      DBuf<uint4> ch = X.alloc<uint4>(2 * cnnz);
+      if (cnnz)
+        D3G_LAUNCH(X, cold_sig_kernel, grid_for(cnnz, 256), 256, 0, ccol.p, cnnz,
+                   reinterpret_cast<const uint4*>(hz.p), ch.p);
+      DBuf<unsigned int> next = X.zeros<unsigned int>(1);
+      DBuf<Tally> tc = X.zeros<Tally>(1);
+      size_t csm = (size_t)d_words * 4 * kColdWarps;
+      with_mode(mode, [&](auto M) {
+        auto kfn = dense_cold_kernel<decltype(M)::value>;
+        D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
+        D3G_LAUNCH(X, kfn, (unsigned)X.sm_count, kColdWarps * 32, csm, xorder, n_live, in.r_ptr,
+                   in.r_col, cptr.p, ccol.p, ch.p, reinterpret_cast<const uint4*>(hx.p), d_words,
+                   in.dl_z, dec, em, next.p, tc.p);
+      });
+      Tally hc;
+      X.to_host(&hc, tc.p, 1);
+      cold.count = hc.count;
+      cold.sum = hc.sum;
+      cold.xr = hc.xr;
+    } else {
+      SparseInputs si{in.r_ptr, in.r_col, in.x_card, cptr.p, ccol.p, in.dl_z, D, Y, in.x_lo, in.x_hi};
+      Filter flt{reinterpret_cast<const uint64_t*>(hx.p), reinterpret_cast<const uint64_t*>(hz.p), kw};
+      run_sparse(X, si, dec, mode, em, cold, flt);
+    }
+  }
+  out.count = h.count + cold.count;
+  out.sum = h.sum + cold.sum;
+  out.xr = h.xr ^ cold.xr;
+  out.inner = K;  // reported as the hot width (diagnostics)
+}
+
+// DenseEC dispatch: v3 (hot + cold residual) by default; D3G_DENSE=v1|v2
+// selects the list-streaming or z-tile-resident kernels (kept for comparison).
+void run_dense(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g::Emit em,
+               KernelOut& out) {
+  const char* v = std::getenv("D3G_DENSE");
+  std::string which = v ? v : "v3";
+  if (which == "v1")
+    run_dense_streaming(X, in, dec, mode, em, out);
+  else if (which == "v2")
+    run_dense_tiles(X, in, dec, mode, em, out);
+  else
+    run_dense_hot(X, in, dec, mode, em, out);
 }
 
 __global__ void decode_pairs_kernel(const uint32_t* __restrict__ xc, const uint32_t* __restrict__ zc,
@@ -377,7 +693,7 @@ __global__ void map_through_kernel(uint32_t* __restrict__ v, uint64_t n,
 
 // Device layouts of the dense block consumed by dense_ec_kernel.
 struct DenseLayout {
-  DBuf<uint32_t> y_rank, dl_z, dl_col, xorder;
+  DBuf<uint32_t> y_rank, y_of_rank, dl_z, dl_col, xorder;
   DBuf<uint64_t> dl_ptr;
   uint64_t n_live = 0, n_dense = 0, max_group_nnz = 0;
 };
@@ -404,6 +720,7 @@ void build_dense_layout(Ctx& X, const d3g::DeviceCsr& rx, uint64_t max_mx,
     radix_sort(X, k.p, v.p, y_card, 32 + bits_for(max_dr));
     L.y_rank = X.alloc<uint32_t>(y_card);
     D3G_LAUNCH(X, scatter_rank_kernel, grid_for(y_card, 256), 256, 0, v.p, y_card, L.y_rank.p);
+    L.y_of_rank = std::move(v);
   }
   // dense rows ordered by m_z descending (uniform trip counts per warp)
   DBuf<uint32_t> rows = X.alloc<uint32_t>(n_dense);
@@ -472,6 +789,7 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   if (shard_index < 0 || shard_index >= shard_count) throw ConfigError("bad shard index");
   std::memset(rep, 0, sizeof(*rep));
   X.launches = 0;
+  X.d2h_bytes = 0;
   X.budget = o->memory_budget_bytes ? o->memory_budget_bytes : (3ull << 30);
   uint64_t base_live = X.live_bytes;
   X.peak_bytes = X.live_bytes;
@@ -750,14 +1068,15 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   // x shard (x code range for SparseBMM, position range for DenseEC)
   uint64_t x_lo = x_card * shard_index / shard_count, x_hi = x_card * (shard_index + 1) / shard_count;
   SparseInputs si{rx.row_ptr.p, rx.col.p, x_card, sp_ptr.p, sp_col.p, sparse_ids.p, n_sparse,
-                  x_lo, x_hi};
+                  y_card, x_lo, x_hi};
   KernelOut ks, kd;
   run_sparse(X, si, dec, mode, no_emit, ks);
   T.mark();  // 7
   uint64_t pos_lo = L.n_live * shard_index / shard_count,
            pos_hi = L.n_live * (shard_index + 1) / shard_count;
   DenseInputs di{L.xorder.p, L.n_live, rx.row_ptr.p, rx.col.p, L.y_rank.p, y_card, L.dl_ptr.p,
-                 L.dl_col.p, L.dl_z.p, L.n_dense, L.max_group_nnz, pos_lo, pos_hi};
+                 L.dl_col.p, L.dl_z.p, L.n_dense, L.max_group_nnz, pos_lo, pos_hi,
+                 L.y_of_rank.p, dR.p, x_card, x_lo, x_hi};
   run_dense(X, di, dec, mode, no_emit, kd);
   T.mark();  // 8
   rep->pairs_sparse = ks.count;
@@ -823,6 +1142,7 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   rep->ms_total = T.ms(0, 9);
   rep->peak_bytes = X.peak_bytes - base_live;
   rep->gpu_launches = X.launches;
+  rep->d2h_bytes += X.d2h_bytes;
 }
 
 }  // namespace
@@ -889,8 +1209,10 @@ int d3g_join_project(d3g_ctx* ctx, const d3g_table* r, const d3g_table* s, const
       join_project_impl(ctx->c, r, s, c, o, rep, pairs);
     } catch (...) {
       cudaStreamSynchronize(ctx->c.stream);
+      ctx->c.budget = 0;  // the memory budget is scoped to one call
       throw;
     }
+    ctx->c.budget = 0;
   });
 }
 
@@ -1001,8 +1323,8 @@ int d3g_sparse_bmm_csr(d3g_ctx* ctx, const d3g_csr* r_by_x, const d3g_csr* s_spa
     upload_csr(X, s_sparse_by_y, sp);
     DBuf<uint32_t> ids = X.alloc<uint32_t>(z_card);
     if (z_card) D3G_LAUNCH(X, iota_kernel, grid_for(z_card, 256), 256, 0, ids.p, (uint64_t)z_card);
-    SparseInputs si{r.row_ptr.p, r.col.p, r.n_rows, sp.row_ptr.p, sp.col.p, ids.p, z_card, 0,
-                    r.n_rows};
+    SparseInputs si{r.row_ptr.p, r.col.p, r.n_rows, sp.row_ptr.p, sp.col.p, ids.p, z_card,
+                    sp.n_rows, 0, r.n_rows};
     Decode dec{nullptr, nullptr, 0};
     Emit none{nullptr, nullptr, nullptr, 0};
     cudaEvent_t e0, e1;
@@ -1083,7 +1405,8 @@ int d3g_dense_ec_rows(d3g_ctx* ctx, const d3g_csr* r_by_x, const d3g_panel* pane
     build_dense_layout(X, r, max_mx, hmx, zptr.p, zcol.p, row_ids.p, rows, max_mz, zids.p, yc,
                        dR.p, L);
     DenseInputs di{L.xorder.p, L.n_live, r.row_ptr.p, r.col.p, L.y_rank.p, yc, L.dl_ptr.p,
-                   L.dl_col.p, L.dl_z.p, L.n_dense, L.max_group_nnz, 0, L.n_live};
+                   L.dl_col.p, L.dl_z.p, L.n_dense, L.max_group_nnz, 0, L.n_live,
+                   L.y_of_rank.p, dR.p, r.n_rows, 0, r.n_rows};
     Decode dec{nullptr, nullptr, 0};
     Emit none{nullptr, nullptr, nullptr, 0};
     cudaEvent_t e0, e1;
@@ -1147,3 +1470,54 @@ uint64_t d3g_cfg_rows(int cfg) { return d3g::cfg_rows(cfg); }
 int d3g_ctx_device(d3g_ctx* ctx) { return ctx ? ctx->c.device : -1; }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Measured integer-pipe peak for the DenseEC roofline: 3-input LOP3 chains,
+// 8 independent chains per thread, 148 x 4 CTAs of 256 threads. Returns
+// logic ops/s (one LOP3 = one 32-bit op).
+namespace {
+__global__ void __launch_bounds__(256) alu_peak_kernel(uint32_t seed, int iters, uint32_t* out) {
+  uint32_t a[8], b = seed * 0x9e3779b1u + threadIdx.x, c = seed ^ (blockIdx.x * 0x85ebca6bu);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) a[j] = threadIdx.x * (j + 1) + seed;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      uint32_t r;
+      asm volatile("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(r) : "r"(a[j]), "r"(b), "r"(c));
+      a[j] = r;
+      asm volatile("lop3.b32 %0, %1, %2, %3, 0xe8;" : "=r"(r) : "r"(a[j]), "r"(c), "r"(b));
+      a[j] = r;
+    }
+  }
+  uint32_t x = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) x ^= a[j];
+  if (x == 0x12345678u) out[0] = x;
+}
+}  // namespace
+
+extern "C" int d3g_alu_peak(d3g_ctx* ctx, double* ops_per_sec) {
+  return guarded([&] {
+    using namespace d3g;
+    Ctx& X = ctx->c;
+    D3G_CUDA(cudaSetDevice(X.device));
+    DBuf<uint32_t> out = X.zeros<uint32_t>(1);
+    const int iters = 4096;
+    const unsigned grid = (unsigned)X.sm_count * 8;
+    alu_peak_kernel<<<grid, 256, 0, X.stream>>>(1u, 64, out.p);  // warm-up
+    cudaEvent_t e0, e1;
+    D3G_CUDA(cudaEventCreate(&e0));
+    D3G_CUDA(cudaEventCreate(&e1));
+    D3G_CUDA(cudaEventRecord(e0, X.stream));
+    alu_peak_kernel<<<grid, 256, 0, X.stream>>>(2u, iters, out.p);
+    D3G_CUDA(cudaEventRecord(e1, X.stream));
+    X.sync();
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    double ops = (double)grid * 256.0 * iters * 16.0;
+    *ops_per_sec = ops / (ms * 1e-3);
+  });
+}

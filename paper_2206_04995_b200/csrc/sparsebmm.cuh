@@ -37,6 +37,23 @@ struct Emit {
 
 enum : int { kModeCount = 0, kModeChecksum = 1, kModeEmit = 2 };
 
+// Optional candidate filter used by DenseEC's cold residual pass: a candidate
+// (x, zi) is skipped when the hot masks of x and of dense row zi intersect
+// (that pair was already produced by the hot bit-sliced pass).
+struct Filter {
+  const uint64_t* hx;  // [x code][kw]
+  const uint64_t* hz;  // [compact index][kw]
+  uint32_t kw;
+  __device__ __forceinline__ bool skip(uint32_t x, uint32_t zi) const {
+    if (hz == nullptr) return false;
+    const uint64_t* a = hx + (uint64_t)x * kw;
+    const uint64_t* b = hz + (uint64_t)zi * kw;
+    for (uint32_t w = 0; w < kw; ++w)
+      if (a[w] & b[w]) return true;
+    return false;
+  }
+};
+
 // Warp-aggregated append of (xc, zc) for lanes with `pred`.
 __device__ __forceinline__ void emit_pair(const Emit& e, bool pred, uint32_t xc, uint32_t zc) {
   uint32_t m = __ballot_sync(__activemask(), pred);
@@ -104,7 +121,8 @@ __global__ void __launch_bounds__(256)
 sparse_small_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
                     const uint64_t* __restrict__ r_ptr, const uint32_t* __restrict__ r_col,
                     const uint64_t* __restrict__ sp_ptr, const uint32_t* __restrict__ sp_col,
-                    const uint32_t* __restrict__ sparse_ids, Decode dec, Emit em, Tally* tally) {
+                    const uint32_t* __restrict__ sparse_ids, Decode dec, Emit em, Tally* tally,
+                    Filter flt) {
   __shared__ uint32_t buf[8][32];
   const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
   uint64_t cnt = 0, sum = 0, xr = 0;
@@ -136,9 +154,10 @@ sparse_small_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
     __syncwarp();
     uint32_t v = lane < nc ? buf[w][lane] : 0xffffffffu;
     __syncwarp();
+    if (v != 0xffffffffu && flt.skip(x, v)) v = 0xffffffffu;
     v = bitonic32(v);
     uint32_t prev = __shfl_up_sync(0xffffffffu, v, 1);
-    bool fresh = lane < nc && (lane == 0 || v != prev);
+    bool fresh = v != 0xffffffffu && (lane == 0 || v != prev);
     cnt += fresh;
     if (kMode == kModeChecksum && fresh) {
       uint64_t h = dec.hash(x, sparse_ids[v]);
@@ -146,6 +165,129 @@ sparse_small_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
       xr ^= h;
     }
     if (kMode == kModeEmit) emit_pair(em, fresh, x, fresh ? sparse_ids[v] : 0);
+  }
+  tally_flush(tally, cnt, sum, xr);
+}
+
+// ---------------------------------------------------------------------------
+// Warp-private shared-memory hash set, one warp per x with 32 < c_x <= cap/2.
+constexpr int kHashWarps = 4;
+constexpr uint32_t kHashCap = 2048;  // u32 slots per warp (8 KB)
+constexpr uint32_t kHashEmpty = 0xffffffffu;
+
+template <int kMode>
+__global__ void __launch_bounds__(kHashWarps * 32)
+sparse_hash_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
+                   const uint64_t* __restrict__ r_ptr, const uint32_t* __restrict__ r_col,
+                   const uint64_t* __restrict__ sp_ptr, const uint32_t* __restrict__ sp_col,
+                   const uint32_t* __restrict__ sparse_ids, Decode dec, Emit em, Tally* tally,
+                   Filter flt) {
+  __shared__ uint32_t table[kHashWarps][kHashCap];
+  const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
+  uint32_t* t = table[w];
+  for (uint32_t i = lane; i < kHashCap; i += 32) t[i] = kHashEmpty;
+  __syncwarp();
+  uint64_t cnt = 0, sum = 0, xr = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * kHashWarps + w; i < n_x; i += (uint64_t)gridDim.x * kHashWarps) {
+    uint32_t x = xs[i];
+    for (uint64_t k = r_ptr[x]; k < r_ptr[x + 1]; ++k) {
+      uint32_t y = r_col[k];
+      uint64_t s0 = sp_ptr[y], s1 = sp_ptr[y + 1];
+      for (uint64_t base = s0; base < s1; base += 32) {
+        uint64_t q = base + lane;
+        bool fresh = false;
+        uint32_t zi = 0;
+        if (q < s1 && !flt.skip(x, sp_col[q])) {
+          zi = sp_col[q];
+          uint32_t s = (zi * 0x9e3779b1u) >> 21;  // 11 bits -> [0, 2048)
+          for (;;) {
+            uint32_t prev = atomicCAS(&t[s], kHashEmpty, zi);
+            if (prev == kHashEmpty) { fresh = true; break; }
+            if (prev == zi) break;
+            s = (s + 1) & (kHashCap - 1);
+          }
+        }
+        cnt += fresh;
+        if (kMode == kModeChecksum && fresh) {
+          uint64_t h = dec.hash(x, sparse_ids[zi]);
+          sum += h;
+          xr ^= h;
+        }
+        if (kMode == kModeEmit) emit_pair(em, fresh, x, fresh ? sparse_ids[zi] : 0);
+      }
+    }
+    __syncwarp();
+    for (uint32_t j = lane; j < kHashCap; j += 32) t[j] = kHashEmpty;
+    __syncwarp();
+  }
+  tally_flush(tally, cnt, sum, xr);
+}
+
+// ---------------------------------------------------------------------------
+// Bitset-row tier for a small sparse side (n_sparse <= 32 * 32 * kBitsetMaxWords
+// bits): S_sp rows are kept as bitsets over the compact sparse index; one warp
+// per x ORs the rows of its y in registers (lane l owns words l, l+32, ...)
+// and pop-counts. No atomics, no dedup structure.
+constexpr int kBitsetMaxWordsPerLane = 8;  // 8192 sparse z
+
+__global__ void sparse_rowbits_build_kernel(const uint64_t* __restrict__ sp_ptr,
+                                            const uint32_t* __restrict__ sp_col, uint64_t y_card,
+                                            uint32_t n_words, uint32_t* __restrict__ rows) {
+  for (uint64_t y = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); y < y_card;
+       y += (uint64_t)gridDim.x * (blockDim.x / 32))
+    for (uint64_t k = sp_ptr[y] + lane_id(); k < sp_ptr[y + 1]; k += 32) {
+      uint32_t zi = sp_col[k];
+      atomicOr(&rows[y * n_words + (zi >> 5)], 1u << (zi & 31));
+    }
+}
+
+template <int kMode, int kWPL>
+__global__ void __launch_bounds__(256)
+sparse_bitset_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
+                     const uint64_t* __restrict__ r_ptr, const uint32_t* __restrict__ r_col,
+                     const uint64_t* __restrict__ sp_ptr, const uint32_t* __restrict__ rows,
+                     uint32_t n_words, const uint32_t* __restrict__ sparse_ids, Decode dec, Emit em,
+                     Tally* tally) {
+  const uint32_t lane = lane_id(), w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  uint64_t cnt = 0, sum = 0, xr = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * nw + w; i < n_x; i += (uint64_t)gridDim.x * nw) {
+    uint32_t x = xs[i];
+    uint32_t acc[kWPL];
+#pragma unroll
+    for (int j = 0; j < kWPL; ++j) acc[j] = 0;
+    for (uint64_t k = r_ptr[x]; k < r_ptr[x + 1]; ++k) {
+      uint32_t y = r_col[k];
+      if (sp_ptr[y + 1] == sp_ptr[y]) continue;
+      const uint32_t* row = rows + (uint64_t)y * n_words;
+#pragma unroll
+      for (int j = 0; j < kWPL; ++j) {
+        uint32_t wi = lane + 32 * j;
+        if (wi < n_words) acc[j] |= __ldg(row + wi);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kWPL; ++j) {
+      cnt += __popc(acc[j]);
+      if (kMode != kModeCount) {
+        uint32_t bits = acc[j];
+        while (bits) {
+          int b = __ffs(bits) - 1;
+          bits &= bits - 1;
+          uint32_t zc = sparse_ids[(lane + 32 * j) * 32 + b];
+          if (kMode == kModeChecksum) {
+            uint64_t h = dec.hash(x, zc);
+            sum += h;
+            xr ^= h;
+          } else {
+            unsigned long long idx = atomicAdd(em.cursor, 1ull);
+            if (idx < em.cap) {
+              em.x[idx] = x;
+              em.z[idx] = zc;
+            }
+          }
+        }
+      }
+    }
   }
   tally_flush(tally, cnt, sum, xr);
 }
@@ -158,7 +300,7 @@ sparse_large_kernel(const uint32_t* __restrict__ xs, uint64_t n_x, const uint64_
                     uint64_t cx_base, const uint64_t* __restrict__ r_ptr, const uint32_t* __restrict__ r_col,
                     const uint64_t* __restrict__ sp_ptr, const uint32_t* __restrict__ sp_col,
                     const uint32_t* __restrict__ sparse_ids, uint32_t n_words, uint32_t* gbm,
-                    Decode dec, Emit em, Tally* tally) {
+                    Decode dec, Emit em, Tally* tally, Filter flt) {
   extern __shared__ uint32_t smem_bm[];
   uint32_t* bm = kGlobalBitmap ? gbm + (uint64_t)blockIdx.x * n_words : smem_bm;
   for (uint32_t i = threadIdx.x; i < n_words; i += blockDim.x) bm[i] = 0;
@@ -174,7 +316,7 @@ sparse_large_kernel(const uint32_t* __restrict__ xs, uint64_t n_x, const uint64_
            t += blockDim.x) {
         bool fresh = false;
         uint32_t zi = 0;
-        if (t < s1) {
+        if (t < s1 && !flt.skip(x, sp_col[t])) {
           zi = sp_col[t];
           uint32_t bit = 1u << (zi & 31);
           uint32_t old = atomicOr(&bm[zi >> 5], bit);

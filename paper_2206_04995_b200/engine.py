@@ -246,7 +246,7 @@ class _KStats(C.Structure):
 EXPORTED = ["d3g_ctx_create", "d3g_ctx_destroy", "d3g_last_error", "d3g_version",
             "d3g_opts_default", "d3g_join_project", "d3g_build_csr", "d3g_sparse_bmm_csr",
             "d3g_dense_ec_rows", "d3g_generate", "d3g_cfg_rows", "d3g_ctx_device",
-            "d3g_f3_threshold", "d3g_f1", "d3g_f2_decide"]
+            "d3g_f3_threshold", "d3g_f1", "d3g_f2_decide", "d3g_alu_peak"]
 
 _lib = None
 
@@ -279,6 +279,7 @@ def lib():
         L.d3g_cfg_rows.argtypes = [C.c_int]
         L.d3g_cfg_rows.restype = C.c_uint64
         L.d3g_ctx_device.argtypes = [C.c_void_p]
+        L.d3g_alu_peak.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
         L.d3g_f3_threshold.argtypes = [C.c_uint32, C.c_uint32, C.POINTER(_Consts)]
         L.d3g_f3_threshold.restype = C.c_uint32
         L.d3g_f1.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.POINTER(_Consts)]
@@ -643,6 +644,14 @@ def generate(cfg: int, side: int, lo: int = 0, hi: int | None = None, device=Non
     _check(lib().d3g_generate(ctx.handle, cfg, side, lo, hi, C.c_void_p(left.data_ptr()),
                               C.c_void_p(right.data_ptr())))
     return left, right
+
+
+def alu_peak(ctx: Context | None = None) -> float:
+    """Measured 32-bit logic ops/s of the device (DenseEC roofline denominator)."""
+    ctx = ctx or default_context()
+    v = C.c_double()
+    _check(lib().d3g_alu_peak(ctx.handle, C.byref(v)))
+    return v.value
 
 
 def cfg_rows(cfg: int) -> int:

@@ -109,3 +109,32 @@ def test_natural_key_fallback_and_errors():
     with pytest.raises(d3.ResourceError):
         d3.join_project(d3.RawTable(*r), d3.RawTable(*s),
                         d3.EngineConfig(force=d3.Strategy.hybrid, memory_budget_bytes=1024), C)
+
+
+def _golden():
+    import json
+    import os
+    return json.load(open(os.path.join(os.path.dirname(__file__), "golden", "golden.json")))
+
+
+@pytest.mark.parametrize("cfg", [2, 3, 4])
+def test_baseline_config_matches_reference(cfg):
+    """Full BASELINE configs: count and (sum, xor) fingerprint of the distinct
+    (x, z) set equal the reference's (tests/golden/golden.json), plus the
+    dense/sparse split and exact OUT_J."""
+    g = _golden().get(f"cfg{cfg}")
+    if g is None:
+        pytest.skip("golden entry not generated")
+    rl, rr = d3.generate(cfg, 0)
+    sl, sr = d3.generate(cfg, 1)
+    out = d3.join_project(d3.RawTable(rl, rr), d3.RawTable(sl, sr),
+                          d3.EngineConfig(force=d3.Strategy.auto_select, count_only=True,
+                                          checksum=True, memory_budget_bytes=64 << 30), C)
+    rep = out.report
+    assert rep.out_p == g["set"]["count"]
+    assert rep.checksum_sum == g["set"]["sum"]
+    assert rep.checksum_xor == g["set"]["xor"]
+    p = g["pipeline"]
+    for k in ("x_card", "y_card", "z_card", "r_nnz", "s_nnz", "out_j", "dense_z", "sparse_z",
+              "sparse_nnz", "dropped_r"):
+        assert getattr(rep, k) == p[k], k
