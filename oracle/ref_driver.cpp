@@ -221,8 +221,11 @@ int ref_pipeline(const std::uint64_t* rl, const std::uint64_t* rr,
                  const RefConsts* consts, RefPipeline* out,
                  std::uint64_t* dense_z_raw, std::uint64_t dense_cap) {
   try {
-    dim3::RawTable R = to_table(rl, rr, nr);
-    dim3::RawTable S = to_table(sl, sr, ns);
+    dim3::RawTable R0 = to_table(rl, rr, nr);
+    dim3::RawTable S0 = to_table(sl, sr, ns);
+    const bool swapped = dim3::engine_will_swap(R0, S0);  // engine.cpp:361-366
+    const dim3::RawTable& R = swapped ? S0 : R0;
+    const dim3::RawTable& S = swapped ? R0 : S0;
     dim3::MappingOutput m = map_like_engine(R, S);
     dim3::CsrMatrix r_by_x = dim3::build_csr(m.r, true);
     dim3::CsrMatrix s_by_z = dim3::build_csr(m.s, true);
