@@ -299,13 +299,22 @@ def main():
     cand = {"map+csr+partition": prep_ms, "sparse_bmm": phase["ms_sparse"],
             "dense_ec": phase["ms_dense"]}
     dom = max(cand, key=cand.get)
-    if dom == "dense_ec" and w_dense:
-        achieved = w_dense / (phase["ms_dense"] * 1e-3)
-        roof = {"kernel": "dense_ec", "bound": "int_alu", "achieved": achieved / 1e12,
-                "peak": alu / 1e12, "unit": "Tops/s", "frac": achieved / alu, "traffic": None,
-                "work": f"W_D = 8*blocks_checked + probes_done of the reference's early-exit "
-                        f"DenseEC on this input = {w_dense:.4g} 32-bit word-ops",
+    p_dense = r0.x_live * r0.dense_z  # pair tests: one existence answer per (live x, dense z)
+    if dom == "dense_ec":
+        achieved = p_dense / (phase["ms_dense"] * 1e-3)
+        roof = {"kernel": "dense_ec (hot bit-sliced pass + cold residual pass)", "bound": "int_alu",
+                "achieved": achieved / 1e12, "peak": alu / 1e12, "unit": "Tops/s",
+                "frac": achieved / alu, "traffic": None,
+                "work": f"P_D = X_live * Z_dense = {p_dense:.4g} pair tests, counted as ONE 32-bit "
+                        f"op each (SURVEY 8(d) lower-bound unit)",
                 "peak_source": "measured LOP3 throughput (d3g_alu_peak) in this run"}
+        if w_dense:
+            roof["reference_equivalent"] = {
+                "work": f"W_D = 8*blocks_checked + probes_done of the reference's early-exit "
+                        f"DenseEC on this input = {w_dense:.4g} word-ops",
+                "achieved_Tops": w_dense / (phase["ms_dense"] * 1e-3) / 1e12,
+                "note": "exceeds the ALU peak because the bit-sliced kernel answers 128 pair "
+                        "tests per 32-bit op; not a utilisation figure"}
     elif dom == "sparse_bmm":
         achieved = b_sparse / (phase["ms_sparse"] * 1e-3) / 1e9
         roof = {"kernel": "sparse_bmm", "bound": "hbm", "achieved": achieved, "peak": hbm,
@@ -323,8 +332,8 @@ def main():
         "sparse_bmm": {"ms": phase["ms_sparse"],
                        "GB/s": b_sparse / (phase["ms_sparse"] * 1e-3) / 1e9 if phase["ms_sparse"] else None},
         "dense_ec": {"ms": phase["ms_dense"],
-                     "Tops/s": (w_dense / (phase["ms_dense"] * 1e-3) / 1e12)
-                     if (w_dense and phase["ms_dense"]) else None},
+                     "pair_tests_per_s": (p_dense / (phase["ms_dense"] * 1e-3))
+                     if phase["ms_dense"] else None},
     }
 
     # ---- e2e through the C ABI from pinned host buffers -------------------

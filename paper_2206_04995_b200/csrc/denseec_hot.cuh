@@ -81,26 +81,32 @@ __global__ void hot_build_z_kernel(const uint64_t* __restrict__ dl_ptr,
 // cold rank (y-major CSR, rows indexed by y code).
 __global__ void cold_count_kernel(const uint64_t* __restrict__ dl_ptr,
                                   const uint32_t* __restrict__ dl_col, uint64_t n_dense, uint32_t K,
-                                  const uint32_t* __restrict__ y_of_rank, uint32_t* __restrict__ cnt) {
+                                  const uint32_t* __restrict__ y_of_rank, uint32_t* __restrict__ cnt,
+                                  uint64_t y_card, uint32_t part_rows) {
   for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < n_dense;
-       i += (uint64_t)gridDim.x * (blockDim.x / 32))
+       i += (uint64_t)gridDim.x * (blockDim.x / 32)) {
+    const uint64_t base = (i / part_rows) * y_card;
     for (uint64_t k = dl_ptr[i] + lane_id(); k < dl_ptr[i + 1]; k += 32) {
       uint32_t r = dl_col[k];
-      if (r >= K) atomicAdd(&cnt[y_of_rank[r]], 1u);
+      if (r >= K) atomicAdd(&cnt[base + y_of_rank[r]], 1u);
     }
+  }
 }
 
 __global__ void cold_scatter_kernel(const uint64_t* __restrict__ dl_ptr,
                                     const uint32_t* __restrict__ dl_col, uint64_t n_dense,
                                     uint32_t K, const uint32_t* __restrict__ y_of_rank,
                                     unsigned long long* __restrict__ cursor,
-                                    uint32_t* __restrict__ out) {
+                                    uint32_t* __restrict__ out, uint64_t y_card,
+                                    uint32_t part_rows) {
   for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < n_dense;
-       i += (uint64_t)gridDim.x * (blockDim.x / 32))
+       i += (uint64_t)gridDim.x * (blockDim.x / 32)) {
+    const uint64_t base = (i / part_rows) * y_card;
     for (uint64_t k = dl_ptr[i] + lane_id(); k < dl_ptr[i + 1]; k += 32) {
       uint32_t r = dl_col[k];
-      if (r >= K) out[atomicAdd(&cursor[y_of_rank[r]], 1ull)] = (uint32_t)i;
+      if (r >= K) out[atomicAdd(&cursor[base + y_of_rank[r]], 1ull)] = (uint32_t)i;
     }
+  }
 }
 
 // --- TMA bulk copy helpers (sm_90+ PTX, used on sm_100a) -------------------
@@ -254,7 +260,7 @@ dense_hot_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
 // 256-bit hot signature inline (ch, 2 x uint4 per entry), so the filter
 // "hot masks intersect => already counted by P1" streams coalesced instead of
 // gathering hz[z] at random. Survivors are deduplicated in the warp's bitmap.
-constexpr int kColdWarps = 8;
+constexpr int kColdWarps = 8;  // warps per CTA (several CTAs per SM)
 
 __global__ void cold_sig_kernel(const uint32_t* __restrict__ ccol, uint64_t n,
                                 const uint4* __restrict__ hz4 /* [D][2] */,
@@ -268,57 +274,78 @@ __global__ void cold_sig_kernel(const uint32_t* __restrict__ ccol, uint64_t n,
 }
 
 template <int kMode>
-__global__ void __launch_bounds__(kColdWarps * 32, 1)
+__global__ void __launch_bounds__(kColdWarps * 32)
 dense_cold_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
                   const uint64_t* __restrict__ r_ptr, const uint32_t* __restrict__ r_col,
-                  const uint64_t* __restrict__ cptr, const uint32_t* __restrict__ ccol,
-                  const uint4* __restrict__ ch, const uint4* __restrict__ hx4 /* [X][2] */,
-                  uint32_t d_words, const uint32_t* __restrict__ dl_z, Decode dec, Emit em,
+                  const uint64_t* __restrict__ cptr /* [parts][y_card] + 1 */,
+                  const uint32_t* __restrict__ ccol, const uint4* __restrict__ ch,
+                  const uint4* __restrict__ hx4 /* [X][2] */, uint64_t y_card, uint32_t parts,
+                  uint32_t part_rows, const uint32_t* __restrict__ dl_z, Decode dec, Emit em,
                   unsigned int* __restrict__ next, Tally* tally) {
-  extern __shared__ __align__(16) uint32_t cbm[];  // [kColdWarps][d_words]
+  extern __shared__ __align__(16) uint32_t cbm[];  // [kColdWarps][part_rows / 32]
   const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
-  uint32_t* bm = cbm + (uint64_t)w * d_words;
-  for (uint32_t i = lane; i < d_words; i += 32) bm[i] = 0;
+  const uint32_t pw = part_rows / 32;
+  uint32_t* bm = cbm + (uint64_t)w * pw;
+  for (uint32_t i = lane; i < pw; i += 32) bm[i] = 0;
   __syncwarp();
   uint64_t cnt = 0, sum = 0, xr = 0;
+  const uint64_t n_items = n_x * parts;
   for (;;) {
     uint32_t item = 0;
     if (lane == 0) item = atomicAdd(next, 1u);
     item = __shfl_sync(0xffffffffu, item, 0);
-    if (item >= n_x) break;
-    const uint32_t x = xs[item];
+    if (item >= n_items) break;
+    const uint32_t part = (uint32_t)(item / n_x);
+    const uint32_t x = xs[item % n_x];
+    const uint32_t zbase = part * part_rows;
+    const uint64_t* cp = cptr + (uint64_t)part * y_card;
     const uint4 a0 = hx4[2 * (uint64_t)x], a1 = hx4[2 * (uint64_t)x + 1];
     bool touched = false;
-    for (uint64_t k = r_ptr[x]; k < r_ptr[x + 1]; ++k) {
-      const uint32_t y = r_col[k];
-      const uint64_t s0 = cptr[y], s1 = cptr[y + 1];
-      for (uint64_t t = s0 + lane; t < s1; t += 32) {
-        const uint4 b0 = ch[2 * t], b1 = ch[2 * t + 1];
-        const bool hot = ((a0.x & b0.x) | (a0.y & b0.y) | (a0.z & b0.z) | (a0.w & b0.w) |
-                          (a1.x & b1.x) | (a1.y & b1.y) | (a1.z & b1.z) | (a1.w & b1.w)) != 0;
-        if (hot) continue;
-        const uint32_t zi = ccol[t];
-        const uint32_t bit = 1u << (zi & 31);
-        const uint32_t old = atomicOr(&bm[zi >> 5], bit);
-        touched = true;
-        if (old & bit) continue;
-        ++cnt;
-        if (kMode == kModeChecksum) {
-          const uint64_t h = dec.hash(x, dl_z[zi]);
-          sum += h;
-          xr ^= h;
-        } else if (kMode == kModeEmit) {
-          const unsigned long long idx = atomicAdd(em.cursor, 1ull);
-          if (idx < em.cap) {
-            em.x[idx] = x;
-            em.z[idx] = dl_z[zi];
+    const uint64_t r0 = r_ptr[x], r1 = r_ptr[x + 1];
+    for (uint64_t kb = r0; kb < r1; kb += 32) {
+      // one coalesced load of up to 32 of x's y and their cold segments
+      const uint64_t kk = kb + lane;
+      uint64_t seg0 = 0, seg1 = 0;
+      if (kk < r1) {
+        const uint32_t y = r_col[kk];
+        seg0 = cp[y];
+        seg1 = cp[y + 1];
+      }
+      const uint32_t nseg = (uint32_t)((r1 - kb) < 32 ? (r1 - kb) : 32);
+      for (uint32_t j = 0; j < nseg; ++j) {
+        const uint64_t s0 = __shfl_sync(0xffffffffu, seg0, j);
+        const uint64_t s1 = __shfl_sync(0xffffffffu, seg1, j);
+        for (uint64_t t = s0 + lane; t < s1; t += 32) {
+          const uint4 b0 = ch[2 * t], b1 = ch[2 * t + 1];
+          const uint32_t zl = ccol[t] - zbase;
+          const bool hot = ((a0.x & b0.x) | (a0.y & b0.y) | (a0.z & b0.z) | (a0.w & b0.w) |
+                            (a1.x & b1.x) | (a1.y & b1.y) | (a1.z & b1.z) | (a1.w & b1.w)) != 0;
+          if (hot) continue;
+          const uint32_t bit = 1u << (zl & 31);
+          const uint32_t old = atomicOr(&bm[zl >> 5], bit);
+          touched = true;
+          if (old & bit) continue;
+          ++cnt;
+          if (kMode != kModeCount) {
+            const uint32_t zc = dl_z[zbase + zl];
+            if (kMode == kModeChecksum) {
+              const uint64_t h = dec.hash(x, zc);
+              sum += h;
+              xr ^= h;
+            } else {
+              const unsigned long long idx = atomicAdd(em.cursor, 1ull);
+              if (idx < em.cap) {
+                em.x[idx] = x;
+                em.z[idx] = zc;
+              }
+            }
           }
         }
       }
     }
     __syncwarp();
     if (__any_sync(0xffffffffu, touched))
-      for (uint32_t i = lane; i < d_words; i += 32) bm[i] = 0;
+      for (uint32_t i = lane; i < pw; i += 32) bm[i] = 0;
     __syncwarp();
   }
   tally_flush(tally, cnt, sum, xr);

@@ -540,8 +540,9 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   uint32_t K = kv[best];
   if (K * 2 <= k_cap && K == 256 && k_cap >= 384) K = 384;  // use the slack of the batch slice
   // the warp-bitmap cold kernel carries 256-bit hot signatures: K = 256
-  const uint32_t d_words = (uint32_t)((D + 31) / 32);
-  const bool cold_kernel_ok = (uint64_t)d_words * 4 * kColdWarps <= budget && k_cap >= 256;
+  // (the dense rows are split into at most 16 bitmap partitions, see P2)
+  const uint64_t cold_rows_cap = std::max<uint64_t>(32, (budget / 3 / kColdWarps) * 8 / 32 * 32);
+  const bool cold_kernel_ok = k_cap >= 256 && (D + cold_rows_cap - 1) / cold_rows_cap <= 16;
   if (cold_kernel_ok) K = 256;
   const uint32_t kw = (K + 63) / 64;
   const uint32_t n_batches = (groups + 31) / 32;
@@ -579,20 +580,30 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   });
   Tally h;
   X.to_host(&h, t.p, 1);
-  // P2: cold residual join (SparseBMM tiers, hot-hit candidates filtered)
+  // P2: cold residual join, hot-hit candidates filtered. With the warp-bitmap
+  // kernel the dense rows are cut into `parts` ranges so that 24 warps per SM
+  // each hold a part_rows-bit bitmap; the cold CSR is keyed by (part, y).
   KernelOut cold;
   if (e[best] > 0) {
-    DBuf<uint32_t> cc = X.zeros<uint32_t>(Y);
+    uint32_t parts = 1, part_rows = (uint32_t)(((D + 31) / 32) * 32);
+    if (cold_kernel_ok) {
+      const uint64_t per_warp = budget / 3 / kColdWarps;  // 3 CTAs of 8 warps per SM
+      const uint64_t rows_cap = std::max<uint64_t>(32, per_warp * 8 / 32 * 32);
+      parts = (uint32_t)((D + rows_cap - 1) / rows_cap);
+      part_rows = (uint32_t)((((D + parts - 1) / parts) + 31) / 32 * 32);
+    }
+    const uint64_t rows_key = (uint64_t)parts * Y;
+    DBuf<uint32_t> cc = X.zeros<uint32_t>(rows_key);
     D3G_LAUNCH(X, cold_count_kernel, grid_for(D * 32, 256), 256, 0, in.dl_ptr, in.dl_col, D, K,
-               in.y_of_rank, cc.p);
-    DBuf<uint64_t> cptr = X.alloc<uint64_t>(Y + 1);
-    exclusive_scan<uint32_t>(X, cc.p, Y, cptr.p);
-    const uint64_t cnnz = X.scalar(cptr.p + Y);
+               in.y_of_rank, cc.p, Y, part_rows);
+    DBuf<uint64_t> cptr = X.alloc<uint64_t>(rows_key + 1);
+    exclusive_scan<uint32_t>(X, cc.p, rows_key, cptr.p);
+    const uint64_t cnnz = X.scalar(cptr.p + rows_key);
     DBuf<uint32_t> ccol = X.alloc<uint32_t>(cnnz);
-    DBuf<unsigned long long> cur = X.alloc<unsigned long long>(Y + 1);
-    D3G_CUDA(cudaMemcpyAsync(cur.p, cptr.p, (Y + 1) * 8, cudaMemcpyDeviceToDevice, X.stream));
+    DBuf<unsigned long long> cur = X.alloc<unsigned long long>(rows_key + 1);
+    D3G_CUDA(cudaMemcpyAsync(cur.p, cptr.p, (rows_key + 1) * 8, cudaMemcpyDeviceToDevice, X.stream));
     D3G_LAUNCH(X, cold_scatter_kernel, grid_for(D * 32, 256), 256, 0, in.dl_ptr, in.dl_col, D, K,
-               in.y_of_rank, cur.p, ccol.p);
+               in.y_of_rank, cur.p, ccol.p, Y, part_rows);
     if (cold_kernel_ok) {
       DBuf<uint4> ch = X.alloc<uint4>(2 * cnnz);
       if (cnnz)
@@ -600,13 +611,14 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
                    reinterpret_cast<const uint4*>(hz.p), ch.p);
       DBuf<unsigned int> next = X.zeros<unsigned int>(1);
       DBuf<Tally> tc = X.zeros<Tally>(1);
-      size_t csm = (size_t)d_words * 4 * kColdWarps;
+      size_t csm = (size_t)(part_rows / 32) * 4 * kColdWarps;
       with_mode(mode, [&](auto M) {
         auto kfn = dense_cold_kernel<decltype(M)::value>;
-        D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
-        D3G_LAUNCH(X, kfn, (unsigned)X.sm_count, kColdWarps * 32, csm, xorder, n_live, in.r_ptr,
-                   in.r_col, cptr.p, ccol.p, ch.p, reinterpret_cast<const uint4*>(hx.p), d_words,
-                   in.dl_z, dec, em, next.p, tc.p);
+        if (csm > 48 * 1024)
+          D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
+        D3G_LAUNCH(X, kfn, (unsigned)X.sm_count * 3, kColdWarps * 32, csm, xorder, n_live, in.r_ptr,
+                   in.r_col, cptr.p, ccol.p, ch.p, reinterpret_cast<const uint4*>(hx.p), Y, parts,
+                   part_rows, in.dl_z, dec, em, next.p, tc.p);
       });
       Tally hc;
       X.to_host(&hc, tc.p, 1);
