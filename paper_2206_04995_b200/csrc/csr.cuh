@@ -10,7 +10,7 @@
 // with a 128-bit accumulator (out_j_from_degrees, :350-364).
 #pragma once
 
-#include "prims.cuh"
+#include "segsort.cuh"
 
 namespace d3g {
 
@@ -60,36 +60,32 @@ __global__ void row_bounds_kernel(const uint32_t* __restrict__ row_of, uint64_t 
   }
 }
 
+// Counting-scatter + segmented sort/unique (segsort.cuh).
 inline void build_csr_device(Ctx& ctx, const uint32_t* maj, const uint32_t* mnr, uint64_t n,
                              uint64_t n_rows, uint64_t n_cols, DeviceCsr& out) {
   out.n_rows = n_rows;
   out.n_cols = n_cols;
   out.row_ptr = ctx.alloc<uint64_t>(n_rows + 1);
-  if (n == 0) {
+  if (n == 0 || n_rows == 0) {
     D3G_CUDA(cudaMemsetAsync(out.row_ptr.p, 0, (n_rows + 1) * 8, ctx.stream));
     out.col = ctx.alloc<uint32_t>(0);
     out.nnz = 0;
     return;
   }
-  int minor_bits = bits_for(n_cols ? n_cols - 1 : 0);
-  int major_bits = bits_for(n_rows ? n_rows - 1 : 0);
-  if (minor_bits + major_bits > 64) throw ResourceError("composite key exceeds 64 bits");
-  DBuf<uint64_t> keys = ctx.alloc<uint64_t>(n);
   unsigned g = grid_for(n, 256);
-  D3G_LAUNCH(ctx, composite_key_kernel, g, 256, 0, maj, mnr, n, minor_bits, keys.p);
-  radix_sort(ctx, keys.p, nullptr, n, minor_bits + major_bits);
-  DBuf<uint32_t> flag = ctx.alloc<uint32_t>(n);
-  DBuf<uint64_t> pos = ctx.alloc<uint64_t>(n + 1);
-  D3G_LAUNCH(ctx, uniq_flag_kernel, g, 256, 0, keys.p, n, flag.p);
-  exclusive_scan<uint32_t>(ctx, flag.p, n, pos.p);
-  uint64_t nnz = ctx.scalar(pos.p + n);
-  out.nnz = nnz;
-  out.col = ctx.alloc<uint32_t>(nnz);
-  DBuf<uint32_t> row_of = ctx.alloc<uint32_t>(nnz);
-  D3G_LAUNCH(ctx, uniq_write_kernel, g, 256, 0, keys.p, flag.p, pos.p, n, minor_bits, out.col.p,
-             row_of.p);
-  D3G_LAUNCH(ctx, row_bounds_kernel, grid_for(nnz + 1, 256), 256, 0, row_of.p, nnz, n_rows,
-             out.row_ptr.p);
+  DBuf<uint32_t> cnt = ctx.zeros<uint32_t>(n_rows);
+  D3G_LAUNCH(ctx, major_hist_kernel, g, 256, 0, maj, n, cnt.p);
+  DBuf<uint64_t> off = ctx.alloc<uint64_t>(n_rows + 1);
+  exclusive_scan<uint32_t>(ctx, cnt.p, n_rows, off.p);
+  D3G_CUDA(cudaMemsetAsync(cnt.p, 0, n_rows * 4, ctx.stream));  // reused as the fill cursor
+  DBuf<uint32_t> tmp = ctx.alloc<uint32_t>(n);
+  D3G_LAUNCH(ctx, major_scatter_kernel, g, 256, 0, maj, mnr, n, off.p, cnt.p, tmp.p);
+  segmented_sort(ctx, tmp.p, off.p, n_rows, /*unique=*/true, cnt.p);  // cnt <- kept per row
+  exclusive_scan<uint32_t>(ctx, cnt.p, n_rows, out.row_ptr.p);
+  out.nnz = ctx.scalar(out.row_ptr.p + n_rows);
+  out.col = ctx.alloc<uint32_t>(out.nnz);
+  D3G_LAUNCH(ctx, row_compact_kernel, grid_for(n_rows * 32, 256), 256, 0, tmp.p, off.p,
+             out.row_ptr.p, n_rows, out.col.p);
 }
 
 // ---------------------------------------------------------------------------

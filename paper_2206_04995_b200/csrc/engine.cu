@@ -748,16 +748,12 @@ void build_dense_layout(Ctx& X, const d3g::DeviceCsr& rx, uint64_t max_mx,
   exclusive_scan<uint32_t>(X, len.p, n_dense, L.dl_ptr.p);
   len.reset();
   uint64_t dnnz = X.scalar(L.dl_ptr.p + n_dense);
-  int ybits = bits_for(y_card ? y_card - 1 : 0);
-  int pbits = bits_for(n_dense - 1);
-  if (ybits + pbits > 64) throw ResourceError("dense list key exceeds 64 bits");
   {
-    DBuf<uint64_t> lk = X.alloc<uint64_t>(dnnz);
-    D3G_LAUNCH(X, dense_list_key_kernel, grid_for(n_dense * 32, 256), 256, 0, rows.p, n_dense,
-               zrow_ptr, zcol, L.dl_ptr.p, L.y_rank.p, ybits, lk.p);
-    radix_sort(X, lk.p, nullptr, dnnz, ybits + pbits);
     L.dl_col = X.alloc<uint32_t>(dnnz);
-    D3G_LAUNCH(X, low_bits_kernel, grid_for(dnnz, 256), 256, 0, lk.p, dnnz, ybits, L.dl_col.p);
+    D3G_LAUNCH(X, dense_list_fill_kernel, grid_for(n_dense * 32, 256), 256, 0, rows.p, n_dense,
+               zrow_ptr, zcol, L.dl_ptr.p, L.y_rank.p, L.dl_col.p);
+    DBuf<uint32_t> kept = X.alloc<uint32_t>(n_dense);
+    segmented_sort(X, L.dl_col.p, L.dl_ptr.p, n_dense, /*unique=*/false, kept.p);
   }
   if (z_of_row) D3G_LAUNCH(X, map_through_kernel, grid_for(n_dense, 256), 256, 0, rows.p, n_dense, z_of_row);
   L.dl_z = std::move(rows);

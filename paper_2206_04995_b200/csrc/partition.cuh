@@ -20,6 +20,7 @@
 #pragma once
 
 #include "csr.cuh"
+#include "segsort.cuh"
 
 namespace d3g {
 
@@ -35,13 +36,6 @@ __global__ void dense_flag_kernel(const uint64_t* __restrict__ row_ptr, uint64_t
   }
 }
 
-__global__ void index_compact_kernel(const uint32_t* __restrict__ flag,
-                                     const uint64_t* __restrict__ pos, uint64_t n,
-                                     uint32_t* __restrict__ out) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x)
-    if (flag[i]) out[pos[i]] = (uint32_t)i;
-}
 
 // per-y count of sparse tuples
 __global__ void sparse_y_count_kernel(const uint64_t* __restrict__ row_ptr,
@@ -115,6 +109,21 @@ __global__ void dense_list_key_kernel(const uint32_t* __restrict__ ids, uint64_t
     uint64_t s0 = src_ptr[id], s1 = src_ptr[id + 1], d0 = dst_ptr[i];
     for (uint64_t k = s0 + lane_id(); k < s1; k += 32)
       keys[d0 + (k - s0)] = ((uint64_t)i << ybits) | y_rank[src_col[k]];
+  }
+}
+
+// dl_col[dl_ptr[i] + k] = y_rank[src_col[src_ptr[ids[i]] + k]] (warp per row)
+__global__ void dense_list_fill_kernel(const uint32_t* __restrict__ ids, uint64_t n,
+                                       const uint64_t* __restrict__ src_ptr,
+                                       const uint32_t* __restrict__ src_col,
+                                       const uint64_t* __restrict__ dst_ptr,
+                                       const uint32_t* __restrict__ y_rank,
+                                       uint32_t* __restrict__ out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < n;
+       i += (uint64_t)gridDim.x * (blockDim.x / 32)) {
+    uint32_t id = ids[i];
+    uint64_t s0 = src_ptr[id], s1 = src_ptr[id + 1], d0 = dst_ptr[i];
+    for (uint64_t k = s0 + lane_id(); k < s1; k += 32) out[d0 + (k - s0)] = y_rank[src_col[k]];
   }
 }
 

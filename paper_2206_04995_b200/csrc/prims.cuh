@@ -236,6 +236,14 @@ inline void radix_sort(Ctx& ctx, uint64_t* keys, uint32_t* vals, uint64_t n, int
   }
 }
 
+__global__ void index_compact_kernel(const uint32_t* __restrict__ flag,
+                                     const uint64_t* __restrict__ pos, uint64_t n,
+                                     uint32_t* __restrict__ out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    if (flag[i]) out[pos[i]] = (uint32_t)i;
+}
+
 inline int bits_for(uint64_t max_value) {
   int b = 0;
   while (b < 64 && (max_value >> b) != 0) ++b;

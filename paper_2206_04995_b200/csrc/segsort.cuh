@@ -1,0 +1,300 @@
+// Counting-scatter CSR build + warp-level segmented sort/unique.
+//
+// build_csr (P/src/relation.cpp:206-258) needs rows sorted by minor with
+// duplicates collapsed. Rows on the BASELINE configs are short (10-45
+// entries), so instead of a full-width LSD radix sort of (major, minor) keys
+// (5-6 passes of 24 B/tuple) the GPU path:
+//   1. histograms the major codes (one pass),
+//   2. exclusive-scans the counts into row offsets,
+//   3. scatters the minor codes into their row (atomic per-row cursor),
+//   4. sorts and de-duplicates every row in registers: one warp per row,
+//      bitonic network over 32*E lanes-elements (E = 1, 2, 4 -> rows <= 128),
+//      rows up to 8192 in shared memory by one CTA, longer rows through the
+//      radix sort,
+//   5. scans the unique counts and compacts the rows into the final CSR.
+// About 5 passes of 4-8 B/tuple.
+#pragma once
+
+#include "prims.cuh"
+
+namespace d3g {
+
+__global__ void major_hist_kernel(const uint32_t* __restrict__ maj, uint64_t n,
+                                  uint32_t* __restrict__ cnt) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    atomicAdd(&cnt[maj[i]], 1u);
+}
+
+__global__ void major_scatter_kernel(const uint32_t* __restrict__ maj,
+                                     const uint32_t* __restrict__ mnr, uint64_t n,
+                                     const uint64_t* __restrict__ off, uint32_t* __restrict__ fill,
+                                     uint32_t* __restrict__ out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t m = maj[i];
+    out[off[m] + atomicAdd(&fill[m], 1u)] = mnr[i];
+  }
+}
+
+// Bitonic sort of 32*E elements held striped (element e*32 + lane) by a warp.
+template <int E>
+__device__ __forceinline__ void warp_bitonic(uint32_t (&v)[E]) {
+  const uint32_t lane = lane_id();
+#pragma unroll
+  for (int k = 2; k <= 32 * E; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
+        const int ej = j / 32;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int p = e ^ ej;
+          if (p > e) {
+            const uint32_t i = (uint32_t)e * 32 + lane;
+            const bool up = (i & k) == 0;
+            const uint32_t a = v[e], b = v[p];
+            const uint32_t mn = a < b ? a : b, mx = a < b ? b : a;
+            v[e] = up ? mn : mx;
+            v[p] = up ? mx : mn;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const uint32_t i = (uint32_t)e * 32 + lane;
+          const uint32_t o = __shfl_xor_sync(0xffffffffu, v[e], j);
+          const bool up = (i & k) == 0;
+          const bool lower = (lane & j) == 0;
+          const uint32_t mn = v[e] < o ? v[e] : o, mx = v[e] < o ? o : v[e];
+          v[e] = (lower == up) ? mn : mx;
+        }
+      }
+    }
+  }
+}
+
+// Sort (and optionally unique) a row of len <= 32*E held in data[base..):
+// writes the result back in place, returns the kept count (warp-uniform).
+template <int E>
+__device__ __forceinline__ uint32_t warp_sort_row(uint32_t* __restrict__ data, uint64_t base,
+                                                  uint32_t len, bool unique) {
+  const uint32_t lane = lane_id();
+  uint32_t v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const uint32_t i = (uint32_t)e * 32 + lane;
+    v[e] = i < len ? data[base + i] : 0xffffffffu;
+  }
+  warp_bitonic<E>(v);
+  uint32_t written = 0;
+  uint32_t prev_last = 0xffffffffu;  // last element of the previous chunk
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const uint32_t i = (uint32_t)e * 32 + lane;
+    uint32_t prev = __shfl_up_sync(0xffffffffu, v[e], 1);
+    if (lane == 0) prev = prev_last;
+    const bool valid = i < len;
+    const bool keep = valid && (!unique || i == 0 || v[e] != prev);
+    const uint32_t m = __ballot_sync(0xffffffffu, keep);
+    if (keep) data[base + written + __popc(m & ((1u << lane) - 1))] = v[e];
+    written += __popc(m);
+    prev_last = __shfl_sync(0xffffffffu, v[e], 31);
+  }
+  return written;
+}
+
+// One warp per row for rows of length <= 128; longer rows are flagged.
+__global__ void row_sort_small_kernel(uint32_t* __restrict__ data, const uint64_t* __restrict__ off,
+                                      uint64_t n_rows, int unique, uint32_t* __restrict__ kept,
+                                      uint32_t* __restrict__ long_flag) {
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x / 32);
+  for (uint64_t r = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); r < n_rows;
+       r += warps) {
+    const uint64_t b = off[r];
+    const uint32_t len = (uint32_t)(off[r + 1] - b);
+    uint32_t k = len;
+    bool lng = false;
+    if (len <= 1) {
+      k = len;
+    } else if (len <= 32) {
+      k = warp_sort_row<1>(data, b, len, unique);
+    } else if (len <= 64) {
+      k = warp_sort_row<2>(data, b, len, unique);
+    } else if (len <= 128) {
+      k = warp_sort_row<4>(data, b, len, unique);
+    } else {
+      lng = true;
+    }
+    if (lane_id() == 0) {
+      kept[r] = k;
+      long_flag[r] = lng ? 1u : 0u;
+    }
+  }
+}
+
+// One CTA per long row (129..8192 entries): bitonic sort in shared memory.
+constexpr int kLongRowMax = 8192;
+__global__ void __launch_bounds__(1024)
+row_sort_long_kernel(uint32_t* __restrict__ data, const uint64_t* __restrict__ off,
+                     const uint32_t* __restrict__ rows, uint64_t n, int unique,
+                     uint32_t* __restrict__ kept) {
+  __shared__ uint32_t s[kLongRowMax];
+  __shared__ uint32_t wsum[32];
+  for (uint64_t q = blockIdx.x; q < n; q += gridDim.x) {
+    const uint32_t r = rows[q];
+    const uint64_t b = off[r];
+    const uint32_t len = (uint32_t)(off[r + 1] - b);
+    if (len > kLongRowMax) continue;  // handled by the radix fallback
+    uint32_t p2 = 1;
+    while (p2 < len) p2 <<= 1;
+    for (uint32_t i = threadIdx.x; i < p2; i += blockDim.x) s[i] = i < len ? data[b + i] : 0xffffffffu;
+    __syncthreads();
+    for (uint32_t k = 2; k <= p2; k <<= 1)
+      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+        for (uint32_t i = threadIdx.x; i < p2; i += blockDim.x) {
+          const uint32_t pj = i ^ j;
+          if (pj > i) {
+            const bool up = (i & k) == 0;
+            const uint32_t a = s[i], c = s[pj];
+            if ((a > c) == up) {
+              s[i] = c;
+              s[pj] = a;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    // unique + compaction in index order (block scan over 1024-element chunks)
+    uint32_t written = 0;
+    for (uint32_t base = 0; base < len; base += blockDim.x) {
+      const uint32_t i = base + threadIdx.x;
+      const bool keep = i < len && (!unique || i == 0 || s[i] != s[i - 1]);
+      const uint32_t m = __ballot_sync(0xffffffffu, keep);
+      if (lane_id() == 0) wsum[threadIdx.x >> 5] = __popc(m);
+      __syncthreads();
+      uint32_t before = 0;
+      for (uint32_t w = 0; w < (threadIdx.x >> 5); ++w) before += wsum[w];
+      uint32_t tot = 0;
+      for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) tot += wsum[w];
+      if (keep) data[b + written + before + __popc(m & ((1u << lane_id()) - 1))] = s[i];
+      written += tot;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) kept[r] = written;
+    __syncthreads();
+  }
+}
+
+__global__ void row_len_kernel(const uint64_t* __restrict__ off, const uint32_t* __restrict__ rows,
+                               uint64_t n, uint32_t* __restrict__ len) {
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t r = rows[q];
+    len[q] = (uint32_t)(off[r + 1] - off[r]);
+  }
+}
+
+// Radix fallback for rows longer than kLongRowMax: gather (row, value) keys.
+__global__ void huge_gather_kernel(const uint32_t* __restrict__ data, const uint64_t* __restrict__ off,
+                                   const uint32_t* __restrict__ rows, uint64_t n,
+                                   const uint64_t* __restrict__ goff, int vbits,
+                                   uint64_t* __restrict__ keys) {
+  for (uint64_t q = blockIdx.x; q < n; q += gridDim.x) {
+    const uint32_t r = rows[q];
+    const uint64_t b = off[r], len = off[r + 1] - b;
+    for (uint64_t i = threadIdx.x; i < len; i += blockDim.x)
+      keys[goff[q] + i] = ((uint64_t)q << vbits) | data[b + i];
+  }
+}
+
+__global__ void huge_scatter_kernel(uint32_t* __restrict__ data, const uint64_t* __restrict__ off,
+                                    const uint32_t* __restrict__ rows, uint64_t n,
+                                    const uint64_t* __restrict__ goff, int vbits, int unique,
+                                    const uint64_t* __restrict__ keys, uint32_t* __restrict__ kept) {
+  // one CTA per huge row, sequential-by-chunk compaction of the sorted run
+  __shared__ uint32_t wsum[32];
+  const uint64_t vmask = (1ull << vbits) - 1;
+  for (uint64_t q = blockIdx.x; q < n; q += gridDim.x) {
+    const uint32_t r = rows[q];
+    const uint64_t b = off[r], len = off[r + 1] - b, g = goff[q];
+    uint64_t written = 0;
+    for (uint64_t base = 0; base < len; base += blockDim.x) {
+      const uint64_t i = base + threadIdx.x;
+      const bool keep = i < len && (!unique || i == 0 || keys[g + i] != keys[g + i - 1]);
+      const uint32_t m = __ballot_sync(0xffffffffu, keep);
+      if (lane_id() == 0) wsum[threadIdx.x >> 5] = __popc(m);
+      __syncthreads();
+      uint32_t before = 0, tot = 0;
+      for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) {
+        if (w < (threadIdx.x >> 5)) before += wsum[w];
+        tot += wsum[w];
+      }
+      if (keep) data[b + written + before + __popc(m & ((1u << lane_id()) - 1))] =
+          (uint32_t)(keys[g + i] & vmask);
+      written += tot;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) kept[r] = (uint32_t)written;
+    __syncthreads();
+  }
+}
+
+// rows compaction: copy kept[r] values of row r from data[off[r]..] to
+// col[row_ptr[r]..] (one warp per row)
+__global__ void row_compact_kernel(const uint32_t* __restrict__ data, const uint64_t* __restrict__ off,
+                                   const uint64_t* __restrict__ row_ptr, uint64_t n_rows,
+                                   uint32_t* __restrict__ col) {
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x / 32);
+  for (uint64_t r = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); r < n_rows;
+       r += warps) {
+    const uint64_t s = off[r], d = row_ptr[r], k = row_ptr[r + 1] - d;
+    for (uint64_t i = lane_id(); i < k; i += 32) col[d + i] = data[s + i];
+  }
+}
+
+// Sorts every row data[off[r] .. off[r+1]) ascending, optionally dropping
+// duplicates; kept[r] receives the resulting length (rows stay in place).
+inline void segmented_sort(Ctx& ctx, uint32_t* data, const uint64_t* off, uint64_t n_rows,
+                           bool unique, uint32_t* kept) {
+  if (n_rows == 0) return;
+  DBuf<uint32_t> lf = ctx.alloc<uint32_t>(n_rows);
+  D3G_LAUNCH(ctx, row_sort_small_kernel, grid_for(n_rows * 32, 256, ctx.sm_count * 64), 256, 0,
+             data, off, n_rows, unique ? 1 : 0, kept, lf.p);
+  DBuf<uint64_t> lp = ctx.alloc<uint64_t>(n_rows + 1);
+  exclusive_scan<uint32_t>(ctx, lf.p, n_rows, lp.p);
+  const uint64_t n_long = ctx.scalar(lp.p + n_rows);
+  if (n_long == 0) return;
+  DBuf<uint32_t> rows = ctx.alloc<uint32_t>(n_long);
+  D3G_LAUNCH(ctx, index_compact_kernel, grid_for(n_rows, 256), 256, 0, lf.p, lp.p, n_rows, rows.p);
+  D3G_LAUNCH(ctx, row_sort_long_kernel, (unsigned)std::min<uint64_t>(n_long, ctx.sm_count * 2), 1024,
+             0, data, off, rows.p, n_long, unique ? 1 : 0, kept);
+  // rows longer than kLongRowMax: radix fallback
+  DBuf<uint32_t> len = ctx.alloc<uint32_t>(n_long);
+  D3G_LAUNCH(ctx, row_len_kernel, grid_for(n_long, 256), 256, 0, off, rows.p, n_long, len.p);
+  std::vector<uint32_t> hl(n_long), hr(n_long);
+  ctx.to_host(hl.data(), len.p, n_long);
+  ctx.to_host(hr.data(), rows.p, n_long);
+  std::vector<uint32_t> huge;
+  std::vector<uint64_t> goff{0};
+  for (uint64_t i = 0; i < n_long; ++i)
+    if (hl[i] > (uint32_t)kLongRowMax) {
+      huge.push_back(hr[i]);
+      goff.push_back(goff.back() + hl[i]);
+    }
+  if (huge.empty()) return;
+  const uint64_t nh = huge.size(), tot = goff.back();
+  DBuf<uint32_t> dh = ctx.alloc<uint32_t>(nh);
+  DBuf<uint64_t> dg = ctx.alloc<uint64_t>(nh + 1);
+  ctx.to_device(dh.p, huge.data(), nh);
+  ctx.to_device(dg.p, goff.data(), nh + 1);
+  DBuf<uint64_t> keys = ctx.alloc<uint64_t>(tot);
+  const int vbits = 32;
+  D3G_LAUNCH(ctx, huge_gather_kernel, (unsigned)std::min<uint64_t>(nh, ctx.sm_count * 4), 256, 0,
+             data, off, dh.p, nh, dg.p, vbits, keys.p);
+  radix_sort(ctx, keys.p, nullptr, tot, vbits + bits_for(nh));
+  D3G_LAUNCH(ctx, huge_scatter_kernel, (unsigned)std::min<uint64_t>(nh, ctx.sm_count * 4), 256, 0,
+             data, off, dh.p, nh, dg.p, vbits, unique ? 1 : 0, keys.p, kept);
+}
+
+}  // namespace d3g
