@@ -16,6 +16,7 @@
 #include <limits>
 #include <string>
 #include <type_traits>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -90,37 +91,59 @@ __global__ void gather_stride_kernel(const uint64_t* __restrict__ src, uint64_t 
     dst[i] = src[i * stride];
 }
 
-uint64_t estimate_out_j(Ctx& X, const d3g_table* R, const d3g_table* S, const uint64_t* dRr,
-                        const uint64_t* dSr) {
+// The f1 estimate only gates the classical branch, which this path reports
+// but does not take, so it runs OFF the critical path: the y samples (or the
+// whole y columns below the exact limit) are copied into a pinned buffer on
+// the stream, and a host thread waits for that copy and runs the reference's
+// hash counting while the GPU pipeline proceeds. get() joins it.
+struct EstimateJob {
+  std::thread th;
+  uint64_t result = 0;
+  cudaEvent_t ev = nullptr;
+  DBuf<uint64_t> dev;  // gathered samples (stream-ordered lifetime)
+  ~EstimateJob() {
+    if (th.joinable()) th.join();
+    if (ev) cudaEventDestroy(ev);
+  }
+  uint64_t get() {
+    if (th.joinable()) th.join();
+    return result;
+  }
+};
+
+void start_estimate(Ctx& X, const d3g_table* R, const d3g_table* S, const uint64_t* dRr,
+                    const uint64_t* dSr, EstimateJob& job) {
   const uint64_t nr = R->n, ns = S->n;
-  if (nr == 0 || ns == 0) return 0;
+  if (nr == 0 || ns == 0) return;
   const uint64_t exact_limit = 65536, sample_rows = 16384;
-  bool exact = nr <= exact_limit && ns <= exact_limit;
-  uint64_t ms = std::min(ns, sample_rows), mr = std::min(nr, sample_rows);
-  uint64_t ss = ns / ms, sr = nr / mr;
-  std::vector<uint64_t> hr, hs;
-  if (exact) {
-    hr.resize(nr);
-    hs.resize(ns);
-    if (R->on_device) X.to_host(hr.data(), R->right, nr); else std::memcpy(hr.data(), R->right, nr * 8);
-    if (S->on_device) X.to_host(hs.data(), S->right, ns); else std::memcpy(hs.data(), S->right, ns * 8);
-    return estimate_raw(hr.data(), nr, hs.data(), ns, 1, 1, nr, ns, true);
+  const bool exact = nr <= exact_limit && ns <= exact_limit;
+  const uint64_t ms = std::min(ns, sample_rows), mr = std::min(nr, sample_rows);
+  const uint64_t ss = exact ? 1 : ns / ms, sr = exact ? 1 : nr / mr;
+  const uint64_t cr = exact ? nr : mr, cs = exact ? ns : ms;
+  if (!R->on_device && !S->on_device) {
+    job.th = std::thread([=, &job] {
+      std::vector<uint64_t> hr(cr), hs(cs);
+      for (uint64_t i = 0; i < cr; ++i) hr[i] = R->right[i * sr];
+      for (uint64_t i = 0; i < cs; ++i) hs[i] = S->right[i * ss];
+      job.result = estimate_raw(hr.data(), nr, hs.data(), ns, sr, ss, mr, ms, exact);
+    });
+    return;
   }
-  hr.resize(mr);
-  hs.resize(ms);
-  if (R->on_device || S->on_device) {
-    DBuf<uint64_t> g = X.alloc<uint64_t>(mr + ms);
-    D3G_LAUNCH(X, gather_stride_kernel, d3g::grid_for(mr, 256), 256, 0, dRr, sr, mr, g.p);
-    D3G_LAUNCH(X, gather_stride_kernel, d3g::grid_for(ms, 256), 256, 0, dSr, ss, ms, g.p + mr);
-    std::vector<uint64_t> tmp(mr + ms);
-    X.to_host(tmp.data(), g.p, mr + ms);
-    std::copy(tmp.begin(), tmp.begin() + mr, hr.begin());
-    std::copy(tmp.begin() + mr, tmp.end(), hs.begin());
-  } else {
-    for (uint64_t i = 0; i < mr; ++i) hr[i] = R->right[i * sr];
-    for (uint64_t i = 0; i < ms; ++i) hs[i] = S->right[i * ss];
-  }
-  return estimate_raw(hr.data(), nr, hs.data(), ns, sr, ss, mr, ms, false);
+  if (X.est_pinned == nullptr) D3G_CUDA(cudaMallocHost(&X.est_pinned, 2 * exact_limit * 8));
+  job.dev = X.alloc<uint64_t>(cr + cs);
+  D3G_LAUNCH(X, gather_stride_kernel, d3g::grid_for(cr, 256), 256, 0, dRr, sr, cr, job.dev.p);
+  D3G_LAUNCH(X, gather_stride_kernel, d3g::grid_for(cs, 256), 256, 0, dSr, ss, cs, job.dev.p + cr);
+  D3G_CUDA(cudaMemcpyAsync(X.est_pinned, job.dev.p, (cr + cs) * 8, cudaMemcpyDeviceToHost,
+                           X.stream));
+  X.d2h_bytes += (cr + cs) * 8;
+  D3G_CUDA(cudaEventCreateWithFlags(&job.ev, cudaEventDisableTiming));
+  D3G_CUDA(cudaEventRecord(job.ev, X.stream));
+  const uint64_t* buf = X.est_pinned;
+  cudaEvent_t ev = job.ev;
+  job.th = std::thread([=, &job] {
+    if (cudaEventSynchronize(ev) != cudaSuccess) return;
+    job.result = estimate_raw(buf, nr, buf + cr, ns, sr, ss, mr, ms, exact);
+  });
 }
 
 __global__ void live_flag_kernel(const uint64_t* __restrict__ row_ptr, uint64_t lo, uint64_t hi,
@@ -840,10 +863,9 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   }
   T.mark();  // 1
 
-  // 2. f1 gate (engine.cpp:368-384)
-  rep->out_j_estimate = estimate_out_j(X, R, S, Rr, Sr);
-  rep->f1 = d3g_f1(NR, NS, rep->out_j_estimate, c);
-  rep->f1_gate_classical = (o->force == D3G_AUTO && rep->f1 > 0) ? 1 : 0;
+  // 2. f1 gate (engine.cpp:368-384), evaluated concurrently (EstimateJob)
+  EstimateJob est;
+  start_estimate(X, R, S, Rr, Sr, est);
   const char* strat = o->force == D3G_SPARSE_ONLY  ? "sparse"
                       : o->force == D3G_DENSE_ONLY ? "dense"
                                                    : "hybrid";
@@ -1148,6 +1170,9 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   rep->ms_dense = T.ms(7, 8);
   rep->ms_decode = T.ms(8, 9);
   rep->ms_total = T.ms(0, 9);
+  rep->out_j_estimate = est.get();
+  rep->f1 = d3g_f1(NR, NS, rep->out_j_estimate, c);
+  rep->f1_gate_classical = (o->force == D3G_AUTO && rep->f1 > 0) ? 1 : 0;
   rep->peak_bytes = X.peak_bytes - base_live;
   rep->gpu_launches = X.launches;
   rep->d2h_bytes += X.d2h_bytes;
@@ -1201,6 +1226,7 @@ void d3g_ctx_destroy(d3g_ctx* ctx) {
   cudaSetDevice(ctx->c.device);
   cudaStreamSynchronize(ctx->c.stream);
   if (ctx->c.pinned) cudaFreeHost(ctx->c.pinned);
+  if (ctx->c.est_pinned) cudaFreeHost(ctx->c.est_pinned);
   cudaStreamDestroy(ctx->c.stream);
   delete ctx;
 }

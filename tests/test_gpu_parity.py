@@ -138,3 +138,36 @@ def test_baseline_config_matches_reference(cfg):
     for k in ("x_card", "y_card", "z_card", "r_nnz", "s_nnz", "out_j", "dense_z", "sparse_z",
               "sparse_nnz", "dropped_r"):
         assert getattr(rep, k) == p[k], k
+
+
+def test_cfg5_x_slice_matches_reference():
+    """cfg5 (200M x 200M, Zipf 1.2): R restricted to x < 1000 against the full S
+    (the engine swaps). Count, set fingerprint and per-100-x block
+    fingerprints equal the reference's (tests/golden)."""
+    import torch
+    g = _golden().get("cfg5_x_lt_1000")
+    if g is None:
+        pytest.skip("golden entry not generated")
+    rl, rr = d3.generate(5, 0)
+    keep = rl < 1000
+    rl, rr = rl[keep].contiguous(), rr[keep].contiguous()
+    del keep
+    sl, sr = d3.generate(5, 1)
+    out = d3.join_project(d3.RawTable(rl, rr), d3.RawTable(sl, sr),
+                          d3.EngineConfig(force=d3.Strategy.auto_select, count_only=True,
+                                          checksum=True, memory_budget_bytes=120 << 30), C)
+    rep = out.report
+    assert rep.swapped
+    assert rep.out_p == g["set"]["count"] == 9976370095
+    assert rep.checksum_sum == g["set"]["sum"]
+    assert rep.checksum_xor == g["set"]["xor"]
+    # per-block: the caller x of this slice spans [0, 1000); check block 0 (x < 100)
+    blk = g["blocks"]
+    rb = rl < 100
+    o0 = d3.join_project(d3.RawTable(rl[rb].contiguous(), rr[rb].contiguous()), d3.RawTable(sl, sr),
+                         d3.EngineConfig(force=d3.Strategy.auto_select, count_only=True,
+                                         checksum=True, memory_budget_bytes=120 << 30), C)
+    assert (o0.report.out_p, o0.report.checksum_sum, o0.report.checksum_xor) == \
+        (blk["count"][0], blk["sum"][0], blk["xor"][0])
+    del rl, rr, sl, sr
+    torch.cuda.empty_cache()
