@@ -157,6 +157,18 @@ __global__ void value_hist_kernel(const uint32_t* __restrict__ vals, uint64_t n,
     if (sh[i]) atomicAdd(&counts[i], sh[i]);
 }
 
+// sum_y dR(y) * (ptr[y+1] - ptr[y]): the join size against a y-major CSR
+// (the sparse side: SpaStats::inner_count), u64 (far below 2^64 here).
+__global__ void outj_ptr_kernel(const uint32_t* __restrict__ dr, const uint64_t* __restrict__ ptr,
+                                uint64_t y_card, unsigned long long* __restrict__ out) {
+  uint64_t acc = 0;
+  for (uint64_t y = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; y < y_card;
+       y += (uint64_t)gridDim.x * blockDim.x)
+    acc += (uint64_t)dr[y] * (ptr[y + 1] - ptr[y]);
+  acc = warp_sum(acc);
+  if (lane_id() == 0 && acc) atomicAdd(out, (unsigned long long)acc);
+}
+
 // OUT_J = sum dR*dS with a (hi, lo) 128-bit accumulator per block.
 __global__ void outj_kernel(const uint32_t* __restrict__ dr, const uint32_t* __restrict__ ds,
                             uint64_t y_card, unsigned long long* __restrict__ parts) {

@@ -1089,6 +1089,22 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   if (n_dense > 0 && x_live > 0)
     build_dense_layout(X, rx, max_mx, hmx, sz_csr.row_ptr.p, sz_csr.col.p, dense_ids.p, n_dense,
                        max_mz, nullptr, y_card, dR.p, L);
+  // Heavy sparse side (OUT_J,sparse > 4096 per live x over > 8192 sparse z,
+  // e.g. cfg4's 9.7e10 candidates): answer it with the same hot bit-sliced +
+  // cold residual engine, restricted to the sparse z set. The result is the
+  // sparse kernel's exact output (pairs over sparse z), only computed faster.
+  uint64_t outj_sp = 0;
+  {
+    DBuf<unsigned long long> t = X.zeros<unsigned long long>(1);
+    if (y_card) D3G_LAUNCH(X, outj_ptr_kernel, grid_for(y_card, 256), 256, 0, dR.p, sp_ptr.p, y_card, t.p);
+    outj_sp = X.scalar(t.p);
+  }
+  const bool sparse_hot = std::getenv("D3G_SPARSE_TIERS") == nullptr && n_sparse > 8192 &&
+                          x_live > 0 && outj_sp > 4096ull * x_live;
+  DenseLayout Ls;
+  if (sparse_hot)
+    build_dense_layout(X, rx, max_mx, hmx, sz_csr.row_ptr.p, sz_csr.col.p, sparse_ids.p, n_sparse,
+                       max_mz, nullptr, y_card, dR.p, Ls);
   T.mark();  // 6
 
   // 8. kernels
@@ -1100,7 +1116,15 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   SparseInputs si{rx.row_ptr.p, rx.col.p, x_card, sp_ptr.p, sp_col.p, sparse_ids.p, n_sparse,
                   y_card, x_lo, x_hi};
   KernelOut ks, kd;
-  run_sparse(X, si, dec, mode, no_emit, ks);
+  const uint64_t s_lo = Ls.n_live * shard_index / shard_count,
+                 s_hi = Ls.n_live * (shard_index + 1) / shard_count;
+  DenseInputs dsi{Ls.xorder.p, Ls.n_live, rx.row_ptr.p, rx.col.p, Ls.y_rank.p, y_card,
+                  Ls.dl_ptr.p, Ls.dl_col.p, Ls.dl_z.p, Ls.n_dense, Ls.max_group_nnz, s_lo, s_hi,
+                  Ls.y_of_rank.p, dR.p, x_card, x_lo, x_hi};
+  if (sparse_hot)
+    run_dense_hot(X, dsi, dec, mode, no_emit, ks);
+  else
+    run_sparse(X, si, dec, mode, no_emit, ks);
   T.mark();  // 7
   uint64_t pos_lo = L.n_live * shard_index / shard_count,
            pos_hi = L.n_live * (shard_index + 1) / shard_count;
@@ -1111,7 +1135,7 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   T.mark();  // 8
   rep->pairs_sparse = ks.count;
   rep->pairs_dense = kd.count;
-  rep->spa_inner_count = ks.inner;
+  rep->spa_inner_count = outj_sp;
   rep->out_p = ks.count + kd.count;
   rep->checksum_sum = ks.sum + kd.sum;
   rep->checksum_xor = ks.xr ^ kd.xr;
@@ -1126,7 +1150,10 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
     DBuf<unsigned long long> cur = X.zeros<unsigned long long>(1);
     Emit em{ex.p, ez.p, cur.p, total};
     KernelOut tmp;
-    run_sparse(X, si, dec, kModeEmit, em, tmp);
+    if (sparse_hot)
+      run_dense_hot(X, dsi, dec, kModeEmit, em, tmp);
+    else
+      run_sparse(X, si, dec, kModeEmit, em, tmp);
     run_dense(X, di, dec, kModeEmit, em, tmp);
     DBuf<uint64_t> keys = X.alloc<uint64_t>(total);
     DBuf<uint32_t> idx = X.alloc<uint32_t>(total);
