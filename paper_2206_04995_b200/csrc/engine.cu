@@ -752,7 +752,7 @@ void build_dense_layout(Ctx& X, const d3g::DeviceCsr& rx, uint64_t max_mx,
     DBuf<uint32_t> v = X.alloc<uint32_t>(y_card);
     D3G_LAUNCH(X, degree_order_key_kernel, grid_for(y_card, 256), 256, 0, (const uint32_t*)nullptr,
                y_card, (const uint64_t*)nullptr, dR, max_dr, k.p, v.p);
-    radix_sort(X, k.p, v.p, y_card, 32 + bits_for(max_dr));
+    radix_sort(X, k.p, v.p, y_card, bits_for(max_dr));
     L.y_rank = X.alloc<uint32_t>(y_card);
     D3G_LAUNCH(X, scatter_rank_kernel, grid_for(y_card, 256), 256, 0, v.p, y_card, L.y_rank.p);
     L.y_of_rank = std::move(v);
@@ -763,7 +763,7 @@ void build_dense_layout(Ctx& X, const d3g::DeviceCsr& rx, uint64_t max_mx,
     DBuf<uint64_t> k = X.alloc<uint64_t>(n_dense);
     D3G_LAUNCH(X, degree_order_key_kernel, grid_for(n_dense, 256), 256, 0, row_ids, n_dense,
                zrow_ptr, (const uint32_t*)nullptr, max_mz, k.p, rows.p);
-    radix_sort(X, k.p, rows.p, n_dense, 32 + bits_for(max_mz));
+    radix_sort(X, k.p, rows.p, n_dense, bits_for(max_mz));
   }
   DBuf<uint32_t> len = X.alloc<uint32_t>(n_dense);
   D3G_LAUNCH(X, gather_len_kernel, grid_for(n_dense, 256), 256, 0, rows.p, n_dense, zrow_ptr, len.p);
@@ -796,7 +796,7 @@ void build_dense_layout(Ctx& X, const d3g::DeviceCsr& rx, uint64_t max_mx,
     if (L.n_live)
       D3G_LAUNCH(X, degree_order_key_kernel, grid_for(L.n_live, 256), 256, 0, live_ids.p, L.n_live,
                  rx.row_ptr.p, (const uint32_t*)nullptr, max_mx, k.p, L.xorder.p);
-    radix_sort(X, k.p, L.xorder.p, L.n_live, 32 + bits_for(max_mx));
+    radix_sort(X, k.p, L.xorder.p, L.n_live, bits_for(max_mx));
   }
   // group 0 holds the 128 largest m_x: bound for the per-group cold table
   uint64_t top = 0, seen = 0;

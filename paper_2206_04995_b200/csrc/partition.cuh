@@ -65,7 +65,8 @@ __global__ void sparse_y_scatter_kernel(const uint64_t* __restrict__ row_ptr,
   }
 }
 
-// (key = (maxd - d) << 32 | id) for ordering ids by degree descending.
+// key = maxd - d for ordering ids by degree descending (the radix sort is
+// stable, so equal degrees keep ascending id order).
 __global__ void degree_order_key_kernel(const uint32_t* __restrict__ ids, uint64_t n,
                                         const uint64_t* __restrict__ row_ptr,
                                         const uint32_t* __restrict__ deg_arr, uint64_t maxd,
@@ -74,7 +75,7 @@ __global__ void degree_order_key_kernel(const uint32_t* __restrict__ ids, uint64
        i += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t id = ids ? ids[i] : (uint32_t)i;
     uint64_t d = row_ptr ? row_ptr[id + 1] - row_ptr[id] : deg_arr[id];
-    keys[i] = ((maxd - d) << 32) | id;
+    keys[i] = maxd - d;  // stable sort keeps equal degrees in id order
     vals[i] = id;
   }
 }
