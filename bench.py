@@ -119,7 +119,7 @@ class ClockSampler:
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
@@ -139,6 +139,9 @@ def dist_env():
 
 
 # ---------------------------------------------------------------------------
+_X_ROWS: dict = {}
+
+
 def cpu_reference_sample(cfg: int, frac: float, threads: int, tables=None):
     """Reference prep on the whole job + reference kernels on an x-slice,
     extrapolated linearly in x. Returns (seconds_full_job_estimate, detail)."""
@@ -148,11 +151,13 @@ def cpu_reference_sample(cfg: int, frac: float, threads: int, tables=None):
         s = O.gen(cfg, 1)
     else:
         r, s = tables
-    x_hi = None
     # x codes are natural for cfg 1/2/3/5 (identity), dictionary codes for cfg4;
-    # slicing rows of r_by_x is the same either way.
-    probe = O.ref_timed_sample(r, s, threads, 0, 0)
-    x_rows = probe["x_rows"]
+    # slicing rows of r_by_x is the same either way. |X| is known from the
+    # generator for natural keys; otherwise probe once.
+    x_rows = _X_ROWS.get(cfg)
+    if x_rows is None:
+        x_rows = O.ref_timed_sample(r, s, threads, 0, 0)["x_rows"]
+        _X_ROWS[cfg] = x_rows
     x_hi = max(1, int(x_rows * frac))
     t = O.ref_timed_sample(r, s, threads, 0, x_hi)
     est = t["sec_prep"] + t["sec_kernels"] * (x_rows / x_hi)
