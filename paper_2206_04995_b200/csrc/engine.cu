@@ -23,6 +23,7 @@
 #include "datagen.cuh"
 #include "denseec.cuh"
 #include "denseec_hot.cuh"
+#include "denseec_tc.cuh"
 #include "mapping.cuh"
 #include "partition.cuh"
 #include "sparsebmm.cuh"
@@ -596,11 +597,34 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   DBuf<Tally> t = X.zeros<Tally>(1);
   size_t sm = (size_t)K * 32 * 16;
   unsigned g = (unsigned)std::min<uint64_t>((uint64_t)n_batches * hp.z_chunks, (uint64_t)X.sm_count);
-  with_mode(mode, [&](auto M) {
-    auto kfn = dense_hot_kernel<decltype(M)::value>;
-    D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    D3G_LAUNCH(X, kfn, g, kHotThreads, sm, hp, in.dl_ptr, in.dl_col, dec, em, t.p);
-  });
+  const char* hot_impl = std::getenv("D3G_HOT");
+  const bool use_tc = hot_impl && std::string(hot_impl) == "tc" && mode == kModeCount &&
+                      K % 32 == 0 && K <= 384;
+  if (use_tc) {
+    // tensor-core comparison path (denseec_tc.cuh): count-only
+    const uint32_t n_xt = (uint32_t)((n_live + kTcM - 1) / kTcM);
+    const uint32_t n_zt = (uint32_t)((D + kTcN - 1) / kTcN);
+    DBuf<uint8_t> A = X.zeros<uint8_t>((uint64_t)n_xt * kTcM * K);
+    DBuf<uint8_t> B = X.zeros<uint8_t>((uint64_t)n_zt * kTcN * K);
+    D3G_LAUNCH(X, tc_build_a_kernel, grid_for(n_live * 32, 256), 256, 0, xorder, n_live, in.r_ptr,
+               in.r_col, in.y_rank, K, A.p);
+    D3G_LAUNCH(X, tc_build_b_kernel, grid_for(D * 32, 256), 256, 0, in.dl_ptr, in.dl_col, D, K,
+               B.p);
+    const uint32_t x_chunks = std::max<uint32_t>(
+        1, std::min<uint32_t>(n_xt, ((uint32_t)X.sm_count * 4 + n_zt - 1) / n_zt));
+    DBuf<unsigned int> tw = X.zeros<unsigned int>(1);
+    const size_t tsm = (size_t)(kTcN + 2 * kTcM) * K;
+    auto kfn = dense_tc_kernel<kModeCount>;
+    D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
+    D3G_LAUNCH(X, kfn, (unsigned)std::min<uint64_t>((uint64_t)n_zt * x_chunks, X.sm_count),
+               kTcThreads, tsm, A.p, B.p, K, n_xt, n_zt, n_live, D, x_chunks, tw.p, t.p);
+  } else {
+    with_mode(mode, [&](auto M) {
+      auto kfn = dense_hot_kernel<decltype(M)::value>;
+      D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      D3G_LAUNCH(X, kfn, g, kHotThreads, sm, hp, in.dl_ptr, in.dl_col, dec, em, t.p);
+    });
+  }
   Tally h;
   X.to_host(&h, t.p, 1);
   // P2: cold residual join, hot-hit candidates filtered. With the warp-bitmap

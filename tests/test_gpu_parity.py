@@ -171,3 +171,17 @@ def test_cfg5_x_slice_matches_reference():
         (blk["count"][0], blk["sum"][0], blk["xor"][0])
     del rl, rr, sl, sr
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_tcgen05_hot_pass_matches_bit_sliced(cfg, monkeypatch):
+    """The tcgen05 kind::i8 hot pass (comparison kernel) counts exactly the
+    same dense pairs as the bit-sliced default."""
+    rl, rr = d3.generate(cfg, 0)
+    sl, sr = d3.generate(cfg, 1)
+    e = d3.EngineConfig(force=d3.Strategy.auto_select, count_only=True, memory_budget_bytes=64 << 30)
+    monkeypatch.delenv("D3G_HOT", raising=False)
+    a = d3.join_project(d3.RawTable(rl, rr), d3.RawTable(sl, sr), e, C).report
+    monkeypatch.setenv("D3G_HOT", "tc")
+    b = d3.join_project(d3.RawTable(rl, rr), d3.RawTable(sl, sr), e, C).report
+    assert (a.out_p, a.pairs_dense, a.pairs_sparse) == (b.out_p, b.pairs_dense, b.pairs_sparse)
