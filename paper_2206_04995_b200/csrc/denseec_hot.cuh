@@ -79,16 +79,26 @@ __global__ void hot_build_z_kernel(const uint64_t* __restrict__ dl_ptr,
 
 // Cold residual side: per y, dense row positions whose lists hold y at a
 // cold rank (y-major CSR, rows indexed by y code).
+// Rows of the cold CSR are keyed (variant, part, y). variant v in
+// [0, 2^var_bits) holds only the dense rows z whose hot mask avoids every rank
+// r < var_bits set in v: an x whose own top-var_bits mask is v can only get a
+// surviving (not hot-hit) candidate from such z, so it streams variant v.
 __global__ void cold_count_kernel(const uint64_t* __restrict__ dl_ptr,
                                   const uint32_t* __restrict__ dl_col, uint64_t n_dense, uint32_t K,
                                   const uint32_t* __restrict__ y_of_rank, uint32_t* __restrict__ cnt,
-                                  uint64_t y_card, uint32_t part_rows) {
+                                  uint64_t y_card, uint32_t part_rows, uint32_t parts,
+                                  const uint64_t* __restrict__ hz, uint32_t kw, uint32_t var_bits) {
+  const uint32_t nvar = 1u << var_bits, vmask = nvar - 1;
   for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < n_dense;
        i += (uint64_t)gridDim.x * (blockDim.x / 32)) {
-    const uint64_t base = (i / part_rows) * y_card;
+    const uint64_t part = i / part_rows;
+    const uint32_t zm = var_bits ? (uint32_t)(hz[i * kw] & vmask) : 0;
     for (uint64_t k = dl_ptr[i] + lane_id(); k < dl_ptr[i + 1]; k += 32) {
-      uint32_t r = dl_col[k];
-      if (r >= K) atomicAdd(&cnt[base + y_of_rank[r]], 1u);
+      const uint32_t r = dl_col[k];
+      if (r < K) continue;
+      const uint32_t y = y_of_rank[r];
+      for (uint32_t v = 0; v < nvar; ++v)
+        if ((zm & v) == 0) atomicAdd(&cnt[((uint64_t)v * parts + part) * y_card + y], 1u);
     }
   }
 }
@@ -98,13 +108,21 @@ __global__ void cold_scatter_kernel(const uint64_t* __restrict__ dl_ptr,
                                     uint32_t K, const uint32_t* __restrict__ y_of_rank,
                                     unsigned long long* __restrict__ cursor,
                                     uint32_t* __restrict__ out, uint64_t y_card,
-                                    uint32_t part_rows) {
+                                    uint32_t part_rows, uint32_t parts,
+                                    const uint64_t* __restrict__ hz, uint32_t kw,
+                                    uint32_t var_bits) {
+  const uint32_t nvar = 1u << var_bits, vmask = nvar - 1;
   for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < n_dense;
        i += (uint64_t)gridDim.x * (blockDim.x / 32)) {
-    const uint64_t base = (i / part_rows) * y_card;
+    const uint64_t part = i / part_rows;
+    const uint32_t zm = var_bits ? (uint32_t)(hz[i * kw] & vmask) : 0;
     for (uint64_t k = dl_ptr[i] + lane_id(); k < dl_ptr[i + 1]; k += 32) {
-      uint32_t r = dl_col[k];
-      if (r >= K) out[atomicAdd(&cursor[base + y_of_rank[r]], 1ull)] = (uint32_t)i;
+      const uint32_t r = dl_col[k];
+      if (r < K) continue;
+      const uint32_t y = y_of_rank[r];
+      for (uint32_t v = 0; v < nvar; ++v)
+        if ((zm & v) == 0)
+          out[atomicAdd(&cursor[((uint64_t)v * parts + part) * y_card + y], 1ull)] = (uint32_t)i;
     }
   }
 }
@@ -280,7 +298,8 @@ dense_cold_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
                   const uint64_t* __restrict__ cptr /* [parts][y_card] + 1 */,
                   const uint32_t* __restrict__ ccol, const uint4* __restrict__ ch,
                   const uint4* __restrict__ hx4 /* [X][2] */, uint64_t y_card, uint32_t parts,
-                  uint32_t part_rows, const uint32_t* __restrict__ dl_z, Decode dec, Emit em,
+                  uint32_t part_rows, uint32_t var_bits, const uint32_t* __restrict__ dl_z,
+                  Decode dec, Emit em,
                   unsigned int* __restrict__ next, Tally* tally) {
   extern __shared__ __align__(16) uint32_t cbm[];  // [kColdWarps][part_rows / 32]
   const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
@@ -298,8 +317,9 @@ dense_cold_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
     const uint32_t part = (uint32_t)(item / n_x);
     const uint32_t x = xs[item % n_x];
     const uint32_t zbase = part * part_rows;
-    const uint64_t* cp = cptr + (uint64_t)part * y_card;
     const uint4 a0 = hx4[2 * (uint64_t)x], a1 = hx4[2 * (uint64_t)x + 1];
+    const uint32_t v = a0.x & ((1u << var_bits) - 1);  // x's top-var_bits hot mask
+    const uint64_t* cp = cptr + ((uint64_t)v * parts + part) * y_card;
     bool touched = false;
     const uint64_t r0 = r_ptr[x], r1 = r_ptr[x + 1];
     for (uint64_t kb = r0; kb < r1; kb += 32) {

@@ -532,6 +532,12 @@ __global__ void k_estimate_kernel(const uint32_t* __restrict__ y_of_rank,
   }
 }
 
+__global__ void top_dr_kernel(const uint32_t* __restrict__ y_of_rank,
+                              const uint32_t* __restrict__ dR, uint64_t y_card,
+                              uint32_t* __restrict__ out) {
+  if (threadIdx.x < 3) out[threadIdx.x] = threadIdx.x < y_card ? dR[y_of_rank[threadIdx.x]] : 0;
+}
+
 void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g::Emit em,
                    KernelOut& out) {
   using namespace d3g;
@@ -639,10 +645,22 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
       parts = (uint32_t)((D + rows_cap - 1) / rows_cap);
       part_rows = (uint32_t)((((D + parts - 1) / parts) + 31) / 32 * 32);
     }
-    const uint64_t rows_key = (uint64_t)parts * Y;
+    // top-rank variants of the cold CSR (only for the warp-bitmap kernel): one
+    // bit per top rank that at least half of the live x contain (cfg2: ranks
+    // 0-2; cfg4's flatter Zipf(0.8): none)
+    uint32_t var_bits = 0;
+    if (cold_kernel_ok) {
+      DBuf<uint32_t> top = X.alloc<uint32_t>(3);
+      D3G_LAUNCH(X, top_dr_kernel, 1, 32, 0, in.y_of_rank, in.dR, Y, top.p);
+      uint32_t h[3];
+      X.to_host(h, top.p, 3);
+      while (var_bits < 3 && var_bits < Y && 2ull * h[var_bits] >= in.x_card) ++var_bits;
+    }
+    const uint64_t rows_key = ((uint64_t)1 << var_bits) * parts * Y;
     DBuf<uint32_t> cc = X.zeros<uint32_t>(rows_key);
     D3G_LAUNCH(X, cold_count_kernel, grid_for(D * 32, 256), 256, 0, in.dl_ptr, in.dl_col, D, K,
-               in.y_of_rank, cc.p, Y, part_rows);
+               in.y_of_rank, cc.p, Y, part_rows, parts,
+               reinterpret_cast<const uint64_t*>(hz.p), kw, var_bits);
     DBuf<uint64_t> cptr = X.alloc<uint64_t>(rows_key + 1);
     exclusive_scan<uint32_t>(X, cc.p, rows_key, cptr.p);
     const uint64_t cnnz = X.scalar(cptr.p + rows_key);
@@ -650,7 +668,8 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     DBuf<unsigned long long> cur = X.alloc<unsigned long long>(rows_key + 1);
     D3G_CUDA(cudaMemcpyAsync(cur.p, cptr.p, (rows_key + 1) * 8, cudaMemcpyDeviceToDevice, X.stream));
     D3G_LAUNCH(X, cold_scatter_kernel, grid_for(D * 32, 256), 256, 0, in.dl_ptr, in.dl_col, D, K,
-               in.y_of_rank, cur.p, ccol.p, Y, part_rows);
+               in.y_of_rank, cur.p, ccol.p, Y, part_rows, parts,
+               reinterpret_cast<const uint64_t*>(hz.p), kw, var_bits);
     if (cold_kernel_ok) {
       DBuf<uint4> ch = X.alloc<uint4>(2 * cnnz);
       if (cnnz)
@@ -665,7 +684,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
           D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
         D3G_LAUNCH(X, kfn, (unsigned)X.sm_count * 3, kColdWarps * 32, csm, xorder, n_live, in.r_ptr,
                    in.r_col, cptr.p, ccol.p, ch.p, reinterpret_cast<const uint4*>(hx.p), Y, parts,
-                   part_rows, in.dl_z, dec, em, next.p, tc.p);
+                   part_rows, var_bits, in.dl_z, dec, em, next.p, tc.p);
       });
       Tally hc;
       X.to_host(&hc, tc.p, 1);
