@@ -41,6 +41,9 @@ WORKLOADS = {
        "1e5 y, y~Zipf(0.8), seed 4",
     5: "cfg5: R,S 200,000,000 tuples each, x,z~U[0,1e7), y~Zipf(1.2) over [0,1e6), seed 5",
 }
+# workloads whose f1 cost-model gate is positive: auto runs the classical
+# hash join in both the reference and this engine (cfg3 f1=+15.67)
+CLASSICAL_CFGS = {3}
 METRIC = "input tuples/sec and distinct (x,z) pairs/sec at 1/2/4/8 B200 vs roofline"
 L2_BYTES = 126 * 1024 * 1024
 
@@ -151,6 +154,15 @@ def cpu_reference_sample(cfg: int, frac: float, threads: int, tables=None):
         s = O.gen(cfg, 1)
     else:
         r, s = tables
+    if cfg in CLASSICAL_CFGS:
+        # the reference's own f1 gate sends this workload to hash_join_dedup
+        # (engine.cpp:368-384); time the whole job through its public API
+        t0 = time.perf_counter()
+        d = O.ref_join_project(r, s, force="auto", threads=threads, count_only=True)
+        est = time.perf_counter() - t0
+        assert "classical" in str(d["strategy"]), "reference did not take the classical branch"
+        return est, {"x_slice": "all", "est_full_s": est, "strategy": "classical",
+                     "out_p": d["out_p"]}
     # x codes are natural for cfg 1/2/3/5 (identity), dictionary codes for cfg4;
     # slicing rows of r_by_x is the same either way. |X| is known from the
     # generator for natural keys; otherwise probe once.
@@ -163,6 +175,16 @@ def cpu_reference_sample(cfg: int, frac: float, threads: int, tables=None):
     est = t["sec_prep"] + t["sec_kernels"] * (x_rows / x_hi)
     detail = dict(t, x_slice=[0, x_hi], est_full_s=est)
     return est, detail
+
+
+def _sample_text(detail):
+    if detail.get("strategy") == "classical":
+        return ("whole job through the reference's join_project(auto) -> f1 gate -> "
+                "hash_join_dedup")
+    return (f"reference map/CSR/partition on the whole job + reference sparse_bmm/dense_ec "
+            f"on x rows {detail['x_slice']} of {detail['x_rows']}, kernels extrapolated "
+            f"linearly in x (prep {detail['sec_prep']:.2f}s, slice kernels "
+            f"{detail['sec_kernels']:.2f}s)")
 
 
 def run_reference(args):
@@ -190,9 +212,7 @@ def run_reference(args):
         "config": {"workload": WORKLOADS[cfg], "count_only": True, "force": "auto",
                    "consts": "test_consts()"},
         "cpu_baseline": {"value": value, "unit": "tuples/s", "cores": threads, "kind": "reference",
-                         "sample": f"reference prep (map/CSR/stats/partition) on the whole job + "
-                                   f"reference sparse_bmm/dense_ec on x rows {detail['x_slice']} "
-                                   f"of {detail['x_rows']}, kernel time extrapolated linearly in x"},
+                         "sample": _sample_text(detail)},
         "e2e": {"value": value, "unit": "tuples/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "detail": detail,
@@ -263,7 +283,7 @@ def main():
     dev_s = sum(r.ms_total for r in reps) * 1e-3
     phase = {k: sum(getattr(r, k) for r in reps) / len(reps)
              for k in ("ms_estimate", "ms_map", "ms_csr", "ms_stats", "ms_partition", "ms_sparse",
-                       "ms_dense", "ms_decode", "ms_total")}
+                       "ms_dense", "ms_decode", "ms_classical", "ms_total")}
     launches = sum(r.gpu_launches for r in reps)
     t = torch.tensor([dev_s, float(local_pairs), float(launches)], dtype=torch.float64,
                      device=dev)
@@ -300,12 +320,25 @@ def main():
     w_dense = None
     if ref_rep and world == 1:
         w_dense = 8 * ref_rep["dense_blocks_checked"] + ref_rep["dense_probes_done"]
+    # the global-set classical variant (D3G_CLASSICAL=global) has no pipeline phases
+    classical = r0.strategy == "classical" and phase["ms_map"] == 0
+    # classical hash join: read the four input columns once, build/probe the y
+    # groups, and one 8-byte CAS slot read+write per intermediate pair
+    b_cls = 2 * s_in * n_tuples + 8 * r0.intermediate_pairs * 2
     prep_ms = phase["ms_map"] + phase["ms_csr"] + phase["ms_stats"] + phase["ms_partition"]
     cand = {"map+csr+partition": prep_ms, "sparse_bmm": phase["ms_sparse"],
             "dense_ec": phase["ms_dense"]}
     dom = max(cand, key=cand.get)
     p_dense = r0.x_live * r0.dense_z  # pair tests: one existence answer per (live x, dense z)
-    if dom == "dense_ec":
+    if classical:
+        achieved = b_cls / (phase["ms_classical"] * 1e-3) / 1e9
+        roof = {"kernel": "classical hash_join_dedup (group scatter + dedup-set probe)",
+                "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": None,
+                "work": f"B_C = 16 B/input row + 16 B/intermediate pair = {b_cls:.4g} bytes "
+                        f"({r0.intermediate_pairs} intermediate pairs)",
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+    elif dom == "dense_ec":
         achieved = p_dense / (phase["ms_dense"] * 1e-3)
         roof = {"kernel": "dense_ec (hot bit-sliced pass + cold residual pass)", "bound": "int_alu",
                 "achieved": achieved / 1e12, "peak": alu / 1e12, "unit": "Tops/s",
@@ -375,11 +408,7 @@ def main():
                 est, detail = cpu_reference_sample(cfg_id, args.cpu_frac, threads)
                 cpu = {"value": n_tuples / est, "unit": "tuples/s", "cores": threads,
                        "kind": "reference",
-                       "sample": f"reference map/CSR/partition on the whole job + reference "
-                                 f"sparse_bmm/dense_ec on x rows {detail['x_slice']} of "
-                                 f"{detail['x_rows']}, kernels extrapolated linearly in x "
-                                 f"(prep {detail['sec_prep']:.2f}s, slice kernels "
-                                 f"{detail['sec_kernels']:.2f}s)",
+                       "sample": _sample_text(detail),
                        "est_full_job_s": est}
             else:
                 cpu = {"value": None, "unavailable": "oracle/_ref not built"}
@@ -399,7 +428,8 @@ def main():
         "roofline": roof, "phases": phases_roof, "phase_ms": phase,
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
         "clocks": clocks, "wall_s_timed": wall,
-        "report": {k: getattr(r0, k) for k in ("strategy", "f1_gate_classical", "dense_z",
+        "report": {k: getattr(r0, k) for k in ("strategy", "f1_gate_classical", "f1_value",
+                                                 "intermediate_pairs", "dense_z",
                                                  "sparse_z", "x_live", "out_j", "spa_inner_count",
                                                  "peak_bytes")},
     }

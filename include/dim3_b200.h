@@ -115,6 +115,9 @@ typedef struct {
   double ms_total, ms_h2d, ms_estimate, ms_map, ms_csr, ms_stats, ms_partition;
   double ms_sparse, ms_dense, ms_decode;
   uint64_t gpu_launches;      /* kernels launched by this call */
+  /* classical branch (hash_join_dedup, P/src/classical.cpp:111-210) */
+  uint64_t pairs_classical, intermediate_pairs;
+  double ms_classical;
 } d3g_report;
 
 /* Materialized output: caller-owned host (or device, on_device != 0)

@@ -82,7 +82,6 @@ struct Ctx {
   cudaEvent_t ev[24] = {};
   uint64_t launches = 0;
   uint64_t d2h_bytes = 0;  // device->host bytes read back by the current call
-  uint64_t* est_pinned = nullptr;  // pinned staging for the f1 samples
   uint64_t live_bytes = 0, peak_bytes = 0, budget = 0;
   int sm_count = kNumSMs;
   size_t smem_optin = 0;

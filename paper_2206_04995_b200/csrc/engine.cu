@@ -13,6 +13,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
+#include <functional>
 #include <limits>
 #include <string>
 #include <type_traits>
@@ -20,6 +21,7 @@
 #include <unordered_map>
 #include <vector>
 
+#include "classical.cuh"
 #include "datagen.cuh"
 #include "denseec.cuh"
 #include "denseec_hot.cuh"
@@ -53,98 +55,11 @@ int guarded(F&& f) {
 using d3g::Ctx;
 using d3g::DBuf;
 
-// estimate_out_j_raw (P/src/costmodel.cpp:375-423) for u64 columns, on host
-// copies of the y columns (exact path) or of the strided samples.
-uint64_t estimate_raw(const uint64_t* r_y, uint64_t nr, const uint64_t* s_y, uint64_t ns,
-                      uint64_t sr, uint64_t ss, uint64_t mr, uint64_t ms, bool exact) {
-  if (exact) {
-    std::unordered_map<uint64_t, uint64_t> counts;
-    counts.reserve(ns);
-    for (uint64_t i = 0; i < ns; ++i) counts[s_y[i]]++;
-    uint64_t sum = 0;
-    for (uint64_t i = 0; i < nr; ++i) {
-      auto it = counts.find(r_y[i]);
-      if (it != counts.end()) sum += it->second;
-    }
-    return sum;
-  }
-  // samples already gathered: r_y[i] = R.y[i * sr], s_y[i] = S.y[i * ss]
-  std::unordered_map<uint64_t, uint64_t> counts;
-  counts.reserve(ms);
-  for (uint64_t i = 0; i < ms; ++i) counts[s_y[i]]++;
-  unsigned __int128 hits = 0;
-  for (uint64_t i = 0; i < mr; ++i) {
-    auto it = counts.find(r_y[i]);
-    if (it != counts.end()) hits += it->second;
-  }
-  long double scaled = static_cast<long double>(static_cast<uint64_t>(hits)) *
-                       (static_cast<long double>(ns) / ms) *
-                       (static_cast<long double>(nr) / mr);
-  if (scaled > static_cast<long double>(std::numeric_limits<uint64_t>::max()))
-    return std::numeric_limits<uint64_t>::max();
-  return static_cast<uint64_t>(scaled);
-}
-
 __global__ void gather_stride_kernel(const uint64_t* __restrict__ src, uint64_t stride, uint64_t m,
                                      uint64_t* __restrict__ dst) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
        i += (uint64_t)gridDim.x * blockDim.x)
     dst[i] = src[i * stride];
-}
-
-// The f1 estimate only gates the classical branch, which this path reports
-// but does not take, so it runs OFF the critical path: the y samples (or the
-// whole y columns below the exact limit) are copied into a pinned buffer on
-// the stream, and a host thread waits for that copy and runs the reference's
-// hash counting while the GPU pipeline proceeds. get() joins it.
-struct EstimateJob {
-  std::thread th;
-  uint64_t result = 0;
-  cudaEvent_t ev = nullptr;
-  DBuf<uint64_t> dev;  // gathered samples (stream-ordered lifetime)
-  ~EstimateJob() {
-    if (th.joinable()) th.join();
-    if (ev) cudaEventDestroy(ev);
-  }
-  uint64_t get() {
-    if (th.joinable()) th.join();
-    return result;
-  }
-};
-
-void start_estimate(Ctx& X, const d3g_table* R, const d3g_table* S, const uint64_t* dRr,
-                    const uint64_t* dSr, EstimateJob& job) {
-  const uint64_t nr = R->n, ns = S->n;
-  if (nr == 0 || ns == 0) return;
-  const uint64_t exact_limit = 65536, sample_rows = 16384;
-  const bool exact = nr <= exact_limit && ns <= exact_limit;
-  const uint64_t ms = std::min(ns, sample_rows), mr = std::min(nr, sample_rows);
-  const uint64_t ss = exact ? 1 : ns / ms, sr = exact ? 1 : nr / mr;
-  const uint64_t cr = exact ? nr : mr, cs = exact ? ns : ms;
-  if (!R->on_device && !S->on_device) {
-    job.th = std::thread([=, &job] {
-      std::vector<uint64_t> hr(cr), hs(cs);
-      for (uint64_t i = 0; i < cr; ++i) hr[i] = R->right[i * sr];
-      for (uint64_t i = 0; i < cs; ++i) hs[i] = S->right[i * ss];
-      job.result = estimate_raw(hr.data(), nr, hs.data(), ns, sr, ss, mr, ms, exact);
-    });
-    return;
-  }
-  if (X.est_pinned == nullptr) D3G_CUDA(cudaMallocHost(&X.est_pinned, 2 * exact_limit * 8));
-  job.dev = X.alloc<uint64_t>(cr + cs);
-  D3G_LAUNCH(X, gather_stride_kernel, d3g::grid_for(cr, 256), 256, 0, dRr, sr, cr, job.dev.p);
-  D3G_LAUNCH(X, gather_stride_kernel, d3g::grid_for(cs, 256), 256, 0, dSr, ss, cs, job.dev.p + cr);
-  D3G_CUDA(cudaMemcpyAsync(X.est_pinned, job.dev.p, (cr + cs) * 8, cudaMemcpyDeviceToHost,
-                           X.stream));
-  X.d2h_bytes += (cr + cs) * 8;
-  D3G_CUDA(cudaEventCreateWithFlags(&job.ev, cudaEventDisableTiming));
-  D3G_CUDA(cudaEventRecord(job.ev, X.stream));
-  const uint64_t* buf = X.est_pinned;
-  cudaEvent_t ev = job.ev;
-  job.th = std::thread([=, &job] {
-    if (cudaEventSynchronize(ev) != cudaSuccess) return;
-    job.result = estimate_raw(buf, nr, buf + cr, ns, sr, ss, mr, ms, exact);
-  });
 }
 
 __global__ void live_flag_kernel(const uint64_t* __restrict__ row_ptr, uint64_t lo, uint64_t hi,
@@ -851,6 +766,155 @@ void build_dense_layout(Ctx& X, const d3g::DeviceCsr& rx, uint64_t max_mx,
   L.max_group_nnz = top;
 }
 
+// Materialized output: emit code pairs (emit runs the producing kernels in
+// kModeEmit), order them by (x, z) code, decode through the dictionaries
+// (identity when rev is null) in the caller's orientation, copy out.
+void materialize_pairs(Ctx& X, uint64_t total, const std::function<void(d3g::Emit)>& emit,
+                       const uint64_t* rev_x, const uint64_t* rev_z, bool swapped,
+                       d3g_pairs* pairs, d3g_report* rep) {
+  using namespace d3g;
+  if (pairs->cap < total)
+    throw ResourceError("output buffer holds " + std::to_string(pairs->cap) + " pairs, need " +
+                        std::to_string(total));
+  DBuf<uint32_t> ex = X.alloc<uint32_t>(total), ez = X.alloc<uint32_t>(total);
+  DBuf<unsigned long long> cur = X.zeros<unsigned long long>(1);
+  emit(Emit{ex.p, ez.p, cur.p, total});
+  DBuf<uint64_t> keys = X.alloc<uint64_t>(total);
+  DBuf<uint32_t> idx = X.alloc<uint32_t>(total);
+  if (total) {
+    D3G_LAUNCH(X, pair_key_kernel, grid_for(total, 256), 256, 0, ex.p, ez.p, total,
+               swapped ? 1 : 0, keys.p, idx.p);
+    radix_sort(X, keys.p, idx.p, total, 64);
+  }
+  DBuf<uint32_t> sx2 = X.alloc<uint32_t>(total), sz2 = X.alloc<uint32_t>(total);
+  if (total)
+    D3G_LAUNCH(X, permute_pairs_kernel, grid_for(total, 256), 256, 0, idx.p, total, ex.p, ez.p,
+               sx2.p, sz2.p);
+  DBuf<uint64_t> ox, oz;
+  uint64_t* dox = pairs->x;
+  uint64_t* doz = pairs->z;
+  if (!pairs->on_device) {
+    ox = X.alloc<uint64_t>(total);
+    oz = X.alloc<uint64_t>(total);
+    dox = ox.p;
+    doz = oz.p;
+  }
+  if (total)
+    D3G_LAUNCH(X, decode_pairs_kernel, grid_for(total, 256), 256, 0, sx2.p, sz2.p, total, rev_x,
+               rev_z, swapped ? 1 : 0, dox, doz);
+  if (!pairs->on_device && total) {
+    D3G_CUDA(cudaMemcpyAsync(pairs->x, ox.p, total * 8, cudaMemcpyDeviceToHost, X.stream));
+    D3G_CUDA(cudaMemcpyAsync(pairs->z, oz.p, total * 8, cudaMemcpyDeviceToHost, X.stream));
+    rep->d2h_bytes += total * 16;
+  }
+  pairs->n = total;
+}
+
+// estimate_out_j_raw on the device-resident y columns (see classical.cuh).
+uint64_t estimate_out_j_gpu(Ctx& X, const uint64_t* r_y, uint64_t nr, const uint64_t* s_y,
+                            uint64_t ns) {
+  using namespace d3g;
+  if (nr == 0 || ns == 0) return 0;
+  const uint64_t exact_limit = 65536, sample_rows = 16384;
+  const bool exact = nr <= exact_limit && ns <= exact_limit;
+  const uint64_t ms = exact ? ns : std::min(ns, sample_rows), mr = exact ? nr : std::min(nr, sample_rows);
+  const uint64_t ss = exact ? 1 : ns / ms, sr = exact ? 1 : nr / mr;
+  DBuf<uint64_t> smp = X.alloc<uint64_t>(mr + ms);
+  D3G_LAUNCH(X, gather_stride_kernel, grid_for(mr, 256), 256, 0, r_y, sr, mr, smp.p);
+  D3G_LAUNCH(X, gather_stride_kernel, grid_for(ms, 256), 256, 0, s_y, ss, ms, smp.p + mr);
+  uint64_t cap = 1024;
+  while (cap < 2 * ms) cap <<= 1;
+  DBuf<unsigned long long> keys = X.alloc<unsigned long long>(cap);
+  DBuf<uint32_t> used = X.zeros<uint32_t>(cap);
+  DBuf<unsigned int> counts = X.zeros<unsigned int>(cap);
+  DBuf<unsigned long long> hits = X.zeros<unsigned long long>(1);
+  D3G_LAUNCH(X, est_insert_kernel, grid_for(ms, 256), 256, 0, smp.p + mr, ms, keys.p, used.p,
+             counts.p, cap - 1);
+  D3G_LAUNCH(X, est_probe_kernel, grid_for(mr, 256), 256, 0, smp.p, mr, keys.p, used.p, counts.p,
+             cap - 1, hits.p);
+  const uint64_t h = X.scalar(hits.p);
+  if (exact) return h;
+  long double scaled = static_cast<long double>(h) * (static_cast<long double>(ns) / ms) *
+                       (static_cast<long double>(nr) / mr);
+  if (scaled > static_cast<long double>(std::numeric_limits<uint64_t>::max()))
+    return std::numeric_limits<uint64_t>::max();
+  return static_cast<uint64_t>(scaled);
+}
+
+// hash_join_dedup (P/src/classical.cpp:111-210) on the GPU, in engine
+// orientation; pairs swap back through decode.
+void classical_impl(Ctx& X, const uint64_t* Rl, const uint64_t* Rr, uint64_t NR,
+                    const uint64_t* Sl, const uint64_t* Sr, uint64_t NS, bool swapped, int mode,
+                    bool materialize, d3g_report* rep, d3g_pairs* pairs) {
+  using namespace d3g;
+  const bool trace = std::getenv("D3G_CLS_TRACE") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  auto tr = [&](const char* what) {
+    if (!trace) return;
+    X.sync();
+    auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[cls] %-10s %8.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  };
+  DictBundle D;
+  DBuf<uint32_t> s_y = X.alloc<uint32_t>(NS), s_z = X.alloc<uint32_t>(NS);
+  DBuf<uint32_t> r_y = X.alloc<uint32_t>(NR), keep = X.alloc<uint32_t>(NR);
+  DBuf<uint32_t> r_x = X.alloc<uint32_t>(NR);
+  dict_build(X, Sr, NS, D.y, s_y.p);  // y groups (FlatMap over S.y)
+  dict_build(X, Sl, NS, D.z, s_z.p);  // z interner
+  dict_build(X, Rl, NR, D.x, r_x.p);  // x interner
+  tr("dicts");
+  if (NR)
+    D3G_LAUNCH(X, dict_lookup_kernel, grid_for(NR, 256), 256, 0, Rr, NR, D.y.keys.p,
+               D.y.slot_code.p, D.y.mask, r_y.p, keep.p);
+  const uint64_t G = D.y.card;
+  DBuf<uint32_t> gcnt = X.zeros<uint32_t>(G);
+  if (NS) D3G_LAUNCH(X, group_hist_kernel, grid_for(NS, 256), 256, 0, s_y.p, NS, gcnt.p);
+  DBuf<uint64_t> gptr = X.alloc<uint64_t>(G + 1);
+  exclusive_scan<uint32_t>(X, gcnt.p, G, gptr.p);
+  if (G) D3G_CUDA(cudaMemsetAsync(gcnt.p, 0, G * 4, X.stream));
+  DBuf<uint32_t> gz = X.alloc<uint32_t>(NS);
+  if (NS)
+    D3G_LAUNCH(X, group_scatter_kernel, grid_for(NS, 256), 256, 0, s_y.p, s_z.p, NS, gptr.p,
+               gcnt.p, gz.p);
+  DBuf<unsigned long long> bag = X.zeros<unsigned long long>(1);
+  if (NR)
+    D3G_LAUNCH(X, classical_bag_kernel, grid_for(NR, 256), 256, 0, r_y.p, keep.p, NR, gptr.p,
+               bag.p);
+  const uint64_t inter = X.scalar(bag.p);
+  tr("groups");
+  rep->intermediate_pairs = inter;
+  uint64_t cap = 1024;
+  while (cap < 2 * inter) cap <<= 1;
+  DBuf<unsigned long long> set = X.alloc<unsigned long long>(cap);  // ResourceError if too big
+  Decode dec{rev_or_null(D.x), rev_or_null(D.z), swapped ? 1 : 0};
+  auto run = [&](int m, Emit em, Tally* t) {
+    D3G_CUDA(cudaMemsetAsync(set.p, 0xff, cap * 8, X.stream));
+    if (NR == 0) return;
+    const unsigned g = grid_for(NR * 32, 256, X.sm_count * 32);
+    with_mode(m, [&](auto M) {
+      D3G_LAUNCH(X, classical_probe_kernel<decltype(M)::value>, g, 256, 0, r_x.p, r_y.p, keep.p,
+                 NR, gptr.p, gz.p, set.p, cap - 1, dec, em, t);
+    });
+  };
+  tr("set alloc");
+  DBuf<Tally> t = X.zeros<Tally>(1);
+  run(mode, Emit{nullptr, nullptr, nullptr, 0}, t.p);
+  Tally h;
+  X.to_host(&h, t.p, 1);
+  tr("probe");
+  rep->pairs_classical = h.count;
+  rep->out_p = h.count;
+  rep->checksum_sum = h.sum;
+  rep->checksum_xor = h.xr;
+  if (materialize) {
+    DBuf<Tally> t2 = X.zeros<Tally>(1);
+    materialize_pairs(X, h.count, [&](Emit em) { run(kModeEmit, em, t2.p); }, rev_or_null(D.x),
+                      rev_or_null(D.z), swapped, pairs, rep);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // The pipeline.
 void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g_consts* c,
@@ -906,14 +970,36 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   }
   T.mark();  // 1
 
-  // 2. f1 gate (engine.cpp:368-384), evaluated concurrently (EstimateJob)
-  EstimateJob est;
-  start_estimate(X, R, S, Rr, Sr, est);
-  const char* strat = o->force == D3G_SPARSE_ONLY  ? "sparse"
-                      : o->force == D3G_DENSE_ONLY ? "dense"
-                                                   : "hybrid";
+  // 2. f1 gate (engine.cpp:368-384): auto takes the classical join iff f1 > 0
+  rep->out_j_estimate = estimate_out_j_gpu(X, Rr, NR, Sr, NS);
+  rep->f1 = d3g_f1(NR, NS, rep->out_j_estimate, c);
+  rep->f1_gate_classical = (o->force == D3G_AUTO && rep->f1 > 0) ? 1 : 0;
+  const bool classical = o->force == D3G_CLASSICAL || rep->f1_gate_classical;
+  const char* strat = classical                    ? "classical"
+                      : o->force == D3G_SPARSE_ONLY ? "sparse"
+                      : o->force == D3G_DENSE_ONLY  ? "dense"
+                                                    : "hybrid";
   std::snprintf(rep->strategy, sizeof(rep->strategy), "%s", strat);
   T.mark();  // 2
+  // On the GPU the classical branch runs x-partitioned: the y-grouped hash
+  // join is the sparse probe of the pipeline below with every z sparse, and
+  // the dedup is per x in shared memory instead of one global pair set. The
+  // global-set hash_join_dedup stays available (D3G_CLASSICAL=global).
+  const char* cls_env = std::getenv("D3G_CLASSICAL");
+  if (classical && cls_env && std::strcmp(cls_env, "global") == 0) {
+    classical_impl(X, Rl, Rr, NR, Sl, Sr, NS, swapped, o->checksum ? kModeChecksum : kModeCount,
+                   materialize, rep, pairs);
+    T.mark();  // 3
+    X.sync();
+    rep->ms_h2d = T.ms(0, 1);
+    rep->ms_estimate = T.ms(1, 2);
+    rep->ms_classical = T.ms(2, 3);
+    rep->ms_total = T.ms(0, 3);
+    rep->peak_bytes = X.peak_bytes - base_live;
+    rep->gpu_launches = X.launches;
+    rep->d2h_bytes += X.d2h_bytes;
+    return;
+  }
 
   // 3. natural-key resolution (engine.cpp:25-50, mapping.cpp:281-338)
   DBuf<ColStat> cs = X.zeros<ColStat>(4);
@@ -1015,6 +1101,15 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   rep->x_card = x_card;
   rep->y_card = y_card;
   rep->z_card = z_card;
+  if (classical) {  // intermediate_pairs = bag join size, duplicates included
+    DBuf<uint32_t> cnt = X.zeros<uint32_t>(y_card);
+    if (NS) D3G_LAUNCH(X, group_hist_kernel, grid_for(NS, 256), 256, 0, s_y.p, NS, cnt.p);
+    DBuf<unsigned long long> bag = X.zeros<unsigned long long>(1);
+    if (kept)
+      D3G_LAUNCH(X, bag_from_counts_kernel, grid_for(kept, 256), 256, 0, r_y.p, kept, cnt.p,
+                 bag.p);
+    rep->intermediate_pairs = X.scalar(bag.p);
+  }
   if (x_card >= (1ull << 32) || y_card >= (1ull << 32) || z_card >= (1ull << 32))
     throw ConfigError("code space exceeds 2^32");
   T.mark();  // 3
@@ -1078,7 +1173,7 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
 
   // 7. f2 decisions per degree value (policy.cpp), then the partition
   std::vector<uint8_t> table(max_mz + 1, 0);
-  int pforce = o->force == D3G_SPARSE_ONLY ? D3G_SPARSE_ONLY
+  int pforce = (classical || o->force == D3G_SPARSE_ONLY) ? D3G_SPARSE_ONLY
                : o->force == D3G_DENSE_ONLY ? D3G_DENSE_ONLY
                                             : D3G_HYBRID;
   uint64_t evals = 0;
@@ -1184,50 +1279,15 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   rep->checksum_xor = ks.xr ^ kd.xr;
 
   // 9. materialization (decode, engine.cpp:502-529)
-  if (materialize) {
-    uint64_t total = rep->out_p;
-    if (pairs->cap < total)
-      throw ResourceError("output buffer holds " + std::to_string(pairs->cap) + " pairs, need " +
-                          std::to_string(total));
-    DBuf<uint32_t> ex = X.alloc<uint32_t>(total), ez = X.alloc<uint32_t>(total);
-    DBuf<unsigned long long> cur = X.zeros<unsigned long long>(1);
-    Emit em{ex.p, ez.p, cur.p, total};
-    KernelOut tmp;
-    if (sparse_hot)
-      run_dense_hot(X, dsi, dec, kModeEmit, em, tmp);
-    else
-      run_sparse(X, si, dec, kModeEmit, em, tmp);
-    run_dense(X, di, dec, kModeEmit, em, tmp);
-    DBuf<uint64_t> keys = X.alloc<uint64_t>(total);
-    DBuf<uint32_t> idx = X.alloc<uint32_t>(total);
-    if (total) {
-      D3G_LAUNCH(X, pair_key_kernel, grid_for(total, 256), 256, 0, ex.p, ez.p, total,
-                 swapped ? 1 : 0, keys.p, idx.p);
-      radix_sort(X, keys.p, idx.p, total, 64);
-    }
-    DBuf<uint32_t> sx2 = X.alloc<uint32_t>(total), sz2 = X.alloc<uint32_t>(total);
-    if (total)
-      D3G_LAUNCH(X, permute_pairs_kernel, grid_for(total, 256), 256, 0, idx.p, total, ex.p, ez.p,
-                 sx2.p, sz2.p);
-    DBuf<uint64_t> ox, oz;
-    uint64_t* dox = pairs->x;
-    uint64_t* doz = pairs->z;
-    if (!pairs->on_device) {
-      ox = X.alloc<uint64_t>(total);
-      oz = X.alloc<uint64_t>(total);
-      dox = ox.p;
-      doz = oz.p;
-    }
-    if (total)
-      D3G_LAUNCH(X, decode_pairs_kernel, grid_for(total, 256), 256, 0, sx2.p, sz2.p, total,
-                 rev_or_null(D.x), rev_or_null(D.z), swapped ? 1 : 0, dox, doz);
-    if (!pairs->on_device && total) {
-      D3G_CUDA(cudaMemcpyAsync(pairs->x, ox.p, total * 8, cudaMemcpyDeviceToHost, X.stream));
-      D3G_CUDA(cudaMemcpyAsync(pairs->z, oz.p, total * 8, cudaMemcpyDeviceToHost, X.stream));
-      rep->d2h_bytes += total * 16;
-    }
-    pairs->n = total;
-  }
+  if (materialize)
+    materialize_pairs(X, rep->out_p, [&](Emit em) {
+      KernelOut tmp;
+      if (sparse_hot)
+        run_dense_hot(X, dsi, dec, kModeEmit, em, tmp);
+      else
+        run_sparse(X, si, dec, kModeEmit, em, tmp);
+      run_dense(X, di, dec, kModeEmit, em, tmp);
+    }, rev_or_null(D.x), rev_or_null(D.z), swapped, pairs, rep);
   T.mark();  // 9
   X.sync();
   rep->ms_h2d = T.ms(0, 1);
@@ -1240,9 +1300,10 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   rep->ms_dense = T.ms(7, 8);
   rep->ms_decode = T.ms(8, 9);
   rep->ms_total = T.ms(0, 9);
-  rep->out_j_estimate = est.get();
-  rep->f1 = d3g_f1(NR, NS, rep->out_j_estimate, c);
-  rep->f1_gate_classical = (o->force == D3G_AUTO && rep->f1 > 0) ? 1 : 0;
+  if (classical) {
+    rep->pairs_classical = rep->out_p;
+    rep->ms_classical = T.ms(2, 9);
+  }
   rep->peak_bytes = X.peak_bytes - base_live;
   rep->gpu_launches = X.launches;
   rep->d2h_bytes += X.d2h_bytes;
@@ -1296,7 +1357,6 @@ void d3g_ctx_destroy(d3g_ctx* ctx) {
   cudaSetDevice(ctx->c.device);
   cudaStreamSynchronize(ctx->c.stream);
   if (ctx->c.pinned) cudaFreeHost(ctx->c.pinned);
-  if (ctx->c.est_pinned) cudaFreeHost(ctx->c.est_pinned);
   cudaStreamDestroy(ctx->c.stream);
   delete ctx;
 }

@@ -217,7 +217,9 @@ class _Report(C.Structure):
                 ("natural_y", C.c_int32), ("natural_z", C.c_int32), ("materialized", C.c_int32)] + \
                [(k, C.c_uint64) for k in _REPORT_U64_A] + [("f1", C.c_double)] + \
                [(k, C.c_uint64) for k in _REPORT_U64_B] + \
-               [(k, C.c_double) for k in _REPORT_MS] + [("gpu_launches", C.c_uint64)]
+               [(k, C.c_double) for k in _REPORT_MS] + [("gpu_launches", C.c_uint64)] + \
+               [("pairs_classical", C.c_uint64), ("intermediate_pairs", C.c_uint64),
+                ("ms_classical", C.c_double)]
 
 
 class _Pairs(C.Structure):
@@ -394,6 +396,9 @@ class ExecutionReport:
     ms_dense: float = 0.0
     ms_decode: float = 0.0
     gpu_launches: int = 0
+    pairs_classical: int = 0
+    intermediate_pairs: int = 0
+    ms_classical: float = 0.0
 
     def to_kv(self):
         """Insertion-ordered key/value view with the reference's key names
@@ -401,17 +406,17 @@ class ExecutionReport:
         kv = [("strategy", self.strategy), ("swapped", "true" if self.swapped else "false"),
               ("r_rows", str(self.r_rows)), ("s_rows", str(self.s_rows)),
               ("out_j_estimate", str(self.out_j_estimate)), ("f1", f"{self.f1_value:.6g}"),
-              ("out_p", str(self.out_p)), ("pairs_classical", "0"),
+              ("out_p", str(self.out_p)), ("pairs_classical", str(self.pairs_classical)),
               ("pairs_sparse", str(self.pairs_sparse)), ("pairs_dense", str(self.pairs_dense)),
               ("pairs_cached", "0"), ("sparse_z", str(self.sparse_z)),
               ("dense_z", str(self.dense_z)), ("cached_z", "0"),
               ("f2_evaluations", str(self.f2_evaluations)), ("dropped_r", str(self.dropped_r)),
-              ("intermediate_pairs", "0"), ("x_card", str(self.x_card)),
+              ("intermediate_pairs", str(self.intermediate_pairs)), ("x_card", str(self.x_card)),
               ("y_card", str(self.y_card)), ("z_card", str(self.z_card)),
               ("panel_bytes", str(self.panel_bytes)), ("peak_bytes", str(self.peak_bytes)),
               ("spa_inner_count", str(self.spa_inner_count))]
         for k in ("ms_total", "ms_estimate", "ms_map", "ms_csr", "ms_partition", "ms_sparse",
-                  "ms_dense", "ms_decode"):
+                  "ms_dense", "ms_classical", "ms_decode"):
             kv.append((k, f"{getattr(self, k):.3f}"))
         for k in ("f1_gate_classical", "x_live", "out_j", "r_nnz", "s_nnz", "sparse_nnz",
                   "checksum_sum", "checksum_xor", "ms_h2d", "ms_stats", "gpu_launches"):

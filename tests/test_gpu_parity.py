@@ -9,7 +9,8 @@ from support import SplitMix64, oracle_pairs, pair_set, random_instance
 
 pytestmark = pytest.mark.gpu
 C = d3.CostConstants.test_consts()
-FORCES = [d3.Strategy.hybrid, d3.Strategy.sparse_only, d3.Strategy.dense_only, d3.Strategy.auto_select]
+FORCES = [d3.Strategy.hybrid, d3.Strategy.sparse_only, d3.Strategy.dense_only, d3.Strategy.classical,
+          d3.Strategy.auto_select]
 
 
 def _run(r, s, force, count_only=False, checksum=False, **kw):
@@ -127,8 +128,11 @@ def test_baseline_config_matches_reference(cfg):
         pytest.skip("golden entry not generated")
     rl, rr = d3.generate(cfg, 0)
     sl, sr = d3.generate(cfg, 1)
+    # cfg3 is f1-gated to the classical join under auto (covered below); the
+    # pipeline statistics of the golden record come from the DIM3 pipeline
+    force = d3.Strategy.hybrid if cfg == 3 else d3.Strategy.auto_select
     out = d3.join_project(d3.RawTable(rl, rr), d3.RawTable(sl, sr),
-                          d3.EngineConfig(force=d3.Strategy.auto_select, count_only=True,
+                          d3.EngineConfig(force=force, count_only=True,
                                           checksum=True, memory_budget_bytes=64 << 30), C)
     rep = out.report
     assert rep.out_p == g["set"]["count"]
@@ -185,3 +189,62 @@ def test_tcgen05_hot_pass_matches_bit_sliced(cfg, monkeypatch):
     monkeypatch.setenv("D3G_HOT", "tc")
     b = d3.join_project(d3.RawTable(rl, rr), d3.RawTable(sl, sr), e, C).report
     assert (a.out_p, a.pairs_dense, a.pairs_sparse) == (b.out_p, b.pairs_dense, b.pairs_sparse)
+
+
+def _bag(r, s):
+    """oracle_out_j_bag (P/tests/support.hpp:74-84)."""
+    ys, cnt = np.unique(s[1], return_counts=True)
+    d = dict(zip(ys.tolist(), cnt.tolist()))
+    return int(sum(d.get(y, 0) for y in r[1].tolist()))
+
+
+@pytest.mark.parametrize("variant", ["partitioned", "global"])
+def test_classical_branch_matches_reference(variant, monkeypatch):
+    """force=classical (hash_join_dedup, P/src/classical.cpp:111-210): same set,
+    intermediate_pairs = the bag join size, strategy named in the report. Both
+    GPU variants: x-partitioned (default) and the global pair-set dedup."""
+    if variant == "global":
+        monkeypatch.setenv("D3G_CLASSICAL", "global")
+    else:
+        monkeypatch.delenv("D3G_CLASSICAL", raising=False)
+    rng = SplitMix64(503)
+    for _ in range(10):
+        r, s = random_instance(rng)
+        out = _run(r, s, d3.Strategy.classical)
+        assert out.report.strategy == "classical"
+        assert pair_set(out.result.raw_x, out.result.raw_z) == oracle_pairs(r, s)
+        big, small = (r, s) if len(r[0]) >= len(s[0]) else (s, r)
+        assert out.report.intermediate_pairs == _bag(big, small)
+        assert out.report.pairs_classical == out.report.out_p
+
+
+def test_auto_gate_takes_classical_on_cfg3():
+    """cfg3 has f1 = +15.67 > 0: auto runs the classical join, like
+    the reference, and still produces the reference's set."""
+    g = _golden()["cfg3"]
+    rl, rr = d3.generate(3, 0)
+    sl, sr = d3.generate(3, 1)
+    out = d3.join_project(d3.RawTable(rl, rr), d3.RawTable(sl, sr),
+                          d3.EngineConfig(force=d3.Strategy.auto_select, count_only=True,
+                                          checksum=True, memory_budget_bytes=64 << 30), C)
+    rep = out.report
+    assert rep.strategy == "classical" and rep.f1_gate_classical and rep.f1_value > 0
+    assert (rep.out_p, rep.checksum_sum, rep.checksum_xor) == \
+        (g["set"]["count"], g["set"]["sum"], g["set"]["xor"])
+
+
+def test_classical_variants_agree_on_cfg3(monkeypatch):
+    """The global-set and x-partitioned classical variants give the same count,
+    fingerprint and bag join size on the full cfg3 workload."""
+    rl, rr = d3.generate(3, 0)
+    sl, sr = d3.generate(3, 1)
+    e = d3.EngineConfig(force=d3.Strategy.classical, count_only=True, checksum=True,
+                        memory_budget_bytes=64 << 30)
+    monkeypatch.delenv("D3G_CLASSICAL", raising=False)
+    a = d3.join_project(d3.RawTable(rl, rr), d3.RawTable(sl, sr), e, C).report
+    monkeypatch.setenv("D3G_CLASSICAL", "global")
+    b = d3.join_project(d3.RawTable(rl, rr), d3.RawTable(sl, sr), e, C).report
+    assert a.strategy == b.strategy == "classical"
+    assert (a.out_p, a.checksum_sum, a.checksum_xor, a.intermediate_pairs) == \
+        (b.out_p, b.checksum_sum, b.checksum_xor, b.intermediate_pairs)
+    assert a.pairs_classical == a.out_p
