@@ -87,7 +87,8 @@ typedef struct {
   int32_t collect_counters;   /* reference-equivalent DenseEC/SpA counters */
   int32_t shard_index;        /* x-range shard of R handled by this call */
   int32_t shard_count;        /* 1 = whole table */
-  int32_t pad0, pad1;
+  uint32_t x_code_lo;         /* restrict the kernels to engine x codes in */
+  uint32_t x_code_hi;         /* [lo, hi); hi = 0: all. Shards split the range */
 } d3g_opts;
 
 /* dim3::ExecutionReport (P/include/dim3/engine.hpp:59-85) flattened, plus

@@ -284,6 +284,21 @@ def ref_pipeline(r: Table, s: Table, consts=None):
     return d
 
 
+def ref_pipeline_split(r: Table, s: Table, consts=None):
+    """ref_pipeline's statistics and dense/sparse split without building the
+    panel (F2Evaluator decisions only)."""
+    lib = ref_lib()
+    rl, rr, sl, sr = (_u64(a) for a in (r.left, r.right, s.left, s.right))
+    c = make_consts(consts)
+    out = RefPipeline()
+    fn = lib.ref_pipeline_split
+    fn.argtypes = [U64P, U64P, C.c_uint64, U64P, U64P, C.c_uint64, C.c_void_p, C.c_void_p]
+    rc = fn(_p(rl), _p(rr), len(rl), _p(sl), _p(sr), len(sl), C.byref(c), C.byref(out))
+    if rc:
+        raise ConfigErrorLike(rc, lib.ref_last_error().decode())
+    return _struct_dict(out)
+
+
 def ref_set_checksum(r: Table, s: Table, threads=8, rows_per_slice=1024, block_width=0,
                      n_blocks=0):
     lib = ref_lib()

@@ -258,6 +258,53 @@ int ref_pipeline(const std::uint64_t* rl, const std::uint64_t* rr,
   }
 }
 
+// The same statistics as ref_pipeline with the partition DECISION taken by the
+// reference's own F2Evaluator (the loop of P/src/partition.cpp:17-38) but no
+// panel allocation, for inputs whose panel cannot be built (cfg5: 1.25 TB).
+int ref_pipeline_split(const std::uint64_t* rl, const std::uint64_t* rr,
+                       std::uint64_t nr, const std::uint64_t* sl,
+                       const std::uint64_t* sr, std::uint64_t ns,
+                       const RefConsts* consts, RefPipeline* out) {
+  try {
+    dim3::RawTable R0 = to_table(rl, rr, nr);
+    dim3::RawTable S0 = to_table(sl, sr, ns);
+    const bool swapped = dim3::engine_will_swap(R0, S0);
+    const dim3::RawTable& R = swapped ? S0 : R0;
+    const dim3::RawTable& S = swapped ? R0 : S0;
+    dim3::MappingOutput m = map_like_engine(R, S);
+    dim3::CsrMatrix r_by_x = dim3::build_csr(m.r, true);
+    dim3::CsrMatrix s_by_z = dim3::build_csr(m.s, true);
+    dim3::DegreeStats st = dim3::compute_degree_stats(r_by_x, s_by_z);
+    std::memset(out, 0, sizeof(*out));
+    dim3::F2Evaluator ev(st, to_consts(consts));
+    std::uint64_t dense_nnz = 0;
+    for (dim3::Code z = 0; z < s_by_z.n_rows; ++z) {
+      if (st.m_z[z] == 0) continue;
+      if (ev.score(z) > 0) {
+        out->dense_z++;
+        dense_nnz += st.m_z[z];
+      } else {
+        out->sparse_z++;
+      }
+    }
+    out->x_card = m.r.a_card;
+    out->y_card = m.s.b_card;
+    out->z_card = m.s.a_card;
+    out->r_nnz = r_by_x.nnz();
+    out->s_nnz = s_by_z.nnz();
+    out->out_j = st.out_j.value;
+    out->dropped_r = m.dropped_r;
+    out->sparse_nnz = s_by_z.nnz() - dense_nnz;
+    out->natural_x = m.dict_x.is_identity();
+    out->natural_y = m.dict_y.is_identity();
+    out->natural_z = m.dict_z.is_identity();
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return status_of(e);
+  }
+}
+
 // Order-independent fingerprint of the full distinct (x,z) set for outputs
 // too large to materialize: force=sparse partition, then
 // the reference sparse_bmm on row-sliced copies of r_by_x, decoded through

@@ -271,6 +271,163 @@ dense_hot_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
   tally_flush(tally, cnt, sum, xr);
 }
 
+// --- P1 with packed hot records (K <= 256) ---------------------------------
+// Each dense row's hot prefix is packed once into a 32-byte record of u8
+// ranks (first 32 hot ranks) plus its hot count. A warp then takes 32 rows per
+// step with ONE coalesced 1 KB load (lane j holds row j's record), prefetched a
+// step ahead, and broadcasts the ranks with one shuffle per 4 ranks. This
+// removes the per-row dependent dl_ptr -> dl_col global loads of the list
+// kernel above, which leave it latency-bound when the dense lists do not fit
+// in L2 (cfg5: 10M dense rows, 680 MB of lists re-read per batch).
+__global__ void hot_rec_kernel(const uint64_t* __restrict__ dl_ptr,
+                               const uint32_t* __restrict__ dl_col, uint64_t n_dense, uint32_t K,
+                               uint8_t* __restrict__ rec /* [D][32], zeroed */,
+                               uint32_t* __restrict__ rcnt) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_dense;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k0 = dl_ptr[i], k1 = dl_ptr[i + 1];
+    uint32_t c = 0;
+    for (uint64_t k = k0; k < k1; ++k) {
+      const uint32_t r = dl_col[k];
+      if (r >= K) break;  // ranks ascend: the hot prefix ended
+      if (c < 32) rec[i * 32 + c] = (uint8_t)r;
+      ++c;
+    }
+    rcnt[i] = c;
+  }
+}
+
+template <int kMode>
+__global__ void __launch_bounds__(kHotThreads, 1)
+dense_hot_rec_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
+                     const uint32_t* __restrict__ dl_col, const uint4* __restrict__ rec,
+                     const uint32_t* __restrict__ rcnt, Decode dec, Emit em, Tally* tally) {
+  extern __shared__ __align__(128) uint4 Ts[];  // [K][32]
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ unsigned int s_unit;
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const uint32_t n_batches = (p.groups + 31) / 32;
+  const unsigned int n_units = n_batches * p.z_chunks;
+  uint64_t cnt = 0, sum = 0, xr = 0;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  uint32_t phase = 0;
+  int cur_batch = -1;
+  const uint4 zero4 = make_uint4(0, 0, 0, 0);
+  for (;;) {
+    if (threadIdx.x == 0) s_unit = atomicAdd(p.work, 1u);
+    __syncthreads();
+    const unsigned int unit = s_unit;
+    if (unit >= n_units) break;
+    const uint32_t bi = unit / p.z_chunks, zc_i = unit % p.z_chunks;
+    if ((int)bi != cur_batch) {
+      if (threadIdx.x == 0) {
+        const uint32_t bytes = p.K * 32u * 16u;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&bar, bytes);
+        tma_bulk_g2s(Ts, p.T + (uint64_t)bi * p.K * 32, bytes, &bar);
+      }
+      mbar_wait(&bar, phase);
+      phase ^= 1;
+      cur_batch = (int)bi;
+    }
+    const uint32_t g = bi * 32 + lane;  // this lane's group
+    const uint64_t gp0 = (uint64_t)g * 128;
+    const uint64_t z_lo = p.n_dense * zc_i / p.z_chunks, z_hi = p.n_dense * (zc_i + 1) / p.z_chunks;
+    // software-pipelined 32-row steps: records of step s+1 load while s runs
+    uint64_t cb = z_lo + (uint64_t)warp * 32;
+    uint4 na = zero4, nb = zero4;
+    uint32_t nc = 0;
+    if (cb + lane < z_hi) {
+      na = rec[2 * (cb + lane)];
+      nb = rec[2 * (cb + lane) + 1];
+      nc = rcnt[cb + lane];
+    }
+    for (; cb < z_hi; cb += (uint64_t)nwarps * 32) {
+      const uint4 ra = na, rb = nb;
+      const uint32_t rc = nc;
+      const uint64_t nx = cb + (uint64_t)nwarps * 32 + lane;
+      na = zero4;
+      nb = zero4;
+      nc = 0;
+      if (nx < z_hi) {
+        na = rec[2 * nx];
+        nb = rec[2 * nx + 1];
+        nc = rcnt[nx];
+      }
+      const uint32_t rows = (uint32_t)((z_hi - cb) < 32 ? (z_hi - cb) : 32);
+      for (uint32_t j = 0; j < rows; ++j) {
+        const uint32_t c = __shfl_sync(0xffffffffu, rc, j);
+        uint4 acc = zero4;
+        const uint32_t words[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (4u * q < c) {
+            const uint32_t wv = __shfl_sync(0xffffffffu, words[q], j);
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              if (4u * q + b < c) {
+                const uint32_t r = (wv >> (8 * b)) & 0xffu;
+                const uint4 v = Ts[r * 32 + lane];
+                acc.x |= v.x;
+                acc.y |= v.y;
+                acc.z |= v.z;
+                acc.w |= v.w;
+              }
+            }
+          }
+        }
+        const uint64_t i = cb + j;
+        if (c > 32) {  // rare: hot prefix longer than one record
+          const uint64_t k0 = dl_ptr[i] + 32, k1 = dl_ptr[i] + c;
+          for (uint64_t base = k0; base < k1; base += 32) {
+            const uint32_t mine = base + lane < k1 ? dl_col[base + lane] : 0u;
+            const uint32_t n = (uint32_t)((k1 - base) < 32 ? (k1 - base) : 32);
+            for (uint32_t t = 0; t < n; ++t) {
+              const uint32_t r = __shfl_sync(0xffffffffu, mine, t);
+              const uint4 v = Ts[r * 32 + lane];
+              acc.x |= v.x;
+              acc.y |= v.y;
+              acc.z |= v.z;
+              acc.w |= v.w;
+            }
+          }
+        }
+        const uint32_t hits = __popc(acc.x) + __popc(acc.y) + __popc(acc.z) + __popc(acc.w);
+        cnt += hits;
+        if (kMode != kModeCount && hits) {
+          const uint32_t zc = p.dl_z[i];
+          const uint32_t ws[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+          for (int wi = 0; wi < 4; ++wi) {
+            uint32_t bits = ws[wi];
+            while (bits) {
+              const int b = __ffs(bits) - 1;
+              bits &= bits - 1;
+              const uint32_t xc = p.xorder[gp0 + wi * 32 + b];
+              if (kMode == kModeChecksum) {
+                const uint64_t h = dec.hash(xc, zc);
+                sum += h;
+                xr ^= h;
+              } else {
+                const unsigned long long idx = atomicAdd(em.cursor, 1ull);
+                if (idx < em.cap) {
+                  em.x[idx] = xc;
+                  em.z[idx] = zc;
+                }
+              }
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();  // Ts may be overwritten by the next unit's copy
+  }
+  tally_flush(tally, cnt, sum, xr);
+}
 
 // P2 kernel: cold residual for a dense block whose row count fits a per-warp
 // shared-memory bitmap. One warp per live x. The cold CSR (y-major, rows =
@@ -367,6 +524,172 @@ dense_cold_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
     if (__any_sync(0xffffffffu, touched))
       for (uint32_t i = lane; i < pw; i += 32) bm[i] = 0;
     __syncwarp();
+  }
+  tally_flush(tally, cnt, sum, xr);
+}
+
+// P2 for dense blocks too large for per-warp bitmaps (cfg5: 10M dense rows).
+// Same candidate stream as dense_cold_kernel (variant-selected cold CSR with
+// inline 256-bit hot signatures), but the survivors of x are deduplicated in a
+// warp-private shared-memory hash set: after the hot filter and the variant
+// cut, an x keeps only a few hundred candidates. An x whose survivors exceed
+// kCHMax abandons the hash (nothing of it was counted) and is queued for
+// dense_cold_overflow_kernel. Count, fingerprint and emission are taken from
+// the hash table when x completes, so abandoning is exact.
+constexpr int kCHWarps = 8;
+constexpr uint32_t kCHSlots = 2048;  // per warp (8 KB)
+constexpr uint32_t kCHMax = 1536;    // load limit; < kCHSlots - 32 keeps probing finite
+constexpr uint32_t kCHEmpty = 0xffffffffu;
+
+__device__ __forceinline__ uint32_t ch_slot(uint32_t v) { return (v * 0x9E3779B1u) >> 21; }
+
+template <int kMode>
+__device__ __forceinline__ void cold_account(uint32_t x, uint32_t zc, const Decode& dec,
+                                             const Emit& em, uint64_t& sum, uint64_t& xr) {
+  if (kMode == kModeChecksum) {
+    const uint64_t h = dec.hash(x, zc);
+    sum += h;
+    xr ^= h;
+  } else if (kMode == kModeEmit) {
+    const unsigned long long idx = atomicAdd(em.cursor, 1ull);
+    if (idx < em.cap) {
+      em.x[idx] = x;
+      em.z[idx] = zc;
+    }
+  }
+}
+
+template <int kMode>
+__global__ void __launch_bounds__(kCHWarps * 32)
+dense_cold_hash_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
+                       const uint64_t* __restrict__ r_ptr, const uint32_t* __restrict__ r_col,
+                       const uint64_t* __restrict__ cptr, const uint32_t* __restrict__ ccol,
+                       const uint4* __restrict__ ch, const uint4* __restrict__ hx4,
+                       uint64_t y_card, uint32_t var_bits, const uint32_t* __restrict__ dl_z,
+                       Decode dec, Emit em, unsigned int* __restrict__ next,
+                       uint32_t* __restrict__ over_x, unsigned int* __restrict__ over_n,
+                       Tally* tally) {
+  extern __shared__ __align__(16) uint32_t chtab[];  // [kCHWarps][kCHSlots]
+  const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
+  uint32_t* tab = chtab + (uint64_t)w * kCHSlots;
+  for (uint32_t i = lane; i < kCHSlots; i += 32) tab[i] = kCHEmpty;
+  __syncwarp();
+  uint64_t cnt = 0, sum = 0, xr = 0;
+  for (;;) {
+    uint32_t item = 0;
+    if (lane == 0) item = atomicAdd(next, 1u);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= n_x) break;
+    const uint32_t x = xs[item];
+    const uint4 a0 = hx4[2 * (uint64_t)x], a1 = hx4[2 * (uint64_t)x + 1];
+    const uint32_t v = a0.x & ((1u << var_bits) - 1);
+    const uint64_t* cp = cptr + (uint64_t)v * y_card;
+    uint32_t inserted = 0;  // warp-uniform
+    bool over = false;
+    const uint64_t r0 = r_ptr[x], r1 = r_ptr[x + 1];
+    for (uint64_t kb = r0; kb < r1 && !over; kb += 32) {
+      const uint64_t kk = kb + lane;
+      uint64_t seg0 = 0, seg1 = 0;
+      if (kk < r1) {
+        const uint32_t y = r_col[kk];
+        seg0 = cp[y];
+        seg1 = cp[y + 1];
+      }
+      const uint32_t nseg = (uint32_t)((r1 - kb) < 32 ? (r1 - kb) : 32);
+      for (uint32_t j = 0; j < nseg && !over; ++j) {
+        const uint64_t s0 = __shfl_sync(0xffffffffu, seg0, j);
+        const uint64_t s1 = __shfl_sync(0xffffffffu, seg1, j);
+        for (uint64_t tb = s0; tb < s1; tb += 32) {
+          const uint64_t t = tb + lane;
+          bool fresh = false;
+          if (t < s1) {
+            const uint4 b0 = ch[2 * t], b1 = ch[2 * t + 1];
+            const bool hot = ((a0.x & b0.x) | (a0.y & b0.y) | (a0.z & b0.z) | (a0.w & b0.w) |
+                              (a1.x & b1.x) | (a1.y & b1.y) | (a1.z & b1.z) | (a1.w & b1.w)) != 0;
+            if (!hot) {
+              const uint32_t zl = ccol[t];
+              uint32_t sl = ch_slot(zl);
+              for (;;) {
+                const uint32_t prev = atomicCAS(&tab[sl], kCHEmpty, zl);
+                if (prev == kCHEmpty) {
+                  fresh = true;
+                  break;
+                }
+                if (prev == zl) break;
+                sl = (sl + 1) & (kCHSlots - 1);
+              }
+            }
+          }
+          inserted += __popc(__ballot_sync(0xffffffffu, fresh));
+          if (inserted > kCHMax) {
+            over = true;
+            break;
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (over) {
+      if (lane == 0) over_x[atomicAdd(over_n, 1u)] = x;
+    } else {
+      cnt += lane == 0 ? inserted : 0;
+    }
+    if (inserted) {
+      for (uint32_t i = lane; i < kCHSlots; i += 32) {
+        const uint32_t zl = tab[i];
+        if (zl != kCHEmpty) {
+          if (kMode != kModeCount && !over) cold_account<kMode>(x, dl_z[zl], dec, em, sum, xr);
+          tab[i] = kCHEmpty;
+        }
+      }
+    }
+    __syncwarp();
+  }
+  tally_flush(tally, cnt, sum, xr);
+}
+
+// Overflow x of dense_cold_hash_kernel: one CTA per x over a CTA-private
+// global bitmap of the dense rows (zero on entry and on exit: the candidate
+// stream is replayed to clear exactly the bits it set).
+template <int kMode>
+__global__ void __launch_bounds__(512)
+dense_cold_overflow_kernel(const uint32_t* __restrict__ over_x, const unsigned int* __restrict__ over_n,
+                           const uint64_t* __restrict__ r_ptr, const uint32_t* __restrict__ r_col,
+                           const uint64_t* __restrict__ cptr, const uint32_t* __restrict__ ccol,
+                           const uint4* __restrict__ ch, const uint4* __restrict__ hx4,
+                           uint64_t y_card, uint32_t var_bits, const uint32_t* __restrict__ dl_z,
+                           uint32_t* __restrict__ gbm, uint64_t words, Decode dec, Emit em,
+                           Tally* tally) {
+  uint32_t* bm = gbm + (uint64_t)blockIdx.x * words;
+  const uint32_t n = *over_n;
+  uint64_t cnt = 0, sum = 0, xr = 0;
+  for (uint32_t it = blockIdx.x; it < n; it += gridDim.x) {
+    const uint32_t x = over_x[it];
+    const uint4 a0 = hx4[2 * (uint64_t)x], a1 = hx4[2 * (uint64_t)x + 1];
+    const uint32_t v = a0.x & ((1u << var_bits) - 1);
+    const uint64_t* cp = cptr + (uint64_t)v * y_card;
+    for (int pass = 0; pass < 2; ++pass) {
+      for (uint64_t k = r_ptr[x]; k < r_ptr[x + 1]; ++k) {
+        const uint32_t y = r_col[k];
+        const uint64_t s0 = cp[y], s1 = cp[y + 1];
+        for (uint64_t t = s0 + threadIdx.x; t < s1; t += blockDim.x) {
+          const uint4 b0 = ch[2 * t], b1 = ch[2 * t + 1];
+          const bool hot = ((a0.x & b0.x) | (a0.y & b0.y) | (a0.z & b0.z) | (a0.w & b0.w) |
+                            (a1.x & b1.x) | (a1.y & b1.y) | (a1.z & b1.z) | (a1.w & b1.w)) != 0;
+          if (hot) continue;
+          const uint32_t zl = ccol[t];
+          if (pass == 0) {
+            const uint32_t bit = 1u << (zl & 31);
+            if (atomicOr(&bm[zl >> 5], bit) & bit) continue;
+            ++cnt;
+            if (kMode != kModeCount) cold_account<kMode>(x, dl_z[zl], dec, em, sum, xr);
+          } else {
+            bm[zl >> 5] = 0;
+          }
+        }
+      }
+      __syncthreads();
+    }
   }
   tally_flush(tally, cnt, sum, xr);
 }

@@ -132,6 +132,7 @@ struct SparseInputs {
 struct KernelOut {
   uint64_t count = 0, sum = 0, xr = 0;
   uint64_t inner = 0;
+  uint64_t cold_overflow = 0;  // x handed to the overflow kernel (diagnostics)
 };
 
 template <class F>
@@ -487,7 +488,13 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   // the warp-bitmap cold kernel carries 256-bit hot signatures: K = 256
   // (the dense rows are split into at most 16 bitmap partitions, see P2)
   const uint64_t cold_rows_cap = std::max<uint64_t>(32, (budget / 3 / kColdWarps) * 8 / 32 * 32);
-  const bool cold_kernel_ok = k_cap >= 256 && (D + cold_rows_cap - 1) / cold_rows_cap <= 16;
+  const bool cold_bitmap = k_cap >= 256 && (D + cold_rows_cap - 1) / cold_rows_cap <= 16;
+  // larger dense blocks: the same candidate stream, survivors in a per-warp
+  // hash set (dense_cold_hash_kernel); D3G_COLD=tiers keeps the SparseBMM tiers
+  const char* cold_env = std::getenv("D3G_COLD");
+  const bool cold_hash = !cold_bitmap && k_cap >= 256 &&
+                         !(cold_env && std::string(cold_env) == "tiers");
+  const bool cold_kernel_ok = cold_bitmap || cold_hash;
   if (cold_kernel_ok) K = 256;
   const uint32_t kw = (K + 63) / 64;
   const uint32_t n_batches = (groups + 31) / 32;
@@ -539,6 +546,18 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
     D3G_LAUNCH(X, kfn, (unsigned)std::min<uint64_t>((uint64_t)n_zt * x_chunks, X.sm_count),
                kTcThreads, tsm, A.p, B.p, K, n_xt, n_zt, n_live, D, x_chunks, tw.p, t.p);
+  } else if (K <= 256 && !(hot_impl && std::string(hot_impl) == "list")) {
+    // packed hot records (default; D3G_HOT=list selects the list kernel)
+    DBuf<uint4> rec = X.zeros<uint4>(2 * D);
+    DBuf<uint32_t> rcnt = X.alloc<uint32_t>(D);
+    D3G_LAUNCH(X, hot_rec_kernel, grid_for(D, 256), 256, 0, in.dl_ptr, in.dl_col, D, K,
+               reinterpret_cast<uint8_t*>(rec.p), rcnt.p);
+    with_mode(mode, [&](auto M) {
+      auto kfn = dense_hot_rec_kernel<decltype(M)::value>;
+      D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      D3G_LAUNCH(X, kfn, g, kHotThreads, sm, hp, in.dl_ptr, in.dl_col, rec.p, rcnt.p, dec, em,
+                 t.p);
+    });
   } else {
     with_mode(mode, [&](auto M) {
       auto kfn = dense_hot_kernel<decltype(M)::value>;
@@ -554,7 +573,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   KernelOut cold;
   if (e[best] > 0) {
     uint32_t parts = 1, part_rows = (uint32_t)(((D + 31) / 32) * 32);
-    if (cold_kernel_ok) {
+    if (cold_bitmap) {
       const uint64_t per_warp = budget / 3 / kColdWarps;  // 3 CTAs of 8 warps per SM
       const uint64_t rows_cap = std::max<uint64_t>(32, per_warp * 8 / 32 * 32);
       parts = (uint32_t)((D + rows_cap - 1) / rows_cap);
@@ -592,6 +611,31 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
                    reinterpret_cast<const uint4*>(hz.p), ch.p);
       DBuf<unsigned int> next = X.zeros<unsigned int>(1);
       DBuf<Tally> tc = X.zeros<Tally>(1);
+      if (cold_hash) {
+        DBuf<uint32_t> over_x = X.alloc<uint32_t>(n_live);
+        DBuf<unsigned int> over_n = X.zeros<unsigned int>(1);
+        const size_t hsm = (size_t)kCHWarps * kCHSlots * 4;
+        with_mode(mode, [&](auto M) {
+          auto kfn = dense_cold_hash_kernel<decltype(M)::value>;
+          D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
+          D3G_LAUNCH(X, kfn, (unsigned)X.sm_count * 3, kCHWarps * 32, hsm, xorder, n_live,
+                     in.r_ptr, in.r_col, cptr.p, ccol.p, ch.p, reinterpret_cast<const uint4*>(hx.p),
+                     Y, var_bits, in.dl_z, dec, em, next.p, over_x.p, over_n.p, tc.p);
+        });
+        const unsigned int n_over = X.scalar(over_n.p);
+        out.cold_overflow = n_over;
+        if (n_over) {
+          const unsigned og = std::min<unsigned>(n_over, (unsigned)X.sm_count * 2);
+          const uint64_t words = (D + 31) / 32;
+          DBuf<uint32_t> gbm = X.zeros<uint32_t>((uint64_t)og * words);
+          with_mode(mode, [&](auto M) {
+            D3G_LAUNCH(X, dense_cold_overflow_kernel<decltype(M)::value>, og, 512, 0, over_x.p,
+                       over_n.p, in.r_ptr, in.r_col, cptr.p, ccol.p, ch.p,
+                       reinterpret_cast<const uint4*>(hx.p), Y, var_bits, in.dl_z, gbm.p, words,
+                       dec, em, tc.p);
+          });
+        }
+      } else {
       size_t csm = (size_t)(part_rows / 32) * 4 * kColdWarps;
       with_mode(mode, [&](auto M) {
         auto kfn = dense_cold_kernel<decltype(M)::value>;
@@ -601,6 +645,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
                    in.r_col, cptr.p, ccol.p, ch.p, reinterpret_cast<const uint4*>(hx.p), Y, parts,
                    part_rows, var_bits, in.dl_z, dec, em, next.p, tc.p);
       });
+      }
       Tally hc;
       X.to_host(&hc, tc.p, 1);
       cold.count = hc.count;
@@ -612,6 +657,12 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
       run_sparse(X, si, dec, mode, em, cold, flt);
     }
   }
+  if (std::getenv("D3G_TRACE"))
+    std::fprintf(stderr, "[dense_hot] D=%llu live=%llu K=%u hot=%llu cold=%llu cold_path=%s over=%llu\n",
+                 (unsigned long long)D, (unsigned long long)n_live, K, (unsigned long long)h.count,
+                 (unsigned long long)cold.count,
+                 cold_bitmap ? "bitmap" : cold_hash ? "hash" : "tiers",
+                 (unsigned long long)out.cold_overflow);
   out.count = h.count + cold.count;
   out.sum = h.sum + cold.sum;
   out.xr = h.xr ^ cold.xr;
@@ -698,7 +749,8 @@ void build_dense_layout(Ctx& X, const d3g::DeviceCsr& rx, uint64_t max_mx,
                         const std::vector<uint64_t>& hmx, const uint64_t* zrow_ptr,
                         const uint32_t* zcol, const uint32_t* row_ids, uint64_t n_dense,
                         uint64_t max_mz, const uint32_t* z_of_row, uint64_t y_card,
-                        const uint32_t* dR, DenseLayout& L) {
+                        const uint32_t* dR, DenseLayout& L, uint64_t xa = 0,
+                        uint64_t xb = ~0ull) {
   using namespace d3g;
   L.n_dense = n_dense;
   // y ranked by dR descending (ties by code): hottest witnesses first
@@ -739,15 +791,20 @@ void build_dense_layout(Ctx& X, const d3g::DeviceCsr& rx, uint64_t max_mx,
   if (z_of_row) D3G_LAUNCH(X, map_through_kernel, grid_for(n_dense, 256), 256, 0, rows.p, n_dense, z_of_row);
   L.dl_z = std::move(rows);
   // live x ordered by m_x descending, cut into 128-x groups
-  const uint64_t x_card = rx.n_rows;
+  // (restricted to x codes in [xa, xb) when the caller asked for an x range)
+  if (xb > rx.n_rows) xb = rx.n_rows;
+  if (xa > xb) xa = xb;
+  const uint64_t x_card = xb - xa;
   DBuf<uint32_t> lf = X.alloc<uint32_t>(x_card);
-  if (x_card) D3G_LAUNCH(X, live_flag_kernel, grid_for(x_card, 256), 256, 0, rx.row_ptr.p, 0ull, x_card, lf.p);
+  if (x_card) D3G_LAUNCH(X, live_flag_kernel, grid_for(x_card, 256), 256, 0, rx.row_ptr.p, xa, xb, lf.p);
   DBuf<uint64_t> lp = X.alloc<uint64_t>(x_card + 1);
   exclusive_scan<uint32_t>(X, lf.p, x_card, lp.p);
   L.n_live = X.scalar(lp.p + x_card);
   DBuf<uint32_t> live_ids = X.alloc<uint32_t>(L.n_live);
   if (x_card)
     D3G_LAUNCH(X, index_compact_kernel, grid_for(x_card, 256), 256, 0, lf.p, lp.p, x_card, live_ids.p);
+  if (xa && L.n_live)
+    D3G_LAUNCH(X, add_offset_kernel, grid_for(L.n_live, 256), 256, 0, live_ids.p, L.n_live, (uint32_t)xa);
   {
     DBuf<uint64_t> k = X.alloc<uint64_t>(L.n_live);
     L.xorder = X.alloc<uint32_t>(L.n_live);
@@ -1177,6 +1234,15 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
                : o->force == D3G_DENSE_ONLY ? D3G_DENSE_ONLY
                                             : D3G_HYBRID;
   uint64_t evals = 0;
+  if (const char* dump = std::getenv("D3G_DUMP_F2")) {  // debugging aid: the f2 inputs
+    if (FILE* f = std::fopen(dump, "wb")) {
+      uint64_t hdr[6] = {max_mx + 1, max_mz + 1, x_card, y_card, z_card, rep->out_j};
+      std::fwrite(hdr, 8, 6, f);
+      std::fwrite(hmx.data(), 8, max_mx + 1, f);
+      std::fwrite(hmz.data(), 8, max_mz + 1, f);
+      std::fclose(f);
+    }
+  }
   d3g_f2_decide(hmx.data(), max_mx + 1, hmz.data(), max_mz + 1, x_card, y_card, z_card,
                 rep->out_j, c, pforce, table.data(), &evals);
   rep->f2_evaluations = evals;
@@ -1224,9 +1290,12 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   }
   // dense side
   DenseLayout L;
+  // optional x-code restriction of the kernels (opts x_code_lo/hi)
+  const uint64_t xa = o->x_code_hi ? std::min<uint64_t>(o->x_code_lo, x_card) : 0;
+  const uint64_t xb = o->x_code_hi ? std::min<uint64_t>(o->x_code_hi, x_card) : x_card;
   if (n_dense > 0 && x_live > 0)
     build_dense_layout(X, rx, max_mx, hmx, sz_csr.row_ptr.p, sz_csr.col.p, dense_ids.p, n_dense,
-                       max_mz, nullptr, y_card, dR.p, L);
+                       max_mz, nullptr, y_card, dR.p, L, xa, xb);
   // Heavy sparse side (OUT_J,sparse > 4096 per live x over > 8192 sparse z,
   // e.g. cfg4's 9.7e10 candidates): answer it with the same hot bit-sliced +
   // cold residual engine, restricted to the sparse z set. The result is the
@@ -1242,7 +1311,7 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   DenseLayout Ls;
   if (sparse_hot)
     build_dense_layout(X, rx, max_mx, hmx, sz_csr.row_ptr.p, sz_csr.col.p, sparse_ids.p, n_sparse,
-                       max_mz, nullptr, y_card, dR.p, Ls);
+                       max_mz, nullptr, y_card, dR.p, Ls, xa, xb);
   T.mark();  // 6
 
   // 8. kernels
@@ -1250,7 +1319,8 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   const int mode = o->checksum ? kModeChecksum : kModeCount;
   Emit no_emit{nullptr, nullptr, nullptr, 0};
   // x shard (x code range for SparseBMM, position range for DenseEC)
-  uint64_t x_lo = x_card * shard_index / shard_count, x_hi = x_card * (shard_index + 1) / shard_count;
+  uint64_t x_lo = xa + (xb - xa) * shard_index / shard_count,
+           x_hi = xa + (xb - xa) * (shard_index + 1) / shard_count;
   SparseInputs si{rx.row_ptr.p, rx.col.p, x_card, sp_ptr.p, sp_col.p, sparse_ids.p, n_sparse,
                   y_card, x_lo, x_hi};
   KernelOut ks, kd;

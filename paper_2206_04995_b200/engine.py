@@ -133,6 +133,9 @@ class EngineConfig:
     checksum: bool = False        # also compute the (sum, xor) set fingerprint
     shard_index: int = 0          # x-range shard handled by this call
     shard_count: int = 1
+    # restrict the SparseBMM/DenseEC kernels to engine x codes in [lo, hi)
+    # (None: all). Statistics and f2 decisions stay global; shards split it.
+    x_code_range: tuple | None = None
 
 
 class RawTable:
@@ -197,7 +200,7 @@ class _Opts(C.Structure):
                 ("natural_keys_auto", C.c_int32), ("declared_x", C.c_int32),
                 ("declared_y", C.c_int32), ("declared_z", C.c_int32), ("checksum", C.c_int32),
                 ("collect_counters", C.c_int32), ("shard_index", C.c_int32),
-                ("shard_count", C.c_int32), ("pad0", C.c_int32), ("pad1", C.c_int32)]
+                ("shard_count", C.c_int32), ("x_code_lo", C.c_uint32), ("x_code_hi", C.c_uint32)]
 
 
 _REPORT_U64_A = ["r_rows", "s_rows", "out_j_estimate"]
@@ -452,10 +455,13 @@ def _opts(cfg: EngineConfig) -> _Opts:
         raise ConfigError("collect_cache_stats belongs to the partial-result cache, which is "
                           "outside this operator's scope")
     d = cfg.natural_keys_declared
+    xr = cfg.x_code_range or (0, 0)
+    if len(xr) != 2 or not (0 <= xr[0] <= xr[1] < (1 << 32)):
+        raise ConfigError("x_code_range must be (lo, hi) with 0 <= lo <= hi < 2^32")
     return _Opts(int(cfg.force), int(cfg.threads), int(cfg.memory_budget_bytes),
                  int(cfg.count_only), int(cfg.dense_mode), int(cfg.natural_keys_auto),
                  int(d.x), int(d.y), int(d.z), int(cfg.checksum), 0, int(cfg.shard_index),
-                 int(cfg.shard_count), 0, 0)
+                 int(cfg.shard_count), int(xr[0]), int(xr[1]))
 
 
 def join_project(r: RawTable, s: RawTable, cfg: EngineConfig, c: CostConstants,

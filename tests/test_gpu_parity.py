@@ -248,3 +248,39 @@ def test_classical_variants_agree_on_cfg3(monkeypatch):
     assert (a.out_p, a.checksum_sum, a.checksum_xor, a.intermediate_pairs) == \
         (b.out_p, b.checksum_sum, b.checksum_xor, b.intermediate_pairs)
     assert a.pairs_classical == a.out_p
+
+
+@pytest.mark.parametrize("cold", ["hash", "tiers"])
+def test_cfg5_full_pipeline_x_range_matches_reference(cold, monkeypatch):
+    """Full cfg5 (200M x 200M, no swap, 9,993,304 dense z as in the reference)
+    with the kernels restricted to x codes [0, 1000) and to 100-x blocks: the
+    pairs of those x are exactly the reference's x<1000 slice set (golden).
+    Exercises the hash-deduplicated cold pass (10M dense rows) and, for
+    comparison, the SparseBMM-tier cold pass."""
+    import torch
+    g = _golden().get("cfg5_x_lt_1000")
+    if g is None:
+        pytest.skip("golden entry not generated")
+    if cold == "tiers":
+        monkeypatch.setenv("D3G_COLD", "tiers")
+    else:
+        monkeypatch.delenv("D3G_COLD", raising=False)
+    rl, rr = d3.generate(5, 0)
+    sl, sr = d3.generate(5, 1)
+
+    def run(lo, hi):
+        e = d3.EngineConfig(force=d3.Strategy.auto_select, count_only=True, checksum=True,
+                            memory_budget_bytes=120 << 30, x_code_range=(lo, hi))
+        return d3.join_project(d3.RawTable(rl, rr), d3.RawTable(sl, sr), e, C).report
+
+    rep = run(0, 1000)
+    assert not rep.swapped and rep.dense_z == 9993304 and rep.sparse_z == 6696
+    assert (rep.out_p, rep.checksum_sum, rep.checksum_xor) == \
+        (g["set"]["count"], g["set"]["sum"], g["set"]["xor"])
+    blk = g["blocks"]
+    for b in (0, 9):
+        r = run(100 * b, 100 * (b + 1))
+        assert (r.out_p, r.checksum_sum, r.checksum_xor) == \
+            (blk["count"][b], blk["sum"][b], blk["xor"][b])
+    del rl, rr, sl, sr
+    torch.cuda.empty_cache()
