@@ -279,21 +279,27 @@ dense_hot_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
 // removes the per-row dependent dl_ptr -> dl_col global loads of the list
 // kernel above, which leave it latency-bound when the dense lists do not fit
 // in L2 (cfg5: 10M dense rows, 680 MB of lists re-read per batch).
+// With tb > 0 the ranks below tb are not listed; their presence mask goes to
+// bits 24.. of the count word instead (table kernel below).
 __global__ void hot_rec_kernel(const uint64_t* __restrict__ dl_ptr,
                                const uint32_t* __restrict__ dl_col, uint64_t n_dense, uint32_t K,
-                               uint8_t* __restrict__ rec /* [D][32], zeroed */,
+                               uint32_t tb, uint8_t* __restrict__ rec /* [D][32], zeroed */,
                                uint32_t* __restrict__ rcnt) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_dense;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t k0 = dl_ptr[i], k1 = dl_ptr[i + 1];
-    uint32_t c = 0;
+    uint32_t c = 0, top = 0;
     for (uint64_t k = k0; k < k1; ++k) {
       const uint32_t r = dl_col[k];
       if (r >= K) break;  // ranks ascend: the hot prefix ended
+      if (r < tb) {
+        top |= 1u << r;
+        continue;
+      }
       if (c < 32) rec[i * 32 + c] = (uint8_t)r;
       ++c;
     }
-    rcnt[i] = c;
+    rcnt[i] = c | (top << 24);
   }
 }
 
@@ -389,6 +395,171 @@ dense_hot_rec_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
             for (uint32_t t = 0; t < n; ++t) {
               const uint32_t r = __shfl_sync(0xffffffffu, mine, t);
               const uint4 v = Ts[r * 32 + lane];
+              acc.x |= v.x;
+              acc.y |= v.y;
+              acc.z |= v.z;
+              acc.w |= v.w;
+            }
+          }
+        }
+        const uint32_t hits = __popc(acc.x) + __popc(acc.y) + __popc(acc.z) + __popc(acc.w);
+        cnt += hits;
+        if (kMode != kModeCount && hits) {
+          const uint32_t zc = p.dl_z[i];
+          const uint32_t ws[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+          for (int wi = 0; wi < 4; ++wi) {
+            uint32_t bits = ws[wi];
+            while (bits) {
+              const int b = __ffs(bits) - 1;
+              bits &= bits - 1;
+              const uint32_t xc = p.xorder[gp0 + wi * 32 + b];
+              if (kMode == kModeChecksum) {
+                const uint64_t h = dec.hash(xc, zc);
+                sum += h;
+                xr ^= h;
+              } else {
+                const unsigned long long idx = atomicAdd(em.cursor, 1ull);
+                if (idx < em.cap) {
+                  em.x[idx] = xc;
+                  em.z[idx] = zc;
+                }
+              }
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();  // Ts may be overwritten by the next unit's copy
+  }
+  tally_flush(tally, cnt, sum, xr);
+}
+
+// --- P1 with a subset table over the top ranks -----------------------------
+// The top kTabBits ranks sit in most dense rows (cfg5: rank 0 in 95% of rows,
+// rank 1 in 70%). Per batch, shared memory holds OR-combinations of their
+// slices for every subset (2^kTabBits rows of 512 B, built in kTabBits-1
+// rounds from the single-rank rows that TMA drops at the power-of-two
+// entries), followed by the slices of ranks kTabBits..K-1. A dense row then
+// costs ONE LDS.128 for its whole top-rank subset plus one per further hot
+// rank. Records list only the ranks >= kTabBits; the subset mask rides in bits
+// 24.. of the count word.
+constexpr uint32_t kTabBits = 7;
+constexpr uint32_t kTabRows = 1u << kTabBits;
+
+template <int kMode>
+__global__ void __launch_bounds__(kHotThreads, 1)
+dense_hot_tab_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
+                     const uint32_t* __restrict__ dl_col, const uint4* __restrict__ rec,
+                     const uint32_t* __restrict__ rcnt, Decode dec, Emit em, Tally* tally) {
+  extern __shared__ __align__(128) uint4 Ts[];  // [kTabRows + K - kTabBits][32]
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ unsigned int s_unit;
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const uint32_t n_batches = (p.groups + 31) / 32;
+  const unsigned int n_units = n_batches * p.z_chunks;
+  uint64_t cnt = 0, sum = 0, xr = 0;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  if (threadIdx.x < 32) Ts[threadIdx.x] = make_uint4(0, 0, 0, 0);  // entry 0: empty subset
+  __syncthreads();
+  uint32_t phase = 0;
+  int cur_batch = -1;
+  const uint4 zero4 = make_uint4(0, 0, 0, 0);
+  // rank r >= kTabBits lives at row kTabRows + (r - kTabBits)
+  const uint4* rows_hi = Ts + (kTabRows - kTabBits) * 32 + lane;
+  for (;;) {
+    if (threadIdx.x == 0) s_unit = atomicAdd(p.work, 1u);
+    __syncthreads();
+    const unsigned int unit = s_unit;
+    if (unit >= n_units) break;
+    const uint32_t bi = unit / p.z_chunks, zc_i = unit % p.z_chunks;
+    if ((int)bi != cur_batch) {
+      if (threadIdx.x == 0) {
+        const uint4* src = p.T + (uint64_t)bi * p.K * 32;
+        const uint32_t hi_bytes = (p.K - kTabBits) * 32u * 16u;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&bar, hi_bytes + kTabBits * 512u);
+        for (uint32_t b = 0; b < kTabBits; ++b)
+          tma_bulk_g2s(Ts + (1u << b) * 32, src + b * 32, 512u, &bar);
+        tma_bulk_g2s(Ts + kTabRows * 32, src + kTabBits * 32, hi_bytes, &bar);
+      }
+      mbar_wait(&bar, phase);
+      phase ^= 1;
+      cur_batch = (int)bi;
+      // subset rows: round b fills (2^b, 2^(b+1)) from 2^b and the lower rows
+      for (uint32_t b = 1; b < kTabBits; ++b) {
+        const uint32_t lo = 1u << b, n = (lo - 1) * 32;
+        for (uint32_t t = threadIdx.x; t < n; t += blockDim.x) {
+          const uint32_t e = lo + 1 + (t >> 5), l = t & 31;
+          const uint4 a = Ts[lo * 32 + l], c = Ts[(e - lo) * 32 + l];
+          Ts[e * 32 + l] = make_uint4(a.x | c.x, a.y | c.y, a.z | c.z, a.w | c.w);
+        }
+        __syncthreads();
+      }
+    }
+    const uint32_t g = bi * 32 + lane;  // this lane's group
+    const uint64_t gp0 = (uint64_t)g * 128;
+    const uint64_t z_lo = p.n_dense * zc_i / p.z_chunks, z_hi = p.n_dense * (zc_i + 1) / p.z_chunks;
+    uint64_t cb = z_lo + (uint64_t)warp * 32;
+    uint4 na = zero4, nb = zero4;
+    uint32_t nc = 0;
+    if (cb + lane < z_hi) {
+      na = rec[2 * (cb + lane)];
+      nb = rec[2 * (cb + lane) + 1];
+      nc = rcnt[cb + lane];
+    }
+    for (; cb < z_hi; cb += (uint64_t)nwarps * 32) {
+      const uint4 ra = na, rb = nb;
+      const uint32_t rc = nc;
+      const uint64_t nx = cb + (uint64_t)nwarps * 32 + lane;
+      na = zero4;
+      nb = zero4;
+      nc = 0;
+      if (nx < z_hi) {
+        na = rec[2 * nx];
+        nb = rec[2 * nx + 1];
+        nc = rcnt[nx];
+      }
+      const uint32_t rows = (uint32_t)((z_hi - cb) < 32 ? (z_hi - cb) : 32);
+      for (uint32_t j = 0; j < rows; ++j) {
+        const uint32_t cw = __shfl_sync(0xffffffffu, rc, j);
+        const uint32_t c = cw & 0xffffffu, top = cw >> 24;
+        uint4 acc = Ts[top * 32 + lane];  // entry 0 is the empty subset
+        const uint32_t words[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (4u * q < c) {
+            const uint32_t wv = __shfl_sync(0xffffffffu, words[q], j);
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              if (4u * q + b < c) {
+                const uint32_t r = (wv >> (8 * b)) & 0xffu;
+                const uint4 v = rows_hi[r * 32];
+                acc.x |= v.x;
+                acc.y |= v.y;
+                acc.z |= v.z;
+                acc.w |= v.w;
+              }
+            }
+          }
+        }
+        const uint64_t i = cb + j;
+        if (c > 32) {  // rare: more than 32 listed ranks; the tail is in the list
+          const uint64_t k1 = dl_ptr[i + 1];
+          uint64_t k = dl_ptr[i];
+          // skip the top ranks and the 32 listed ones
+          const uint32_t skip = __popc(top) + 32;
+          const uint64_t kend = k + skip + (c - 32);
+          k += skip;
+          for (uint64_t base = k; base < kend && base < k1; base += 32) {
+            const uint32_t mine = base + lane < kend ? dl_col[base + lane] : 0u;
+            const uint32_t n = (uint32_t)((kend - base) < 32 ? (kend - base) : 32);
+            for (uint32_t t = 0; t < n; ++t) {
+              const uint32_t r = __shfl_sync(0xffffffffu, mine, t);
+              const uint4 v = rows_hi[r * 32];
               acc.x |= v.x;
               acc.y |= v.y;
               acc.z |= v.z;

@@ -547,16 +547,27 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     D3G_LAUNCH(X, kfn, (unsigned)std::min<uint64_t>((uint64_t)n_zt * x_chunks, X.sm_count),
                kTcThreads, tsm, A.p, B.p, K, n_xt, n_zt, n_live, D, x_chunks, tw.p, t.p);
   } else if (K <= 256 && !(hot_impl && std::string(hot_impl) == "list")) {
-    // packed hot records (default; D3G_HOT=list selects the list kernel)
+    // packed hot records (default; D3G_HOT=list selects the list kernel), with
+    // the top-rank subset table when it fits (D3G_HOT=rec disables it)
+    const size_t tsm = (size_t)(kTabRows + K - kTabBits) * 32 * 16;
+    const bool tab = K > kTabBits && tsm <= (size_t)dense_smem_bytes(X) &&
+                     !(hot_impl && std::string(hot_impl) == "rec");
     DBuf<uint4> rec = X.zeros<uint4>(2 * D);
     DBuf<uint32_t> rcnt = X.alloc<uint32_t>(D);
     D3G_LAUNCH(X, hot_rec_kernel, grid_for(D, 256), 256, 0, in.dl_ptr, in.dl_col, D, K,
-               reinterpret_cast<uint8_t*>(rec.p), rcnt.p);
+               tab ? kTabBits : 0u, reinterpret_cast<uint8_t*>(rec.p), rcnt.p);
     with_mode(mode, [&](auto M) {
-      auto kfn = dense_hot_rec_kernel<decltype(M)::value>;
-      D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      D3G_LAUNCH(X, kfn, g, kHotThreads, sm, hp, in.dl_ptr, in.dl_col, rec.p, rcnt.p, dec, em,
-                 t.p);
+      if (tab) {
+        auto kfn = dense_hot_tab_kernel<decltype(M)::value>;
+        D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
+        D3G_LAUNCH(X, kfn, g, kHotThreads, tsm, hp, in.dl_ptr, in.dl_col, rec.p, rcnt.p, dec, em,
+                   t.p);
+      } else {
+        auto kfn = dense_hot_rec_kernel<decltype(M)::value>;
+        D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        D3G_LAUNCH(X, kfn, g, kHotThreads, sm, hp, in.dl_ptr, in.dl_col, rec.p, rcnt.p, dec, em,
+                   t.p);
+      }
     });
   } else {
     with_mode(mode, [&](auto M) {
