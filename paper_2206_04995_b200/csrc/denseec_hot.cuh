@@ -529,23 +529,44 @@ dense_hot_tab_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
         const uint32_t c = cw & 0xffffffu, top = cw >> 24;
         uint4 acc = Ts[top * 32 + lane];  // entry 0 is the empty subset
         const uint32_t words[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
+        // row address = rows_hi + rank * 512 B: PRMT pulls the rank byte out,
+        // one LEA-style add forms the address; full words OR two slices per
+        // 3-input LOP3
+        const char* hb = reinterpret_cast<const char*>(rows_hi);
+#define D3G_ROW(wv, b) \
+  (*reinterpret_cast<const uint4*>(hb + (__byte_perm((wv), 0u, 0x4440u + (b)) << 9)))
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          if (4u * q < c) {
+          if (4u * q + 4 <= c) {
             const uint32_t wv = __shfl_sync(0xffffffffu, words[q], j);
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-              if (4u * q + b < c) {
-                const uint32_t r = (wv >> (8 * b)) & 0xffu;
-                const uint4 v = rows_hi[r * 32];
-                acc.x |= v.x;
-                acc.y |= v.y;
-                acc.z |= v.z;
-                acc.w |= v.w;
-              }
-            }
+            const uint4 v0 = D3G_ROW(wv, 0), v1 = D3G_ROW(wv, 1);
+            const uint4 v2 = D3G_ROW(wv, 2), v3 = D3G_ROW(wv, 3);
+            acc.x |= v0.x | v1.x;
+            acc.y |= v0.y | v1.y;
+            acc.z |= v0.z | v1.z;
+            acc.w |= v0.w | v1.w;
+            acc.x |= v2.x | v3.x;
+            acc.y |= v2.y | v3.y;
+            acc.z |= v2.z | v3.z;
+            acc.w |= v2.w | v3.w;
+          } else if (4u * q < c) {
+            const uint32_t wv = __shfl_sync(0xffffffffu, words[q], j);
+            const uint32_t left = c - 4u * q;  // 1..3
+            const uint4 v0 = D3G_ROW(wv, 0);
+            uint4 v1 = make_uint4(0, 0, 0, 0), v2 = make_uint4(0, 0, 0, 0);
+            if (left > 1) v1 = D3G_ROW(wv, 1);
+            if (left > 2) v2 = D3G_ROW(wv, 2);
+            acc.x |= v0.x | v1.x;
+            acc.y |= v0.y | v1.y;
+            acc.z |= v0.z | v1.z;
+            acc.w |= v0.w | v1.w;
+            acc.x |= v2.x;
+            acc.y |= v2.y;
+            acc.z |= v2.z;
+            acc.w |= v2.w;
           }
         }
+#undef D3G_ROW
         const uint64_t i = cb + j;
         if (c > 32) {  // rare: more than 32 listed ranks; the tail is in the list
           const uint64_t k1 = dl_ptr[i + 1];
