@@ -496,7 +496,12 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
                          !(cold_env && std::string(cold_env) == "tiers");
   const bool cold_kernel_ok = cold_bitmap || cold_hash;
   if (cold_kernel_ok) K = 256;
-  const uint32_t kw = (K + 63) / 64;
+  if (const char* kenv = std::getenv("D3G_K")) {  // experiments: force the hot width
+    const uint32_t k = (uint32_t)std::strtoul(kenv, nullptr, 10);
+    if (k >= 64 && k % 64 == 0 && k <= (cold_kernel_ok ? 256u : k_cap)) K = k;
+  }
+  // the cold kernels read 256-bit hot signatures: keep that layout for K < 256
+  const uint32_t kw = cold_kernel_ok ? 4u : (K + 63) / 64;
   const uint32_t n_batches = (groups + 31) / 32;
   // hot structures
   DBuf<uint4> T = X.zeros<uint4>((uint64_t)n_batches * K * 32);
