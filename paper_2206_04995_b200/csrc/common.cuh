@@ -83,6 +83,7 @@ struct Ctx {
   uint64_t launches = 0;
   uint64_t d2h_bytes = 0;  // device->host bytes read back by the current call
   uint64_t live_bytes = 0, peak_bytes = 0, budget = 0;
+  uint64_t reserved = 0;  // size of the largest block pre-faulted into the pool
   int sm_count = kNumSMs;
   size_t smem_optin = 0;
   // small pinned host staging area for scalars read back mid-pipeline
@@ -127,6 +128,22 @@ struct Ctx {
     return b;
   }
   void sync() { D3G_CUDA(cudaStreamSynchronize(stream)); }
+  // After a call whose working set outgrew the pool's largest block, fault in
+  // one block of (peak + 25%) and return it to the pool: the stream-ordered
+  // allocator then carves later calls' buffers out of it instead of mapping
+  // new physical memory mid-pipeline (which stalls the stream for ms).
+  void reserve_for(uint64_t peak) {
+    if (peak <= reserved) return;
+    const uint64_t want = peak + peak / 4 + (64ull << 20);
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, want, stream) != cudaSuccess) {
+      cudaGetLastError();
+      return;
+    }
+    cudaFreeAsync(p, stream);
+    sync();
+    reserved = want;
+  }
   // Copies n device values to host (through pinned staging) and syncs.
   template <class T>
   void to_host(T* dst, const T* src, uint64_t n) {

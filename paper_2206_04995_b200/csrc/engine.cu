@@ -1071,6 +1071,7 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
     rep->peak_bytes = X.peak_bytes - base_live;
     rep->gpu_launches = X.launches;
     rep->d2h_bytes += X.d2h_bytes;
+    X.reserve_for(X.peak_bytes);
     return;
   }
 
@@ -1078,10 +1079,22 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   DBuf<ColStat> cs = X.zeros<ColStat>(4);
   const uint64_t* cols[4] = {Rl, Rr, Sl, Sr};
   const uint64_t lens[4] = {NR, NR, NS, NS};
-  for (int i = 0; i < 4; ++i)
-    if (lens[i])
-      D3G_LAUNCH(X, colstat_kernel, grid_for(lens[i], 256, X.sm_count * 4), 256, 0, cols[i],
-                 lens[i], cs.p + i);
+  // one pass over the four columns: statistics + speculative u32 codes
+  DBuf<uint32_t> nar = X.alloc<uint32_t>(2 * NR + 2 * NS);
+  uint32_t* ncol[4] = {nar.p, nar.p + NR, nar.p + 2 * NR, nar.p + 2 * NR + NS};
+  {
+    Cols4 c4{};
+    for (int i = 0; i < 4; ++i) {
+      c4.col[i] = cols[i];
+      c4.n[i] = lens[i];
+      c4.narrow[i] = ncol[i];
+    }
+    const uint64_t mx = std::max(NR, NS);
+    if (mx) {
+      dim3 grid(grid_for(mx, 256, X.sm_count * 4), 4);
+      D3G_LAUNCH(X, colstat4_kernel, grid, 256, 0, c4, cs.p);
+    }
+  }
   ColStat hs[4];
   X.to_host(hs, cs.p, 4);
   auto det = [&](int i) { return lens[i] > 0 && hs[i].sample_fail == 0; };
@@ -1110,64 +1123,72 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   rep->natural_y = sy;
   rep->natural_z = sz;
 
-  // 4. mapping (map_tables, mapping.cpp:342-420)
+  // 4. mapping (map_tables, mapping.cpp:342-420). Natural columns use the
+  // narrowed codes of the statistics pass; the others go through dictionaries.
   DictBundle D;
-  DBuf<uint32_t> s_y = X.alloc<uint32_t>(NS), s_z = X.alloc<uint32_t>(NS);
+  DBuf<uint32_t> s_y_own, s_z_own, r_y_own, r_x_own;
+  const uint32_t *s_y = ncol[3], *s_z = ncol[2], *r_y = ncol[1], *r_x = ncol[0];
   uint64_t y_card, z_card, x_card;
   if (sy) {
     uint64_t a = NS ? hs[3].max + 1 : 0, b = NR ? hs[1].max + 1 : 0;
     y_card = std::max(a, b);
     D.y.identity = true;
     D.y.card = y_card;
-    if (NS) D3G_LAUNCH(X, narrow_kernel, grid_for(NS, 256), 256, 0, Sr, NS, s_y.p);
   } else {
-    dict_build(X, Sr, NS, D.y, s_y.p);
+    s_y_own = X.alloc<uint32_t>(NS);
+    dict_build(X, Sr, NS, D.y, s_y_own.p);
+    s_y = s_y_own.p;
     y_card = D.y.card;
   }
   if (sz) {
     z_card = NS ? hs[2].max + 1 : 0;
     D.z.identity = true;
     D.z.card = z_card;
-    if (NS) D3G_LAUNCH(X, narrow_kernel, grid_for(NS, 256), 256, 0, Sl, NS, s_z.p);
   } else {
-    dict_build(X, Sl, NS, D.z, s_z.p);
+    s_z_own = X.alloc<uint32_t>(NS);
+    dict_build(X, Sl, NS, D.z, s_z_own.p);
+    s_z = s_z_own.p;
     z_card = D.z.card;
   }
-  // R pass: semi-join filter on y, then x over the survivors
-  DBuf<uint32_t> r_y = X.alloc<uint32_t>(NR), keep = X.alloc<uint32_t>(NR);
-  if (NR) {
-    if (sy)
-      D3G_LAUNCH(X, identity_keep_kernel, grid_for(NR, 256), 256, 0, Rr, NR, y_card, r_y.p, keep.p);
-    else
-      D3G_LAUNCH(X, dict_lookup_kernel, grid_for(NR, 256), 256, 0, Rr, NR, D.y.keys.p,
-                 D.y.slot_code.p, D.y.mask, r_y.p, keep.p);
-  }
-  DBuf<uint64_t> kpos = X.alloc<uint64_t>(NR + 1);
-  exclusive_scan<uint32_t>(X, keep.p, NR, kpos.p);
-  const uint64_t kept = X.scalar(kpos.p + NR);
-  rep->dropped_r = NR - kept;
+  // R pass: semi-join filter on y, then x over the survivors. With identity y
+  // the filter is disabled (every R.y < y_card = max over both sides + 1).
+  uint64_t kept = NR;
   const uint64_t* Rx = Rl;
   DBuf<uint64_t> rx_kept;
-  if (kept != NR) {
-    rx_kept = X.alloc<uint64_t>(kept);
-    DBuf<uint32_t> ry2 = X.alloc<uint32_t>(kept);
-    D3G_LAUNCH(X, compact_kernel<uint64_t>, grid_for(NR, 256), 256, 0, Rl, keep.p, kpos.p, NR,
-               rx_kept.p);
-    D3G_LAUNCH(X, compact_kernel<uint32_t>, grid_for(NR, 256), 256, 0, r_y.p, keep.p, kpos.p, NR,
-               ry2.p);
-    r_y = std::move(ry2);
-    Rx = rx_kept.p;
+  if (!sy && NR) {
+    r_y_own = X.alloc<uint32_t>(NR);
+    DBuf<uint32_t> keep = X.alloc<uint32_t>(NR);
+    D3G_LAUNCH(X, dict_lookup_kernel, grid_for(NR, 256), 256, 0, Rr, NR, D.y.keys.p,
+               D.y.slot_code.p, D.y.mask, r_y_own.p, keep.p);
+    DBuf<uint64_t> kpos = X.alloc<uint64_t>(NR + 1);
+    exclusive_scan<uint32_t>(X, keep.p, NR, kpos.p);
+    kept = X.scalar(kpos.p + NR);
+    if (kept != NR) {
+      rx_kept = X.alloc<uint64_t>(kept);
+      DBuf<uint32_t> ry2 = X.alloc<uint32_t>(kept);
+      D3G_LAUNCH(X, compact_kernel<uint64_t>, grid_for(NR, 256), 256, 0, Rl, keep.p, kpos.p, NR,
+                 rx_kept.p);
+      D3G_LAUNCH(X, compact_kernel<uint32_t>, grid_for(NR, 256), 256, 0, r_y_own.p, keep.p,
+                 kpos.p, NR, ry2.p);
+      r_y_own = std::move(ry2);
+      Rx = rx_kept.p;
+    }
+    r_y = r_y_own.p;
   }
-  keep.reset();
-  kpos.reset();
-  DBuf<uint32_t> r_x = X.alloc<uint32_t>(kept);
+  rep->dropped_r = NR - kept;
   if (sx) {
     x_card = NR ? hs[0].max + 1 : 0;  // over all of R.left (mapping.cpp:404-413)
     D.x.identity = true;
     D.x.card = x_card;
-    if (kept) D3G_LAUNCH(X, narrow_kernel, grid_for(kept, 256), 256, 0, Rx, kept, r_x.p);
+    if (kept != NR) {
+      r_x_own = X.alloc<uint32_t>(kept);
+      if (kept) D3G_LAUNCH(X, narrow_kernel, grid_for(kept, 256), 256, 0, Rx, kept, r_x_own.p);
+      r_x = r_x_own.p;
+    }
   } else {
-    dict_build(X, Rx, kept, D.x, r_x.p);
+    r_x_own = X.alloc<uint32_t>(kept);
+    dict_build(X, Rx, kept, D.x, r_x_own.p);
+    r_x = r_x_own.p;
     x_card = D.x.card;
   }
   rx_kept.reset();
@@ -1176,10 +1197,10 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   rep->z_card = z_card;
   if (classical) {  // intermediate_pairs = bag join size, duplicates included
     DBuf<uint32_t> cnt = X.zeros<uint32_t>(y_card);
-    if (NS) D3G_LAUNCH(X, group_hist_kernel, grid_for(NS, 256), 256, 0, s_y.p, NS, cnt.p);
+    if (NS) D3G_LAUNCH(X, group_hist_kernel, grid_for(NS, 256), 256, 0, s_y, NS, cnt.p);
     DBuf<unsigned long long> bag = X.zeros<unsigned long long>(1);
     if (kept)
-      D3G_LAUNCH(X, bag_from_counts_kernel, grid_for(kept, 256), 256, 0, r_y.p, kept, cnt.p,
+      D3G_LAUNCH(X, bag_from_counts_kernel, grid_for(kept, 256), 256, 0, r_y, kept, cnt.p,
                  bag.p);
     rep->intermediate_pairs = X.scalar(bag.p);
   }
@@ -1189,12 +1210,13 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
 
   // 5. CSR (build_csr, relation.cpp:206-258)
   DeviceCsr rx, sz_csr;
-  build_csr_device(X, r_x.p, r_y.p, kept, x_card, y_card, rx);
-  r_x.reset();
-  r_y.reset();
-  build_csr_device(X, s_z.p, s_y.p, NS, z_card, y_card, sz_csr);
-  s_z.reset();
-  s_y.reset();
+  build_csr_device(X, r_x, r_y, kept, x_card, y_card, rx);
+  r_x_own.reset();
+  r_y_own.reset();
+  build_csr_device(X, s_z, s_y, NS, z_card, y_card, sz_csr);
+  s_z_own.reset();
+  s_y_own.reset();
+  nar.reset();
   rep->r_nnz = rx.nnz;
   rep->s_nnz = sz_csr.nnz;
   T.mark();  // 4
@@ -1393,6 +1415,7 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   rep->peak_bytes = X.peak_bytes - base_live;
   rep->gpu_launches = X.launches;
   rep->d2h_bytes += X.d2h_bytes;
+  X.reserve_for(X.peak_bytes);
 }
 
 }  // namespace

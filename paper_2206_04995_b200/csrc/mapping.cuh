@@ -52,6 +52,55 @@ __global__ void colstat_kernel(const uint64_t* __restrict__ col, uint64_t n, Col
   }
 }
 
+// All four input columns in one launch (blockIdx.y = column): max, the
+// detect_natural_keys sample test, and the speculative u32 narrowing the
+// natural-key mapping uses (codes = values), written while the values stream
+// by so a natural column is read exactly once.
+struct Cols4 {
+  const uint64_t* col[4];
+  uint64_t n[4];
+  uint32_t* narrow[4];
+};
+
+__global__ void __launch_bounds__(256) colstat4_kernel(Cols4 c, ColStat* st) {
+  const int ci = blockIdx.y;
+  const uint64_t* __restrict__ col = c.col[ci];
+  uint32_t* __restrict__ out = c.narrow[ci];
+  const uint64_t n = c.n[ci];
+  uint64_t m = 0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n; i += 4 * stride) {  // 4 independent loads in flight
+    const uint64_t v0 = col[i], v1 = col[i + stride], v2 = col[i + 2 * stride],
+                   v3 = col[i + 3 * stride];
+    out[i] = (uint32_t)v0;
+    out[i + stride] = (uint32_t)v1;
+    out[i + 2 * stride] = (uint32_t)v2;
+    out[i + 3 * stride] = (uint32_t)v3;
+    const uint64_t a = v0 > v1 ? v0 : v1, b = v2 > v3 ? v2 : v3;
+    const uint64_t ab = a > b ? a : b;
+    m = ab > m ? ab : m;
+  }
+  for (; i < n; i += stride) {
+    const uint64_t v = col[i];
+    out[i] = (uint32_t)v;
+    m = v > m ? v : m;
+  }
+  m = warp_max(m);
+  if (lane_id() == 0 && m) atomicMax(&st[ci].max, (unsigned long long)m);
+  if (blockIdx.x == 0) {
+    uint64_t samples = n < 4096 ? n : 4096;
+    uint64_t sstride = samples ? n / samples : 1;
+    if (sstride < 1) sstride = 1;
+    double bound = 2.0 * (double)n;
+    for (uint64_t k = threadIdx.x; k < samples; k += blockDim.x) {
+      uint64_t idx = k * sstride;
+      if (idx > n - 1) idx = n - 1;
+      if ((double)col[idx] >= bound) st[ci].sample_fail = 1;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Dictionary.
 struct DeviceDict {
