@@ -554,9 +554,17 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   } else if (K <= 256 && !(hot_impl && std::string(hot_impl) == "list")) {
     // packed hot records (default; D3G_HOT=list selects the list kernel), with
     // the top-rank subset table when it fits (D3G_HOT=rec disables it)
+    // the table pays off when the top ranks are common in the dense rows
+    // (cfg2/cfg5: >= 3 of the top 7 per row; cfg4's flat Zipf(0.8): < 1)
     const size_t tsm = (size_t)(kTabRows + K - kTabBits) * 32 * 16;
+    uint32_t top_cnt[kTabBits] = {};
+    X.to_host(top_cnt, cnt_rank.p, std::min<uint64_t>(kTabBits, Y));
+    double top_per_row = 0;
+    for (uint32_t r = 0; r < kTabBits; ++r) top_per_row += (double)top_cnt[r] / (double)D;
+    const bool force_tab = hot_impl && std::string(hot_impl) == "tab";
     const bool tab = K > kTabBits && tsm <= (size_t)dense_smem_bytes(X) &&
-                     !(hot_impl && std::string(hot_impl) == "rec");
+                     !(hot_impl && std::string(hot_impl) == "rec") &&
+                     (force_tab || top_per_row >= 1.5);
     DBuf<uint4> rec = X.zeros<uint4>(2 * D);
     DBuf<uint32_t> rcnt = X.alloc<uint32_t>(D);
     D3G_LAUNCH(X, hot_rec_kernel, grid_for(D, 256), 256, 0, in.dl_ptr, in.dl_col, D, K,
