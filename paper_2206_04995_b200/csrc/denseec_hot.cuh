@@ -103,26 +103,41 @@ __global__ void cold_count_kernel(const uint64_t* __restrict__ dl_ptr,
   }
 }
 
+// With sig != null the row's 256-bit hot signature (hz, kw == 4) is stored
+// inline next to each entry (2 x uint4 per entry).
 __global__ void cold_scatter_kernel(const uint64_t* __restrict__ dl_ptr,
                                     const uint32_t* __restrict__ dl_col, uint64_t n_dense,
                                     uint32_t K, const uint32_t* __restrict__ y_of_rank,
                                     unsigned long long* __restrict__ cursor,
-                                    uint32_t* __restrict__ out, uint64_t y_card,
-                                    uint32_t part_rows, uint32_t parts,
+                                    uint32_t* __restrict__ out, uint4* __restrict__ sig,
+                                    uint64_t y_card, uint32_t part_rows, uint32_t parts,
                                     const uint64_t* __restrict__ hz, uint32_t kw,
                                     uint32_t var_bits) {
   const uint32_t nvar = 1u << var_bits, vmask = nvar - 1;
+  const uint4* hz4 = reinterpret_cast<const uint4*>(hz);
   for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < n_dense;
        i += (uint64_t)gridDim.x * (blockDim.x / 32)) {
     const uint64_t part = i / part_rows;
     const uint32_t zm = var_bits ? (uint32_t)(hz[i * kw] & vmask) : 0;
+    uint4 s0 = make_uint4(0, 0, 0, 0), s1 = s0;
+    if (sig) {
+      s0 = hz4[2 * i];
+      s1 = hz4[2 * i + 1];
+    }
     for (uint64_t k = dl_ptr[i] + lane_id(); k < dl_ptr[i + 1]; k += 32) {
       const uint32_t r = dl_col[k];
       if (r < K) continue;
       const uint32_t y = y_of_rank[r];
       for (uint32_t v = 0; v < nvar; ++v)
-        if ((zm & v) == 0)
-          out[atomicAdd(&cursor[((uint64_t)v * parts + part) * y_card + y], 1ull)] = (uint32_t)i;
+        if ((zm & v) == 0) {
+          const unsigned long long pos =
+              atomicAdd(&cursor[((uint64_t)v * parts + part) * y_card + y], 1ull);
+          out[pos] = (uint32_t)i;
+          if (sig) {
+            sig[2 * pos] = s0;
+            sig[2 * pos + 1] = s1;
+          }
+        }
     }
   }
 }
@@ -628,17 +643,6 @@ dense_hot_tab_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
 // "hot masks intersect => already counted by P1" streams coalesced instead of
 // gathering hz[z] at random. Survivors are deduplicated in the warp's bitmap.
 constexpr int kColdWarps = 8;  // warps per CTA (several CTAs per SM)
-
-__global__ void cold_sig_kernel(const uint32_t* __restrict__ ccol, uint64_t n,
-                                const uint4* __restrict__ hz4 /* [D][2] */,
-                                uint4* __restrict__ ch /* [n][2] */) {
-  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
-       t += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t zi = ccol[t];
-    ch[2 * t] = hz4[2 * (uint64_t)zi];
-    ch[2 * t + 1] = hz4[2 * (uint64_t)zi + 1];
-  }
-}
 
 template <int kMode>
 __global__ void __launch_bounds__(kColdWarps * 32)

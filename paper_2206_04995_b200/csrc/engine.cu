@@ -623,16 +623,15 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     exclusive_scan<uint32_t>(X, cc.p, rows_key, cptr.p);
     const uint64_t cnnz = X.scalar(cptr.p + rows_key);
     DBuf<uint32_t> ccol = X.alloc<uint32_t>(cnnz);
+    DBuf<uint4> ch;  // inline hot signatures (cold kernels only)
+    if (cold_kernel_ok) ch = X.alloc<uint4>(2 * cnnz);
     DBuf<unsigned long long> cur = X.alloc<unsigned long long>(rows_key + 1);
     D3G_CUDA(cudaMemcpyAsync(cur.p, cptr.p, (rows_key + 1) * 8, cudaMemcpyDeviceToDevice, X.stream));
     D3G_LAUNCH(X, cold_scatter_kernel, grid_for(D * 32, 256), 256, 0, in.dl_ptr, in.dl_col, D, K,
-               in.y_of_rank, cur.p, ccol.p, Y, part_rows, parts,
+               in.y_of_rank, cur.p, ccol.p, cold_kernel_ok ? ch.p : nullptr, Y, part_rows, parts,
                reinterpret_cast<const uint64_t*>(hz.p), kw, var_bits);
+    cur.reset();
     if (cold_kernel_ok) {
-      DBuf<uint4> ch = X.alloc<uint4>(2 * cnnz);
-      if (cnnz)
-        D3G_LAUNCH(X, cold_sig_kernel, grid_for(cnnz, 256), 256, 0, ccol.p, cnnz,
-                   reinterpret_cast<const uint4*>(hz.p), ch.p);
       DBuf<unsigned int> next = X.zeros<unsigned int>(1);
       DBuf<Tally> tc = X.zeros<Tally>(1);
       if (cold_hash) {
