@@ -38,6 +38,7 @@ extern "C" {
 #define D3G_IO_ERROR 3
 #define D3G_RESOURCE_ERROR 4
 #define D3G_INTERNAL_ERROR 5
+#define D3G_FORMAT_ERROR 6   /* dim3::FormatError; the CLI maps it to exit 3 like IoError */
 
 /* dim3::Strategy (P/include/dim3/engine.hpp:25-31). */
 #define D3G_AUTO 0
@@ -197,6 +198,31 @@ uint64_t d3g_cfg_rows(int cfg);
  * the denominator of the DenseEC integer-pipe roofline. */
 int d3g_alu_peak(d3g_ctx* ctx, double* ops_per_sec);
 int d3g_ctx_device(d3g_ctx* ctx);
+
+/* ---- table files (P/src/relation.cpp) -------------------------------------
+ * Binary table = little-endian u64 (left, right) pairs, no header. Text =
+ * "left<sep>right\n" in decimal, sep '\t' (tsv) or ',' (csv). */
+#define D3G_FMT_AUTO 0
+#define D3G_FMT_TSV 1
+#define D3G_FMT_CSV 2
+#define D3G_FMT_BINARY 3
+/* detect_format (relation.cpp:13-20): requested unless AUTO, else by
+ * extension (.tsv/.txt tsv, .csv csv, .bin binary, otherwise tsv). */
+int d3g_detect_format(const char* path, int requested);
+/* Rows of a binary table file: D3G_IO_ERROR if it cannot be opened,
+ * D3G_FORMAT_ERROR if its length is not a multiple of 16 (read_binary,
+ * relation.cpp:98-107). Host-only. */
+int d3g_binary_rows(const char* path, uint64_t* n);
+/* read_binary (relation.cpp:98-127) into the DEVICE columns left/right
+ * (n = d3g_binary_rows): the file streams through pinned chunks into HBM and
+ * is de-interleaved on the GPU. */
+int d3g_read_binary(d3g_ctx* ctx, const char* path, uint64_t* left, uint64_t* right, uint64_t n);
+/* save_table (relation.cpp:164-204) of n (left, right) pairs, device or host
+ * columns: interleaving (binary) or decimal formatting (tsv/csv) runs on the
+ * GPU, the bytes are copied back in chunks and written. The CLI's --out of
+ * the decoded (x, z) pairs (P/tools/dim3.cpp:212-218). */
+int d3g_save_pairs(d3g_ctx* ctx, const uint64_t* left, const uint64_t* right, uint64_t n,
+                   int on_device, const char* path, int format);
 
 /* Host-only policy entry points (callable without a GPU). */
 uint32_t d3g_f3_threshold(uint32_t m_x, uint32_t y_card, const d3g_consts* c);

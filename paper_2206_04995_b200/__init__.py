@@ -17,6 +17,7 @@ from .engine import (  # noqa: F401
     Dim3Error,
     EngineConfig,
     ExecutionReport,
+    FileFormat,
     FormatError,
     IoError,
     JoinProjectOutput,
@@ -26,6 +27,11 @@ from .engine import (  # noqa: F401
     ResultSet,
     SkipFlags,
     alu_peak,
+    binary_rows,
+    detect_format,
+    load_table,
+    save_result,
+    save_table,
     Strategy,
     build_csr,
     cfg_rows,

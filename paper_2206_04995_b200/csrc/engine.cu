@@ -26,6 +26,7 @@
 #include "denseec.cuh"
 #include "denseec_hot.cuh"
 #include "denseec_tc.cuh"
+#include "io.cuh"
 #include "mapping.cuh"
 #include "partition.cuh"
 #include "sparsebmm.cuh"
@@ -1746,6 +1747,163 @@ int d3g_generate(d3g_ctx* ctx, int cfg, int side, uint64_t lo, uint64_t hi, uint
 }
 
 uint64_t d3g_cfg_rows(int cfg) { return d3g::cfg_rows(cfg); }
+
+// ---- table files ------------------------------------------------------------
+int d3g_detect_format(const char* path, int requested) {
+  if (requested != D3G_FMT_AUTO) return requested;
+  std::string p = path ? path : "";
+  const size_t slash = p.find_last_of('/');
+  const size_t dot = p.find_last_of('.');
+  std::string ext = (dot == std::string::npos || (slash != std::string::npos && dot < slash))
+                        ? ""
+                        : p.substr(dot);
+  if (ext == ".tsv" || ext == ".txt") return D3G_FMT_TSV;
+  if (ext == ".csv") return D3G_FMT_CSV;
+  if (ext == ".bin") return D3G_FMT_BINARY;
+  return D3G_FMT_TSV;
+}
+
+namespace {
+struct FileCloser {
+  FILE* f;
+  ~FileCloser() {
+    if (f) std::fclose(f);
+  }
+};
+uint64_t binary_rows_or_throw(const char* path) {
+  FILE* f = std::fopen(path, "rb");
+  if (!f) throw d3g::Error(D3G_IO_ERROR, std::string("cannot open ") + path);
+  FileCloser fc{f};
+  if (std::fseek(f, 0, SEEK_END) != 0) throw d3g::Error(D3G_IO_ERROR, std::string("cannot seek ") + path);
+  const long long len = std::ftell(f);
+  if (len < 0 || len % 16 != 0)
+    throw d3g::Error(D3G_FORMAT_ERROR, std::string(path) + ": binary table length " +
+                                           std::to_string(len) + " is not a multiple of 16");
+  return (uint64_t)len / 16;
+}
+// Two pinned staging chunks with their own events (double buffering).
+struct Staging {
+  d3g::Ctx& X;
+  void* host[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  size_t bytes;
+  Staging(d3g::Ctx& x, size_t b) : X(x), bytes(b) {
+    for (int i = 0; i < 2; ++i) {
+      D3G_CUDA(cudaMallocHost(&host[i], bytes));
+      D3G_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+    }
+  }
+  ~Staging() {
+    for (int i = 0; i < 2; ++i) {
+      if (ev[i]) cudaEventSynchronize(ev[i]), cudaEventDestroy(ev[i]);
+      if (host[i]) cudaFreeHost(host[i]);
+    }
+  }
+};
+}  // namespace
+
+int d3g_binary_rows(const char* path, uint64_t* n) {
+  return guarded([&] { *n = binary_rows_or_throw(path); });
+}
+
+int d3g_read_binary(d3g_ctx* ctx, const char* path, uint64_t* left, uint64_t* right, uint64_t n) {
+  return guarded([&] {
+    using namespace d3g;
+    Ctx& X = ctx->c;
+    D3G_CUDA(cudaSetDevice(X.device));
+    const uint64_t rows = binary_rows_or_throw(path);
+    if (rows != n)
+      throw ConfigError("d3g_read_binary: n = " + std::to_string(n) + " but the file holds " +
+                        std::to_string(rows) + " rows");
+    if (n == 0) return;
+    FILE* f = std::fopen(path, "rb");
+    if (!f) throw Error(D3G_IO_ERROR, std::string("cannot open ") + path);
+    FileCloser fc{f};
+    const uint64_t chunk_rows = std::min<uint64_t>(n, 4ull << 20);  // 64 MB chunks
+    Staging st(X, chunk_rows * 16);
+    DBuf<uint64_t> dev[2] = {X.alloc<uint64_t>(2 * chunk_rows), X.alloc<uint64_t>(2 * chunk_rows)};
+    uint64_t done = 0;
+    for (int b = 0; done < n; b ^= 1) {
+      const uint64_t take = std::min(chunk_rows, n - done);
+      D3G_CUDA(cudaEventSynchronize(st.ev[b]));  // the chunk's previous copy has drained
+      if (std::fread(st.host[b], 16, take, f) != take)
+        throw Error(D3G_IO_ERROR, std::string("read error on ") + path);
+      D3G_CUDA(cudaMemcpyAsync(dev[b].p, st.host[b], take * 16, cudaMemcpyHostToDevice, X.stream));
+      D3G_LAUNCH(X, deinterleave_kernel, grid_for(take, 256), 256, 0, dev[b].p, take, left + done,
+                 right + done);
+      D3G_CUDA(cudaEventRecord(st.ev[b], X.stream));
+      done += take;
+    }
+    X.sync();
+  });
+}
+
+int d3g_save_pairs(d3g_ctx* ctx, const uint64_t* left, const uint64_t* right, uint64_t n,
+                   int on_device, const char* path, int format) {
+  return guarded([&] {
+    using namespace d3g;
+    Ctx& X = ctx->c;
+    D3G_CUDA(cudaSetDevice(X.device));
+    const int fmt = d3g_detect_format(path, format);
+    if (fmt < D3G_FMT_TSV || fmt > D3G_FMT_BINARY) throw ConfigError("unknown table format");
+    FILE* f = std::fopen(path, "wb");
+    if (!f) throw Error(D3G_IO_ERROR, std::string("cannot open ") + path + " for writing");
+    FileCloser fc{f};
+    const uint64_t chunk_rows = std::max<uint64_t>(1, std::min<uint64_t>(n, 2ull << 20));
+    const size_t out_bytes = fmt == D3G_FMT_BINARY ? chunk_rows * 16 : chunk_rows * 42;
+    Staging st(X, out_bytes);
+    DBuf<uint64_t> in_l, in_r;
+    if (!on_device) {
+      in_l = X.alloc<uint64_t>(chunk_rows);
+      in_r = X.alloc<uint64_t>(chunk_rows);
+    }
+    DBuf<char> dout[2] = {X.alloc<char>(out_bytes), X.alloc<char>(out_bytes)};
+    DBuf<uint32_t> len = X.alloc<uint32_t>(chunk_rows);
+    DBuf<uint64_t> off = X.alloc<uint64_t>(chunk_rows + 1);
+    size_t pending[2] = {0, 0};
+    auto flush = [&](int b) {
+      if (!pending[b]) return;
+      D3G_CUDA(cudaEventSynchronize(st.ev[b]));
+      if (std::fwrite(st.host[b], 1, pending[b], f) != pending[b])
+        throw Error(D3G_IO_ERROR, std::string("write error on ") + path);
+      pending[b] = 0;
+    };
+    uint64_t done = 0;
+    int b = 0;
+    for (; done < n; b ^= 1) {
+      const uint64_t take = std::min(chunk_rows, n - done);
+      flush(b);  // staging buffer b is free again
+      const uint64_t* l = left + done;
+      const uint64_t* r = right + done;
+      if (!on_device) {
+        X.to_device(in_l.p, l, take);
+        X.to_device(in_r.p, r, take);
+        l = in_l.p;
+        r = in_r.p;
+      }
+      size_t bytes;
+      if (fmt == D3G_FMT_BINARY) {
+        D3G_LAUNCH(X, interleave_kernel, grid_for(take, 256), 256, 0, l, r, take,
+                   reinterpret_cast<uint64_t*>(dout[b].p));
+        bytes = take * 16;
+      } else {
+        D3G_LAUNCH(X, text_len_kernel, grid_for(take, 256), 256, 0, l, r, take, len.p);
+        exclusive_scan<uint32_t>(X, len.p, take, off.p);
+        bytes = X.scalar(off.p + take);
+        D3G_LAUNCH(X, text_write_kernel, grid_for(take, 256), 256, 0, l, r, take, off.p,
+                   fmt == D3G_FMT_CSV ? ',' : '\t', dout[b].p);
+      }
+      D3G_CUDA(cudaMemcpyAsync(st.host[b], dout[b].p, bytes, cudaMemcpyDeviceToHost, X.stream));
+      D3G_CUDA(cudaEventRecord(st.ev[b], X.stream));
+      pending[b] = bytes;
+      done += take;
+      if (!on_device) X.sync();  // the host-input staging is reused next chunk
+    }
+    flush(b);      // the older of the two pending chunks first
+    flush(b ^ 1);
+    if (std::fflush(f) != 0) throw Error(D3G_IO_ERROR, std::string("write error on ") + path);
+  });
+}
 
 int d3g_ctx_device(d3g_ctx* ctx) { return ctx ? ctx->c.device : -1; }
 

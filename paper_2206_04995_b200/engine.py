@@ -68,7 +68,7 @@ class CudaError(Dim3Error):
     status = 5
 
 
-_STATUS = {2: ConfigError, 3: IoError, 4: ResourceError, 5: CudaError}
+_STATUS = {2: ConfigError, 3: IoError, 4: ResourceError, 5: CudaError, 6: FormatError}
 
 
 class Strategy(enum.IntEnum):
@@ -251,7 +251,8 @@ class _KStats(C.Structure):
 EXPORTED = ["d3g_ctx_create", "d3g_ctx_destroy", "d3g_last_error", "d3g_version",
             "d3g_opts_default", "d3g_join_project", "d3g_build_csr", "d3g_sparse_bmm_csr",
             "d3g_dense_ec_rows", "d3g_generate", "d3g_cfg_rows", "d3g_ctx_device",
-            "d3g_f3_threshold", "d3g_f1", "d3g_f2_decide", "d3g_alu_peak"]
+            "d3g_f3_threshold", "d3g_f1", "d3g_f2_decide", "d3g_alu_peak",
+            "d3g_detect_format", "d3g_binary_rows", "d3g_read_binary", "d3g_save_pairs"]
 
 _lib = None
 
@@ -292,6 +293,11 @@ def lib():
         L.d3g_f2_decide.argtypes = [U64P, C.c_uint64, U64P, C.c_uint64, C.c_uint64, C.c_uint64,
                                     C.c_uint64, C.c_uint64, C.POINTER(_Consts), C.c_int,
                                     C.POINTER(C.c_uint8), U64P]
+        L.d3g_detect_format.argtypes = [C.c_char_p, C.c_int]
+        L.d3g_binary_rows.argtypes = [C.c_char_p, U64P]
+        L.d3g_read_binary.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p, C.c_void_p, C.c_uint64]
+        L.d3g_save_pairs.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int,
+                                     C.c_char_p, C.c_int]
         _lib = L
     return _lib
 
@@ -667,3 +673,72 @@ def alu_peak(ctx: Context | None = None) -> float:
 
 def cfg_rows(cfg: int) -> int:
     return int(lib().d3g_cfg_rows(cfg))
+
+
+# ---------------------------------------------------------------------------
+# Table files (P/src/relation.cpp; P/include/dim3/relation.hpp FileFormat).
+class FileFormat(enum.IntEnum):
+    auto_detect = 0
+    tsv = 1
+    csv = 2
+    binary = 3
+
+
+def detect_format(path, requested: FileFormat = FileFormat.auto_detect) -> FileFormat:
+    """detect_format (relation.cpp:13-20)."""
+    return FileFormat(lib().d3g_detect_format(os.fsencode(str(path)), int(requested)))
+
+
+def binary_rows(path) -> int:
+    """Rows of a binary table file; IoError / FormatError like read_binary
+    (relation.cpp:98-107). Host-only."""
+    n = C.c_uint64()
+    _check(lib().d3g_binary_rows(os.fsencode(str(path)), C.byref(n)))
+    return n.value
+
+
+def load_table(path, fmt: FileFormat = FileFormat.auto_detect, ctx: "Context | None" = None,
+               device=None) -> RawTable:
+    """load_table (relation.cpp:130-139) for binary tables: the file streams
+    through pinned chunks into HBM and is de-interleaved on the GPU; returns
+    a RawTable of device columns. Text tables (TSV/CSV parsing) are outside
+    this path's scope and raise FormatError."""
+    import torch
+    if detect_format(path, fmt) != FileFormat.binary:
+        raise FormatError("only binary tables load on the device path "
+                          "(TSV/CSV parsing is outside this operator's scope)")
+    n = binary_rows(path)
+    ctx = ctx or default_context(device)
+    dev = torch.device("cuda", ctx.device)
+    left = torch.empty(n, dtype=torch.int64, device=dev)
+    right = torch.empty(n, dtype=torch.int64, device=dev)
+    torch.cuda.synchronize(dev)
+    _check(lib().d3g_read_binary(ctx.handle, os.fsencode(str(path)), C.c_void_p(left.data_ptr()),
+                                 C.c_void_p(right.data_ptr()), n))
+    return RawTable(left, right)
+
+
+def save_table(t: RawTable, path, fmt: FileFormat = FileFormat.auto_detect,
+               ctx: "Context | None" = None, device=None) -> None:
+    """save_table (relation.cpp:164-204): binary = interleaved little-endian
+    u64 pairs, tsv/csv = "left<sep>right\\n" in decimal. Interleaving or
+    formatting runs on the GPU; host or device columns."""
+    ctx = ctx or default_context(device)
+    n = t.size()
+    on_dev = _is_cuda(t.left)
+    if on_dev:
+        import torch
+        torch.cuda.synchronize(t.left.device)
+        lp, rp = C.c_void_p(t.left.data_ptr()), C.c_void_p(t.right.data_ptr())
+    else:
+        lp, rp = C.c_void_p(t.left.ctypes.data), C.c_void_p(t.right.ctypes.data)
+    _check(lib().d3g_save_pairs(ctx.handle, lp, rp, n, int(on_dev), os.fsencode(str(path)),
+                                int(fmt)))
+
+
+def save_result(out: "JoinProjectOutput", path, fmt: FileFormat = FileFormat.auto_detect,
+                ctx: "Context | None" = None) -> None:
+    """The CLI's --out (P/tools/dim3.cpp:212-218): result_to_raw, then
+    save_table of the decoded (x, z) pairs."""
+    raw = result_to_raw(out)
+    save_table(RawTable(raw.raw_x, raw.raw_z), path, fmt, ctx)
