@@ -684,11 +684,32 @@ dense_cold_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
         seg0 = cp[y];
         seg1 = cp[y + 1];
       }
-      const uint32_t nseg = (uint32_t)((r1 - kb) < 32 ? (r1 - kb) : 32);
-      for (uint32_t j = 0; j < nseg; ++j) {
-        const uint64_t s0 = __shfl_sync(0xffffffffu, seg0, j);
-        const uint64_t s1 = __shfl_sync(0xffffffffu, seg1, j);
-        for (uint64_t t = s0 + lane; t < s1; t += 32) {
+      // flatten the (segment, entry) space: an inclusive warp scan of the
+      // segment lengths, then every lane takes one candidate per step and
+      // finds its segment by a 5-step binary search over the scan (short
+      // cold segments no longer leave most lanes idle)
+      const uint32_t len = (uint32_t)(seg1 - seg0);
+      uint32_t incl = len;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= (uint32_t)o) incl += u;
+      }
+      const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+      for (uint32_t tb = 0; tb < total; tb += 32) {
+        const uint32_t tf = tb + lane;
+        // smallest k with incl[k] > tf
+        uint32_t k = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+          const uint32_t probe = __shfl_sync(0xffffffffu, incl, k + step - 1);
+          if (probe <= tf) k += step;
+        }
+        const uint32_t before = __shfl_sync(0xffffffffu, incl - len, k);
+        const uint64_t base_k = __shfl_sync(0xffffffffu, seg0, k);
+        if (tf >= total) continue;
+        {
+          const uint64_t t = base_k + (tf - before);
           const uint4 b0 = ch[2 * t], b1 = ch[2 * t + 1];
           const uint32_t zl = ccol[t] - zbase;
           const bool hot = ((a0.x & b0.x) | (a0.y & b0.y) | (a0.z & b0.z) | (a0.w & b0.w) |
