@@ -199,6 +199,50 @@ uint64_t d3g_cfg_rows(int cfg);
 int d3g_alu_peak(d3g_ctx* ctx, double* ops_per_sec);
 int d3g_ctx_device(d3g_ctx* ctx);
 
+/* ---- join-aggregate (P/src/engine.cpp:537-722) -----------------------------
+ * dim3::ValuedTable (relation.hpp:49-53): a table plus one double per row;
+ * values live in device memory iff base.on_device. */
+typedef struct {
+  d3g_table base;
+  const double* values;
+} d3g_valued_table;
+
+/* dim3::AggFn / dim3::CombineFn (P/include/dim3/engine.hpp:129-130). */
+#define D3G_AGG_SUM 0
+#define D3G_AGG_COUNT 1
+#define D3G_AGG_MIN 2
+#define D3G_AGG_MAX 3
+#define D3G_AGG_AVG 4
+#define D3G_COMBINE_MULTIPLY 0
+#define D3G_COMBINE_ADD 1
+#define D3G_COMBINE_ABS_DIFF 2
+#define D3G_COMBINE_LEFT 3
+#define D3G_COMBINE_RIGHT 4
+
+/* AggregateResult's pairs (decoded raw x, z) and values; cap rows, n set. */
+typedef struct {
+  uint64_t* x;
+  uint64_t* z;
+  double* values;
+  uint64_t cap;
+  uint64_t n;
+  int32_t on_device;
+  int32_t pad;
+} d3g_agg_pairs;
+
+/* join_aggregate_both (engine.cpp:537-722), caller orientation (no swap):
+ * one row per distinct (x, z) with agg over every match of
+ * combine(r.value, s.value). Values are bit-identical to the reference's
+ * (same accumulation order, round-to-nearest, no FMA). force = classical
+ * raises D3G_CONFIG_ERROR like the reference. out == NULL or
+ * opts->count_only: the count and report only. Report: strategy "hybrid",
+ * cards, dropped_r, out_j (= out_j_estimate, exact), f2_evaluations,
+ * dense_z/sparse_z, pairs_sparse/pairs_dense, out_p; ms_sparse is the whole
+ * aggregation pass. */
+int d3g_join_aggregate(d3g_ctx* ctx, const d3g_valued_table* r, const d3g_valued_table* s,
+                       int combine, int agg, const d3g_consts* c, const d3g_opts* o,
+                       d3g_report* rep, d3g_agg_pairs* out);
+
 /* ---- table files (P/src/relation.cpp) -------------------------------------
  * Binary table = little-endian u64 (left, right) pairs, no header. Text =
  * "left<sep>right\n" in decimal, sep '\t' (tsv) or ',' (csv). */

@@ -284,6 +284,79 @@ def ref_pipeline(r: Table, s: Table, consts=None):
     return d
 
 
+AGG = {"sum": 0, "count": 1, "min": 2, "max": 3, "avg": 4}
+COMBINE = {"multiply": 0, "add": 1, "abs_diff": 2, "left": 3, "right": 4}
+
+
+def ref_join_aggregate(r: Table, s: Table, rv, sv, combine="multiply", agg="sum", force="hybrid",
+                       count_only=False, consts=None):
+    """dim3::join_aggregate_both through the reference library: the report
+    and, unless count_only, {(raw x, raw z): value}."""
+    lib = ref_lib()
+    rl, rr, sl, sr = (_u64(a) for a in (r.left, r.right, s.left, s.right))
+    rv = np.ascontiguousarray(rv, dtype=np.float64)
+    sv = np.ascontiguousarray(sv, dtype=np.float64)
+    c = make_consts(consts)
+    rep = RefReport()
+    cap = max(1, len(rl) * max(1, len(sl)))
+    cap = min(cap, 20_000_000)
+    ox = np.zeros(cap, dtype=np.uint64)
+    oz = np.zeros(cap, dtype=np.uint64)
+    ov = np.zeros(cap, dtype=np.float64)
+    fn = lib.ref_join_aggregate
+    D = C.POINTER(C.c_double)
+    fn.argtypes = [U64P, U64P, D, C.c_uint64, U64P, U64P, D, C.c_uint64, C.c_int, C.c_int,
+                   C.c_int, C.c_int, C.c_void_p, C.c_void_p, U64P, U64P, D, C.c_uint64]
+    rc = fn(_p(rl), _p(rr), rv.ctypes.data_as(D), len(rl), _p(sl), _p(sr), sv.ctypes.data_as(D),
+            len(sl), COMBINE[combine], AGG[agg], STRATEGY[force], int(count_only), C.byref(c),
+            C.byref(rep), _p(ox), _p(oz), ov.ctypes.data_as(D), cap)
+    if rc:
+        raise ConfigErrorLike(rc, lib.ref_last_error().decode())
+    d = _struct_dict(rep)
+    if not count_only:
+        n = min(d["out_p"], cap)
+        d["cells"] = {(int(a), int(b)): float(v) for a, b, v in zip(ox[:n], oz[:n], ov[:n])}
+        d["order"] = [(int(a), int(b)) for a, b in zip(ox[:n], oz[:n])]
+    return d
+
+
+def oracle_aggregate(r: Table, s: Table, rv, sv, combine="multiply", agg="sum"):
+    """Brute-force restatement of join_aggregate_both's semantics for small
+    inputs (P/tests/test_engine.cpp:42-86 OracleCell): {(x, z): value} with the
+    accumulation in the reference's order (R rows of x in input order, S rows
+    of y in input order). Pure Python; a checker only."""
+    import math
+    by_y = {}
+    for j, (z, y) in enumerate(zip(np.asarray(s.left).tolist(), np.asarray(s.right).tolist())):
+        by_y.setdefault(y, []).append((z, float(sv[j])))
+    rows_by_x = {}
+    for i, (x, y) in enumerate(zip(np.asarray(r.left).tolist(), np.asarray(r.right).tolist())):
+        rows_by_x.setdefault(x, []).append((y, float(rv[i])))
+    comb = {"multiply": lambda a, b: a * b, "add": lambda a, b: a + b,
+            "abs_diff": lambda a, b: math.fabs(a - b), "left": lambda a, b: a,
+            "right": lambda a, b: b}[combine]
+    cells = {}
+    for x, rows in rows_by_x.items():
+        for y, v in rows:
+            for z, u in by_y.get(y, ()):
+                cv = comb(v, u)
+                c = cells.get((x, z))
+                if c is None:
+                    cells[(x, z)] = [0.0 if agg == "count" else cv, 1]
+                else:
+                    if agg in ("sum", "avg"):
+                        c[0] = c[0] + cv
+                    elif agg == "min":
+                        c[0] = cv if cv < c[0] else c[0]
+                    elif agg == "max":
+                        c[0] = cv if c[0] < cv else c[0]
+                    c[1] += 1
+    out = {}
+    for k, (acc, cnt) in cells.items():
+        out[k] = float(cnt) if agg == "count" else (acc / cnt if agg == "avg" else acc)
+    return out
+
+
 def ref_pipeline_split(r: Table, s: Table, consts=None):
     """ref_pipeline's statistics and dense/sparse split without building the
     panel (F2Evaluator decisions only)."""

@@ -204,6 +204,61 @@ int ref_join_project(const std::uint64_t* rl, const std::uint64_t* rr,
   }
 }
 
+// dim3::join_aggregate_both through the reference API (engine.cpp:537-722);
+// the decoded pairs (aggregate_to_raw) and values in emission order, up to
+// out_cap rows. combine / agg follow dim3::CombineFn / dim3::AggFn order.
+int ref_join_aggregate(const std::uint64_t* rl, const std::uint64_t* rr,
+                       const double* rv, std::uint64_t nr,
+                       const std::uint64_t* sl, const std::uint64_t* sr,
+                       const double* sv, std::uint64_t ns, int combine, int agg,
+                       int force, int count_only, const RefConsts* consts,
+                       RefReport* rep, std::uint64_t* out_x,
+                       std::uint64_t* out_z, double* out_v,
+                       std::uint64_t out_cap) {
+  try {
+    dim3::ValuedTable r, s;
+    r.base = to_table(rl, rr, nr);
+    s.base = to_table(sl, sr, ns);
+    r.values.assign(rv, rv + nr);
+    s.values.assign(sv, sv + ns);
+    dim3::EngineConfig cfg;
+    cfg.force = static_cast<dim3::Strategy>(force);
+    cfg.count_only = count_only != 0;
+    auto out = dim3::join_aggregate_both(r, s, static_cast<dim3::CombineFn>(combine),
+                                         static_cast<dim3::AggFn>(agg), cfg,
+                                         to_consts(consts));
+    const auto& e = out.report;
+    std::memset(rep, 0, sizeof(*rep));
+    std::strncpy(rep->strategy, e.strategy.c_str(), sizeof(rep->strategy) - 1);
+    rep->r_rows = e.r_rows;
+    rep->s_rows = e.s_rows;
+    rep->out_j_estimate = e.out_j_estimate;
+    rep->out_p = e.out_p;
+    rep->pairs_sparse = e.pairs_sparse;
+    rep->pairs_dense = e.pairs_dense;
+    rep->sparse_z = e.sparse_z;
+    rep->dense_z = e.dense_z;
+    rep->f2_evaluations = e.f2_evaluations;
+    rep->dropped_r = e.dropped_r;
+    rep->x_card = e.x_card;
+    rep->y_card = e.y_card;
+    rep->z_card = e.z_card;
+    if (out.base.materialized && out_x != nullptr) {
+      dim3::ResultSet raw = dim3::aggregate_to_raw(out);
+      std::uint64_t n = raw.raw_x.ints.size();
+      for (std::uint64_t i = 0; i < n && i < out_cap; ++i) {
+        out_x[i] = raw.raw_x.ints[i];
+        out_z[i] = raw.raw_z.ints[i];
+        out_v[i] = out.values[i];
+      }
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return status_of(e);
+  }
+}
+
 // Pipeline facts the parity tests compare against: code-space cards, post-
 // collapse nnz, the exact distinct OUT_J (DegreeStats::out_j), and the raw
 // values of the z columns f2 marks dense (PartitionResult::panel.z_ids),

@@ -27,6 +27,7 @@
 #include "denseec_hot.cuh"
 #include "denseec_tc.cuh"
 #include "io.cuh"
+#include "aggregate.cuh"
 #include "mapping.cuh"
 #include "partition.cuh"
 #include "sparsebmm.cuh"
@@ -997,6 +998,265 @@ void classical_impl(Ctx& X, const uint64_t* Rl, const uint64_t* Rr, uint64_t NR,
 }
 
 // ---------------------------------------------------------------------------
+// Pipeline stages shared by join_project and join_aggregate_both.
+
+// Steps 3-4: natural-key resolution (engine.cpp:25-50, mapping.cpp:281-338)
+// and map_tables (mapping.cpp:342-420). Natural columns use the narrowed
+// codes of the one-pass statistics kernel; the others go through HBM
+// dictionaries. With want_kept the original indices of the surviving R rows
+// are produced too (when the semi-join dropped any).
+struct Mapped {
+  DictBundle D;
+  DBuf<uint32_t> nar, s_y_own, s_z_own, r_y_own, r_x_own, r_kept;
+  const uint32_t *r_x = nullptr, *r_y = nullptr, *s_z = nullptr, *s_y = nullptr;
+  uint64_t kept = 0, x_card = 0, y_card = 0, z_card = 0;
+  void release_codes() {
+    r_x_own.reset();
+    r_y_own.reset();
+    s_z_own.reset();
+    s_y_own.reset();
+    nar.reset();
+  }
+};
+
+void map_inputs(Ctx& X, const uint64_t* Rl, const uint64_t* Rr, uint64_t NR, const uint64_t* Sl,
+                const uint64_t* Sr, uint64_t NS, const d3g_opts* o, d3g_report* rep, bool want_kept,
+                Mapped& M) {
+  using namespace d3g;
+  DBuf<ColStat> cs = X.zeros<ColStat>(4);
+  const uint64_t* cols[4] = {Rl, Rr, Sl, Sr};
+  const uint64_t lens[4] = {NR, NR, NS, NS};
+  // one pass over the four columns: statistics + speculative u32 codes
+  M.nar = X.alloc<uint32_t>(2 * NR + 2 * NS);
+  uint32_t* ncol[4] = {M.nar.p, M.nar.p + NR, M.nar.p + 2 * NR, M.nar.p + 2 * NR + NS};
+  {
+    Cols4 c4{};
+    for (int i = 0; i < 4; ++i) {
+      c4.col[i] = cols[i];
+      c4.n[i] = lens[i];
+      c4.narrow[i] = ncol[i];
+    }
+    const uint64_t mx = std::max(NR, NS);
+    if (mx) {
+      dim3 grid(grid_for(mx, 256, X.sm_count * 4), 4);
+      D3G_LAUNCH(X, colstat4_kernel, grid, 256, 0, c4, cs.p);
+    }
+  }
+  ColStat hs[4];
+  X.to_host(hs, cs.p, 4);
+  auto det = [&](int i) { return lens[i] > 0 && hs[i].sample_fail == 0; };
+  auto fits = [&](int i) { return lens[i] == 0 || hs[i].max < (1ull << 32); };
+  bool sx = o->declared_x != 0, sy = o->declared_y != 0, sz = o->declared_z != 0;
+  if (o->natural_keys_auto) {
+    sx = sx || det(0);
+    sy = sy || (det(1) && det(3));
+    sz = sz || det(2);
+  }
+  auto feasible = [&](bool ax, bool ay, bool az) {
+    if (ay && (!fits(1) || !fits(3))) return false;
+    if (az && !fits(2)) return false;
+    if (ax && !fits(0)) return false;
+    return true;
+  };
+  if (!feasible(sx, sy, sz)) {
+    bool dx = o->declared_x != 0, dy = o->declared_y != 0, dz = o->declared_z != 0;
+    if ((sx == dx && sy == dy && sz == dz) || !feasible(dx, dy, dz))
+      throw ConfigError("natural-key skip requires integer values below 2^32");
+    sx = dx;
+    sy = dy;
+    sz = dz;
+  }
+  rep->natural_x = sx;
+  rep->natural_y = sy;
+  rep->natural_z = sz;
+
+  DictBundle& D = M.D;
+  M.s_y = ncol[3];
+  M.s_z = ncol[2];
+  M.r_y = ncol[1];
+  M.r_x = ncol[0];
+  if (sy) {
+    uint64_t a = NS ? hs[3].max + 1 : 0, b = NR ? hs[1].max + 1 : 0;
+    M.y_card = std::max(a, b);
+    D.y.identity = true;
+    D.y.card = M.y_card;
+  } else {
+    M.s_y_own = X.alloc<uint32_t>(NS);
+    dict_build(X, Sr, NS, D.y, M.s_y_own.p);
+    M.s_y = M.s_y_own.p;
+    M.y_card = D.y.card;
+  }
+  if (sz) {
+    M.z_card = NS ? hs[2].max + 1 : 0;
+    D.z.identity = true;
+    D.z.card = M.z_card;
+  } else {
+    M.s_z_own = X.alloc<uint32_t>(NS);
+    dict_build(X, Sl, NS, D.z, M.s_z_own.p);
+    M.s_z = M.s_z_own.p;
+    M.z_card = D.z.card;
+  }
+  // R pass: semi-join filter on y, then x over the survivors. With identity y
+  // the filter is disabled (every R.y < y_card = max over both sides + 1).
+  M.kept = NR;
+  const uint64_t* Rx = Rl;
+  DBuf<uint64_t> rx_kept;
+  if (!sy && NR) {
+    M.r_y_own = X.alloc<uint32_t>(NR);
+    DBuf<uint32_t> keep = X.alloc<uint32_t>(NR);
+    D3G_LAUNCH(X, dict_lookup_kernel, grid_for(NR, 256), 256, 0, Rr, NR, D.y.keys.p,
+               D.y.slot_code.p, D.y.mask, M.r_y_own.p, keep.p);
+    DBuf<uint64_t> kpos = X.alloc<uint64_t>(NR + 1);
+    exclusive_scan<uint32_t>(X, keep.p, NR, kpos.p);
+    M.kept = X.scalar(kpos.p + NR);
+    if (M.kept != NR) {
+      rx_kept = X.alloc<uint64_t>(M.kept);
+      DBuf<uint32_t> ry2 = X.alloc<uint32_t>(M.kept);
+      D3G_LAUNCH(X, compact_kernel<uint64_t>, grid_for(NR, 256), 256, 0, Rl, keep.p, kpos.p, NR,
+                 rx_kept.p);
+      D3G_LAUNCH(X, compact_kernel<uint32_t>, grid_for(NR, 256), 256, 0, M.r_y_own.p, keep.p,
+                 kpos.p, NR, ry2.p);
+      M.r_y_own = std::move(ry2);
+      Rx = rx_kept.p;
+      if (want_kept) {  // m.r_kept (mapping.hpp): original indices of the survivors
+        M.r_kept = X.alloc<uint32_t>(M.kept);
+        D3G_LAUNCH(X, index_compact_kernel, grid_for(NR, 256), 256, 0, keep.p, kpos.p, NR,
+                   M.r_kept.p);
+      }
+    }
+    M.r_y = M.r_y_own.p;
+  }
+  rep->dropped_r = NR - M.kept;
+  if (sx) {
+    M.x_card = NR ? hs[0].max + 1 : 0;  // over all of R.left (mapping.cpp:404-413)
+    D.x.identity = true;
+    D.x.card = M.x_card;
+    if (M.kept != NR) {
+      M.r_x_own = X.alloc<uint32_t>(M.kept);
+      if (M.kept)
+        D3G_LAUNCH(X, narrow_kernel, grid_for(M.kept, 256), 256, 0, Rx, M.kept, M.r_x_own.p);
+      M.r_x = M.r_x_own.p;
+    }
+  } else {
+    M.r_x_own = X.alloc<uint32_t>(M.kept);
+    dict_build(X, Rx, M.kept, D.x, M.r_x_own.p);
+    M.r_x = M.r_x_own.p;
+    M.x_card = D.x.card;
+  }
+  rep->x_card = M.x_card;
+  rep->y_card = M.y_card;
+  rep->z_card = M.z_card;
+  if (M.x_card >= (1ull << 32) || M.y_card >= (1ull << 32) || M.z_card >= (1ull << 32))
+    throw ConfigError("code space exceeds 2^32");
+}
+
+// Step 6: compute_degree_stats (costmodel.cpp:425-438) on the collapsed CSRs:
+// degree histograms, dR/dS and the exact OUT_J (128-bit, saturating).
+struct DegreeStats {
+  uint64_t max_mx = 0, x_live = 0, max_mz = 0;
+  std::vector<uint64_t> hmx, hmz;
+  DBuf<uint32_t> dR, dS;
+};
+
+void degree_stats(Ctx& X, const d3g::DeviceCsr& rx, const d3g::DeviceCsr& sz_csr,
+                  uint64_t y_card, d3g_report* rep, DegreeStats& G) {
+  using namespace d3g;
+  const uint64_t x_card = rx.n_rows, z_card = sz_csr.n_rows;
+  DBuf<unsigned long long> sc = X.zeros<unsigned long long>(4);  // max_mx, live_x, max_mz, live_z
+  if (x_card)
+    D3G_LAUNCH(X, max_degree_kernel, grid_for(x_card, 256), 256, 0, rx.row_ptr.p, x_card, sc.p,
+               sc.p + 1);
+  if (z_card)
+    D3G_LAUNCH(X, max_degree_kernel, grid_for(z_card, 256), 256, 0, sz_csr.row_ptr.p, z_card,
+               sc.p + 2, sc.p + 3);
+  unsigned long long scal[4];
+  X.to_host(scal, sc.p, 4);
+  G.max_mx = scal[0];
+  G.x_live = scal[1];
+  G.max_mz = scal[2];
+  rep->x_live = G.x_live;
+  DBuf<unsigned long long> mxh = X.zeros<unsigned long long>(G.max_mx + 1);
+  DBuf<unsigned long long> mzh = X.zeros<unsigned long long>(G.max_mz + 1);
+  if (x_card)
+    D3G_LAUNCH(X, degree_hist_kernel, grid_for(x_card, 256), 256, 0, rx.row_ptr.p, x_card,
+               G.max_mx + 1, mxh.p);
+  if (z_card)
+    D3G_LAUNCH(X, degree_hist_kernel, grid_for(z_card, 256), 256, 0, sz_csr.row_ptr.p, z_card,
+               G.max_mz + 1, mzh.p);
+  G.dR = X.zeros<uint32_t>(y_card);
+  G.dS = X.zeros<uint32_t>(y_card);
+  if (rx.nnz)
+    D3G_LAUNCH(X, value_hist_kernel, grid_for(rx.nnz, 256), 256, 0, rx.col.p, rx.nnz, G.dR.p,
+               (uint32_t)y_card);
+  if (sz_csr.nnz)
+    D3G_LAUNCH(X, value_hist_kernel, grid_for(sz_csr.nnz, 256), 256, 0, sz_csr.col.p, sz_csr.nnz,
+               G.dS.p, (uint32_t)y_card);
+  {
+    unsigned gb = grid_for(y_card, 1024, 296);
+    DBuf<unsigned long long> parts = X.zeros<unsigned long long>(2 * gb);
+    if (y_card) D3G_LAUNCH(X, outj_kernel, gb, 1024, 0, G.dR.p, G.dS.p, y_card, parts.p);
+    std::vector<unsigned long long> hp(2 * gb);
+    X.to_host(hp.data(), parts.p, 2 * gb);
+    unsigned __int128 acc = 0;
+    for (unsigned i = 0; i < gb; ++i)
+      acc += ((unsigned __int128)hp[2 * i + 1] << 64) | hp[2 * i];
+    rep->out_j = acc > (unsigned __int128)std::numeric_limits<uint64_t>::max()
+                     ? std::numeric_limits<uint64_t>::max()
+                     : (uint64_t)acc;
+  }
+  G.hmx.resize(G.max_mx + 1);
+  G.hmz.resize(G.max_mz + 1);
+  X.to_host(reinterpret_cast<unsigned long long*>(G.hmx.data()), mxh.p, G.max_mx + 1);
+  X.to_host(reinterpret_cast<unsigned long long*>(G.hmz.data()), mzh.p, G.max_mz + 1);
+}
+
+// Step 7a: the f2 decision per degree value (policy.cpp) and the per-z
+// dense/sparse flags (the partition.cpp:17-38 decision loop).
+struct Split {
+  DBuf<uint32_t> isd, iss;  // per z: dense / sparse (m_z == 0: neither)
+  uint64_t n_dense = 0, n_sparse = 0;
+};
+
+void f2_split(Ctx& X, const d3g::DeviceCsr& sz_csr, const DegreeStats& G, uint64_t x_card,
+              uint64_t y_card, const d3g_consts* c, int pforce, d3g_report* rep, Split& P,
+              DBuf<uint64_t>* pd_out = nullptr, DBuf<uint64_t>* psp_out = nullptr) {
+  using namespace d3g;
+  const uint64_t z_card = sz_csr.n_rows;
+  std::vector<uint8_t> table(G.max_mz + 1, 0);
+  uint64_t evals = 0;
+  if (const char* dump = std::getenv("D3G_DUMP_F2")) {  // debugging aid: the f2 inputs
+    if (FILE* f = std::fopen(dump, "wb")) {
+      uint64_t hdr[6] = {G.max_mx + 1, G.max_mz + 1, x_card, y_card, z_card, rep->out_j};
+      std::fwrite(hdr, 8, 6, f);
+      std::fwrite(G.hmx.data(), 8, G.max_mx + 1, f);
+      std::fwrite(G.hmz.data(), 8, G.max_mz + 1, f);
+      std::fclose(f);
+    }
+  }
+  d3g_f2_decide(G.hmx.data(), G.max_mx + 1, G.hmz.data(), G.max_mz + 1, x_card, y_card, z_card,
+                rep->out_j, c, pforce, table.data(), &evals);
+  rep->f2_evaluations = evals;
+  DBuf<uint8_t> dtable = X.alloc<uint8_t>(G.max_mz + 1);
+  X.to_device(dtable.p, table.data(), G.max_mz + 1);
+  P.isd = X.alloc<uint32_t>(z_card);
+  P.iss = X.alloc<uint32_t>(z_card);
+  if (z_card)
+    D3G_LAUNCH(X, dense_flag_kernel, grid_for(z_card, 256), 256, 0, sz_csr.row_ptr.p, z_card,
+               dtable.p, G.max_mz + 1, P.isd.p, P.iss.p);
+  DBuf<uint64_t> pd = X.alloc<uint64_t>(z_card + 1), psp = X.alloc<uint64_t>(z_card + 1);
+  exclusive_scan<uint32_t>(X, P.isd.p, z_card, pd.p);
+  exclusive_scan<uint32_t>(X, P.iss.p, z_card, psp.p);
+  P.n_dense = X.scalar(pd.p + z_card);
+  P.n_sparse = X.scalar(psp.p + z_card);
+  rep->dense_z = P.n_dense;
+  rep->sparse_z = P.n_sparse;
+  const uint64_t row_words = ((y_card + c->w - 1) / c->w * c->w) / 64;
+  rep->panel_bytes = P.n_dense * row_words * 8;
+  if (pd_out) *pd_out = std::move(pd);
+  if (psp_out) *psp_out = std::move(psp);
+}
+
+// ---------------------------------------------------------------------------
 // The pipeline.
 void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g_consts* c,
                        const d3g_opts* o, d3g_report* rep, d3g_pairs* pairs) {
@@ -1083,238 +1343,56 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
     return;
   }
 
-  // 3. natural-key resolution (engine.cpp:25-50, mapping.cpp:281-338)
-  DBuf<ColStat> cs = X.zeros<ColStat>(4);
-  const uint64_t* cols[4] = {Rl, Rr, Sl, Sr};
-  const uint64_t lens[4] = {NR, NR, NS, NS};
-  // one pass over the four columns: statistics + speculative u32 codes
-  DBuf<uint32_t> nar = X.alloc<uint32_t>(2 * NR + 2 * NS);
-  uint32_t* ncol[4] = {nar.p, nar.p + NR, nar.p + 2 * NR, nar.p + 2 * NR + NS};
-  {
-    Cols4 c4{};
-    for (int i = 0; i < 4; ++i) {
-      c4.col[i] = cols[i];
-      c4.n[i] = lens[i];
-      c4.narrow[i] = ncol[i];
-    }
-    const uint64_t mx = std::max(NR, NS);
-    if (mx) {
-      dim3 grid(grid_for(mx, 256, X.sm_count * 4), 4);
-      D3G_LAUNCH(X, colstat4_kernel, grid, 256, 0, c4, cs.p);
-    }
-  }
-  ColStat hs[4];
-  X.to_host(hs, cs.p, 4);
-  auto det = [&](int i) { return lens[i] > 0 && hs[i].sample_fail == 0; };
-  auto fits = [&](int i) { return lens[i] == 0 || hs[i].max < (1ull << 32); };
-  bool sx = o->declared_x != 0, sy = o->declared_y != 0, sz = o->declared_z != 0;
-  if (o->natural_keys_auto) {
-    sx = sx || det(0);
-    sy = sy || (det(1) && det(3));
-    sz = sz || det(2);
-  }
-  auto feasible = [&](bool ax, bool ay, bool az) {
-    if (ay && (!fits(1) || !fits(3))) return false;
-    if (az && !fits(2)) return false;
-    if (ax && !fits(0)) return false;
-    return true;
-  };
-  if (!feasible(sx, sy, sz)) {
-    bool dx = o->declared_x != 0, dy = o->declared_y != 0, dz = o->declared_z != 0;
-    if ((sx == dx && sy == dy && sz == dz) || !feasible(dx, dy, dz))
-      throw ConfigError("natural-key skip requires integer values below 2^32");
-    sx = dx;
-    sy = dy;
-    sz = dz;
-  }
-  rep->natural_x = sx;
-  rep->natural_y = sy;
-  rep->natural_z = sz;
-
-  // 4. mapping (map_tables, mapping.cpp:342-420). Natural columns use the
-  // narrowed codes of the statistics pass; the others go through dictionaries.
-  DictBundle D;
-  DBuf<uint32_t> s_y_own, s_z_own, r_y_own, r_x_own;
-  const uint32_t *s_y = ncol[3], *s_z = ncol[2], *r_y = ncol[1], *r_x = ncol[0];
-  uint64_t y_card, z_card, x_card;
-  if (sy) {
-    uint64_t a = NS ? hs[3].max + 1 : 0, b = NR ? hs[1].max + 1 : 0;
-    y_card = std::max(a, b);
-    D.y.identity = true;
-    D.y.card = y_card;
-  } else {
-    s_y_own = X.alloc<uint32_t>(NS);
-    dict_build(X, Sr, NS, D.y, s_y_own.p);
-    s_y = s_y_own.p;
-    y_card = D.y.card;
-  }
-  if (sz) {
-    z_card = NS ? hs[2].max + 1 : 0;
-    D.z.identity = true;
-    D.z.card = z_card;
-  } else {
-    s_z_own = X.alloc<uint32_t>(NS);
-    dict_build(X, Sl, NS, D.z, s_z_own.p);
-    s_z = s_z_own.p;
-    z_card = D.z.card;
-  }
-  // R pass: semi-join filter on y, then x over the survivors. With identity y
-  // the filter is disabled (every R.y < y_card = max over both sides + 1).
-  uint64_t kept = NR;
-  const uint64_t* Rx = Rl;
-  DBuf<uint64_t> rx_kept;
-  if (!sy && NR) {
-    r_y_own = X.alloc<uint32_t>(NR);
-    DBuf<uint32_t> keep = X.alloc<uint32_t>(NR);
-    D3G_LAUNCH(X, dict_lookup_kernel, grid_for(NR, 256), 256, 0, Rr, NR, D.y.keys.p,
-               D.y.slot_code.p, D.y.mask, r_y_own.p, keep.p);
-    DBuf<uint64_t> kpos = X.alloc<uint64_t>(NR + 1);
-    exclusive_scan<uint32_t>(X, keep.p, NR, kpos.p);
-    kept = X.scalar(kpos.p + NR);
-    if (kept != NR) {
-      rx_kept = X.alloc<uint64_t>(kept);
-      DBuf<uint32_t> ry2 = X.alloc<uint32_t>(kept);
-      D3G_LAUNCH(X, compact_kernel<uint64_t>, grid_for(NR, 256), 256, 0, Rl, keep.p, kpos.p, NR,
-                 rx_kept.p);
-      D3G_LAUNCH(X, compact_kernel<uint32_t>, grid_for(NR, 256), 256, 0, r_y_own.p, keep.p,
-                 kpos.p, NR, ry2.p);
-      r_y_own = std::move(ry2);
-      Rx = rx_kept.p;
-    }
-    r_y = r_y_own.p;
-  }
-  rep->dropped_r = NR - kept;
-  if (sx) {
-    x_card = NR ? hs[0].max + 1 : 0;  // over all of R.left (mapping.cpp:404-413)
-    D.x.identity = true;
-    D.x.card = x_card;
-    if (kept != NR) {
-      r_x_own = X.alloc<uint32_t>(kept);
-      if (kept) D3G_LAUNCH(X, narrow_kernel, grid_for(kept, 256), 256, 0, Rx, kept, r_x_own.p);
-      r_x = r_x_own.p;
-    }
-  } else {
-    r_x_own = X.alloc<uint32_t>(kept);
-    dict_build(X, Rx, kept, D.x, r_x_own.p);
-    r_x = r_x_own.p;
-    x_card = D.x.card;
-  }
-  rx_kept.reset();
-  rep->x_card = x_card;
-  rep->y_card = y_card;
-  rep->z_card = z_card;
+  // 3-4. natural keys + mapping
+  Mapped M;
+  map_inputs(X, Rl, Rr, NR, Sl, Sr, NS, o, rep, /*want_kept=*/false, M);
+  const uint64_t kept = M.kept, x_card = M.x_card, y_card = M.y_card, z_card = M.z_card;
+  DictBundle& D = M.D;
   if (classical) {  // intermediate_pairs = bag join size, duplicates included
     DBuf<uint32_t> cnt = X.zeros<uint32_t>(y_card);
-    if (NS) D3G_LAUNCH(X, group_hist_kernel, grid_for(NS, 256), 256, 0, s_y, NS, cnt.p);
+    if (NS) D3G_LAUNCH(X, group_hist_kernel, grid_for(NS, 256), 256, 0, M.s_y, NS, cnt.p);
     DBuf<unsigned long long> bag = X.zeros<unsigned long long>(1);
     if (kept)
-      D3G_LAUNCH(X, bag_from_counts_kernel, grid_for(kept, 256), 256, 0, r_y, kept, cnt.p,
+      D3G_LAUNCH(X, bag_from_counts_kernel, grid_for(kept, 256), 256, 0, M.r_y, kept, cnt.p,
                  bag.p);
     rep->intermediate_pairs = X.scalar(bag.p);
   }
-  if (x_card >= (1ull << 32) || y_card >= (1ull << 32) || z_card >= (1ull << 32))
-    throw ConfigError("code space exceeds 2^32");
   T.mark();  // 3
 
   // 5. CSR (build_csr, relation.cpp:206-258)
   DeviceCsr rx, sz_csr;
-  build_csr_device(X, r_x, r_y, kept, x_card, y_card, rx);
-  r_x_own.reset();
-  r_y_own.reset();
-  build_csr_device(X, s_z, s_y, NS, z_card, y_card, sz_csr);
-  s_z_own.reset();
-  s_y_own.reset();
-  nar.reset();
+  build_csr_device(X, M.r_x, M.r_y, kept, x_card, y_card, rx);
+  build_csr_device(X, M.s_z, M.s_y, NS, z_card, y_card, sz_csr);
+  M.release_codes();
   rep->r_nnz = rx.nnz;
   rep->s_nnz = sz_csr.nnz;
   T.mark();  // 4
 
   // 6. degree statistics (compute_degree_stats, costmodel.cpp:425-438)
-  DBuf<unsigned long long> sc = X.zeros<unsigned long long>(4);  // max_mx, live_x, max_mz, live_z
-  if (x_card)
-    D3G_LAUNCH(X, max_degree_kernel, grid_for(x_card, 256), 256, 0, rx.row_ptr.p, x_card, sc.p,
-               sc.p + 1);
-  if (z_card)
-    D3G_LAUNCH(X, max_degree_kernel, grid_for(z_card, 256), 256, 0, sz_csr.row_ptr.p, z_card,
-               sc.p + 2, sc.p + 3);
-  unsigned long long scal[4];
-  X.to_host(scal, sc.p, 4);
-  const uint64_t max_mx = scal[0], x_live = scal[1], max_mz = scal[2];
-  rep->x_live = x_live;
-  DBuf<unsigned long long> mxh = X.zeros<unsigned long long>(max_mx + 1);
-  DBuf<unsigned long long> mzh = X.zeros<unsigned long long>(max_mz + 1);
-  if (x_card)
-    D3G_LAUNCH(X, degree_hist_kernel, grid_for(x_card, 256), 256, 0, rx.row_ptr.p, x_card,
-               max_mx + 1, mxh.p);
-  if (z_card)
-    D3G_LAUNCH(X, degree_hist_kernel, grid_for(z_card, 256), 256, 0, sz_csr.row_ptr.p, z_card,
-               max_mz + 1, mzh.p);
-  DBuf<uint32_t> dR = X.zeros<uint32_t>(y_card), dS = X.zeros<uint32_t>(y_card);
-  if (rx.nnz)
-    D3G_LAUNCH(X, value_hist_kernel, grid_for(rx.nnz, 256), 256, 0, rx.col.p, rx.nnz, dR.p,
-               (uint32_t)y_card);
-  if (sz_csr.nnz)
-    D3G_LAUNCH(X, value_hist_kernel, grid_for(sz_csr.nnz, 256), 256, 0, sz_csr.col.p, sz_csr.nnz,
-               dS.p, (uint32_t)y_card);
-  {
-    unsigned gb = grid_for(y_card, 1024, 296);
-    DBuf<unsigned long long> parts = X.zeros<unsigned long long>(2 * gb);
-    if (y_card) D3G_LAUNCH(X, outj_kernel, gb, 1024, 0, dR.p, dS.p, y_card, parts.p);
-    std::vector<unsigned long long> hp(2 * gb);
-    X.to_host(hp.data(), parts.p, 2 * gb);
-    unsigned __int128 acc = 0;
-    for (unsigned i = 0; i < gb; ++i)
-      acc += ((unsigned __int128)hp[2 * i + 1] << 64) | hp[2 * i];
-    rep->out_j = acc > (unsigned __int128)std::numeric_limits<uint64_t>::max()
-                     ? std::numeric_limits<uint64_t>::max()
-                     : (uint64_t)acc;
-  }
-  std::vector<uint64_t> hmx(max_mx + 1), hmz(max_mz + 1);
-  X.to_host(reinterpret_cast<unsigned long long*>(hmx.data()), mxh.p, max_mx + 1);
-  X.to_host(reinterpret_cast<unsigned long long*>(hmz.data()), mzh.p, max_mz + 1);
+  DegreeStats G;
+  degree_stats(X, rx, sz_csr, y_card, rep, G);
+  const uint64_t max_mx = G.max_mx, x_live = G.x_live, max_mz = G.max_mz;
+  const std::vector<uint64_t>& hmx = G.hmx;
+  DBuf<uint32_t>& dR = G.dR;
   T.mark();  // 5
 
   // 7. f2 decisions per degree value (policy.cpp), then the partition
-  std::vector<uint8_t> table(max_mz + 1, 0);
-  int pforce = (classical || o->force == D3G_SPARSE_ONLY) ? D3G_SPARSE_ONLY
-               : o->force == D3G_DENSE_ONLY ? D3G_DENSE_ONLY
-                                            : D3G_HYBRID;
-  uint64_t evals = 0;
-  if (const char* dump = std::getenv("D3G_DUMP_F2")) {  // debugging aid: the f2 inputs
-    if (FILE* f = std::fopen(dump, "wb")) {
-      uint64_t hdr[6] = {max_mx + 1, max_mz + 1, x_card, y_card, z_card, rep->out_j};
-      std::fwrite(hdr, 8, 6, f);
-      std::fwrite(hmx.data(), 8, max_mx + 1, f);
-      std::fwrite(hmz.data(), 8, max_mz + 1, f);
-      std::fclose(f);
-    }
-  }
-  d3g_f2_decide(hmx.data(), max_mx + 1, hmz.data(), max_mz + 1, x_card, y_card, z_card,
-                rep->out_j, c, pforce, table.data(), &evals);
-  rep->f2_evaluations = evals;
-  DBuf<uint8_t> dtable = X.alloc<uint8_t>(max_mz + 1);
-  X.to_device(dtable.p, table.data(), max_mz + 1);
-  DBuf<uint32_t> isd = X.alloc<uint32_t>(z_card), iss = X.alloc<uint32_t>(z_card);
-  if (z_card)
-    D3G_LAUNCH(X, dense_flag_kernel, grid_for(z_card, 256), 256, 0, sz_csr.row_ptr.p, z_card,
-               dtable.p, max_mz + 1, isd.p, iss.p);
-  DBuf<uint64_t> pd = X.alloc<uint64_t>(z_card + 1), psp = X.alloc<uint64_t>(z_card + 1);
-  exclusive_scan<uint32_t>(X, isd.p, z_card, pd.p);
-  exclusive_scan<uint32_t>(X, iss.p, z_card, psp.p);
-  const uint64_t n_dense = X.scalar(pd.p + z_card), n_sparse = X.scalar(psp.p + z_card);
-  rep->dense_z = n_dense;
-  rep->sparse_z = n_sparse;
-  const uint64_t row_words = ((y_card + c->w - 1) / c->w * c->w) / 64;
-  rep->panel_bytes = n_dense * row_words * 8;
+  const int pforce = (classical || o->force == D3G_SPARSE_ONLY) ? D3G_SPARSE_ONLY
+                     : o->force == D3G_DENSE_ONLY ? D3G_DENSE_ONLY
+                                                  : D3G_HYBRID;
+  Split P;
+  DBuf<uint64_t> pd, psp;
+  f2_split(X, sz_csr, G, x_card, y_card, c, pforce, rep, P, &pd, &psp);
+  const uint64_t n_dense = P.n_dense, n_sparse = P.n_sparse;
   DBuf<uint32_t> dense_ids = X.alloc<uint32_t>(n_dense), sparse_ids = X.alloc<uint32_t>(n_sparse);
   if (z_card) {
-    D3G_LAUNCH(X, index_compact_kernel, grid_for(z_card, 256), 256, 0, isd.p, pd.p, z_card,
+    D3G_LAUNCH(X, index_compact_kernel, grid_for(z_card, 256), 256, 0, P.isd.p, pd.p, z_card,
                dense_ids.p);
-    D3G_LAUNCH(X, index_compact_kernel, grid_for(z_card, 256), 256, 0, iss.p, psp.p, z_card,
+    D3G_LAUNCH(X, index_compact_kernel, grid_for(z_card, 256), 256, 0, P.iss.p, psp.p, z_card,
                sparse_ids.p);
   }
-  isd.reset();
-  iss.reset();
+  P.isd.reset();
+  P.iss.reset();
   pd.reset();
   psp.reset();
   // sparse side: y-major CSR over compact sparse indices
@@ -1420,6 +1498,224 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
     rep->pairs_classical = rep->out_p;
     rep->ms_classical = T.ms(2, 9);
   }
+  rep->peak_bytes = X.peak_bytes - base_live;
+  rep->gpu_launches = X.launches;
+  rep->d2h_bytes += X.d2h_bytes;
+  X.reserve_for(X.peak_bytes);
+}
+
+// ---------------------------------------------------------------------------
+// join_aggregate_both (engine.cpp:537-722); kernels and the parity argument in
+// aggregate.cuh.
+// Stable grouping of rows by a u32 code: permutation (input order within a
+// code) and row_ptr[n_rows + 1].
+void stable_group(Ctx& X, const uint32_t* code, uint64_t n, uint64_t n_rows, DBuf<uint32_t>& perm,
+                  DBuf<uint64_t>& row_ptr) {
+  using namespace d3g;
+  DBuf<uint64_t> key = X.alloc<uint64_t>(n);
+  perm = X.alloc<uint32_t>(n);
+  if (n) D3G_LAUNCH(X, code_key_kernel, grid_for(n, 256), 256, 0, code, n, key.p, perm.p);
+  radix_sort(X, key.p, perm.p, n, bits_for(n_rows ? n_rows - 1 : 0));
+  DBuf<uint32_t> cnt = X.zeros<uint32_t>(n_rows);
+  if (n) D3G_LAUNCH(X, count_codes_kernel, grid_for(n, 256), 256, 0, code, n, cnt.p);
+  row_ptr = X.alloc<uint64_t>(n_rows + 1);
+  exclusive_scan<uint32_t>(X, cnt.p, n_rows, row_ptr.p);
+}
+
+void join_aggregate_impl(Ctx& X, const d3g_valued_table* r, const d3g_valued_table* s,
+                         int combine, int agg, const d3g_consts* c, const d3g_opts* o,
+                         d3g_report* rep, d3g_agg_pairs* out) {
+  using namespace d3g;
+  if (o->threads < 1) throw ConfigError("threads must be >= 1");
+  if (o->force == D3G_CLASSICAL) throw ConfigError("join-aggregate always runs the mapped pipeline");
+  if (combine < 0 || combine > 4) throw ConfigError("unknown combine function");
+  if (agg < 0 || agg > 4) throw ConfigError("unknown aggregate function");
+  if (c->w == 0 || c->w % 64 != 0) throw ConfigError("block width W must be a positive multiple of 64");
+  if ((r->base.n && !r->values) || (s->base.n && !s->values))
+    throw ConfigError("value column length does not match table length");
+  std::memset(rep, 0, sizeof(*rep));
+  X.launches = 0;
+  X.d2h_bytes = 0;
+  X.budget = o->memory_budget_bytes ? o->memory_budget_bytes : (3ull << 30);
+  const uint64_t base_live = X.live_bytes;
+  X.peak_bytes = X.live_bytes;
+  Timer T(X);
+  T.mark();  // 0
+  std::snprintf(rep->strategy, sizeof(rep->strategy), "hybrid");
+  const uint64_t NR = r->base.n, NS = s->base.n;
+  rep->r_rows = NR;
+  rep->s_rows = NS;
+  const bool materialize = out != nullptr && !o->count_only;
+  rep->materialized = materialize;
+
+  // inputs and values resident in HBM (caller orientation: no swap)
+  DBuf<uint64_t> hb[4];
+  DBuf<double> hv[2];
+  const uint64_t *Rl = r->base.left, *Rr = r->base.right, *Sl = s->base.left, *Sr = s->base.right;
+  const double *Rv = r->values, *Sv = s->values;
+  if (!r->base.on_device) {
+    hb[0] = X.alloc<uint64_t>(NR);
+    hb[1] = X.alloc<uint64_t>(NR);
+    hv[0] = X.alloc<double>(NR);
+    X.to_device(hb[0].p, Rl, NR);
+    X.to_device(hb[1].p, Rr, NR);
+    X.to_device(hv[0].p, Rv, NR);
+    Rl = hb[0].p;
+    Rr = hb[1].p;
+    Rv = hv[0].p;
+    rep->h2d_bytes += NR * 24;
+  }
+  if (!s->base.on_device) {
+    hb[2] = X.alloc<uint64_t>(NS);
+    hb[3] = X.alloc<uint64_t>(NS);
+    hv[1] = X.alloc<double>(NS);
+    X.to_device(hb[2].p, Sl, NS);
+    X.to_device(hb[3].p, Sr, NS);
+    X.to_device(hv[1].p, Sv, NS);
+    Sl = hb[2].p;
+    Sr = hb[3].p;
+    Sv = hv[1].p;
+    rep->h2d_bytes += NS * 24;
+  }
+  T.mark();  // 1
+
+  // map_with_fallback; the R values follow the surviving rows (m.r_kept)
+  Mapped M;
+  map_inputs(X, Rl, Rr, NR, Sl, Sr, NS, o, rep, /*want_kept=*/true, M);
+  const uint64_t kept = M.kept, x_card = M.x_card, y_card = M.y_card, z_card = M.z_card;
+  T.mark();  // 2
+
+  // collapsed matrices drive the per-z density decision only (engine.cpp:570-577)
+  DeviceCsr rx, sz_csr;
+  build_csr_device(X, M.r_x, M.r_y, kept, x_card, y_card, rx);
+  build_csr_device(X, M.s_z, M.s_y, NS, z_card, y_card, sz_csr);
+  rep->r_nnz = rx.nnz;
+  rep->s_nnz = sz_csr.nnz;
+  DegreeStats G;
+  degree_stats(X, rx, sz_csr, y_card, rep, G);
+  rep->out_j_estimate = rep->out_j;
+  T.mark();  // 3
+
+  const int pforce = o->force == D3G_SPARSE_ONLY ? D3G_SPARSE_ONLY
+                     : o->force == D3G_DENSE_ONLY ? D3G_DENSE_ONLY
+                                                  : D3G_HYBRID;
+  Split P;
+  f2_split(X, sz_csr, G, x_card, y_card, c, pforce, rep, P);
+  rx = DeviceCsr();
+  sz_csr = DeviceCsr();
+  // valued CSRs (build_valued_csr, engine.cpp:148-171): duplicates kept,
+  // stable, one value per entry
+  DBuf<uint32_t> rperm, sperm;
+  DBuf<uint64_t> rptr, sptr;
+  stable_group(X, M.r_x, kept, x_card, rperm, rptr);
+  stable_group(X, M.s_y, NS, y_card, sperm, sptr);
+  DBuf<uint32_t> ry = X.alloc<uint32_t>(kept), sz = X.alloc<uint32_t>(NS);
+  DBuf<double> rv = X.alloc<double>(kept), sv = X.alloc<double>(NS);
+  if (kept) {
+    D3G_LAUNCH(X, gather_u32_kernel, grid_for(kept, 256), 256, 0, M.r_y, rperm.p, kept, ry.p);
+    D3G_LAUNCH(X, gather_f64_kernel, grid_for(kept, 256), 256, 0, Rv, rperm.p,
+               M.r_kept.p ? M.r_kept.p : (const uint32_t*)nullptr, kept, rv.p);
+  }
+  if (NS) {
+    D3G_LAUNCH(X, gather_u32_kernel, grid_for(NS, 256), 256, 0, M.s_z, sperm.p, NS, sz.p);
+    D3G_LAUNCH(X, gather_f64_kernel, grid_for(NS, 256), 256, 0, Sv, sperm.p,
+               (const uint32_t*)nullptr, NS, sv.p);
+  }
+  rperm.reset();
+  sperm.reset();
+  M.release_codes();
+  M.r_kept.reset();
+  T.mark();  // 4
+
+  // candidates per x, then chunks of x whose candidates fit the buffers
+  DBuf<uint64_t> cand = X.alloc<uint64_t>(x_card), coff = X.alloc<uint64_t>(x_card + 1);
+  if (x_card)
+    D3G_LAUNCH(X, agg_cand_kernel, grid_for(x_card, 256), 256, 0, rptr.p, ry.p, sptr.p, x_card,
+               cand.p);
+  exclusive_scan<uint64_t>(X, cand.p, x_card, coff.p);
+  cand.reset();
+  std::vector<uint64_t> hoff(x_card + 1);
+  X.to_host(reinterpret_cast<unsigned long long*>(hoff.data()),
+            reinterpret_cast<unsigned long long*>(coff.p), x_card + 1);
+  rep->intermediate_pairs = hoff[x_card];  // bag join size
+  uint64_t max_c = 0;
+  for (uint64_t x = 0; x < x_card; ++x) max_c = std::max(max_c, hoff[x + 1] - hoff[x]);
+  const uint64_t cap_chunk = std::max<uint64_t>(max_c, 1ull << 25);
+  DBuf<uint64_t> key = X.alloc<uint64_t>(std::min(cap_chunk, std::max<uint64_t>(hoff[x_card], 1)));
+  const uint64_t kcap = key.n;
+  DBuf<double> val = X.alloc<double>(kcap);
+  DBuf<uint32_t> perm = X.alloc<uint32_t>(kcap), head = X.alloc<uint32_t>(kcap);
+  DBuf<uint64_t> hpos = X.alloc<uint64_t>(kcap + 1);
+  DBuf<uint32_t> starts = X.alloc<uint32_t>(kcap);
+  DBuf<uint32_t> ox, oz;
+  DBuf<double> ov;
+  if (materialize) {
+    ox = X.alloc<uint32_t>(out->cap);
+    oz = X.alloc<uint32_t>(out->cap);
+    ov = X.alloc<double>(out->cap);
+  }
+  DBuf<unsigned long long> dense_pairs = X.zeros<unsigned long long>(1);
+  DBuf<unsigned int> too_many = X.zeros<unsigned int>(1);
+  uint64_t total = 0;
+  for (uint64_t x0 = 0; x0 < x_card;) {
+    uint64_t x1 = x0;
+    while (x1 < x_card && hoff[x1 + 1] - hoff[x0] <= kcap) ++x1;
+    const uint64_t n = hoff[x1] - hoff[x0];
+    if (n) {
+      D3G_LAUNCH(X, agg_enum_kernel, grid_for((x1 - x0) * 32, 256), 256, 0, x0, x1, coff.p, rptr.p,
+                 ry.p, rv.p, sptr.p, sz.p, sv.p, combine, key.p, val.p);
+      D3G_LAUNCH(X, iota_kernel, grid_for(n, 256), 256, 0, perm.p, n);
+      radix_sort(X, key.p, perm.p, n, 32 + bits_for(x1 - x0 - 1));
+      D3G_LAUNCH(X, seg_head_kernel, grid_for(n, 256), 256, 0, key.p, n, head.p);
+      exclusive_scan<uint32_t>(X, head.p, n, hpos.p);
+      const uint64_t nseg = X.scalar(hpos.p + n);
+      D3G_LAUNCH(X, index_compact_kernel, grid_for(n, 256), 256, 0, head.p, hpos.p, n, starts.p);
+      if (materialize && total + nseg > out->cap)
+        throw ResourceError("output buffer holds " + std::to_string(out->cap) +
+                            " aggregate rows, need more");
+      D3G_LAUNCH(X, agg_fold_kernel, grid_for(nseg, 256), 256, 0, key.p, perm.p, val.p, starts.p,
+                 nseg, n, x0, agg, P.isd.p, materialize ? ox.p + total : nullptr,
+                 materialize ? oz.p + total : nullptr, materialize ? ov.p + total : nullptr,
+                 dense_pairs.p, too_many.p);
+      total += nseg;
+    }
+    x0 = x1;
+  }
+  if (X.scalar(too_many.p)) throw ResourceError("count aggregate exceeds exact integer range");
+  rep->pairs_dense = X.scalar(dense_pairs.p);
+  rep->pairs_sparse = total - rep->pairs_dense;
+  rep->out_p = total;
+  if (materialize) {
+    DBuf<uint64_t> dx, dz;
+    uint64_t* px = out->x;
+    uint64_t* pz = out->z;
+    if (!out->on_device) {
+      dx = X.alloc<uint64_t>(total);
+      dz = X.alloc<uint64_t>(total);
+      px = dx.p;
+      pz = dz.p;
+    }
+    if (total)
+      D3G_LAUNCH(X, decode_pairs_kernel, grid_for(total, 256), 256, 0, ox.p, oz.p, total,
+                 rev_or_null(M.D.x), rev_or_null(M.D.z), 0, px, pz);
+    if (out->on_device) {
+      D3G_CUDA(cudaMemcpyAsync(out->values, ov.p, total * 8, cudaMemcpyDeviceToDevice, X.stream));
+    } else if (total) {
+      D3G_CUDA(cudaMemcpyAsync(out->x, dx.p, total * 8, cudaMemcpyDeviceToHost, X.stream));
+      D3G_CUDA(cudaMemcpyAsync(out->z, dz.p, total * 8, cudaMemcpyDeviceToHost, X.stream));
+      D3G_CUDA(cudaMemcpyAsync(out->values, ov.p, total * 8, cudaMemcpyDeviceToHost, X.stream));
+      rep->d2h_bytes += total * 24;
+    }
+    out->n = total;
+  }
+  T.mark();  // 5
+  X.sync();
+  rep->ms_h2d = T.ms(0, 1);
+  rep->ms_map = T.ms(1, 2);
+  rep->ms_csr = T.ms(2, 3);
+  rep->ms_partition = T.ms(3, 4);
+  rep->ms_sparse = T.ms(4, 5);
+  rep->ms_total = T.ms(0, 5);
   rep->peak_bytes = X.peak_bytes - base_live;
   rep->gpu_launches = X.launches;
   rep->d2h_bytes += X.d2h_bytes;
@@ -1747,6 +2043,18 @@ int d3g_generate(d3g_ctx* ctx, int cfg, int side, uint64_t lo, uint64_t hi, uint
 }
 
 uint64_t d3g_cfg_rows(int cfg) { return d3g::cfg_rows(cfg); }
+
+int d3g_join_aggregate(d3g_ctx* ctx, const d3g_valued_table* r, const d3g_valued_table* s,
+                       int combine, int agg, const d3g_consts* c, const d3g_opts* o,
+                       d3g_report* rep, d3g_agg_pairs* out) {
+  d3g::Ctx& X = ctx->c;
+  int rc = guarded([&] {
+    D3G_CUDA(cudaSetDevice(X.device));
+    join_aggregate_impl(X, r, s, combine, agg, c, o, rep, out);
+  });
+  X.budget = 0;  // the memory budget is scoped to one call
+  return rc;
+}
 
 // ---- table files ------------------------------------------------------------
 int d3g_detect_format(const char* path, int requested) {

@@ -252,7 +252,8 @@ EXPORTED = ["d3g_ctx_create", "d3g_ctx_destroy", "d3g_last_error", "d3g_version"
             "d3g_opts_default", "d3g_join_project", "d3g_build_csr", "d3g_sparse_bmm_csr",
             "d3g_dense_ec_rows", "d3g_generate", "d3g_cfg_rows", "d3g_ctx_device",
             "d3g_f3_threshold", "d3g_f1", "d3g_f2_decide", "d3g_alu_peak",
-            "d3g_detect_format", "d3g_binary_rows", "d3g_read_binary", "d3g_save_pairs"]
+            "d3g_detect_format", "d3g_binary_rows", "d3g_read_binary", "d3g_save_pairs",
+            "d3g_join_aggregate"]
 
 _lib = None
 
@@ -293,6 +294,9 @@ def lib():
         L.d3g_f2_decide.argtypes = [U64P, C.c_uint64, U64P, C.c_uint64, C.c_uint64, C.c_uint64,
                                     C.c_uint64, C.c_uint64, C.POINTER(_Consts), C.c_int,
                                     C.POINTER(C.c_uint8), U64P]
+        L.d3g_join_aggregate.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int,
+                                         C.POINTER(_Consts), C.POINTER(_Opts), C.POINTER(_Report),
+                                         C.c_void_p]
         L.d3g_detect_format.argtypes = [C.c_char_p, C.c_int]
         L.d3g_binary_rows.argtypes = [C.c_char_p, U64P]
         L.d3g_read_binary.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p, C.c_void_p, C.c_uint64]
@@ -742,3 +746,120 @@ def save_result(out: "JoinProjectOutput", path, fmt: FileFormat = FileFormat.aut
     save_table of the decoded (x, z) pairs."""
     raw = result_to_raw(out)
     save_table(RawTable(raw.raw_x, raw.raw_z), path, fmt, ctx)
+
+
+# ---------------------------------------------------------------------------
+# Join-aggregate (P/include/dim3/engine.hpp:126-154, P/src/engine.cpp:537-722)
+class AggFn(enum.IntEnum):
+    sum = 0
+    count = 1
+    min = 2
+    max = 3
+    avg = 4
+
+
+class CombineFn(enum.IntEnum):
+    multiply = 0
+    add = 1
+    abs_diff = 2
+    left = 3
+    right = 4
+
+
+def agg_from_name(name: str) -> "AggFn | None":
+    return AggFn.__members__.get(name)
+
+
+def combine_from_name(name: str) -> "CombineFn | None":
+    return CombineFn.__members__.get(name)
+
+
+class ValuedTable:
+    """dim3::ValuedTable (relation.hpp:49-53): a RawTable plus one double per
+    row (numpy array, or a CUDA float64 tensor when the table is on the
+    device)."""
+
+    def __init__(self, base: RawTable, values):
+        self.base = base
+        if _is_cuda(values):
+            if values.dtype.itemsize != 8 or not values.is_contiguous() or \
+                    not values.dtype.is_floating_point:
+                raise FormatError("device values must be a contiguous float64 tensor")
+            self.values = values
+        else:
+            self.values = np.ascontiguousarray(values, dtype=np.float64)
+        if _length(self.values) != base.size():
+            raise ConfigError("value column length does not match table length")
+
+    def size(self) -> int:
+        return self.base.size()
+
+
+class _ValuedTable(C.Structure):
+    _fields_ = [("base", _Table), ("values", C.c_void_p)]
+
+
+class _AggPairs(C.Structure):
+    _fields_ = [("x", U64P), ("z", U64P), ("values", C.c_void_p), ("cap", C.c_uint64),
+                ("n", C.c_uint64), ("on_device", C.c_int32), ("pad", C.c_int32)]
+
+
+@dataclass
+class AggregateResult:
+    """AggregateResult (engine.hpp:139-146): base = the (x, z) pairs (raw
+    values, already decoded), values[i] belongs to pair i."""
+    base: ResultSet
+    values: np.ndarray
+    report: ExecutionReport
+
+
+def _valued_struct(t: ValuedTable) -> _ValuedTable:
+    base = _table_struct(t.base)
+    if t.base.on_device != _is_cuda(t.values):
+        raise ConfigError("values must live where the table lives (host or device)")
+    vp = C.c_void_p(t.values.data_ptr()) if _is_cuda(t.values) else C.c_void_p(t.values.ctypes.data)
+    return _ValuedTable(base, vp)
+
+
+def join_aggregate_both(r: ValuedTable, s: ValuedTable, combine: CombineFn, agg: AggFn,
+                        cfg: EngineConfig, c: CostConstants,
+                        ctx: Context | None = None) -> AggregateResult:
+    """dim3::join_aggregate_both on the GPU, caller orientation (no swap).
+    Values are bit-identical to the reference's; force=classical raises
+    ConfigError like the reference."""
+    if cfg.threads < 1:
+        raise ConfigError("threads must be >= 1")
+    if cfg.force == Strategy.classical:
+        raise ConfigError("join-aggregate always runs the mapped pipeline")
+    ctx = ctx or default_context()
+    rt, st = _valued_struct(r), _valued_struct(s)
+    cs, op = _consts(c), _opts(cfg)
+    rep = _Report()
+    out_p = None
+    ox = oz = ov = None
+    if not cfg.count_only:
+        cnt_op = _opts(cfg)
+        cnt_op.count_only = 1
+        _check(lib().d3g_join_aggregate(ctx.handle, C.byref(rt), C.byref(st), int(combine),
+                                        int(agg), C.byref(cs), C.byref(cnt_op), C.byref(rep),
+                                        None))
+        n = int(rep.out_p)
+        ox = np.zeros(max(n, 1), dtype=np.uint64)
+        oz = np.zeros(max(n, 1), dtype=np.uint64)
+        ov = np.zeros(max(n, 1), dtype=np.float64)
+        outs = _AggPairs(ox.ctypes.data_as(U64P), oz.ctypes.data_as(U64P),
+                         C.c_void_p(ov.ctypes.data), n, 0, 0, 0)
+        out_p = C.byref(outs)
+    _check(lib().d3g_join_aggregate(ctx.handle, C.byref(rt), C.byref(st), int(combine), int(agg),
+                                    C.byref(cs), C.byref(op), C.byref(rep), out_p))
+    report = _to_report(rep)
+    n = report.out_p
+    if cfg.count_only:
+        return AggregateResult(ResultSet(count=n, materialized=False), np.zeros(0), report)
+    return AggregateResult(ResultSet(count=n, materialized=True, raw_x=ox[:n], raw_z=oz[:n]),
+                           ov[:n], report)
+
+
+def aggregate_to_raw(out: AggregateResult) -> ResultSet:
+    """aggregate_to_raw (engine.cpp:530-532): pairs are already raw."""
+    return out.base
