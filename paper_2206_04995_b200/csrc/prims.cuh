@@ -9,32 +9,11 @@
 namespace d3g {
 
 // ---------------------------------------------------------------------------
-// Exclusive scan: out[i] = sum(in[0..i)), out[n] = total. Three phases:
-// per-tile reduce, recursive scan of tile sums, per-tile scan with offset.
+// Exclusive scan: out[i] = sum(in[0..i)), out[n] = total; one tile in one
+// block, larger inputs in one single-pass launch (decoupled look-back).
 constexpr int kScanThreads = 512;
 constexpr int kScanItems = 8;
 constexpr int kScanTile = kScanThreads * kScanItems;
-
-template <class Tin>
-__global__ void __launch_bounds__(kScanThreads)
-scan_reduce_kernel(const Tin* __restrict__ in, uint64_t n, uint64_t* __restrict__ partial) {
-  __shared__ uint64_t warp_tot[kScanThreads / 32];
-  uint64_t base = (uint64_t)blockIdx.x * kScanTile;
-  uint64_t s = 0;
-#pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    uint64_t i = base + (uint64_t)k * kScanThreads + threadIdx.x;
-    if (i < n) s += (uint64_t)in[i];
-  }
-  s = warp_sum(s);
-  if (lane_id() == 0) warp_tot[threadIdx.x >> 5] = s;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    uint64_t v = threadIdx.x < kScanThreads / 32 ? warp_tot[threadIdx.x] : 0;
-    v = warp_sum(v);
-    if (threadIdx.x == 0) partial[blockIdx.x] = v;
-  }
-}
 
 // Block-wide exclusive scan of one value per thread; returns the prefix and
 // writes the block total to *total.
@@ -96,6 +75,75 @@ scan_tile_kernel(const Tin* __restrict__ in, uint64_t n, const uint64_t* __restr
     out[n] = tot + (offsets ? offsets[blockIdx.x] : 0);
 }
 
+// Single-pass exclusive scan with decoupled look-back: tiles take tickets in
+// launch order, publish their aggregate, and warp 0 of each tile walks back
+// over its predecessors 32 at a time until it meets an inclusive prefix.
+// state[t] = flag << 62 | value (flag 1: aggregate, 2: inclusive prefix);
+// state[tiles] holds the ticket counter. One launch instead of three.
+template <class Tin>
+__global__ void __launch_bounds__(kScanThreads)
+scan_onepass_kernel(const Tin* __restrict__ in, uint64_t n, uint64_t* __restrict__ out,
+                    unsigned long long* __restrict__ state, uint32_t tiles) {
+  constexpr unsigned long long kAgg = 1ull << 62, kPre = 2ull << 62, kVal = (1ull << 62) - 1;
+  __shared__ uint32_t s_tile;
+  __shared__ uint64_t s_excl;
+  if (threadIdx.x == 0)
+    s_tile = atomicAdd(reinterpret_cast<unsigned int*>(&state[tiles]), 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint64_t base = (uint64_t)tile * kScanTile + (uint64_t)threadIdx.x * kScanItems;
+  uint64_t vals[kScanItems];
+  uint64_t sum = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const uint64_t i = base + k;
+    vals[k] = i < n ? (uint64_t)in[i] : 0;
+    sum += vals[k];
+  }
+  uint64_t tot;
+  const uint64_t local = block_exclusive_scan(sum, &tot);
+  if (threadIdx.x == 0) {
+    if (tile == 0) {
+      atomicExch(&state[0], kPre | tot);
+      s_excl = 0;
+    } else {
+      atomicExch(&state[tile], kAgg | tot);
+    }
+  }
+  if (tile > 0 && threadIdx.x < 32) {
+    const uint32_t lane = threadIdx.x;
+    uint64_t excl = 0;
+    int64_t t = (int64_t)tile - 1;
+    for (;;) {
+      const int64_t my = t - (int64_t)lane;
+      unsigned long long st = kPre;  // before tile 0: an empty prefix
+      if (my >= 0) {
+        do {
+          st = atomicAdd(&state[my], 0ull);
+        } while ((st >> 62) == 0);
+      }
+      const unsigned pre = __ballot_sync(0xffffffffu, (st >> 62) == 2);
+      const int first = pre ? __ffs(pre) - 1 : 32;
+      excl += warp_sum((uint64_t)((int)lane <= first && my >= 0 ? (st & kVal) : 0));
+      if (pre) break;
+      t -= 32;
+    }
+    if (lane == 0) {
+      atomicExch(&state[tile], kPre | (excl + tot));
+      s_excl = excl;
+    }
+  }
+  __syncthreads();
+  uint64_t run = s_excl + local;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const uint64_t i = base + k;
+    if (i < n) out[i] = run;
+    run += vals[k];
+  }
+  if (tile == tiles - 1 && threadIdx.x == blockDim.x - 1) out[n] = s_excl + tot;
+}
+
 // out must hold n + 1 entries. Returns nothing; out[n] is the total.
 template <class Tin>
 void exclusive_scan(Ctx& ctx, const Tin* in, uint64_t n, uint64_t* out) {
@@ -109,13 +157,10 @@ void exclusive_scan(Ctx& ctx, const Tin* in, uint64_t n, uint64_t* out) {
                (const uint64_t*)nullptr, out);
     return;
   }
-  DBuf<uint64_t> partial = ctx.alloc<uint64_t>(tiles);
-  DBuf<uint64_t> offs = ctx.alloc<uint64_t>(tiles + 1);
-  D3G_LAUNCH(ctx, scan_reduce_kernel<Tin>, (unsigned)tiles, kScanThreads, 0, in, n,
-             partial.p);
-  exclusive_scan<uint64_t>(ctx, partial.p, tiles, offs.p);
-  D3G_LAUNCH(ctx, scan_tile_kernel<Tin>, (unsigned)tiles, kScanThreads, 0, in, n,
-             (const uint64_t*)offs.p, out);
+  if (tiles >= (1ull << 31)) throw ResourceError("exclusive_scan: too many tiles");
+  DBuf<unsigned long long> state = ctx.zeros<unsigned long long>(tiles + 1);
+  D3G_LAUNCH(ctx, scan_onepass_kernel<Tin>, (unsigned)tiles, kScanThreads, 0, in, n, out,
+             state.p, (uint32_t)tiles);
 }
 
 // ---------------------------------------------------------------------------
