@@ -998,6 +998,51 @@ void classical_impl(Ctx& X, const uint64_t* Rl, const uint64_t* Rr, uint64_t NR,
 }
 
 // ---------------------------------------------------------------------------
+// Self-join detection: R and S element-wise identical (cfg2's S := R). Blocks
+// stop at the first difference any of them has seen.
+__global__ void tables_differ_kernel(const uint64_t* __restrict__ a0, const uint64_t* __restrict__ b0,
+                                     const uint64_t* __restrict__ a1, const uint64_t* __restrict__ b1,
+                                     uint64_t n, unsigned int* __restrict__ differ) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += stride * 4) {
+    bool d = false;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint64_t i = base + k * stride + threadIdx.x;
+      if (i < n) d |= (a0[i] != b0[i]) | (a1[i] != b1[i]);
+    }
+    if (__syncthreads_or(d)) {  // block-uniform exits only
+      if (threadIdx.x == 0) atomicExch(differ, 1u);
+      return;
+    }
+    if (__syncthreads_or(*(volatile unsigned int*)differ != 0)) return;
+  }
+}
+
+bool tables_identical(Ctx& X, const uint64_t* Rl, const uint64_t* Rr, const uint64_t* Sl,
+                      const uint64_t* Sr, uint64_t NR, uint64_t NS) {
+  using namespace d3g;
+  if (NR != NS || NR == 0) return false;
+  if (Rl == Sl && Rr == Sr) return true;
+  DBuf<unsigned int> differ = X.zeros<unsigned int>(1);
+  D3G_LAUNCH(X, tables_differ_kernel, grid_for(NR, 256, X.sm_count * 4), 256, 0, Rl, Sl, Rr, Sr,
+             NR, differ.p);
+  return X.scalar(differ.p) == 0;
+}
+
+void copy_csr(Ctx& X, const d3g::DeviceCsr& a, d3g::DeviceCsr& b) {
+  b.n_rows = a.n_rows;
+  b.n_cols = a.n_cols;
+  b.nnz = a.nnz;
+  b.row_ptr = X.alloc<uint64_t>(a.n_rows + 1);
+  b.col = X.alloc<uint32_t>(a.nnz);
+  D3G_CUDA(cudaMemcpyAsync(b.row_ptr.p, a.row_ptr.p, (a.n_rows + 1) * 8, cudaMemcpyDeviceToDevice,
+                           X.stream));
+  if (a.nnz)
+    D3G_CUDA(cudaMemcpyAsync(b.col.p, a.col.p, a.nnz * 4, cudaMemcpyDeviceToDevice, X.stream));
+}
+
+// ---------------------------------------------------------------------------
 // Pipeline stages shared by join_project and join_aggregate_both.
 
 // Steps 3-4: natural-key resolution (engine.cpp:25-50, mapping.cpp:281-338)
@@ -1344,6 +1389,8 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   }
 
   // 3-4. natural keys + mapping
+  const bool self_join = std::getenv("D3G_NO_SELFJOIN") == nullptr &&
+                         tables_identical(X, Rl, Rr, Sl, Sr, NR, NS);
   Mapped M;
   map_inputs(X, Rl, Rr, NR, Sl, Sr, NS, o, rep, /*want_kept=*/false, M);
   const uint64_t kept = M.kept, x_card = M.x_card, y_card = M.y_card, z_card = M.z_card;
@@ -1359,10 +1406,14 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   }
   T.mark();  // 3
 
-  // 5. CSR (build_csr, relation.cpp:206-258)
+  // 5. CSR (build_csr, relation.cpp:206-258). A self-join (S identical to R)
+  // maps both sides identically, so S-by-z is R-by-x: built once.
   DeviceCsr rx, sz_csr;
   build_csr_device(X, M.r_x, M.r_y, kept, x_card, y_card, rx);
-  build_csr_device(X, M.s_z, M.s_y, NS, z_card, y_card, sz_csr);
+  if (self_join && kept == NR && x_card == z_card)
+    copy_csr(X, rx, sz_csr);
+  else
+    build_csr_device(X, M.s_z, M.s_y, NS, z_card, y_card, sz_csr);
   M.release_codes();
   rep->r_nnz = rx.nnz;
   rep->s_nnz = sz_csr.nnz;

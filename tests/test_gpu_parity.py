@@ -284,3 +284,21 @@ def test_cfg5_full_pipeline_x_range_matches_reference(cold, monkeypatch):
             (blk["count"][b], blk["sum"][b], blk["xor"][b])
     del rl, rr, sl, sr
     torch.cuda.empty_cache()
+
+
+def test_self_join_reuses_the_csr_and_matches(monkeypatch):
+    """S element-wise identical to R (cfg2's S := R): the engine builds the
+    CSR once; sets, split and report equal the general path and the oracle
+    (dictionary and natural keys)."""
+    rng = SplitMix64(513)
+    for _ in range(6):
+        r, _s = random_instance(rng)
+        s = (r[0].copy(), r[1].copy())
+        want = oracle_pairs(r, s)
+        monkeypatch.delenv("D3G_NO_SELFJOIN", raising=False)
+        a = _run(r, s, d3.Strategy.hybrid)
+        monkeypatch.setenv("D3G_NO_SELFJOIN", "1")
+        b = _run(r, s, d3.Strategy.hybrid)
+        assert pair_set(a.result.raw_x, a.result.raw_z) == want
+        for k in ("out_p", "pairs_dense", "pairs_sparse", "dense_z", "s_nnz", "r_nnz", "out_j"):
+            assert getattr(a.report, k) == getattr(b.report, k), k
