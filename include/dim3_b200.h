@@ -120,6 +120,11 @@ typedef struct {
   /* classical branch (hash_join_dedup, P/src/classical.cpp:111-210) */
   uint64_t pairs_classical, intermediate_pairs;
   double ms_classical;
+  /* DenseEC P1 (hot bit-sliced pass) alone: CUDA-event time of its launches
+   * and their algorithmic shared-memory bytes (one 512 B LDS.128 per
+   * (row, batch, slice read)), the roofline inputs. */
+  double ms_dense_hot;
+  uint64_t hot_lds_bytes;
 } d3g_report;
 
 /* Materialized output: caller-owned host (or device, on_device != 0)
@@ -197,6 +202,10 @@ uint64_t d3g_cfg_rows(int cfg);
 /* Measured 32-bit logic-op throughput of this device (LOP3 chains, ops/s);
  * the denominator of the DenseEC integer-pipe roofline. */
 int d3g_alu_peak(d3g_ctx* ctx, double* ops_per_sec);
+/* Measured shared-memory read bandwidth of this device (conflict-free
+ * LDS.128 streams on every SM, bytes/s): the roofline denominator of the
+ * smem-bound DenseEC hot pass. */
+int d3g_smem_peak(d3g_ctx* ctx, double* bytes_per_sec);
 int d3g_ctx_device(d3g_ctx* ctx);
 
 /* ---- join-aggregate (P/src/engine.cpp:537-722) -----------------------------

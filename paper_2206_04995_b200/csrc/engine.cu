@@ -135,6 +135,8 @@ struct KernelOut {
   uint64_t count = 0, sum = 0, xr = 0;
   uint64_t inner = 0;
   uint64_t cold_overflow = 0;  // x handed to the overflow kernel (diagnostics)
+  double ms_hot = 0;          // CUDA-event time of the hot-pass launch
+  uint64_t hot_lds_bytes = 0;  // its algorithmic shared-memory bytes
 };
 
 template <class F>
@@ -450,6 +452,16 @@ __global__ void k_estimate_kernel(const uint32_t* __restrict__ y_of_rank,
   }
 }
 
+__global__ void rec_sum_kernel(const uint32_t* __restrict__ rcnt, uint64_t n, uint32_t add,
+                               unsigned long long* __restrict__ out) {
+  uint64_t acc = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    acc += (rcnt[i] & 0xffffffu) + add;
+  acc = d3g::warp_sum(acc);
+  if (d3g::lane_id() == 0 && acc) atomicAdd(out, (unsigned long long)acc);
+}
+
 __global__ void top_dr_kernel(const uint32_t* __restrict__ y_of_rank,
                               const uint32_t* __restrict__ dR, uint64_t y_card,
                               uint32_t* __restrict__ out) {
@@ -571,6 +583,14 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     DBuf<uint32_t> rcnt = X.alloc<uint32_t>(D);
     D3G_LAUNCH(X, hot_rec_kernel, grid_for(D, 256), 256, 0, in.dl_ptr, in.dl_col, D, K,
                tab ? kTabBits : 0u, reinterpret_cast<uint8_t*>(rec.p), rcnt.p);
+    // algorithmic LDS traffic: every (row, batch) reads its listed slices plus
+    // (tab) one subset-table entry, 512 B each
+    DBuf<unsigned long long> lds = X.zeros<unsigned long long>(1);
+    D3G_LAUNCH(X, rec_sum_kernel, grid_for(D, 256), 256, 0, rcnt.p, D, tab ? 1u : 0u, lds.p);
+    cudaEvent_t ev0, ev1;
+    D3G_CUDA(cudaEventCreate(&ev0));
+    D3G_CUDA(cudaEventCreate(&ev1));
+    D3G_CUDA(cudaEventRecord(ev0, X.stream));
     with_mode(mode, [&](auto M) {
       if (tab) {
         auto kfn = dense_hot_tab_kernel<decltype(M)::value>;
@@ -584,6 +604,14 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
                    t.p);
       }
     });
+    D3G_CUDA(cudaEventRecord(ev1, X.stream));
+    const uint64_t units = X.scalar(lds.p);
+    float ms = 0;
+    D3G_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+    out.ms_hot = ms;
+    out.hot_lds_bytes = units * n_batches * 512ull;
   } else {
     with_mode(mode, [&](auto M) {
       auto kfn = dense_hot_kernel<decltype(M)::value>;
@@ -1518,6 +1546,8 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   T.mark();  // 8
   rep->pairs_sparse = ks.count;
   rep->pairs_dense = kd.count;
+  rep->ms_dense_hot = ks.ms_hot + kd.ms_hot;
+  rep->hot_lds_bytes = ks.hot_lds_bytes + kd.hot_lds_bytes;
   rep->spa_inner_count = outj_sp;
   rep->out_p = ks.count + kd.count;
   rep->checksum_sum = ks.sum + kd.sum;
@@ -2293,6 +2323,61 @@ __global__ void __launch_bounds__(256) alu_peak_kernel(uint32_t seed, int iters,
   if (x == 0x12345678u) out[0] = x;
 }
 }  // namespace
+
+namespace {
+// conflict-free LDS.128 streams: lane l of warp w reads row (i + w) % rows,
+// column l; 8 independent loads per iteration, xor-folded
+__global__ void __launch_bounds__(1024) smem_peak_kernel(int iters, uint32_t* out) {
+  extern __shared__ __align__(16) uint4 sbuf[];  // [rows][32]
+  constexpr int kRows = 256;
+  for (int i = threadIdx.x; i < kRows * 32; i += blockDim.x)
+    sbuf[i] = make_uint4(i, i * 3u, i ^ 0x55u, i + 7u);
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint4 acc = make_uint4(0, 0, 0, 0);
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t row = (uint32_t)(it * 8 + j + w) & (kRows - 1);
+      const uint4 v = sbuf[row * 32 + lane];
+      acc.x ^= v.x;
+      acc.y ^= v.y;
+      acc.z ^= v.z;
+      acc.w ^= v.w;
+    }
+  }
+  if ((acc.x ^ acc.y ^ acc.z ^ acc.w) == 0x12345678u) out[0] = acc.x;
+}
+}  // namespace
+
+extern "C" int d3g_smem_peak(d3g_ctx* ctx, double* bytes_per_sec) {
+  return guarded([&] {
+    using namespace d3g;
+    Ctx& X = ctx->c;
+    D3G_CUDA(cudaSetDevice(X.device));
+    DBuf<uint32_t> out = X.zeros<uint32_t>(1);
+    const size_t sm = 256 * 32 * 16;  // 128 KB: one CTA of 1024 threads per SM
+    D3G_CUDA(cudaFuncSetAttribute(smem_peak_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sm));
+    const unsigned grid = (unsigned)X.sm_count;
+    const int iters = 8192;
+    smem_peak_kernel<<<grid, 1024, sm, X.stream>>>(64, out.p);  // warm-up
+    cudaEvent_t e0, e1;
+    D3G_CUDA(cudaEventCreate(&e0));
+    D3G_CUDA(cudaEventCreate(&e1));
+    D3G_CUDA(cudaEventRecord(e0, X.stream));
+    smem_peak_kernel<<<grid, 1024, sm, X.stream>>>(iters, out.p);
+    D3G_CUDA(cudaEventRecord(e1, X.stream));
+    X.sync();
+    D3G_CUDA(cudaGetLastError());
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    const double bytes = (double)grid * 1024.0 * iters * 8.0 * 16.0;
+    *bytes_per_sec = bytes / (ms * 1e-3);
+  });
+}
 
 extern "C" int d3g_alu_peak(d3g_ctx* ctx, double* ops_per_sec) {
   return guarded([&] {

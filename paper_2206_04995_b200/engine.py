@@ -222,7 +222,8 @@ class _Report(C.Structure):
                [(k, C.c_uint64) for k in _REPORT_U64_B] + \
                [(k, C.c_double) for k in _REPORT_MS] + [("gpu_launches", C.c_uint64)] + \
                [("pairs_classical", C.c_uint64), ("intermediate_pairs", C.c_uint64),
-                ("ms_classical", C.c_double)]
+                ("ms_classical", C.c_double), ("ms_dense_hot", C.c_double),
+                ("hot_lds_bytes", C.c_uint64)]
 
 
 class _Pairs(C.Structure):
@@ -253,7 +254,7 @@ EXPORTED = ["d3g_ctx_create", "d3g_ctx_destroy", "d3g_last_error", "d3g_version"
             "d3g_dense_ec_rows", "d3g_generate", "d3g_cfg_rows", "d3g_ctx_device",
             "d3g_f3_threshold", "d3g_f1", "d3g_f2_decide", "d3g_alu_peak",
             "d3g_detect_format", "d3g_binary_rows", "d3g_read_binary", "d3g_save_pairs",
-            "d3g_join_aggregate"]
+            "d3g_join_aggregate", "d3g_smem_peak"]
 
 _lib = None
 
@@ -287,6 +288,7 @@ def lib():
         L.d3g_cfg_rows.restype = C.c_uint64
         L.d3g_ctx_device.argtypes = [C.c_void_p]
         L.d3g_alu_peak.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
+        L.d3g_smem_peak.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
         L.d3g_f3_threshold.argtypes = [C.c_uint32, C.c_uint32, C.POINTER(_Consts)]
         L.d3g_f3_threshold.restype = C.c_uint32
         L.d3g_f1.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.POINTER(_Consts)]
@@ -412,6 +414,8 @@ class ExecutionReport:
     pairs_classical: int = 0
     intermediate_pairs: int = 0
     ms_classical: float = 0.0
+    ms_dense_hot: float = 0.0
+    hot_lds_bytes: int = 0
 
     def to_kv(self):
         """Insertion-ordered key/value view with the reference's key names
@@ -625,6 +629,14 @@ def dense_ec(r_by_x: CsrMatrix, z_ids: np.ndarray, panel_blocks: np.ndarray, y_c
 
 # ---------------------------------------------------------------------------
 # Host-only policy (no GPU needed)
+def smem_peak(ctx: "Context | None" = None) -> float:
+    """Measured shared-memory read bandwidth (bytes/s), d3g_smem_peak."""
+    ctx = ctx or default_context()
+    v = C.c_double()
+    _check(lib().d3g_smem_peak(ctx.handle, C.byref(v)))
+    return v.value
+
+
 def f1(size_r: int, size_s: int, out_j: int, c: CostConstants) -> float:
     cs = _consts(c)
     return lib().d3g_f1(size_r, size_s, out_j, C.byref(cs))

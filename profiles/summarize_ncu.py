@@ -53,7 +53,12 @@ def launches(path):
             if d.get("Metric Name") == "gpu__time_duration.sum":
                 seq.append((d["Kernel Name"].split("(")[0].replace("void ", "")[:70],
                             float(d["Metric Value"])))
-    half = seq[len(seq) // 2:]  # the timed step (the first half is the warm-up step)
+    # the last step: from the last launch of the step's first kernel (the
+    # fused column-statistics pass) on; the bench's peak micro-benchmarks and
+    # the input generator are not part of a step
+    starts = [i for i, (k, _) in enumerate(seq) if "colstat" in k]
+    half = seq[starts[-1]:] if starts else seq[len(seq) // 2:]
+    half = [(k, v) for k, v in half if "peak_kernel" not in k and "gen_kernel" not in k]
     agg = collections.defaultdict(float)
     cnt = collections.Counter()
     for k, v in half:
