@@ -204,7 +204,8 @@ def cpu_reference_sample(cfg: int, frac: float, threads: int, tables=None):
         (p1, k1, _), (p2, k2, o2) = runs
         marginal = max(k2 - k1, 0.0) / 900.0
         est = p2 + k1 + marginal * (x_card - 100)
-        return est, {"x_slice": "x<100 and x<1000 (marginal per-x cost)", "x_rows": x_card,
+        return est, {"slices": "cfg5", "x_slice": "x<100 and x<1000 (marginal per-x cost)",
+                     "x_rows": x_card,
                      "sec_prep": p2, "sec_kernels": k2, "sec_kernels_x100": k1,
                      "est_full_s": est, "slice_out_p": o2}
     x_rows = _X_ROWS.get(cfg)
@@ -219,6 +220,12 @@ def cpu_reference_sample(cfg: int, frac: float, threads: int, tables=None):
 
 
 def _sample_text(detail):
+    if detail.get("slices") == "cfg5":
+        return ("reference join_project(auto) on R restricted to x<100 and to x<1000 against the "
+                "full S (its engine swaps; the 1.25 TB panel of the whole job cannot be built): "
+                f"prep {detail['sec_prep']:.1f}s once + the marginal per-x kernel cost "
+                f"({(detail['sec_kernels'] - detail['sec_kernels_x100']) / 900 * 1e3:.2f} ms/x) "
+                "x 1e7 x values")
     if detail.get("strategy") == "classical":
         return ("whole job through the reference's join_project(auto) -> f1 gate -> "
                 "hash_join_dedup")
