@@ -501,7 +501,16 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   if (K * 2 <= k_cap && K == 256 && k_cap >= 384) K = 384;  // use the slack of the batch slice
   // the warp-bitmap cold kernel carries 256-bit hot signatures: K = 256
   // (the dense rows are split into at most 16 bitmap partitions, see P2)
-  const uint64_t cold_rows_cap = std::max<uint64_t>(32, (budget / 3 / kColdWarps) * 8 / 32 * 32);
+  // CTAs of the bitmap cold kernel per SM (its per-warp bitmaps share the
+  // SM's shared memory): more, smaller partitions raise occupancy for the
+  // latency-bound candidate stream
+  const char* cc_env = std::getenv("D3G_COLD_CTAS");
+  uint32_t cold_ctas = 4;  // measured best on cfg2 (4 > 3 > 6 > 8)
+  if ((D + (budget / 4 / kColdWarps) * 8 - 1) / ((budget / 4 / kColdWarps) * 8) > 16)
+    cold_ctas = 3;  // keep the dense rows within 16 bitmap partitions (cfg4)
+  if (cc_env) cold_ctas = std::max(1, std::atoi(cc_env));
+  const uint64_t cold_rows_cap =
+      std::max<uint64_t>(32, (budget / cold_ctas / kColdWarps) * 8 / 32 * 32);
   const bool cold_bitmap = k_cap >= 256 && (D + cold_rows_cap - 1) / cold_rows_cap <= 16;
   // larger dense blocks: the same candidate stream, survivors in a per-warp
   // hash set (dense_cold_hash_kernel); D3G_COLD=tiers keeps the SparseBMM tiers
@@ -628,7 +637,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   if (e[best] > 0) {
     uint32_t parts = 1, part_rows = (uint32_t)(((D + 31) / 32) * 32);
     if (cold_bitmap) {
-      const uint64_t per_warp = budget / 3 / kColdWarps;  // 3 CTAs of 8 warps per SM
+      const uint64_t per_warp = budget / cold_ctas / kColdWarps;
       const uint64_t rows_cap = std::max<uint64_t>(32, per_warp * 8 / 32 * 32);
       parts = (uint32_t)((D + rows_cap - 1) / rows_cap);
       part_rows = (uint32_t)((((D + parts - 1) / parts) + 31) / 32 * 32);
@@ -694,7 +703,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
         auto kfn = dense_cold_kernel<decltype(M)::value>;
         if (csm > 48 * 1024)
           D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
-        D3G_LAUNCH(X, kfn, (unsigned)X.sm_count * 3, kColdWarps * 32, csm, xorder, n_live, in.r_ptr,
+        D3G_LAUNCH(X, kfn, (unsigned)X.sm_count * cold_ctas, kColdWarps * 32, csm, xorder, n_live, in.r_ptr,
                    in.r_col, cptr.p, ccol.p, ch.p, reinterpret_cast<const uint4*>(hx.p), Y, parts,
                    part_rows, var_bits, in.dl_z, dec, em, next.p, tc.p);
       });
