@@ -812,13 +812,12 @@ void build_dense_layout(Ctx& X, const d3g::DeviceCsr& rx, uint64_t max_mx,
                         const uint32_t* zcol, const uint32_t* row_ids, uint64_t n_dense,
                         uint64_t max_mz, const uint32_t* z_of_row, uint64_t y_card,
                         const uint32_t* dR, DenseLayout& L, uint64_t xa = 0,
-                        uint64_t xb = ~0ull) {
+                        uint64_t xb = ~0ull, uint64_t dnnz_hint = ~0ull) {
   using namespace d3g;
   L.n_dense = n_dense;
-  // y ranked by dR descending (ties by code): hottest witnesses first
-  DBuf<unsigned long long> mx = X.zeros<unsigned long long>(1);
-  if (y_card) D3G_LAUNCH(X, max_u32_kernel, grid_for(y_card, 256), 256, 0, dR, y_card, mx.p);
-  uint64_t max_dr = X.scalar(mx.p);
+  // y ranked by dR descending (ties by code): hottest witnesses first. dR(y)
+  // <= x_card bounds the key without a device round trip.
+  const uint64_t max_dr = rx.n_rows;
   {
     DBuf<uint64_t> k = X.alloc<uint64_t>(y_card);
     DBuf<uint32_t> v = X.alloc<uint32_t>(y_card);
@@ -842,7 +841,7 @@ void build_dense_layout(Ctx& X, const d3g::DeviceCsr& rx, uint64_t max_mx,
   L.dl_ptr = X.alloc<uint64_t>(n_dense + 1);
   exclusive_scan<uint32_t>(X, len.p, n_dense, L.dl_ptr.p);
   len.reset();
-  uint64_t dnnz = X.scalar(L.dl_ptr.p + n_dense);
+  const uint64_t dnnz = dnnz_hint != ~0ull ? dnnz_hint : X.scalar(L.dl_ptr.p + n_dense);
   {
     L.dl_col = X.alloc<uint32_t>(dnnz);
     D3G_LAUNCH(X, dense_list_fill_kernel, grid_for(n_dense * 32, 256), 256, 0, rows.p, n_dense,
@@ -861,7 +860,12 @@ void build_dense_layout(Ctx& X, const d3g::DeviceCsr& rx, uint64_t max_mx,
   if (x_card) D3G_LAUNCH(X, live_flag_kernel, grid_for(x_card, 256), 256, 0, rx.row_ptr.p, xa, xb, lf.p);
   DBuf<uint64_t> lp = X.alloc<uint64_t>(x_card + 1);
   exclusive_scan<uint32_t>(X, lf.p, x_card, lp.p);
-  L.n_live = X.scalar(lp.p + x_card);
+  if (xa == 0 && xb == rx.n_rows) {  // every live x: the m_x histogram knows how many
+    L.n_live = 0;
+    for (uint64_t m = 1; m < hmx.size(); ++m) L.n_live += hmx[m];
+  } else {
+    L.n_live = X.scalar(lp.p + x_card);
+  }
   DBuf<uint32_t> live_ids = X.alloc<uint32_t>(L.n_live);
   if (x_card)
     D3G_LAUNCH(X, index_compact_kernel, grid_for(x_card, 256), 256, 0, lf.p, lp.p, x_card, live_ids.p);
@@ -1297,6 +1301,9 @@ void degree_stats(Ctx& X, const d3g::DeviceCsr& rx, const d3g::DeviceCsr& sz_csr
 struct Split {
   DBuf<uint32_t> isd, iss;  // per z: dense / sparse (m_z == 0: neither)
   uint64_t n_dense = 0, n_sparse = 0;
+  // sums of m_z over the dense / sparse rows; exact on the host because the
+  // decision is a function of m_z alone (read off the m_z histogram)
+  uint64_t dense_nnz = 0, sparse_nnz = 0;
 };
 
 void f2_split(Ctx& X, const d3g::DeviceCsr& sz_csr, const DegreeStats& G, uint64_t x_card,
@@ -1328,8 +1335,15 @@ void f2_split(Ctx& X, const d3g::DeviceCsr& sz_csr, const DegreeStats& G, uint64
   DBuf<uint64_t> pd = X.alloc<uint64_t>(z_card + 1), psp = X.alloc<uint64_t>(z_card + 1);
   exclusive_scan<uint32_t>(X, P.isd.p, z_card, pd.p);
   exclusive_scan<uint32_t>(X, P.iss.p, z_card, psp.p);
-  P.n_dense = X.scalar(pd.p + z_card);
-  P.n_sparse = X.scalar(psp.p + z_card);
+  for (uint64_t m = 1; m < G.hmz.size(); ++m) {
+    if (table[m]) {
+      P.n_dense += G.hmz[m];
+      P.dense_nnz += m * G.hmz[m];
+    } else {
+      P.n_sparse += G.hmz[m];
+      P.sparse_nnz += m * G.hmz[m];
+    }
+  }
   rep->dense_z = P.n_dense;
   rep->sparse_z = P.n_sparse;
   const uint64_t row_words = ((y_card + c->w - 1) / c->w * c->w) / 64;
@@ -1492,7 +1506,7 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
       D3G_LAUNCH(X, sparse_y_count_kernel, grid_for(n_sparse * 32, 256), 256, 0,
                  sz_csr.row_ptr.p, sz_csr.col.p, sparse_ids.p, n_sparse, cnt.p);
     exclusive_scan<uint32_t>(X, cnt.p, y_card, sp_ptr.p);
-    rep->sparse_nnz = X.scalar(sp_ptr.p + y_card);
+    rep->sparse_nnz = P.sparse_nnz;  // = sp_ptr[y_card], known on the host
     sp_col = X.alloc<uint32_t>(rep->sparse_nnz);
     DBuf<unsigned long long> cur = X.alloc<unsigned long long>(y_card + 1);
     D3G_CUDA(cudaMemcpyAsync(cur.p, sp_ptr.p, (y_card + 1) * 8, cudaMemcpyDeviceToDevice, X.stream));
@@ -1507,7 +1521,7 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   const uint64_t xb = o->x_code_hi ? std::min<uint64_t>(o->x_code_hi, x_card) : x_card;
   if (n_dense > 0 && x_live > 0)
     build_dense_layout(X, rx, max_mx, hmx, sz_csr.row_ptr.p, sz_csr.col.p, dense_ids.p, n_dense,
-                       max_mz, nullptr, y_card, dR.p, L, xa, xb);
+                       max_mz, nullptr, y_card, dR.p, L, xa, xb, P.dense_nnz);
   // Heavy sparse side (OUT_J,sparse > 4096 per live x over > 8192 sparse z,
   // e.g. cfg4's 9.7e10 candidates): answer it with the same hot bit-sliced +
   // cold residual engine, restricted to the sparse z set. The result is the
@@ -1523,7 +1537,7 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   DenseLayout Ls;
   if (sparse_hot)
     build_dense_layout(X, rx, max_mx, hmx, sz_csr.row_ptr.p, sz_csr.col.p, sparse_ids.p, n_sparse,
-                       max_mz, nullptr, y_card, dR.p, Ls, xa, xb);
+                       max_mz, nullptr, y_card, dR.p, Ls, xa, xb, P.sparse_nnz);
   T.mark();  // 6
 
   // 8. kernels
