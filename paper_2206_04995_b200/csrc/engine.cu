@@ -187,8 +187,17 @@ void run_sparse(Ctx& X, const SparseInputs& in, d3g::Decode dec, int mode, d3g::
   D3G_LAUNCH(X, sparse_bin_kernel, grid_for(nx, 256), 256, 0, cx.p, nx, 32ull, mid_max, fl[0].p,
              fl[1].p, fl[2].p);
   for (int b = 0; b < 3; ++b) exclusive_scan<uint32_t>(X, fl[b].p, nx, pos[b].p);
+  {  // the three tier sizes and the candidate total in one round trip
+    DBuf<unsigned long long> sizes = X.alloc<unsigned long long>(4);
+    for (int b = 0; b < 3; ++b)
+      D3G_CUDA(cudaMemcpyAsync(sizes.p + b, pos[b].p + nx, 8, cudaMemcpyDeviceToDevice, X.stream));
+    D3G_CUDA(cudaMemcpyAsync(sizes.p + 3, tot.p, 8, cudaMemcpyDeviceToDevice, X.stream));
+    unsigned long long hs[4];
+    X.to_host(hs, sizes.p, 4);
+    for (int b = 0; b < 3; ++b) cnt[b] = hs[b];
+    out.inner = hs[3];
+  }
   for (int b = 0; b < 3; ++b) {
-    cnt[b] = X.scalar(pos[b].p + nx);
     lists[b] = X.alloc<uint32_t>(cnt[b]);
     if (cnt[b]) {
       D3G_LAUNCH(X, index_compact_kernel, grid_for(nx, 256), 256, 0, fl[b].p, pos[b].p, nx,
@@ -198,7 +207,6 @@ void run_sparse(Ctx& X, const SparseInputs& in, d3g::Decode dec, int mode, d3g::
                    (uint32_t)in.x_lo);
     }
   }
-  out.inner = X.scalar(tot.p);
   DBuf<Tally> t = X.zeros<Tally>(1);
   const uint64_t* rp = in.r_ptr;
   if (cnt[0]) {
@@ -280,6 +288,7 @@ struct DenseInputs {
   const uint32_t* dR;      // R-side degree per y code
   uint64_t x_card;
   uint64_t x_lo, x_hi;     // x code range of the cold residual pass
+  uint64_t dnnz = ~0ull;   // entries of the dense lists (~0: read dl_ptr[n_dense])
 };
 
 // DenseEC driver: the z-tile-resident kernel (dense_ec_tile_kernel) when the
@@ -462,10 +471,16 @@ __global__ void rec_sum_kernel(const uint32_t* __restrict__ rcnt, uint64_t n, ui
   if (d3g::lane_id() == 0 && acc) atomicAdd(out, (unsigned long long)acc);
 }
 
-__global__ void top_dr_kernel(const uint32_t* __restrict__ y_of_rank,
-                              const uint32_t* __restrict__ dR, uint64_t y_card,
-                              uint32_t* __restrict__ out) {
-  if (threadIdx.x < 3) out[threadIdx.x] = threadIdx.x < y_card ? dR[y_of_rank[threadIdx.x]] : 0;
+// out[0..6] = dense rows holding rank r (cnt_rank), out[7..10] = dR of ranks 0..3
+__global__ void hot_small_stats_kernel(const uint32_t* __restrict__ cnt_rank,
+                                       const uint32_t* __restrict__ y_of_rank,
+                                       const uint32_t* __restrict__ dR, uint64_t y_card,
+                                       unsigned long long* __restrict__ out) {
+  const uint32_t t = threadIdx.x;
+  if (t < 7)
+    out[t] = t < y_card ? cnt_rank[t] : 0;
+  else if (t < 11)
+    out[t] = (t - 7) < y_card ? dR[y_of_rank[t - 7]] : 0;
 }
 
 void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g::Emit em,
@@ -476,14 +491,20 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   const uint32_t* xorder = in.xorder + in.pos_lo;
   const uint32_t groups = (uint32_t)((n_live + 127) / 128);
   const uint64_t D = in.n_dense, Y = in.y_card;
-  const uint64_t dnnz = X.scalar(in.dl_ptr + D);
+  const uint64_t dnnz = in.dnnz != ~0ull ? in.dnnz : X.scalar(in.dl_ptr + D);
   // choose K
   DBuf<uint32_t> cnt_rank = X.zeros<uint32_t>(Y);
   if (dnnz) D3G_LAUNCH(X, value_hist_kernel, grid_for(dnnz, 256), 256, 0, in.dl_col, dnnz, cnt_rank.p, (uint32_t)Y);
-  DBuf<unsigned long long> est = X.zeros<unsigned long long>(2 * kKCand);
+  // one read-back: K estimates, then the dense-row counts of ranks 0..6 (the
+  // subset-table decision) and dR of ranks 0..3 (the cold variant bits)
+  DBuf<unsigned long long> est = X.zeros<unsigned long long>(2 * kKCand + 11);
   D3G_LAUNCH(X, k_estimate_kernel, grid_for(Y, 256), 256, 0, in.y_of_rank, in.dR, cnt_rank.p, Y, est.p);
-  unsigned long long e[2 * kKCand];
-  X.to_host(e, est.p, 2 * kKCand);
+  D3G_LAUNCH(X, hot_small_stats_kernel, 1, 32, 0, cnt_rank.p, in.y_of_rank, in.dR, Y,
+             est.p + 2 * kKCand);
+  unsigned long long e[2 * kKCand + 11];
+  X.to_host(e, est.p, 2 * kKCand + 11);
+  const unsigned long long* top_rank_rows = e + 2 * kKCand;   // [7]
+  const unsigned long long* top_rank_dr = e + 2 * kKCand + 7;  // [4]
   static const uint32_t kv[kKCand] = {64, 128, 256, 512, 1024};
   // K is bounded by the shared-memory slice of a 32-group batch (K * 512 B)
   const uint64_t budget = (uint64_t)dense_smem_bytes(X) - 1024;
@@ -550,7 +571,11 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
       (D + 255) / 256, ((uint64_t)X.sm_count * 8 + n_batches - 1) / n_batches));
   DBuf<unsigned int> work = X.zeros<unsigned int>(1);
   hp.work = work.p;
-  DBuf<Tally> t = X.zeros<Tally>(1);
+  // [hot tally | cold tally | hot-pass LDS units]: read back once at the end
+  DBuf<Tally> tallies = X.zeros<Tally>(3);
+  Tally* t = tallies.p;
+  unsigned long long* lds_units = &tallies.p[2].count;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   size_t sm = (size_t)K * 32 * 16;
   unsigned g = (unsigned)std::min<uint64_t>((uint64_t)n_batches * hp.z_chunks, (uint64_t)X.sm_count);
   const char* hot_impl = std::getenv("D3G_HOT");
@@ -573,17 +598,15 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     auto kfn = dense_tc_kernel<kModeCount>;
     D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
     D3G_LAUNCH(X, kfn, (unsigned)std::min<uint64_t>((uint64_t)n_zt * x_chunks, X.sm_count),
-               kTcThreads, tsm, A.p, B.p, K, n_xt, n_zt, n_live, D, x_chunks, tw.p, t.p);
+               kTcThreads, tsm, A.p, B.p, K, n_xt, n_zt, n_live, D, x_chunks, tw.p, t);
   } else if (K <= 256 && !(hot_impl && std::string(hot_impl) == "list")) {
     // packed hot records (default; D3G_HOT=list selects the list kernel), with
     // the top-rank subset table when it fits (D3G_HOT=rec disables it)
     // the table pays off when the top ranks are common in the dense rows
     // (cfg2/cfg5: >= 3 of the top 7 per row; cfg4's flat Zipf(0.8): < 1)
     const size_t tsm = (size_t)(kTabRows + K - kTabBits) * 32 * 16;
-    uint32_t top_cnt[kTabBits] = {};
-    X.to_host(top_cnt, cnt_rank.p, std::min<uint64_t>(kTabBits, Y));
     double top_per_row = 0;
-    for (uint32_t r = 0; r < kTabBits; ++r) top_per_row += (double)top_cnt[r] / (double)D;
+    for (uint32_t r = 0; r < kTabBits; ++r) top_per_row += (double)top_rank_rows[r] / (double)D;
     const bool force_tab = hot_impl && std::string(hot_impl) == "tab";
     const bool tab = K > kTabBits && tsm <= (size_t)dense_smem_bytes(X) &&
                      !(hot_impl && std::string(hot_impl) == "rec") &&
@@ -594,9 +617,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
                tab ? kTabBits : 0u, reinterpret_cast<uint8_t*>(rec.p), rcnt.p);
     // algorithmic LDS traffic: every (row, batch) reads its listed slices plus
     // (tab) one subset-table entry, 512 B each
-    DBuf<unsigned long long> lds = X.zeros<unsigned long long>(1);
-    D3G_LAUNCH(X, rec_sum_kernel, grid_for(D, 256), 256, 0, rcnt.p, D, tab ? 1u : 0u, lds.p);
-    cudaEvent_t ev0, ev1;
+    D3G_LAUNCH(X, rec_sum_kernel, grid_for(D, 256), 256, 0, rcnt.p, D, tab ? 1u : 0u, lds_units);
     D3G_CUDA(cudaEventCreate(&ev0));
     D3G_CUDA(cudaEventCreate(&ev1));
     D3G_CUDA(cudaEventRecord(ev0, X.stream));
@@ -605,31 +626,22 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
         auto kfn = dense_hot_tab_kernel<decltype(M)::value>;
         D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
         D3G_LAUNCH(X, kfn, g, kHotThreads, tsm, hp, in.dl_ptr, in.dl_col, rec.p, rcnt.p, dec, em,
-                   t.p);
+                   t);
       } else {
         auto kfn = dense_hot_rec_kernel<decltype(M)::value>;
         D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         D3G_LAUNCH(X, kfn, g, kHotThreads, sm, hp, in.dl_ptr, in.dl_col, rec.p, rcnt.p, dec, em,
-                   t.p);
+                   t);
       }
     });
     D3G_CUDA(cudaEventRecord(ev1, X.stream));
-    const uint64_t units = X.scalar(lds.p);
-    float ms = 0;
-    D3G_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
-    cudaEventDestroy(ev0);
-    cudaEventDestroy(ev1);
-    out.ms_hot = ms;
-    out.hot_lds_bytes = units * n_batches * 512ull;
   } else {
     with_mode(mode, [&](auto M) {
       auto kfn = dense_hot_kernel<decltype(M)::value>;
       D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      D3G_LAUNCH(X, kfn, g, kHotThreads, sm, hp, in.dl_ptr, in.dl_col, dec, em, t.p);
+      D3G_LAUNCH(X, kfn, g, kHotThreads, sm, hp, in.dl_ptr, in.dl_col, dec, em, t);
     });
   }
-  Tally h;
-  X.to_host(&h, t.p, 1);
   // P2: cold residual join, hot-hit candidates filtered. With the warp-bitmap
   // kernel the dense rows are cut into `parts` ranges so that 24 warps per SM
   // each hold a part_rows-bit bitmap; the cold CSR is keyed by (part, y).
@@ -646,13 +658,9 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     // bit per top rank that at least half of the live x contain (cfg2: ranks
     // 0-2; cfg4's flatter Zipf(0.8): none)
     uint32_t var_bits = 0;
-    if (cold_kernel_ok) {
-      DBuf<uint32_t> top = X.alloc<uint32_t>(3);
-      D3G_LAUNCH(X, top_dr_kernel, 1, 32, 0, in.y_of_rank, in.dR, Y, top.p);
-      uint32_t h[3];
-      X.to_host(h, top.p, 3);
-      while (var_bits < 3 && var_bits < Y && 2ull * h[var_bits] >= in.x_card) ++var_bits;
-    }
+    if (cold_kernel_ok)
+      while (var_bits < 3 && var_bits < Y && 2ull * top_rank_dr[var_bits] >= in.x_card)
+        ++var_bits;
     const uint64_t rows_key = ((uint64_t)1 << var_bits) * parts * Y;
     DBuf<uint32_t> cc = X.zeros<uint32_t>(rows_key);
     D3G_LAUNCH(X, cold_count_kernel, grid_for(D * 32, 256), 256, 0, in.dl_ptr, in.dl_col, D, K,
@@ -672,7 +680,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     cur.reset();
     if (cold_kernel_ok) {
       DBuf<unsigned int> next = X.zeros<unsigned int>(1);
-      DBuf<Tally> tc = X.zeros<Tally>(1);
+      Tally* tc = tallies.p + 1;
       if (cold_hash) {
         DBuf<uint32_t> over_x = X.alloc<uint32_t>(n_live);
         DBuf<unsigned int> over_n = X.zeros<unsigned int>(1);
@@ -682,7 +690,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
           D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
           D3G_LAUNCH(X, kfn, (unsigned)X.sm_count * 3, kCHWarps * 32, hsm, xorder, n_live,
                      in.r_ptr, in.r_col, cptr.p, ccol.p, ch.p, reinterpret_cast<const uint4*>(hx.p),
-                     Y, var_bits, in.dl_z, dec, em, next.p, over_x.p, over_n.p, tc.p);
+                     Y, var_bits, in.dl_z, dec, em, next.p, over_x.p, over_n.p, tc);
         });
         const unsigned int n_over = X.scalar(over_n.p);
         out.cold_overflow = n_over;
@@ -694,7 +702,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
             D3G_LAUNCH(X, dense_cold_overflow_kernel<decltype(M)::value>, og, 512, 0, over_x.p,
                        over_n.p, in.r_ptr, in.r_col, cptr.p, ccol.p, ch.p,
                        reinterpret_cast<const uint4*>(hx.p), Y, var_bits, in.dl_z, gbm.p, words,
-                       dec, em, tc.p);
+                       dec, em, tc);
           });
         }
       } else {
@@ -705,19 +713,30 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
           D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
         D3G_LAUNCH(X, kfn, (unsigned)X.sm_count * cold_ctas, kColdWarps * 32, csm, xorder, n_live, in.r_ptr,
                    in.r_col, cptr.p, ccol.p, ch.p, reinterpret_cast<const uint4*>(hx.p), Y, parts,
-                   part_rows, var_bits, in.dl_z, dec, em, next.p, tc.p);
+                   part_rows, var_bits, in.dl_z, dec, em, next.p, tc);
       });
       }
-      Tally hc;
-      X.to_host(&hc, tc.p, 1);
-      cold.count = hc.count;
-      cold.sum = hc.sum;
-      cold.xr = hc.xr;
     } else {
       SparseInputs si{in.r_ptr, in.r_col, in.x_card, cptr.p, ccol.p, in.dl_z, D, Y, in.x_lo, in.x_hi};
       Filter flt{reinterpret_cast<const uint64_t*>(hx.p), reinterpret_cast<const uint64_t*>(hz.p), kw};
       run_sparse(X, si, dec, mode, em, cold, flt);
     }
+  }
+  Tally th[3];
+  X.to_host(th, tallies.p, 3);
+  const Tally& h = th[0];
+  if (cold_kernel_ok && e[best] > 0) {
+    cold.count = th[1].count;
+    cold.sum = th[1].sum;
+    cold.xr = th[1].xr;
+  }
+  if (ev0) {
+    float ms = 0;
+    D3G_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+    out.ms_hot = ms;
+    out.hot_lds_bytes = th[2].count * n_batches * 512ull;
   }
   if (std::getenv("D3G_TRACE"))
     std::fprintf(stderr, "[dense_hot] D=%llu live=%llu K=%u hot=%llu cold=%llu cold_path=%s over=%llu\n",
@@ -801,7 +820,7 @@ __global__ void map_through_kernel(uint32_t* __restrict__ v, uint64_t n,
 struct DenseLayout {
   DBuf<uint32_t> y_rank, y_of_rank, dl_z, dl_col, xorder;
   DBuf<uint64_t> dl_ptr;
-  uint64_t n_live = 0, n_dense = 0, max_group_nnz = 0;
+  uint64_t n_live = 0, n_dense = 0, max_group_nnz = 0, dnnz = 0;
 };
 
 // rows: dense z rows given as (row_ptr, col) indexed by row id; row_ids
@@ -842,6 +861,7 @@ void build_dense_layout(Ctx& X, const d3g::DeviceCsr& rx, uint64_t max_mx,
   exclusive_scan<uint32_t>(X, len.p, n_dense, L.dl_ptr.p);
   len.reset();
   const uint64_t dnnz = dnnz_hint != ~0ull ? dnnz_hint : X.scalar(L.dl_ptr.p + n_dense);
+  L.dnnz = dnnz;
   {
     L.dl_col = X.alloc<uint32_t>(dnnz);
     D3G_LAUNCH(X, dense_list_fill_kernel, grid_for(n_dense * 32, 256), 256, 0, rows.p, n_dense,
@@ -1261,14 +1281,19 @@ void degree_stats(Ctx& X, const d3g::DeviceCsr& rx, const d3g::DeviceCsr& sz_csr
   G.x_live = scal[1];
   G.max_mz = scal[2];
   rep->x_live = G.x_live;
-  DBuf<unsigned long long> mxh = X.zeros<unsigned long long>(G.max_mx + 1);
-  DBuf<unsigned long long> mzh = X.zeros<unsigned long long>(G.max_mz + 1);
+  // one buffer, one read-back: [m_x histogram | m_z histogram | OUT_J partials]
+  const unsigned gb = grid_for(y_card, 1024, 296);
+  const uint64_t nbuf = (G.max_mx + 1) + (G.max_mz + 1) + 2ull * gb;
+  DBuf<unsigned long long> hbuf = X.zeros<unsigned long long>(nbuf);
+  unsigned long long* mxh_p = hbuf.p;
+  unsigned long long* mzh_p = hbuf.p + G.max_mx + 1;
+  unsigned long long* parts_p = mzh_p + G.max_mz + 1;
   if (x_card)
     D3G_LAUNCH(X, degree_hist_kernel, grid_for(x_card, 256), 256, 0, rx.row_ptr.p, x_card,
-               G.max_mx + 1, mxh.p);
+               G.max_mx + 1, mxh_p);
   if (z_card)
     D3G_LAUNCH(X, degree_hist_kernel, grid_for(z_card, 256), 256, 0, sz_csr.row_ptr.p, z_card,
-               G.max_mz + 1, mzh.p);
+               G.max_mz + 1, mzh_p);
   G.dR = X.zeros<uint32_t>(y_card);
   G.dS = X.zeros<uint32_t>(y_card);
   if (rx.nnz)
@@ -1277,23 +1302,17 @@ void degree_stats(Ctx& X, const d3g::DeviceCsr& rx, const d3g::DeviceCsr& sz_csr
   if (sz_csr.nnz)
     D3G_LAUNCH(X, value_hist_kernel, grid_for(sz_csr.nnz, 256), 256, 0, sz_csr.col.p, sz_csr.nnz,
                G.dS.p, (uint32_t)y_card);
-  {
-    unsigned gb = grid_for(y_card, 1024, 296);
-    DBuf<unsigned long long> parts = X.zeros<unsigned long long>(2 * gb);
-    if (y_card) D3G_LAUNCH(X, outj_kernel, gb, 1024, 0, G.dR.p, G.dS.p, y_card, parts.p);
-    std::vector<unsigned long long> hp(2 * gb);
-    X.to_host(hp.data(), parts.p, 2 * gb);
-    unsigned __int128 acc = 0;
-    for (unsigned i = 0; i < gb; ++i)
-      acc += ((unsigned __int128)hp[2 * i + 1] << 64) | hp[2 * i];
-    rep->out_j = acc > (unsigned __int128)std::numeric_limits<uint64_t>::max()
-                     ? std::numeric_limits<uint64_t>::max()
-                     : (uint64_t)acc;
-  }
-  G.hmx.resize(G.max_mx + 1);
-  G.hmz.resize(G.max_mz + 1);
-  X.to_host(reinterpret_cast<unsigned long long*>(G.hmx.data()), mxh.p, G.max_mx + 1);
-  X.to_host(reinterpret_cast<unsigned long long*>(G.hmz.data()), mzh.p, G.max_mz + 1);
+  if (y_card) D3G_LAUNCH(X, outj_kernel, gb, 1024, 0, G.dR.p, G.dS.p, y_card, parts_p);
+  std::vector<unsigned long long> hb(nbuf);
+  X.to_host(hb.data(), hbuf.p, nbuf);
+  G.hmx.assign(hb.begin(), hb.begin() + (G.max_mx + 1));
+  G.hmz.assign(hb.begin() + (G.max_mx + 1), hb.begin() + (G.max_mx + 1) + (G.max_mz + 1));
+  const unsigned long long* hp = hb.data() + (G.max_mx + 1) + (G.max_mz + 1);
+  unsigned __int128 acc = 0;
+  for (unsigned i = 0; i < gb; ++i) acc += ((unsigned __int128)hp[2 * i + 1] << 64) | hp[2 * i];
+  rep->out_j = acc > (unsigned __int128)std::numeric_limits<uint64_t>::max()
+                   ? std::numeric_limits<uint64_t>::max()
+                   : (uint64_t)acc;
 }
 
 // Step 7a: the f2 decision per degree value (policy.cpp) and the per-z
@@ -1554,7 +1573,7 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
                  s_hi = Ls.n_live * (shard_index + 1) / shard_count;
   DenseInputs dsi{Ls.xorder.p, Ls.n_live, rx.row_ptr.p, rx.col.p, Ls.y_rank.p, y_card,
                   Ls.dl_ptr.p, Ls.dl_col.p, Ls.dl_z.p, Ls.n_dense, Ls.max_group_nnz, s_lo, s_hi,
-                  Ls.y_of_rank.p, dR.p, x_card, x_lo, x_hi};
+                  Ls.y_of_rank.p, dR.p, x_card, x_lo, x_hi, Ls.dnnz};
   if (sparse_hot)
     run_dense_hot(X, dsi, dec, mode, no_emit, ks);
   else
@@ -1564,7 +1583,7 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
            pos_hi = L.n_live * (shard_index + 1) / shard_count;
   DenseInputs di{L.xorder.p, L.n_live, rx.row_ptr.p, rx.col.p, L.y_rank.p, y_card, L.dl_ptr.p,
                  L.dl_col.p, L.dl_z.p, L.n_dense, L.max_group_nnz, pos_lo, pos_hi,
-                 L.y_of_rank.p, dR.p, x_card, x_lo, x_hi};
+                 L.y_of_rank.p, dR.p, x_card, x_lo, x_hi, L.dnnz};
   run_dense(X, di, dec, mode, no_emit, kd);
   T.mark();  // 8
   rep->pairs_sparse = ks.count;
