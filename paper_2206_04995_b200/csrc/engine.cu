@@ -1265,7 +1265,7 @@ struct DegreeStats {
 };
 
 void degree_stats(Ctx& X, const d3g::DeviceCsr& rx, const d3g::DeviceCsr& sz_csr,
-                  uint64_t y_card, d3g_report* rep, DegreeStats& G) {
+                  uint64_t y_card, d3g_report* rep, DegreeStats& G, bool same = false) {
   using namespace d3g;
   const uint64_t x_card = rx.n_rows, z_card = sz_csr.n_rows;
   DBuf<unsigned long long> sc = X.zeros<unsigned long long>(4);  // max_mx, live_x, max_mz, live_z
@@ -1299,7 +1299,9 @@ void degree_stats(Ctx& X, const d3g::DeviceCsr& rx, const d3g::DeviceCsr& sz_csr
   if (rx.nnz)
     D3G_LAUNCH(X, value_hist_kernel, grid_for(rx.nnz, 256), 256, 0, rx.col.p, rx.nnz, G.dR.p,
                (uint32_t)y_card);
-  if (sz_csr.nnz)
+  if (same && y_card)  // self-join: S-by-z is R-by-x, so dS = dR
+    D3G_CUDA(cudaMemcpyAsync(G.dS.p, G.dR.p, y_card * 4, cudaMemcpyDeviceToDevice, X.stream));
+  else if (sz_csr.nnz)
     D3G_LAUNCH(X, value_hist_kernel, grid_for(sz_csr.nnz, 256), 256, 0, sz_csr.col.p, sz_csr.nnz,
                G.dS.p, (uint32_t)y_card);
   if (y_card) D3G_LAUNCH(X, outj_kernel, gb, 1024, 0, G.dR.p, G.dS.p, y_card, parts_p);
@@ -1480,7 +1482,8 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   // maps both sides identically, so S-by-z is R-by-x: built once.
   DeviceCsr rx, sz_csr;
   build_csr_device(X, M.r_x, M.r_y, kept, x_card, y_card, rx);
-  if (self_join && kept == NR && x_card == z_card)
+  const bool same_csr = self_join && kept == NR && x_card == z_card;
+  if (same_csr)
     copy_csr(X, rx, sz_csr);
   else
     build_csr_device(X, M.s_z, M.s_y, NS, z_card, y_card, sz_csr);
@@ -1491,7 +1494,7 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
 
   // 6. degree statistics (compute_degree_stats, costmodel.cpp:425-438)
   DegreeStats G;
-  degree_stats(X, rx, sz_csr, y_card, rep, G);
+  degree_stats(X, rx, sz_csr, y_card, rep, G, same_csr);
   const uint64_t max_mx = G.max_mx, x_live = G.x_live, max_mz = G.max_mz;
   const std::vector<uint64_t>& hmx = G.hmx;
   DBuf<uint32_t>& dR = G.dR;
