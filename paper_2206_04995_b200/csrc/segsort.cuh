@@ -104,15 +104,54 @@ __device__ __forceinline__ uint32_t warp_sort_row(uint32_t* __restrict__ data, u
   return written;
 }
 
-// One warp per row for rows of length <= 128; longer rows are flagged.
+// Half-warp sort of a row of <= 16 entries (lanes 16h..16h+15), in place,
+// unique-compacted; returns the kept count (uniform within the half).
+__device__ __forceinline__ uint32_t half_sort_row(uint32_t* __restrict__ data, uint64_t base,
+                                                  uint32_t len, bool unique) {
+  const uint32_t lane = lane_id(), l16 = lane & 15, half = lane >> 4;
+  uint32_t v = l16 < len ? data[base + l16] : 0xffffffffu;
+#pragma unroll
+  for (uint32_t k = 2; k <= 16; k <<= 1) {
+#pragma unroll
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      const uint32_t u = __shfl_xor_sync(0xffffffffu, v, j);
+      const bool asc = (l16 & k) == 0, low = (l16 & j) == 0;
+      v = (asc == low) ? (u < v ? u : v) : (u > v ? u : v);
+    }
+  }
+  const uint32_t prev = __shfl_up_sync(0xffffffffu, v, 1, 16);
+  const bool keep = l16 < len && (!unique || l16 == 0 || v != prev);
+  const uint32_t m = (__ballot_sync(0xffffffffu, keep) >> (16 * half)) & 0xffffu;
+  if (keep) data[base + __popc(m & ((1u << l16) - 1))] = v;
+  return __popc(m);
+}
+
+// One warp per row for rows of length <= 128 (two rows per warp, one per
+// half-warp, when both hold <= 16 entries); longer rows are flagged.
 __global__ void row_sort_small_kernel(uint32_t* __restrict__ data, const uint64_t* __restrict__ off,
                                       uint64_t n_rows, int unique, uint32_t* __restrict__ kept,
                                       uint32_t* __restrict__ long_flag) {
   const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x / 32);
-  for (uint64_t r = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); r < n_rows;
-       r += warps) {
-    const uint64_t b = off[r];
-    const uint32_t len = (uint32_t)(off[r + 1] - b);
+  const uint32_t lane = lane_id();
+  for (uint64_t r2 = ((uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5)) * 2;
+       r2 < n_rows; r2 += warps * 2) {
+    const uint64_t b0 = off[r2], b1 = off[r2 + 1];
+    const uint64_t b2 = r2 + 1 < n_rows ? off[r2 + 2] : b1;
+    const uint32_t l0 = (uint32_t)(b1 - b0), l1 = (uint32_t)(b2 - b1);
+    if (l0 <= 16 && l1 <= 16) {  // both rows in one pass, a half-warp each
+      const uint32_t h = lane >> 4;
+      const uint64_t b = h ? b1 : b0;
+      const uint32_t len = h ? l1 : l0;
+      const uint32_t k = half_sort_row(data, b, len, unique);  // both halves converge
+      if ((lane & 15) == 0 && r2 + h < n_rows) {
+        kept[r2 + h] = k;
+        long_flag[r2 + h] = 0u;
+      }
+      continue;
+    }
+    for (uint64_t r = r2; r < r2 + 2 && r < n_rows; ++r) {
+    const uint64_t b = r == r2 ? b0 : b1;
+    const uint32_t len = r == r2 ? l0 : l1;
     uint32_t k = len;
     bool lng = false;
     if (len <= 1) {
@@ -129,6 +168,7 @@ __global__ void row_sort_small_kernel(uint32_t* __restrict__ data, const uint64_
     if (lane_id() == 0) {
       kept[r] = k;
       long_flag[r] = lng ? 1u : 0u;
+    }
     }
   }
 }
