@@ -184,8 +184,11 @@ void run_sparse(Ctx& X, const SparseInputs& in, d3g::Decode dec, int mode, d3g::
     fl[b] = X.alloc<uint32_t>(nx);
     pos[b] = X.alloc<uint64_t>(nx + 1);
   }
-  D3G_LAUNCH(X, sparse_bin_kernel, grid_for(nx, 256), 256, 0, cx.p, nx, 32ull, mid_max, fl[0].p,
-             fl[1].p, fl[2].p);
+  // the register-sort tier takes c_x <= 128 unless the bitset tier applies
+  // (cfg2's 3,406 sparse z), where c_x > 32 goes to the bitset rows
+  const uint64_t small_max = bitset_tier ? 32ull : (uint64_t)kSmallMax;
+  D3G_LAUNCH(X, sparse_bin_kernel, grid_for(nx, 256), 256, 0, cx.p, nx, small_max, mid_max,
+             fl[0].p, fl[1].p, fl[2].p);
   for (int b = 0; b < 3; ++b) exclusive_scan<uint32_t>(X, fl[b].p, nx, pos[b].p);
   {  // the three tier sizes and the candidate total in one round trip
     DBuf<unsigned long long> sizes = X.alloc<unsigned long long>(4);

@@ -115,7 +115,71 @@ __device__ __forceinline__ uint32_t bitonic32(uint32_t v) {
   return v;
 }
 
-// One warp per x with c_x <= 32.
+// Sorted-unique count of one warp-held candidate set of up to 32*E values
+// (sentinel 0xffffffff pads), with the pair accounting of the tiers.
+template <int kMode, int E>
+__device__ __forceinline__ void small_tier_finish(uint32_t (&v)[E], uint32_t x,
+                                                  const uint32_t* __restrict__ sparse_ids,
+                                                  const Decode& dec, const Emit& em, uint64_t& cnt,
+                                                  uint64_t& sum, uint64_t& xr) {
+  const uint32_t lane = lane_id();
+  if (E == 1) {
+    v[0] = bitonic32(v[0]);
+  } else {
+    // bitonic over 32*E values, element e*32+lane in v[e]
+#pragma unroll
+    for (int k = 2; k <= 32 * E; k <<= 1) {
+#pragma unroll
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        if (j >= 32) {
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const int pe = e ^ (j / 32);
+            if (pe > e) {
+              const uint32_t i = (uint32_t)e * 32 + lane;
+              const bool up = (i & k) == 0;
+              const uint32_t a = v[e], bb = v[pe];
+              const bool swap = up ? (a > bb) : (a < bb);
+              if (swap) {
+                v[e] = bb;
+                v[pe] = a;
+              }
+            }
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const uint32_t i = (uint32_t)e * 32 + lane;
+            const uint32_t o = __shfl_xor_sync(0xffffffffu, v[e], j);
+            const bool up = (i & k) == 0, lower = (lane & j) == 0;
+            const uint32_t mn = v[e] < o ? v[e] : o, mx = v[e] < o ? o : v[e];
+            v[e] = (lower == up) ? mn : mx;
+          }
+        }
+      }
+    }
+  }
+  uint32_t prev_last = 0xffffffffu;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    uint32_t prev = __shfl_up_sync(0xffffffffu, v[e], 1);
+    if (lane == 0) prev = prev_last;
+    const bool fresh = v[e] != 0xffffffffu && ((e == 0 && lane == 0) || v[e] != prev);
+    cnt += fresh;
+    if (kMode == kModeChecksum && fresh) {
+      const uint64_t h = dec.hash(x, sparse_ids[v[e]]);
+      sum += h;
+      xr ^= h;
+    }
+    if (kMode == kModeEmit) emit_pair(em, fresh, x, fresh ? sparse_ids[v[e]] : 0);
+    prev_last = __shfl_sync(0xffffffffu, v[e], 31);
+  }
+}
+
+// One warp per x with c_x <= 128: the candidates are gathered into a
+// per-warp shared buffer, sorted in registers (bitonic over 32, 64 or 128
+// values) and counted unique.
+constexpr int kSmallMax = 128;
 template <int kMode>
 __global__ void __launch_bounds__(256)
 sparse_small_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
@@ -123,7 +187,7 @@ sparse_small_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
                     const uint64_t* __restrict__ sp_ptr, const uint32_t* __restrict__ sp_col,
                     const uint32_t* __restrict__ sparse_ids, Decode dec, Emit em, Tally* tally,
                     Filter flt) {
-  __shared__ uint32_t buf[8][32];
+  __shared__ uint32_t buf[8][kSmallMax];
   const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
   uint64_t cnt = 0, sum = 0, xr = 0;
   for (uint64_t i = (uint64_t)blockIdx.x * 8 + w; i < n_x; i += (uint64_t)gridDim.x * 8) {
@@ -132,11 +196,10 @@ sparse_small_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
     uint32_t nc = 0;
     for (uint64_t base = r0; base < r1; base += 32) {
       uint64_t k = base + lane;
-      uint32_t y = 0;
       uint32_t len = 0;
       uint64_t s0 = 0;
       if (k < r1) {
-        y = r_col[k];
+        const uint32_t y = r_col[k];
         s0 = sp_ptr[y];
         len = (uint32_t)(sp_ptr[y + 1] - s0);
       }
@@ -148,23 +211,28 @@ sparse_small_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
       }
       uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
       uint32_t off = nc + incl - len;
-      for (uint32_t t = 0; t < len && off + t < 32; ++t) buf[w][off + t] = sp_col[s0 + t];
+      for (uint32_t t = 0; t < len && off + t < kSmallMax; ++t) buf[w][off + t] = sp_col[s0 + t];
       nc += tot;
     }
     __syncwarp();
-    uint32_t v = lane < nc ? buf[w][lane] : 0xffffffffu;
-    __syncwarp();
-    if (v != 0xffffffffu && flt.skip(x, v)) v = 0xffffffffu;
-    v = bitonic32(v);
-    uint32_t prev = __shfl_up_sync(0xffffffffu, v, 1);
-    bool fresh = v != 0xffffffffu && (lane == 0 || v != prev);
-    cnt += fresh;
-    if (kMode == kModeChecksum && fresh) {
-      uint64_t h = dec.hash(x, sparse_ids[v]);
-      sum += h;
-      xr ^= h;
+    auto load = [&](uint32_t idx) {
+      uint32_t v = idx < nc ? buf[w][idx] : 0xffffffffu;
+      if (v != 0xffffffffu && flt.skip(x, v)) v = 0xffffffffu;
+      return v;
+    };
+    if (nc <= 32) {
+      uint32_t v[1] = {load(lane)};
+      __syncwarp();
+      small_tier_finish<kMode, 1>(v, x, sparse_ids, dec, em, cnt, sum, xr);
+    } else if (nc <= 64) {
+      uint32_t v[2] = {load(lane), load(32 + lane)};
+      __syncwarp();
+      small_tier_finish<kMode, 2>(v, x, sparse_ids, dec, em, cnt, sum, xr);
+    } else {
+      uint32_t v[4] = {load(lane), load(32 + lane), load(64 + lane), load(96 + lane)};
+      __syncwarp();
+      small_tier_finish<kMode, 4>(v, x, sparse_ids, dec, em, cnt, sum, xr);
     }
-    if (kMode == kModeEmit) emit_pair(em, fresh, x, fresh ? sparse_ids[v] : 0);
   }
   tally_flush(tally, cnt, sum, xr);
 }
