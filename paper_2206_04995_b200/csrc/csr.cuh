@@ -84,7 +84,7 @@ inline void build_csr_device(Ctx& ctx, const uint32_t* maj, const uint32_t* mnr,
   exclusive_scan<uint32_t>(ctx, cnt.p, n_rows, out.row_ptr.p);
   out.nnz = ctx.scalar(out.row_ptr.p + n_rows);
   out.col = ctx.alloc<uint32_t>(out.nnz);
-  D3G_LAUNCH(ctx, row_compact_kernel, grid_for(n_rows * 32, 256), 256, 0, tmp.p, off.p,
+  D3G_LAUNCH(ctx, row_compact_kernel, grid_for(n_rows * 8, 256), 256, 0, tmp.p, off.p,
              out.row_ptr.p, n_rows, out.col.p);
 }
 

@@ -1528,7 +1528,7 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   {
     DBuf<uint32_t> cnt = X.zeros<uint32_t>(y_card);
     if (n_sparse)
-      D3G_LAUNCH(X, sparse_y_count_kernel, grid_for(n_sparse * 32, 256), 256, 0,
+      D3G_LAUNCH(X, sparse_y_count_kernel, grid_for(n_sparse * 8, 256), 256, 0,
                  sz_csr.row_ptr.p, sz_csr.col.p, sparse_ids.p, n_sparse, cnt.p);
     exclusive_scan<uint32_t>(X, cnt.p, y_card, sp_ptr.p);
     rep->sparse_nnz = P.sparse_nnz;  // = sp_ptr[y_card], known on the host
@@ -1536,7 +1536,7 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
     DBuf<unsigned long long> cur = X.alloc<unsigned long long>(y_card + 1);
     D3G_CUDA(cudaMemcpyAsync(cur.p, sp_ptr.p, (y_card + 1) * 8, cudaMemcpyDeviceToDevice, X.stream));
     if (n_sparse)
-      D3G_LAUNCH(X, sparse_y_scatter_kernel, grid_for(n_sparse * 32, 256), 256, 0,
+      D3G_LAUNCH(X, sparse_y_scatter_kernel, grid_for(n_sparse * 8, 256), 256, 0,
                  sz_csr.row_ptr.p, sz_csr.col.p, sparse_ids.p, n_sparse, cur.p, sp_col.p);
   }
   // dense side

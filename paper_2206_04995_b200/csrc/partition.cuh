@@ -38,15 +38,18 @@ __global__ void dense_flag_kernel(const uint64_t* __restrict__ row_ptr, uint64_t
 
 
 // per-y count of sparse tuples
+// Both passes take four rows per warp (8 lanes each): the sparse rows are
+// short (cfg3: ~10 entries), and a warp per row left most lanes idle.
 __global__ void sparse_y_count_kernel(const uint64_t* __restrict__ row_ptr,
                                       const uint32_t* __restrict__ col,
                                       const uint32_t* __restrict__ sparse_ids, uint64_t n_sparse,
                                       uint32_t* __restrict__ cnt) {
-  for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < n_sparse;
-       i += (uint64_t)gridDim.x * (blockDim.x / 32)) {
-    uint32_t z = sparse_ids[i];
-    for (uint64_t k = row_ptr[z] + lane_id(); k < row_ptr[z + 1]; k += 32)
-      atomicAdd(&cnt[col[k]], 1u);
+  const uint32_t gl = threadIdx.x & 7;
+  for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 8) + (threadIdx.x >> 3); i < n_sparse;
+       i += (uint64_t)gridDim.x * (blockDim.x / 8)) {
+    const uint32_t z = sparse_ids[i];
+    const uint64_t e = row_ptr[z + 1];
+    for (uint64_t k = row_ptr[z] + gl; k < e; k += 8) atomicAdd(&cnt[col[k]], 1u);
   }
 }
 
@@ -55,11 +58,13 @@ __global__ void sparse_y_scatter_kernel(const uint64_t* __restrict__ row_ptr,
                                         const uint32_t* __restrict__ sparse_ids, uint64_t n_sparse,
                                         unsigned long long* __restrict__ cursor,
                                         uint32_t* __restrict__ out_col) {
-  for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < n_sparse;
-       i += (uint64_t)gridDim.x * (blockDim.x / 32)) {
-    uint32_t z = sparse_ids[i];
-    for (uint64_t k = row_ptr[z] + lane_id(); k < row_ptr[z + 1]; k += 32) {
-      uint64_t p = atomicAdd(&cursor[col[k]], 1ull);
+  const uint32_t gl = threadIdx.x & 7;
+  for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 8) + (threadIdx.x >> 3); i < n_sparse;
+       i += (uint64_t)gridDim.x * (blockDim.x / 8)) {
+    const uint32_t z = sparse_ids[i];
+    const uint64_t e = row_ptr[z + 1];
+    for (uint64_t k = row_ptr[z] + gl; k < e; k += 8) {
+      const uint64_t p = atomicAdd(&cursor[col[k]], 1ull);
       out_col[p] = (uint32_t)i;  // compact sparse index
     }
   }

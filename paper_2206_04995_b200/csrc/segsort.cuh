@@ -285,11 +285,12 @@ __global__ void huge_scatter_kernel(uint32_t* __restrict__ data, const uint64_t*
 __global__ void row_compact_kernel(const uint32_t* __restrict__ data, const uint64_t* __restrict__ off,
                                    const uint64_t* __restrict__ row_ptr, uint64_t n_rows,
                                    uint32_t* __restrict__ col) {
-  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x / 32);
-  for (uint64_t r = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); r < n_rows;
-       r += warps) {
+  // 8 lanes per row: most rows are short
+  const uint32_t gl = threadIdx.x & 7;
+  for (uint64_t r = (uint64_t)blockIdx.x * (blockDim.x / 8) + (threadIdx.x >> 3); r < n_rows;
+       r += (uint64_t)gridDim.x * (blockDim.x / 8)) {
     const uint64_t s = off[r], d = row_ptr[r], k = row_ptr[r + 1] - d;
-    for (uint64_t i = lane_id(); i < k; i += 32) col[d + i] = data[s + i];
+    for (uint64_t i = gl; i < k; i += 8) col[d + i] = data[s + i];
   }
 }
 
