@@ -41,13 +41,15 @@ __global__ void hot_build_x_kernel(const uint32_t* __restrict__ xorder, uint64_t
                                    const uint32_t* __restrict__ r_col,
                                    const uint32_t* __restrict__ y_rank, uint32_t K, uint32_t kw,
                                    uint32_t* __restrict__ T, unsigned long long* __restrict__ hx) {
-  for (uint64_t p = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); p < n_live;
-       p += (uint64_t)gridDim.x * (blockDim.x / 32)) {
+  // 8 lanes per x (rows hold ~10-30 entries)
+  const uint32_t sl = threadIdx.x & 7;
+  for (uint64_t p = (uint64_t)blockIdx.x * (blockDim.x / 8) + (threadIdx.x >> 3); p < n_live;
+       p += (uint64_t)gridDim.x * (blockDim.x / 8)) {
     uint32_t x = xorder[p];
     uint64_t g = p >> 7;
     uint64_t bi = g >> 5, gl = g & 31;
     uint32_t b = (uint32_t)(p & 127);
-    for (uint64_t k = r_ptr[x] + lane_id(); k < r_ptr[x + 1]; k += 32) {
+    for (uint64_t k = r_ptr[x] + sl; k < r_ptr[x + 1]; k += 8) {
       uint32_t r = y_rank[r_col[k]];
       if (r < K) {
         atomicOr(&T[((bi * K + r) * 32 + gl) * 4 + (b >> 5)], 1u << (b & 31));
@@ -60,20 +62,16 @@ __global__ void hot_build_x_kernel(const uint32_t* __restrict__ xorder, uint64_t
 // hz from the dense lists (ranks ascending: the hot ranks are a prefix).
 __global__ void hot_build_z_kernel(const uint64_t* __restrict__ dl_ptr,
                                    const uint32_t* __restrict__ dl_col, uint64_t n_dense,
-                                   uint32_t K, uint32_t kw, unsigned long long* __restrict__ hz,
-                                   uint32_t* __restrict__ cold_len) {
-  for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < n_dense;
-       i += (uint64_t)gridDim.x * (blockDim.x / 32)) {
-    uint32_t ncold = 0;
-    for (uint64_t k = dl_ptr[i] + lane_id(); k < dl_ptr[i + 1]; k += 32) {
-      uint32_t r = dl_col[k];
-      if (r < K)
-        atomicOr(&hz[i * kw + (r >> 6)], 1ull << (r & 63));
-      else
-        ++ncold;
+                                   uint32_t K, uint32_t kw, unsigned long long* __restrict__ hz) {
+  const uint32_t sl = threadIdx.x & 7;  // 8 lanes per row
+  for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 8) + (threadIdx.x >> 3); i < n_dense;
+       i += (uint64_t)gridDim.x * (blockDim.x / 8)) {
+    const uint64_t e = dl_ptr[i + 1];
+    for (uint64_t k = dl_ptr[i] + sl; k < e; k += 8) {
+      const uint32_t r = dl_col[k];
+      if (r >= K) break;  // ranks ascend: the hot prefix ended
+      atomicOr(&hz[i * kw + (r >> 6)], 1ull << (r & 63));
     }
-    ncold = warp_sum(ncold);
-    if (lane_id() == 0 && cold_len) cold_len[i] = ncold;
   }
 }
 
@@ -89,11 +87,13 @@ __global__ void cold_count_kernel(const uint64_t* __restrict__ dl_ptr,
                                   uint64_t y_card, uint32_t part_rows, uint32_t parts,
                                   const uint64_t* __restrict__ hz, uint32_t kw, uint32_t var_bits) {
   const uint32_t nvar = 1u << var_bits, vmask = nvar - 1;
-  for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < n_dense;
-       i += (uint64_t)gridDim.x * (blockDim.x / 32)) {
+  const uint32_t sl = threadIdx.x & 7;  // 8 lanes per row
+  for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 8) + (threadIdx.x >> 3); i < n_dense;
+       i += (uint64_t)gridDim.x * (blockDim.x / 8)) {
     const uint64_t part = i / part_rows;
     const uint32_t zm = var_bits ? (uint32_t)(hz[i * kw] & vmask) : 0;
-    for (uint64_t k = dl_ptr[i] + lane_id(); k < dl_ptr[i + 1]; k += 32) {
+    const uint64_t e = dl_ptr[i + 1];
+    for (uint64_t k = dl_ptr[i] + sl; k < e; k += 8) {
       const uint32_t r = dl_col[k];
       if (r < K) continue;
       const uint32_t y = y_of_rank[r];
@@ -115,8 +115,9 @@ __global__ void cold_scatter_kernel(const uint64_t* __restrict__ dl_ptr,
                                     uint32_t var_bits) {
   const uint32_t nvar = 1u << var_bits, vmask = nvar - 1;
   const uint4* hz4 = reinterpret_cast<const uint4*>(hz);
-  for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < n_dense;
-       i += (uint64_t)gridDim.x * (blockDim.x / 32)) {
+  const uint32_t sl = threadIdx.x & 7;  // 8 lanes per row
+  for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 8) + (threadIdx.x >> 3); i < n_dense;
+       i += (uint64_t)gridDim.x * (blockDim.x / 8)) {
     const uint64_t part = i / part_rows;
     const uint32_t zm = var_bits ? (uint32_t)(hz[i * kw] & vmask) : 0;
     uint4 s0 = make_uint4(0, 0, 0, 0), s1 = s0;
@@ -124,7 +125,8 @@ __global__ void cold_scatter_kernel(const uint64_t* __restrict__ dl_ptr,
       s0 = hz4[2 * i];
       s1 = hz4[2 * i + 1];
     }
-    for (uint64_t k = dl_ptr[i] + lane_id(); k < dl_ptr[i + 1]; k += 32) {
+    const uint64_t e = dl_ptr[i + 1];
+    for (uint64_t k = dl_ptr[i] + sl; k < e; k += 8) {
       const uint32_t r = dl_col[k];
       if (r < K) continue;
       const uint32_t y = y_of_rank[r];

@@ -554,10 +554,10 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   DBuf<uint4> T = X.zeros<uint4>((uint64_t)n_batches * K * 32);
   DBuf<unsigned long long> hx = X.zeros<unsigned long long>(in.x_card * kw);
   DBuf<unsigned long long> hz = X.zeros<unsigned long long>(D * kw);
-  D3G_LAUNCH(X, hot_build_x_kernel, grid_for(n_live * 32, 256), 256, 0, xorder, n_live, in.r_ptr,
+  D3G_LAUNCH(X, hot_build_x_kernel, grid_for(n_live * 8, 256), 256, 0, xorder, n_live, in.r_ptr,
              in.r_col, in.y_rank, K, kw, reinterpret_cast<uint32_t*>(T.p), hx.p);
-  D3G_LAUNCH(X, hot_build_z_kernel, grid_for(D * 32, 256), 256, 0, in.dl_ptr, in.dl_col, D, K, kw,
-             hz.p, (uint32_t*)nullptr);
+  D3G_LAUNCH(X, hot_build_z_kernel, grid_for(D * 8, 256), 256, 0, in.dl_ptr, in.dl_col, D, K, kw,
+             hz.p);
   // P1: hot bit-sliced pass
   HotParams hp{};
   hp.T = T.p;
@@ -666,7 +666,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
         ++var_bits;
     const uint64_t rows_key = ((uint64_t)1 << var_bits) * parts * Y;
     DBuf<uint32_t> cc = X.zeros<uint32_t>(rows_key);
-    D3G_LAUNCH(X, cold_count_kernel, grid_for(D * 32, 256), 256, 0, in.dl_ptr, in.dl_col, D, K,
+    D3G_LAUNCH(X, cold_count_kernel, grid_for(D * 8, 256), 256, 0, in.dl_ptr, in.dl_col, D, K,
                in.y_of_rank, cc.p, Y, part_rows, parts,
                reinterpret_cast<const uint64_t*>(hz.p), kw, var_bits);
     DBuf<uint64_t> cptr = X.alloc<uint64_t>(rows_key + 1);
@@ -677,7 +677,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     if (cold_kernel_ok) ch = X.alloc<uint4>(2 * cnnz);
     DBuf<unsigned long long> cur = X.alloc<unsigned long long>(rows_key + 1);
     D3G_CUDA(cudaMemcpyAsync(cur.p, cptr.p, (rows_key + 1) * 8, cudaMemcpyDeviceToDevice, X.stream));
-    D3G_LAUNCH(X, cold_scatter_kernel, grid_for(D * 32, 256), 256, 0, in.dl_ptr, in.dl_col, D, K,
+    D3G_LAUNCH(X, cold_scatter_kernel, grid_for(D * 8, 256), 256, 0, in.dl_ptr, in.dl_col, D, K,
                in.y_of_rank, cur.p, ccol.p, cold_kernel_ok ? ch.p : nullptr, Y, part_rows, parts,
                reinterpret_cast<const uint64_t*>(hz.p), kw, var_bits);
     cur.reset();
