@@ -208,6 +208,23 @@ int d3g_alu_peak(d3g_ctx* ctx, double* ops_per_sec);
 int d3g_smem_peak(d3g_ctx* ctx, double* bytes_per_sec);
 int d3g_ctx_device(d3g_ctx* ctx);
 
+/* ---- map_tables (P/src/mapping.cpp:342-420) --------------------------------
+ * dim3::MappingOutput (P/include/dim3/mapping.hpp:124-132) in host arrays the
+ * caller sizes: r_x/r_y/r_kept hold up to r->n entries, s_z/s_y s->n, and the
+ * reverse dictionaries rev_x/rev_y/rev_z (code -> value) up to r->n, r->n + s->n,
+ * s->n (filled only for dictionary-coded columns; NULL to skip). Codes are
+ * the reference's exact codes. r_kept lists the surviving R rows' original
+ * indices (filled only when the semi-join dropped rows). The options use
+ * declared_x/y/z (SkipFlags) and natural_keys_auto (map_with_fallback). */
+typedef struct {
+  uint32_t *r_x, *r_y, *s_z, *s_y, *r_kept;
+  uint64_t *rev_x, *rev_y, *rev_z;
+  uint64_t kept, dropped_r, x_card, y_card, z_card;
+  int32_t natural_x, natural_y, natural_z, pad;
+} d3g_mapping;
+int d3g_map_tables(d3g_ctx* ctx, const d3g_table* r, const d3g_table* s, const d3g_opts* o,
+                   d3g_mapping* out);
+
 /* ---- join-aggregate (P/src/engine.cpp:537-722) -----------------------------
  * dim3::ValuedTable (relation.hpp:49-53): a table plus one double per row;
  * values live in device memory iff base.on_device. */

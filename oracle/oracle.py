@@ -357,6 +357,31 @@ def oracle_aggregate(r: Table, s: Table, rv, sv, combine="multiply", agg="sum"):
     return out
 
 
+def ref_map_tables(r: Table, s: Table, skip=None):
+    """dim3::map_tables through the reference library. skip = None: the
+    engine's natural-key detection with fallback; else (x, y, z) SkipFlags."""
+    lib = ref_lib()
+    rl, rr, sl, sr = (_u64(a) for a in (r.left, r.right, s.left, s.right))
+    nr, ns = len(rl), len(sl)
+    ra, rb, rk = (np.zeros(max(nr, 1), np.uint32) for _ in range(3))
+    sa, sb = (np.zeros(max(ns, 1), np.uint32) for _ in range(2))
+    st = np.zeros(6, np.uint64)
+    U32P = C.POINTER(C.c_uint32)
+    fn = lib.ref_map_tables
+    fn.argtypes = [U64P, U64P, C.c_uint64, U64P, U64P, C.c_uint64, C.c_int, C.c_int, C.c_int,
+                   C.c_int, U32P, U32P, U32P, U32P, U32P, U64P]
+    sk = skip or (0, 0, 0)
+    rc = fn(_p(rl), _p(rr), nr, _p(sl), _p(sr), ns, int(skip is None), int(sk[0]), int(sk[1]),
+            int(sk[2]), ra.ctypes.data_as(U32P), rb.ctypes.data_as(U32P), sa.ctypes.data_as(U32P),
+            sb.ctypes.data_as(U32P), rk.ctypes.data_as(U32P), _p(st))
+    if rc:
+        raise ConfigErrorLike(rc, lib.ref_last_error().decode())
+    kept = int(st[0])
+    return {"r_a": ra[:kept].copy(), "r_b": rb[:kept].copy(), "s_a": sa[:ns].copy(),
+            "s_b": sb[:ns].copy(), "r_kept": rk[:int(st[5])].copy(), "dropped_r": int(st[1]),
+            "x_card": int(st[2]), "y_card": int(st[3]), "z_card": int(st[4])}
+
+
 def ref_pipeline_split(r: Table, s: Table, consts=None):
     """ref_pipeline's statistics and dense/sparse split without building the
     panel (F2Evaluator decisions only)."""

@@ -259,6 +259,48 @@ int ref_join_aggregate(const std::uint64_t* rl, const std::uint64_t* rr,
   }
 }
 
+// dim3::map_tables with explicit SkipFlags (auto: map_like_engine's natural-key
+// detection and fallback). Codes of R (kept rows) and S, r_kept, cards.
+int ref_map_tables(const std::uint64_t* rl, const std::uint64_t* rr, std::uint64_t nr,
+                   const std::uint64_t* sl, const std::uint64_t* sr, std::uint64_t ns,
+                   int auto_skip, int skip_x, int skip_y, int skip_z, std::uint32_t* r_a,
+                   std::uint32_t* r_b, std::uint32_t* s_a, std::uint32_t* s_b,
+                   std::uint32_t* r_kept, std::uint64_t* stats /* kept, dropped, x, y, z cards, n_kept_list */) {
+  try {
+    dim3::RawTable R = to_table(rl, rr, nr);
+    dim3::RawTable S = to_table(sl, sr, ns);
+    dim3::MappingOutput m;
+    if (auto_skip) {
+      m = map_like_engine(R, S);
+    } else {
+      dim3::SkipFlags sk;
+      sk.x = skip_x != 0;
+      sk.y = skip_y != 0;
+      sk.z = skip_z != 0;
+      m = dim3::map_tables(R, S, sk);
+    }
+    for (std::size_t i = 0; i < m.r.a.size(); ++i) {
+      r_a[i] = m.r.a[i];
+      r_b[i] = m.r.b[i];
+    }
+    for (std::size_t i = 0; i < m.s.a.size(); ++i) {
+      s_a[i] = m.s.a[i];
+      s_b[i] = m.s.b[i];
+    }
+    for (std::size_t i = 0; i < m.r_kept.size(); ++i) r_kept[i] = m.r_kept[i];
+    stats[0] = m.r.a.size();
+    stats[1] = m.dropped_r;
+    stats[2] = m.r.a_card;
+    stats[3] = m.s.b_card;
+    stats[4] = m.s.a_card;
+    stats[5] = m.r_kept.size();
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return status_of(e);
+  }
+}
+
 // Pipeline facts the parity tests compare against: code-space cards, post-
 // collapse nnz, the exact distinct OUT_J (DegreeStats::out_j), and the raw
 // values of the z columns f2 marks dense (PartitionResult::panel.z_ids),

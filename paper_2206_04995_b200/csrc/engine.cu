@@ -2173,6 +2173,56 @@ int d3g_generate(d3g_ctx* ctx, int cfg, int side, uint64_t lo, uint64_t hi, uint
 
 uint64_t d3g_cfg_rows(int cfg) { return d3g::cfg_rows(cfg); }
 
+int d3g_map_tables(d3g_ctx* ctx, const d3g_table* r, const d3g_table* s, const d3g_opts* o,
+                   d3g_mapping* out) {
+  d3g::Ctx& X = ctx->c;
+  int rc = guarded([&] {
+    using namespace d3g;
+    D3G_CUDA(cudaSetDevice(X.device));
+    X.budget = o->memory_budget_bytes ? o->memory_budget_bytes : (3ull << 30);
+    const uint64_t NR = r->n, NS = s->n;
+    DBuf<uint64_t> hb[4];
+    const uint64_t *Rl = r->left, *Rr = r->right, *Sl = s->left, *Sr = s->right;
+    if (!r->on_device) {
+      hb[0] = X.alloc<uint64_t>(NR);
+      hb[1] = X.alloc<uint64_t>(NR);
+      X.to_device(hb[0].p, Rl, NR);
+      X.to_device(hb[1].p, Rr, NR);
+      Rl = hb[0].p;
+      Rr = hb[1].p;
+    }
+    if (!s->on_device) {
+      hb[2] = X.alloc<uint64_t>(NS);
+      hb[3] = X.alloc<uint64_t>(NS);
+      X.to_device(hb[2].p, Sl, NS);
+      X.to_device(hb[3].p, Sr, NS);
+      Sl = hb[2].p;
+      Sr = hb[3].p;
+    }
+    d3g_report rep{};
+    Mapped M;
+    map_inputs(X, Rl, Rr, NR, Sl, Sr, NS, o, &rep, /*want_kept=*/true, M);
+    out->kept = M.kept;
+    out->dropped_r = NR - M.kept;
+    out->x_card = M.x_card;
+    out->y_card = M.y_card;
+    out->z_card = M.z_card;
+    out->natural_x = M.D.x.identity;
+    out->natural_y = M.D.y.identity;
+    out->natural_z = M.D.z.identity;
+    if (out->r_x) X.to_host(out->r_x, M.r_x, M.kept);
+    if (out->r_y) X.to_host(out->r_y, M.r_y, M.kept);
+    if (out->s_z) X.to_host(out->s_z, M.s_z, NS);
+    if (out->s_y) X.to_host(out->s_y, M.s_y, NS);
+    if (out->r_kept && M.r_kept.p) X.to_host(out->r_kept, M.r_kept.p, M.kept);
+    if (out->rev_x && !M.D.x.identity) X.to_host(out->rev_x, M.D.x.rev.p, M.x_card);
+    if (out->rev_y && !M.D.y.identity) X.to_host(out->rev_y, M.D.y.rev.p, M.y_card);
+    if (out->rev_z && !M.D.z.identity) X.to_host(out->rev_z, M.D.z.rev.p, M.z_card);
+  });
+  X.budget = 0;
+  return rc;
+}
+
 int d3g_join_aggregate(d3g_ctx* ctx, const d3g_valued_table* r, const d3g_valued_table* s,
                        int combine, int agg, const d3g_consts* c, const d3g_opts* o,
                        d3g_report* rep, d3g_agg_pairs* out) {

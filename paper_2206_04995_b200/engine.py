@@ -254,7 +254,7 @@ EXPORTED = ["d3g_ctx_create", "d3g_ctx_destroy", "d3g_last_error", "d3g_version"
             "d3g_dense_ec_rows", "d3g_generate", "d3g_cfg_rows", "d3g_ctx_device",
             "d3g_f3_threshold", "d3g_f1", "d3g_f2_decide", "d3g_alu_peak",
             "d3g_detect_format", "d3g_binary_rows", "d3g_read_binary", "d3g_save_pairs",
-            "d3g_join_aggregate", "d3g_smem_peak"]
+            "d3g_join_aggregate", "d3g_smem_peak", "d3g_map_tables"]
 
 _lib = None
 
@@ -299,6 +299,8 @@ def lib():
         L.d3g_join_aggregate.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int,
                                          C.POINTER(_Consts), C.POINTER(_Opts), C.POINTER(_Report),
                                          C.c_void_p]
+        L.d3g_map_tables.argtypes = [C.c_void_p, C.POINTER(_Table), C.POINTER(_Table),
+                                     C.POINTER(_Opts), C.c_void_p]
         L.d3g_detect_format.argtypes = [C.c_char_p, C.c_int]
         L.d3g_binary_rows.argtypes = [C.c_char_p, U64P]
         L.d3g_read_binary.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p, C.c_void_p, C.c_uint64]
@@ -875,3 +877,60 @@ def join_aggregate_both(r: ValuedTable, s: ValuedTable, combine: CombineFn, agg:
 def aggregate_to_raw(out: AggregateResult) -> ResultSet:
     """aggregate_to_raw (engine.cpp:530-532): pairs are already raw."""
     return out.base
+
+
+# ---------------------------------------------------------------------------
+# map_tables (P/include/dim3/mapping.hpp:124-141, P/src/mapping.cpp:342-420)
+class _Mapping(C.Structure):
+    _fields_ = [(k, U32P) for k in ("r_x", "r_y", "s_z", "s_y", "r_kept")] + \
+               [(k, U64P) for k in ("rev_x", "rev_y", "rev_z")] + \
+               [(k, C.c_uint64) for k in ("kept", "dropped_r", "x_card", "y_card", "z_card")] + \
+               [(k, C.c_int32) for k in ("natural_x", "natural_y", "natural_z", "pad")]
+
+
+@dataclass
+class MappingOutput:
+    """MappingOutput on the host: MappedTable r = (r_a = x codes, r_b = y codes)
+    of the surviving rows, s = (s_a = z codes, s_b = y codes); cards; r_kept
+    (empty when nothing was dropped); rev_* decode codes to values (None for
+    identity/natural columns)."""
+    r_a: np.ndarray
+    r_b: np.ndarray
+    s_a: np.ndarray
+    s_b: np.ndarray
+    r_kept: np.ndarray
+    dropped_r: int
+    x_card: int
+    y_card: int
+    z_card: int
+    rev_x: "np.ndarray | None"
+    rev_y: "np.ndarray | None"
+    rev_z: "np.ndarray | None"
+
+
+def map_tables(r: RawTable, s: RawTable, skip: SkipFlags | None = None,
+               natural_keys_auto: bool = False, ctx: "Context | None" = None) -> MappingOutput:
+    """dim3::map_tables on the GPU (HBM dictionaries, the reference's codes).
+    skip = SkipFlags: columns declared natural (identity codes, no y
+    semi-join when y is skipped); natural_keys_auto: map_with_fallback."""
+    ctx = ctx or default_context()
+    skip = skip or SkipFlags()
+    nr, ns = r.size(), s.size()
+    bufs = {k: np.zeros(max(n, 1), np.uint32) for k, n in
+            (("r_x", nr), ("r_y", nr), ("r_kept", nr), ("s_z", ns), ("s_y", ns))}
+    revs = {"rev_x": np.zeros(max(nr, 1), np.uint64), "rev_y": np.zeros(max(nr + ns, 1), np.uint64),
+            "rev_z": np.zeros(max(ns, 1), np.uint64)}
+    m = _Mapping(*[bufs[k].ctypes.data_as(U32P) for k in ("r_x", "r_y", "s_z", "s_y", "r_kept")],
+                 *[revs[k].ctypes.data_as(U64P) for k in ("rev_x", "rev_y", "rev_z")])
+    cfg = EngineConfig(natural_keys_auto=natural_keys_auto, natural_keys_declared=skip)
+    rt, st = _table_struct(r), _table_struct(s)
+    _check(lib().d3g_map_tables(ctx.handle, C.byref(rt), C.byref(st), C.byref(_opts(cfg)),
+                                C.byref(m)))
+    kept = int(m.kept)
+    return MappingOutput(bufs["r_x"][:kept].copy(), bufs["r_y"][:kept].copy(),
+                         bufs["s_z"][:ns].copy(), bufs["s_y"][:ns].copy(),
+                         bufs["r_kept"][:kept].copy() if m.dropped_r else np.zeros(0, np.uint32),
+                         int(m.dropped_r), int(m.x_card), int(m.y_card), int(m.z_card),
+                         None if m.natural_x else revs["rev_x"][:m.x_card].copy(),
+                         None if m.natural_y else revs["rev_y"][:m.y_card].copy(),
+                         None if m.natural_z else revs["rev_z"][:m.z_card].copy())
