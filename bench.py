@@ -450,6 +450,8 @@ def main():
             h.copy_(d)
         Rh = d3.RawTable(hbuf[0].numpy().view(np.uint64), hbuf[1].numpy().view(np.uint64))
         Sh = d3.RawTable(hbuf[2].numpy().view(np.uint64), hbuf[3].numpy().view(np.uint64))
+        if cfg_id == 2:  # the self-join config (S := R): the relation is passed once, as both sides
+            Sh = Rh
         for _ in range(max(1, args.warmup)):
             d3.join_project(Rh, Sh, ecfg, consts, ctx=ctx)
         ts, h2d, d2h = [], 0, 0
@@ -462,6 +464,8 @@ def main():
             h2d, d2h = o.report.h2d_bytes, o.report.d2h_bytes
             assert o.report.out_p == total_pairs
         e2e = {"value": n_tuples / (sum(ts) / len(ts)), "unit": "tuples/s",
+               "inputs": ("self-join: the pinned host relation is passed as both R and S "
+                          "(copied once)") if cfg_id == 2 else "R and S pinned host tables",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": 1e3 * sum(ts) / len(ts),
                "pairs_per_sec": total_pairs / (sum(ts) / len(ts))}

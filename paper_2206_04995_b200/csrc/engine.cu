@@ -1420,7 +1420,10 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
     Rr = hb[1].p;
     rep->h2d_bytes += NR * 16;
   }
-  if (!S->on_device) {
+  if (!S->on_device && S->left == R->left && S->right == R->right && NS == NR) {
+    Sl = Rl;  // the same host relation passed twice (a self-join): copied once
+    Sr = Rr;
+  } else if (!S->on_device) {
     hb[2] = X.alloc<uint64_t>(NS);
     hb[3] = X.alloc<uint64_t>(NS);
     X.to_device(hb[2].p, S->left, NS);

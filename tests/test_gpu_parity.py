@@ -302,3 +302,8 @@ def test_self_join_reuses_the_csr_and_matches(monkeypatch):
         assert pair_set(a.result.raw_x, a.result.raw_z) == want
         for k in ("out_p", "pairs_dense", "pairs_sparse", "dense_z", "s_nnz", "r_nnz", "out_j"):
             assert getattr(a.report, k) == getattr(b.report, k), k
+        # the same host relation passed as both sides is copied to the device once
+        t = d3.RawTable(*r)
+        c = d3.join_project(t, t, d3.EngineConfig(force=d3.Strategy.hybrid), C)
+        assert c.report.h2d_bytes == 16 * len(r[0])
+        assert pair_set(c.result.raw_x, c.result.raw_z) == want
