@@ -24,25 +24,25 @@ __device__ __forceinline__ uint64_t est_slot(uint64_t v, uint64_t mask) {
   return h & mask;
 }
 
-// counts[slot] = multiplicity of key in the S sample
+// counts[slot] = multiplicity of key in the S sample. Open addressing with a
+// 64-bit atomicCAS on the key (empty = all ones), so the slot a value lands
+// in is decided atomically at L2 -- no published-flag protocol, whose
+// key reads could be served stale from another SM's L1 and split a value
+// across two slots. The value 2^64-1 itself is counted in counts[cap].
 __global__ void est_insert_kernel(const uint64_t* __restrict__ vals, uint64_t n,
-                                  unsigned long long* __restrict__ keys, uint32_t* __restrict__ used,
+                                  unsigned long long* __restrict__ keys,
                                   unsigned int* __restrict__ counts, uint64_t mask) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t v = vals[i];
+    if (v == ~0ull) {
+      atomicAdd(&counts[mask + 1], 1u);
+      continue;
+    }
     uint64_t s = est_slot(v, mask);
     for (;;) {
-      if (atomicCAS(&used[s], 0u, 1u) == 0u) {
-        keys[s] = v;
-        __threadfence();
-        atomicExch(&used[s], 2u);  // published
-        atomicAdd(&counts[s], 1u);
-        break;
-      }
-      while (atomicAdd(&used[s], 0u) == 1u) {
-      }  // wait until the owner publishes the key
-      if (keys[s] == v) {
+      const unsigned long long prev = atomicCAS(&keys[s], ~0ull, (unsigned long long)v);
+      if (prev == ~0ull || prev == v) {
         atomicAdd(&counts[s], 1u);
         break;
       }
@@ -53,16 +53,21 @@ __global__ void est_insert_kernel(const uint64_t* __restrict__ vals, uint64_t n,
 
 __global__ void est_probe_kernel(const uint64_t* __restrict__ vals, uint64_t n,
                                  const unsigned long long* __restrict__ keys,
-                                 const uint32_t* __restrict__ used,
                                  const unsigned int* __restrict__ counts, uint64_t mask,
                                  unsigned long long* __restrict__ hits) {
   uint64_t acc = 0;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t v = vals[i];
+    if (v == ~0ull) {
+      acc += counts[mask + 1];
+      continue;
+    }
     uint64_t s = est_slot(v, mask);
-    while (used[s]) {
-      if (keys[s] == v) {
+    for (;;) {
+      const uint64_t k = keys[s];
+      if (k == ~0ull) break;  // not in the sample
+      if (k == v) {
         acc += counts[s];
         break;
       }

@@ -971,13 +971,13 @@ uint64_t estimate_out_j_gpu(Ctx& X, const uint64_t* r_y, uint64_t nr, const uint
   uint64_t cap = 1024;
   while (cap < 2 * ms) cap <<= 1;
   DBuf<unsigned long long> keys = X.alloc<unsigned long long>(cap);
-  DBuf<uint32_t> used = X.zeros<uint32_t>(cap);
-  DBuf<unsigned int> counts = X.zeros<unsigned int>(cap);
+  D3G_CUDA(cudaMemsetAsync(keys.p, 0xff, cap * 8, X.stream));
+  DBuf<unsigned int> counts = X.zeros<unsigned int>(cap + 1);
   DBuf<unsigned long long> hits = X.zeros<unsigned long long>(1);
-  D3G_LAUNCH(X, est_insert_kernel, grid_for(ms, 256), 256, 0, smp.p + mr, ms, keys.p, used.p,
-             counts.p, cap - 1);
-  D3G_LAUNCH(X, est_probe_kernel, grid_for(mr, 256), 256, 0, smp.p, mr, keys.p, used.p, counts.p,
-             cap - 1, hits.p);
+  D3G_LAUNCH(X, est_insert_kernel, grid_for(ms, 256), 256, 0, smp.p + mr, ms, keys.p, counts.p,
+             cap - 1);
+  D3G_LAUNCH(X, est_probe_kernel, grid_for(mr, 256), 256, 0, smp.p, mr, keys.p, counts.p, cap - 1,
+             hits.p);
   const uint64_t h = X.scalar(hits.p);
   if (exact) return h;
   long double scaled = static_cast<long double>(h) * (static_cast<long double>(ns) / ms) *
@@ -1627,8 +1627,15 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   rep->ms_decode = T.ms(8, 9);
   rep->ms_total = T.ms(0, 9);
   if (classical) {
+    // hash_join_dedup's report (engine.cpp:386-395): no mapping/partition
+    // fields; the x-partitioned internals are kept only in the phase times
     rep->pairs_classical = rep->out_p;
     rep->ms_classical = T.ms(2, 9);
+    rep->dropped_r = rep->x_card = rep->y_card = rep->z_card = 0;
+    rep->sparse_z = rep->dense_z = rep->f2_evaluations = rep->panel_bytes = 0;
+    rep->pairs_sparse = rep->pairs_dense = rep->r_nnz = rep->s_nnz = rep->out_j = 0;
+    rep->spa_inner_count = rep->x_live = rep->sparse_nnz = 0;
+    rep->natural_x = rep->natural_y = rep->natural_z = 0;
   }
   rep->peak_bytes = X.peak_bytes - base_live;
   rep->gpu_launches = X.launches;

@@ -154,7 +154,8 @@ def test_x_code_ranges_partition_the_output():
     for _ in range(6):
         r, s = random_instance(rng)
         want = oracle_pairs(r, s)
-        full = d3.join_project(d3.RawTable(*r), d3.RawTable(*s), d3.EngineConfig(), C)
+        hy = d3.Strategy.hybrid  # the classical report carries no code cards
+        full = d3.join_project(d3.RawTable(*r), d3.RawTable(*s), d3.EngineConfig(force=hy), C)
         swapped = full.report.swapped
         xc = full.report.x_card
         cuts = sorted({0, xc, rng.bounded(xc + 1), rng.bounded(xc + 1)})
@@ -163,7 +164,7 @@ def test_x_code_ranges_partition_the_output():
             if lo == hi:
                 continue
             out = d3.join_project(d3.RawTable(*r), d3.RawTable(*s),
-                                  d3.EngineConfig(x_code_range=(lo, hi)), C)
+                                  d3.EngineConfig(force=hy, x_code_range=(lo, hi)), C)
             part = pair_set(out.result.raw_x, out.result.raw_z)
             assert not (part & got)
             got |= part
