@@ -79,7 +79,6 @@ struct DBuf {
 struct Ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
-  cudaEvent_t ev[24] = {};
   uint64_t launches = 0;
   uint64_t d2h_bytes = 0;  // device->host bytes read back by the current call
   uint64_t live_bytes = 0, peak_bytes = 0, budget = 0;

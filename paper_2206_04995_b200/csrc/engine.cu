@@ -1910,6 +1910,9 @@ void d3g_ctx_destroy(d3g_ctx* ctx) {
   cudaStreamSynchronize(ctx->c.stream);
   if (ctx->c.pinned) cudaFreeHost(ctx->c.pinned);
   cudaStreamDestroy(ctx->c.stream);
+  // return the memory this context kept reserved in the device pool
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, ctx->c.device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
   delete ctx;
 }
 
