@@ -10,6 +10,7 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/dim3_b200.h"
@@ -164,12 +165,70 @@ struct Ctx {
     to_host(&v, src, 1);
     return v;
   }
+  // Device -> pageable host copy of a large buffer: 64 MB chunks through two
+  // pinned staging buffers, the D2H of chunk k+1 overlapping the (threaded)
+  // host copy of chunk k. A plain cudaMemcpy into pageable memory runs at a
+  // few GB/s; this path runs near the PCIe rate.
+  void* stage[2] = {nullptr, nullptr};
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+  static constexpr size_t kStage = 64ull << 20;
+  void copy_to_pageable(void* dst, const void* src, size_t bytes);
   template <class T>
   void to_device(T* dst, const T* src, uint64_t n) {
     if (n == 0) return;
     D3G_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyHostToDevice, stream));
   }
 };
+
+inline void Ctx::copy_to_pageable(void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return;
+  for (int b = 0; b < 2; ++b)
+    if (!stage[b]) {
+      D3G_CUDA(cudaMallocHost(&stage[b], kStage));
+      D3G_CUDA(cudaEventCreateWithFlags(&stage_ev[b], cudaEventDisableTiming));
+    }
+  auto host_copy = [](char* d, const char* s, size_t n) {
+    const unsigned nt = n >= (8u << 20) ? 8u : 1u;
+    if (nt == 1) {
+      std::memcpy(d, s, n);
+      return;
+    }
+    std::vector<std::thread> th;
+    const size_t part = (n + nt - 1) / nt;
+    for (unsigned t = 0; t < nt; ++t) {
+      const size_t o = t * part;
+      if (o >= n) break;
+      th.emplace_back([=] { std::memcpy(d + o, s + o, (n - o) < part ? (n - o) : part); });
+    }
+    for (auto& t : th) t.join();
+  };
+  const char* s = static_cast<const char*>(src);
+  char* d = static_cast<char*>(dst);
+  size_t issued = 0, done = 0;
+  size_t len[2] = {0, 0}, off[2] = {0, 0};
+  int b = 0;
+  // prime: chunk 0
+  len[0] = bytes < kStage ? bytes : kStage;
+  D3G_CUDA(cudaMemcpyAsync(stage[0], s, len[0], cudaMemcpyDeviceToHost, stream));
+  D3G_CUDA(cudaEventRecord(stage_ev[0], stream));
+  off[0] = 0;
+  issued = len[0];
+  while (done < bytes) {
+    const int nb = b ^ 1;
+    if (issued < bytes) {  // next chunk into the other buffer (free: copied out before)
+      len[nb] = (bytes - issued) < kStage ? (bytes - issued) : kStage;
+      off[nb] = issued;
+      D3G_CUDA(cudaMemcpyAsync(stage[nb], s + issued, len[nb], cudaMemcpyDeviceToHost, stream));
+      D3G_CUDA(cudaEventRecord(stage_ev[nb], stream));
+      issued += len[nb];
+    }
+    D3G_CUDA(cudaEventSynchronize(stage_ev[b]));
+    host_copy(d + off[b], static_cast<const char*>(stage[b]), len[b]);
+    done += len[b];
+    b = nb;
+  }
+  d2h_bytes += bytes;
+}
 
 template <class T>
 DBuf<T>& DBuf<T>::operator=(DBuf&& o) noexcept {

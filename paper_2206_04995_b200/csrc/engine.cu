@@ -781,12 +781,12 @@ __global__ void decode_pairs_kernel(const uint32_t* __restrict__ xc, const uint3
 }
 
 __global__ void pair_key_kernel(const uint32_t* __restrict__ xc, const uint32_t* __restrict__ zc,
-                                uint64_t n, int swapped, uint64_t* __restrict__ keys,
+                                uint64_t n, int swapped, int lo_bits, uint64_t* __restrict__ keys,
                                 uint32_t* __restrict__ idx) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     uint64_t a = swapped ? zc[i] : xc[i], b = swapped ? xc[i] : zc[i];
-    keys[i] = (a << 32) | b;
+    keys[i] = (a << lo_bits) | b;
     idx[i] = (uint32_t)i;
   }
 }
@@ -917,21 +917,38 @@ void build_dense_layout(Ctx& X, const d3g::DeviceCsr& rx, uint64_t max_mx,
 // (identity when rev is null) in the caller's orientation, copy out.
 void materialize_pairs(Ctx& X, uint64_t total, const std::function<void(d3g::Emit)>& emit,
                        const uint64_t* rev_x, const uint64_t* rev_z, bool swapped,
-                       d3g_pairs* pairs, d3g_report* rep) {
+                       d3g_pairs* pairs, d3g_report* rep, uint64_t x_card, uint64_t z_card) {
   using namespace d3g;
   if (pairs->cap < total)
     throw ResourceError("output buffer holds " + std::to_string(pairs->cap) + " pairs, need " +
                         std::to_string(total));
+  const bool trace = std::getenv("D3G_TRACE") != nullptr;
+  auto tp = std::chrono::steady_clock::now();
+  auto tr = [&](const char* what) {
+    if (!trace) return;
+    X.sync();
+    auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[materialize] %-8s %8.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t1 - tp).count());
+    tp = t1;
+  };
   DBuf<uint32_t> ex = X.alloc<uint32_t>(total), ez = X.alloc<uint32_t>(total);
   DBuf<unsigned long long> cur = X.zeros<unsigned long long>(1);
   emit(Emit{ex.p, ez.p, cur.p, total});
+  tr("emit");
   DBuf<uint64_t> keys = X.alloc<uint64_t>(total);
   DBuf<uint32_t> idx = X.alloc<uint32_t>(total);
   if (total) {
+    // sort key = (caller x code, caller z code) packed in as few bits as the
+    // code spaces need (fewer 8-bit radix passes than a 64-bit key)
+    const uint64_t a_card = swapped ? z_card : x_card, b_card = swapped ? x_card : z_card;
+    const int lo = std::max(1, bits_for(b_card ? b_card - 1 : 0));
+    const int hi = std::max(1, bits_for(a_card ? a_card - 1 : 0));
     D3G_LAUNCH(X, pair_key_kernel, grid_for(total, 256), 256, 0, ex.p, ez.p, total,
-               swapped ? 1 : 0, keys.p, idx.p);
-    radix_sort(X, keys.p, idx.p, total, 64);
+               swapped ? 1 : 0, lo, keys.p, idx.p);
+    radix_sort(X, keys.p, idx.p, total, std::min(64, lo + hi));
   }
+  tr("sort");
   DBuf<uint32_t> sx2 = X.alloc<uint32_t>(total), sz2 = X.alloc<uint32_t>(total);
   if (total)
     D3G_LAUNCH(X, permute_pairs_kernel, grid_for(total, 256), 256, 0, idx.p, total, ex.p, ez.p,
@@ -948,11 +965,12 @@ void materialize_pairs(Ctx& X, uint64_t total, const std::function<void(d3g::Emi
   if (total)
     D3G_LAUNCH(X, decode_pairs_kernel, grid_for(total, 256), 256, 0, sx2.p, sz2.p, total, rev_x,
                rev_z, swapped ? 1 : 0, dox, doz);
+  tr("decode");
   if (!pairs->on_device && total) {
-    D3G_CUDA(cudaMemcpyAsync(pairs->x, ox.p, total * 8, cudaMemcpyDeviceToHost, X.stream));
-    D3G_CUDA(cudaMemcpyAsync(pairs->z, oz.p, total * 8, cudaMemcpyDeviceToHost, X.stream));
-    rep->d2h_bytes += total * 16;
+    X.copy_to_pageable(pairs->x, ox.p, total * 8);
+    X.copy_to_pageable(pairs->z, oz.p, total * 8);
   }
+  tr("d2h");
   pairs->n = total;
 }
 
@@ -1057,7 +1075,7 @@ void classical_impl(Ctx& X, const uint64_t* Rl, const uint64_t* Rr, uint64_t NR,
   if (materialize) {
     DBuf<Tally> t2 = X.zeros<Tally>(1);
     materialize_pairs(X, h.count, [&](Emit em) { run(kModeEmit, em, t2.p); }, rev_or_null(D.x),
-                      rev_or_null(D.z), swapped, pairs, rep);
+                      rev_or_null(D.z), swapped, pairs, rep, D.x.card, D.z.card);
   }
 }
 
@@ -1613,7 +1631,7 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
       else
         run_sparse(X, si, dec, kModeEmit, em, tmp);
       run_dense(X, di, dec, kModeEmit, em, tmp);
-    }, rev_or_null(D.x), rev_or_null(D.z), swapped, pairs, rep);
+    }, rev_or_null(D.x), rev_or_null(D.z), swapped, pairs, rep, x_card, z_card);
   T.mark();  // 9
   X.sync();
   rep->ms_h2d = T.ms(0, 1);
@@ -1840,10 +1858,9 @@ void join_aggregate_impl(Ctx& X, const d3g_valued_table* r, const d3g_valued_tab
     if (out->on_device) {
       D3G_CUDA(cudaMemcpyAsync(out->values, ov.p, total * 8, cudaMemcpyDeviceToDevice, X.stream));
     } else if (total) {
-      D3G_CUDA(cudaMemcpyAsync(out->x, dx.p, total * 8, cudaMemcpyDeviceToHost, X.stream));
-      D3G_CUDA(cudaMemcpyAsync(out->z, dz.p, total * 8, cudaMemcpyDeviceToHost, X.stream));
-      D3G_CUDA(cudaMemcpyAsync(out->values, ov.p, total * 8, cudaMemcpyDeviceToHost, X.stream));
-      rep->d2h_bytes += total * 24;
+      X.copy_to_pageable(out->x, dx.p, total * 8);
+      X.copy_to_pageable(out->z, dz.p, total * 8);
+      X.copy_to_pageable(out->values, ov.p, total * 8);
     }
     out->n = total;
   }
@@ -1909,6 +1926,10 @@ void d3g_ctx_destroy(d3g_ctx* ctx) {
   cudaSetDevice(ctx->c.device);
   cudaStreamSynchronize(ctx->c.stream);
   if (ctx->c.pinned) cudaFreeHost(ctx->c.pinned);
+  for (int b = 0; b < 2; ++b) {
+    if (ctx->c.stage[b]) cudaFreeHost(ctx->c.stage[b]);
+    if (ctx->c.stage_ev[b]) cudaEventDestroy(ctx->c.stage_ev[b]);
+  }
   cudaStreamDestroy(ctx->c.stream);
   // return the memory this context kept reserved in the device pool
   cudaMemPool_t pool;
@@ -2007,7 +2028,7 @@ void sort_and_copy_pairs(Ctx& X, uint32_t* ex, uint32_t* ez, uint64_t total, uin
   if (total == 0) return;
   DBuf<uint64_t> keys = X.alloc<uint64_t>(total);
   DBuf<uint32_t> idx = X.alloc<uint32_t>(total);
-  D3G_LAUNCH(X, pair_key_kernel, grid_for(total, 256), 256, 0, ex, ez, total, 0, keys.p, idx.p);
+  D3G_LAUNCH(X, pair_key_kernel, grid_for(total, 256), 256, 0, ex, ez, total, 0, 32, keys.p, idx.p);
   radix_sort(X, keys.p, idx.p, total, 64);
   DBuf<uint32_t> sx = X.alloc<uint32_t>(total), sz = X.alloc<uint32_t>(total);
   D3G_LAUNCH(X, permute_pairs_kernel, grid_for(total, 256), 256, 0, idx.p, total, ex, ez, sx.p, sz.p);
