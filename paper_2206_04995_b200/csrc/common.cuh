@@ -127,7 +127,35 @@ struct Ctx {
     D3G_CUDA(cudaMemsetAsync(b.p, 0, n * sizeof(T) + (n == 0 ? 16 : 0), stream));
     return b;
   }
-  void sync() { D3G_CUDA(cudaStreamSynchronize(stream)); }
+  uint64_t syncs = 0;  // host round trips of the current call (diagnostics)
+  // Deferred reads: small device values copied into pinned memory now and
+  // delivered to their host destinations at the next synchronisation, so
+  // independent scalars share one round trip instead of one each.
+  void* defer_host = nullptr;
+  static constexpr size_t kDeferBytes = 4096;
+  struct Deferred {
+    void* dst;
+    size_t off, bytes;
+  };
+  std::vector<Deferred> deferred;
+  size_t defer_used = 0;
+  void defer(void* dst, const void* src, size_t bytes) {
+    if (!defer_host) D3G_CUDA(cudaMallocHost(&defer_host, kDeferBytes));
+    if (defer_used + bytes > kDeferBytes) sync();  // flush first
+    D3G_CUDA(cudaMemcpyAsync(static_cast<char*>(defer_host) + defer_used, src, bytes,
+                             cudaMemcpyDeviceToHost, stream));
+    deferred.push_back({dst, defer_used, bytes});
+    defer_used += (bytes + 7) & ~size_t(7);
+  }
+  bool has_deferred() const { return !deferred.empty(); }
+  void sync() {
+    ++syncs;
+    D3G_CUDA(cudaStreamSynchronize(stream));
+    for (const Deferred& d : deferred)
+      std::memcpy(d.dst, static_cast<const char*>(defer_host) + d.off, d.bytes);
+    deferred.clear();
+    defer_used = 0;
+  }
   // After a call whose working set outgrew the pool's largest block, fault in
   // one block of (peak + 25%) and return it to the pool: the stream-ordered
   // allocator then carves later calls' buffers out of it instead of mapping

@@ -975,35 +975,54 @@ void materialize_pairs(Ctx& X, uint64_t total, const std::function<void(d3g::Emi
 }
 
 // estimate_out_j_raw on the device-resident y columns (see classical.cuh).
-uint64_t estimate_out_j_gpu(Ctx& X, const uint64_t* r_y, uint64_t nr, const uint64_t* s_y,
-                            uint64_t ns) {
+// Launched early, read at the next round trip (EstimateJob::value).
+struct EstimateJob {
+  DBuf<uint64_t> smp;
+  DBuf<unsigned long long> keys, hits;
+  DBuf<unsigned int> counts;
+  unsigned long long h = 0;
+  bool exact = true, empty = true;
+  uint64_t nr = 0, ns = 0, mr = 0, ms = 0;
+  uint64_t value(Ctx& X) {
+    if (empty) return 0;
+    if (X.has_deferred()) X.sync();
+    if (exact) return h;
+    long double scaled = static_cast<long double>(h) * (static_cast<long double>(ns) / ms) *
+                         (static_cast<long double>(nr) / mr);
+    if (scaled > static_cast<long double>(std::numeric_limits<uint64_t>::max()))
+      return std::numeric_limits<uint64_t>::max();
+    return static_cast<uint64_t>(scaled);
+  }
+};
+
+void estimate_out_j_start(Ctx& X, const uint64_t* r_y, uint64_t nr, const uint64_t* s_y,
+                          uint64_t ns, EstimateJob& J) {
   using namespace d3g;
-  if (nr == 0 || ns == 0) return 0;
+  J.empty = nr == 0 || ns == 0;
+  if (J.empty) return;
   const uint64_t exact_limit = 65536, sample_rows = 16384;
-  const bool exact = nr <= exact_limit && ns <= exact_limit;
-  const uint64_t ms = exact ? ns : std::min(ns, sample_rows), mr = exact ? nr : std::min(nr, sample_rows);
-  const uint64_t ss = exact ? 1 : ns / ms, sr = exact ? 1 : nr / mr;
-  DBuf<uint64_t> smp = X.alloc<uint64_t>(mr + ms);
-  D3G_LAUNCH(X, gather_stride_kernel, grid_for(mr, 256), 256, 0, r_y, sr, mr, smp.p);
-  D3G_LAUNCH(X, gather_stride_kernel, grid_for(ms, 256), 256, 0, s_y, ss, ms, smp.p + mr);
+  J.exact = nr <= exact_limit && ns <= exact_limit;
+  J.nr = nr;
+  J.ns = ns;
+  J.ms = J.exact ? ns : std::min(ns, sample_rows);
+  J.mr = J.exact ? nr : std::min(nr, sample_rows);
+  const uint64_t ss = J.exact ? 1 : ns / J.ms, sr = J.exact ? 1 : nr / J.mr;
+  J.smp = X.alloc<uint64_t>(J.mr + J.ms);
+  D3G_LAUNCH(X, gather_stride_kernel, grid_for(J.mr, 256), 256, 0, r_y, sr, J.mr, J.smp.p);
+  D3G_LAUNCH(X, gather_stride_kernel, grid_for(J.ms, 256), 256, 0, s_y, ss, J.ms, J.smp.p + J.mr);
   uint64_t cap = 1024;
-  while (cap < 2 * ms) cap <<= 1;
-  DBuf<unsigned long long> keys = X.alloc<unsigned long long>(cap);
-  D3G_CUDA(cudaMemsetAsync(keys.p, 0xff, cap * 8, X.stream));
-  DBuf<unsigned int> counts = X.zeros<unsigned int>(cap + 1);
-  DBuf<unsigned long long> hits = X.zeros<unsigned long long>(1);
-  D3G_LAUNCH(X, est_insert_kernel, grid_for(ms, 256), 256, 0, smp.p + mr, ms, keys.p, counts.p,
-             cap - 1);
-  D3G_LAUNCH(X, est_probe_kernel, grid_for(mr, 256), 256, 0, smp.p, mr, keys.p, counts.p, cap - 1,
-             hits.p);
-  const uint64_t h = X.scalar(hits.p);
-  if (exact) return h;
-  long double scaled = static_cast<long double>(h) * (static_cast<long double>(ns) / ms) *
-                       (static_cast<long double>(nr) / mr);
-  if (scaled > static_cast<long double>(std::numeric_limits<uint64_t>::max()))
-    return std::numeric_limits<uint64_t>::max();
-  return static_cast<uint64_t>(scaled);
+  while (cap < 2 * J.ms) cap <<= 1;
+  J.keys = X.alloc<unsigned long long>(cap);
+  D3G_CUDA(cudaMemsetAsync(J.keys.p, 0xff, cap * 8, X.stream));
+  J.counts = X.zeros<unsigned int>(cap + 1);
+  J.hits = X.zeros<unsigned long long>(1);
+  D3G_LAUNCH(X, est_insert_kernel, grid_for(J.ms, 256), 256, 0, J.smp.p + J.mr, J.ms, J.keys.p,
+             J.counts.p, cap - 1);
+  D3G_LAUNCH(X, est_probe_kernel, grid_for(J.mr, 256), 256, 0, J.smp.p, J.mr, J.keys.p,
+             J.counts.p, cap - 1, J.hits.p);
+  X.defer(&J.h, J.hits.p, 8);
 }
+
 
 // hash_join_dedup (P/src/classical.cpp:111-210) on the GPU, in engine
 // orientation; pairs swap back through decode.
@@ -1101,15 +1120,33 @@ __global__ void tables_differ_kernel(const uint64_t* __restrict__ a0, const uint
   }
 }
 
-bool tables_identical(Ctx& X, const uint64_t* Rl, const uint64_t* Rr, const uint64_t* Sl,
-                      const uint64_t* Sr, uint64_t NR, uint64_t NS) {
+// Launched early, read at the next round trip (IdentityJob::value).
+struct IdentityJob {
+  DBuf<unsigned int> differ;
+  unsigned int h = 1;
+  int known = -1;  // 0/1 when decided on the host
+  bool value(Ctx& X) {
+    if (known >= 0) return known != 0;
+    if (X.has_deferred()) X.sync();
+    return h == 0;
+  }
+};
+
+void tables_identical_start(Ctx& X, const uint64_t* Rl, const uint64_t* Rr, const uint64_t* Sl,
+                            const uint64_t* Sr, uint64_t NR, uint64_t NS, IdentityJob& J) {
   using namespace d3g;
-  if (NR != NS || NR == 0) return false;
-  if (Rl == Sl && Rr == Sr) return true;
-  DBuf<unsigned int> differ = X.zeros<unsigned int>(1);
+  if (NR != NS || NR == 0) {
+    J.known = 0;
+    return;
+  }
+  if (Rl == Sl && Rr == Sr) {
+    J.known = 1;
+    return;
+  }
+  J.differ = X.zeros<unsigned int>(1);
   D3G_LAUNCH(X, tables_differ_kernel, grid_for(NR, 256, X.sm_count * 4), 256, 0, Rl, Sl, Rr, Sr,
-             NR, differ.p);
-  return X.scalar(differ.p) == 0;
+             NR, J.differ.p);
+  X.defer(&J.h, J.differ.p, 4);
 }
 
 void copy_csr(Ctx& X, const d3g::DeviceCsr& a, d3g::DeviceCsr& b) {
@@ -1406,6 +1443,7 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   if (shard_index < 0 || shard_index >= shard_count) throw ConfigError("bad shard index");
   std::memset(rep, 0, sizeof(*rep));
   X.launches = 0;
+  X.syncs = 0;
   X.d2h_bytes = 0;
   X.budget = o->memory_budget_bytes ? o->memory_budget_bytes : (3ull << 30);
   uint64_t base_live = X.live_bytes;
@@ -1452,23 +1490,35 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   }
   T.mark();  // 1
 
-  // 2. f1 gate (engine.cpp:368-384): auto takes the classical join iff f1 > 0
-  rep->out_j_estimate = estimate_out_j_gpu(X, Rr, NR, Sr, NS);
-  rep->f1 = d3g_f1(NR, NS, rep->out_j_estimate, c);
-  rep->f1_gate_classical = (o->force == D3G_AUTO && rep->f1 > 0) ? 1 : 0;
-  const bool classical = o->force == D3G_CLASSICAL || rep->f1_gate_classical;
-  const char* strat = classical                    ? "classical"
-                      : o->force == D3G_SPARSE_ONLY ? "sparse"
-                      : o->force == D3G_DENSE_ONLY  ? "dense"
-                                                    : "hybrid";
-  std::snprintf(rep->strategy, sizeof(rep->strategy), "%s", strat);
+  // 2. f1 gate (engine.cpp:368-384): auto takes the classical join iff f1 > 0.
+  // The estimate and the self-join test are launched now and read back with
+  // the column statistics (one round trip for the three).
+  EstimateJob est;
+  estimate_out_j_start(X, Rr, NR, Sr, NS, est);
+  IdentityJob ident;
+  const bool try_selfjoin = std::getenv("D3G_NO_SELFJOIN") == nullptr;
+  if (try_selfjoin) tables_identical_start(X, Rl, Rr, Sl, Sr, NR, NS, ident);
+  const char* cls_env = std::getenv("D3G_CLASSICAL");
+  const bool global_classical = cls_env && std::strcmp(cls_env, "global") == 0;
+  bool classical = false;
+  auto decide_f1 = [&] {
+    rep->out_j_estimate = est.value(X);
+    rep->f1 = d3g_f1(NR, NS, rep->out_j_estimate, c);
+    rep->f1_gate_classical = (o->force == D3G_AUTO && rep->f1 > 0) ? 1 : 0;
+    classical = o->force == D3G_CLASSICAL || rep->f1_gate_classical;
+    const char* strat = classical                    ? "classical"
+                        : o->force == D3G_SPARSE_ONLY ? "sparse"
+                        : o->force == D3G_DENSE_ONLY  ? "dense"
+                                                      : "hybrid";
+    std::snprintf(rep->strategy, sizeof(rep->strategy), "%s", strat);
+  };
+  if (global_classical) decide_f1();
   T.mark();  // 2
   // On the GPU the classical branch runs x-partitioned: the y-grouped hash
   // join is the sparse probe of the pipeline below with every z sparse, and
   // the dedup is per x in shared memory instead of one global pair set. The
   // global-set hash_join_dedup stays available (D3G_CLASSICAL=global).
-  const char* cls_env = std::getenv("D3G_CLASSICAL");
-  if (classical && cls_env && std::strcmp(cls_env, "global") == 0) {
+  if (global_classical && classical) {
     classical_impl(X, Rl, Rr, NR, Sl, Sr, NS, swapped, o->checksum ? kModeChecksum : kModeCount,
                    materialize, rep, pairs);
     T.mark();  // 3
@@ -1485,10 +1535,10 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   }
 
   // 3-4. natural keys + mapping
-  const bool self_join = std::getenv("D3G_NO_SELFJOIN") == nullptr &&
-                         tables_identical(X, Rl, Rr, Sl, Sr, NR, NS);
   Mapped M;
   map_inputs(X, Rl, Rr, NR, Sl, Sr, NS, o, rep, /*want_kept=*/false, M);
+  if (!global_classical) decide_f1();  // delivered by map_inputs' first round trip
+  const bool self_join = try_selfjoin && ident.value(X);
   const uint64_t kept = M.kept, x_card = M.x_card, y_card = M.y_card, z_card = M.z_card;
   DictBundle& D = M.D;
   if (classical) {  // intermediate_pairs = bag join size, duplicates included
@@ -1658,6 +1708,9 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   rep->peak_bytes = X.peak_bytes - base_live;
   rep->gpu_launches = X.launches;
   rep->d2h_bytes += X.d2h_bytes;
+  if (std::getenv("D3G_TRACE"))
+    std::fprintf(stderr, "[join_project] %llu launches, %llu host round trips\n",
+                 (unsigned long long)X.launches, (unsigned long long)X.syncs);
   X.reserve_for(X.peak_bytes);
 }
 
