@@ -144,6 +144,14 @@ __global__ void cold_scatter_kernel(const uint64_t* __restrict__ dl_ptr,
   }
 }
 
+// Pairs whose dense row is a folded-in SPARSE z (row_sp[i] != 0) are also
+// counted separately, so the report keeps the reference's pairs_sparse /
+// pairs_dense split when the sparse side runs through this engine.
+__device__ __forceinline__ void flush_sp(unsigned long long* cnt_sp, uint64_t v) {
+  v = warp_sum(v);
+  if (cnt_sp && lane_id() == 0 && v) atomicAdd(cnt_sp, (unsigned long long)v);
+}
+
 // --- TMA bulk copy helpers (sm_90+ PTX, used on sm_100a) -------------------
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
@@ -301,7 +309,7 @@ dense_hot_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
 __global__ void hot_rec_kernel(const uint64_t* __restrict__ dl_ptr,
                                const uint32_t* __restrict__ dl_col, uint64_t n_dense, uint32_t K,
                                uint32_t tb, uint8_t* __restrict__ rec /* [D][32], zeroed */,
-                               uint32_t* __restrict__ rcnt) {
+                               uint32_t* __restrict__ rcnt, const uint8_t* __restrict__ row_sp) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_dense;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t k0 = dl_ptr[i], k1 = dl_ptr[i + 1];
@@ -316,7 +324,7 @@ __global__ void hot_rec_kernel(const uint64_t* __restrict__ dl_ptr,
       if (c < 32) rec[i * 32 + c] = (uint8_t)r;
       ++c;
     }
-    rcnt[i] = c | (top << 24);
+    rcnt[i] = c | (top << 24) | ((row_sp && row_sp[i]) ? 0x80000000u : 0u);
   }
 }
 
@@ -324,14 +332,15 @@ template <int kMode>
 __global__ void __launch_bounds__(kHotThreads, 1)
 dense_hot_rec_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
                      const uint32_t* __restrict__ dl_col, const uint4* __restrict__ rec,
-                     const uint32_t* __restrict__ rcnt, Decode dec, Emit em, Tally* tally) {
+                     const uint32_t* __restrict__ rcnt, Decode dec, Emit em, Tally* tally,
+                     unsigned long long* __restrict__ cnt_sp) {
   extern __shared__ __align__(128) uint4 Ts[];  // [K][32]
   __shared__ __align__(8) uint64_t bar;
   __shared__ unsigned int s_unit;
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const uint32_t n_batches = (p.groups + 31) / 32;
   const unsigned int n_units = n_batches * p.z_chunks;
-  uint64_t cnt = 0, sum = 0, xr = 0;
+  uint64_t cnt = 0, sum = 0, xr = 0, csp = 0;
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     fence_mbar_init();
@@ -383,7 +392,8 @@ dense_hot_rec_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
       }
       const uint32_t rows = (uint32_t)((z_hi - cb) < 32 ? (z_hi - cb) : 32);
       for (uint32_t j = 0; j < rows; ++j) {
-        const uint32_t c = __shfl_sync(0xffffffffu, rc, j);
+        const uint32_t cw = __shfl_sync(0xffffffffu, rc, j);
+        const uint32_t c = cw & 0xffffffu;
         uint4 acc = zero4;
         const uint32_t words[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
 #pragma unroll
@@ -421,6 +431,7 @@ dense_hot_rec_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
         }
         const uint32_t hits = __popc(acc.x) + __popc(acc.y) + __popc(acc.z) + __popc(acc.w);
         cnt += hits;
+        if (cw >> 31) csp += hits;
         if (kMode != kModeCount && hits) {
           const uint32_t zc = p.dl_z[i];
           const uint32_t ws[4] = {acc.x, acc.y, acc.z, acc.w};
@@ -449,6 +460,7 @@ dense_hot_rec_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
     }
     __syncthreads();  // Ts may be overwritten by the next unit's copy
   }
+  flush_sp(cnt_sp, csp);
   tally_flush(tally, cnt, sum, xr);
 }
 
@@ -468,14 +480,15 @@ template <int kMode>
 __global__ void __launch_bounds__(kHotThreads, 1)
 dense_hot_tab_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
                      const uint32_t* __restrict__ dl_col, const uint4* __restrict__ rec,
-                     const uint32_t* __restrict__ rcnt, Decode dec, Emit em, Tally* tally) {
+                     const uint32_t* __restrict__ rcnt, Decode dec, Emit em, Tally* tally,
+                     unsigned long long* __restrict__ cnt_sp) {
   extern __shared__ __align__(128) uint4 Ts[];  // [kTabRows + K - kTabBits][32]
   __shared__ __align__(8) uint64_t bar;
   __shared__ unsigned int s_unit;
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const uint32_t n_batches = (p.groups + 31) / 32;
   const unsigned int n_units = n_batches * p.z_chunks;
-  uint64_t cnt = 0, sum = 0, xr = 0;
+  uint64_t cnt = 0, sum = 0, xr = 0, csp = 0;
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     fence_mbar_init();
@@ -543,7 +556,7 @@ dense_hot_tab_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
       const uint32_t rows = (uint32_t)((z_hi - cb) < 32 ? (z_hi - cb) : 32);
       for (uint32_t j = 0; j < rows; ++j) {
         const uint32_t cw = __shfl_sync(0xffffffffu, rc, j);
-        const uint32_t c = cw & 0xffffffu, top = cw >> 24;
+        const uint32_t c = cw & 0xffffffu, top = (cw >> 24) & 0x7fu;
         uint4 acc = Ts[top * 32 + lane];  // entry 0 is the empty subset
         const uint32_t words[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
         // row address = rows_hi + rank * 512 B: PRMT pulls the rank byte out,
@@ -607,6 +620,7 @@ dense_hot_tab_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
         }
         const uint32_t hits = __popc(acc.x) + __popc(acc.y) + __popc(acc.z) + __popc(acc.w);
         cnt += hits;
+        if (cw >> 31) csp += hits;
         if (kMode != kModeCount && hits) {
           const uint32_t zc = p.dl_z[i];
           const uint32_t ws[4] = {acc.x, acc.y, acc.z, acc.w};
@@ -635,6 +649,7 @@ dense_hot_tab_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
     }
     __syncthreads();  // Ts may be overwritten by the next unit's copy
   }
+  flush_sp(cnt_sp, csp);
   tally_flush(tally, cnt, sum, xr);
 }
 
@@ -655,14 +670,15 @@ dense_cold_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
                   const uint4* __restrict__ hx4 /* [X][2] */, uint64_t y_card, uint32_t parts,
                   uint32_t part_rows, uint32_t var_bits, const uint32_t* __restrict__ dl_z,
                   Decode dec, Emit em,
-                  unsigned int* __restrict__ next, Tally* tally) {
+                  unsigned int* __restrict__ next, Tally* tally,
+                  const uint8_t* __restrict__ row_sp, unsigned long long* __restrict__ cnt_sp) {
   extern __shared__ __align__(16) uint32_t cbm[];  // [kColdWarps][part_rows / 32]
   const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
   const uint32_t pw = part_rows / 32;
   uint32_t* bm = cbm + (uint64_t)w * pw;
   for (uint32_t i = lane; i < pw; i += 32) bm[i] = 0;
   __syncwarp();
-  uint64_t cnt = 0, sum = 0, xr = 0;
+  uint64_t cnt = 0, sum = 0, xr = 0, csp = 0;
   const uint64_t n_items = n_x * parts;
   for (;;) {
     uint32_t item = 0;
@@ -722,6 +738,7 @@ dense_cold_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
           touched = true;
           if (old & bit) continue;
           ++cnt;
+          if (row_sp && row_sp[zbase + zl]) ++csp;
           if (kMode != kModeCount) {
             const uint32_t zc = dl_z[zbase + zl];
             if (kMode == kModeChecksum) {
@@ -744,6 +761,7 @@ dense_cold_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
       for (uint32_t i = lane; i < pw; i += 32) bm[i] = 0;
     __syncwarp();
   }
+  flush_sp(cnt_sp, csp);
   tally_flush(tally, cnt, sum, xr);
 }
 
@@ -787,13 +805,14 @@ dense_cold_hash_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
                        uint64_t y_card, uint32_t var_bits, const uint32_t* __restrict__ dl_z,
                        Decode dec, Emit em, unsigned int* __restrict__ next,
                        uint32_t* __restrict__ over_x, unsigned int* __restrict__ over_n,
-                       Tally* tally) {
+                       Tally* tally, const uint8_t* __restrict__ row_sp,
+                       unsigned long long* __restrict__ cnt_sp) {
   extern __shared__ __align__(16) uint32_t chtab[];  // [kCHWarps][kCHSlots]
   const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
   uint32_t* tab = chtab + (uint64_t)w * kCHSlots;
   for (uint32_t i = lane; i < kCHSlots; i += 32) tab[i] = kCHEmpty;
   __syncwarp();
-  uint64_t cnt = 0, sum = 0, xr = 0;
+  uint64_t cnt = 0, sum = 0, xr = 0, csp = 0;
   for (;;) {
     uint32_t item = 0;
     if (lane == 0) item = atomicAdd(next, 1u);
@@ -858,12 +877,14 @@ dense_cold_hash_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
         const uint32_t zl = tab[i];
         if (zl != kCHEmpty) {
           if (kMode != kModeCount && !over) cold_account<kMode>(x, dl_z[zl], dec, em, sum, xr);
+          if (row_sp && !over && row_sp[zl]) ++csp;
           tab[i] = kCHEmpty;
         }
       }
     }
     __syncwarp();
   }
+  flush_sp(cnt_sp, csp);
   tally_flush(tally, cnt, sum, xr);
 }
 
@@ -878,10 +899,11 @@ dense_cold_overflow_kernel(const uint32_t* __restrict__ over_x, const unsigned i
                            const uint4* __restrict__ ch, const uint4* __restrict__ hx4,
                            uint64_t y_card, uint32_t var_bits, const uint32_t* __restrict__ dl_z,
                            uint32_t* __restrict__ gbm, uint64_t words, Decode dec, Emit em,
-                           Tally* tally) {
+                           Tally* tally, const uint8_t* __restrict__ row_sp,
+                           unsigned long long* __restrict__ cnt_sp) {
   uint32_t* bm = gbm + (uint64_t)blockIdx.x * words;
   const uint32_t n = *over_n;
-  uint64_t cnt = 0, sum = 0, xr = 0;
+  uint64_t cnt = 0, sum = 0, xr = 0, csp = 0;
   for (uint32_t it = blockIdx.x; it < n; it += gridDim.x) {
     const uint32_t x = over_x[it];
     const uint4 a0 = hx4[2 * (uint64_t)x], a1 = hx4[2 * (uint64_t)x + 1];
@@ -901,6 +923,7 @@ dense_cold_overflow_kernel(const uint32_t* __restrict__ over_x, const unsigned i
             const uint32_t bit = 1u << (zl & 31);
             if (atomicOr(&bm[zl >> 5], bit) & bit) continue;
             ++cnt;
+            if (row_sp && row_sp[zl]) ++csp;
             if (kMode != kModeCount) cold_account<kMode>(x, dl_z[zl], dec, em, sum, xr);
           } else {
             bm[zl >> 5] = 0;
@@ -910,6 +933,7 @@ dense_cold_overflow_kernel(const uint32_t* __restrict__ over_x, const unsigned i
       __syncthreads();
     }
   }
+  flush_sp(cnt_sp, csp);
   tally_flush(tally, cnt, sum, xr);
 }
 

@@ -135,6 +135,7 @@ struct KernelOut {
   uint64_t count = 0, sum = 0, xr = 0;
   uint64_t inner = 0;
   uint64_t cold_overflow = 0;  // x handed to the overflow kernel (diagnostics)
+  uint64_t count_sp = 0;      // pairs of rows flagged in DenseInputs::row_sp
   double ms_hot = 0;          // CUDA-event time of the hot-pass launch
   uint64_t hot_lds_bytes = 0;  // its algorithmic shared-memory bytes
 };
@@ -292,6 +293,7 @@ struct DenseInputs {
   uint64_t x_card;
   uint64_t x_lo, x_hi;     // x code range of the cold residual pass
   uint64_t dnnz = ~0ull;   // entries of the dense lists (~0: read dl_ptr[n_dense])
+  const uint8_t* row_sp = nullptr;  // per row: a folded-in sparse z (count apart)
 };
 
 // DenseEC driver: the z-tile-resident kernel (dense_ec_tile_kernel) when the
@@ -542,6 +544,8 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   const bool cold_hash = !cold_bitmap && k_cap >= 256 &&
                          !(cold_env && std::string(cold_env) == "tiers");
   const bool cold_kernel_ok = cold_bitmap || cold_hash;
+  if (in.row_sp && !cold_kernel_ok)
+    throw d3g::Error(D3G_INTERNAL_ERROR, "folded sparse rows need the cold kernels");
   if (cold_kernel_ok) K = 256;
   if (const char* kenv = std::getenv("D3G_K")) {  // experiments: force the hot width
     const uint32_t k = (uint32_t)std::strtoul(kenv, nullptr, 10);
@@ -575,9 +579,11 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   DBuf<unsigned int> work = X.zeros<unsigned int>(1);
   hp.work = work.p;
   // [hot tally | cold tally | hot-pass LDS units]: read back once at the end
-  DBuf<Tally> tallies = X.zeros<Tally>(3);
+  // [hot | cold | LDS units | pairs of folded sparse rows]
+  DBuf<Tally> tallies = X.zeros<Tally>(4);
   Tally* t = tallies.p;
   unsigned long long* lds_units = &tallies.p[2].count;
+  unsigned long long* cnt_sp = in.row_sp ? &tallies.p[3].count : nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   size_t sm = (size_t)K * 32 * 16;
   unsigned g = (unsigned)std::min<uint64_t>((uint64_t)n_batches * hp.z_chunks, (uint64_t)X.sm_count);
@@ -617,7 +623,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     DBuf<uint4> rec = X.zeros<uint4>(2 * D);
     DBuf<uint32_t> rcnt = X.alloc<uint32_t>(D);
     D3G_LAUNCH(X, hot_rec_kernel, grid_for(D, 256), 256, 0, in.dl_ptr, in.dl_col, D, K,
-               tab ? kTabBits : 0u, reinterpret_cast<uint8_t*>(rec.p), rcnt.p);
+               tab ? kTabBits : 0u, reinterpret_cast<uint8_t*>(rec.p), rcnt.p, in.row_sp);
     // algorithmic LDS traffic: every (row, batch) reads its listed slices plus
     // (tab) one subset-table entry, 512 B each
     D3G_LAUNCH(X, rec_sum_kernel, grid_for(D, 256), 256, 0, rcnt.p, D, tab ? 1u : 0u, lds_units);
@@ -629,12 +635,12 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
         auto kfn = dense_hot_tab_kernel<decltype(M)::value>;
         D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
         D3G_LAUNCH(X, kfn, g, kHotThreads, tsm, hp, in.dl_ptr, in.dl_col, rec.p, rcnt.p, dec, em,
-                   t);
+                   t, cnt_sp);
       } else {
         auto kfn = dense_hot_rec_kernel<decltype(M)::value>;
         D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         D3G_LAUNCH(X, kfn, g, kHotThreads, sm, hp, in.dl_ptr, in.dl_col, rec.p, rcnt.p, dec, em,
-                   t);
+                   t, cnt_sp);
       }
     });
     D3G_CUDA(cudaEventRecord(ev1, X.stream));
@@ -693,7 +699,8 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
           D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
           D3G_LAUNCH(X, kfn, (unsigned)X.sm_count * 3, kCHWarps * 32, hsm, xorder, n_live,
                      in.r_ptr, in.r_col, cptr.p, ccol.p, ch.p, reinterpret_cast<const uint4*>(hx.p),
-                     Y, var_bits, in.dl_z, dec, em, next.p, over_x.p, over_n.p, tc);
+                     Y, var_bits, in.dl_z, dec, em, next.p, over_x.p, over_n.p, tc, in.row_sp,
+                     cnt_sp);
         });
         const unsigned int n_over = X.scalar(over_n.p);
         out.cold_overflow = n_over;
@@ -705,7 +712,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
             D3G_LAUNCH(X, dense_cold_overflow_kernel<decltype(M)::value>, og, 512, 0, over_x.p,
                        over_n.p, in.r_ptr, in.r_col, cptr.p, ccol.p, ch.p,
                        reinterpret_cast<const uint4*>(hx.p), Y, var_bits, in.dl_z, gbm.p, words,
-                       dec, em, tc);
+                       dec, em, tc, in.row_sp, cnt_sp);
           });
         }
       } else {
@@ -716,7 +723,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
           D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
         D3G_LAUNCH(X, kfn, (unsigned)X.sm_count * cold_ctas, kColdWarps * 32, csm, xorder, n_live, in.r_ptr,
                    in.r_col, cptr.p, ccol.p, ch.p, reinterpret_cast<const uint4*>(hx.p), Y, parts,
-                   part_rows, var_bits, in.dl_z, dec, em, next.p, tc);
+                   part_rows, var_bits, in.dl_z, dec, em, next.p, tc, in.row_sp, cnt_sp);
       });
       }
     } else {
@@ -725,8 +732,9 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
       run_sparse(X, si, dec, mode, em, cold, flt);
     }
   }
-  Tally th[3];
-  X.to_host(th, tallies.p, 3);
+  Tally th[4];
+  X.to_host(th, tallies.p, 4);
+  out.count_sp = th[3].count;
   const Tally& h = th[0];
   if (cold_kernel_ok && e[best] > 0) {
     cold.count = th[1].count;
@@ -801,6 +809,20 @@ __global__ void permute_pairs_kernel(const uint32_t* __restrict__ idx, uint64_t 
   }
 }
 
+
+__global__ void mark_ids_kernel(const uint32_t* __restrict__ ids, uint64_t n,
+                                uint8_t* __restrict__ flag) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    flag[ids[i]] = 1;
+}
+
+__global__ void gather_u8_kernel(const uint32_t* __restrict__ idx, uint64_t n,
+                                 const uint8_t* __restrict__ src, uint8_t* __restrict__ out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = src[idx[i]];
+}
 
 __global__ void max_u32_kernel(const uint32_t* __restrict__ v, uint64_t n,
                                unsigned long long* __restrict__ out) {
@@ -1610,26 +1632,53 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
       D3G_LAUNCH(X, sparse_y_scatter_kernel, grid_for(n_sparse * 8, 256), 256, 0,
                  sz_csr.row_ptr.p, sz_csr.col.p, sparse_ids.p, n_sparse, cur.p, sp_col.p);
   }
-  // dense side
-  DenseLayout L;
   // optional x-code restriction of the kernels (opts x_code_lo/hi)
   const uint64_t xa = o->x_code_hi ? std::min<uint64_t>(o->x_code_lo, x_card) : 0;
   const uint64_t xb = o->x_code_hi ? std::min<uint64_t>(o->x_code_hi, x_card) : x_card;
-  if (n_dense > 0 && x_live > 0)
-    build_dense_layout(X, rx, max_mx, hmx, sz_csr.row_ptr.p, sz_csr.col.p, dense_ids.p, n_dense,
-                       max_mz, nullptr, y_card, dR.p, L, xa, xb, P.dense_nnz);
-  // Heavy sparse side (OUT_J,sparse > 4096 per live x over > 8192 sparse z,
-  // e.g. cfg4's 9.7e10 candidates): answer it with the same hot bit-sliced +
-  // cold residual engine, restricted to the sparse z set. The result is the
-  // sparse kernel's exact output (pairs over sparse z), only computed faster.
+  // Heavy sparse side (OUT_J,sparse > 4096 per live x): answer it with the
+  // same hot bit-sliced + cold residual engine instead of the SparseBMM
+  // tiers. Without a dense side (cfg4: 9.7e10 candidates over > 8192 sparse
+  // z) it gets its own layout; next to a dense side (cfg2: 1.25e9 candidates
+  // over 3,406 sparse z) the sparse rows are FOLDED into the dense layout and
+  // their pairs counted apart, so one pass answers both and pairs_sparse /
+  // pairs_dense stay the reference's split. Either way the result is exactly
+  // the sparse kernel's output, computed faster.
   uint64_t outj_sp = 0;
   {
     DBuf<unsigned long long> t = X.zeros<unsigned long long>(1);
     if (y_card) D3G_LAUNCH(X, outj_ptr_kernel, grid_for(y_card, 256), 256, 0, dR.p, sp_ptr.p, y_card, t.p);
     outj_sp = X.scalar(t.p);
   }
-  const bool sparse_hot = std::getenv("D3G_SPARSE_TIERS") == nullptr && n_sparse > 8192 &&
-                          x_live > 0 && outj_sp > 4096ull * x_live;
+  const bool heavy_sparse = std::getenv("D3G_SPARSE_TIERS") == nullptr && x_live > 0 &&
+                            n_sparse > 0 && outj_sp > 4096ull * x_live;
+  const bool default_engine = std::getenv("D3G_HOT") == nullptr &&
+                              std::getenv("D3G_COLD") == nullptr &&
+                              std::getenv("D3G_DENSE") == nullptr;
+  const bool fold = heavy_sparse && n_dense > 0 && default_engine &&
+                    std::getenv("D3G_NO_FOLD") == nullptr;
+  const bool sparse_hot = heavy_sparse && !fold && n_sparse > 8192;
+  // dense side (plus the folded sparse rows)
+  DenseLayout L;
+  DBuf<uint8_t> row_sp;
+  if (n_dense > 0 && x_live > 0) {
+    if (fold) {
+      DBuf<uint32_t> ids = X.alloc<uint32_t>(n_dense + n_sparse);
+      D3G_CUDA(cudaMemcpyAsync(ids.p, dense_ids.p, n_dense * 4, cudaMemcpyDeviceToDevice, X.stream));
+      D3G_CUDA(cudaMemcpyAsync(ids.p + n_dense, sparse_ids.p, n_sparse * 4,
+                               cudaMemcpyDeviceToDevice, X.stream));
+      build_dense_layout(X, rx, max_mx, hmx, sz_csr.row_ptr.p, sz_csr.col.p, ids.p,
+                         n_dense + n_sparse, max_mz, nullptr, y_card, dR.p, L, xa, xb,
+                         P.dense_nnz + P.sparse_nnz);
+      DBuf<uint8_t> zsp = X.zeros<uint8_t>(z_card);
+      D3G_LAUNCH(X, mark_ids_kernel, grid_for(n_sparse, 256), 256, 0, sparse_ids.p, n_sparse, zsp.p);
+      row_sp = X.alloc<uint8_t>(L.n_dense);
+      D3G_LAUNCH(X, gather_u8_kernel, grid_for(L.n_dense, 256), 256, 0, L.dl_z.p, L.n_dense, zsp.p,
+                 row_sp.p);
+    } else {
+      build_dense_layout(X, rx, max_mx, hmx, sz_csr.row_ptr.p, sz_csr.col.p, dense_ids.p, n_dense,
+                         max_mz, nullptr, y_card, dR.p, L, xa, xb, P.dense_nnz);
+    }
+  }
   DenseLayout Ls;
   if (sparse_hot)
     build_dense_layout(X, rx, max_mx, hmx, sz_csr.row_ptr.p, sz_csr.col.p, sparse_ids.p, n_sparse,
@@ -1653,16 +1702,20 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
                   Ls.y_of_rank.p, dR.p, x_card, x_lo, x_hi, Ls.dnnz};
   if (sparse_hot)
     run_dense_hot(X, dsi, dec, mode, no_emit, ks);
-  else
+  else if (!fold)
     run_sparse(X, si, dec, mode, no_emit, ks);
   T.mark();  // 7
   uint64_t pos_lo = L.n_live * shard_index / shard_count,
            pos_hi = L.n_live * (shard_index + 1) / shard_count;
   DenseInputs di{L.xorder.p, L.n_live, rx.row_ptr.p, rx.col.p, L.y_rank.p, y_card, L.dl_ptr.p,
                  L.dl_col.p, L.dl_z.p, L.n_dense, L.max_group_nnz, pos_lo, pos_hi,
-                 L.y_of_rank.p, dR.p, x_card, x_lo, x_hi, L.dnnz};
+                 L.y_of_rank.p, dR.p, x_card, x_lo, x_hi, L.dnnz, row_sp.p};
   run_dense(X, di, dec, mode, no_emit, kd);
   T.mark();  // 8
+  if (fold) {  // the folded sparse rows' pairs, counted apart inside the engine
+    ks.count = kd.count_sp;
+    kd.count -= kd.count_sp;
+  }
   rep->pairs_sparse = ks.count;
   rep->pairs_dense = kd.count;
   rep->ms_dense_hot = ks.ms_hot + kd.ms_hot;
@@ -1678,7 +1731,7 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
       KernelOut tmp;
       if (sparse_hot)
         run_dense_hot(X, dsi, dec, kModeEmit, em, tmp);
-      else
+      else if (!fold)
         run_sparse(X, si, dec, kModeEmit, em, tmp);
       run_dense(X, di, dec, kModeEmit, em, tmp);
     }, rev_or_null(D.x), rev_or_null(D.z), swapped, pairs, rep, x_card, z_card);

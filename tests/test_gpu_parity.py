@@ -142,6 +142,9 @@ def test_baseline_config_matches_reference(cfg):
     for k in ("x_card", "y_card", "z_card", "r_nnz", "s_nnz", "out_j", "dense_z", "sparse_z",
               "sparse_nnz", "dropped_r"):
         assert getattr(rep, k) == p[k], k
+    ref = g.get("ref_hybrid_report")
+    if ref and cfg != 3:  # the reference's own pairs split (cfg2 folds its sparse rows)
+        assert (rep.pairs_sparse, rep.pairs_dense) == (ref["pairs_sparse"], ref["pairs_dense"])
 
 
 def test_cfg5_x_slice_matches_reference():
