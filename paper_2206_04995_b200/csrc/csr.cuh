@@ -157,14 +157,14 @@ __global__ void value_hist_kernel(const uint32_t* __restrict__ vals, uint64_t n,
     if (sh[i]) atomicAdd(&counts[i], sh[i]);
 }
 
-// sum_y dR(y) * (ptr[y+1] - ptr[y]): the join size against a y-major CSR
-// (the sparse side: SpaStats::inner_count), u64 (far below 2^64 here).
-__global__ void outj_ptr_kernel(const uint32_t* __restrict__ dr, const uint64_t* __restrict__ ptr,
+// sum_y dR(y) * cnt(y): the join size against the rows counted in cnt (the
+// sparse side: SpaStats::inner_count), u64 (far below 2^64 here).
+__global__ void outj_cnt_kernel(const uint32_t* __restrict__ dr, const uint32_t* __restrict__ cnt,
                                 uint64_t y_card, unsigned long long* __restrict__ out) {
   uint64_t acc = 0;
   for (uint64_t y = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; y < y_card;
        y += (uint64_t)gridDim.x * blockDim.x)
-    acc += (uint64_t)dr[y] * (ptr[y + 1] - ptr[y]);
+    acc += (uint64_t)dr[y] * cnt[y];
   acc = warp_sum(acc);
   if (lane_id() == 0 && acc) atomicAdd(out, (unsigned long long)acc);
 }

@@ -1615,23 +1615,15 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   P.iss.reset();
   pd.reset();
   psp.reset();
-  // sparse side: y-major CSR over compact sparse indices
+  // sparse side: per-y counts of the sparse rows (OUT_J,sparse and, when the
+  // SparseBMM tiers run, the y-major CSR over compact sparse indices)
   DBuf<uint64_t> sp_ptr = X.alloc<uint64_t>(y_card + 1);
   DBuf<uint32_t> sp_col;
-  {
-    DBuf<uint32_t> cnt = X.zeros<uint32_t>(y_card);
-    if (n_sparse)
-      D3G_LAUNCH(X, sparse_y_count_kernel, grid_for(n_sparse * 8, 256), 256, 0,
-                 sz_csr.row_ptr.p, sz_csr.col.p, sparse_ids.p, n_sparse, cnt.p);
-    exclusive_scan<uint32_t>(X, cnt.p, y_card, sp_ptr.p);
-    rep->sparse_nnz = P.sparse_nnz;  // = sp_ptr[y_card], known on the host
-    sp_col = X.alloc<uint32_t>(rep->sparse_nnz);
-    DBuf<unsigned long long> cur = X.alloc<unsigned long long>(y_card + 1);
-    D3G_CUDA(cudaMemcpyAsync(cur.p, sp_ptr.p, (y_card + 1) * 8, cudaMemcpyDeviceToDevice, X.stream));
-    if (n_sparse)
-      D3G_LAUNCH(X, sparse_y_scatter_kernel, grid_for(n_sparse * 8, 256), 256, 0,
-                 sz_csr.row_ptr.p, sz_csr.col.p, sparse_ids.p, n_sparse, cur.p, sp_col.p);
-  }
+  DBuf<uint32_t> sp_cnt = X.zeros<uint32_t>(y_card);
+  if (n_sparse)
+    D3G_LAUNCH(X, sparse_y_count_kernel, grid_for(n_sparse * 8, 256), 256, 0, sz_csr.row_ptr.p,
+               sz_csr.col.p, sparse_ids.p, n_sparse, sp_cnt.p);
+  rep->sparse_nnz = P.sparse_nnz;  // = sum of sp_cnt, known on the host
   // optional x-code restriction of the kernels (opts x_code_lo/hi)
   const uint64_t xa = o->x_code_hi ? std::min<uint64_t>(o->x_code_lo, x_card) : 0;
   const uint64_t xb = o->x_code_hi ? std::min<uint64_t>(o->x_code_hi, x_card) : x_card;
@@ -1646,7 +1638,7 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   uint64_t outj_sp = 0;
   {
     DBuf<unsigned long long> t = X.zeros<unsigned long long>(1);
-    if (y_card) D3G_LAUNCH(X, outj_ptr_kernel, grid_for(y_card, 256), 256, 0, dR.p, sp_ptr.p, y_card, t.p);
+    if (y_card) D3G_LAUNCH(X, outj_cnt_kernel, grid_for(y_card, 256), 256, 0, dR.p, sp_cnt.p, y_card, t.p);
     outj_sp = X.scalar(t.p);
   }
   const bool heavy_sparse = std::getenv("D3G_SPARSE_TIERS") == nullptr && x_live > 0 &&
@@ -1657,6 +1649,16 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   const bool fold = heavy_sparse && n_dense > 0 && default_engine &&
                     std::getenv("D3G_NO_FOLD") == nullptr;
   const bool sparse_hot = heavy_sparse && !fold && n_sparse > 8192;
+  if (!fold && !sparse_hot) {  // the SparseBMM tiers read S_sparse by y
+    exclusive_scan<uint32_t>(X, sp_cnt.p, y_card, sp_ptr.p);
+    sp_col = X.alloc<uint32_t>(rep->sparse_nnz);
+    DBuf<unsigned long long> cur = X.alloc<unsigned long long>(y_card + 1);
+    D3G_CUDA(cudaMemcpyAsync(cur.p, sp_ptr.p, (y_card + 1) * 8, cudaMemcpyDeviceToDevice, X.stream));
+    if (n_sparse)
+      D3G_LAUNCH(X, sparse_y_scatter_kernel, grid_for(n_sparse * 8, 256), 256, 0,
+                 sz_csr.row_ptr.p, sz_csr.col.p, sparse_ids.p, n_sparse, cur.p, sp_col.p);
+  }
+  sp_cnt.reset();
   // dense side (plus the folded sparse rows)
   DenseLayout L;
   DBuf<uint8_t> row_sp;
