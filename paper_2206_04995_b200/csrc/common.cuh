@@ -90,6 +90,19 @@ struct Ctx {
   void* pinned = nullptr;
   size_t pinned_bytes = 0;
 
+  // Buffers up to kCacheMax bytes are rounded up to a power of two and
+  // recycled through per-size free lists on the host: a pipeline call makes
+  // ~100 short-lived allocations, and every API call the host saves while the
+  // GPU runs the small prelude kernels is GPU time saved. Reuse needs no
+  // event: everything runs on this context's one stream, so a recycled block
+  // is only touched after the work that used it before.
+  static constexpr uint64_t kCacheMax = 64ull << 20;
+  std::vector<void*> cache[40];
+  static int size_class(uint64_t bytes) {
+    int c = 8;
+    while ((1ull << c) < bytes) ++c;
+    return c;
+  }
   void* raw_alloc(uint64_t bytes) {
     if (bytes == 0) bytes = 16;
     if (budget != 0 && live_bytes + bytes > budget)
@@ -97,11 +110,18 @@ struct Ctx {
                           std::to_string(live_bytes + bytes) + " bytes, limit " +
                           std::to_string(budget) + " bytes");
     void* p = nullptr;
-    cudaError_t e = cudaMallocAsync(&p, bytes, stream);
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      throw ResourceError("device allocation of " + std::to_string(bytes) +
-                          " bytes failed: " + cudaGetErrorString(e));
+    const bool cached = bytes <= kCacheMax;
+    const int c = cached ? size_class(bytes) : 0;
+    if (cached && !cache[c].empty()) {
+      p = cache[c].back();
+      cache[c].pop_back();
+    } else {
+      cudaError_t e = cudaMallocAsync(&p, cached ? (1ull << c) : bytes, stream);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw ResourceError("device allocation of " + std::to_string(bytes) +
+                            " bytes failed: " + cudaGetErrorString(e));
+      }
     }
     live_bytes += bytes;
     if (live_bytes > peak_bytes) peak_bytes = live_bytes;
@@ -110,8 +130,17 @@ struct Ctx {
   void raw_free(void* p, uint64_t bytes) {
     if (p == nullptr) return;
     if (bytes == 0) bytes = 16;
-    cudaFreeAsync(p, stream);
+    if (bytes <= kCacheMax)
+      cache[size_class(bytes)].push_back(p);
+    else
+      cudaFreeAsync(p, stream);
     live_bytes -= bytes;
+  }
+  void release_cache() {
+    for (auto& l : cache) {
+      for (void* p : l) cudaFreeAsync(p, stream);
+      l.clear();
+    }
   }
   template <class T>
   DBuf<T> alloc(uint64_t n) {
@@ -121,11 +150,51 @@ struct Ctx {
     b.ctx = this;
     return b;
   }
+  // Zero arena: small zero-filled buffers are carved from one block that
+  // begin_call() re-zeroes with a single memset, instead of one memset each.
+  // Slices live until the end of the call (DBuf with ctx == nullptr: no free).
+  static constexpr uint64_t kZeroArena = 4ull << 20, kZeroSlice = 512ull << 10;
+  char* zarena = nullptr;
+  uint64_t zused = 0;
+  void begin_call() {
+    if (!zarena) {
+      D3G_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&zarena), kZeroArena, stream));
+      D3G_CUDA(cudaMemsetAsync(zarena, 0, kZeroArena, stream));
+    } else if (zused) {
+      D3G_CUDA(cudaMemsetAsync(zarena, 0, zused, stream));
+    }
+    zused = 0;
+  }
   template <class T>
   DBuf<T> zeros(uint64_t n) {
+    const uint64_t bytes = ((n == 0 ? 16 : n * sizeof(T)) + 255) & ~255ull;
+    if (zarena && bytes <= kZeroSlice && zused + bytes <= kZeroArena) {
+      DBuf<T> b;
+      b.p = reinterpret_cast<T*>(zarena + zused);
+      b.n = n;
+      zused += bytes;
+      return b;
+    }
     DBuf<T> b = alloc<T>(n);
     D3G_CUDA(cudaMemsetAsync(b.p, 0, n * sizeof(T) + (n == 0 ? 16 : 0), stream));
     return b;
+  }
+  // Persistent look-back state of scan_onepass_kernel (prims.cuh): tile
+  // flags carry the parity of the scan that wrote them and every scan clears
+  // the entries past its own tiles, so no scan needs a memset; the ticket
+  // counter (entry scan_cap) only grows.
+  unsigned long long* scan_state = nullptr;
+  uint64_t scan_cap = 0, scan_tickets = 0, scan_hw = 0;
+  uint32_t scan_parity = 0;
+  void scan_reserve(uint64_t tiles) {
+    if (tiles <= scan_cap) return;
+    uint64_t cap = 4096;
+    while (cap < tiles) cap <<= 1;
+    if (scan_state) cudaFreeAsync(scan_state, stream);
+    D3G_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scan_state), (cap + 1) * 8, stream));
+    D3G_CUDA(cudaMemsetAsync(scan_state, 0, (cap + 1) * 8, stream));
+    scan_cap = cap;
+    scan_tickets = scan_hw = 0;
   }
   uint64_t syncs = 0;  // host round trips of the current call (diagnostics)
   // Deferred reads: small device values copied into pinned memory now and
@@ -146,15 +215,37 @@ struct Ctx {
                              cudaMemcpyDeviceToHost, stream));
     deferred.push_back({dst, defer_used, bytes});
     defer_used += (bytes + 7) & ~size_t(7);
+    d2h_bytes += bytes;
   }
   bool has_deferred() const { return !deferred.empty(); }
+  void deliver(size_t n = ~size_t(0)) {  // the first n deferred reads
+    if (n > deferred.size()) n = deferred.size();
+    for (size_t i = 0; i < n; ++i)
+      std::memcpy(deferred[i].dst, static_cast<const char*>(defer_host) + deferred[i].off,
+                  deferred[i].bytes);
+    deferred.erase(deferred.begin(), deferred.begin() + n);
+    if (deferred.empty()) defer_used = 0;
+  }
   void sync() {
     ++syncs;
     D3G_CUDA(cudaStreamSynchronize(stream));
-    for (const Deferred& d : deferred)
-      std::memcpy(d.dst, static_cast<const char*>(defer_host) + d.off, d.bytes);
-    deferred.clear();
-    defer_used = 0;
+    deliver();
+  }
+  // Marks the point after the deferred reads issued so far; wait_mark()
+  // delivers them once the stream reaches it, while the work enqueued after
+  // the mark keeps the GPU busy (the host reads a size during a long kernel).
+  cudaEvent_t mark_ev = nullptr;
+  size_t mark_n = 0;
+  void mark() {
+    if (!mark_ev) D3G_CUDA(cudaEventCreateWithFlags(&mark_ev, cudaEventDisableTiming));
+    D3G_CUDA(cudaEventRecord(mark_ev, stream));
+    mark_n = deferred.size();
+  }
+  void wait_mark() {
+    ++syncs;
+    D3G_CUDA(cudaEventSynchronize(mark_ev));
+    deliver(mark_n);
+    mark_n = 0;
   }
   // After a call whose working set outgrew the pool's largest block, fault in
   // one block of (peak + 25%) and return it to the pool: the stream-ordered

@@ -18,7 +18,27 @@ struct DeviceCsr {
   DBuf<uint64_t> row_ptr;  // n_rows + 1
   DBuf<uint32_t> col;      // nnz
   uint64_t n_rows = 0, n_cols = 0, nnz = 0;
+  // largest row and number of non-empty rows (~0ull: not known on the host)
+  uint64_t max_deg = ~0ull, live_rows = 0;
 };
+
+// max and number of non-zero entries of a u32 array (the kept row lengths)
+__global__ void len_stats_kernel(const uint32_t* __restrict__ len, uint64_t n,
+                                 unsigned long long* __restrict__ out /* max, nonzero */) {
+  uint64_t m = 0, live = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t d = len[i];
+    m = d > m ? d : m;
+    live += d > 0;
+  }
+  m = warp_max(m);
+  live = warp_sum(live);
+  if (lane_id() == 0) {
+    if (m) atomicMax(out, (unsigned long long)m);
+    if (live) atomicAdd(out + 1, (unsigned long long)live);
+  }
+}
 
 __global__ void composite_key_kernel(const uint32_t* __restrict__ maj,
                                      const uint32_t* __restrict__ mnr, uint64_t n, int minor_bits,
@@ -70,6 +90,7 @@ inline void build_csr_device(Ctx& ctx, const uint32_t* maj, const uint32_t* mnr,
     D3G_CUDA(cudaMemsetAsync(out.row_ptr.p, 0, (n_rows + 1) * 8, ctx.stream));
     out.col = ctx.alloc<uint32_t>(0);
     out.nnz = 0;
+    out.max_deg = out.live_rows = 0;
     return;
   }
   unsigned g = grid_for(n, 256);
@@ -77,12 +98,19 @@ inline void build_csr_device(Ctx& ctx, const uint32_t* maj, const uint32_t* mnr,
   D3G_LAUNCH(ctx, major_hist_kernel, g, 256, 0, maj, n, cnt.p);
   DBuf<uint64_t> off = ctx.alloc<uint64_t>(n_rows + 1);
   exclusive_scan<uint32_t>(ctx, cnt.p, n_rows, off.p);
-  D3G_CUDA(cudaMemsetAsync(cnt.p, 0, n_rows * 4, ctx.stream));  // reused as the fill cursor
   DBuf<uint32_t> tmp = ctx.alloc<uint32_t>(n);
   D3G_LAUNCH(ctx, major_scatter_kernel, g, 256, 0, maj, mnr, n, off.p, cnt.p, tmp.p);
   segmented_sort(ctx, tmp.p, off.p, n_rows, /*unique=*/true, cnt.p);  // cnt <- kept per row
   exclusive_scan<uint32_t>(ctx, cnt.p, n_rows, out.row_ptr.p);
-  out.nnz = ctx.scalar(out.row_ptr.p + n_rows);
+  // one round trip: nnz, the largest row and the non-empty rows (degree stats)
+  DBuf<unsigned long long> st = ctx.zeros<unsigned long long>(2);
+  D3G_LAUNCH(ctx, len_stats_kernel, grid_for(n_rows, 256), 256, 0, cnt.p, n_rows, st.p);
+  unsigned long long hs[2];
+  ctx.defer(&out.nnz, out.row_ptr.p + n_rows, 8);
+  ctx.defer(hs, st.p, 16);
+  ctx.sync();
+  out.max_deg = hs[0];
+  out.live_rows = hs[1];
   out.col = ctx.alloc<uint32_t>(out.nnz);
   D3G_LAUNCH(ctx, row_compact_kernel, grid_for(n_rows * 8, 256), 256, 0, tmp.p, off.p,
              out.row_ptr.p, n_rows, out.col.p);
@@ -155,6 +183,44 @@ __global__ void value_hist_kernel(const uint32_t* __restrict__ vals, uint64_t n,
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < hot; i += blockDim.x)
     if (sh[i]) atomicAdd(&counts[i], sh[i]);
+}
+
+// wz[deg(z)] += sum_{y in row z} dR(y): per-degree join sizes of the rows
+// (8 lanes per row; degrees below kDegSmem privatised in shared memory).
+__global__ void row_join_hist_kernel(const uint64_t* __restrict__ row_ptr,
+                                     const uint32_t* __restrict__ col, uint64_t n_rows,
+                                     const uint32_t* __restrict__ dr, uint64_t hist_len,
+                                     unsigned long long* __restrict__ wz) {
+  constexpr int kW = 2048;
+  __shared__ unsigned long long sh[kW];
+  for (int i = threadIdx.x; i < kW; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const uint32_t sl = threadIdx.x & 7;
+  const uint64_t stride = (uint64_t)gridDim.x * (blockDim.x / 8);
+  const uint64_t first = (uint64_t)blockIdx.x * (blockDim.x / 8) + (threadIdx.x >> 3);
+  // uniform trip count per warp so the 8-lane reductions stay converged
+  const uint64_t trips = n_rows > first ? (n_rows - first + stride - 1) / stride : 0;
+  const uint64_t wtrips = __reduce_max_sync(0xffffffffu, (unsigned)trips);
+  for (uint64_t t = 0; t < wtrips; ++t) {
+    const uint64_t r = first + t * stride;
+    uint64_t sum = 0, d = 0;
+    if (r < n_rows) {
+      const uint64_t b = row_ptr[r], e = row_ptr[r + 1];
+      d = e - b;
+      for (uint64_t k = b + sl; k < e; k += 8) sum += dr[col[k]];
+    }
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (sl == 0 && sum) {
+      if (d < (uint64_t)kW)
+        atomicAdd(&sh[d], (unsigned long long)sum);
+      else
+        atomicAdd(&wz[d], (unsigned long long)sum);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kW && (uint64_t)i < hist_len; i += blockDim.x)
+    if (sh[i]) atomicAdd(&wz[i], sh[i]);
 }
 
 // sum_y dR(y) * cnt(y): the join size against the rows counted in cnt (the

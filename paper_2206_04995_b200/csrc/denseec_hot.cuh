@@ -108,7 +108,8 @@ __global__ void cold_count_kernel(const uint64_t* __restrict__ dl_ptr,
 __global__ void cold_scatter_kernel(const uint64_t* __restrict__ dl_ptr,
                                     const uint32_t* __restrict__ dl_col, uint64_t n_dense,
                                     uint32_t K, const uint32_t* __restrict__ y_of_rank,
-                                    unsigned long long* __restrict__ cursor,
+                                    const uint64_t* __restrict__ base,
+                                    uint32_t* __restrict__ left /* counts, consumed */,
                                     uint32_t* __restrict__ out, uint4* __restrict__ sig,
                                     uint64_t y_card, uint32_t part_rows, uint32_t parts,
                                     const uint64_t* __restrict__ hz, uint32_t kw,
@@ -132,8 +133,8 @@ __global__ void cold_scatter_kernel(const uint64_t* __restrict__ dl_ptr,
       const uint32_t y = y_of_rank[r];
       for (uint32_t v = 0; v < nvar; ++v)
         if ((zm & v) == 0) {
-          const unsigned long long pos =
-              atomicAdd(&cursor[((uint64_t)v * parts + part) * y_card + y], 1ull);
+          const uint64_t key = ((uint64_t)v * parts + part) * y_card + y;
+          const uint64_t pos = base[key] + atomicSub(&left[key], 1u) - 1u;
           out[pos] = (uint32_t)i;
           if (sig) {
             sig[2 * pos] = s0;

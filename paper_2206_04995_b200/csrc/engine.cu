@@ -562,6 +562,41 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
              in.r_col, in.y_rank, K, kw, reinterpret_cast<uint32_t*>(T.p), hx.p);
   D3G_LAUNCH(X, hot_build_z_kernel, grid_for(D * 8, 256), 256, 0, in.dl_ptr, in.dl_col, D, K, kw,
              hz.p);
+  // P2 setup, enqueued BEFORE the hot pass: the cold CSR's size is read back
+  // while P1 runs (the host waits on a mark, not on the stream), so P2's
+  // scatter and kernel queue behind P1 without an idle gap. With the
+  // warp-bitmap kernel the dense rows are cut into `parts` ranges so that 24
+  // warps per SM each hold a part_rows-bit bitmap; the cold CSR is keyed by
+  // (variant, part, y).
+  const bool run_cold = e[best] > 0;
+  uint32_t parts = 1, part_rows = (uint32_t)(((D + 31) / 32) * 32);
+  uint32_t var_bits = 0;
+  uint64_t rows_key = 0, cnnz = 0;
+  DBuf<uint32_t> cc;
+  DBuf<uint64_t> cptr;
+  if (run_cold) {
+    if (cold_bitmap) {
+      const uint64_t per_warp = budget / cold_ctas / kColdWarps;
+      const uint64_t rows_cap = std::max<uint64_t>(32, per_warp * 8 / 32 * 32);
+      parts = (uint32_t)((D + rows_cap - 1) / rows_cap);
+      part_rows = (uint32_t)((((D + parts - 1) / parts) + 31) / 32 * 32);
+    }
+    // top-rank variants of the cold CSR (only for the warp-bitmap kernel): one
+    // bit per top rank that at least half of the live x contain (cfg2: ranks
+    // 0-2; cfg4's flatter Zipf(0.8): none)
+    if (cold_kernel_ok)
+      while (var_bits < 3 && var_bits < Y && 2ull * top_rank_dr[var_bits] >= in.x_card)
+        ++var_bits;
+    rows_key = ((uint64_t)1 << var_bits) * parts * Y;
+    cc = X.zeros<uint32_t>(rows_key);
+    D3G_LAUNCH(X, cold_count_kernel, grid_for(D * 8, 256), 256, 0, in.dl_ptr, in.dl_col, D, K,
+               in.y_of_rank, cc.p, Y, part_rows, parts,
+               reinterpret_cast<const uint64_t*>(hz.p), kw, var_bits);
+    cptr = X.alloc<uint64_t>(rows_key + 1);
+    exclusive_scan<uint32_t>(X, cc.p, rows_key, cptr.p);
+    X.defer(&cnnz, cptr.p + rows_key, 8);
+    X.mark();
+  }
   // P1: hot bit-sliced pass
   HotParams hp{};
   hp.T = T.p;
@@ -651,42 +686,17 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
       D3G_LAUNCH(X, kfn, g, kHotThreads, sm, hp, in.dl_ptr, in.dl_col, dec, em, t);
     });
   }
-  // P2: cold residual join, hot-hit candidates filtered. With the warp-bitmap
-  // kernel the dense rows are cut into `parts` ranges so that 24 warps per SM
-  // each hold a part_rows-bit bitmap; the cold CSR is keyed by (part, y).
+  // P2: cold residual join, hot-hit candidates filtered
   KernelOut cold;
-  if (e[best] > 0) {
-    uint32_t parts = 1, part_rows = (uint32_t)(((D + 31) / 32) * 32);
-    if (cold_bitmap) {
-      const uint64_t per_warp = budget / cold_ctas / kColdWarps;
-      const uint64_t rows_cap = std::max<uint64_t>(32, per_warp * 8 / 32 * 32);
-      parts = (uint32_t)((D + rows_cap - 1) / rows_cap);
-      part_rows = (uint32_t)((((D + parts - 1) / parts) + 31) / 32 * 32);
-    }
-    // top-rank variants of the cold CSR (only for the warp-bitmap kernel): one
-    // bit per top rank that at least half of the live x contain (cfg2: ranks
-    // 0-2; cfg4's flatter Zipf(0.8): none)
-    uint32_t var_bits = 0;
-    if (cold_kernel_ok)
-      while (var_bits < 3 && var_bits < Y && 2ull * top_rank_dr[var_bits] >= in.x_card)
-        ++var_bits;
-    const uint64_t rows_key = ((uint64_t)1 << var_bits) * parts * Y;
-    DBuf<uint32_t> cc = X.zeros<uint32_t>(rows_key);
-    D3G_LAUNCH(X, cold_count_kernel, grid_for(D * 8, 256), 256, 0, in.dl_ptr, in.dl_col, D, K,
-               in.y_of_rank, cc.p, Y, part_rows, parts,
-               reinterpret_cast<const uint64_t*>(hz.p), kw, var_bits);
-    DBuf<uint64_t> cptr = X.alloc<uint64_t>(rows_key + 1);
-    exclusive_scan<uint32_t>(X, cc.p, rows_key, cptr.p);
-    const uint64_t cnnz = X.scalar(cptr.p + rows_key);
+  if (run_cold) {
+    X.wait_mark();  // cnnz
     DBuf<uint32_t> ccol = X.alloc<uint32_t>(cnnz);
     DBuf<uint4> ch;  // inline hot signatures (cold kernels only)
     if (cold_kernel_ok) ch = X.alloc<uint4>(2 * cnnz);
-    DBuf<unsigned long long> cur = X.alloc<unsigned long long>(rows_key + 1);
-    D3G_CUDA(cudaMemcpyAsync(cur.p, cptr.p, (rows_key + 1) * 8, cudaMemcpyDeviceToDevice, X.stream));
     D3G_LAUNCH(X, cold_scatter_kernel, grid_for(D * 8, 256), 256, 0, in.dl_ptr, in.dl_col, D, K,
-               in.y_of_rank, cur.p, ccol.p, cold_kernel_ok ? ch.p : nullptr, Y, part_rows, parts,
-               reinterpret_cast<const uint64_t*>(hz.p), kw, var_bits);
-    cur.reset();
+               in.y_of_rank, cptr.p, cc.p, ccol.p, cold_kernel_ok ? ch.p : nullptr, Y, part_rows,
+               parts, reinterpret_cast<const uint64_t*>(hz.p), kw, var_bits);
+    cc.reset();
     if (cold_kernel_ok) {
       DBuf<unsigned int> next = X.zeros<unsigned int>(1);
       Tally* tc = tallies.p + 1;
@@ -867,7 +877,7 @@ void build_dense_layout(Ctx& X, const d3g::DeviceCsr& rx, uint64_t max_mx,
     DBuf<uint32_t> v = X.alloc<uint32_t>(y_card);
     D3G_LAUNCH(X, degree_order_key_kernel, grid_for(y_card, 256), 256, 0, (const uint32_t*)nullptr,
                y_card, (const uint64_t*)nullptr, dR, max_dr, k.p, v.p);
-    radix_sort(X, k.p, v.p, y_card, bits_for(max_dr));
+    radix_sort(X, k.p, v.p, y_card, bits_for(max_dr), false);
     L.y_rank = X.alloc<uint32_t>(y_card);
     D3G_LAUNCH(X, scatter_rank_kernel, grid_for(y_card, 256), 256, 0, v.p, y_card, L.y_rank.p);
     L.y_of_rank = std::move(v);
@@ -878,7 +888,7 @@ void build_dense_layout(Ctx& X, const d3g::DeviceCsr& rx, uint64_t max_mx,
     DBuf<uint64_t> k = X.alloc<uint64_t>(n_dense);
     D3G_LAUNCH(X, degree_order_key_kernel, grid_for(n_dense, 256), 256, 0, row_ids, n_dense,
                zrow_ptr, (const uint32_t*)nullptr, max_mz, k.p, rows.p);
-    radix_sort(X, k.p, rows.p, n_dense, bits_for(max_mz));
+    radix_sort(X, k.p, rows.p, n_dense, bits_for(max_mz), false);
   }
   DBuf<uint32_t> len = X.alloc<uint32_t>(n_dense);
   D3G_LAUNCH(X, gather_len_kernel, grid_for(n_dense, 256), 256, 0, rows.p, n_dense, zrow_ptr, len.p);
@@ -892,7 +902,7 @@ void build_dense_layout(Ctx& X, const d3g::DeviceCsr& rx, uint64_t max_mx,
     D3G_LAUNCH(X, dense_list_fill_kernel, grid_for(n_dense * 32, 256), 256, 0, rows.p, n_dense,
                zrow_ptr, zcol, L.dl_ptr.p, L.y_rank.p, L.dl_col.p);
     DBuf<uint32_t> kept = X.alloc<uint32_t>(n_dense);
-    segmented_sort(X, L.dl_col.p, L.dl_ptr.p, n_dense, /*unique=*/false, kept.p);
+    segmented_sort(X, L.dl_col.p, L.dl_ptr.p, n_dense, /*unique=*/false, kept.p, max_mz);
   }
   if (z_of_row) D3G_LAUNCH(X, map_through_kernel, grid_for(n_dense, 256), 256, 0, rows.p, n_dense, z_of_row);
   L.dl_z = std::move(rows);
@@ -922,7 +932,7 @@ void build_dense_layout(Ctx& X, const d3g::DeviceCsr& rx, uint64_t max_mx,
     if (L.n_live)
       D3G_LAUNCH(X, degree_order_key_kernel, grid_for(L.n_live, 256), 256, 0, live_ids.p, L.n_live,
                  rx.row_ptr.p, (const uint32_t*)nullptr, max_mx, k.p, L.xorder.p);
-    radix_sort(X, k.p, L.xorder.p, L.n_live, bits_for(max_mx));
+    radix_sort(X, k.p, L.xorder.p, L.n_live, bits_for(max_mx), false);
   }
   // group 0 holds the 128 largest m_x: bound for the per-group cold table
   uint64_t top = 0, seen = 0;
@@ -968,7 +978,7 @@ void materialize_pairs(Ctx& X, uint64_t total, const std::function<void(d3g::Emi
     const int hi = std::max(1, bits_for(a_card ? a_card - 1 : 0));
     D3G_LAUNCH(X, pair_key_kernel, grid_for(total, 256), 256, 0, ex.p, ez.p, total,
                swapped ? 1 : 0, lo, keys.p, idx.p);
-    radix_sort(X, keys.p, idx.p, total, std::min(64, lo + hi));
+    radix_sort(X, keys.p, idx.p, total, std::min(64, lo + hi), false);
   }
   tr("sort");
   DBuf<uint32_t> sx2 = X.alloc<uint32_t>(total), sz2 = X.alloc<uint32_t>(total);
@@ -1171,16 +1181,18 @@ void tables_identical_start(Ctx& X, const uint64_t* Rl, const uint64_t* Rr, cons
   X.defer(&J.h, J.differ.p, 4);
 }
 
-void copy_csr(Ctx& X, const d3g::DeviceCsr& a, d3g::DeviceCsr& b) {
+// A read-only view of a (the self-join's S-by-z is R-by-x): b shares a's
+// buffers without owning them; a must outlive b.
+void view_csr(const d3g::DeviceCsr& a, d3g::DeviceCsr& b) {
   b.n_rows = a.n_rows;
   b.n_cols = a.n_cols;
   b.nnz = a.nnz;
-  b.row_ptr = X.alloc<uint64_t>(a.n_rows + 1);
-  b.col = X.alloc<uint32_t>(a.nnz);
-  D3G_CUDA(cudaMemcpyAsync(b.row_ptr.p, a.row_ptr.p, (a.n_rows + 1) * 8, cudaMemcpyDeviceToDevice,
-                           X.stream));
-  if (a.nnz)
-    D3G_CUDA(cudaMemcpyAsync(b.col.p, a.col.p, a.nnz * 4, cudaMemcpyDeviceToDevice, X.stream));
+  b.max_deg = a.max_deg;
+  b.live_rows = a.live_rows;
+  b.row_ptr.p = a.row_ptr.p;
+  b.row_ptr.n = a.row_ptr.n;
+  b.col.p = a.col.p;
+  b.col.n = a.col.n;
 }
 
 // ---------------------------------------------------------------------------
@@ -1341,6 +1353,10 @@ void map_inputs(Ctx& X, const uint64_t* Rl, const uint64_t* Rr, uint64_t NR, con
 struct DegreeStats {
   uint64_t max_mx = 0, x_live = 0, max_mz = 0;
   std::vector<uint64_t> hmx, hmz;
+  // wz[m] = sum over z rows of degree m of sum_{y in S_z} dR(y): the join size
+  // of those rows, so OUT_J of any degree-defined row set (the f2 sparse side:
+  // SpaStats::inner_count) is known on the host without another round trip
+  std::vector<uint64_t> wz;
   DBuf<uint32_t> dR, dS;
 };
 
@@ -1348,30 +1364,37 @@ void degree_stats(Ctx& X, const d3g::DeviceCsr& rx, const d3g::DeviceCsr& sz_csr
                   uint64_t y_card, d3g_report* rep, DegreeStats& G, bool same = false) {
   using namespace d3g;
   const uint64_t x_card = rx.n_rows, z_card = sz_csr.n_rows;
-  DBuf<unsigned long long> sc = X.zeros<unsigned long long>(4);  // max_mx, live_x, max_mz, live_z
-  if (x_card)
-    D3G_LAUNCH(X, max_degree_kernel, grid_for(x_card, 256), 256, 0, rx.row_ptr.p, x_card, sc.p,
-               sc.p + 1);
-  if (z_card)
-    D3G_LAUNCH(X, max_degree_kernel, grid_for(z_card, 256), 256, 0, sz_csr.row_ptr.p, z_card,
-               sc.p + 2, sc.p + 3);
-  unsigned long long scal[4];
-  X.to_host(scal, sc.p, 4);
-  G.max_mx = scal[0];
-  G.x_live = scal[1];
-  G.max_mz = scal[2];
+  if (rx.max_deg != ~0ull && sz_csr.max_deg != ~0ull) {  // read back with the CSR's nnz
+    G.max_mx = rx.max_deg;
+    G.x_live = rx.live_rows;
+    G.max_mz = sz_csr.max_deg;
+  } else {
+    DBuf<unsigned long long> sc = X.zeros<unsigned long long>(4);  // max_mx, live_x, max_mz, live_z
+    if (x_card)
+      D3G_LAUNCH(X, max_degree_kernel, grid_for(x_card, 256), 256, 0, rx.row_ptr.p, x_card, sc.p,
+                 sc.p + 1);
+    if (z_card)
+      D3G_LAUNCH(X, max_degree_kernel, grid_for(z_card, 256), 256, 0, sz_csr.row_ptr.p, z_card,
+                 sc.p + 2, sc.p + 3);
+    unsigned long long scal[4];
+    X.to_host(scal, sc.p, 4);
+    G.max_mx = scal[0];
+    G.x_live = scal[1];
+    G.max_mz = scal[2];
+  }
   rep->x_live = G.x_live;
-  // one buffer, one read-back: [m_x histogram | m_z histogram | OUT_J partials]
+  // one buffer, one read-back: [m_x histogram | m_z histogram | wz | OUT_J partials]
   const unsigned gb = grid_for(y_card, 1024, 296);
-  const uint64_t nbuf = (G.max_mx + 1) + (G.max_mz + 1) + 2ull * gb;
+  const uint64_t nbuf = (G.max_mx + 1) + 2 * (G.max_mz + 1) + 2ull * gb;
   DBuf<unsigned long long> hbuf = X.zeros<unsigned long long>(nbuf);
   unsigned long long* mxh_p = hbuf.p;
   unsigned long long* mzh_p = hbuf.p + G.max_mx + 1;
-  unsigned long long* parts_p = mzh_p + G.max_mz + 1;
+  unsigned long long* wz_p = mzh_p + G.max_mz + 1;
+  unsigned long long* parts_p = wz_p + G.max_mz + 1;
   if (x_card)
     D3G_LAUNCH(X, degree_hist_kernel, grid_for(x_card, 256), 256, 0, rx.row_ptr.p, x_card,
                G.max_mx + 1, mxh_p);
-  if (z_card)
+  if (z_card && !same)
     D3G_LAUNCH(X, degree_hist_kernel, grid_for(z_card, 256), 256, 0, sz_csr.row_ptr.p, z_card,
                G.max_mz + 1, mzh_p);
   G.dR = X.zeros<uint32_t>(y_card);
@@ -1385,11 +1408,19 @@ void degree_stats(Ctx& X, const d3g::DeviceCsr& rx, const d3g::DeviceCsr& sz_csr
     D3G_LAUNCH(X, value_hist_kernel, grid_for(sz_csr.nnz, 256), 256, 0, sz_csr.col.p, sz_csr.nnz,
                G.dS.p, (uint32_t)y_card);
   if (y_card) D3G_LAUNCH(X, outj_kernel, gb, 1024, 0, G.dR.p, G.dS.p, y_card, parts_p);
+  if (z_card)
+    D3G_LAUNCH(X, row_join_hist_kernel, grid_for(z_card * 8, 256), 256, 0, sz_csr.row_ptr.p,
+               sz_csr.col.p, z_card, G.dR.p, G.max_mz + 1, wz_p);
   std::vector<unsigned long long> hb(nbuf);
   X.to_host(hb.data(), hbuf.p, nbuf);
   G.hmx.assign(hb.begin(), hb.begin() + (G.max_mx + 1));
-  G.hmz.assign(hb.begin() + (G.max_mx + 1), hb.begin() + (G.max_mx + 1) + (G.max_mz + 1));
-  const unsigned long long* hp = hb.data() + (G.max_mx + 1) + (G.max_mz + 1);
+  if (same)
+    G.hmz = G.hmx;
+  else
+    G.hmz.assign(hb.begin() + (G.max_mx + 1), hb.begin() + (G.max_mx + 1) + (G.max_mz + 1));
+  G.wz.assign(hb.begin() + (G.max_mx + 1) + (G.max_mz + 1),
+              hb.begin() + (G.max_mx + 1) + 2 * (G.max_mz + 1));
+  const unsigned long long* hp = hb.data() + (G.max_mx + 1) + 2 * (G.max_mz + 1);
   unsigned __int128 acc = 0;
   for (unsigned i = 0; i < gb; ++i) acc += ((unsigned __int128)hp[2 * i + 1] << 64) | hp[2 * i];
   rep->out_j = acc > (unsigned __int128)std::numeric_limits<uint64_t>::max()
@@ -1405,6 +1436,7 @@ struct Split {
   // sums of m_z over the dense / sparse rows; exact on the host because the
   // decision is a function of m_z alone (read off the m_z histogram)
   uint64_t dense_nnz = 0, sparse_nnz = 0;
+  uint64_t outj_sparse = 0;  // join size of the sparse rows (from DegreeStats::wz)
 };
 
 void f2_split(Ctx& X, const d3g::DeviceCsr& sz_csr, const DegreeStats& G, uint64_t x_card,
@@ -1443,6 +1475,7 @@ void f2_split(Ctx& X, const d3g::DeviceCsr& sz_csr, const DegreeStats& G, uint64
     } else {
       P.n_sparse += G.hmz[m];
       P.sparse_nnz += m * G.hmz[m];
+      if (m < G.wz.size()) P.outj_sparse += G.wz[m];
     }
   }
   rep->dense_z = P.n_dense;
@@ -1580,7 +1613,7 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   build_csr_device(X, M.r_x, M.r_y, kept, x_card, y_card, rx);
   const bool same_csr = self_join && kept == NR && x_card == z_card;
   if (same_csr)
-    copy_csr(X, rx, sz_csr);
+    view_csr(rx, sz_csr);  // declared after rx: released first
   else
     build_csr_device(X, M.s_z, M.s_y, NS, z_card, y_card, sz_csr);
   M.release_codes();
@@ -1615,15 +1648,12 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   P.iss.reset();
   pd.reset();
   psp.reset();
-  // sparse side: per-y counts of the sparse rows (OUT_J,sparse and, when the
-  // SparseBMM tiers run, the y-major CSR over compact sparse indices)
+  // sparse side: OUT_J,sparse (SpaStats::inner_count) comes from the
+  // per-degree join sizes; the y-major CSR over compact sparse indices is
+  // built only when the SparseBMM tiers run
   DBuf<uint64_t> sp_ptr = X.alloc<uint64_t>(y_card + 1);
   DBuf<uint32_t> sp_col;
-  DBuf<uint32_t> sp_cnt = X.zeros<uint32_t>(y_card);
-  if (n_sparse)
-    D3G_LAUNCH(X, sparse_y_count_kernel, grid_for(n_sparse * 8, 256), 256, 0, sz_csr.row_ptr.p,
-               sz_csr.col.p, sparse_ids.p, n_sparse, sp_cnt.p);
-  rep->sparse_nnz = P.sparse_nnz;  // = sum of sp_cnt, known on the host
+  rep->sparse_nnz = P.sparse_nnz;  // known on the host (m_z histogram)
   // optional x-code restriction of the kernels (opts x_code_lo/hi)
   const uint64_t xa = o->x_code_hi ? std::min<uint64_t>(o->x_code_lo, x_card) : 0;
   const uint64_t xb = o->x_code_hi ? std::min<uint64_t>(o->x_code_hi, x_card) : x_card;
@@ -1635,12 +1665,7 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   // their pairs counted apart, so one pass answers both and pairs_sparse /
   // pairs_dense stay the reference's split. Either way the result is exactly
   // the sparse kernel's output, computed faster.
-  uint64_t outj_sp = 0;
-  {
-    DBuf<unsigned long long> t = X.zeros<unsigned long long>(1);
-    if (y_card) D3G_LAUNCH(X, outj_cnt_kernel, grid_for(y_card, 256), 256, 0, dR.p, sp_cnt.p, y_card, t.p);
-    outj_sp = X.scalar(t.p);
-  }
+  const uint64_t outj_sp = P.outj_sparse;
   const bool heavy_sparse = std::getenv("D3G_SPARSE_TIERS") == nullptr && x_live > 0 &&
                             n_sparse > 0 && outj_sp > 4096ull * x_live;
   const bool default_engine = std::getenv("D3G_HOT") == nullptr &&
@@ -1650,15 +1675,17 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
                     std::getenv("D3G_NO_FOLD") == nullptr;
   const bool sparse_hot = heavy_sparse && !fold && n_sparse > 8192;
   if (!fold && !sparse_hot) {  // the SparseBMM tiers read S_sparse by y
+    DBuf<uint32_t> sp_cnt = X.zeros<uint32_t>(y_card);
+    if (n_sparse)
+      D3G_LAUNCH(X, sparse_y_count_kernel, grid_for(n_sparse * 8, 256), 256, 0, sz_csr.row_ptr.p,
+                 sz_csr.col.p, sparse_ids.p, n_sparse, sp_cnt.p);
     exclusive_scan<uint32_t>(X, sp_cnt.p, y_card, sp_ptr.p);
     sp_col = X.alloc<uint32_t>(rep->sparse_nnz);
-    DBuf<unsigned long long> cur = X.alloc<unsigned long long>(y_card + 1);
-    D3G_CUDA(cudaMemcpyAsync(cur.p, sp_ptr.p, (y_card + 1) * 8, cudaMemcpyDeviceToDevice, X.stream));
     if (n_sparse)
       D3G_LAUNCH(X, sparse_y_scatter_kernel, grid_for(n_sparse * 8, 256), 256, 0,
-                 sz_csr.row_ptr.p, sz_csr.col.p, sparse_ids.p, n_sparse, cur.p, sp_col.p);
+                 sz_csr.row_ptr.p, sz_csr.col.p, sparse_ids.p, n_sparse, sp_ptr.p, sp_cnt.p,
+                 sp_col.p);
   }
-  sp_cnt.reset();
   // dense side (plus the folded sparse rows)
   DenseLayout L;
   DBuf<uint8_t> row_sp;
@@ -1780,7 +1807,7 @@ void stable_group(Ctx& X, const uint32_t* code, uint64_t n, uint64_t n_rows, DBu
   DBuf<uint64_t> key = X.alloc<uint64_t>(n);
   perm = X.alloc<uint32_t>(n);
   if (n) D3G_LAUNCH(X, code_key_kernel, grid_for(n, 256), 256, 0, code, n, key.p, perm.p);
-  radix_sort(X, key.p, perm.p, n, bits_for(n_rows ? n_rows - 1 : 0));
+  radix_sort(X, key.p, perm.p, n, bits_for(n_rows ? n_rows - 1 : 0), false);
   DBuf<uint32_t> cnt = X.zeros<uint32_t>(n_rows);
   if (n) D3G_LAUNCH(X, count_codes_kernel, grid_for(n, 256), 256, 0, code, n, cnt.p);
   row_ptr = X.alloc<uint64_t>(n_rows + 1);
@@ -2034,6 +2061,12 @@ void d3g_ctx_destroy(d3g_ctx* ctx) {
   cudaSetDevice(ctx->c.device);
   cudaStreamSynchronize(ctx->c.stream);
   if (ctx->c.pinned) cudaFreeHost(ctx->c.pinned);
+  if (ctx->c.defer_host) cudaFreeHost(ctx->c.defer_host);
+  ctx->c.release_cache();
+  if (ctx->c.zarena) cudaFreeAsync(ctx->c.zarena, ctx->c.stream);
+  if (ctx->c.scan_state) cudaFreeAsync(ctx->c.scan_state, ctx->c.stream);
+  if (ctx->c.mark_ev) cudaEventDestroy(ctx->c.mark_ev);
+  cudaStreamSynchronize(ctx->c.stream);
   for (int b = 0; b < 2; ++b) {
     if (ctx->c.stage[b]) cudaFreeHost(ctx->c.stage[b]);
     if (ctx->c.stage_ev[b]) cudaEventDestroy(ctx->c.stage_ev[b]);
@@ -2053,6 +2086,7 @@ int d3g_join_project(d3g_ctx* ctx, const d3g_table* r, const d3g_table* s, const
   }
   return guarded([&] {
     D3G_CUDA(cudaSetDevice(ctx->c.device));
+    ctx->c.begin_call();
     try {
       join_project_impl(ctx->c, r, s, c, o, rep, pairs);
     } catch (...) {
@@ -2069,6 +2103,7 @@ int d3g_build_csr(d3g_ctx* ctx, const uint32_t* a, const uint32_t* b, uint64_t n
   return guarded([&] {
     Ctx& X = ctx->c;
     D3G_CUDA(cudaSetDevice(X.device));
+    X.begin_call();
     X.budget = 0;
     const uint32_t* maj = major_is_a ? a : b;
     const uint32_t* mnr = major_is_a ? b : a;
@@ -2137,7 +2172,7 @@ void sort_and_copy_pairs(Ctx& X, uint32_t* ex, uint32_t* ez, uint64_t total, uin
   DBuf<uint64_t> keys = X.alloc<uint64_t>(total);
   DBuf<uint32_t> idx = X.alloc<uint32_t>(total);
   D3G_LAUNCH(X, pair_key_kernel, grid_for(total, 256), 256, 0, ex, ez, total, 0, 32, keys.p, idx.p);
-  radix_sort(X, keys.p, idx.p, total, 64);
+  radix_sort(X, keys.p, idx.p, total, 64, false);
   DBuf<uint32_t> sx = X.alloc<uint32_t>(total), sz = X.alloc<uint32_t>(total);
   D3G_LAUNCH(X, permute_pairs_kernel, grid_for(total, 256), 256, 0, idx.p, total, ex, ez, sx.p, sz.p);
   X.to_host(hx, sx.p, total);
@@ -2165,6 +2200,7 @@ int d3g_sparse_bmm_csr(d3g_ctx* ctx, const d3g_csr* r_by_x, const d3g_csr* s_spa
     using namespace d3g;
     Ctx& X = ctx->c;
     D3G_CUDA(cudaSetDevice(X.device));
+    X.begin_call();
     X.budget = 0;
     DeviceCsr r, sp;
     upload_csr(X, r_by_x, r);
@@ -2214,6 +2250,7 @@ int d3g_dense_ec_rows(d3g_ctx* ctx, const d3g_csr* r_by_x, const d3g_panel* pane
     using namespace d3g;
     Ctx& X = ctx->c;
     D3G_CUDA(cudaSetDevice(X.device));
+    X.begin_call();
     X.budget = 0;
     DeviceCsr r;
     upload_csr(X, r_by_x, r);
@@ -2291,6 +2328,7 @@ int d3g_generate(d3g_ctx* ctx, int cfg, int side, uint64_t lo, uint64_t hi, uint
     using namespace d3g;
     Ctx& X = ctx->c;
     D3G_CUDA(cudaSetDevice(X.device));
+    X.begin_call();
     uint64_t n = cfg_rows(cfg);
     if (n == 0 || hi > n || lo > hi) throw ConfigError("bad generator request");
     GenSpec g = gen_spec(cfg, side);
@@ -2321,6 +2359,7 @@ int d3g_map_tables(d3g_ctx* ctx, const d3g_table* r, const d3g_table* s, const d
   int rc = guarded([&] {
     using namespace d3g;
     D3G_CUDA(cudaSetDevice(X.device));
+    X.begin_call();
     X.budget = o->memory_budget_bytes ? o->memory_budget_bytes : (3ull << 30);
     const uint64_t NR = r->n, NS = s->n;
     DBuf<uint64_t> hb[4];
@@ -2371,6 +2410,7 @@ int d3g_join_aggregate(d3g_ctx* ctx, const d3g_valued_table* r, const d3g_valued
   d3g::Ctx& X = ctx->c;
   int rc = guarded([&] {
     D3G_CUDA(cudaSetDevice(X.device));
+    X.begin_call();
     join_aggregate_impl(X, r, s, combine, agg, c, o, rep, out);
   });
   X.budget = 0;  // the memory budget is scoped to one call
@@ -2440,6 +2480,7 @@ int d3g_read_binary(d3g_ctx* ctx, const char* path, uint64_t* left, uint64_t* ri
     using namespace d3g;
     Ctx& X = ctx->c;
     D3G_CUDA(cudaSetDevice(X.device));
+    X.begin_call();
     const uint64_t rows = binary_rows_or_throw(path);
     if (rows != n)
       throw ConfigError("d3g_read_binary: n = " + std::to_string(n) + " but the file holds " +
@@ -2473,6 +2514,7 @@ int d3g_save_pairs(d3g_ctx* ctx, const uint64_t* left, const uint64_t* right, ui
     using namespace d3g;
     Ctx& X = ctx->c;
     D3G_CUDA(cudaSetDevice(X.device));
+    X.begin_call();
     const int fmt = d3g_detect_format(path, format);
     if (fmt < D3G_FMT_TSV || fmt > D3G_FMT_BINARY) throw ConfigError("unknown table format");
     FILE* f = std::fopen(path, "wb");
@@ -2595,6 +2637,7 @@ extern "C" int d3g_smem_peak(d3g_ctx* ctx, double* bytes_per_sec) {
     using namespace d3g;
     Ctx& X = ctx->c;
     D3G_CUDA(cudaSetDevice(X.device));
+    X.begin_call();
     DBuf<uint32_t> out = X.zeros<uint32_t>(1);
     const size_t sm = 256 * 32 * 16;  // 128 KB: one CTA of 1024 threads per SM
     D3G_CUDA(cudaFuncSetAttribute(smem_peak_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2624,6 +2667,7 @@ extern "C" int d3g_alu_peak(d3g_ctx* ctx, double* ops_per_sec) {
     using namespace d3g;
     Ctx& X = ctx->c;
     D3G_CUDA(cudaSetDevice(X.device));
+    X.begin_call();
     DBuf<uint32_t> out = X.zeros<uint32_t>(1);
     const int iters = 4096;
     const unsigned grid = (unsigned)X.sm_count * 8;

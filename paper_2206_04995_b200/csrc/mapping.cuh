@@ -265,7 +265,7 @@ inline void dict_build(Ctx& ctx, const uint64_t* vals, uint64_t n, DeviceDict& d
   int k = partition_bits_for(n);
   D3G_LAUNCH(ctx, dict_collect_kernel, grid_for(slots, 256), 256, 0, d.keys.p, first.p, slots, k,
              pos.p, sk.p, ss.p);
-  radix_sort(ctx, sk.p, ss.p, distinct, 32 + k);
+  radix_sort(ctx, sk.p, ss.p, distinct, 32 + k, false);
   d.slot_code = ctx.alloc<uint32_t>(slots);
   D3G_CUDA(cudaMemsetAsync(d.slot_code.p, 0xff, slots * 4, ctx.stream));
   d.rev = ctx.alloc<uint64_t>(distinct);

@@ -56,7 +56,8 @@ __global__ void sparse_y_count_kernel(const uint64_t* __restrict__ row_ptr,
 __global__ void sparse_y_scatter_kernel(const uint64_t* __restrict__ row_ptr,
                                         const uint32_t* __restrict__ col,
                                         const uint32_t* __restrict__ sparse_ids, uint64_t n_sparse,
-                                        unsigned long long* __restrict__ cursor,
+                                        const uint64_t* __restrict__ base,
+                                        uint32_t* __restrict__ left /* counts, consumed */,
                                         uint32_t* __restrict__ out_col) {
   const uint32_t gl = threadIdx.x & 7;
   for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 8) + (threadIdx.x >> 3); i < n_sparse;
@@ -64,7 +65,8 @@ __global__ void sparse_y_scatter_kernel(const uint64_t* __restrict__ row_ptr,
     const uint32_t z = sparse_ids[i];
     const uint64_t e = row_ptr[z + 1];
     for (uint64_t k = row_ptr[z] + gl; k < e; k += 8) {
-      const uint64_t p = atomicAdd(&cursor[col[k]], 1ull);
+      const uint32_t y = col[k];
+      const uint64_t p = base[y] + atomicSub(&left[y], 1u) - 1u;
       out_col[p] = (uint32_t)i;  // compact sparse index
     }
   }

@@ -78,17 +78,27 @@ scan_tile_kernel(const Tin* __restrict__ in, uint64_t n, const uint64_t* __restr
 // Single-pass exclusive scan with decoupled look-back: tiles take tickets in
 // launch order, publish their aggregate, and warp 0 of each tile walks back
 // over its predecessors 32 at a time until it meets an inclusive prefix.
-// state[t] = flag << 62 | value (flag 1: aggregate, 2: inclusive prefix);
-// state[tiles] holds the ticket counter. One launch instead of three.
+// state[t] = flag << 61 | value, flag = 1 + 2*parity (aggregate) or
+// 2 + 2*parity (inclusive prefix); entries of the other parity (the previous
+// scan) read as "not yet published". The state persists across scans
+// (Ctx::scan_state): tickets count up from `ticket0`, and the blocks clear
+// the entries in [tiles, hw) that an earlier, longer scan left behind, so the
+// next scan (other parity) sees only its own or empty entries. One launch, no
+// memset.
 template <class Tin>
 __global__ void __launch_bounds__(kScanThreads)
 scan_onepass_kernel(const Tin* __restrict__ in, uint64_t n, uint64_t* __restrict__ out,
-                    unsigned long long* __restrict__ state, uint32_t tiles) {
-  constexpr unsigned long long kAgg = 1ull << 62, kPre = 2ull << 62, kVal = (1ull << 62) - 1;
+                    unsigned long long* __restrict__ state, uint32_t tiles,
+                    unsigned long long* __restrict__ ticket, unsigned long long ticket0,
+                    uint32_t parity, uint32_t hw) {
+  const unsigned long long kAgg = (1ull + 2 * parity) << 61, kPre = (2ull + 2 * parity) << 61;
+  constexpr unsigned long long kVal = (1ull << 61) - 1;
   __shared__ uint32_t s_tile;
   __shared__ uint64_t s_excl;
-  if (threadIdx.x == 0)
-    s_tile = atomicAdd(reinterpret_cast<unsigned int*>(&state[tiles]), 1u);
+  if (threadIdx.x == 0) s_tile = (uint32_t)(atomicAdd(ticket, 1ull) - ticket0);
+  for (uint64_t t = (uint64_t)tiles + blockIdx.x * blockDim.x + threadIdx.x; t < hw;
+       t += (uint64_t)gridDim.x * blockDim.x)
+    state[t] = 0;
   __syncthreads();
   const uint32_t tile = s_tile;
   const uint64_t base = (uint64_t)tile * kScanTile + (uint64_t)threadIdx.x * kScanItems;
@@ -120,9 +130,9 @@ scan_onepass_kernel(const Tin* __restrict__ in, uint64_t n, uint64_t* __restrict
       if (my >= 0) {
         do {
           st = atomicAdd(&state[my], 0ull);
-        } while ((st >> 62) == 0);
+        } while ((st & ~kVal) != kAgg && (st & ~kVal) != kPre);
       }
-      const unsigned pre = __ballot_sync(0xffffffffu, (st >> 62) == 2);
+      const unsigned pre = __ballot_sync(0xffffffffu, (st & ~kVal) == kPre);
       const int first = pre ? __ffs(pre) - 1 : 32;
       excl += warp_sum((uint64_t)((int)lane <= first && my >= 0 ? (st & kVal) : 0));
       if (pre) break;
@@ -158,9 +168,14 @@ void exclusive_scan(Ctx& ctx, const Tin* in, uint64_t n, uint64_t* out) {
     return;
   }
   if (tiles >= (1ull << 31)) throw ResourceError("exclusive_scan: too many tiles");
-  DBuf<unsigned long long> state = ctx.zeros<unsigned long long>(tiles + 1);
+  ctx.scan_reserve(tiles);
+  const uint64_t hw = ctx.scan_hw > tiles ? ctx.scan_hw : tiles;
   D3G_LAUNCH(ctx, scan_onepass_kernel<Tin>, (unsigned)tiles, kScanThreads, 0, in, n, out,
-             state.p, (uint32_t)tiles);
+             ctx.scan_state, (uint32_t)tiles, ctx.scan_state + ctx.scan_cap, ctx.scan_tickets,
+             ctx.scan_parity, (uint32_t)hw);
+  ctx.scan_tickets += tiles;
+  ctx.scan_parity ^= 1u;
+  ctx.scan_hw = tiles;
 }
 
 // ---------------------------------------------------------------------------
@@ -247,9 +262,10 @@ radix_scatter_kernel(const uint64_t* __restrict__ keys_in, const uint32_t* __res
 }
 
 // Sorts keys (and vals, if non-null) by the low `bits` bits of the key.
-// Ping-pongs through the caller's scratch buffers; the sorted result ends up
-// back in keys/vals. Requires n < 2^32.
-inline void radix_sort(Ctx& ctx, uint64_t* keys, uint32_t* vals, uint64_t n, int bits) {
+// Ping-pongs through scratch buffers; the sorted result ends up back in
+// keys/vals (keys left unspecified when !keys_needed). Requires n < 2^32.
+inline void radix_sort(Ctx& ctx, uint64_t* keys, uint32_t* vals, uint64_t n, int bits,
+                       bool keys_needed = true) {
   if (n <= 1 || bits <= 0) return;
   if (n >= (1ull << 32)) throw ResourceError("radix_sort: more than 2^32 keys");
   uint32_t n_tiles = (uint32_t)((n + kSortTile - 1) / kSortTile);
@@ -276,7 +292,8 @@ inline void radix_sort(Ctx& ctx, uint64_t* keys, uint32_t* vals, uint64_t n, int
     std::swap(vin, vout);
   }
   if (kin != keys) {
-    D3G_CUDA(cudaMemcpyAsync(keys, kin, n * 8, cudaMemcpyDeviceToDevice, ctx.stream));
+    if (keys_needed || !vals)
+      D3G_CUDA(cudaMemcpyAsync(keys, kin, n * 8, cudaMemcpyDeviceToDevice, ctx.stream));
     if (vals) D3G_CUDA(cudaMemcpyAsync(vals, vin, n * 4, cudaMemcpyDeviceToDevice, ctx.stream));
   }
 }

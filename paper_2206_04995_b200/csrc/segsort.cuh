@@ -9,8 +9,8 @@
 //   3. scatters the minor codes into their row (atomic per-row cursor),
 //   4. sorts and de-duplicates every row in registers: one warp per row,
 //      bitonic network over 32*E lanes-elements (E = 1, 2, 4 -> rows <= 128),
-//      rows up to 8192 in shared memory by one CTA, longer rows through the
-//      radix sort,
+//      longer rows by one CTA (shared memory up to 8192 entries, global
+//      memory beyond), with no host round trip,
 //   5. scans the unique counts and compacts the rows into the final CSR.
 // About 5 passes of 4-8 B/tuple.
 #pragma once
@@ -28,12 +28,13 @@ __global__ void major_hist_kernel(const uint32_t* __restrict__ maj, uint64_t n,
 
 __global__ void major_scatter_kernel(const uint32_t* __restrict__ maj,
                                      const uint32_t* __restrict__ mnr, uint64_t n,
-                                     const uint64_t* __restrict__ off, uint32_t* __restrict__ fill,
+                                     const uint64_t* __restrict__ off,
+                                     uint32_t* __restrict__ left /* counts, consumed */,
                                      uint32_t* __restrict__ out) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t m = maj[i];
-    out[off[m] + atomicAdd(&fill[m], 1u)] = mnr[i];
+    out[off[m] + atomicSub(&left[m], 1u) - 1u] = mnr[i];
   }
 }
 
@@ -127,10 +128,12 @@ __device__ __forceinline__ uint32_t half_sort_row(uint32_t* __restrict__ data, u
 }
 
 // One warp per row for rows of length <= 128 (two rows per warp, one per
-// half-warp, when both hold <= 16 entries); longer rows are flagged.
+// half-warp, when both hold <= 16 entries); longer rows are appended to
+// long_rows (any order) for row_sort_long_kernel.
 __global__ void row_sort_small_kernel(uint32_t* __restrict__ data, const uint64_t* __restrict__ off,
                                       uint64_t n_rows, int unique, uint32_t* __restrict__ kept,
-                                      uint32_t* __restrict__ long_flag) {
+                                      uint32_t* __restrict__ long_rows,
+                                      unsigned int* __restrict__ n_long) {
   const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x / 32);
   const uint32_t lane = lane_id();
   for (uint64_t r2 = ((uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5)) * 2;
@@ -143,10 +146,7 @@ __global__ void row_sort_small_kernel(uint32_t* __restrict__ data, const uint64_
       const uint64_t b = h ? b1 : b0;
       const uint32_t len = h ? l1 : l0;
       const uint32_t k = half_sort_row(data, b, len, unique);  // both halves converge
-      if ((lane & 15) == 0 && r2 + h < n_rows) {
-        kept[r2 + h] = k;
-        long_flag[r2 + h] = 0u;
-      }
+      if ((lane & 15) == 0 && r2 + h < n_rows) kept[r2 + h] = k;
       continue;
     }
     for (uint64_t r = r2; r < r2 + 2 && r < n_rows; ++r) {
@@ -167,113 +167,123 @@ __global__ void row_sort_small_kernel(uint32_t* __restrict__ data, const uint64_
     }
     if (lane_id() == 0) {
       kept[r] = k;
-      long_flag[r] = lng ? 1u : 0u;
+      if (lng && long_rows) long_rows[atomicAdd(n_long, 1u)] = (uint32_t)r;
     }
     }
   }
 }
 
-// One CTA per long row (129..8192 entries): bitonic sort in shared memory.
+// One CTA per long row: rows of 129..8192 entries are sorted by a bitonic
+// network in shared memory; longer rows (rare: one x or z holding > 8192
+// tuples) in place in global memory by the same CTA, with the direction-free
+// network (a mirror step per merge size, then half-cleaners, all ascending)
+// so that the virtual +inf padding past the row's end never moves. The row
+// count comes from the device (n_long): no host round trip.
 constexpr int kLongRowMax = 8192;
+
+__device__ __forceinline__ void cas_global(uint32_t* d, uint64_t a, uint64_t b) {
+  const uint32_t x = __ldcg(d + a), y = __ldcg(d + b);
+  if (y < x) {
+    __stcg(d + a, y);
+    __stcg(d + b, x);
+  }
+}
+
+__device__ void sort_row_global(uint32_t* __restrict__ d, uint64_t len) {
+  uint64_t p2 = 1;
+  while (p2 < len) p2 <<= 1;
+  for (uint64_t k = 2; k <= p2; k <<= 1) {
+    const uint64_t hk = k >> 1;
+    for (uint64_t i = threadIdx.x; i < p2 / 2; i += blockDim.x) {
+      const uint64_t blk = (i / hk) * k, o = i % hk;
+      const uint64_t a = blk + o, b = blk + k - 1 - o;
+      if (b < len) cas_global(d, a, b);
+    }
+    __syncthreads();
+    for (uint64_t j = k >> 2; j >= 1; j >>= 1) {
+      for (uint64_t i = threadIdx.x; i < p2 / 2; i += blockDim.x) {
+        const uint64_t a = (i / j) * 2 * j + (i % j), b = a + j;
+        if (b < len) cas_global(d, a, b);
+      }
+      __syncthreads();
+    }
+  }
+}
+
 __global__ void __launch_bounds__(1024)
 row_sort_long_kernel(uint32_t* __restrict__ data, const uint64_t* __restrict__ off,
-                     const uint32_t* __restrict__ rows, uint64_t n, int unique,
-                     uint32_t* __restrict__ kept) {
+                     const uint32_t* __restrict__ rows, const unsigned int* __restrict__ n_long,
+                     int unique, uint32_t* __restrict__ kept) {
   __shared__ uint32_t s[kLongRowMax];
   __shared__ uint32_t wsum[32];
+  const uint64_t n = *n_long;
   for (uint64_t q = blockIdx.x; q < n; q += gridDim.x) {
     const uint32_t r = rows[q];
     const uint64_t b = off[r];
-    const uint32_t len = (uint32_t)(off[r + 1] - b);
-    if (len > kLongRowMax) continue;  // handled by the radix fallback
-    uint32_t p2 = 1;
-    while (p2 < len) p2 <<= 1;
-    for (uint32_t i = threadIdx.x; i < p2; i += blockDim.x) s[i] = i < len ? data[b + i] : 0xffffffffu;
-    __syncthreads();
-    for (uint32_t k = 2; k <= p2; k <<= 1)
-      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-        for (uint32_t i = threadIdx.x; i < p2; i += blockDim.x) {
-          const uint32_t pj = i ^ j;
-          if (pj > i) {
-            const bool up = (i & k) == 0;
-            const uint32_t a = s[i], c = s[pj];
-            if ((a > c) == up) {
-              s[i] = c;
-              s[pj] = a;
+    const uint64_t len = off[r + 1] - b;
+    uint64_t written = 0;
+    if (len <= (uint64_t)kLongRowMax) {
+      uint32_t p2 = 1;
+      while (p2 < len) p2 <<= 1;
+      for (uint32_t i = threadIdx.x; i < p2; i += blockDim.x)
+        s[i] = i < len ? data[b + i] : 0xffffffffu;
+      __syncthreads();
+      for (uint32_t k = 2; k <= p2; k <<= 1)
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+          for (uint32_t i = threadIdx.x; i < p2; i += blockDim.x) {
+            const uint32_t pj = i ^ j;
+            if (pj > i) {
+              const bool up = (i & k) == 0;
+              const uint32_t a = s[i], c = s[pj];
+              if ((a > c) == up) {
+                s[i] = c;
+                s[pj] = a;
+              }
             }
           }
+          __syncthreads();
         }
+      // unique + compaction in index order (block scan over 1024-element chunks)
+      for (uint32_t base = 0; base < len; base += blockDim.x) {
+        const uint32_t i = base + threadIdx.x;
+        const bool keep = i < len && (!unique || i == 0 || s[i] != s[i - 1]);
+        const uint32_t m = __ballot_sync(0xffffffffu, keep);
+        if (lane_id() == 0) wsum[threadIdx.x >> 5] = __popc(m);
+        __syncthreads();
+        uint32_t before = 0, tot = 0;
+        for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) {
+          if (w < (threadIdx.x >> 5)) before += wsum[w];
+          tot += wsum[w];
+        }
+        if (keep) data[b + written + before + __popc(m & ((1u << lane_id()) - 1))] = s[i];
+        written += tot;
         __syncthreads();
       }
-    // unique + compaction in index order (block scan over 1024-element chunks)
-    uint32_t written = 0;
-    for (uint32_t base = 0; base < len; base += blockDim.x) {
-      const uint32_t i = base + threadIdx.x;
-      const bool keep = i < len && (!unique || i == 0 || s[i] != s[i - 1]);
-      const uint32_t m = __ballot_sync(0xffffffffu, keep);
-      if (lane_id() == 0) wsum[threadIdx.x >> 5] = __popc(m);
-      __syncthreads();
-      uint32_t before = 0;
-      for (uint32_t w = 0; w < (threadIdx.x >> 5); ++w) before += wsum[w];
-      uint32_t tot = 0;
-      for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) tot += wsum[w];
-      if (keep) data[b + written + before + __popc(m & ((1u << lane_id()) - 1))] = s[i];
-      written += tot;
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) kept[r] = written;
-    __syncthreads();
-  }
-}
-
-__global__ void row_len_kernel(const uint64_t* __restrict__ off, const uint32_t* __restrict__ rows,
-                               uint64_t n, uint32_t* __restrict__ len) {
-  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
-       q += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t r = rows[q];
-    len[q] = (uint32_t)(off[r + 1] - off[r]);
-  }
-}
-
-// Radix fallback for rows longer than kLongRowMax: gather (row, value) keys.
-__global__ void huge_gather_kernel(const uint32_t* __restrict__ data, const uint64_t* __restrict__ off,
-                                   const uint32_t* __restrict__ rows, uint64_t n,
-                                   const uint64_t* __restrict__ goff, int vbits,
-                                   uint64_t* __restrict__ keys) {
-  for (uint64_t q = blockIdx.x; q < n; q += gridDim.x) {
-    const uint32_t r = rows[q];
-    const uint64_t b = off[r], len = off[r + 1] - b;
-    for (uint64_t i = threadIdx.x; i < len; i += blockDim.x)
-      keys[goff[q] + i] = ((uint64_t)q << vbits) | data[b + i];
-  }
-}
-
-__global__ void huge_scatter_kernel(uint32_t* __restrict__ data, const uint64_t* __restrict__ off,
-                                    const uint32_t* __restrict__ rows, uint64_t n,
-                                    const uint64_t* __restrict__ goff, int vbits, int unique,
-                                    const uint64_t* __restrict__ keys, uint32_t* __restrict__ kept) {
-  // one CTA per huge row, sequential-by-chunk compaction of the sorted run
-  __shared__ uint32_t wsum[32];
-  const uint64_t vmask = (1ull << vbits) - 1;
-  for (uint64_t q = blockIdx.x; q < n; q += gridDim.x) {
-    const uint32_t r = rows[q];
-    const uint64_t b = off[r], len = off[r + 1] - b, g = goff[q];
-    uint64_t written = 0;
-    for (uint64_t base = 0; base < len; base += blockDim.x) {
-      const uint64_t i = base + threadIdx.x;
-      const bool keep = i < len && (!unique || i == 0 || keys[g + i] != keys[g + i - 1]);
-      const uint32_t m = __ballot_sync(0xffffffffu, keep);
-      if (lane_id() == 0) wsum[threadIdx.x >> 5] = __popc(m);
-      __syncthreads();
-      uint32_t before = 0, tot = 0;
-      for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) {
-        if (w < (threadIdx.x >> 5)) before += wsum[w];
-        tot += wsum[w];
+    } else {
+      uint32_t* d = data + b;
+      sort_row_global(d, len);
+      // in-place compaction: a chunk reads (value, predecessor) before any of
+      // its writes, and writes land at or below their source index
+      for (uint64_t base = 0; base < len; base += blockDim.x) {
+        const uint64_t i = base + threadIdx.x;
+        uint32_t v = 0;
+        bool keep = false;
+        if (i < len) {
+          v = __ldcg(d + i);
+          keep = !unique || i == 0 || v != __ldcg(d + i - 1);
+        }
+        const uint32_t m = __ballot_sync(0xffffffffu, keep);
+        if (lane_id() == 0) wsum[threadIdx.x >> 5] = __popc(m);
+        __syncthreads();
+        uint32_t before = 0, tot = 0;
+        for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) {
+          if (w < (threadIdx.x >> 5)) before += wsum[w];
+          tot += wsum[w];
+        }
+        if (keep) __stcg(d + written + before + __popc(m & ((1u << lane_id()) - 1)), v);
+        written += tot;
+        __syncthreads();
       }
-      if (keep) data[b + written + before + __popc(m & ((1u << lane_id()) - 1))] =
-          (uint32_t)(keys[g + i] & vmask);
-      written += tot;
-      __syncthreads();
     }
     if (threadIdx.x == 0) kept[r] = (uint32_t)written;
     __syncthreads();
@@ -296,46 +306,23 @@ __global__ void row_compact_kernel(const uint32_t* __restrict__ data, const uint
 
 // Sorts every row data[off[r] .. off[r+1]) ascending, optionally dropping
 // duplicates; kept[r] receives the resulting length (rows stay in place).
+// max_len (when known on the host) skips the long-row launch.
 inline void segmented_sort(Ctx& ctx, uint32_t* data, const uint64_t* off, uint64_t n_rows,
-                           bool unique, uint32_t* kept) {
+                           bool unique, uint32_t* kept, uint64_t max_len = ~0ull) {
   if (n_rows == 0) return;
-  DBuf<uint32_t> lf = ctx.alloc<uint32_t>(n_rows);
+  const bool may_be_long = max_len > 128;
+  DBuf<uint32_t> rows;
+  DBuf<unsigned int> n_long;
+  if (may_be_long) {
+    rows = ctx.alloc<uint32_t>(n_rows);
+    n_long = ctx.zeros<unsigned int>(1);
+  }
   D3G_LAUNCH(ctx, row_sort_small_kernel, grid_for(n_rows * 32, 256, ctx.sm_count * 64), 256, 0,
-             data, off, n_rows, unique ? 1 : 0, kept, lf.p);
-  DBuf<uint64_t> lp = ctx.alloc<uint64_t>(n_rows + 1);
-  exclusive_scan<uint32_t>(ctx, lf.p, n_rows, lp.p);
-  const uint64_t n_long = ctx.scalar(lp.p + n_rows);
-  if (n_long == 0) return;
-  DBuf<uint32_t> rows = ctx.alloc<uint32_t>(n_long);
-  D3G_LAUNCH(ctx, index_compact_kernel, grid_for(n_rows, 256), 256, 0, lf.p, lp.p, n_rows, rows.p);
-  D3G_LAUNCH(ctx, row_sort_long_kernel, (unsigned)std::min<uint64_t>(n_long, ctx.sm_count * 2), 1024,
-             0, data, off, rows.p, n_long, unique ? 1 : 0, kept);
-  // rows longer than kLongRowMax: radix fallback
-  DBuf<uint32_t> len = ctx.alloc<uint32_t>(n_long);
-  D3G_LAUNCH(ctx, row_len_kernel, grid_for(n_long, 256), 256, 0, off, rows.p, n_long, len.p);
-  std::vector<uint32_t> hl(n_long), hr(n_long);
-  ctx.to_host(hl.data(), len.p, n_long);
-  ctx.to_host(hr.data(), rows.p, n_long);
-  std::vector<uint32_t> huge;
-  std::vector<uint64_t> goff{0};
-  for (uint64_t i = 0; i < n_long; ++i)
-    if (hl[i] > (uint32_t)kLongRowMax) {
-      huge.push_back(hr[i]);
-      goff.push_back(goff.back() + hl[i]);
-    }
-  if (huge.empty()) return;
-  const uint64_t nh = huge.size(), tot = goff.back();
-  DBuf<uint32_t> dh = ctx.alloc<uint32_t>(nh);
-  DBuf<uint64_t> dg = ctx.alloc<uint64_t>(nh + 1);
-  ctx.to_device(dh.p, huge.data(), nh);
-  ctx.to_device(dg.p, goff.data(), nh + 1);
-  DBuf<uint64_t> keys = ctx.alloc<uint64_t>(tot);
-  const int vbits = 32;
-  D3G_LAUNCH(ctx, huge_gather_kernel, (unsigned)std::min<uint64_t>(nh, ctx.sm_count * 4), 256, 0,
-             data, off, dh.p, nh, dg.p, vbits, keys.p);
-  radix_sort(ctx, keys.p, nullptr, tot, vbits + bits_for(nh));
-  D3G_LAUNCH(ctx, huge_scatter_kernel, (unsigned)std::min<uint64_t>(nh, ctx.sm_count * 4), 256, 0,
-             data, off, dh.p, nh, dg.p, vbits, unique ? 1 : 0, keys.p, kept);
+             data, off, n_rows, unique ? 1 : 0, kept, rows.p, n_long.p);
+  if (may_be_long)
+    D3G_LAUNCH(ctx, row_sort_long_kernel,
+               (unsigned)std::min<uint64_t>(n_rows, (uint64_t)ctx.sm_count * 2), 1024, 0, data, off,
+               rows.p, n_long.p, unique ? 1 : 0, kept);
 }
 
 }  // namespace d3g
