@@ -158,8 +158,10 @@ __global__ void degree_hist_kernel(const uint64_t* __restrict__ row_ptr, uint64_
     if (sh[i]) atomicAdd(&hist[i], (unsigned long long)sh[i]);
 }
 
-// counts[v] += 1 for every v in vals; codes below kHotSmem privatised in smem,
-// others warp-aggregated with __match_any_sync.
+// counts[v] += 1 for every v in vals. Warps first merge equal values
+// (__match_any_sync: one atomic per distinct value per warp, which matters
+// for Zipf-skewed y columns where one code holds ~10% of the entries), then
+// codes below kHotSmem count in shared memory, others in global memory.
 constexpr int kHotSmem = 12288;
 __global__ void value_hist_kernel(const uint32_t* __restrict__ vals, uint64_t n,
                                   uint32_t* __restrict__ counts, uint32_t card) {
@@ -170,15 +172,15 @@ __global__ void value_hist_kernel(const uint32_t* __restrict__ vals, uint64_t n,
   uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   uint64_t n_pad = (n + 31) / 32 * 32;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pad; i += stride) {
-    bool valid = i < n;
-    uint32_t v = valid ? vals[i] : 0xffffffffu;
-    if (valid && v < hot) {
-      atomicAdd(&sh[v], 1u);
-      v = 0xffffffffu;
+    const uint32_t v = i < n ? vals[i] : 0xffffffffu;
+    const uint32_t peers = __match_any_sync(0xffffffffu, v);
+    if (v != 0xffffffffu && (peers & ((1u << lane_id()) - 1)) == 0) {
+      const unsigned c = (unsigned)__popc(peers);
+      if (v < hot)
+        atomicAdd(&sh[v], c);
+      else
+        atomicAdd(&counts[v], c);
     }
-    uint32_t peers = __match_any_sync(0xffffffffu, v);
-    if (v != 0xffffffffu && (peers & ((1u << lane_id()) - 1)) == 0)
-      atomicAdd(&counts[v], (unsigned)__popc(peers));
   }
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < hot; i += blockDim.x)

@@ -715,24 +715,46 @@ dense_cold_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
         if (lane >= (uint32_t)o) incl += u;
       }
       const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-      for (uint32_t tb = 0; tb < total; tb += 32) {
-        const uint32_t tf = tb + lane;
-        // smallest k with incl[k] > tf
-        uint32_t k = 0;
+      // two candidates per lane per step: their loads are independent, so
+      // twice the memory requests are in flight (the loop is latency bound)
+      for (uint32_t tb = 0; tb < total; tb += 64) {
+        uint32_t tf[2], kx[2];
+        uint64_t t[2];
 #pragma unroll
-        for (int step = 16; step >= 1; step >>= 1) {
-          const uint32_t probe = __shfl_sync(0xffffffffu, incl, k + step - 1);
-          if (probe <= tf) k += step;
+        for (int h = 0; h < 2; ++h) {
+          tf[h] = tb + 32 * h + lane;
+          // smallest k with incl[k] > tf
+          uint32_t k = 0;
+#pragma unroll
+          for (int step = 16; step >= 1; step >>= 1) {
+            const uint32_t probe = __shfl_sync(0xffffffffu, incl, k + step - 1);
+            if (probe <= tf[h]) k += step;
+          }
+          kx[h] = k;
         }
-        const uint32_t before = __shfl_sync(0xffffffffu, incl - len, k);
-        const uint64_t base_k = __shfl_sync(0xffffffffu, seg0, k);
-        if (tf >= total) continue;
-        {
-          const uint64_t t = base_k + (tf - before);
-          const uint4 b0 = ch[2 * t], b1 = ch[2 * t + 1];
-          const uint32_t zl = ccol[t] - zbase;
-          const bool hot = ((a0.x & b0.x) | (a0.y & b0.y) | (a0.z & b0.z) | (a0.w & b0.w) |
-                            (a1.x & b1.x) | (a1.y & b1.y) | (a1.z & b1.z) | (a1.w & b1.w)) != 0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t before = __shfl_sync(0xffffffffu, incl - len, kx[h]);
+          const uint64_t base_k = __shfl_sync(0xffffffffu, seg0, kx[h]);
+          t[h] = base_k + (tf[h] - before);
+        }
+        uint4 b0[2], b1[2];
+        uint32_t zc[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (tf[h] < total) {
+            b0[h] = ch[2 * t[h]];
+            b1[h] = ch[2 * t[h] + 1];
+            zc[h] = ccol[t[h]];
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (tf[h] >= total) continue;
+          const uint32_t zl = zc[h] - zbase;
+          const bool hot = ((a0.x & b0[h].x) | (a0.y & b0[h].y) | (a0.z & b0[h].z) |
+                            (a0.w & b0[h].w) | (a1.x & b1[h].x) | (a1.y & b1[h].y) |
+                            (a1.z & b1[h].z) | (a1.w & b1[h].w)) != 0;
           if (hot) continue;
           const uint32_t bit = 1u << (zl & 31);
           const uint32_t old = atomicOr(&bm[zl >> 5], bit);
@@ -741,16 +763,16 @@ dense_cold_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
           ++cnt;
           if (row_sp && row_sp[zbase + zl]) ++csp;
           if (kMode != kModeCount) {
-            const uint32_t zc = dl_z[zbase + zl];
+            const uint32_t zcode = dl_z[zbase + zl];
             if (kMode == kModeChecksum) {
-              const uint64_t h = dec.hash(x, zc);
-              sum += h;
-              xr ^= h;
+              const uint64_t hh = dec.hash(x, zcode);
+              sum += hh;
+              xr ^= hh;
             } else {
               const unsigned long long idx = atomicAdd(em.cursor, 1ull);
               if (idx < em.cap) {
                 em.x[idx] = x;
-                em.z[idx] = zc;
+                em.z[idx] = zcode;
               }
             }
           }

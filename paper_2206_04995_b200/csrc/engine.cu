@@ -294,7 +294,18 @@ struct DenseInputs {
   uint64_t x_lo, x_hi;     // x code range of the cold residual pass
   uint64_t dnnz = ~0ull;   // entries of the dense lists (~0: read dl_ptr[n_dense])
   const uint8_t* row_sp = nullptr;  // per row: a folded-in sparse z (count apart)
+  // dS over all of S when the dense rows are every live z row: the dense rows
+  // holding y are then simply dS(y) (no histogram over the dense lists)
+  const uint32_t* dS_all = nullptr;
 };
+
+__global__ void gather_by_rank_kernel(const uint32_t* __restrict__ y_of_rank,
+                                      const uint32_t* __restrict__ d, uint64_t n,
+                                      uint32_t* __restrict__ out) {
+  for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
+       r += (uint64_t)gridDim.x * blockDim.x)
+    out[r] = d[y_of_rank[r]];
+}
 
 // DenseEC driver: the z-tile-resident kernel (dense_ec_tile_kernel) when the
 // group's cold entries and the longest dense list fit in shared memory, the
@@ -498,8 +509,17 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   const uint64_t D = in.n_dense, Y = in.y_card;
   const uint64_t dnnz = in.dnnz != ~0ull ? in.dnnz : X.scalar(in.dl_ptr + D);
   // choose K
-  DBuf<uint32_t> cnt_rank = X.zeros<uint32_t>(Y);
-  if (dnnz) D3G_LAUNCH(X, value_hist_kernel, grid_for(dnnz, 256), 256, 0, in.dl_col, dnnz, cnt_rank.p, (uint32_t)Y);
+  DBuf<uint32_t> cnt_rank;
+  if (in.dS_all) {
+    cnt_rank = X.alloc<uint32_t>(Y);
+    D3G_LAUNCH(X, gather_by_rank_kernel, grid_for(Y, 256), 256, 0, in.y_of_rank, in.dS_all, Y,
+               cnt_rank.p);
+  } else {
+    cnt_rank = X.zeros<uint32_t>(Y);
+    if (dnnz)
+      D3G_LAUNCH(X, value_hist_kernel, grid_for(dnnz, 512, X.sm_count * 2), 512, 0, in.dl_col,
+                 dnnz, cnt_rank.p, (uint32_t)Y);
+  }
   // one read-back: K estimates, then the dense-row counts of ranks 0..6 (the
   // subset-table decision) and dR of ranks 0..3 (the cold variant bits)
   DBuf<unsigned long long> est = X.zeros<unsigned long long>(2 * kKCand + 11);
@@ -1398,14 +1418,17 @@ void degree_stats(Ctx& X, const d3g::DeviceCsr& rx, const d3g::DeviceCsr& sz_csr
     D3G_LAUNCH(X, degree_hist_kernel, grid_for(z_card, 256), 256, 0, sz_csr.row_ptr.p, z_card,
                G.max_mz + 1, mzh_p);
   G.dR = X.zeros<uint32_t>(y_card);
-  G.dS = X.zeros<uint32_t>(y_card);
   if (rx.nnz)
-    D3G_LAUNCH(X, value_hist_kernel, grid_for(rx.nnz, 256), 256, 0, rx.col.p, rx.nnz, G.dR.p,
+    D3G_LAUNCH(X, value_hist_kernel, grid_for(rx.nnz, 512, X.sm_count * 2), 512, 0, rx.col.p, rx.nnz, G.dR.p,
                (uint32_t)y_card);
-  if (same && y_card)  // self-join: S-by-z is R-by-x, so dS = dR
-    D3G_CUDA(cudaMemcpyAsync(G.dS.p, G.dR.p, y_card * 4, cudaMemcpyDeviceToDevice, X.stream));
-  else if (sz_csr.nnz)
-    D3G_LAUNCH(X, value_hist_kernel, grid_for(sz_csr.nnz, 256), 256, 0, sz_csr.col.p, sz_csr.nnz,
+  if (same) {  // self-join: S-by-z is R-by-x, so dS = dR (a view)
+    G.dS.p = G.dR.p;
+    G.dS.n = G.dR.n;
+  } else {
+    G.dS = X.zeros<uint32_t>(y_card);
+  }
+  if (!same && sz_csr.nnz)
+    D3G_LAUNCH(X, value_hist_kernel, grid_for(sz_csr.nnz, 512, X.sm_count * 2), 512, 0, sz_csr.col.p, sz_csr.nnz,
                G.dS.p, (uint32_t)y_card);
   if (y_card) D3G_LAUNCH(X, outj_kernel, gb, 1024, 0, G.dR.p, G.dS.p, y_card, parts_p);
   if (z_card)
@@ -1728,7 +1751,8 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
                  s_hi = Ls.n_live * (shard_index + 1) / shard_count;
   DenseInputs dsi{Ls.xorder.p, Ls.n_live, rx.row_ptr.p, rx.col.p, Ls.y_rank.p, y_card,
                   Ls.dl_ptr.p, Ls.dl_col.p, Ls.dl_z.p, Ls.n_dense, Ls.max_group_nnz, s_lo, s_hi,
-                  Ls.y_of_rank.p, dR.p, x_card, x_lo, x_hi, Ls.dnnz};
+                  Ls.y_of_rank.p, dR.p, x_card, x_lo, x_hi, Ls.dnnz, nullptr,
+                  Ls.n_dense == sz_csr.live_rows ? G.dS.p : nullptr};
   if (sparse_hot)
     run_dense_hot(X, dsi, dec, mode, no_emit, ks);
   else if (!fold)
@@ -1738,7 +1762,8 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
            pos_hi = L.n_live * (shard_index + 1) / shard_count;
   DenseInputs di{L.xorder.p, L.n_live, rx.row_ptr.p, rx.col.p, L.y_rank.p, y_card, L.dl_ptr.p,
                  L.dl_col.p, L.dl_z.p, L.n_dense, L.max_group_nnz, pos_lo, pos_hi,
-                 L.y_of_rank.p, dR.p, x_card, x_lo, x_hi, L.dnnz, row_sp.p};
+                 L.y_of_rank.p, dR.p, x_card, x_lo, x_hi, L.dnnz, row_sp.p,
+                 L.n_dense == sz_csr.live_rows ? G.dS.p : nullptr};
   run_dense(X, di, dec, mode, no_emit, kd);
   T.mark();  // 8
   if (fold) {  // the folded sparse rows' pairs, counted apart inside the engine
@@ -2280,7 +2305,7 @@ int d3g_dense_ec_rows(d3g_ctx* ctx, const d3g_csr* r_by_x, const d3g_panel* pane
     // R-side degrees
     uint64_t yc = std::max<uint64_t>(y_card, r.n_cols);
     DBuf<uint32_t> dR = X.zeros<uint32_t>(yc);
-    D3G_LAUNCH(X, value_hist_kernel, grid_for(r.nnz, 256), 256, 0, r.col.p, r.nnz, dR.p, (uint32_t)yc);
+    D3G_LAUNCH(X, value_hist_kernel, grid_for(r.nnz, 512, X.sm_count * 2), 512, 0, r.col.p, r.nnz, dR.p, (uint32_t)yc);
     uint64_t max_mx = 0;
     for (uint32_t i = 0; i < r_by_x->n_rows; ++i)
       max_mx = std::max<uint64_t>(max_mx, r_by_x->row_ptr[i + 1] - r_by_x->row_ptr[i]);
