@@ -662,8 +662,13 @@ dense_hot_tab_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
 // gathering hz[z] at random. Survivors are deduplicated in the warp's bitmap.
 constexpr int kColdWarps = 8;  // warps per CTA (several CTAs per SM)
 
+#ifndef D3G_COLD_UNROLL
+#define D3G_COLD_UNROLL 2
+#endif
+constexpr int kColdUnroll = D3G_COLD_UNROLL;
+
 template <int kMode>
-__global__ void __launch_bounds__(kColdWarps * 32)
+__global__ void __launch_bounds__(kColdWarps * 32, 4)
 dense_cold_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
                   const uint64_t* __restrict__ r_ptr, const uint32_t* __restrict__ r_col,
                   const uint64_t* __restrict__ cptr /* [parts][y_card] + 1 */,
@@ -715,13 +720,13 @@ dense_cold_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
         if (lane >= (uint32_t)o) incl += u;
       }
       const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-      // two candidates per lane per step: their loads are independent, so
-      // twice the memory requests are in flight (the loop is latency bound)
-      for (uint32_t tb = 0; tb < total; tb += 64) {
-        uint32_t tf[2], kx[2];
-        uint64_t t[2];
+      // kColdUnroll candidates per lane per step: their loads are independent,
+      // so that many memory requests are in flight (the loop is latency bound)
+      for (uint32_t tb = 0; tb < total; tb += 32 * kColdUnroll) {
+        uint32_t tf[kColdUnroll], kx[kColdUnroll];
+        uint64_t t[kColdUnroll];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < kColdUnroll; ++h) {
           tf[h] = tb + 32 * h + lane;
           // smallest k with incl[k] > tf
           uint32_t k = 0;
@@ -733,15 +738,15 @@ dense_cold_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
           kx[h] = k;
         }
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < kColdUnroll; ++h) {
           const uint32_t before = __shfl_sync(0xffffffffu, incl - len, kx[h]);
           const uint64_t base_k = __shfl_sync(0xffffffffu, seg0, kx[h]);
           t[h] = base_k + (tf[h] - before);
         }
-        uint4 b0[2], b1[2];
-        uint32_t zc[2];
+        uint4 b0[kColdUnroll], b1[kColdUnroll];
+        uint32_t zc[kColdUnroll];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < kColdUnroll; ++h) {
           if (tf[h] < total) {
             b0[h] = ch[2 * t[h]];
             b1[h] = ch[2 * t[h] + 1];
@@ -749,7 +754,7 @@ dense_cold_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
           }
         }
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < kColdUnroll; ++h) {
           if (tf[h] >= total) continue;
           const uint32_t zl = zc[h] - zbase;
           const bool hot = ((a0.x & b0[h].x) | (a0.y & b0[h].y) | (a0.z & b0[h].z) |
