@@ -225,18 +225,6 @@ __global__ void row_join_hist_kernel(const uint64_t* __restrict__ row_ptr,
     if (sh[i]) atomicAdd(&wz[i], sh[i]);
 }
 
-// sum_y dR(y) * cnt(y): the join size against the rows counted in cnt (the
-// sparse side: SpaStats::inner_count), u64 (far below 2^64 here).
-__global__ void outj_cnt_kernel(const uint32_t* __restrict__ dr, const uint32_t* __restrict__ cnt,
-                                uint64_t y_card, unsigned long long* __restrict__ out) {
-  uint64_t acc = 0;
-  for (uint64_t y = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; y < y_card;
-       y += (uint64_t)gridDim.x * blockDim.x)
-    acc += (uint64_t)dr[y] * cnt[y];
-  acc = warp_sum(acc);
-  if (lane_id() == 0 && acc) atomicAdd(out, (unsigned long long)acc);
-}
-
 // OUT_J = sum dR*dS with a (hi, lo) 128-bit accumulator per block.
 __global__ void outj_kernel(const uint32_t* __restrict__ dr, const uint32_t* __restrict__ ds,
                             uint64_t y_card, unsigned long long* __restrict__ parts) {

@@ -840,20 +840,6 @@ __global__ void permute_pairs_kernel(const uint32_t* __restrict__ idx, uint64_t 
 }
 
 
-__global__ void mark_ids_kernel(const uint32_t* __restrict__ ids, uint64_t n,
-                                uint8_t* __restrict__ flag) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x)
-    flag[ids[i]] = 1;
-}
-
-__global__ void gather_u8_kernel(const uint32_t* __restrict__ idx, uint64_t n,
-                                 const uint8_t* __restrict__ src, uint8_t* __restrict__ out) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x)
-    out[i] = src[idx[i]];
-}
-
 __global__ void max_u32_kernel(const uint32_t* __restrict__ v, uint64_t n,
                                unsigned long long* __restrict__ out) {
   uint64_t m = 0;
@@ -878,48 +864,133 @@ struct DenseLayout {
   uint64_t n_live = 0, n_dense = 0, max_group_nnz = 0, dnnz = 0;
 };
 
+// Rows of a CSR ordered by degree, descending, in one counting scatter whose
+// offsets come from the host degree histogram (hist[d] = rows of degree d,
+// all rows). mode / table: see degree_scatter_kernel. With want_ptr the rows'
+// list offsets are written too (rows of equal degree have equal lengths).
+struct DegreeOrder {
+  DBuf<uint32_t> rows;
+  DBuf<uint64_t> ptr;
+  DBuf<uint8_t> sp;
+  uint64_t n = 0, nnz = 0;
+};
+
+void order_by_degree(Ctx& X, const uint64_t* row_ptr, uint64_t r0, uint64_t r1,
+                     const std::vector<uint64_t>& hist, const uint8_t* d_table,
+                     const std::vector<uint8_t>* h_table, int mode, bool want_ptr, bool want_sp,
+                     DegreeOrder& o) {
+  using namespace d3g;
+  const uint64_t maxd = hist.empty() ? 0 : hist.size() - 1;
+  std::vector<uint64_t> oe(2 * (maxd + 1), 0);
+  uint64_t pos = 0, e = 0;
+  for (uint64_t d = maxd; d >= 1; --d) {
+    const bool sparse = !(h_table && d < h_table->size() && (*h_table)[d]);
+    if (!(mode == 0 || (mode == 1 ? !sparse : sparse))) continue;
+    oe[d] = pos;
+    oe[maxd + 1 + d] = e;
+    pos += hist[d];
+    e += hist[d] * d;
+  }
+  o.n = pos;
+  o.nnz = e;
+  DBuf<uint64_t> doe = X.alloc<uint64_t>(oe.size());
+  X.to_device(doe.p, oe.data(), oe.size());
+  DBuf<unsigned int> cur = X.zeros<unsigned int>(maxd + 1);
+  o.rows = X.alloc<uint32_t>(o.n);
+  if (want_ptr) o.ptr = X.alloc<uint64_t>(o.n + 1);
+  if (want_sp) o.sp = X.alloc<uint8_t>(o.n);
+  if (r1 > r0 || want_ptr)
+    D3G_LAUNCH(X, degree_scatter_kernel, grid_for(std::max<uint64_t>(r1 - r0, 1), 256), 256, 0,
+               row_ptr, r0, r1, d_table, h_table ? (uint64_t)h_table->size() : 0ull, mode, doe.p,
+               doe.p + maxd + 1, cur.p, o.rows.p, want_ptr ? o.ptr.p : nullptr, o.n, o.nnz,
+               want_sp ? o.sp.p : nullptr);
+}
+
+// Selection of the layout's rows by degree (the f2 table), instead of a
+// row-id list: rows come out ordered and with their list offsets in one pass.
+struct RowSel {
+  const std::vector<uint64_t>* hmz;   // m_z histogram (all rows)
+  const uint8_t* d_table;             // f2 table on the device
+  const std::vector<uint8_t>* table;  // and on the host
+  int mode;                           // degree_scatter_kernel mode
+  DBuf<uint8_t>* sp_out;              // mode 0: per layout row, "is a sparse z"
+};
+
+// y codes ordered by dR descending (ties in any order): a counting sort when
+// the value range is small, else the LSD radix sort.
+void order_y_by_degree(Ctx& X, const uint32_t* dR, uint64_t y_card, uint64_t max_dr,
+                       DBuf<uint32_t>& order) {
+  using namespace d3g;
+  order = X.alloc<uint32_t>(y_card);
+  if (y_card == 0) return;
+  if (max_dr < (1ull << 20)) {
+    DBuf<uint32_t> cnt = X.zeros<uint32_t>(max_dr + 1);
+    D3G_LAUNCH(X, desc_hist_kernel, grid_for(y_card, 256), 256, 0, dR, y_card, (uint32_t)max_dr,
+               cnt.p);
+    DBuf<uint64_t> off = X.alloc<uint64_t>(max_dr + 2);
+    exclusive_scan<uint32_t>(X, cnt.p, max_dr + 1, off.p);
+    D3G_LAUNCH(X, desc_scatter_kernel, grid_for(y_card, 256), 256, 0, dR, y_card,
+               (uint32_t)max_dr, off.p, cnt.p, order.p);
+    return;
+  }
+  DBuf<uint64_t> k = X.alloc<uint64_t>(y_card);
+  D3G_LAUNCH(X, degree_order_key_kernel, grid_for(y_card, 256), 256, 0, (const uint32_t*)nullptr,
+             y_card, (const uint64_t*)nullptr, dR, max_dr, k.p, order.p);
+  radix_sort(X, k.p, order.p, y_card, bits_for(max_dr), false);
+}
+
 // rows: dense z rows given as (row_ptr, col) indexed by row id; row_ids
-// lists the n_dense row ids; z_of_row (nullable) maps a row id to its z code
-// (identity when null). dR: per-y R-side degrees (hotness).
+// lists the n_dense row ids (or sel selects them by degree); z_of_row
+// (nullable) maps a row id to its z code (identity when null). dR: per-y
+// R-side degrees (hotness).
 void build_dense_layout(Ctx& X, const d3g::DeviceCsr& rx, uint64_t max_mx,
                         const std::vector<uint64_t>& hmx, const uint64_t* zrow_ptr,
                         const uint32_t* zcol, const uint32_t* row_ids, uint64_t n_dense,
                         uint64_t max_mz, const uint32_t* z_of_row, uint64_t y_card,
                         const uint32_t* dR, DenseLayout& L, uint64_t xa = 0,
-                        uint64_t xb = ~0ull, uint64_t dnnz_hint = ~0ull) {
+                        uint64_t xb = ~0ull, uint64_t dnnz_hint = ~0ull,
+                        const RowSel* sel = nullptr, uint64_t z_rows = 0,
+                        bool stable_x = false) {
   using namespace d3g;
-  L.n_dense = n_dense;
-  // y ranked by dR descending (ties by code): hottest witnesses first. dR(y)
-  // <= x_card bounds the key without a device round trip.
+  // y ranked by dR descending: hottest witnesses first. dR(y) <= x_card
+  // bounds the key without a device round trip.
   const uint64_t max_dr = rx.n_rows;
-  {
-    DBuf<uint64_t> k = X.alloc<uint64_t>(y_card);
-    DBuf<uint32_t> v = X.alloc<uint32_t>(y_card);
-    D3G_LAUNCH(X, degree_order_key_kernel, grid_for(y_card, 256), 256, 0, (const uint32_t*)nullptr,
-               y_card, (const uint64_t*)nullptr, dR, max_dr, k.p, v.p);
-    radix_sort(X, k.p, v.p, y_card, bits_for(max_dr), false);
-    L.y_rank = X.alloc<uint32_t>(y_card);
-    D3G_LAUNCH(X, scatter_rank_kernel, grid_for(y_card, 256), 256, 0, v.p, y_card, L.y_rank.p);
-    L.y_of_rank = std::move(v);
-  }
+  order_y_by_degree(X, dR, y_card, max_dr, L.y_of_rank);
+  L.y_rank = X.alloc<uint32_t>(y_card);
+  D3G_LAUNCH(X, scatter_rank_kernel, grid_for(y_card, 256), 256, 0, L.y_of_rank.p, y_card,
+             L.y_rank.p);
   // dense rows ordered by m_z descending (uniform trip counts per warp)
-  DBuf<uint32_t> rows = X.alloc<uint32_t>(n_dense);
-  {
-    DBuf<uint64_t> k = X.alloc<uint64_t>(n_dense);
-    D3G_LAUNCH(X, degree_order_key_kernel, grid_for(n_dense, 256), 256, 0, row_ids, n_dense,
-               zrow_ptr, (const uint32_t*)nullptr, max_mz, k.p, rows.p);
-    radix_sort(X, k.p, rows.p, n_dense, bits_for(max_mz), false);
+  DBuf<uint32_t> rows;
+  uint64_t dnnz = 0;
+  if (sel) {
+    DegreeOrder o;
+    order_by_degree(X, zrow_ptr, 0, z_rows, *sel->hmz, sel->d_table, sel->table, sel->mode, true,
+                    sel->sp_out != nullptr, o);
+    n_dense = o.n;
+    dnnz = o.nnz;
+    rows = std::move(o.rows);
+    L.dl_ptr = std::move(o.ptr);
+    if (sel->sp_out) *sel->sp_out = std::move(o.sp);
+  } else {
+    rows = X.alloc<uint32_t>(n_dense);
+    {
+      DBuf<uint64_t> k = X.alloc<uint64_t>(n_dense);
+      D3G_LAUNCH(X, degree_order_key_kernel, grid_for(n_dense, 256), 256, 0, row_ids, n_dense,
+                 zrow_ptr, (const uint32_t*)nullptr, max_mz, k.p, rows.p);
+      radix_sort(X, k.p, rows.p, n_dense, bits_for(max_mz), false);
+    }
+    DBuf<uint32_t> len = X.alloc<uint32_t>(n_dense);
+    D3G_LAUNCH(X, gather_len_kernel, grid_for(n_dense, 256), 256, 0, rows.p, n_dense, zrow_ptr, len.p);
+    L.dl_ptr = X.alloc<uint64_t>(n_dense + 1);
+    exclusive_scan<uint32_t>(X, len.p, n_dense, L.dl_ptr.p);
+    len.reset();
+    dnnz = dnnz_hint != ~0ull ? dnnz_hint : X.scalar(L.dl_ptr.p + n_dense);
   }
-  DBuf<uint32_t> len = X.alloc<uint32_t>(n_dense);
-  D3G_LAUNCH(X, gather_len_kernel, grid_for(n_dense, 256), 256, 0, rows.p, n_dense, zrow_ptr, len.p);
-  L.dl_ptr = X.alloc<uint64_t>(n_dense + 1);
-  exclusive_scan<uint32_t>(X, len.p, n_dense, L.dl_ptr.p);
-  len.reset();
-  const uint64_t dnnz = dnnz_hint != ~0ull ? dnnz_hint : X.scalar(L.dl_ptr.p + n_dense);
+  L.n_dense = n_dense;
   L.dnnz = dnnz;
   {
     L.dl_col = X.alloc<uint32_t>(dnnz);
-    D3G_LAUNCH(X, dense_list_fill_kernel, grid_for(n_dense * 32, 256), 256, 0, rows.p, n_dense,
+    D3G_LAUNCH(X, dense_list_fill_kernel, grid_for(n_dense * 8, 256), 256, 0, rows.p, n_dense,
                zrow_ptr, zcol, L.dl_ptr.p, L.y_rank.p, L.dl_col.p);
     DBuf<uint32_t> kept = X.alloc<uint32_t>(n_dense);
     segmented_sort(X, L.dl_col.p, L.dl_ptr.p, n_dense, /*unique=*/false, kept.p, max_mz);
@@ -931,22 +1002,32 @@ void build_dense_layout(Ctx& X, const d3g::DeviceCsr& rx, uint64_t max_mx,
   if (xb > rx.n_rows) xb = rx.n_rows;
   if (xa > xb) xa = xb;
   const uint64_t x_card = xb - xa;
-  DBuf<uint32_t> lf = X.alloc<uint32_t>(x_card);
-  if (x_card) D3G_LAUNCH(X, live_flag_kernel, grid_for(x_card, 256), 256, 0, rx.row_ptr.p, xa, xb, lf.p);
-  DBuf<uint64_t> lp = X.alloc<uint64_t>(x_card + 1);
-  exclusive_scan<uint32_t>(X, lf.p, x_card, lp.p);
-  if (xa == 0 && xb == rx.n_rows) {  // every live x: the m_x histogram knows how many
-    L.n_live = 0;
-    for (uint64_t m = 1; m < hmx.size(); ++m) L.n_live += hmx[m];
+  // Every live x: one counting scatter with offsets from the m_x histogram
+  // (ties in arbitrary order). x shards split the x ORDER by position, so
+  // sharded calls (stable_x) use the stable sort: every rank then sees the
+  // same order and the shards partition the x exactly.
+  const bool full_range = xa == 0 && xb == rx.n_rows;
+  if (full_range && !stable_x) {
+    DegreeOrder o;
+    order_by_degree(X, rx.row_ptr.p, 0, x_card, hmx, nullptr, nullptr, 0, false, false, o);
+    L.n_live = o.n;
+    L.xorder = std::move(o.rows);
   } else {
-    L.n_live = X.scalar(lp.p + x_card);
-  }
-  DBuf<uint32_t> live_ids = X.alloc<uint32_t>(L.n_live);
-  if (x_card)
-    D3G_LAUNCH(X, index_compact_kernel, grid_for(x_card, 256), 256, 0, lf.p, lp.p, x_card, live_ids.p);
-  if (xa && L.n_live)
-    D3G_LAUNCH(X, add_offset_kernel, grid_for(L.n_live, 256), 256, 0, live_ids.p, L.n_live, (uint32_t)xa);
-  {
+    DBuf<uint32_t> lf = X.alloc<uint32_t>(x_card);
+    if (x_card) D3G_LAUNCH(X, live_flag_kernel, grid_for(x_card, 256), 256, 0, rx.row_ptr.p, xa, xb, lf.p);
+    DBuf<uint64_t> lp = X.alloc<uint64_t>(x_card + 1);
+    exclusive_scan<uint32_t>(X, lf.p, x_card, lp.p);
+    if (full_range) {  // the m_x histogram knows how many
+      L.n_live = 0;
+      for (uint64_t m = 1; m < hmx.size(); ++m) L.n_live += hmx[m];
+    } else {
+      L.n_live = X.scalar(lp.p + x_card);
+    }
+    DBuf<uint32_t> live_ids = X.alloc<uint32_t>(L.n_live);
+    if (x_card)
+      D3G_LAUNCH(X, index_compact_kernel, grid_for(x_card, 256), 256, 0, lf.p, lp.p, x_card, live_ids.p);
+    if (xa && L.n_live)
+      D3G_LAUNCH(X, add_offset_kernel, grid_for(L.n_live, 256), 256, 0, live_ids.p, L.n_live, (uint32_t)xa);
     DBuf<uint64_t> k = X.alloc<uint64_t>(L.n_live);
     L.xorder = X.alloc<uint32_t>(L.n_live);
     if (L.n_live)
@@ -1460,14 +1541,18 @@ struct Split {
   // decision is a function of m_z alone (read off the m_z histogram)
   uint64_t dense_nnz = 0, sparse_nnz = 0;
   uint64_t outj_sparse = 0;  // join size of the sparse rows (from DegreeStats::wz)
+  std::vector<uint8_t> table;  // the f2 decision per m_z (1 = dense)
+  DBuf<uint8_t> dtable;        // and on the device
 };
 
 void f2_split(Ctx& X, const d3g::DeviceCsr& sz_csr, const DegreeStats& G, uint64_t x_card,
               uint64_t y_card, const d3g_consts* c, int pforce, d3g_report* rep, Split& P,
-              DBuf<uint64_t>* pd_out = nullptr, DBuf<uint64_t>* psp_out = nullptr) {
+              DBuf<uint64_t>* pd_out = nullptr, DBuf<uint64_t>* psp_out = nullptr,
+              bool flags = true) {
   using namespace d3g;
   const uint64_t z_card = sz_csr.n_rows;
-  std::vector<uint8_t> table(G.max_mz + 1, 0);
+  P.table.assign(G.max_mz + 1, 0);
+  std::vector<uint8_t>& table = P.table;
   uint64_t evals = 0;
   if (const char* dump = std::getenv("D3G_DUMP_F2")) {  // debugging aid: the f2 inputs
     if (FILE* f = std::fopen(dump, "wb")) {
@@ -1481,16 +1566,20 @@ void f2_split(Ctx& X, const d3g::DeviceCsr& sz_csr, const DegreeStats& G, uint64
   d3g_f2_decide(G.hmx.data(), G.max_mx + 1, G.hmz.data(), G.max_mz + 1, x_card, y_card, z_card,
                 rep->out_j, c, pforce, table.data(), &evals);
   rep->f2_evaluations = evals;
-  DBuf<uint8_t> dtable = X.alloc<uint8_t>(G.max_mz + 1);
-  X.to_device(dtable.p, table.data(), G.max_mz + 1);
-  P.isd = X.alloc<uint32_t>(z_card);
-  P.iss = X.alloc<uint32_t>(z_card);
-  if (z_card)
-    D3G_LAUNCH(X, dense_flag_kernel, grid_for(z_card, 256), 256, 0, sz_csr.row_ptr.p, z_card,
-               dtable.p, G.max_mz + 1, P.isd.p, P.iss.p);
-  DBuf<uint64_t> pd = X.alloc<uint64_t>(z_card + 1), psp = X.alloc<uint64_t>(z_card + 1);
-  exclusive_scan<uint32_t>(X, P.isd.p, z_card, pd.p);
-  exclusive_scan<uint32_t>(X, P.iss.p, z_card, psp.p);
+  P.dtable = X.alloc<uint8_t>(G.max_mz + 1);
+  X.to_device(P.dtable.p, table.data(), G.max_mz + 1);
+  if (flags) {
+    P.isd = X.alloc<uint32_t>(z_card);
+    P.iss = X.alloc<uint32_t>(z_card);
+    if (z_card)
+      D3G_LAUNCH(X, dense_flag_kernel, grid_for(z_card, 256), 256, 0, sz_csr.row_ptr.p, z_card,
+                 P.dtable.p, G.max_mz + 1, P.isd.p, P.iss.p);
+    DBuf<uint64_t> pd = X.alloc<uint64_t>(z_card + 1), psp = X.alloc<uint64_t>(z_card + 1);
+    exclusive_scan<uint32_t>(X, P.isd.p, z_card, pd.p);
+    exclusive_scan<uint32_t>(X, P.iss.p, z_card, psp.p);
+    if (pd_out) *pd_out = std::move(pd);
+    if (psp_out) *psp_out = std::move(psp);
+  }
   for (uint64_t m = 1; m < G.hmz.size(); ++m) {
     if (table[m]) {
       P.n_dense += G.hmz[m];
@@ -1505,8 +1594,6 @@ void f2_split(Ctx& X, const d3g::DeviceCsr& sz_csr, const DegreeStats& G, uint64
   rep->sparse_z = P.n_sparse;
   const uint64_t row_words = ((y_card + c->w - 1) / c->w * c->w) / 64;
   rep->panel_bytes = P.n_dense * row_words * 8;
-  if (pd_out) *pd_out = std::move(pd);
-  if (psp_out) *psp_out = std::move(psp);
 }
 
 // ---------------------------------------------------------------------------
@@ -1657,25 +1744,8 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
                      : o->force == D3G_DENSE_ONLY ? D3G_DENSE_ONLY
                                                   : D3G_HYBRID;
   Split P;
-  DBuf<uint64_t> pd, psp;
-  f2_split(X, sz_csr, G, x_card, y_card, c, pforce, rep, P, &pd, &psp);
+  f2_split(X, sz_csr, G, x_card, y_card, c, pforce, rep, P, nullptr, nullptr, /*flags=*/false);
   const uint64_t n_dense = P.n_dense, n_sparse = P.n_sparse;
-  DBuf<uint32_t> dense_ids = X.alloc<uint32_t>(n_dense), sparse_ids = X.alloc<uint32_t>(n_sparse);
-  if (z_card) {
-    D3G_LAUNCH(X, index_compact_kernel, grid_for(z_card, 256), 256, 0, P.isd.p, pd.p, z_card,
-               dense_ids.p);
-    D3G_LAUNCH(X, index_compact_kernel, grid_for(z_card, 256), 256, 0, P.iss.p, psp.p, z_card,
-               sparse_ids.p);
-  }
-  P.isd.reset();
-  P.iss.reset();
-  pd.reset();
-  psp.reset();
-  // sparse side: OUT_J,sparse (SpaStats::inner_count) comes from the
-  // per-degree join sizes; the y-major CSR over compact sparse indices is
-  // built only when the SparseBMM tiers run
-  DBuf<uint64_t> sp_ptr = X.alloc<uint64_t>(y_card + 1);
-  DBuf<uint32_t> sp_col;
   rep->sparse_nnz = P.sparse_nnz;  // known on the host (m_z histogram)
   // optional x-code restriction of the kernels (opts x_code_lo/hi)
   const uint64_t xa = o->x_code_hi ? std::min<uint64_t>(o->x_code_lo, x_card) : 0;
@@ -1687,7 +1757,8 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   // over 3,406 sparse z) the sparse rows are FOLDED into the dense layout and
   // their pairs counted apart, so one pass answers both and pairs_sparse /
   // pairs_dense stay the reference's split. Either way the result is exactly
-  // the sparse kernel's output, computed faster.
+  // the sparse kernel's output, computed faster. OUT_J,sparse
+  // (SpaStats::inner_count) comes from the per-degree join sizes.
   const uint64_t outj_sp = P.outj_sparse;
   const bool heavy_sparse = std::getenv("D3G_SPARSE_TIERS") == nullptr && x_live > 0 &&
                             n_sparse > 0 && outj_sp > 4096ull * x_live;
@@ -1697,7 +1768,23 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   const bool fold = heavy_sparse && n_dense > 0 && default_engine &&
                     std::getenv("D3G_NO_FOLD") == nullptr;
   const bool sparse_hot = heavy_sparse && !fold && n_sparse > 8192;
-  if (!fold && !sparse_hot) {  // the SparseBMM tiers read S_sparse by y
+  const bool tiers = !fold && !sparse_hot;  // the SparseBMM tiers answer the sparse side
+  // the sparse z as a compact id list, and the y-major CSR over those ids
+  // (partition.cpp:59-78), only when the tiers run
+  DBuf<uint32_t> sparse_ids;
+  DBuf<uint64_t> sp_ptr = X.alloc<uint64_t>(y_card + 1);
+  DBuf<uint32_t> sp_col;
+  if (tiers) {
+    sparse_ids = X.alloc<uint32_t>(n_sparse);
+    if (n_sparse) {
+      DBuf<uint32_t> iss = X.alloc<uint32_t>(z_card), isd = X.alloc<uint32_t>(z_card);
+      D3G_LAUNCH(X, dense_flag_kernel, grid_for(z_card, 256), 256, 0, sz_csr.row_ptr.p, z_card,
+                 P.dtable.p, G.max_mz + 1, isd.p, iss.p);
+      DBuf<uint64_t> psp = X.alloc<uint64_t>(z_card + 1);
+      exclusive_scan<uint32_t>(X, iss.p, z_card, psp.p);
+      D3G_LAUNCH(X, index_compact_kernel, grid_for(z_card, 256), 256, 0, iss.p, psp.p, z_card,
+                 sparse_ids.p);
+    }
     DBuf<uint32_t> sp_cnt = X.zeros<uint32_t>(y_card);
     if (n_sparse)
       D3G_LAUNCH(X, sparse_y_count_kernel, grid_for(n_sparse * 8, 256), 256, 0, sz_csr.row_ptr.p,
@@ -1709,32 +1796,21 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
                  sz_csr.row_ptr.p, sz_csr.col.p, sparse_ids.p, n_sparse, sp_ptr.p, sp_cnt.p,
                  sp_col.p);
   }
-  // dense side (plus the folded sparse rows)
+  // dense side (plus the folded sparse rows): rows selected by m_z through
+  // the f2 table and ordered by degree in one counting scatter
   DenseLayout L;
   DBuf<uint8_t> row_sp;
   if (n_dense > 0 && x_live > 0) {
-    if (fold) {
-      DBuf<uint32_t> ids = X.alloc<uint32_t>(n_dense + n_sparse);
-      D3G_CUDA(cudaMemcpyAsync(ids.p, dense_ids.p, n_dense * 4, cudaMemcpyDeviceToDevice, X.stream));
-      D3G_CUDA(cudaMemcpyAsync(ids.p + n_dense, sparse_ids.p, n_sparse * 4,
-                               cudaMemcpyDeviceToDevice, X.stream));
-      build_dense_layout(X, rx, max_mx, hmx, sz_csr.row_ptr.p, sz_csr.col.p, ids.p,
-                         n_dense + n_sparse, max_mz, nullptr, y_card, dR.p, L, xa, xb,
-                         P.dense_nnz + P.sparse_nnz);
-      DBuf<uint8_t> zsp = X.zeros<uint8_t>(z_card);
-      D3G_LAUNCH(X, mark_ids_kernel, grid_for(n_sparse, 256), 256, 0, sparse_ids.p, n_sparse, zsp.p);
-      row_sp = X.alloc<uint8_t>(L.n_dense);
-      D3G_LAUNCH(X, gather_u8_kernel, grid_for(L.n_dense, 256), 256, 0, L.dl_z.p, L.n_dense, zsp.p,
-                 row_sp.p);
-    } else {
-      build_dense_layout(X, rx, max_mx, hmx, sz_csr.row_ptr.p, sz_csr.col.p, dense_ids.p, n_dense,
-                         max_mz, nullptr, y_card, dR.p, L, xa, xb, P.dense_nnz);
-    }
+    RowSel sel{&G.hmz, P.dtable.p, &P.table, fold ? 0 : 1, fold ? &row_sp : nullptr};
+    build_dense_layout(X, rx, max_mx, hmx, sz_csr.row_ptr.p, sz_csr.col.p, nullptr, 0, max_mz,
+                       nullptr, y_card, dR.p, L, xa, xb, ~0ull, &sel, z_card, shard_count > 1);
   }
   DenseLayout Ls;
-  if (sparse_hot)
-    build_dense_layout(X, rx, max_mx, hmx, sz_csr.row_ptr.p, sz_csr.col.p, sparse_ids.p, n_sparse,
-                       max_mz, nullptr, y_card, dR.p, Ls, xa, xb, P.sparse_nnz);
+  if (sparse_hot) {
+    RowSel sel{&G.hmz, P.dtable.p, &P.table, 2, nullptr};
+    build_dense_layout(X, rx, max_mx, hmx, sz_csr.row_ptr.p, sz_csr.col.p, nullptr, 0, max_mz,
+                       nullptr, y_card, dR.p, Ls, xa, xb, ~0ull, &sel, z_card, shard_count > 1);
+  }
   T.mark();  // 6
 
   // 8. kernels

@@ -37,6 +37,87 @@ __global__ void dense_flag_kernel(const uint64_t* __restrict__ row_ptr, uint64_t
 }
 
 
+// Counting scatter of rows by degree, descending (ties in arbitrary order),
+// with the first position (off) and first list entry (ent) of every degree
+// precomputed on the host from the degree histogram: one launch replaces the
+// flag / scan / compact / key / radix-sort chain. Selection by the f2 table:
+// mode 0 = every row with d > 0 (sp_flag[pos] = the row is sparse), 1 = dense
+// rows (table[d] != 0), 2 = sparse rows (table[d] == 0, d > 0). out_ptr (the
+// rows' list offsets, with out_ptr[n_out] = total_ent) is optional.
+__global__ void degree_scatter_kernel(const uint64_t* __restrict__ row_ptr, uint64_t r0,
+                                      uint64_t r1, const uint8_t* __restrict__ table,
+                                      uint64_t table_len, int mode,
+                                      const uint64_t* __restrict__ off,
+                                      const uint64_t* __restrict__ ent,
+                                      unsigned int* __restrict__ cur, uint32_t* __restrict__ out,
+                                      uint64_t* __restrict__ out_ptr, uint64_t n_out,
+                                      uint64_t total_ent, uint8_t* __restrict__ sp_flag) {
+  const uint32_t lane = lane_id();
+  const uint64_t n = r1 - r0, n_pad = (n + 31) / 32 * 32;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pad;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = r0 + i;
+    uint64_t d = 0;
+    bool take = false, sparse = false;
+    if (i < n) {
+      d = row_ptr[r + 1] - row_ptr[r];
+      if (d > 0) {
+        sparse = !(d < table_len && table[d]);
+        take = mode == 0 || (mode == 1 ? !sparse : sparse);
+      }
+    }
+    const uint32_t key = take ? (uint32_t)d : 0xffffffffu;
+    const uint32_t peers = __match_any_sync(0xffffffffu, key);
+    if (take) {
+      const int leader = __ffs(peers) - 1;
+      const uint32_t rank = __popc(peers & ((1u << lane) - 1));
+      uint32_t base = 0;
+      if ((int)lane == leader) base = atomicAdd(&cur[d], (unsigned)__popc(peers));
+      base = __shfl_sync(peers, base, leader);
+      const uint64_t pos = off[d] + base + rank;
+      out[pos] = (uint32_t)r;
+      if (out_ptr) out_ptr[pos] = ent[d] + (uint64_t)(base + rank) * d;
+      if (sp_flag) sp_flag[pos] = sparse ? 1 : 0;
+    }
+  }
+  if (out_ptr && blockIdx.x == 0 && threadIdx.x == 0) out_ptr[n_out] = total_ent;
+}
+
+// Counting sort of indices by a u32 value, descending (ties in arbitrary
+// order): desc_hist_kernel counts key = max_val - val[i] (equal keys merged
+// per warp), an exclusive scan gives the offsets, desc_scatter_kernel places
+// each index (the counts are consumed as cursors).
+__global__ void desc_hist_kernel(const uint32_t* __restrict__ val, uint64_t n, uint32_t max_val,
+                                 uint32_t* __restrict__ cnt) {
+  const uint64_t n_pad = (n + 31) / 32 * 32;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pad;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t key = i < n ? max_val - val[i] : 0xffffffffu;
+    const uint32_t peers = __match_any_sync(0xffffffffu, key);
+    if (key != 0xffffffffu && (peers & ((1u << lane_id()) - 1)) == 0)
+      atomicAdd(&cnt[key], (unsigned)__popc(peers));
+  }
+}
+
+__global__ void desc_scatter_kernel(const uint32_t* __restrict__ val, uint64_t n,
+                                    uint32_t max_val, const uint64_t* __restrict__ off,
+                                    uint32_t* __restrict__ left, uint32_t* __restrict__ order) {
+  const uint32_t lane = lane_id();
+  const uint64_t n_pad = (n + 31) / 32 * 32;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pad;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t key = i < n ? max_val - val[i] : 0xffffffffu;
+    const uint32_t peers = __match_any_sync(0xffffffffu, key);
+    if (key == 0xffffffffu) continue;
+    const int leader = __ffs(peers) - 1;
+    const uint32_t k = (uint32_t)__popc(peers);
+    uint32_t top = 0;
+    if ((int)lane == leader) top = atomicSub(&left[key], k);
+    top = __shfl_sync(peers, top, leader);
+    order[off[key] + top - k + __popc(peers & ((1u << lane) - 1))] = (uint32_t)i;
+  }
+}
+
 // per-y count of sparse tuples
 // Both passes take four rows per warp (8 lanes each): the sparse rows are
 // short (cfg3: ~10 entries), and a warp per row left most lanes idle.
@@ -120,18 +201,19 @@ __global__ void dense_list_key_kernel(const uint32_t* __restrict__ ids, uint64_t
   }
 }
 
-// dl_col[dl_ptr[i] + k] = y_rank[src_col[src_ptr[ids[i]] + k]] (warp per row)
+// dl_col[dl_ptr[i] + k] = y_rank[src_col[src_ptr[ids[i]] + k]] (8 lanes per row)
 __global__ void dense_list_fill_kernel(const uint32_t* __restrict__ ids, uint64_t n,
                                        const uint64_t* __restrict__ src_ptr,
                                        const uint32_t* __restrict__ src_col,
                                        const uint64_t* __restrict__ dst_ptr,
                                        const uint32_t* __restrict__ y_rank,
                                        uint32_t* __restrict__ out) {
-  for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < n;
-       i += (uint64_t)gridDim.x * (blockDim.x / 32)) {
+  const uint32_t gl = threadIdx.x & 7;
+  for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 8) + (threadIdx.x >> 3); i < n;
+       i += (uint64_t)gridDim.x * (blockDim.x / 8)) {
     uint32_t id = ids[i];
     uint64_t s0 = src_ptr[id], s1 = src_ptr[id + 1], d0 = dst_ptr[i];
-    for (uint64_t k = s0 + lane_id(); k < s1; k += 32) out[d0 + (k - s0)] = y_rank[src_col[k]];
+    for (uint64_t k = s0 + gl; k < s1; k += 8) out[d0 + (k - s0)] = y_rank[src_col[k]];
   }
 }
 
