@@ -388,6 +388,21 @@ __host__ __device__ __forceinline__ uint64_t pair_hash(uint64_t x, uint64_t z) {
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 
+// 32-byte global accesses in ONE instruction (LDG/STG.E.ENL2.256, sm_100):
+// a warp reading 32 B per lane touches each 32 B sector once instead of
+// twice (two 16 B loads). p must be 32 B aligned.
+__device__ __forceinline__ void ld256(const uint4* p, uint4& a, uint4& b) {
+  asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z),
+                 "=r"(b.w)
+               : "l"(p));
+}
+__device__ __forceinline__ void st256(uint4* p, const uint4& a, const uint4& b) {
+  asm volatile("st.global.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a.x), "r"(a.y),
+               "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+               : "memory");
+}
+
 template <class T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll

@@ -123,8 +123,7 @@ __global__ void cold_scatter_kernel(const uint64_t* __restrict__ dl_ptr,
     const uint32_t zm = var_bits ? (uint32_t)(hz[i * kw] & vmask) : 0;
     uint4 s0 = make_uint4(0, 0, 0, 0), s1 = s0;
     if (sig) {
-      s0 = hz4[2 * i];
-      s1 = hz4[2 * i + 1];
+      ld256(hz4 + 2 * i, s0, s1);
     }
     const uint64_t e = dl_ptr[i + 1];
     for (uint64_t k = dl_ptr[i] + sl; k < e; k += 8) {
@@ -136,10 +135,7 @@ __global__ void cold_scatter_kernel(const uint64_t* __restrict__ dl_ptr,
           const uint64_t key = ((uint64_t)v * parts + part) * y_card + y;
           const uint64_t pos = base[key] + atomicSub(&left[key], 1u) - 1u;
           out[pos] = (uint32_t)i;
-          if (sig) {
-            sig[2 * pos] = s0;
-            sig[2 * pos + 1] = s1;
-          }
+          if (sig) st256(sig + 2 * pos, s0, s1);
         }
     }
   }
@@ -375,8 +371,7 @@ dense_hot_rec_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
     uint4 na = zero4, nb = zero4;
     uint32_t nc = 0;
     if (cb + lane < z_hi) {
-      na = rec[2 * (cb + lane)];
-      nb = rec[2 * (cb + lane) + 1];
+      ld256(rec + 2 * (cb + lane), na, nb);
       nc = rcnt[cb + lane];
     }
     for (; cb < z_hi; cb += (uint64_t)nwarps * 32) {
@@ -387,8 +382,7 @@ dense_hot_rec_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
       nb = zero4;
       nc = 0;
       if (nx < z_hi) {
-        na = rec[2 * nx];
-        nb = rec[2 * nx + 1];
+        ld256(rec + 2 * nx, na, nb);
         nc = rcnt[nx];
       }
       const uint32_t rows = (uint32_t)((z_hi - cb) < 32 ? (z_hi - cb) : 32);
@@ -538,8 +532,7 @@ dense_hot_tab_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
     uint4 na = zero4, nb = zero4;
     uint32_t nc = 0;
     if (cb + lane < z_hi) {
-      na = rec[2 * (cb + lane)];
-      nb = rec[2 * (cb + lane) + 1];
+      ld256(rec + 2 * (cb + lane), na, nb);
       nc = rcnt[cb + lane];
     }
     for (; cb < z_hi; cb += (uint64_t)nwarps * 32) {
@@ -550,8 +543,7 @@ dense_hot_tab_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
       nb = zero4;
       nc = 0;
       if (nx < z_hi) {
-        na = rec[2 * nx];
-        nb = rec[2 * nx + 1];
+        ld256(rec + 2 * nx, na, nb);
         nc = rcnt[nx];
       }
       const uint32_t rows = (uint32_t)((z_hi - cb) < 32 ? (z_hi - cb) : 32);
@@ -694,7 +686,8 @@ dense_cold_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
     const uint32_t part = (uint32_t)(item / n_x);
     const uint32_t x = xs[item % n_x];
     const uint32_t zbase = part * part_rows;
-    const uint4 a0 = hx4[2 * (uint64_t)x], a1 = hx4[2 * (uint64_t)x + 1];
+    uint4 a0, a1;
+    ld256(hx4 + 2 * (uint64_t)x, a0, a1);
     const uint32_t v = a0.x & ((1u << var_bits) - 1);  // x's top-var_bits hot mask
     const uint64_t* cp = cptr + ((uint64_t)v * parts + part) * y_card;
     bool touched = false;
@@ -748,8 +741,7 @@ dense_cold_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
 #pragma unroll
         for (int h = 0; h < kColdUnroll; ++h) {
           if (tf[h] < total) {
-            b0[h] = ch[2 * t[h]];
-            b1[h] = ch[2 * t[h] + 1];
+            ld256(ch + 2 * t[h], b0[h], b1[h]);
             zc[h] = ccol[t[h]];
           }
         }
@@ -847,7 +839,8 @@ dense_cold_hash_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
     item = __shfl_sync(0xffffffffu, item, 0);
     if (item >= n_x) break;
     const uint32_t x = xs[item];
-    const uint4 a0 = hx4[2 * (uint64_t)x], a1 = hx4[2 * (uint64_t)x + 1];
+    uint4 a0, a1;
+    ld256(hx4 + 2 * (uint64_t)x, a0, a1);
     const uint32_t v = a0.x & ((1u << var_bits) - 1);
     const uint64_t* cp = cptr + (uint64_t)v * y_card;
     uint32_t inserted = 0;  // warp-uniform
@@ -869,7 +862,8 @@ dense_cold_hash_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
           const uint64_t t = tb + lane;
           bool fresh = false;
           if (t < s1) {
-            const uint4 b0 = ch[2 * t], b1 = ch[2 * t + 1];
+            uint4 b0, b1;
+            ld256(ch + 2 * t, b0, b1);
             const bool hot = ((a0.x & b0.x) | (a0.y & b0.y) | (a0.z & b0.z) | (a0.w & b0.w) |
                               (a1.x & b1.x) | (a1.y & b1.y) | (a1.z & b1.z) | (a1.w & b1.w)) != 0;
             if (!hot) {
@@ -934,7 +928,8 @@ dense_cold_overflow_kernel(const uint32_t* __restrict__ over_x, const unsigned i
   uint64_t cnt = 0, sum = 0, xr = 0, csp = 0;
   for (uint32_t it = blockIdx.x; it < n; it += gridDim.x) {
     const uint32_t x = over_x[it];
-    const uint4 a0 = hx4[2 * (uint64_t)x], a1 = hx4[2 * (uint64_t)x + 1];
+    uint4 a0, a1;
+    ld256(hx4 + 2 * (uint64_t)x, a0, a1);
     const uint32_t v = a0.x & ((1u << var_bits) - 1);
     const uint64_t* cp = cptr + (uint64_t)v * y_card;
     for (int pass = 0; pass < 2; ++pass) {
@@ -942,7 +937,8 @@ dense_cold_overflow_kernel(const uint32_t* __restrict__ over_x, const unsigned i
         const uint32_t y = r_col[k];
         const uint64_t s0 = cp[y], s1 = cp[y + 1];
         for (uint64_t t = s0 + threadIdx.x; t < s1; t += blockDim.x) {
-          const uint4 b0 = ch[2 * t], b1 = ch[2 * t + 1];
+          uint4 b0, b1;
+          ld256(ch + 2 * t, b0, b1);
           const bool hot = ((a0.x & b0.x) | (a0.y & b0.y) | (a0.z & b0.z) | (a0.w & b0.w) |
                             (a1.x & b1.x) | (a1.y & b1.y) | (a1.z & b1.z) | (a1.w & b1.w)) != 0;
           if (hot) continue;
