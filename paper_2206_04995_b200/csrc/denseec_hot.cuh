@@ -306,7 +306,8 @@ dense_hot_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
 __global__ void hot_rec_kernel(const uint64_t* __restrict__ dl_ptr,
                                const uint32_t* __restrict__ dl_col, uint64_t n_dense, uint32_t K,
                                uint32_t tb, uint8_t* __restrict__ rec /* [D][32], zeroed */,
-                               uint32_t* __restrict__ rcnt, const uint8_t* __restrict__ row_sp) {
+                               uint32_t* __restrict__ rcnt, const uint8_t* __restrict__ row_sp,
+                               uint32_t sub = 0 /* stored rank = r - sub */) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_dense;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t k0 = dl_ptr[i], k1 = dl_ptr[i + 1];
@@ -318,7 +319,7 @@ __global__ void hot_rec_kernel(const uint64_t* __restrict__ dl_ptr,
         top |= 1u << r;
         continue;
       }
-      if (c < 32) rec[i * 32 + c] = (uint8_t)r;
+      if (c < 32) rec[i * 32 + c] = (uint8_t)(r - sub);
       ++c;
     }
     rcnt[i] = c | (top << 24) | ((row_sp && row_sp[i]) ? 0x80000000u : 0u);
@@ -642,6 +643,577 @@ dense_hot_tab_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
     }
     __syncthreads();  // Ts may be overwritten by the next unit's copy
   }
+  flush_sp(cnt_sp, csp);
+  tally_flush(tally, cnt, sum, xr);
+}
+
+// Sort key of a tab-mode record for the prefix-shared kernel: (subset mask,
+// first listed rank + 1, second listed rank + 1), 0 = absent.
+__global__ void trie_key_kernel(const uint8_t* __restrict__ rec, const uint32_t* __restrict__ rcnt,
+                                uint64_t n, uint64_t* __restrict__ key, uint32_t* __restrict__ idx,
+                                uint32_t off /* stored rank byte + off = rank - 6 */) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t cw = rcnt[i], c = cw & 0xffffffu;
+    const uint32_t r1 = c >= 1 ? rec[i * 32] + off : 0u;
+    const uint32_t r2 = c >= 2 ? rec[i * 32 + 1] + off : 0u;
+    key[i] = ((uint64_t)((cw >> 24) & 0x7fu) << 16) | (r1 << 8) | r2;
+    idx[i] = (uint32_t)i;
+  }
+}
+
+// Records in sorted order plus the shared-prefix length L with the previous
+// sorted row (levels: subset, r1, r2; a level counts only if present).
+__global__ void trie_gather_kernel(const uint4* __restrict__ rec, const uint32_t* __restrict__ rcnt,
+                                   const uint64_t* __restrict__ key, const uint32_t* __restrict__ perm,
+                                   uint64_t n, uint4* __restrict__ rec_s, uint32_t* __restrict__ rcnt_s) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t src = perm[i];
+    uint4 a, b;
+    ld256(rec + 2 * (uint64_t)src, a, b);
+    st256(rec_s + 2 * i, a, b);
+    const uint64_t k = key[i];
+    uint32_t L = 0;
+    if (i > 0) {
+      const uint64_t kp = key[i - 1];
+      if ((k >> 16) == (kp >> 16)) {
+        L = 1;
+        if ((k & 0xff00u) && ((k >> 8) == (kp >> 8))) {
+          L = 2;
+          if ((k & 0xffu) && k == kp) L = 3;
+        }
+      }
+    }
+    rcnt_s[i] = rcnt[src] | (L << 22);
+  }
+}
+// --- P1 with prefix-shared records ----------------------------------------
+// Dense rows sorted by (subset mask, first listed rank, second listed rank)
+// share their leading slices with the row before them: cfg2's sorted rows
+// repeat their first kTrieDepth sequence elements (subset, r1, r2) often
+// enough to cut the slice reads per (row, batch) by a third (cfg5: by half).
+// The warp keeps the partial ORs after each of those elements in registers
+// (a0 = subset entry, a1 = a0 | T[r1], a2 = a1 | T[r2]) and a row whose
+// shared-prefix length with its predecessor is L (bits 22-23 of the count
+// word, set by trie_gather_kernel) restarts from a_{L-1}. The first row of
+// each warp step starts from scratch (its predecessor ran on another warp).
+// perm maps a sorted position back to the dense row (dl_z, dl_ptr).
+constexpr uint32_t kTrieCntMask = 0x3fffffu;
+#ifndef D3G_TRIE_THREADS
+#define D3G_TRIE_THREADS 768
+#endif
+constexpr int kTrieThreads = D3G_TRIE_THREADS;
+
+__device__ __forceinline__ void or4(uint4& a, const uint4& v) {
+  a.x |= v.x;
+  a.y |= v.y;
+  a.z |= v.z;
+  a.w |= v.w;
+}
+
+template <int kMode>
+__global__ void __launch_bounds__(kTrieThreads, 1)
+dense_hot_trie_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
+                      const uint32_t* __restrict__ dl_col, const uint4* __restrict__ rec,
+                      const uint32_t* __restrict__ rcnt, const uint32_t* __restrict__ perm,
+                      Decode dec, Emit em, Tally* tally, unsigned long long* __restrict__ cnt_sp,
+                      unsigned long long* __restrict__ lds_units) {
+  extern __shared__ __align__(128) uint4 Ts[];  // [kTabRows + K - kTabBits][32]
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ unsigned int s_unit;
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const uint32_t n_batches = (p.groups + 31) / 32;
+  const unsigned int n_units = n_batches * p.z_chunks;
+  uint64_t cnt = 0, sum = 0, xr = 0, csp = 0, lds = 0;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  if (threadIdx.x < 32) Ts[threadIdx.x] = make_uint4(0, 0, 0, 0);  // entry 0: empty subset
+  __syncthreads();
+  uint32_t phase = 0;
+  int cur_batch = -1;
+  const uint4 zero4 = make_uint4(0, 0, 0, 0);
+  const uint4* rows_hi = Ts + (kTabRows - kTabBits) * 32 + lane;
+  const char* hb = reinterpret_cast<const char*>(rows_hi);
+#define D3G_ROW(wv, b) \
+  (*reinterpret_cast<const uint4*>(hb + (__byte_perm((wv), 0u, 0x4440u + (b)) << 9)))
+  for (;;) {
+    if (threadIdx.x == 0) s_unit = atomicAdd(p.work, 1u);
+    __syncthreads();
+    const unsigned int unit = s_unit;
+    if (unit >= n_units) break;
+    const uint32_t bi = unit / p.z_chunks, zc_i = unit % p.z_chunks;
+    if ((int)bi != cur_batch) {
+      if (threadIdx.x == 0) {
+        const uint4* src = p.T + (uint64_t)bi * p.K * 32;
+        const uint32_t hi_bytes = (p.K - kTabBits) * 32u * 16u;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&bar, hi_bytes + kTabBits * 512u);
+        for (uint32_t b = 0; b < kTabBits; ++b)
+          tma_bulk_g2s(Ts + (1u << b) * 32, src + b * 32, 512u, &bar);
+        tma_bulk_g2s(Ts + kTabRows * 32, src + kTabBits * 32, hi_bytes, &bar);
+      }
+      mbar_wait(&bar, phase);
+      phase ^= 1;
+      cur_batch = (int)bi;
+      for (uint32_t b = 1; b < kTabBits; ++b) {
+        const uint32_t lo = 1u << b, n = (lo - 1) * 32;
+        for (uint32_t t = threadIdx.x; t < n; t += blockDim.x) {
+          const uint32_t e = lo + 1 + (t >> 5), l = t & 31;
+          const uint4 a = Ts[lo * 32 + l], c = Ts[(e - lo) * 32 + l];
+          Ts[e * 32 + l] = make_uint4(a.x | c.x, a.y | c.y, a.z | c.z, a.w | c.w);
+        }
+        __syncthreads();
+      }
+    }
+    const uint32_t g = bi * 32 + lane;
+    const uint64_t gp0 = (uint64_t)g * 128;
+    const uint64_t z_lo = p.n_dense * zc_i / p.z_chunks, z_hi = p.n_dense * (zc_i + 1) / p.z_chunks;
+    uint64_t cb = z_lo + (uint64_t)warp * 32;
+    uint4 na = zero4, nb = zero4;
+    uint32_t nc = 0;
+    if (cb + lane < z_hi) {
+      ld256(rec + 2 * (cb + lane), na, nb);
+      nc = rcnt[cb + lane];
+    }
+    uint4 a0 = zero4, a1 = zero4, a2 = zero4;
+    for (; cb < z_hi; cb += (uint64_t)nwarps * 32) {
+      const uint4 ra = na, rb = nb;
+      const uint32_t rc = nc;
+      const uint64_t nx = cb + (uint64_t)nwarps * 32 + lane;
+      na = zero4;
+      nb = zero4;
+      nc = 0;
+      if (nx < z_hi) {
+        ld256(rec + 2 * nx, na, nb);
+        nc = rcnt[nx];
+      }
+      const uint32_t rows = (uint32_t)((z_hi - cb) < 32 ? (z_hi - cb) : 32);
+      for (uint32_t j = 0; j < rows; ++j) {
+        const uint32_t cw = __shfl_sync(0xffffffffu, rc, j);
+        const uint32_t c = cw & kTrieCntMask, top = (cw >> 24) & 0x7fu;
+        const uint32_t L = j ? (cw >> 22) & 3u : 0u;
+        const uint32_t w0 = __shfl_sync(0xffffffffu, ra.x, j);
+        if (L == 0) a0 = Ts[top * 32 + lane];  // entry 0 is the empty subset
+        if (L <= 1) {
+          a1 = a0;
+          if (c >= 1) or4(a1, D3G_ROW(w0, 0));
+        }
+        if (L <= 2) {
+          a2 = a1;
+          if (c >= 2) or4(a2, D3G_ROW(w0, 1));
+        }
+        lds += (L == 0 ? 1u : 0u) + c - (L > 1 ? L - 1 : 0u);
+        uint4 acc = a2;
+        if (c > 2) {
+          const uint4 v2 = D3G_ROW(w0, 2);
+          uint4 v3 = zero4;
+          if (c > 3) v3 = D3G_ROW(w0, 3);
+          acc.x |= v2.x | v3.x;
+          acc.y |= v2.y | v3.y;
+          acc.z |= v2.z | v3.z;
+          acc.w |= v2.w | v3.w;
+        }
+        const uint32_t words[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
+#pragma unroll
+        for (int q = 1; q < 8; ++q) {
+          if (4u * q + 4 <= c) {
+            const uint32_t wv = __shfl_sync(0xffffffffu, words[q], j);
+            const uint4 v0 = D3G_ROW(wv, 0), v1 = D3G_ROW(wv, 1);
+            const uint4 v2 = D3G_ROW(wv, 2), v3 = D3G_ROW(wv, 3);
+            acc.x |= v0.x | v1.x;
+            acc.y |= v0.y | v1.y;
+            acc.z |= v0.z | v1.z;
+            acc.w |= v0.w | v1.w;
+            acc.x |= v2.x | v3.x;
+            acc.y |= v2.y | v3.y;
+            acc.z |= v2.z | v3.z;
+            acc.w |= v2.w | v3.w;
+          } else if (4u * q < c) {
+            const uint32_t wv = __shfl_sync(0xffffffffu, words[q], j);
+            const uint32_t left = c - 4u * q;  // 1..3
+            const uint4 v0 = D3G_ROW(wv, 0);
+            uint4 v1 = zero4, v2 = zero4;
+            if (left > 1) v1 = D3G_ROW(wv, 1);
+            if (left > 2) v2 = D3G_ROW(wv, 2);
+            acc.x |= v0.x | v1.x;
+            acc.y |= v0.y | v1.y;
+            acc.z |= v0.z | v1.z;
+            acc.w |= v0.w | v1.w;
+            acc.x |= v2.x;
+            acc.y |= v2.y;
+            acc.z |= v2.z;
+            acc.w |= v2.w;
+          }
+        }
+        const uint64_t i = cb + j;
+        if (c > 32) {  // rare: more than 32 listed ranks; the tail is in the list
+          const uint32_t row = perm[i];
+          const uint64_t k1 = dl_ptr[row + 1];
+          uint64_t k = dl_ptr[row];
+          const uint32_t skip = __popc(top) + 32;
+          const uint64_t kend = k + skip + (c - 32);
+          k += skip;
+          for (uint64_t base = k; base < kend && base < k1; base += 32) {
+            const uint32_t mine = base + lane < kend ? dl_col[base + lane] : 0u;
+            const uint32_t n = (uint32_t)((kend - base) < 32 ? (kend - base) : 32);
+            for (uint32_t t = 0; t < n; ++t) {
+              const uint32_t r = __shfl_sync(0xffffffffu, mine, t);
+              or4(acc, rows_hi[r * 32]);
+            }
+          }
+        }
+        const uint32_t hits = __popc(acc.x) + __popc(acc.y) + __popc(acc.z) + __popc(acc.w);
+        cnt += hits;
+        if (cw >> 31) csp += hits;
+        if (kMode != kModeCount && hits) {
+          const uint32_t zc = p.dl_z[perm[i]];
+          const uint32_t ws[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+          for (int wi = 0; wi < 4; ++wi) {
+            uint32_t bits = ws[wi];
+            while (bits) {
+              const int b = __ffs(bits) - 1;
+              bits &= bits - 1;
+              const uint32_t xc = p.xorder[gp0 + wi * 32 + b];
+              if (kMode == kModeChecksum) {
+                const uint64_t h = dec.hash(xc, zc);
+                sum += h;
+                xr ^= h;
+              } else {
+                const unsigned long long idx = atomicAdd(em.cursor, 1ull);
+                if (idx < em.cap) {
+                  em.x[idx] = xc;
+                  em.z[idx] = zc;
+                }
+              }
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();  // Ts may be overwritten by the next unit's copy
+  }
+#undef D3G_ROW
+  flush_sp(cnt_sp, csp);
+  if (lane == 0 && lds) atomicAdd(lds_units, (unsigned long long)lds);
+  tally_flush(tally, cnt, sum, xr);
+}
+
+// --- P1 with a jump table over the listed ranks (default with the table) ---
+// Same work as dense_hot_tab_kernel, fewer instructions per (row, batch): the
+// tab kernel's eight guarded 4-rank steps cost ~30 branch/compare instructions
+// per row even when skipped (ncu on cfg2: 140 instructions and 32 branches per
+// (row, batch), issue-bound at 71% of peak). Here the listed-rank count picks
+// one entry of a switch; the entry ORs the partial top quad and jumps into a
+// straight-line run of full 4-rank quads. Listed ranks are stored as r - 7,
+// so shared memory is [listed rows 0..K-8][subset table], and byte b reads
+// row b directly.
+// Slice reads per batch of the prefix-shared jump-table kernel, summed over
+// rows: (L == 0) + c - max(L - 1, 0), with L forced to 0 on the first row of
+// each warp step (positions z_lo + 32k of the row's z chunk).
+__global__ void trie_lds_kernel(const uint32_t* __restrict__ rcnt, uint64_t n, uint32_t z_chunks,
+                                unsigned long long* __restrict__ out) {
+  uint64_t acc = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t zc = i * z_chunks / n;
+    while (zc + 1 < z_chunks && n * (zc + 1) / z_chunks <= i) ++zc;
+    while (zc > 0 && n * zc / z_chunks > i) --zc;
+    const uint64_t z_lo = n * zc / z_chunks;
+    const uint32_t cw = rcnt[i], c = cw & kTrieCntMask;
+    const uint32_t L = ((i - z_lo) % 32 == 0) ? 0u : (cw >> 22) & 3u;
+    acc += (L == 0 ? 1u : 0u) + c - (L > 1 ? L - 1 : 0u);
+  }
+  acc = warp_sum(acc);
+  if (lane_id() == 0 && acc) atomicAdd(out, (unsigned long long)acc);
+}
+
+template <int kMode, bool kTrie>
+__global__ void __launch_bounds__(kHotThreads, 1)
+dense_hot_jt_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
+                    const uint32_t* __restrict__ dl_col, const uint4* __restrict__ rec,
+                    const uint32_t* __restrict__ rcnt, const uint32_t* __restrict__ perm,
+                    Decode dec, Emit em, Tally* tally, unsigned long long* __restrict__ cnt_sp) {
+  extern __shared__ __align__(128) uint4 Ts[];  // [K - kTabBits listed][kTabRows subset][32]
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ unsigned int s_unit;
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const uint32_t n_batches = (p.groups + 31) / 32;
+  const unsigned int n_units = n_batches * p.z_chunks;
+  const uint32_t n_listed = p.K - kTabBits;
+  uint4* const sub_tab = Ts + n_listed * 32;  // entry e at sub_tab[e * 32 + lane]
+  uint64_t cnt = 0, sum = 0, xr = 0, csp = 0;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  if (threadIdx.x < 32) sub_tab[threadIdx.x] = make_uint4(0, 0, 0, 0);  // empty subset
+  __syncthreads();
+  uint32_t phase = 0;
+  int cur_batch = -1;
+  const uint4 zero4 = make_uint4(0, 0, 0, 0);
+  const char* hb = reinterpret_cast<const char*>(Ts + lane);
+  const uint4* sub_lane = sub_tab + lane;
+#define D3G_ROW(wv, b) \
+  (*reinterpret_cast<const uint4*>(hb + (__byte_perm((wv), 0u, 0x4440u + (b)) << 9)))
+#define D3G_Q4(W)                                                   \
+  {                                                                 \
+    const uint32_t wv = __shfl_sync(0xffffffffu, (W), j);           \
+    const uint4 v0 = D3G_ROW(wv, 0), v1 = D3G_ROW(wv, 1);           \
+    const uint4 v2 = D3G_ROW(wv, 2), v3 = D3G_ROW(wv, 3);           \
+    acc.x |= v0.x | v1.x;                                           \
+    acc.y |= v0.y | v1.y;                                           \
+    acc.z |= v0.z | v1.z;                                           \
+    acc.w |= v0.w | v1.w;                                           \
+    acc.x |= v2.x | v3.x;                                           \
+    acc.y |= v2.y | v3.y;                                           \
+    acc.z |= v2.z | v3.z;                                           \
+    acc.w |= v2.w | v3.w;                                           \
+  }
+#define D3G_QP(W, n)                                                \
+  {                                                                 \
+    const uint32_t wv = __shfl_sync(0xffffffffu, (W), j);           \
+    uint4 v0 = D3G_ROW(wv, 0), v1 = zero4, v2 = zero4;              \
+    if ((n) > 1) v1 = D3G_ROW(wv, 1);                               \
+    if ((n) > 2) v2 = D3G_ROW(wv, 2);                               \
+    acc.x |= v0.x | v1.x;                                           \
+    acc.y |= v0.y | v1.y;                                           \
+    acc.z |= v0.z | v1.z;                                           \
+    acc.w |= v0.w | v1.w;                                           \
+    acc.x |= v2.x;                                                  \
+    acc.y |= v2.y;                                                  \
+    acc.z |= v2.z;                                                  \
+    acc.w |= v2.w;                                                  \
+  }
+  for (;;) {
+    if (threadIdx.x == 0) s_unit = atomicAdd(p.work, 1u);
+    __syncthreads();
+    const unsigned int unit = s_unit;
+    if (unit >= n_units) break;
+    const uint32_t bi = unit / p.z_chunks, zc_i = unit % p.z_chunks;
+    if ((int)bi != cur_batch) {
+      if (threadIdx.x == 0) {
+        const uint4* src = p.T + (uint64_t)bi * p.K * 32;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&bar, (n_listed + kTabBits) * 512u);
+        tma_bulk_g2s(Ts, src + kTabBits * 32, n_listed * 512u, &bar);
+        for (uint32_t b = 0; b < kTabBits; ++b)
+          tma_bulk_g2s(sub_tab + (1u << b) * 32, src + b * 32, 512u, &bar);
+      }
+      mbar_wait(&bar, phase);
+      phase ^= 1;
+      cur_batch = (int)bi;
+      for (uint32_t b = 1; b < kTabBits; ++b) {
+        const uint32_t lo = 1u << b, n = (lo - 1) * 32;
+        for (uint32_t t = threadIdx.x; t < n; t += blockDim.x) {
+          const uint32_t e = lo + 1 + (t >> 5), l = t & 31;
+          const uint4 a = sub_tab[lo * 32 + l], c = sub_tab[(e - lo) * 32 + l];
+          sub_tab[e * 32 + l] = make_uint4(a.x | c.x, a.y | c.y, a.z | c.z, a.w | c.w);
+        }
+        __syncthreads();
+      }
+    }
+    const uint32_t g = bi * 32 + lane;
+    const uint64_t gp0 = (uint64_t)g * 128;
+    const uint64_t z_lo = p.n_dense * zc_i / p.z_chunks, z_hi = p.n_dense * (zc_i + 1) / p.z_chunks;
+    uint64_t cb = z_lo + (uint64_t)warp * 32;
+    uint4 na = zero4, nb = zero4;
+    uint32_t nc = 0;
+    uint4 a0 = zero4, a1 = zero4, a2 = zero4;  // kTrie: prefix ORs (subset, +r1, +r2)
+    if (cb + lane < z_hi) {
+      ld256(rec + 2 * (cb + lane), na, nb);
+      nc = rcnt[cb + lane];
+    }
+    for (; cb < z_hi; cb += (uint64_t)nwarps * 32) {
+      const uint4 ra = na, rb = nb;
+      const uint32_t rc = nc;
+      const uint64_t nx = cb + (uint64_t)nwarps * 32 + lane;
+      na = zero4;
+      nb = zero4;
+      nc = 0;
+      if (nx < z_hi) {
+        ld256(rec + 2 * nx, na, nb);
+        nc = rcnt[nx];
+      }
+      const uint32_t rows = (uint32_t)((z_hi - cb) < 32 ? (z_hi - cb) : 32);
+      const uint32_t words[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
+      for (uint32_t j = 0; j < rows; ++j) {
+        const uint32_t cw = __shfl_sync(0xffffffffu, rc, j);
+        const uint32_t c = cw & (kTrie ? kTrieCntMask : 0xffffffu), top = (cw >> 24) & 0x7fu;
+        const uint32_t cc = c < 32 ? c : 32;
+        uint4 acc;
+        if constexpr (!kTrie) {
+          acc = sub_lane[top * 32];
+          switch (cc) {
+            case 0: goto q_done;
+            case 1: D3G_QP(words[0], 1); goto q_done;
+            case 2: D3G_QP(words[0], 2); goto q_done;
+            case 3: D3G_QP(words[0], 3); goto q_done;
+            case 4: goto q_full0;
+            case 5: D3G_QP(words[1], 1); goto q_full0;
+            case 6: D3G_QP(words[1], 2); goto q_full0;
+            case 7: D3G_QP(words[1], 3); goto q_full0;
+            case 8: goto q_full1;
+            case 9: D3G_QP(words[2], 1); goto q_full1;
+            case 10: D3G_QP(words[2], 2); goto q_full1;
+            case 11: D3G_QP(words[2], 3); goto q_full1;
+            case 12: goto q_full2;
+            case 13: D3G_QP(words[3], 1); goto q_full2;
+            case 14: D3G_QP(words[3], 2); goto q_full2;
+            case 15: D3G_QP(words[3], 3); goto q_full2;
+            case 16: goto q_full3;
+            case 17: D3G_QP(words[4], 1); goto q_full3;
+            case 18: D3G_QP(words[4], 2); goto q_full3;
+            case 19: D3G_QP(words[4], 3); goto q_full3;
+            case 20: goto q_full4;
+            case 21: D3G_QP(words[5], 1); goto q_full4;
+            case 22: D3G_QP(words[5], 2); goto q_full4;
+            case 23: D3G_QP(words[5], 3); goto q_full4;
+            case 24: goto q_full5;
+            case 25: D3G_QP(words[6], 1); goto q_full5;
+            case 26: D3G_QP(words[6], 2); goto q_full5;
+            case 27: D3G_QP(words[6], 3); goto q_full5;
+            case 28: goto q_full6;
+            case 29: D3G_QP(words[7], 1); goto q_full6;
+            case 30: D3G_QP(words[7], 2); goto q_full6;
+            case 31: D3G_QP(words[7], 3); goto q_full6;
+            case 32: goto q_full7;
+            default: break;
+          }
+          q_full7: D3G_Q4(words[7]);
+          q_full6: D3G_Q4(words[6]);
+          q_full5: D3G_Q4(words[5]);
+          q_full4: D3G_Q4(words[4]);
+          q_full3: D3G_Q4(words[3]);
+          q_full2: D3G_Q4(words[2]);
+          q_full1: D3G_Q4(words[1]);
+          q_full0: D3G_Q4(words[0]);
+          q_done:
+          ;
+        } else {
+          // quads 1.. through the table, then quad 0 with the shared prefix
+          acc = zero4;
+          switch (cc) {
+            case 0: case 1: case 2: case 3: case 4: goto t_done;
+            case 5: D3G_QP(words[1], 1); goto t_done;
+            case 6: D3G_QP(words[1], 2); goto t_done;
+            case 7: D3G_QP(words[1], 3); goto t_done;
+            case 8: goto t_full1;
+            case 9: D3G_QP(words[2], 1); goto t_full1;
+            case 10: D3G_QP(words[2], 2); goto t_full1;
+            case 11: D3G_QP(words[2], 3); goto t_full1;
+            case 12: goto t_full2;
+            case 13: D3G_QP(words[3], 1); goto t_full2;
+            case 14: D3G_QP(words[3], 2); goto t_full2;
+            case 15: D3G_QP(words[3], 3); goto t_full2;
+            case 16: goto t_full3;
+            case 17: D3G_QP(words[4], 1); goto t_full3;
+            case 18: D3G_QP(words[4], 2); goto t_full3;
+            case 19: D3G_QP(words[4], 3); goto t_full3;
+            case 20: goto t_full4;
+            case 21: D3G_QP(words[5], 1); goto t_full4;
+            case 22: D3G_QP(words[5], 2); goto t_full4;
+            case 23: D3G_QP(words[5], 3); goto t_full4;
+            case 24: goto t_full5;
+            case 25: D3G_QP(words[6], 1); goto t_full5;
+            case 26: D3G_QP(words[6], 2); goto t_full5;
+            case 27: D3G_QP(words[6], 3); goto t_full5;
+            case 28: goto t_full6;
+            case 29: D3G_QP(words[7], 1); goto t_full6;
+            case 30: D3G_QP(words[7], 2); goto t_full6;
+            case 31: D3G_QP(words[7], 3); goto t_full6;
+            case 32: goto t_full7;
+            default: break;
+          }
+          t_full7: D3G_Q4(words[7]);
+          t_full6: D3G_Q4(words[6]);
+          t_full5: D3G_Q4(words[5]);
+          t_full4: D3G_Q4(words[4]);
+          t_full3: D3G_Q4(words[3]);
+          t_full2: D3G_Q4(words[2]);
+          t_full1: D3G_Q4(words[1]);
+          t_done:
+          ;
+          const uint32_t w0 = __shfl_sync(0xffffffffu, words[0], j);
+          const uint32_t L = j ? (cw >> 22) & 3u : 0u;
+          if (L == 0) a0 = sub_lane[top * 32];
+          if (L <= 1) {
+            a1 = a0;
+            if (c >= 1) or4(a1, D3G_ROW(w0, 0));
+          }
+          if (L <= 2) {
+            a2 = a1;
+            if (c >= 2) or4(a2, D3G_ROW(w0, 1));
+          }
+          or4(acc, a2);
+          if (c > 2) {
+            const uint4 v2 = D3G_ROW(w0, 2);
+            uint4 v3 = zero4;
+            if (c > 3) v3 = D3G_ROW(w0, 3);
+            acc.x |= v2.x | v3.x;
+            acc.y |= v2.y | v3.y;
+            acc.z |= v2.z | v3.z;
+            acc.w |= v2.w | v3.w;
+          }
+        }
+        const uint64_t i = cb + j;
+        if (c > 32) {  // rare: more than 32 listed ranks; the tail is in the list
+          const uint64_t row = kTrie ? perm[i] : i;
+          const uint64_t k1 = dl_ptr[row + 1];
+          uint64_t k = dl_ptr[row];
+          const uint32_t skip = __popc(top) + 32;
+          const uint64_t kend = k + skip + (c - 32);
+          k += skip;
+          for (uint64_t base = k; base < kend && base < k1; base += 32) {
+            const uint32_t mine = base + lane < kend ? dl_col[base + lane] : 0u;
+            const uint32_t n = (uint32_t)((kend - base) < 32 ? (kend - base) : 32);
+            for (uint32_t t = 0; t < n; ++t) {
+              const uint32_t r = __shfl_sync(0xffffffffu, mine, t);
+              const uint4 v = Ts[(r - kTabBits) * 32 + lane];
+              acc.x |= v.x;
+              acc.y |= v.y;
+              acc.z |= v.z;
+              acc.w |= v.w;
+            }
+          }
+        }
+        const uint32_t hits = __popc(acc.x) + __popc(acc.y) + __popc(acc.z) + __popc(acc.w);
+        cnt += hits;
+        if (cw >> 31) csp += hits;
+        if (kMode != kModeCount && hits) {
+          const uint32_t zc = p.dl_z[kTrie ? perm[i] : i];
+          const uint32_t ws[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+          for (int wi = 0; wi < 4; ++wi) {
+            uint32_t bits = ws[wi];
+            while (bits) {
+              const int b = __ffs(bits) - 1;
+              bits &= bits - 1;
+              const uint32_t xc = p.xorder[gp0 + wi * 32 + b];
+              if (kMode == kModeChecksum) {
+                const uint64_t h = dec.hash(xc, zc);
+                sum += h;
+                xr ^= h;
+              } else {
+                const unsigned long long idx = atomicAdd(em.cursor, 1ull);
+                if (idx < em.cap) {
+                  em.x[idx] = xc;
+                  em.z[idx] = zc;
+                }
+              }
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();  // Ts may be overwritten by the next unit's copy
+  }
+#undef D3G_QP
+#undef D3G_Q4
+#undef D3G_ROW
   flush_sp(cnt_sp, csp);
   tally_flush(tally, cnt, sum, xr);
 }

@@ -640,6 +640,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   unsigned long long* lds_units = &tallies.p[2].count;
   unsigned long long* cnt_sp = in.row_sp ? &tallies.p[3].count : nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  bool trie = false, jt_trie = false;
   size_t sm = (size_t)K * 32 * 16;
   unsigned g = (unsigned)std::min<uint64_t>((uint64_t)n_batches * hp.z_chunks, (uint64_t)X.sm_count);
   const char* hot_impl = std::getenv("D3G_HOT");
@@ -671,22 +672,66 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     const size_t tsm = (size_t)(kTabRows + K - kTabBits) * 32 * 16;
     double top_per_row = 0;
     for (uint32_t r = 0; r < kTabBits; ++r) top_per_row += (double)top_rank_rows[r] / (double)D;
-    const bool force_tab = hot_impl && std::string(hot_impl) == "tab";
+    const std::string hv = hot_impl ? hot_impl : "";
+    const bool force_tab = hv == "tab" || hv == "trie" || hv == "jt";
     const bool tab = K > kTabBits && tsm <= (size_t)dense_smem_bytes(X) &&
                      !(hot_impl && std::string(hot_impl) == "rec") &&
                      (force_tab || top_per_row >= 1.5);
     DBuf<uint4> rec = X.zeros<uint4>(2 * D);
     DBuf<uint32_t> rcnt = X.alloc<uint32_t>(D);
+    // with the table: the jump-table kernel by default; D3G_HOT=tab|trie select
+    // the guarded-step kernel or the prefix-shared one (kept for comparison)
+    const bool jt = tab && hv != "tab" && hv != "trie";
+    // prefix-shared rows with the jump-table kernel by default (D3G_HOT=jt
+    // keeps the dense-row order); D3G_HOT=trie runs the standalone
+    // prefix-shared kernel (comparison)
+    jt_trie = jt && hv != "jt";
+    trie = tab && (hv == "trie" || jt_trie);
     D3G_LAUNCH(X, hot_rec_kernel, grid_for(D, 256), 256, 0, in.dl_ptr, in.dl_col, D, K,
-               tab ? kTabBits : 0u, reinterpret_cast<uint8_t*>(rec.p), rcnt.p, in.row_sp);
-    // algorithmic LDS traffic: every (row, batch) reads its listed slices plus
-    // (tab) one subset-table entry, 512 B each
-    D3G_LAUNCH(X, rec_sum_kernel, grid_for(D, 256), 256, 0, rcnt.p, D, tab ? 1u : 0u, lds_units);
+               tab ? kTabBits : 0u, reinterpret_cast<uint8_t*>(rec.p), rcnt.p, in.row_sp,
+               jt ? kTabBits : 0u);
+    // prefix-shared records: rows sorted by (subset, r1, r2), records gathered
+    DBuf<uint32_t> perm;
+    if (trie) {
+      DBuf<uint64_t> key = X.alloc<uint64_t>(D);
+      perm = X.alloc<uint32_t>(D);
+      D3G_LAUNCH(X, trie_key_kernel, grid_for(D, 256), 256, 0, reinterpret_cast<const uint8_t*>(rec.p),
+                 rcnt.p, D, key.p, perm.p, jt ? 1u : 1u - kTabBits);
+      radix_sort(X, key.p, perm.p, D, 23, true);
+      DBuf<uint4> rec_s = X.alloc<uint4>(2 * D);
+      DBuf<uint32_t> rcnt_s = X.alloc<uint32_t>(D);
+      D3G_LAUNCH(X, trie_gather_kernel, grid_for(D, 256), 256, 0, rec.p, rcnt.p, key.p, perm.p, D,
+                 rec_s.p, rcnt_s.p);
+      rec = std::move(rec_s);
+      rcnt = std::move(rcnt_s);
+      if (jt_trie)
+        D3G_LAUNCH(X, trie_lds_kernel, grid_for(D, 256), 256, 0, rcnt.p, D, hp.z_chunks, lds_units);
+    } else {
+      // algorithmic LDS traffic: every (row, batch) reads its listed slices plus
+      // (tab) one subset-table entry, 512 B each
+      D3G_LAUNCH(X, rec_sum_kernel, grid_for(D, 256), 256, 0, rcnt.p, D, tab ? 1u : 0u, lds_units);
+    }
     D3G_CUDA(cudaEventCreate(&ev0));
     D3G_CUDA(cudaEventCreate(&ev1));
     D3G_CUDA(cudaEventRecord(ev0, X.stream));
     with_mode(mode, [&](auto M) {
-      if (tab) {
+      if (jt) {
+        auto run = [&](auto kfn) {
+          D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
+          D3G_LAUNCH(X, kfn, g, kHotThreads, tsm, hp, in.dl_ptr, in.dl_col, rec.p, rcnt.p, perm.p,
+                     dec, em, t, cnt_sp);
+        };
+        if (jt_trie)
+          run(dense_hot_jt_kernel<decltype(M)::value, true>);
+        else
+          run(dense_hot_jt_kernel<decltype(M)::value, false>);
+      } else if (trie) {
+        // the kernel counts its own slice reads (over every batch)
+        auto kfn = dense_hot_trie_kernel<decltype(M)::value>;
+        D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
+        D3G_LAUNCH(X, kfn, g, kTrieThreads, tsm, hp, in.dl_ptr, in.dl_col, rec.p, rcnt.p, perm.p,
+                   dec, em, t, cnt_sp, lds_units);
+      } else if (tab) {
         auto kfn = dense_hot_tab_kernel<decltype(M)::value>;
         D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
         D3G_LAUNCH(X, kfn, g, kHotThreads, tsm, hp, in.dl_ptr, in.dl_col, rec.p, rcnt.p, dec, em,
@@ -777,7 +822,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     cudaEventDestroy(ev0);
     cudaEventDestroy(ev1);
     out.ms_hot = ms;
-    out.hot_lds_bytes = th[2].count * n_batches * 512ull;
+    out.hot_lds_bytes = th[2].count * (trie && !jt_trie ? 1ull : (uint64_t)n_batches) * 512ull;
   }
   if (std::getenv("D3G_TRACE"))
     std::fprintf(stderr, "[dense_hot] D=%llu live=%llu K=%u hot=%llu cold=%llu cold_path=%s over=%llu\n",
