@@ -647,8 +647,8 @@ dense_hot_tab_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
   tally_flush(tally, cnt, sum, xr);
 }
 
-// Sort key of a tab-mode record for the prefix-shared kernel: (subset mask,
-// first listed rank + 1, second listed rank + 1), 0 = absent.
+// Sort key of a record for the prefix-shared kernels: (subset mask, first
+// listed rank + 1, second listed rank + 1; 7/9/9 bits), 0 = absent.
 __global__ void trie_key_kernel(const uint8_t* __restrict__ rec, const uint32_t* __restrict__ rcnt,
                                 uint64_t n, uint64_t* __restrict__ key, uint32_t* __restrict__ idx,
                                 uint32_t off /* stored rank byte + off = rank - 6 */) {
@@ -657,7 +657,7 @@ __global__ void trie_key_kernel(const uint8_t* __restrict__ rec, const uint32_t*
     const uint32_t cw = rcnt[i], c = cw & 0xffffffu;
     const uint32_t r1 = c >= 1 ? rec[i * 32] + off : 0u;
     const uint32_t r2 = c >= 2 ? rec[i * 32 + 1] + off : 0u;
-    key[i] = ((uint64_t)((cw >> 24) & 0x7fu) << 16) | (r1 << 8) | r2;
+    key[i] = ((uint64_t)((cw >> 24) & 0x7fu) << 18) | (r1 << 9) | r2;
     idx[i] = (uint32_t)i;
   }
 }
@@ -677,11 +677,11 @@ __global__ void trie_gather_kernel(const uint4* __restrict__ rec, const uint32_t
     uint32_t L = 0;
     if (i > 0) {
       const uint64_t kp = key[i - 1];
-      if ((k >> 16) == (kp >> 16)) {
+      if ((k >> 18) == (kp >> 18)) {
         L = 1;
-        if ((k & 0xff00u) && ((k >> 8) == (kp >> 8))) {
+        if ((k & 0x3fe00u) && ((k >> 9) == (kp >> 9))) {
           L = 2;
-          if ((k & 0xffu) && k == kp) L = 3;
+          if ((k & 0x1ffu) && k == kp) L = 3;
         }
       }
     }
@@ -915,7 +915,7 @@ dense_hot_trie_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
 // rows: (L == 0) + c - max(L - 1, 0), with L forced to 0 on the first row of
 // each warp step (positions z_lo + 32k of the row's z chunk).
 __global__ void trie_lds_kernel(const uint32_t* __restrict__ rcnt, uint64_t n, uint32_t z_chunks,
-                                unsigned long long* __restrict__ out) {
+                                uint32_t sub_read, unsigned long long* __restrict__ out) {
   uint64_t acc = 0;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
@@ -925,13 +925,13 @@ __global__ void trie_lds_kernel(const uint32_t* __restrict__ rcnt, uint64_t n, u
     const uint64_t z_lo = n * zc / z_chunks;
     const uint32_t cw = rcnt[i], c = cw & kTrieCntMask;
     const uint32_t L = ((i - z_lo) % 32 == 0) ? 0u : (cw >> 22) & 3u;
-    acc += (L == 0 ? 1u : 0u) + c - (L > 1 ? L - 1 : 0u);
+    acc += (L == 0 ? sub_read : 0u) + c - (L > 1 ? L - 1 : 0u);
   }
   acc = warp_sum(acc);
   if (lane_id() == 0 && acc) atomicAdd(out, (unsigned long long)acc);
 }
 
-template <int kMode, bool kTrie>
+template <int kMode, bool kTrie, bool kTab = true>
 __global__ void __launch_bounds__(kHotThreads, 1)
 dense_hot_jt_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
                     const uint32_t* __restrict__ dl_col, const uint4* __restrict__ rec,
@@ -943,7 +943,8 @@ dense_hot_jt_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const uint32_t n_batches = (p.groups + 31) / 32;
   const unsigned int n_units = n_batches * p.z_chunks;
-  const uint32_t n_listed = p.K - kTabBits;
+  constexpr uint32_t kTB = kTab ? kTabBits : 0u;  // ranks in the subset table
+  const uint32_t n_listed = p.K - kTB;
   uint4* const sub_tab = Ts + n_listed * 32;  // entry e at sub_tab[e * 32 + lane]
   uint64_t cnt = 0, sum = 0, xr = 0, csp = 0;
   if (threadIdx.x == 0) {
@@ -998,15 +999,15 @@ dense_hot_jt_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
       if (threadIdx.x == 0) {
         const uint4* src = p.T + (uint64_t)bi * p.K * 32;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&bar, (n_listed + kTabBits) * 512u);
-        tma_bulk_g2s(Ts, src + kTabBits * 32, n_listed * 512u, &bar);
-        for (uint32_t b = 0; b < kTabBits; ++b)
+        mbar_expect_tx(&bar, (n_listed + kTB) * 512u);
+        tma_bulk_g2s(Ts, src + kTB * 32, n_listed * 512u, &bar);
+        for (uint32_t b = 0; b < kTB; ++b)
           tma_bulk_g2s(sub_tab + (1u << b) * 32, src + b * 32, 512u, &bar);
       }
       mbar_wait(&bar, phase);
       phase ^= 1;
       cur_batch = (int)bi;
-      for (uint32_t b = 1; b < kTabBits; ++b) {
+      for (uint32_t b = 1; b < kTB; ++b) {
         const uint32_t lo = 1u << b, n = (lo - 1) * 32;
         for (uint32_t t = threadIdx.x; t < n; t += blockDim.x) {
           const uint32_t e = lo + 1 + (t >> 5), l = t & 31;
@@ -1046,7 +1047,7 @@ dense_hot_jt_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
         const uint32_t cc = c < 32 ? c : 32;
         uint4 acc;
         if constexpr (!kTrie) {
-          acc = sub_lane[top * 32];
+          acc = kTab ? sub_lane[top * 32] : zero4;
           switch (cc) {
             case 0: goto q_done;
             case 1: D3G_QP(words[0], 1); goto q_done;
@@ -1139,7 +1140,7 @@ dense_hot_jt_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
           ;
           const uint32_t w0 = __shfl_sync(0xffffffffu, words[0], j);
           const uint32_t L = j ? (cw >> 22) & 3u : 0u;
-          if (L == 0) a0 = sub_lane[top * 32];
+          if (kTab && L == 0) a0 = sub_lane[top * 32];
           if (L <= 1) {
             a1 = a0;
             if (c >= 1) or4(a1, D3G_ROW(w0, 0));
@@ -1172,7 +1173,7 @@ dense_hot_jt_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
             const uint32_t n = (uint32_t)((kend - base) < 32 ? (kend - base) : 32);
             for (uint32_t t = 0; t < n; ++t) {
               const uint32_t r = __shfl_sync(0xffffffffu, mine, t);
-              const uint4 v = Ts[(r - kTabBits) * 32 + lane];
+              const uint4 v = Ts[(r - kTB) * 32 + lane];
               acc.x |= v.x;
               acc.y |= v.y;
               acc.z |= v.z;

@@ -673,23 +673,24 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     double top_per_row = 0;
     for (uint32_t r = 0; r < kTabBits; ++r) top_per_row += (double)top_rank_rows[r] / (double)D;
     const std::string hv = hot_impl ? hot_impl : "";
-    const bool force_tab = hv == "tab" || hv == "trie" || hv == "jt";
+    const bool force_tab = hv == "tab" || hv == "trie";
     const bool tab = K > kTabBits && tsm <= (size_t)dense_smem_bytes(X) &&
                      !(hot_impl && std::string(hot_impl) == "rec") &&
                      (force_tab || top_per_row >= 1.5);
     DBuf<uint4> rec = X.zeros<uint4>(2 * D);
     DBuf<uint32_t> rcnt = X.alloc<uint32_t>(D);
-    // with the table: the jump-table kernel by default; D3G_HOT=tab|trie select
-    // the guarded-step kernel or the prefix-shared one (kept for comparison)
-    const bool jt = tab && hv != "tab" && hv != "trie";
-    // prefix-shared rows with the jump-table kernel by default (D3G_HOT=jt
-    // keeps the dense-row order); D3G_HOT=trie runs the standalone
-    // prefix-shared kernel (comparison)
-    jt_trie = jt && hv != "jt";
-    trie = tab && (hv == "trie" || jt_trie);
+    // the jump-table kernel by default, with or without the subset table;
+    // D3G_HOT=tab|trie|rec select the guarded-step table kernel, the standalone
+    // prefix-shared kernel or the guarded-step record kernel (comparison)
+    const bool jt = hv != "tab" && hv != "trie" && hv != "rec";
+    // prefix-shared rows by default with the table (D3G_HOT=jt keeps the
+    // dense-row order; D3G_HOT=jttrie forces them without the table, where
+    // they measured slower: cfg4 23.2 vs 17.2 ms)
+    jt_trie = jt && ((tab && hv != "jt") || hv == "jttrie");
+    trie = jt_trie || (tab && hv == "trie");
     D3G_LAUNCH(X, hot_rec_kernel, grid_for(D, 256), 256, 0, in.dl_ptr, in.dl_col, D, K,
                tab ? kTabBits : 0u, reinterpret_cast<uint8_t*>(rec.p), rcnt.p, in.row_sp,
-               jt ? kTabBits : 0u);
+               jt && tab ? kTabBits : 0u);
     // prefix-shared records: rows sorted by (subset, r1, r2), records gathered
     DBuf<uint32_t> perm;
     if (trie) {
@@ -697,7 +698,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
       perm = X.alloc<uint32_t>(D);
       D3G_LAUNCH(X, trie_key_kernel, grid_for(D, 256), 256, 0, reinterpret_cast<const uint8_t*>(rec.p),
                  rcnt.p, D, key.p, perm.p, jt ? 1u : 1u - kTabBits);
-      radix_sort(X, key.p, perm.p, D, 23, true);
+      radix_sort(X, key.p, perm.p, D, 25, true);
       DBuf<uint4> rec_s = X.alloc<uint4>(2 * D);
       DBuf<uint32_t> rcnt_s = X.alloc<uint32_t>(D);
       D3G_LAUNCH(X, trie_gather_kernel, grid_for(D, 256), 256, 0, rec.p, rcnt.p, key.p, perm.p, D,
@@ -705,7 +706,8 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
       rec = std::move(rec_s);
       rcnt = std::move(rcnt_s);
       if (jt_trie)
-        D3G_LAUNCH(X, trie_lds_kernel, grid_for(D, 256), 256, 0, rcnt.p, D, hp.z_chunks, lds_units);
+        D3G_LAUNCH(X, trie_lds_kernel, grid_for(D, 256), 256, 0, rcnt.p, D, hp.z_chunks,
+                   tab ? 1u : 0u, lds_units);
     } else {
       // algorithmic LDS traffic: every (row, batch) reads its listed slices plus
       // (tab) one subset-table entry, 512 B each
@@ -716,15 +718,22 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     D3G_CUDA(cudaEventRecord(ev0, X.stream));
     with_mode(mode, [&](auto M) {
       if (jt) {
+        // without the table: K listed rows plus one (zero) subset row
+        const size_t jsm = tab ? tsm : (size_t)(K + 1) * 32 * 16;
         auto run = [&](auto kfn) {
-          D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
-          D3G_LAUNCH(X, kfn, g, kHotThreads, tsm, hp, in.dl_ptr, in.dl_col, rec.p, rcnt.p, perm.p,
+          D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jsm));
+          D3G_LAUNCH(X, kfn, g, kHotThreads, jsm, hp, in.dl_ptr, in.dl_col, rec.p, rcnt.p, perm.p,
                      dec, em, t, cnt_sp);
         };
-        if (jt_trie)
-          run(dense_hot_jt_kernel<decltype(M)::value, true>);
+        constexpr int Md = decltype(M)::value;
+        if (tab && jt_trie)
+          run(dense_hot_jt_kernel<Md, true, true>);
+        else if (tab)
+          run(dense_hot_jt_kernel<Md, false, true>);
+        else if (jt_trie)
+          run(dense_hot_jt_kernel<Md, true, false>);
         else
-          run(dense_hot_jt_kernel<decltype(M)::value, false>);
+          run(dense_hot_jt_kernel<Md, false, false>);
       } else if (trie) {
         // the kernel counts its own slice reads (over every batch)
         auto kfn = dense_hot_trie_kernel<decltype(M)::value>;
