@@ -395,16 +395,25 @@ def main():
         # answers the heavy sparse side): bound by shared-memory bandwidth
         achieved = hot_bytes / (hot_ms * 1e-3) / 1e9
         smem = d3.smem_peak(ctx) / 1e9
-        roof = {"kernel": "DenseEC P1 hot bit-sliced pass (dense_hot_tab_kernel / "
-                          "dense_hot_rec_kernel)",
+        unshared = r0.hot_lds_bytes_unshared or hot_bytes
+        roof = {"kernel": "DenseEC P1 hot bit-sliced pass (dense_hot_jt_kernel: jump table over "
+                          "the listed ranks, prefix-shared sorted rows)",
                 "bound": "smem", "achieved": achieved, "peak": smem, "unit": "GB/s",
                 "frac": achieved / smem, "traffic": _ncu_dram_bytes(cfg_id),
-                "work": f"algorithmic LDS bytes = 512 B x (subset-table read + listed hot ranks) "
-                        f"per (dense row, 4096-x batch) = {hot_bytes:.4g} B per launch; "
+                "work": f"LDS bytes issued = 512 B per slice read: (subset-table entry unless "
+                        f"shared with the previous sorted row + listed hot ranks past the shared "
+                        f"prefix) per (dense row, 4096-x batch) = {hot_bytes:.4g} B per launch; "
                         f"kernel time {hot_ms:.3f} ms (CUDA events on the library stream)",
                 "peak_source": "measured conflict-free LDS.128 bandwidth (d3g_smem_peak) in this "
                                "run",
-                "share_of_step": hot_ms / phase["ms_total"]}
+                "share_of_step": hot_ms / phase["ms_total"],
+                "unshared": {"bytes": unshared,
+                             "effective_GBs": unshared / (hot_ms * 1e-3) / 1e9,
+                             "effective_frac": unshared / (hot_ms * 1e-3) / 1e9 / smem,
+                             "note": "the same pass without prefix sharing (every row reads its "
+                                     "subset entry and all listed slices); the sharing removes "
+                                     "the difference, so the kernel is issue-bound rather than "
+                                     "smem-bound (ncu: profiles/)"}}
         ach_pd = p_dense / (phase["ms_dense"] * 1e-3) if phase["ms_dense"] else 0.0
         if p_dense:
             roof["survey_unit"] = {

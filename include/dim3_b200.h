@@ -125,6 +125,9 @@ typedef struct {
    * (row, batch, slice read)), the roofline inputs. */
   double ms_dense_hot;
   uint64_t hot_lds_bytes;
+  /* the same pass without the prefix sharing of sorted rows (every row reads
+   * its subset entry and all listed slices): the work the sharing removed */
+  uint64_t hot_lds_bytes_unshared;
 } d3g_report;
 
 /* Materialized output: caller-owned host (or device, on_device != 0)

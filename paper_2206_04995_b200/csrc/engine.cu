@@ -138,6 +138,7 @@ struct KernelOut {
   uint64_t count_sp = 0;      // pairs of rows flagged in DenseInputs::row_sp
   double ms_hot = 0;          // CUDA-event time of the hot-pass launch
   uint64_t hot_lds_bytes = 0;  // its algorithmic shared-memory bytes
+  uint64_t hot_lds_bytes_unshared = 0;  // without the prefix sharing
 };
 
 template <class F>
@@ -482,7 +483,7 @@ __global__ void rec_sum_kernel(const uint32_t* __restrict__ rcnt, uint64_t n, ui
   uint64_t acc = 0;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x)
-    acc += (rcnt[i] & 0xffffffu) + add;
+    acc += (rcnt[i] & 0x3fffffu) + add;
   acc = d3g::warp_sum(acc);
   if (d3g::lane_id() == 0 && acc) atomicAdd(out, (unsigned long long)acc);
 }
@@ -635,7 +636,8 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   hp.work = work.p;
   // [hot tally | cold tally | hot-pass LDS units]: read back once at the end
   // [hot | cold | LDS units | pairs of folded sparse rows]
-  DBuf<Tally> tallies = X.zeros<Tally>(4);
+  // [.. | slice reads without prefix sharing]
+  DBuf<Tally> tallies = X.zeros<Tally>(5);
   Tally* t = tallies.p;
   unsigned long long* lds_units = &tallies.p[2].count;
   unsigned long long* cnt_sp = in.row_sp ? &tallies.p[3].count : nullptr;
@@ -705,9 +707,12 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
                  rec_s.p, rcnt_s.p);
       rec = std::move(rec_s);
       rcnt = std::move(rcnt_s);
-      if (jt_trie)
+      if (jt_trie) {
         D3G_LAUNCH(X, trie_lds_kernel, grid_for(D, 256), 256, 0, rcnt.p, D, hp.z_chunks,
                    tab ? 1u : 0u, lds_units);
+        D3G_LAUNCH(X, rec_sum_kernel, grid_for(D, 256), 256, 0, rcnt.p, D, tab ? 1u : 0u,
+                   &tallies.p[4].count);
+      }
     } else {
       // algorithmic LDS traffic: every (row, batch) reads its listed slices plus
       // (tab) one subset-table entry, 512 B each
@@ -816,8 +821,8 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
       run_sparse(X, si, dec, mode, em, cold, flt);
     }
   }
-  Tally th[4];
-  X.to_host(th, tallies.p, 4);
+  Tally th[5];
+  X.to_host(th, tallies.p, 5);
   out.count_sp = th[3].count;
   const Tally& h = th[0];
   if (cold_kernel_ok && e[best] > 0) {
@@ -832,6 +837,8 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     cudaEventDestroy(ev1);
     out.ms_hot = ms;
     out.hot_lds_bytes = th[2].count * (trie && !jt_trie ? 1ull : (uint64_t)n_batches) * 512ull;
+    out.hot_lds_bytes_unshared =
+        jt_trie ? th[4].count * (uint64_t)n_batches * 512ull : out.hot_lds_bytes;
   }
   if (std::getenv("D3G_TRACE"))
     std::fprintf(stderr, "[dense_hot] D=%llu live=%llu K=%u hot=%llu cold=%llu cold_path=%s over=%llu\n",
@@ -1904,6 +1911,7 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   rep->pairs_dense = kd.count;
   rep->ms_dense_hot = ks.ms_hot + kd.ms_hot;
   rep->hot_lds_bytes = ks.hot_lds_bytes + kd.hot_lds_bytes;
+  rep->hot_lds_bytes_unshared = ks.hot_lds_bytes_unshared + kd.hot_lds_bytes_unshared;
   rep->spa_inner_count = outj_sp;
   rep->out_p = ks.count + kd.count;
   rep->checksum_sum = ks.sum + kd.sum;
