@@ -128,6 +128,9 @@ typedef struct {
   /* the same pass without the prefix sharing of sorted rows (every row reads
    * its subset entry and all listed slices): the work the sharing removed */
   uint64_t hot_lds_bytes_unshared;
+  /* count-only: (x, z) pairs counted as hits without a test by the rank-0
+   * split (x and z both hold the top-ranked y) */
+  uint64_t hot_direct_pairs;
 } d3g_report;
 
 /* Materialized output: caller-owned host (or device, on_device != 0)

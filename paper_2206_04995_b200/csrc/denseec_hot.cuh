@@ -33,7 +33,72 @@ struct HotParams {
   uint32_t batch;          // groups per smem batch
   uint32_t z_chunks;       // z ranges per batch (units = batches * z_chunks)
   unsigned int* work;
+  // rank-0 split (count-only): batches >= first_a_batch hold only x with the
+  // top rank and test only the first n_dense_a rows (the rows without it),
+  // in za_chunks ranges per batch; every other (batch, row) pair is a hit
+  uint32_t first_a_batch = ~0u;
+  uint32_t za_chunks = 1;
+  uint64_t n_dense_a = 0;
 };
+
+// Unit -> (batch, row range). Units are batch-major: the first_a_batch
+// full batches (z_chunks ranges over all rows), then the A batches.
+__device__ __forceinline__ void hot_unit(const HotParams& p, uint32_t n_batches, uint32_t unit,
+                                         uint32_t& bi, uint64_t& z_lo, uint64_t& z_hi) {
+  const uint32_t fb = p.first_a_batch < n_batches ? p.first_a_batch : n_batches;
+  const uint32_t nbu = fb * p.z_chunks;
+  if (unit < nbu) {
+    bi = unit / p.z_chunks;
+    const uint32_t zc = unit % p.z_chunks;
+    z_lo = p.n_dense * zc / p.z_chunks;
+    z_hi = p.n_dense * (zc + 1) / p.z_chunks;
+  } else {
+    const uint32_t u = unit - nbu;
+    bi = fb + u / p.za_chunks;
+    const uint32_t zc = u % p.za_chunks;
+    z_lo = p.n_dense_a * zc / p.za_chunks;
+    z_hi = p.n_dense_a * (zc + 1) / p.za_chunks;
+  }
+}
+
+__device__ __forceinline__ uint32_t hot_units(const HotParams& p, uint32_t n_batches) {
+  const uint32_t fb = p.first_a_batch < n_batches ? p.first_a_batch : n_batches;
+  return fb * p.z_chunks + (n_batches - fb) * p.za_chunks;
+}
+
+// 1 if live x (in xorder) holds y0 = y_of_rank[0] (rows are sorted by y).
+__global__ void rank0_flag_kernel(const uint32_t* __restrict__ xorder, uint64_t n_live,
+                                  const uint64_t* __restrict__ r_ptr,
+                                  const uint32_t* __restrict__ r_col,
+                                  const uint32_t* __restrict__ y_of_rank,
+                                  uint32_t* __restrict__ not_a) {
+  const uint32_t y0 = y_of_rank[0];
+  for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n_live;
+       p += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t x = xorder[p];
+    uint64_t lo = r_ptr[x], hi = r_ptr[x + 1];
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (r_col[mid] < y0) lo = mid + 1; else hi = mid;
+    }
+    const bool has = lo < r_ptr[x + 1] && r_col[lo] == y0;
+    not_a[p] = has ? 0u : 1u;
+  }
+}
+
+// Stable split of xorder: x without the top rank first (pos_b = exclusive
+// scan of not_a), then the others in order.
+__global__ void rank0_split_kernel(const uint32_t* __restrict__ xorder, uint64_t n_live,
+                                   const uint32_t* __restrict__ not_a,
+                                   const uint64_t* __restrict__ pos_b,
+                                   uint32_t* __restrict__ out) {
+  const uint64_t nb = pos_b[n_live];
+  for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n_live;
+       p += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t b = pos_b[p];
+    out[not_a[p] ? b : nb + (p - b)] = xorder[p];
+  }
+}
 
 // T, hx from the live x in degree order: warp per x position.
 __global__ void hot_build_x_kernel(const uint32_t* __restrict__ xorder, uint64_t n_live,
@@ -647,6 +712,17 @@ dense_hot_tab_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
   tally_flush(tally, cnt, sum, xr);
 }
 
+// Rows in [lo, hi) flagged as folded sparse rows (bit 31 of the count word).
+__global__ void sp_rows_kernel(const uint32_t* __restrict__ rcnt, uint64_t lo, uint64_t hi,
+                               unsigned long long* __restrict__ out) {
+  uint64_t acc = 0;
+  for (uint64_t i = lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hi;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    acc += rcnt[i] >> 31;
+  acc = warp_sum(acc);
+  if (lane_id() == 0 && acc) atomicAdd(out, (unsigned long long)acc);
+}
+
 // Sort key of a record for the prefix-shared kernels: (subset mask, first
 // listed rank + 1, second listed rank + 1; 7/9/9 bits), 0 = absent.
 __global__ void trie_key_kernel(const uint8_t* __restrict__ rec, const uint32_t* __restrict__ rcnt,
@@ -657,7 +733,8 @@ __global__ void trie_key_kernel(const uint8_t* __restrict__ rec, const uint32_t*
     const uint32_t cw = rcnt[i], c = cw & 0xffffffu;
     const uint32_t r1 = c >= 1 ? rec[i * 32] + off : 0u;
     const uint32_t r2 = c >= 2 ? rec[i * 32 + 1] + off : 0u;
-    key[i] = ((uint64_t)((cw >> 24) & 0x7fu) << 18) | (r1 << 9) | r2;
+    const uint32_t top = (cw >> 24) & 0x7fu;  // rank 0 first: rows without it sort first
+    key[i] = ((uint64_t)(top & 1u) << 24) | ((uint64_t)(top >> 1) << 18) | (r1 << 9) | r2;
     idx[i] = (uint32_t)i;
   }
 }
@@ -915,7 +992,8 @@ dense_hot_trie_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
 // rows: (L == 0) + c - max(L - 1, 0), with L forced to 0 on the first row of
 // each warp step (positions z_lo + 32k of the row's z chunk).
 __global__ void trie_lds_kernel(const uint32_t* __restrict__ rcnt, uint64_t n, uint32_t z_chunks,
-                                uint32_t sub_read, unsigned long long* __restrict__ out) {
+                                uint32_t sub_read, unsigned long long* __restrict__ out,
+                                uint64_t mult = 1, uint32_t shared = 1) {
   uint64_t acc = 0;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
@@ -924,11 +1002,11 @@ __global__ void trie_lds_kernel(const uint32_t* __restrict__ rcnt, uint64_t n, u
     while (zc > 0 && n * zc / z_chunks > i) --zc;
     const uint64_t z_lo = n * zc / z_chunks;
     const uint32_t cw = rcnt[i], c = cw & kTrieCntMask;
-    const uint32_t L = ((i - z_lo) % 32 == 0) ? 0u : (cw >> 22) & 3u;
+    const uint32_t L = (!shared || (i - z_lo) % 32 == 0) ? 0u : (cw >> 22) & 3u;
     acc += (L == 0 ? sub_read : 0u) + c - (L > 1 ? L - 1 : 0u);
   }
   acc = warp_sum(acc);
-  if (lane_id() == 0 && acc) atomicAdd(out, (unsigned long long)acc);
+  if (lane_id() == 0 && acc) atomicAdd(out, (unsigned long long)(acc * mult));
 }
 
 template <int kMode, bool kTrie, bool kTab = true>
@@ -942,7 +1020,7 @@ dense_hot_jt_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
   __shared__ unsigned int s_unit;
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const uint32_t n_batches = (p.groups + 31) / 32;
-  const unsigned int n_units = n_batches * p.z_chunks;
+  const unsigned int n_units = hot_units(p, n_batches);
   constexpr uint32_t kTB = kTab ? kTabBits : 0u;  // ranks in the subset table
   const uint32_t n_listed = p.K - kTB;
   uint4* const sub_tab = Ts + n_listed * 32;  // entry e at sub_tab[e * 32 + lane]
@@ -994,7 +1072,9 @@ dense_hot_jt_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
     __syncthreads();
     const unsigned int unit = s_unit;
     if (unit >= n_units) break;
-    const uint32_t bi = unit / p.z_chunks, zc_i = unit % p.z_chunks;
+    uint32_t bi;
+    uint64_t z_lo, z_hi;
+    hot_unit(p, n_batches, unit, bi, z_lo, z_hi);
     if ((int)bi != cur_batch) {
       if (threadIdx.x == 0) {
         const uint4* src = p.T + (uint64_t)bi * p.K * 32;
@@ -1019,7 +1099,6 @@ dense_hot_jt_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
     }
     const uint32_t g = bi * 32 + lane;
     const uint64_t gp0 = (uint64_t)g * 128;
-    const uint64_t z_lo = p.n_dense * zc_i / p.z_chunks, z_hi = p.n_dense * (zc_i + 1) / p.z_chunks;
     uint64_t cb = z_lo + (uint64_t)warp * 32;
     uint4 na = zero4, nb = zero4;
     uint32_t nc = 0;

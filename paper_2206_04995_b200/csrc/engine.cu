@@ -139,6 +139,7 @@ struct KernelOut {
   double ms_hot = 0;          // CUDA-event time of the hot-pass launch
   uint64_t hot_lds_bytes = 0;  // its algorithmic shared-memory bytes
   uint64_t hot_lds_bytes_unshared = 0;  // without the prefix sharing
+  uint64_t split_direct_pairs = 0;  // hits counted without a test (rank-0 split)
 };
 
 template <class F>
@@ -575,6 +576,44 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   // the cold kernels read 256-bit hot signatures: keep that layout for K < 256
   const uint32_t kw = cold_kernel_ok ? 4u : (K + 63) / 64;
   const uint32_t n_batches = (groups + 31) / 32;
+  // Rank-0 split (count-only; the table kernel with prefix-shared rows): an x
+  // holding the top rank y_of_rank[0] hits every dense row that holds it.
+  // Live x are split stably into B (without it) then A (with it); batches made
+  // only of A x test only the rows without the top rank (sorted first), and
+  // their other pairs are counted as hits without a test. cfg5: 95% of x and
+  // rows hold rank 0, so ~10x fewer (batch, row) tests; cfg2: ~4x.
+  const char* hot_sel_env = std::getenv("D3G_HOT");
+  const std::string hot_sel = hot_sel_env ? hot_sel_env : "";
+  double top_rows = 0;
+  for (uint32_t r = 0; r < kTabBits; ++r) top_rows += (double)top_rank_rows[r] / (double)D;
+  const bool tab_planned = K <= 256 && K > kTabBits && hot_sel.empty() &&
+                           (size_t)(kTabRows + K - kTabBits) * 32 * 16 <= (size_t)dense_smem_bytes(X) &&
+                           top_rows >= 1.5;
+  const uint64_t rows_r0 = std::min<uint64_t>(top_rank_rows[0], D);
+  const uint64_t d_not0 = D - rows_r0;
+  uint32_t first_a_batch = n_batches;  // no split
+  uint64_t n_a_direct = 0;             // x in pure-A batches
+  DBuf<uint32_t> xsplit;
+  if (tab_planned && mode == kModeCount && rows_r0 > 0 && std::getenv("D3G_NO_SPLIT") == nullptr) {
+    DBuf<uint32_t> not_a = X.alloc<uint32_t>(n_live);
+    D3G_LAUNCH(X, rank0_flag_kernel, grid_for(n_live, 256), 256, 0, xorder, n_live, in.r_ptr,
+               in.r_col, in.y_of_rank, not_a.p);
+    DBuf<uint64_t> pos_b = X.alloc<uint64_t>(n_live + 1);
+    exclusive_scan<uint32_t>(X, not_a.p, n_live, pos_b.p);
+    const uint64_t n_b = X.scalar(pos_b.p + n_live);
+    const uint32_t fb = (uint32_t)((n_b + 4095) / 4096);
+    const uint64_t a_direct = n_live > (uint64_t)fb * 4096 ? n_live - (uint64_t)fb * 4096 : 0;
+    const double full = (double)n_batches * (double)D;
+    const double part = (double)fb * (double)D + (double)(n_batches - fb) * (double)d_not0;
+    if (a_direct > 0 && part < 0.8 * full) {
+      xsplit = X.alloc<uint32_t>(n_live);
+      D3G_LAUNCH(X, rank0_split_kernel, grid_for(n_live, 256), 256, 0, xorder, n_live, not_a.p,
+                 pos_b.p, xsplit.p);
+      xorder = xsplit.p;
+      first_a_batch = fb;
+      n_a_direct = a_direct;
+    }
+  }
   // hot structures
   DBuf<uint4> T = X.zeros<uint4>((uint64_t)n_batches * K * 32);
   DBuf<unsigned long long> hx = X.zeros<unsigned long long>(in.x_card * kw);
@@ -630,21 +669,34 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   hp.K = K;
   hp.kw = kw;
   hp.batch = 32;
+  const uint32_t n_full_b = std::max<uint32_t>(1, std::min(first_a_batch, n_batches));
   hp.z_chunks = std::max<uint32_t>(1, (uint32_t)std::min<uint64_t>(
-      (D + 255) / 256, ((uint64_t)X.sm_count * 8 + n_batches - 1) / n_batches));
+      (D + 255) / 256, ((uint64_t)X.sm_count * 8 + n_full_b - 1) / n_full_b));
+  if (first_a_batch < n_batches) {
+    const uint32_t n_a_b = n_batches - first_a_batch;
+    hp.first_a_batch = first_a_batch;
+    hp.n_dense_a = d_not0;
+    hp.za_chunks = std::max<uint32_t>(1, (uint32_t)std::min<uint64_t>(
+        (d_not0 + 255) / 256, ((uint64_t)X.sm_count * 8 + n_a_b - 1) / n_a_b));
+  }
   DBuf<unsigned int> work = X.zeros<unsigned int>(1);
   hp.work = work.p;
   // [hot tally | cold tally | hot-pass LDS units]: read back once at the end
   // [hot | cold | LDS units | pairs of folded sparse rows]
   // [.. | slice reads without prefix sharing]
-  DBuf<Tally> tallies = X.zeros<Tally>(5);
+  // [.. | folded sparse rows among the rows with the top rank (split)]
+  DBuf<Tally> tallies = X.zeros<Tally>(6);
   Tally* t = tallies.p;
   unsigned long long* lds_units = &tallies.p[2].count;
   unsigned long long* cnt_sp = in.row_sp ? &tallies.p[3].count : nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool trie = false, jt_trie = false;
   size_t sm = (size_t)K * 32 * 16;
-  unsigned g = (unsigned)std::min<uint64_t>((uint64_t)n_batches * hp.z_chunks, (uint64_t)X.sm_count);
+  const uint64_t n_units = first_a_batch < n_batches
+                              ? (uint64_t)first_a_batch * hp.z_chunks +
+                                    (uint64_t)(n_batches - first_a_batch) * hp.za_chunks
+                              : (uint64_t)n_batches * hp.z_chunks;
+  unsigned g = (unsigned)std::min<uint64_t>(n_units, (uint64_t)X.sm_count);
   const char* hot_impl = std::getenv("D3G_HOT");
   const bool use_tc = hot_impl && std::string(hot_impl) == "tc" && mode == kModeCount &&
                       K % 32 == 0 && K <= 384;
@@ -676,7 +728,8 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     for (uint32_t r = 0; r < kTabBits; ++r) top_per_row += (double)top_rank_rows[r] / (double)D;
     const std::string hv = hot_impl ? hot_impl : "";
     const bool force_tab = hv == "tab" || hv == "trie";
-    const bool tab = K > kTabBits && tsm <= (size_t)dense_smem_bytes(X) &&
+    const bool tab = first_a_batch < n_batches ||
+                     K > kTabBits && tsm <= (size_t)dense_smem_bytes(X) &&
                      !(hot_impl && std::string(hot_impl) == "rec") &&
                      (force_tab || top_per_row >= 1.5);
     DBuf<uint4> rec = X.zeros<uint4>(2 * D);
@@ -708,10 +761,21 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
       rec = std::move(rec_s);
       rcnt = std::move(rcnt_s);
       if (jt_trie) {
-        D3G_LAUNCH(X, trie_lds_kernel, grid_for(D, 256), 256, 0, rcnt.p, D, hp.z_chunks,
-                   tab ? 1u : 0u, lds_units);
-        D3G_LAUNCH(X, rec_sum_kernel, grid_for(D, 256), 256, 0, rcnt.p, D, tab ? 1u : 0u,
-                   &tallies.p[4].count);
+        // slice reads of every (batch, row) the kernel tests, with and without
+        // the prefix sharing
+        const uint32_t fb = std::min(first_a_batch, n_batches);
+        for (uint32_t shared = 0; shared < 2; ++shared) {
+          unsigned long long* dst = shared ? lds_units : &tallies.p[4].count;
+          if (fb)
+            D3G_LAUNCH(X, trie_lds_kernel, grid_for(D, 256), 256, 0, rcnt.p, D, hp.z_chunks,
+                       tab ? 1u : 0u, dst, (uint64_t)fb, shared);
+          if (fb < n_batches && d_not0)
+            D3G_LAUNCH(X, trie_lds_kernel, grid_for(d_not0, 256), 256, 0, rcnt.p, d_not0,
+                       hp.za_chunks, tab ? 1u : 0u, dst, (uint64_t)(n_batches - fb), shared);
+        }
+        if (fb < n_batches && cnt_sp)
+          D3G_LAUNCH(X, sp_rows_kernel, grid_for(rows_r0, 256), 256, 0, rcnt.p, d_not0, D,
+                     &tallies.p[5].count);
       }
     } else {
       // algorithmic LDS traffic: every (row, batch) reads its listed slices plus
@@ -821,9 +885,11 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
       run_sparse(X, si, dec, mode, em, cold, flt);
     }
   }
-  Tally th[5];
-  X.to_host(th, tallies.p, 5);
-  out.count_sp = th[3].count;
+  Tally th[6];
+  X.to_host(th, tallies.p, 6);
+  // pairs of pure-A batches with the rows holding the top rank: hits, untested
+  const uint64_t direct = first_a_batch < n_batches ? n_a_direct * rows_r0 : 0;
+  out.count_sp = th[3].count + (first_a_batch < n_batches ? n_a_direct * th[5].count : 0);
   const Tally& h = th[0];
   if (cold_kernel_ok && e[best] > 0) {
     cold.count = th[1].count;
@@ -836,9 +902,11 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     cudaEventDestroy(ev0);
     cudaEventDestroy(ev1);
     out.ms_hot = ms;
-    out.hot_lds_bytes = th[2].count * (trie && !jt_trie ? 1ull : (uint64_t)n_batches) * 512ull;
-    out.hot_lds_bytes_unshared =
-        jt_trie ? th[4].count * (uint64_t)n_batches * 512ull : out.hot_lds_bytes;
+    // jump-table kernel with prefix sharing / standalone trie kernel: the
+    // counters already cover every batch
+    out.hot_lds_bytes = th[2].count * (trie ? 1ull : (uint64_t)n_batches) * 512ull;
+    out.hot_lds_bytes_unshared = jt_trie ? th[4].count * 512ull : out.hot_lds_bytes;
+    out.split_direct_pairs = n_a_direct * rows_r0;
   }
   if (std::getenv("D3G_TRACE"))
     std::fprintf(stderr, "[dense_hot] D=%llu live=%llu K=%u hot=%llu cold=%llu cold_path=%s over=%llu\n",
@@ -846,7 +914,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
                  (unsigned long long)cold.count,
                  cold_bitmap ? "bitmap" : cold_hash ? "hash" : "tiers",
                  (unsigned long long)out.cold_overflow);
-  out.count = h.count + cold.count;
+  out.count = h.count + direct + cold.count;
   out.sum = h.sum + cold.sum;
   out.xr = h.xr ^ cold.xr;
   out.inner = K;  // reported as the hot width (diagnostics)
@@ -1823,7 +1891,11 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   const uint64_t outj_sp = P.outj_sparse;
   const bool heavy_sparse = std::getenv("D3G_SPARSE_TIERS") == nullptr && x_live > 0 &&
                             n_sparse > 0 && outj_sp > 4096ull * x_live;
-  const bool default_engine = std::getenv("D3G_HOT") == nullptr &&
+  // folded rows need the record-based hot kernels and the cold kernels
+  const char* hot_env = std::getenv("D3G_HOT");
+  const std::string hot_sel = hot_env ? hot_env : "";
+  const bool default_engine = (hot_sel.empty() || hot_sel == "jt" || hot_sel == "jttrie" ||
+                               hot_sel == "tab" || hot_sel == "rec") &&
                               std::getenv("D3G_COLD") == nullptr &&
                               std::getenv("D3G_DENSE") == nullptr;
   const bool fold = heavy_sparse && n_dense > 0 && default_engine &&
@@ -1912,6 +1984,7 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   rep->ms_dense_hot = ks.ms_hot + kd.ms_hot;
   rep->hot_lds_bytes = ks.hot_lds_bytes + kd.hot_lds_bytes;
   rep->hot_lds_bytes_unshared = ks.hot_lds_bytes_unshared + kd.hot_lds_bytes_unshared;
+  rep->hot_direct_pairs = ks.split_direct_pairs + kd.split_direct_pairs;
   rep->spa_inner_count = outj_sp;
   rep->out_p = ks.count + kd.count;
   rep->checksum_sum = ks.sum + kd.sum;

@@ -223,7 +223,8 @@ class _Report(C.Structure):
                [(k, C.c_double) for k in _REPORT_MS] + [("gpu_launches", C.c_uint64)] + \
                [("pairs_classical", C.c_uint64), ("intermediate_pairs", C.c_uint64),
                 ("ms_classical", C.c_double), ("ms_dense_hot", C.c_double),
-                ("hot_lds_bytes", C.c_uint64), ("hot_lds_bytes_unshared", C.c_uint64)]
+                ("hot_lds_bytes", C.c_uint64), ("hot_lds_bytes_unshared", C.c_uint64),
+                ("hot_direct_pairs", C.c_uint64)]
 
 
 class _Pairs(C.Structure):
@@ -419,6 +420,7 @@ class ExecutionReport:
     ms_dense_hot: float = 0.0
     hot_lds_bytes: int = 0
     hot_lds_bytes_unshared: int = 0
+    hot_direct_pairs: int = 0
 
     def to_kv(self):
         """Insertion-ordered key/value view with the reference's key names

@@ -310,3 +310,43 @@ def test_self_join_reuses_the_csr_and_matches(monkeypatch):
         c = d3.join_project(t, t, d3.EngineConfig(force=d3.Strategy.hybrid), C)
         assert c.report.h2d_bytes == 16 * len(r[0])
         assert pair_set(c.result.raw_x, c.result.raw_z) == want
+
+
+def test_rank0_split_count_only_cfg2(monkeypatch):
+    """Count-only runs split the live x by the top-ranked y: pairs of x and z
+    that both hold it are counted without a test. cfg2 at full size: the
+    count and the reference's pairs_sparse/pairs_dense split are unchanged,
+    with and without the split (D3G_NO_SPLIT)."""
+    g = _golden()["cfg2"]
+    ref = g["ref_hybrid_report"]
+    rl, rr = d3.generate(2, 0)
+    sl, sr = d3.generate(2, 1)
+    e = d3.EngineConfig(force=d3.Strategy.auto_select, count_only=True,
+                        memory_budget_bytes=64 << 30)
+    a = d3.join_project(d3.RawTable(rl, rr), d3.RawTable(sl, sr), e, C).report
+    assert a.hot_direct_pairs > 0
+    assert a.out_p == g["set"]["count"]
+    assert (a.pairs_sparse, a.pairs_dense) == (ref["pairs_sparse"], ref["pairs_dense"])
+    monkeypatch.setenv("D3G_NO_SPLIT", "1")
+    b = d3.join_project(d3.RawTable(rl, rr), d3.RawTable(sl, sr), e, C).report
+    assert b.hot_direct_pairs == 0
+    assert (b.out_p, b.pairs_sparse, b.pairs_dense) == (a.out_p, a.pairs_sparse, a.pairs_dense)
+
+
+def test_rank0_split_count_only_cfg5_x_range():
+    """cfg5 (200M x 200M) restricted to x codes [0, 300000): the split
+    count-only run equals the checksum-mode run (which tests every pair)."""
+    import torch
+    rl, rr = d3.generate(5, 0)
+    sl, sr = d3.generate(5, 1)
+
+    def run(checksum):
+        e = d3.EngineConfig(force=d3.Strategy.auto_select, count_only=True, checksum=checksum,
+                            memory_budget_bytes=120 << 30, x_code_range=(0, 300000))
+        return d3.join_project(d3.RawTable(rl, rr), d3.RawTable(sl, sr), e, C).report
+
+    a, b = run(False), run(True)
+    assert a.hot_direct_pairs > 0 and b.hot_direct_pairs == 0
+    assert (a.out_p, a.pairs_sparse, a.pairs_dense) == (b.out_p, b.pairs_sparse, b.pairs_dense)
+    del rl, rr, sl, sr
+    torch.cuda.empty_cache()
