@@ -188,8 +188,9 @@ constexpr int kSortPerLane = 8;
 constexpr int kSortChunk = 32 * kSortPerLane;           // keys per warp
 constexpr int kSortTile = kSortWarps * kSortChunk;      // 2048 keys per block
 
+template <class KT = uint64_t>
 __global__ void __launch_bounds__(kSortThreads)
-radix_hist_kernel(const uint64_t* __restrict__ keys, uint64_t n, int shift, uint32_t n_tiles,
+radix_hist_kernel(const KT* __restrict__ keys, uint64_t n, int shift, uint32_t n_tiles,
                   uint32_t* __restrict__ hist) {
   __shared__ uint32_t cnt[256];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) cnt[i] = 0;
@@ -204,18 +205,18 @@ radix_hist_kernel(const uint64_t* __restrict__ keys, uint64_t n, int shift, uint
     hist[(uint64_t)d * n_tiles + blockIdx.x] = cnt[d];
 }
 
-template <bool kHasVals>
+template <bool kHasVals, class KT = uint64_t>
 __global__ void __launch_bounds__(kSortThreads)
-radix_scatter_kernel(const uint64_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
+radix_scatter_kernel(const KT* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
                      uint64_t n, int shift, uint32_t n_tiles,
                      const uint64_t* __restrict__ offsets,  // scanned hist, digit-major
-                     uint64_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out) {
+                     KT* __restrict__ keys_out, uint32_t* __restrict__ vals_out) {
   __shared__ uint32_t whist[kSortWarps][256];
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < kSortWarps * 256; i += blockDim.x) (&whist[0][0])[i] = 0;
   __syncthreads();
   const uint64_t chunk = (uint64_t)blockIdx.x * kSortTile + (uint64_t)warp * kSortChunk;
-  uint64_t k[kSortPerLane];
+  KT k[kSortPerLane];
   uint32_t v[kSortPerLane];
   uint32_t rank[kSortPerLane];
   const uint32_t lt = (1u << lane) - 1;
@@ -280,13 +281,13 @@ inline void radix_sort(Ctx& ctx, uint64_t* keys, uint32_t* vals, uint64_t n, int
   int passes = (bits + 7) / 8;
   for (int p = 0; p < passes; ++p) {
     int shift = 8 * p;
-    D3G_LAUNCH(ctx, radix_hist_kernel, n_tiles, kSortThreads, 0, kin, n, shift, n_tiles, hist.p);
+    D3G_LAUNCH(ctx, radix_hist_kernel<uint64_t>, n_tiles, kSortThreads, 0, kin, n, shift, n_tiles, hist.p);
     exclusive_scan<uint32_t>(ctx, hist.p, (uint64_t)256 * n_tiles, offs.p);
     if (vals)
-      D3G_LAUNCH(ctx, radix_scatter_kernel<true>, n_tiles, kSortThreads, 0, kin, vin, n, shift,
+      D3G_LAUNCH(ctx, (radix_scatter_kernel<true, uint64_t>), n_tiles, kSortThreads, 0, kin, vin, n, shift,
                  n_tiles, offs.p, kout, vout);
     else
-      D3G_LAUNCH(ctx, radix_scatter_kernel<false>, n_tiles, kSortThreads, 0, kin, vin, n, shift,
+      D3G_LAUNCH(ctx, (radix_scatter_kernel<false, uint64_t>), n_tiles, kSortThreads, 0, kin, vin, n, shift,
                  n_tiles, offs.p, kout, vout);
     std::swap(kin, kout);
     std::swap(vin, vout);
@@ -296,6 +297,23 @@ inline void radix_sort(Ctx& ctx, uint64_t* keys, uint32_t* vals, uint64_t n, int
       D3G_CUDA(cudaMemcpyAsync(keys, kin, n * 8, cudaMemcpyDeviceToDevice, ctx.stream));
     if (vals) D3G_CUDA(cudaMemcpyAsync(vals, vin, n * 4, cudaMemcpyDeviceToDevice, ctx.stream));
   }
+}
+
+// One stable 8-bit LSD pass over u32 (key, value) pairs: digit (key >> shift)
+// & 255. Used to bucket a large CSR build by its high row bits first, so the
+// per-row scatter that follows writes into an L2-sized window.
+inline void radix_pass_u32(Ctx& ctx, const uint32_t* keys, const uint32_t* vals, uint64_t n,
+                           int shift, uint32_t* keys_out, uint32_t* vals_out) {
+  if (n == 0) return;
+  if (n >= (1ull << 32)) throw ResourceError("radix_pass_u32: more than 2^32 keys");
+  const uint32_t n_tiles = (uint32_t)((n + kSortTile - 1) / kSortTile);
+  DBuf<uint32_t> hist = ctx.alloc<uint32_t>((uint64_t)256 * n_tiles);
+  DBuf<uint64_t> offs = ctx.alloc<uint64_t>((uint64_t)256 * n_tiles + 1);
+  D3G_LAUNCH(ctx, radix_hist_kernel<uint32_t>, n_tiles, kSortThreads, 0, keys, n, shift, n_tiles,
+             hist.p);
+  exclusive_scan<uint32_t>(ctx, hist.p, (uint64_t)256 * n_tiles, offs.p);
+  D3G_LAUNCH(ctx, (radix_scatter_kernel<true, uint32_t>), n_tiles, kSortThreads, 0, keys, vals, n,
+             shift, n_tiles, offs.p, keys_out, vals_out);
 }
 
 __global__ void index_compact_kernel(const uint32_t* __restrict__ flag,

@@ -1,0 +1,59 @@
+#!/usr/bin/env python
+"""Per-shard device time of an N-way x-shard split, each shard run alone on
+one B200 (this pool gives one GPU per call). With one process per GPU every
+rank holds the same inputs, builds the same replicated mapping / CSR /
+statistics / partition and runs its own x shard of SparseBMM + DenseEC with
+no cross-rank wait, so max over shards of the per-shard device time is what
+an N-GPU run spends per step (plus the broadcast of the inputs and the
+all-reduce of a few counters, not included). Prints one JSON line per config.
+
+  python scripts/shard_projection.py --config 5 --shards 1 2 4 8
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--shards", type=int, nargs="+", default=[1, 2, 4, 8])
+    ap.add_argument("--reps", type=int, default=2)
+    a = ap.parse_args()
+    import torch
+    import paper_2206_04995_b200 as d3
+    C = d3.CostConstants.test_consts()
+    rl, rr = d3.generate(a.config, 0)
+    sl, sr = d3.generate(a.config, 1)
+    R, S = d3.RawTable(rl, rr), d3.RawTable(sl, sr)
+    res = {"config": a.config, "shards": {}}
+    base = None
+    total = None
+    for n in a.shards:
+        per = []
+        cnt = 0
+        for k in range(n):
+            e = d3.EngineConfig(force=d3.Strategy.auto_select, count_only=True,
+                                memory_budget_bytes=150 << 30, shard_index=k, shard_count=n)
+            best = None
+            for _ in range(a.reps):
+                rep = d3.join_project(R, S, e, C).report
+                best = rep.ms_total if best is None else min(best, rep.ms_total)
+            per.append(best)
+            cnt += rep.out_p
+        if total is None:
+            total = cnt
+        assert cnt == total, (n, cnt, total)
+        worst = max(per)
+        base = worst if base is None else base
+        res["shards"][n] = {"max_ms": worst, "per_shard_ms": per,
+                            "speedup": base / worst, "out_p": cnt}
+        torch.cuda.empty_cache()
+    print(json.dumps(res))
+
+
+if __name__ == "__main__":
+    main()
