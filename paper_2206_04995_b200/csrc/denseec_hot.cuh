@@ -1478,7 +1478,7 @@ dense_cold_hash_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
                        Decode dec, Emit em, unsigned int* __restrict__ next,
                        uint32_t* __restrict__ over_x, unsigned int* __restrict__ over_n,
                        Tally* tally, const uint8_t* __restrict__ row_sp,
-                       unsigned long long* __restrict__ cnt_sp) {
+                       unsigned long long* __restrict__ cnt_sp, uint32_t ch_max = kCHMax) {
   extern __shared__ __align__(16) uint32_t chtab[];  // [kCHWarps][kCHSlots]
   const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
   uint32_t* tab = chtab + (uint64_t)w * kCHSlots;
@@ -1533,7 +1533,7 @@ dense_cold_hash_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
             }
           }
           inserted += __popc(__ballot_sync(0xffffffffu, fresh));
-          if (inserted > kCHMax) {
+          if (inserted > ch_max) {
             over = true;
             break;
           }
@@ -1564,9 +1564,15 @@ dense_cold_hash_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
 
 // Overflow x of dense_cold_hash_kernel: one CTA per x over a CTA-private
 // global bitmap of the dense rows (zero on entry and on exit: the candidate
-// stream is replayed to clear exactly the bits it set).
+// stream is replayed to clear exactly the bits it set). The (segment, entry)
+// space of x's y rows is flattened with a CTA-wide scan of the segment
+// lengths, so every thread takes one candidate per step however short the
+// cold segments are (per-y loops left most of the 512 threads idle).
+constexpr int kOvThreads = 512;
+constexpr uint32_t kOvTouched = 65536;  // touched-word list per CTA
+
 template <int kMode>
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(kOvThreads)
 dense_cold_overflow_kernel(const uint32_t* __restrict__ over_x, const unsigned int* __restrict__ over_n,
                            const uint64_t* __restrict__ r_ptr, const uint32_t* __restrict__ r_col,
                            const uint64_t* __restrict__ cptr, const uint32_t* __restrict__ ccol,
@@ -1574,7 +1580,16 @@ dense_cold_overflow_kernel(const uint32_t* __restrict__ over_x, const unsigned i
                            uint64_t y_card, uint32_t var_bits, const uint32_t* __restrict__ dl_z,
                            uint32_t* __restrict__ gbm, uint64_t words, Decode dec, Emit em,
                            Tally* tally, const uint8_t* __restrict__ row_sp,
-                           unsigned long long* __restrict__ cnt_sp) {
+                           unsigned long long* __restrict__ cnt_sp,
+                           uint32_t* __restrict__ touched /* [gridDim.x][kOvTouched] */) {
+  __shared__ uint64_t s_seg0[kOvThreads];
+  __shared__ uint32_t s_off[kOvThreads];
+  __shared__ uint32_t s_wsum[kOvThreads / 32];
+  __shared__ uint32_t s_total;
+  __shared__ unsigned int s_nt;  // bitmap words this x made non-zero (touched list)
+  uint32_t* tl = touched + (uint64_t)blockIdx.x * kOvTouched;
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  constexpr uint32_t kW = kOvThreads / 32;
   uint32_t* bm = gbm + (uint64_t)blockIdx.x * words;
   const uint32_t n = *over_n;
   uint64_t cnt = 0, sum = 0, xr = 0, csp = 0;
@@ -1584,11 +1599,60 @@ dense_cold_overflow_kernel(const uint32_t* __restrict__ over_x, const unsigned i
     ld256(hx4 + 2 * (uint64_t)x, a0, a1);
     const uint32_t v = a0.x & ((1u << var_bits) - 1);
     const uint64_t* cp = cptr + (uint64_t)v * y_card;
+    const uint64_t r0 = r_ptr[x], r1 = r_ptr[x + 1];
+    if (threadIdx.x == 0) s_nt = 0;
+    __syncthreads();
     for (int pass = 0; pass < 2; ++pass) {
-      for (uint64_t k = r_ptr[x]; k < r_ptr[x + 1]; ++k) {
-        const uint32_t y = r_col[k];
-        const uint64_t s0 = cp[y], s1 = cp[y + 1];
-        for (uint64_t t = s0 + threadIdx.x; t < s1; t += blockDim.x) {
+      if (pass == 1) {
+        // clear through the touched list; replay the stream only if it overflowed
+        const uint32_t nt = s_nt;
+        if (nt <= kOvTouched) {
+          for (uint32_t i = threadIdx.x; i < nt; i += kOvThreads) bm[tl[i]] = 0;
+          __syncthreads();
+          break;
+        }
+      }
+      for (uint64_t yb = r0; yb < r1; yb += kOvThreads) {
+        const uint64_t k = yb + threadIdx.x;
+        uint64_t sg0 = 0;
+        uint32_t len = 0;
+        if (k < r1) {
+          const uint32_t y = r_col[k];
+          sg0 = cp[y];
+          len = (uint32_t)(cp[y + 1] - sg0);
+        }
+        uint32_t incl = len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= (uint32_t)o) incl += u;
+        }
+        if (lane == 31) s_wsum[warp] = incl;
+        __syncthreads();
+        if (warp == 0) {
+          const uint32_t wv = lane < kW ? s_wsum[lane] : 0u;
+          uint32_t wi = wv;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= (uint32_t)o) wi += u;
+          }
+          if (lane < kW) s_wsum[lane] = wi - wv;  // exclusive over warps
+          if (lane == kW - 1) s_total = wi;
+        }
+        __syncthreads();
+        s_off[threadIdx.x] = s_wsum[warp] + incl - len;
+        s_seg0[threadIdx.x] = sg0;
+        __syncthreads();
+        const uint32_t total = s_total;
+        const uint32_t ny = (uint32_t)((r1 - yb) < kOvThreads ? (r1 - yb) : kOvThreads);
+        for (uint32_t f = threadIdx.x; f < total; f += kOvThreads) {
+          uint32_t lo = 0, hi = ny;  // last segment starting at or before f
+          while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (s_off[mid] <= f) lo = mid; else hi = mid;
+          }
+          const uint64_t t = s_seg0[lo] + (f - s_off[lo]);
           uint4 b0, b1;
           ld256(ch + 2 * t, b0, b1);
           const bool hot = ((a0.x & b0.x) | (a0.y & b0.y) | (a0.z & b0.z) | (a0.w & b0.w) |
@@ -1597,7 +1661,12 @@ dense_cold_overflow_kernel(const uint32_t* __restrict__ over_x, const unsigned i
           const uint32_t zl = ccol[t];
           if (pass == 0) {
             const uint32_t bit = 1u << (zl & 31);
-            if (atomicOr(&bm[zl >> 5], bit) & bit) continue;
+            const uint32_t old = atomicOr(&bm[zl >> 5], bit);
+            if (old & bit) continue;
+            if (old == 0) {
+              const unsigned int slot = atomicAdd(&s_nt, 1u);
+              if (slot < kOvTouched) tl[slot] = zl >> 5;
+            }
             ++cnt;
             if (row_sp && row_sp[zl]) ++csp;
             if (kMode != kModeCount) cold_account<kMode>(x, dl_z[zl], dec, em, sum, xr);
@@ -1605,6 +1674,7 @@ dense_cold_overflow_kernel(const uint32_t* __restrict__ over_x, const unsigned i
             bm[zl >> 5] = 0;
           }
         }
+        __syncthreads();  // s_off / s_seg0 are rewritten by the next chunk
       }
       __syncthreads();
     }

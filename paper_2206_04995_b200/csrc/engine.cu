@@ -501,6 +501,14 @@ __global__ void hot_small_stats_kernel(const uint32_t* __restrict__ cnt_rank,
     out[t] = (t - 7) < y_card ? dR[y_of_rank[t - 7]] : 0;
 }
 
+// Test/experiment override of a kernel limit: env value clamped to [lo, hi].
+static uint32_t env_u32(const char* name, uint32_t dflt, uint32_t lo, uint32_t hi) {
+  const char* v = std::getenv(name);
+  if (!v) return dflt;
+  const unsigned long x = std::strtoul(v, nullptr, 10);
+  return (uint32_t)std::min<unsigned long>(std::max<unsigned long>(x, lo), hi);
+}
+
 void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g::Emit em,
                    KernelOut& out) {
   using namespace d3g;
@@ -853,19 +861,24 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
           D3G_LAUNCH(X, kfn, (unsigned)X.sm_count * 3, kCHWarps * 32, hsm, xorder, n_live,
                      in.r_ptr, in.r_col, cptr.p, ccol.p, ch.p, reinterpret_cast<const uint4*>(hx.p),
                      Y, var_bits, in.dl_z, dec, em, next.p, over_x.p, over_n.p, tc, in.row_sp,
-                     cnt_sp);
+                     cnt_sp, env_u32("D3G_COLD_HASH_MAX", kCHMax, 1, kCHMax));
         });
         const unsigned int n_over = X.scalar(over_n.p);
         out.cold_overflow = n_over;
         if (n_over) {
-          const unsigned og = std::min<unsigned>(n_over, (unsigned)X.sm_count * 2);
+          // CTAs per SM: the candidate stream is latency-bound, more CTAs in
+          // flight win (cfg5: 1/SM 89 ms, 2/SM 62 ms)
           const uint64_t words = (D + 31) / 32;
+          const unsigned og = (unsigned)std::min<uint64_t>(
+              (uint64_t)n_over,
+              (uint64_t)X.sm_count * env_u32("D3G_OVERFLOW_CTAS_PER_SM", 4, 1, 16));
           DBuf<uint32_t> gbm = X.zeros<uint32_t>((uint64_t)og * words);
+          DBuf<uint32_t> touched = X.alloc<uint32_t>((uint64_t)og * kOvTouched);
           with_mode(mode, [&](auto M) {
-            D3G_LAUNCH(X, dense_cold_overflow_kernel<decltype(M)::value>, og, 512, 0, over_x.p,
+            D3G_LAUNCH(X, dense_cold_overflow_kernel<decltype(M)::value>, og, kOvThreads, 0, over_x.p,
                        over_n.p, in.r_ptr, in.r_col, cptr.p, ccol.p, ch.p,
                        reinterpret_cast<const uint4*>(hx.p), Y, var_bits, in.dl_z, gbm.p, words,
-                       dec, em, tc, in.row_sp, cnt_sp);
+                       dec, em, tc, in.row_sp, cnt_sp, touched.p);
           });
         }
       } else {

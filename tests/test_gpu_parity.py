@@ -350,3 +350,23 @@ def test_rank0_split_count_only_cfg5_x_range():
     assert (a.out_p, a.pairs_sparse, a.pairs_dense) == (b.out_p, b.pairs_sparse, b.pairs_dense)
     del rl, rr, sl, sr
     torch.cuda.empty_cache()
+
+
+def test_cfg5_cold_overflow_matches_reference(monkeypatch):
+    """cfg5's hash cold pass with its per-warp limit forced down, so that most
+    x overflow into the flattened global-bitmap kernel: the x<1000 slice still
+    equals the reference's."""
+    import torch
+    g = _golden().get("cfg5_x_lt_1000")
+    if g is None:
+        pytest.skip("golden entry not generated")
+    monkeypatch.setenv("D3G_COLD_HASH_MAX", "64")
+    rl, rr = d3.generate(5, 0)
+    sl, sr = d3.generate(5, 1)
+    e = d3.EngineConfig(force=d3.Strategy.auto_select, count_only=True, checksum=True,
+                        memory_budget_bytes=120 << 30, x_code_range=(0, 1000))
+    rep = d3.join_project(d3.RawTable(rl, rr), d3.RawTable(sl, sr), e, C).report
+    assert (rep.out_p, rep.checksum_sum, rep.checksum_xor) == \
+        (g["set"]["count"], g["set"]["sum"], g["set"]["xor"])
+    del rl, rr, sl, sr
+    torch.cuda.empty_cache()
