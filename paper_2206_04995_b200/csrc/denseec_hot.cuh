@@ -33,71 +33,102 @@ struct HotParams {
   uint32_t batch;          // groups per smem batch
   uint32_t z_chunks;       // z ranges per batch (units = batches * z_chunks)
   unsigned int* work;
-  // rank-0 split (count-only): batches >= first_a_batch hold only x with the
-  // top rank and test only the first n_dense_a rows (the rows without it),
-  // in za_chunks ranges per batch; every other (batch, row) pair is a hit
-  uint32_t first_a_batch = ~0u;
-  uint32_t za_chunks = 1;
-  uint64_t n_dense_a = 0;
+  // Pivot plan (count-only): x and dense rows are classed by which of the
+  // two top ranks (pivots) they hold; a batch of x of one class tests only
+  // the rows sharing no pivot with it (one of four contiguous row ranges),
+  // every other (x, row) pair of that batch is a hit. plan_units == 0: every
+  // batch tests all rows in z_chunks ranges.
+  const uint32_t* unit_off = nullptr;  // [n_batches + 1] first unit of each batch
+  const uint8_t* batch_kind = nullptr; // [n_batches] row-range kind 0..3
+  uint64_t kind_lo[4] = {0, 0, 0, 0}, kind_hi[4] = {0, 0, 0, 0};
+  uint32_t kind_zc[4] = {1, 1, 1, 1};
+  uint32_t plan_units = 0;
 };
 
-// Unit -> (batch, row range). Units are batch-major: the first_a_batch
-// full batches (z_chunks ranges over all rows), then the A batches.
+// Unit -> (batch, row range). Units are batch-major.
 __device__ __forceinline__ void hot_unit(const HotParams& p, uint32_t n_batches, uint32_t unit,
                                          uint32_t& bi, uint64_t& z_lo, uint64_t& z_hi) {
-  const uint32_t fb = p.first_a_batch < n_batches ? p.first_a_batch : n_batches;
-  const uint32_t nbu = fb * p.z_chunks;
-  if (unit < nbu) {
+  if (p.plan_units == 0) {
     bi = unit / p.z_chunks;
     const uint32_t zc = unit % p.z_chunks;
     z_lo = p.n_dense * zc / p.z_chunks;
     z_hi = p.n_dense * (zc + 1) / p.z_chunks;
-  } else {
-    const uint32_t u = unit - nbu;
-    bi = fb + u / p.za_chunks;
-    const uint32_t zc = u % p.za_chunks;
-    z_lo = p.n_dense_a * zc / p.za_chunks;
-    z_hi = p.n_dense_a * (zc + 1) / p.za_chunks;
+    return;
   }
+  uint32_t lo = 0, hi = n_batches;  // last batch whose first unit <= unit
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (p.unit_off[mid] <= unit) lo = mid; else hi = mid;
+  }
+  bi = lo;
+  const uint32_t k = p.batch_kind[lo];
+  const uint32_t zcs = p.kind_zc[k], zc = unit - p.unit_off[lo];
+  const uint64_t n = p.kind_hi[k] - p.kind_lo[k];
+  z_lo = p.kind_lo[k] + n * zc / zcs;
+  z_hi = p.kind_lo[k] + n * (zc + 1) / zcs;
 }
 
 __device__ __forceinline__ uint32_t hot_units(const HotParams& p, uint32_t n_batches) {
-  const uint32_t fb = p.first_a_batch < n_batches ? p.first_a_batch : n_batches;
-  return fb * p.z_chunks + (n_batches - fb) * p.za_chunks;
+  return p.plan_units ? p.plan_units : n_batches * p.z_chunks;
 }
 
-// 1 if live x (in xorder) holds y0 = y_of_rank[0] (rows are sorted by y).
-__global__ void rank0_flag_kernel(const uint32_t* __restrict__ xorder, uint64_t n_live,
-                                  const uint64_t* __restrict__ r_ptr,
-                                  const uint32_t* __restrict__ r_col,
-                                  const uint32_t* __restrict__ y_of_rank,
-                                  uint32_t* __restrict__ not_a) {
-  const uint32_t y0 = y_of_rank[0];
+// Pivot class of each live x: bit 1 = holds y_of_rank[0], bit 0 = holds
+// y_of_rank[1] (rows are sorted by y); out[4] counts per class.
+__global__ void pivot_class_x_kernel(const uint32_t* __restrict__ xorder, uint64_t n_live,
+                                     const uint64_t* __restrict__ r_ptr,
+                                     const uint32_t* __restrict__ r_col,
+                                     const uint32_t* __restrict__ y_of_rank,
+                                     uint32_t* __restrict__ cls, unsigned long long* __restrict__ out) {
+  __shared__ unsigned int c4[4];
+  if (threadIdx.x < 4) c4[threadIdx.x] = 0;
+  __syncthreads();
+  const uint32_t y0 = y_of_rank[0], y1 = y_of_rank[1];
   for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n_live;
        p += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t x = xorder[p];
-    uint64_t lo = r_ptr[x], hi = r_ptr[x + 1];
-    while (lo < hi) {
-      const uint64_t mid = (lo + hi) >> 1;
-      if (r_col[mid] < y0) lo = mid + 1; else hi = mid;
+    const uint64_t e = r_ptr[x + 1];
+    uint32_t c = 0;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const uint32_t yq = q ? y1 : y0;
+      uint64_t lo = r_ptr[x], hi = e;
+      while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (r_col[mid] < yq) lo = mid + 1; else hi = mid;
+      }
+      if (lo < e && r_col[lo] == yq) c |= q ? 1u : 2u;
     }
-    const bool has = lo < r_ptr[x + 1] && r_col[lo] == y0;
-    not_a[p] = has ? 0u : 1u;
+    cls[p] = c;
+    atomicAdd(&c4[c], 1u);
   }
+  __syncthreads();
+  if (threadIdx.x < 4 && c4[threadIdx.x]) atomicAdd(&out[threadIdx.x], (unsigned long long)c4[threadIdx.x]);
 }
 
-// Stable split of xorder: x without the top rank first (pos_b = exclusive
-// scan of not_a), then the others in order.
-__global__ void rank0_split_kernel(const uint32_t* __restrict__ xorder, uint64_t n_live,
-                                   const uint32_t* __restrict__ not_a,
-                                   const uint64_t* __restrict__ pos_b,
-                                   uint32_t* __restrict__ out) {
-  const uint64_t nb = pos_b[n_live];
-  for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n_live;
-       p += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t b = pos_b[p];
-    out[not_a[p] ? b : nb + (p - b)] = xorder[p];
+// Dense rows per pivot class (bit 1 = rank 0, bit 0 = rank 1; the lists are
+// rank-ascending, so both sit at the front) and folded sparse rows per class:
+// out[0..3] rows, out[4..7] flagged rows.
+__global__ void pivot_class_rows_kernel(const uint64_t* __restrict__ dl_ptr,
+                                        const uint32_t* __restrict__ dl_col, uint64_t n,
+                                        const uint8_t* __restrict__ row_sp,
+                                        unsigned long long* __restrict__ out) {
+  __shared__ unsigned int c8[8];
+  if (threadIdx.x < 8) c8[threadIdx.x] = 0;
+  __syncthreads();
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k0 = dl_ptr[i], k1 = dl_ptr[i + 1];
+    uint32_t c = 0;
+    if (k0 < k1) {
+      const uint32_t a = dl_col[k0];
+      if (a == 0) c |= 2u;
+      if (a == 1 || (a == 0 && k0 + 1 < k1 && dl_col[k0 + 1] == 1)) c |= 1u;
+    }
+    atomicAdd(&c8[c], 1u);
+    if (row_sp && row_sp[i]) atomicAdd(&c8[4 + c], 1u);
   }
+  __syncthreads();
+  if (threadIdx.x < 8 && c8[threadIdx.x]) atomicAdd(&out[threadIdx.x], (unsigned long long)c8[threadIdx.x]);
 }
 
 // T, hx from the live x in degree order: warp per x position.
@@ -733,8 +764,12 @@ __global__ void trie_key_kernel(const uint8_t* __restrict__ rec, const uint32_t*
     const uint32_t cw = rcnt[i], c = cw & 0xffffffu;
     const uint32_t r1 = c >= 1 ? rec[i * 32] + off : 0u;
     const uint32_t r2 = c >= 2 ? rec[i * 32 + 1] + off : 0u;
-    const uint32_t top = (cw >> 24) & 0x7fu;  // rank 0 first: rows without it sort first
-    key[i] = ((uint64_t)(top & 1u) << 24) | ((uint64_t)(top >> 1) << 18) | (r1 << 9) | r2;
+    // rows grouped by pivot class in the order (r0,r1) = 01, 00, 10, 11, so
+    // that the rows lacking r0, lacking r1, or lacking both are contiguous
+    const uint32_t top = (cw >> 24) & 0x7fu;
+    const uint32_t pc = ((top & 1u) << 1) | ((top >> 1) & 1u);  // bit1 = r0, bit0 = r1
+    const uint32_t grp = pc == 1 ? 0u : pc == 0 ? 1u : pc;
+    key[i] = ((uint64_t)grp << 23) | ((uint64_t)(top >> 2) << 18) | (r1 << 9) | r2;
     idx[i] = (uint32_t)i;
   }
 }
@@ -993,7 +1028,8 @@ dense_hot_trie_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
 // each warp step (positions z_lo + 32k of the row's z chunk).
 __global__ void trie_lds_kernel(const uint32_t* __restrict__ rcnt, uint64_t n, uint32_t z_chunks,
                                 uint32_t sub_read, unsigned long long* __restrict__ out,
-                                uint64_t mult = 1, uint32_t shared = 1) {
+                                uint64_t mult = 1, uint32_t shared = 1, uint64_t row0 = 0) {
+  rcnt += row0;  // rows [row0, row0 + n), chunked as the kernel chunks them
   uint64_t acc = 0;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {

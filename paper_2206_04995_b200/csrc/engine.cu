@@ -597,29 +597,78 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   const bool tab_planned = K <= 256 && K > kTabBits && hot_sel.empty() &&
                            (size_t)(kTabRows + K - kTabBits) * 32 * 16 <= (size_t)dense_smem_bytes(X) &&
                            top_rows >= 1.5;
-  const uint64_t rows_r0 = std::min<uint64_t>(top_rank_rows[0], D);
-  const uint64_t d_not0 = D - rows_r0;
-  uint32_t first_a_batch = n_batches;  // no split
-  uint64_t n_a_direct = 0;             // x in pure-A batches
+  // Pivot plan (count-only): classes by which of the two top ranks
+  // (pivots) an x or a dense row holds. A batch of x of one class tests only
+  // the rows sharing no pivot with it; its other pairs are hits (counted
+  // without a test). Rows are grouped (sorted) 01, 00, 10, 11 by (rank 0,
+  // rank 1), so each class's test range is contiguous.
+  uint64_t plan_direct = 0, plan_direct_sp = 0;  // untested hits (all / folded sparse rows)
+  uint64_t kind_lo[4] = {0, 0, 0, 0}, kind_hi[4] = {D, D, D, D};
+  uint32_t kind_zc[4] = {1, 1, 1, 1};
+  uint32_t kind_batches[4] = {n_batches, 0, 0, 0};
+  std::vector<uint32_t> unit_off_h;
+  std::vector<uint8_t> batch_kind_h;
   DBuf<uint32_t> xsplit;
-  if (tab_planned && mode == kModeCount && rows_r0 > 0 && std::getenv("D3G_NO_SPLIT") == nullptr) {
-    DBuf<uint32_t> not_a = X.alloc<uint32_t>(n_live);
-    D3G_LAUNCH(X, rank0_flag_kernel, grid_for(n_live, 256), 256, 0, xorder, n_live, in.r_ptr,
-               in.r_col, in.y_of_rank, not_a.p);
-    DBuf<uint64_t> pos_b = X.alloc<uint64_t>(n_live + 1);
-    exclusive_scan<uint32_t>(X, not_a.p, n_live, pos_b.p);
-    const uint64_t n_b = X.scalar(pos_b.p + n_live);
-    const uint32_t fb = (uint32_t)((n_b + 4095) / 4096);
-    const uint64_t a_direct = n_live > (uint64_t)fb * 4096 ? n_live - (uint64_t)fb * 4096 : 0;
-    const double full = (double)n_batches * (double)D;
-    const double part = (double)fb * (double)D + (double)(n_batches - fb) * (double)d_not0;
-    if (a_direct > 0 && part < 0.8 * full) {
+  const bool try_plan = tab_planned && mode == kModeCount && Y >= 2 && top_rank_rows[0] > 0 &&
+                        std::getenv("D3G_NO_SPLIT") == nullptr;
+  if (try_plan) {
+    DBuf<uint32_t> cls = X.alloc<uint32_t>(n_live);
+    DBuf<unsigned long long> cc = X.zeros<unsigned long long>(12);  // x[4] rows[4] sp[4]
+    D3G_LAUNCH(X, pivot_class_x_kernel, grid_for(n_live, 256), 256, 0, xorder, n_live, in.r_ptr,
+               in.r_col, in.y_of_rank, cls.p, cc.p);
+    D3G_LAUNCH(X, pivot_class_rows_kernel, grid_for(D, 256), 256, 0, in.dl_ptr, in.dl_col, D,
+               in.row_sp, cc.p + 4);
+    unsigned long long c[12];
+    X.to_host(c, cc.p, 12);
+    const unsigned long long* nx = c;  // x per class (bit1 = rank 0, bit0 = rank 1)
+    const unsigned long long* nr = c + 4;  // rows per class
+    const unsigned long long* nsp = c + 8;  // folded sparse rows per class
+    // row groups in sorted order: class 1, 0, 2, 3
+    kind_lo[1] = nr[1];
+    kind_hi[1] = nr[1] + nr[0] + nr[2];  // lacking rank 1
+    kind_lo[2] = 0;
+    kind_hi[2] = nr[1] + nr[0];          // lacking rank 0
+    kind_lo[3] = nr[1];
+    kind_hi[3] = nr[1] + nr[0];          // lacking both
+    const uint64_t sp_all = nsp[0] + nsp[1] + nsp[2] + nsp[3];
+    const uint64_t sp_in[4] = {sp_all, nsp[0] + nsp[2], nsp[1] + nsp[0], nsp[0]};
+    // batches: pure when all their x share one class, else kind 0 (all rows)
+    uint64_t cstart[5] = {0, nx[0], nx[0] + nx[1], nx[0] + nx[1] + nx[2], n_live};
+    batch_kind_h.assign(n_batches, 0);
+    double tested = 0;
+    uint64_t direct = 0, direct_sp = 0;
+    for (uint32_t b = 0; b < n_batches; ++b) {
+      const uint64_t p0 = (uint64_t)b * 4096, p1 = std::min<uint64_t>(p0 + 4096, n_live);
+      uint32_t k = 0;
+      for (uint32_t q = 0; q < 4; ++q)
+        if (p0 >= cstart[q] && p1 <= cstart[q + 1]) k = q;
+      batch_kind_h[b] = (uint8_t)k;
+      tested += (double)(kind_hi[k] - kind_lo[k]);
+      direct += (p1 - p0) * (D - (kind_hi[k] - kind_lo[k]));
+      direct_sp += (p1 - p0) * (sp_all - sp_in[k]);
+    }
+    if (tested < 0.8 * (double)n_batches * (double)D) {
       xsplit = X.alloc<uint32_t>(n_live);
-      D3G_LAUNCH(X, rank0_split_kernel, grid_for(n_live, 256), 256, 0, xorder, n_live, not_a.p,
-                 pos_b.p, xsplit.p);
+      DBuf<uint32_t> cls_s = X.alloc<uint32_t>(n_live);
+      radix_pass_u32(X, cls.p, xorder, n_live, 0, cls_s.p, xsplit.p);  // stable by class
       xorder = xsplit.p;
-      first_a_batch = fb;
-      n_a_direct = a_direct;
+      plan_direct = direct;
+      plan_direct_sp = direct_sp;
+      std::fill(kind_batches, kind_batches + 4, 0u);
+      for (uint32_t b = 0; b < n_batches; ++b) ++kind_batches[batch_kind_h[b]];
+      unit_off_h.assign(n_batches + 1, 0);
+      // units of about equal row counts (~8 per SM over the whole pass), so a
+      // few all-row batches do not leave one CTA with millions of rows
+      const double per_unit = std::max(256.0, tested / ((double)X.sm_count * 8));
+      for (uint32_t q = 0; q < 4; ++q) {
+        const uint64_t rows = kind_hi[q] - kind_lo[q];
+        kind_zc[q] = std::max<uint32_t>(1, (uint32_t)std::min<double>(
+            std::ceil((double)rows / per_unit), (double)((rows + 255) / 256)));
+      }
+      for (uint32_t b = 0; b < n_batches; ++b)
+        unit_off_h[b + 1] = unit_off_h[b] + kind_zc[batch_kind_h[b]];
+    } else {
+      batch_kind_h.clear();
     }
   }
   // hot structures
@@ -677,15 +726,24 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   hp.K = K;
   hp.kw = kw;
   hp.batch = 32;
-  const uint32_t n_full_b = std::max<uint32_t>(1, std::min(first_a_batch, n_batches));
   hp.z_chunks = std::max<uint32_t>(1, (uint32_t)std::min<uint64_t>(
-      (D + 255) / 256, ((uint64_t)X.sm_count * 8 + n_full_b - 1) / n_full_b));
-  if (first_a_batch < n_batches) {
-    const uint32_t n_a_b = n_batches - first_a_batch;
-    hp.first_a_batch = first_a_batch;
-    hp.n_dense_a = d_not0;
-    hp.za_chunks = std::max<uint32_t>(1, (uint32_t)std::min<uint64_t>(
-        (d_not0 + 255) / 256, ((uint64_t)X.sm_count * 8 + n_a_b - 1) / n_a_b));
+      (D + 255) / 256, ((uint64_t)X.sm_count * 8 + n_batches - 1) / n_batches));
+  const bool plan = !unit_off_h.empty();
+  DBuf<uint32_t> unit_off_d;
+  DBuf<uint8_t> batch_kind_d;
+  if (plan) {
+    unit_off_d = X.alloc<uint32_t>(n_batches + 1);
+    batch_kind_d = X.alloc<uint8_t>(n_batches);
+    X.to_device(unit_off_d.p, unit_off_h.data(), n_batches + 1);
+    X.to_device(batch_kind_d.p, batch_kind_h.data(), n_batches);
+    hp.unit_off = unit_off_d.p;
+    hp.batch_kind = batch_kind_d.p;
+    for (uint32_t q = 0; q < 4; ++q) {
+      hp.kind_lo[q] = kind_lo[q];
+      hp.kind_hi[q] = kind_hi[q];
+      hp.kind_zc[q] = kind_zc[q];
+    }
+    hp.plan_units = unit_off_h[n_batches];
   }
   DBuf<unsigned int> work = X.zeros<unsigned int>(1);
   hp.work = work.p;
@@ -700,10 +758,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool trie = false, jt_trie = false;
   size_t sm = (size_t)K * 32 * 16;
-  const uint64_t n_units = first_a_batch < n_batches
-                              ? (uint64_t)first_a_batch * hp.z_chunks +
-                                    (uint64_t)(n_batches - first_a_batch) * hp.za_chunks
-                              : (uint64_t)n_batches * hp.z_chunks;
+  const uint64_t n_units = plan ? (uint64_t)hp.plan_units : (uint64_t)n_batches * hp.z_chunks;
   unsigned g = (unsigned)std::min<uint64_t>(n_units, (uint64_t)X.sm_count);
   const char* hot_impl = std::getenv("D3G_HOT");
   const bool use_tc = hot_impl && std::string(hot_impl) == "tc" && mode == kModeCount &&
@@ -736,7 +791,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     for (uint32_t r = 0; r < kTabBits; ++r) top_per_row += (double)top_rank_rows[r] / (double)D;
     const std::string hv = hot_impl ? hot_impl : "";
     const bool force_tab = hv == "tab" || hv == "trie";
-    const bool tab = first_a_batch < n_batches ||
+    const bool tab = plan ||
                      K > kTabBits && tsm <= (size_t)dense_smem_bytes(X) &&
                      !(hot_impl && std::string(hot_impl) == "rec") &&
                      (force_tab || top_per_row >= 1.5);
@@ -771,19 +826,16 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
       if (jt_trie) {
         // slice reads of every (batch, row) the kernel tests, with and without
         // the prefix sharing
-        const uint32_t fb = std::min(first_a_batch, n_batches);
         for (uint32_t shared = 0; shared < 2; ++shared) {
           unsigned long long* dst = shared ? lds_units : &tallies.p[4].count;
-          if (fb)
-            D3G_LAUNCH(X, trie_lds_kernel, grid_for(D, 256), 256, 0, rcnt.p, D, hp.z_chunks,
-                       tab ? 1u : 0u, dst, (uint64_t)fb, shared);
-          if (fb < n_batches && d_not0)
-            D3G_LAUNCH(X, trie_lds_kernel, grid_for(d_not0, 256), 256, 0, rcnt.p, d_not0,
-                       hp.za_chunks, tab ? 1u : 0u, dst, (uint64_t)(n_batches - fb), shared);
+          for (uint32_t q = 0; q < 4; ++q) {
+            const uint64_t rows = kind_hi[q] - kind_lo[q];
+            if (!kind_batches[q] || !rows) continue;
+            D3G_LAUNCH(X, trie_lds_kernel, grid_for(rows, 256), 256, 0, rcnt.p, rows,
+                       plan ? kind_zc[q] : hp.z_chunks, tab ? 1u : 0u, dst,
+                       (uint64_t)kind_batches[q], shared, kind_lo[q]);
+          }
         }
-        if (fb < n_batches && cnt_sp)
-          D3G_LAUNCH(X, sp_rows_kernel, grid_for(rows_r0, 256), 256, 0, rcnt.p, d_not0, D,
-                     &tallies.p[5].count);
       }
     } else {
       // algorithmic LDS traffic: every (row, batch) reads its listed slices plus
@@ -900,9 +952,9 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   }
   Tally th[6];
   X.to_host(th, tallies.p, 6);
-  // pairs of pure-A batches with the rows holding the top rank: hits, untested
-  const uint64_t direct = first_a_batch < n_batches ? n_a_direct * rows_r0 : 0;
-  out.count_sp = th[3].count + (first_a_batch < n_batches ? n_a_direct * th[5].count : 0);
+  // pairs of pure batches with rows sharing a pivot: hits, untested
+  const uint64_t direct = plan_direct;
+  out.count_sp = th[3].count + plan_direct_sp;
   const Tally& h = th[0];
   if (cold_kernel_ok && e[best] > 0) {
     cold.count = th[1].count;
@@ -919,7 +971,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     // counters already cover every batch
     out.hot_lds_bytes = th[2].count * (trie ? 1ull : (uint64_t)n_batches) * 512ull;
     out.hot_lds_bytes_unshared = jt_trie ? th[4].count * 512ull : out.hot_lds_bytes;
-    out.split_direct_pairs = n_a_direct * rows_r0;
+    out.split_direct_pairs = plan_direct;
   }
   if (std::getenv("D3G_TRACE"))
     std::fprintf(stderr, "[dense_hot] D=%llu live=%llu K=%u hot=%llu cold=%llu cold_path=%s over=%llu\n",
