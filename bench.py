@@ -48,21 +48,23 @@ METRIC = "input tuples/sec and distinct (x,z) pairs/sec at 1/2/4/8 B200 vs roofl
 L2_BYTES = 126 * 1024 * 1024
 
 
-def _ncu_dram_bytes(cfg: int):
-    """dram__bytes_read.sum + dram__bytes_write.sum of the hot-pass kernel per
-    launch, from the committed `ncu --set full` capture of this config
-    (profiles/r01_cfg<N>_ncu_hotpass.csv), or None."""
+def _ncu_dram_bytes(cfg: int, which: str = "hotpass"):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one step's launches of
+    the kernel(s) in the committed `ncu --set full` capture of this config
+    (profiles/r01_cfg<N>_ncu_<which>.csv: the hot pass, or the cold-pass
+    kernels summed), or None."""
     import csv
-    path = os.path.join(ROOT, "profiles", f"r01_cfg{cfg}_ncu_hotpass.csv")
+    path = os.path.join(ROOT, "profiles", f"r01_cfg{cfg}_ncu_{which}.csv")
     if not os.path.exists(path):
         return None
     rows = list(csv.reader(open(path)))
-    hdr, units, vals = rows[0], rows[1], rows[2]
+    hdr, units = rows[0], rows[1]
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
     tot = 0.0
-    for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-        i = hdr.index(k)
-        tot += float(vals[i].replace(",", "")) * scale.get(units[i], 1)
+    for vals in rows[2:]:
+        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            i = hdr.index(k)
+            tot += float(vals[i].replace(",", "")) * scale.get(units[i], 1)
     return tot
 
 
@@ -390,6 +392,35 @@ def main():
                 "work": f"B_C = 16 B/input row + 16 B/intermediate pair = {b_cls:.4g} bytes "
                         f"({r0.intermediate_pairs} intermediate pairs)",
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+    cold_ms = sum(r.ms_dense_cold for r in reps) / len(reps)
+    cold_bytes = r0.cold_bytes
+    cold_roof = None
+    if cold_ms > 0 and cold_bytes:
+        ach_c = cold_bytes / (cold_ms * 1e-3) / 1e9
+        cold_roof = {"kernel": "DenseEC P2 cold residual pass (dense_cold_kernel, or "
+                               "dense_cold_hash_kernel + dense_cold_overflow_kernel)",
+                     "bound": "hbm", "achieved": ach_c, "peak": hbm, "unit": "GB/s",
+                     "frac": ach_c / hbm, "traffic": _ncu_dram_bytes(cfg_id, "cold"),
+                     "work": f"candidate stream = 36 B (32-byte hot signature + 4-byte row id) x "
+                             f"{cold_bytes // 36} candidates = {cold_bytes:.4g} B per step; kernel "
+                             f"time {cold_ms:.3f} ms (CUDA events on the library stream); the "
+                             f"stream is L2-resident in part, so traffic < work is possible",
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                     "share_of_step": cold_ms / phase["ms_total"]}
+    if dom in ("dense_ec", "sparse_bmm") and cold_roof and cold_ms > hot_ms:
+        # the cold pass is the dominant kernel (cfg2, cfg4, cfg5 since the
+        # pivot plan cut the hot pass); the hot pass is reported beside it
+        roof = dict(cold_roof)
+        if hot_ms > 0:
+            ach_h = hot_bytes / (hot_ms * 1e-3) / 1e9
+            smem = d3.smem_peak(ctx) / 1e9
+            roof["hot_pass"] = {
+                "kernel": "DenseEC P1 hot bit-sliced pass (dense_hot_jt_kernel)", "bound": "smem",
+                "achieved": ach_h, "peak": smem, "unit": "GB/s", "frac": ach_h / smem,
+                "traffic": _ncu_dram_bytes(cfg_id), "ms": hot_ms,
+                "share_of_step": hot_ms / phase["ms_total"],
+                "work": f"LDS bytes issued (512 B per slice read) = {hot_bytes:.4g} B; "
+                        f"{r0.hot_direct_pairs:.4g} pairs counted untested by the pivot plan"}
     elif dom in ("dense_ec", "sparse_bmm") and hot_ms > 0:
         # the dominant KERNEL is the DenseEC hot bit-sliced pass (on cfg4 it
         # answers the heavy sparse side): bound by shared-memory bandwidth
@@ -442,6 +473,8 @@ def main():
                 "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
                 "work": f"B_M = {b_map:.4g} compulsory bytes (SURVEY 8(d))",
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+    if cold_roof and roof.get("kernel", "").startswith("DenseEC P1"):
+        roof["cold_pass"] = cold_roof
     phases_roof = {
         "map+csr+partition": {"ms": prep_ms, "GB/s": b_map / (prep_ms * 1e-3) / 1e9 if prep_ms else None},
         "sparse_bmm": {"ms": phase["ms_sparse"],

@@ -131,6 +131,10 @@ typedef struct {
   /* count-only: (x, z) pairs counted as hits without a test by the rank-0
    * split (x and z both hold the top-ranked y) */
   uint64_t hot_direct_pairs;
+  /* DenseEC P2 (cold residual) kernels: CUDA-event time and candidate bytes
+   * streamed (36 B per candidate: 32-byte hot signature + 4-byte row id) */
+  double ms_dense_cold;
+  uint64_t cold_bytes;
 } d3g_report;
 
 /* Materialized output: caller-owned host (or device, on_device != 0)

@@ -1334,6 +1334,14 @@ dense_hot_jt_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
   tally_flush(tally, cnt, sum, xr);
 }
 
+// Candidates streamed by a cold kernel (one 36-byte entry each: 32-byte hot
+// signature + 4-byte row id): the cold pass's algorithmic traffic.
+__device__ __forceinline__ void flush_cand(unsigned long long* cand, uint64_t v) {
+  if (!cand) return;
+  v = warp_sum(v);
+  if (lane_id() == 0 && v) atomicAdd(cand, (unsigned long long)v);
+}
+
 // P2 kernel: cold residual for a dense block whose row count fits a per-warp
 // shared-memory bitmap. One warp per live x. The cold CSR (y-major, rows =
 // dense row positions holding y at a cold rank) stores each candidate's
@@ -1357,14 +1365,15 @@ dense_cold_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
                   uint32_t part_rows, uint32_t var_bits, const uint32_t* __restrict__ dl_z,
                   Decode dec, Emit em,
                   unsigned int* __restrict__ next, Tally* tally,
-                  const uint8_t* __restrict__ row_sp, unsigned long long* __restrict__ cnt_sp) {
+                  const uint8_t* __restrict__ row_sp, unsigned long long* __restrict__ cnt_sp,
+                  unsigned long long* __restrict__ cand = nullptr) {
   extern __shared__ __align__(16) uint32_t cbm[];  // [kColdWarps][part_rows / 32]
   const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
   const uint32_t pw = part_rows / 32;
   uint32_t* bm = cbm + (uint64_t)w * pw;
   for (uint32_t i = lane; i < pw; i += 32) bm[i] = 0;
   __syncwarp();
-  uint64_t cnt = 0, sum = 0, xr = 0, csp = 0;
+  uint64_t cnt = 0, sum = 0, xr = 0, csp = 0, ncand = 0;
   const uint64_t n_items = n_x * parts;
   for (;;) {
     uint32_t item = 0;
@@ -1401,6 +1410,7 @@ dense_cold_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
         if (lane >= (uint32_t)o) incl += u;
       }
       const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+      ncand += lane == 0 ? total : 0u;
       // kColdUnroll candidates per lane per step: their loads are independent,
       // so that many memory requests are in flight (the loop is latency bound)
       for (uint32_t tb = 0; tb < total; tb += 32 * kColdUnroll) {
@@ -1470,6 +1480,7 @@ dense_cold_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
     __syncwarp();
   }
   flush_sp(cnt_sp, csp);
+  flush_cand(cand, ncand);
   tally_flush(tally, cnt, sum, xr);
 }
 
@@ -1514,13 +1525,14 @@ dense_cold_hash_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
                        Decode dec, Emit em, unsigned int* __restrict__ next,
                        uint32_t* __restrict__ over_x, unsigned int* __restrict__ over_n,
                        Tally* tally, const uint8_t* __restrict__ row_sp,
-                       unsigned long long* __restrict__ cnt_sp, uint32_t ch_max = kCHMax) {
+                       unsigned long long* __restrict__ cnt_sp, uint32_t ch_max = kCHMax,
+                       unsigned long long* __restrict__ cand = nullptr) {
   extern __shared__ __align__(16) uint32_t chtab[];  // [kCHWarps][kCHSlots]
   const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
   uint32_t* tab = chtab + (uint64_t)w * kCHSlots;
   for (uint32_t i = lane; i < kCHSlots; i += 32) tab[i] = kCHEmpty;
   __syncwarp();
-  uint64_t cnt = 0, sum = 0, xr = 0, csp = 0;
+  uint64_t cnt = 0, sum = 0, xr = 0, csp = 0, ncand = 0;
   for (;;) {
     uint32_t item = 0;
     if (lane == 0) item = atomicAdd(next, 1u);
@@ -1550,6 +1562,7 @@ dense_cold_hash_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
           const uint64_t t = tb + lane;
           bool fresh = false;
           if (t < s1) {
+            ++ncand;
             uint4 b0, b1;
             ld256(ch + 2 * t, b0, b1);
             const bool hot = ((a0.x & b0.x) | (a0.y & b0.y) | (a0.z & b0.z) | (a0.w & b0.w) |
@@ -1595,6 +1608,7 @@ dense_cold_hash_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
     __syncwarp();
   }
   flush_sp(cnt_sp, csp);
+  flush_cand(cand, ncand);
   tally_flush(tally, cnt, sum, xr);
 }
 
@@ -1617,7 +1631,8 @@ dense_cold_overflow_kernel(const uint32_t* __restrict__ over_x, const unsigned i
                            uint32_t* __restrict__ gbm, uint64_t words, Decode dec, Emit em,
                            Tally* tally, const uint8_t* __restrict__ row_sp,
                            unsigned long long* __restrict__ cnt_sp,
-                           uint32_t* __restrict__ touched /* [gridDim.x][kOvTouched] */) {
+                           uint32_t* __restrict__ touched /* [gridDim.x][kOvTouched] */,
+                           unsigned long long* __restrict__ cand = nullptr) {
   __shared__ uint64_t s_seg0[kOvThreads];
   __shared__ uint32_t s_off[kOvThreads];
   __shared__ uint32_t s_wsum[kOvThreads / 32];
@@ -1628,7 +1643,7 @@ dense_cold_overflow_kernel(const uint32_t* __restrict__ over_x, const unsigned i
   constexpr uint32_t kW = kOvThreads / 32;
   uint32_t* bm = gbm + (uint64_t)blockIdx.x * words;
   const uint32_t n = *over_n;
-  uint64_t cnt = 0, sum = 0, xr = 0, csp = 0;
+  uint64_t cnt = 0, sum = 0, xr = 0, csp = 0, ncand = 0;
   for (uint32_t it = blockIdx.x; it < n; it += gridDim.x) {
     const uint32_t x = over_x[it];
     uint4 a0, a1;
@@ -1689,6 +1704,7 @@ dense_cold_overflow_kernel(const uint32_t* __restrict__ over_x, const unsigned i
             if (s_off[mid] <= f) lo = mid; else hi = mid;
           }
           const uint64_t t = s_seg0[lo] + (f - s_off[lo]);
+          ++ncand;
           uint4 b0, b1;
           ld256(ch + 2 * t, b0, b1);
           const bool hot = ((a0.x & b0.x) | (a0.y & b0.y) | (a0.z & b0.z) | (a0.w & b0.w) |
@@ -1716,6 +1732,7 @@ dense_cold_overflow_kernel(const uint32_t* __restrict__ over_x, const unsigned i
     }
   }
   flush_sp(cnt_sp, csp);
+  flush_cand(cand, ncand);
   tally_flush(tally, cnt, sum, xr);
 }
 

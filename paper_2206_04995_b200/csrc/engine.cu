@@ -139,7 +139,9 @@ struct KernelOut {
   double ms_hot = 0;          // CUDA-event time of the hot-pass launch
   uint64_t hot_lds_bytes = 0;  // its algorithmic shared-memory bytes
   uint64_t hot_lds_bytes_unshared = 0;  // without the prefix sharing
-  uint64_t split_direct_pairs = 0;  // hits counted without a test (rank-0 split)
+  uint64_t split_direct_pairs = 0;  // hits counted without a test (pivot plan)
+  double ms_cold = 0;          // CUDA-event time of the cold-pass kernels
+  uint64_t cold_bytes = 0;     // their candidate stream (36 B per candidate)
 };
 
 template <class F>
@@ -755,7 +757,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   Tally* t = tallies.p;
   unsigned long long* lds_units = &tallies.p[2].count;
   unsigned long long* cnt_sp = in.row_sp ? &tallies.p[3].count : nullptr;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
   bool trie = false, jt_trie = false;
   size_t sm = (size_t)K * 32 * 16;
   const uint64_t n_units = plan ? (uint64_t)hp.plan_units : (uint64_t)n_batches * hp.z_chunks;
@@ -903,6 +905,10 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     if (cold_kernel_ok) {
       DBuf<unsigned int> next = X.zeros<unsigned int>(1);
       Tally* tc = tallies.p + 1;
+      unsigned long long* cand = &tallies.p[5].count;  // candidates streamed
+      D3G_CUDA(cudaEventCreate(&ev2));
+      D3G_CUDA(cudaEventCreate(&ev3));
+      D3G_CUDA(cudaEventRecord(ev2, X.stream));
       if (cold_hash) {
         DBuf<uint32_t> over_x = X.alloc<uint32_t>(n_live);
         DBuf<unsigned int> over_n = X.zeros<unsigned int>(1);
@@ -913,7 +919,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
           D3G_LAUNCH(X, kfn, (unsigned)X.sm_count * 3, kCHWarps * 32, hsm, xorder, n_live,
                      in.r_ptr, in.r_col, cptr.p, ccol.p, ch.p, reinterpret_cast<const uint4*>(hx.p),
                      Y, var_bits, in.dl_z, dec, em, next.p, over_x.p, over_n.p, tc, in.row_sp,
-                     cnt_sp, env_u32("D3G_COLD_HASH_MAX", kCHMax, 1, kCHMax));
+                     cnt_sp, env_u32("D3G_COLD_HASH_MAX", kCHMax, 1, kCHMax), cand);
         });
         const unsigned int n_over = X.scalar(over_n.p);
         out.cold_overflow = n_over;
@@ -930,7 +936,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
             D3G_LAUNCH(X, dense_cold_overflow_kernel<decltype(M)::value>, og, kOvThreads, 0, over_x.p,
                        over_n.p, in.r_ptr, in.r_col, cptr.p, ccol.p, ch.p,
                        reinterpret_cast<const uint4*>(hx.p), Y, var_bits, in.dl_z, gbm.p, words,
-                       dec, em, tc, in.row_sp, cnt_sp, touched.p);
+                       dec, em, tc, in.row_sp, cnt_sp, touched.p, cand);
           });
         }
       } else {
@@ -941,9 +947,10 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
           D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
         D3G_LAUNCH(X, kfn, (unsigned)X.sm_count * cold_ctas, kColdWarps * 32, csm, xorder, n_live, in.r_ptr,
                    in.r_col, cptr.p, ccol.p, ch.p, reinterpret_cast<const uint4*>(hx.p), Y, parts,
-                   part_rows, var_bits, in.dl_z, dec, em, next.p, tc, in.row_sp, cnt_sp);
+                   part_rows, var_bits, in.dl_z, dec, em, next.p, tc, in.row_sp, cnt_sp, cand);
       });
       }
+      D3G_CUDA(cudaEventRecord(ev3, X.stream));
     } else {
       SparseInputs si{in.r_ptr, in.r_col, in.x_card, cptr.p, ccol.p, in.dl_z, D, Y, in.x_lo, in.x_hi};
       Filter flt{reinterpret_cast<const uint64_t*>(hx.p), reinterpret_cast<const uint64_t*>(hz.p), kw};
@@ -972,6 +979,14 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     out.hot_lds_bytes = th[2].count * (trie ? 1ull : (uint64_t)n_batches) * 512ull;
     out.hot_lds_bytes_unshared = jt_trie ? th[4].count * 512ull : out.hot_lds_bytes;
     out.split_direct_pairs = plan_direct;
+  }
+  if (ev2) {
+    float ms = 0;
+    D3G_CUDA(cudaEventElapsedTime(&ms, ev2, ev3));
+    cudaEventDestroy(ev2);
+    cudaEventDestroy(ev3);
+    out.ms_cold = ms;
+    out.cold_bytes = th[5].count * 36ull;  // 32-byte signature + 4-byte row id
   }
   if (std::getenv("D3G_TRACE"))
     std::fprintf(stderr, "[dense_hot] D=%llu live=%llu K=%u hot=%llu cold=%llu cold_path=%s over=%llu\n",
@@ -2050,6 +2065,8 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   rep->hot_lds_bytes = ks.hot_lds_bytes + kd.hot_lds_bytes;
   rep->hot_lds_bytes_unshared = ks.hot_lds_bytes_unshared + kd.hot_lds_bytes_unshared;
   rep->hot_direct_pairs = ks.split_direct_pairs + kd.split_direct_pairs;
+  rep->ms_dense_cold = ks.ms_cold + kd.ms_cold;
+  rep->cold_bytes = ks.cold_bytes + kd.cold_bytes;
   rep->spa_inner_count = outj_sp;
   rep->out_p = ks.count + kd.count;
   rep->checksum_sum = ks.sum + kd.sum;

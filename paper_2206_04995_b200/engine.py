@@ -224,7 +224,8 @@ class _Report(C.Structure):
                [("pairs_classical", C.c_uint64), ("intermediate_pairs", C.c_uint64),
                 ("ms_classical", C.c_double), ("ms_dense_hot", C.c_double),
                 ("hot_lds_bytes", C.c_uint64), ("hot_lds_bytes_unshared", C.c_uint64),
-                ("hot_direct_pairs", C.c_uint64)]
+                ("hot_direct_pairs", C.c_uint64), ("ms_dense_cold", C.c_double),
+                ("cold_bytes", C.c_uint64)]
 
 
 class _Pairs(C.Structure):
@@ -421,6 +422,8 @@ class ExecutionReport:
     hot_lds_bytes: int = 0
     hot_lds_bytes_unshared: int = 0
     hot_direct_pairs: int = 0
+    ms_dense_cold: float = 0.0
+    cold_bytes: int = 0
 
     def to_kv(self):
         """Insertion-ordered key/value view with the reference's key names
