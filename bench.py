@@ -61,10 +61,16 @@ def _ncu_dram_bytes(cfg: int, which: str = "hotpass"):
     hdr, units = rows[0], rows[1]
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
     tot = 0.0
+    import math
     for vals in rows[2:]:
         for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
             i = hdr.index(k)
-            tot += float(vals[i].replace(",", "")) * scale.get(units[i], 1)
+            try:
+                v = float(vals[i].replace(",", "")) * scale.get(units[i], 1)
+            except ValueError:
+                continue
+            if math.isfinite(v):  # a kernel ncu could not replay reports nan
+                tot += v
     return tot
 
 

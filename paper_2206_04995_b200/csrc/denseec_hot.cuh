@@ -1554,21 +1554,57 @@ dense_cold_hash_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
         seg0 = cp[y];
         seg1 = cp[y + 1];
       }
-      const uint32_t nseg = (uint32_t)((r1 - kb) < 32 ? (r1 - kb) : 32);
-      for (uint32_t j = 0; j < nseg && !over; ++j) {
-        const uint64_t s0 = __shfl_sync(0xffffffffu, seg0, j);
-        const uint64_t s1 = __shfl_sync(0xffffffffu, seg1, j);
-        for (uint64_t tb = s0; tb < s1; tb += 32) {
-          const uint64_t t = tb + lane;
+      // flattened (segment, entry) space, as in dense_cold_kernel: a warp scan
+      // of the segment lengths, then kColdUnroll candidates per lane per step
+      // found by a 5-step binary search (short cold segments keep lanes busy)
+      const uint32_t len = (uint32_t)(seg1 - seg0);
+      uint32_t incl = len;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= (uint32_t)o) incl += u;
+      }
+      const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+      ncand += lane == 0 ? total : 0u;
+      for (uint32_t tb = 0; tb < total && !over; tb += 32 * kColdUnroll) {
+        uint32_t tf[kColdUnroll], kx[kColdUnroll];
+        uint64_t t[kColdUnroll];
+#pragma unroll
+        for (int hh = 0; hh < kColdUnroll; ++hh) {
+          tf[hh] = tb + 32 * hh + lane;
+          uint32_t k = 0;
+#pragma unroll
+          for (int step = 16; step >= 1; step >>= 1) {
+            const uint32_t probe = __shfl_sync(0xffffffffu, incl, k + step - 1);
+            if (probe <= tf[hh]) k += step;
+          }
+          kx[hh] = k;
+        }
+#pragma unroll
+        for (int hh = 0; hh < kColdUnroll; ++hh) {
+          const uint32_t before = __shfl_sync(0xffffffffu, incl - len, kx[hh]);
+          const uint64_t base_k = __shfl_sync(0xffffffffu, seg0, kx[hh]);
+          t[hh] = base_k + (tf[hh] - before);
+        }
+        uint4 b0[kColdUnroll], b1[kColdUnroll];
+        uint32_t zc[kColdUnroll];
+#pragma unroll
+        for (int hh = 0; hh < kColdUnroll; ++hh) {
+          if (tf[hh] < total) {
+            ld256(ch + 2 * t[hh], b0[hh], b1[hh]);
+            zc[hh] = ccol[t[hh]];
+          }
+        }
+        uint32_t nfresh = 0;
+#pragma unroll
+        for (int hh = 0; hh < kColdUnroll; ++hh) {
           bool fresh = false;
-          if (t < s1) {
-            ++ncand;
-            uint4 b0, b1;
-            ld256(ch + 2 * t, b0, b1);
-            const bool hot = ((a0.x & b0.x) | (a0.y & b0.y) | (a0.z & b0.z) | (a0.w & b0.w) |
-                              (a1.x & b1.x) | (a1.y & b1.y) | (a1.z & b1.z) | (a1.w & b1.w)) != 0;
+          if (tf[hh] < total) {
+            const bool hot = ((a0.x & b0[hh].x) | (a0.y & b0[hh].y) | (a0.z & b0[hh].z) |
+                              (a0.w & b0[hh].w) | (a1.x & b1[hh].x) | (a1.y & b1[hh].y) |
+                              (a1.z & b1[hh].z) | (a1.w & b1[hh].w)) != 0;
             if (!hot) {
-              const uint32_t zl = ccol[t];
+              const uint32_t zl = zc[hh];
               uint32_t sl = ch_slot(zl);
               for (;;) {
                 const uint32_t prev = atomicCAS(&tab[sl], kCHEmpty, zl);
@@ -1581,12 +1617,10 @@ dense_cold_hash_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
               }
             }
           }
-          inserted += __popc(__ballot_sync(0xffffffffu, fresh));
-          if (inserted > ch_max) {
-            over = true;
-            break;
-          }
+          nfresh += __popc(__ballot_sync(0xffffffffu, fresh));
         }
+        inserted += nfresh;
+        if (inserted > ch_max) over = true;
       }
     }
     __syncwarp();
