@@ -107,7 +107,10 @@ inline void build_csr_device(Ctx& ctx, const uint32_t* maj, const uint32_t* mnr,
   const int row_bits = bits_for(n_rows - 1);
   if (n >= (1ull << 24) && row_bits > 12 && std::getenv("D3G_CSR_DIRECT") == nullptr) {
     DBuf<uint32_t> pm = ctx.alloc<uint32_t>(n), pv = ctx.alloc<uint32_t>(n);
-    radix_pass_u32(ctx, maj, mnr, n, row_bits - 8, pm.p, pv.p);
+    if (std::getenv("D3G_CSR_STABLE_BUCKETS"))
+      radix_pass_u32(ctx, maj, mnr, n, row_bits - 8, pm.p, pv.p);
+    else
+      bucket_pass_u32(ctx, maj, mnr, n, row_bits - 8, pm.p, pv.p);
     D3G_LAUNCH(ctx, major_scatter_kernel, g, 256, 0, pm.p, pv.p, n, off.p, cnt.p, tmp.p);
   } else {
     D3G_LAUNCH(ctx, major_scatter_kernel, g, 256, 0, maj, mnr, n, off.p, cnt.p, tmp.p);

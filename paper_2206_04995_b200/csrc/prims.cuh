@@ -316,6 +316,109 @@ inline void radix_pass_u32(Ctx& ctx, const uint32_t* keys, const uint32_t* vals,
              shift, n_tiles, offs.p, keys_out, vals_out);
 }
 
+// Unstable one-pass bucketing of u32 (key, value) pairs by the 8-bit digit
+// (key >> shift) & 255, for callers that re-sort inside each bucket (the
+// large CSR build). A CTA ranks its tile in shared memory (per-digit
+// counters), stages the tile in digit order and writes it out in runs, so the
+// global writes are contiguous per digit instead of scattered per element.
+constexpr int kBucketThreads = 1024;
+constexpr int kBucketPer = 4;
+constexpr int kBucketTile = kBucketThreads * kBucketPer;  // 4096 pairs per CTA
+
+__global__ void __launch_bounds__(kBucketThreads)
+bucket_hist_kernel(const uint32_t* __restrict__ keys, uint64_t n, int shift, uint32_t n_tiles,
+                   uint32_t* __restrict__ hist /* [256][n_tiles] */) {
+  __shared__ uint32_t cnt[256];
+  if (threadIdx.x < 256) cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const uint64_t base = (uint64_t)blockIdx.x * kBucketTile;
+#pragma unroll
+  for (int k = 0; k < kBucketPer; ++k) {
+    const uint64_t i = base + (uint64_t)k * kBucketThreads + threadIdx.x;
+    if (i < n) atomicAdd(&cnt[(keys[i] >> shift) & 255], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x < 256) hist[(uint64_t)threadIdx.x * n_tiles + blockIdx.x] = cnt[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(kBucketThreads)
+bucket_scatter_kernel(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+                      uint64_t n, int shift, uint32_t n_tiles,
+                      const uint64_t* __restrict__ offsets /* scanned hist, digit-major */,
+                      uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out) {
+  __shared__ uint32_t s_cnt[256], s_loc[256];
+  __shared__ uint64_t s_glb[256];
+  __shared__ uint32_t s_key[kBucketTile], s_val[kBucketTile];
+  const uint32_t t = threadIdx.x;
+  if (t < 256) s_cnt[t] = 0;
+  __syncthreads();
+  const uint64_t base = (uint64_t)blockIdx.x * kBucketTile;
+  uint32_t k[kBucketPer], v[kBucketPer], r[kBucketPer];
+#pragma unroll
+  for (int q = 0; q < kBucketPer; ++q) {
+    const uint64_t i = base + (uint64_t)q * kBucketThreads + t;
+    if (i < n) {
+      k[q] = keys[i];
+      v[q] = vals[i];
+      r[q] = atomicAdd(&s_cnt[(k[q] >> shift) & 255], 1u);
+    }
+  }
+  __syncthreads();
+  if (t < 32) {  // exclusive scan of the 256 tile counts, 8 per lane
+    uint32_t c[8], s = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      c[j] = s_cnt[t * 8 + j];
+      s += c[j];
+    }
+    uint32_t incl = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (t >= (uint32_t)o) incl += u;
+    }
+    uint32_t run = incl - s;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      s_loc[t * 8 + j] = run;
+      run += c[j];
+    }
+  }
+  if (t < 256) s_glb[t] = offsets[(uint64_t)t * n_tiles + blockIdx.x];
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < kBucketPer; ++q) {
+    const uint64_t i = base + (uint64_t)q * kBucketThreads + t;
+    if (i < n) {
+      const uint32_t p = s_loc[(k[q] >> shift) & 255] + r[q];
+      s_key[p] = k[q];
+      s_val[p] = v[q];
+    }
+  }
+  __syncthreads();
+  const uint32_t in_tile = (uint32_t)((n - base) < (uint64_t)kBucketTile ? (n - base) : kBucketTile);
+  for (uint32_t p = t; p < in_tile; p += kBucketThreads) {
+    const uint32_t key = s_key[p], d = (key >> shift) & 255;
+    const uint64_t g = s_glb[d] + (p - s_loc[d]);
+    keys_out[g] = key;
+    vals_out[g] = s_val[p];
+  }
+}
+
+// Unstable bucketing by one 8-bit digit (see bucket_scatter_kernel).
+inline void bucket_pass_u32(Ctx& ctx, const uint32_t* keys, const uint32_t* vals, uint64_t n,
+                            int shift, uint32_t* keys_out, uint32_t* vals_out) {
+  if (n == 0) return;
+  if (n >= (1ull << 32)) throw ResourceError("bucket_pass_u32: more than 2^32 keys");
+  const uint32_t n_tiles = (uint32_t)((n + kBucketTile - 1) / kBucketTile);
+  DBuf<uint32_t> hist = ctx.alloc<uint32_t>((uint64_t)256 * n_tiles);
+  DBuf<uint64_t> offs = ctx.alloc<uint64_t>((uint64_t)256 * n_tiles + 1);
+  D3G_LAUNCH(ctx, bucket_hist_kernel, n_tiles, kBucketThreads, 0, keys, n, shift, n_tiles, hist.p);
+  exclusive_scan<uint32_t>(ctx, hist.p, (uint64_t)256 * n_tiles, offs.p);
+  D3G_LAUNCH(ctx, bucket_scatter_kernel, n_tiles, kBucketThreads, 0, keys, vals, n, shift, n_tiles,
+             offs.p, keys_out, vals_out);
+}
+
 __global__ void index_compact_kernel(const uint32_t* __restrict__ flag,
                                      const uint64_t* __restrict__ pos, uint64_t n,
                                      uint32_t* __restrict__ out) {

@@ -370,3 +370,23 @@ def test_cfg5_cold_overflow_matches_reference(monkeypatch):
         (g["set"]["count"], g["set"]["sum"], g["set"]["xor"])
     del rl, rr, sl, sr
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("cfg", [3, 4])
+def test_count_only_matches_reference(cfg):
+    """The count-only path (the bench's step: no fingerprint, the pivot plan
+    where it applies, the jump-table hot kernel without the subset table on
+    cfg4) gives the reference's count and pairs split."""
+    g = _golden().get(f"cfg{cfg}")
+    if g is None:
+        pytest.skip("golden entry not generated")
+    rl, rr = d3.generate(cfg, 0)
+    sl, sr = d3.generate(cfg, 1)
+    out = d3.join_project(d3.RawTable(rl, rr), d3.RawTable(sl, sr),
+                          d3.EngineConfig(force=d3.Strategy.auto_select, count_only=True,
+                                          memory_budget_bytes=64 << 30), C)
+    rep = out.report
+    assert rep.out_p == g["set"]["count"]
+    ref = g.get("ref_hybrid_report")
+    if ref and cfg != 3:
+        assert (rep.pairs_sparse, rep.pairs_dense) == (ref["pairs_sparse"], ref["pairs_dense"])
