@@ -34,14 +34,15 @@ struct HotParams {
   uint32_t z_chunks;       // z ranges per batch (units = batches * z_chunks)
   unsigned int* work;
   // Pivot plan (count-only): x and dense rows are classed by which of the
-  // two top ranks (pivots) they hold; a batch of x of one class tests only
-  // the rows sharing no pivot with it (one of four contiguous row ranges),
-  // every other (x, row) pair of that batch is a hit. plan_units == 0: every
-  // batch tests all rows in z_chunks ranges.
+  // top ranks (pivots) they hold; a batch whose x share the pivot set k (the
+  // AND of their classes) tests only the rows sharing no pivot with k (kind
+  // k: a contiguous segment [kind_lo, kind_hi) of the concatenated per-kind
+  // row arrays); every other (x, row) pair of that batch is a hit.
+  // plan_units == 0: every batch tests all rows in z_chunks ranges.
   const uint32_t* unit_off = nullptr;  // [n_batches + 1] first unit of each batch
-  const uint8_t* batch_kind = nullptr; // [n_batches] row-range kind 0..3
-  uint64_t kind_lo[4] = {0, 0, 0, 0}, kind_hi[4] = {0, 0, 0, 0};
-  uint32_t kind_zc[4] = {1, 1, 1, 1};
+  const uint8_t* batch_kind = nullptr; // [n_batches] row-range kind 0..7
+  uint64_t kind_lo[8] = {0, 0, 0, 0, 0, 0, 0, 0}, kind_hi[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  uint32_t kind_zc[8] = {1, 1, 1, 1, 1, 1, 1, 1};
   uint32_t plan_units = 0;
 };
 
@@ -72,63 +73,109 @@ __device__ __forceinline__ uint32_t hot_units(const HotParams& p, uint32_t n_bat
   return p.plan_units ? p.plan_units : n_batches * p.z_chunks;
 }
 
-// Pivot class of each live x: bit 1 = holds y_of_rank[0], bit 0 = holds
-// y_of_rank[1] (rows are sorted by y); out[4] counts per class.
+// Pivot class of each live x: bit q = holds y_of_rank[q] (q < n_piv; rows are
+// sorted by y, binary search); out[8] counts per class.
 __global__ void pivot_class_x_kernel(const uint32_t* __restrict__ xorder, uint64_t n_live,
                                      const uint64_t* __restrict__ r_ptr,
                                      const uint32_t* __restrict__ r_col,
-                                     const uint32_t* __restrict__ y_of_rank,
+                                     const uint32_t* __restrict__ y_of_rank, uint32_t n_piv,
                                      uint32_t* __restrict__ cls, unsigned long long* __restrict__ out) {
-  __shared__ unsigned int c4[4];
-  if (threadIdx.x < 4) c4[threadIdx.x] = 0;
+  __shared__ unsigned int c8[8];
+  if (threadIdx.x < 8) c8[threadIdx.x] = 0;
   __syncthreads();
-  const uint32_t y0 = y_of_rank[0], y1 = y_of_rank[1];
   for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n_live;
        p += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t x = xorder[p];
     const uint64_t e = r_ptr[x + 1];
     uint32_t c = 0;
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const uint32_t yq = q ? y1 : y0;
+    for (uint32_t q = 0; q < n_piv; ++q) {
+      const uint32_t yq = y_of_rank[q];
       uint64_t lo = r_ptr[x], hi = e;
       while (lo < hi) {
         const uint64_t mid = (lo + hi) >> 1;
         if (r_col[mid] < yq) lo = mid + 1; else hi = mid;
       }
-      if (lo < e && r_col[lo] == yq) c |= q ? 1u : 2u;
+      if (lo < e && r_col[lo] == yq) c |= 1u << q;
     }
     cls[p] = c;
-    atomicAdd(&c4[c], 1u);
+    atomicAdd(&c8[c], 1u);
   }
   __syncthreads();
-  if (threadIdx.x < 4 && c4[threadIdx.x]) atomicAdd(&out[threadIdx.x], (unsigned long long)c4[threadIdx.x]);
+  if (threadIdx.x < 8 && c8[threadIdx.x]) atomicAdd(&out[threadIdx.x], (unsigned long long)c8[threadIdx.x]);
 }
 
-// Dense rows per pivot class (bit 1 = rank 0, bit 0 = rank 1; the lists are
-// rank-ascending, so both sit at the front) and folded sparse rows per class:
-// out[0..3] rows, out[4..7] flagged rows.
+// Dense rows per pivot class (bit q = holds rank q; the lists are
+// rank-ascending, so the pivots sit at the front) and folded sparse rows per
+// class: out[0..7] rows, out[8..15] flagged rows.
 __global__ void pivot_class_rows_kernel(const uint64_t* __restrict__ dl_ptr,
                                         const uint32_t* __restrict__ dl_col, uint64_t n,
-                                        const uint8_t* __restrict__ row_sp,
+                                        uint32_t n_piv, const uint8_t* __restrict__ row_sp,
                                         unsigned long long* __restrict__ out) {
-  __shared__ unsigned int c8[8];
-  if (threadIdx.x < 8) c8[threadIdx.x] = 0;
+  __shared__ unsigned int c16[16];
+  if (threadIdx.x < 16) c16[threadIdx.x] = 0;
   __syncthreads();
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t k0 = dl_ptr[i], k1 = dl_ptr[i + 1];
     uint32_t c = 0;
-    if (k0 < k1) {
-      const uint32_t a = dl_col[k0];
-      if (a == 0) c |= 2u;
-      if (a == 1 || (a == 0 && k0 + 1 < k1 && dl_col[k0 + 1] == 1)) c |= 1u;
+    for (uint64_t k = k0; k < k1 && k < k0 + n_piv; ++k) {
+      const uint32_t r = dl_col[k];
+      if (r < n_piv) c |= 1u << r; else break;
     }
-    atomicAdd(&c8[c], 1u);
-    if (row_sp && row_sp[i]) atomicAdd(&c8[4 + c], 1u);
+    atomicAdd(&c16[c], 1u);
+    if (row_sp && row_sp[i]) atomicAdd(&c16[8 + c], 1u);
   }
   __syncthreads();
-  if (threadIdx.x < 8 && c8[threadIdx.x]) atomicAdd(&out[threadIdx.x], (unsigned long long)c8[threadIdx.x]);
+  if (threadIdx.x < 16 && c16[threadIdx.x]) atomicAdd(&out[threadIdx.x], (unsigned long long)c16[threadIdx.x]);
+}
+
+// Per-kind row segment: the sorted rows sharing no pivot with kind k (class
+// bits = the low n_piv bits of the subset mask), compacted in sorted order.
+__global__ void kind_flag_kernel(const uint32_t* __restrict__ rcnt, uint64_t n, uint32_t k,
+                                 uint32_t* __restrict__ flag) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    flag[i] = ((rcnt[i] >> 24) & k) == 0 ? 1u : 0u;
+}
+
+__global__ void kind_gather_kernel(const uint4* __restrict__ rec, const uint32_t* __restrict__ rcnt,
+                                   const uint64_t* __restrict__ key, const uint32_t* __restrict__ perm,
+                                   const uint32_t* __restrict__ flag, const uint64_t* __restrict__ pos,
+                                   uint64_t n, uint64_t dst0, uint4* __restrict__ rec_o,
+                                   uint32_t* __restrict__ rcnt_o, uint64_t* __restrict__ key_o,
+                                   uint32_t* __restrict__ perm_o) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    if (!flag[i]) continue;
+    const uint64_t d = dst0 + pos[i];
+    uint4 a, b;
+    ld256(rec + 2 * i, a, b);
+    st256(rec_o + 2 * d, a, b);
+    rcnt_o[d] = rcnt[i];
+    key_o[d] = key[i];
+    perm_o[d] = perm[i];
+  }
+}
+
+// Shared-prefix length L (bits 22-23 of the count word) against the previous
+// row of the same segment [seg_lo, seg_hi).
+__global__ void kind_prefix_kernel(uint32_t* __restrict__ rcnt, const uint64_t* __restrict__ key,
+                                   uint64_t seg_lo, uint64_t seg_hi) {
+  for (uint64_t i = seg_lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < seg_hi;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t L = 0;
+    if (i > seg_lo) {
+      const uint64_t k = key[i], kp = key[i - 1];
+      if ((k >> 18) == (kp >> 18)) {
+        L = 1;
+        if ((k & 0x3fe00u) && ((k >> 9) == (kp >> 9))) {
+          L = 2;
+          if ((k & 0x1ffu) && k == kp) L = 3;
+        }
+      }
+    }
+    rcnt[i] = (rcnt[i] & ~(3u << 22)) | (L << 22);
+  }
 }
 
 // T, hx from the live x in degree order: warp per x position.
@@ -758,18 +805,23 @@ __global__ void sp_rows_kernel(const uint32_t* __restrict__ rcnt, uint64_t lo, u
 // listed rank + 1, second listed rank + 1; 7/9/9 bits), 0 = absent.
 __global__ void trie_key_kernel(const uint8_t* __restrict__ rec, const uint32_t* __restrict__ rcnt,
                                 uint64_t n, uint64_t* __restrict__ key, uint32_t* __restrict__ idx,
-                                uint32_t off /* stored rank byte + off = rank - 6 */) {
+                                uint32_t off /* stored rank byte + off = rank - 6 */,
+                                uint32_t group2 = 0) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t cw = rcnt[i], c = cw & 0xffffffu;
     const uint32_t r1 = c >= 1 ? rec[i * 32] + off : 0u;
     const uint32_t r2 = c >= 2 ? rec[i * 32 + 1] + off : 0u;
-    // rows grouped by pivot class in the order (r0,r1) = 01, 00, 10, 11, so
-    // that the rows lacking r0, lacking r1, or lacking both are contiguous
     const uint32_t top = (cw >> 24) & 0x7fu;
-    const uint32_t pc = ((top & 1u) << 1) | ((top >> 1) & 1u);  // bit1 = r0, bit0 = r1
-    const uint32_t grp = pc == 1 ? 0u : pc == 0 ? 1u : pc;
-    key[i] = ((uint64_t)grp << 23) | ((uint64_t)(top >> 2) << 18) | (r1 << 9) | r2;
+    if (group2) {
+      // two-pivot plan without segments: rows grouped by (rank 1, rank 0)
+      // class in the order 2, 0, 1, 3 so that the rows lacking rank 0, lacking
+      // rank 1, or lacking both are contiguous ranges
+      const uint32_t c = top & 3u, grp = c == 2 ? 0u : c == 0 ? 1u : c == 1 ? 2u : 3u;
+      key[i] = ((uint64_t)grp << 23) | ((uint64_t)(top >> 2) << 18) | (r1 << 9) | r2;
+    } else {
+      key[i] = ((uint64_t)top << 18) | (r1 << 9) | r2;
+    }
     idx[i] = (uint32_t)i;
   }
 }

@@ -599,55 +599,69 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   const bool tab_planned = K <= 256 && K > kTabBits && hot_sel.empty() &&
                            (size_t)(kTabRows + K - kTabBits) * 32 * 16 <= (size_t)dense_smem_bytes(X) &&
                            top_rows >= 1.5;
-  // Pivot plan (count-only): classes by which of the two top ranks
-  // (pivots) an x or a dense row holds. A batch of x of one class tests only
-  // the rows sharing no pivot with it; its other pairs are hits (counted
-  // without a test). Rows are grouped (sorted) 01, 00, 10, 11 by (rank 0,
-  // rank 1), so each class's test range is contiguous.
+  // Pivot plan (count-only): x and dense rows are classed by which of the
+  // n_piv top ranks (pivots) they hold (bit q = rank q). A pair sharing a
+  // pivot is a hit without a test. x are split stably by class into batches;
+  // a batch whose x share the pivot set k (the AND of their classes) tests
+  // only the rows with no pivot in k: kind k's row segment, compacted from
+  // the sorted rows (kind 0 = all rows); every other pair of the batch is
+  // counted as a hit.
+  // three pivots pay for their per-kind row segments only on large passes
+  // (cfg5: hot 48 -> 31 ms; cfg2: +0.1 ms of segment builds); two pivots use
+  // contiguous ranges of the grouped row order instead (no segments)
+  const uint32_t piv_dflt = (double)n_batches * (double)D > 1e9 ? 3u : 2u;
+  const uint32_t n_piv =
+      (uint32_t)std::min<uint64_t>(env_u32("D3G_PIVOTS", piv_dflt, 1, 3), Y);
+  const bool piv_ranges = n_piv == 2;  // grouped rows, kinds are ranges of [0, D)
+  const uint32_t n_kinds = 1u << n_piv;
   uint64_t plan_direct = 0, plan_direct_sp = 0;  // untested hits (all / folded sparse rows)
-  uint64_t kind_lo[4] = {0, 0, 0, 0}, kind_hi[4] = {D, D, D, D};
-  uint32_t kind_zc[4] = {1, 1, 1, 1};
-  uint32_t kind_batches[4] = {n_batches, 0, 0, 0};
+  uint64_t kind_rows[8] = {D, 0, 0, 0, 0, 0, 0, 0};  // rows tested by a batch of kind k
+  uint64_t kind_lo[8] = {0, 0, 0, 0, 0, 0, 0, 0}, kind_hi[8] = {D, 0, 0, 0, 0, 0, 0, 0};
+  uint32_t kind_zc[8] = {1, 1, 1, 1, 1, 1, 1, 1};
+  uint32_t kind_batches[8] = {n_batches, 0, 0, 0, 0, 0, 0, 0};
+  uint64_t seg_rows = D;  // rows of the concatenated kind segments
   std::vector<uint32_t> unit_off_h;
   std::vector<uint8_t> batch_kind_h;
   DBuf<uint32_t> xsplit;
-  const bool try_plan = tab_planned && mode == kModeCount && Y >= 2 && top_rank_rows[0] > 0 &&
+  const bool try_plan = tab_planned && mode == kModeCount && Y >= 1 && top_rank_rows[0] > 0 &&
                         std::getenv("D3G_NO_SPLIT") == nullptr;
   if (try_plan) {
     DBuf<uint32_t> cls = X.alloc<uint32_t>(n_live);
-    DBuf<unsigned long long> cc = X.zeros<unsigned long long>(12);  // x[4] rows[4] sp[4]
+    DBuf<unsigned long long> cc = X.zeros<unsigned long long>(24);  // x[8] rows[8] sp[8]
     D3G_LAUNCH(X, pivot_class_x_kernel, grid_for(n_live, 256), 256, 0, xorder, n_live, in.r_ptr,
-               in.r_col, in.y_of_rank, cls.p, cc.p);
+               in.r_col, in.y_of_rank, n_piv, cls.p, cc.p);
     D3G_LAUNCH(X, pivot_class_rows_kernel, grid_for(D, 256), 256, 0, in.dl_ptr, in.dl_col, D,
-               in.row_sp, cc.p + 4);
-    unsigned long long c[12];
-    X.to_host(c, cc.p, 12);
-    const unsigned long long* nx = c;  // x per class (bit1 = rank 0, bit0 = rank 1)
-    const unsigned long long* nr = c + 4;  // rows per class
-    const unsigned long long* nsp = c + 8;  // folded sparse rows per class
-    // row groups in sorted order: class 1, 0, 2, 3
-    kind_lo[1] = nr[1];
-    kind_hi[1] = nr[1] + nr[0] + nr[2];  // lacking rank 1
-    kind_lo[2] = 0;
-    kind_hi[2] = nr[1] + nr[0];          // lacking rank 0
-    kind_lo[3] = nr[1];
-    kind_hi[3] = nr[1] + nr[0];          // lacking both
-    const uint64_t sp_all = nsp[0] + nsp[1] + nsp[2] + nsp[3];
-    const uint64_t sp_in[4] = {sp_all, nsp[0] + nsp[2], nsp[1] + nsp[0], nsp[0]};
-    // batches: pure when all their x share one class, else kind 0 (all rows)
-    uint64_t cstart[5] = {0, nx[0], nx[0] + nx[1], nx[0] + nx[1] + nx[2], n_live};
+               n_piv, in.row_sp, cc.p + 8);
+    unsigned long long c[24];
+    X.to_host(c, cc.p, 24);
+    const unsigned long long* nx = c;       // x per class
+    const unsigned long long* nr = c + 8;   // dense rows per class
+    const unsigned long long* nsp = c + 16; // folded sparse rows per class
+    uint64_t sp_rows[8] = {0, 0, 0, 0, 0, 0, 0, 0}, sp_all = 0;
+    for (uint32_t q = 0; q < n_kinds; ++q) sp_all += nsp[q];
+    for (uint32_t k = 0; k < n_kinds; ++k) {
+      kind_rows[k] = 0;
+      for (uint32_t q = 0; q < n_kinds; ++q)
+        if ((q & k) == 0) {
+          kind_rows[k] += nr[q];
+          sp_rows[k] += nsp[q];
+        }
+    }
+    // class q occupies x positions [cstart[q], cstart[q + 1]) after the split
+    uint64_t cstart[9] = {0};
+    for (uint32_t q = 0; q < 8; ++q) cstart[q + 1] = cstart[q] + (q < n_kinds ? nx[q] : 0);
     batch_kind_h.assign(n_batches, 0);
     double tested = 0;
     uint64_t direct = 0, direct_sp = 0;
     for (uint32_t b = 0; b < n_batches; ++b) {
       const uint64_t p0 = (uint64_t)b * 4096, p1 = std::min<uint64_t>(p0 + 4096, n_live);
-      uint32_t k = 0;
-      for (uint32_t q = 0; q < 4; ++q)
-        if (p0 >= cstart[q] && p1 <= cstart[q + 1]) k = q;
+      uint32_t k = n_kinds - 1;
+      for (uint32_t q = 0; q < n_kinds; ++q)
+        if (cstart[q + 1] > p0 && cstart[q] < p1) k &= q;  // classes present
       batch_kind_h[b] = (uint8_t)k;
-      tested += (double)(kind_hi[k] - kind_lo[k]);
-      direct += (p1 - p0) * (D - (kind_hi[k] - kind_lo[k]));
-      direct_sp += (p1 - p0) * (sp_all - sp_in[k]);
+      tested += (double)kind_rows[k];
+      direct += (p1 - p0) * (D - kind_rows[k]);
+      direct_sp += (p1 - p0) * (sp_all - sp_rows[k]);
     }
     if (tested < 0.8 * (double)n_batches * (double)D) {
       xsplit = X.alloc<uint32_t>(n_live);
@@ -656,17 +670,36 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
       xorder = xsplit.p;
       plan_direct = direct;
       plan_direct_sp = direct_sp;
-      std::fill(kind_batches, kind_batches + 4, 0u);
+      std::fill(kind_batches, kind_batches + 8, 0u);
       for (uint32_t b = 0; b < n_batches; ++b) ++kind_batches[batch_kind_h[b]];
-      unit_off_h.assign(n_batches + 1, 0);
+      // segments: kind 0 = the sorted rows themselves, then each used kind;
+      // with two pivots the grouped order (classes 2, 0, 1, 3) makes every
+      // kind a range of [0, D)
+      seg_rows = D;
+      if (piv_ranges) {
+        kind_lo[1] = 0;
+        kind_hi[1] = nr[2] + nr[0];          // lacking rank 0
+        kind_lo[2] = nr[2];
+        kind_hi[2] = nr[2] + nr[0] + nr[1];  // lacking rank 1
+        kind_lo[3] = nr[2];
+        kind_hi[3] = nr[2] + nr[0];          // lacking both
+      } else {
+        for (uint32_t k = 1; k < n_kinds; ++k)
+          if (kind_batches[k]) {
+            kind_lo[k] = seg_rows;
+            kind_hi[k] = seg_rows + kind_rows[k];
+            seg_rows += kind_rows[k];
+          }
+      }
       // units of about equal row counts (~8 per SM over the whole pass), so a
       // few all-row batches do not leave one CTA with millions of rows
       const double per_unit = std::max(256.0, tested / ((double)X.sm_count * 8));
-      for (uint32_t q = 0; q < 4; ++q) {
-        const uint64_t rows = kind_hi[q] - kind_lo[q];
-        kind_zc[q] = std::max<uint32_t>(1, (uint32_t)std::min<double>(
+      for (uint32_t k = 0; k < n_kinds; ++k) {
+        const uint64_t rows = kind_hi[k] - kind_lo[k];
+        kind_zc[k] = std::max<uint32_t>(1, (uint32_t)std::min<double>(
             std::ceil((double)rows / per_unit), (double)((rows + 255) / 256)));
       }
+      unit_off_h.assign(n_batches + 1, 0);
       for (uint32_t b = 0; b < n_batches; ++b)
         unit_off_h[b + 1] = unit_off_h[b] + kind_zc[batch_kind_h[b]];
     } else {
@@ -740,7 +773,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     X.to_device(batch_kind_d.p, batch_kind_h.data(), n_batches);
     hp.unit_off = unit_off_d.p;
     hp.batch_kind = batch_kind_d.p;
-    for (uint32_t q = 0; q < 4; ++q) {
+    for (uint32_t q = 0; q < 8; ++q) {
       hp.kind_lo[q] = kind_lo[q];
       hp.kind_hi[q] = kind_hi[q];
       hp.kind_zc[q] = kind_zc[q];
@@ -817,7 +850,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
       DBuf<uint64_t> key = X.alloc<uint64_t>(D);
       perm = X.alloc<uint32_t>(D);
       D3G_LAUNCH(X, trie_key_kernel, grid_for(D, 256), 256, 0, reinterpret_cast<const uint8_t*>(rec.p),
-                 rcnt.p, D, key.p, perm.p, jt ? 1u : 1u - kTabBits);
+                 rcnt.p, D, key.p, perm.p, jt ? 1u : 1u - kTabBits, plan && piv_ranges ? 1u : 0u);
       radix_sort(X, key.p, perm.p, D, 25, true);
       DBuf<uint4> rec_s = X.alloc<uint4>(2 * D);
       DBuf<uint32_t> rcnt_s = X.alloc<uint32_t>(D);
@@ -825,12 +858,37 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
                  rec_s.p, rcnt_s.p);
       rec = std::move(rec_s);
       rcnt = std::move(rcnt_s);
+      if (plan && seg_rows > D) {
+        // per-kind row segments after the sorted rows: compacted in sorted
+        // order, their shared-prefix lengths recomputed within the segment
+        DBuf<uint4> rec_a = X.alloc<uint4>(2 * seg_rows);
+        DBuf<uint32_t> rcnt_a = X.alloc<uint32_t>(seg_rows), perm_a = X.alloc<uint32_t>(seg_rows);
+        DBuf<uint64_t> key_a = X.alloc<uint64_t>(seg_rows);
+        D3G_CUDA(cudaMemcpyAsync(rec_a.p, rec.p, D * 32, cudaMemcpyDeviceToDevice, X.stream));
+        D3G_CUDA(cudaMemcpyAsync(rcnt_a.p, rcnt.p, D * 4, cudaMemcpyDeviceToDevice, X.stream));
+        D3G_CUDA(cudaMemcpyAsync(perm_a.p, perm.p, D * 4, cudaMemcpyDeviceToDevice, X.stream));
+        D3G_CUDA(cudaMemcpyAsync(key_a.p, key.p, D * 8, cudaMemcpyDeviceToDevice, X.stream));
+        DBuf<uint32_t> flag = X.alloc<uint32_t>(D);
+        DBuf<uint64_t> pos = X.alloc<uint64_t>(D + 1);
+        for (uint32_t k = 1; k < n_kinds; ++k) {
+          if (!kind_batches[k] || kind_hi[k] == kind_lo[k]) continue;
+          D3G_LAUNCH(X, kind_flag_kernel, grid_for(D, 256), 256, 0, rcnt.p, D, k, flag.p);
+          exclusive_scan<uint32_t>(X, flag.p, D, pos.p);
+          D3G_LAUNCH(X, kind_gather_kernel, grid_for(D, 256), 256, 0, rec.p, rcnt.p, key.p, perm.p,
+                     flag.p, pos.p, D, kind_lo[k], rec_a.p, rcnt_a.p, key_a.p, perm_a.p);
+          D3G_LAUNCH(X, kind_prefix_kernel, grid_for(kind_hi[k] - kind_lo[k], 256), 256, 0,
+                     rcnt_a.p, key_a.p, kind_lo[k], kind_hi[k]);
+        }
+        rec = std::move(rec_a);
+        rcnt = std::move(rcnt_a);
+        perm = std::move(perm_a);
+      }
       if (jt_trie) {
         // slice reads of every (batch, row) the kernel tests, with and without
         // the prefix sharing
         for (uint32_t shared = 0; shared < 2; ++shared) {
           unsigned long long* dst = shared ? lds_units : &tallies.p[4].count;
-          for (uint32_t q = 0; q < 4; ++q) {
+          for (uint32_t q = 0; q < 8; ++q) {
             const uint64_t rows = kind_hi[q] - kind_lo[q];
             if (!kind_batches[q] || !rows) continue;
             D3G_LAUNCH(X, trie_lds_kernel, grid_for(rows, 256), 256, 0, rcnt.p, rows,
