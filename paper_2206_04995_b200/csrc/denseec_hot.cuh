@@ -1706,9 +1706,13 @@ dense_cold_hash_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
 // cold segments are (per-y loops left most of the 512 threads idle).
 constexpr int kOvThreads = 512;
 constexpr uint32_t kOvTouched = 65536;  // touched-word list per CTA
+#ifndef D3G_OV_UNROLL
+#define D3G_OV_UNROLL 2
+#endif
+constexpr int kOvUnroll = D3G_OV_UNROLL;
 
 template <int kMode>
-__global__ void __launch_bounds__(kOvThreads)
+__global__ void __launch_bounds__(kOvThreads, 3)
 dense_cold_overflow_kernel(const uint32_t* __restrict__ over_x, const unsigned int* __restrict__ over_n,
                            const uint64_t* __restrict__ r_ptr, const uint32_t* __restrict__ r_col,
                            const uint64_t* __restrict__ cptr, const uint32_t* __restrict__ ccol,
@@ -1783,33 +1787,54 @@ dense_cold_overflow_kernel(const uint32_t* __restrict__ over_x, const unsigned i
         __syncthreads();
         const uint32_t total = s_total;
         const uint32_t ny = (uint32_t)((r1 - yb) < kOvThreads ? (r1 - yb) : kOvThreads);
-        for (uint32_t f = threadIdx.x; f < total; f += kOvThreads) {
-          uint32_t lo = 0, hi = ny;  // last segment starting at or before f
-          while (hi - lo > 1) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (s_off[mid] <= f) lo = mid; else hi = mid;
-          }
-          const uint64_t t = s_seg0[lo] + (f - s_off[lo]);
-          ++ncand;
-          uint4 b0, b1;
-          ld256(ch + 2 * t, b0, b1);
-          const bool hot = ((a0.x & b0.x) | (a0.y & b0.y) | (a0.z & b0.z) | (a0.w & b0.w) |
-                            (a1.x & b1.x) | (a1.y & b1.y) | (a1.z & b1.z) | (a1.w & b1.w)) != 0;
-          if (hot) continue;
-          const uint32_t zl = ccol[t];
-          if (pass == 0) {
-            const uint32_t bit = 1u << (zl & 31);
-            const uint32_t old = atomicOr(&bm[zl >> 5], bit);
-            if (old & bit) continue;
-            if (old == 0) {
-              const unsigned int slot = atomicAdd(&s_nt, 1u);
-              if (slot < kOvTouched) tl[slot] = zl >> 5;
+        // kOvUnroll candidates per thread in flight: the signature and row-id
+        // loads of all of them are issued before any is consumed (the loop is
+        // bound by the dependent global loads, not by bandwidth)
+        for (uint32_t fb = threadIdx.x; fb < total; fb += kOvThreads * kOvUnroll) {
+          uint64_t t[kOvUnroll];
+          bool ok[kOvUnroll];
+#pragma unroll
+          for (int u = 0; u < kOvUnroll; ++u) {
+            const uint32_t f = fb + u * kOvThreads;
+            ok[u] = f < total;
+            uint32_t lo = 0, hi = ny;  // last segment starting at or before f
+            while (ok[u] && hi - lo > 1) {
+              const uint32_t mid = (lo + hi) >> 1;
+              if (s_off[mid] <= f) lo = mid; else hi = mid;
             }
-            ++cnt;
-            if (row_sp && row_sp[zl]) ++csp;
-            if (kMode != kModeCount) cold_account<kMode>(x, dl_z[zl], dec, em, sum, xr);
-          } else {
-            bm[zl >> 5] = 0;
+            t[u] = ok[u] ? s_seg0[lo] + (f - s_off[lo]) : 0;
+          }
+          uint4 b0[kOvUnroll], b1[kOvUnroll];
+          uint32_t zc[kOvUnroll];
+#pragma unroll
+          for (int u = 0; u < kOvUnroll; ++u)
+            if (ok[u]) {
+              ++ncand;
+              ld256(ch + 2 * t[u], b0[u], b1[u]);
+              zc[u] = ccol[t[u]];
+            }
+#pragma unroll
+          for (int u = 0; u < kOvUnroll; ++u) {
+            if (!ok[u]) continue;
+            const bool hot = ((a0.x & b0[u].x) | (a0.y & b0[u].y) | (a0.z & b0[u].z) |
+                              (a0.w & b0[u].w) | (a1.x & b1[u].x) | (a1.y & b1[u].y) |
+                              (a1.z & b1[u].z) | (a1.w & b1[u].w)) != 0;
+            if (hot) continue;
+            const uint32_t zl = zc[u];
+            if (pass == 0) {
+              const uint32_t bit = 1u << (zl & 31);
+              const uint32_t old = atomicOr(&bm[zl >> 5], bit);
+              if (old & bit) continue;
+              if (old == 0) {
+                const unsigned int slot = atomicAdd(&s_nt, 1u);
+                if (slot < kOvTouched) tl[slot] = zl >> 5;
+              }
+              ++cnt;
+              if (row_sp && row_sp[zl]) ++csp;
+              if (kMode != kModeCount) cold_account<kMode>(x, dl_z[zl], dec, em, sum, xr);
+            } else {
+              bm[zl >> 5] = 0;
+            }
           }
         }
         __syncthreads();  // s_off / s_seg0 are rewritten by the next chunk
