@@ -1847,4 +1847,163 @@ dense_cold_overflow_kernel(const uint32_t* __restrict__ over_x, const unsigned i
   tally_flush(tally, cnt, sum, xr);
 }
 
+// Overflow x of dense_cold_hash_kernel, first tier: one CTA per x with a
+// CTA-wide shared-memory hash set of kCCSlots rows over the same flattened
+// candidate stream as dense_cold_overflow_kernel (no global bitmap: those are
+// 1.25 MB per CTA on cfg5 and thrash L2, 130 GB of DRAM traffic). An x whose
+// survivors pass cc_max is abandoned exactly and queued for the bitmap kernel.
+constexpr int kCCThreads = 1024;
+constexpr uint32_t kCCSlots = 32768;  // 128 KB
+constexpr uint32_t kCCMax = 24576;    // load limit 0.75
+
+__device__ __forceinline__ uint32_t cc_slot(uint32_t v) { return (v * 0x9E3779B1u) >> 17; }
+
+template <int kMode>
+__global__ void __launch_bounds__(kCCThreads, 1)
+dense_cold_cta_kernel(const uint32_t* __restrict__ over_x, const unsigned int* __restrict__ over_n,
+                           const uint64_t* __restrict__ r_ptr, const uint32_t* __restrict__ r_col,
+                           const uint64_t* __restrict__ cptr, const uint32_t* __restrict__ ccol,
+                           const uint4* __restrict__ ch, const uint4* __restrict__ hx4,
+                           uint64_t y_card, uint32_t var_bits, const uint32_t* __restrict__ dl_z,
+                           Decode dec, Emit em, uint32_t* __restrict__ over2_x,
+                           unsigned int* __restrict__ over2_n, uint32_t cc_max,
+                           Tally* tally, const uint8_t* __restrict__ row_sp,
+                           unsigned long long* __restrict__ cnt_sp,
+                           unsigned long long* __restrict__ cand = nullptr) {
+  __shared__ uint64_t s_seg0[kCCThreads];
+  __shared__ uint32_t s_off[kCCThreads];
+  __shared__ uint32_t s_wsum[kCCThreads / 32];
+  __shared__ uint32_t s_total;
+  __shared__ unsigned int s_ins, s_over;
+  extern __shared__ __align__(16) uint32_t cctab[];  // [kCCSlots]
+  for (uint32_t i = threadIdx.x; i < kCCSlots; i += kCCThreads) cctab[i] = kCHEmpty;
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  constexpr uint32_t kW = kCCThreads / 32;
+  const uint32_t n = *over_n;
+  uint64_t cnt = 0, sum = 0, xr = 0, csp = 0, ncand = 0;
+  for (uint32_t it = blockIdx.x; it < n; it += gridDim.x) {
+    const uint32_t x = over_x[it];
+    uint4 a0, a1;
+    ld256(hx4 + 2 * (uint64_t)x, a0, a1);
+    const uint32_t v = a0.x & ((1u << var_bits) - 1);
+    const uint64_t* cp = cptr + (uint64_t)v * y_card;
+    const uint64_t r0 = r_ptr[x], r1 = r_ptr[x + 1];
+    if (threadIdx.x == 0) {
+      s_ins = 0;
+      s_over = 0;
+    }
+    __syncthreads();
+    {
+      for (uint64_t yb = r0; yb < r1 && !s_over; yb += kCCThreads) {
+        const uint64_t k = yb + threadIdx.x;
+        uint64_t sg0 = 0;
+        uint32_t len = 0;
+        if (k < r1) {
+          const uint32_t y = r_col[k];
+          sg0 = cp[y];
+          len = (uint32_t)(cp[y + 1] - sg0);
+        }
+        uint32_t incl = len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= (uint32_t)o) incl += u;
+        }
+        if (lane == 31) s_wsum[warp] = incl;
+        __syncthreads();
+        if (warp == 0) {
+          const uint32_t wv = lane < kW ? s_wsum[lane] : 0u;
+          uint32_t wi = wv;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= (uint32_t)o) wi += u;
+          }
+          if (lane < kW) s_wsum[lane] = wi - wv;  // exclusive over warps
+          if (lane == kW - 1) s_total = wi;
+        }
+        __syncthreads();
+        s_off[threadIdx.x] = s_wsum[warp] + incl - len;
+        s_seg0[threadIdx.x] = sg0;
+        __syncthreads();
+        const uint32_t total = s_total;
+        const uint32_t ny = (uint32_t)((r1 - yb) < kCCThreads ? (r1 - yb) : kCCThreads);
+        // kOvUnroll candidates per thread in flight: the signature and row-id
+        // loads of all of them are issued before any is consumed (the loop is
+        // bound by the dependent global loads, not by bandwidth)
+        for (uint32_t fb0 = 0; fb0 < total && !*(volatile unsigned int*)&s_over;
+             fb0 += kCCThreads * kOvUnroll) {
+          const uint32_t fb = fb0 + threadIdx.x;
+          uint32_t nf = 0;  // fresh inserts by this thread in this step
+          uint64_t t[kOvUnroll];
+          bool ok[kOvUnroll];
+#pragma unroll
+          for (int u = 0; u < kOvUnroll; ++u) {
+            const uint32_t f = fb + u * kCCThreads;
+            ok[u] = f < total;
+            uint32_t lo = 0, hi = ny;  // last segment starting at or before f
+            while (ok[u] && hi - lo > 1) {
+              const uint32_t mid = (lo + hi) >> 1;
+              if (s_off[mid] <= f) lo = mid; else hi = mid;
+            }
+            t[u] = ok[u] ? s_seg0[lo] + (f - s_off[lo]) : 0;
+          }
+          uint4 b0[kOvUnroll], b1[kOvUnroll];
+          uint32_t zc[kOvUnroll];
+#pragma unroll
+          for (int u = 0; u < kOvUnroll; ++u)
+            if (ok[u]) {
+              ++ncand;
+              ld256(ch + 2 * t[u], b0[u], b1[u]);
+              zc[u] = ccol[t[u]];
+            }
+#pragma unroll
+          for (int u = 0; u < kOvUnroll; ++u) {
+            if (!ok[u]) continue;
+            const bool hot = ((a0.x & b0[u].x) | (a0.y & b0[u].y) | (a0.z & b0[u].z) |
+                              (a0.w & b0[u].w) | (a1.x & b1[u].x) | (a1.y & b1[u].y) |
+                              (a1.z & b1[u].z) | (a1.w & b1[u].w)) != 0;
+            if (hot) continue;
+            const uint32_t zl = zc[u];
+            uint32_t sl = cc_slot(zl);
+            for (uint32_t probe = 0; probe < kCCSlots; ++probe) {
+              const uint32_t prev = atomicCAS(&cctab[sl], kCHEmpty, zl);
+              if (prev == kCHEmpty) {
+                ++nf;
+                break;
+              }
+              if (prev == zl) break;
+              sl = (sl + 1) & (kCCSlots - 1);
+            }
+          }
+          const uint32_t wf = warp_sum(nf);
+          if (lane == 0 && wf && atomicAdd(&s_ins, wf) + wf > cc_max) s_over = 1;
+        }
+        __syncthreads();  // s_off / s_seg0 are rewritten by the next chunk
+      }
+    }
+    __syncthreads();
+    const bool over = s_over != 0;
+    if (over) {
+      if (threadIdx.x == 0) over2_x[atomicAdd(over2_n, 1u)] = x;
+    } else if (threadIdx.x == 0) {
+      cnt += s_ins;
+    }
+    for (uint32_t i = threadIdx.x; i < kCCSlots; i += kCCThreads) {
+      const uint32_t zl = cctab[i];
+      if (zl != kCHEmpty) {
+        if (!over) {
+          if (kMode != kModeCount) cold_account<kMode>(x, dl_z[zl], dec, em, sum, xr);
+          if (row_sp && row_sp[zl]) ++csp;
+        }
+        cctab[i] = kCHEmpty;
+      }
+    }
+    __syncthreads();
+  }
+  flush_sp(cnt_sp, csp);
+  flush_cand(cand, ncand);
+  tally_flush(tally, cnt, sum, xr);
+}
+
 }  // namespace d3g

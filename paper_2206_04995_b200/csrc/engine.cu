@@ -135,6 +135,7 @@ struct KernelOut {
   uint64_t count = 0, sum = 0, xr = 0;
   uint64_t inner = 0;
   uint64_t cold_overflow = 0;  // x handed to the overflow kernel (diagnostics)
+  uint64_t cold_overflow2 = 0;  // of those, x past the CTA hash tier
   uint64_t count_sp = 0;      // pairs of rows flagged in DenseInputs::row_sp
   double ms_hot = 0;          // CUDA-event time of the hot-pass launch
   uint64_t hot_lds_bytes = 0;  // its algorithmic shared-memory bytes
@@ -981,22 +982,46 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
         });
         const unsigned int n_over = X.scalar(over_n.p);
         out.cold_overflow = n_over;
-        if (n_over) {
-          // CTAs per SM: the candidate stream is latency-bound, more CTAs in
-          // flight win (cfg5: 1/SM 89 ms, 2/SM 62 ms)
+        // overflowing x: a CTA-wide shared-memory hash first; the few past its
+        // limit go on to the CTA-private global bitmaps (1.25 MB each on cfg5,
+        // which thrash L2 when every overflowing x uses one)
+        const char* ov_env = std::getenv("D3G_COLD_OVERFLOW");
+        const bool cta_tier = !(ov_env && std::string(ov_env) == "bitmap");
+        unsigned int n_over2 = n_over;
+        DBuf<uint32_t> over2_x;
+        DBuf<unsigned int> over2_n;
+        if (n_over && cta_tier) {
+          over2_x = X.alloc<uint32_t>(n_over);
+          over2_n = X.zeros<unsigned int>(1);
+          const size_t csm2 = (size_t)kCCSlots * 4;
+          with_mode(mode, [&](auto M) {
+            auto kfn = dense_cold_cta_kernel<decltype(M)::value>;
+            D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm2));
+            D3G_LAUNCH(X, kfn, std::min<unsigned>(n_over, (unsigned)X.sm_count), kCCThreads, csm2,
+                       over_x.p, over_n.p, in.r_ptr, in.r_col, cptr.p, ccol.p, ch.p,
+                       reinterpret_cast<const uint4*>(hx.p), Y, var_bits, in.dl_z, dec, em,
+                       over2_x.p, over2_n.p, env_u32("D3G_COLD_CTA_MAX", kCCMax, 1, kCCMax), tc,
+                       in.row_sp, cnt_sp, cand);
+          });
+          n_over2 = X.scalar(over2_n.p);
+        }
+        if (n_over2) {
+          const uint32_t* ox = cta_tier ? over2_x.p : over_x.p;
+          const unsigned int* on = cta_tier ? over2_n.p : over_n.p;
           const uint64_t words = (D + 31) / 32;
           const unsigned og = (unsigned)std::min<uint64_t>(
-              (uint64_t)n_over,
+              (uint64_t)n_over2,
               (uint64_t)X.sm_count * env_u32("D3G_OVERFLOW_CTAS_PER_SM", 3, 1, 16));
           DBuf<uint32_t> gbm = X.zeros<uint32_t>((uint64_t)og * words);
           DBuf<uint32_t> touched = X.alloc<uint32_t>((uint64_t)og * kOvTouched);
           with_mode(mode, [&](auto M) {
-            D3G_LAUNCH(X, dense_cold_overflow_kernel<decltype(M)::value>, og, kOvThreads, 0, over_x.p,
-                       over_n.p, in.r_ptr, in.r_col, cptr.p, ccol.p, ch.p,
+            D3G_LAUNCH(X, dense_cold_overflow_kernel<decltype(M)::value>, og, kOvThreads, 0, ox,
+                       on, in.r_ptr, in.r_col, cptr.p, ccol.p, ch.p,
                        reinterpret_cast<const uint4*>(hx.p), Y, var_bits, in.dl_z, gbm.p, words,
                        dec, em, tc, in.row_sp, cnt_sp, touched.p, cand);
           });
         }
+        out.cold_overflow2 = n_over2;
       } else {
       size_t csm = (size_t)(part_rows / 32) * 4 * kColdWarps;
       with_mode(mode, [&](auto M) {
@@ -1047,11 +1072,11 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     out.cold_bytes = th[5].count * 36ull;  // 32-byte signature + 4-byte row id
   }
   if (std::getenv("D3G_TRACE"))
-    std::fprintf(stderr, "[dense_hot] D=%llu live=%llu K=%u hot=%llu cold=%llu cold_path=%s over=%llu\n",
+    std::fprintf(stderr, "[dense_hot] D=%llu live=%llu K=%u hot=%llu cold=%llu cold_path=%s over=%llu over2=%llu\n",
                  (unsigned long long)D, (unsigned long long)n_live, K, (unsigned long long)h.count,
                  (unsigned long long)cold.count,
                  cold_bitmap ? "bitmap" : cold_hash ? "hash" : "tiers",
-                 (unsigned long long)out.cold_overflow);
+                 (unsigned long long)out.cold_overflow, (unsigned long long)out.cold_overflow2);
   out.count = h.count + direct + cold.count;
   out.sum = h.sum + cold.sum;
   out.xr = h.xr ^ cold.xr;

@@ -390,3 +390,25 @@ def test_count_only_matches_reference(cfg):
     ref = g.get("ref_hybrid_report")
     if ref and cfg != 3:
         assert (rep.pairs_sparse, rep.pairs_dense) == (ref["pairs_sparse"], ref["pairs_dense"])
+
+
+def test_cfg5_cold_overflow_tiers_match_reference(monkeypatch):
+    """Both overflow tiers of the hash cold pass forced on the cfg5 slice: a
+    tiny per-warp limit sends most x to the CTA-hash tier and a tiny CTA limit
+    sends them on to the global-bitmap tier; the x<1000 slice still equals
+    the reference's."""
+    import torch
+    g = _golden().get("cfg5_x_lt_1000")
+    if g is None:
+        pytest.skip("golden entry not generated")
+    monkeypatch.setenv("D3G_COLD_HASH_MAX", "64")
+    monkeypatch.setenv("D3G_COLD_CTA_MAX", "256")
+    rl, rr = d3.generate(5, 0)
+    sl, sr = d3.generate(5, 1)
+    e = d3.EngineConfig(force=d3.Strategy.auto_select, count_only=True, checksum=True,
+                        memory_budget_bytes=120 << 30, x_code_range=(0, 1000))
+    rep = d3.join_project(d3.RawTable(rl, rr), d3.RawTable(sl, sr), e, C).report
+    assert (rep.out_p, rep.checksum_sum, rep.checksum_xor) == \
+        (g["set"]["count"], g["set"]["sum"], g["set"]["xor"])
+    del rl, rr, sl, sr
+    torch.cuda.empty_cache()
