@@ -327,6 +327,13 @@ def test_rank0_split_count_only_cfg2(monkeypatch):
     assert a.hot_direct_pairs > 0
     assert a.out_p == g["set"]["count"]
     assert (a.pairs_sparse, a.pairs_dense) == (ref["pairs_sparse"], ref["pairs_dense"])
+    # one, two (contiguous row ranges) and three pivots (row segments)
+    for piv in ("1", "2", "3"):
+        monkeypatch.setenv("D3G_PIVOTS", piv)
+        p = d3.join_project(d3.RawTable(rl, rr), d3.RawTable(sl, sr), e, C).report
+        assert p.hot_direct_pairs > 0, piv
+        assert (p.out_p, p.pairs_sparse, p.pairs_dense) == (a.out_p, a.pairs_sparse, a.pairs_dense)
+    monkeypatch.delenv("D3G_PIVOTS")
     monkeypatch.setenv("D3G_NO_SPLIT", "1")
     b = d3.join_project(d3.RawTable(rl, rr), d3.RawTable(sl, sr), e, C).report
     assert b.hot_direct_pairs == 0
