@@ -790,17 +790,6 @@ dense_hot_tab_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
   tally_flush(tally, cnt, sum, xr);
 }
 
-// Rows in [lo, hi) flagged as folded sparse rows (bit 31 of the count word).
-__global__ void sp_rows_kernel(const uint32_t* __restrict__ rcnt, uint64_t lo, uint64_t hi,
-                               unsigned long long* __restrict__ out) {
-  uint64_t acc = 0;
-  for (uint64_t i = lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hi;
-       i += (uint64_t)gridDim.x * blockDim.x)
-    acc += rcnt[i] >> 31;
-  acc = warp_sum(acc);
-  if (lane_id() == 0 && acc) atomicAdd(out, (unsigned long long)acc);
-}
-
 // Sort key of a record for the prefix-shared kernels: (subset mask, first
 // listed rank + 1, second listed rank + 1; 7/9/9 bits), 0 = absent.
 __global__ void trie_key_kernel(const uint8_t* __restrict__ rec, const uint32_t* __restrict__ rcnt,
@@ -1169,13 +1158,14 @@ dense_hot_jt_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(&bar, (n_listed + kTB) * 512u);
         tma_bulk_g2s(Ts, src + kTB * 32, n_listed * 512u, &bar);
-        for (uint32_t b = 0; b < kTB; ++b)
-          tma_bulk_g2s(sub_tab + (1u << b) * 32, src + b * 32, 512u, &bar);
+        if constexpr (kTab)
+          for (uint32_t b = 0; b < kTB; ++b)
+            tma_bulk_g2s(sub_tab + (1u << b) * 32, src + b * 32, 512u, &bar);
       }
       mbar_wait(&bar, phase);
       phase ^= 1;
       cur_batch = (int)bi;
-      for (uint32_t b = 1; b < kTB; ++b) {
+      if constexpr (kTab) for (uint32_t b = 1; b < kTB; ++b) {
         const uint32_t lo = 1u << b, n = (lo - 1) * 32;
         for (uint32_t t = threadIdx.x; t < n; t += blockDim.x) {
           const uint32_t e = lo + 1 + (t >> 5), l = t & 31;
