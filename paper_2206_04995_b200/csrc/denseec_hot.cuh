@@ -1671,7 +1671,7 @@ dense_cold_hash_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
     } else {
       cnt += lane == 0 ? inserted : 0;
     }
-    if (inserted) {
+    if (inserted && (kMode != kModeCount || row_sp)) {
       for (uint32_t i = lane; i < kCHSlots; i += 32) {
         const uint32_t zl = tab[i];
         if (zl != kCHEmpty) {
@@ -1680,6 +1680,12 @@ dense_cold_hash_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
           tab[i] = kCHEmpty;
         }
       }
+    } else if (inserted) {
+      // count only: nothing to read back, reset the table with 16-byte stores
+      uint4* t4 = reinterpret_cast<uint4*>(tab);
+      const uint4 e4 = make_uint4(kCHEmpty, kCHEmpty, kCHEmpty, kCHEmpty);
+#pragma unroll 4
+      for (uint32_t i = lane; i < kCHSlots / 4; i += 32) t4[i] = e4;
     }
     __syncwarp();
   }
