@@ -1068,10 +1068,11 @@ dense_hot_trie_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
 // rows: (L == 0) + c - max(L - 1, 0), with L forced to 0 on the first row of
 // each warp step (positions z_lo + 32k of the row's z chunk).
 __global__ void trie_lds_kernel(const uint32_t* __restrict__ rcnt, uint64_t n, uint32_t z_chunks,
-                                uint32_t sub_read, unsigned long long* __restrict__ out,
-                                uint64_t mult = 1, uint32_t shared = 1, uint64_t row0 = 0) {
+                                uint32_t sub_read, unsigned long long* __restrict__ out_shared,
+                                unsigned long long* __restrict__ out_unshared, uint64_t mult = 1,
+                                uint64_t row0 = 0) {
   rcnt += row0;  // rows [row0, row0 + n), chunked as the kernel chunks them
-  uint64_t acc = 0;
+  uint64_t acc = 0, acc_u = 0;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     uint64_t zc = i * z_chunks / n;
@@ -1079,11 +1080,15 @@ __global__ void trie_lds_kernel(const uint32_t* __restrict__ rcnt, uint64_t n, u
     while (zc > 0 && n * zc / z_chunks > i) --zc;
     const uint64_t z_lo = n * zc / z_chunks;
     const uint32_t cw = rcnt[i], c = cw & kTrieCntMask;
-    const uint32_t L = (!shared || (i - z_lo) % 32 == 0) ? 0u : (cw >> 22) & 3u;
+    const uint32_t L = ((i - z_lo) % 32 == 0) ? 0u : (cw >> 22) & 3u;
     acc += (L == 0 ? sub_read : 0u) + c - (L > 1 ? L - 1 : 0u);
+    acc_u += sub_read + c;  // the same row without prefix sharing
   }
   acc = warp_sum(acc);
-  if (lane_id() == 0 && acc) atomicAdd(out, (unsigned long long)(acc * mult));
+  acc_u = warp_sum(acc_u);
+  if (lane_id() == 0 && acc) atomicAdd(out_shared, (unsigned long long)(acc * mult));
+  if (lane_id() == 0 && acc_u && out_unshared)
+    atomicAdd(out_unshared, (unsigned long long)(acc_u * mult));
 }
 
 template <int kMode, bool kTrie, bool kTab = true>

@@ -887,15 +887,12 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
       if (jt_trie) {
         // slice reads of every (batch, row) the kernel tests, with and without
         // the prefix sharing
-        for (uint32_t shared = 0; shared < 2; ++shared) {
-          unsigned long long* dst = shared ? lds_units : &tallies.p[4].count;
-          for (uint32_t q = 0; q < 8; ++q) {
-            const uint64_t rows = kind_hi[q] - kind_lo[q];
-            if (!kind_batches[q] || !rows) continue;
-            D3G_LAUNCH(X, trie_lds_kernel, grid_for(rows, 256), 256, 0, rcnt.p, rows,
-                       plan ? kind_zc[q] : hp.z_chunks, tab ? 1u : 0u, dst,
-                       (uint64_t)kind_batches[q], shared, kind_lo[q]);
-          }
+        for (uint32_t q = 0; q < 8; ++q) {
+          const uint64_t rows = kind_hi[q] - kind_lo[q];
+          if (!kind_batches[q] || !rows) continue;
+          D3G_LAUNCH(X, trie_lds_kernel, grid_for(rows, 256), 256, 0, rcnt.p, rows,
+                     plan ? kind_zc[q] : hp.z_chunks, tab ? 1u : 0u, lds_units,
+                     &tallies.p[4].count, (uint64_t)kind_batches[q], kind_lo[q]);
         }
       }
     } else {
