@@ -539,8 +539,28 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   D3G_LAUNCH(X, k_estimate_kernel, grid_for(Y, 256), 256, 0, in.y_of_rank, in.dR, cnt_rank.p, Y, est.p);
   D3G_LAUNCH(X, hot_small_stats_kernel, 1, 32, 0, cnt_rank.p, in.y_of_rank, in.dR, Y,
              est.p + 2 * kKCand);
+  // the pivot-plan class counts (count-only) ride on the same read-back
+  const bool piv_pre = mode == kModeCount && std::getenv("D3G_HOT") == nullptr &&
+                       std::getenv("D3G_NO_SPLIT") == nullptr && Y >= 1;
+  const uint32_t n_batches_pre = (groups + 31) / 32;
+  const uint32_t piv_dflt = (double)n_batches_pre * (double)D > 1e9 ? 3u : 2u;
+  const uint32_t n_piv =
+      (uint32_t)std::min<uint64_t>(env_u32("D3G_PIVOTS", piv_dflt, 1, 3), std::max<uint64_t>(Y, 1));
+  DBuf<uint32_t> cls;
+  DBuf<unsigned long long> pcnt;
+  unsigned long long c[24] = {0};
+  if (piv_pre) {
+    cls = X.alloc<uint32_t>(n_live);
+    pcnt = X.zeros<unsigned long long>(24);  // x[8] rows[8] sp[8]
+    D3G_LAUNCH(X, pivot_class_x_kernel, grid_for(n_live, 256), 256, 0, xorder, n_live, in.r_ptr,
+               in.r_col, in.y_of_rank, n_piv, cls.p, pcnt.p);
+    D3G_LAUNCH(X, pivot_class_rows_kernel, grid_for(D, 256), 256, 0, in.dl_ptr, in.dl_col, D,
+               n_piv, in.row_sp, pcnt.p + 8);
+  }
   unsigned long long e[2 * kKCand + 11];
-  X.to_host(e, est.p, 2 * kKCand + 11);
+  X.defer(e, est.p, (2 * kKCand + 11) * 8);
+  if (piv_pre) X.defer(c, pcnt.p, 24 * 8);
+  X.sync();
   const unsigned long long* top_rank_rows = e + 2 * kKCand;   // [7]
   const unsigned long long* top_rank_dr = e + 2 * kKCand + 7;  // [4]
   static const uint32_t kv[kKCand] = {64, 128, 256, 512, 1024};
@@ -607,12 +627,9 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   // only the rows with no pivot in k: kind k's row segment, compacted from
   // the sorted rows (kind 0 = all rows); every other pair of the batch is
   // counted as a hit.
-  // three pivots pay for their per-kind row segments only on large passes
-  // (cfg5: hot 48 -> 31 ms; cfg2: +0.1 ms of segment builds); two pivots use
-  // contiguous ranges of the grouped row order instead (no segments)
-  const uint32_t piv_dflt = (double)n_batches * (double)D > 1e9 ? 3u : 2u;
-  const uint32_t n_piv =
-      (uint32_t)std::min<uint64_t>(env_u32("D3G_PIVOTS", piv_dflt, 1, 3), Y);
+  // three pivots (n_piv, above) pay for their per-kind row segments only on
+  // large passes (cfg5: hot 48 -> 31 ms; cfg2: +0.1 ms of segment builds);
+  // two pivots use contiguous ranges of the grouped row order instead
   const bool piv_ranges = n_piv == 2;  // grouped rows, kinds are ranges of [0, D)
   const uint32_t n_kinds = 1u << n_piv;
   uint64_t plan_direct = 0, plan_direct_sp = 0;  // untested hits (all / folded sparse rows)
@@ -624,17 +641,8 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   std::vector<uint32_t> unit_off_h;
   std::vector<uint8_t> batch_kind_h;
   DBuf<uint32_t> xsplit;
-  const bool try_plan = tab_planned && mode == kModeCount && Y >= 1 && top_rank_rows[0] > 0 &&
-                        std::getenv("D3G_NO_SPLIT") == nullptr;
+  const bool try_plan = piv_pre && tab_planned && top_rank_rows[0] > 0;
   if (try_plan) {
-    DBuf<uint32_t> cls = X.alloc<uint32_t>(n_live);
-    DBuf<unsigned long long> cc = X.zeros<unsigned long long>(24);  // x[8] rows[8] sp[8]
-    D3G_LAUNCH(X, pivot_class_x_kernel, grid_for(n_live, 256), 256, 0, xorder, n_live, in.r_ptr,
-               in.r_col, in.y_of_rank, n_piv, cls.p, cc.p);
-    D3G_LAUNCH(X, pivot_class_rows_kernel, grid_for(D, 256), 256, 0, in.dl_ptr, in.dl_col, D,
-               n_piv, in.row_sp, cc.p + 8);
-    unsigned long long c[24];
-    X.to_host(c, cc.p, 24);
     const unsigned long long* nx = c;       // x per class
     const unsigned long long* nr = c + 8;   // dense rows per class
     const unsigned long long* nsp = c + 16; // folded sparse rows per class
