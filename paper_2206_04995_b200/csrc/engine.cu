@@ -748,6 +748,8 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     if (cold_kernel_ok)
       while (var_bits < 3 && var_bits < Y && 2ull * top_rank_dr[var_bits] >= in.x_card)
         ++var_bits;
+    if (cold_kernel_ok && std::getenv("D3G_VAR_BITS"))  // experiments: 0..4
+      var_bits = (uint32_t)std::min<uint64_t>(env_u32("D3G_VAR_BITS", var_bits, 0, 4), Y);
     rows_key = ((uint64_t)1 << var_bits) * parts * Y;
     cc = X.zeros<uint32_t>(rows_key);
     D3G_LAUNCH(X, cold_count_kernel, grid_for(D * 8, 256), 256, 0, in.dl_ptr, in.dl_col, D, K,
