@@ -419,3 +419,29 @@ def test_cfg5_cold_overflow_tiers_match_reference(monkeypatch):
         (g["set"]["count"], g["set"]["sum"], g["set"]["xor"])
     del rl, rr, sl, sr
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("seed", [7, 8, 9])
+def test_pivot_plan_mid_size_instances(seed, monkeypatch):
+    """Mid-size skewed instances (x over 20-40k, Zipf y over a few hundred
+    values) where the pivot plan engages with mixed and pure batches: the
+    count-only count and pairs split equal the checksum-mode run (every pair
+    tested) for one, two and three pivots, in both orientations."""
+    rng = np.random.default_rng(seed)
+    nx, ny, n = int(rng.integers(20000, 40000)), int(rng.integers(200, 600)), 150000
+    w = 1.0 / np.arange(1, ny + 1) ** float(rng.uniform(0.9, 1.3))
+    w /= w.sum()
+    r = (rng.integers(0, nx, n).astype(np.uint64), rng.choice(ny, n, p=w).astype(np.uint64))
+    s = (rng.integers(0, nx // 2, n // 2).astype(np.uint64),
+         rng.choice(ny, n // 2, p=w).astype(np.uint64))
+    direct = 0
+    for a, b in ((r, s), (s, r)):
+        base = _run(a, b, d3.Strategy.auto_select, count_only=True, checksum=True).report
+        for piv in ("1", "2", "3"):
+            monkeypatch.setenv("D3G_PIVOTS", piv)
+            got = _run(a, b, d3.Strategy.auto_select, count_only=True).report
+            assert (got.out_p, got.pairs_sparse, got.pairs_dense) == \
+                (base.out_p, base.pairs_sparse, base.pairs_dense), (seed, piv)
+            direct += got.hot_direct_pairs
+        monkeypatch.delenv("D3G_PIVOTS")
+    assert direct > 0  # the plan engaged
