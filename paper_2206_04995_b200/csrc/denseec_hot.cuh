@@ -40,9 +40,9 @@ struct HotParams {
   // row arrays); every other (x, row) pair of that batch is a hit.
   // plan_units == 0: every batch tests all rows in z_chunks ranges.
   const uint32_t* unit_off = nullptr;  // [n_batches + 1] first unit of each batch
-  const uint8_t* batch_kind = nullptr; // [n_batches] row-range kind 0..7
-  uint64_t kind_lo[8] = {0, 0, 0, 0, 0, 0, 0, 0}, kind_hi[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  uint32_t kind_zc[8] = {1, 1, 1, 1, 1, 1, 1, 1};
+  const uint8_t* batch_kind = nullptr; // [n_batches] row-range kind 0..15
+  uint64_t kind_lo[16] = {}, kind_hi[16] = {};
+  uint32_t kind_zc[16] = {1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1};
   uint32_t plan_units = 0;
 };
 
@@ -74,14 +74,14 @@ __device__ __forceinline__ uint32_t hot_units(const HotParams& p, uint32_t n_bat
 }
 
 // Pivot class of each live x: bit q = holds y_of_rank[q] (q < n_piv; rows are
-// sorted by y, binary search); out[8] counts per class.
+// sorted by y, binary search); out[16] counts per class.
 __global__ void pivot_class_x_kernel(const uint32_t* __restrict__ xorder, uint64_t n_live,
                                      const uint64_t* __restrict__ r_ptr,
                                      const uint32_t* __restrict__ r_col,
                                      const uint32_t* __restrict__ y_of_rank, uint32_t n_piv,
                                      uint32_t* __restrict__ cls, unsigned long long* __restrict__ out) {
-  __shared__ unsigned int c8[8];
-  if (threadIdx.x < 8) c8[threadIdx.x] = 0;
+  __shared__ unsigned int c8[16];
+  if (threadIdx.x < 16) c8[threadIdx.x] = 0;
   __syncthreads();
   for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n_live;
        p += (uint64_t)gridDim.x * blockDim.x) {
@@ -101,18 +101,18 @@ __global__ void pivot_class_x_kernel(const uint32_t* __restrict__ xorder, uint64
     atomicAdd(&c8[c], 1u);
   }
   __syncthreads();
-  if (threadIdx.x < 8 && c8[threadIdx.x]) atomicAdd(&out[threadIdx.x], (unsigned long long)c8[threadIdx.x]);
+  if (threadIdx.x < 16 && c8[threadIdx.x]) atomicAdd(&out[threadIdx.x], (unsigned long long)c8[threadIdx.x]);
 }
 
 // Dense rows per pivot class (bit q = holds rank q; the lists are
 // rank-ascending, so the pivots sit at the front) and folded sparse rows per
-// class: out[0..7] rows, out[8..15] flagged rows.
+// class: out[0..15] rows, out[16..31] flagged rows.
 __global__ void pivot_class_rows_kernel(const uint64_t* __restrict__ dl_ptr,
                                         const uint32_t* __restrict__ dl_col, uint64_t n,
                                         uint32_t n_piv, const uint8_t* __restrict__ row_sp,
                                         unsigned long long* __restrict__ out) {
-  __shared__ unsigned int c16[16];
-  if (threadIdx.x < 16) c16[threadIdx.x] = 0;
+  __shared__ unsigned int c16[32];
+  if (threadIdx.x < 32) c16[threadIdx.x] = 0;
   __syncthreads();
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
@@ -123,10 +123,10 @@ __global__ void pivot_class_rows_kernel(const uint64_t* __restrict__ dl_ptr,
       if (r < n_piv) c |= 1u << r; else break;
     }
     atomicAdd(&c16[c], 1u);
-    if (row_sp && row_sp[i]) atomicAdd(&c16[8 + c], 1u);
+    if (row_sp && row_sp[i]) atomicAdd(&c16[16 + c], 1u);
   }
   __syncthreads();
-  if (threadIdx.x < 16 && c16[threadIdx.x]) atomicAdd(&out[threadIdx.x], (unsigned long long)c16[threadIdx.x]);
+  if (threadIdx.x < 32 && c16[threadIdx.x]) atomicAdd(&out[threadIdx.x], (unsigned long long)c16[threadIdx.x]);
 }
 
 // Per-kind row segment: the sorted rows sharing no pivot with kind k (class

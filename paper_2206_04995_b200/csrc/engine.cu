@@ -543,23 +543,24 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   const bool piv_pre = mode == kModeCount && std::getenv("D3G_HOT") == nullptr &&
                        std::getenv("D3G_NO_SPLIT") == nullptr && Y >= 1;
   const uint32_t n_batches_pre = (groups + 31) / 32;
-  const uint32_t piv_dflt = (double)n_batches_pre * (double)D > 1e9 ? 3u : 2u;
+  const double units_pre = (double)n_batches_pre * (double)D;
+  const uint32_t piv_dflt = units_pre > 1e10 ? 4u : units_pre > 1e9 ? 3u : 2u;
   const uint32_t n_piv =
-      (uint32_t)std::min<uint64_t>(env_u32("D3G_PIVOTS", piv_dflt, 1, 3), std::max<uint64_t>(Y, 1));
+      (uint32_t)std::min<uint64_t>(env_u32("D3G_PIVOTS", piv_dflt, 1, 4), std::max<uint64_t>(Y, 1));
   DBuf<uint32_t> cls;
   DBuf<unsigned long long> pcnt;
-  unsigned long long c[24] = {0};
+  unsigned long long c[48] = {0};
   if (piv_pre) {
     cls = X.alloc<uint32_t>(n_live);
-    pcnt = X.zeros<unsigned long long>(24);  // x[8] rows[8] sp[8]
+    pcnt = X.zeros<unsigned long long>(48);  // x[16] rows[16] sp[16]
     D3G_LAUNCH(X, pivot_class_x_kernel, grid_for(n_live, 256), 256, 0, xorder, n_live, in.r_ptr,
                in.r_col, in.y_of_rank, n_piv, cls.p, pcnt.p);
     D3G_LAUNCH(X, pivot_class_rows_kernel, grid_for(D, 256), 256, 0, in.dl_ptr, in.dl_col, D,
-               n_piv, in.row_sp, pcnt.p + 8);
+               n_piv, in.row_sp, pcnt.p + 16);
   }
   unsigned long long e[2 * kKCand + 11];
   X.defer(e, est.p, (2 * kKCand + 11) * 8);
-  if (piv_pre) X.defer(c, pcnt.p, 24 * 8);
+  if (piv_pre) X.defer(c, pcnt.p, 48 * 8);
   X.sync();
   const unsigned long long* top_rank_rows = e + 2 * kKCand;   // [7]
   const unsigned long long* top_rank_dr = e + 2 * kKCand + 7;  // [4]
@@ -633,10 +634,10 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   const bool piv_ranges = n_piv == 2;  // grouped rows, kinds are ranges of [0, D)
   const uint32_t n_kinds = 1u << n_piv;
   uint64_t plan_direct = 0, plan_direct_sp = 0;  // untested hits (all / folded sparse rows)
-  uint64_t kind_rows[8] = {D, 0, 0, 0, 0, 0, 0, 0};  // rows tested by a batch of kind k
-  uint64_t kind_lo[8] = {0, 0, 0, 0, 0, 0, 0, 0}, kind_hi[8] = {D, 0, 0, 0, 0, 0, 0, 0};
-  uint32_t kind_zc[8] = {1, 1, 1, 1, 1, 1, 1, 1};
-  uint32_t kind_batches[8] = {n_batches, 0, 0, 0, 0, 0, 0, 0};
+  uint64_t kind_rows[16] = {D};  // rows tested by a batch of kind k
+  uint64_t kind_lo[16] = {}, kind_hi[16] = {D};
+  uint32_t kind_zc[16] = {1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1};
+  uint32_t kind_batches[16] = {n_batches};
   uint64_t seg_rows = D;  // rows of the concatenated kind segments
   std::vector<uint32_t> unit_off_h;
   std::vector<uint8_t> batch_kind_h;
@@ -644,9 +645,9 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   const bool try_plan = piv_pre && tab_planned && top_rank_rows[0] > 0;
   if (try_plan) {
     const unsigned long long* nx = c;       // x per class
-    const unsigned long long* nr = c + 8;   // dense rows per class
-    const unsigned long long* nsp = c + 16; // folded sparse rows per class
-    uint64_t sp_rows[8] = {0, 0, 0, 0, 0, 0, 0, 0}, sp_all = 0;
+    const unsigned long long* nr = c + 16;  // dense rows per class
+    const unsigned long long* nsp = c + 32; // folded sparse rows per class
+    uint64_t sp_rows[16] = {}, sp_all = 0;
     for (uint32_t q = 0; q < n_kinds; ++q) sp_all += nsp[q];
     for (uint32_t k = 0; k < n_kinds; ++k) {
       kind_rows[k] = 0;
@@ -657,8 +658,8 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
         }
     }
     // class q occupies x positions [cstart[q], cstart[q + 1]) after the split
-    uint64_t cstart[9] = {0};
-    for (uint32_t q = 0; q < 8; ++q) cstart[q + 1] = cstart[q] + (q < n_kinds ? nx[q] : 0);
+    uint64_t cstart[17] = {0};
+    for (uint32_t q = 0; q < 16; ++q) cstart[q + 1] = cstart[q] + (q < n_kinds ? nx[q] : 0);
     batch_kind_h.assign(n_batches, 0);
     double tested = 0;
     uint64_t direct = 0, direct_sp = 0;
@@ -679,7 +680,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
       xorder = xsplit.p;
       plan_direct = direct;
       plan_direct_sp = direct_sp;
-      std::fill(kind_batches, kind_batches + 8, 0u);
+      std::fill(kind_batches, kind_batches + 16, 0u);
       for (uint32_t b = 0; b < n_batches; ++b) ++kind_batches[batch_kind_h[b]];
       // segments: kind 0 = the sorted rows themselves, then each used kind;
       // with two pivots the grouped order (classes 2, 0, 1, 3) makes every
@@ -784,7 +785,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     X.to_device(batch_kind_d.p, batch_kind_h.data(), n_batches);
     hp.unit_off = unit_off_d.p;
     hp.batch_kind = batch_kind_d.p;
-    for (uint32_t q = 0; q < 8; ++q) {
+    for (uint32_t q = 0; q < 16; ++q) {
       hp.kind_lo[q] = kind_lo[q];
       hp.kind_hi[q] = kind_hi[q];
       hp.kind_zc[q] = kind_zc[q];
@@ -897,7 +898,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
       if (jt_trie) {
         // slice reads of every (batch, row) the kernel tests, with and without
         // the prefix sharing
-        for (uint32_t q = 0; q < 8; ++q) {
+        for (uint32_t q = 0; q < 16; ++q) {
           const uint64_t rows = kind_hi[q] - kind_lo[q];
           if (!kind_batches[q] || !rows) continue;
           D3G_LAUNCH(X, trie_lds_kernel, grid_for(rows, 256), 256, 0, rcnt.p, rows,

@@ -328,7 +328,7 @@ def test_rank0_split_count_only_cfg2(monkeypatch):
     assert a.out_p == g["set"]["count"]
     assert (a.pairs_sparse, a.pairs_dense) == (ref["pairs_sparse"], ref["pairs_dense"])
     # one, two (contiguous row ranges) and three pivots (row segments)
-    for piv in ("1", "2", "3"):
+    for piv in ("1", "2", "3", "4"):
         monkeypatch.setenv("D3G_PIVOTS", piv)
         p = d3.join_project(d3.RawTable(rl, rr), d3.RawTable(sl, sr), e, C).report
         assert p.hot_direct_pairs > 0, piv
@@ -437,7 +437,7 @@ def test_pivot_plan_mid_size_instances(seed, monkeypatch):
     direct = 0
     for a, b in ((r, s), (s, r)):
         base = _run(a, b, d3.Strategy.auto_select, count_only=True, checksum=True).report
-        for piv in ("1", "2", "3"):
+        for piv in ("1", "2", "3", "4"):
             monkeypatch.setenv("D3G_PIVOTS", piv)
             got = _run(a, b, d3.Strategy.auto_select, count_only=True).report
             assert (got.out_p, got.pairs_sparse, got.pairs_dense) == \
