@@ -35,14 +35,15 @@ struct HotParams {
   unsigned int* work;
   // Pivot plan (count-only): x and dense rows are classed by which of the
   // top ranks (pivots) they hold; a batch whose x share the pivot set k (the
-  // AND of their classes) tests only the rows sharing no pivot with k (kind
-  // k: a contiguous segment [kind_lo, kind_hi) of the concatenated per-kind
-  // row arrays); every other (x, row) pair of that batch is a hit.
-  // plan_units == 0: every batch tests all rows in z_chunks ranges.
+  // AND of their classes) tests only the rows of the classes sharing no pivot
+  // with k (kind k: those class runs of the class-major row order); every
+  // other (x, row) pair of that batch is a hit. plan_units == 0: every batch
+  // tests all rows in z_chunks ranges.
   const uint32_t* unit_off = nullptr;  // [n_batches + 1] first unit of each batch
   const uint8_t* batch_kind = nullptr; // [n_batches] row-range kind 0..15
-  uint64_t kind_lo[16] = {}, kind_hi[16] = {};
-  uint32_t kind_zc[16] = {1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1};
+  uint64_t run_lo[17] = {};  // class c's rows: [run_lo[c], run_lo[c + 1]) (class-major order)
+  uint32_t run_zc[16] = {};  // chunks (units per batch) of class c's run
+  uint32_t n_classes = 1;
   uint32_t plan_units = 0;
 };
 
@@ -63,10 +64,19 @@ __device__ __forceinline__ void hot_unit(const HotParams& p, uint32_t n_batches,
   }
   bi = lo;
   const uint32_t k = p.batch_kind[lo];
-  const uint32_t zcs = p.kind_zc[k], zc = unit - p.unit_off[lo];
-  const uint64_t n = p.kind_hi[k] - p.kind_lo[k];
-  z_lo = p.kind_lo[k] + n * zc / zcs;
-  z_hi = p.kind_lo[k] + n * (zc + 1) / zcs;
+  uint32_t u = unit - p.unit_off[lo];
+  z_lo = z_hi = 0;
+  for (uint32_t c = 0; c < p.n_classes; ++c) {  // the runs of kind k, in order
+    if (c & k) continue;
+    const uint32_t zcs = p.run_zc[c];
+    if (u < zcs) {
+      const uint64_t r0 = p.run_lo[c], n = p.run_lo[c + 1] - r0;
+      z_lo = r0 + n * u / zcs;
+      z_hi = r0 + n * (u + 1) / zcs;
+      return;
+    }
+    u -= zcs;
+  }
 }
 
 __device__ __forceinline__ uint32_t hot_units(const HotParams& p, uint32_t n_batches) {
@@ -127,55 +137,6 @@ __global__ void pivot_class_rows_kernel(const uint64_t* __restrict__ dl_ptr,
   }
   __syncthreads();
   if (threadIdx.x < 32 && c16[threadIdx.x]) atomicAdd(&out[threadIdx.x], (unsigned long long)c16[threadIdx.x]);
-}
-
-// Per-kind row segment: the sorted rows sharing no pivot with kind k (class
-// bits = the low n_piv bits of the subset mask), compacted in sorted order.
-__global__ void kind_flag_kernel(const uint32_t* __restrict__ rcnt, uint64_t n, uint32_t k,
-                                 uint32_t* __restrict__ flag) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x)
-    flag[i] = ((rcnt[i] >> 24) & k) == 0 ? 1u : 0u;
-}
-
-__global__ void kind_gather_kernel(const uint4* __restrict__ rec, const uint32_t* __restrict__ rcnt,
-                                   const uint64_t* __restrict__ key, const uint32_t* __restrict__ perm,
-                                   const uint32_t* __restrict__ flag, const uint64_t* __restrict__ pos,
-                                   uint64_t n, uint64_t dst0, uint4* __restrict__ rec_o,
-                                   uint32_t* __restrict__ rcnt_o, uint64_t* __restrict__ key_o,
-                                   uint32_t* __restrict__ perm_o) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    if (!flag[i]) continue;
-    const uint64_t d = dst0 + pos[i];
-    uint4 a, b;
-    ld256(rec + 2 * i, a, b);
-    st256(rec_o + 2 * d, a, b);
-    rcnt_o[d] = rcnt[i];
-    key_o[d] = key[i];
-    perm_o[d] = perm[i];
-  }
-}
-
-// Shared-prefix length L (bits 22-23 of the count word) against the previous
-// row of the same segment [seg_lo, seg_hi).
-__global__ void kind_prefix_kernel(uint32_t* __restrict__ rcnt, const uint64_t* __restrict__ key,
-                                   uint64_t seg_lo, uint64_t seg_hi) {
-  for (uint64_t i = seg_lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < seg_hi;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t L = 0;
-    if (i > seg_lo) {
-      const uint64_t k = key[i], kp = key[i - 1];
-      if ((k >> 18) == (kp >> 18)) {
-        L = 1;
-        if ((k & 0x3fe00u) && ((k >> 9) == (kp >> 9))) {
-          L = 2;
-          if ((k & 0x1ffu) && k == kp) L = 3;
-        }
-      }
-    }
-    rcnt[i] = (rcnt[i] & ~(3u << 22)) | (L << 22);
-  }
 }
 
 // T, hx from the live x in degree order: warp per x position.
@@ -795,22 +756,16 @@ dense_hot_tab_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
 __global__ void trie_key_kernel(const uint8_t* __restrict__ rec, const uint32_t* __restrict__ rcnt,
                                 uint64_t n, uint64_t* __restrict__ key, uint32_t* __restrict__ idx,
                                 uint32_t off /* stored rank byte + off = rank - 6 */,
-                                uint32_t group2 = 0) {
+                                uint32_t class_bits = 0) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t cw = rcnt[i], c = cw & 0xffffffu;
     const uint32_t r1 = c >= 1 ? rec[i * 32] + off : 0u;
     const uint32_t r2 = c >= 2 ? rec[i * 32 + 1] + off : 0u;
-    const uint32_t top = (cw >> 24) & 0x7fu;
-    if (group2) {
-      // two-pivot plan without segments: rows grouped by (rank 1, rank 0)
-      // class in the order 2, 0, 1, 3 so that the rows lacking rank 0, lacking
-      // rank 1, or lacking both are contiguous ranges
-      const uint32_t c = top & 3u, grp = c == 2 ? 0u : c == 0 ? 1u : c == 1 ? 2u : 3u;
-      key[i] = ((uint64_t)grp << 23) | ((uint64_t)(top >> 2) << 18) | (r1 << 9) | r2;
-    } else {
-      key[i] = ((uint64_t)top << 18) | (r1 << 9) | r2;
-    }
+    // pivot plan: rows class-major (class = the low class_bits bits of the
+    // subset mask), so every class is one contiguous run
+    const uint32_t top = (cw >> 24) & 0x7fu, cls = top & ((1u << class_bits) - 1u);
+    key[i] = ((uint64_t)cls << 25) | ((uint64_t)top << 18) | (r1 << 9) | r2;
     idx[i] = (uint32_t)i;
   }
 }

@@ -544,6 +544,8 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
                        std::getenv("D3G_NO_SPLIT") == nullptr && Y >= 1;
   const uint32_t n_batches_pre = (groups + 31) / 32;
   const double units_pre = (double)n_batches_pre * (double)D;
+  // measured: cfg5 (2.4e10 units) 2/3/4 pivots 153/135/132 ms; cfg2 (1e7)
+  // 2.30/2.31/2.41 ms
   const uint32_t piv_dflt = units_pre > 1e10 ? 4u : units_pre > 1e9 ? 3u : 2u;
   const uint32_t n_piv =
       (uint32_t)std::min<uint64_t>(env_u32("D3G_PIVOTS", piv_dflt, 1, 4), std::max<uint64_t>(Y, 1));
@@ -625,20 +627,14 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   // n_piv top ranks (pivots) they hold (bit q = rank q). A pair sharing a
   // pivot is a hit without a test. x are split stably by class into batches;
   // a batch whose x share the pivot set k (the AND of their classes) tests
-  // only the rows with no pivot in k: kind k's row segment, compacted from
-  // the sorted rows (kind 0 = all rows); every other pair of the batch is
-  // counted as a hit.
-  // three pivots (n_piv, above) pay for their per-kind row segments only on
-  // large passes (cfg5: hot 48 -> 31 ms; cfg2: +0.1 ms of segment builds);
-  // two pivots use contiguous ranges of the grouped row order instead
-  const bool piv_ranges = n_piv == 2;  // grouped rows, kinds are ranges of [0, D)
+  // only the rows of the classes with no pivot in k. The sorted rows are
+  // class-major, so those are a few contiguous class runs (no copies); every
+  // other pair of the batch is counted as a hit.
   const uint32_t n_kinds = 1u << n_piv;
   uint64_t plan_direct = 0, plan_direct_sp = 0;  // untested hits (all / folded sparse rows)
-  uint64_t kind_rows[16] = {D};  // rows tested by a batch of kind k
-  uint64_t kind_lo[16] = {}, kind_hi[16] = {D};
-  uint32_t kind_zc[16] = {1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1};
-  uint32_t kind_batches[16] = {n_batches};
-  uint64_t seg_rows = D;  // rows of the concatenated kind segments
+  uint64_t run_lo[17] = {0};     // class c's rows [run_lo[c], run_lo[c + 1])
+  uint32_t run_zc[16] = {0};     // units per batch over class c's run
+  uint64_t run_mult[16] = {0};   // batches that test class c's run
   std::vector<uint32_t> unit_off_h;
   std::vector<uint8_t> batch_kind_h;
   DBuf<uint32_t> xsplit;
@@ -647,16 +643,14 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     const unsigned long long* nx = c;       // x per class
     const unsigned long long* nr = c + 16;  // dense rows per class
     const unsigned long long* nsp = c + 32; // folded sparse rows per class
-    uint64_t sp_rows[16] = {}, sp_all = 0;
+    uint64_t kind_rows[16] = {}, sp_rows[16] = {}, sp_all = 0;
     for (uint32_t q = 0; q < n_kinds; ++q) sp_all += nsp[q];
-    for (uint32_t k = 0; k < n_kinds; ++k) {
-      kind_rows[k] = 0;
+    for (uint32_t k = 0; k < n_kinds; ++k)
       for (uint32_t q = 0; q < n_kinds; ++q)
         if ((q & k) == 0) {
           kind_rows[k] += nr[q];
           sp_rows[k] += nsp[q];
         }
-    }
     // class q occupies x positions [cstart[q], cstart[q + 1]) after the split
     uint64_t cstart[17] = {0};
     for (uint32_t q = 0; q < 16; ++q) cstart[q + 1] = cstart[q] + (q < n_kinds ? nx[q] : 0);
@@ -680,38 +674,26 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
       xorder = xsplit.p;
       plan_direct = direct;
       plan_direct_sp = direct_sp;
-      std::fill(kind_batches, kind_batches + 16, 0u);
-      for (uint32_t b = 0; b < n_batches; ++b) ++kind_batches[batch_kind_h[b]];
-      // segments: kind 0 = the sorted rows themselves, then each used kind;
-      // with two pivots the grouped order (classes 2, 0, 1, 3) makes every
-      // kind a range of [0, D)
-      seg_rows = D;
-      if (piv_ranges) {
-        kind_lo[1] = 0;
-        kind_hi[1] = nr[2] + nr[0];          // lacking rank 0
-        kind_lo[2] = nr[2];
-        kind_hi[2] = nr[2] + nr[0] + nr[1];  // lacking rank 1
-        kind_lo[3] = nr[2];
-        kind_hi[3] = nr[2] + nr[0];          // lacking both
-      } else {
-        for (uint32_t k = 1; k < n_kinds; ++k)
-          if (kind_batches[k]) {
-            kind_lo[k] = seg_rows;
-            kind_hi[k] = seg_rows + kind_rows[k];
-            seg_rows += kind_rows[k];
-          }
-      }
+      for (uint32_t q = 0; q < n_kinds; ++q) run_lo[q + 1] = run_lo[q] + nr[q];
       // units of about equal row counts (~8 per SM over the whole pass), so a
       // few all-row batches do not leave one CTA with millions of rows
       const double per_unit = std::max(256.0, tested / ((double)X.sm_count * 8));
-      for (uint32_t k = 0; k < n_kinds; ++k) {
-        const uint64_t rows = kind_hi[k] - kind_lo[k];
-        kind_zc[k] = std::max<uint32_t>(1, (uint32_t)std::min<double>(
-            std::ceil((double)rows / per_unit), (double)((rows + 255) / 256)));
+      for (uint32_t q = 0; q < n_kinds; ++q) {
+        const uint64_t rows = nr[q];
+        run_zc[q] = rows ? std::max<uint32_t>(1, (uint32_t)std::min<double>(
+                               std::ceil((double)rows / per_unit), (double)((rows + 255) / 256)))
+                         : 0u;
       }
       unit_off_h.assign(n_batches + 1, 0);
-      for (uint32_t b = 0; b < n_batches; ++b)
-        unit_off_h[b + 1] = unit_off_h[b] + kind_zc[batch_kind_h[b]];
+      for (uint32_t b = 0; b < n_batches; ++b) {
+        uint32_t u = 0;
+        for (uint32_t q = 0; q < n_kinds; ++q)
+          if ((q & batch_kind_h[b]) == 0) {
+            u += run_zc[q];
+            ++run_mult[q];
+          }
+        unit_off_h[b + 1] = unit_off_h[b] + u;
+      }
     } else {
       batch_kind_h.clear();
     }
@@ -785,11 +767,9 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     X.to_device(batch_kind_d.p, batch_kind_h.data(), n_batches);
     hp.unit_off = unit_off_d.p;
     hp.batch_kind = batch_kind_d.p;
-    for (uint32_t q = 0; q < 16; ++q) {
-      hp.kind_lo[q] = kind_lo[q];
-      hp.kind_hi[q] = kind_hi[q];
-      hp.kind_zc[q] = kind_zc[q];
-    }
+    for (uint32_t q = 0; q <= 16; ++q) hp.run_lo[q] = run_lo[q];
+    for (uint32_t q = 0; q < 16; ++q) hp.run_zc[q] = run_zc[q];
+    hp.n_classes = n_kinds;
     hp.plan_units = unit_off_h[n_batches];
   }
   DBuf<unsigned int> work = X.zeros<unsigned int>(1);
@@ -862,48 +842,27 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
       DBuf<uint64_t> key = X.alloc<uint64_t>(D);
       perm = X.alloc<uint32_t>(D);
       D3G_LAUNCH(X, trie_key_kernel, grid_for(D, 256), 256, 0, reinterpret_cast<const uint8_t*>(rec.p),
-                 rcnt.p, D, key.p, perm.p, jt ? 1u : 1u - kTabBits, plan && piv_ranges ? 1u : 0u);
-      radix_sort(X, key.p, perm.p, D, 25, true);
+                 rcnt.p, D, key.p, perm.p, jt ? 1u : 1u - kTabBits, plan ? n_piv : 0u);
+      radix_sort(X, key.p, perm.p, D, 25 + (plan ? (int)n_piv : 0), true);
       DBuf<uint4> rec_s = X.alloc<uint4>(2 * D);
       DBuf<uint32_t> rcnt_s = X.alloc<uint32_t>(D);
       D3G_LAUNCH(X, trie_gather_kernel, grid_for(D, 256), 256, 0, rec.p, rcnt.p, key.p, perm.p, D,
                  rec_s.p, rcnt_s.p);
       rec = std::move(rec_s);
       rcnt = std::move(rcnt_s);
-      if (plan && seg_rows > D) {
-        // per-kind row segments after the sorted rows: compacted in sorted
-        // order, their shared-prefix lengths recomputed within the segment
-        DBuf<uint4> rec_a = X.alloc<uint4>(2 * seg_rows);
-        DBuf<uint32_t> rcnt_a = X.alloc<uint32_t>(seg_rows), perm_a = X.alloc<uint32_t>(seg_rows);
-        DBuf<uint64_t> key_a = X.alloc<uint64_t>(seg_rows);
-        D3G_CUDA(cudaMemcpyAsync(rec_a.p, rec.p, D * 32, cudaMemcpyDeviceToDevice, X.stream));
-        D3G_CUDA(cudaMemcpyAsync(rcnt_a.p, rcnt.p, D * 4, cudaMemcpyDeviceToDevice, X.stream));
-        D3G_CUDA(cudaMemcpyAsync(perm_a.p, perm.p, D * 4, cudaMemcpyDeviceToDevice, X.stream));
-        D3G_CUDA(cudaMemcpyAsync(key_a.p, key.p, D * 8, cudaMemcpyDeviceToDevice, X.stream));
-        DBuf<uint32_t> flag = X.alloc<uint32_t>(D);
-        DBuf<uint64_t> pos = X.alloc<uint64_t>(D + 1);
-        for (uint32_t k = 1; k < n_kinds; ++k) {
-          if (!kind_batches[k] || kind_hi[k] == kind_lo[k]) continue;
-          D3G_LAUNCH(X, kind_flag_kernel, grid_for(D, 256), 256, 0, rcnt.p, D, k, flag.p);
-          exclusive_scan<uint32_t>(X, flag.p, D, pos.p);
-          D3G_LAUNCH(X, kind_gather_kernel, grid_for(D, 256), 256, 0, rec.p, rcnt.p, key.p, perm.p,
-                     flag.p, pos.p, D, kind_lo[k], rec_a.p, rcnt_a.p, key_a.p, perm_a.p);
-          D3G_LAUNCH(X, kind_prefix_kernel, grid_for(kind_hi[k] - kind_lo[k], 256), 256, 0,
-                     rcnt_a.p, key_a.p, kind_lo[k], kind_hi[k]);
-        }
-        rec = std::move(rec_a);
-        rcnt = std::move(rcnt_a);
-        perm = std::move(perm_a);
-      }
       if (jt_trie) {
         // slice reads of every (batch, row) the kernel tests, with and without
         // the prefix sharing
-        for (uint32_t q = 0; q < 16; ++q) {
-          const uint64_t rows = kind_hi[q] - kind_lo[q];
-          if (!kind_batches[q] || !rows) continue;
-          D3G_LAUNCH(X, trie_lds_kernel, grid_for(rows, 256), 256, 0, rcnt.p, rows,
-                     plan ? kind_zc[q] : hp.z_chunks, tab ? 1u : 0u, lds_units,
-                     &tallies.p[4].count, (uint64_t)kind_batches[q], kind_lo[q]);
+        if (plan) {
+          for (uint32_t q = 0; q < n_kinds; ++q) {  // each class run, times its batches
+            const uint64_t rows = run_lo[q + 1] - run_lo[q];
+            if (!run_mult[q] || !rows) continue;
+            D3G_LAUNCH(X, trie_lds_kernel, grid_for(rows, 256), 256, 0, rcnt.p, rows, run_zc[q],
+                       tab ? 1u : 0u, lds_units, &tallies.p[4].count, run_mult[q], run_lo[q]);
+          }
+        } else {
+          D3G_LAUNCH(X, trie_lds_kernel, grid_for(D, 256), 256, 0, rcnt.p, D, hp.z_chunks,
+                     tab ? 1u : 0u, lds_units, &tallies.p[4].count, (uint64_t)n_batches, 0ull);
         }
       }
     } else {
