@@ -45,12 +45,13 @@ struct HotParams {
   uint32_t run_zc[16] = {};  // chunks (units per batch) of class c's run
   uint32_t n_classes = 1;
   uint32_t plan_units = 0;
+  uint32_t plan_on = 0;  // 1: units follow the plan (plan_units may be 0)
 };
 
 // Unit -> (batch, row range). Units are batch-major.
 __device__ __forceinline__ void hot_unit(const HotParams& p, uint32_t n_batches, uint32_t unit,
                                          uint32_t& bi, uint64_t& z_lo, uint64_t& z_hi) {
-  if (p.plan_units == 0) {
+  if (!p.plan_on) {
     bi = unit / p.z_chunks;
     const uint32_t zc = unit % p.z_chunks;
     z_lo = p.n_dense * zc / p.z_chunks;
@@ -80,7 +81,7 @@ __device__ __forceinline__ void hot_unit(const HotParams& p, uint32_t n_batches,
 }
 
 __device__ __forceinline__ uint32_t hot_units(const HotParams& p, uint32_t n_batches) {
-  return p.plan_units ? p.plan_units : n_batches * p.z_chunks;
+  return p.plan_on ? p.plan_units : n_batches * p.z_chunks;
 }
 
 // Pivot class of each live x: bit q = holds y_of_rank[q] (q < n_piv; rows are

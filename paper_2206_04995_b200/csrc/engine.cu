@@ -771,6 +771,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     for (uint32_t q = 0; q < 16; ++q) hp.run_zc[q] = run_zc[q];
     hp.n_classes = n_kinds;
     hp.plan_units = unit_off_h[n_batches];
+    hp.plan_on = 1;
   }
   DBuf<unsigned int> work = X.zeros<unsigned int>(1);
   hp.work = work.p;
@@ -786,7 +787,8 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   bool trie = false, jt_trie = false;
   size_t sm = (size_t)K * 32 * 16;
   const uint64_t n_units = plan ? (uint64_t)hp.plan_units : (uint64_t)n_batches * hp.z_chunks;
-  unsigned g = (unsigned)std::min<uint64_t>(n_units, (uint64_t)X.sm_count);
+  // (a plan can leave nothing to test: every pair shares a pivot)
+  unsigned g = (unsigned)std::min<uint64_t>(std::max<uint64_t>(n_units, 1), (uint64_t)X.sm_count);
   const char* hot_impl = std::getenv("D3G_HOT");
   const bool use_tc = hot_impl && std::string(hot_impl) == "tc" && mode == kModeCount &&
                       K % 32 == 0 && K <= 384;

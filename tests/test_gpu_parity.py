@@ -445,3 +445,22 @@ def test_pivot_plan_mid_size_instances(seed, monkeypatch):
             direct += got.hot_direct_pairs
         monkeypatch.delenv("D3G_PIVOTS")
     assert direct > 0  # the plan engaged
+
+
+def test_pivot_plan_with_nothing_left_to_test():
+    """Every x and every z hold the two top-ranked y (plus a few others): the
+    pivot plan answers every pair without a test (zero units for the hot
+    kernel); the count equals the checksum-mode run and |X| * |Z|."""
+    rng = np.random.default_rng(11)
+    nx, nz, extra = 9000, 7000, 40
+    def rel(n, keys):
+        a = np.concatenate([np.arange(n), np.arange(n), np.arange(n)]).astype(np.uint64)
+        b = np.concatenate([np.zeros(n), np.ones(n), 2 + rng.integers(0, extra, n)]).astype(np.uint64)
+        return a, b
+    r, s = rel(nx, 0), rel(nz, 1)
+    base = _run(r, s, d3.Strategy.auto_select, count_only=True, checksum=True).report
+    got = _run(r, s, d3.Strategy.auto_select, count_only=True).report
+    assert base.out_p == nx * nz
+    assert (got.out_p, got.pairs_sparse, got.pairs_dense) == \
+        (base.out_p, base.pairs_sparse, base.pairs_dense)
+    assert got.pairs_dense > 0 and got.hot_direct_pairs == got.pairs_dense  # all untested
