@@ -1496,11 +1496,17 @@ dense_cold_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
 // dense_cold_overflow_kernel. Count, fingerprint and emission are taken from
 // the hash table when x completes, so abandoning is exact.
 constexpr int kCHWarps = 8;
-constexpr uint32_t kCHSlots = 2048;  // per warp (8 KB)
-constexpr uint32_t kCHMax = 1536;    // load limit; < kCHSlots - 32 keeps probing finite
+// 1024 slots per warp and 4 CTAs per SM: more x overflow into the CTA-hash
+// tier, which handles them well, and the common x run at higher occupancy
+// (cfg5 cold pass: 2048 slots x 3 CTAs 61 ms, 1024 x 4 52 ms, 512 x 4 58 ms)
+#ifndef D3G_CH_BITS
+#define D3G_CH_BITS 10
+#endif
+constexpr uint32_t kCHSlots = 1u << D3G_CH_BITS;  // per warp (8 KB at 11 bits)
+constexpr uint32_t kCHMax = kCHSlots * 3 / 4;    // load limit; < kCHSlots - 64 keeps probing finite
 constexpr uint32_t kCHEmpty = 0xffffffffu;
 
-__device__ __forceinline__ uint32_t ch_slot(uint32_t v) { return (v * 0x9E3779B1u) >> 21; }
+__device__ __forceinline__ uint32_t ch_slot(uint32_t v) { return (v * 0x9E3779B1u) >> (32 - D3G_CH_BITS); }
 
 template <int kMode>
 __device__ __forceinline__ void cold_account(uint32_t x, uint32_t zc, const Decode& dec,
