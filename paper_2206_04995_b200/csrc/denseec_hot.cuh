@@ -1524,8 +1524,11 @@ __device__ __forceinline__ void cold_account(uint32_t x, uint32_t zc, const Deco
   }
 }
 
+#ifndef D3G_CH_CTAS
+#define D3G_CH_CTAS 4
+#endif
 template <int kMode>
-__global__ void __launch_bounds__(kCHWarps * 32)
+__global__ void __launch_bounds__(kCHWarps * 32, D3G_CH_CTAS)
 dense_cold_hash_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
                        const uint64_t* __restrict__ r_ptr, const uint32_t* __restrict__ r_col,
                        const uint64_t* __restrict__ cptr, const uint32_t* __restrict__ ccol,

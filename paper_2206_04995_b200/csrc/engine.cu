@@ -944,7 +944,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
         with_mode(mode, [&](auto M) {
           auto kfn = dense_cold_hash_kernel<decltype(M)::value>;
           D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
-          D3G_LAUNCH(X, kfn, (unsigned)X.sm_count * (D3G_CH_BITS <= 10 ? 4 : 3), kCHWarps * 32, hsm,
+          D3G_LAUNCH(X, kfn, (unsigned)X.sm_count * (D3G_CH_BITS <= 10 ? D3G_CH_CTAS : 3), kCHWarps * 32, hsm,
                      xorder, n_live,
                      in.r_ptr, in.r_col, cptr.p, ccol.p, ch.p, reinterpret_cast<const uint4*>(hx.p),
                      Y, var_bits, in.dl_z, dec, em, next.p, over_x.p, over_n.p, tc, in.row_sp,
