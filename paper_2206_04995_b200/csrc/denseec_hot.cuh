@@ -1818,14 +1818,22 @@ dense_cold_overflow_kernel(const uint32_t* __restrict__ over_x, const unsigned i
 // candidate stream as dense_cold_overflow_kernel (no global bitmap: those are
 // 1.25 MB per CTA on cfg5 and thrash L2, 130 GB of DRAM traffic). An x whose
 // survivors pass cc_max is abandoned exactly and queued for the bitmap kernel.
-constexpr int kCCThreads = 1024;
-constexpr uint32_t kCCSlots = 32768;  // 128 KB
-constexpr uint32_t kCCMax = 24576;    // load limit 0.75
+#ifndef D3G_CC_BITS
+#define D3G_CC_BITS 15
+#endif
+#ifndef D3G_CC_THREADS
+#define D3G_CC_THREADS 1024
+#endif
+constexpr int kCCThreads = D3G_CC_THREADS;
+constexpr uint32_t kCCSlots = 1u << D3G_CC_BITS;  // 128 KB at 15 bits
+constexpr uint32_t kCCMax = kCCSlots * 3 / 4;      // load limit 0.75
+constexpr int kCCPerSm = (1024 / D3G_CC_THREADS) * (D3G_CC_BITS >= 15 ? 1 : 2) > 2
+                             ? 2 : (1024 / D3G_CC_THREADS) * (D3G_CC_BITS >= 15 ? 1 : 2);
 
-__device__ __forceinline__ uint32_t cc_slot(uint32_t v) { return (v * 0x9E3779B1u) >> 17; }
+__device__ __forceinline__ uint32_t cc_slot(uint32_t v) { return (v * 0x9E3779B1u) >> (32 - D3G_CC_BITS); }
 
 template <int kMode>
-__global__ void __launch_bounds__(kCCThreads, 1)
+__global__ void __launch_bounds__(kCCThreads, kCCPerSm)
 dense_cold_cta_kernel(const uint32_t* __restrict__ over_x, const unsigned int* __restrict__ over_n,
                            const uint64_t* __restrict__ r_ptr, const uint32_t* __restrict__ r_col,
                            const uint64_t* __restrict__ cptr, const uint32_t* __restrict__ ccol,

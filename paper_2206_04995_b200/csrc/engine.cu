@@ -967,7 +967,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
           with_mode(mode, [&](auto M) {
             auto kfn = dense_cold_cta_kernel<decltype(M)::value>;
             D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm2));
-            D3G_LAUNCH(X, kfn, std::min<unsigned>(n_over, (unsigned)X.sm_count), kCCThreads, csm2,
+            D3G_LAUNCH(X, kfn, std::min<unsigned>(n_over, (unsigned)X.sm_count * kCCPerSm), kCCThreads, csm2,
                        over_x.p, over_n.p, in.r_ptr, in.r_col, cptr.p, ccol.p, ch.p,
                        reinterpret_cast<const uint4*>(hx.p), Y, var_bits, in.dl_z, dec, em,
                        over2_x.p, over2_n.p, env_u32("D3G_COLD_CTA_MAX", kCCMax, 1, kCCMax), tc,
