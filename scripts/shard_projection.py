@@ -29,6 +29,10 @@ def main():
     rl, rr = d3.generate(a.config, 0)
     sl, sr = d3.generate(a.config, 1)
     R, S = d3.RawTable(rl, rr), d3.RawTable(sl, sr)
+    # one untimed call first: the context's memory pool and module loads
+    warm = d3.EngineConfig(force=d3.Strategy.auto_select, count_only=True,
+                           memory_budget_bytes=150 << 30)
+    d3.join_project(R, S, warm, C)
     res = {"config": a.config, "shards": {}}
     base = None
     total = None
