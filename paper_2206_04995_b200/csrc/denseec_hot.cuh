@@ -1505,6 +1505,10 @@ constexpr int kCHWarps = 8;
 constexpr uint32_t kCHSlots = 1u << D3G_CH_BITS;  // per warp (8 KB at 11 bits)
 constexpr uint32_t kCHMax = kCHSlots * 3 / 4;    // load limit; < kCHSlots - 64 keeps probing finite
 constexpr uint32_t kCHEmpty = 0xffffffffu;
+#ifndef D3G_HASH_UNROLL
+#define D3G_HASH_UNROLL 2
+#endif
+constexpr int kHashUnroll = D3G_HASH_UNROLL;  // candidates in flight per lane
 
 __device__ __forceinline__ uint32_t ch_slot(uint32_t v) { return (v * 0x9E3779B1u) >> (32 - D3G_CH_BITS); }
 
@@ -1567,7 +1571,7 @@ dense_cold_hash_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
         seg1 = cp[y + 1];
       }
       // flattened (segment, entry) space, as in dense_cold_kernel: a warp scan
-      // of the segment lengths, then kColdUnroll candidates per lane per step
+      // of the segment lengths, then kHashUnroll candidates per lane per step
       // found by a 5-step binary search (short cold segments keep lanes busy)
       const uint32_t len = (uint32_t)(seg1 - seg0);
       uint32_t incl = len;
@@ -1578,11 +1582,11 @@ dense_cold_hash_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
       }
       const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
       ncand += lane == 0 ? total : 0u;
-      for (uint32_t tb = 0; tb < total && !over; tb += 32 * kColdUnroll) {
-        uint32_t tf[kColdUnroll], kx[kColdUnroll];
-        uint64_t t[kColdUnroll];
+      for (uint32_t tb = 0; tb < total && !over; tb += 32 * kHashUnroll) {
+        uint32_t tf[kHashUnroll], kx[kHashUnroll];
+        uint64_t t[kHashUnroll];
 #pragma unroll
-        for (int hh = 0; hh < kColdUnroll; ++hh) {
+        for (int hh = 0; hh < kHashUnroll; ++hh) {
           tf[hh] = tb + 32 * hh + lane;
           uint32_t k = 0;
 #pragma unroll
@@ -1593,15 +1597,15 @@ dense_cold_hash_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
           kx[hh] = k;
         }
 #pragma unroll
-        for (int hh = 0; hh < kColdUnroll; ++hh) {
+        for (int hh = 0; hh < kHashUnroll; ++hh) {
           const uint32_t before = __shfl_sync(0xffffffffu, incl - len, kx[hh]);
           const uint64_t base_k = __shfl_sync(0xffffffffu, seg0, kx[hh]);
           t[hh] = base_k + (tf[hh] - before);
         }
-        uint4 b0[kColdUnroll], b1[kColdUnroll];
-        uint32_t zc[kColdUnroll];
+        uint4 b0[kHashUnroll], b1[kHashUnroll];
+        uint32_t zc[kHashUnroll];
 #pragma unroll
-        for (int hh = 0; hh < kColdUnroll; ++hh) {
+        for (int hh = 0; hh < kHashUnroll; ++hh) {
           if (tf[hh] < total) {
             ld256(ch + 2 * t[hh], b0[hh], b1[hh]);
             zc[hh] = ccol[t[hh]];
@@ -1609,7 +1613,7 @@ dense_cold_hash_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
         }
         uint32_t nfresh = 0;
 #pragma unroll
-        for (int hh = 0; hh < kColdUnroll; ++hh) {
+        for (int hh = 0; hh < kHashUnroll; ++hh) {
           bool fresh = false;
           if (tf[hh] < total) {
             const bool hot = ((a0.x & b0[hh].x) | (a0.y & b0[hh].y) | (a0.z & b0[hh].z) |
