@@ -677,7 +677,14 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
       for (uint32_t q = 0; q < n_kinds; ++q) run_lo[q + 1] = run_lo[q] + nr[q];
       // units of about equal row counts (~8 per SM over the whole pass), so a
       // few all-row batches do not leave one CTA with millions of rows
-      const double per_unit = std::max(256.0, tested / ((double)X.sm_count * 8));
+      // units per SM grow with the batch count: a unit that switches batch
+      // reloads the batch's slice table (193 KB), so few batches want few,
+      // large units (cfg2, 49 batches: 3/SM, hot 0.33 -> 0.27 ms) and many
+      // batches want finer balance (cfg5, 2442 batches: 16/SM)
+      const uint32_t u_dflt = (uint32_t)std::min<double>(
+          16.0, std::max<double>(2.0, std::round(8.0 * n_batches / X.sm_count)));
+      const double per_unit = std::max(
+          256.0, tested / ((double)X.sm_count * env_u32("D3G_UNITS_PER_SM", u_dflt, 1, 64)));
       for (uint32_t q = 0; q < n_kinds; ++q) {
         const uint64_t rows = nr[q];
         run_zc[q] = rows ? std::max<uint32_t>(1, (uint32_t)std::min<double>(
