@@ -762,8 +762,11 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   hp.K = K;
   hp.kw = kw;
   hp.batch = 32;
+  // (batch, z range) units per SM without the pivot plan (cfg4: 8 -> 16,
+  // hot 17.6 -> 16.8 ms)
+  const uint64_t zc_per_sm = env_u32("D3G_ZCHUNKS_PER_SM", 16, 1, 64);
   hp.z_chunks = std::max<uint32_t>(1, (uint32_t)std::min<uint64_t>(
-      (D + 255) / 256, ((uint64_t)X.sm_count * 8 + n_batches - 1) / n_batches));
+      (D + 255) / 256, ((uint64_t)X.sm_count * zc_per_sm + n_batches - 1) / n_batches));
   const bool plan = !unit_off_h.empty();
   DBuf<uint32_t> unit_off_d;
   DBuf<uint8_t> batch_kind_d;
