@@ -4,7 +4,8 @@
 A step = one full join_project (count-only, force=auto, test_consts()) over
 one batch of convention-G synthetic input: map -> CSR -> degree stats -> f2
 partition -> SparseBMM + DenseEC -> count. Default workload: BASELINE
-configs[1] (cfg2, the self-join whose dense block exercises DenseEC).
+configs[4] (cfg5, 200M x 200M Zipf(1.2)), the config the metric's 1/2/4/8
+GPU figure is quoted on; it fits one B200 (peak working set ~7 GB).
 
   value  = input tuples/s with R, S resident in HBM (CUDA-event time of the
            pipeline on the library's stream, max over ranks)
@@ -14,10 +15,12 @@ configs[1] (cfg2, the self-join whose dense block exercises DenseEC).
            built from /root/reference) on the box's host cores, on a bounded
            x-slice sample extrapolated to the full job.
 
-Multi-GPU (torchrun): rank 0 generates the tables and broadcasts them over
-NVLink with NCCL; every rank builds the (replicated) mapping/CSR/partition
-and runs SparseBMM/DenseEC on its own x shard (intersection-free, no dedup
-across GPUs); counts are all-reduced.
+Multi-GPU: `--gpus N` without torchrun re-launches itself under
+torch.distributed.run with N ranks (127.0.0.1); under torchrun rank 0
+generates the tables and broadcasts them over NVLink with NCCL; every rank
+builds the (replicated) mapping/CSR/partition and runs SparseBMM/DenseEC on
+its own x shard (intersection-free, no dedup across GPUs); counts are
+all-reduced.
 """
 from __future__ import annotations
 
@@ -151,7 +154,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
@@ -165,6 +168,33 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def relaunch_under_torchrun(n: int) -> int:
+    """`bench.py --gpus N` run directly (no WORLD_SIZE): start N ranks, one per
+    GPU, through torch.distributed.run on 127.0.0.1, with the same arguments.
+    Returns the launcher's exit code."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # the communicator lines (NVLS/P2P) go to stderr
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
 
 # ---------------------------------------------------------------------------
@@ -252,16 +282,32 @@ def run_reference(args):
     n_tuples = 2 * O.cfg_rows(cfg)
     threads = os.cpu_count() or 1
     r, s = O.gen(cfg, 0), O.gen(cfg, 1)
-    for _ in range(args.warmup):
-        cpu_reference_sample(cfg, args.cpu_frac, threads, (r, s))
     if cfg == 5:  # each reference sample prepares the full 200M-row S (~20-40 s)
         args.warmup, args.steps = 0, min(args.steps, 2)
+    elif cfg in (2, 4):  # each sample is the full prep + a 2% x-slice (10-40 s)
+        args.warmup, args.steps = min(args.warmup, 1), min(args.steps, 3)
+    for _ in range(args.warmup):
+        cpu_reference_sample(cfg, args.cpu_frac, threads, (r, s))
     ests = []
     for _ in range(args.steps):
         est, detail = cpu_reference_sample(cfg, args.cpu_frac, threads, (r, s))
         ests.append(est)
     sec = sum(ests) / len(ests)
     value = n_tuples / sec
+    # the same reference at threads=1 (one bounded sample)
+    t1_frac = args.cpu_frac / 4
+    est1, det1 = cpu_reference_sample(cfg, t1_frac, 1, (r, s))
+    detail["threads_1"] = {"est_full_job_s": est1, "tuples_per_s": n_tuples / est1,
+                           "sample": _sample_text(det1), "speedup_all_threads": est1 / sec}
+    if cfg in CLASSICAL_CFGS:  # also the forced-hybrid reference time
+        t0 = time.perf_counter()
+        d = O.ref_join_project(r, s, force="hybrid", threads=threads, count_only=True,
+                               budget_bytes=1 << 40)
+        hy = time.perf_counter() - t0
+        detail["force_hybrid"] = {"s": hy, "tuples_per_s": n_tuples / hy, "out_p": d["out_p"],
+                                  "ms_phases": {k: d[k] for k in ("ms_map", "ms_csr",
+                                                                  "ms_partition", "ms_sparse",
+                                                                  "ms_dense")}}
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tuples/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -270,6 +316,8 @@ def run_reference(args):
         "config": {"workload": WORKLOADS[cfg], "count_only": True, "force": "auto",
                    "consts": "test_consts()"},
         "cpu_baseline": {"value": value, "unit": "tuples/s", "cores": threads, "kind": "reference",
+                         "cpu_model": cpu_model(),
+                         "extrapolated": detail.get("strategy") != "classical",
                          "sample": _sample_text(detail)},
         "e2e": {"value": value, "unit": "tuples/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -281,10 +329,14 @@ def run_reference(args):
 # ---------------------------------------------------------------------------
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args.gpus))
     if args.impl == "reference":
         run_reference(args)
         return
     rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -527,7 +579,8 @@ def main():
                 threads = os.cpu_count() or 1
                 est, detail = cpu_reference_sample(cfg_id, args.cpu_frac, threads)
                 cpu = {"value": n_tuples / est, "unit": "tuples/s", "cores": threads,
-                       "kind": "reference",
+                       "kind": "reference", "cpu_model": cpu_model(),
+                       "extrapolated": detail.get("strategy") != "classical",
                        "sample": _sample_text(detail),
                        "est_full_job_s": est}
             else:

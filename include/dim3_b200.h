@@ -47,9 +47,11 @@ extern "C" {
 #define D3G_SPARSE_ONLY 3
 #define D3G_DENSE_ONLY 4
 
-/* dim3::DensePathMode (P/include/dim3/denseec.hpp:56). The GPU kernel
- * answers every (x, dense z) encounter with one bit-sliced OR sweep; the mode
- * only selects how the reference-equivalent work counters are attributed. */
+/* dim3::DensePathMode (P/include/dim3/denseec.hpp:18). The GPU answers every
+ * (x, dense z) encounter with its own kernels whatever the mode (the output
+ * set is the same); the mode decides which reference sweep the
+ * reference-equivalent counters describe: the wide (block_and_any) or probe
+ * (probe_any) path per encounter, exactly as P/src/denseec.cpp:26-43 picks. */
 #define D3G_DENSE_COST_BASED 0
 #define D3G_DENSE_FORCE_WIDE 1
 #define D3G_DENSE_FORCE_PROBE 2
@@ -85,7 +87,9 @@ typedef struct {
   int32_t natural_keys_auto;
   int32_t declared_x, declared_y, declared_z;  /* natural_keys_declared */
   int32_t checksum;           /* also compute (sum, xor) of mix64(mix64(x)^z) */
-  int32_t collect_counters;   /* reference-equivalent DenseEC/SpA counters */
+  int32_t collect_counters;   /* also compute dense_blocks_checked and
+                                 dense_probes_done (a per-pair pass: for tests
+                                 and W_D; |Y| must fit one smem bitmap) */
   int32_t shard_index;        /* x-range shard of R handled by this call */
   int32_t shard_count;        /* 1 = whole table */
   uint32_t x_code_lo;         /* restrict the kernels to engine x codes in */
@@ -110,6 +114,11 @@ typedef struct {
   uint64_t panel_bytes;       /* reference panel size (dense_z * padded(|Y|)/8) */
   uint64_t peak_bytes;        /* device working set high-water mark */
   uint64_t spa_inner_count;   /* OUT_J over sparse z (SpaStats::inner_count) */
+  /* DenseEcStats (P/include/dim3/denseec.hpp:20-29): what the reference's
+   * dense_ec counts on this input under opts.dense_mode. Encounters and row
+   * bitmaps are always filled (exact, from the degree histograms and the
+   * f3 thresholds); blocks_checked / probes_done only with collect_counters
+   * (0 otherwise). Over the x codes this call processed. */
   uint64_t dense_wide_encounters, dense_probe_encounters;
   uint64_t dense_blocks_checked, dense_probes_done, dense_row_bitmaps_built;
   uint64_t checksum_sum, checksum_xor;
@@ -132,9 +141,14 @@ typedef struct {
    * split (x and z both hold the top-ranked y) */
   uint64_t hot_direct_pairs;
   /* DenseEC P2 (cold residual) kernels: CUDA-event time and candidate bytes
-   * streamed (36 B per candidate: 32-byte hot signature + 4-byte row id) */
+   * (36 B per candidate: 32-byte hot signature + 4-byte row id), each x's
+   * candidate stream counted once, in the tier that completes it */
   double ms_dense_cold;
   uint64_t cold_bytes;
+  /* SpaStats::spa_allocations / spa_entries (P/include/dim3/sparsebmm.hpp:15-19):
+   * the stamp arrays the reference's run_chunked would allocate for
+   * opts.threads over the engine's x rows, and |Z| per array. */
+  uint64_t spa_allocations, spa_entries;
 } d3g_report;
 
 /* Materialized output: caller-owned host (or device, on_device != 0)

@@ -76,7 +76,8 @@ class RefReport(C.Structure):
                 ("r_rows", C.c_uint64), ("s_rows", C.c_uint64), ("out_j_estimate", C.c_uint64),
                 ("f1", C.c_double)] + [(k, C.c_uint64) for k in _REF_U64] + \
                [(k, C.c_double) for k in _REF_MS] + \
-               [("checksum_sum", C.c_uint64), ("checksum_xor", C.c_uint64)]
+               [("checksum_sum", C.c_uint64), ("checksum_xor", C.c_uint64),
+                ("spa_allocations", C.c_uint64), ("spa_entries", C.c_uint64)]
 
 
 class RefPipeline(C.Structure):

@@ -61,6 +61,7 @@ struct RefReport {
   double ms_total, ms_estimate, ms_map, ms_csr, ms_partition, ms_sparse,
       ms_dense, ms_classical;
   std::uint64_t checksum_sum, checksum_xor;  // over decoded pairs, if materialized
+  std::uint64_t spa_allocations, spa_entries;
 };
 
 dim3::CostConstants to_consts(const RefConsts* c) {
@@ -173,6 +174,8 @@ int ref_join_project(const std::uint64_t* rl, const std::uint64_t* rr,
     rep->dense_blocks_checked = e.dense.blocks_checked;
     rep->dense_probes_done = e.dense.probes_done;
     rep->dense_row_bitmaps_built = e.dense.row_bitmaps_built;
+    rep->spa_allocations = e.spa.spa_allocations;
+    rep->spa_entries = e.spa.spa_entries;
     rep->ms_total = e.ms_total;
     rep->ms_estimate = e.ms_estimate;
     rep->ms_map = e.ms_map;
@@ -428,8 +431,10 @@ int ref_set_checksum(const std::uint64_t* rl, const std::uint64_t* rr,
     dim3::CostConstants c;  // unused by all_sparse
     dim3::PartitionResult part = dim3::partition_s_csr(
         s_by_z, st, c, dim3::PartitionForce::all_sparse);
-    const dim3::Dictionary& dx = swapped ? m.dict_z : m.dict_x;
-    const dim3::Dictionary& dz = swapped ? m.dict_x : m.dict_z;
+    // decode ENGINE codes with the engine's dictionaries (row = engine x,
+    // pair z = engine z), then swap back to the caller's orientation
+    const dim3::Dictionary& dx = m.dict_x;
+    const dim3::Dictionary& dz = m.dict_z;
     std::uint64_t n_rows = r_by_x.n_rows;
     if (rows_per_slice == 0) rows_per_slice = 256;
     std::uint64_t n_slices = (n_rows + rows_per_slice - 1) / rows_per_slice;

@@ -10,11 +10,13 @@
 //      acc = OR_{r in hz[z]} T[g][r]   (early exit once acc == all-live)
 // and popc(acc) pairs are hit. T for a batch of groups is staged into shared
 // memory with one TMA bulk copy (cp.async.bulk + mbarrier transaction count).
-// P2 (engine.cu, through the SparseBMM tiers with a filter) counts pairs that
-// share only COLD y: the cold join R_cold x S_cold restricted to dense z,
-// dedup'd per x, skipping candidates whose hot masks already intersect. The
-// two parts are disjoint and together equal the reference's dense_ec output
-// (P/src/denseec.cpp:8-86): {(x, z) : R[x] and S[z] share a y}, z dense.
+// P2 (the cold kernels at the end of this file: dense_cold_kernel, or
+// dense_cold_hash_kernel with its CTA-hash and global-bitmap overflow tiers)
+// counts pairs that share only COLD y: the cold join R_cold x S_cold
+// restricted to dense z, dedup'd per x, skipping candidates whose hot masks
+// already intersect. The two parts are disjoint and together equal the
+// reference's dense_ec output (P/src/denseec.cpp:8-86): {(x, z) : R[x] and
+// S[z] share a y}, z dense.
 #pragma once
 
 #include "sparsebmm.cuh"
@@ -276,17 +278,26 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_
       "l"(src), "r"(bytes), "r"(b)
       : "memory");
 }
+// Bounded wait on the TMA transaction barrier: a byte-count or phase mismatch
+// traps (the launch fails with an error the host reports) instead of hanging
+// the device. try_wait suspends for a bounded time per call, so 2^24 polls
+// are seconds, far beyond any real copy.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(a),
-      "r"(phase)
-      : "memory");
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  for (uint32_t it = 0;; ++it) {
+    uint32_t ok;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(phase)
+        : "memory");
+    if (ok) return;
+    if (it > (1u << 24)) asm volatile("trap;");
+  }
 }
 
 __device__ __forceinline__ uint4 full_mask(uint32_t members) {
@@ -1561,6 +1572,7 @@ dense_cold_hash_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
     const uint64_t* cp = cptr + (uint64_t)v * y_card;
     uint32_t inserted = 0;  // warp-uniform
     bool over = false;
+    uint64_t xcand = 0;  // x's candidates, credited only if x completes in this tier
     const uint64_t r0 = r_ptr[x], r1 = r_ptr[x + 1];
     for (uint64_t kb = r0; kb < r1 && !over; kb += 32) {
       const uint64_t kk = kb + lane;
@@ -1581,7 +1593,7 @@ dense_cold_hash_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
         if (lane >= (uint32_t)o) incl += u;
       }
       const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-      ncand += lane == 0 ? total : 0u;
+      xcand += lane == 0 ? total : 0u;
       for (uint32_t tb = 0; tb < total && !over; tb += 32 * kHashUnroll) {
         uint32_t tf[kHashUnroll], kx[kHashUnroll];
         uint64_t t[kHashUnroll];
@@ -1644,6 +1656,7 @@ dense_cold_hash_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
       if (lane == 0) over_x[atomicAdd(over_n, 1u)] = x;
     } else {
       cnt += lane == 0 ? inserted : 0;
+      ncand += xcand;  // each x's stream counted once, in the tier that finishes it
     }
     if (inserted && (kMode != kModeCount || row_sp)) {
       for (uint32_t i = lane; i < kCHSlots; i += 32) {
@@ -1779,7 +1792,7 @@ dense_cold_overflow_kernel(const uint32_t* __restrict__ over_x, const unsigned i
 #pragma unroll
           for (int u = 0; u < kOvUnroll; ++u)
             if (ok[u]) {
-              ++ncand;
+              ncand += pass == 0 ? 1u : 0u;  // the clearing replay is not new work
               ld256(ch + 2 * t[u], b0[u], b1[u]);
               zc[u] = ccol[t[u]];
             }
@@ -1871,6 +1884,7 @@ dense_cold_cta_kernel(const uint32_t* __restrict__ over_x, const unsigned int* _
       s_over = 0;
     }
     __syncthreads();
+    uint64_t xcand = 0;  // credited only if x completes in this tier
     {
       for (uint64_t yb = r0; yb < r1 && !s_over; yb += kCCThreads) {
         const uint64_t k = yb + threadIdx.x;
@@ -1931,7 +1945,7 @@ dense_cold_cta_kernel(const uint32_t* __restrict__ over_x, const unsigned int* _
 #pragma unroll
           for (int u = 0; u < kOvUnroll; ++u)
             if (ok[u]) {
-              ++ncand;
+              ++xcand;
               ld256(ch + 2 * t[u], b0[u], b1[u]);
               zc[u] = ccol[t[u]];
             }
@@ -1964,8 +1978,9 @@ dense_cold_cta_kernel(const uint32_t* __restrict__ over_x, const unsigned int* _
     const bool over = s_over != 0;
     if (over) {
       if (threadIdx.x == 0) over2_x[atomicAdd(over2_n, 1u)] = x;
-    } else if (threadIdx.x == 0) {
-      cnt += s_ins;
+    } else {
+      ncand += xcand;
+      if (threadIdx.x == 0) cnt += s_ins;
     }
     for (uint32_t i = threadIdx.x; i < kCCSlots; i += kCCThreads) {
       const uint32_t zl = cctab[i];

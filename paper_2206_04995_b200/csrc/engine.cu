@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "classical.cuh"
+#include "counters.cuh"
 #include "datagen.cuh"
 #include "denseec.cuh"
 #include "denseec_hot.cuh"
@@ -1340,6 +1341,14 @@ void materialize_pairs(Ctx& X, uint64_t total, const std::function<void(d3g::Emi
   DBuf<uint32_t> ex = X.alloc<uint32_t>(total), ez = X.alloc<uint32_t>(total);
   DBuf<unsigned long long> cur = X.zeros<unsigned long long>(1);
   emit(Emit{ex.p, ez.p, cur.p, total});
+  {
+    // the buffer was sized by the counting pass; the emitting kernels must
+    // have produced exactly that many pairs (no truncation, no unwritten slots)
+    const uint64_t emitted = X.scalar(cur.p);
+    if (emitted != total)
+      throw CudaError("materialize: emitted " + std::to_string(emitted) + " pairs, counted " +
+                      std::to_string(total));
+  }
   tr("emit");
   DBuf<uint64_t> keys = X.alloc<uint64_t>(total);
   DBuf<uint32_t> idx = X.alloc<uint32_t>(total);
@@ -1869,6 +1878,86 @@ void f2_split(Ctx& X, const d3g::DeviceCsr& sz_csr, const DegreeStats& G, uint64
 }
 
 // ---------------------------------------------------------------------------
+// Reference-equivalent work counters (SpaStats, DenseEcStats): what the
+// reference's sparse_bmm / dense_ec would count on this input (the GPU
+// kernels do different work; see counters.cuh).
+
+// wide/probe threshold per x degree under a DensePathMode
+// (P/src/denseec.cpp:26-43): cost_based = f3_threshold(m_x), force_wide = 0
+// (every dense z has m_z >= 1 > 0), force_probe = never wide.
+std::vector<uint32_t> mode_thresholds(uint64_t max_mx, uint64_t y_card, const d3g_consts* c,
+                                      int dense_mode) {
+  std::vector<uint32_t> thr(max_mx + 1, 0);
+  for (uint64_t m = 1; m <= max_mx; ++m)
+    thr[m] = dense_mode == D3G_DENSE_FORCE_WIDE    ? 0u
+             : dense_mode == D3G_DENSE_FORCE_PROBE ? 0xffffffffu
+                                                   : d3g_f3_threshold((uint32_t)m, (uint32_t)y_card, c);
+  return thr;
+}
+
+// Encounter counts and row bitmaps from the degree histograms alone:
+// hx[m] live x of degree m, hd[m] dense rows of degree m.
+void encounter_counts(const std::vector<uint64_t>& hx, const std::vector<uint64_t>& hd,
+                      const std::vector<uint32_t>& thr, d3g::DenseCounters& out) {
+  // gt[t] = dense rows with m_z > t
+  std::vector<uint64_t> gt(hd.size() + 1, 0);
+  for (uint64_t t = hd.size(); t-- > 0;) gt[t] = gt[t + 1] + (t + 1 < hd.size() ? hd[t + 1] : 0);
+  const uint64_t n_dense = gt[0];
+  if (n_dense == 0) return;
+  for (uint64_t m = 1; m < hx.size(); ++m) {
+    if (!hx[m]) continue;
+    const uint64_t t = m < thr.size() ? thr[m] : 0;
+    const uint64_t w = t < gt.size() ? gt[t] : 0;
+    out.wide += hx[m] * w;
+    out.probe += hx[m] * (n_dense - w);
+    if (w) out.bitmaps += hx[m];
+  }
+}
+
+// Per-pair counters (blocks_checked, probes_done) on the device, plus the
+// encounter counts, for x codes [x_lo, x_hi) of r against the dense rows.
+void dense_counters_device(Ctx& X, const d3g::DeviceCsr& r, uint64_t x_lo, uint64_t x_hi,
+                           const uint64_t* zptr, const uint32_t* zcol, uint64_t z_rows,
+                           const uint8_t* dsel, uint64_t dsel_n, const std::vector<uint32_t>& thr,
+                           uint32_t w, uint64_t y_card, d3g::DenseCounters& out) {
+  using namespace d3g;
+  if (x_hi <= x_lo || z_rows == 0) return;
+  const uint64_t words = (std::max<uint64_t>(y_card, 1) + 31) / 32;
+  const uint64_t smem = words * 4;
+  if (smem > 220 * 1024)
+    throw ConfigError("collect_counters: |Y| = " + std::to_string(y_card) +
+                      " does not fit one shared-memory row bitmap");
+  DBuf<uint32_t> dthr = X.alloc<uint32_t>(thr.size());
+  X.to_device(dthr.p, thr.data(), thr.size());
+  DBuf<DenseCounters> dc = X.zeros<DenseCounters>(1);
+  DBuf<unsigned int> next = X.zeros<unsigned int>(1);
+  D3G_CUDA(cudaFuncSetAttribute(dense_counters_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+  const uint64_t n_blocks = (y_card + w - 1) / w;
+  const int per_sm = smem <= 48 * 1024 ? 4 : smem <= 100 * 1024 ? 2 : 1;
+  const unsigned grid = (unsigned)std::min<uint64_t>(x_hi - x_lo, (uint64_t)X.sm_count * per_sm);
+  D3G_LAUNCH(X, dense_counters_kernel, grid, kCntThreads, smem, r.row_ptr.p, r.col.p, x_lo, x_hi,
+             zptr, zcol, z_rows, dsel, dsel_n, dthr.p, (uint64_t)thr.size(), w, n_blocks,
+             (uint32_t)words, next.p, dc.p);
+  DenseCounters h{};
+  X.to_host(&h, dc.p, 1);
+  out.wide += h.wide;
+  out.probe += h.probe;
+  out.blocks += h.blocks;
+  out.probes += h.probes;
+  out.bitmaps += h.bitmaps;
+}
+
+// SpaStats::spa_allocations / spa_entries (P/src/sparsebmm.cpp:17-21,
+// :79-104): one stamp array of |Z| entries per chunk run_chunked executes.
+void spa_counters(uint64_t x_rows, uint64_t z_card, int threads, d3g_report* rep) {
+  uint64_t chunks = 0;
+  if (x_rows > 0) chunks = (threads <= 1 || x_rows <= 1) ? 1 : std::min<uint64_t>(threads, x_rows);
+  rep->spa_allocations = chunks;
+  rep->spa_entries = chunks ? z_card : 0;
+}
+
+// ---------------------------------------------------------------------------
 // The pipeline.
 void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g_consts* c,
                        const d3g_opts* o, d3g_report* rep, d3g_pairs* pairs) {
@@ -2098,6 +2187,36 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
            x_hi = xa + (xb - xa) * (shard_index + 1) / shard_count;
   SparseInputs si{rx.row_ptr.p, rx.col.p, x_card, sp_ptr.p, sp_col.p, sparse_ids.p, n_sparse,
                   y_card, x_lo, x_hi};
+  // reference-equivalent work counters over this call's x codes (SpaStats,
+  // DenseEcStats; counters.cuh)
+  if (!classical) {
+    spa_counters(x_card, z_card, o->threads, rep);
+    DenseCounters dc{};
+    const std::vector<uint32_t> thr = mode_thresholds(max_mx, y_card, c, o->dense_mode);
+    if (o->collect_counters) {
+      dense_counters_device(X, rx, x_lo, x_hi, sz_csr.row_ptr.p, sz_csr.col.p, z_card,
+                            P.dtable.p, max_mz + 1, thr, c->w, y_card, dc);
+    } else if (n_dense > 0 && x_hi > x_lo) {
+      std::vector<uint64_t> hd(max_mz + 1, 0);
+      for (uint64_t m = 1; m <= max_mz; ++m) hd[m] = P.table[m] ? G.hmz[m] : 0;
+      std::vector<uint64_t> hx_range;
+      const std::vector<uint64_t>* hx = &hmx;
+      if (x_lo != 0 || x_hi != x_card) {  // the m_x histogram of this call's x range
+        DBuf<unsigned long long> h = X.zeros<unsigned long long>(max_mx + 1);
+        D3G_LAUNCH(X, degree_hist_kernel, grid_for(x_hi - x_lo, 256), 256, 0,
+                   rx.row_ptr.p + x_lo, x_hi - x_lo, max_mx + 1, h.p);
+        hx_range.resize(max_mx + 1);
+        X.to_host(reinterpret_cast<unsigned long long*>(hx_range.data()), h.p, max_mx + 1);
+        hx = &hx_range;
+      }
+      encounter_counts(*hx, hd, thr, dc);
+    }
+    rep->dense_wide_encounters = dc.wide;
+    rep->dense_probe_encounters = dc.probe;
+    rep->dense_blocks_checked = dc.blocks;
+    rep->dense_probes_done = dc.probes;
+    rep->dense_row_bitmaps_built = dc.bitmaps;
+  }
   KernelOut ks, kd;
   const uint64_t s_lo = Ls.n_live * shard_index / shard_count,
                  s_hi = Ls.n_live * (shard_index + 1) / shard_count;
@@ -2617,6 +2736,7 @@ int d3g_sparse_bmm_csr(d3g_ctx* ctx, const d3g_csr* r_by_x, const d3g_csr* s_spa
       Emit em{ex.p, ez.p, cur.p, ko.count};
       KernelOut t;
       run_sparse(X, si, dec, kModeEmit, em, t);
+      if (X.scalar(cur.p) != ko.count) throw CudaError("sparse_bmm: emitted != counted");
       sort_and_copy_pairs(X, ex.p, ez.p, ko.count, pairs_x, pairs_z);
     }
   });
@@ -2625,8 +2745,6 @@ int d3g_sparse_bmm_csr(d3g_ctx* ctx, const d3g_csr* r_by_x, const d3g_csr* s_spa
 int d3g_dense_ec_rows(d3g_ctx* ctx, const d3g_csr* r_by_x, const d3g_panel* panel,
                       const d3g_consts* c, int dense_mode, uint32_t* pairs_x, uint32_t* pairs_z,
                       uint64_t pairs_cap, uint64_t* count, d3g_kernel_stats* st) {
-  (void)c;
-  (void)dense_mode;
   return guarded([&] {
     using namespace d3g;
     Ctx& X = ctx->c;
@@ -2688,7 +2806,26 @@ int d3g_dense_ec_rows(d3g_ctx* ctx, const d3g_csr* r_by_x, const d3g_panel* pane
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     *count = ko.count;
-    if (st) st->ms_kernel = ms;
+    if (st) {
+      st->ms_kernel = ms;
+      // DenseEcStats of the reference's dense_ec on this panel under
+      // dense_mode (counters.cuh): every panel row is dense
+      const std::vector<uint32_t> thr = mode_thresholds(max_mx, y_card, c, dense_mode);
+      DenseCounters dc{};
+      if ((std::max<uint64_t>(y_card, 1) + 31) / 32 * 4 <= 220 * 1024) {
+        dense_counters_device(X, r, 0, r.n_rows, zptr.p, zcol.p, rows, nullptr, 0, thr, panel->w,
+                              y_card, dc);
+      } else {  // |Y| too large for one smem row bitmap: encounters only
+        std::vector<uint64_t> hd(max_mz + 1, 0);
+        for (uint64_t j = 0; j < rows; ++j) hd[panel->m_z[j]]++;
+        encounter_counts(hmx, hd, thr, dc);
+      }
+      st->wide_encounters = dc.wide;
+      st->probe_encounters = dc.probe;
+      st->blocks_checked = dc.blocks;
+      st->probes_done = dc.probes;
+      st->row_bitmaps_built = dc.bitmaps;
+    }
     if (pairs_x && pairs_z) {
       if (pairs_cap < ko.count) throw ResourceError("pair buffer too small");
       DBuf<uint32_t> ex = X.alloc<uint32_t>(ko.count), ez = X.alloc<uint32_t>(ko.count);
@@ -2696,6 +2833,7 @@ int d3g_dense_ec_rows(d3g_ctx* ctx, const d3g_csr* r_by_x, const d3g_panel* pane
       Emit em{ex.p, ez.p, cur.p, ko.count};
       KernelOut t;
       run_dense(X, di, dec, kModeEmit, em, t);
+      if (X.scalar(cur.p) != ko.count) throw CudaError("dense_ec: emitted != counted");
       sort_and_copy_pairs(X, ex.p, ez.p, ko.count, pairs_x, pairs_z);
     }
   });

@@ -131,6 +131,9 @@ class EngineConfig:
     natural_keys_declared: SkipFlags = field(default_factory=SkipFlags)
     # GPU extensions
     checksum: bool = False        # also compute the (sum, xor) set fingerprint
+    # also compute the reference's per-pair DenseEC counters (dense_blocks_checked,
+    # dense_probes_done): a separate per-pair pass, for tests and W_D
+    collect_counters: bool = False
     shard_index: int = 0          # x-range shard handled by this call
     shard_count: int = 1
     # restrict the SparseBMM/DenseEC kernels to engine x codes in [lo, hi)
@@ -225,7 +228,8 @@ class _Report(C.Structure):
                 ("ms_classical", C.c_double), ("ms_dense_hot", C.c_double),
                 ("hot_lds_bytes", C.c_uint64), ("hot_lds_bytes_unshared", C.c_uint64),
                 ("hot_direct_pairs", C.c_uint64), ("ms_dense_cold", C.c_double),
-                ("cold_bytes", C.c_uint64)]
+                ("cold_bytes", C.c_uint64), ("spa_allocations", C.c_uint64),
+                ("spa_entries", C.c_uint64)]
 
 
 class _Pairs(C.Structure):
@@ -424,6 +428,8 @@ class ExecutionReport:
     hot_direct_pairs: int = 0
     ms_dense_cold: float = 0.0
     cold_bytes: int = 0
+    spa_allocations: int = 0
+    spa_entries: int = 0
 
     def to_kv(self):
         """Insertion-ordered key/value view with the reference's key names
@@ -439,7 +445,14 @@ class ExecutionReport:
               ("intermediate_pairs", str(self.intermediate_pairs)), ("x_card", str(self.x_card)),
               ("y_card", str(self.y_card)), ("z_card", str(self.z_card)),
               ("panel_bytes", str(self.panel_bytes)), ("peak_bytes", str(self.peak_bytes)),
-              ("spa_inner_count", str(self.spa_inner_count))]
+              ("spa_inner_count", str(self.spa_inner_count)),
+              ("spa_allocations", str(self.spa_allocations)),
+              ("spa_entries", str(self.spa_entries)),
+              ("dense_wide_encounters", str(self.dense_wide_encounters)),
+              ("dense_probe_encounters", str(self.dense_probe_encounters)),
+              ("dense_blocks_checked", str(self.dense_blocks_checked)),
+              ("dense_probes_done", str(self.dense_probes_done)),
+              ("dense_row_bitmaps_built", str(self.dense_row_bitmaps_built))]
         for k in ("ms_total", "ms_estimate", "ms_map", "ms_csr", "ms_partition", "ms_sparse",
                   "ms_dense", "ms_classical", "ms_decode"):
             kv.append((k, f"{getattr(self, k):.3f}"))
@@ -482,7 +495,8 @@ def _opts(cfg: EngineConfig) -> _Opts:
         raise ConfigError("x_code_range must be (lo, hi) with 0 <= lo <= hi < 2^32")
     return _Opts(int(cfg.force), int(cfg.threads), int(cfg.memory_budget_bytes),
                  int(cfg.count_only), int(cfg.dense_mode), int(cfg.natural_keys_auto),
-                 int(d.x), int(d.y), int(d.z), int(cfg.checksum), 0, int(cfg.shard_index),
+                 int(d.x), int(d.y), int(d.z), int(cfg.checksum), int(cfg.collect_counters),
+                 int(cfg.shard_index),
                  int(cfg.shard_count), int(xr[0]), int(xr[1]))
 
 
@@ -615,7 +629,12 @@ def dense_ec(r_by_x: CsrMatrix, z_ids: np.ndarray, panel_blocks: np.ndarray, y_c
     r = r_by_x._struct()
     z_ids = np.ascontiguousarray(z_ids, dtype=np.uint32)
     blocks = np.ascontiguousarray(panel_blocks, dtype=np.uint64)
+    # BitmapPanel::m_z: the degree of each row (its popcount)
+    row_words = blocks.size // max(z_ids.size, 1)
     mz = np.zeros(max(z_ids.size, 1), np.uint32)
+    if z_ids.size:
+        bits = np.unpackbits(blocks.view(np.uint8).reshape(z_ids.size, row_words * 8), axis=1)
+        mz[:z_ids.size] = bits.sum(axis=1, dtype=np.uint64).astype(np.uint32)
     panel = _Panel(z_ids.ctypes.data_as(U32P), mz.ctypes.data_as(U32P),
                    blocks.ctypes.data_as(U64P), z_ids.size, y_card, c.w)
     cs = _consts(c)
