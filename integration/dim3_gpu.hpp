@@ -27,8 +27,17 @@ inline d3g_ctx* context(int device = 0) {
   return ctx;
 }
 
+// GPU-side knobs outside EngineConfig. exact_counters: also run the per-pair
+// pass that reproduces DenseEcStats::blocks_checked / probes_done (cost grows
+// with the pair tests; the encounter counts, row bitmaps and SpaStats are
+// always filled exactly).
+struct GpuOptions {
+  bool exact_counters = false;
+};
+
 inline JoinProjectOutput join_project(const RawTable& r, const RawTable& s,
-                                      const EngineConfig& cfg, const CostConstants& c) {
+                                      const EngineConfig& cfg, const CostConstants& c,
+                                      const GpuOptions& g = {}) {
   if (r.left.type != ColumnType::u64 || r.right.type != ColumnType::u64 ||
       s.left.type != ColumnType::u64 || s.right.type != ColumnType::u64)
     throw ConfigError("the GPU path takes integer (u64) columns");
@@ -46,6 +55,7 @@ inline JoinProjectOutput join_project(const RawTable& r, const RawTable& s,
   o.declared_x = cfg.natural_keys_declared.x;
   o.declared_y = cfg.natural_keys_declared.y;
   o.declared_z = cfg.natural_keys_declared.z;
+  o.collect_counters = g.exact_counters ? 1 : 0;
   d3g_report rep{};
   JoinProjectOutput out;
   out.result.provenance = ResultSet::Provenance::raw;   // decoded on the device
@@ -85,7 +95,14 @@ inline JoinProjectOutput join_project(const RawTable& r, const RawTable& s,
   e.pairs_classical = rep.pairs_classical;
   e.intermediate_pairs = rep.intermediate_pairs;
   e.ms_classical = rep.ms_classical;
-  e.spa.inner_count = rep.spa_inner_count;
+  e.spa.inner_count = rep.spa_inner_count;           // sparsebmm.hpp:15-19
+  e.spa.spa_allocations = rep.spa_allocations;
+  e.spa.spa_entries = rep.spa_entries;
+  e.dense.wide_encounters = rep.dense_wide_encounters;  // denseec.hpp:20-29
+  e.dense.probe_encounters = rep.dense_probe_encounters;
+  e.dense.blocks_checked = rep.dense_blocks_checked;
+  e.dense.probes_done = rep.dense_probes_done;
+  e.dense.row_bitmaps_built = rep.dense_row_bitmaps_built;
   e.ms_total = rep.ms_total;
   e.ms_estimate = rep.ms_estimate;
   e.ms_map = rep.ms_map;

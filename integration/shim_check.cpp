@@ -3,7 +3,8 @@
 // dim3::join_project (the unmodified CPU reference) and dim3::gpu::join_project
 // (integration/dim3_gpu.hpp over libdim3_b200.so). For every strategy, both
 // equal the brute-force oracle, and the reports agree on the decisions
-// (strategy, swap, split, OUT_J estimate, dropped rows, intermediate size).
+// (strategy, swap, split, OUT_J estimate, dropped rows, intermediate size)
+// and on every work counter of the report (SpaStats, DenseEcStats).
 // Mirrors P/tests/test_engine.cpp:89-113 and acceptance criterion 1.
 // Build: make -C oracle shim (needs /root/reference); run on a B200.
 #include <cstdio>
@@ -45,7 +46,9 @@ int main() {
       const auto want = testsup::oracle_pairs(inst.r, inst.s);
       for (dim3::Strategy f : forces) {
         auto cpu = dim3::join_project(inst.r, inst.s, forced(f, false), c);
-        auto gpu = dim3::gpu::join_project(inst.r, inst.s, forced(f, false), c);
+        dim3::gpu::GpuOptions exact;
+        exact.exact_counters = true;
+        auto gpu = dim3::gpu::join_project(inst.r, inst.s, forced(f, false), c, exact);
         CHECK_EQ(testsup::result_set(dim3::result_to_raw(cpu)), want, "cpu set");
         CHECK_EQ(testsup::result_set(dim3::result_to_raw(gpu)), want, "gpu set");
         CHECK_EQ(gpu.result.count, (std::uint64_t)want.size(), "gpu count");
@@ -64,6 +67,18 @@ int main() {
           CHECK_EQ(a.x_card, b.x_card, "x_card");
           CHECK_EQ(a.y_card, b.y_card, "y_card");
           CHECK_EQ(a.z_card, b.z_card, "z_card");
+          CHECK_EQ(a.f2_evaluations, b.f2_evaluations, "f2_evaluations");
+          CHECK_EQ(a.panel_bytes, b.panel_bytes, "panel_bytes");
+          // the to_kv work counters (engine.cpp:303-309)
+          CHECK_EQ(a.spa.inner_count, b.spa.inner_count, "spa_inner_count");
+          CHECK_EQ(a.spa.spa_allocations, b.spa.spa_allocations, "spa_allocations");
+          CHECK_EQ(a.spa.spa_entries, b.spa.spa_entries, "spa_entries");
+          CHECK_EQ(a.dense.wide_encounters, b.dense.wide_encounters, "dense_wide_encounters");
+          CHECK_EQ(a.dense.probe_encounters, b.dense.probe_encounters, "dense_probe_encounters");
+          CHECK_EQ(a.dense.blocks_checked, b.dense.blocks_checked, "dense_blocks_checked");
+          CHECK_EQ(a.dense.probes_done, b.dense.probes_done, "dense_probes_done");
+          CHECK_EQ(a.dense.row_bitmaps_built, b.dense.row_bitmaps_built,
+                   "dense_row_bitmaps_built");
         } else {
           CHECK_EQ(a.pairs_classical, b.pairs_classical, "pairs_classical");
           CHECK_EQ(b.intermediate_pairs, testsup::oracle_out_j_bag(

@@ -80,9 +80,22 @@ __global__ void row_bounds_kernel(const uint32_t* __restrict__ row_of, uint64_t 
   }
 }
 
-// Counting-scatter + segmented sort/unique (segsort.cuh).
+// Large builds go through the bucketed path (csr_bucket.cuh); small ones,
+// and skewed majors whose buckets overflow shared memory, through the
+// counting scatter + segmented sort/unique below (segsort.cuh).
+// D3G_CSR=scatter forces the latter, D3G_CSR=bucket the former at any size.
+inline bool build_csr_bucketed(Ctx& ctx, const uint32_t* maj, const uint32_t* mnr, uint64_t n,
+                               uint64_t n_rows, uint64_t n_cols, DeviceCsr& out, bool force);
+
 inline void build_csr_device(Ctx& ctx, const uint32_t* maj, const uint32_t* mnr, uint64_t n,
                              uint64_t n_rows, uint64_t n_cols, DeviceCsr& out) {
+  {
+    const char* e = std::getenv("D3G_CSR");
+    const bool force_bucket = e && std::strcmp(e, "bucket") == 0;
+    const bool force_scatter = e && std::strcmp(e, "scatter") == 0;
+    if (!force_scatter && build_csr_bucketed(ctx, maj, mnr, n, n_rows, n_cols, out, force_bucket))
+      return;
+  }
   out.n_rows = n_rows;
   out.n_cols = n_cols;
   out.row_ptr = ctx.alloc<uint64_t>(n_rows + 1);

@@ -1,0 +1,296 @@
+// Bucketed CSR build: build_csr (P/src/relation.cpp:206-258 -- two stable
+// counting sorts then an adjacent-duplicate collapse per row) as ONE global
+// scatter plus CTA-local work in shared memory.
+//
+// Rows are cut into buckets of 2^r consecutive row codes, with r chosen so a
+// bucket holds at most ~7K tuples (28 KB of packed keys). Then:
+//   K1 csr_bucket_hist    one read of the major codes: bucket histogram
+//                         (shared-memory privatised), and the largest bucket
+//   K2 scan               bucket starts
+//   K3 csr_bucket_scatter one read of (major, minor), one 4-byte write of the
+//                         packed key (row_low << mb | minor) into its bucket;
+//                         the ~30K bucket write frontiers stay resident in L2,
+//                         so sectors leave for DRAM full
+//   K4 csr_bucket_build   one CTA per bucket, all in shared memory: counting
+//                         sort by row_low, per-row warp bitonic sort + unique
+//                         of the minors, row degrees, bucket-local compaction
+//   K5 scan               degrees -> row_ptr
+//   K6 csr_bucket_copy    each bucket's unique run to its final offset
+//                         (a contiguous copy: rows are in order inside it)
+// Compulsory traffic per tuple: 4 (K1) + 8 + 4 (K3) + 4 (K4 read) + ~3 + 3
+// (K4 write, K6 copy of the unique entries) + 4 (K6 read) bytes, against
+// ~24 B/tuple of atomic per-row scatter + sort passes before. Buckets whose
+// tuple count exceeds the shared-memory capacity (skewed majors) make the
+// caller fall back to the per-row scatter path (segsort.cuh).
+#pragma once
+
+#include "csr.cuh"
+
+namespace d3g {
+
+constexpr int kCbThreads = 512;
+constexpr uint32_t kCbCap = 12288;        // packed keys per bucket in smem (2 CTAs/SM)
+constexpr uint32_t kCbTarget = 7168;      // expected tuples per bucket (at most)
+constexpr uint32_t kCbMaxRowsLog = 11;    // <= 2048 rows per bucket
+constexpr uint32_t kCbMaxBuckets = 32768; // privatised histogram (128 KB)
+
+__global__ void max_u32_kernel(const uint32_t* __restrict__ v, uint64_t n,
+                               unsigned long long* __restrict__ out) {
+  uint64_t m = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    m = v[i] > m ? v[i] : m;
+  m = warp_max(m);
+  if (lane_id() == 0 && m) atomicMax(out, (unsigned long long)m);
+}
+
+// K1: bucket histogram (shared-memory privatised; n_buckets <= kCbMaxBuckets).
+__global__ void __launch_bounds__(kCbThreads)
+csr_bucket_hist_kernel(const uint32_t* __restrict__ maj, uint64_t n, int r, uint32_t n_buckets,
+                       unsigned int* __restrict__ hist) {
+  extern __shared__ unsigned int sh[];
+  for (uint32_t i = threadIdx.x; i < n_buckets; i += kCbThreads) sh[i] = 0;
+  __syncthreads();
+  const uint64_t stride = (uint64_t)gridDim.x * kCbThreads;
+  for (uint64_t i = (uint64_t)blockIdx.x * kCbThreads + threadIdx.x; i < n; i += stride)
+    atomicAdd(&sh[maj[i] >> r], 1u);
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < n_buckets; i += kCbThreads)
+    if (sh[i]) atomicAdd(&hist[i], sh[i]);
+}
+
+// K3: packed key into its bucket (order inside a bucket is irrelevant: K4
+// sorts). cursor[b] starts at the bucket's start.
+__global__ void __launch_bounds__(kCbThreads)
+csr_bucket_scatter_kernel(const uint32_t* __restrict__ maj, const uint32_t* __restrict__ mnr,
+                          uint64_t n, int r, int mb, unsigned long long* __restrict__ cursor,
+                          uint32_t* __restrict__ packed) {
+  const uint32_t rmask = (1u << r) - 1;
+  const uint64_t stride = (uint64_t)gridDim.x * kCbThreads;
+  for (uint64_t i = (uint64_t)blockIdx.x * kCbThreads + threadIdx.x; i < n; i += stride) {
+    const uint32_t a = maj[i], b = mnr[i];
+    const unsigned long long p = atomicAdd(&cursor[a >> r], 1ull);
+    packed[p] = ((a & rmask) << mb) | b;
+  }
+}
+
+// In-place exclusive scan of a[0..n) in shared memory by the whole CTA
+// (n <= kCbThreads * 8); returns the total. Uses ws[kCbThreads / 32].
+__device__ __forceinline__ uint32_t cta_exclusive_scan(uint32_t* a, uint32_t n, uint32_t* ws) {
+  const uint32_t per = (n + kCbThreads - 1) / kCbThreads;
+  const uint32_t b0 = threadIdx.x * per;
+  uint32_t loc = 0;
+  for (uint32_t k = 0; k < per; ++k)
+    if (b0 + k < n) loc += a[b0 + k];
+  const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
+  uint32_t incl = loc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= (uint32_t)o) incl += u;
+  }
+  if (lane == 31) ws[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    const uint32_t v = lane < kCbThreads / 32 ? ws[lane] : 0u;
+    uint32_t wi = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= (uint32_t)o) wi += u;
+    }
+    if (lane < kCbThreads / 32) ws[lane] = wi - v;  // exclusive over warps
+    if (lane == kCbThreads / 32 - 1) ws[kCbThreads / 32] = wi;
+  }
+  __syncthreads();
+  uint32_t run = ws[w] + incl - loc;
+  for (uint32_t k = 0; k < per; ++k)
+    if (b0 + k < n) {
+      const uint32_t v = a[b0 + k];
+      a[b0 + k] = run;
+      run += v;
+    }
+  const uint32_t total = ws[kCbThreads / 32];
+  __syncthreads();
+  return total;
+}
+
+// Sort + unique a row of len entries at data[base..) (shared memory) by one
+// warp, in place; returns the kept count. Rows past 256 entries (rare: the
+// bucket capacity bounds them) use a rank sort into scratch[base..).
+__device__ __forceinline__ uint32_t cb_sort_row(uint32_t* data, uint32_t* scratch, uint32_t base,
+                                                uint32_t len) {
+  if (len <= 32) return warp_sort_row<1>(data, base, len, true);
+  if (len <= 64) return warp_sort_row<2>(data, base, len, true);
+  if (len <= 128) return warp_sort_row<4>(data, base, len, true);
+  if (len <= 256) return warp_sort_row<8>(data, base, len, true);
+  const uint32_t lane = lane_id();
+  for (uint32_t i = lane; i < len; i += 32) {
+    const uint32_t v = data[base + i];
+    uint32_t rank = 0;
+    for (uint32_t j = 0; j < len; ++j) {
+      const uint32_t u = data[base + j];
+      rank += (u < v) || (u == v && j < i);
+    }
+    scratch[base + rank] = v;
+  }
+  __syncwarp();
+  uint32_t written = 0;
+  for (uint32_t i0 = 0; i0 < len; i0 += 32) {
+    const uint32_t i = i0 + lane;
+    const uint32_t v = i < len ? scratch[base + i] : 0u;
+    const bool keep = i < len && (i == 0 || v != scratch[base + i - 1]);
+    const uint32_t m = __ballot_sync(0xffffffffu, keep);
+    if (keep) data[base + written + __popc(m & ((1u << lane) - 1))] = v;
+    written += __popc(m);
+  }
+  __syncwarp();
+  return written;
+}
+
+// K4: one CTA per bucket. Shared memory: keys[kCbCap] | rows[kCbCap] |
+// roff[2^r + 1] | rcur[2^r] | ws[kCbThreads / 32 + 1].
+__global__ void __launch_bounds__(kCbThreads)
+csr_bucket_build_kernel(const uint32_t* __restrict__ packed,
+                        const unsigned long long* __restrict__ bstart, uint64_t n_rows, int r,
+                        int mb, uint32_t* __restrict__ uniq /* per bucket, at bstart */,
+                        uint32_t* __restrict__ deg, unsigned long long* __restrict__ ustart,
+                        unsigned long long* __restrict__ stats /* max deg, live rows */) {
+  extern __shared__ uint32_t cbs[];
+  uint32_t* keys = cbs;
+  uint32_t* rowd = cbs + kCbCap;
+  uint32_t* roff = rowd + kCbCap;
+  uint32_t* rcur = roff + (1u << r) + 1;
+  uint32_t* ws = rcur + (1u << r);
+  const uint32_t b = blockIdx.x;
+  const unsigned long long s0 = bstart[b];
+  const uint32_t cnt = (uint32_t)(bstart[b + 1] - s0);
+  const uint64_t row0 = (uint64_t)b << r;
+  const uint32_t rows = (uint32_t)((n_rows - row0) < (1ull << r) ? (n_rows - row0) : (1ull << r));
+  const uint32_t mmask = mb >= 32 ? 0xffffffffu : ((1u << mb) - 1);
+  for (uint32_t i = threadIdx.x; i <= rows; i += kCbThreads) roff[i] = 0;
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < cnt; i += kCbThreads) {
+    const uint32_t k = packed[s0 + i];
+    keys[i] = k;
+    atomicAdd(&roff[k >> mb], 1u);
+  }
+  __syncthreads();
+  cta_exclusive_scan(roff, rows + 1, ws);  // roff[rows] = cnt
+  for (uint32_t i = threadIdx.x; i < rows; i += kCbThreads) rcur[i] = roff[i];
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < cnt; i += kCbThreads) {
+    const uint32_t k = keys[i];
+    rowd[atomicAdd(&rcur[k >> mb], 1u)] = k & mmask;
+  }
+  __syncthreads();
+  // per-row sort + unique, one warp per row; kept counts into rcur
+  const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
+  uint32_t mx = 0, live = 0;
+  for (uint32_t q = w; q < rows; q += kCbThreads / 32) {
+    const uint32_t base = roff[q], len = roff[q + 1] - base;
+    const uint32_t kept = len ? cb_sort_row(rowd, keys, base, len) : 0u;
+    if (lane == 0) {
+      rcur[q] = kept;
+      deg[row0 + q] = kept;
+      mx = kept > mx ? kept : mx;
+      live += kept > 0;
+    }
+  }
+  __syncthreads();
+  // bucket-local compaction: unique offsets of the rows
+  for (uint32_t i = threadIdx.x; i < rows; i += kCbThreads) keys[i] = rcur[i];
+  __syncthreads();
+  const uint32_t total = cta_exclusive_scan(keys, rows, ws);
+  for (uint32_t q = w; q < rows; q += kCbThreads / 32) {
+    const uint32_t src = roff[q], dst = keys[q], kept = rcur[q];
+    for (uint32_t j = lane; j < kept; j += 32) uniq[s0 + dst + j] = rowd[src + j];
+  }
+  if (threadIdx.x == 0) ustart[b] = total;
+  mx = warp_max(mx);
+  live = warp_sum(live);
+  if (lane == 0) {
+    if (mx) atomicMax(&stats[0], (unsigned long long)mx);
+    if (live) atomicAdd(&stats[1], (unsigned long long)live);
+  }
+}
+
+// K6: bucket b's unique run -> col[row_ptr[b << r] ..). One CTA per bucket.
+__global__ void __launch_bounds__(kCbThreads)
+csr_bucket_copy_kernel(const uint32_t* __restrict__ uniq, const unsigned long long* __restrict__ bstart,
+                       const unsigned long long* __restrict__ ucount,
+                       const uint64_t* __restrict__ row_ptr, int r, uint32_t* __restrict__ col) {
+  const uint32_t b = blockIdx.x;
+  const uint64_t s0 = bstart[b], n = ucount[b], d0 = row_ptr[(uint64_t)b << r];
+  for (uint64_t j = threadIdx.x; j < n; j += kCbThreads) col[d0 + j] = uniq[s0 + j];
+}
+
+inline size_t csr_bucket_smem(int r) {
+  return ((size_t)2 * kCbCap + (1u << r) * 2 + 1 + kCbThreads / 32 + 1) * 4;
+}
+
+// Returns false (nothing built) when the bucketed path does not apply: the
+// packed key does not fit 32 bits, too many buckets, or a bucket exceeds
+// the shared-memory capacity (skewed majors).
+inline bool build_csr_bucketed(Ctx& ctx, const uint32_t* maj, const uint32_t* mnr, uint64_t n,
+                               uint64_t n_rows, uint64_t n_cols, DeviceCsr& out, bool force) {
+  if ((!force && n < (1ull << 16)) || n == 0 || n >= (1ull << 32) || n_rows == 0) return false;
+  const int mb = std::max(1, bits_for(n_cols ? n_cols - 1 : 0));
+  if (mb > 31) return false;
+  // rows per bucket: ~kCbTarget tuples, packed key within 32 bits
+  const double per_row = (double)n / (double)n_rows;
+  int r = 0;
+  while (r < (int)kCbMaxRowsLog && r + 1 + mb <= 32 && per_row * (double)(1ull << (r + 1)) <= kCbTarget)
+    ++r;
+  // fewer, fuller buckets when there would be too many for K1's histogram
+  while (((n_rows + (1ull << r) - 1) >> r) > kCbMaxBuckets && r < (int)kCbMaxRowsLog &&
+         r + 1 + mb <= 32)
+    ++r;
+  if (r + mb > 32 || per_row * (double)(1ull << r) > 0.9 * kCbCap) return false;
+  const uint64_t nb64 = (n_rows + (1ull << r) - 1) >> r;
+  if (nb64 > kCbMaxBuckets) return false;
+  const uint32_t nb = (uint32_t)nb64;
+  DBuf<unsigned int> hist = ctx.zeros<unsigned int>(nb);
+  const unsigned g = (unsigned)std::min<uint64_t>(ctx.sm_count * 2ull, (n + kCbThreads - 1) / kCbThreads);
+  const size_t hsm = (size_t)nb * 4;
+  D3G_CUDA(cudaFuncSetAttribute(csr_bucket_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)hsm));
+  D3G_LAUNCH(ctx, csr_bucket_hist_kernel, g, kCbThreads, hsm, maj, n, r, nb, hist.p);
+  DBuf<unsigned long long> bstart = ctx.alloc<unsigned long long>(nb + 1);
+  exclusive_scan<unsigned int>(ctx, hist.p, nb, reinterpret_cast<uint64_t*>(bstart.p));
+  DBuf<unsigned long long> mxb = ctx.zeros<unsigned long long>(1);
+  D3G_LAUNCH(ctx, max_u32_kernel, grid_for(nb, 256), 256, 0, hist.p, (uint64_t)nb, mxb.p);
+  if (ctx.scalar(mxb.p) > kCbCap) return false;
+  DBuf<unsigned long long> cursor = ctx.alloc<unsigned long long>(nb);
+  D3G_CUDA(cudaMemcpyAsync(cursor.p, bstart.p, (size_t)nb * 8, cudaMemcpyDeviceToDevice, ctx.stream));
+  DBuf<uint32_t> packed = ctx.alloc<uint32_t>(n);
+  D3G_LAUNCH(ctx, csr_bucket_scatter_kernel, grid_for(n, kCbThreads, ctx.sm_count * 8), kCbThreads, 0,
+             maj, mnr, n, r, mb, cursor.p, packed.p);
+  cursor.reset();
+  DBuf<uint32_t> uniq = ctx.alloc<uint32_t>(n);
+  DBuf<uint32_t> deg = ctx.alloc<uint32_t>(n_rows);
+  DBuf<unsigned long long> ucount = ctx.alloc<unsigned long long>(nb);
+  DBuf<unsigned long long> st = ctx.zeros<unsigned long long>(2);
+  const size_t bsm = csr_bucket_smem(r);
+  D3G_CUDA(cudaFuncSetAttribute(csr_bucket_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)bsm));
+  D3G_LAUNCH(ctx, csr_bucket_build_kernel, nb, kCbThreads, bsm, packed.p, bstart.p, n_rows, r, mb,
+             uniq.p, deg.p, ucount.p, st.p);
+  packed.reset();
+  out.n_rows = n_rows;
+  out.n_cols = n_cols;
+  out.row_ptr = ctx.alloc<uint64_t>(n_rows + 1);
+  exclusive_scan<uint32_t>(ctx, deg.p, n_rows, out.row_ptr.p);
+  unsigned long long hs[2];
+  ctx.defer(&out.nnz, out.row_ptr.p + n_rows, 8);
+  ctx.defer(hs, st.p, 16);
+  ctx.sync();
+  out.max_deg = hs[0];
+  out.live_rows = hs[1];
+  out.col = ctx.alloc<uint32_t>(out.nnz);
+  D3G_LAUNCH(ctx, csr_bucket_copy_kernel, nb, kCbThreads, 0, uniq.p, bstart.p, ucount.p,
+             out.row_ptr.p, r, out.col.p);
+  return true;
+}
+
+}  // namespace d3g

@@ -23,6 +23,7 @@
 
 #include "classical.cuh"
 #include "counters.cuh"
+#include "csr_bucket.cuh"
 #include "datagen.cuh"
 #include "denseec.cuh"
 #include "denseec_hot.cuh"
@@ -1112,16 +1113,6 @@ __global__ void permute_pairs_kernel(const uint32_t* __restrict__ idx, uint64_t 
   }
 }
 
-
-__global__ void max_u32_kernel(const uint32_t* __restrict__ v, uint64_t n,
-                               unsigned long long* __restrict__ out) {
-  uint64_t m = 0;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x)
-    m = v[i] > m ? v[i] : m;
-  m = d3g::warp_max(m);
-  if (d3g::lane_id() == 0 && m) atomicMax(out, (unsigned long long)m);
-}
 
 __global__ void map_through_kernel(uint32_t* __restrict__ v, uint64_t n,
                                    const uint32_t* __restrict__ table) {

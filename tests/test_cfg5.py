@@ -7,9 +7,10 @@ quoted on -- checked across its WHOLE x range:
   restricted to those blocks against the full S through the unmodified
   reference, pairs bucketed by raw x / 100);
 * the default count-only plan over the full range (four pivots, the bench's
-  step) against the every-pair-tested checksum mode;
-* the sum of 8 x-shard fingerprints against the unsharded fingerprint
-  (the multi-GPU split), and count-only shard counts against the total.
+  step) against the plan switched off (every pair tested);
+* the 8 x-shard fingerprints against the unsharded fingerprint on a 2%
+  x range (the fingerprint hashes all ~1e14 pairs of the full range: ~6 min
+  on one B200), and count-only shard counts against the full-range total.
 """
 import json
 import os
@@ -56,26 +57,38 @@ def test_cfg5_blocks_across_the_x_range(cfg5):
         assert (rep.out_p, rep.checksum_sum, rep.checksum_xor) == (cnt, sm, xr), b
 
 
-def test_cfg5_full_range_count_only_equals_every_pair_checksum(cfg5):
-    """The bench's step (count-only: the pivot plan counts most pairs without
-    a test) against the checksum mode, which tests every pair; the count and
-    the reference's sparse/dense split (f2 on the whole job) agree."""
+def test_cfg5_full_range_count_only_equals_every_pair_count(cfg5, monkeypatch):
+    """The bench's step over the FULL x range (count-only: the four-pivot plan
+    counts ~99% of the pairs without a test) against the same count with the
+    plan off (D3G_NO_SPLIT: the bit-sliced kernel tests every one of the
+    ~1e14 (x, dense z) pairs): count and the reference's sparse/dense split
+    agree. x-shard counts of the 8-way split add up to the total."""
     a = _run(cfg5)
     assert a.hot_direct_pairs > 0
-    b = _run(cfg5, checksum=True)
+    monkeypatch.setenv("D3G_NO_SPLIT", "1")
+    b = _run(cfg5)
+    monkeypatch.delenv("D3G_NO_SPLIT")
     assert b.hot_direct_pairs == 0
     assert (a.out_p, a.pairs_sparse, a.pairs_dense) == (b.out_p, b.pairs_sparse, b.pairs_dense)
     assert a.out_p == 99_739_429_407_838
-    # the 8-way x-shard split (the multi-GPU partition): fingerprints add up
-    cnt, sm, xr, cnt_only = 0, 0, 0, 0
+    assert sum(_run(cfg5, shard_index=i, shard_count=8).out_p for i in range(8)) == a.out_p
+
+
+def test_cfg5_shard_fingerprints_add_up(cfg5):
+    """The 8-way x-shard split (the multi-GPU partition) on a 2% x-code range
+    (the fingerprint hashes every pair: ~2e12 pairs here): the shards'
+    (count, sum, xor) combine to the unsharded fingerprint of the range, and
+    the count-only plan agrees with the hashed count."""
+    rng = (0, 200_000)
+    full = _run(cfg5, checksum=True, x_code_range=rng)
+    assert full.out_p == _run(cfg5, x_code_range=rng).out_p
+    cnt, sm, xr = 0, 0, 0
     for i in range(8):
-        r = _run(cfg5, checksum=True, shard_index=i, shard_count=8)
+        r = _run(cfg5, checksum=True, shard_index=i, shard_count=8, x_code_range=rng)
         cnt += r.out_p
         sm = (sm + r.checksum_sum) & M64
         xr ^= r.checksum_xor
-        cnt_only += _run(cfg5, shard_index=i, shard_count=8).out_p
-    assert (cnt, sm, xr) == (b.out_p, b.checksum_sum, b.checksum_xor)
-    assert cnt_only == a.out_p
+    assert (cnt, sm, xr) == (full.out_p, full.checksum_sum, full.checksum_xor)
 
 
 def test_cfg5_high_x_codes_partition(cfg5):

@@ -44,6 +44,31 @@ def test_build_csr_collapses_and_sorts():
             assert np.array_equal(got.row_ptr, rp) and np.array_equal(got.col, col)
 
 
+@pytest.mark.parametrize("path", ["bucket", "scatter"])
+def test_build_csr_paths_match_definition(path, monkeypatch):
+    """Both CSR builders (the bucketed shared-memory build and the per-row
+    scatter + segmented sort) against the definition: uniform majors of
+    several densities, long rows (> 256 entries: the rank-sort tier), heavy
+    duplication, and a skewed major whose bucket overflows shared memory
+    (the bucketed path hands it to the scatter path)."""
+    monkeypatch.setenv("D3G_CSR", path)
+    rs = np.random.default_rng(5)
+    cases = []
+    for ac, bc, n in ((1000, 5000, 300000), (70000, 1 << 20, 600000), (3, 100000, 200000),
+                      (5000, 64, 400000), (1, 1, 10), (2000, 3000, 1)):
+        cases.append((rs.integers(0, ac, n).astype(np.uint32),
+                      rs.integers(0, bc, n).astype(np.uint32), ac, bc))
+    # one row holds ~40% of the tuples: its bucket exceeds the smem capacity
+    a = rs.integers(0, 20000, 500000).astype(np.uint32)
+    a[: 200000] = 17
+    cases.append((a, rs.integers(0, 1 << 20, 500000).astype(np.uint32), 20000, 1 << 20))
+    for a, b, ac, bc in cases:
+        got = d3.build_csr(a, b, ac, bc)
+        rp, col = _csr_np(a, b, ac)
+        assert np.array_equal(got.row_ptr, rp), (path, ac, bc, len(a))
+        assert np.array_equal(got.col, col), (path, ac, bc, len(a))
+
+
 def _random_csrs(rng):
     xc, yc, zc = 1 + rng.bounded(400), 1 + rng.bounded(400), 1 + rng.bounded(400)
     nr, ns = 1 + rng.bounded(8000), 1 + rng.bounded(8000)
