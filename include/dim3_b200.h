@@ -61,13 +61,17 @@ typedef struct d3g_ctx d3g_ctx;
 /* A two-column relation, row i = (left[i], right[i]); the same shape as
  * dim3::RawTable with ColumnType::u64 columns (P/include/dim3/relation.hpp:21-46).
  * on_device != 0: the pointers are CUDA device pointers on the context's
- * device (no H2D copy is made). */
+ * device (no H2D copy is made).
+ * value_bytes: 0 or 8 = u64 values (ColumnData::ints); 4 = the columns hold
+ * uint32_t values (cast the pointers): the int32 workloads copy half the
+ * bytes host -> device and are widened on the GPU (d3g_join_project only;
+ * the other entry points take u64 columns and raise ConfigError on 4). */
 typedef struct {
   const uint64_t* left;
   const uint64_t* right;
   uint64_t n;
   int32_t on_device;
-  int32_t pad;
+  int32_t value_bytes;
 } d3g_table;
 
 /* dim3::CostConstants (P/include/dim3/costmodel.hpp:21-30). */

@@ -79,6 +79,25 @@ __global__ void add_offset_kernel(uint32_t* __restrict__ v, uint64_t n, uint32_t
     v[i] += off;
 }
 
+// u32 -> u64 columns, four values per thread (16-byte loads, 2 x 16-byte stores)
+__global__ void widen_u32_kernel(const uint32_t* __restrict__ in, uint64_t n,
+                                 uint64_t* __restrict__ out) {
+  const uint64_t n4 = n / 4;
+  const bool aligned = (reinterpret_cast<uintptr_t>(in) & 15) == 0 &&
+                       (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (n + 3) / 4;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    if (aligned && i < n4) {
+      const uint4 v = reinterpret_cast<const uint4*>(in)[i];
+      ulonglong2* o = reinterpret_cast<ulonglong2*>(out + 4 * i);
+      o[0] = make_ulonglong2(v.x, v.y);
+      o[1] = make_ulonglong2(v.z, v.w);
+    } else {
+      for (uint64_t k = 4 * i; k < 4 * i + 4 && k < n; ++k) out[k] = in[k];
+    }
+  }
+}
+
 __global__ void iota_kernel(uint32_t* __restrict__ v, uint64_t n) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x)
@@ -1949,6 +1968,51 @@ void spa_counters(uint64_t x_rows, uint64_t z_card, int threads, d3g_report* rep
 }
 
 // ---------------------------------------------------------------------------
+// Input columns in HBM as u64. d3g_table::value_bytes == 4: the columns are
+// uint32_t (the int32 workloads), copied at 4 bytes per value and widened on
+// the GPU; u64 host columns are copied as they are.
+int table_value_bytes(const d3g_table* t) {
+  if (t->value_bytes == 0 || t->value_bytes == 8) return 8;
+  if (t->value_bytes == 4) return 4;
+  throw d3g::ConfigError("d3g_table.value_bytes must be 0, 4 or 8");
+}
+
+void resident_columns(Ctx& X, const d3g_table* t, DBuf<uint64_t>& lb, DBuf<uint64_t>& rb,
+                      const uint64_t*& l, const uint64_t*& r, d3g_report* rep) {
+  using namespace d3g;
+  const uint64_t n = t->n;
+  if (table_value_bytes(t) == 8) {
+    if (t->on_device) return;
+    lb = X.alloc<uint64_t>(n);
+    rb = X.alloc<uint64_t>(n);
+    X.to_device(lb.p, t->left, n);
+    X.to_device(rb.p, t->right, n);
+    l = lb.p;
+    r = rb.p;
+    rep->h2d_bytes += n * 16;
+    return;
+  }
+  lb = X.alloc<uint64_t>(n);
+  rb = X.alloc<uint64_t>(n);
+  const uint32_t* src[2] = {reinterpret_cast<const uint32_t*>(t->left),
+                            reinterpret_cast<const uint32_t*>(t->right)};
+  uint64_t* dst[2] = {lb.p, rb.p};
+  DBuf<uint32_t> stage;
+  if (!t->on_device && n) stage = X.alloc<uint32_t>(n);
+  for (int c = 0; c < 2; ++c) {
+    const uint32_t* in = src[c];
+    if (!t->on_device && n) {
+      X.to_device(stage.p, src[c], n);
+      in = stage.p;
+      rep->h2d_bytes += n * 4;
+    }
+    if (n) D3G_LAUNCH(X, widen_u32_kernel, grid_for((n + 3) / 4, 256), 256, 0, in, n, dst[c]);
+  }
+  l = lb.p;
+  r = rb.p;
+}
+
+// ---------------------------------------------------------------------------
 // The pipeline.
 void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g_consts* c,
                        const d3g_opts* o, d3g_report* rep, d3g_pairs* pairs) {
@@ -1978,32 +2042,20 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   const bool materialize = pairs != nullptr && !o->count_only;
   rep->materialized = materialize;
 
-  // 1. inputs resident in HBM
+  // 1. inputs resident in HBM (u64 columns; 4-byte columns are copied as
+  // such and widened on the device)
   DBuf<uint64_t> hb[4];
   const uint64_t* Rl = R->left;
   const uint64_t* Rr = R->right;
   const uint64_t* Sl = S->left;
   const uint64_t* Sr = S->right;
-  if (!R->on_device) {
-    hb[0] = X.alloc<uint64_t>(NR);
-    hb[1] = X.alloc<uint64_t>(NR);
-    X.to_device(hb[0].p, R->left, NR);
-    X.to_device(hb[1].p, R->right, NR);
-    Rl = hb[0].p;
-    Rr = hb[1].p;
-    rep->h2d_bytes += NR * 16;
-  }
-  if (!S->on_device && S->left == R->left && S->right == R->right && NS == NR) {
+  resident_columns(X, R, hb[0], hb[1], Rl, Rr, rep);
+  if (!S->on_device && S->left == R->left && S->right == R->right && NS == NR &&
+      S->value_bytes == R->value_bytes) {
     Sl = Rl;  // the same host relation passed twice (a self-join): copied once
     Sr = Rr;
-  } else if (!S->on_device) {
-    hb[2] = X.alloc<uint64_t>(NS);
-    hb[3] = X.alloc<uint64_t>(NS);
-    X.to_device(hb[2].p, S->left, NS);
-    X.to_device(hb[3].p, S->right, NS);
-    Sl = hb[2].p;
-    Sr = hb[3].p;
-    rep->h2d_bytes += NS * 16;
+  } else {
+    resident_columns(X, S, hb[2], hb[3], Sl, Sr, rep);
   }
   T.mark();  // 1
 
@@ -2308,6 +2360,8 @@ void stable_group(Ctx& X, const uint32_t* code, uint64_t n, uint64_t n_rows, DBu
 void join_aggregate_impl(Ctx& X, const d3g_valued_table* r, const d3g_valued_table* s,
                          int combine, int agg, const d3g_consts* c, const d3g_opts* o,
                          d3g_report* rep, d3g_agg_pairs* out) {
+  if (table_value_bytes(&r->base) != 8 || table_value_bytes(&s->base) != 8)
+    throw d3g::ConfigError("join_aggregate takes u64 columns (value_bytes 0 or 8)");
   using namespace d3g;
   if (o->threads < 1) throw ConfigError("threads must be >= 1");
   if (o->force == D3G_CLASSICAL) throw ConfigError("join-aggregate always runs the mapped pipeline");
@@ -2868,6 +2922,8 @@ int d3g_map_tables(d3g_ctx* ctx, const d3g_table* r, const d3g_table* s, const d
   d3g::Ctx& X = ctx->c;
   int rc = guarded([&] {
     using namespace d3g;
+    if (table_value_bytes(r) != 8 || table_value_bytes(s) != 8)
+      throw ConfigError("map_tables takes u64 columns (value_bytes 0 or 8)");
     D3G_CUDA(cudaSetDevice(X.device));
     X.begin_call();
     X.budget = o->memory_budget_bytes ? o->memory_budget_bytes : (3ull << 30);

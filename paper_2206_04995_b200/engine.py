@@ -152,6 +152,8 @@ class RawTable:
         self.right = _as_col(right if right is not None else [])
         if _length(self.left) != _length(self.right):
             raise FormatError("left and right columns differ in length")
+        if _itemsize(self.left) != _itemsize(self.right):
+            raise FormatError("left and right columns differ in width")
 
     def size(self) -> int:
         return _length(self.left)
@@ -167,16 +169,25 @@ def _is_cuda(a) -> bool:
     return getattr(a, "is_cuda", False)
 
 
+def _itemsize(a) -> int:
+    return int(a.element_size()) if _is_cuda(a) else int(a.dtype.itemsize)
+
+
 def _length(a) -> int:
     return int(a.shape[0]) if hasattr(a, "shape") else len(a)
 
 
 def _as_col(a):
+    """A column as the library takes it: 64-bit (u64 values), or 32-bit for
+    uint32 numpy arrays / int32 tensors (d3g_table.value_bytes = 4: half the
+    host->device bytes, widened on the GPU)."""
     if _is_cuda(a):
-        if a.element_size() != 8 or not a.is_contiguous():
-            raise FormatError("device columns must be contiguous 64-bit tensors")
+        if a.element_size() not in (4, 8) or not a.is_contiguous():
+            raise FormatError("device columns must be contiguous 32- or 64-bit tensors")
         return a
     arr = np.asarray(a)
+    if arr.dtype == np.uint32:
+        return np.ascontiguousarray(arr)
     if arr.dtype != np.uint64:
         if arr.size and arr.dtype.kind == "i" and int(arr.min()) < 0:
             raise FormatError("integer columns must be non-negative")
@@ -188,7 +199,7 @@ def _as_col(a):
 # ctypes mirror of include/dim3_b200.h
 class _Table(C.Structure):
     _fields_ = [("left", U64P), ("right", U64P), ("n", C.c_uint64), ("on_device", C.c_int32),
-                ("pad", C.c_int32)]
+                ("value_bytes", C.c_int32)]
 
 
 class _Consts(C.Structure):
@@ -479,10 +490,12 @@ class JoinProjectOutput:
 
 
 def _table_struct(t: RawTable) -> _Table:
+    vb = _itemsize(t.left)
     if t.on_device:
         return _Table(C.cast(C.c_void_p(t.left.data_ptr()), U64P),
-                      C.cast(C.c_void_p(t.right.data_ptr()), U64P), t.size(), 1, 0)
-    return _Table(t.left.ctypes.data_as(U64P), t.right.ctypes.data_as(U64P), t.size(), 0, 0)
+                      C.cast(C.c_void_p(t.right.data_ptr()), U64P), t.size(), 1, vb)
+    return _Table(C.cast(t.left.ctypes.data, U64P), C.cast(t.right.ctypes.data, U64P), t.size(), 0,
+                  vb)
 
 
 def _opts(cfg: EngineConfig) -> _Opts:

@@ -117,3 +117,16 @@ def test_forced_partitions():
     t, ev = d3.f2_decide(inp["mx_hist"], inp["mz_hist"], inp["x_card"], inp["y_card"],
                          inp["z_card"], inp["out_j"], C, force=d3.Strategy.dense_only)
     assert t[0] == 0 and all(t[m] == (inp["mz_hist"][m] > 0) for m in range(1, len(t)))
+
+
+def test_raw_table_column_widths():
+    """uint32 host columns keep their width (d3g_table.value_bytes = 4); other
+    integer dtypes are widened to u64; mixed widths are a FormatError."""
+    t = d3.RawTable(np.array([1, 2], np.uint32), np.array([3, 4], np.uint32))
+    assert t.left.dtype == np.uint32 and t.right.dtype == np.uint32
+    t = d3.RawTable(np.array([1, 2], np.int64), np.array([3, 4], np.int32))
+    assert t.left.dtype == np.uint64 and t.right.dtype == np.uint64
+    with pytest.raises(d3.FormatError):
+        d3.RawTable(np.array([1, 2], np.uint32), np.array([3, 4], np.uint64))
+    with pytest.raises(d3.FormatError):
+        d3.RawTable(np.array([-1, 2], np.int64), np.array([3, 4], np.int64))

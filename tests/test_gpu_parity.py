@@ -464,3 +464,32 @@ def test_pivot_plan_with_nothing_left_to_test():
     assert (got.out_p, got.pairs_sparse, got.pairs_dense) == \
         (base.out_p, base.pairs_sparse, base.pairs_dense)
     assert got.pairs_dense > 0 and got.hot_direct_pairs == got.pairs_dense  # all untested
+
+
+def test_int32_columns_match_u64(monkeypatch):
+    """d3g_table.value_bytes = 4 (the int32 workloads): uint32 host columns and
+    int32 device tensors give the same sets and reports as u64 columns, with
+    half the host->device bytes."""
+    import torch
+    rng = SplitMix64(611)
+    for _ in range(8):
+        r, s = random_instance(rng)
+        if max(int(r[0].max(initial=0)), int(r[1].max(initial=0)), int(s[0].max(initial=0)),
+               int(s[1].max(initial=0))) >= (1 << 32):
+            continue
+        a = _run(r, s, d3.Strategy.auto_select)
+        r32 = tuple(np.asarray(c, np.uint32) for c in r)
+        s32 = tuple(np.asarray(c, np.uint32) for c in s)
+        b = _run(r32, s32, d3.Strategy.auto_select)
+        assert pair_set(a.result.raw_x, a.result.raw_z) == pair_set(b.result.raw_x, b.result.raw_z)
+        assert (a.report.out_p, a.report.dense_z, a.report.strategy) == \
+            (b.report.out_p, b.report.dense_z, b.report.strategy)
+        assert b.report.h2d_bytes * 2 == a.report.h2d_bytes
+    g = [O.gen(1, 0).left, O.gen(1, 0).right, O.gen(1, 1).left, O.gen(1, 1).right]
+    dev = [torch.from_numpy(c.astype(np.int32)).cuda() for c in g]
+    out = d3.join_project(d3.RawTable(dev[0], dev[1]), d3.RawTable(dev[2], dev[3]),
+                          d3.EngineConfig(force=d3.Strategy.hybrid, count_only=True,
+                                          checksum=True), C).report
+    assert (out.out_p, out.checksum_sum, out.checksum_xor) == \
+        (9429141, 0x6F2F5D2033C05DA4, 0x50CAA74071957968)
+    assert out.h2d_bytes == 0
