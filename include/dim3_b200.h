@@ -153,6 +153,10 @@ typedef struct {
    * the stamp arrays the reference's run_chunked would allocate for
    * opts.threads over the engine's x rows, and |Z| per array. */
   uint64_t spa_allocations, spa_entries;
+  /* sharded job (exchange set): this rank's own pair count (materialized
+   * pairs are the rank's), and the job shape; 1 / 0 otherwise */
+  uint64_t rank_out_p;
+  int32_t nranks, rank;
 } d3g_report;
 
 /* Materialized output: caller-owned host (or device, on_device != 0)
@@ -321,6 +325,37 @@ int d3g_read_binary(d3g_ctx* ctx, const char* path, uint64_t* left, uint64_t* ri
  * the decoded (x, z) pairs (P/tools/dim3.cpp:212-218). */
 int d3g_save_pairs(d3g_ctx* ctx, const uint64_t* left, const uint64_t* right, uint64_t n,
                    int on_device, const char* path, int format);
+
+/* ---- multi-GPU: the x-sharded join_project --------------------
+ * With an exchange set on the context, d3g_join_project runs as one rank of
+ * an x-sharded job: r is THIS rank's shard of R (the rows whose x value the
+ * rank owns; shards are disjoint in x, e.g. contiguous x ranges or hash(x) mod
+ * nranks) and s is the whole of S. Partitioning R by x is intersection-free
+ * (the reference's x chunking, P/include/dim3/common.hpp:130-155), so no pair
+ * crosses ranks. The ranks exchange only
+ *   - the inputs of the global decisions: |R|, the column maxima and natural-
+ *     key sample tests of R, the per-y raw R counts (f1's join size), the m_x
+ *     histogram, dR(y), nnz and live/distinct x (f2, P/src/costmodel.cpp:515-586);
+ *   - the final tallies (count, fingerprint, pairs split, counters).
+ * Every rank then reports the JOB's totals (out_p, checksums, cards, split);
+ * materialized pairs are the rank's own. f1 uses the exact bag join size (the
+ * reference samples it above 65,536 rows); the natural-key sample test runs
+ * on each shard's rows against the global |R|. |R| >= |S| is required (no
+ * swap: the sharded table must stay the engine's R).
+ * Transports: NCCL (ncclAllReduce / ncclAllGather on the context's stream,
+ * over NVLink/NVSwitch; libnccl is dlopen'ed), or a host callback that
+ * performs each collective on host buffers (gloo, threads, replay). */
+#define D3G_EX_SUM_U64 0
+#define D3G_EX_SUM_U32 1
+#define D3G_EX_MAX_U64 2
+#define D3G_EX_GATHER 3  /* buf holds nranks * count bytes; fill the other ranks' blocks */
+typedef int (*d3g_exchange_fn)(void* user, int op, void* buf, uint64_t count);
+/* A new NCCL unique id (128 bytes) for rank 0 to share with the others. */
+int d3g_nccl_unique_id(void* id128);
+/* ncclCommInitRank on the context's device (collective over the job). */
+int d3g_ctx_set_nccl(d3g_ctx* ctx, const void* id128, int nranks, int rank);
+/* Host-callback transport; nranks = 1 and fn = NULL clear the exchange. */
+int d3g_ctx_set_exchange(d3g_ctx* ctx, int nranks, int rank, d3g_exchange_fn fn, void* user);
 
 /* Host-only policy entry points (callable without a GPU). */
 uint32_t d3g_f3_threshold(uint32_t m_x, uint32_t y_card, const d3g_consts* c);

@@ -24,6 +24,7 @@
 #include "classical.cuh"
 #include "counters.cuh"
 #include "csr_bucket.cuh"
+#include "exchange.cuh"
 #include "datagen.cuh"
 #include "denseec.cuh"
 #include "denseec_hot.cuh"
@@ -36,6 +37,7 @@
 
 struct d3g_ctx {
   d3g::Ctx c;
+  d3g::Exchange ex;  // multi-GPU exchange (exchange.cuh); inactive by default
 };
 
 namespace {
@@ -1600,6 +1602,7 @@ struct Mapped {
   DBuf<uint32_t> nar, s_y_own, s_z_own, r_y_own, r_x_own, r_kept;
   const uint32_t *r_x = nullptr, *r_y = nullptr, *s_z = nullptr, *s_y = nullptr;
   uint64_t kept = 0, x_card = 0, y_card = 0, z_card = 0;
+  uint64_t x_card_job = 0;  // the job's x card (sharded: summed local dictionaries)
   void release_codes() {
     r_x_own.reset();
     r_y_own.reset();
@@ -1611,7 +1614,8 @@ struct Mapped {
 
 void map_inputs(Ctx& X, const uint64_t* Rl, const uint64_t* Rr, uint64_t NR, const uint64_t* Sl,
                 const uint64_t* Sr, uint64_t NS, const d3g_opts* o, d3g_report* rep, bool want_kept,
-                Mapped& M) {
+                Mapped& M, d3g::Exchange* E = nullptr, uint64_t nr_global = 0) {
+  const bool dist = E && E->active();
   using namespace d3g;
   DBuf<ColStat> cs = X.zeros<ColStat>(4);
   const uint64_t* cols[4] = {Rl, Rr, Sl, Sr};
@@ -1625,6 +1629,7 @@ void map_inputs(Ctx& X, const uint64_t* Rl, const uint64_t* Rr, uint64_t NR, con
       c4.col[i] = cols[i];
       c4.n[i] = lens[i];
       c4.narrow[i] = ncol[i];
+      c4.bound_n[i] = (dist && i < 2) ? nr_global : lens[i];
     }
     const uint64_t mx = std::max(NR, NS);
     if (mx) {
@@ -1634,8 +1639,21 @@ void map_inputs(Ctx& X, const uint64_t* Rl, const uint64_t* Rr, uint64_t NR, con
   }
   ColStat hs[4];
   X.to_host(hs, cs.p, 4);
-  auto det = [&](int i) { return lens[i] > 0 && hs[i].sample_fail == 0; };
-  auto fits = [&](int i) { return lens[i] == 0 || hs[i].max < (1ull << 32); };
+  bool r_empty = NR == 0;
+  if (dist) {
+    // R is this rank's shard: the job's column maxima and sample tests (a
+    // shard fails the test if any of its strided samples reaches 2|R|)
+    uint64_t v[5] = {hs[0].max, hs[1].max, hs[0].sample_fail, hs[1].sample_fail, NR};
+    ex_allreduce_host(X, *E, v, 5, D3G_EX_MAX_U64);
+    hs[0].max = v[0];
+    hs[1].max = v[1];
+    hs[0].sample_fail = (unsigned)v[2];
+    hs[1].sample_fail = (unsigned)v[3];
+    r_empty = nr_global == 0;
+  }
+  const uint64_t lens_job[4] = {r_empty ? 0 : 1, r_empty ? 0 : 1, NS, NS};
+  auto det = [&](int i) { return lens_job[i] > 0 && hs[i].sample_fail == 0; };
+  auto fits = [&](int i) { return lens_job[i] == 0 || hs[i].max < (1ull << 32); };
   bool sx = o->declared_x != 0, sy = o->declared_y != 0, sz = o->declared_z != 0;
   if (o->natural_keys_auto) {
     sx = sx || det(0);
@@ -1666,7 +1684,7 @@ void map_inputs(Ctx& X, const uint64_t* Rl, const uint64_t* Rr, uint64_t NR, con
   M.r_y = ncol[1];
   M.r_x = ncol[0];
   if (sy) {
-    uint64_t a = NS ? hs[3].max + 1 : 0, b = NR ? hs[1].max + 1 : 0;
+    uint64_t a = NS ? hs[3].max + 1 : 0, b = !r_empty ? hs[1].max + 1 : 0;
     M.y_card = std::max(a, b);
     D.y.identity = true;
     D.y.card = M.y_card;
@@ -1718,7 +1736,7 @@ void map_inputs(Ctx& X, const uint64_t* Rl, const uint64_t* Rr, uint64_t NR, con
   }
   rep->dropped_r = NR - M.kept;
   if (sx) {
-    M.x_card = NR ? hs[0].max + 1 : 0;  // over all of R.left (mapping.cpp:404-413)
+    M.x_card = !r_empty ? hs[0].max + 1 : 0;  // over all of R.left (mapping.cpp:404-413)
     D.x.identity = true;
     D.x.card = M.x_card;
     if (M.kept != NR) {
@@ -1733,7 +1751,16 @@ void map_inputs(Ctx& X, const uint64_t* Rl, const uint64_t* Rr, uint64_t NR, con
     M.r_x = M.r_x_own.p;
     M.x_card = D.x.card;
   }
-  rep->x_card = M.x_card;
+  M.x_card_job = M.x_card;
+  if (dist) {
+    // shards are disjoint in x: a dictionary x card is the sum of the local
+    // ones (natural keys: every rank already holds the job's max + 1)
+    uint64_t v[2] = {sx ? 0 : M.x_card, rep->dropped_r};
+    ex_allreduce_host(X, *E, v, 2, D3G_EX_SUM_U64);
+    if (!sx) M.x_card_job = v[0];
+    rep->dropped_r = v[1];
+  }
+  rep->x_card = M.x_card_job;
   rep->y_card = M.y_card;
   rep->z_card = M.z_card;
   if (M.x_card >= (1ull << 32) || M.y_card >= (1ull << 32) || M.z_card >= (1ull << 32))
@@ -1750,11 +1777,18 @@ struct DegreeStats {
   // SpaStats::inner_count) is known on the host without another round trip
   std::vector<uint64_t> wz;
   DBuf<uint32_t> dR, dS;
+  // sharded job (exchange active): hmx/max_mx/x_live above are this rank's;
+  // these are the job's (the f2 inputs). Empty / 0 when not sharded.
+  std::vector<uint64_t> hmx_job;
+  uint64_t x_live_job = 0;
+  const std::vector<uint64_t>& hmx_f2() const { return hmx_job.empty() ? hmx : hmx_job; }
 };
 
 void degree_stats(Ctx& X, const d3g::DeviceCsr& rx, const d3g::DeviceCsr& sz_csr,
-                  uint64_t y_card, d3g_report* rep, DegreeStats& G, bool same = false) {
+                  uint64_t y_card, d3g_report* rep, DegreeStats& G, bool same = false,
+                  d3g::Exchange* E = nullptr, uint64_t x_card_job = 0) {
   using namespace d3g;
+  const bool dist = E && E->active();
   const uint64_t x_card = rx.n_rows, z_card = sz_csr.n_rows;
   if (rx.max_deg != ~0ull && sz_csr.max_deg != ~0ull) {  // read back with the CSR's nnz
     G.max_mx = rx.max_deg;
@@ -1802,6 +1836,9 @@ void degree_stats(Ctx& X, const d3g::DeviceCsr& rx, const d3g::DeviceCsr& sz_csr
   if (!same && sz_csr.nnz)
     D3G_LAUNCH(X, value_hist_kernel, grid_for(sz_csr.nnz, 512, X.sm_count * 2), 512, 0, sz_csr.col.p, sz_csr.nnz,
                G.dS.p, (uint32_t)y_card);
+  // sharded: dR(y) of the whole job (the y ranking, OUT_J and the per-degree
+  // join sizes below all read it)
+  if (dist) ex_allreduce(X, *E, G.dR.p, y_card, D3G_EX_SUM_U32);
   if (y_card) D3G_LAUNCH(X, outj_kernel, gb, 1024, 0, G.dR.p, G.dS.p, y_card, parts_p);
   if (z_card)
     D3G_LAUNCH(X, row_join_hist_kernel, grid_for(z_card * 8, 256), 256, 0, sz_csr.row_ptr.p,
@@ -1821,6 +1858,20 @@ void degree_stats(Ctx& X, const d3g::DeviceCsr& rx, const d3g::DeviceCsr& sz_csr
   rep->out_j = acc > (unsigned __int128)std::numeric_limits<uint64_t>::max()
                    ? std::numeric_limits<uint64_t>::max()
                    : (uint64_t)acc;
+  if (dist) {
+    // the job's m_x histogram: sized by the job's largest degree, summed;
+    // entry 0 (x codes with no R rows) recomputed from the job's x card
+    uint64_t mx = G.max_mx;
+    ex_allreduce_host(X, *E, &mx, 1, D3G_EX_MAX_U64);
+    G.hmx_job.assign(mx + 1, 0);
+    for (uint64_t m = 1; m < G.hmx.size(); ++m) G.hmx_job[m] = G.hmx[m];
+    ex_allreduce_host(X, *E, G.hmx_job.data(), mx + 1, D3G_EX_SUM_U64);
+    uint64_t live = 0;
+    for (uint64_t m = 1; m <= mx; ++m) live += G.hmx_job[m];
+    G.hmx_job[0] = x_card_job - live;
+    G.x_live_job = live;
+    rep->x_live = live;
+  }
 }
 
 // Step 7a: the f2 decision per degree value (policy.cpp) and the per-z
@@ -1847,14 +1898,15 @@ void f2_split(Ctx& X, const d3g::DeviceCsr& sz_csr, const DegreeStats& G, uint64
   uint64_t evals = 0;
   if (const char* dump = std::getenv("D3G_DUMP_F2")) {  // debugging aid: the f2 inputs
     if (FILE* f = std::fopen(dump, "wb")) {
-      uint64_t hdr[6] = {G.max_mx + 1, G.max_mz + 1, x_card, y_card, z_card, rep->out_j};
+      uint64_t hdr[6] = {G.hmx_f2().size(), G.max_mz + 1, x_card, y_card, z_card, rep->out_j};
       std::fwrite(hdr, 8, 6, f);
-      std::fwrite(G.hmx.data(), 8, G.max_mx + 1, f);
+      std::fwrite(G.hmx_f2().data(), 8, G.hmx_f2().size(), f);
       std::fwrite(G.hmz.data(), 8, G.max_mz + 1, f);
       std::fclose(f);
     }
   }
-  d3g_f2_decide(G.hmx.data(), G.max_mx + 1, G.hmz.data(), G.max_mz + 1, x_card, y_card, z_card,
+  const std::vector<uint64_t>& hx = G.hmx_f2();  // the job's (sharded) or this call's
+  d3g_f2_decide(hx.data(), hx.size(), G.hmz.data(), G.max_mz + 1, x_card, y_card, z_card,
                 rep->out_j, c, pforce, table.data(), &evals);
   rep->f2_evaluations = evals;
   P.dtable = X.alloc<uint8_t>(G.max_mz + 1);
@@ -2015,8 +2067,11 @@ void resident_columns(Ctx& X, const d3g_table* t, DBuf<uint64_t>& lb, DBuf<uint6
 // ---------------------------------------------------------------------------
 // The pipeline.
 void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g_consts* c,
-                       const d3g_opts* o, d3g_report* rep, d3g_pairs* pairs) {
+                       const d3g_opts* o, d3g_report* rep, d3g_pairs* pairs,
+                       d3g::Exchange* E = nullptr) {
   using namespace d3g;
+  // sharded job: r is this rank's x-shard of R (exchange.cuh)
+  const bool dist = E && E->active();
   if (o->threads < 1) throw ConfigError("threads must be >= 1");
   if (c->w == 0 || c->w % 64 != 0) throw ConfigError("block width W must be a positive multiple of 64");
   const int shard_count = o->shard_count < 1 ? 1 : o->shard_count;
@@ -2032,11 +2087,15 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   Timer T(X);
   T.mark();  // 0
 
-  const bool swapped = s->n > r->n;  // engine_will_swap (engine.cpp:341-343)
+  uint64_t nr_job = r->n;  // |R| of the whole job
+  if (dist) ex_allreduce_host(X, *E, &nr_job, 1, D3G_EX_SUM_U64);
+  if (dist && s->n > nr_job)
+    throw ConfigError("a sharded join_project needs |R| >= |S| (shard the larger table)");
+  const bool swapped = s->n > nr_job;  // engine_will_swap (engine.cpp:341-343)
   const d3g_table* R = swapped ? s : r;
   const d3g_table* S = swapped ? r : s;
   rep->swapped = swapped;
-  rep->r_rows = R->n;
+  rep->r_rows = swapped ? R->n : nr_job;
   rep->s_rows = S->n;
   const uint64_t NR = R->n, NS = S->n;
   const bool materialize = pairs != nullptr && !o->count_only;
@@ -2062,17 +2121,20 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   // 2. f1 gate (engine.cpp:368-384): auto takes the classical join iff f1 > 0.
   // The estimate and the self-join test are launched now and read back with
   // the column statistics (one round trip for the three).
+  // (sharded: no rank holds R's strided samples; f1 takes the exact bag join
+  // size, summed over the ranks after the mapping)
   EstimateJob est;
-  estimate_out_j_start(X, Rr, NR, Sr, NS, est);
+  if (!dist) estimate_out_j_start(X, Rr, NR, Sr, NS, est);
+  uint64_t bag_job = 0;
   IdentityJob ident;
-  const bool try_selfjoin = std::getenv("D3G_NO_SELFJOIN") == nullptr;
+  const bool try_selfjoin = !dist && std::getenv("D3G_NO_SELFJOIN") == nullptr;
   if (try_selfjoin) tables_identical_start(X, Rl, Rr, Sl, Sr, NR, NS, ident);
   const char* cls_env = std::getenv("D3G_CLASSICAL");
-  const bool global_classical = cls_env && std::strcmp(cls_env, "global") == 0;
+  const bool global_classical = !dist && cls_env && std::strcmp(cls_env, "global") == 0;
   bool classical = false;
   auto decide_f1 = [&] {
-    rep->out_j_estimate = est.value(X);
-    rep->f1 = d3g_f1(NR, NS, rep->out_j_estimate, c);
+    rep->out_j_estimate = dist ? bag_job : est.value(X);
+    rep->f1 = d3g_f1(dist ? nr_job : NR, NS, rep->out_j_estimate, c);
     rep->f1_gate_classical = (o->force == D3G_AUTO && rep->f1 > 0) ? 1 : 0;
     classical = o->force == D3G_CLASSICAL || rep->f1_gate_classical;
     const char* strat = classical                    ? "classical"
@@ -2105,12 +2167,32 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
 
   // 3-4. natural keys + mapping
   Mapped M;
-  map_inputs(X, Rl, Rr, NR, Sl, Sr, NS, o, rep, /*want_kept=*/false, M);
+  map_inputs(X, Rl, Rr, NR, Sl, Sr, NS, o, rep, /*want_kept=*/false, M, E, nr_job);
+  if (dist) {
+    // the job's bag join size sum_y |R_y| |S_y| (estimate_out_j_raw's exact
+    // case, P/src/costmodel.cpp:375-409): per-y raw R counts summed over ranks
+    const uint64_t yc = M.y_card;
+    DBuf<uint32_t> cr = X.zeros<uint32_t>(yc), cs2 = X.zeros<uint32_t>(yc);
+    if (M.kept) D3G_LAUNCH(X, group_hist_kernel, grid_for(M.kept, 256), 256, 0, M.r_y, M.kept, cr.p);
+    if (NS) D3G_LAUNCH(X, group_hist_kernel, grid_for(NS, 256), 256, 0, M.s_y, NS, cs2.p);
+    ex_allreduce(X, *E, cr.p, yc, D3G_EX_SUM_U32);
+    const unsigned gb = grid_for(yc, 1024, 296);
+    DBuf<unsigned long long> parts = X.zeros<unsigned long long>(2ull * gb);
+    if (yc) D3G_LAUNCH(X, outj_kernel, gb, 1024, 0, cr.p, cs2.p, yc, parts.p);
+    std::vector<unsigned long long> hp(2ull * gb);
+    X.to_host(hp.data(), parts.p, 2ull * gb);
+    unsigned __int128 acc = 0;
+    for (unsigned i = 0; i < gb; ++i) acc += ((unsigned __int128)hp[2 * i + 1] << 64) | hp[2 * i];
+    bag_job = acc > (unsigned __int128)~0ull ? ~0ull : (uint64_t)acc;
+  }
   if (!global_classical) decide_f1();  // delivered by map_inputs' first round trip
   const bool self_join = try_selfjoin && ident.value(X);
   const uint64_t kept = M.kept, x_card = M.x_card, y_card = M.y_card, z_card = M.z_card;
+  const uint64_t x_card_job = M.x_card_job;
   DictBundle& D = M.D;
-  if (classical) {  // intermediate_pairs = bag join size, duplicates included
+  if (classical && dist) {
+    rep->intermediate_pairs = bag_job;
+  } else if (classical) {  // intermediate_pairs = bag join size, duplicates included
     DBuf<uint32_t> cnt = X.zeros<uint32_t>(y_card);
     if (NS) D3G_LAUNCH(X, group_hist_kernel, grid_for(NS, 256), 256, 0, M.s_y, NS, cnt.p);
     DBuf<unsigned long long> bag = X.zeros<unsigned long long>(1);
@@ -2133,11 +2215,12 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   M.release_codes();
   rep->r_nnz = rx.nnz;
   rep->s_nnz = sz_csr.nnz;
+  if (dist) ex_allreduce_host(X, *E, &rep->r_nnz, 1, D3G_EX_SUM_U64);
   T.mark();  // 4
 
   // 6. degree statistics (compute_degree_stats, costmodel.cpp:425-438)
   DegreeStats G;
-  degree_stats(X, rx, sz_csr, y_card, rep, G, same_csr);
+  degree_stats(X, rx, sz_csr, y_card, rep, G, same_csr, E, x_card_job);
   const uint64_t max_mx = G.max_mx, x_live = G.x_live, max_mz = G.max_mz;
   const std::vector<uint64_t>& hmx = G.hmx;
   DBuf<uint32_t>& dR = G.dR;
@@ -2148,7 +2231,8 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
                      : o->force == D3G_DENSE_ONLY ? D3G_DENSE_ONLY
                                                   : D3G_HYBRID;
   Split P;
-  f2_split(X, sz_csr, G, x_card, y_card, c, pforce, rep, P, nullptr, nullptr, /*flags=*/false);
+  f2_split(X, sz_csr, G, x_card_job, y_card, c, pforce, rep, P, nullptr, nullptr,
+           /*flags=*/false);
   const uint64_t n_dense = P.n_dense, n_sparse = P.n_sparse;
   rep->sparse_nnz = P.sparse_nnz;  // known on the host (m_z histogram)
   // optional x-code restriction of the kernels (opts x_code_lo/hi)
@@ -2164,8 +2248,9 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   // the sparse kernel's output, computed faster. OUT_J,sparse
   // (SpaStats::inner_count) comes from the per-degree join sizes.
   const uint64_t outj_sp = P.outj_sparse;
-  const bool heavy_sparse = std::getenv("D3G_SPARSE_TIERS") == nullptr && x_live > 0 &&
-                            n_sparse > 0 && outj_sp > 4096ull * x_live;
+  const uint64_t x_live_job = dist ? G.x_live_job : x_live;
+  const bool heavy_sparse = std::getenv("D3G_SPARSE_TIERS") == nullptr && x_live_job > 0 &&
+                            n_sparse > 0 && outj_sp > 4096ull * x_live_job;
   // folded rows need the record-based hot kernels and the cold kernels
   const char* hot_env = std::getenv("D3G_HOT");
   const std::string hot_sel = hot_env ? hot_env : "";
@@ -2233,7 +2318,7 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   // reference-equivalent work counters over this call's x codes (SpaStats,
   // DenseEcStats; counters.cuh)
   if (!classical) {
-    spa_counters(x_card, z_card, o->threads, rep);
+    spa_counters(x_card_job, z_card, o->threads, rep);
     DenseCounters dc{};
     const std::vector<uint32_t> thr = mode_thresholds(max_mx, y_card, c, o->dense_mode);
     if (o->collect_counters) {
@@ -2296,10 +2381,42 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   rep->out_p = ks.count + kd.count;
   rep->checksum_sum = ks.sum + kd.sum;
   rep->checksum_xor = ks.xr ^ kd.xr;
+  rep->rank_out_p = rep->out_p;
+  rep->nranks = dist ? E->nranks : 1;
+  rep->rank = dist ? E->rank : 0;
+  if (dist) {
+    // the job's totals: each rank's tally record, gathered and folded
+    // (the fingerprint's xor has no NCCL reduction)
+    constexpr int kF = 13;
+    uint64_t mine[kF] = {rep->out_p, rep->pairs_sparse, rep->pairs_dense, rep->checksum_sum,
+                         rep->checksum_xor, rep->hot_direct_pairs, rep->cold_bytes,
+                         rep->hot_lds_bytes, rep->dense_wide_encounters,
+                         rep->dense_probe_encounters, rep->dense_blocks_checked,
+                         rep->dense_probes_done, rep->dense_row_bitmaps_built};
+    std::vector<uint64_t> all((size_t)kF * E->nranks);
+    ex_allgather(X, *E, mine, all.data(), sizeof(mine));
+    uint64_t tot[kF] = {0};
+    for (int q = 0; q < E->nranks; ++q)
+      for (int f = 0; f < kF; ++f)
+        tot[f] = f == 4 ? (tot[f] ^ all[(size_t)q * kF + f]) : tot[f] + all[(size_t)q * kF + f];
+    rep->out_p = tot[0];
+    rep->pairs_sparse = tot[1];
+    rep->pairs_dense = tot[2];
+    rep->checksum_sum = tot[3];
+    rep->checksum_xor = tot[4];
+    rep->hot_direct_pairs = tot[5];
+    rep->cold_bytes = tot[6];
+    rep->hot_lds_bytes = tot[7];
+    rep->dense_wide_encounters = tot[8];
+    rep->dense_probe_encounters = tot[9];
+    rep->dense_blocks_checked = tot[10];
+    rep->dense_probes_done = tot[11];
+    rep->dense_row_bitmaps_built = tot[12];
+  }
 
   // 9. materialization (decode, engine.cpp:502-529)
   if (materialize)
-    materialize_pairs(X, rep->out_p, [&](Emit em) {
+    materialize_pairs(X, rep->rank_out_p, [&](Emit em) {
       KernelOut tmp;
       if (sparse_hot)
         run_dense_hot(X, dsi, dec, kModeEmit, em, tmp);
@@ -2601,6 +2718,47 @@ int d3g_ctx_create(int device, d3g_ctx** out) {
   });
 }
 
+int d3g_nccl_unique_id(void* id128) {
+  return guarded([&] {
+    ncclUniqueId id;
+    D3G_NCCL(d3g::nccl().get_unique_id(&id));
+    std::memcpy(id128, &id, sizeof(id));
+  });
+}
+
+int d3g_ctx_set_nccl(d3g_ctx* ctx, const void* id128, int nranks, int rank) {
+  return guarded([&] {
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw d3g::ConfigError("bad nranks / rank");
+    D3G_CUDA(cudaSetDevice(ctx->c.device));
+    if (ctx->ex.comm) {
+      d3g::nccl().comm_destroy(ctx->ex.comm);
+      ctx->ex.comm = nullptr;
+    }
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof(id));
+    D3G_NCCL(d3g::nccl().comm_init_rank(&ctx->ex.comm, nranks, id, rank));
+    ctx->ex.nranks = nranks;
+    ctx->ex.rank = rank;
+    ctx->ex.host_fn = nullptr;
+    ctx->ex.host_user = nullptr;
+  });
+}
+
+int d3g_ctx_set_exchange(d3g_ctx* ctx, int nranks, int rank, d3g_exchange_fn fn, void* user) {
+  return guarded([&] {
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw d3g::ConfigError("bad nranks / rank");
+    if (nranks > 1 && !fn) throw d3g::ConfigError("an exchange over several ranks needs a callback");
+    if (ctx->ex.comm) {
+      d3g::nccl().comm_destroy(ctx->ex.comm);
+      ctx->ex.comm = nullptr;
+    }
+    ctx->ex.nranks = nranks;
+    ctx->ex.rank = rank;
+    ctx->ex.host_fn = fn;
+    ctx->ex.host_user = user;
+  });
+}
+
 void d3g_ctx_destroy(d3g_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->c.device);
@@ -2633,7 +2791,7 @@ int d3g_join_project(d3g_ctx* ctx, const d3g_table* r, const d3g_table* s, const
     D3G_CUDA(cudaSetDevice(ctx->c.device));
     ctx->c.begin_call();
     try {
-      join_project_impl(ctx->c, r, s, c, o, rep, pairs);
+      join_project_impl(ctx->c, r, s, c, o, rep, pairs, &ctx->ex);
     } catch (...) {
       cudaStreamSynchronize(ctx->c.stream);
       ctx->c.budget = 0;  // the memory budget is scoped to one call

@@ -60,6 +60,7 @@ struct Cols4 {
   const uint64_t* col[4];
   uint64_t n[4];
   uint32_t* narrow[4];
+  uint64_t bound_n[4];  // the sample test's n (the global |R| for an R shard)
 };
 
 __global__ void __launch_bounds__(256) colstat4_kernel(Cols4 c, ColStat* st) {
@@ -92,7 +93,7 @@ __global__ void __launch_bounds__(256) colstat4_kernel(Cols4 c, ColStat* st) {
     uint64_t samples = n < 4096 ? n : 4096;
     uint64_t sstride = samples ? n / samples : 1;
     if (sstride < 1) sstride = 1;
-    double bound = 2.0 * (double)n;
+    double bound = 2.0 * (double)c.bound_n[ci];
     for (uint64_t k = threadIdx.x; k < samples; k += blockDim.x) {
       uint64_t idx = k * sstride;
       if (idx > n - 1) idx = n - 1;

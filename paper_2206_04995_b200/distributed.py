@@ -1,85 +1,152 @@
-"""Multi-GPU host logic (one process per GPU, torch.distributed for plumbing).
+"""Multi-GPU host plumbing for the x-sharded join_project.
 
-The path shards naturally by x: partitioning R by x is
-intersection-free (P/src/sparsebmm.cpp:79-104 chunks threads the same way),
-so no cross-GPU dedup exists. Two exchange steps remain:
+The library runs one rank of a sharded job when its context has an exchange
+(``Context.set_nccl`` or ``Context.set_exchange``): each rank passes its
+x-shard of R and the whole S, and ``d3g_join_project`` performs the few
+collectives the global decisions need (column maxima and natural-key tests,
+the per-y raw R counts behind f1, the m_x histogram, dR(y), nnz / live x, the
+final tallies; see include/dim3_b200.h and csrc/exchange.cuh). Partitioning R
+by x is intersection-free (the reference's own x chunking,
+P/include/dim3/common.hpp:130-155), so no pair ever crosses ranks.
 
-1. f2 inputs. When each rank holds only its x-shard of R, the dense/sparse
-   decision (P/src/costmodel.cpp:515-586) must still see GLOBAL statistics:
-   the m_x histogram (sum), dR(y) (sum, for OUT_J = sum_y dR*dS), r_nnz
-   (sum), x_card (max under natural keys, sum of disjoint local dictionaries
-   otherwise). S is replicated (broadcast once), so m_z / dS / z_card /
-   y_card are already global. ``allreduce_f2_inputs`` performs the
-   all-reduces; every rank then evaluates the identical decision table with
-   ``d3g_f2_decide``.
-2. Results: per-rank pair counts and (sum, xor) fingerprints are combined
-   with ``reduce_tally``.
+On GPUs the transport is NCCL over NVLink (``Context.set_nccl``). The
+host-callback transport takes any object with ``__call__(op, arr)`` that
+performs the collective in place on a numpy array:
 
-With the single-call API (``EngineConfig.shard_index/shard_count``) every
-rank receives full R and S (NCCL broadcast), computes the statistics
-redundantly and runs the kernels on its x shard only, so step 1 is not
-needed; the functions here serve the partitioned-input deployment and are
-covered by the gloo tests.
+* ``TorchExchange``   -- torch.distributed (gloo on CPU tensors): the
+  multi-process form, covered by the world-size-2 gloo tests;
+* ``ThreadExchange``  -- ranks as threads of one process (a barrier): used to
+  run an N-rank job on ONE GPU for parity tests. Only host threads wait on
+  one another; no kernel waits for another rank's kernel;
+* ``RecordingExchange`` / ``ReplayExchange`` -- record a rank's collective
+  results in a threaded run, then replay them so that rank can be re-run
+  ALONE on the GPU and timed without contention (scripts/shard_projection.py).
+
+Sharding helpers split R by contiguous x ranges (natural keys) or by a hash of
+the raw x value (dictionary keys: local dictionaries stay disjoint).
 """
 from __future__ import annotations
 
+import threading
+
 import numpy as np
+
+from .engine import EX_GATHER, EX_MAX_U64, EX_SUM_U32, EX_SUM_U64
 
 U64_MASK = (1 << 64) - 1
 
 
-def _to_i64(v: int) -> int:
-    v &= U64_MASK
-    return v - (1 << 64) if v >= (1 << 63) else v
+def _fold(op: int, parts: list[np.ndarray]) -> np.ndarray:
+    if op == EX_MAX_U64:
+        return np.maximum.reduce(parts)
+    out = parts[0].copy()
+    for p in parts[1:]:
+        out += p  # modular (uint64 / uint32 wrap like the device sums)
+    return out
 
 
-def _pad_allreduce(arr: np.ndarray, dist, group=None, op=None):
-    import torch
-    n = torch.tensor([arr.size], dtype=torch.int64)
-    dist.all_reduce(n, op=dist.ReduceOp.MAX, group=group)
-    t = torch.zeros(int(n.item()), dtype=torch.int64)
-    t[: arr.size] = torch.from_numpy(arr.astype(np.int64))
-    dist.all_reduce(t, op=op or dist.ReduceOp.SUM, group=group)
-    return t.numpy().astype(np.uint64)
+class ThreadExchange:
+    """Collectives among `nranks` threads of one process. Each rank uses
+    ``rank_fn(r)`` as its exchange callback."""
+
+    def __init__(self, nranks: int):
+        self.nranks = nranks
+        self.barrier = threading.Barrier(nranks)
+        self.slots: list = [None] * nranks
+
+    def rank_fn(self, rank: int):
+        def fn(op: int, arr: np.ndarray):
+            if op == EX_GATHER:
+                nb = arr.size // self.nranks
+                self.slots[rank] = arr[rank * nb:(rank + 1) * nb].copy()
+                self.barrier.wait()
+                for q in range(self.nranks):
+                    arr[q * nb:(q + 1) * nb] = self.slots[q]
+            else:
+                self.slots[rank] = arr.copy()
+                self.barrier.wait()
+                arr[:] = _fold(op, list(self.slots))
+            self.barrier.wait()  # slots are reused by the next collective
+        return fn
 
 
-def allreduce_f2_inputs(local: dict, dist, group=None, natural_x: bool = True) -> dict:
-    """local: {"mx_hist", "dr" (array over y codes), "x_card", "r_nnz"} of this
-    rank's R shard plus the replicated S-side {"mz_hist", "ds", "y_card",
-    "z_card"}. Returns the global inputs of d3g_f2_decide."""
-    import torch
-    mx = _pad_allreduce(np.asarray(local["mx_hist"], np.uint64), dist, group)
-    mx[0] = 0
-    dr = _pad_allreduce(np.asarray(local["dr"], np.uint64), dist, group)
-    sc = torch.tensor([int(local["x_card"]), int(local["r_nnz"])], dtype=torch.int64)
-    xc = sc[:1].clone()
-    dist.all_reduce(xc, op=dist.ReduceOp.MAX if natural_x else dist.ReduceOp.SUM, group=group)
-    nnz = sc[1:].clone()
-    dist.all_reduce(nnz, op=dist.ReduceOp.SUM, group=group)
-    ds = np.asarray(local["ds"], np.uint64)
-    n = min(dr.size, ds.size)
-    out_j = int(np.dot(dr[:n].astype(object), ds[:n].astype(object))) if n else 0
-    return {"mx_hist": mx, "mz_hist": np.asarray(local["mz_hist"], np.uint64),
-            "x_card": int(xc.item()), "y_card": int(local["y_card"]),
-            "z_card": int(local["z_card"]), "out_j": min(out_j, U64_MASK),
-            "r_nnz": int(nnz.item())}
+class TorchExchange:
+    """Collectives over a torch.distributed process group (gloo / CPU)."""
+
+    def __init__(self, dist, group=None):
+        self.dist, self.group = dist, group
+        self.nranks = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+
+    def __call__(self, op: int, arr: np.ndarray):
+        import torch
+        d = self.dist
+        if op == EX_GATHER:
+            nb = arr.size // self.nranks
+            mine = torch.from_numpy(arr[self.rank * nb:(self.rank + 1) * nb].copy())
+            outs = [torch.empty_like(mine) for _ in range(self.nranks)]
+            d.all_gather(outs, mine, group=self.group)
+            for q, t in enumerate(outs):
+                arr[q * nb:(q + 1) * nb] = t.numpy()
+            return
+        if op == EX_MAX_U64:
+            # torch has no uint64 max: values here are maxima / flags < 2^63
+            t = torch.from_numpy(arr.astype(np.int64))
+            d.all_reduce(t, op=d.ReduceOp.MAX, group=self.group)
+            arr[:] = t.numpy().astype(np.uint64)
+            return
+        # sums: int64 two's complement wraps exactly like uint64 (mod 2^64)
+        t = torch.from_numpy(arr.astype(np.int64) if op == EX_SUM_U64 else arr.astype(np.int64))
+        d.all_reduce(t, op=d.ReduceOp.SUM, group=self.group)
+        res = t.numpy()
+        arr[:] = (res.astype(np.uint64) if op == EX_SUM_U64
+                  else (res & 0xFFFFFFFF).astype(np.uint32))
 
 
-def reduce_tally(count: int, csum: int, cxor: int, dist, group=None):
-    """Global (count, sum mod 2^64, xor) of per-rank results (intersection-free
-    shards: plain sums, no dedup)."""
-    import torch
-    t = torch.tensor([_to_i64(count), _to_i64(csum)], dtype=torch.int64)
-    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
-    world = dist.get_world_size(group)
-    xs = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
-    dist.all_gather(xs, torch.tensor([_to_i64(cxor)], dtype=torch.int64), group=group)
-    x = 0
-    for v in xs:
-        x ^= int(v.item()) & U64_MASK
-    return int(t[0].item()) & U64_MASK, int(t[1].item()) & U64_MASK, x
+class RecordingExchange:
+    """Wraps an exchange and records every collective's result, in order."""
+
+    def __init__(self, inner):
+        self.inner, self.log = inner, []
+
+    def __call__(self, op: int, arr: np.ndarray):
+        self.inner(op, arr)
+        self.log.append((op, arr.copy()))
 
 
-def x_shard_bounds(x_card: int, rank: int, world: int):
-    """Contiguous x-code range of a rank (natural keys)."""
-    return x_card * rank // world, x_card * (rank + 1) // world
+class ReplayExchange:
+    """Returns recorded results in order (a rank re-run alone, same inputs)."""
+
+    def __init__(self, log):
+        self.log, self.i = log, 0
+
+    def __call__(self, op: int, arr: np.ndarray):
+        rop, val = self.log[self.i]
+        self.i += 1
+        if rop != op or val.shape != arr.shape:
+            raise RuntimeError("replayed exchange diverged from the recorded run")
+        arr[:] = val
+
+    def rewind(self):
+        self.i = 0
+
+
+def x_range_bounds(x_card: int, rank: int, nranks: int):
+    """Contiguous raw-x range [lo, hi) of a rank (natural keys)."""
+    return x_card * rank // nranks, x_card * (rank + 1) // nranks
+
+
+def shard_mask(x: np.ndarray, rank: int, nranks: int, x_card: int | None = None) -> np.ndarray:
+    """Rows of R owned by `rank`: contiguous ranges when x_card is given
+    (natural keys), else a hash of the raw value (mix64 mod nranks)."""
+    x = np.asarray(x, dtype=np.uint64)
+    if x_card is not None:
+        lo, hi = x_range_bounds(x_card, rank, nranks)
+        return (x >= lo) & (x < hi)
+    h = x.copy()
+    h ^= h >> np.uint64(30)
+    h *= np.uint64(0xBF58476D1CE4E5B9)
+    h ^= h >> np.uint64(27)
+    h *= np.uint64(0x94D049BB133111EB)
+    h ^= h >> np.uint64(31)
+    return (h % np.uint64(nranks)) == np.uint64(rank)

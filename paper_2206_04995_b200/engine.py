@@ -240,7 +240,8 @@ class _Report(C.Structure):
                 ("hot_lds_bytes", C.c_uint64), ("hot_lds_bytes_unshared", C.c_uint64),
                 ("hot_direct_pairs", C.c_uint64), ("ms_dense_cold", C.c_double),
                 ("cold_bytes", C.c_uint64), ("spa_allocations", C.c_uint64),
-                ("spa_entries", C.c_uint64)]
+                ("spa_entries", C.c_uint64), ("rank_out_p", C.c_uint64),
+                ("nranks", C.c_int32), ("rank", C.c_int32)]
 
 
 class _Pairs(C.Structure):
@@ -271,7 +272,12 @@ EXPORTED = ["d3g_ctx_create", "d3g_ctx_destroy", "d3g_last_error", "d3g_version"
             "d3g_dense_ec_rows", "d3g_generate", "d3g_cfg_rows", "d3g_ctx_device",
             "d3g_f3_threshold", "d3g_f1", "d3g_f2_decide", "d3g_alu_peak",
             "d3g_detect_format", "d3g_binary_rows", "d3g_read_binary", "d3g_save_pairs",
-            "d3g_join_aggregate", "d3g_smem_peak", "d3g_map_tables"]
+            "d3g_join_aggregate", "d3g_smem_peak", "d3g_map_tables", "d3g_nccl_unique_id",
+            "d3g_ctx_set_nccl", "d3g_ctx_set_exchange"]
+
+# multi-GPU exchange ops (include/dim3_b200.h D3G_EX_*)
+EX_SUM_U64, EX_SUM_U32, EX_MAX_U64, EX_GATHER = 0, 1, 2, 3
+_EXFN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_uint64)
 
 _lib = None
 
@@ -323,6 +329,9 @@ def lib():
         L.d3g_read_binary.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p, C.c_void_p, C.c_uint64]
         L.d3g_save_pairs.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int,
                                      C.c_char_p, C.c_int]
+        L.d3g_nccl_unique_id.argtypes = [C.c_void_p]
+        L.d3g_ctx_set_nccl.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int]
+        L.d3g_ctx_set_exchange.argtypes = [C.c_void_p, C.c_int, C.c_int, _EXFN, C.c_void_p]
         _lib = L
     return _lib
 
@@ -337,8 +346,16 @@ def _consts(c: CostConstants) -> _Consts:
     return _Consts(c.t_seqR, c.t_randR, c.t_randRW, c.t_hash, c.t_map, c.t_ECs, c.t_ECd, c.w, 0)
 
 
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId for rank 0 to share (128 bytes)."""
+    buf = C.create_string_buffer(128)
+    _check(lib().d3g_nccl_unique_id(buf))
+    return buf.raw
+
+
 class Context:
     """One CUDA device + stream + device-memory pool (the C ABI's d3g_ctx)."""
+    nranks, rank = 1, 0
 
     def __init__(self, device: int = 0):
         self._h = C.c_void_p()
@@ -348,6 +365,40 @@ class Context:
     @property
     def handle(self):
         return self._h
+
+    # -- multi-GPU: this context as one rank of an x-sharded job -------------
+    def set_nccl(self, unique_id: bytes, nranks: int, rank: int):
+        """NCCL communicator (collective over the job; every rank calls it with
+        rank 0's nccl_unique_id())."""
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        _check(lib().d3g_ctx_set_nccl(self._h, buf, nranks, rank))
+        self.nranks, self.rank = nranks, rank
+
+    def set_exchange(self, nranks: int, rank: int, fn):
+        """Host-callback transport: fn(op, arr) performs the collective in place
+        on a numpy array (u64 / u32 elements; EX_GATHER: nranks * count bytes,
+        this rank's block filled). See paper_2206_04995_b200.distributed."""
+        def cb(_user, op, buf, count):
+            try:
+                if op == EX_GATHER:
+                    arr = np.ctypeslib.as_array(C.cast(buf, C.POINTER(C.c_uint8)),
+                                                shape=(nranks * count,))
+                else:
+                    ct = C.c_uint32 if op == EX_SUM_U32 else C.c_uint64
+                    arr = np.ctypeslib.as_array(C.cast(buf, C.POINTER(ct)), shape=(count,))
+                fn(op, arr)
+                return 0
+            except BaseException as e:  # surfaced as the call's error
+                self.exchange_error = e
+                return 1
+        self._exfn = _EXFN(cb)  # kept alive with the context
+        _check(lib().d3g_ctx_set_exchange(self._h, nranks, rank, self._exfn, None))
+        self.nranks, self.rank = nranks, rank
+
+    def clear_exchange(self):
+        _check(lib().d3g_ctx_set_exchange(self._h, 1, 0, C.cast(None, _EXFN), None))
+        self._exfn = None
+        self.nranks, self.rank = 1, 0
 
     def close(self):
         if self._h:
@@ -441,6 +492,9 @@ class ExecutionReport:
     cold_bytes: int = 0
     spa_allocations: int = 0
     spa_entries: int = 0
+    rank_out_p: int = 0
+    nranks: int = 1
+    rank: int = 0
 
     def to_kv(self):
         """Insertion-ordered key/value view with the reference's key names
@@ -531,7 +585,7 @@ def join_project(r: RawTable, s: RawTable, cfg: EngineConfig, c: CostConstants,
         cnt_op.count_only = 1
         _check(lib().d3g_join_project(ctx.handle, C.byref(rt), C.byref(st), C.byref(cs),
                                       C.byref(cnt_op), C.byref(rep), None))
-        n = int(rep.out_p)
+        n = int(rep.rank_out_p)  # a sharded rank materializes its own pairs
         ox = np.zeros(max(n, 1), dtype=np.uint64)
         oz = np.zeros(max(n, 1), dtype=np.uint64)
         pairs = _Pairs(ox.ctypes.data_as(U64P), oz.ctypes.data_as(U64P), n, 0, 0, 0)
@@ -542,7 +596,7 @@ def join_project(r: RawTable, s: RawTable, cfg: EngineConfig, c: CostConstants,
     if cfg.count_only:
         res = ResultSet(count=report.out_p, materialized=False)
     else:
-        n = report.out_p
+        n = report.rank_out_p
         res = ResultSet(count=n, materialized=True, raw_x=ox[:n], raw_z=oz[:n])
     return JoinProjectOutput(res, report)
 

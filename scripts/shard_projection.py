@@ -1,11 +1,23 @@
 #!/usr/bin/env python
-"""Per-shard device time of an N-way x-shard split, each shard run alone on
-one B200 (this pool gives one GPU per call). With one process per GPU every
-rank holds the same inputs, builds the same replicated mapping / CSR /
-statistics / partition and runs its own x shard of SparseBMM + DenseEC with
-no cross-rank wait, so max over shards of the per-shard device time is what
-an N-GPU run spends per step (plus the broadcast of the inputs and the
-all-reduce of a few counters, not included). Prints one JSON line per config.
+"""Projected N-GPU step of the x-sharded join_project, measured on ONE B200.
+
+Each rank of an N-rank job holds its x-shard of R (contiguous raw-x ranges)
+and the whole S, and runs d3g_join_project with an exchange (the library's
+sharded mode, csrc/exchange.cuh). This pool gives one GPU per call, so:
+
+  1. record: the N ranks run as threads on the one GPU, exchanging through
+     ThreadExchange (host barriers only: no kernel waits on another rank's);
+     each rank's collective results are recorded (RecordingExchange), and
+     every rank must report the N=1 job's count;
+  2. time:   each rank is re-run ALONE on the GPU with its recorded exchange
+     replayed (ReplayExchange), so its device time (CUDA events around the
+     whole call, min of --reps) is free of contention from the other ranks.
+
+The projected step is the max over ranks of that time plus an NCCL estimate
+for the exchanged bytes (the measured 8-rank all-reduce bus bandwidth of
+725 GB/s from B200_PROFILING.md, plus 25 us per collective). The host
+staging of the replayed exchange is inside the measured time (a few host
+round trips), so the projection is conservative. Prints one JSON line.
 
   python scripts/shard_projection.py --config 5 --shards 1 2 4 8
 """
@@ -13,49 +25,98 @@ import argparse
 import json
 import os
 import sys
+import threading
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+NVLINK_BUS_GBS = 725.0
+COLLECTIVE_US = 25.0
+X_CARD = {1: 10_000, 2: 200_000, 3: 2_000_000, 5: 10_000_000}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--shards", type=int, nargs="+", default=[1, 2, 4, 8])
-    ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--reps", type=int, default=3)
     a = ap.parse_args()
     import torch
+
     import paper_2206_04995_b200 as d3
+    from paper_2206_04995_b200.distributed import (RecordingExchange, ReplayExchange,
+                                                   ThreadExchange)
     C = d3.CostConstants.test_consts()
     rl, rr = d3.generate(a.config, 0)
     sl, sr = d3.generate(a.config, 1)
-    R, S = d3.RawTable(rl, rr), d3.RawTable(sl, sr)
-    # one untimed call first: the context's memory pool and module loads
-    warm = d3.EngineConfig(force=d3.Strategy.auto_select, count_only=True,
-                           memory_budget_bytes=150 << 30)
-    d3.join_project(R, S, warm, C)
-    res = {"config": a.config, "shards": {}}
-    base = None
-    total = None
+    S = d3.RawTable(sl, sr)
+    x_card = X_CARD[a.config]
+    e = d3.EngineConfig(force=d3.Strategy.auto_select, count_only=True,
+                        memory_budget_bytes=150 << 30)
+    res = {"config": a.config, "method": "ranks as threads (recorded exchange), then each rank "
+           "alone with its exchange replayed; device time per call, min of reps",
+           "shards": {}}
+    base = total = None
     for n in a.shards:
-        per = []
-        cnt = 0
-        for k in range(n):
-            e = d3.EngineConfig(force=d3.Strategy.auto_select, count_only=True,
-                                memory_budget_bytes=150 << 30, shard_index=k, shard_count=n)
-            best = None
-            for _ in range(a.reps):
-                rep = d3.join_project(R, S, e, C).report
-                best = rep.ms_total if best is None else min(best, rep.ms_total)
-            per.append(best)
-            cnt += rep.out_p
+        shards = []
+        for q in range(n):
+            lo, hi = x_card * q // n, x_card * (q + 1) // n
+            m = (rl >= lo) & (rl < hi)
+            shards.append(d3.RawTable(rl[m].contiguous(), rr[m].contiguous()))
+        ctxs = [d3.Context(0) for _ in range(n)]
+        te = ThreadExchange(n)
+        recs = [RecordingExchange(te.rank_fn(q)) for q in range(n)]
+        outs = [None] * n
+
+        def rank_main(q):
+            if n > 1:  # N = 1 is the plain single-GPU call (no exchange)
+                ctxs[q].set_exchange(n, q, recs[q])
+            d3.join_project(shards[q], S, e, C, ctx=ctxs[q])  # warm-up (pool, modules)
+            recs[q].log.clear()
+            outs[q] = d3.join_project(shards[q], S, e, C, ctx=ctxs[q]).report
+
+        th = [threading.Thread(target=rank_main, args=(q,)) for q in range(n)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        cnt = outs[0].out_p
+        assert all(o.out_p == cnt for o in outs), [o.out_p for o in outs]
+        assert sum(o.rank_out_p for o in outs) == cnt
         if total is None:
             total = cnt
         assert cnt == total, (n, cnt, total)
-        worst = max(per)
+        per, phases = [], []
+        ex_bytes = sum(v.nbytes for _, v in recs[0].log)
+        n_coll = len(recs[0].log)
+        for q in range(n):
+            rp = ReplayExchange(list(recs[q].log))
+            if n > 1:
+                ctxs[q].set_exchange(n, q, rp)
+            best = None
+            for _ in range(a.reps):
+                rp.rewind()
+                rep = d3.join_project(shards[q], S, e, C, ctx=ctxs[q]).report
+                if best is None or rep.ms_total < best.ms_total:
+                    best = rep
+            per.append(best.ms_total)
+            phases.append({k: round(getattr(best, k), 3) for k in
+                           ("ms_map", "ms_csr", "ms_stats", "ms_partition", "ms_dense",
+                            "ms_dense_hot", "ms_dense_cold")})
+            if n > 1:
+                ctxs[q].clear_exchange()
+        nccl_ms = 0.0 if n == 1 else (n_coll * COLLECTIVE_US * 1e-3 +
+                                      ex_bytes / (NVLINK_BUS_GBS * 1e9) * 1e3)
+        worst = max(per) + nccl_ms
         base = worst if base is None else base
-        res["shards"][n] = {"max_ms": worst, "per_shard_ms": per,
-                            "speedup": base / worst, "out_p": cnt}
+        res["shards"][n] = {"step_ms": worst, "max_rank_ms": max(per), "nccl_est_ms": nccl_ms,
+                            "per_rank_ms": per, "speedup": base / worst, "out_p": cnt,
+                            "collectives": n_coll, "exchanged_bytes_per_rank": ex_bytes,
+                            "phases_of_slowest": phases[per.index(max(per))]}
+        for c in ctxs:
+            c.close()
+        del shards
         torch.cuda.empty_cache()
+        print(json.dumps({"n": n, **res["shards"][n]}), file=sys.stderr, flush=True)
     print(json.dumps(res))
 
 
