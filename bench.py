@@ -158,6 +158,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="print each rank's (rank, world) and exit (launcher check, no GPU)")
     ap.add_argument("--cpu-frac", type=float, default=0.02,
                     help="x-slice fraction timed on the CPU reference")
     return ap.parse_args()
@@ -184,6 +186,27 @@ def relaunch_under_torchrun(n: int) -> int:
            "--master-addr", "127.0.0.1", "--master-port", str(port),
            os.path.abspath(__file__)] + sys.argv[1:]
     return subprocess.call(cmd, env=env)
+
+
+# raw x range of the natural-key configs (contiguous x shards); cfg4's random
+# u64 keys are sharded by a hash of the value
+X_CARD = {1: 10_000, 2: 200_000, 3: 2_000_000, 5: 10_000_000}
+
+
+def shard_mask_torch(x, rank: int, world: int, x_card=None):
+    """Rows of R owned by `rank` (paper_2206_04995_b200.distributed.shard_mask
+    on device tensors)."""
+    import torch
+    if x_card is not None:
+        lo, hi = x_card * rank // world, x_card * (rank + 1) // world
+        return (x >= lo) & (x < hi)
+    h = x.clone()  # mix64 in int64 arithmetic (wrapping multiplies)
+    h ^= (h >> 30) & ((1 << 34) - 1)
+    h *= torch.tensor(0xBF58476D1CE4E5B9 - (1 << 64), dtype=torch.int64, device=x.device)
+    h ^= (h >> 27) & ((1 << 37) - 1)
+    h *= torch.tensor(0x94D049BB133111EB - (1 << 64), dtype=torch.int64, device=x.device)
+    h ^= (h >> 31) & ((1 << 33) - 1)
+    return torch.remainder(h, world) == rank  # any disjoint split works
 
 
 def cpu_model() -> str:
@@ -337,6 +360,10 @@ def main():
     rank, world, local = dist_env()
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.dry_run:
+        print(json.dumps({"rank": rank, "world": world, "local_rank": local,
+                          "nccl_debug": os.environ.get("NCCL_DEBUG")}), flush=True)
+        return
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -350,21 +377,27 @@ def main():
     cfg_id = args.config
     ctx = d3.Context(local)
     n_rows = d3.cfg_rows(cfg_id)
-    # inputs: generated on rank 0's GPU, broadcast over NVLink (NCCL)
-    if rank == 0:
-        rl, rr = d3.generate(cfg_id, 0, ctx=ctx)
-        sl, sr = d3.generate(cfg_id, 1, ctx=ctx)
-    else:
-        rl, rr, sl, sr = (torch.empty(n_rows, dtype=torch.int64, device=dev) for _ in range(4))
+    # Inputs: the convention-G tables, generated on each rank's GPU (the
+    # generator is deterministic, so every rank holds the same S). With N
+    # ranks each keeps its x-shard of R -- contiguous raw-x ranges under
+    # natural keys, a hash of the raw value for cfg4's u64 keys -- and the
+    # library runs the sharded join over an NCCL communicator (exchange.cuh):
+    # only the f2 inputs and the tallies cross NVLink, never pairs.
+    rl, rr = d3.generate(cfg_id, 0, ctx=ctx)
+    sl, sr = d3.generate(cfg_id, 1, ctx=ctx)
     if world > 1:
-        for t in (rl, rr, sl, sr):
-            dist.broadcast(t, src=0)
+        uid = [d3.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx.set_nccl(uid[0], world, rank)
+        keep = shard_mask_torch(rl, rank, world, X_CARD.get(cfg_id))
+        rl, rr = rl[keep].contiguous(), rr[keep].contiguous()
+        del keep
     torch.cuda.synchronize(dev)
     R, S = d3.RawTable(rl, rr), d3.RawTable(sl, sr)
     n_tuples = 2 * n_rows
     consts = d3.CostConstants.test_consts()
     ecfg = d3.EngineConfig(force=d3.Strategy.auto_select, count_only=True,
-                           memory_budget_bytes=150 << 30, shard_index=rank, shard_count=world)
+                           memory_budget_bytes=150 << 30)
     flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device=dev)
 
     def one_step():
@@ -374,7 +407,8 @@ def main():
 
     for _ in range(max(args.warmup, 1)):
         rep = one_step().report
-    local_pairs = rep.out_p
+    local_pairs = rep.rank_out_p  # this rank's pairs (rep.out_p is the job's)
+    job_pairs = rep.out_p
 
     # ---- timed region -----------------------------------------------------
     if world > 1:
@@ -403,6 +437,7 @@ def main():
         sm = t.clone()
         dist.all_reduce(sm, op=dist.ReduceOp.SUM)
         dev_s, total_pairs, launches = mx[0].item(), int(sm[1].item()), int(sm[2].item())
+        assert total_pairs == job_pairs, (total_pairs, job_pairs)  # shards add up to the job
     else:
         total_pairs = local_pairs
     sec_per_step = dev_s / args.steps

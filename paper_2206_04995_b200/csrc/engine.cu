@@ -1235,11 +1235,12 @@ void build_dense_layout(Ctx& X, const d3g::DeviceCsr& rx, uint64_t max_mx,
                         const uint32_t* dR, DenseLayout& L, uint64_t xa = 0,
                         uint64_t xb = ~0ull, uint64_t dnnz_hint = ~0ull,
                         const RowSel* sel = nullptr, uint64_t z_rows = 0,
-                        bool stable_x = false) {
+                        bool stable_x = false, uint64_t dr_bound = 0) {
   using namespace d3g;
   // y ranked by dR descending: hottest witnesses first. dR(y) <= x_card
-  // bounds the key without a device round trip.
-  const uint64_t max_dr = rx.n_rows;
+  // bounds the key without a device round trip (sharded: dR is the job's,
+  // bounded by the job's x card, dr_bound).
+  const uint64_t max_dr = std::max<uint64_t>(rx.n_rows, dr_bound);
   order_y_by_degree(X, dR, y_card, max_dr, L.y_of_rank);
   L.y_rank = X.alloc<uint32_t>(y_card);
   D3G_LAUNCH(X, scatter_rank_kernel, grid_for(y_card, 256), 256, 0, L.y_of_rank.p, y_card,
@@ -2173,8 +2174,14 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
     // case, P/src/costmodel.cpp:375-409): per-y raw R counts summed over ranks
     const uint64_t yc = M.y_card;
     DBuf<uint32_t> cr = X.zeros<uint32_t>(yc), cs2 = X.zeros<uint32_t>(yc);
-    if (M.kept) D3G_LAUNCH(X, group_hist_kernel, grid_for(M.kept, 256), 256, 0, M.r_y, M.kept, cr.p);
-    if (NS) D3G_LAUNCH(X, group_hist_kernel, grid_for(NS, 256), 256, 0, M.s_y, NS, cs2.p);
+    // (hot y privatised in shared memory: Zipf-skewed y would serialise on
+    // plain global atomics)
+    if (M.kept)
+      D3G_LAUNCH(X, value_hist_kernel, grid_for(M.kept, 512, X.sm_count * 2), 512, 0, M.r_y,
+                 M.kept, cr.p, (uint32_t)yc);
+    if (NS)
+      D3G_LAUNCH(X, value_hist_kernel, grid_for(NS, 512, X.sm_count * 2), 512, 0, M.s_y, NS,
+                 cs2.p, (uint32_t)yc);
     ex_allreduce(X, *E, cr.p, yc, D3G_EX_SUM_U32);
     const unsigned gb = grid_for(yc, 1024, 296);
     DBuf<unsigned long long> parts = X.zeros<unsigned long long>(2ull * gb);
@@ -2296,13 +2303,15 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   if (n_dense > 0 && x_live > 0) {
     RowSel sel{&G.hmz, P.dtable.p, &P.table, fold ? 0 : 1, fold ? &row_sp : nullptr};
     build_dense_layout(X, rx, max_mx, hmx, sz_csr.row_ptr.p, sz_csr.col.p, nullptr, 0, max_mz,
-                       nullptr, y_card, dR.p, L, xa, xb, ~0ull, &sel, z_card, shard_count > 1);
+                       nullptr, y_card, dR.p, L, xa, xb, ~0ull, &sel, z_card, shard_count > 1,
+                       x_card_job);
   }
   DenseLayout Ls;
-  if (sparse_hot) {
+  if (sparse_hot && x_live > 0) {
     RowSel sel{&G.hmz, P.dtable.p, &P.table, 2, nullptr};
     build_dense_layout(X, rx, max_mx, hmx, sz_csr.row_ptr.p, sz_csr.col.p, nullptr, 0, max_mz,
-                       nullptr, y_card, dR.p, Ls, xa, xb, ~0ull, &sel, z_card, shard_count > 1);
+                       nullptr, y_card, dR.p, Ls, xa, xb, ~0ull, &sel, z_card, shard_count > 1,
+                       x_card_job);
   }
   T.mark();  // 6
 

@@ -207,3 +207,23 @@ def test_exchange_ops_gloo_and_threads():
             t.join()
         for r in range(n):
             assert tuple(got[r]) == _ops_expected(n)
+
+
+def test_bench_gpus_flag_launches_one_rank_per_gpu():
+    """`bench.py --gpus N` without torchrun re-launches itself with N ranks
+    (torch.distributed.run on 127.0.0.1); N = 1 stays a single process."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    for n in (1, 2):
+        p = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", str(n),
+                            "--dry-run"], capture_output=True, text=True, timeout=300, env=env)
+        assert p.returncode == 0, p.stderr[-2000:]
+        import re
+        lines = [json.loads(m) for m in re.findall(r"\{[^{}]*\}", p.stdout)]
+        assert sorted(d["rank"] for d in lines) == list(range(n))
+        assert all(d["world"] == n for d in lines)
+        if n > 1:
+            assert all(d["nccl_debug"] == "INFO" for d in lines)
