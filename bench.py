@@ -158,6 +158,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
+    ap.add_argument("--mode", default="count", choices=["count", "checksum", "materialize"],
+                    help="count-only (default), + (sum, xor) fingerprint of every pair, or the "
+                         "sorted, decoded pair list copied to the host")
     ap.add_argument("--dry-run", action="store_true",
                     help="print each rank's (rank, world) and exit (launcher check, no GPU)")
     ap.add_argument("--cpu-frac", type=float, default=0.02,
@@ -396,8 +399,8 @@ def main():
     R, S = d3.RawTable(rl, rr), d3.RawTable(sl, sr)
     n_tuples = 2 * n_rows
     consts = d3.CostConstants.test_consts()
-    ecfg = d3.EngineConfig(force=d3.Strategy.auto_select, count_only=True,
-                           memory_budget_bytes=150 << 30)
+    ecfg = d3.EngineConfig(force=d3.Strategy.auto_select, count_only=args.mode != "materialize",
+                           checksum=args.mode == "checksum", memory_budget_bytes=150 << 30)
     flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device=dev)
 
     def one_step():
@@ -600,7 +603,10 @@ def main():
             t0 = time.perf_counter()
             o = d3.join_project(Rh, Sh, ecfg, consts, ctx=ctx)
             ts.append(time.perf_counter() - t0)
-            h2d, d2h = o.report.h2d_bytes, o.report.d2h_bytes
+            # the materialized pairs (two u64 columns) come back with the result
+            h2d, d2h = o.report.h2d_bytes, o.report.d2h_bytes + 16 * int(o.result.raw_x.size
+                                                                       if o.result.materialized
+                                                                       else 0)
             assert o.report.out_p == total_pairs
         e2e = {"value": n_tuples / (sum(ts) / len(ts)), "unit": "tuples/s",
                "inputs": (("self-join: the pinned host relation is passed as both R and S "
@@ -634,7 +640,8 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec_per_step * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (convention G, generated on device)",
-        "config": {"workload": WORKLOADS[cfg_id], "count_only": True, "force": "auto",
+        "config": {"workload": WORKLOADS[cfg_id], "mode": args.mode,
+                   "count_only": args.mode != "materialize", "force": "auto",
                    "consts": "test_consts()", "parallelism": f"x-shard x{world}",
                    "l2": "256 MB buffer zeroed between steps (outside the timed device region); "
                          f"inputs {n_tuples * 8 / 1e6:.0f} MB"},

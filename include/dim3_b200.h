@@ -161,7 +161,9 @@ typedef struct {
 
 /* Materialized output: caller-owned host (or device, on_device != 0)
  * buffers of cap entries. On return n = pairs written, sorted by (x, z),
- * raw values in the caller's orientation. */
+ * raw values in the caller's orientation. x == NULL: the library keeps the
+ * result on the device (n is set) for d3g_take_pairs -- one pipeline pass
+ * without knowing the output size beforehand. */
 typedef struct {
   uint64_t* x;
   uint64_t* z;
@@ -207,6 +209,10 @@ void d3g_opts_default(d3g_opts* o);
 int d3g_join_project(d3g_ctx* ctx, const d3g_table* r, const d3g_table* s,
                      const d3g_consts* c, const d3g_opts* o, d3g_report* rep,
                      d3g_pairs* pairs /* NULL = count only */);
+/* Copies the first n pairs of the result the last d3g_join_project kept on
+ * the device (d3g_pairs.x == NULL) into x / z (host, or device when
+ * on_device) and releases it. */
+int d3g_take_pairs(d3g_ctx* ctx, uint64_t* x, uint64_t* z, uint64_t n, int on_device);
 
 /* build_csr over mapped code pairs (a = major when major_is_a). Host arrays
  * in, host CSR out (row_ptr/col must hold n_rows+1 / n entries). */

@@ -63,13 +63,13 @@ inline JoinProjectOutput join_project(const RawTable& r, const RawTable& s,
   if (cfg.count_only) {
     throw_status(d3g_join_project(context(), &R, &S, &k, &o, &rep, nullptr));
   } else {
-    d3g_opts oc = o;
-    oc.count_only = 1;  // size the output exactly, then materialize
-    throw_status(d3g_join_project(context(), &R, &S, &k, &oc, &rep, nullptr));
-    out.result.raw_x.ints.resize(rep.out_p);
-    out.result.raw_z.ints.resize(rep.out_p);
-    d3g_pairs p{out.result.raw_x.ints.data(), out.result.raw_z.ints.data(), rep.out_p, 0, 0, 0};
+    // one pipeline pass: the library holds the result, sized on return
+    d3g_pairs p{nullptr, nullptr, 0, 0, 0, 0};
     throw_status(d3g_join_project(context(), &R, &S, &k, &o, &rep, &p));
+    out.result.raw_x.ints.resize(p.n);
+    out.result.raw_z.ints.resize(p.n);
+    throw_status(d3g_take_pairs(context(), out.result.raw_x.ints.data(),
+                                out.result.raw_z.ints.data(), p.n, 0));
   }
   out.result.materialized = !cfg.count_only;
   out.result.count = rep.out_p;

@@ -292,6 +292,9 @@ struct Ctx {
   cudaEvent_t stage_ev[2] = {nullptr, nullptr};
   static constexpr size_t kStage = 64ull << 20;
   void copy_to_pageable(void* dst, const void* src, size_t bytes);
+  // a materialized result kept on the device for d3g_take_pairs
+  DBuf<uint64_t> held_x, held_z;
+  uint64_t held_n = 0;
   template <class T>
   void to_device(T* dst, const T* src, uint64_t n) {
     if (n == 0) return;

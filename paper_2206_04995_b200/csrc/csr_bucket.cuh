@@ -44,6 +44,15 @@ __global__ void max_u32_kernel(const uint32_t* __restrict__ v, uint64_t n,
   if (lane_id() == 0 && m) atomicMax(out, (unsigned long long)m);
 }
 
+// Latency, not bandwidth, bounds these passes (one dependent load -> atomic
+// chain per element): every thread keeps kCbIlp elements in flight, loaded
+// as 16-byte vectors when the column is aligned.
+constexpr int kCbIlp = 8;
+
+__device__ __forceinline__ bool aligned16(const void* p) {
+  return (reinterpret_cast<uintptr_t>(p) & 15) == 0;
+}
+
 // K1: bucket histogram (shared-memory privatised; n_buckets <= kCbMaxBuckets).
 __global__ void __launch_bounds__(kCbThreads)
 csr_bucket_hist_kernel(const uint32_t* __restrict__ maj, uint64_t n, int r, uint32_t n_buckets,
@@ -51,27 +60,62 @@ csr_bucket_hist_kernel(const uint32_t* __restrict__ maj, uint64_t n, int r, uint
   extern __shared__ unsigned int sh[];
   for (uint32_t i = threadIdx.x; i < n_buckets; i += kCbThreads) sh[i] = 0;
   __syncthreads();
-  const uint64_t stride = (uint64_t)gridDim.x * kCbThreads;
-  for (uint64_t i = (uint64_t)blockIdx.x * kCbThreads + threadIdx.x; i < n; i += stride)
-    atomicAdd(&sh[maj[i] >> r], 1u);
+  const uint64_t stride = (uint64_t)gridDim.x * kCbThreads * kCbIlp;
+  uint64_t i0 = ((uint64_t)blockIdx.x * kCbThreads + threadIdx.x) * kCbIlp;
+  if (aligned16(maj)) {
+    for (; i0 + kCbIlp <= n; i0 += stride) {
+      uint4 v[kCbIlp / 4];
+#pragma unroll
+      for (int k = 0; k < kCbIlp / 4; ++k) v[k] = reinterpret_cast<const uint4*>(maj + i0)[k];
+#pragma unroll
+      for (int k = 0; k < kCbIlp / 4; ++k) {
+        atomicAdd(&sh[v[k].x >> r], 1u);
+        atomicAdd(&sh[v[k].y >> r], 1u);
+        atomicAdd(&sh[v[k].z >> r], 1u);
+        atomicAdd(&sh[v[k].w >> r], 1u);
+      }
+    }
+  }
+  for (; i0 < n; i0 += stride)  // the tail (and unaligned columns)
+    for (uint64_t i = i0; i < i0 + kCbIlp && i < n; ++i) atomicAdd(&sh[maj[i] >> r], 1u);
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < n_buckets; i += kCbThreads)
     if (sh[i]) atomicAdd(&hist[i], sh[i]);
 }
 
 // K3: packed key into its bucket (order inside a bucket is irrelevant: K4
-// sorts). cursor[b] starts at the bucket's start.
+// sorts). cursor[b] starts at the bucket's start. kCbIlp independent
+// (load, atomic, store) chains per thread.
 __global__ void __launch_bounds__(kCbThreads)
 csr_bucket_scatter_kernel(const uint32_t* __restrict__ maj, const uint32_t* __restrict__ mnr,
                           uint64_t n, int r, int mb, unsigned long long* __restrict__ cursor,
                           uint32_t* __restrict__ packed) {
   const uint32_t rmask = (1u << r) - 1;
-  const uint64_t stride = (uint64_t)gridDim.x * kCbThreads;
-  for (uint64_t i = (uint64_t)blockIdx.x * kCbThreads + threadIdx.x; i < n; i += stride) {
-    const uint32_t a = maj[i], b = mnr[i];
-    const unsigned long long p = atomicAdd(&cursor[a >> r], 1ull);
-    packed[p] = ((a & rmask) << mb) | b;
+  const uint64_t stride = (uint64_t)gridDim.x * kCbThreads * kCbIlp;
+  uint64_t i0 = ((uint64_t)blockIdx.x * kCbThreads + threadIdx.x) * kCbIlp;
+  if (aligned16(maj) && aligned16(mnr)) {
+    for (; i0 + kCbIlp <= n; i0 += stride) {
+      uint32_t a[kCbIlp], b[kCbIlp];
+#pragma unroll
+      for (int k = 0; k < kCbIlp / 4; ++k) {
+        const uint4 va = reinterpret_cast<const uint4*>(maj + i0)[k];
+        const uint4 vb = reinterpret_cast<const uint4*>(mnr + i0)[k];
+        a[4 * k] = va.x, a[4 * k + 1] = va.y, a[4 * k + 2] = va.z, a[4 * k + 3] = va.w;
+        b[4 * k] = vb.x, b[4 * k + 1] = vb.y, b[4 * k + 2] = vb.z, b[4 * k + 3] = vb.w;
+      }
+      unsigned long long p[kCbIlp];
+#pragma unroll
+      for (int k = 0; k < kCbIlp; ++k) p[k] = atomicAdd(&cursor[a[k] >> r], 1ull);
+#pragma unroll
+      for (int k = 0; k < kCbIlp; ++k) packed[p[k]] = ((a[k] & rmask) << mb) | b[k];
+    }
   }
+  for (; i0 < n; i0 += stride)
+    for (uint64_t i = i0; i < i0 + kCbIlp && i < n; ++i) {
+      const uint32_t a = maj[i], b = mnr[i];
+      const unsigned long long p = atomicAdd(&cursor[a >> r], 1ull);
+      packed[p] = ((a & rmask) << mb) | b;
+    }
 }
 
 // In-place exclusive scan of a[0..n) in shared memory by the whole CTA
@@ -169,12 +213,30 @@ csr_bucket_build_kernel(const uint32_t* __restrict__ packed,
   const uint32_t rows = (uint32_t)((n_rows - row0) < (1ull << r) ? (n_rows - row0) : (1ull << r));
   const uint32_t mmask = mb >= 32 ? 0xffffffffu : ((1u << mb) - 1);
   for (uint32_t i = threadIdx.x; i <= rows; i += kCbThreads) roff[i] = 0;
-  __syncthreads();
-  for (uint32_t i = threadIdx.x; i < cnt; i += kCbThreads) {
-    const uint32_t k = packed[s0 + i];
-    keys[i] = k;
-    atomicAdd(&roff[k >> mb], 1u);
+  // the bucket's keys into shared memory: 16-byte loads from the first
+  // aligned key on, all issued before any is consumed
+  const uint32_t head = (uint32_t)((4 - (s0 & 3)) & 3) < cnt ? (uint32_t)((4 - (s0 & 3)) & 3) : cnt;
+  const uint32_t nv = (cnt - head) / 4;
+  const uint4* pv = reinterpret_cast<const uint4*>(packed + s0 + head);
+  for (uint32_t v0 = threadIdx.x; v0 < nv; v0 += kCbThreads * 4) {
+    uint4 q[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (v0 + u * kCbThreads < nv) q[u] = pv[v0 + u * kCbThreads];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (v0 + u * kCbThreads < nv) {
+        const uint32_t i = head + 4 * (v0 + u * kCbThreads);
+        keys[i] = q[u].x;
+        keys[i + 1] = q[u].y;
+        keys[i + 2] = q[u].z;
+        keys[i + 3] = q[u].w;
+      }
   }
+  for (uint32_t i = threadIdx.x; i < head; i += kCbThreads) keys[i] = packed[s0 + i];
+  for (uint32_t i = head + 4 * nv + threadIdx.x; i < cnt; i += kCbThreads) keys[i] = packed[s0 + i];
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < cnt; i += kCbThreads) atomicAdd(&roff[keys[i] >> mb], 1u);
   __syncthreads();
   cta_exclusive_scan(roff, rows + 1, ws);  // roff[rows] = cnt
   for (uint32_t i = threadIdx.x; i < rows; i += kCbThreads) rcur[i] = roff[i];

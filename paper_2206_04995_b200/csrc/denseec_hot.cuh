@@ -1313,6 +1313,9 @@ dense_hot_jt_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
         const uint32_t hits = __popc(acc.x) + __popc(acc.y) + __popc(acc.z) + __popc(acc.w);
         cnt += hits;
         if (cw >> 31) csp += hits;
+        // emission: one warp-aggregated reservation per row step (all lanes
+        // are converged here: they share the row, each holds one x group)
+        unsigned long long slot = kMode == kModeEmit ? warp_reserve(em, hits) : 0ull;
         if (kMode != kModeCount && hits) {
           const uint32_t zc = p.dl_z[kTrie ? perm[i] : i];
           const uint32_t ws[4] = {acc.x, acc.y, acc.z, acc.w};
@@ -1328,11 +1331,7 @@ dense_hot_jt_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
                 sum += h;
                 xr ^= h;
               } else {
-                const unsigned long long idx = atomicAdd(em.cursor, 1ull);
-                if (idx < em.cap) {
-                  em.x[idx] = xc;
-                  em.z[idx] = zc;
-                }
+                emit_at(em, slot++, xc, zc);
               }
             }
           }
@@ -1458,32 +1457,32 @@ dense_cold_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
           }
         }
 #pragma unroll
-        for (int h = 0; h < kColdUnroll; ++h) {
-          if (tf[h] >= total) continue;
+        for (int h = 0; h < kColdUnroll; ++h) {  // converged: no per-lane exits
+          bool fresh = false;
           const uint32_t zl = zc[h] - zbase;
-          const bool hot = ((a0.x & b0[h].x) | (a0.y & b0[h].y) | (a0.z & b0[h].z) |
-                            (a0.w & b0[h].w) | (a1.x & b1[h].x) | (a1.y & b1[h].y) |
-                            (a1.z & b1[h].z) | (a1.w & b1[h].w)) != 0;
-          if (hot) continue;
-          const uint32_t bit = 1u << (zl & 31);
-          const uint32_t old = atomicOr(&bm[zl >> 5], bit);
-          touched = true;
-          if (old & bit) continue;
-          ++cnt;
-          if (row_sp && row_sp[zbase + zl]) ++csp;
-          if (kMode != kModeCount) {
-            const uint32_t zcode = dl_z[zbase + zl];
+          if (tf[h] < total) {
+            const bool hot = ((a0.x & b0[h].x) | (a0.y & b0[h].y) | (a0.z & b0[h].z) |
+                              (a0.w & b0[h].w) | (a1.x & b1[h].x) | (a1.y & b1[h].y) |
+                              (a1.z & b1[h].z) | (a1.w & b1[h].w)) != 0;
+            if (!hot) {
+              const uint32_t bit = 1u << (zl & 31);
+              const uint32_t old = atomicOr(&bm[zl >> 5], bit);
+              touched = true;
+              fresh = (old & bit) == 0;
+            }
+          }
+          if (fresh) {
+            ++cnt;
+            if (row_sp && row_sp[zbase + zl]) ++csp;
             if (kMode == kModeChecksum) {
-              const uint64_t hh = dec.hash(x, zcode);
+              const uint64_t hh = dec.hash(x, dl_z[zbase + zl]);
               sum += hh;
               xr ^= hh;
-            } else {
-              const unsigned long long idx = atomicAdd(em.cursor, 1ull);
-              if (idx < em.cap) {
-                em.x[idx] = x;
-                em.z[idx] = zcode;
-              }
             }
+          }
+          if (kMode == kModeEmit) {  // warp-aggregated reservation
+            const unsigned long long slot = warp_reserve(em, fresh ? 1u : 0u);
+            if (fresh) emit_at(em, slot, x, dl_z[zbase + zl]);
           }
         }
       }
@@ -1659,10 +1658,16 @@ dense_cold_hash_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
       ncand += xcand;  // each x's stream counted once, in the tier that finishes it
     }
     if (inserted && (kMode != kModeCount || row_sp)) {
-      for (uint32_t i = lane; i < kCHSlots; i += 32) {
+      for (uint32_t i = lane; i < kCHSlots; i += 32) {  // uniform trip count
         const uint32_t zl = tab[i];
-        if (zl != kCHEmpty) {
-          if (kMode != kModeCount && !over) cold_account<kMode>(x, dl_z[zl], dec, em, sum, xr);
+        const bool live = zl != kCHEmpty;
+        if (kMode == kModeEmit) {  // warp-aggregated reservation
+          const unsigned long long slot = warp_reserve(em, live && !over ? 1u : 0u);
+          if (live && !over) emit_at(em, slot, x, dl_z[zl]);
+        } else if (kMode == kModeChecksum && live && !over) {
+          cold_account<kMode>(x, dl_z[zl], dec, em, sum, xr);
+        }
+        if (live) {
           if (row_sp && !over && row_sp[zl]) ++csp;
           tab[i] = kCHEmpty;
         }
@@ -1982,13 +1987,17 @@ dense_cold_cta_kernel(const uint32_t* __restrict__ over_x, const unsigned int* _
       ncand += xcand;
       if (threadIdx.x == 0) cnt += s_ins;
     }
-    for (uint32_t i = threadIdx.x; i < kCCSlots; i += kCCThreads) {
+    for (uint32_t i = threadIdx.x; i < kCCSlots; i += kCCThreads) {  // uniform trip count
       const uint32_t zl = cctab[i];
-      if (zl != kCHEmpty) {
-        if (!over) {
-          if (kMode != kModeCount) cold_account<kMode>(x, dl_z[zl], dec, em, sum, xr);
-          if (row_sp && row_sp[zl]) ++csp;
-        }
+      const bool live = zl != kCHEmpty;
+      if (kMode == kModeEmit) {
+        const unsigned long long slot = warp_reserve(em, live && !over ? 1u : 0u);
+        if (live && !over) emit_at(em, slot, x, dl_z[zl]);
+      } else if (kMode == kModeChecksum && live && !over) {
+        cold_account<kMode>(x, dl_z[zl], dec, em, sum, xr);
+      }
+      if (live) {
+        if (!over && row_sp && row_sp[zl]) ++csp;
         cctab[i] = kCHEmpty;
       }
     }

@@ -1334,23 +1334,17 @@ void build_dense_layout(Ctx& X, const d3g::DeviceCsr& rx, uint64_t max_mx,
 // Materialized output: emit code pairs (emit runs the producing kernels in
 // kModeEmit), order them by (x, z) code, decode through the dictionaries
 // (identity when rev is null) in the caller's orientation, copy out.
+void finish_pairs(Ctx& X, DBuf<uint32_t>& ex, DBuf<uint32_t>& ez, uint64_t total,
+                  const uint64_t* rev_x, const uint64_t* rev_z, bool swapped, d3g_pairs* pairs,
+                  d3g_report* rep, uint64_t x_card, uint64_t z_card);
+
 void materialize_pairs(Ctx& X, uint64_t total, const std::function<void(d3g::Emit)>& emit,
                        const uint64_t* rev_x, const uint64_t* rev_z, bool swapped,
                        d3g_pairs* pairs, d3g_report* rep, uint64_t x_card, uint64_t z_card) {
   using namespace d3g;
-  if (pairs->cap < total)
+  if (pairs->x && pairs->cap < total)
     throw ResourceError("output buffer holds " + std::to_string(pairs->cap) + " pairs, need " +
                         std::to_string(total));
-  const bool trace = std::getenv("D3G_TRACE") != nullptr;
-  auto tp = std::chrono::steady_clock::now();
-  auto tr = [&](const char* what) {
-    if (!trace) return;
-    X.sync();
-    auto t1 = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "[materialize] %-8s %8.3f ms\n", what,
-                 std::chrono::duration<double, std::milli>(t1 - tp).count());
-    tp = t1;
-  };
   DBuf<uint32_t> ex = X.alloc<uint32_t>(total), ez = X.alloc<uint32_t>(total);
   DBuf<unsigned long long> cur = X.zeros<unsigned long long>(1);
   emit(Emit{ex.p, ez.p, cur.p, total});
@@ -1362,6 +1356,27 @@ void materialize_pairs(Ctx& X, uint64_t total, const std::function<void(d3g::Emi
       throw CudaError("materialize: emitted " + std::to_string(emitted) + " pairs, counted " +
                       std::to_string(total));
   }
+  finish_pairs(X, ex, ez, total, rev_x, rev_z, swapped, pairs, rep, x_card, z_card);
+}
+
+// Emitted code pairs -> sorted by (x, z), decoded to raw values in the
+// caller's orientation, copied to the caller's buffers -- or, when the
+// caller passed no buffer (pairs->x == NULL), kept on the device for
+// d3g_take_pairs (one pipeline pass whatever the output size).
+void finish_pairs(Ctx& X, DBuf<uint32_t>& ex, DBuf<uint32_t>& ez, uint64_t total,
+                  const uint64_t* rev_x, const uint64_t* rev_z, bool swapped, d3g_pairs* pairs,
+                  d3g_report* rep, uint64_t x_card, uint64_t z_card) {
+  using namespace d3g;
+  const bool trace = std::getenv("D3G_TRACE") != nullptr;
+  auto tp = std::chrono::steady_clock::now();
+  auto tr = [&](const char* what) {
+    if (!trace) return;
+    X.sync();
+    auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[materialize] %-8s %8.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t1 - tp).count());
+    tp = t1;
+  };
   tr("emit");
   DBuf<uint64_t> keys = X.alloc<uint64_t>(total);
   DBuf<uint32_t> idx = X.alloc<uint32_t>(total);
@@ -1383,7 +1398,8 @@ void materialize_pairs(Ctx& X, uint64_t total, const std::function<void(d3g::Emi
   DBuf<uint64_t> ox, oz;
   uint64_t* dox = pairs->x;
   uint64_t* doz = pairs->z;
-  if (!pairs->on_device) {
+  const bool held = pairs->x == nullptr;  // library-owned result
+  if (!pairs->on_device || held) {
     ox = X.alloc<uint64_t>(total);
     oz = X.alloc<uint64_t>(total);
     dox = ox.p;
@@ -1393,7 +1409,13 @@ void materialize_pairs(Ctx& X, uint64_t total, const std::function<void(d3g::Emi
     D3G_LAUNCH(X, decode_pairs_kernel, grid_for(total, 256), 256, 0, sx2.p, sz2.p, total, rev_x,
                rev_z, swapped ? 1 : 0, dox, doz);
   tr("decode");
-  if (!pairs->on_device && total) {
+  if (held) {
+    ex.reset();
+    ez.reset();
+    X.held_x = std::move(ox);
+    X.held_z = std::move(oz);
+    X.held_n = total;
+  } else if (!pairs->on_device && total) {
     X.copy_to_pageable(pairs->x, ox.p, total * 8);
     X.copy_to_pageable(pairs->z, oz.p, total * 8);
   }
@@ -2354,6 +2376,30 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
     rep->dense_probes_done = dc.probes;
     rep->dense_row_bitmaps_built = dc.bitmaps;
   }
+  // Materialized calls emit in ONE kernel pass when the join size (an upper
+  // bound on the distinct pairs) fits the memory budget: no counting pass
+  // first. Otherwise (or with the fingerprint requested) count, then emit.
+  bool direct = false;
+  uint64_t direct_cap = 0;
+  if (materialize && !o->checksum && std::getenv("D3G_COUNT_FIRST") == nullptr) {
+    const uint64_t bound = std::min<uint64_t>(rep->out_j, x_live * (n_dense + n_sparse));
+    const uint64_t need = bound * 48;  // emit + sort + decode buffers
+    if (bound < (1ull << 32) && (X.budget == 0 || X.live_bytes + need <= X.budget)) {
+      direct = true;
+      direct_cap = bound;
+    }
+  }
+  DBuf<uint32_t> dex, dez;
+  DBuf<unsigned long long> dcur;
+  Emit em_run = no_emit;
+  int kmode = mode;
+  if (direct) {
+    dex = X.alloc<uint32_t>(direct_cap);
+    dez = X.alloc<uint32_t>(direct_cap);
+    dcur = X.zeros<unsigned long long>(1);
+    em_run = Emit{dex.p, dez.p, dcur.p, direct_cap};
+    kmode = kModeEmit;
+  }
   KernelOut ks, kd;
   const uint64_t s_lo = Ls.n_live * shard_index / shard_count,
                  s_hi = Ls.n_live * (shard_index + 1) / shard_count;
@@ -2362,9 +2408,9 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
                   Ls.y_of_rank.p, dR.p, x_card, x_lo, x_hi, Ls.dnnz, nullptr,
                   Ls.n_dense == sz_csr.live_rows ? G.dS.p : nullptr};
   if (sparse_hot)
-    run_dense_hot(X, dsi, dec, mode, no_emit, ks);
+    run_dense_hot(X, dsi, dec, kmode, em_run, ks);
   else if (!fold)
-    run_sparse(X, si, dec, mode, no_emit, ks);
+    run_sparse(X, si, dec, kmode, em_run, ks);
   T.mark();  // 7
   uint64_t pos_lo = L.n_live * shard_index / shard_count,
            pos_hi = L.n_live * (shard_index + 1) / shard_count;
@@ -2372,7 +2418,7 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
                  L.dl_col.p, L.dl_z.p, L.n_dense, L.max_group_nnz, pos_lo, pos_hi,
                  L.y_of_rank.p, dR.p, x_card, x_lo, x_hi, L.dnnz, row_sp.p,
                  L.n_dense == sz_csr.live_rows ? G.dS.p : nullptr};
-  run_dense(X, di, dec, mode, no_emit, kd);
+  run_dense(X, di, dec, kmode, em_run, kd);
   T.mark();  // 8
   if (fold) {  // the folded sparse rows' pairs, counted apart inside the engine
     ks.count = kd.count_sp;
@@ -2424,7 +2470,17 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   }
 
   // 9. materialization (decode, engine.cpp:502-529)
-  if (materialize)
+  if (materialize && direct) {
+    const uint64_t emitted = X.scalar(dcur.p);
+    if (emitted != rep->rank_out_p)
+      throw CudaError("materialize: emitted " + std::to_string(emitted) + " pairs, counted " +
+                      std::to_string(rep->rank_out_p));
+    if (pairs->x && pairs->cap < emitted)
+      throw ResourceError("output buffer holds " + std::to_string(pairs->cap) + " pairs, need " +
+                          std::to_string(emitted));
+    finish_pairs(X, dex, dez, emitted, rev_or_null(D.x), rev_or_null(D.z), swapped, pairs, rep,
+                 x_card, z_card);
+  } else if (materialize)
     materialize_pairs(X, rep->rank_out_p, [&](Emit em) {
       KernelOut tmp;
       if (sparse_hot)
@@ -2768,10 +2824,34 @@ int d3g_ctx_set_exchange(d3g_ctx* ctx, int nranks, int rank, d3g_exchange_fn fn,
   });
 }
 
+int d3g_take_pairs(d3g_ctx* ctx, uint64_t* x, uint64_t* z, uint64_t n, int on_device) {
+  return guarded([&] {
+    d3g::Ctx& X = ctx->c;
+    D3G_CUDA(cudaSetDevice(X.device));
+    if (n > X.held_n) throw d3g::ConfigError("d3g_take_pairs: only " + std::to_string(X.held_n) +
+                                             " pairs are held");
+    if (n) {
+      if (on_device) {
+        D3G_CUDA(cudaMemcpyAsync(x, X.held_x.p, n * 8, cudaMemcpyDeviceToDevice, X.stream));
+        D3G_CUDA(cudaMemcpyAsync(z, X.held_z.p, n * 8, cudaMemcpyDeviceToDevice, X.stream));
+        X.sync();
+      } else {
+        X.copy_to_pageable(x, X.held_x.p, n * 8);
+        X.copy_to_pageable(z, X.held_z.p, n * 8);
+      }
+    }
+    X.held_x.reset();
+    X.held_z.reset();
+    X.held_n = 0;
+  });
+}
+
 void d3g_ctx_destroy(d3g_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->c.device);
   cudaStreamSynchronize(ctx->c.stream);
+  ctx->c.held_x.reset();
+  ctx->c.held_z.reset();
   if (ctx->c.pinned) cudaFreeHost(ctx->c.pinned);
   if (ctx->c.defer_host) cudaFreeHost(ctx->c.defer_host);
   ctx->c.release_cache();

@@ -37,6 +37,33 @@ struct Emit {
 
 enum : int { kModeCount = 0, kModeChecksum = 1, kModeEmit = 2 };
 
+// Warp-aggregated output reservation: every lane of a converged warp passes
+// the number of pairs it will write; one atomicAdd reserves the warp's run
+// and each lane gets its first slot (exclusive warp scan), so the output
+// cursor sees one atomic per warp step instead of one per pair.
+__device__ __forceinline__ unsigned long long warp_reserve(const Emit& em, uint32_t n) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t incl = n;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= (uint32_t)o) incl += u;
+  }
+  const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+  unsigned long long base = 0;
+  if (lane == 0 && total) base = atomicAdd(em.cursor, (unsigned long long)total);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  return base + incl - n;
+}
+
+__device__ __forceinline__ void emit_at(const Emit& em, unsigned long long slot, uint32_t x,
+                                        uint32_t z) {
+  if (slot < em.cap) {
+    em.x[slot] = x;
+    em.z[slot] = z;
+  }
+}
+
 // Optional candidate filter used by DenseEC's cold residual pass: a candidate
 // (x, zi) is skipped when the hot masks of x and of dense row zi intersect
 // (that pair was already produced by the hot bit-sliced pass).

@@ -273,7 +273,7 @@ EXPORTED = ["d3g_ctx_create", "d3g_ctx_destroy", "d3g_last_error", "d3g_version"
             "d3g_f3_threshold", "d3g_f1", "d3g_f2_decide", "d3g_alu_peak",
             "d3g_detect_format", "d3g_binary_rows", "d3g_read_binary", "d3g_save_pairs",
             "d3g_join_aggregate", "d3g_smem_peak", "d3g_map_tables", "d3g_nccl_unique_id",
-            "d3g_ctx_set_nccl", "d3g_ctx_set_exchange"]
+            "d3g_ctx_set_nccl", "d3g_ctx_set_exchange", "d3g_take_pairs"]
 
 # multi-GPU exchange ops (include/dim3_b200.h D3G_EX_*)
 EX_SUM_U64, EX_SUM_U32, EX_MAX_U64, EX_GATHER = 0, 1, 2, 3
@@ -329,6 +329,7 @@ def lib():
         L.d3g_read_binary.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p, C.c_void_p, C.c_uint64]
         L.d3g_save_pairs.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int,
                                      C.c_char_p, C.c_int]
+        L.d3g_take_pairs.argtypes = [C.c_void_p, U64P, U64P, C.c_uint64, C.c_int]
         L.d3g_nccl_unique_id.argtypes = [C.c_void_p]
         L.d3g_ctx_set_nccl.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int]
         L.d3g_ctx_set_exchange.argtypes = [C.c_void_p, C.c_int, C.c_int, _EXFN, C.c_void_p]
@@ -580,18 +581,18 @@ def join_project(r: RawTable, s: RawTable, cfg: EngineConfig, c: CostConstants,
     pairs_p = None
     ox = oz = None
     if not cfg.count_only:
-        # first pass counts, second materializes into an exactly sized buffer
-        cnt_op = _opts(cfg)
-        cnt_op.count_only = 1
-        _check(lib().d3g_join_project(ctx.handle, C.byref(rt), C.byref(st), C.byref(cs),
-                                      C.byref(cnt_op), C.byref(rep), None))
-        n = int(rep.rank_out_p)  # a sharded rank materializes its own pairs
-        ox = np.zeros(max(n, 1), dtype=np.uint64)
-        oz = np.zeros(max(n, 1), dtype=np.uint64)
-        pairs = _Pairs(ox.ctypes.data_as(U64P), oz.ctypes.data_as(U64P), n, 0, 0, 0)
+        # one pipeline pass: the library keeps the sorted, decoded pairs on the
+        # device (d3g_pairs.x == NULL) and they are copied out once sized
+        pairs = _Pairs(None, None, 0, 0, 0, 0)
         pairs_p = C.byref(pairs)
     _check(lib().d3g_join_project(ctx.handle, C.byref(rt), C.byref(st), C.byref(cs), C.byref(op),
                                   C.byref(rep), pairs_p))
+    if not cfg.count_only:
+        n = int(pairs.n)  # a sharded rank materializes its own pairs
+        ox = np.zeros(max(n, 1), dtype=np.uint64)
+        oz = np.zeros(max(n, 1), dtype=np.uint64)
+        _check(lib().d3g_take_pairs(ctx.handle, ox.ctypes.data_as(U64P), oz.ctypes.data_as(U64P),
+                                    n, 0))
     report = _to_report(rep)
     if cfg.count_only:
         res = ResultSet(count=report.out_p, materialized=False)
