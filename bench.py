@@ -227,7 +227,7 @@ def cpu_model() -> str:
 _X_ROWS: dict = {}
 
 
-def cpu_reference_sample(cfg: int, frac: float, threads: int, tables=None):
+def cpu_reference_sample(cfg: int, frac: float, threads: int, tables=None, cfg5_slices=(100, 1000)):
     """Reference prep on the whole job + reference kernels on an x-slice,
     extrapolated linearly in x. Returns (seconds_full_job_estimate, detail)."""
     from oracle import oracle as O
@@ -257,7 +257,8 @@ def cpu_reference_sample(cfg: int, frac: float, threads: int, tables=None):
         # the MARGINAL per-x cost, the estimate most favourable to the reference.
         import numpy as np
         x_card, runs = 10_000_000, []
-        for xs in (100, 1000):
+        xa, xb = cfg5_slices
+        for xs in (xa, xb):
             keep = np.asarray(r.left) < xs
             rs = O.Table(np.ascontiguousarray(np.asarray(r.left)[keep]),
                          np.ascontiguousarray(np.asarray(r.right)[keep]))
@@ -266,10 +267,10 @@ def cpu_reference_sample(cfg: int, frac: float, threads: int, tables=None):
             runs.append(((d["ms_estimate"] + d["ms_map"] + d["ms_csr"] + d["ms_partition"]) * 1e-3,
                          (d["ms_sparse"] + d["ms_dense"]) * 1e-3, d["out_p"]))
         (p1, k1, _), (p2, k2, o2) = runs
-        marginal = max(k2 - k1, 0.0) / 900.0
-        est = p2 + k1 + marginal * (x_card - 100)
-        return est, {"slices": "cfg5", "x_slice": "x<100 and x<1000 (marginal per-x cost)",
-                     "x_rows": x_card,
+        marginal = max(k2 - k1, 0.0) / (xb - xa)
+        est = p2 + k1 + marginal * (x_card - xa)
+        return est, {"slices": "cfg5", "x_slice": f"x<{xa} and x<{xb} (marginal per-x cost)",
+                     "x_rows": x_card, "slice_lo": xa, "slice_hi": xb,
                      "sec_prep": p2, "sec_kernels": k2, "sec_kernels_x100": k1,
                      "est_full_s": est, "slice_out_p": o2}
     x_rows = _X_ROWS.get(cfg)
@@ -285,11 +286,12 @@ def cpu_reference_sample(cfg: int, frac: float, threads: int, tables=None):
 
 def _sample_text(detail):
     if detail.get("slices") == "cfg5":
-        return ("reference join_project(auto) on R restricted to x<100 and to x<1000 against the "
-                "full S (its engine swaps; the 1.25 TB panel of the whole job cannot be built): "
-                f"prep {detail['sec_prep']:.1f}s once + the marginal per-x kernel cost "
-                f"({(detail['sec_kernels'] - detail['sec_kernels_x100']) / 900 * 1e3:.2f} ms/x) "
-                "x 1e7 x values")
+        xa, xb = detail["slice_lo"], detail["slice_hi"]
+        return (f"reference join_project(auto) on R restricted to x<{xa} and to x<{xb} against "
+                "the full S (its engine swaps; the 1.25 TB panel of the whole job cannot be "
+                f"built): prep {detail['sec_prep']:.1f}s once + the marginal per-x kernel cost "
+                f"({(detail['sec_kernels'] - detail['sec_kernels_x100']) / (xb - xa) * 1e3:.2f} "
+                "ms/x) x 1e7 x values, extrapolated")
     if detail.get("strategy") == "classical":
         return ("whole job through the reference's join_project(auto) -> f1 gate -> "
                 "hash_join_dedup")
@@ -322,7 +324,7 @@ def run_reference(args):
     value = n_tuples / sec
     # the same reference at threads=1 (one bounded sample)
     t1_frac = args.cpu_frac / 4
-    est1, det1 = cpu_reference_sample(cfg, t1_frac, 1, (r, s))
+    est1, det1 = cpu_reference_sample(cfg, t1_frac, 1, (r, s), cfg5_slices=(20, 200))
     detail["threads_1"] = {"est_full_job_s": est1, "tuples_per_s": n_tuples / est1,
                            "sample": _sample_text(det1), "speedup_all_threads": est1 / sec}
     if cfg in CLASSICAL_CFGS:  # also the forced-hybrid reference time

@@ -33,6 +33,7 @@ constexpr uint32_t kCbCap = 12288;        // packed keys per bucket in smem (2 C
 constexpr uint32_t kCbTarget = 7168;      // expected tuples per bucket (at most)
 constexpr uint32_t kCbMaxRowsLog = 11;    // <= 2048 rows per bucket
 constexpr uint32_t kCbMaxBuckets = 32768; // privatised histogram (128 KB)
+constexpr uint32_t kCbThreadRow = 48;     // rows up to this length: one thread each
 
 __global__ void max_u32_kernel(const uint32_t* __restrict__ v, uint64_t n,
                                unsigned long long* __restrict__ out) {
@@ -246,17 +247,42 @@ csr_bucket_build_kernel(const uint32_t* __restrict__ packed,
     rowd[atomicAdd(&rcur[k >> mb], 1u)] = k & mmask;
   }
   __syncthreads();
-  // per-row sort + unique, one warp per row; kept counts into rcur
+  // per-row sort + unique; kept counts into rcur. Short rows (the common
+  // case: ~20 entries) by one thread each -- an insertion sort in shared
+  // memory costs ~len^2/4 moves, far fewer issued instructions than a warp
+  // bitonic network per row; rows past kCbThreadRow entries by a warp.
   const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
   uint32_t mx = 0, live = 0;
+  for (uint32_t q = threadIdx.x; q < rows; q += kCbThreads) {
+    const uint32_t base = roff[q], len = roff[q + 1] - base;
+    if (len > kCbThreadRow) continue;
+    uint32_t* a = rowd + base;
+    for (uint32_t i = 1; i < len; ++i) {
+      const uint32_t v = a[i];
+      uint32_t j = i;
+      while (j > 0 && a[j - 1] > v) {
+        a[j] = a[j - 1];
+        --j;
+      }
+      a[j] = v;
+    }
+    uint32_t kept = len ? 1u : 0u;
+    for (uint32_t i = 1; i < len; ++i)
+      if (a[i] != a[kept - 1]) a[kept++] = a[i];
+    rcur[q] = kept;
+    deg[row0 + q] = kept;
+    mx = kept > mx ? kept : mx;
+    live += kept > 0;
+  }
   for (uint32_t q = w; q < rows; q += kCbThreads / 32) {
     const uint32_t base = roff[q], len = roff[q + 1] - base;
-    const uint32_t kept = len ? cb_sort_row(rowd, keys, base, len) : 0u;
+    if (len <= kCbThreadRow) continue;  // warp-uniform
+    const uint32_t kept = cb_sort_row(rowd, keys, base, len);
     if (lane == 0) {
       rcur[q] = kept;
       deg[row0 + q] = kept;
       mx = kept > mx ? kept : mx;
-      live += kept > 0;
+      live += 1;
     }
   }
   __syncthreads();

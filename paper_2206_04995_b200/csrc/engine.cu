@@ -1113,6 +1113,26 @@ __global__ void decode_pairs_kernel(const uint32_t* __restrict__ xc, const uint3
   }
 }
 
+// Rows of a pair CSR (caller x code -> sorted caller z codes) to decoded
+// raw pairs, 8 lanes per row (rev == null: identity codes).
+__global__ void csr_decode_kernel(const uint64_t* __restrict__ row_ptr,
+                                  const uint32_t* __restrict__ col, uint64_t n_rows,
+                                  const uint64_t* __restrict__ rev_a,
+                                  const uint64_t* __restrict__ rev_b, uint64_t* __restrict__ ox,
+                                  uint64_t* __restrict__ oz) {
+  const uint32_t sl = threadIdx.x & 7;
+  for (uint64_t r = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3; r < n_rows;
+       r += ((uint64_t)gridDim.x * blockDim.x) >> 3) {
+    const uint64_t b = row_ptr[r], e = row_ptr[r + 1];
+    if (b == e) continue;
+    const uint64_t a = rev_a ? rev_a[r] : r;
+    for (uint64_t k = b + sl; k < e; k += 8) {
+      ox[k] = a;
+      oz[k] = rev_b ? rev_b[col[k]] : col[k];
+    }
+  }
+}
+
 __global__ void pair_key_kernel(const uint32_t* __restrict__ xc, const uint32_t* __restrict__ zc,
                                 uint64_t n, int swapped, int lo_bits, uint64_t* __restrict__ keys,
                                 uint32_t* __restrict__ idx) {
@@ -1378,6 +1398,48 @@ void finish_pairs(Ctx& X, DBuf<uint32_t>& ex, DBuf<uint32_t>& ez, uint64_t total
     tp = t1;
   };
   tr("emit");
+  DBuf<uint64_t> ox, oz;
+  uint64_t* dox = pairs->x;
+  uint64_t* doz = pairs->z;
+  const bool held = pairs->x == nullptr;  // library-owned result
+  auto out_buffers = [&] {
+    if (!pairs->on_device || held) {
+      ox = X.alloc<uint64_t>(total);
+      oz = X.alloc<uint64_t>(total);
+      dox = ox.p;
+      doz = oz.p;
+    }
+  };
+  // (x, z) order through the bucketed CSR build (the pairs are distinct, so
+  // rows of caller-x codes with sorted caller-z codes ARE the sorted list):
+  // one scatter + shared-memory sorts instead of a 6-8 pass radix sort
+  {
+    const uint64_t a_card = swapped ? z_card : x_card, b_card = swapped ? x_card : z_card;
+    DeviceCsr g;
+    if (total && std::getenv("D3G_PAIR_RADIX") == nullptr &&
+        build_csr_bucketed(X, swapped ? ez.p : ex.p, swapped ? ex.p : ez.p, total, a_card, b_card,
+                           g, false)) {
+      if (g.nnz != total) throw CudaError("materialize: duplicate pairs emitted");
+      tr("sort");
+      ex.reset();
+      ez.reset();
+      out_buffers();
+      D3G_LAUNCH(X, csr_decode_kernel, grid_for(a_card * 8, 256), 256, 0, g.row_ptr.p, g.col.p,
+                 a_card, swapped ? rev_z : rev_x, swapped ? rev_x : rev_z, dox, doz);
+      tr("decode");
+      if (held) {
+        X.held_x = std::move(ox);
+        X.held_z = std::move(oz);
+        X.held_n = total;
+      } else if (!pairs->on_device) {
+        X.copy_to_pageable(pairs->x, ox.p, total * 8);
+        X.copy_to_pageable(pairs->z, oz.p, total * 8);
+      }
+      tr("d2h");
+      pairs->n = total;
+      return;
+    }
+  }
   DBuf<uint64_t> keys = X.alloc<uint64_t>(total);
   DBuf<uint32_t> idx = X.alloc<uint32_t>(total);
   if (total) {
@@ -1395,16 +1457,7 @@ void finish_pairs(Ctx& X, DBuf<uint32_t>& ex, DBuf<uint32_t>& ez, uint64_t total
   if (total)
     D3G_LAUNCH(X, permute_pairs_kernel, grid_for(total, 256), 256, 0, idx.p, total, ex.p, ez.p,
                sx2.p, sz2.p);
-  DBuf<uint64_t> ox, oz;
-  uint64_t* dox = pairs->x;
-  uint64_t* doz = pairs->z;
-  const bool held = pairs->x == nullptr;  // library-owned result
-  if (!pairs->on_device || held) {
-    ox = X.alloc<uint64_t>(total);
-    oz = X.alloc<uint64_t>(total);
-    dox = ox.p;
-    doz = oz.p;
-  }
+  out_buffers();
   if (total)
     D3G_LAUNCH(X, decode_pairs_kernel, grid_for(total, 256), 256, 0, sx2.p, sz2.p, total, rev_x,
                rev_z, swapped ? 1 : 0, dox, doz);
@@ -1538,6 +1591,8 @@ void classical_impl(Ctx& X, const uint64_t* Rl, const uint64_t* Rr, uint64_t NR,
   tr("probe");
   rep->pairs_classical = h.count;
   rep->out_p = h.count;
+  rep->rank_out_p = h.count;
+  rep->nranks = 1;
   rep->checksum_sum = h.sum;
   rep->checksum_xor = h.xr;
   if (materialize) {

@@ -597,7 +597,7 @@ def join_project(r: RawTable, s: RawTable, cfg: EngineConfig, c: CostConstants,
     if cfg.count_only:
         res = ResultSet(count=report.out_p, materialized=False)
     else:
-        n = report.rank_out_p
+        n = int(pairs.n)
         res = ResultSet(count=n, materialized=True, raw_x=ox[:n], raw_z=oz[:n])
     return JoinProjectOutput(res, report)
 
