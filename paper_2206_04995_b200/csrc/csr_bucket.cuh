@@ -33,7 +33,7 @@ constexpr uint32_t kCbCap = 12288;        // packed keys per bucket in smem (2 C
 constexpr uint32_t kCbTarget = 7168;      // expected tuples per bucket (at most)
 constexpr uint32_t kCbMaxRowsLog = 11;    // <= 2048 rows per bucket
 constexpr uint32_t kCbMaxBuckets = 32768; // privatised histogram (128 KB)
-constexpr uint32_t kCbThreadRow = 48;     // rows up to this length: one thread each
+constexpr uint32_t kCbThreadRow = 0;      // rows up to this length: one thread each (measured slower than the warp sort on cfg5: 0 = off)
 
 __global__ void max_u32_kernel(const uint32_t* __restrict__ v, uint64_t n,
                                unsigned long long* __restrict__ out) {
@@ -117,6 +117,98 @@ csr_bucket_scatter_kernel(const uint32_t* __restrict__ maj, const uint32_t* __re
       const unsigned long long p = atomicAdd(&cursor[a >> r], 1ull);
       packed[p] = ((a & rmask) << mb) | b;
     }
+}
+
+// Two-level alternative to K3 for many buckets: after an 8-bit bucketing pass
+// on the high bucket bits (prims.cuh bucket_pass_u32: tile-local ranks, runs
+// written per digit, no atomics), every 4096-pair tile lies inside one region
+// of <= 256 consecutive buckets. The tile is ranked by bucket in shared
+// memory, each (tile, bucket) run is reserved with ONE global atomic, and the
+// packed keys are written out in runs -- instead of one returning global
+// atomic per pair (K3 is bound by L2 atomic throughput: ~45 G/s).
+constexpr int kRbThreads = 1024;
+constexpr int kRbPer = 4;
+constexpr int kRbTile = kRbThreads * kRbPer;
+
+struct RbTile {
+  unsigned long long start;  // first pair of the tile (region-ordered arrays)
+  uint32_t len;              // <= kRbTile
+  uint32_t region;           // high bucket bits (bucket >> sub_bits)
+};
+
+__global__ void __launch_bounds__(kRbThreads)
+csr_region_scatter_kernel(const uint32_t* __restrict__ maj, const uint32_t* __restrict__ mnr,
+                          const RbTile* __restrict__ tiles, int r, int mb, int sub_bits,
+                          unsigned long long* __restrict__ cursor,
+                          uint32_t* __restrict__ packed) {
+  __shared__ uint32_t s_cnt[256], s_loc[256];
+  __shared__ unsigned long long s_glb[256];
+  __shared__ uint32_t s_out[kRbTile];
+  const uint32_t t = threadIdx.x;
+  const RbTile tl = tiles[blockIdx.x];
+  const uint32_t smask = (1u << sub_bits) - 1, rmask = (1u << r) - 1;
+  if (t < 256) s_cnt[t] = 0;
+  __syncthreads();
+  uint32_t key[kRbPer], sub[kRbPer], rk[kRbPer];
+#pragma unroll
+  for (int q = 0; q < kRbPer; ++q) {
+    const uint32_t i = (uint32_t)q * kRbThreads + t;
+    if (i < tl.len) {
+      const uint32_t a = maj[tl.start + i], b = mnr[tl.start + i];
+      sub[q] = (a >> r) & smask;
+      key[q] = ((a & rmask) << mb) | b;
+      rk[q] = atomicAdd(&s_cnt[sub[q]], 1u);
+    }
+  }
+  __syncthreads();
+  if (t < 32) {  // exclusive scan of the 256 sub-bucket counts, 8 per lane
+    uint32_t c[8], sum = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      c[j] = s_cnt[t * 8 + j];
+      sum += c[j];
+    }
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (t >= (uint32_t)o) incl += u;
+    }
+    uint32_t run = incl - sum;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      s_loc[t * 8 + j] = run;
+      run += c[j];
+    }
+  }
+  // one global reservation per (tile, bucket)
+  if (t < 256 && s_cnt[t])
+    s_glb[t] = atomicAdd(&cursor[((uint64_t)tl.region << sub_bits) | t],
+                         (unsigned long long)s_cnt[t]);
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < kRbPer; ++q) {
+    const uint32_t i = (uint32_t)q * kRbThreads + t;
+    if (i < tl.len) s_out[s_loc[sub[q]] + rk[q]] = key[q];
+  }
+  __syncthreads();
+  // the staged tile out in runs: position p belongs to the last sub-bucket
+  // whose local start is <= p (empty sub-buckets start where the next does)
+  for (uint32_t p = t; p < tl.len; p += kRbThreads) {
+    uint32_t lo = 0, hi = 256;
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (s_loc[mid] <= p) lo = mid; else hi = mid;
+    }
+    packed[s_glb[lo] + (p - s_loc[lo])] = s_out[p];
+  }
+}
+
+__global__ void gather_region_starts_kernel(const uint64_t* __restrict__ offs, uint32_t n_tiles,
+                                            uint64_t* __restrict__ out /* [257] */) {
+  const uint32_t d = threadIdx.x;
+  if (d < 256) out[d] = offs[(uint64_t)d * n_tiles];
+  if (d == 256) out[256] = offs[(uint64_t)256 * n_tiles];
 }
 
 // In-place exclusive scan of a[0..n) in shared memory by the whole CTA
@@ -352,8 +444,42 @@ inline bool build_csr_bucketed(Ctx& ctx, const uint32_t* maj, const uint32_t* mn
   DBuf<unsigned long long> cursor = ctx.alloc<unsigned long long>(nb);
   D3G_CUDA(cudaMemcpyAsync(cursor.p, bstart.p, (size_t)nb * 8, cudaMemcpyDeviceToDevice, ctx.stream));
   DBuf<uint32_t> packed = ctx.alloc<uint32_t>(n);
-  D3G_LAUNCH(ctx, csr_bucket_scatter_kernel, grid_for(n, kCbThreads, ctx.sm_count * 8), kCbThreads, 0,
-             maj, mnr, n, r, mb, cursor.p, packed.p);
+  const char* sc = std::getenv("D3G_CSR_SCATTER");
+  if (sc && std::strcmp(sc, "atomic") == 0) {  // K3: one global atomic per pair (comparison)
+    D3G_LAUNCH(ctx, csr_bucket_scatter_kernel, grid_for(n, kCbThreads, ctx.sm_count * 8),
+               kCbThreads, 0, maj, mnr, n, r, mb, cursor.p, packed.p);
+  } else {
+    // two levels: an 8-bit bucketing pass on the high bucket bits, then the
+    // region-local tile scatter with one atomic per (tile, bucket)
+    const int bucket_bits = std::max(1, bits_for(nb - 1));
+    const int sub_bits = std::max(0, bucket_bits - 8);
+    DBuf<uint32_t> am = ctx.alloc<uint32_t>(n), av = ctx.alloc<uint32_t>(n);
+    const uint32_t n_tiles = (uint32_t)((n + kBucketTile - 1) / kBucketTile);
+    {
+      DBuf<uint32_t> hist = ctx.alloc<uint32_t>((uint64_t)256 * n_tiles);
+      DBuf<uint64_t> offs = ctx.alloc<uint64_t>((uint64_t)256 * n_tiles + 1);
+      D3G_LAUNCH(ctx, bucket_hist_kernel, n_tiles, kBucketThreads, 0, maj, n, r + sub_bits,
+                 n_tiles, hist.p);
+      exclusive_scan<uint32_t>(ctx, hist.p, (uint64_t)256 * n_tiles, offs.p);
+      D3G_LAUNCH(ctx, bucket_scatter_kernel, n_tiles, kBucketThreads, 0, maj, mnr, n,
+                 r + sub_bits, n_tiles, offs.p, am.p, av.p);
+      DBuf<uint64_t> rs = ctx.alloc<uint64_t>(257);
+      D3G_LAUNCH(ctx, gather_region_starts_kernel, 1, 288, 0, offs.p, n_tiles, rs.p);
+      uint64_t h[257];
+      ctx.to_host(h, rs.p, 257);
+      std::vector<RbTile> tv;
+      tv.reserve(n / kRbTile + 257);
+      for (uint32_t d = 0; d < 256; ++d)
+        for (uint64_t p = h[d]; p < h[d + 1]; p += kRbTile)
+          tv.push_back(RbTile{p, (uint32_t)std::min<uint64_t>(kRbTile, h[d + 1] - p), d});
+      DBuf<RbTile> tiles = ctx.alloc<RbTile>(tv.size());
+      ctx.to_device(tiles.p, tv.data(), tv.size());
+      if (!tv.empty())
+        D3G_LAUNCH(ctx, csr_region_scatter_kernel, (unsigned)tv.size(), kRbThreads, 0, am.p,
+                   av.p, tiles.p, r, mb, sub_bits, cursor.p, packed.p);
+      ctx.sync();  // tv (host) is the source of the async tile copy above
+    }
+  }
   cursor.reset();
   DBuf<uint32_t> uniq = ctx.alloc<uint32_t>(n);
   DBuf<uint32_t> deg = ctx.alloc<uint32_t>(n_rows);

@@ -1660,15 +1660,16 @@ dense_cold_hash_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
     if (inserted && (kMode != kModeCount || row_sp)) {
       for (uint32_t i = lane; i < kCHSlots; i += 32) {  // uniform trip count
         const uint32_t zl = tab[i];
-        const bool live = zl != kCHEmpty;
         if (kMode == kModeEmit) {  // warp-aggregated reservation
-          const unsigned long long slot = warp_reserve(em, live && !over ? 1u : 0u);
-          if (live && !over) emit_at(em, slot, x, dl_z[zl]);
-        } else if (kMode == kModeChecksum && live && !over) {
-          cold_account<kMode>(x, dl_z[zl], dec, em, sum, xr);
+          const bool e = zl != kCHEmpty && !over;
+          const unsigned long long slot = warp_reserve(em, e ? 1u : 0u);
+          if (e) emit_at(em, slot, x, dl_z[zl]);
         }
-        if (live) {
-          if (row_sp && !over && row_sp[zl]) ++csp;
+        if (zl != kCHEmpty) {
+          if (!over) {
+            if (kMode == kModeChecksum) cold_account<kMode>(x, dl_z[zl], dec, em, sum, xr);
+            if (row_sp && row_sp[zl]) ++csp;
+          }
           tab[i] = kCHEmpty;
         }
       }
@@ -1989,15 +1990,16 @@ dense_cold_cta_kernel(const uint32_t* __restrict__ over_x, const unsigned int* _
     }
     for (uint32_t i = threadIdx.x; i < kCCSlots; i += kCCThreads) {  // uniform trip count
       const uint32_t zl = cctab[i];
-      const bool live = zl != kCHEmpty;
-      if (kMode == kModeEmit) {
-        const unsigned long long slot = warp_reserve(em, live && !over ? 1u : 0u);
-        if (live && !over) emit_at(em, slot, x, dl_z[zl]);
-      } else if (kMode == kModeChecksum && live && !over) {
-        cold_account<kMode>(x, dl_z[zl], dec, em, sum, xr);
+      if (kMode == kModeEmit) {  // warp-aggregated reservation
+        const bool e = zl != kCHEmpty && !over;
+        const unsigned long long slot = warp_reserve(em, e ? 1u : 0u);
+        if (e) emit_at(em, slot, x, dl_z[zl]);
       }
-      if (live) {
-        if (!over && row_sp && row_sp[zl]) ++csp;
+      if (zl != kCHEmpty) {
+        if (!over) {
+          if (kMode == kModeChecksum) cold_account<kMode>(x, dl_z[zl], dec, em, sum, xr);
+          if (row_sp && row_sp[zl]) ++csp;
+        }
         cctab[i] = kCHEmpty;
       }
     }
