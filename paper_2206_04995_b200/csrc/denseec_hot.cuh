@@ -211,7 +211,9 @@ __global__ void cold_count_kernel(const uint64_t* __restrict__ dl_ptr,
 }
 
 // With sig != null the row's 256-bit hot signature (hz, kw == 4) is stored
-// inline next to each entry (2 x uint4 per entry).
+// inline next to each entry (2 x uint4 per entry). The scatter itself writes
+// only the 4-byte row ids (the atomic cursor bounds it); cold_sig_gather_kernel
+// then fills the signatures in one coalesced pass (sig == null here).
 __global__ void cold_scatter_kernel(const uint64_t* __restrict__ dl_ptr,
                                     const uint32_t* __restrict__ dl_col, uint64_t n_dense,
                                     uint32_t K, const uint32_t* __restrict__ y_of_rank,
@@ -245,6 +247,18 @@ __global__ void cold_scatter_kernel(const uint64_t* __restrict__ dl_ptr,
           if (sig) st256(sig + 2 * pos, s0, s1);
         }
     }
+  }
+}
+
+// The cold CSR's inline signatures, entry order: ch[k] = hz[ccol[k]] (a
+// coalesced 32-byte write per entry, the hz rows gathered).
+__global__ void cold_sig_gather_kernel(const uint32_t* __restrict__ ccol, uint64_t cnnz,
+                                       const uint4* __restrict__ hz4, uint4* __restrict__ ch) {
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cnnz;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    uint4 a, b;
+    ld256(hz4 + 2 * (uint64_t)ccol[k], a, b);
+    st256(ch + 2 * k, a, b);
   }
 }
 

@@ -960,9 +960,12 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     DBuf<uint4> ch;  // inline hot signatures (cold kernels only)
     if (cold_kernel_ok) ch = X.alloc<uint4>(2 * cnnz);
     D3G_LAUNCH(X, cold_scatter_kernel, grid_for(D * 8, 256), 256, 0, in.dl_ptr, in.dl_col, D, K,
-               in.y_of_rank, cptr.p, cc.p, ccol.p, cold_kernel_ok ? ch.p : nullptr, Y, part_rows,
-               parts, reinterpret_cast<const uint64_t*>(hz.p), kw, var_bits);
+               in.y_of_rank, cptr.p, cc.p, ccol.p, nullptr, Y, part_rows, parts,
+               reinterpret_cast<const uint64_t*>(hz.p), kw, var_bits);
     cc.reset();
+    if (cold_kernel_ok && cnnz)  // the inline signatures, one coalesced pass
+      D3G_LAUNCH(X, cold_sig_gather_kernel, grid_for(cnnz, 256), 256, 0, ccol.p, cnnz,
+                 reinterpret_cast<const uint4*>(hz.p), ch.p);
     if (cold_kernel_ok) {
       DBuf<unsigned int> next = X.zeros<unsigned int>(1);
       Tally* tc = tallies.p + 1;
