@@ -285,52 +285,6 @@ __device__ __forceinline__ uint32_t cb_sort_row(uint32_t* data, uint32_t* scratc
   return written;
 }
 
-// Sort + unique of a row of len <= 32 by a HALF warp: 16 lanes x 2 elements
-// (element e * 16 + l16), so one warp sorts two rows per bitonic network --
-// half the issued instructions of a 32-lane network per row (rows are ~20
-// long on the BASELINE configs). Both halves must call it (len 0 = idle).
-// In place; returns the kept count (uniform within the half).
-__device__ __forceinline__ uint32_t half_sort_row32(uint32_t* data, uint32_t base, uint32_t len) {
-  const uint32_t lane = lane_id(), l16 = lane & 15, half = lane >> 4;
-  uint32_t v0 = l16 < len ? data[base + l16] : 0xffffffffu;
-  uint32_t v1 = l16 + 16 < len ? data[base + l16 + 16] : 0xffffffffu;
-#pragma unroll
-  for (uint32_t k = 2; k <= 32; k <<= 1) {
-#pragma unroll
-    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-      if (j == 16) {  // k == 32: elements l16 and 16 + l16, ascending
-        const uint32_t mn = v0 < v1 ? v0 : v1, mx = v0 < v1 ? v1 : v0;
-        v0 = mn;
-        v1 = mx;
-      } else {
-        const uint32_t o0 = __shfl_xor_sync(0xffffffffu, v0, j);
-        const uint32_t o1 = __shfl_xor_sync(0xffffffffu, v1, j);
-        const bool lower = (l16 & j) == 0;
-        const bool up0 = (l16 & k) == 0, up1 = ((16 + l16) & k) == 0;
-        const uint32_t mn0 = v0 < o0 ? v0 : o0, mx0 = v0 < o0 ? o0 : v0;
-        const uint32_t mn1 = v1 < o1 ? v1 : o1, mx1 = v1 < o1 ? o1 : v1;
-        v0 = (lower == up0) ? mn0 : mx0;
-        v1 = (lower == up1) ? mn1 : mx1;
-      }
-    }
-  }
-  const uint32_t lt = (1u << l16) - 1;
-  // element i = e * 16 + l16; predecessor of (0, 0) is none, of (1, 0) is (0, 15)
-  uint32_t p0 = __shfl_up_sync(0xffffffffu, v0, 1, 16);
-  uint32_t p1 = __shfl_up_sync(0xffffffffu, v1, 1, 16);
-  const uint32_t last0 = __shfl_sync(0xffffffffu, v0, 15, 16);
-  if (l16 == 0) p1 = last0;
-  const bool k0 = l16 < len && (l16 == 0 || v0 != p0);
-  const bool k1 = l16 + 16 < len && v1 != p1;
-  const uint32_t m0 = (__ballot_sync(0xffffffffu, k0) >> (16 * half)) & 0xffffu;
-  const uint32_t m1 = (__ballot_sync(0xffffffffu, k1) >> (16 * half)) & 0xffffu;
-  __syncwarp();
-  if (k0) data[base + __popc(m0 & lt)] = v0;
-  if (k1) data[base + __popc(m0) + __popc(m1 & lt)] = v1;
-  __syncwarp();
-  return __popc(m0) + __popc(m1);
-}
-
 // K4: one CTA per bucket. Shared memory: keys[kCbCap] | rows[kCbCap] |
 // roff[2^r + 1] | rcur[2^r] | ws[kCbThreads / 32 + 1].
 __global__ void __launch_bounds__(kCbThreads)
@@ -421,7 +375,7 @@ csr_bucket_build_kernel(const uint32_t* __restrict__ packed,
       len = roff[q + 1] - base;
     }
     const bool mine = q < rows && len > kCbThreadRow && len <= 32;
-    const uint32_t kept = half_sort_row32(rowd, base, mine ? len : 0u);
+    const uint32_t kept = half_sort_row32(rowd, base, mine ? len : 0u, true);
     if (mine && (lane & 15) == 0) {
       rcur[q] = kept;
       deg[row0 + q] = kept;

@@ -127,6 +127,53 @@ __device__ __forceinline__ uint32_t half_sort_row(uint32_t* __restrict__ data, u
   return __popc(m);
 }
 
+// Sort (+ unique) of a row of len <= 32 by a HALF warp: 16 lanes x 2 elements
+// (element e * 16 + l16), so one warp sorts two rows per bitonic network --
+// half the issued instructions of a 32-lane network per row (rows are ~20
+// long on the BASELINE configs). Both halves must call it (len 0 = idle).
+// In place; returns the kept count (uniform within the half).
+__device__ __forceinline__ uint32_t half_sort_row32(uint32_t* data, uint64_t base, uint32_t len,
+                                                  bool unique) {
+  const uint32_t lane = lane_id(), l16 = lane & 15, half = lane >> 4;
+  uint32_t v0 = l16 < len ? data[base + l16] : 0xffffffffu;
+  uint32_t v1 = l16 + 16 < len ? data[base + l16 + 16] : 0xffffffffu;
+#pragma unroll
+  for (uint32_t k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      if (j == 16) {  // k == 32: elements l16 and 16 + l16, ascending
+        const uint32_t mn = v0 < v1 ? v0 : v1, mx = v0 < v1 ? v1 : v0;
+        v0 = mn;
+        v1 = mx;
+      } else {
+        const uint32_t o0 = __shfl_xor_sync(0xffffffffu, v0, j);
+        const uint32_t o1 = __shfl_xor_sync(0xffffffffu, v1, j);
+        const bool lower = (l16 & j) == 0;
+        const bool up0 = (l16 & k) == 0, up1 = ((16 + l16) & k) == 0;
+        const uint32_t mn0 = v0 < o0 ? v0 : o0, mx0 = v0 < o0 ? o0 : v0;
+        const uint32_t mn1 = v1 < o1 ? v1 : o1, mx1 = v1 < o1 ? o1 : v1;
+        v0 = (lower == up0) ? mn0 : mx0;
+        v1 = (lower == up1) ? mn1 : mx1;
+      }
+    }
+  }
+  const uint32_t lt = (1u << l16) - 1;
+  // element i = e * 16 + l16; predecessor of (0, 0) is none, of (1, 0) is (0, 15)
+  uint32_t p0 = __shfl_up_sync(0xffffffffu, v0, 1, 16);
+  uint32_t p1 = __shfl_up_sync(0xffffffffu, v1, 1, 16);
+  const uint32_t last0 = __shfl_sync(0xffffffffu, v0, 15, 16);
+  if (l16 == 0) p1 = last0;
+  const bool k0 = l16 < len && (!unique || l16 == 0 || v0 != p0);
+  const bool k1 = l16 + 16 < len && (!unique || v1 != p1);
+  const uint32_t m0 = (__ballot_sync(0xffffffffu, k0) >> (16 * half)) & 0xffffu;
+  const uint32_t m1 = (__ballot_sync(0xffffffffu, k1) >> (16 * half)) & 0xffffu;
+  __syncwarp();
+  if (k0) data[base + __popc(m0 & lt)] = v0;
+  if (k1) data[base + __popc(m0) + __popc(m1 & lt)] = v1;
+  __syncwarp();
+  return __popc(m0) + __popc(m1);
+}
+
 // One warp per row for rows of length <= 128 (two rows per warp, one per
 // half-warp, when both hold <= 16 entries); longer rows are appended to
 // long_rows (any order) for row_sort_long_kernel.
@@ -141,11 +188,12 @@ __global__ void row_sort_small_kernel(uint32_t* __restrict__ data, const uint64_
     const uint64_t b0 = off[r2], b1 = off[r2 + 1];
     const uint64_t b2 = r2 + 1 < n_rows ? off[r2 + 2] : b1;
     const uint32_t l0 = (uint32_t)(b1 - b0), l1 = (uint32_t)(b2 - b1);
-    if (l0 <= 16 && l1 <= 16) {  // both rows in one pass, a half-warp each
+    if (l0 <= 32 && l1 <= 32) {  // both rows in one pass, a half-warp each
       const uint32_t h = lane >> 4;
       const uint64_t b = h ? b1 : b0;
       const uint32_t len = h ? l1 : l0;
-      const uint32_t k = half_sort_row(data, b, len, unique);  // both halves converge
+      const uint32_t k = (l0 <= 16 && l1 <= 16) ? half_sort_row(data, b, len, unique)
+                                                : half_sort_row32(data, b, len, unique);
       if ((lane & 15) == 0 && r2 + h < n_rows) kept[r2 + h] = k;
       continue;
     }
