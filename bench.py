@@ -54,11 +54,16 @@ L2_BYTES = 126 * 1024 * 1024
 def _ncu_dram_bytes(cfg: int, which: str = "hotpass"):
     """dram__bytes_read.sum + dram__bytes_write.sum of one step's launches of
     the kernel(s) in the committed `ncu --set full` capture of this config
-    (profiles/r01_cfg<N>_ncu_<which>.csv: the hot pass, or the cold-pass
-    kernels summed), or None."""
+    (profiles/r02_ or r01_cfg<N>_ncu_<which>.csv: the hot pass, or the
+    cold-pass kernels summed), or None."""
     import csv
-    path = os.path.join(ROOT, "profiles", f"r01_cfg{cfg}_ncu_{which}.csv")
-    if not os.path.exists(path):
+    path = None
+    for rnd in ("r02", "r01"):  # the newest capture of this config
+        p = os.path.join(ROOT, "profiles", f"{rnd}_cfg{cfg}_ncu_{which}.csv")
+        if os.path.exists(p):
+            path = p
+            break
+    if path is None:
         return None
     rows = list(csv.reader(open(path)))
     hdr, units = rows[0], rows[1]
