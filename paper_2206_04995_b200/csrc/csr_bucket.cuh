@@ -434,8 +434,11 @@ inline bool build_csr_bucketed(Ctx& ctx, const uint32_t* maj, const uint32_t* mn
   if ((!force && n < (1ull << 16)) || n == 0 || n >= (1ull << 32) || n_rows == 0) return false;
   const int mb = std::max(1, bits_for(n_cols ? n_cols - 1 : 0));
   if (mb > 31) return false;
-  // rows per bucket: ~kCbTarget tuples, packed key within 32 bits
+  // rows per bucket: ~kCbTarget tuples, packed key within 32 bits. Long
+  // average rows (> 64 tuples) go to the scatter path, whose CTA-wide
+  // shared-memory sorts suit them (the bucket kernel sorts rows by warps)
   const double per_row = (double)n / (double)n_rows;
+  if (!force && per_row > 64.0) return false;
   int r = 0;
   while (r < (int)kCbMaxRowsLog && r + 1 + mb <= 32 && per_row * (double)(1ull << (r + 1)) <= kCbTarget)
     ++r;
