@@ -21,6 +21,10 @@
 
 #include "sparsebmm.cuh"
 
+#ifndef D3G_COMPARISON_KERNELS
+#define D3G_COMPARISON_KERNELS 0
+#endif
+
 namespace d3g {
 
 constexpr int kHotThreads = 1024;
@@ -456,6 +460,11 @@ __global__ void hot_rec_kernel(const uint64_t* __restrict__ dl_ptr,
   }
 }
 
+// top-rank subset table of the hot kernels (see dense_hot_tab_kernel)
+constexpr uint32_t kTabBits = 7;
+constexpr uint32_t kTabRows = 1u << kTabBits;
+
+#if D3G_COMPARISON_KERNELS  // record / guarded-step table kernels: measured comparisons
 template <int kMode>
 __global__ void __launch_bounds__(kHotThreads, 1)
 dense_hot_rec_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
@@ -599,8 +608,6 @@ dense_hot_rec_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
 // costs ONE LDS.128 for its whole top-rank subset plus one per further hot
 // rank. Records list only the ranks >= kTabBits; the subset mask rides in bits
 // 24.. of the count word.
-constexpr uint32_t kTabBits = 7;
-constexpr uint32_t kTabRows = 1u << kTabBits;
 
 template <int kMode>
 __global__ void __launch_bounds__(kHotThreads, 1)
@@ -777,6 +784,8 @@ dense_hot_tab_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
   tally_flush(tally, cnt, sum, xr);
 }
 
+#endif  // D3G_COMPARISON_KERNELS
+
 // Sort key of a record for the prefix-shared kernels: (subset mask, first
 // listed rank + 1, second listed rank + 1; 7/9/9 bits), 0 = absent.
 __global__ void trie_key_kernel(const uint8_t* __restrict__ rec, const uint32_t* __restrict__ rcnt,
@@ -846,6 +855,7 @@ __device__ __forceinline__ void or4(uint4& a, const uint4& v) {
   a.w |= v.w;
 }
 
+#if D3G_COMPARISON_KERNELS  // standalone prefix-shared kernel: measured comparison
 template <int kMode>
 __global__ void __launch_bounds__(kTrieThreads, 1)
 dense_hot_trie_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
@@ -1035,6 +1045,8 @@ dense_hot_trie_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
   if (lane == 0 && lds) atomicAdd(lds_units, (unsigned long long)lds);
   tally_flush(tally, cnt, sum, xr);
 }
+
+#endif  // D3G_COMPARISON_KERNELS
 
 // --- P1 with a jump table over the listed ranks (default with the table) ---
 // Same work as dense_hot_tab_kernel, fewer instructions per (row, batch): the

@@ -335,6 +335,7 @@ __global__ void gather_by_rank_kernel(const uint32_t* __restrict__ y_of_rank,
     out[r] = d[y_of_rank[r]];
 }
 
+#if D3G_COMPARISON_KERNELS  // earlier DenseEC designs (D3G_DENSE=v1|v2), measured comparisons
 // DenseEC driver: the z-tile-resident kernel (dense_ec_tile_kernel) when the
 // group's cold entries and the longest dense list fit in shared memory, the
 // list-streaming kernel (dense_ec_kernel) otherwise.
@@ -471,6 +472,7 @@ void run_dense_tiles(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d
   out.sum = h.sum;
   out.xr = h.xr;
 }
+#endif  // D3G_COMPARISON_KERNELS
 
 // ---------------------------------------------------------------------------
 // DenseEC v3 driver (denseec_hot.cuh): hot bit-sliced pass + cold residual
@@ -926,6 +928,10 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
           run(dense_hot_jt_kernel<Md, true, false>);
         else
           run(dense_hot_jt_kernel<Md, false, false>);
+      } else if (!D3G_COMPARISON_KERNELS) {
+        throw ConfigError("D3G_HOT=" + hv + " selects a comparison kernel; build with make "
+                          "COMPARE=1");
+#if D3G_COMPARISON_KERNELS
       } else if (trie) {
         // the kernel counts its own slice reads (over every batch)
         auto kfn = dense_hot_trie_kernel<decltype(M)::value>;
@@ -942,10 +948,12 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
         D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         D3G_LAUNCH(X, kfn, g, kHotThreads, sm, hp, in.dl_ptr, in.dl_col, rec.p, rcnt.p, dec, em,
                    t, cnt_sp);
+#endif
       }
     });
     D3G_CUDA(cudaEventRecord(ev1, X.stream));
   } else {
+    // K > 256 (no cold kernel: D3G_COLD=tiers) or D3G_HOT=list: the list kernel
     with_mode(mode, [&](auto M) {
       auto kfn = dense_hot_kernel<decltype(M)::value>;
       D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -1095,12 +1103,19 @@ void run_dense(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g::Em
                KernelOut& out) {
   const char* v = std::getenv("D3G_DENSE");
   std::string which = v ? v : "v3";
+#if D3G_COMPARISON_KERNELS
   if (which == "v1")
     run_dense_streaming(X, in, dec, mode, em, out);
   else if (which == "v2")
     run_dense_tiles(X, in, dec, mode, em, out);
   else
     run_dense_hot(X, in, dec, mode, em, out);
+#else
+  if (which == "v1" || which == "v2")
+    throw d3g::ConfigError("D3G_DENSE=" + which + " selects a comparison kernel; build with make "
+                           "COMPARE=1");
+  run_dense_hot(X, in, dec, mode, em, out);
+#endif
 }
 
 __global__ void decode_pairs_kernel(const uint32_t* __restrict__ xc, const uint32_t* __restrict__ zc,
