@@ -144,9 +144,10 @@ typedef struct {
   /* count-only: (x, z) pairs counted as hits without a test by the rank-0
    * split (x and z both hold the top-ranked y) */
   uint64_t hot_direct_pairs;
-  /* DenseEC P2 (cold residual) kernels: CUDA-event time and candidate bytes
-   * (36 B per candidate: 32-byte hot signature + 4-byte row id), each x's
-   * candidate stream counted once, in the tier that completes it */
+  /* DenseEC P2 (cold residual) kernels: CUDA-event time and algorithmic
+   * bytes = 16 B per candidate record streamed (hot word 0, folded tail,
+   * row id) + 32 B per exact tail check (cold_candidates / cold_tail_checks
+   * below), each x's stream counted once, in the tier that completes it */
   double ms_dense_cold;
   uint64_t cold_bytes;
   /* SpaStats::spa_allocations / spa_entries (P/include/dim3/sparsebmm.hpp:15-19):
@@ -157,6 +158,8 @@ typedef struct {
    * pairs are the rank's), and the job shape; 1 / 0 otherwise */
   uint64_t rank_out_p;
   int32_t nranks, rank;
+  /* DenseEC P2: candidate records streamed, exact tail checks (gathers) */
+  uint64_t cold_candidates, cold_tail_checks;
 } d3g_report;
 
 /* Materialized output: caller-owned host (or device, on_device != 0)

@@ -186,85 +186,6 @@ __global__ void hot_build_z_kernel(const uint64_t* __restrict__ dl_ptr,
   }
 }
 
-// Cold residual side: per y, dense row positions whose lists hold y at a
-// cold rank (y-major CSR, rows indexed by y code).
-// Rows of the cold CSR are keyed (variant, part, y). variant v in
-// [0, 2^var_bits) holds only the dense rows z whose hot mask avoids every rank
-// r < var_bits set in v: an x whose own top-var_bits mask is v can only get a
-// surviving (not hot-hit) candidate from such z, so it streams variant v.
-__global__ void cold_count_kernel(const uint64_t* __restrict__ dl_ptr,
-                                  const uint32_t* __restrict__ dl_col, uint64_t n_dense, uint32_t K,
-                                  const uint32_t* __restrict__ y_of_rank, uint32_t* __restrict__ cnt,
-                                  uint64_t y_card, uint32_t part_rows, uint32_t parts,
-                                  const uint64_t* __restrict__ hz, uint32_t kw, uint32_t var_bits) {
-  const uint32_t nvar = 1u << var_bits, vmask = nvar - 1;
-  const uint32_t sl = threadIdx.x & 7;  // 8 lanes per row
-  for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 8) + (threadIdx.x >> 3); i < n_dense;
-       i += (uint64_t)gridDim.x * (blockDim.x / 8)) {
-    const uint64_t part = i / part_rows;
-    const uint32_t zm = var_bits ? (uint32_t)(hz[i * kw] & vmask) : 0;
-    const uint64_t e = dl_ptr[i + 1];
-    for (uint64_t k = dl_ptr[i] + sl; k < e; k += 8) {
-      const uint32_t r = dl_col[k];
-      if (r < K) continue;
-      const uint32_t y = y_of_rank[r];
-      for (uint32_t v = 0; v < nvar; ++v)
-        if ((zm & v) == 0) atomicAdd(&cnt[((uint64_t)v * parts + part) * y_card + y], 1u);
-    }
-  }
-}
-
-// With sig != null the row's 256-bit hot signature (hz, kw == 4) is stored
-// inline next to each entry (2 x uint4 per entry). The scatter itself writes
-// only the 4-byte row ids (the atomic cursor bounds it); cold_sig_gather_kernel
-// then fills the signatures in one coalesced pass (sig == null here).
-__global__ void cold_scatter_kernel(const uint64_t* __restrict__ dl_ptr,
-                                    const uint32_t* __restrict__ dl_col, uint64_t n_dense,
-                                    uint32_t K, const uint32_t* __restrict__ y_of_rank,
-                                    const uint64_t* __restrict__ base,
-                                    uint32_t* __restrict__ left /* counts, consumed */,
-                                    uint32_t* __restrict__ out, uint4* __restrict__ sig,
-                                    uint64_t y_card, uint32_t part_rows, uint32_t parts,
-                                    const uint64_t* __restrict__ hz, uint32_t kw,
-                                    uint32_t var_bits) {
-  const uint32_t nvar = 1u << var_bits, vmask = nvar - 1;
-  const uint4* hz4 = reinterpret_cast<const uint4*>(hz);
-  const uint32_t sl = threadIdx.x & 7;  // 8 lanes per row
-  for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 8) + (threadIdx.x >> 3); i < n_dense;
-       i += (uint64_t)gridDim.x * (blockDim.x / 8)) {
-    const uint64_t part = i / part_rows;
-    const uint32_t zm = var_bits ? (uint32_t)(hz[i * kw] & vmask) : 0;
-    uint4 s0 = make_uint4(0, 0, 0, 0), s1 = s0;
-    if (sig) {
-      ld256(hz4 + 2 * i, s0, s1);
-    }
-    const uint64_t e = dl_ptr[i + 1];
-    for (uint64_t k = dl_ptr[i] + sl; k < e; k += 8) {
-      const uint32_t r = dl_col[k];
-      if (r < K) continue;
-      const uint32_t y = y_of_rank[r];
-      for (uint32_t v = 0; v < nvar; ++v)
-        if ((zm & v) == 0) {
-          const uint64_t key = ((uint64_t)v * parts + part) * y_card + y;
-          const uint64_t pos = base[key] + atomicSub(&left[key], 1u) - 1u;
-          out[pos] = (uint32_t)i;
-          if (sig) st256(sig + 2 * pos, s0, s1);
-        }
-    }
-  }
-}
-
-// The cold CSR's inline signatures, entry order: ch[k] = hz[ccol[k]] (a
-// coalesced 32-byte write per entry, the hz rows gathered).
-__global__ void cold_sig_gather_kernel(const uint32_t* __restrict__ ccol, uint64_t cnnz,
-                                       const uint4* __restrict__ hz4, uint4* __restrict__ ch) {
-  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cnnz;
-       k += (uint64_t)gridDim.x * blockDim.x) {
-    uint4 a, b;
-    ld256(hz4 + 2 * (uint64_t)ccol[k], a, b);
-    st256(ch + 2 * k, a, b);
-  }
-}
 
 // Pairs whose dense row is a folded-in SPARSE z (row_sp[i] != 0) are also
 // counted separately, so the report keeps the reference's pairs_sparse /
@@ -1373,667 +1294,5 @@ dense_hot_jt_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
   tally_flush(tally, cnt, sum, xr);
 }
 
-// Candidates streamed by a cold kernel (one 36-byte entry each: 32-byte hot
-// signature + 4-byte row id): the cold pass's algorithmic traffic.
-__device__ __forceinline__ void flush_cand(unsigned long long* cand, uint64_t v) {
-  if (!cand) return;
-  v = warp_sum(v);
-  if (lane_id() == 0 && v) atomicAdd(cand, (unsigned long long)v);
-}
-
-// P2 kernel: cold residual for a dense block whose row count fits a per-warp
-// shared-memory bitmap. One warp per live x. The cold CSR (y-major, rows =
-// dense row positions holding y at a cold rank) stores each candidate's
-// 256-bit hot signature inline (ch, 2 x uint4 per entry), so the filter
-// "hot masks intersect => already counted by P1" streams coalesced instead of
-// gathering hz[z] at random. Survivors are deduplicated in the warp's bitmap.
-constexpr int kColdWarps = 8;  // warps per CTA (several CTAs per SM)
-
-#ifndef D3G_COLD_UNROLL
-#define D3G_COLD_UNROLL 2
-#endif
-constexpr int kColdUnroll = D3G_COLD_UNROLL;
-
-template <int kMode>
-__global__ void __launch_bounds__(kColdWarps * 32, 4)
-dense_cold_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
-                  const uint64_t* __restrict__ r_ptr, const uint32_t* __restrict__ r_col,
-                  const uint64_t* __restrict__ cptr /* [parts][y_card] + 1 */,
-                  const uint32_t* __restrict__ ccol, const uint4* __restrict__ ch,
-                  const uint4* __restrict__ hx4 /* [X][2] */, uint64_t y_card, uint32_t parts,
-                  uint32_t part_rows, uint32_t var_bits, const uint32_t* __restrict__ dl_z,
-                  Decode dec, Emit em,
-                  unsigned int* __restrict__ next, Tally* tally,
-                  const uint8_t* __restrict__ row_sp, unsigned long long* __restrict__ cnt_sp,
-                  unsigned long long* __restrict__ cand = nullptr) {
-  extern __shared__ __align__(16) uint32_t cbm[];  // [kColdWarps][part_rows / 32]
-  const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
-  const uint32_t pw = part_rows / 32;
-  uint32_t* bm = cbm + (uint64_t)w * pw;
-  for (uint32_t i = lane; i < pw; i += 32) bm[i] = 0;
-  __syncwarp();
-  uint64_t cnt = 0, sum = 0, xr = 0, csp = 0, ncand = 0;
-  const uint64_t n_items = n_x * parts;
-  for (;;) {
-    uint32_t item = 0;
-    if (lane == 0) item = atomicAdd(next, 1u);
-    item = __shfl_sync(0xffffffffu, item, 0);
-    if (item >= n_items) break;
-    const uint32_t part = (uint32_t)(item / n_x);
-    const uint32_t x = xs[item % n_x];
-    const uint32_t zbase = part * part_rows;
-    uint4 a0, a1;
-    ld256(hx4 + 2 * (uint64_t)x, a0, a1);
-    const uint32_t v = a0.x & ((1u << var_bits) - 1);  // x's top-var_bits hot mask
-    const uint64_t* cp = cptr + ((uint64_t)v * parts + part) * y_card;
-    bool touched = false;
-    const uint64_t r0 = r_ptr[x], r1 = r_ptr[x + 1];
-    for (uint64_t kb = r0; kb < r1; kb += 32) {
-      // one coalesced load of up to 32 of x's y and their cold segments
-      const uint64_t kk = kb + lane;
-      uint64_t seg0 = 0, seg1 = 0;
-      if (kk < r1) {
-        const uint32_t y = r_col[kk];
-        seg0 = cp[y];
-        seg1 = cp[y + 1];
-      }
-      // flatten the (segment, entry) space: an inclusive warp scan of the
-      // segment lengths, then every lane takes one candidate per step and
-      // finds its segment by a 5-step binary search over the scan (short
-      // cold segments no longer leave most lanes idle)
-      const uint32_t len = (uint32_t)(seg1 - seg0);
-      uint32_t incl = len;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= (uint32_t)o) incl += u;
-      }
-      const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-      ncand += lane == 0 ? total : 0u;
-      // kColdUnroll candidates per lane per step: their loads are independent,
-      // so that many memory requests are in flight (the loop is latency bound)
-      for (uint32_t tb = 0; tb < total; tb += 32 * kColdUnroll) {
-        uint32_t tf[kColdUnroll], kx[kColdUnroll];
-        uint64_t t[kColdUnroll];
-#pragma unroll
-        for (int h = 0; h < kColdUnroll; ++h) {
-          tf[h] = tb + 32 * h + lane;
-          // smallest k with incl[k] > tf
-          uint32_t k = 0;
-#pragma unroll
-          for (int step = 16; step >= 1; step >>= 1) {
-            const uint32_t probe = __shfl_sync(0xffffffffu, incl, k + step - 1);
-            if (probe <= tf[h]) k += step;
-          }
-          kx[h] = k;
-        }
-#pragma unroll
-        for (int h = 0; h < kColdUnroll; ++h) {
-          const uint32_t before = __shfl_sync(0xffffffffu, incl - len, kx[h]);
-          const uint64_t base_k = __shfl_sync(0xffffffffu, seg0, kx[h]);
-          t[h] = base_k + (tf[h] - before);
-        }
-        uint4 b0[kColdUnroll], b1[kColdUnroll];
-        uint32_t zc[kColdUnroll];
-#pragma unroll
-        for (int h = 0; h < kColdUnroll; ++h) {
-          if (tf[h] < total) {
-            ld256(ch + 2 * t[h], b0[h], b1[h]);
-            zc[h] = ccol[t[h]];
-          }
-        }
-#pragma unroll
-        for (int h = 0; h < kColdUnroll; ++h) {  // converged: no per-lane exits
-          bool fresh = false;
-          const uint32_t zl = zc[h] - zbase;
-          if (tf[h] < total) {
-            const bool hot = ((a0.x & b0[h].x) | (a0.y & b0[h].y) | (a0.z & b0[h].z) |
-                              (a0.w & b0[h].w) | (a1.x & b1[h].x) | (a1.y & b1[h].y) |
-                              (a1.z & b1[h].z) | (a1.w & b1[h].w)) != 0;
-            if (!hot) {
-              const uint32_t bit = 1u << (zl & 31);
-              const uint32_t old = atomicOr(&bm[zl >> 5], bit);
-              touched = true;
-              fresh = (old & bit) == 0;
-            }
-          }
-          if (fresh) {
-            ++cnt;
-            if (row_sp && row_sp[zbase + zl]) ++csp;
-            if (kMode == kModeChecksum) {
-              const uint64_t hh = dec.hash(x, dl_z[zbase + zl]);
-              sum += hh;
-              xr ^= hh;
-            }
-          }
-          if (kMode == kModeEmit) {  // warp-aggregated reservation
-            const unsigned long long slot = warp_reserve(em, fresh ? 1u : 0u);
-            if (fresh) emit_at(em, slot, x, dl_z[zbase + zl]);
-          }
-        }
-      }
-    }
-    __syncwarp();
-    if (__any_sync(0xffffffffu, touched))
-      for (uint32_t i = lane; i < pw; i += 32) bm[i] = 0;
-    __syncwarp();
-  }
-  flush_sp(cnt_sp, csp);
-  flush_cand(cand, ncand);
-  tally_flush(tally, cnt, sum, xr);
-}
-
-// P2 for dense blocks too large for per-warp bitmaps (cfg5: 10M dense rows).
-// Same candidate stream as dense_cold_kernel (variant-selected cold CSR with
-// inline 256-bit hot signatures), but the survivors of x are deduplicated in a
-// warp-private shared-memory hash set: after the hot filter and the variant
-// cut, an x keeps only a few hundred candidates. An x whose survivors exceed
-// kCHMax abandons the hash (nothing of it was counted) and is queued for
-// dense_cold_overflow_kernel. Count, fingerprint and emission are taken from
-// the hash table when x completes, so abandoning is exact.
-constexpr int kCHWarps = 8;
-// 1024 slots per warp and 4 CTAs per SM: more x overflow into the CTA-hash
-// tier, which handles them well, and the common x run at higher occupancy
-// (cfg5 cold pass: 2048 slots x 3 CTAs 61 ms, 1024 x 4 52 ms, 512 x 4 58 ms)
-#ifndef D3G_CH_BITS
-#define D3G_CH_BITS 10
-#endif
-constexpr uint32_t kCHSlots = 1u << D3G_CH_BITS;  // per warp (8 KB at 11 bits)
-constexpr uint32_t kCHMax = kCHSlots * 3 / 4;    // load limit; < kCHSlots - 64 keeps probing finite
-constexpr uint32_t kCHEmpty = 0xffffffffu;
-#ifndef D3G_HASH_UNROLL
-#define D3G_HASH_UNROLL 2
-#endif
-constexpr int kHashUnroll = D3G_HASH_UNROLL;  // candidates in flight per lane
-
-__device__ __forceinline__ uint32_t ch_slot(uint32_t v) { return (v * 0x9E3779B1u) >> (32 - D3G_CH_BITS); }
-
-template <int kMode>
-__device__ __forceinline__ void cold_account(uint32_t x, uint32_t zc, const Decode& dec,
-                                             const Emit& em, uint64_t& sum, uint64_t& xr) {
-  if (kMode == kModeChecksum) {
-    const uint64_t h = dec.hash(x, zc);
-    sum += h;
-    xr ^= h;
-  } else if (kMode == kModeEmit) {
-    const unsigned long long idx = atomicAdd(em.cursor, 1ull);
-    if (idx < em.cap) {
-      em.x[idx] = x;
-      em.z[idx] = zc;
-    }
-  }
-}
-
-#ifndef D3G_CH_CTAS
-#define D3G_CH_CTAS 4
-#endif
-template <int kMode>
-__global__ void __launch_bounds__(kCHWarps * 32, D3G_CH_CTAS)
-dense_cold_hash_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
-                       const uint64_t* __restrict__ r_ptr, const uint32_t* __restrict__ r_col,
-                       const uint64_t* __restrict__ cptr, const uint32_t* __restrict__ ccol,
-                       const uint4* __restrict__ ch, const uint4* __restrict__ hx4,
-                       uint64_t y_card, uint32_t var_bits, const uint32_t* __restrict__ dl_z,
-                       Decode dec, Emit em, unsigned int* __restrict__ next,
-                       uint32_t* __restrict__ over_x, unsigned int* __restrict__ over_n,
-                       Tally* tally, const uint8_t* __restrict__ row_sp,
-                       unsigned long long* __restrict__ cnt_sp, uint32_t ch_max = kCHMax,
-                       unsigned long long* __restrict__ cand = nullptr) {
-  extern __shared__ __align__(16) uint32_t chtab[];  // [kCHWarps][kCHSlots]
-  const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
-  uint32_t* tab = chtab + (uint64_t)w * kCHSlots;
-  for (uint32_t i = lane; i < kCHSlots; i += 32) tab[i] = kCHEmpty;
-  __syncwarp();
-  uint64_t cnt = 0, sum = 0, xr = 0, csp = 0, ncand = 0;
-  for (;;) {
-    uint32_t item = 0;
-    if (lane == 0) item = atomicAdd(next, 1u);
-    item = __shfl_sync(0xffffffffu, item, 0);
-    if (item >= n_x) break;
-    const uint32_t x = xs[item];
-    uint4 a0, a1;
-    ld256(hx4 + 2 * (uint64_t)x, a0, a1);
-    const uint32_t v = a0.x & ((1u << var_bits) - 1);
-    const uint64_t* cp = cptr + (uint64_t)v * y_card;
-    uint32_t inserted = 0;  // warp-uniform
-    bool over = false;
-    uint64_t xcand = 0;  // x's candidates, credited only if x completes in this tier
-    const uint64_t r0 = r_ptr[x], r1 = r_ptr[x + 1];
-    for (uint64_t kb = r0; kb < r1 && !over; kb += 32) {
-      const uint64_t kk = kb + lane;
-      uint64_t seg0 = 0, seg1 = 0;
-      if (kk < r1) {
-        const uint32_t y = r_col[kk];
-        seg0 = cp[y];
-        seg1 = cp[y + 1];
-      }
-      // flattened (segment, entry) space, as in dense_cold_kernel: a warp scan
-      // of the segment lengths, then kHashUnroll candidates per lane per step
-      // found by a 5-step binary search (short cold segments keep lanes busy)
-      const uint32_t len = (uint32_t)(seg1 - seg0);
-      uint32_t incl = len;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= (uint32_t)o) incl += u;
-      }
-      const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-      xcand += lane == 0 ? total : 0u;
-      for (uint32_t tb = 0; tb < total && !over; tb += 32 * kHashUnroll) {
-        uint32_t tf[kHashUnroll], kx[kHashUnroll];
-        uint64_t t[kHashUnroll];
-#pragma unroll
-        for (int hh = 0; hh < kHashUnroll; ++hh) {
-          tf[hh] = tb + 32 * hh + lane;
-          uint32_t k = 0;
-#pragma unroll
-          for (int step = 16; step >= 1; step >>= 1) {
-            const uint32_t probe = __shfl_sync(0xffffffffu, incl, k + step - 1);
-            if (probe <= tf[hh]) k += step;
-          }
-          kx[hh] = k;
-        }
-#pragma unroll
-        for (int hh = 0; hh < kHashUnroll; ++hh) {
-          const uint32_t before = __shfl_sync(0xffffffffu, incl - len, kx[hh]);
-          const uint64_t base_k = __shfl_sync(0xffffffffu, seg0, kx[hh]);
-          t[hh] = base_k + (tf[hh] - before);
-        }
-        uint4 b0[kHashUnroll], b1[kHashUnroll];
-        uint32_t zc[kHashUnroll];
-#pragma unroll
-        for (int hh = 0; hh < kHashUnroll; ++hh) {
-          if (tf[hh] < total) {
-            ld256(ch + 2 * t[hh], b0[hh], b1[hh]);
-            zc[hh] = ccol[t[hh]];
-          }
-        }
-        uint32_t nfresh = 0;
-#pragma unroll
-        for (int hh = 0; hh < kHashUnroll; ++hh) {
-          bool fresh = false;
-          if (tf[hh] < total) {
-            const bool hot = ((a0.x & b0[hh].x) | (a0.y & b0[hh].y) | (a0.z & b0[hh].z) |
-                              (a0.w & b0[hh].w) | (a1.x & b1[hh].x) | (a1.y & b1[hh].y) |
-                              (a1.z & b1[hh].z) | (a1.w & b1[hh].w)) != 0;
-            if (!hot) {
-              const uint32_t zl = zc[hh];
-              uint32_t sl = ch_slot(zl);
-              for (;;) {
-                const uint32_t prev = atomicCAS(&tab[sl], kCHEmpty, zl);
-                if (prev == kCHEmpty) {
-                  fresh = true;
-                  break;
-                }
-                if (prev == zl) break;
-                sl = (sl + 1) & (kCHSlots - 1);
-              }
-            }
-          }
-          nfresh += __popc(__ballot_sync(0xffffffffu, fresh));
-        }
-        inserted += nfresh;
-        if (inserted > ch_max) over = true;
-      }
-    }
-    __syncwarp();
-    if (over) {
-      if (lane == 0) over_x[atomicAdd(over_n, 1u)] = x;
-    } else {
-      cnt += lane == 0 ? inserted : 0;
-      ncand += xcand;  // each x's stream counted once, in the tier that finishes it
-    }
-    if (inserted && (kMode != kModeCount || row_sp)) {
-      for (uint32_t i = lane; i < kCHSlots; i += 32) {  // uniform trip count
-        const uint32_t zl = tab[i];
-        if (kMode == kModeEmit) {  // warp-aggregated reservation
-          const bool e = zl != kCHEmpty && !over;
-          const unsigned long long slot = warp_reserve(em, e ? 1u : 0u);
-          if (e) emit_at(em, slot, x, dl_z[zl]);
-        }
-        if (zl != kCHEmpty) {
-          if (!over) {
-            if (kMode == kModeChecksum) cold_account<kMode>(x, dl_z[zl], dec, em, sum, xr);
-            if (row_sp && row_sp[zl]) ++csp;
-          }
-          tab[i] = kCHEmpty;
-        }
-      }
-    } else if (inserted) {
-      // count only: nothing to read back, reset the table with 16-byte stores
-      uint4* t4 = reinterpret_cast<uint4*>(tab);
-      const uint4 e4 = make_uint4(kCHEmpty, kCHEmpty, kCHEmpty, kCHEmpty);
-#pragma unroll 4
-      for (uint32_t i = lane; i < kCHSlots / 4; i += 32) t4[i] = e4;
-    }
-    __syncwarp();
-  }
-  flush_sp(cnt_sp, csp);
-  flush_cand(cand, ncand);
-  tally_flush(tally, cnt, sum, xr);
-}
-
-// Overflow x of dense_cold_hash_kernel: one CTA per x over a CTA-private
-// global bitmap of the dense rows (zero on entry and on exit: the candidate
-// stream is replayed to clear exactly the bits it set). The (segment, entry)
-// space of x's y rows is flattened with a CTA-wide scan of the segment
-// lengths, so every thread takes one candidate per step however short the
-// cold segments are (per-y loops left most of the 512 threads idle).
-constexpr int kOvThreads = 512;
-constexpr uint32_t kOvTouched = 65536;  // touched-word list per CTA
-#ifndef D3G_OV_UNROLL
-#define D3G_OV_UNROLL 2
-#endif
-constexpr int kOvUnroll = D3G_OV_UNROLL;
-
-template <int kMode>
-__global__ void __launch_bounds__(kOvThreads, 3)
-dense_cold_overflow_kernel(const uint32_t* __restrict__ over_x, const unsigned int* __restrict__ over_n,
-                           const uint64_t* __restrict__ r_ptr, const uint32_t* __restrict__ r_col,
-                           const uint64_t* __restrict__ cptr, const uint32_t* __restrict__ ccol,
-                           const uint4* __restrict__ ch, const uint4* __restrict__ hx4,
-                           uint64_t y_card, uint32_t var_bits, const uint32_t* __restrict__ dl_z,
-                           uint32_t* __restrict__ gbm, uint64_t words, Decode dec, Emit em,
-                           Tally* tally, const uint8_t* __restrict__ row_sp,
-                           unsigned long long* __restrict__ cnt_sp,
-                           uint32_t* __restrict__ touched /* [gridDim.x][kOvTouched] */,
-                           unsigned long long* __restrict__ cand = nullptr) {
-  __shared__ uint64_t s_seg0[kOvThreads];
-  __shared__ uint32_t s_off[kOvThreads];
-  __shared__ uint32_t s_wsum[kOvThreads / 32];
-  __shared__ uint32_t s_total;
-  __shared__ unsigned int s_nt;  // bitmap words this x made non-zero (touched list)
-  uint32_t* tl = touched + (uint64_t)blockIdx.x * kOvTouched;
-  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-  constexpr uint32_t kW = kOvThreads / 32;
-  uint32_t* bm = gbm + (uint64_t)blockIdx.x * words;
-  const uint32_t n = *over_n;
-  uint64_t cnt = 0, sum = 0, xr = 0, csp = 0, ncand = 0;
-  for (uint32_t it = blockIdx.x; it < n; it += gridDim.x) {
-    const uint32_t x = over_x[it];
-    uint4 a0, a1;
-    ld256(hx4 + 2 * (uint64_t)x, a0, a1);
-    const uint32_t v = a0.x & ((1u << var_bits) - 1);
-    const uint64_t* cp = cptr + (uint64_t)v * y_card;
-    const uint64_t r0 = r_ptr[x], r1 = r_ptr[x + 1];
-    if (threadIdx.x == 0) s_nt = 0;
-    __syncthreads();
-    for (int pass = 0; pass < 2; ++pass) {
-      if (pass == 1) {
-        // clear through the touched list; replay the stream only if it overflowed
-        const uint32_t nt = s_nt;
-        if (nt <= kOvTouched) {
-          for (uint32_t i = threadIdx.x; i < nt; i += kOvThreads) bm[tl[i]] = 0;
-          __syncthreads();
-          break;
-        }
-      }
-      for (uint64_t yb = r0; yb < r1; yb += kOvThreads) {
-        const uint64_t k = yb + threadIdx.x;
-        uint64_t sg0 = 0;
-        uint32_t len = 0;
-        if (k < r1) {
-          const uint32_t y = r_col[k];
-          sg0 = cp[y];
-          len = (uint32_t)(cp[y + 1] - sg0);
-        }
-        uint32_t incl = len;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= (uint32_t)o) incl += u;
-        }
-        if (lane == 31) s_wsum[warp] = incl;
-        __syncthreads();
-        if (warp == 0) {
-          const uint32_t wv = lane < kW ? s_wsum[lane] : 0u;
-          uint32_t wi = wv;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t u = __shfl_up_sync(0xffffffffu, wi, o);
-            if (lane >= (uint32_t)o) wi += u;
-          }
-          if (lane < kW) s_wsum[lane] = wi - wv;  // exclusive over warps
-          if (lane == kW - 1) s_total = wi;
-        }
-        __syncthreads();
-        s_off[threadIdx.x] = s_wsum[warp] + incl - len;
-        s_seg0[threadIdx.x] = sg0;
-        __syncthreads();
-        const uint32_t total = s_total;
-        const uint32_t ny = (uint32_t)((r1 - yb) < kOvThreads ? (r1 - yb) : kOvThreads);
-        // kOvUnroll candidates per thread in flight: the signature and row-id
-        // loads of all of them are issued before any is consumed (the loop is
-        // bound by the dependent global loads, not by bandwidth)
-        for (uint32_t fb = threadIdx.x; fb < total; fb += kOvThreads * kOvUnroll) {
-          uint64_t t[kOvUnroll];
-          bool ok[kOvUnroll];
-#pragma unroll
-          for (int u = 0; u < kOvUnroll; ++u) {
-            const uint32_t f = fb + u * kOvThreads;
-            ok[u] = f < total;
-            uint32_t lo = 0, hi = ny;  // last segment starting at or before f
-            while (ok[u] && hi - lo > 1) {
-              const uint32_t mid = (lo + hi) >> 1;
-              if (s_off[mid] <= f) lo = mid; else hi = mid;
-            }
-            t[u] = ok[u] ? s_seg0[lo] + (f - s_off[lo]) : 0;
-          }
-          uint4 b0[kOvUnroll], b1[kOvUnroll];
-          uint32_t zc[kOvUnroll];
-#pragma unroll
-          for (int u = 0; u < kOvUnroll; ++u)
-            if (ok[u]) {
-              ncand += pass == 0 ? 1u : 0u;  // the clearing replay is not new work
-              ld256(ch + 2 * t[u], b0[u], b1[u]);
-              zc[u] = ccol[t[u]];
-            }
-#pragma unroll
-          for (int u = 0; u < kOvUnroll; ++u) {
-            if (!ok[u]) continue;
-            const bool hot = ((a0.x & b0[u].x) | (a0.y & b0[u].y) | (a0.z & b0[u].z) |
-                              (a0.w & b0[u].w) | (a1.x & b1[u].x) | (a1.y & b1[u].y) |
-                              (a1.z & b1[u].z) | (a1.w & b1[u].w)) != 0;
-            if (hot) continue;
-            const uint32_t zl = zc[u];
-            if (pass == 0) {
-              const uint32_t bit = 1u << (zl & 31);
-              const uint32_t old = atomicOr(&bm[zl >> 5], bit);
-              if (old & bit) continue;
-              if (old == 0) {
-                const unsigned int slot = atomicAdd(&s_nt, 1u);
-                if (slot < kOvTouched) tl[slot] = zl >> 5;
-              }
-              ++cnt;
-              if (row_sp && row_sp[zl]) ++csp;
-              if (kMode != kModeCount) cold_account<kMode>(x, dl_z[zl], dec, em, sum, xr);
-            } else {
-              bm[zl >> 5] = 0;
-            }
-          }
-        }
-        __syncthreads();  // s_off / s_seg0 are rewritten by the next chunk
-      }
-      __syncthreads();
-    }
-  }
-  flush_sp(cnt_sp, csp);
-  flush_cand(cand, ncand);
-  tally_flush(tally, cnt, sum, xr);
-}
-
-// Overflow x of dense_cold_hash_kernel, first tier: one CTA per x with a
-// CTA-wide shared-memory hash set of kCCSlots rows over the same flattened
-// candidate stream as dense_cold_overflow_kernel (no global bitmap: those are
-// 1.25 MB per CTA on cfg5 and thrash L2, 130 GB of DRAM traffic). An x whose
-// survivors pass cc_max is abandoned exactly and queued for the bitmap kernel.
-#ifndef D3G_CC_BITS
-#define D3G_CC_BITS 15
-#endif
-#ifndef D3G_CC_THREADS
-#define D3G_CC_THREADS 1024
-#endif
-constexpr int kCCThreads = D3G_CC_THREADS;
-constexpr uint32_t kCCSlots = 1u << D3G_CC_BITS;  // 128 KB at 15 bits
-constexpr uint32_t kCCMax = kCCSlots * 3 / 4;      // load limit 0.75
-constexpr int kCCPerSm = (1024 / D3G_CC_THREADS) * (D3G_CC_BITS >= 15 ? 1 : 2) > 2
-                             ? 2 : (1024 / D3G_CC_THREADS) * (D3G_CC_BITS >= 15 ? 1 : 2);
-
-__device__ __forceinline__ uint32_t cc_slot(uint32_t v) { return (v * 0x9E3779B1u) >> (32 - D3G_CC_BITS); }
-
-template <int kMode>
-__global__ void __launch_bounds__(kCCThreads, kCCPerSm)
-dense_cold_cta_kernel(const uint32_t* __restrict__ over_x, const unsigned int* __restrict__ over_n,
-                           const uint64_t* __restrict__ r_ptr, const uint32_t* __restrict__ r_col,
-                           const uint64_t* __restrict__ cptr, const uint32_t* __restrict__ ccol,
-                           const uint4* __restrict__ ch, const uint4* __restrict__ hx4,
-                           uint64_t y_card, uint32_t var_bits, const uint32_t* __restrict__ dl_z,
-                           Decode dec, Emit em, uint32_t* __restrict__ over2_x,
-                           unsigned int* __restrict__ over2_n, uint32_t cc_max,
-                           Tally* tally, const uint8_t* __restrict__ row_sp,
-                           unsigned long long* __restrict__ cnt_sp,
-                           unsigned long long* __restrict__ cand = nullptr) {
-  __shared__ uint64_t s_seg0[kCCThreads];
-  __shared__ uint32_t s_off[kCCThreads];
-  __shared__ uint32_t s_wsum[kCCThreads / 32];
-  __shared__ uint32_t s_total;
-  __shared__ unsigned int s_ins, s_over;
-  extern __shared__ __align__(16) uint32_t cctab[];  // [kCCSlots]
-  for (uint32_t i = threadIdx.x; i < kCCSlots; i += kCCThreads) cctab[i] = kCHEmpty;
-  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-  constexpr uint32_t kW = kCCThreads / 32;
-  const uint32_t n = *over_n;
-  uint64_t cnt = 0, sum = 0, xr = 0, csp = 0, ncand = 0;
-  for (uint32_t it = blockIdx.x; it < n; it += gridDim.x) {
-    const uint32_t x = over_x[it];
-    uint4 a0, a1;
-    ld256(hx4 + 2 * (uint64_t)x, a0, a1);
-    const uint32_t v = a0.x & ((1u << var_bits) - 1);
-    const uint64_t* cp = cptr + (uint64_t)v * y_card;
-    const uint64_t r0 = r_ptr[x], r1 = r_ptr[x + 1];
-    if (threadIdx.x == 0) {
-      s_ins = 0;
-      s_over = 0;
-    }
-    __syncthreads();
-    uint64_t xcand = 0;  // credited only if x completes in this tier
-    {
-      for (uint64_t yb = r0; yb < r1 && !s_over; yb += kCCThreads) {
-        const uint64_t k = yb + threadIdx.x;
-        uint64_t sg0 = 0;
-        uint32_t len = 0;
-        if (k < r1) {
-          const uint32_t y = r_col[k];
-          sg0 = cp[y];
-          len = (uint32_t)(cp[y + 1] - sg0);
-        }
-        uint32_t incl = len;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= (uint32_t)o) incl += u;
-        }
-        if (lane == 31) s_wsum[warp] = incl;
-        __syncthreads();
-        if (warp == 0) {
-          const uint32_t wv = lane < kW ? s_wsum[lane] : 0u;
-          uint32_t wi = wv;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t u = __shfl_up_sync(0xffffffffu, wi, o);
-            if (lane >= (uint32_t)o) wi += u;
-          }
-          if (lane < kW) s_wsum[lane] = wi - wv;  // exclusive over warps
-          if (lane == kW - 1) s_total = wi;
-        }
-        __syncthreads();
-        s_off[threadIdx.x] = s_wsum[warp] + incl - len;
-        s_seg0[threadIdx.x] = sg0;
-        __syncthreads();
-        const uint32_t total = s_total;
-        const uint32_t ny = (uint32_t)((r1 - yb) < kCCThreads ? (r1 - yb) : kCCThreads);
-        // kOvUnroll candidates per thread in flight: the signature and row-id
-        // loads of all of them are issued before any is consumed (the loop is
-        // bound by the dependent global loads, not by bandwidth)
-        for (uint32_t fb0 = 0; fb0 < total && !*(volatile unsigned int*)&s_over;
-             fb0 += kCCThreads * kOvUnroll) {
-          const uint32_t fb = fb0 + threadIdx.x;
-          uint32_t nf = 0;  // fresh inserts by this thread in this step
-          uint64_t t[kOvUnroll];
-          bool ok[kOvUnroll];
-#pragma unroll
-          for (int u = 0; u < kOvUnroll; ++u) {
-            const uint32_t f = fb + u * kCCThreads;
-            ok[u] = f < total;
-            uint32_t lo = 0, hi = ny;  // last segment starting at or before f
-            while (ok[u] && hi - lo > 1) {
-              const uint32_t mid = (lo + hi) >> 1;
-              if (s_off[mid] <= f) lo = mid; else hi = mid;
-            }
-            t[u] = ok[u] ? s_seg0[lo] + (f - s_off[lo]) : 0;
-          }
-          uint4 b0[kOvUnroll], b1[kOvUnroll];
-          uint32_t zc[kOvUnroll];
-#pragma unroll
-          for (int u = 0; u < kOvUnroll; ++u)
-            if (ok[u]) {
-              ++xcand;
-              ld256(ch + 2 * t[u], b0[u], b1[u]);
-              zc[u] = ccol[t[u]];
-            }
-#pragma unroll
-          for (int u = 0; u < kOvUnroll; ++u) {
-            if (!ok[u]) continue;
-            const bool hot = ((a0.x & b0[u].x) | (a0.y & b0[u].y) | (a0.z & b0[u].z) |
-                              (a0.w & b0[u].w) | (a1.x & b1[u].x) | (a1.y & b1[u].y) |
-                              (a1.z & b1[u].z) | (a1.w & b1[u].w)) != 0;
-            if (hot) continue;
-            const uint32_t zl = zc[u];
-            uint32_t sl = cc_slot(zl);
-            for (uint32_t probe = 0; probe < kCCSlots; ++probe) {
-              const uint32_t prev = atomicCAS(&cctab[sl], kCHEmpty, zl);
-              if (prev == kCHEmpty) {
-                ++nf;
-                break;
-              }
-              if (prev == zl) break;
-              sl = (sl + 1) & (kCCSlots - 1);
-            }
-          }
-          const uint32_t wf = warp_sum(nf);
-          if (lane == 0 && wf && atomicAdd(&s_ins, wf) + wf > cc_max) s_over = 1;
-        }
-        __syncthreads();  // s_off / s_seg0 are rewritten by the next chunk
-      }
-    }
-    __syncthreads();
-    const bool over = s_over != 0;
-    if (over) {
-      if (threadIdx.x == 0) over2_x[atomicAdd(over2_n, 1u)] = x;
-    } else {
-      ncand += xcand;
-      if (threadIdx.x == 0) cnt += s_ins;
-    }
-    for (uint32_t i = threadIdx.x; i < kCCSlots; i += kCCThreads) {  // uniform trip count
-      const uint32_t zl = cctab[i];
-      if (kMode == kModeEmit) {  // warp-aggregated reservation
-        const bool e = zl != kCHEmpty && !over;
-        const unsigned long long slot = warp_reserve(em, e ? 1u : 0u);
-        if (e) emit_at(em, slot, x, dl_z[zl]);
-      }
-      if (zl != kCHEmpty) {
-        if (!over) {
-          if (kMode == kModeChecksum) cold_account<kMode>(x, dl_z[zl], dec, em, sum, xr);
-          if (row_sp && row_sp[zl]) ++csp;
-        }
-        cctab[i] = kCHEmpty;
-      }
-    }
-    __syncthreads();
-  }
-  flush_sp(cnt_sp, csp);
-  flush_cand(cand, ncand);
-  tally_flush(tally, cnt, sum, xr);
-}
 
 }  // namespace d3g

@@ -28,6 +28,7 @@
 #include "datagen.cuh"
 #include "denseec.cuh"
 #include "denseec_hot.cuh"
+#include "denseec_cold.cuh"
 #include "denseec_tc.cuh"
 #include "io.cuh"
 #include "aggregate.cuh"
@@ -165,7 +166,8 @@ struct KernelOut {
   uint64_t hot_lds_bytes_unshared = 0;  // without the prefix sharing
   uint64_t split_direct_pairs = 0;  // hits counted without a test (pivot plan)
   double ms_cold = 0;          // CUDA-event time of the cold-pass kernels
-  uint64_t cold_bytes = 0;     // their candidate stream (36 B per candidate)
+  uint64_t cold_bytes = 0;     // their algorithmic bytes (16 B records + 32 B tail checks)
+  uint64_t cold_candidates = 0, cold_tail_checks = 0;
 };
 
 template <class F>
@@ -617,7 +619,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     cold_ctas = 3;  // keep the dense rows within 16 bitmap partitions (cfg4)
   if (cc_env) cold_ctas = std::max(1, std::atoi(cc_env));
   const uint64_t cold_rows_cap =
-      std::max<uint64_t>(32, (budget / cold_ctas / kColdWarps) * 8 / 32 * 32);
+      std::max<uint64_t>(32, (budget / cold_ctas / kColdWarps - (kDQ + kSegWords) * 4) * 8 / 32 * 32);
   const bool cold_bitmap = k_cap >= 256 && (D + cold_rows_cap - 1) / cold_rows_cap <= 16;
   // larger dense blocks: the same candidate stream, survivors in a per-warp
   // hash set (dense_cold_hash_kernel); D3G_COLD=tiers keeps the SparseBMM tiers
@@ -752,7 +754,8 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   DBuf<uint64_t> cptr;
   if (run_cold) {
     if (cold_bitmap) {
-      const uint64_t per_warp = budget / cold_ctas / kColdWarps;
+      // bitmap + deferred rows + compacted segments
+      const uint64_t per_warp = budget / cold_ctas / kColdWarps - (kDQ + kSegWords) * 4;
       const uint64_t rows_cap = std::max<uint64_t>(32, per_warp * 8 / 32 * 32);
       parts = (uint32_t)((D + rows_cap - 1) / rows_cap);
       part_rows = (uint32_t)((((D + parts - 1) / parts) + 31) / 32 * 32);
@@ -964,35 +967,44 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   KernelOut cold;
   if (run_cold) {
     X.wait_mark();  // cnnz
-    DBuf<uint32_t> ccol = X.alloc<uint32_t>(cnnz);
-    DBuf<uint4> ch;  // inline hot signatures (cold kernels only)
-    if (cold_kernel_ok) ch = X.alloc<uint4>(2 * cnnz);
+    // cold kernels: 16-byte records {hz word 0, fold of words 1-3, row}; the
+    // scatter writes the row fields, one coalesced pass fills the signatures.
+    // D3G_COLD=tiers: a plain column of row ids for the SparseBMM tiers.
+    DBuf<uint32_t> ccol;
+    DBuf<uint4> crec;
+    if (cold_kernel_ok && D >= kRowMask)
+      throw d3g::Error(D3G_INTERNAL_ERROR, "cold records hold row ids below 2^31 - 1");
+    if (cold_kernel_ok) crec = X.alloc<uint4>(cnnz);
+    else ccol = X.alloc<uint32_t>(cnnz);
+    uint32_t* cout = cold_kernel_ok ? reinterpret_cast<uint32_t*>(crec.p) + 3 : ccol.p;
     D3G_LAUNCH(X, cold_scatter_kernel, grid_for(D * 8, 256), 256, 0, in.dl_ptr, in.dl_col, D, K,
-               in.y_of_rank, cptr.p, cc.p, ccol.p, nullptr, Y, part_rows, parts,
+               in.y_of_rank, cptr.p, cc.p, cout, cold_kernel_ok ? 4u : 1u, Y, part_rows, parts,
                reinterpret_cast<const uint64_t*>(hz.p), kw, var_bits);
     cc.reset();
-    if (cold_kernel_ok && cnnz)  // the inline signatures, one coalesced pass
-      D3G_LAUNCH(X, cold_sig_gather_kernel, grid_for(cnnz, 256), 256, 0, ccol.p, cnnz,
-                 reinterpret_cast<const uint4*>(hz.p), ch.p);
+    const uint4* hz4 = reinterpret_cast<const uint4*>(hz.p);
+    if (cold_kernel_ok && cnnz)
+      D3G_LAUNCH(X, cold_rec_fill_kernel, grid_for(cnnz, 256), 256, 0, crec.p, cnnz, hz4, in.row_sp);
     if (cold_kernel_ok) {
       DBuf<unsigned int> next = X.zeros<unsigned int>(1);
       Tally* tc = tallies.p + 1;
-      unsigned long long* cand = &tallies.p[5].count;  // candidates streamed
+      // records streamed (.count) and exact tail checks (.sum)
+      unsigned long long* cand = &tallies.p[5].count;
       D3G_CUDA(cudaEventCreate(&ev2));
       D3G_CUDA(cudaEventCreate(&ev3));
       D3G_CUDA(cudaEventRecord(ev2, X.stream));
       if (cold_hash) {
         DBuf<uint32_t> over_x = X.alloc<uint32_t>(n_live);
         DBuf<unsigned int> over_n = X.zeros<unsigned int>(1);
-        const size_t hsm = (size_t)kCHWarps * kCHSlots * 4;
+        const size_t hsm = kCHSmem;
         with_mode(mode, [&](auto M) {
           auto kfn = dense_cold_hash_kernel<decltype(M)::value>;
           D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
           D3G_LAUNCH(X, kfn, (unsigned)X.sm_count * (D3G_CH_BITS <= 10 ? D3G_CH_CTAS : 3), kCHWarps * 32, hsm,
-                     xorder, n_live,
-                     in.r_ptr, in.r_col, cptr.p, ccol.p, ch.p, reinterpret_cast<const uint4*>(hx.p),
-                     Y, var_bits, in.dl_z, dec, em, next.p, over_x.p, over_n.p, tc, in.row_sp,
-                     cnt_sp, env_u32("D3G_COLD_HASH_MAX", kCHMax, 1, kCHMax), cand);
+                     xorder, n_live, in.r_ptr, in.r_col, cptr.p, crec.p, hz4,
+                     reinterpret_cast<const uint4*>(hx.p), Y, var_bits, in.dl_z, dec, em, next.p,
+                     over_x.p, over_n.p, tc, cnt_sp,
+                     env_u32("D3G_COLD_HASH_MAX", kCHMax, 1, kCHMax),
+                     env_u32("D3G_COLD_ROUTE", D3G_COLD_ROUTE, 1, 0xffffffffu), cand);
         });
         const unsigned int n_over = X.scalar(over_n.p);
         out.cold_overflow = n_over;
@@ -1007,15 +1019,14 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
         if (n_over && cta_tier) {
           over2_x = X.alloc<uint32_t>(n_over);
           over2_n = X.zeros<unsigned int>(1);
-          const size_t csm2 = (size_t)kCCSlots * 4;
           with_mode(mode, [&](auto M) {
             auto kfn = dense_cold_cta_kernel<decltype(M)::value>;
-            D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm2));
-            D3G_LAUNCH(X, kfn, std::min<unsigned>(n_over, (unsigned)X.sm_count * kCCPerSm), kCCThreads, csm2,
-                       over_x.p, over_n.p, in.r_ptr, in.r_col, cptr.p, ccol.p, ch.p,
+            D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCCSmem));
+            D3G_LAUNCH(X, kfn, std::min<unsigned>(n_over, (unsigned)X.sm_count * kCCPerSm), kCCThreads,
+                       kCCSmem, over_x.p, over_n.p, in.r_ptr, in.r_col, cptr.p, crec.p, hz4,
                        reinterpret_cast<const uint4*>(hx.p), Y, var_bits, in.dl_z, dec, em,
                        over2_x.p, over2_n.p, env_u32("D3G_COLD_CTA_MAX", kCCMax, 1, kCCMax), tc,
-                       in.row_sp, cnt_sp, cand);
+                       cnt_sp, cand);
           });
           n_over2 = X.scalar(over2_n.p);
         }
@@ -1029,23 +1040,23 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
           DBuf<uint32_t> gbm = X.zeros<uint32_t>((uint64_t)og * words);
           DBuf<uint32_t> touched = X.alloc<uint32_t>((uint64_t)og * kOvTouched);
           with_mode(mode, [&](auto M) {
-            D3G_LAUNCH(X, dense_cold_overflow_kernel<decltype(M)::value>, og, kOvThreads, 0, ox,
-                       on, in.r_ptr, in.r_col, cptr.p, ccol.p, ch.p,
+            D3G_LAUNCH(X, dense_cold_overflow_kernel<decltype(M)::value>, og, kOvThreads, kOvSmem, ox,
+                       on, in.r_ptr, in.r_col, cptr.p, crec.p, hz4,
                        reinterpret_cast<const uint4*>(hx.p), Y, var_bits, in.dl_z, gbm.p, words,
-                       dec, em, tc, in.row_sp, cnt_sp, touched.p, cand);
+                       dec, em, tc, cnt_sp, touched.p, cand);
           });
         }
         out.cold_overflow2 = n_over2;
       } else {
-      size_t csm = (size_t)(part_rows / 32) * 4 * kColdWarps;
-      with_mode(mode, [&](auto M) {
-        auto kfn = dense_cold_kernel<decltype(M)::value>;
-        if (csm > 48 * 1024)
-          D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
-        D3G_LAUNCH(X, kfn, (unsigned)X.sm_count * cold_ctas, kColdWarps * 32, csm, xorder, n_live, in.r_ptr,
-                   in.r_col, cptr.p, ccol.p, ch.p, reinterpret_cast<const uint4*>(hx.p), Y, parts,
-                   part_rows, var_bits, in.dl_z, dec, em, next.p, tc, in.row_sp, cnt_sp, cand);
-      });
+        const size_t csm = ((size_t)(part_rows / 32) + kDQ + kSegWords) * 4 * kColdWarps;
+        with_mode(mode, [&](auto M) {
+          auto kfn = dense_cold_kernel<decltype(M)::value>;
+          if (csm > 48 * 1024)
+            D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
+          D3G_LAUNCH(X, kfn, (unsigned)X.sm_count * cold_ctas, kColdWarps * 32, csm, xorder, n_live,
+                     in.r_ptr, in.r_col, cptr.p, crec.p, hz4, reinterpret_cast<const uint4*>(hx.p), Y,
+                     parts, part_rows, var_bits, in.dl_z, dec, em, next.p, tc, cnt_sp, cand);
+        });
       }
       D3G_CUDA(cudaEventRecord(ev3, X.stream));
     } else {
@@ -1083,7 +1094,10 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     cudaEventDestroy(ev2);
     cudaEventDestroy(ev3);
     out.ms_cold = ms;
-    out.cold_bytes = th[5].count * 36ull;  // 32-byte signature + 4-byte row id
+    // 16-byte records streamed + 32-byte hz rows of the exact tail checks
+    out.cold_bytes = th[5].count * 16ull + th[5].sum * 32ull;
+    out.cold_candidates = th[5].count;
+    out.cold_tail_checks = th[5].sum;
   }
   if (std::getenv("D3G_TRACE"))
     std::fprintf(stderr, "[dense_hot] D=%llu live=%llu K=%u hot=%llu cold=%llu cold_path=%s over=%llu over2=%llu\n",
@@ -2505,6 +2519,8 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   rep->hot_direct_pairs = ks.split_direct_pairs + kd.split_direct_pairs;
   rep->ms_dense_cold = ks.ms_cold + kd.ms_cold;
   rep->cold_bytes = ks.cold_bytes + kd.cold_bytes;
+  rep->cold_candidates = ks.cold_candidates + kd.cold_candidates;
+  rep->cold_tail_checks = ks.cold_tail_checks + kd.cold_tail_checks;
   rep->spa_inner_count = outj_sp;
   rep->out_p = ks.count + kd.count;
   rep->checksum_sum = ks.sum + kd.sum;
@@ -2515,12 +2531,13 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   if (dist) {
     // the job's totals: each rank's tally record, gathered and folded
     // (the fingerprint's xor has no NCCL reduction)
-    constexpr int kF = 13;
+    constexpr int kF = 15;
     uint64_t mine[kF] = {rep->out_p, rep->pairs_sparse, rep->pairs_dense, rep->checksum_sum,
                          rep->checksum_xor, rep->hot_direct_pairs, rep->cold_bytes,
                          rep->hot_lds_bytes, rep->dense_wide_encounters,
                          rep->dense_probe_encounters, rep->dense_blocks_checked,
-                         rep->dense_probes_done, rep->dense_row_bitmaps_built};
+                         rep->dense_probes_done, rep->dense_row_bitmaps_built,
+                         rep->cold_candidates, rep->cold_tail_checks};
     std::vector<uint64_t> all((size_t)kF * E->nranks);
     ex_allgather(X, *E, mine, all.data(), sizeof(mine));
     uint64_t tot[kF] = {0};
@@ -2540,6 +2557,8 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
     rep->dense_blocks_checked = tot[10];
     rep->dense_probes_done = tot[11];
     rep->dense_row_bitmaps_built = tot[12];
+    rep->cold_candidates = tot[13];
+    rep->cold_tail_checks = tot[14];
   }
 
   // 9. materialization (decode, engine.cpp:502-529)

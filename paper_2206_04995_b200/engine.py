@@ -241,7 +241,8 @@ class _Report(C.Structure):
                 ("hot_direct_pairs", C.c_uint64), ("ms_dense_cold", C.c_double),
                 ("cold_bytes", C.c_uint64), ("spa_allocations", C.c_uint64),
                 ("spa_entries", C.c_uint64), ("rank_out_p", C.c_uint64),
-                ("nranks", C.c_int32), ("rank", C.c_int32)]
+                ("nranks", C.c_int32), ("rank", C.c_int32),
+                ("cold_candidates", C.c_uint64), ("cold_tail_checks", C.c_uint64)]
 
 
 class _Pairs(C.Structure):
@@ -496,6 +497,8 @@ class ExecutionReport:
     rank_out_p: int = 0
     nranks: int = 1
     rank: int = 0
+    cold_candidates: int = 0
+    cold_tail_checks: int = 0
 
     def to_kv(self):
         """Insertion-ordered key/value view with the reference's key names
