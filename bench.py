@@ -501,13 +501,16 @@ def main():
     if cold_ms > 0 and cold_bytes:
         ach_c = cold_bytes / (cold_ms * 1e-3) / 1e9
         cold_roof = {"kernel": "DenseEC P2 cold residual pass (dense_cold_kernel, or "
-                               "dense_cold_hash_kernel + dense_cold_overflow_kernel)",
+                               "dense_cold_hash_kernel + dense_cold_cta_kernel + "
+                               "dense_cold_overflow_kernel)",
                      "bound": "hbm", "achieved": ach_c, "peak": hbm, "unit": "GB/s",
                      "frac": ach_c / hbm, "traffic": _ncu_dram_bytes(cfg_id, "cold"),
-                     "work": f"candidate stream = 36 B (32-byte hot signature + 4-byte row id) x "
-                             f"{cold_bytes // 36} candidates = {cold_bytes:.4g} B per step; kernel "
-                             f"time {cold_ms:.3f} ms (CUDA events on the library stream); the "
-                             f"stream is L2-resident in part, so traffic < work is possible",
+                     "work": f"16-byte candidate records x {r0.cold_candidates} + 32-byte exact "
+                             f"tail checks x {r0.cold_tail_checks} = {cold_bytes:.4g} B per step "
+                             f"(each x's stream counted once); kernel time {cold_ms:.3f} ms "
+                             f"(CUDA events on the library stream); the records are L2-resident "
+                             f"in part, so traffic < work is possible; the kernels are issue-bound "
+                             f"(ncu: IPC 2.2-2.5, profiles/), not bandwidth-bound",
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs",
                      "share_of_step": cold_ms / phase["ms_total"]}
     if dom in ("dense_ec", "sparse_bmm") and cold_roof and cold_ms > hot_ms:

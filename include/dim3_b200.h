@@ -160,6 +160,12 @@ typedef struct {
   int32_t nranks, rank;
   /* DenseEC P2: candidate records streamed, exact tail checks (gathers) */
   uint64_t cold_candidates, cold_tail_checks;
+  /* sharded job: collectives issued, bytes a ring collective moves per rank
+   * over the links, host time of host-staged collectives (callback
+   * transport; 0 under NCCL), and whether the S side was split by z */
+  uint64_t exchange_calls, exchange_bus_bytes;
+  double ms_exchange_host;
+  int32_t zsplit, pad1;
 } d3g_report;
 
 /* Materialized output: caller-owned host (or device, on_device != 0)

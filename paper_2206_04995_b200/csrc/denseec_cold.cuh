@@ -40,12 +40,13 @@ __global__ void cold_count_kernel(const uint64_t* __restrict__ dl_ptr,
                                   const uint32_t* __restrict__ dl_col, uint64_t n_dense, uint32_t K,
                                   const uint32_t* __restrict__ y_of_rank, uint32_t* __restrict__ cnt,
                                   uint64_t y_card, uint32_t part_rows, uint32_t parts,
-                                  const uint64_t* __restrict__ hz, uint32_t kw, uint32_t var_bits) {
+                                  const uint64_t* __restrict__ hz, uint32_t kw, uint32_t var_bits,
+                                  uint64_t row_base = 0 /* z-split: global id of row 0 */) {
   const uint32_t nvar = 1u << var_bits, vmask = nvar - 1;
   const uint32_t sl = threadIdx.x & 7;  // 8 lanes per row
   for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 8) + (threadIdx.x >> 3); i < n_dense;
        i += (uint64_t)gridDim.x * (blockDim.x / 8)) {
-    const uint64_t part = i / part_rows;
+    const uint64_t part = (row_base + i) / part_rows;
     const uint32_t zm = var_bits ? (uint32_t)(hz[i * kw] & vmask) : 0;
     const uint64_t e = dl_ptr[i + 1];
     for (uint64_t k = dl_ptr[i] + sl; k < e; k += 8) {
@@ -69,12 +70,12 @@ __global__ void cold_scatter_kernel(const uint64_t* __restrict__ dl_ptr,
                                     uint32_t* __restrict__ out, uint32_t ostride,
                                     uint64_t y_card, uint32_t part_rows, uint32_t parts,
                                     const uint64_t* __restrict__ hz, uint32_t kw,
-                                    uint32_t var_bits) {
+                                    uint32_t var_bits, uint64_t row_base = 0) {
   const uint32_t nvar = 1u << var_bits, vmask = nvar - 1;
   const uint32_t sl = threadIdx.x & 7;  // 8 lanes per row
   for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 8) + (threadIdx.x >> 3); i < n_dense;
        i += (uint64_t)gridDim.x * (blockDim.x / 8)) {
-    const uint64_t part = i / part_rows;
+    const uint64_t part = (row_base + i) / part_rows;
     const uint32_t zm = var_bits ? (uint32_t)(hz[i * kw] & vmask) : 0;
     const uint64_t e = dl_ptr[i + 1];
     for (uint64_t k = dl_ptr[i] + sl; k < e; k += 8) {
@@ -85,7 +86,7 @@ __global__ void cold_scatter_kernel(const uint64_t* __restrict__ dl_ptr,
         if ((zm & v) == 0) {
           const uint64_t key = ((uint64_t)v * parts + part) * y_card + y;
           const uint64_t pos = base[key] + atomicSub(&left[key], 1u) - 1u;
-          out[pos * ostride] = (uint32_t)i;
+          out[pos * ostride] = (uint32_t)(row_base + i);
         }
     }
   }

@@ -52,6 +52,12 @@ struct HotParams {
   uint32_t n_classes = 1;
   uint32_t plan_units = 0;
   uint32_t plan_on = 0;  // 1: units follow the plan (plan_units may be 0)
+  // z-split (zsplit.cuh): the long rows' list tails, gathered (sorted row
+  // ids, tail starts, ranks); null: the tails are read from dl_ptr / dl_col
+  const uint32_t* tail_rows = nullptr;
+  const uint64_t* tail_ptr = nullptr;
+  const uint32_t* tail_col = nullptr;
+  uint32_t n_tail = 0;
 };
 
 // Unit -> (batch, row range). Units are batch-major.
@@ -1239,13 +1245,22 @@ dense_hot_jt_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,
         const uint64_t i = cb + j;
         if (c > 32) {  // rare: more than 32 listed ranks; the tail is in the list
           const uint64_t row = kTrie ? perm[i] : i;
-          const uint64_t k1 = dl_ptr[row + 1];
-          uint64_t k = dl_ptr[row];
-          const uint32_t skip = __popc(top) + 32;
-          const uint64_t kend = k + skip + (c - 32);
-          k += skip;
-          for (uint64_t base = k; base < kend && base < k1; base += 32) {
-            const uint32_t mine = base + lane < kend ? dl_col[base + lane] : 0u;
+          const uint32_t* tl = dl_col;
+          uint64_t k;
+          if (p.tail_rows) {  // z-split: the gathered tails (sorted row ids)
+            uint32_t lo = 0, hi = p.n_tail;
+            while (hi - lo > 1) {
+              const uint32_t mid = (lo + hi) >> 1;
+              if (p.tail_rows[mid] <= row) lo = mid; else hi = mid;
+            }
+            k = p.tail_ptr[lo];
+            tl = p.tail_col;
+          } else {
+            k = dl_ptr[row] + __popc(top) + 32;
+          }
+          const uint64_t kend = k + (c - 32);
+          for (uint64_t base = k; base < kend; base += 32) {
+            const uint32_t mine = base + lane < kend ? tl[base + lane] : 0u;
             const uint32_t n = (uint32_t)((kend - base) < 32 ? (kend - base) : 32);
             for (uint32_t t = 0; t < n; ++t) {
               const uint32_t r = __shfl_sync(0xffffffffu, mine, t);

@@ -29,6 +29,7 @@
 #include "denseec.cuh"
 #include "denseec_hot.cuh"
 #include "denseec_cold.cuh"
+#include "zsplit.cuh"
 #include "denseec_tc.cuh"
 #include "io.cuh"
 #include "aggregate.cuh"
@@ -327,6 +328,14 @@ struct DenseInputs {
   // dS over all of S when the dense rows are every live z row: the dense rows
   // holding y are then simply dS(y) (no histogram over the dense lists)
   const uint32_t* dS_all = nullptr;
+  // z-split S side of a sharded job (zsplit.cuh): dl_ptr / dl_col / dl_z /
+  // row_sp / dnnz describe only this rank's dense rows, the global rows
+  // [row_lo, row_lo + n_dense_local) of n_dense; the S-side products are built
+  // for them and gathered over zx. Null zx: every row is local.
+  d3g::Exchange* zx = nullptr;
+  uint64_t row_lo = 0, n_dense_local = 0;
+  std::vector<uint64_t> rows_per_rank;
+  uint64_t x_card_job = 0, n_live_job = 0;
 };
 
 __global__ void gather_by_rank_kernel(const uint32_t* __restrict__ y_of_rank,
@@ -542,12 +551,16 @@ static uint32_t env_u32(const char* name, uint32_t dflt, uint32_t lo, uint32_t h
 void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g::Emit em,
                    KernelOut& out) {
   using namespace d3g;
-  if (in.n_dense == 0 || in.pos_hi <= in.pos_lo) return;
-  const uint64_t n_live = in.pos_hi - in.pos_lo;
+  // z-split: every rank takes part in the S-side gathers, live x or not
+  const bool zs = in.zx != nullptr;
+  if (in.n_dense == 0 || (!zs && in.pos_hi <= in.pos_lo)) return;
+  const uint64_t n_live = in.pos_hi > in.pos_lo ? in.pos_hi - in.pos_lo : 0;
   const uint32_t* xorder = in.xorder + in.pos_lo;
   const uint32_t groups = (uint32_t)((n_live + 127) / 128);
   const uint64_t D = in.n_dense, Y = in.y_card;
-  const uint64_t dnnz = in.dnnz != ~0ull ? in.dnnz : X.scalar(in.dl_ptr + D);
+  // this rank's dense rows (all of them unless z-split) and their global base
+  const uint64_t DL = zs ? in.n_dense_local : D, row_lo = zs ? in.row_lo : 0;
+  const uint64_t dnnz = in.dnnz != ~0ull ? in.dnnz : X.scalar(in.dl_ptr + DL);
   // choose K
   DBuf<uint32_t> cnt_rank;
   if (in.dS_all) {
@@ -559,6 +572,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     if (dnnz)
       D3G_LAUNCH(X, value_hist_kernel, grid_for(dnnz, 512, X.sm_count * 2), 512, 0, in.dl_col,
                  dnnz, cnt_rank.p, (uint32_t)Y);
+    if (zs) ex_allreduce(X, *in.zx, cnt_rank.p, Y, D3G_EX_SUM_U32);
   }
   // one read-back: K estimates, then the dense-row counts of ranks 0..6 (the
   // subset-table decision) and dR of ranks 0..3 (the cold variant bits)
@@ -569,7 +583,9 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   // the pivot-plan class counts (count-only) ride on the same read-back
   const bool piv_pre = mode == kModeCount && std::getenv("D3G_HOT") == nullptr &&
                        std::getenv("D3G_NO_SPLIT") == nullptr && Y >= 1;
-  const uint32_t n_batches_pre = (groups + 31) / 32;
+  // (z-split: from the job's live x, so every rank picks the same pivots)
+  const uint32_t n_batches_pre =
+      zs ? (uint32_t)((in.n_live_job + 4095) / 4096) : (groups + 31) / 32;
   const double units_pre = (double)n_batches_pre * (double)D;
   // measured: cfg5 (2.4e10 units) 2/3/4 pivots 153/135/132 ms; cfg2 (1e7)
   // 2.30/2.31/2.41 ms
@@ -582,15 +598,20 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   if (piv_pre) {
     cls = X.alloc<uint32_t>(n_live);
     pcnt = X.zeros<unsigned long long>(48);  // x[16] rows[16] sp[16]
-    D3G_LAUNCH(X, pivot_class_x_kernel, grid_for(n_live, 256), 256, 0, xorder, n_live, in.r_ptr,
-               in.r_col, in.y_of_rank, n_piv, cls.p, pcnt.p);
-    D3G_LAUNCH(X, pivot_class_rows_kernel, grid_for(D, 256), 256, 0, in.dl_ptr, in.dl_col, D,
-               n_piv, in.row_sp, pcnt.p + 16);
+    if (n_live)
+      D3G_LAUNCH(X, pivot_class_x_kernel, grid_for(n_live, 256), 256, 0, xorder, n_live, in.r_ptr,
+                 in.r_col, in.y_of_rank, n_piv, cls.p, pcnt.p);
+    if (DL)
+      D3G_LAUNCH(X, pivot_class_rows_kernel, grid_for(DL, 256), 256, 0, in.dl_ptr, in.dl_col, DL,
+                 n_piv, in.row_sp, pcnt.p + 16);
   }
   unsigned long long e[2 * kKCand + 11];
   X.defer(e, est.p, (2 * kKCand + 11) * 8);
   if (piv_pre) X.defer(c, pcnt.p, 48 * 8);
   X.sync();
+  // z-split: the dense-row class counts of the job (the x classes stay local)
+  if (zs && piv_pre)
+    ex_allreduce_host(X, *in.zx, reinterpret_cast<uint64_t*>(c + 16), 32, D3G_EX_SUM_U64);
   const unsigned long long* top_rank_rows = e + 2 * kKCand;   // [7]
   const unsigned long long* top_rank_dr = e + 2 * kKCand + 7;  // [4]
   static const uint32_t kv[kKCand] = {64, 128, 256, 512, 1024};
@@ -736,17 +757,47 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   DBuf<uint4> T = X.zeros<uint4>((uint64_t)n_batches * K * 32);
   DBuf<unsigned long long> hx = X.zeros<unsigned long long>(in.x_card * kw);
   DBuf<unsigned long long> hz = X.zeros<unsigned long long>(D * kw);
-  D3G_LAUNCH(X, hot_build_x_kernel, grid_for(n_live * 8, 256), 256, 0, xorder, n_live, in.r_ptr,
-             in.r_col, in.y_rank, K, kw, reinterpret_cast<uint32_t*>(T.p), hx.p);
-  D3G_LAUNCH(X, hot_build_z_kernel, grid_for(D * 8, 256), 256, 0, in.dl_ptr, in.dl_col, D, K, kw,
-             hz.p);
+  // z-split: this rank's rows' masks, gathered into hz (every rank's rows)
+  DBuf<unsigned long long> hz_loc;
+  unsigned long long* hzl = hz.p;
+  if (zs) {
+    hz_loc = X.zeros<unsigned long long>(DL * kw);
+    hzl = hz_loc.p;
+  }
+  if (n_live)
+    D3G_LAUNCH(X, hot_build_x_kernel, grid_for(n_live * 8, 256), 256, 0, xorder, n_live, in.r_ptr,
+               in.r_col, in.y_rank, K, kw, reinterpret_cast<uint32_t*>(T.p), hx.p);
+  if (DL)
+    D3G_LAUNCH(X, hot_build_z_kernel, grid_for(DL * 8, 256), 256, 0, in.dl_ptr, in.dl_col, DL, K,
+               kw, hzl);
+  if (zs) ex_allgatherv_dev(X, *in.zx, hzl, in.rows_per_rank, kw * 8, hz.p);
+  // z-split: the job's per-row z codes and folded-sparse flags
+  DBuf<uint32_t> dlz_g;
+  DBuf<uint8_t> rsp_g;
+  const uint32_t* dlz = in.dl_z;
+  const uint8_t* rsp = in.row_sp;
+  if (zs) {
+    dlz_g = X.alloc<uint32_t>(D);
+    ex_allgatherv_dev(X, *in.zx, in.dl_z, in.rows_per_rank, 4, dlz_g.p);
+    dlz = dlz_g.p;
+    if (in.row_sp) {
+      rsp_g = X.alloc<uint8_t>(D);
+      ex_allgatherv_dev(X, *in.zx, in.row_sp, in.rows_per_rank, 1, rsp_g.p);
+      rsp = rsp_g.p;
+    }
+  }
   // P2 setup, enqueued BEFORE the hot pass: the cold CSR's size is read back
   // while P1 runs (the host waits on a mark, not on the stream), so P2's
   // scatter and kernel queue behind P1 without an idle gap. With the
   // warp-bitmap kernel the dense rows are cut into `parts` ranges so that 24
   // warps per SM each hold a part_rows-bit bitmap; the cold CSR is keyed by
   // (variant, part, y).
-  const bool run_cold = e[best] > 0;
+  // the cold join of the K actually used (its estimate is exact: the job's dR
+  // and dense-row counts), so every rank of a z-split job agrees
+  int kidx = best;
+  for (int j = 0; j < kKCand; ++j)
+    if (kv[j] == K) kidx = j;
+  const bool run_cold = e[kidx] > 0;
   uint32_t parts = 1, part_rows = (uint32_t)(((D + 31) / 32) * 32);
   uint32_t var_bits = 0;
   uint64_t rows_key = 0, cnnz = 0;
@@ -763,27 +814,79 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     // top-rank variants of the cold CSR (only for the warp-bitmap kernel): one
     // bit per top rank that at least half of the live x contain (cfg2: ranks
     // 0-2; cfg4's flatter Zipf(0.8): none)
+    const uint64_t xc_job = zs ? in.x_card_job : in.x_card;  // the same bits on every rank
     if (cold_kernel_ok)
-      while (var_bits < 3 && var_bits < Y && 2ull * top_rank_dr[var_bits] >= in.x_card)
+      while (var_bits < 3 && var_bits < Y && 2ull * top_rank_dr[var_bits] >= xc_job)
         ++var_bits;
     if (cold_kernel_ok && std::getenv("D3G_VAR_BITS"))  // experiments: 0..4
       var_bits = (uint32_t)std::min<uint64_t>(env_u32("D3G_VAR_BITS", var_bits, 0, 4), Y);
     rows_key = ((uint64_t)1 << var_bits) * parts * Y;
     cc = X.zeros<uint32_t>(rows_key);
-    D3G_LAUNCH(X, cold_count_kernel, grid_for(D * 8, 256), 256, 0, in.dl_ptr, in.dl_col, D, K,
-               in.y_of_rank, cc.p, Y, part_rows, parts,
-               reinterpret_cast<const uint64_t*>(hz.p), kw, var_bits);
+    if (DL)
+      D3G_LAUNCH(X, cold_count_kernel, grid_for(DL * 8, 256), 256, 0, in.dl_ptr, in.dl_col, DL, K,
+                 in.y_of_rank, cc.p, Y, part_rows, parts,
+                 reinterpret_cast<const uint64_t*>(hzl), kw, var_bits, row_lo);
     cptr = X.alloc<uint64_t>(rows_key + 1);
     exclusive_scan<uint32_t>(X, cc.p, rows_key, cptr.p);
     X.defer(&cnnz, cptr.p + rows_key, 8);
     X.mark();
   }
+  // z-split: the cold CSR is built now, for this rank's rows, and merged with
+  // the other ranks' parts into the job's (variant, part, y)-major layout
+  DBuf<uint4> crec_g;
+  if (zs && run_cold) {
+    if (!cold_kernel_ok) throw d3g::Error(D3G_INTERNAL_ERROR, "z-split needs the cold kernels");
+    X.wait_mark();  // cnnz of this rank
+    const int N = in.zx->nranks;
+    DBuf<uint32_t> cnt_all = X.alloc<uint32_t>(rows_key * N);
+    ex_allgatherv_dev(X, *in.zx, cc.p, std::vector<uint64_t>(N, rows_key), 4, cnt_all.p);
+    DBuf<uint4> crec_l = X.alloc<uint4>(cnnz);
+    if (DL)
+      D3G_LAUNCH(X, cold_scatter_kernel, grid_for(DL * 8, 256), 256, 0, in.dl_ptr, in.dl_col, DL,
+                 K, in.y_of_rank, cptr.p, cc.p, reinterpret_cast<uint32_t*>(crec_l.p) + 3, 4u, Y,
+                 part_rows, parts, reinterpret_cast<const uint64_t*>(hzl), kw, var_bits, row_lo);
+    cc.reset();
+    if (cnnz)
+      D3G_LAUNCH(X, cold_rec_fill_kernel, grid_for(cnnz, 256), 256, 0, crec_l.p, cnnz,
+                 reinterpret_cast<const uint4*>(hz.p), rsp);
+    // the ranks' record counts, their parts gathered rank-major
+    uint64_t mine = cnnz;
+    std::vector<uint64_t> part_n(N);
+    ex_allgather(X, *in.zx, &mine, part_n.data(), 8);
+    std::vector<uint64_t> part_b(N, 0);
+    uint64_t tot = 0;
+    for (int q = 0; q < N; ++q) {
+      part_b[q] = tot;
+      tot += part_n[q];
+    }
+    DBuf<uint4> crec_all = X.alloc<uint4>(tot);
+    ex_allgatherv_dev(X, *in.zx, crec_l.p, part_n, 16, crec_all.p);
+    crec_l.reset();
+    // every rank's exclusive scan, the job's counts and their scan
+    DBuf<uint64_t> src_off = X.alloc<uint64_t>((rows_key + 1) * N);
+    for (int q = 0; q < N; ++q)
+      exclusive_scan<uint32_t>(X, cnt_all.p + (uint64_t)q * rows_key, rows_key,
+                               src_off.p + (uint64_t)q * (rows_key + 1));
+    DBuf<uint32_t> tcnt = X.alloc<uint32_t>(rows_key);
+    D3G_LAUNCH(X, sum_rows_u32_kernel, grid_for(rows_key, 256), 256, 0, cnt_all.p, rows_key, N,
+               tcnt.p);
+    exclusive_scan<uint32_t>(X, tcnt.p, rows_key, cptr.p);
+    tcnt.reset();
+    DBuf<uint64_t> pb = X.alloc<uint64_t>(N);
+    X.to_device(pb.p, part_b.data(), N);
+    crec_g = X.alloc<uint4>(tot);
+    D3G_LAUNCH(X, cold_merge_kernel, grid_for(rows_key * 32, 256), 256, 0, cnt_all.p, src_off.p,
+               pb.p, crec_all.p, cptr.p, rows_key, N, crec_g.p);
+    cnnz = tot;
+  }
   // P1: hot bit-sliced pass
+  DBuf<uint32_t> tail_rows_g, tail_col_g;  // z-split: the long rows' tails
+  DBuf<uint64_t> tail_ptr_g;
   HotParams hp{};
   hp.T = T.p;
   hp.hz = reinterpret_cast<const uint64_t*>(hz.p);
   hp.xorder = xorder;
-  hp.dl_z = in.dl_z;
+  hp.dl_z = dlz;
   hp.n_live = n_live;
   hp.n_dense = D;
   hp.groups = groups;
@@ -794,7 +897,8 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   // hot 17.6 -> 16.8 ms)
   const uint64_t zc_per_sm = env_u32("D3G_ZCHUNKS_PER_SM", 16, 1, 64);
   hp.z_chunks = std::max<uint32_t>(1, (uint32_t)std::min<uint64_t>(
-      (D + 255) / 256, ((uint64_t)X.sm_count * zc_per_sm + n_batches - 1) / n_batches));
+      (D + 255) / 256,
+      ((uint64_t)X.sm_count * zc_per_sm + n_batches - 1) / std::max<uint32_t>(n_batches, 1)));
   const bool plan = !unit_off_h.empty();
   DBuf<uint32_t> unit_off_d;
   DBuf<uint8_t> batch_kind_d;
@@ -858,7 +962,8 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     for (uint32_t r = 0; r < kTabBits; ++r) top_per_row += (double)top_rank_rows[r] / (double)D;
     const std::string hv = hot_impl ? hot_impl : "";
     const bool force_tab = hv == "tab" || hv == "trie";
-    const bool tab = plan ||
+    // (z-split: the job-wide plan decision, so every rank's records agree)
+    const bool tab = (zs ? try_plan : plan) ||
                      K > kTabBits && tsm <= (size_t)dense_smem_bytes(X) &&
                      !(hot_impl && std::string(hot_impl) == "rec") &&
                      (force_tab || top_per_row >= 1.5);
@@ -873,17 +978,78 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     // they measured slower: cfg4 23.2 vs 17.2 ms)
     jt_trie = jt && ((tab && hv != "jt") || hv == "jttrie");
     trie = jt_trie || (tab && hv == "trie");
-    D3G_LAUNCH(X, hot_rec_kernel, grid_for(D, 256), 256, 0, in.dl_ptr, in.dl_col, D, K,
-               tab ? kTabBits : 0u, reinterpret_cast<uint8_t*>(rec.p), rcnt.p, in.row_sp,
-               jt && tab ? kTabBits : 0u);
+    if (!zs) {
+      D3G_LAUNCH(X, hot_rec_kernel, grid_for(D, 256), 256, 0, in.dl_ptr, in.dl_col, D, K,
+                 tab ? kTabBits : 0u, reinterpret_cast<uint8_t*>(rec.p), rcnt.p, in.row_sp,
+                 jt && tab ? kTabBits : 0u);
+    } else {
+      // z-split: this rank's rows' records and count words, gathered; the long
+      // rows' list tails (past the record's 32 listed ranks) gathered apart
+      DBuf<uint4> rec_l = X.zeros<uint4>(2 * DL);
+      DBuf<uint32_t> rcnt_l = X.alloc<uint32_t>(DL);
+      if (DL)
+        D3G_LAUNCH(X, hot_rec_kernel, grid_for(DL, 256), 256, 0, in.dl_ptr, in.dl_col, DL, K,
+                   tab ? kTabBits : 0u, reinterpret_cast<uint8_t*>(rec_l.p), rcnt_l.p, in.row_sp,
+                   jt && tab ? kTabBits : 0u);
+      std::vector<uint64_t> rr2(in.rows_per_rank);
+      for (auto& v : rr2) v *= 2;
+      ex_allgatherv_dev(X, *in.zx, rec_l.p, rr2, 16, rec.p);
+      ex_allgatherv_dev(X, *in.zx, rcnt_l.p, in.rows_per_rank, 4, rcnt.p);
+      const int N = in.zx->nranks;
+      DBuf<uint32_t> tlen = X.alloc<uint32_t>(DL), ist = X.alloc<uint32_t>(DL);
+      DBuf<uint64_t> toff = X.alloc<uint64_t>(DL + 1), tpos = X.alloc<uint64_t>(DL + 1);
+      if (DL)
+        D3G_LAUNCH(X, tail_len_kernel, grid_for(DL, 256), 256, 0, rcnt_l.p, DL, tlen.p, ist.p);
+      exclusive_scan<uint32_t>(X, tlen.p, DL, toff.p);
+      exclusive_scan<uint32_t>(X, ist.p, DL, tpos.p);
+      uint64_t tn[2] = {0, 0};  // tail rows, tail ranks
+      X.defer(&tn[0], tpos.p + DL, 8);
+      X.defer(&tn[1], toff.p + DL, 8);
+      X.sync();
+      DBuf<uint32_t> t_rows = X.alloc<uint32_t>(tn[0]), t_col = X.alloc<uint32_t>(tn[1]);
+      DBuf<uint64_t> t_ptr = X.alloc<uint64_t>(tn[0]);
+      if (DL && tn[0])
+        D3G_LAUNCH(X, tail_fill_kernel, grid_for(DL, 256), 256, 0, rcnt_l.p, DL, ist.p, tpos.p,
+                   toff.p, in.dl_ptr, in.dl_col, row_lo, t_rows.p, t_ptr.p, t_col.p);
+      std::vector<uint64_t> all_tn(2 * N);
+      ex_allgather(X, *in.zx, tn, all_tn.data(), 16);
+      std::vector<uint64_t> nrows(N), ncols(N), r0(N + 1, 0), c0(N + 1, 0);
+      for (int q = 0; q < N; ++q) {
+        nrows[q] = all_tn[2 * q];
+        ncols[q] = all_tn[2 * q + 1];
+        r0[q + 1] = r0[q] + nrows[q];
+        c0[q + 1] = c0[q] + ncols[q];
+      }
+      if (r0[N]) {
+        tail_rows_g = X.alloc<uint32_t>(r0[N]);
+        tail_ptr_g = X.alloc<uint64_t>(r0[N]);
+        tail_col_g = X.alloc<uint32_t>(c0[N]);
+        ex_allgatherv_dev(X, *in.zx, t_rows.p, nrows, 4, tail_rows_g.p);
+        ex_allgatherv_dev(X, *in.zx, t_ptr.p, nrows, 8, tail_ptr_g.p);
+        ex_allgatherv_dev(X, *in.zx, t_col.p, ncols, 4, tail_col_g.p);
+        DBuf<uint64_t> dr0 = X.alloc<uint64_t>(N + 1), dc0 = X.alloc<uint64_t>(N + 1);
+        X.to_device(dr0.p, r0.data(), N + 1);
+        X.to_device(dc0.p, c0.data(), N + 1);
+        D3G_LAUNCH(X, tail_rebase_kernel, grid_for(r0[N], 256), 256, 0, tail_ptr_g.p, dr0.p, dc0.p,
+                   N);
+      }
+      hp.tail_rows = tail_rows_g.p;
+      hp.tail_ptr = tail_ptr_g.p;
+      hp.tail_col = tail_col_g.p;
+      hp.n_tail = (uint32_t)r0[N];
+      // no long rows anywhere: a non-null table keeps the kernel off the
+      // (local) lists; with no row past 32 listed ranks it is never read
+      if (!hp.tail_rows) hp.tail_rows = rcnt.p;
+    }
     // prefix-shared records: rows sorted by (subset, r1, r2), records gathered
     DBuf<uint32_t> perm;
     if (trie) {
       DBuf<uint64_t> key = X.alloc<uint64_t>(D);
       perm = X.alloc<uint32_t>(D);
       D3G_LAUNCH(X, trie_key_kernel, grid_for(D, 256), 256, 0, reinterpret_cast<const uint8_t*>(rec.p),
-                 rcnt.p, D, key.p, perm.p, jt ? 1u : 1u - kTabBits, plan ? n_piv : 0u);
-      radix_sort(X, key.p, perm.p, D, 25 + (plan ? (int)n_piv : 0), true);
+                 rcnt.p, D, key.p, perm.p, jt ? 1u : 1u - kTabBits,
+                 (zs ? try_plan : plan) ? n_piv : 0u);
+      radix_sort(X, key.p, perm.p, D, 25 + ((zs ? try_plan : plan) ? (int)n_piv : 0), true);
       DBuf<uint4> rec_s = X.alloc<uint4>(2 * D);
       DBuf<uint32_t> rcnt_s = X.alloc<uint32_t>(D);
       D3G_LAUNCH(X, trie_gather_kernel, grid_for(D, 256), 256, 0, rec.p, rcnt.p, key.p, perm.p, D,
@@ -970,20 +1136,25 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     // cold kernels: 16-byte records {hz word 0, fold of words 1-3, row}; the
     // scatter writes the row fields, one coalesced pass fills the signatures.
     // D3G_COLD=tiers: a plain column of row ids for the SparseBMM tiers.
+    // (z-split: built and merged before the hot pass)
     DBuf<uint32_t> ccol;
     DBuf<uint4> crec;
     if (cold_kernel_ok && D >= kRowMask)
       throw d3g::Error(D3G_INTERNAL_ERROR, "cold records hold row ids below 2^31 - 1");
-    if (cold_kernel_ok) crec = X.alloc<uint4>(cnnz);
-    else ccol = X.alloc<uint32_t>(cnnz);
-    uint32_t* cout = cold_kernel_ok ? reinterpret_cast<uint32_t*>(crec.p) + 3 : ccol.p;
-    D3G_LAUNCH(X, cold_scatter_kernel, grid_for(D * 8, 256), 256, 0, in.dl_ptr, in.dl_col, D, K,
-               in.y_of_rank, cptr.p, cc.p, cout, cold_kernel_ok ? 4u : 1u, Y, part_rows, parts,
-               reinterpret_cast<const uint64_t*>(hz.p), kw, var_bits);
-    cc.reset();
     const uint4* hz4 = reinterpret_cast<const uint4*>(hz.p);
-    if (cold_kernel_ok && cnnz)
-      D3G_LAUNCH(X, cold_rec_fill_kernel, grid_for(cnnz, 256), 256, 0, crec.p, cnnz, hz4, in.row_sp);
+    if (zs) {
+      crec = std::move(crec_g);
+    } else {
+      if (cold_kernel_ok) crec = X.alloc<uint4>(cnnz);
+      else ccol = X.alloc<uint32_t>(cnnz);
+      uint32_t* cout = cold_kernel_ok ? reinterpret_cast<uint32_t*>(crec.p) + 3 : ccol.p;
+      D3G_LAUNCH(X, cold_scatter_kernel, grid_for(D * 8, 256), 256, 0, in.dl_ptr, in.dl_col, D, K,
+                 in.y_of_rank, cptr.p, cc.p, cout, cold_kernel_ok ? 4u : 1u, Y, part_rows, parts,
+                 reinterpret_cast<const uint64_t*>(hz.p), kw, var_bits);
+      cc.reset();
+      if (cold_kernel_ok && cnnz)
+        D3G_LAUNCH(X, cold_rec_fill_kernel, grid_for(cnnz, 256), 256, 0, crec.p, cnnz, hz4, rsp);
+    }
     if (cold_kernel_ok) {
       DBuf<unsigned int> next = X.zeros<unsigned int>(1);
       Tally* tc = tallies.p + 1;
@@ -1001,7 +1172,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
           D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
           D3G_LAUNCH(X, kfn, (unsigned)X.sm_count * (D3G_CH_BITS <= 10 ? D3G_CH_CTAS : 3), kCHWarps * 32, hsm,
                      xorder, n_live, in.r_ptr, in.r_col, cptr.p, crec.p, hz4,
-                     reinterpret_cast<const uint4*>(hx.p), Y, var_bits, in.dl_z, dec, em, next.p,
+                     reinterpret_cast<const uint4*>(hx.p), Y, var_bits, dlz, dec, em, next.p,
                      over_x.p, over_n.p, tc, cnt_sp,
                      env_u32("D3G_COLD_HASH_MAX", kCHMax, 1, kCHMax),
                      env_u32("D3G_COLD_ROUTE", D3G_COLD_ROUTE, 1, 0xffffffffu), cand);
@@ -1024,7 +1195,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
             D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCCSmem));
             D3G_LAUNCH(X, kfn, std::min<unsigned>(n_over, (unsigned)X.sm_count * kCCPerSm), kCCThreads,
                        kCCSmem, over_x.p, over_n.p, in.r_ptr, in.r_col, cptr.p, crec.p, hz4,
-                       reinterpret_cast<const uint4*>(hx.p), Y, var_bits, in.dl_z, dec, em,
+                       reinterpret_cast<const uint4*>(hx.p), Y, var_bits, dlz, dec, em,
                        over2_x.p, over2_n.p, env_u32("D3G_COLD_CTA_MAX", kCCMax, 1, kCCMax), tc,
                        cnt_sp, cand);
           });
@@ -1042,7 +1213,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
           with_mode(mode, [&](auto M) {
             D3G_LAUNCH(X, dense_cold_overflow_kernel<decltype(M)::value>, og, kOvThreads, kOvSmem, ox,
                        on, in.r_ptr, in.r_col, cptr.p, crec.p, hz4,
-                       reinterpret_cast<const uint4*>(hx.p), Y, var_bits, in.dl_z, gbm.p, words,
+                       reinterpret_cast<const uint4*>(hx.p), Y, var_bits, dlz, gbm.p, words,
                        dec, em, tc, cnt_sp, touched.p, cand);
           });
         }
@@ -1055,7 +1226,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
             D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
           D3G_LAUNCH(X, kfn, (unsigned)X.sm_count * cold_ctas, kColdWarps * 32, csm, xorder, n_live,
                      in.r_ptr, in.r_col, cptr.p, crec.p, hz4, reinterpret_cast<const uint4*>(hx.p), Y,
-                     parts, part_rows, var_bits, in.dl_z, dec, em, next.p, tc, cnt_sp, cand);
+                     parts, part_rows, var_bits, dlz, dec, em, next.p, tc, cnt_sp, cand);
         });
       }
       D3G_CUDA(cudaEventRecord(ev3, X.stream));
@@ -1071,7 +1242,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   const uint64_t direct = plan_direct;
   out.count_sp = th[3].count + plan_direct_sp;
   const Tally& h = th[0];
-  if (cold_kernel_ok && e[best] > 0) {
+  if (cold_kernel_ok && run_cold) {
     cold.count = th[1].count;
     cold.sum = th[1].sum;
     cold.xr = th[1].xr;
@@ -1256,11 +1427,13 @@ struct RowSel {
 // y codes ordered by dR descending (ties in any order): a counting sort when
 // the value range is small, else the LSD radix sort.
 void order_y_by_degree(Ctx& X, const uint32_t* dR, uint64_t y_card, uint64_t max_dr,
-                       DBuf<uint32_t>& order) {
+                       DBuf<uint32_t>& order, bool deterministic = false) {
   using namespace d3g;
   order = X.alloc<uint32_t>(y_card);
   if (y_card == 0) return;
-  if (max_dr < (1ull << 20)) {
+  // (the counting scatter orders ties as its atomics land; ranks of a z-split
+  // job must agree on the ranking: the stable radix sort then)
+  if (max_dr < (1ull << 20) && !deterministic) {
     DBuf<uint32_t> cnt = X.zeros<uint32_t>(max_dr + 1);
     D3G_LAUNCH(X, desc_hist_kernel, grid_for(y_card, 256), 256, 0, dR, y_card, (uint32_t)max_dr,
                cnt.p);
@@ -1287,13 +1460,14 @@ void build_dense_layout(Ctx& X, const d3g::DeviceCsr& rx, uint64_t max_mx,
                         const uint32_t* dR, DenseLayout& L, uint64_t xa = 0,
                         uint64_t xb = ~0ull, uint64_t dnnz_hint = ~0ull,
                         const RowSel* sel = nullptr, uint64_t z_rows = 0,
-                        bool stable_x = false, uint64_t dr_bound = 0) {
+                        bool stable_x = false, uint64_t dr_bound = 0, uint64_t z_base = 0,
+                        bool det_rank = false) {
   using namespace d3g;
   // y ranked by dR descending: hottest witnesses first. dR(y) <= x_card
   // bounds the key without a device round trip (sharded: dR is the job's,
   // bounded by the job's x card, dr_bound).
   const uint64_t max_dr = std::max<uint64_t>(rx.n_rows, dr_bound);
-  order_y_by_degree(X, dR, y_card, max_dr, L.y_of_rank);
+  order_y_by_degree(X, dR, y_card, max_dr, L.y_of_rank, det_rank);
   L.y_rank = X.alloc<uint32_t>(y_card);
   D3G_LAUNCH(X, scatter_rank_kernel, grid_for(y_card, 256), 256, 0, L.y_of_rank.p, y_card,
              L.y_rank.p);
@@ -1334,6 +1508,9 @@ void build_dense_layout(Ctx& X, const d3g::DeviceCsr& rx, uint64_t max_mx,
     segmented_sort(X, L.dl_col.p, L.dl_ptr.p, n_dense, /*unique=*/false, kept.p, max_mz);
   }
   if (z_of_row) D3G_LAUNCH(X, map_through_kernel, grid_for(n_dense, 256), 256, 0, rows.p, n_dense, z_of_row);
+  // z-split: the rows are this rank's z codes counted from z_base
+  if (z_base && n_dense)
+    D3G_LAUNCH(X, add_offset_kernel, grid_for(n_dense, 256), 256, 0, rows.p, n_dense, (uint32_t)z_base);
   L.dl_z = std::move(rows);
   // live x ordered by m_x descending, cut into 128-x groups
   // (restricted to x codes in [xa, xb) when the caller asked for an x range)
@@ -1891,12 +2068,16 @@ struct DegreeStats {
   // these are the job's (the f2 inputs). Empty / 0 when not sharded.
   std::vector<uint64_t> hmx_job;
   uint64_t x_live_job = 0;
+  // z-split (this rank built S-by-z for its z range only): hmz, wz, dS and
+  // max_mz above are the job's; hmz_local orders this rank's rows
+  std::vector<uint64_t> hmz_local;
+  uint64_t z_live_job = 0;
   const std::vector<uint64_t>& hmx_f2() const { return hmx_job.empty() ? hmx : hmx_job; }
 };
 
 void degree_stats(Ctx& X, const d3g::DeviceCsr& rx, const d3g::DeviceCsr& sz_csr,
                   uint64_t y_card, d3g_report* rep, DegreeStats& G, bool same = false,
-                  d3g::Exchange* E = nullptr, uint64_t x_card_job = 0) {
+                  d3g::Exchange* E = nullptr, uint64_t x_card_job = 0, bool zsplit = false) {
   using namespace d3g;
   const bool dist = E && E->active();
   const uint64_t x_card = rx.n_rows, z_card = sz_csr.n_rows;
@@ -1918,6 +2099,7 @@ void degree_stats(Ctx& X, const d3g::DeviceCsr& rx, const d3g::DeviceCsr& sz_csr
     G.x_live = scal[1];
     G.max_mz = scal[2];
   }
+  if (zsplit) ex_allreduce_host(X, *E, &G.max_mz, 1, D3G_EX_MAX_U64);  // size the job's histogram
   rep->x_live = G.x_live;
   // one buffer, one read-back: [m_x histogram | m_z histogram | wz | OUT_J partials]
   const unsigned gb = grid_for(y_card, 1024, 296);
@@ -1947,8 +2129,9 @@ void degree_stats(Ctx& X, const d3g::DeviceCsr& rx, const d3g::DeviceCsr& sz_csr
     D3G_LAUNCH(X, value_hist_kernel, grid_for(sz_csr.nnz, 512, X.sm_count * 2), 512, 0, sz_csr.col.p, sz_csr.nnz,
                G.dS.p, (uint32_t)y_card);
   // sharded: dR(y) of the whole job (the y ranking, OUT_J and the per-degree
-  // join sizes below all read it)
+  // join sizes below all read it); z-split: dS(y) of the whole job too
   if (dist) ex_allreduce(X, *E, G.dR.p, y_card, D3G_EX_SUM_U32);
+  if (zsplit) ex_allreduce(X, *E, G.dS.p, y_card, D3G_EX_SUM_U32);
   if (y_card) D3G_LAUNCH(X, outj_kernel, gb, 1024, 0, G.dR.p, G.dS.p, y_card, parts_p);
   if (z_card)
     D3G_LAUNCH(X, row_join_hist_kernel, grid_for(z_card * 8, 256), 256, 0, sz_csr.row_ptr.p,
@@ -1962,6 +2145,18 @@ void degree_stats(Ctx& X, const d3g::DeviceCsr& rx, const d3g::DeviceCsr& sz_csr
     G.hmz.assign(hb.begin() + (G.max_mx + 1), hb.begin() + (G.max_mx + 1) + (G.max_mz + 1));
   G.wz.assign(hb.begin() + (G.max_mx + 1) + (G.max_mz + 1),
               hb.begin() + (G.max_mx + 1) + 2 * (G.max_mz + 1));
+  if (zsplit) {
+    // the job's m_z histogram and per-degree join sizes (this rank's rows
+    // keep their own histogram for the degree order of its layout)
+    G.hmz_local = G.hmz;
+    std::vector<uint64_t> v(2 * (G.max_mz + 1));
+    std::copy(G.hmz.begin(), G.hmz.end(), v.begin());
+    std::copy(G.wz.begin(), G.wz.end(), v.begin() + (G.max_mz + 1));
+    ex_allreduce_host(X, *E, v.data(), v.size(), D3G_EX_SUM_U64);
+    G.hmz.assign(v.begin(), v.begin() + (G.max_mz + 1));
+    G.wz.assign(v.begin() + (G.max_mz + 1), v.end());
+    for (uint64_t m = 1; m <= G.max_mz; ++m) G.z_live_job += G.hmz[m];
+  }
   const unsigned long long* hp = hb.data() + (G.max_mx + 1) + 2 * (G.max_mz + 1);
   unsigned __int128 acc = 0;
   for (unsigned i = 0; i < gb; ++i) acc += ((unsigned __int128)hp[2 * i + 1] << 64) | hp[2 * i];
@@ -2000,9 +2195,9 @@ struct Split {
 void f2_split(Ctx& X, const d3g::DeviceCsr& sz_csr, const DegreeStats& G, uint64_t x_card,
               uint64_t y_card, const d3g_consts* c, int pforce, d3g_report* rep, Split& P,
               DBuf<uint64_t>* pd_out = nullptr, DBuf<uint64_t>* psp_out = nullptr,
-              bool flags = true) {
+              bool flags = true, uint64_t z_card_job = ~0ull) {
   using namespace d3g;
-  const uint64_t z_card = sz_csr.n_rows;
+  const uint64_t z_card = z_card_job != ~0ull ? z_card_job : sz_csr.n_rows;
   P.table.assign(G.max_mz + 1, 0);
   std::vector<uint8_t>& table = P.table;
   uint64_t evals = 0;
@@ -2192,6 +2387,7 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   X.syncs = 0;
   X.d2h_bytes = 0;
   X.budget = o->memory_budget_bytes ? o->memory_budget_bytes : (3ull << 30);
+  if (E) E->reset_stats();
   uint64_t base_live = X.live_bytes;
   X.peak_bytes = X.live_bytes;
   Timer T(X);
@@ -2321,22 +2517,44 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
 
   // 5. CSR (build_csr, relation.cpp:206-258). A self-join (S identical to R)
   // maps both sides identically, so S-by-z is R-by-x: built once.
+  // A sharded job splits the S side by z (the z-split, zsplit.cuh): rank q
+  // builds S-by-z for the z codes [z_lo, z_hi) only; the statistics are
+  // all-reduced and the dense-row products gathered (run_dense_hot). It falls
+  // back to the whole S-by-z when the sparse side needs the SparseBMM tiers
+  // or a layout of its own (decided after the f2 split).
   DeviceCsr rx, sz_csr;
   build_csr_device(X, M.r_x, M.r_y, kept, x_card, y_card, rx);
   const bool same_csr = self_join && kept == NR && x_card == z_card;
-  if (same_csr)
+  const bool zsplit_try = dist && !classical && !o->collect_counters &&
+                          std::getenv("D3G_NO_ZSPLIT") == nullptr &&
+                          std::getenv("D3G_HOT") == nullptr && std::getenv("D3G_COLD") == nullptr &&
+                          std::getenv("D3G_DENSE") == nullptr && z_card < (1ull << 31);
+  uint64_t z_lo = 0, z_hi = z_card;
+  if (zsplit_try) {
+    z_lo = z_card * (uint64_t)E->rank / (uint64_t)E->nranks;
+    z_hi = z_card * (uint64_t)(E->rank + 1) / (uint64_t)E->nranks;
+    DBuf<uint32_t> zs_z = X.alloc<uint32_t>(NS), zs_y = X.alloc<uint32_t>(NS);
+    DBuf<unsigned long long> cur = X.zeros<unsigned long long>(1);
+    if (NS)
+      D3G_LAUNCH(X, zrange_compact_kernel, grid_for(NS, 256, X.sm_count * 8), 256, 0, M.s_z,
+                 M.s_y, NS, (uint32_t)z_lo, (uint32_t)z_hi, zs_z.p, zs_y.p, cur.p);
+    const uint64_t n_loc = X.scalar(cur.p);
+    build_csr_device(X, zs_z.p, zs_y.p, n_loc, z_hi - z_lo, y_card, sz_csr);
+  } else if (same_csr) {
     view_csr(rx, sz_csr);  // declared after rx: released first
-  else
+  } else {
     build_csr_device(X, M.s_z, M.s_y, NS, z_card, y_card, sz_csr);
-  M.release_codes();
+  }
+  if (!zsplit_try) M.release_codes();  // (z-split: kept for the fallback)
   rep->r_nnz = rx.nnz;
   rep->s_nnz = sz_csr.nnz;
   if (dist) ex_allreduce_host(X, *E, &rep->r_nnz, 1, D3G_EX_SUM_U64);
+  if (zsplit_try) ex_allreduce_host(X, *E, &rep->s_nnz, 1, D3G_EX_SUM_U64);
   T.mark();  // 4
 
   // 6. degree statistics (compute_degree_stats, costmodel.cpp:425-438)
   DegreeStats G;
-  degree_stats(X, rx, sz_csr, y_card, rep, G, same_csr, E, x_card_job);
+  degree_stats(X, rx, sz_csr, y_card, rep, G, same_csr, E, x_card_job, zsplit_try);
   const uint64_t max_mx = G.max_mx, x_live = G.x_live, max_mz = G.max_mz;
   const std::vector<uint64_t>& hmx = G.hmx;
   DBuf<uint32_t>& dR = G.dR;
@@ -2348,7 +2566,7 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
                                                   : D3G_HYBRID;
   Split P;
   f2_split(X, sz_csr, G, x_card_job, y_card, c, pforce, rep, P, nullptr, nullptr,
-           /*flags=*/false);
+           /*flags=*/false, z_card);
   const uint64_t n_dense = P.n_dense, n_sparse = P.n_sparse;
   rep->sparse_nnz = P.sparse_nnz;  // known on the host (m_z histogram)
   // optional x-code restriction of the kernels (opts x_code_lo/hi)
@@ -2378,6 +2596,17 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
                     std::getenv("D3G_NO_FOLD") == nullptr;
   const bool sparse_hot = heavy_sparse && !fold && n_sparse > 8192;
   const bool tiers = !fold && !sparse_hot;  // the SparseBMM tiers answer the sparse side
+  // the z-split holds when the dense layout (with any folded sparse rows) is
+  // all the S side there is; else every rank builds the whole S-by-z now
+  const bool zsplit = zsplit_try && n_dense > 0 && (fold || n_sparse == 0) &&
+                      G.x_live_job > 0;
+  if (zsplit_try && !zsplit) {
+    DeviceCsr full;
+    build_csr_device(X, M.s_z, M.s_y, NS, z_card, y_card, full);
+    sz_csr = std::move(full);
+  }
+  M.release_codes();
+  rep->zsplit = zsplit ? 1 : 0;
   // the sparse z as a compact id list, and the y-major CSR over those ids
   // (partition.cpp:59-78), only when the tiers run
   DBuf<uint32_t> sparse_ids;
@@ -2409,11 +2638,32 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   // the f2 table and ordered by degree in one counting scatter
   DenseLayout L;
   DBuf<uint8_t> row_sp;
-  if (n_dense > 0 && x_live > 0) {
-    RowSel sel{&G.hmz, P.dtable.p, &P.table, fold ? 0 : 1, fold ? &row_sp : nullptr};
+  // (z-split: this rank's z rows, counted from z_lo; every rank builds its
+  // part, live x or not: the gathers in run_dense_hot take all of them)
+  if (n_dense > 0 && (zsplit || x_live > 0)) {
+    RowSel sel{zsplit ? &G.hmz_local : &G.hmz, P.dtable.p, &P.table, fold ? 0 : 1,
+               fold ? &row_sp : nullptr};
     build_dense_layout(X, rx, max_mx, hmx, sz_csr.row_ptr.p, sz_csr.col.p, nullptr, 0, max_mz,
-                       nullptr, y_card, dR.p, L, xa, xb, ~0ull, &sel, z_card, shard_count > 1,
-                       x_card_job);
+                       nullptr, y_card, dR.p, L, xa, xb, ~0ull, &sel, sz_csr.n_rows,
+                       shard_count > 1, x_card_job, zsplit ? z_lo : 0, zsplit);
+  }
+  // z-split: the global dense rows are the ranks' blocks in rank order
+  std::vector<uint64_t> rows_per_rank;
+  uint64_t row_lo = 0, rows_job = 0;
+  if (zsplit) {
+    rows_per_rank.assign(E->nranks, 0);
+    uint64_t mine = L.n_dense;
+    ex_allgather(X, *E, &mine, rows_per_rank.data(), 8);
+    uint64_t tot = 0;
+    for (int q = 0; q < E->nranks; ++q) {
+      if (q == E->rank) row_lo = tot;
+      tot += rows_per_rank[q];
+    }
+    // the layout's rows: the dense z, plus the sparse z folded into it
+    const uint64_t want = fold ? n_dense + n_sparse : n_dense;
+    if (tot != want) throw CudaError("z-split: layout rows " + std::to_string(tot) +
+                                     " != the f2 split's " + std::to_string(want));
+    rows_job = tot;
   }
   DenseLayout Ls;
   if (sparse_hot && x_live > 0) {
@@ -2476,6 +2726,13 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
       direct_cap = bound;
     }
   }
+  if (zsplit && materialize) {
+    // the ranks run the same kernel passes (one emitting pass, or count then
+    // emit): the z-split's gathers pair up only if they agree
+    uint64_t no_direct = direct ? 0 : 1;
+    ex_allreduce_host(X, *E, &no_direct, 1, D3G_EX_MAX_U64);
+    direct = no_direct == 0;
+  }
   DBuf<uint32_t> dex, dez;
   DBuf<unsigned long long> dcur;
   Emit em_run = no_emit;
@@ -2501,10 +2758,19 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   T.mark();  // 7
   uint64_t pos_lo = L.n_live * shard_index / shard_count,
            pos_hi = L.n_live * (shard_index + 1) / shard_count;
+  const uint64_t live_z = zsplit ? G.z_live_job : sz_csr.live_rows;
   DenseInputs di{L.xorder.p, L.n_live, rx.row_ptr.p, rx.col.p, L.y_rank.p, y_card, L.dl_ptr.p,
-                 L.dl_col.p, L.dl_z.p, L.n_dense, L.max_group_nnz, pos_lo, pos_hi,
-                 L.y_of_rank.p, dR.p, x_card, x_lo, x_hi, L.dnnz, row_sp.p,
-                 L.n_dense == sz_csr.live_rows ? G.dS.p : nullptr};
+                 L.dl_col.p, L.dl_z.p, zsplit ? rows_job : L.n_dense, L.max_group_nnz, pos_lo,
+                 pos_hi, L.y_of_rank.p, dR.p, x_card, x_lo, x_hi, L.dnnz, row_sp.p,
+                 (zsplit ? rows_job : L.n_dense) == live_z ? G.dS.p : nullptr};
+  if (zsplit) {
+    di.zx = E;
+    di.row_lo = row_lo;
+    di.n_dense_local = L.n_dense;
+    di.rows_per_rank = rows_per_rank;
+    di.x_card_job = x_card_job;
+    di.n_live_job = G.x_live_job;
+  }
   run_dense(X, di, dec, kmode, em_run, kd);
   T.mark();  // 8
   if (fold) {  // the folded sparse rows' pairs, counted apart inside the engine
@@ -2607,6 +2873,11 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
   rep->peak_bytes = X.peak_bytes - base_live;
   rep->gpu_launches = X.launches;
   rep->d2h_bytes += X.d2h_bytes;
+  if (E) {
+    rep->exchange_calls = E->calls;
+    rep->exchange_bus_bytes = E->bus_bytes;
+    rep->ms_exchange_host = E->host_ms;
+  }
   if (std::getenv("D3G_TRACE"))
     std::fprintf(stderr, "[join_project] %llu launches, %llu host round trips\n",
                  (unsigned long long)X.launches, (unsigned long long)X.syncs);

@@ -23,6 +23,8 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <chrono>
+
 #include "common.cuh"
 
 namespace d3g {
@@ -74,6 +76,16 @@ struct Exchange {
   ncclComm_t comm = nullptr;
   d3g_exchange_fn host_fn = nullptr;
   void* host_user = nullptr;
+  // accounting of the current call: collectives, bytes a ring collective
+  // moves per rank over the links (all-reduce 2 (N-1)/N B, all-gather the
+  // other ranks' parts), and the host time of host-staged collectives (the
+  // one-GPU shard projection replaces it by an NVLink estimate)
+  uint64_t calls = 0, bus_bytes = 0;
+  double host_ms = 0;
+  void reset_stats() {
+    calls = bus_bytes = 0;
+    host_ms = 0;
+  }
   bool active() const { return nranks > 1 || comm != nullptr || host_fn != nullptr; }
   ~Exchange() {
     if (comm) nccl().comm_destroy(comm);
@@ -82,10 +94,28 @@ struct Exchange {
 
 inline size_t ex_elem_bytes(int op) { return op == D3G_EX_SUM_U32 ? 4 : op == D3G_EX_GATHER ? 1 : 8; }
 
+// Host-time bracket of a host-staged collective: the stream is drained first
+// (so earlier kernels are not counted) and after (the upload is counted).
+struct ExHostTimer {
+  Ctx& X;
+  Exchange& E;
+  std::chrono::steady_clock::time_point t0;
+  ExHostTimer(Ctx& x, Exchange& e) : X(x), E(e) {
+    X.sync();
+    t0 = std::chrono::steady_clock::now();
+  }
+  ~ExHostTimer() {
+    cudaStreamSynchronize(X.stream);
+    E.host_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
+};
+
 // In-place collective over a device buffer of `count` elements (op's type):
 // SUM_U64 / SUM_U32 / MAX_U64. Stream-ordered on X.stream.
 inline void ex_allreduce(Ctx& X, Exchange& E, void* dbuf, uint64_t count, int op) {
   if (count == 0 || !E.active()) return;
+  ++E.calls;
+  E.bus_bytes += 2 * count * ex_elem_bytes(op) * (E.nranks - 1) / std::max(E.nranks, 1);
   if (E.comm) {
     const ncclDataType_t t = op == D3G_EX_SUM_U32 ? ncclUint32 : ncclUint64;
     const ncclRedOp_t o = op == D3G_EX_MAX_U64 ? ncclMax : ncclSum;
@@ -93,6 +123,7 @@ inline void ex_allreduce(Ctx& X, Exchange& E, void* dbuf, uint64_t count, int op
     return;
   }
   const size_t bytes = count * ex_elem_bytes(op);
+  ExHostTimer timer(X, E);
   std::vector<char> h(bytes);
   X.to_host(h.data(), static_cast<const char*>(dbuf), bytes);
   if (E.host_fn(E.host_user, op, h.data(), count) != 0)
@@ -107,6 +138,8 @@ inline void ex_allgather(Ctx& X, Exchange& E, const void* mine, void* out, uint6
     std::memcpy(out, mine, bytes);
     return;
   }
+  ++E.calls;
+  E.bus_bytes += bytes * (E.nranks - 1);
   if (E.comm) {
     DBuf<char> din = X.alloc<char>(bytes), dout = X.alloc<char>(bytes * E.nranks);
     X.to_device(din.p, static_cast<const char*>(mine), bytes);
@@ -114,9 +147,51 @@ inline void ex_allgather(Ctx& X, Exchange& E, const void* mine, void* out, uint6
     X.to_host(static_cast<char*>(out), dout.p, bytes * E.nranks);
     return;
   }
+  ExHostTimer timer(X, E);
   std::memcpy(static_cast<char*>(out) + (size_t)E.rank * bytes, mine, bytes);
   if (E.host_fn(E.host_user, D3G_EX_GATHER, out, bytes) != 0)
     throw Error(D3G_INTERNAL_ERROR, "exchange callback failed (allgather)");
+}
+
+// Allgather of variable-size DEVICE segments: rank q contributes counts[q]
+// elements of `elem` bytes (`mine` is this rank's); `out` (device, sum of the
+// counts) receives them rank-major. NCCL: one ncclAllGather of slots padded
+// to the largest part, then one device copy per part; host transport: the
+// parts are staged through the host callback.
+inline void ex_allgatherv_dev(Ctx& X, Exchange& E, const void* mine,
+                              const std::vector<uint64_t>& counts, size_t elem, void* out) {
+  const int N = E.nranks;
+  uint64_t maxn = 0, total = 0;
+  std::vector<uint64_t> off(N + 1, 0);
+  for (int q = 0; q < N; ++q) {
+    maxn = std::max(maxn, counts[q]);
+    off[q + 1] = off[q] + counts[q];
+  }
+  total = off[N];
+  char* o = static_cast<char*>(out);
+  const uint64_t slot = maxn * elem;
+  if (slot == 0) return;
+  ++E.calls;
+  E.bus_bytes += (total - counts[E.rank]) * elem;
+  if (E.comm) {
+    DBuf<char> tin = X.alloc<char>(slot), tout = X.alloc<char>(slot * N);
+    if (counts[E.rank])
+      D3G_CUDA(cudaMemcpyAsync(tin.p, mine, counts[E.rank] * elem, cudaMemcpyDeviceToDevice, X.stream));
+    D3G_NCCL(nccl().all_gather(tin.p, tout.p, slot, ncclUint8, E.comm, X.stream));
+    for (int q = 0; q < N; ++q)
+      if (counts[q])
+        D3G_CUDA(cudaMemcpyAsync(o + off[q] * elem, tout.p + (uint64_t)q * slot, counts[q] * elem,
+                                 cudaMemcpyDeviceToDevice, X.stream));
+    return;
+  }
+  ExHostTimer timer(X, E);
+  std::vector<char> h(slot * N);
+  if (counts[E.rank])
+    X.copy_to_pageable(h.data() + (uint64_t)E.rank * slot, mine, counts[E.rank] * elem);
+  if (E.host_fn(E.host_user, D3G_EX_GATHER, h.data(), slot) != 0)
+    throw Error(D3G_INTERNAL_ERROR, "exchange callback failed (allgatherv)");
+  for (int q = 0; q < N; ++q)
+    if (counts[q]) X.to_device(o + off[q] * elem, h.data() + (uint64_t)q * slot, counts[q] * elem);
 }
 
 // Host scalars through the same transport (a tiny device round trip).

@@ -242,7 +242,9 @@ class _Report(C.Structure):
                 ("cold_bytes", C.c_uint64), ("spa_allocations", C.c_uint64),
                 ("spa_entries", C.c_uint64), ("rank_out_p", C.c_uint64),
                 ("nranks", C.c_int32), ("rank", C.c_int32),
-                ("cold_candidates", C.c_uint64), ("cold_tail_checks", C.c_uint64)]
+                ("cold_candidates", C.c_uint64), ("cold_tail_checks", C.c_uint64),
+                ("exchange_calls", C.c_uint64), ("exchange_bus_bytes", C.c_uint64),
+                ("ms_exchange_host", C.c_double), ("zsplit", C.c_int32), ("pad1", C.c_int32)]
 
 
 class _Pairs(C.Structure):
@@ -499,6 +501,10 @@ class ExecutionReport:
     rank: int = 0
     cold_candidates: int = 0
     cold_tail_checks: int = 0
+    exchange_calls: int = 0
+    exchange_bus_bytes: int = 0
+    ms_exchange_host: float = 0.0
+    zsplit: bool = False
 
     def to_kv(self):
         """Insertion-ordered key/value view with the reference's key names
@@ -616,7 +622,7 @@ def _to_report(rep: _Report) -> ExecutionReport:
             v = bool(v)
         setattr(out, f.name, v)
     for b in ("swapped", "f1_gate_classical", "natural_x", "natural_y", "natural_z",
-              "materialized"):
+              "materialized", "zsplit"):
         setattr(out, b, bool(getattr(out, b)))
     return out
 

@@ -39,7 +39,7 @@ def run_sharded(r, s, nranks, cfg, x_card=None, contexts=None):
             rq = d3.RawTable(np.ascontiguousarray(r[0][keep]), np.ascontiguousarray(r[1][keep]))
             outs[q] = d3.join_project(rq, d3.RawTable(*s), cfg, C, ctx=ctx)
         except BaseException as e:  # noqa: BLE001
-            errs.append(e)
+            errs.append((q, e, getattr(ctxs[q], "exchange_error", None)))
             ex.barrier.abort()
         finally:
             ctxs[q].clear_exchange()
@@ -50,7 +50,13 @@ def run_sharded(r, s, nranks, cfg, x_card=None, contexts=None):
     for t in th:
         t.join()
     if errs:
-        raise errs[0]
+        # the first rank to fail aborts the barrier; the others then fail in
+        # their exchange callback: report the root cause
+        root = [e for e in errs if not isinstance(e[2], threading.BrokenBarrierError)]
+        q, e, cb = (root or errs)[0]
+        if isinstance(e, (d3.ConfigError, d3.ResourceError)) and len(root) == len(errs):
+            raise e
+        raise AssertionError(f"rank {q}: {e!r} (callback: {cb!r}); all: {errs!r}")
     return outs
 
 
@@ -129,3 +135,47 @@ def test_nccl_one_rank_transport():
         assert getattr(got, k) == getattr(full, k), k
     assert got.nranks == 1
     ctx.clear_exchange()
+
+
+@pytest.mark.parametrize("nranks", [2, 5])
+def test_zsplit_dense_only_instances(nranks):
+    """The z-split S side (csrc/zsplit.cuh): with every z dense the ranks build
+    S-by-z, the dense lists, hot records and the cold CSR for their own z
+    range and gather them; every rank reports the unsharded job and the
+    ranks' pairs are the oracle's set."""
+    rng = SplitMix64(4200 + nranks)
+    ctxs = [d3.Context(0) for _ in range(nranks)]
+    done = 0
+    while done < 6:
+        r, s = random_instance(rng)
+        if len(s[0]) > len(r[0]):
+            continue
+        done += 1
+        cfg = d3.EngineConfig(force=d3.Strategy.dense_only, checksum=True)
+        full = d3.join_project(d3.RawTable(*r), d3.RawTable(*s), cfg, C)
+        outs = run_sharded(r, s, nranks, cfg, contexts=ctxs)
+        got = set()
+        for q, o in enumerate(outs):
+            if full.report.dense_z and full.report.x_live:
+                assert o.report.zsplit, q
+            for k in JOB_KEYS:
+                assert getattr(o.report, k) == getattr(full.report, k), (k, q)
+            got |= pair_set(o.result.raw_x, o.result.raw_z)
+        assert got == oracle_pairs(r, s)
+
+
+def test_zsplit_cfg2_folded_layout():
+    """cfg2 sharded 4 ways takes the z-split with its sparse rows folded into
+    the dense layout; count, fingerprint and the pairs_sparse / pairs_dense
+    split equal the unsharded call, and the z-split's collectives are
+    accounted (calls, link bytes)."""
+    r, s = O.gen(2, 0), O.gen(2, 1)
+    e = d3.EngineConfig(count_only=True, checksum=True, memory_budget_bytes=32 << 30)
+    full = d3.join_project(d3.RawTable(r.left, r.right), d3.RawTable(s.left, s.right), e, C).report
+    outs = run_sharded((r.left, r.right), (s.left, s.right), 4, e, x_card=200_000)
+    for o in outs:
+        assert o.report.zsplit
+        assert o.report.exchange_calls > 0 and o.report.exchange_bus_bytes > 0
+        for k in ("out_p", "checksum_sum", "checksum_xor", "pairs_sparse", "pairs_dense",
+                  "dense_z", "sparse_z", "out_j", "s_nnz", "r_nnz"):
+            assert getattr(o.report, k) == getattr(full, k), k
