@@ -163,6 +163,7 @@ __global__ void hot_build_x_kernel(const uint32_t* __restrict__ xorder, uint64_t
   for (uint64_t p = (uint64_t)blockIdx.x * (blockDim.x / 8) + (threadIdx.x >> 3); p < n_live;
        p += (uint64_t)gridDim.x * (blockDim.x / 8)) {
     uint32_t x = xorder[p];
+    if (x == 0xffffffffu) continue;  // an empty slot of a class-aligned batch
     uint64_t g = p >> 7;
     uint64_t bi = g >> 5, gl = g & 31;
     uint32_t b = (uint32_t)(p & 127);

@@ -540,6 +540,20 @@ __global__ void hot_small_stats_kernel(const uint32_t* __restrict__ cnt_rank,
     out[t] = (t - 7) < y_card ? dR[y_of_rank[t - 7]] : 0;
 }
 
+// Class-aligned hot positions: the x at class-split position i (class q =
+// cls[i], its rank within the class i - cstart[q]) goes to pstart[q] + that.
+struct PadStarts {
+  uint64_t cstart[16], pstart[16];
+};
+__global__ void pad_scatter_kernel(const uint32_t* __restrict__ cls, const uint32_t* __restrict__ xs,
+                                   uint64_t n, PadStarts ps, uint32_t* __restrict__ out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t q = cls[i];
+    out[ps.pstart[q] + (i - ps.cstart[q])] = xs[i];
+  }
+}
+
 // Test/experiment override of a kernel limit: env value clamped to [lo, hi].
 static uint32_t env_u32(const char* name, uint32_t dflt, uint32_t lo, uint32_t hi) {
   const char* v = std::getenv(name);
@@ -657,7 +671,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   }
   // the cold kernels read 256-bit hot signatures: keep that layout for K < 256
   const uint32_t kw = cold_kernel_ok ? 4u : (K + 63) / 64;
-  const uint32_t n_batches = (groups + 31) / 32;
+  uint32_t n_batches = (groups + 31) / 32;  // of the hot pass (class-aligned: padded)
   // Rank-0 split (count-only; the table kernel with prefix-shared rows): an x
   // holding the top rank y_of_rank[0] hits every dense row that holds it.
   // Live x are split stably into B (without it) then A (with it); batches made
@@ -679,6 +693,10 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   // class-major, so those are a few contiguous class runs (no copies); every
   // other pair of the batch is counted as a hit.
   const uint32_t n_kinds = 1u << n_piv;
+  // the hot pass's x positions (class-aligned plan: padded with empty slots)
+  const uint32_t* hot_xorder = xorder;
+  uint64_t hot_n = n_live;
+  DBuf<uint32_t> xpad;
   uint64_t plan_direct = 0, plan_direct_sp = 0;  // untested hits (all / folded sparse rows)
   uint64_t run_lo[17] = {0};     // class c's rows [run_lo[c], run_lo[c + 1])
   uint32_t run_zc[16] = {0};     // units per batch over class c's run
@@ -715,11 +733,50 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
       direct += (p1 - p0) * (D - kind_rows[k]);
       direct_sp += (p1 - p0) * (sp_all - sp_rows[k]);
     }
-    if (tested < 0.8 * (double)n_batches * (double)D) {
+    // Class-aligned batches: every class padded to whole batches, so no batch
+    // mixes classes. A mixed batch tests the rows of the AND of its classes'
+    // pivot sets: a batch straddling classes 1 and 2 (pivot 0 only / pivot 1
+    // only) tests EVERY row, and an x shard has such boundaries of its own.
+    uint64_t pstart[17] = {0};
+    double tested_pad = 0;
+    for (uint32_t q = 0; q < n_kinds; ++q) {
+      const uint64_t nb = (nx[q] + 4095) / 4096;
+      pstart[q + 1] = pstart[q] + nb * 4096;
+      tested_pad += (double)nb * (double)kind_rows[q];
+    }
+    const bool pad = tested_pad < tested && std::getenv("D3G_NO_PAD") == nullptr;
+    uint32_t n_batches_plan = n_batches;
+    if (pad) {
+      n_batches_plan = (uint32_t)(pstart[n_kinds] / 4096);
+      batch_kind_h.assign(n_batches_plan, 0);
+      direct = direct_sp = 0;
+      for (uint32_t q = 0; q < n_kinds; ++q) {
+        for (uint64_t b = pstart[q] / 4096; b < pstart[q + 1] / 4096; ++b) batch_kind_h[b] = (uint8_t)q;
+        direct += nx[q] * (D - kind_rows[q]);
+        direct_sp += nx[q] * (sp_all - sp_rows[q]);
+      }
+      tested = tested_pad;
+    }
+    if (tested < 0.8 * (double)n_batches_plan * (double)D) {
       xsplit = X.alloc<uint32_t>(n_live);
       DBuf<uint32_t> cls_s = X.alloc<uint32_t>(n_live);
       radix_pass_u32(X, cls.p, xorder, n_live, 0, cls_s.p, xsplit.p);  // stable by class
       xorder = xsplit.p;
+      if (pad) {  // the hot pass's x positions: each class from a batch start
+        n_batches = n_batches_plan;
+        hot_n = pstart[n_kinds];
+        xpad = X.alloc<uint32_t>(hot_n);
+        D3G_CUDA(cudaMemsetAsync(xpad.p, 0xff, hot_n * 4, X.stream));  // empty positions
+        PadStarts ps{};
+        for (uint32_t q = 0; q < 16; ++q) {
+          ps.cstart[q] = cstart[q];
+          ps.pstart[q] = pstart[q];
+        }
+        if (n_live)
+          D3G_LAUNCH(X, pad_scatter_kernel, grid_for(n_live, 256), 256, 0, cls_s.p, xsplit.p,
+                     n_live, ps, xpad.p);
+        hot_xorder = xpad.p;
+      }
       plan_direct = direct;
       plan_direct_sp = direct_sp;
       for (uint32_t q = 0; q < n_kinds; ++q) run_lo[q + 1] = run_lo[q] + nr[q];
@@ -764,9 +821,10 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     hz_loc = X.zeros<unsigned long long>(DL * kw);
     hzl = hz_loc.p;
   }
+  if (!xpad.p) hot_xorder = xorder;  // the class-split order when planned
   if (n_live)
-    D3G_LAUNCH(X, hot_build_x_kernel, grid_for(n_live * 8, 256), 256, 0, xorder, n_live, in.r_ptr,
-               in.r_col, in.y_rank, K, kw, reinterpret_cast<uint32_t*>(T.p), hx.p);
+    D3G_LAUNCH(X, hot_build_x_kernel, grid_for(hot_n * 8, 256), 256, 0, hot_xorder, hot_n,
+               in.r_ptr, in.r_col, in.y_rank, K, kw, reinterpret_cast<uint32_t*>(T.p), hx.p);
   if (DL)
     D3G_LAUNCH(X, hot_build_z_kernel, grid_for(DL * 8, 256), 256, 0, in.dl_ptr, in.dl_col, DL, K,
                kw, hzl);
@@ -838,8 +896,9 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     if (!cold_kernel_ok) throw d3g::Error(D3G_INTERNAL_ERROR, "z-split needs the cold kernels");
     X.wait_mark();  // cnnz of this rank
     const int N = in.zx->nranks;
-    DBuf<uint32_t> cnt_all = X.alloc<uint32_t>(rows_key * N);
-    ex_allgatherv_dev(X, *in.zx, cc.p, std::vector<uint64_t>(N, rows_key), 4, cnt_all.p);
+    // every rank's offsets (its exclusive scan over its counts)
+    DBuf<uint64_t> cp_all = X.alloc<uint64_t>((rows_key + 1) * N);
+    ex_allgatherv_dev(X, *in.zx, cptr.p, std::vector<uint64_t>(N, rows_key + 1), 8, cp_all.p);
     DBuf<uint4> crec_l = X.alloc<uint4>(cnnz);
     if (DL)
       D3G_LAUNCH(X, cold_scatter_kernel, grid_for(DL * 8, 256), 256, 0, in.dl_ptr, in.dl_col, DL,
@@ -862,21 +921,19 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     DBuf<uint4> crec_all = X.alloc<uint4>(tot);
     ex_allgatherv_dev(X, *in.zx, crec_l.p, part_n, 16, crec_all.p);
     crec_l.reset();
-    // every rank's exclusive scan, the job's counts and their scan
-    DBuf<uint64_t> src_off = X.alloc<uint64_t>((rows_key + 1) * N);
-    for (int q = 0; q < N; ++q)
-      exclusive_scan<uint32_t>(X, cnt_all.p + (uint64_t)q * rows_key, rows_key,
-                               src_off.p + (uint64_t)q * (rows_key + 1));
-    DBuf<uint32_t> tcnt = X.alloc<uint32_t>(rows_key);
-    D3G_LAUNCH(X, sum_rows_u32_kernel, grid_for(rows_key, 256), 256, 0, cnt_all.p, rows_key, N,
-               tcnt.p);
-    exclusive_scan<uint32_t>(X, tcnt.p, rows_key, cptr.p);
-    tcnt.reset();
+    // the job's offsets: the sum of the ranks' scans
+    D3G_LAUNCH(X, sum_rows_u64_kernel, grid_for(rows_key + 1, 256), 256, 0, cp_all.p, rows_key + 1,
+               N, cptr.p);
     DBuf<uint64_t> pb = X.alloc<uint64_t>(N);
     X.to_device(pb.p, part_b.data(), N);
     crec_g = X.alloc<uint4>(tot);
-    D3G_LAUNCH(X, cold_merge_kernel, grid_for(rows_key * 32, 256), 256, 0, cnt_all.p, src_off.p,
-               pb.p, crec_all.p, cptr.p, rows_key, N, crec_g.p);
+    // long segments: at most tot / kMergeLong of them
+    DBuf<LongSeg> longs = X.alloc<LongSeg>(tot / kMergeLong + 1);
+    DBuf<unsigned int> n_long = X.zeros<unsigned int>(1);
+    D3G_LAUNCH(X, cold_merge_kernel, grid_for((rows_key + 31) / 32 * 32, 256, X.sm_count * 16), 256,
+               0, cp_all.p, pb.p, crec_all.p, cptr.p, rows_key, N, crec_g.p, longs.p, n_long.p);
+    D3G_LAUNCH(X, cold_merge_long_kernel, X.sm_count * 8, 256, 0, longs.p, n_long.p, crec_all.p,
+               crec_g.p);
     cnnz = tot;
   }
   // P1: hot bit-sliced pass
@@ -885,11 +942,11 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   HotParams hp{};
   hp.T = T.p;
   hp.hz = reinterpret_cast<const uint64_t*>(hz.p);
-  hp.xorder = xorder;
+  hp.xorder = hot_xorder;
   hp.dl_z = dlz;
-  hp.n_live = n_live;
+  hp.n_live = hot_n;
   hp.n_dense = D;
-  hp.groups = groups;
+  hp.groups = (uint32_t)((hot_n + 127) / 128);
   hp.K = K;
   hp.kw = kw;
   hp.batch = 32;
@@ -2484,10 +2541,14 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
     if (M.kept)
       D3G_LAUNCH(X, value_hist_kernel, grid_for(M.kept, 512, X.sm_count * 2), 512, 0, M.r_y,
                  M.kept, cr.p, (uint32_t)yc);
-    if (NS)
-      D3G_LAUNCH(X, value_hist_kernel, grid_for(NS, 512, X.sm_count * 2), 512, 0, M.s_y, NS,
-                 cs2.p, (uint32_t)yc);
+    // (every rank holds all of S: each counts a 1/N slice, summed with R's)
+    const uint64_t s0 = NS * (uint64_t)E->rank / (uint64_t)E->nranks,
+                   s1 = NS * (uint64_t)(E->rank + 1) / (uint64_t)E->nranks;
+    if (s1 > s0)
+      D3G_LAUNCH(X, value_hist_kernel, grid_for(s1 - s0, 512, X.sm_count * 2), 512, 0,
+                 M.s_y + s0, s1 - s0, cs2.p, (uint32_t)yc);
     ex_allreduce(X, *E, cr.p, yc, D3G_EX_SUM_U32);
+    ex_allreduce(X, *E, cs2.p, yc, D3G_EX_SUM_U32);
     const unsigned gb = grid_for(yc, 1024, 296);
     DBuf<unsigned long long> parts = X.zeros<unsigned long long>(2ull * gb);
     if (yc) D3G_LAUNCH(X, outj_kernel, gb, 1024, 0, cr.p, cs2.p, yc, parts.p);
@@ -2536,7 +2597,7 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
     DBuf<uint32_t> zs_z = X.alloc<uint32_t>(NS), zs_y = X.alloc<uint32_t>(NS);
     DBuf<unsigned long long> cur = X.zeros<unsigned long long>(1);
     if (NS)
-      D3G_LAUNCH(X, zrange_compact_kernel, grid_for(NS, 256, X.sm_count * 8), 256, 0, M.s_z,
+      D3G_LAUNCH(X, zrange_compact_kernel, grid_for(NS, kZcThreads * kZcPer, X.sm_count * 8), kZcThreads, 0, M.s_z,
                  M.s_y, NS, (uint32_t)z_lo, (uint32_t)z_hi, zs_z.p, zs_y.p, cur.p);
     const uint64_t n_loc = X.scalar(cur.p);
     build_csr_device(X, zs_z.p, zs_y.p, n_loc, z_hi - z_lo, y_card, sz_csr);

@@ -21,64 +21,132 @@
 namespace d3g {
 
 // This rank's S tuples: z codes in [z_lo, z_hi), compacted as (z - z_lo, y)
-// (their order is irrelevant: the CSR build sorts). Warp-aggregated cursor.
-__global__ void zrange_compact_kernel(const uint32_t* __restrict__ sz, const uint32_t* __restrict__ sy,
-                                      uint64_t n, uint32_t z_lo, uint32_t z_hi,
-                                      uint32_t* __restrict__ oz, uint32_t* __restrict__ oy,
-                                      unsigned long long* __restrict__ cursor) {
-  const uint32_t lane = lane_id();
-  for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x; i0 < n; i0 += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t i = i0 + threadIdx.x;
-    bool in = false;
-    uint32_t z = 0;
-    if (i < n) {
-      z = sz[i];
-      in = z >= z_lo && z < z_hi;
+// (their order is irrelevant: the CSR build sorts). Tiles of 256 x 8 codes;
+// one cursor atomic per tile (a per-warp atomic serialised the pass: 5 ms for
+// cfg5's 200M codes).
+constexpr int kZcThreads = 256, kZcPer = 8;
+__global__ void __launch_bounds__(kZcThreads)
+zrange_compact_kernel(const uint32_t* __restrict__ sz, const uint32_t* __restrict__ sy, uint64_t n,
+                      uint32_t z_lo, uint32_t z_hi, uint32_t* __restrict__ oz,
+                      uint32_t* __restrict__ oy, unsigned long long* __restrict__ cursor) {
+  __shared__ uint32_t wsum[kZcThreads / 32];
+  __shared__ unsigned long long base_s;
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  constexpr uint64_t kTile = (uint64_t)kZcThreads * kZcPer;
+  for (uint64_t t0 = (uint64_t)blockIdx.x * kTile; t0 < n; t0 += (uint64_t)gridDim.x * kTile) {
+    uint32_t z[kZcPer], cnt = 0, inm = 0;
+#pragma unroll
+    for (int k = 0; k < kZcPer; ++k) {
+      const uint64_t i = t0 + threadIdx.x + (uint64_t)k * kZcThreads;
+      z[k] = i < n ? sz[i] : z_hi;
+      if (z[k] >= z_lo && z[k] < z_hi) {
+        inm |= 1u << k;
+        ++cnt;
+      }
     }
-    const uint32_t m = __ballot_sync(0xffffffffu, in);
-    unsigned long long base = 0;
-    if (lane == 0 && m) base = atomicAdd(cursor, (unsigned long long)__popc(m));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (in) {
-      const uint64_t o = base + __popc(m & ((1u << lane) - 1u));
-      oz[o] = z - z_lo;
-      oy[o] = sy[i];
+    const uint32_t incl = warp_incl_scan(cnt);
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t v = lane < kZcThreads / 32 ? wsum[lane] : 0u;
+      const uint32_t vi = warp_incl_scan(v);
+      if (lane < kZcThreads / 32) wsum[lane] = vi - v;
+      if (lane == kZcThreads / 32 - 1) base_s = vi ? atomicAdd(cursor, (unsigned long long)vi) : 0ull;
     }
+    __syncthreads();
+    uint64_t o = base_s + wsum[warp] + incl - cnt;
+#pragma unroll
+    for (int k = 0; k < kZcPer; ++k)
+      if (inm >> k & 1u) {
+        const uint64_t i = t0 + threadIdx.x + (uint64_t)k * kZcThreads;
+        oz[o] = z[k] - z_lo;
+        oy[o] = sy[i];
+        ++o;
+      }
+    __syncthreads();  // wsum / base_s are rewritten by the next tile
   }
 }
 
-// Sum of the ranks' count rows: tot[k] = sum_q cnt[q][k].
-__global__ void sum_rows_u32_kernel(const uint32_t* __restrict__ cnt, uint64_t keys, int nranks,
-                                    uint32_t* __restrict__ tot) {
-  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < keys;
+// The job's cold CSR offsets: the sum of the ranks' exclusive scans is the
+// exclusive scan of the summed counts, cptr[k] = sum_q cptr_q[k].
+__global__ void sum_rows_u64_kernel(const uint64_t* __restrict__ cp /* [N][keys + 1] */,
+                                    uint64_t keys1, int nranks, uint64_t* __restrict__ tot) {
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < keys1;
        k += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t s = 0;
-    for (int q = 0; q < nranks; ++q) s += cnt[(uint64_t)q * keys + k];
+    uint64_t s = 0;
+    for (int q = 0; q < nranks; ++q) s += cp[(uint64_t)q * keys1 + k];
     tot[k] = s;
   }
 }
 
-// The global cold CSR from the ranks' gathered parts: key k's segment is
-// rank 0's segment of k, then rank 1's, ... (src_off[q]: rank q's exclusive
-// scan over its counts, part_base[q]: where rank q's records start in src).
-// A warp per key: lanes copy the records of each rank's segment in turn.
-__global__ void cold_merge_kernel(const uint32_t* __restrict__ cnt /* [N][keys] */,
-                                  const uint64_t* __restrict__ src_off /* [N][keys + 1] */,
+// The job's cold CSR from the ranks' gathered parts: key k's segment is rank
+// 0's segment of k, then rank 1's, ... A warp takes 32 consecutive keys: for
+// each rank q their short segments are ONE contiguous range of q's part
+// (its segments are key-major), read coalesced; each record's key is found
+// from the warp scan of the 32 lengths and it lands at cptr[k] + (the lower
+// ranks' records of k) + its offset in q's segment. Long segments (>= 256
+// records: the cold y just past the hot ranks) are queued whole and copied
+// by a warp each (cold_merge_long_kernel), so no warp serialises a hot key.
+struct LongSeg {
+  uint64_t src, dst;
+  uint32_t len, pad;
+};
+constexpr uint32_t kMergeLong = 256;
+__global__ void cold_merge_kernel(const uint64_t* __restrict__ cp /* [N][keys + 1] */,
                                   const uint64_t* __restrict__ part_base /* [N] */,
                                   const uint4* __restrict__ src, const uint64_t* __restrict__ cptr,
-                                  uint64_t keys, int nranks, uint4* __restrict__ dst) {
+                                  uint64_t keys, int nranks, uint4* __restrict__ dst,
+                                  LongSeg* __restrict__ longs, unsigned int* __restrict__ n_long) {
   const uint32_t lane = lane_id();
-  const uint64_t w0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t k = w0; k < keys; k += nw) {
-    uint64_t d = cptr[k];
+  for (uint64_t kb = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; kb * 32 < keys;
+       kb += nw) {
+    const uint64_t k0 = kb * 32, k = k0 + lane;
+    uint64_t d = k < keys ? cptr[k] : 0;  // next free slot of key k
     for (int q = 0; q < nranks; ++q) {
-      const uint32_t n = cnt[(uint64_t)q * keys + k];
-      if (n == 0) continue;
-      const uint4* s = src + part_base[q] + src_off[(uint64_t)q * (keys + 1) + k];
-      for (uint32_t j = lane; j < n; j += 32) dst[d + j] = s[j];
-      d += n;
+      const uint64_t* c = cp + (uint64_t)q * (keys + 1);
+      uint64_t s = 0;
+      uint32_t len = 0;
+      if (k < keys) {
+        s = c[k];
+        len = (uint32_t)(c[k + 1] - s);
+      }
+      const bool is_long = len >= kMergeLong;
+      if (is_long) {
+        const unsigned int slot = atomicAdd(n_long, 1u);
+        longs[slot] = LongSeg{part_base[q] + s, d, len, 0};
+      }
+      const uint32_t sl = is_long ? 0u : len;  // the short ones, copied here
+      const uint32_t incl = warp_incl_scan(sl);
+      const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+      // record f of the short segments belongs to lane j (the warp scan of
+      // their lengths) at offset f - before in both its source and its slot
+      for (uint32_t f = lane; f < ((total + 31) & ~31u); f += 32) {
+        uint32_t j = 0;
+#pragma unroll
+        for (int st = 16; st >= 1; st >>= 1) {
+          const uint32_t probe = __shfl_sync(0xffffffffu, incl, j + st - 1);
+          if (probe <= f) j += st;
+        }
+        const uint32_t jj = j & 31;
+        const uint32_t before = __shfl_sync(0xffffffffu, incl - sl, jj);
+        const uint64_t dj = __shfl_sync(0xffffffffu, d, jj);
+        const uint64_t sj = __shfl_sync(0xffffffffu, s, jj);
+        if (f < total) dst[dj + (f - before)] = __ldg(src + part_base[q] + sj + (f - before));
+      }
+      d += len;
     }
+  }
+}
+__global__ void cold_merge_long_kernel(const LongSeg* __restrict__ longs,
+                                       const unsigned int* __restrict__ n_long,
+                                       const uint4* __restrict__ src, uint4* __restrict__ dst) {
+  const uint32_t lane = lane_id();
+  const uint32_t n = *n_long;
+  for (uint32_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n;
+       w += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+    const LongSeg g = longs[w];
+    for (uint32_t f = lane; f < g.len; f += 32) dst[g.dst + f] = __ldg(src + g.src + f);
   }
 }
 
