@@ -157,16 +157,18 @@ __global__ void hot_build_x_kernel(const uint32_t* __restrict__ xorder, uint64_t
                                    const uint64_t* __restrict__ r_ptr,
                                    const uint32_t* __restrict__ r_col,
                                    const uint32_t* __restrict__ y_rank, uint32_t K, uint32_t kw,
-                                   uint32_t* __restrict__ T, unsigned long long* __restrict__ hx) {
+                                   uint32_t* __restrict__ T, unsigned long long* __restrict__ hx,
+                                   uint64_t pos_base = 0 /* T position of xorder[0] */) {
   // 8 lanes per x (rows hold ~10-30 entries)
   const uint32_t sl = threadIdx.x & 7;
   for (uint64_t p = (uint64_t)blockIdx.x * (blockDim.x / 8) + (threadIdx.x >> 3); p < n_live;
        p += (uint64_t)gridDim.x * (blockDim.x / 8)) {
     uint32_t x = xorder[p];
     if (x == 0xffffffffu) continue;  // an empty slot of a class-aligned batch
-    uint64_t g = p >> 7;
+    const uint64_t tp = pos_base + p;
+    uint64_t g = tp >> 7;
     uint64_t bi = g >> 5, gl = g & 31;
-    uint32_t b = (uint32_t)(p & 127);
+    uint32_t b = (uint32_t)(tp & 127);
     for (uint64_t k = r_ptr[x] + sl; k < r_ptr[x + 1]; k += 8) {
       uint32_t r = y_rank[r_col[k]];
       if (r < K) {

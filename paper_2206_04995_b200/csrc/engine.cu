@@ -550,6 +550,7 @@ __global__ void pad_scatter_kernel(const uint32_t* __restrict__ cls, const uint3
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t q = cls[i];
+    if (ps.pstart[q] == ~0ull) continue;  // a class handled elsewhere (shared batches)
     out[ps.pstart[q] + (i - ps.cstart[q])] = xs[i];
   }
 }
@@ -693,6 +694,11 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   // class-major, so those are a few contiguous class runs (no copies); every
   // other pair of the batch is counted as a hit.
   const uint32_t n_kinds = 1u << n_piv;
+  // z-split: pool the ranks' class-0 x (tested against every row) into shared
+  // batches, each rank testing them against a slice of the rows
+  const bool share0_try = zs && piv_pre && std::getenv("D3G_NO_SHARE0") == nullptr;
+  bool share0_local = false;  // this rank's class-0 x left its own batches
+  uint64_t n0_local = 0;
   // the hot pass's x positions (class-aligned plan: padded with empty slots)
   const uint32_t* hot_xorder = xorder;
   uint64_t hot_n = n_live;
@@ -737,14 +743,16 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     // mixes classes. A mixed batch tests the rows of the AND of its classes'
     // pivot sets: a batch straddling classes 1 and 2 (pivot 0 only / pivot 1
     // only) tests EVERY row, and an x shard has such boundaries of its own.
+    // (z-split: class 0 -- x holding no pivot, so every row is tested -- is
+    // pooled across the ranks into shared batches, see below)
     uint64_t pstart[17] = {0};
     double tested_pad = 0;
     for (uint32_t q = 0; q < n_kinds; ++q) {
-      const uint64_t nb = (nx[q] + 4095) / 4096;
+      const uint64_t nb = (share0_try && q == 0) ? 0 : (nx[q] + 4095) / 4096;
       pstart[q + 1] = pstart[q] + nb * 4096;
       tested_pad += (double)nb * (double)kind_rows[q];
     }
-    const bool pad = tested_pad < tested && std::getenv("D3G_NO_PAD") == nullptr;
+    const bool pad = (share0_try || tested_pad < tested) && std::getenv("D3G_NO_PAD") == nullptr;
     uint32_t n_batches_plan = n_batches;
     if (pad) {
       n_batches_plan = (uint32_t)(pstart[n_kinds] / 4096);
@@ -771,6 +779,11 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
         for (uint32_t q = 0; q < 16; ++q) {
           ps.cstart[q] = cstart[q];
           ps.pstart[q] = pstart[q];
+        }
+        if (share0_try) {  // class 0 goes to the shared batches
+          ps.pstart[0] = ~0ull;
+          share0_local = true;
+          n0_local = nx[0];
         }
         if (n_live)
           D3G_LAUNCH(X, pad_scatter_kernel, grid_for(n_live, 256), 256, 0, cls_s.p, xsplit.p,
@@ -828,6 +841,33 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   if (DL)
     D3G_LAUNCH(X, hot_build_z_kernel, grid_for(DL * 8, 256), 256, 0, in.dl_ptr, in.dl_col, DL, K,
                kw, hzl);
+  // z-split shared class-0 batches: every rank ORs its class-0 x into the
+  // pooled slice tables (disjoint bits: a sum all-reduce is the OR), then
+  // tests them against rows [D r / N, D (r + 1) / N) of the sorted records
+  DBuf<uint4> T0;
+  uint64_t n0_job = 0, sh_lo = 0, sh_hi = 0;
+  uint32_t nb0 = 0;
+  if (share0_try && try_plan) {
+    const int N = in.zx->nranks, rk = in.zx->rank;
+    uint64_t mine = share0_local ? n0_local : 0;
+    std::vector<uint64_t> all(N);
+    ex_allgather(X, *in.zx, &mine, all.data(), 8);
+    uint64_t off = 0;
+    for (int q = 0; q < N; ++q) {
+      if (q < rk) off += all[q];
+      n0_job += all[q];
+    }
+    if (n0_job) {
+      nb0 = (uint32_t)((n0_job + 4095) / 4096);
+      T0 = X.zeros<uint4>((uint64_t)nb0 * K * 32);
+      if (mine)  // class 0 leads the class-split order
+        D3G_LAUNCH(X, hot_build_x_kernel, grid_for(mine * 8, 256), 256, 0, xorder, mine, in.r_ptr,
+                   in.r_col, in.y_rank, K, kw, reinterpret_cast<uint32_t*>(T0.p), hx.p, off);
+      ex_allreduce(X, *in.zx, T0.p, (uint64_t)nb0 * K * 32 * 4, D3G_EX_SUM_U32);
+      sh_lo = D * (uint64_t)rk / (uint64_t)N;
+      sh_hi = D * (uint64_t)(rk + 1) / (uint64_t)N;
+    }
+  }
   if (zs) ex_allgatherv_dev(X, *in.zx, hzl, in.rows_per_rank, kw * 8, hz.p);
   // z-split: the job's per-row z codes and folded-sparse flags
   DBuf<uint32_t> dlz_g;
@@ -974,6 +1014,35 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   }
   DBuf<unsigned int> work = X.zeros<unsigned int>(1);
   hp.work = work.p;
+  // the shared class-0 batches: the same kernel on the pooled slice tables,
+  // one class run = this rank's row slice, every batch of kind 0
+  HotParams h0 = hp;
+  DBuf<uint32_t> uoff0;
+  DBuf<uint8_t> bkind0;
+  DBuf<unsigned int> work0;
+  uint32_t zc0 = 0;
+  if (n0_job) {
+    const uint64_t slice = sh_hi - sh_lo;
+    zc0 = (uint32_t)std::max<uint64_t>(
+        1, std::min<uint64_t>((slice + 255) / 256, ((uint64_t)X.sm_count * 4 + nb0 - 1) / nb0));
+    std::vector<uint32_t> uo(nb0 + 1);
+    for (uint32_t b = 0; b <= nb0; ++b) uo[b] = b * (slice ? zc0 : 0u);
+    uoff0 = X.alloc<uint32_t>(nb0 + 1);
+    bkind0 = X.zeros<uint8_t>(nb0);
+    X.to_device(uoff0.p, uo.data(), nb0 + 1);
+    work0 = X.zeros<unsigned int>(1);
+    h0.T = T0.p;
+    h0.n_live = n0_job;
+    h0.groups = (uint32_t)((n0_job + 127) / 128);
+    h0.unit_off = uoff0.p;
+    h0.batch_kind = bkind0.p;
+    for (uint32_t q = 0; q <= 16; ++q) h0.run_lo[q] = q == 0 ? sh_lo : sh_hi;
+    for (uint32_t q = 0; q < 16; ++q) h0.run_zc[q] = q == 0 ? (slice ? zc0 : 0u) : 0u;
+    h0.n_classes = 1;
+    h0.plan_units = uo[nb0];
+    h0.plan_on = 1;
+    h0.work = work0.p;
+  }
   // [hot tally | cold tally | hot-pass LDS units]: read back once at the end
   // [hot | cold | LDS units | pairs of folded sparse rows]
   // [.. | slice reads without prefix sharing]
@@ -1127,6 +1196,10 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
           D3G_LAUNCH(X, trie_lds_kernel, grid_for(D, 256), 256, 0, rcnt.p, D, hp.z_chunks,
                      tab ? 1u : 0u, lds_units, &tallies.p[4].count, (uint64_t)n_batches, 0ull);
         }
+        if (n0_job && sh_hi > sh_lo)  // the shared class-0 batches over this rank's row slice
+          D3G_LAUNCH(X, trie_lds_kernel, grid_for(sh_hi - sh_lo, 256), 256, 0, rcnt.p,
+                     sh_hi - sh_lo, zc0, tab ? 1u : 0u, lds_units, &tallies.p[4].count,
+                     (uint64_t)nb0, sh_lo);
       }
     } else {
       // algorithmic LDS traffic: every (row, batch) reads its listed slices plus
@@ -1144,6 +1217,13 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
           D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jsm));
           D3G_LAUNCH(X, kfn, g, kHotThreads, jsm, hp, in.dl_ptr, in.dl_col, rec.p, rcnt.p, perm.p,
                      dec, em, t, cnt_sp);
+          h0.tail_rows = hp.tail_rows;  // (set with the records, after h0 was made)
+          h0.tail_ptr = hp.tail_ptr;
+          h0.tail_col = hp.tail_col;
+          h0.n_tail = hp.n_tail;
+          if (n0_job && h0.plan_units)  // the shared class-0 batches
+            D3G_LAUNCH(X, kfn, std::min<unsigned>(h0.plan_units, X.sm_count), kHotThreads, jsm, h0,
+                       in.dl_ptr, in.dl_col, rec.p, rcnt.p, perm.p, dec, em, t, cnt_sp);
         };
         constexpr int Md = decltype(M)::value;
         if (tab && jt_trie)
