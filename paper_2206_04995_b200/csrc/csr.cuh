@@ -193,21 +193,24 @@ __global__ void degree_hist_kernel(const uint64_t* __restrict__ row_ptr, uint64_
 constexpr int kHotSmem = 12288;
 __global__ void value_hist_kernel(const uint32_t* __restrict__ vals, uint64_t n,
                                   uint32_t* __restrict__ counts, uint32_t card) {
+  // hot values (the small codes: Zipf-ranked y) in a shared-memory histogram,
+  // the rest straight to global; four independent loads in flight per thread
+  // (the pass is bound by load latency, not by the atomics)
   __shared__ unsigned int sh[kHotSmem];
   const uint32_t hot = card < kHotSmem ? card : kHotSmem;
   for (uint32_t i = threadIdx.x; i < hot; i += blockDim.x) sh[i] = 0;
   __syncthreads();
-  uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  uint64_t n_pad = (n + 31) / 32 * 32;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pad; i += stride) {
-    const uint32_t v = i < n ? vals[i] : 0xffffffffu;
-    const uint32_t peers = __match_any_sync(0xffffffffu, v);
-    if (v != 0xffffffffu && (peers & ((1u << lane_id()) - 1)) == 0) {
-      const unsigned c = (unsigned)__popc(peers);
-      if (v < hot)
-        atomicAdd(&sh[v], c);
-      else
-        atomicAdd(&counts[v], c);
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += 4 * stride) {
+    uint32_t v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = i + k * stride < n ? vals[i + k * stride] : 0xffffffffu;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (v[k] < hot)
+        atomicAdd(&sh[v[k]], 1u);
+      else if (v[k] != 0xffffffffu)
+        atomicAdd(&counts[v[k]], 1u);
     }
   }
   __syncthreads();

@@ -70,13 +70,25 @@ __global__ void cold_scatter_kernel(const uint64_t* __restrict__ dl_ptr,
                                     uint32_t* __restrict__ out, uint32_t ostride,
                                     uint64_t y_card, uint32_t part_rows, uint32_t parts,
                                     const uint64_t* __restrict__ hz, uint32_t kw,
-                                    uint32_t var_bits, uint64_t row_base = 0) {
+                                    uint32_t var_bits, uint64_t row_base = 0,
+                                    uint4* __restrict__ rec = nullptr,
+                                    const uint8_t* __restrict__ row_sp = nullptr) {
   const uint32_t nvar = 1u << var_bits, vmask = nvar - 1;
   const uint32_t sl = threadIdx.x & 7;  // 8 lanes per row
   for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 8) + (threadIdx.x >> 3); i < n_dense;
        i += (uint64_t)gridDim.x * (blockDim.x / 8)) {
     const uint64_t part = (row_base + i) / part_rows;
     const uint32_t zm = var_bits ? (uint32_t)(hz[i * kw] & vmask) : 0;
+    // rec: the whole 16-byte record is written here (its hot word, folded
+    // tail and flags are the row's), no separate fill pass; a scattered
+    // 16-byte store costs the same DRAM sector as a 4-byte one
+    uint4 rv = make_uint4(0, 0, 0, 0);
+    if (rec) {
+      uint4 a, b;
+      ld256(reinterpret_cast<const uint4*>(hz) + 2 * i, a, b);
+      rv = make_uint4(a.x, a.y, a.z | a.w | b.x | b.y | b.z | b.w,
+                      (uint32_t)(row_base + i) | (row_sp && row_sp[i] ? 0x80000000u : 0u));
+    }
     const uint64_t e = dl_ptr[i + 1];
     for (uint64_t k = dl_ptr[i] + sl; k < e; k += 8) {
       const uint32_t r = dl_col[k];
@@ -86,7 +98,8 @@ __global__ void cold_scatter_kernel(const uint64_t* __restrict__ dl_ptr,
         if ((zm & v) == 0) {
           const uint64_t key = ((uint64_t)v * parts + part) * y_card + y;
           const uint64_t pos = base[key] + atomicSub(&left[key], 1u) - 1u;
-          out[pos * ostride] = (uint32_t)(row_base + i);
+          if (rec) rec[pos] = rv;
+          else out[pos * ostride] = (uint32_t)(row_base + i);
         }
     }
   }
@@ -100,21 +113,6 @@ constexpr uint32_t kRowMask = 0x7fffffffu;
 
 __device__ __forceinline__ uint32_t fold_tail(const uint4& a0, const uint4& a1) {
   return a0.z | a0.w | a1.x | a1.y | a1.z | a1.w;
-}
-
-// The records' signature fields from hz (row ids already in place): one
-// coalesced 16-byte read-modify-write per entry plus the 32-byte hz row.
-__global__ void cold_rec_fill_kernel(uint4* __restrict__ rec, uint64_t cnnz,
-                                     const uint4* __restrict__ hz4,
-                                     const uint8_t* __restrict__ row_sp) {
-  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cnnz;
-       k += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t row = rec[k].w;
-    uint4 a, b;
-    ld256(hz4 + 2 * (uint64_t)row, a, b);
-    const uint32_t fl = row_sp && row_sp[row] ? kSpFlag : 0u;
-    rec[k] = make_uint4(a.x, a.y, fold_tail(a, b), row | fl);
-  }
 }
 
 // ---- the hot filter on a record ----------------------------------------------

@@ -179,6 +179,104 @@ __global__ void hot_build_x_kernel(const uint32_t* __restrict__ xorder, uint64_t
   }
 }
 
+// hx (K = 256: four 64-bit words per x) from the R rows of the live x, 8
+// lanes per x each OR-ing its entries' hot ranks into registers, reduced
+// across the 8 lanes and stored once (no atomics).
+__global__ void hx_build_kernel(const uint32_t* __restrict__ xorder, uint64_t n_live,
+                                const uint64_t* __restrict__ r_ptr,
+                                const uint32_t* __restrict__ r_col,
+                                const uint32_t* __restrict__ y_rank, uint32_t K,
+                                uint4* __restrict__ hx4) {
+  // xorder null: the x codes [0, n_live) in order (coalesced row reads; rows
+  // without entries produce zero masks)
+  const uint32_t sl = threadIdx.x & 7;
+  for (uint64_t p0 = (uint64_t)blockIdx.x * (blockDim.x / 8); p0 < n_live;
+       p0 += (uint64_t)gridDim.x * (blockDim.x / 8)) {
+    const uint64_t p = p0 + (threadIdx.x >> 3);
+    uint64_t w[4] = {0, 0, 0, 0};
+    uint32_t x = 0xffffffffu;
+    if (p < n_live) {
+      x = xorder ? xorder[p] : (uint32_t)p;
+      for (uint64_t k = r_ptr[x] + sl; k < r_ptr[x + 1]; k += 8) {
+        const uint32_t r = y_rank[r_col[k]];
+        if (r < K) w[r >> 6] |= 1ull << (r & 63);
+      }
+    }
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) w[q] |= __shfl_xor_sync(0xffffffffu, w[q], o);
+    if (p < n_live && sl == 0)
+      st256(hx4 + 2 * (uint64_t)x,
+            make_uint4((uint32_t)w[0], (uint32_t)(w[0] >> 32), (uint32_t)w[1], (uint32_t)(w[1] >> 32)),
+            make_uint4((uint32_t)w[2], (uint32_t)(w[2] >> 32), (uint32_t)w[3], (uint32_t)(w[3] >> 32)));
+  }
+}
+
+// Pivot class of each live x read off its hot mask (pivot q = rank q, bit q
+// of word 0); out[16] counts per class.
+__global__ void pivot_class_hx_kernel(const uint32_t* __restrict__ xorder, uint64_t n_live,
+                                      const unsigned long long* __restrict__ hx, uint32_t kw,
+                                      uint32_t n_piv, uint32_t* __restrict__ cls,
+                                      unsigned long long* __restrict__ out) {
+  __shared__ unsigned int c16[16];
+  if (threadIdx.x < 16) c16[threadIdx.x] = 0;
+  __syncthreads();
+  for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n_live;
+       p += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t c = (uint32_t)(hx[(uint64_t)xorder[p] * kw] & ((1u << n_piv) - 1u));
+    cls[p] = c;
+    atomicAdd(&c16[c], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x < 16 && c16[threadIdx.x]) atomicAdd(&out[threadIdx.x], (unsigned long long)c16[threadIdx.x]);
+}
+
+// The slice tables T from the hot masks: a warp owns one 128-x group (lane l
+// holds positions l, l + 32, l + 64, l + 96: the group's four words), so for
+// rank r the group's 16-byte slice is four ballots, kept by lane r % 32 and
+// stored with one 16-byte store per lane per 32 ranks. Every slice of every
+// batch is written (no memset, no atomics); positions past n or holding the
+// empty marker contribute no bits.
+__global__ void hot_T_from_hx_kernel(const uint32_t* __restrict__ xorder, uint64_t n,
+                                     uint64_t n_pos /* whole batches */,
+                                     const uint4* __restrict__ hx4, uint32_t K,
+                                     uint4* __restrict__ T) {
+  const uint32_t lane = lane_id();
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t g = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; g * 128 < n_pos;
+       g += nw) {
+    uint32_t w[4][8];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint64_t p = g * 128 + (uint64_t)j * 32 + lane;
+      uint4 a = make_uint4(0, 0, 0, 0), b = a;
+      if (p < n) {
+        const uint32_t x = xorder[p];
+        if (x != 0xffffffffu) ld256(hx4 + 2 * (uint64_t)x, a, b);
+      }
+      w[j][0] = a.x; w[j][1] = a.y; w[j][2] = a.z; w[j][3] = a.w;
+      w[j][4] = b.x; w[j][5] = b.y; w[j][6] = b.z; w[j][7] = b.w;
+    }
+    const uint64_t bi = g >> 5, gl = g & 31;
+    uint4* base = T + (bi * K) * 32 + gl;  // rank r's slice at base + r * 32
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if ((uint32_t)q * 32 >= K) break;
+      uint4 mine = make_uint4(0, 0, 0, 0);  // lane t keeps rank q * 32 + t
+#pragma unroll
+      for (int t = 0; t < 32; ++t) {
+        const uint32_t m0 = __ballot_sync(0xffffffffu, (w[0][q] >> t) & 1u);
+        const uint32_t m1 = __ballot_sync(0xffffffffu, (w[1][q] >> t) & 1u);
+        const uint32_t m2 = __ballot_sync(0xffffffffu, (w[2][q] >> t) & 1u);
+        const uint32_t m3 = __ballot_sync(0xffffffffu, (w[3][q] >> t) & 1u);
+        if (lane == (uint32_t)t) mine = make_uint4(m0, m1, m2, m3);
+      }
+      base[(uint64_t)(q * 32 + lane) * 32] = mine;
+    }
+  }
+}
+
 // hz from the dense lists (ranks ascending: the hot ranks are a prefix).
 __global__ void hot_build_z_kernel(const uint64_t* __restrict__ dl_ptr,
                                    const uint32_t* __restrict__ dl_col, uint64_t n_dense,

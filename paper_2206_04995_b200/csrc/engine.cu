@@ -610,10 +610,35 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   DBuf<uint32_t> cls;
   DBuf<unsigned long long> pcnt;
   unsigned long long c[48] = {0};
+  // With the cold kernels (K = 256, known before the K estimates return) the
+  // x hot masks come first, built without atomics; the pivot classes are
+  // read off them and the slice tables are transposed from them by ballots.
+  const uint64_t budget_pre = (uint64_t)dense_smem_bytes(X) - 1024;
+  const char* cold_env_pre = std::getenv("D3G_COLD");
+  const bool hx_first = std::min<uint64_t>(1024, budget_pre / 512 / 64 * 64) >= 256 &&
+                        !(cold_env_pre && std::string(cold_env_pre) == "tiers") &&
+                        std::getenv("D3G_K") == nullptr && std::getenv("D3G_HOT") == nullptr;
+  DBuf<unsigned long long> hx;
+  if (hx_first) {
+    hx = X.zeros<unsigned long long>(in.x_card * 4);
+    // every x code of R when the call covers them all (rows read in order),
+    // else the call's live x
+    const bool all_x = in.pos_lo == 0 && in.pos_hi == in.n_live && in.x_lo == 0 &&
+                       in.x_hi >= in.x_card;
+    if (all_x && in.x_card)
+      D3G_LAUNCH(X, hx_build_kernel, grid_for(in.x_card * 8, 256), 256, 0, (const uint32_t*)nullptr,
+                 in.x_card, in.r_ptr, in.r_col, in.y_rank, 256u, reinterpret_cast<uint4*>(hx.p));
+    else if (n_live)
+      D3G_LAUNCH(X, hx_build_kernel, grid_for(n_live * 8, 256), 256, 0, xorder, n_live, in.r_ptr,
+                 in.r_col, in.y_rank, 256u, reinterpret_cast<uint4*>(hx.p));
+  }
   if (piv_pre) {
     cls = X.alloc<uint32_t>(n_live);
     pcnt = X.zeros<unsigned long long>(48);  // x[16] rows[16] sp[16]
-    if (n_live)
+    if (n_live && hx_first)
+      D3G_LAUNCH(X, pivot_class_hx_kernel, grid_for(n_live, 256), 256, 0, xorder, n_live, hx.p, 4u,
+                 n_piv, cls.p, pcnt.p);
+    else if (n_live)
       D3G_LAUNCH(X, pivot_class_x_kernel, grid_for(n_live, 256), 256, 0, xorder, n_live, in.r_ptr,
                  in.r_col, in.y_of_rank, n_piv, cls.p, pcnt.p);
     if (DL)
@@ -824,8 +849,12 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     }
   }
   // hot structures
-  DBuf<uint4> T = X.zeros<uint4>((uint64_t)n_batches * K * 32);
-  DBuf<unsigned long long> hx = X.zeros<unsigned long long>(in.x_card * kw);
+  if (hx_first && (K != 256 || kw != 4))
+    throw d3g::Error(D3G_INTERNAL_ERROR, "hot masks built for K = 256");
+  // (from the masks every word of T is written: no memset)
+  DBuf<uint4> T = hx_first ? X.alloc<uint4>((uint64_t)n_batches * K * 32)
+                           : X.zeros<uint4>((uint64_t)n_batches * K * 32);
+  if (!hx_first) hx = X.zeros<unsigned long long>(in.x_card * kw);
   DBuf<unsigned long long> hz = X.zeros<unsigned long long>(D * kw);
   // z-split: this rank's rows' masks, gathered into hz (every rank's rows)
   DBuf<unsigned long long> hz_loc;
@@ -835,7 +864,11 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     hzl = hz_loc.p;
   }
   if (!xpad.p) hot_xorder = xorder;  // the class-split order when planned
-  if (n_live)
+  if (hx_first && n_batches)
+    D3G_LAUNCH(X, hot_T_from_hx_kernel, grid_for((uint64_t)n_batches * 32 * 32, 256), 256, 0,
+               hot_xorder, hot_n, (uint64_t)n_batches * 4096, reinterpret_cast<const uint4*>(hx.p),
+               K, T.p);
+  else if (n_live)
     D3G_LAUNCH(X, hot_build_x_kernel, grid_for(hot_n * 8, 256), 256, 0, hot_xorder, hot_n,
                in.r_ptr, in.r_col, in.y_rank, K, kw, reinterpret_cast<uint32_t*>(T.p), hx.p);
   if (DL)
@@ -942,12 +975,10 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     DBuf<uint4> crec_l = X.alloc<uint4>(cnnz);
     if (DL)
       D3G_LAUNCH(X, cold_scatter_kernel, grid_for(DL * 8, 256), 256, 0, in.dl_ptr, in.dl_col, DL,
-                 K, in.y_of_rank, cptr.p, cc.p, reinterpret_cast<uint32_t*>(crec_l.p) + 3, 4u, Y,
-                 part_rows, parts, reinterpret_cast<const uint64_t*>(hzl), kw, var_bits, row_lo);
+                 K, in.y_of_rank, cptr.p, cc.p, nullptr, 4u, Y, part_rows, parts,
+                 reinterpret_cast<const uint64_t*>(hzl), kw, var_bits, row_lo, crec_l.p,
+                 in.row_sp);
     cc.reset();
-    if (cnnz)
-      D3G_LAUNCH(X, cold_rec_fill_kernel, grid_for(cnnz, 256), 256, 0, crec_l.p, cnnz,
-                 reinterpret_cast<const uint4*>(hz.p), rsp);
     // the ranks' record counts, their parts gathered rank-major
     uint64_t mine = cnnz;
     std::vector<uint64_t> part_n(N);
@@ -1284,13 +1315,11 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     } else {
       if (cold_kernel_ok) crec = X.alloc<uint4>(cnnz);
       else ccol = X.alloc<uint32_t>(cnnz);
-      uint32_t* cout = cold_kernel_ok ? reinterpret_cast<uint32_t*>(crec.p) + 3 : ccol.p;
       D3G_LAUNCH(X, cold_scatter_kernel, grid_for(D * 8, 256), 256, 0, in.dl_ptr, in.dl_col, D, K,
-                 in.y_of_rank, cptr.p, cc.p, cout, cold_kernel_ok ? 4u : 1u, Y, part_rows, parts,
-                 reinterpret_cast<const uint64_t*>(hz.p), kw, var_bits);
+                 in.y_of_rank, cptr.p, cc.p, ccol.p, 1u, Y, part_rows, parts,
+                 reinterpret_cast<const uint64_t*>(hz.p), kw, var_bits, 0ull,
+                 cold_kernel_ok ? crec.p : nullptr, rsp);
       cc.reset();
-      if (cold_kernel_ok && cnnz)
-        D3G_LAUNCH(X, cold_rec_fill_kernel, grid_for(cnnz, 256), 256, 0, crec.p, cnnz, hz4, rsp);
     }
     if (cold_kernel_ok) {
       DBuf<unsigned int> next = X.zeros<unsigned int>(1);

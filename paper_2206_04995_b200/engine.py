@@ -36,7 +36,9 @@ from dataclasses import dataclass, field, fields
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdim3_b200.so")
+# D3G_LIB: an experiment build of the same library (other compile-time tile
+# constants); the default is the in-tree build
+LIB_PATH = os.environ.get("D3G_LIB") or os.path.join(_HERE, "libdim3_b200.so")
 
 U64P = C.POINTER(C.c_uint64)
 U32P = C.POINTER(C.c_uint32)
