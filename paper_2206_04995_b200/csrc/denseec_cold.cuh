@@ -35,72 +35,109 @@ namespace d3g {
 
 // ---- cold CSR build --------------------------------------------------------
 
-// Per (variant, part, y) the number of dense rows holding y at a cold rank.
-__global__ void cold_count_kernel(const uint64_t* __restrict__ dl_ptr,
-                                  const uint32_t* __restrict__ dl_col, uint64_t n_dense, uint32_t K,
-                                  const uint32_t* __restrict__ y_of_rank, uint32_t* __restrict__ cnt,
-                                  uint64_t y_card, uint32_t part_rows, uint32_t parts,
-                                  const uint64_t* __restrict__ hz, uint32_t kw, uint32_t var_bits,
-                                  uint64_t row_base = 0 /* z-split: global id of row 0 */) {
-  const uint32_t nvar = 1u << var_bits, vmask = nvar - 1;
+// Cold CSR build in two passes with ONE atomic per cold entry (the variant
+// expansion multiplies entries by ~1.7 on cfg5): per (part, y, zm) -- zm the
+// row's top-var_bits hot mask -- a histogram H; the (variant, part, y) counts
+// follow as sums of H over the masks compatible with the variant; the scatter
+// takes each entry's rank within its (part, y, zm) group from a second counter
+// array and places it in every compatible variant at
+//   cptr[v, part, y] + (H of the compatible masks below zm) + rank.
+// Four list entries are in flight per lane (the passes are latency-bound).
+__global__ void cold_hist_kernel(const uint64_t* __restrict__ dl_ptr,
+                                 const uint32_t* __restrict__ dl_col, uint64_t n_dense, uint32_t K,
+                                 const uint32_t* __restrict__ y_of_rank, uint32_t* __restrict__ H,
+                                 uint64_t y_card, uint32_t part_rows,
+                                 const uint64_t* __restrict__ hz, uint32_t kw, uint32_t var_bits,
+                                 uint64_t row_base = 0) {
+  const uint32_t vmask = (1u << var_bits) - 1;
   const uint32_t sl = threadIdx.x & 7;  // 8 lanes per row
   for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 8) + (threadIdx.x >> 3); i < n_dense;
        i += (uint64_t)gridDim.x * (blockDim.x / 8)) {
     const uint64_t part = (row_base + i) / part_rows;
     const uint32_t zm = var_bits ? (uint32_t)(hz[i * kw] & vmask) : 0;
     const uint64_t e = dl_ptr[i + 1];
-    for (uint64_t k = dl_ptr[i] + sl; k < e; k += 8) {
-      const uint32_t r = dl_col[k];
-      if (r < K) continue;
-      const uint32_t y = y_of_rank[r];
-      for (uint32_t v = 0; v < nvar; ++v)
-        if ((zm & v) == 0) atomicAdd(&cnt[((uint64_t)v * parts + part) * y_card + y], 1u);
+    for (uint64_t k0 = dl_ptr[i] + sl; k0 < e; k0 += 32) {
+      uint32_t r[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) r[u] = k0 + 8 * u < e ? dl_col[k0 + 8 * u] : 0u;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (r[u] >= K) atomicAdd(&H[((part * y_card) + y_of_rank[r[u]]) * 8 + zm], 1u);
     }
   }
 }
-
-// Scatter of the row ids into their (variant, part, y) segments:
-// out[pos * ostride] = row (ostride 4 with out = &rec[0].w writes the row
-// field of the 16-byte records; ostride 1 writes a plain column array).
-__global__ void cold_scatter_kernel(const uint64_t* __restrict__ dl_ptr,
-                                    const uint32_t* __restrict__ dl_col, uint64_t n_dense,
-                                    uint32_t K, const uint32_t* __restrict__ y_of_rank,
-                                    const uint64_t* __restrict__ base,
-                                    uint32_t* __restrict__ left /* counts, consumed */,
-                                    uint32_t* __restrict__ out, uint32_t ostride,
-                                    uint64_t y_card, uint32_t part_rows, uint32_t parts,
-                                    const uint64_t* __restrict__ hz, uint32_t kw,
-                                    uint32_t var_bits, uint64_t row_base = 0,
-                                    uint4* __restrict__ rec = nullptr,
-                                    const uint8_t* __restrict__ row_sp = nullptr) {
+// (variant, part, y) counts from H: thread per (part, y)
+__global__ void cold_cnt_from_hist_kernel(const uint32_t* __restrict__ H, uint64_t n_py,
+                                          uint64_t y_card, uint32_t parts, uint32_t var_bits,
+                                          uint32_t* __restrict__ cnt) {
+  const uint32_t nvar = 1u << var_bits;
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n_py;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint4 a = reinterpret_cast<const uint4*>(H)[2 * t], b = reinterpret_cast<const uint4*>(H)[2 * t + 1];
+    const uint32_t h[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    const uint64_t part = t / y_card, y = t % y_card;
+    for (uint32_t v = 0; v < nvar; ++v) {
+      uint32_t c = 0;
+      for (uint32_t zm = 0; zm < nvar; ++zm)
+        if ((zm & v) == 0) c += h[zm];
+      cnt[((uint64_t)v * parts + part) * y_card + y] = c;
+    }
+  }
+}
+__global__ void cold_scatter_hist_kernel(const uint64_t* __restrict__ dl_ptr,
+                                         const uint32_t* __restrict__ dl_col, uint64_t n_dense,
+                                         uint32_t K, const uint32_t* __restrict__ y_of_rank,
+                                         const uint64_t* __restrict__ cptr,
+                                         const uint32_t* __restrict__ H,
+                                         uint32_t* __restrict__ Rk /* zeroed, like H */,
+                                         uint64_t y_card, uint32_t part_rows, uint32_t parts,
+                                         const uint64_t* __restrict__ hz, uint32_t kw,
+                                         uint32_t var_bits, uint64_t row_base,
+                                         uint4* __restrict__ rec, uint32_t* __restrict__ col,
+                                         const uint8_t* __restrict__ row_sp) {
   const uint32_t nvar = 1u << var_bits, vmask = nvar - 1;
   const uint32_t sl = threadIdx.x & 7;  // 8 lanes per row
   for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 8) + (threadIdx.x >> 3); i < n_dense;
        i += (uint64_t)gridDim.x * (blockDim.x / 8)) {
     const uint64_t part = (row_base + i) / part_rows;
     const uint32_t zm = var_bits ? (uint32_t)(hz[i * kw] & vmask) : 0;
-    // rec: the whole 16-byte record is written here (its hot word, folded
-    // tail and flags are the row's), no separate fill pass; a scattered
-    // 16-byte store costs the same DRAM sector as a 4-byte one
     uint4 rv = make_uint4(0, 0, 0, 0);
-    if (rec) {
+    if (rec) {  // the whole record (see cold_scatter_kernel)
       uint4 a, b;
       ld256(reinterpret_cast<const uint4*>(hz) + 2 * i, a, b);
       rv = make_uint4(a.x, a.y, a.z | a.w | b.x | b.y | b.z | b.w,
                       (uint32_t)(row_base + i) | (row_sp && row_sp[i] ? 0x80000000u : 0u));
     }
     const uint64_t e = dl_ptr[i + 1];
-    for (uint64_t k = dl_ptr[i] + sl; k < e; k += 8) {
-      const uint32_t r = dl_col[k];
-      if (r < K) continue;
-      const uint32_t y = y_of_rank[r];
-      for (uint32_t v = 0; v < nvar; ++v)
-        if ((zm & v) == 0) {
-          const uint64_t key = ((uint64_t)v * parts + part) * y_card + y;
-          const uint64_t pos = base[key] + atomicSub(&left[key], 1u) - 1u;
-          if (rec) rec[pos] = rv;
-          else out[pos * ostride] = (uint32_t)(row_base + i);
+    for (uint64_t k0 = dl_ptr[i] + sl; k0 < e; k0 += 32) {
+      uint32_t r[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) r[u] = k0 + 8 * u < e ? dl_col[k0 + 8 * u] : 0u;
+      uint64_t g[4];
+      uint32_t rk[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (r[u] >= K) {
+          g[u] = (part * y_card) + y_of_rank[r[u]];
+          rk[u] = atomicAdd(&Rk[g[u] * 8 + zm], 1u);
         }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (r[u] < K) continue;
+        const uint4 a = reinterpret_cast<const uint4*>(H)[2 * g[u]],
+                    b = reinterpret_cast<const uint4*>(H)[2 * g[u] + 1];
+        const uint32_t h[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+        const uint64_t y = g[u] - part * y_card;
+        for (uint32_t v = 0; v < nvar; ++v) {
+          if (zm & v) continue;
+          uint32_t pre = 0;
+          for (uint32_t z2 = 0; z2 < zm; ++z2)
+            if ((z2 & v) == 0) pre += h[z2];
+          const uint64_t pos = cptr[((uint64_t)v * parts + part) * y_card + y] + pre + rk[u];
+          if (rec) rec[pos] = rv;
+          else col[pos] = (uint32_t)(row_base + i);
+        }
+      }
     }
   }
 }

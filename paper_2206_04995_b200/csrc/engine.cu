@@ -932,7 +932,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   uint32_t parts = 1, part_rows = (uint32_t)(((D + 31) / 32) * 32);
   uint32_t var_bits = 0;
   uint64_t rows_key = 0, cnnz = 0;
-  DBuf<uint32_t> cc;
+  DBuf<uint32_t> cc, ch;  // (variant, part, y) counts; (part, y, mask) histogram
   DBuf<uint64_t> cptr;
   if (run_cold) {
     if (cold_bitmap) {
@@ -952,11 +952,17 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     if (cold_kernel_ok && std::getenv("D3G_VAR_BITS"))  // experiments: 0..4
       var_bits = (uint32_t)std::min<uint64_t>(env_u32("D3G_VAR_BITS", var_bits, 0, 4), Y);
     rows_key = ((uint64_t)1 << var_bits) * parts * Y;
-    cc = X.zeros<uint32_t>(rows_key);
+    // per (part, y, top-mask) histogram, then the (variant, part, y) counts
+    const uint64_t n_py = (uint64_t)parts * Y;
+    ch = X.zeros<uint32_t>(n_py * 8);
     if (DL)
-      D3G_LAUNCH(X, cold_count_kernel, grid_for(DL * 8, 256), 256, 0, in.dl_ptr, in.dl_col, DL, K,
-                 in.y_of_rank, cc.p, Y, part_rows, parts,
-                 reinterpret_cast<const uint64_t*>(hzl), kw, var_bits, row_lo);
+      D3G_LAUNCH(X, cold_hist_kernel, grid_for(DL * 8, 256), 256, 0, in.dl_ptr, in.dl_col, DL, K,
+                 in.y_of_rank, ch.p, Y, part_rows, reinterpret_cast<const uint64_t*>(hzl), kw,
+                 var_bits, row_lo);
+    cc = X.alloc<uint32_t>(rows_key);
+    if (n_py)
+      D3G_LAUNCH(X, cold_cnt_from_hist_kernel, grid_for(n_py, 256), 256, 0, ch.p, n_py, Y, parts,
+                 var_bits, cc.p);
     cptr = X.alloc<uint64_t>(rows_key + 1);
     exclusive_scan<uint32_t>(X, cc.p, rows_key, cptr.p);
     X.defer(&cnnz, cptr.p + rows_key, 8);
@@ -973,12 +979,15 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     DBuf<uint64_t> cp_all = X.alloc<uint64_t>((rows_key + 1) * N);
     ex_allgatherv_dev(X, *in.zx, cptr.p, std::vector<uint64_t>(N, rows_key + 1), 8, cp_all.p);
     DBuf<uint4> crec_l = X.alloc<uint4>(cnnz);
-    if (DL)
-      D3G_LAUNCH(X, cold_scatter_kernel, grid_for(DL * 8, 256), 256, 0, in.dl_ptr, in.dl_col, DL,
-                 K, in.y_of_rank, cptr.p, cc.p, nullptr, 4u, Y, part_rows, parts,
+    if (DL) {
+      DBuf<uint32_t> rk = X.zeros<uint32_t>((uint64_t)parts * Y * 8);
+      D3G_LAUNCH(X, cold_scatter_hist_kernel, grid_for(DL * 8, 256), 256, 0, in.dl_ptr, in.dl_col,
+                 DL, K, in.y_of_rank, cptr.p, ch.p, rk.p, Y, part_rows, parts,
                  reinterpret_cast<const uint64_t*>(hzl), kw, var_bits, row_lo, crec_l.p,
-                 in.row_sp);
+                 (uint32_t*)nullptr, in.row_sp);
+    }
     cc.reset();
+    ch.reset();
     // the ranks' record counts, their parts gathered rank-major
     uint64_t mine = cnnz;
     std::vector<uint64_t> part_n(N);
@@ -1315,11 +1324,13 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     } else {
       if (cold_kernel_ok) crec = X.alloc<uint4>(cnnz);
       else ccol = X.alloc<uint32_t>(cnnz);
-      D3G_LAUNCH(X, cold_scatter_kernel, grid_for(D * 8, 256), 256, 0, in.dl_ptr, in.dl_col, D, K,
-                 in.y_of_rank, cptr.p, cc.p, ccol.p, 1u, Y, part_rows, parts,
+      DBuf<uint32_t> rk = X.zeros<uint32_t>((uint64_t)parts * Y * 8);
+      D3G_LAUNCH(X, cold_scatter_hist_kernel, grid_for(D * 8, 256), 256, 0, in.dl_ptr, in.dl_col,
+                 D, K, in.y_of_rank, cptr.p, ch.p, rk.p, Y, part_rows, parts,
                  reinterpret_cast<const uint64_t*>(hz.p), kw, var_bits, 0ull,
-                 cold_kernel_ok ? crec.p : nullptr, rsp);
+                 cold_kernel_ok ? crec.p : nullptr, ccol.p, rsp);
       cc.reset();
+      ch.reset();
     }
     if (cold_kernel_ok) {
       DBuf<unsigned int> next = X.zeros<unsigned int>(1);
