@@ -102,7 +102,10 @@ __global__ void cold_scatter_hist_kernel(const uint64_t* __restrict__ dl_ptr,
     const uint64_t part = (row_base + i) / part_rows;
     const uint32_t zm = var_bits ? (uint32_t)(hz[i * kw] & vmask) : 0;
     uint4 rv = make_uint4(0, 0, 0, 0);
-    if (rec) {  // the whole record (see cold_scatter_kernel)
+    // rec: the whole 16-byte record is written here (its hot word, folded tail
+    // and flags are the row's); a scattered 16-byte store costs the same DRAM
+    // sector as a 4-byte one
+    if (rec) {
       uint4 a, b;
       ld256(reinterpret_cast<const uint4*>(hz) + 2 * i, a, b);
       rv = make_uint4(a.x, a.y, a.z | a.w | b.x | b.y | b.z | b.w,

@@ -681,7 +681,9 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   if (cc_env) cold_ctas = std::max(1, std::atoi(cc_env));
   const uint64_t cold_rows_cap =
       std::max<uint64_t>(32, (budget / cold_ctas / kColdWarps - (kDQ + kSegWords) * 4) * 8 / 32 * 32);
-  const bool cold_bitmap = k_cap >= 256 && (D + cold_rows_cap - 1) / cold_rows_cap <= 16;
+  const char* cpath_env = std::getenv("D3G_COLD_PATH");  // experiments: hash | bitmap
+  const bool cold_bitmap = k_cap >= 256 && (D + cold_rows_cap - 1) / cold_rows_cap <= 16 &&
+                           !(cpath_env && std::string(cpath_env) == "hash");
   // larger dense blocks: the same candidate stream, survivors in a per-warp
   // hash set (dense_cold_hash_kernel); D3G_COLD=tiers keeps the SparseBMM tiers
   const char* cold_env = std::getenv("D3G_COLD");
