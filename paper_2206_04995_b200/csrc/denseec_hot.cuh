@@ -27,7 +27,12 @@
 
 namespace d3g {
 
-constexpr int kHotThreads = 1024;
+#ifndef D3G_HOT_THREADS
+#define D3G_HOT_THREADS 768  // 24 warps, 80 registers (1024: 64 and twice the spills; cfg5 hot 20.8 -> 20.1 ms)
+#endif
+constexpr int kHotThreads = D3G_HOT_THREADS;
+// pivot classes: up to 6 pivots (the top ranks), 64 classes of x and rows
+constexpr uint32_t kMaxPivots = 6, kMaxClasses = 1u << kMaxPivots;
 
 struct HotParams {
   const uint4* T;          // [batch of 32 groups][K][32] (uint4 = 128 member bits)
@@ -47,8 +52,8 @@ struct HotParams {
   // tests all rows in z_chunks ranges.
   const uint32_t* unit_off = nullptr;  // [n_batches + 1] first unit of each batch
   const uint8_t* batch_kind = nullptr; // [n_batches] row-range kind 0..15
-  uint64_t run_lo[17] = {};  // class c's rows: [run_lo[c], run_lo[c + 1]) (class-major order)
-  uint32_t run_zc[16] = {};  // chunks (units per batch) of class c's run
+  uint64_t run_lo[kMaxClasses + 1] = {};  // class c's rows: [run_lo[c], run_lo[c + 1]) (class-major)
+  uint32_t run_zc[kMaxClasses] = {};      // chunks (units per batch) of class c's run
   uint32_t n_classes = 1;
   uint32_t plan_units = 0;
   uint32_t plan_on = 0;  // 1: units follow the plan (plan_units may be 0)
@@ -103,8 +108,8 @@ __global__ void pivot_class_x_kernel(const uint32_t* __restrict__ xorder, uint64
                                      const uint32_t* __restrict__ r_col,
                                      const uint32_t* __restrict__ y_of_rank, uint32_t n_piv,
                                      uint32_t* __restrict__ cls, unsigned long long* __restrict__ out) {
-  __shared__ unsigned int c8[16];
-  if (threadIdx.x < 16) c8[threadIdx.x] = 0;
+  __shared__ unsigned int c8[kMaxClasses];
+  if (threadIdx.x < kMaxClasses) c8[threadIdx.x] = 0;
   __syncthreads();
   for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n_live;
        p += (uint64_t)gridDim.x * blockDim.x) {
@@ -124,18 +129,19 @@ __global__ void pivot_class_x_kernel(const uint32_t* __restrict__ xorder, uint64
     atomicAdd(&c8[c], 1u);
   }
   __syncthreads();
-  if (threadIdx.x < 16 && c8[threadIdx.x]) atomicAdd(&out[threadIdx.x], (unsigned long long)c8[threadIdx.x]);
+  if (threadIdx.x < kMaxClasses && c8[threadIdx.x])
+    atomicAdd(&out[threadIdx.x], (unsigned long long)c8[threadIdx.x]);
 }
 
 // Dense rows per pivot class (bit q = holds rank q; the lists are
 // rank-ascending, so the pivots sit at the front) and folded sparse rows per
-// class: out[0..15] rows, out[16..31] flagged rows.
+// class: out[0, kMaxClasses) rows, out[kMaxClasses, 2 kMaxClasses) flagged rows.
 __global__ void pivot_class_rows_kernel(const uint64_t* __restrict__ dl_ptr,
                                         const uint32_t* __restrict__ dl_col, uint64_t n,
                                         uint32_t n_piv, const uint8_t* __restrict__ row_sp,
                                         unsigned long long* __restrict__ out) {
-  __shared__ unsigned int c16[32];
-  if (threadIdx.x < 32) c16[threadIdx.x] = 0;
+  __shared__ unsigned int c16[2 * kMaxClasses];
+  if (threadIdx.x < 2 * kMaxClasses) c16[threadIdx.x] = 0;
   __syncthreads();
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
@@ -146,10 +152,11 @@ __global__ void pivot_class_rows_kernel(const uint64_t* __restrict__ dl_ptr,
       if (r < n_piv) c |= 1u << r; else break;
     }
     atomicAdd(&c16[c], 1u);
-    if (row_sp && row_sp[i]) atomicAdd(&c16[16 + c], 1u);
+    if (row_sp && row_sp[i]) atomicAdd(&c16[kMaxClasses + c], 1u);
   }
   __syncthreads();
-  if (threadIdx.x < 32 && c16[threadIdx.x]) atomicAdd(&out[threadIdx.x], (unsigned long long)c16[threadIdx.x]);
+  if (threadIdx.x < 2 * kMaxClasses && c16[threadIdx.x])
+    atomicAdd(&out[threadIdx.x], (unsigned long long)c16[threadIdx.x]);
 }
 
 // T, hx from the live x in degree order: warp per x position.
@@ -219,8 +226,8 @@ __global__ void pivot_class_hx_kernel(const uint32_t* __restrict__ xorder, uint6
                                       const unsigned long long* __restrict__ hx, uint32_t kw,
                                       uint32_t n_piv, uint32_t* __restrict__ cls,
                                       unsigned long long* __restrict__ out) {
-  __shared__ unsigned int c16[16];
-  if (threadIdx.x < 16) c16[threadIdx.x] = 0;
+  __shared__ unsigned int c16[kMaxClasses];
+  if (threadIdx.x < kMaxClasses) c16[threadIdx.x] = 0;
   __syncthreads();
   for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n_live;
        p += (uint64_t)gridDim.x * blockDim.x) {
@@ -229,7 +236,8 @@ __global__ void pivot_class_hx_kernel(const uint32_t* __restrict__ xorder, uint6
     atomicAdd(&c16[c], 1u);
   }
   __syncthreads();
-  if (threadIdx.x < 16 && c16[threadIdx.x]) atomicAdd(&out[threadIdx.x], (unsigned long long)c16[threadIdx.x]);
+  if (threadIdx.x < kMaxClasses && c16[threadIdx.x])
+    atomicAdd(&out[threadIdx.x], (unsigned long long)c16[threadIdx.x]);
 }
 
 // The slice tables T from the hot masks: a warp owns one 128-x group (lane l

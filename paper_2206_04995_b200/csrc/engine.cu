@@ -543,7 +543,7 @@ __global__ void hot_small_stats_kernel(const uint32_t* __restrict__ cnt_rank,
 // Class-aligned hot positions: the x at class-split position i (class q =
 // cls[i], its rank within the class i - cstart[q]) goes to pstart[q] + that.
 struct PadStarts {
-  uint64_t cstart[16], pstart[16];
+  uint64_t cstart[d3g::kMaxClasses], pstart[d3g::kMaxClasses];
 };
 __global__ void pad_scatter_kernel(const uint32_t* __restrict__ cls, const uint32_t* __restrict__ xs,
                                    uint64_t n, PadStarts ps, uint32_t* __restrict__ out) {
@@ -604,12 +604,15 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   const double units_pre = (double)n_batches_pre * (double)D;
   // measured: cfg5 (2.4e10 units) 2/3/4 pivots 153/135/132 ms; cfg2 (1e7)
   // 2.30/2.31/2.41 ms
-  const uint32_t piv_dflt = units_pre > 1e10 ? 4u : units_pre > 1e9 ? 3u : 2u;
+  // (cfg5, 2.4e10 units: 4 / 5 / 6 pivots 93.7 / 93.3 / 93.3 ms; cfg2, 1e7: 2.30 / 2.42 / 2.68)
+  const uint32_t piv_dflt = units_pre > 1e10 ? 5u : units_pre > 1e9 ? 3u : 2u;
   const uint32_t n_piv =
-      (uint32_t)std::min<uint64_t>(env_u32("D3G_PIVOTS", piv_dflt, 1, 4), std::max<uint64_t>(Y, 1));
+      (uint32_t)std::min<uint64_t>(env_u32("D3G_PIVOTS", piv_dflt, 1, kMaxPivots), std::max<uint64_t>(Y, 1));
   DBuf<uint32_t> cls;
   DBuf<unsigned long long> pcnt;
-  unsigned long long c[48] = {0};
+  // pivot-class counts: x [kMaxClasses] | rows [kMaxClasses] | folded sparse rows [kMaxClasses]
+  constexpr uint32_t kMC = kMaxClasses;
+  unsigned long long c[3 * kMC] = {0};
   // With the cold kernels (K = 256, known before the K estimates return) the
   // x hot masks come first, built without atomics; the pivot classes are
   // read off them and the slice tables are transposed from them by ballots.
@@ -634,7 +637,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   }
   if (piv_pre) {
     cls = X.alloc<uint32_t>(n_live);
-    pcnt = X.zeros<unsigned long long>(48);  // x[16] rows[16] sp[16]
+    pcnt = X.zeros<unsigned long long>(3 * kMC);
     if (n_live && hx_first)
       D3G_LAUNCH(X, pivot_class_hx_kernel, grid_for(n_live, 256), 256, 0, xorder, n_live, hx.p, 4u,
                  n_piv, cls.p, pcnt.p);
@@ -643,15 +646,15 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
                  in.r_col, in.y_of_rank, n_piv, cls.p, pcnt.p);
     if (DL)
       D3G_LAUNCH(X, pivot_class_rows_kernel, grid_for(DL, 256), 256, 0, in.dl_ptr, in.dl_col, DL,
-                 n_piv, in.row_sp, pcnt.p + 16);
+                 n_piv, in.row_sp, pcnt.p + kMC);
   }
   unsigned long long e[2 * kKCand + 11];
   X.defer(e, est.p, (2 * kKCand + 11) * 8);
-  if (piv_pre) X.defer(c, pcnt.p, 48 * 8);
+  if (piv_pre) X.defer(c, pcnt.p, 3 * kMC * 8);
   X.sync();
   // z-split: the dense-row class counts of the job (the x classes stay local)
   if (zs && piv_pre)
-    ex_allreduce_host(X, *in.zx, reinterpret_cast<uint64_t*>(c + 16), 32, D3G_EX_SUM_U64);
+    ex_allreduce_host(X, *in.zx, reinterpret_cast<uint64_t*>(c + kMC), 2 * kMC, D3G_EX_SUM_U64);
   const unsigned long long* top_rank_rows = e + 2 * kKCand;   // [7]
   const unsigned long long* top_rank_dr = e + 2 * kKCand + 7;  // [4]
   static const uint32_t kv[kKCand] = {64, 128, 256, 512, 1024};
@@ -731,18 +734,18 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   uint64_t hot_n = n_live;
   DBuf<uint32_t> xpad;
   uint64_t plan_direct = 0, plan_direct_sp = 0;  // untested hits (all / folded sparse rows)
-  uint64_t run_lo[17] = {0};     // class c's rows [run_lo[c], run_lo[c + 1])
-  uint32_t run_zc[16] = {0};     // units per batch over class c's run
-  uint64_t run_mult[16] = {0};   // batches that test class c's run
+  uint64_t run_lo[kMC + 1] = {0};  // class c's rows [run_lo[c], run_lo[c + 1])
+  uint32_t run_zc[kMC] = {0};      // units per batch over class c's run
+  uint64_t run_mult[kMC] = {0};    // batches that test class c's run
   std::vector<uint32_t> unit_off_h;
   std::vector<uint8_t> batch_kind_h;
   DBuf<uint32_t> xsplit;
   const bool try_plan = piv_pre && tab_planned && top_rank_rows[0] > 0;
   if (try_plan) {
     const unsigned long long* nx = c;       // x per class
-    const unsigned long long* nr = c + 16;  // dense rows per class
-    const unsigned long long* nsp = c + 32; // folded sparse rows per class
-    uint64_t kind_rows[16] = {}, sp_rows[16] = {}, sp_all = 0;
+    const unsigned long long* nr = c + kMC;       // dense rows per class
+    const unsigned long long* nsp = c + 2 * kMC;  // folded sparse rows per class
+    uint64_t kind_rows[kMC] = {}, sp_rows[kMC] = {}, sp_all = 0;
     for (uint32_t q = 0; q < n_kinds; ++q) sp_all += nsp[q];
     for (uint32_t k = 0; k < n_kinds; ++k)
       for (uint32_t q = 0; q < n_kinds; ++q)
@@ -751,8 +754,8 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
           sp_rows[k] += nsp[q];
         }
     // class q occupies x positions [cstart[q], cstart[q + 1]) after the split
-    uint64_t cstart[17] = {0};
-    for (uint32_t q = 0; q < 16; ++q) cstart[q + 1] = cstart[q] + (q < n_kinds ? nx[q] : 0);
+    uint64_t cstart[kMC + 1] = {0};
+    for (uint32_t q = 0; q < kMC; ++q) cstart[q + 1] = cstart[q] + (q < n_kinds ? nx[q] : 0);
     batch_kind_h.assign(n_batches, 0);
     double tested = 0;
     uint64_t direct = 0, direct_sp = 0;
@@ -772,7 +775,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     // only) tests EVERY row, and an x shard has such boundaries of its own.
     // (z-split: class 0 -- x holding no pivot, so every row is tested -- is
     // pooled across the ranks into shared batches, see below)
-    uint64_t pstart[17] = {0};
+    uint64_t pstart[kMC + 1] = {0};
     double tested_pad = 0;
     for (uint32_t q = 0; q < n_kinds; ++q) {
       const uint64_t nb = (share0_try && q == 0) ? 0 : (nx[q] + 4095) / 4096;
@@ -803,7 +806,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
         xpad = X.alloc<uint32_t>(hot_n);
         D3G_CUDA(cudaMemsetAsync(xpad.p, 0xff, hot_n * 4, X.stream));  // empty positions
         PadStarts ps{};
-        for (uint32_t q = 0; q < 16; ++q) {
+        for (uint32_t q = 0; q < kMC; ++q) {
           ps.cstart[q] = cstart[q];
           ps.pstart[q] = pstart[q];
         }
@@ -1048,8 +1051,8 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     X.to_device(batch_kind_d.p, batch_kind_h.data(), n_batches);
     hp.unit_off = unit_off_d.p;
     hp.batch_kind = batch_kind_d.p;
-    for (uint32_t q = 0; q <= 16; ++q) hp.run_lo[q] = run_lo[q];
-    for (uint32_t q = 0; q < 16; ++q) hp.run_zc[q] = run_zc[q];
+    for (uint32_t q = 0; q <= kMC; ++q) hp.run_lo[q] = run_lo[q];
+    for (uint32_t q = 0; q < kMC; ++q) hp.run_zc[q] = run_zc[q];
     hp.n_classes = n_kinds;
     hp.plan_units = unit_off_h[n_batches];
     hp.plan_on = 1;
@@ -1078,8 +1081,8 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     h0.groups = (uint32_t)((n0_job + 127) / 128);
     h0.unit_off = uoff0.p;
     h0.batch_kind = bkind0.p;
-    for (uint32_t q = 0; q <= 16; ++q) h0.run_lo[q] = q == 0 ? sh_lo : sh_hi;
-    for (uint32_t q = 0; q < 16; ++q) h0.run_zc[q] = q == 0 ? (slice ? zc0 : 0u) : 0u;
+    for (uint32_t q = 0; q <= kMC; ++q) h0.run_lo[q] = q == 0 ? sh_lo : sh_hi;
+    for (uint32_t q = 0; q < kMC; ++q) h0.run_zc[q] = q == 0 ? (slice ? zc0 : 0u) : 0u;
     h0.n_classes = 1;
     h0.plan_units = uo[nb0];
     h0.plan_on = 1;
