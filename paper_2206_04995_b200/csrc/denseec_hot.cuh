@@ -220,6 +220,34 @@ __global__ void hx_build_kernel(const uint32_t* __restrict__ xorder, uint64_t n_
   }
 }
 
+// The same masks, one thread per x code in order (all x of R): a thread walks
+// its own row (adjacent threads read adjacent rows: L1 serves the rest of
+// each line), four rank lookups in flight, no shuffles; rows without
+// entries get zero masks.
+__global__ void hx_build_rows_kernel(uint64_t n_rows, const uint64_t* __restrict__ r_ptr,
+                                     const uint32_t* __restrict__ r_col,
+                                     const uint32_t* __restrict__ y_rank, uint32_t K,
+                                     uint4* __restrict__ hx4) {
+  for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n_rows;
+       x += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t w[4] = {0, 0, 0, 0};
+    const uint64_t e = r_ptr[x + 1];
+    for (uint64_t k = r_ptr[x]; k < e; k += 4) {
+      uint32_t y[4], r[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) y[u] = k + u < e ? r_col[k + u] : 0xffffffffu;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) r[u] = y[u] != 0xffffffffu ? y_rank[y[u]] : K;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (r[u] < K) w[r[u] >> 6] |= 1ull << (r[u] & 63);
+    }
+    st256(hx4 + 2 * x,
+          make_uint4((uint32_t)w[0], (uint32_t)(w[0] >> 32), (uint32_t)w[1], (uint32_t)(w[1] >> 32)),
+          make_uint4((uint32_t)w[2], (uint32_t)(w[2] >> 32), (uint32_t)w[3], (uint32_t)(w[3] >> 32)));
+  }
+}
+
 // Pivot class of each live x read off its hot mask (pivot q = rank q, bit q
 // of word 0); out[16] counts per class.
 __global__ void pivot_class_hx_kernel(const uint32_t* __restrict__ xorder, uint64_t n_live,

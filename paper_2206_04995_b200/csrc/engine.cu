@@ -598,14 +598,17 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   // the pivot-plan class counts (count-only) ride on the same read-back
   const bool piv_pre = mode == kModeCount && std::getenv("D3G_HOT") == nullptr &&
                        std::getenv("D3G_NO_SPLIT") == nullptr && Y >= 1;
-  // (z-split: from the job's live x, so every rank picks the same pivots)
+  // (z-split: from a rank's share of the job's live x, so every rank picks
+  // the same pivots)
   const uint32_t n_batches_pre =
-      zs ? (uint32_t)((in.n_live_job + 4095) / 4096) : (groups + 31) / 32;
+      zs ? (uint32_t)((in.n_live_job / (uint64_t)in.zx->nranks + 4095) / 4096) : (groups + 31) / 32;
   const double units_pre = (double)n_batches_pre * (double)D;
   // measured: cfg5 (2.4e10 units) 2/3/4 pivots 153/135/132 ms; cfg2 (1e7)
   // 2.30/2.31/2.41 ms
   // (cfg5, 2.4e10 units: 4 / 5 / 6 pivots 93.7 / 93.3 / 93.3 ms; cfg2, 1e7: 2.30 / 2.42 / 2.68)
-  const uint32_t piv_dflt = units_pre > 1e10 ? 5u : units_pre > 1e9 ? 3u : 2u;
+  // (a rank of the 8-way sharded cfg5, 3e9: 4 pivots; 5 gave it 32 partial
+  // class batches)
+  const uint32_t piv_dflt = units_pre > 1e10 ? 5u : units_pre > 2e9 ? 4u : units_pre > 1e9 ? 3u : 2u;
   const uint32_t n_piv =
       (uint32_t)std::min<uint64_t>(env_u32("D3G_PIVOTS", piv_dflt, 1, kMaxPivots), std::max<uint64_t>(Y, 1));
   DBuf<uint32_t> cls;
@@ -629,7 +632,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     const bool all_x = in.pos_lo == 0 && in.pos_hi == in.n_live && in.x_lo == 0 &&
                        in.x_hi >= in.x_card;
     if (all_x && in.x_card)
-      D3G_LAUNCH(X, hx_build_kernel, grid_for(in.x_card * 8, 256), 256, 0, (const uint32_t*)nullptr,
+      D3G_LAUNCH(X, hx_build_rows_kernel, grid_for(in.x_card, 256, X.sm_count * 32), 256, 0,
                  in.x_card, in.r_ptr, in.r_col, in.y_rank, 256u, reinterpret_cast<uint4*>(hx.p));
     else if (n_live)
       D3G_LAUNCH(X, hx_build_kernel, grid_for(n_live * 8, 256), 256, 0, xorder, n_live, in.r_ptr,
