@@ -447,20 +447,32 @@ inline bool build_csr_bucketed(Ctx& ctx, const uint32_t* maj, const uint32_t* mn
          r + 1 + mb <= 32)
     ++r;
   if (r + mb > 32 || per_row * (double)(1ull << r) > 0.9 * kCbCap) return false;
-  const uint64_t nb64 = (n_rows + (1ull << r) - 1) >> r;
-  if (nb64 > kCbMaxBuckets) return false;
-  const uint32_t nb = (uint32_t)nb64;
-  DBuf<unsigned int> hist = ctx.zeros<unsigned int>(nb);
-  const unsigned g = (unsigned)std::min<uint64_t>(ctx.sm_count * 2ull, (n + kCbThreads - 1) / kCbThreads);
-  const size_t hsm = (size_t)nb * 4;
-  D3G_CUDA(cudaFuncSetAttribute(csr_bucket_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)hsm));
-  D3G_LAUNCH(ctx, csr_bucket_hist_kernel, g, kCbThreads, hsm, maj, n, r, nb, hist.p);
-  DBuf<unsigned long long> bstart = ctx.alloc<unsigned long long>(nb + 1);
+  // The rows may be far from uniform (an x shard of R: its x sit in one code
+  // range of a job-sized row space): when the fullest bucket overflows the
+  // shared-memory capacity, halve the bucket (up to 3 times) before giving up
+  // to the scatter path.
+  uint32_t nb = 0;
+  DBuf<unsigned int> hist;
+  DBuf<unsigned long long> bstart;
+  for (int attempt = 0;; ++attempt) {
+    const uint64_t nb64 = (n_rows + (1ull << r) - 1) >> r;
+    if (nb64 > kCbMaxBuckets) return false;
+    nb = (uint32_t)nb64;
+    hist = ctx.zeros<unsigned int>(nb);
+    const unsigned g = (unsigned)std::min<uint64_t>(ctx.sm_count * 2ull, (n + kCbThreads - 1) / kCbThreads);
+    const size_t hsm = (size_t)nb * 4;
+    D3G_CUDA(cudaFuncSetAttribute(csr_bucket_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)hsm));
+    D3G_LAUNCH(ctx, csr_bucket_hist_kernel, g, kCbThreads, hsm, maj, n, r, nb, hist.p);
+    DBuf<unsigned long long> mxb = ctx.zeros<unsigned long long>(1);
+    D3G_LAUNCH(ctx, max_u32_kernel, grid_for(nb, 256), 256, 0, hist.p, (uint64_t)nb, mxb.p);
+    const unsigned long long mx = ctx.scalar(mxb.p);
+    if (mx <= kCbCap) break;
+    if (attempt == 3 || r == 0) return false;
+    r = std::max(0, r - std::max(1, (int)std::ceil(std::log2((double)mx / (0.9 * kCbCap)))));
+  }
+  bstart = ctx.alloc<unsigned long long>(nb + 1);
   exclusive_scan<unsigned int>(ctx, hist.p, nb, reinterpret_cast<uint64_t*>(bstart.p));
-  DBuf<unsigned long long> mxb = ctx.zeros<unsigned long long>(1);
-  D3G_LAUNCH(ctx, max_u32_kernel, grid_for(nb, 256), 256, 0, hist.p, (uint64_t)nb, mxb.p);
-  if (ctx.scalar(mxb.p) > kCbCap) return false;
   DBuf<unsigned long long> cursor = ctx.alloc<unsigned long long>(nb);
   D3G_CUDA(cudaMemcpyAsync(cursor.p, bstart.p, (size_t)nb * 8, cudaMemcpyDeviceToDevice, ctx.stream));
   DBuf<uint32_t> packed = ctx.alloc<uint32_t>(n);
