@@ -616,9 +616,9 @@ dense_cold_hash_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
 }
 
 // The per-x candidate loop of the CTA kernels: chunks of kThreads of x's y
-// rows, compacted across the CTA; each warp walks its own 32-candidate
-// windows (its first segment by one warp-uniform binary search, the rest from
-// the window's boundary mask). Candidates are handed to on(st, row) as in
+// rows, compacted across the CTA; each warp walks one contiguous share of the
+// chunk's candidates in 32-candidate windows (its first segment by one
+// warp-uniform binary search, the rest from the windows' boundary masks). Candidates are handed to on(st, row) as in
 // warp_cold_x; step() runs after each group of windows (per warp). The loop
 // stops at the next check once *stop is set (CTA-uniform). Returns this
 // thread's candidates streamed.
@@ -643,27 +643,29 @@ __device__ __forceinline__ uint64_t cta_cold_x(const ColdX& s, uint64_t r0, uint
     }
     uint32_t n;
     const uint32_t total = cta_stream_chunk<kThreads>(sg0, len, s_seg0, s_off, s_wsum, s_tot, n);
-    for (uint32_t fb0 = 32 * warp; fb0 < total && !*stop; fb0 += kThreads * kColdU) {
+    // each warp streams one contiguous share of the chunk: its first segment
+    // by one binary search, then the windows advance it from their masks
+    constexpr uint32_t kW = kThreads / 32;
+    const uint32_t per = ((total + kW - 1) / kW + 31) & ~31u;
+    const uint32_t beg = min(total, warp * per), end = min(total, beg + per);
+    uint32_t c0 = beg < end ? seg_search(beg, n, s_off) : 0u;
+    for (uint32_t tb = beg; tb < end && !*stop; tb += 32 * kColdU) {
       uint64_t t[kColdU];
 #pragma unroll
       for (int u = 0; u < kColdU; ++u) {
-        const uint32_t wb = fb0 + u * kThreads;
-        t[u] = 0;
-        if (wb < total) {
-          uint32_t c0 = seg_search(wb, n, s_off);
-          t[u] = warp_window(wb, c0, n, s_seg0, s_off);
-        }
+        const uint32_t wb = tb + 32 * u;
+        t[u] = wb < end ? warp_window(wb, c0, n, s_seg0, s_off) : 0;
       }
       uint4 c[kColdU];
 #pragma unroll
       for (int u = 0; u < kColdU; ++u)
-        if (fb0 + u * kThreads + lane < total) {
+        if (tb + 32 * u + lane < end) {
           ++mine;
           c[u] = ld_rec(crec + t[u]);
         }
 #pragma unroll
       for (int u = 0; u < kColdU; ++u) {
-        const bool ok = fb0 + u * kThreads + lane < total;
+        const bool ok = tb + 32 * u + lane < end;
         on(ok ? cold_test(c[u], s) : (uint32_t)kColdHot, ok ? c[u].w : 0u);
       }
       step();
