@@ -509,6 +509,8 @@ constexpr uint32_t kCHEmpty = 0xffffffffu;
 constexpr size_t kCHSmem = (size_t)kCHWarps * (kCHSlots + kDQ + kSegWords) * 4;
 
 __device__ __forceinline__ uint32_t ch_slot(uint32_t v) { return (v * 0x9E3779B1u) >> (32 - D3G_CH_BITS); }
+// odd probe step (covers every slot of a power-of-two table)
+__device__ __forceinline__ uint32_t probe_step(uint32_t v) { return ((v * 0x85EBCA6Bu) >> 20) | 1u; }
 
 template <int kMode>
 __global__ void __launch_bounds__(kCHWarps * 32, D3G_CH_CTAS)
@@ -549,6 +551,7 @@ dense_cold_hash_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
       bool fresh = false;
       if (ok) {
         uint32_t sl = ch_slot(key);
+        const uint32_t step = probe_step(key);  // double hashing: short chains at high load
         for (;;) {
           const uint32_t prev = atomicCAS(&tab[sl], kCHEmpty, key);
           if (prev == kCHEmpty) {
@@ -556,7 +559,7 @@ dense_cold_hash_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
             break;
           }
           if (prev == key) break;
-          sl = (sl + 1) & (kCHSlots - 1);
+          sl = (sl + step) & (kCHSlots - 1);
         }
       }
       if (fresh && (key & kSpFlag)) ++xsp;
@@ -735,6 +738,7 @@ dense_cold_cta_kernel(const uint32_t* __restrict__ over_x, const unsigned int* _
     auto ins = [&](bool ok, uint32_t key) {
       if (!ok) return;
       uint32_t sl = cc_slot(key);
+      const uint32_t step = probe_step(key);
       for (uint32_t probe = 0; probe < kCCSlots; ++probe) {
         const uint32_t prev = atomicCAS(&cctab[sl], kCHEmpty, key);
         if (prev == kCHEmpty) {
@@ -743,7 +747,7 @@ dense_cold_cta_kernel(const uint32_t* __restrict__ over_x, const unsigned int* _
           break;
         }
         if (prev == key) break;
-        sl = (sl + 1) & (kCCSlots - 1);
+        sl = (sl + step) & (kCCSlots - 1);
       }
     };
     auto flush_ins = [&]() {
