@@ -3,6 +3,9 @@
 // hashing (mix64, common.hpp:42-49), and small warp/block helpers.
 #pragma once
 
+#include <mutex>
+#include <unordered_map>
+
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -445,6 +448,22 @@ __device__ __forceinline__ void tally_flush(Tally* t, uint64_t cnt, uint64_t sum
     if (sum) atomicAdd(&t->sum, (unsigned long long)sum);
     if (xr) atomicXor(&t->xr, (unsigned long long)xr);
   }
+}
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is per function, shared by every
+// context and thread of the process: only ever RAISE it (a call setting a
+// smaller value would break a concurrent call -- ranks as threads -- that
+// launches with more).
+template <class F>
+inline cudaError_t raise_smem_attr(F* kfn, size_t bytes) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, size_t> cur;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& c = cur[reinterpret_cast<const void*>(kfn)];
+  if (bytes <= c) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) c = bytes;
+  return e;
 }
 
 inline unsigned grid_for(uint64_t n, unsigned block, unsigned cap = 148u * 16u) {

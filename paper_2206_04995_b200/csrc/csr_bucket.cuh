@@ -461,8 +461,10 @@ inline bool build_csr_bucketed(Ctx& ctx, const uint32_t* maj, const uint32_t* mn
     hist = ctx.zeros<unsigned int>(nb);
     const unsigned g = (unsigned)std::min<uint64_t>(ctx.sm_count * 2ull, (n + kCbThreads - 1) / kCbThreads);
     const size_t hsm = (size_t)nb * 4;
-    D3G_CUDA(cudaFuncSetAttribute(csr_bucket_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)hsm));
+    // (the attribute is per function, shared by every context of the process:
+    // set to the largest size any call uses, so concurrent calls -- ranks as
+    // threads -- never launch above another call's setting)
+    D3G_CUDA(raise_smem_attr(csr_bucket_hist_kernel, (int)((size_t)kCbMaxBuckets * 4)));
     D3G_LAUNCH(ctx, csr_bucket_hist_kernel, g, kCbThreads, hsm, maj, n, r, nb, hist.p);
     DBuf<unsigned long long> mxb = ctx.zeros<unsigned long long>(1);
     D3G_LAUNCH(ctx, max_u32_kernel, grid_for(nb, 256), 256, 0, hist.p, (uint64_t)nb, mxb.p);
@@ -518,8 +520,7 @@ inline bool build_csr_bucketed(Ctx& ctx, const uint32_t* maj, const uint32_t* mn
   DBuf<unsigned long long> ucount = ctx.alloc<unsigned long long>(nb);
   DBuf<unsigned long long> st = ctx.zeros<unsigned long long>(2);
   const size_t bsm = csr_bucket_smem(r);
-  D3G_CUDA(cudaFuncSetAttribute(csr_bucket_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)bsm));
+  D3G_CUDA(raise_smem_attr(csr_bucket_build_kernel, (int)csr_bucket_smem((int)kCbMaxRowsLog)));  // (see above)
   D3G_LAUNCH(ctx, csr_bucket_build_kernel, nb, kCbThreads, bsm, packed.p, bstart.p, n_rows, r, mb,
              uniq.p, deg.p, ucount.p, st.p);
   packed.reset();

@@ -498,7 +498,10 @@ constexpr int kCHWarps = 8;
 #define D3G_CH_BITS 10
 #endif
 constexpr uint32_t kCHSlots = 1u << D3G_CH_BITS;
-constexpr uint32_t kCHMax = kCHSlots * 3 / 4;  // load limit; < kCHSlots - 160 keeps probing finite
+#ifndef D3G_CH_LOAD
+#define D3G_CH_LOAD 84  // percent (double hashing: cfg5 60% 90.5, 75% 87.8, 84% 86.5 ms)
+#endif
+constexpr uint32_t kCHMax = kCHSlots * D3G_CH_LOAD / 100;  // load limit; < kCHSlots - 160 keeps probing finite
 constexpr uint32_t kCHEmpty = 0xffffffffu;
 #ifndef D3G_CH_CTAS
 #define D3G_CH_CTAS 4
@@ -692,7 +695,10 @@ __device__ __forceinline__ uint64_t cta_cold_x(const ColdX& s, uint64_t r0, uint
 #endif
 constexpr int kCCThreads = D3G_CC_THREADS;
 constexpr uint32_t kCCSlots = 1u << D3G_CC_BITS;  // 128 KB at 15 bits
-constexpr uint32_t kCCMax = kCCSlots * 3 / 4;      // load limit 0.75
+#ifndef D3G_CC_LOAD
+#define D3G_CC_LOAD 85  // percent
+#endif
+constexpr uint32_t kCCMax = kCCSlots * D3G_CC_LOAD / 100;  // load limit
 constexpr int kCCPerSm = (1024 / D3G_CC_THREADS) * (D3G_CC_BITS >= 15 ? 1 : 2) > 2
                              ? 2 : (1024 / D3G_CC_THREADS) * (D3G_CC_BITS >= 15 ? 1 : 2);
 constexpr size_t kCCSmem = (size_t)kCCSlots * 4 + (size_t)(kCCThreads / 32) * kDQ * 4;

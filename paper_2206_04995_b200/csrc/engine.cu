@@ -289,7 +289,7 @@ void run_sparse(Ctx& X, const SparseInputs& in, d3g::Decode dec, int mode, d3g::
       if (use_smem) {
         auto kfn = sparse_large_kernel<M(), false>;
         if (smem > 48 * 1024)
-          D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+          D3G_CUDA(raise_smem_attr(kfn, (int)smem));
         D3G_LAUNCH(X, kfn, g, 512, smem, lists[2].p, cnt[2], cx.p, in.x_lo, rp, in.r_col,
                    in.sp_ptr, in.sp_col, in.sparse_ids, n_words, gbm.p, dec, em, t.p, flt);
       } else {
@@ -381,7 +381,7 @@ void run_dense_streaming(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mod
   size_t sm = (size_t)std::max<uint64_t>(y_hot, 1) * 16;
   with_mode(mode, [&](auto M) {
     auto kfn = dense_ec_kernel<M()>;
-    D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    D3G_CUDA(raise_smem_attr(kfn, (int)sm));
     D3G_LAUNCH(X, kfn, g, kDenseThreads, sm, p, dec, em, t.p);
   });
   Tally h;
@@ -474,7 +474,7 @@ void run_dense_tiles(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d
   unsigned g = (unsigned)std::min<uint64_t>((uint64_t)n_tiles * x_splits, (uint64_t)X.sm_count);
   with_mode(mode, [&](auto M) {
     auto kfn = dense_ec_tile_kernel<M()>;
-    D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    D3G_CUDA(raise_smem_attr(kfn, (int)sm));
     D3G_LAUNCH(X, kfn, g, kD2Threads, sm, p, dec, em, t.p);
   });
   Tally h;
@@ -1123,7 +1123,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     DBuf<unsigned int> tw = X.zeros<unsigned int>(1);
     const size_t tsm = (size_t)(kTcN + 2 * kTcM) * K;
     auto kfn = dense_tc_kernel<kModeCount>;
-    D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
+    D3G_CUDA(raise_smem_attr(kfn, (int)tsm));
     D3G_LAUNCH(X, kfn, (unsigned)std::min<uint64_t>((uint64_t)n_zt * x_chunks, X.sm_count),
                kTcThreads, tsm, A.p, B.p, K, n_xt, n_zt, n_live, D, x_chunks, tw.p, t);
   } else if (K <= 256 && !(hot_impl && std::string(hot_impl) == "list")) {
@@ -1262,7 +1262,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
         // without the table: K listed rows plus one (zero) subset row
         const size_t jsm = tab ? tsm : (size_t)(K + 1) * 32 * 16;
         auto run = [&](auto kfn) {
-          D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jsm));
+          D3G_CUDA(raise_smem_attr(kfn, (int)jsm));
           D3G_LAUNCH(X, kfn, g, kHotThreads, jsm, hp, in.dl_ptr, in.dl_col, rec.p, rcnt.p, perm.p,
                      dec, em, t, cnt_sp);
           h0.tail_rows = hp.tail_rows;  // (set with the records, after h0 was made)
@@ -1289,17 +1289,17 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
       } else if (trie) {
         // the kernel counts its own slice reads (over every batch)
         auto kfn = dense_hot_trie_kernel<decltype(M)::value>;
-        D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
+        D3G_CUDA(raise_smem_attr(kfn, (int)tsm));
         D3G_LAUNCH(X, kfn, g, kTrieThreads, tsm, hp, in.dl_ptr, in.dl_col, rec.p, rcnt.p, perm.p,
                    dec, em, t, cnt_sp, lds_units);
       } else if (tab) {
         auto kfn = dense_hot_tab_kernel<decltype(M)::value>;
-        D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
+        D3G_CUDA(raise_smem_attr(kfn, (int)tsm));
         D3G_LAUNCH(X, kfn, g, kHotThreads, tsm, hp, in.dl_ptr, in.dl_col, rec.p, rcnt.p, dec, em,
                    t, cnt_sp);
       } else {
         auto kfn = dense_hot_rec_kernel<decltype(M)::value>;
-        D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        D3G_CUDA(raise_smem_attr(kfn, (int)sm));
         D3G_LAUNCH(X, kfn, g, kHotThreads, sm, hp, in.dl_ptr, in.dl_col, rec.p, rcnt.p, dec, em,
                    t, cnt_sp);
 #endif
@@ -1310,7 +1310,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     // K > 256 (no cold kernel: D3G_COLD=tiers) or D3G_HOT=list: the list kernel
     with_mode(mode, [&](auto M) {
       auto kfn = dense_hot_kernel<decltype(M)::value>;
-      D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      D3G_CUDA(raise_smem_attr(kfn, (int)sm));
       D3G_LAUNCH(X, kfn, g, kHotThreads, sm, hp, in.dl_ptr, in.dl_col, dec, em, t);
     });
   }
@@ -1354,7 +1354,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
         const size_t hsm = kCHSmem;
         with_mode(mode, [&](auto M) {
           auto kfn = dense_cold_hash_kernel<decltype(M)::value>;
-          D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
+          D3G_CUDA(raise_smem_attr(kfn, (int)hsm));
           D3G_LAUNCH(X, kfn, (unsigned)X.sm_count * (D3G_CH_BITS <= 10 ? D3G_CH_CTAS : 3), kCHWarps * 32, hsm,
                      xorder, n_live, in.r_ptr, in.r_col, cptr.p, crec.p, hz4,
                      reinterpret_cast<const uint4*>(hx.p), Y, var_bits, dlz, dec, em, next.p,
@@ -1377,7 +1377,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
           over2_n = X.zeros<unsigned int>(1);
           with_mode(mode, [&](auto M) {
             auto kfn = dense_cold_cta_kernel<decltype(M)::value>;
-            D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCCSmem));
+            D3G_CUDA(raise_smem_attr(kfn, (int)kCCSmem));
             D3G_LAUNCH(X, kfn, std::min<unsigned>(n_over, (unsigned)X.sm_count * kCCPerSm), kCCThreads,
                        kCCSmem, over_x.p, over_n.p, in.r_ptr, in.r_col, cptr.p, crec.p, hz4,
                        reinterpret_cast<const uint4*>(hx.p), Y, var_bits, dlz, dec, em,
@@ -1408,7 +1408,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
         with_mode(mode, [&](auto M) {
           auto kfn = dense_cold_kernel<decltype(M)::value>;
           if (csm > 48 * 1024)
-            D3G_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
+            D3G_CUDA(raise_smem_attr(kfn, (int)csm));
           D3G_LAUNCH(X, kfn, (unsigned)X.sm_count * cold_ctas, kColdWarps * 32, csm, xorder, n_live,
                      in.r_ptr, in.r_col, cptr.p, crec.p, hz4, reinterpret_cast<const uint4*>(hx.p), Y,
                      parts, part_rows, var_bits, dlz, dec, em, next.p, tc, cnt_sp, cand);
@@ -2483,8 +2483,7 @@ void dense_counters_device(Ctx& X, const d3g::DeviceCsr& r, uint64_t x_lo, uint6
   X.to_device(dthr.p, thr.data(), thr.size());
   DBuf<DenseCounters> dc = X.zeros<DenseCounters>(1);
   DBuf<unsigned int> next = X.zeros<unsigned int>(1);
-  D3G_CUDA(cudaFuncSetAttribute(dense_counters_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem));
+  D3G_CUDA(raise_smem_attr(dense_counters_kernel, (int)smem));
   const uint64_t n_blocks = (y_card + w - 1) / w;
   const int per_sm = smem <= 48 * 1024 ? 4 : smem <= 100 * 1024 ? 2 : 1;
   const unsigned grid = (unsigned)std::min<uint64_t>(x_hi - x_lo, (uint64_t)X.sm_count * per_sm);
@@ -4005,8 +4004,7 @@ extern "C" int d3g_smem_peak(d3g_ctx* ctx, double* bytes_per_sec) {
     X.begin_call();
     DBuf<uint32_t> out = X.zeros<uint32_t>(1);
     const size_t sm = 256 * 32 * 16;  // 128 KB: one CTA of 1024 threads per SM
-    D3G_CUDA(cudaFuncSetAttribute(smem_peak_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)sm));
+    D3G_CUDA(raise_smem_attr(smem_peak_kernel, (int)sm));
     const unsigned grid = (unsigned)X.sm_count;
     const int iters = 8192;
     smem_peak_kernel<<<grid, 1024, sm, X.stream>>>(64, out.p);  // warm-up
