@@ -327,8 +327,8 @@ def test_rank0_split_count_only_cfg2(monkeypatch):
     assert a.hot_direct_pairs > 0
     assert a.out_p == g["set"]["count"]
     assert (a.pairs_sparse, a.pairs_dense) == (ref["pairs_sparse"], ref["pairs_dense"])
-    # one, two (contiguous row ranges) and three pivots (row segments)
-    for piv in ("1", "2", "3", "4"):
+    # one to six pivots (2 to 64 classes; class-aligned batches)
+    for piv in ("1", "2", "3", "4", "5", "6"):
         monkeypatch.setenv("D3G_PIVOTS", piv)
         p = d3.join_project(d3.RawTable(rl, rr), d3.RawTable(sl, sr), e, C).report
         assert p.hot_direct_pairs > 0, piv
@@ -426,7 +426,8 @@ def test_pivot_plan_mid_size_instances(seed, monkeypatch):
     """Mid-size skewed instances (x over 20-40k, Zipf y over a few hundred
     values) where the pivot plan engages with mixed and pure batches: the
     count-only count and pairs split equal the checksum-mode run (every pair
-    tested) for one, two and three pivots, in both orientations."""
+    tested) for one to six pivots, in both orientations; and with the
+    class-aligned batches switched off (D3G_NO_PAD: mixed batches)."""
     rng = np.random.default_rng(seed)
     nx, ny, n = int(rng.integers(20000, 40000)), int(rng.integers(200, 600)), 150000
     w = 1.0 / np.arange(1, ny + 1) ** float(rng.uniform(0.9, 1.3))
@@ -437,12 +438,17 @@ def test_pivot_plan_mid_size_instances(seed, monkeypatch):
     direct = 0
     for a, b in ((r, s), (s, r)):
         base = _run(a, b, d3.Strategy.auto_select, count_only=True, checksum=True).report
-        for piv in ("1", "2", "3", "4"):
+        for piv in ("1", "2", "3", "4", "5", "6"):
             monkeypatch.setenv("D3G_PIVOTS", piv)
             got = _run(a, b, d3.Strategy.auto_select, count_only=True).report
             assert (got.out_p, got.pairs_sparse, got.pairs_dense) == \
                 (base.out_p, base.pairs_sparse, base.pairs_dense), (seed, piv)
             direct += got.hot_direct_pairs
+        monkeypatch.setenv("D3G_NO_PAD", "1")
+        got = _run(a, b, d3.Strategy.auto_select, count_only=True).report
+        assert (got.out_p, got.pairs_sparse, got.pairs_dense) == \
+            (base.out_p, base.pairs_sparse, base.pairs_dense), (seed, "mixed")
+        monkeypatch.delenv("D3G_NO_PAD")
         monkeypatch.delenv("D3G_PIVOTS")
     assert direct > 0  # the plan engaged
 

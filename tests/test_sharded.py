@@ -179,3 +179,22 @@ def test_zsplit_cfg2_folded_layout():
         for k in ("out_p", "checksum_sum", "checksum_xor", "pairs_sparse", "pairs_dense",
                   "dense_z", "sparse_z", "out_j", "s_nnz", "r_nnz"):
             assert getattr(o.report, k) == getattr(full, k), k
+
+
+@pytest.mark.parametrize("nranks", [3, 8])
+def test_zsplit_count_only_plan_and_pooled_class0(nranks):
+    """Count-only sharded cfg2: the pivot plan runs on every rank (class-
+    aligned batches) and the ranks' class-0 x (no pivot) are pooled into
+    shared batches tested against row slices; the job's count equals the
+    reference's."""
+    import json
+    import os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "golden.json")))
+    r, s = O.gen(2, 0), O.gen(2, 1)
+    e = d3.EngineConfig(count_only=True, memory_budget_bytes=32 << 30)
+    outs = run_sharded((r.left, r.right), (s.left, s.right), nranks, e, x_card=200_000)
+    for o in outs:
+        assert o.report.zsplit
+        assert o.report.out_p == g["cfg2"]["set"]["count"]
+        assert o.report.hot_direct_pairs > 0  # the plan counted pairs without a test
+    assert sum(o.report.rank_out_p for o in outs) == g["cfg2"]["set"]["count"]
