@@ -582,9 +582,15 @@ def main():
     if cold_roof and roof.get("kernel", "").startswith("DenseEC P1"):
         roof["cold_pass"] = cold_roof
     phases_roof = {
-        "map+csr+partition": {"ms": prep_ms, "GB/s": b_map / (prep_ms * 1e-3) / 1e9 if prep_ms else None},
+        "map+csr+partition": {"ms": prep_ms, "GB/s": b_map / (prep_ms * 1e-3) / 1e9 if prep_ms else None,
+                              "frac_of_hbm": b_map / (prep_ms * 1e-3) / 1e9 / hbm if prep_ms else None,
+                              "B_M": b_map,
+                              "by_phase_ms": {k: phase[k] for k in ("ms_map", "ms_csr", "ms_stats",
+                                                                    "ms_partition")}},
         "sparse_bmm": {"ms": phase["ms_sparse"],
-                       "GB/s": b_sparse / (phase["ms_sparse"] * 1e-3) / 1e9 if phase["ms_sparse"] else None},
+                       "GB/s": b_sparse / (phase["ms_sparse"] * 1e-3) / 1e9 if phase["ms_sparse"] else None,
+                       "frac_of_hbm": b_sparse / (phase["ms_sparse"] * 1e-3) / 1e9 / hbm
+                       if phase["ms_sparse"] else None},
         "dense_ec": {"ms": phase["ms_dense"],
                      "pair_tests_per_s": (p_dense / (phase["ms_dense"] * 1e-3))
                      if phase["ms_dense"] else None},
