@@ -16,11 +16,12 @@ GPU figure is quoted on; it fits one B200 (peak working set ~7 GB).
            x-slice sample extrapolated to the full job.
 
 Multi-GPU: `--gpus N` without torchrun re-launches itself under
-torch.distributed.run with N ranks (127.0.0.1); under torchrun rank 0
-generates the tables and broadcasts them over NVLink with NCCL; every rank
-builds the (replicated) mapping/CSR/partition and runs SparseBMM/DenseEC on
-its own x shard (intersection-free, no dedup across GPUs); counts are
-all-reduced.
+torch.distributed.run with N ranks (127.0.0.1). Each rank generates the
+tables on its GPU (deterministic: the same S everywhere) and keeps its x
+shard of R; the library runs the sharded join over an NCCL communicator
+(csrc/exchange.cuh, csrc/zsplit.cuh): statistics all-reduced, the S side
+built per z range and all-gathered over NVLink, SparseBMM/DenseEC on the
+rank's own x (intersection-free, no dedup across GPUs), counts reduced.
 """
 from __future__ import annotations
 
