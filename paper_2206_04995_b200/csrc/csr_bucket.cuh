@@ -304,6 +304,11 @@ csr_bucket_build_kernel(const uint32_t* __restrict__ packed,
   const uint32_t cnt = (uint32_t)(bstart[b + 1] - s0);
   const uint64_t row0 = (uint64_t)b << r;
   const uint32_t rows = (uint32_t)((n_rows - row0) < (1ull << r) ? (n_rows - row0) : (1ull << r));
+  if (cnt == 0) {  // an empty bucket (an x shard's rows sit in one code range)
+    for (uint32_t i = threadIdx.x; i < rows; i += kCbThreads) deg[row0 + i] = 0;
+    if (threadIdx.x == 0) ustart[b] = 0;
+    return;
+  }
   const uint32_t mmask = mb >= 32 ? 0xffffffffu : ((1u << mb) - 1);
   for (uint32_t i = threadIdx.x; i <= rows; i += kCbThreads) roff[i] = 0;
   // the bucket's keys into shared memory: 16-byte loads from the first

@@ -1392,7 +1392,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
           const uint64_t words = (D + 31) / 32;
           const unsigned og = (unsigned)std::min<uint64_t>(
               (uint64_t)n_over2,
-              (uint64_t)X.sm_count * env_u32("D3G_OVERFLOW_CTAS_PER_SM", 3, 1, 16));
+              (uint64_t)env_u32("D3G_OVERFLOW_CTAS", X.sm_count * 3, 1, X.sm_count * 16));
           DBuf<uint32_t> gbm = X.zeros<uint32_t>((uint64_t)og * words);
           DBuf<uint32_t> touched = X.alloc<uint32_t>((uint64_t)og * kOvTouched);
           with_mode(mode, [&](auto M) {
