@@ -957,8 +957,9 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     if (cold_kernel_ok)
       while (var_bits < 3 && var_bits < Y && 2ull * top_rank_dr[var_bits] >= xc_job)
         ++var_bits;
-    if (cold_kernel_ok && std::getenv("D3G_VAR_BITS"))  // experiments: 0..4
-      var_bits = (uint32_t)std::min<uint64_t>(env_u32("D3G_VAR_BITS", var_bits, 0, 4), Y);
+    // experiments: 0..3 (the build's (part, y, top-mask) histogram has 8 slots)
+    if (cold_kernel_ok && std::getenv("D3G_VAR_BITS"))
+      var_bits = (uint32_t)std::min<uint64_t>(env_u32("D3G_VAR_BITS", var_bits, 0, 3), Y);
     rows_key = ((uint64_t)1 << var_bits) * parts * Y;
     // per (part, y, top-mask) histogram, then the (variant, part, y) counts
     const uint64_t n_py = (uint64_t)parts * Y;
