@@ -43,6 +43,26 @@ namespace d3g {
 // array and places it in every compatible variant at
 //   cptr[v, part, y] + (H of the compatible masks below zm) + rank.
 // Four list entries are in flight per lane (the passes are latency-bound).
+// Mask slots per (part, y): variant bits up to 4. With 4 bits the variant
+// with only the 4th top rank set is skipped (its x use variant 0, a
+// superset): the cheapest split for the few x without the top rank.
+constexpr uint32_t kHistSlots = 16;
+#ifndef D3G_MAX_VAR_BITS
+#define D3G_MAX_VAR_BITS 4
+#endif
+constexpr uint32_t kMaxVarBits = D3G_MAX_VAR_BITS;  // the top ranks that split the cold CSR
+__device__ __forceinline__ void load_hist(const uint32_t* __restrict__ H, uint64_t t,
+                                          uint32_t (&h)[kHistSlots]) {
+  const uint4* p = reinterpret_cast<const uint4*>(H) + 4 * t;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint4 a = p[q];
+    h[4 * q] = a.x;
+    h[4 * q + 1] = a.y;
+    h[4 * q + 2] = a.z;
+    h[4 * q + 3] = a.w;
+  }
+}
 __global__ void cold_hist_kernel(const uint64_t* __restrict__ dl_ptr,
                                  const uint32_t* __restrict__ dl_col, uint64_t n_dense, uint32_t K,
                                  const uint32_t* __restrict__ y_of_rank, uint32_t* __restrict__ H,
@@ -62,24 +82,25 @@ __global__ void cold_hist_kernel(const uint64_t* __restrict__ dl_ptr,
       for (int u = 0; u < 4; ++u) r[u] = k0 + 8 * u < e ? dl_col[k0 + 8 * u] : 0u;
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        if (r[u] >= K) atomicAdd(&H[((part * y_card) + y_of_rank[r[u]]) * 8 + zm], 1u);
+        if (r[u] >= K) atomicAdd(&H[((part * y_card) + y_of_rank[r[u]]) * kHistSlots + zm], 1u);
     }
   }
 }
 // (variant, part, y) counts from H: thread per (part, y)
 __global__ void cold_cnt_from_hist_kernel(const uint32_t* __restrict__ H, uint64_t n_py,
                                           uint64_t y_card, uint32_t parts, uint32_t var_bits,
-                                          uint32_t* __restrict__ cnt) {
+                                          uint32_t vskip, uint32_t* __restrict__ cnt) {
   const uint32_t nvar = 1u << var_bits;
   for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n_py;
        t += (uint64_t)gridDim.x * blockDim.x) {
-    const uint4 a = reinterpret_cast<const uint4*>(H)[2 * t], b = reinterpret_cast<const uint4*>(H)[2 * t + 1];
-    const uint32_t h[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    uint32_t h[kHistSlots];
+    load_hist(H, t, h);
     const uint64_t part = t / y_card, y = t % y_card;
     for (uint32_t v = 0; v < nvar; ++v) {
       uint32_t c = 0;
-      for (uint32_t zm = 0; zm < nvar; ++zm)
-        if ((zm & v) == 0) c += h[zm];
+      if (v != vskip)
+        for (uint32_t zm = 0; zm < nvar; ++zm)
+          if ((zm & v) == 0) c += h[zm];
       cnt[((uint64_t)v * parts + part) * y_card + y] = c;
     }
   }
@@ -92,7 +113,7 @@ __global__ void cold_scatter_hist_kernel(const uint64_t* __restrict__ dl_ptr,
                                          uint32_t* __restrict__ Rk /* zeroed, like H */,
                                          uint64_t y_card, uint32_t part_rows, uint32_t parts,
                                          const uint64_t* __restrict__ hz, uint32_t kw,
-                                         uint32_t var_bits, uint64_t row_base,
+                                         uint32_t var_bits, uint32_t vskip, uint64_t row_base,
                                          uint4* __restrict__ rec, uint32_t* __restrict__ col,
                                          const uint8_t* __restrict__ row_sp) {
   const uint32_t nvar = 1u << var_bits, vmask = nvar - 1;
@@ -122,17 +143,16 @@ __global__ void cold_scatter_hist_kernel(const uint64_t* __restrict__ dl_ptr,
       for (int u = 0; u < 4; ++u)
         if (r[u] >= K) {
           g[u] = (part * y_card) + y_of_rank[r[u]];
-          rk[u] = atomicAdd(&Rk[g[u] * 8 + zm], 1u);
+          rk[u] = atomicAdd(&Rk[g[u] * kHistSlots + zm], 1u);
         }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         if (r[u] < K) continue;
-        const uint4 a = reinterpret_cast<const uint4*>(H)[2 * g[u]],
-                    b = reinterpret_cast<const uint4*>(H)[2 * g[u] + 1];
-        const uint32_t h[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+        uint32_t h[kHistSlots];
+        load_hist(H, g[u], h);
         const uint64_t y = g[u] - part * y_card;
         for (uint32_t v = 0; v < nvar; ++v) {
-          if (zm & v) continue;
+          if ((zm & v) || v == vskip) continue;
           uint32_t pre = 0;
           for (uint32_t z2 = 0; z2 < zm; ++z2)
             if ((z2 & v) == 0) pre += h[z2];
@@ -166,6 +186,12 @@ __device__ __forceinline__ ColdX cold_x(const uint4* __restrict__ hx4, uint32_t 
   ld256(hx4 + 2 * (uint64_t)x, s.a0, s.a1);
   s.fold = fold_tail(s.a0, s.a1);
   return s;
+}
+// x's cold-CSR variant: its top-var_bits hot mask (the skipped variant's x
+// stream variant 0, which holds every row)
+__device__ __forceinline__ uint32_t x_variant(uint32_t w0, uint32_t var_bits, uint32_t vskip) {
+  const uint32_t v = w0 & ((1u << var_bits) - 1);
+  return v == vskip ? 0u : v;
 }
 enum : uint32_t { kColdHot = 0, kColdSurvivor = 1, kColdMaybe = 2 };
 __device__ __forceinline__ uint32_t cold_test(const uint4& c, const ColdX& s) {
@@ -406,7 +432,8 @@ dense_cold_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
                   const uint64_t* __restrict__ cptr /* [var][parts][y_card] + 1 */,
                   const uint4* __restrict__ crec, const uint4* __restrict__ hz4,
                   const uint4* __restrict__ hx4, uint64_t y_card, uint32_t parts,
-                  uint32_t part_rows, uint32_t var_bits, const uint32_t* __restrict__ dl_z,
+                  uint32_t part_rows, uint32_t var_bits, uint32_t vskip,
+                  const uint32_t* __restrict__ dl_z,
                   Decode dec, Emit em, unsigned int* __restrict__ next, Tally* tally,
                   unsigned long long* __restrict__ cnt_sp,
                   unsigned long long* __restrict__ cand = nullptr) {
@@ -433,7 +460,7 @@ dense_cold_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
     const uint32_t x = xs[item % n_x];
     const uint32_t zbase = part * part_rows;
     const ColdX s = cold_x(hx4, x);
-    const uint32_t v = s.a0.x & ((1u << var_bits) - 1);
+    const uint32_t v = x_variant(s.a0.x, var_bits, vskip);
     const uint64_t* cp = cptr + ((uint64_t)v * parts + part) * y_card;
     bool touched = false;
     uint32_t qn = 0;
@@ -521,7 +548,8 @@ dense_cold_hash_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
                        const uint64_t* __restrict__ r_ptr, const uint32_t* __restrict__ r_col,
                        const uint64_t* __restrict__ cptr, const uint4* __restrict__ crec,
                        const uint4* __restrict__ hz4, const uint4* __restrict__ hx4,
-                       uint64_t y_card, uint32_t var_bits, const uint32_t* __restrict__ dl_z,
+                       uint64_t y_card, uint32_t var_bits, uint32_t vskip,
+                       const uint32_t* __restrict__ dl_z,
                        Decode dec, Emit em, unsigned int* __restrict__ next,
                        uint32_t* __restrict__ over_x, unsigned int* __restrict__ over_n,
                        Tally* tally, unsigned long long* __restrict__ cnt_sp, uint32_t ch_max,
@@ -545,7 +573,7 @@ dense_cold_hash_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
     if (lane == 0) item_next = atomicAdd(next, 1u);  // consumed next iteration
     const uint32_t x = xs[item];
     const ColdX s = cold_x(hx4, x);
-    const uint32_t v = s.a0.x & ((1u << var_bits) - 1);
+    const uint32_t v = x_variant(s.a0.x, var_bits, vskip);
     const uint64_t* cp = cptr + (uint64_t)v * y_card;
     uint32_t inserted = 0;  // warp-uniform
     uint32_t qn = 0;
@@ -711,7 +739,8 @@ dense_cold_cta_kernel(const uint32_t* __restrict__ over_x, const unsigned int* _
                       const uint64_t* __restrict__ r_ptr, const uint32_t* __restrict__ r_col,
                       const uint64_t* __restrict__ cptr, const uint4* __restrict__ crec,
                       const uint4* __restrict__ hz4, const uint4* __restrict__ hx4,
-                      uint64_t y_card, uint32_t var_bits, const uint32_t* __restrict__ dl_z,
+                      uint64_t y_card, uint32_t var_bits, uint32_t vskip,
+                      const uint32_t* __restrict__ dl_z,
                       Decode dec, Emit em, uint32_t* __restrict__ over2_x,
                       unsigned int* __restrict__ over2_n, uint32_t cc_max, Tally* tally,
                       unsigned long long* __restrict__ cnt_sp,
@@ -730,7 +759,7 @@ dense_cold_cta_kernel(const uint32_t* __restrict__ over_x, const unsigned int* _
   for (uint32_t it = blockIdx.x; it < n; it += gridDim.x) {
     const uint32_t x = over_x[it];
     const ColdX s = cold_x(hx4, x);
-    const uint32_t v = s.a0.x & ((1u << var_bits) - 1);
+    const uint32_t v = x_variant(s.a0.x, var_bits, vskip);
     const uint64_t* cp = cptr + (uint64_t)v * y_card;
     const uint64_t r0 = r_ptr[x], r1 = r_ptr[x + 1];
     if (threadIdx.x == 0) {
@@ -827,7 +856,8 @@ dense_cold_overflow_kernel(const uint32_t* __restrict__ over_x, const unsigned i
                            const uint64_t* __restrict__ r_ptr, const uint32_t* __restrict__ r_col,
                            const uint64_t* __restrict__ cptr, const uint4* __restrict__ crec,
                            const uint4* __restrict__ hz4, const uint4* __restrict__ hx4,
-                           uint64_t y_card, uint32_t var_bits, const uint32_t* __restrict__ dl_z,
+                           uint64_t y_card, uint32_t var_bits, uint32_t vskip,
+                           const uint32_t* __restrict__ dl_z,
                            uint32_t* __restrict__ gbm, uint64_t words, Decode dec, Emit em,
                            Tally* tally, unsigned long long* __restrict__ cnt_sp,
                            uint32_t* __restrict__ touched /* [gridDim.x][kOvTouched] */,
@@ -849,7 +879,7 @@ dense_cold_overflow_kernel(const uint32_t* __restrict__ over_x, const unsigned i
   for (uint32_t it = blockIdx.x; it < n; it += gridDim.x) {
     const uint32_t x = over_x[it];
     const ColdX s = cold_x(hx4, x);
-    const uint32_t v = s.a0.x & ((1u << var_bits) - 1);
+    const uint32_t v = x_variant(s.a0.x, var_bits, vskip);
     const uint64_t* cp = cptr + (uint64_t)v * y_card;
     const uint64_t r0 = r_ptr[x], r1 = r_ptr[x + 1];
     if (threadIdx.x == 0) s_nt = 0;

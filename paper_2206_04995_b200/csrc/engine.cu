@@ -938,7 +938,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     if (kv[j] == K) kidx = j;
   const bool run_cold = e[kidx] > 0;
   uint32_t parts = 1, part_rows = (uint32_t)(((D + 31) / 32) * 32);
-  uint32_t var_bits = 0;
+  uint32_t var_bits = 0, vskip = ~0u;
   uint64_t rows_key = 0, cnnz = 0;
   DBuf<uint32_t> cc, ch;  // (variant, part, y) counts; (part, y, mask) histogram
   DBuf<uint64_t> cptr;
@@ -955,15 +955,20 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     // 0-2; cfg4's flatter Zipf(0.8): none)
     const uint64_t xc_job = zs ? in.x_card_job : in.x_card;  // the same bits on every rank
     if (cold_kernel_ok)
-      while (var_bits < 3 && var_bits < Y && 2ull * top_rank_dr[var_bits] >= xc_job)
+      // (a 4th bit pays on large dense blocks: cfg5 87.3 -> 85.6 ms; cfg2 2.28 -> 2.37)
+      while (var_bits < (D > (4ull << 20) ? kMaxVarBits : 3u) && var_bits < Y &&
+             2ull * top_rank_dr[var_bits] >= xc_job)
         ++var_bits;
-    // experiments: 0..3 (the build's (part, y, top-mask) histogram has 8 slots)
-    if (cold_kernel_ok && std::getenv("D3G_VAR_BITS"))
-      var_bits = (uint32_t)std::min<uint64_t>(env_u32("D3G_VAR_BITS", var_bits, 0, 3), Y);
+    if (cold_kernel_ok && std::getenv("D3G_VAR_BITS"))  // experiments: 0..4
+      var_bits = (uint32_t)std::min<uint64_t>(env_u32("D3G_VAR_BITS", var_bits, 0, 4), Y);
+    // with 4 bits the variant of x holding only the 4th top rank is not built
+    // (it would copy half of all cold entries for the few x without the top
+    // three); those x stream variant 0
+    vskip = var_bits == 4 ? 8u : ~0u;
     rows_key = ((uint64_t)1 << var_bits) * parts * Y;
     // per (part, y, top-mask) histogram, then the (variant, part, y) counts
     const uint64_t n_py = (uint64_t)parts * Y;
-    ch = X.zeros<uint32_t>(n_py * 8);
+    ch = X.zeros<uint32_t>(n_py * kHistSlots);
     if (DL)
       D3G_LAUNCH(X, cold_hist_kernel, grid_for(DL * 8, 256), 256, 0, in.dl_ptr, in.dl_col, DL, K,
                  in.y_of_rank, ch.p, Y, part_rows, reinterpret_cast<const uint64_t*>(hzl), kw,
@@ -971,7 +976,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     cc = X.alloc<uint32_t>(rows_key);
     if (n_py)
       D3G_LAUNCH(X, cold_cnt_from_hist_kernel, grid_for(n_py, 256), 256, 0, ch.p, n_py, Y, parts,
-                 var_bits, cc.p);
+                 var_bits, vskip, cc.p);
     cptr = X.alloc<uint64_t>(rows_key + 1);
     exclusive_scan<uint32_t>(X, cc.p, rows_key, cptr.p);
     X.defer(&cnnz, cptr.p + rows_key, 8);
@@ -989,10 +994,10 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     ex_allgatherv_dev(X, *in.zx, cptr.p, std::vector<uint64_t>(N, rows_key + 1), 8, cp_all.p);
     DBuf<uint4> crec_l = X.alloc<uint4>(cnnz);
     if (DL) {
-      DBuf<uint32_t> rk = X.zeros<uint32_t>((uint64_t)parts * Y * 8);
+      DBuf<uint32_t> rk = X.zeros<uint32_t>((uint64_t)parts * Y * kHistSlots);
       D3G_LAUNCH(X, cold_scatter_hist_kernel, grid_for(DL * 8, 256), 256, 0, in.dl_ptr, in.dl_col,
                  DL, K, in.y_of_rank, cptr.p, ch.p, rk.p, Y, part_rows, parts,
-                 reinterpret_cast<const uint64_t*>(hzl), kw, var_bits, row_lo, crec_l.p,
+                 reinterpret_cast<const uint64_t*>(hzl), kw, var_bits, vskip, row_lo, crec_l.p,
                  (uint32_t*)nullptr, in.row_sp);
     }
     cc.reset();
@@ -1333,10 +1338,10 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     } else {
       if (cold_kernel_ok) crec = X.alloc<uint4>(cnnz);
       else ccol = X.alloc<uint32_t>(cnnz);
-      DBuf<uint32_t> rk = X.zeros<uint32_t>((uint64_t)parts * Y * 8);
+      DBuf<uint32_t> rk = X.zeros<uint32_t>((uint64_t)parts * Y * kHistSlots);
       D3G_LAUNCH(X, cold_scatter_hist_kernel, grid_for(D * 8, 256), 256, 0, in.dl_ptr, in.dl_col,
                  D, K, in.y_of_rank, cptr.p, ch.p, rk.p, Y, part_rows, parts,
-                 reinterpret_cast<const uint64_t*>(hz.p), kw, var_bits, 0ull,
+                 reinterpret_cast<const uint64_t*>(hz.p), kw, var_bits, vskip, 0ull,
                  cold_kernel_ok ? crec.p : nullptr, ccol.p, rsp);
       cc.reset();
       ch.reset();
@@ -1358,7 +1363,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
           D3G_CUDA(raise_smem_attr(kfn, (int)hsm));
           D3G_LAUNCH(X, kfn, (unsigned)X.sm_count * (D3G_CH_BITS <= 10 ? D3G_CH_CTAS : 3), kCHWarps * 32, hsm,
                      xorder, n_live, in.r_ptr, in.r_col, cptr.p, crec.p, hz4,
-                     reinterpret_cast<const uint4*>(hx.p), Y, var_bits, dlz, dec, em, next.p,
+                     reinterpret_cast<const uint4*>(hx.p), Y, var_bits, vskip, dlz, dec, em, next.p,
                      over_x.p, over_n.p, tc, cnt_sp,
                      env_u32("D3G_COLD_HASH_MAX", kCHMax, 1, kCHMax),
                      env_u32("D3G_COLD_ROUTE", D3G_COLD_ROUTE, 1, 0xffffffffu), cand);
@@ -1381,7 +1386,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
             D3G_CUDA(raise_smem_attr(kfn, (int)kCCSmem));
             D3G_LAUNCH(X, kfn, std::min<unsigned>(n_over, (unsigned)X.sm_count * kCCPerSm), kCCThreads,
                        kCCSmem, over_x.p, over_n.p, in.r_ptr, in.r_col, cptr.p, crec.p, hz4,
-                       reinterpret_cast<const uint4*>(hx.p), Y, var_bits, dlz, dec, em,
+                       reinterpret_cast<const uint4*>(hx.p), Y, var_bits, vskip, dlz, dec, em,
                        over2_x.p, over2_n.p, env_u32("D3G_COLD_CTA_MAX", kCCMax, 1, kCCMax), tc,
                        cnt_sp, cand);
           });
@@ -1399,7 +1404,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
           with_mode(mode, [&](auto M) {
             D3G_LAUNCH(X, dense_cold_overflow_kernel<decltype(M)::value>, og, kOvThreads, kOvSmem, ox,
                        on, in.r_ptr, in.r_col, cptr.p, crec.p, hz4,
-                       reinterpret_cast<const uint4*>(hx.p), Y, var_bits, dlz, gbm.p, words,
+                       reinterpret_cast<const uint4*>(hx.p), Y, var_bits, vskip, dlz, gbm.p, words,
                        dec, em, tc, cnt_sp, touched.p, cand);
           });
         }
@@ -1412,7 +1417,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
             D3G_CUDA(raise_smem_attr(kfn, (int)csm));
           D3G_LAUNCH(X, kfn, (unsigned)X.sm_count * cold_ctas, kColdWarps * 32, csm, xorder, n_live,
                      in.r_ptr, in.r_col, cptr.p, crec.p, hz4, reinterpret_cast<const uint4*>(hx.p), Y,
-                     parts, part_rows, var_bits, dlz, dec, em, next.p, tc, cnt_sp, cand);
+                     parts, part_rows, var_bits, vskip, dlz, dec, em, next.p, tc, cnt_sp, cand);
         });
       }
       D3G_CUDA(cudaEventRecord(ev3, X.stream));
