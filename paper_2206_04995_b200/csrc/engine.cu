@@ -681,9 +681,8 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   // SM's shared memory): more, smaller partitions raise occupancy for the
   // latency-bound candidate stream
   const char* cc_env = std::getenv("D3G_COLD_CTAS");
-  uint32_t cold_ctas = 4;  // measured best on cfg2 (4 > 3 > 6 > 8)
-  if ((D + (budget / 4 / kColdWarps) * 8 - 1) / ((budget / 4 / kColdWarps) * 8) > 16)
-    cold_ctas = 3;  // keep the dense rows within 16 bitmap partitions (cfg4)
+  // (16-byte records, window mapping: cfg2 3 CTAs 2.12 ms, 4: 2.27, 2: 2.20)
+  uint32_t cold_ctas = 3;
   if (cc_env) cold_ctas = std::max(1, std::atoi(cc_env));
   const uint64_t cold_rows_cap =
       std::max<uint64_t>(32, (budget / cold_ctas / kColdWarps - (kDQ + kSegWords) * 4) * 8 / 32 * 32);
