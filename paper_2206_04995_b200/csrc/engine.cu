@@ -955,7 +955,9 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     const uint64_t xc_job = zs ? in.x_card_job : in.x_card;  // the same bits on every rank
     if (cold_kernel_ok)
       // (a 4th bit pays on large dense blocks: cfg5 87.3 -> 85.6 ms; cfg2 2.28 -> 2.37)
-      while (var_bits < (D > (4ull << 20) ? kMaxVarBits : 3u) && var_bits < Y &&
+      // (a sharded job gathers the cold CSR: the 4th bit's extra records cost
+      // more NVLink time than they save a rank)
+      while (var_bits < (D > (4ull << 20) && !zs ? kMaxVarBits : 3u) && var_bits < Y &&
              2ull * top_rank_dr[var_bits] >= xc_job)
         ++var_bits;
     if (cold_kernel_ok && std::getenv("D3G_VAR_BITS"))  // experiments: 0..4
