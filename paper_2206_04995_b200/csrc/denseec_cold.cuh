@@ -35,13 +35,14 @@ namespace d3g {
 
 // ---- cold CSR build --------------------------------------------------------
 
-// Cold CSR build in two passes with ONE atomic per cold entry (the variant
-// expansion multiplies entries by ~1.7 on cfg5): per (part, y, zm) -- zm the
-// row's top-var_bits hot mask -- a histogram H; the (variant, part, y) counts
-// follow as sums of H over the masks compatible with the variant; the scatter
-// takes each entry's rank within its (part, y, zm) group from a second counter
-// array and places it in every compatible variant at
-//   cptr[v, part, y] + (H of the compatible masks below zm) + rank.
+// Cold CSR build in two passes: per (part, y, zm) -- zm the row's
+// top-var_bits hot mask -- a histogram H (one atomic per cold entry); the
+// (variant, part, y) counts follow as sums of H over the masks compatible with
+// the variant, and their exclusive scan is the segment starts. The scatter
+// then takes each record's slot from a per-(variant, part, y) cursor (the
+// scan itself, advanced in place by 64-bit atomics), for every variant
+// compatible with the row. Slot order inside a segment is arbitrary: every
+// consumer (the cold kernels, the z-split merge) treats a segment as a set.
 // Four list entries are in flight per lane (the passes are latency-bound).
 // Mask slots per (part, y): variant bits up to 4. With 4 bits the variant
 // with only the 4th top rank set is skipped (its x use variant 0, a
@@ -105,23 +106,26 @@ __global__ void cold_cnt_from_hist_kernel(const uint32_t* __restrict__ H, uint64
     }
   }
 }
-__global__ void cold_scatter_hist_kernel(const uint64_t* __restrict__ dl_ptr,
-                                         const uint32_t* __restrict__ dl_col, uint64_t n_dense,
-                                         uint32_t K, const uint32_t* __restrict__ y_of_rank,
-                                         const uint64_t* __restrict__ cptr,
-                                         const uint32_t* __restrict__ H,
-                                         uint32_t* __restrict__ Rk /* zeroed, like H */,
-                                         uint64_t y_card, uint32_t part_rows, uint32_t parts,
-                                         const uint64_t* __restrict__ hz, uint32_t kw,
-                                         uint32_t var_bits, uint32_t vskip, uint64_t row_base,
-                                         uint4* __restrict__ rec, uint32_t* __restrict__ col,
-                                         const uint8_t* __restrict__ row_sp) {
-  const uint32_t nvar = 1u << var_bits, vmask = nvar - 1;
+// cur: the exclusive scan of the (variant, part, y) counts; on return
+// cur[i] is the END of segment i (= the start of segment i + 1), so the
+// buffer one slot before cur, with a leading 0, is the finished cptr.
+__global__ void cold_scatter_cur_kernel(const uint64_t* __restrict__ dl_ptr,
+                                        const uint32_t* __restrict__ dl_col, uint64_t n_dense,
+                                        uint32_t K, const uint32_t* __restrict__ y_of_rank,
+                                        unsigned long long* __restrict__ cur, uint64_t y_card,
+                                        uint32_t part_rows, uint32_t parts,
+                                        const uint64_t* __restrict__ hz, uint32_t kw,
+                                        uint32_t var_bits, uint32_t vskip, uint64_t row_base,
+                                        uint4* __restrict__ rec, uint32_t* __restrict__ col,
+                                        const uint8_t* __restrict__ row_sp) {
+  const uint32_t vmask = (1u << var_bits) - 1;
+  const uint64_t n_py = (uint64_t)parts * y_card;  // one variant's keys
   const uint32_t sl = threadIdx.x & 7;  // 8 lanes per row
   for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 8) + (threadIdx.x >> 3); i < n_dense;
        i += (uint64_t)gridDim.x * (blockDim.x / 8)) {
     const uint64_t part = (row_base + i) / part_rows;
     const uint32_t zm = var_bits ? (uint32_t)(hz[i * kw] & vmask) : 0;
+    const uint32_t comp = vmask & ~zm;  // the variants that hold this row: v subset of comp
     uint4 rv = make_uint4(0, 0, 0, 0);
     // rec: the whole 16-byte record is written here (its hot word, folded tail
     // and flags are the row's); a scattered 16-byte store costs the same DRAM
@@ -132,33 +136,26 @@ __global__ void cold_scatter_hist_kernel(const uint64_t* __restrict__ dl_ptr,
       rv = make_uint4(a.x, a.y, a.z | a.w | b.x | b.y | b.z | b.w,
                       (uint32_t)(row_base + i) | (row_sp && row_sp[i] ? 0x80000000u : 0u));
     }
+    const uint32_t rowv = (uint32_t)(row_base + i);
     const uint64_t e = dl_ptr[i + 1];
     for (uint64_t k0 = dl_ptr[i] + sl; k0 < e; k0 += 32) {
       uint32_t r[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) r[u] = k0 + 8 * u < e ? dl_col[k0 + 8 * u] : 0u;
       uint64_t g[4];
-      uint32_t rk[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (r[u] >= K) {
-          g[u] = (part * y_card) + y_of_rank[r[u]];
-          rk[u] = atomicAdd(&Rk[g[u] * kHistSlots + zm], 1u);
-        }
+      for (int u = 0; u < 4; ++u) g[u] = r[u] >= K ? part * y_card + y_of_rank[r[u]] : 0;
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         if (r[u] < K) continue;
-        uint32_t h[kHistSlots];
-        load_hist(H, g[u], h);
-        const uint64_t y = g[u] - part * y_card;
-        for (uint32_t v = 0; v < nvar; ++v) {
-          if ((zm & v) || v == vskip) continue;
-          uint32_t pre = 0;
-          for (uint32_t z2 = 0; z2 < zm; ++z2)
-            if ((z2 & v) == 0) pre += h[z2];
-          const uint64_t pos = cptr[((uint64_t)v * parts + part) * y_card + y] + pre + rk[u];
-          if (rec) rec[pos] = rv;
-          else col[pos] = (uint32_t)(row_base + i);
+        // every variant v holding the row (v a submask of comp)
+        for (uint32_t v = comp;; v = (v - 1) & comp) {
+          if (v != vskip) {
+            const unsigned long long pos = atomicAdd(&cur[v * n_py + g[u]], 1ull);
+            if (rec) rec[pos] = rv;
+            else col[pos] = rowv;
+          }
+          if (v == 0) break;
         }
       }
     }

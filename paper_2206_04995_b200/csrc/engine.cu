@@ -940,7 +940,10 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
   uint32_t var_bits = 0, vskip = ~0u;
   uint64_t rows_key = 0, cnnz = 0;
   DBuf<uint32_t> cc, ch;  // (variant, part, y) counts; (part, y, mask) histogram
-  DBuf<uint64_t> cptr;
+  // cptr_buf = {0, segment starts...}: the scan is written one slot in
+  // (cpos, the scatter's cursors); after the scatter cptr_buf is the cptr
+  DBuf<uint64_t> cptr_buf;
+  uint64_t* cpos = nullptr;
   if (run_cold) {
     if (cold_bitmap) {
       // bitmap + deferred rows + compacted segments
@@ -978,9 +981,11 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     if (n_py)
       D3G_LAUNCH(X, cold_cnt_from_hist_kernel, grid_for(n_py, 256), 256, 0, ch.p, n_py, Y, parts,
                  var_bits, vskip, cc.p);
-    cptr = X.alloc<uint64_t>(rows_key + 1);
-    exclusive_scan<uint32_t>(X, cc.p, rows_key, cptr.p);
-    X.defer(&cnnz, cptr.p + rows_key, 8);
+    cptr_buf = X.alloc<uint64_t>(rows_key + 2);
+    cpos = cptr_buf.p + 1;
+    D3G_CUDA(cudaMemsetAsync(cptr_buf.p, 0, 8, X.stream));
+    exclusive_scan<uint32_t>(X, cc.p, rows_key, cpos);
+    X.defer(&cnnz, cpos + rows_key, 8);
     X.mark();
   }
   // z-split: the cold CSR is built now, for this rank's rows, and merged with
@@ -992,15 +997,13 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     const int N = in.zx->nranks;
     // every rank's offsets (its exclusive scan over its counts)
     DBuf<uint64_t> cp_all = X.alloc<uint64_t>((rows_key + 1) * N);
-    ex_allgatherv_dev(X, *in.zx, cptr.p, std::vector<uint64_t>(N, rows_key + 1), 8, cp_all.p);
+    ex_allgatherv_dev(X, *in.zx, cpos, std::vector<uint64_t>(N, rows_key + 1), 8, cp_all.p);
     DBuf<uint4> crec_l = X.alloc<uint4>(cnnz);
-    if (DL) {
-      DBuf<uint32_t> rk = X.zeros<uint32_t>((uint64_t)parts * Y * kHistSlots);
-      D3G_LAUNCH(X, cold_scatter_hist_kernel, grid_for(DL * 8, 256), 256, 0, in.dl_ptr, in.dl_col,
-                 DL, K, in.y_of_rank, cptr.p, ch.p, rk.p, Y, part_rows, parts,
-                 reinterpret_cast<const uint64_t*>(hzl), kw, var_bits, vskip, row_lo, crec_l.p,
-                 (uint32_t*)nullptr, in.row_sp);
-    }
+    if (DL)
+      D3G_LAUNCH(X, cold_scatter_cur_kernel, grid_for(DL * 8, 256), 256, 0, in.dl_ptr, in.dl_col,
+                 DL, K, in.y_of_rank, reinterpret_cast<unsigned long long*>(cpos), Y, part_rows,
+                 parts, reinterpret_cast<const uint64_t*>(hzl), kw, var_bits, vskip, row_lo,
+                 crec_l.p, (uint32_t*)nullptr, in.row_sp);
     cc.reset();
     ch.reset();
     // the ranks' record counts, their parts gathered rank-major
@@ -1018,7 +1021,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     crec_l.reset();
     // the job's offsets: the sum of the ranks' scans
     D3G_LAUNCH(X, sum_rows_u64_kernel, grid_for(rows_key + 1, 256), 256, 0, cp_all.p, rows_key + 1,
-               N, cptr.p);
+               N, cptr_buf.p);
     DBuf<uint64_t> pb = X.alloc<uint64_t>(N);
     X.to_device(pb.p, part_b.data(), N);
     crec_g = X.alloc<uint4>(tot);
@@ -1026,7 +1029,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     DBuf<LongSeg> longs = X.alloc<LongSeg>(tot / kMergeLong + 1);
     DBuf<unsigned int> n_long = X.zeros<unsigned int>(1);
     D3G_LAUNCH(X, cold_merge_kernel, grid_for((rows_key + 31) / 32 * 32, 256, X.sm_count * 16), 256,
-               0, cp_all.p, pb.p, crec_all.p, cptr.p, rows_key, N, crec_g.p, longs.p, n_long.p);
+               0, cp_all.p, pb.p, crec_all.p, cptr_buf.p, rows_key, N, crec_g.p, longs.p, n_long.p);
     D3G_LAUNCH(X, cold_merge_long_kernel, X.sm_count * 8, 256, 0, longs.p, n_long.p, crec_all.p,
                crec_g.p);
     cnnz = tot;
@@ -1339,10 +1342,9 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     } else {
       if (cold_kernel_ok) crec = X.alloc<uint4>(cnnz);
       else ccol = X.alloc<uint32_t>(cnnz);
-      DBuf<uint32_t> rk = X.zeros<uint32_t>((uint64_t)parts * Y * kHistSlots);
-      D3G_LAUNCH(X, cold_scatter_hist_kernel, grid_for(D * 8, 256), 256, 0, in.dl_ptr, in.dl_col,
-                 D, K, in.y_of_rank, cptr.p, ch.p, rk.p, Y, part_rows, parts,
-                 reinterpret_cast<const uint64_t*>(hz.p), kw, var_bits, vskip, 0ull,
+      D3G_LAUNCH(X, cold_scatter_cur_kernel, grid_for(D * 8, 256), 256, 0, in.dl_ptr, in.dl_col,
+                 D, K, in.y_of_rank, reinterpret_cast<unsigned long long*>(cpos), Y, part_rows,
+                 parts, reinterpret_cast<const uint64_t*>(hz.p), kw, var_bits, vskip, 0ull,
                  cold_kernel_ok ? crec.p : nullptr, ccol.p, rsp);
       cc.reset();
       ch.reset();
@@ -1363,7 +1365,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
           auto kfn = dense_cold_hash_kernel<decltype(M)::value>;
           D3G_CUDA(raise_smem_attr(kfn, (int)hsm));
           D3G_LAUNCH(X, kfn, (unsigned)X.sm_count * (D3G_CH_BITS <= 10 ? D3G_CH_CTAS : 3), kCHWarps * 32, hsm,
-                     xorder, n_live, in.r_ptr, in.r_col, cptr.p, crec.p, hz4,
+                     xorder, n_live, in.r_ptr, in.r_col, cptr_buf.p, crec.p, hz4,
                      reinterpret_cast<const uint4*>(hx.p), Y, var_bits, vskip, dlz, dec, em, next.p,
                      over_x.p, over_n.p, tc, cnt_sp,
                      env_u32("D3G_COLD_HASH_MAX", kCHMax, 1, kCHMax),
@@ -1386,7 +1388,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
             auto kfn = dense_cold_cta_kernel<decltype(M)::value>;
             D3G_CUDA(raise_smem_attr(kfn, (int)kCCSmem));
             D3G_LAUNCH(X, kfn, std::min<unsigned>(n_over, (unsigned)X.sm_count * kCCPerSm), kCCThreads,
-                       kCCSmem, over_x.p, over_n.p, in.r_ptr, in.r_col, cptr.p, crec.p, hz4,
+                       kCCSmem, over_x.p, over_n.p, in.r_ptr, in.r_col, cptr_buf.p, crec.p, hz4,
                        reinterpret_cast<const uint4*>(hx.p), Y, var_bits, vskip, dlz, dec, em,
                        over2_x.p, over2_n.p, env_u32("D3G_COLD_CTA_MAX", kCCMax, 1, kCCMax), tc,
                        cnt_sp, cand);
@@ -1404,7 +1406,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
           DBuf<uint32_t> touched = X.alloc<uint32_t>((uint64_t)og * kOvTouched);
           with_mode(mode, [&](auto M) {
             D3G_LAUNCH(X, dense_cold_overflow_kernel<decltype(M)::value>, og, kOvThreads, kOvSmem, ox,
-                       on, in.r_ptr, in.r_col, cptr.p, crec.p, hz4,
+                       on, in.r_ptr, in.r_col, cptr_buf.p, crec.p, hz4,
                        reinterpret_cast<const uint4*>(hx.p), Y, var_bits, vskip, dlz, gbm.p, words,
                        dec, em, tc, cnt_sp, touched.p, cand);
           });
@@ -1417,13 +1419,13 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
           if (csm > 48 * 1024)
             D3G_CUDA(raise_smem_attr(kfn, (int)csm));
           D3G_LAUNCH(X, kfn, (unsigned)X.sm_count * cold_ctas, kColdWarps * 32, csm, xorder, n_live,
-                     in.r_ptr, in.r_col, cptr.p, crec.p, hz4, reinterpret_cast<const uint4*>(hx.p), Y,
+                     in.r_ptr, in.r_col, cptr_buf.p, crec.p, hz4, reinterpret_cast<const uint4*>(hx.p), Y,
                      parts, part_rows, var_bits, vskip, dlz, dec, em, next.p, tc, cnt_sp, cand);
         });
       }
       D3G_CUDA(cudaEventRecord(ev3, X.stream));
     } else {
-      SparseInputs si{in.r_ptr, in.r_col, in.x_card, cptr.p, ccol.p, in.dl_z, D, Y, in.x_lo, in.x_hi};
+      SparseInputs si{in.r_ptr, in.r_col, in.x_card, cptr_buf.p, ccol.p, in.dl_z, D, Y, in.x_lo, in.x_hi};
       Filter flt{reinterpret_cast<const uint64_t*>(hx.p), reinterpret_cast<const uint64_t*>(hz.p), kw};
       run_sparse(X, si, dec, mode, em, cold, flt);
     }
