@@ -64,29 +64,6 @@ __device__ __forceinline__ void load_hist(const uint32_t* __restrict__ H, uint64
     h[4 * q + 3] = a.w;
   }
 }
-__global__ void cold_hist_kernel(const uint64_t* __restrict__ dl_ptr,
-                                 const uint32_t* __restrict__ dl_col, uint64_t n_dense, uint32_t K,
-                                 const uint32_t* __restrict__ y_of_rank, uint32_t* __restrict__ H,
-                                 uint64_t y_card, uint32_t part_rows,
-                                 const uint64_t* __restrict__ hz, uint32_t kw, uint32_t var_bits,
-                                 uint64_t row_base = 0) {
-  const uint32_t vmask = (1u << var_bits) - 1;
-  const uint32_t sl = threadIdx.x & 7;  // 8 lanes per row
-  for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 8) + (threadIdx.x >> 3); i < n_dense;
-       i += (uint64_t)gridDim.x * (blockDim.x / 8)) {
-    const uint64_t part = (row_base + i) / part_rows;
-    const uint32_t zm = var_bits ? (uint32_t)(hz[i * kw] & vmask) : 0;
-    const uint64_t e = dl_ptr[i + 1];
-    for (uint64_t k0 = dl_ptr[i] + sl; k0 < e; k0 += 32) {
-      uint32_t r[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) r[u] = k0 + 8 * u < e ? dl_col[k0 + 8 * u] : 0u;
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (r[u] >= K) atomicAdd(&H[((part * y_card) + y_of_rank[r[u]]) * kHistSlots + zm], 1u);
-    }
-  }
-}
 // (variant, part, y) counts from H: thread per (part, y)
 __global__ void cold_cnt_from_hist_kernel(const uint32_t* __restrict__ H, uint64_t n_py,
                                           uint64_t y_card, uint32_t parts, uint32_t var_bits,
@@ -106,12 +83,54 @@ __global__ void cold_cnt_from_hist_kernel(const uint32_t* __restrict__ H, uint64
     }
   }
 }
+// One thread per dense row. A row's ranks ascend, so its cold entries are
+// the suffix after its popc(hz[row]) hot ones: no lane idles on hot entries
+// and four cold entries of a row are in flight together.
+__device__ __forceinline__ uint32_t row_hot_count(const uint64_t* __restrict__ hz, uint32_t kw,
+                                                  uint64_t i, uint4& a, uint4& b) {
+  if (kw == 4) {
+    ld256(reinterpret_cast<const uint4*>(hz) + 2 * i, a, b);
+    return __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w) + __popc(b.x) + __popc(b.y) +
+           __popc(b.z) + __popc(b.w);
+  }
+  uint32_t n = 0;
+  for (uint32_t w = 0; w < kw; ++w) n += __popcll(hz[i * kw + w]);
+  const uint64_t w0 = hz[i * kw];
+  a = make_uint4((uint32_t)w0, (uint32_t)(w0 >> 32), 0, 0);
+  b = make_uint4(0, 0, 0, 0);
+  return n;
+}
+__global__ void cold_hist_kernel(const uint64_t* __restrict__ dl_ptr,
+                                 const uint32_t* __restrict__ dl_col, uint64_t n_dense,
+                                 const uint32_t* __restrict__ y_of_rank, uint32_t* __restrict__ H,
+                                 uint64_t y_card, uint32_t part_rows,
+                                 const uint64_t* __restrict__ hz, uint32_t kw, uint32_t var_bits,
+                                 uint64_t row_base = 0) {
+  const uint32_t vmask = (1u << var_bits) - 1;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_dense;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint4 a, b;
+    const uint64_t e = dl_ptr[i + 1];
+    uint64_t k = dl_ptr[i] + row_hot_count(hz, kw, i, a, b);
+    if (k >= e) continue;
+    const uint64_t pb = (row_base + i) / part_rows * y_card;
+    const uint32_t zm = a.x & vmask;
+    for (; k < e; k += 4) {
+      uint32_t r[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) r[u] = k + u < e ? dl_col[k + u] : 0u;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (k + u < e) atomicAdd(&H[(pb + y_of_rank[r[u]]) * kHistSlots + zm], 1u);
+    }
+  }
+}
 // cur: the exclusive scan of the (variant, part, y) counts; on return
 // cur[i] is the END of segment i (= the start of segment i + 1), so the
 // buffer one slot before cur, with a leading 0, is the finished cptr.
 __global__ void cold_scatter_cur_kernel(const uint64_t* __restrict__ dl_ptr,
                                         const uint32_t* __restrict__ dl_col, uint64_t n_dense,
-                                        uint32_t K, const uint32_t* __restrict__ y_of_rank,
+                                        const uint32_t* __restrict__ y_of_rank,
                                         unsigned long long* __restrict__ cur, uint64_t y_card,
                                         uint32_t part_rows, uint32_t parts,
                                         const uint64_t* __restrict__ hz, uint32_t kw,
@@ -120,43 +139,38 @@ __global__ void cold_scatter_cur_kernel(const uint64_t* __restrict__ dl_ptr,
                                         const uint8_t* __restrict__ row_sp) {
   const uint32_t vmask = (1u << var_bits) - 1;
   const uint64_t n_py = (uint64_t)parts * y_card;  // one variant's keys
-  const uint32_t sl = threadIdx.x & 7;  // 8 lanes per row
-  for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 8) + (threadIdx.x >> 3); i < n_dense;
-       i += (uint64_t)gridDim.x * (blockDim.x / 8)) {
-    const uint64_t part = (row_base + i) / part_rows;
-    const uint32_t zm = var_bits ? (uint32_t)(hz[i * kw] & vmask) : 0;
-    const uint32_t comp = vmask & ~zm;  // the variants that hold this row: v subset of comp
-    uint4 rv = make_uint4(0, 0, 0, 0);
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_dense;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint4 a, b;
+    const uint64_t e = dl_ptr[i + 1];
+    uint64_t k = dl_ptr[i] + row_hot_count(hz, kw, i, a, b);
+    if (k >= e) continue;
+    const uint64_t pb = (row_base + i) / part_rows * y_card;
+    const uint32_t comp = vmask & ~(a.x & vmask);  // the variants holding the row: v subset of comp
+    const uint32_t rowv = (uint32_t)(row_base + i);
     // rec: the whole 16-byte record is written here (its hot word, folded tail
     // and flags are the row's); a scattered 16-byte store costs the same DRAM
     // sector as a 4-byte one
-    if (rec) {
-      uint4 a, b;
-      ld256(reinterpret_cast<const uint4*>(hz) + 2 * i, a, b);
-      rv = make_uint4(a.x, a.y, a.z | a.w | b.x | b.y | b.z | b.w,
-                      (uint32_t)(row_base + i) | (row_sp && row_sp[i] ? 0x80000000u : 0u));
-    }
-    const uint32_t rowv = (uint32_t)(row_base + i);
-    const uint64_t e = dl_ptr[i + 1];
-    for (uint64_t k0 = dl_ptr[i] + sl; k0 < e; k0 += 32) {
-      uint32_t r[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) r[u] = k0 + 8 * u < e ? dl_col[k0 + 8 * u] : 0u;
+    const uint4 rv = make_uint4(a.x, a.y, a.z | a.w | b.x | b.y | b.z | b.w,
+                                rowv | (row_sp && row_sp[i] ? 0x80000000u : 0u));
+    for (; k < e; k += 4) {
       uint64_t g[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) g[u] = r[u] >= K ? part * y_card + y_of_rank[r[u]] : 0;
+      for (int u = 0; u < 4; ++u) g[u] = k + u < e ? pb + y_of_rank[dl_col[k + u]] : 0;
+      for (uint32_t v = comp;; v = (v - 1) & comp) {
+        if (v != vskip) {
+          unsigned long long pos[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (r[u] < K) continue;
-        // every variant v holding the row (v a submask of comp)
-        for (uint32_t v = comp;; v = (v - 1) & comp) {
-          if (v != vskip) {
-            const unsigned long long pos = atomicAdd(&cur[v * n_py + g[u]], 1ull);
-            if (rec) rec[pos] = rv;
-            else col[pos] = rowv;
-          }
-          if (v == 0) break;
+          for (int u = 0; u < 4; ++u)
+            if (k + u < e) pos[u] = atomicAdd(&cur[v * n_py + g[u]], 1ull);
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (k + u < e) {
+              if (rec) rec[pos[u]] = rv;
+              else col[pos[u]] = rowv;
+            }
         }
+        if (v == 0) break;
       }
     }
   }

@@ -974,7 +974,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     const uint64_t n_py = (uint64_t)parts * Y;
     ch = X.zeros<uint32_t>(n_py * kHistSlots);
     if (DL)
-      D3G_LAUNCH(X, cold_hist_kernel, grid_for(DL * 8, 256), 256, 0, in.dl_ptr, in.dl_col, DL, K,
+      D3G_LAUNCH(X, cold_hist_kernel, grid_for(DL, 256), 256, 0, in.dl_ptr, in.dl_col, DL,
                  in.y_of_rank, ch.p, Y, part_rows, reinterpret_cast<const uint64_t*>(hzl), kw,
                  var_bits, row_lo);
     cc = X.alloc<uint32_t>(rows_key);
@@ -1000,8 +1000,8 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     ex_allgatherv_dev(X, *in.zx, cpos, std::vector<uint64_t>(N, rows_key + 1), 8, cp_all.p);
     DBuf<uint4> crec_l = X.alloc<uint4>(cnnz);
     if (DL)
-      D3G_LAUNCH(X, cold_scatter_cur_kernel, grid_for(DL * 8, 256), 256, 0, in.dl_ptr, in.dl_col,
-                 DL, K, in.y_of_rank, reinterpret_cast<unsigned long long*>(cpos), Y, part_rows,
+      D3G_LAUNCH(X, cold_scatter_cur_kernel, grid_for(DL, 256), 256, 0, in.dl_ptr, in.dl_col,
+                 DL, in.y_of_rank, reinterpret_cast<unsigned long long*>(cpos), Y, part_rows,
                  parts, reinterpret_cast<const uint64_t*>(hzl), kw, var_bits, vskip, row_lo,
                  crec_l.p, (uint32_t*)nullptr, in.row_sp);
     cc.reset();
@@ -1342,8 +1342,8 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
     } else {
       if (cold_kernel_ok) crec = X.alloc<uint4>(cnnz);
       else ccol = X.alloc<uint32_t>(cnnz);
-      D3G_LAUNCH(X, cold_scatter_cur_kernel, grid_for(D * 8, 256), 256, 0, in.dl_ptr, in.dl_col,
-                 D, K, in.y_of_rank, reinterpret_cast<unsigned long long*>(cpos), Y, part_rows,
+      D3G_LAUNCH(X, cold_scatter_cur_kernel, grid_for(D, 256), 256, 0, in.dl_ptr, in.dl_col,
+                 D, in.y_of_rank, reinterpret_cast<unsigned long long*>(cpos), Y, part_rows,
                  parts, reinterpret_cast<const uint64_t*>(hz.p), kw, var_bits, vskip, 0ull,
                  cold_kernel_ok ? crec.p : nullptr, ccol.p, rsp);
       cc.reset();
