@@ -223,6 +223,19 @@ __device__ __forceinline__ uint4 ld_rec(const uint4* __restrict__ p) { return __
 #define D3G_COLD_UNROLL 2
 #endif
 constexpr int kColdU = D3G_COLD_UNROLL;         // candidate windows in flight per warp
+// The star segment (see warp_cold_x): D3G_STAR=0 compiles it out of the warp
+// kernels (the A/B build); windows in flight per warp in its lookup loop.
+#ifndef D3G_STAR
+#define D3G_STAR 1
+#endif
+constexpr bool kStar = D3G_STAR != 0;
+#ifndef D3G_STAR_WARP_UNROLL
+#define D3G_STAR_WARP_UNROLL 1
+#endif
+#ifndef D3G_STAR_CTA_UNROLL
+#define D3G_STAR_CTA_UNROLL 2
+#endif
+constexpr int kStarWarpU = D3G_STAR_WARP_UNROLL, kStarCtaU = D3G_STAR_CTA_UNROLL;
 constexpr uint32_t kDQ = 32u * (kColdU + 1);    // per-warp deferred rows (<= 31 + 32 U)
 constexpr uint32_t kSegWords = 32 * 3;          // per-warp compacted segments (u64 + u32)
 
@@ -383,18 +396,32 @@ __device__ __forceinline__ void cold_account(uint32_t x, uint32_t zc, const Deco
 // windows in flight; `on(st, row)` gets every candidate (st: kColdHot for the
 // lanes past the end), `step()` runs after each group of windows and returns
 // false to stop x. Returns the candidates streamed (warp-uniform).
-template <class On, class Step>
+//
+// The star segment. The rows of ONE segment are distinct (a y's list holds a
+// row once), so the last segment an x streams needs no insertion: its
+// survivors are new iff the dedup set built from the other segments does not
+// hold them. With `defer` the LONGEST segment of x (of its last chunk of 32 y
+// rows: nearly every x has one chunk) is left out of the stream and returned in
+// (star0, star_len) for cold_star: under Zipf it carries most of x's
+// candidates, so the set stays small (fewer overflows to the next tier, shorter
+// probe chains) and those candidates cost a lookup, not a CAS. An x whose other
+// segments pass route_min, or whose star passes star_route, is handed on
+// (`routed`).
+template <bool defer, class On, class Step>
 __device__ __forceinline__ uint32_t warp_cold_x(uint32_t x, const ColdX& s,
                                                 const uint64_t* __restrict__ r_ptr,
                                                 const uint32_t* __restrict__ r_col,
                                                 const uint64_t* __restrict__ cp,
                                                 const uint4* __restrict__ crec, uint64_t* sseg,
                                                 uint32_t* sE, uint32_t route_min, bool& routed,
-                                                On&& on, Step&& step) {
+                                                uint32_t star_route, uint64_t& star0,
+                                                uint32_t& star_len, On&& on, Step&& step) {
   const uint32_t lane = lane_id();
   const uint64_t r0 = r_ptr[x], r1 = r_ptr[x + 1];
   uint32_t streamed = 0;
   routed = false;
+  star0 = 0;
+  star_len = 0;
   for (uint64_t kb = r0; kb < r1; kb += 32) {
     const uint64_t kk = kb + lane;
     uint64_t seg0 = 0, seg1 = 0;
@@ -403,8 +430,22 @@ __device__ __forceinline__ uint32_t warp_cold_x(uint32_t x, const ColdX& s,
       seg0 = cp[y];
       seg1 = cp[y + 1];
     }
+    uint32_t len = (uint32_t)(seg1 - seg0);
+    if (defer && kb + 32 >= r1) {  // the last chunk: its longest segment is the star
+      const uint32_t m = __reduce_max_sync(0xffffffffu, len);
+      if (m > star_route) {
+        routed = true;
+        return streamed;
+      }
+      if (m) {
+        const int src = __ffs(__ballot_sync(0xffffffffu, len == m)) - 1;
+        star0 = __shfl_sync(0xffffffffu, seg0, src);
+        star_len = m;
+        if ((int)lane == src) len = 0;
+      }
+    }
     uint32_t n;
-    const uint32_t total = warp_stream_init(seg0, (uint32_t)(seg1 - seg0), sseg, sE, n);
+    const uint32_t total = warp_stream_init(seg0, len, sseg, sE, n);
     if (streamed + total > route_min) {  // handed on before streaming
       routed = true;
       return streamed;
@@ -430,6 +471,75 @@ __device__ __forceinline__ uint32_t warp_cold_x(uint32_t x, const ColdX& s,
     __syncwarp();  // sseg / sE are rewritten by the next chunk
   }
   return streamed;
+}
+
+// The star segment's candidates [first, star_len) in steps of `stride` windows
+// groups (a warp alone: first 0, stride 1; a CTA: each warp its own groups):
+// one contiguous run of records, so lane j of a window reads record tb + j (no
+// segment mapping). fn(ok, row) is the lookup (called by every lane); maybes
+// go through the warp's deferred queue as in the stream. Returns the lane's
+// candidates read.
+template <int kStarU, class Fn>
+__device__ __forceinline__ uint32_t cold_star(uint64_t star0, uint32_t star_len, uint32_t first,
+                                              uint32_t stride, const ColdX& s,
+                                              const uint4* __restrict__ crec, uint32_t* dq,
+                                              uint32_t& qn, const uint4* __restrict__ hz4,
+                                              uint64_t& ngat, Fn&& fn) {
+  const uint32_t lane = lane_id();
+  const uint4* p = crec + star0;
+  uint32_t mine = 0;
+  for (uint32_t tb = first * (32 * kStarU); tb < star_len; tb += stride * (32 * kStarU)) {
+    uint4 c[kStarU];
+#pragma unroll
+    for (int h = 0; h < kStarU; ++h)
+      if (tb + 32 * h + lane < star_len) {
+        ++mine;
+        c[h] = ld_rec(p + tb + 32 * h + lane);
+      }
+#pragma unroll
+    for (int h = 0; h < kStarU; ++h) {
+      const bool ok = tb + 32 * h + lane < star_len;
+      const uint32_t st = ok ? cold_test(c[h], s) : (uint32_t)kColdHot;
+      const uint32_t row = ok ? c[h].w : 0u;
+      fn(st == kColdSurvivor, row);
+      dq_push(dq, qn, st == kColdMaybe, row);
+      dq_drain(dq, qn, false, s, hz4, ngat, fn);  // the queue holds <= 31 + 32
+    }
+  }
+  dq_drain(dq, qn, true, s, hz4, ngat, fn);
+  return mine;
+}
+
+// The CTA kernels' star: the longest segment among x's y rows [r0, r1), by a
+// CTA-wide max of (length, first index). Returns its index in r_col (~0: x has
+// no candidates). s_best is zero on entry; the caller syncs before reuse.
+template <int kThreads>
+__device__ __forceinline__ uint64_t cta_star(uint64_t r0, uint64_t r1,
+                                             const uint32_t* __restrict__ r_col,
+                                             const uint64_t* __restrict__ cp,
+                                             unsigned long long* s_best, uint64_t& star0,
+                                             uint32_t& star_len) {
+  unsigned long long best = 0;
+  for (uint64_t k = r0 + threadIdx.x; k < r1; k += kThreads) {
+    const uint32_t y = r_col[k];
+    const unsigned long long len = cp[y + 1] - cp[y];
+    const unsigned long long key = (len << 32) | (0xffffffffull - (k - r0));
+    best = key > best ? key : best;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long u = __shfl_xor_sync(0xffffffffu, best, o);
+    best = u > best ? u : best;
+  }
+  if (lane_id() == 0 && (best >> 32)) atomicMax(s_best, best);
+  __syncthreads();
+  const unsigned long long b = *(volatile unsigned long long*)s_best;
+  star_len = (uint32_t)(b >> 32);
+  star0 = 0;
+  if (!star_len) return ~0ull;
+  const uint64_t kstar = r0 + (0xffffffffull - (b & 0xffffffffull));
+  star0 = cp[r_col[kstar]];
+  return kstar;
 }
 
 // ---- P2 with warp-private bitmaps (at most 16 row partitions: cfg2, cfg4) -----
@@ -498,9 +608,13 @@ dense_cold_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
         if (fresh) emit_at(em, slot, x, dl_z[row & kRowMask]);
       }
     };
+    // no star segment here: an atomicOr on the warp's bitmap costs what a bit
+    // test does (cfg2 0.65 -> 0.79 ms with it)
     bool routed;
-    ncand += warp_cold_x(
-        x, s, r_ptr, r_col, cp, crec, sseg, sE, 0xffffffffu, routed,
+    uint64_t star0;
+    uint32_t star_len;
+    ncand += warp_cold_x<false>(
+        x, s, r_ptr, r_col, cp, crec, sseg, sE, 0xffffffffu, routed, 0xffffffffu, star0, star_len,
         [&](uint32_t st, uint32_t row) {
           ins(st == kColdSurvivor, row);
           dq_push(dq, qn, st == kColdMaybe, row);
@@ -564,7 +678,8 @@ dense_cold_hash_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
                        Decode dec, Emit em, unsigned int* __restrict__ next,
                        uint32_t* __restrict__ over_x, unsigned int* __restrict__ over_n,
                        Tally* tally, unsigned long long* __restrict__ cnt_sp, uint32_t ch_max,
-                       uint32_t route_min, unsigned long long* __restrict__ cand = nullptr) {
+                       uint32_t route_min, uint32_t star_route,
+                       unsigned long long* __restrict__ cand = nullptr) {
   // [kCHWarps][kCHSlots] tables, [kCHWarps][kDQ] deferred rows,
   // [kCHWarps][kSegWords] compacted segments
   extern __shared__ __align__(16) uint32_t chtab[];
@@ -608,8 +723,10 @@ dense_cold_hash_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
       inserted += __popc(__ballot_sync(0xffffffffu, fresh));
     };
     bool routed;
-    const uint32_t streamed = warp_cold_x(
-        x, s, r_ptr, r_col, cp, crec, sseg, sE, route_min, routed,
+    uint64_t star0;
+    uint32_t star_len;
+    const uint32_t streamed = warp_cold_x<kStar>(
+        x, s, r_ptr, r_col, cp, crec, sseg, sE, route_min, routed, star_route, star0, star_len,
         [&](uint32_t st, uint32_t row) {
           ins(st == kColdSurvivor, row);
           dq_push(dq, qn, st == kColdMaybe, row);
@@ -624,11 +741,41 @@ dense_cold_hash_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
       over = inserted > ch_max;
     }
     __syncwarp();
+    uint32_t star_new = 0;  // warp-uniform
+    if (!over && star_len) {
+      // the star segment: looked up in the finished set, never inserted
+      auto look = [&](bool ok, uint32_t key) {
+        bool fresh = ok;
+        if (ok && inserted) {
+          uint32_t sl = ch_slot(key);
+          const uint32_t step = probe_step(key);
+          for (;;) {
+            const uint32_t cur = tab[sl];
+            if (cur == kCHEmpty) break;
+            if (cur == key) {
+              fresh = false;
+              break;
+            }
+            sl = (sl + step) & (kCHSlots - 1);
+          }
+        }
+        if (fresh && (key & kSpFlag)) ++xsp;
+        star_new += __popc(__ballot_sync(0xffffffffu, fresh));
+        if (kMode == kModeChecksum && fresh)
+          cold_account<kMode>(x, dl_z[key & kRowMask], dec, em, sum, xr);
+        if (kMode == kModeEmit) {
+          const unsigned long long slot = warp_reserve(em, fresh ? 1u : 0u);
+          if (fresh) emit_at(em, slot, x, dl_z[key & kRowMask]);
+        }
+      };
+      cold_star<kStarWarpU>(star0, star_len, 0, 1, s, crec, dq, qn, hz4, xgat, look);
+    }
     if (over) {
       if (lane == 0) over_x[atomicAdd(over_n, 1u)] = x;
     } else {
-      cnt += lane == 0 ? inserted : 0;
-      ncand += lane == 0 ? streamed : 0;  // x's stream counted once, in the tier that finishes it
+      cnt += lane == 0 ? inserted + star_new : 0;
+      // x's stream counted once, in the tier that finishes it
+      ncand += lane == 0 ? streamed + star_len : 0;
       ngat += xgat;
       csp += xsp;
     }
@@ -666,15 +813,16 @@ dense_cold_hash_kernel(const uint32_t* __restrict__ xs, uint64_t n_x,
 // warp-uniform binary search, the rest from the windows' boundary masks). Candidates are handed to on(st, row) as in
 // warp_cold_x; step() runs after each group of windows (per warp). The loop
 // stops at the next check once *stop is set (CTA-uniform). Returns this
-// thread's candidates streamed.
+// thread's candidates streamed. The segment of r_col index kstar (the star
+// segment, see warp_cold_x) is left out.
 template <int kThreads, class On, class Step>
 __device__ __forceinline__ uint64_t cta_cold_x(const ColdX& s, uint64_t r0, uint64_t r1,
                                                const uint32_t* __restrict__ r_col,
                                                const uint64_t* __restrict__ cp,
                                                const uint4* __restrict__ crec, uint64_t* s_seg0,
                                                uint32_t* s_off, uint32_t* s_wsum, uint32_t* s_tot,
-                                               const volatile unsigned int* stop, On&& on,
-                                               Step&& step) {
+                                               const volatile unsigned int* stop, uint64_t kstar,
+                                               On&& on, Step&& step) {
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   uint64_t mine = 0;
   for (uint64_t yb = r0; yb < r1 && !*stop; yb += kThreads) {
@@ -684,7 +832,7 @@ __device__ __forceinline__ uint64_t cta_cold_x(const ColdX& s, uint64_t r0, uint
     if (k < r1) {
       const uint32_t y = r_col[k];
       sg0 = cp[y];
-      len = (uint32_t)(cp[y + 1] - sg0);
+      len = k == kstar ? 0u : (uint32_t)(cp[y + 1] - sg0);  // the star segment is left out
     }
     uint32_t n;
     const uint32_t total = cta_stream_chunk<kThreads>(sg0, len, s_seg0, s_off, s_wsum, s_tot, n);
@@ -760,7 +908,8 @@ dense_cold_cta_kernel(const uint32_t* __restrict__ over_x, const unsigned int* _
   __shared__ uint32_t s_off[kCCThreads];
   __shared__ uint32_t s_wsum[2 * (kCCThreads / 32)];
   __shared__ uint32_t s_tot[2];
-  __shared__ unsigned int s_ins, s_over;
+  __shared__ unsigned int s_ins, s_over, s_star;
+  __shared__ unsigned long long s_best;
   extern __shared__ __align__(16) uint32_t cctab[];  // [kCCSlots], [warps][kDQ]
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   uint32_t* dq = cctab + kCCSlots + warp * kDQ;
@@ -776,8 +925,14 @@ dense_cold_cta_kernel(const uint32_t* __restrict__ over_x, const unsigned int* _
     if (threadIdx.x == 0) {
       s_ins = 0;
       s_over = 0;
+      s_star = 0;
+      s_best = 0;
     }
     __syncthreads();
+    uint64_t star0 = 0;
+    uint32_t star_len = 0;
+    const uint64_t kstar =
+        kStar ? cta_star<kCCThreads>(r0, r1, r_col, cp, &s_best, star0, star_len) : ~0ull;
     uint64_t xgat = 0, xsp = 0;  // credited only if x completes in this tier
     uint32_t qn = 0;
     uint32_t nf = 0;  // fresh inserts by this thread since the last flush
@@ -801,8 +956,8 @@ dense_cold_cta_kernel(const uint32_t* __restrict__ over_x, const unsigned int* _
       nf = 0;
       if (lane == 0 && wf && atomicAdd(&s_ins, wf) + wf > cc_max) s_over = 1;
     };
-    const uint64_t xcand = cta_cold_x<kCCThreads>(
-        s, r0, r1, r_col, cp, crec, s_seg0, s_off, s_wsum, s_tot, &s_over,
+    uint64_t xcand = cta_cold_x<kCCThreads>(
+        s, r0, r1, r_col, cp, crec, s_seg0, s_off, s_wsum, s_tot, &s_over, kstar,
         [&](uint32_t st, uint32_t row) {
           ins(st == kColdSurvivor, row);
           dq_push(dq, qn, st == kColdMaybe, row);
@@ -815,15 +970,50 @@ dense_cold_cta_kernel(const uint32_t* __restrict__ over_x, const unsigned int* _
       dq_drain(dq, qn, true, s, hz4, xgat, ins);
       flush_ins();
     }
-    __syncthreads();
+    __syncthreads();  // the set is complete
     const bool over = s_over != 0;
+    if (!over && star_len) {
+      // the star segment: looked up in the finished set, never inserted
+      uint32_t ns = 0;
+      auto look = [&](bool ok, uint32_t key) {
+        bool fresh = ok;
+        if (ok) {
+          uint32_t sl = cc_slot(key);
+          const uint32_t step = probe_step(key);
+          for (;;) {
+            const uint32_t cur = cctab[sl];
+            if (cur == kCHEmpty) break;
+            if (cur == key) {
+              fresh = false;
+              break;
+            }
+            sl = (sl + step) & (kCCSlots - 1);
+          }
+        }
+        if (fresh) {
+          ++ns;
+          if (key & kSpFlag) ++xsp;
+          if (kMode == kModeChecksum)
+            cold_account<kMode>(x, dl_z[key & kRowMask], dec, em, sum, xr);
+        }
+        if (kMode == kModeEmit) {
+          const unsigned long long slot = warp_reserve(em, fresh ? 1u : 0u);
+          if (fresh) emit_at(em, slot, x, dl_z[key & kRowMask]);
+        }
+      };
+      qn = 0;
+      xcand += cold_star<kStarCtaU>(star0, star_len, warp, kCCThreads / 32, s, crec, dq, qn, hz4, xgat, look);
+      ns = warp_sum(ns);
+      if (lane == 0 && ns) atomicAdd(&s_star, ns);
+      __syncthreads();
+    }
     if (over) {
       if (threadIdx.x == 0) over2_x[atomicAdd(over2_n, 1u)] = x;
     } else {
       ncand += xcand;
       ngat += xgat;
       csp += xsp;
-      if (threadIdx.x == 0) cnt += s_ins;
+      if (threadIdx.x == 0) cnt += s_ins + s_star;
     }
     if (kMode != kModeCount) {
       for (uint32_t i = threadIdx.x; i < kCCSlots; i += kCCThreads) {  // uniform trip count
@@ -858,11 +1048,15 @@ dense_cold_cta_kernel(const uint32_t* __restrict__ over_x, const unsigned int* _
 // x made non-zero are listed and cleared; if the list overflows, the stream
 // is replayed to clear every word it could have touched.
 constexpr int kOvThreads = 512;
+#ifndef D3G_OV_CTAS
+#define D3G_OV_CTAS 3
+#endif
+constexpr int kOvPerSm = D3G_OV_CTAS;
 constexpr uint32_t kOvTouched = 65536;  // touched-word list per CTA
 constexpr size_t kOvSmem = (size_t)(kOvThreads / 32) * kDQ * 4;
 
 template <int kMode>
-__global__ void __launch_bounds__(kOvThreads, 3)
+__global__ void __launch_bounds__(kOvThreads, kOvPerSm)
 dense_cold_overflow_kernel(const uint32_t* __restrict__ over_x, const unsigned int* __restrict__ over_n,
                            const uint64_t* __restrict__ r_ptr, const uint32_t* __restrict__ r_col,
                            const uint64_t* __restrict__ cptr, const uint4* __restrict__ crec,
@@ -879,6 +1073,7 @@ dense_cold_overflow_kernel(const uint32_t* __restrict__ over_x, const unsigned i
   __shared__ uint32_t s_tot[2];
   __shared__ unsigned int s_nt;  // bitmap words this x made non-zero (touched list)
   __shared__ unsigned int s_never;  // 0: the candidate loop never stops early
+  __shared__ unsigned long long s_best;
   extern __shared__ __align__(16) uint32_t ovdq[];  // [warps][kDQ]
   uint32_t* tl = touched + (uint64_t)blockIdx.x * kOvTouched;
   const uint32_t warp = threadIdx.x >> 5;
@@ -893,8 +1088,15 @@ dense_cold_overflow_kernel(const uint32_t* __restrict__ over_x, const unsigned i
     const uint32_t v = x_variant(s.a0.x, var_bits, vskip);
     const uint64_t* cp = cptr + (uint64_t)v * y_card;
     const uint64_t r0 = r_ptr[x], r1 = r_ptr[x + 1];
-    if (threadIdx.x == 0) s_nt = 0;
+    if (threadIdx.x == 0) {
+      s_nt = 0;
+      s_best = 0;
+    }
     __syncthreads();
+    uint64_t star0 = 0;
+    uint32_t star_len = 0;
+    const uint64_t kstar =
+        kStar ? cta_star<kOvThreads>(r0, r1, r_col, cp, &s_best, star0, star_len) : ~0ull;
     auto ins = [&](bool ok, uint32_t key) {
       if (!ok) return;
       const uint32_t zl = key & kRowMask;
@@ -911,14 +1113,29 @@ dense_cold_overflow_kernel(const uint32_t* __restrict__ over_x, const unsigned i
     };
     uint32_t qn = 0;
     ncand += cta_cold_x<kOvThreads>(
-        s, r0, r1, r_col, cp, crec, s_seg0, s_off, s_wsum, s_tot, &s_never,
+        s, r0, r1, r_col, cp, crec, s_seg0, s_off, s_wsum, s_tot, &s_never, kstar,
         [&](uint32_t st, uint32_t row) {
           ins(st == kColdSurvivor, row);
           dq_push(dq, qn, st == kColdMaybe, row);
         },
         [&]() { dq_drain(dq, qn, false, s, hz4, ngat, ins); });
     dq_drain(dq, qn, true, s, hz4, ngat, ins);
-    __syncthreads();
+    __syncthreads();  // the bitmap is complete
+    if (star_len) {
+      // the star segment: a bit test (L2 reads: the bits were set by atomics),
+      // nothing written, so its words need no clearing either
+      auto look = [&](bool ok, uint32_t key) {
+        if (!ok) return;
+        const uint32_t zl = key & kRowMask;
+        if ((__ldcg(&bm[zl >> 5]) >> (zl & 31)) & 1u) return;
+        ++cnt;
+        if (key & kSpFlag) ++csp;
+        if (kMode != kModeCount) cold_account<kMode>(x, dl_z[zl], dec, em, sum, xr);
+      };
+      qn = 0;
+      ncand += cold_star<kStarCtaU>(star0, star_len, warp, kOvThreads / 32, s, crec, dq, qn, hz4, ngat, look);
+      __syncthreads();
+    }
     // clear through the touched list; replay the stream only if it overflowed
     const uint32_t nt = s_nt;
     if (nt <= kOvTouched) {
@@ -926,7 +1143,7 @@ dense_cold_overflow_kernel(const uint32_t* __restrict__ over_x, const unsigned i
     } else {
       uint32_t dummy = 0;
       cta_cold_x<kOvThreads>(
-          s, r0, r1, r_col, cp, crec, s_seg0, s_off, s_wsum, s_tot, &s_never,
+          s, r0, r1, r_col, cp, crec, s_seg0, s_off, s_wsum, s_tot, &s_never, kstar,
           [&](uint32_t st, uint32_t row) {
             if (st != kColdHot) bm[(row & kRowMask) >> 5] = 0;  // clearing an untouched word is harmless
           },

@@ -1357,11 +1357,25 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
       D3G_CUDA(cudaEventCreate(&ev2));
       D3G_CUDA(cudaEventCreate(&ev3));
       D3G_CUDA(cudaEventRecord(ev2, X.stream));
+      // the star segment (x's longest: looked up, never inserted); an x whose
+      // star is longer than this is handed to the CTA tier
+      const uint32_t star_route = env_u32("D3G_COLD_STAR", D3G_COLD_ROUTE, 1, 0xffffffffu);
+      // D3G_TRACE: per-tier wall time (synchronised; diagnostics only)
+      const bool ttrace = std::getenv("D3G_TRACE") != nullptr;
+      auto tier = [&](const char* name, auto&& launch) {
+        if (!ttrace) return launch();
+        D3G_CUDA(cudaStreamSynchronize(X.stream));
+        const auto t0 = std::chrono::steady_clock::now();
+        launch();
+        D3G_CUDA(cudaStreamSynchronize(X.stream));
+        std::fprintf(stderr, "[cold tier] %s %.3f ms\n", name,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+      };
       if (cold_hash) {
         DBuf<uint32_t> over_x = X.alloc<uint32_t>(n_live);
         DBuf<unsigned int> over_n = X.zeros<unsigned int>(1);
         const size_t hsm = kCHSmem;
-        with_mode(mode, [&](auto M) {
+        tier("warp hash", [&] { with_mode(mode, [&](auto M) {
           auto kfn = dense_cold_hash_kernel<decltype(M)::value>;
           D3G_CUDA(raise_smem_attr(kfn, (int)hsm));
           D3G_LAUNCH(X, kfn, (unsigned)X.sm_count * (D3G_CH_BITS <= 10 ? D3G_CH_CTAS : 3), kCHWarps * 32, hsm,
@@ -1369,8 +1383,8 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
                      reinterpret_cast<const uint4*>(hx.p), Y, var_bits, vskip, dlz, dec, em, next.p,
                      over_x.p, over_n.p, tc, cnt_sp,
                      env_u32("D3G_COLD_HASH_MAX", kCHMax, 1, kCHMax),
-                     env_u32("D3G_COLD_ROUTE", D3G_COLD_ROUTE, 1, 0xffffffffu), cand);
-        });
+                     env_u32("D3G_COLD_ROUTE", D3G_COLD_ROUTE, 1, 0xffffffffu), star_route, cand);
+        }); });
         const unsigned int n_over = X.scalar(over_n.p);
         out.cold_overflow = n_over;
         // overflowing x: a CTA-wide shared-memory hash first; the few past its
@@ -1384,7 +1398,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
         if (n_over && cta_tier) {
           over2_x = X.alloc<uint32_t>(n_over);
           over2_n = X.zeros<unsigned int>(1);
-          with_mode(mode, [&](auto M) {
+          tier("cta hash", [&] { with_mode(mode, [&](auto M) {
             auto kfn = dense_cold_cta_kernel<decltype(M)::value>;
             D3G_CUDA(raise_smem_attr(kfn, (int)kCCSmem));
             D3G_LAUNCH(X, kfn, std::min<unsigned>(n_over, (unsigned)X.sm_count * kCCPerSm), kCCThreads,
@@ -1392,7 +1406,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
                        reinterpret_cast<const uint4*>(hx.p), Y, var_bits, vskip, dlz, dec, em,
                        over2_x.p, over2_n.p, env_u32("D3G_COLD_CTA_MAX", kCCMax, 1, kCCMax), tc,
                        cnt_sp, cand);
-          });
+          }); });
           n_over2 = X.scalar(over2_n.p);
         }
         if (n_over2) {
@@ -1401,15 +1415,15 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
           const uint64_t words = (D + 31) / 32;
           const unsigned og = (unsigned)std::min<uint64_t>(
               (uint64_t)n_over2,
-              (uint64_t)env_u32("D3G_OVERFLOW_CTAS", X.sm_count * 3, 1, X.sm_count * 16));
+              (uint64_t)env_u32("D3G_OVERFLOW_CTAS", X.sm_count * kOvPerSm, 1, X.sm_count * 16));
           DBuf<uint32_t> gbm = X.zeros<uint32_t>((uint64_t)og * words);
           DBuf<uint32_t> touched = X.alloc<uint32_t>((uint64_t)og * kOvTouched);
-          with_mode(mode, [&](auto M) {
+          tier("bitmap", [&] { with_mode(mode, [&](auto M) {
             D3G_LAUNCH(X, dense_cold_overflow_kernel<decltype(M)::value>, og, kOvThreads, kOvSmem, ox,
                        on, in.r_ptr, in.r_col, cptr_buf.p, crec.p, hz4,
                        reinterpret_cast<const uint4*>(hx.p), Y, var_bits, vskip, dlz, gbm.p, words,
                        dec, em, tc, cnt_sp, touched.p, cand);
-          });
+          }); });
         }
         out.cold_overflow2 = n_over2;
       } else {
@@ -2132,7 +2146,8 @@ void map_inputs(Ctx& X, const uint64_t* Rl, const uint64_t* Rr, uint64_t NR, con
     hs[1].sample_fail = (unsigned)v[3];
     r_empty = nr_global == 0;
   }
-  const uint64_t lens_job[4] = {r_empty ? 0 : 1, r_empty ? 0 : 1, NS, NS};
+  const uint64_t one_r = r_empty ? 0u : 1u;
+  const uint64_t lens_job[4] = {one_r, one_r, NS, NS};
   auto det = [&](int i) { return lens_job[i] > 0 && hs[i].sample_fail == 0; };
   auto fits = [&](int i) { return lens_job[i] == 0 || hs[i].max < (1ull << 32); };
   bool sx = o->declared_x != 0, sy = o->declared_y != 0, sz = o->declared_z != 0;

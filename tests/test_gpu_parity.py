@@ -421,6 +421,78 @@ def test_cfg5_cold_overflow_tiers_match_reference(monkeypatch):
     torch.cuda.empty_cache()
 
 
+@pytest.mark.parametrize("env", [
+    {"D3G_COLD_STAR": "1"},                              # every star hands its x to the CTA tier
+    {"D3G_COLD_STAR": "1", "D3G_COLD_CTA_MAX": "256"},   # ... and on to the bitmap tier
+    {"D3G_COLD_STAR": "4000000000", "D3G_COLD_ROUTE": "4000000000"},  # no x routed by size
+    {"D3G_COLD_STAR": "64", "D3G_COLD_HASH_MAX": "200"},
+])
+def test_cfg5_cold_star_segment_matches_reference(env, monkeypatch):
+    """The star segment of the hash cold pass (each x's longest segment is
+    looked up in the finished dedup set instead of inserted) in all three
+    tiers: routing thresholds forced so that the star is resolved by the warp
+    tier, the CTA tier and the bitmap tier; count and fingerprint of the cfg5
+    x<1000 slice equal the reference's."""
+    import torch
+    g = _golden().get("cfg5_x_lt_1000")
+    if g is None:
+        pytest.skip("golden entry not generated")
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    rl, rr = d3.generate(5, 0)
+    sl, sr = d3.generate(5, 1)
+    e = d3.EngineConfig(force=d3.Strategy.auto_select, count_only=True, checksum=True,
+                        memory_budget_bytes=120 << 30, x_code_range=(0, 1000))
+    rep = d3.join_project(d3.RawTable(rl, rr), d3.RawTable(sl, sr), e, C).report
+    assert (rep.out_p, rep.checksum_sum, rep.checksum_xor) == \
+        (g["set"]["count"], g["set"]["sum"], g["set"]["xor"])
+    del rl, rr, sl, sr
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("seed", [11, 12])
+def test_hash_cold_pass_long_rows_match_bitmap_path(seed, monkeypatch):
+    """The hash cold pass forced (D3G_COLD_PATH=hash) on skewed instances whose
+    x rows hold 50-150 y values (several 32-row chunks per x: the star segment
+    is the longest of the LAST chunk) gives the pairs, count and fingerprint
+    of the bitmap cold kernel and of numpy; also with tiny tier limits."""
+    rng = np.random.default_rng(seed)
+    nx, ny, n = int(rng.integers(1200, 1800)), int(rng.integers(20000, 40000)), 120000
+    w = 1.0 / np.arange(1, ny + 1) ** float(rng.uniform(0.6, 0.8))
+    w /= w.sum()
+    r = (rng.integers(0, nx, n).astype(np.uint64), rng.choice(ny, n, p=w).astype(np.uint64))
+    s = (rng.integers(0, 4 * nx, n).astype(np.uint64), rng.choice(ny, n, p=w).astype(np.uint64))
+    base = _run(r, s, d3.Strategy.hybrid, count_only=True, checksum=True).report
+    # numpy: distinct (x, z) of the join, packed x << 32 | z
+    ru = np.unique(np.stack(r, 1), axis=0)
+    su = np.unique(np.stack(s, 1), axis=0)
+    su = su[np.argsort(su[:, 1], kind="stable")]
+    lo = np.searchsorted(su[:, 1], ru[:, 1], "left")
+    hi = np.searchsorted(su[:, 1], ru[:, 1], "right")
+    reps = hi - lo
+    xs = np.repeat(ru[:, 0], reps)
+    idx = np.repeat(lo, reps) + (np.arange(reps.sum()) - np.repeat(np.cumsum(reps) - reps, reps))
+    want = np.unique((xs << np.uint64(32)) | su[idx, 0])
+    assert base.out_p == len(want)
+    assert base.cold_candidates > 0  # the cold pass has work
+    for env in ({}, {"D3G_COLD_HASH_MAX": "32"},
+                {"D3G_COLD_HASH_MAX": "32", "D3G_COLD_CTA_MAX": "64"}, {"D3G_COLD_STAR": "8"}):
+        monkeypatch.setenv("D3G_COLD_PATH", "hash")
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        rep = _run(r, s, d3.Strategy.hybrid, count_only=True, checksum=True).report
+        assert (rep.out_p, rep.checksum_sum, rep.checksum_xor) == \
+            (base.out_p, base.checksum_sum, base.checksum_xor), env
+        cnt = _run(r, s, d3.Strategy.hybrid, count_only=True).report
+        assert cnt.out_p == base.out_p, env
+        out = _run(r, s, d3.Strategy.hybrid)
+        got = np.sort((np.asarray(out.result.raw_x, dtype=np.uint64) << np.uint64(32)) |
+                      np.asarray(out.result.raw_z, dtype=np.uint64))
+        assert np.array_equal(got, want), env
+        for k in env:
+            monkeypatch.delenv(k)
+
+
 @pytest.mark.parametrize("seed", [7, 8, 9])
 def test_pivot_plan_mid_size_instances(seed, monkeypatch):
     """Mid-size skewed instances (x over 20-40k, Zipf y over a few hundred
