@@ -511,7 +511,8 @@ def main():
                              f"(each x's stream counted once); kernel time {cold_ms:.3f} ms "
                              f"(CUDA events on the library stream); the records are L2-resident "
                              f"in part, so traffic < work is possible; the kernels are issue-bound "
-                             f"(ncu: IPC 2.2-2.5, profiles/), not bandwidth-bound",
+                             f"(ncu: IPC 2.0-2.4 of 4, long-scoreboard the top stall; profiles/), "
+                             f"not bandwidth-bound",
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs",
                      "share_of_step": cold_ms / phase["ms_total"]}
     if dom in ("dense_ec", "sparse_bmm") and cold_roof and cold_ms > hot_ms:
@@ -588,10 +589,13 @@ def main():
                               "B_M": b_map,
                               "by_phase_ms": {k: phase[k] for k in ("ms_map", "ms_csr", "ms_stats",
                                                                     "ms_partition")}},
+        # (a phase under 50 us is an empty launch: the sparse rows were folded
+        # into the dense layout, or there are none; no rate is quoted for it)
         "sparse_bmm": {"ms": phase["ms_sparse"],
-                       "GB/s": b_sparse / (phase["ms_sparse"] * 1e-3) / 1e9 if phase["ms_sparse"] else None,
+                       "GB/s": b_sparse / (phase["ms_sparse"] * 1e-3) / 1e9
+                       if phase["ms_sparse"] > 0.05 else None,
                        "frac_of_hbm": b_sparse / (phase["ms_sparse"] * 1e-3) / 1e9 / hbm
-                       if phase["ms_sparse"] else None},
+                       if phase["ms_sparse"] > 0.05 else None},
         "dense_ec": {"ms": phase["ms_dense"],
                      "pair_tests_per_s": (p_dense / (phase["ms_dense"] * 1e-3))
                      if phase["ms_dense"] else None},

@@ -81,6 +81,21 @@ typedef struct {
   uint32_t pad;
 } d3g_consts;
 
+/* d3g_opts.natural_keys_auto bits. D3G_KEYS_AUTO is the reference's
+ * natural_keys_auto. A caller holding ColumnType::bytes columns
+ * (P/include/dim3/relation.hpp:21) passes surrogate u64 ids for them (equal
+ * strings <-> equal ids; integration/dim3_gpu.hpp interns them) and marks the
+ * column, in ENGINE orientation (x = the larger table's left column, z = the
+ * other's, as natural_keys_declared): such a column is always dictionary-coded
+ * (detect_natural_keys is false for bytes, P/src/mapping.cpp:284) and
+ * declaring it natural is a ConfigError (require_natural, :328-331). */
+enum {
+  D3G_KEYS_AUTO = 1,
+  D3G_KEYS_BYTES_X = 2,
+  D3G_KEYS_BYTES_Y = 4,
+  D3G_KEYS_BYTES_Z = 8
+};
+
 /* dim3::EngineConfig (P/include/dim3/engine.hpp:36-48) plus GPU options. */
 typedef struct {
   int32_t force;              /* D3G_AUTO .. D3G_DENSE_ONLY */
@@ -88,7 +103,7 @@ typedef struct {
   uint64_t memory_budget_bytes;  /* device working-set cap; 0 = 3 GiB default */
   int32_t count_only;
   int32_t dense_mode;
-  int32_t natural_keys_auto;
+  int32_t natural_keys_auto;  /* D3G_KEYS_* bits; 1 = EngineConfig::natural_keys_auto */
   int32_t declared_x, declared_y, declared_z;  /* natural_keys_declared */
   int32_t checksum;           /* also compute (sum, xor) of mix64(mix64(x)^z) */
   int32_t collect_counters;   /* also compute dense_blocks_checked and

@@ -3,6 +3,10 @@
 // paper_2206_04995_b200/libdim3_b200.so. Compiled and run against the unmodified
 // reference by integration/shim_check.cpp (oracle/Makefile target `shim`).
 #pragma once
+#include <string>
+#include <unordered_map>
+#include <vector>
+
 #include "dim3/engine.hpp"
 #include "dim3_b200.h"   // from this repo's include/
 
@@ -35,14 +39,67 @@ struct GpuOptions {
   bool exact_counters = false;
 };
 
+// ColumnType::bytes columns (relation.hpp:21): the GPU takes u64 columns, so a
+// byte-string column is interned on the host into surrogate ids (equal strings
+// <-> equal ids, in first-occurrence order) and flagged D3G_KEYS_BYTES_*; the
+// device then dictionary-codes the ids as the reference does the strings, and
+// the result ids are mapped back. The two y columns share one interner; when
+// their types differ no R row finds its y (Dictionary::lookup,
+// mapping.cpp:177-189), which disjoint id ranges reproduce.
+class ColumnInterner {
+ public:
+  // ids of a bytes column; `tag` keeps u64 values and strings apart when the
+  // two y columns differ in type
+  std::vector<std::uint64_t> intern(const ColumnData& col) {
+    std::vector<std::uint64_t> ids(col.size());
+    if (col.type == ColumnType::bytes) {
+      for (std::size_t i = 0; i < ids.size(); ++i) {
+        auto [it, fresh] = str_ids_.try_emplace(col.strs[i], next_);
+        if (fresh) {
+          rev_.push_back(&it->first);
+          ++next_;
+        }
+        ids[i] = it->second;
+      }
+    } else {
+      for (std::size_t i = 0; i < ids.size(); ++i) {
+        auto [it, fresh] = int_ids_.try_emplace(col.ints[i], next_);
+        if (fresh) {
+          rev_.push_back(nullptr);
+          ++next_;
+        }
+        ids[i] = it->second;
+      }
+    }
+    return ids;
+  }
+  const std::string& value(std::uint64_t id) const { return *rev_[id]; }
+
+ private:
+  std::unordered_map<std::string, std::uint64_t> str_ids_;  // node-based: keys stay put
+  std::unordered_map<std::uint64_t, std::uint64_t> int_ids_;
+  std::vector<const std::string*> rev_;
+  std::uint64_t next_ = 0;
+};
+
 inline JoinProjectOutput join_project(const RawTable& r, const RawTable& s,
                                       const EngineConfig& cfg, const CostConstants& c,
                                       const GpuOptions& g = {}) {
-  if (r.left.type != ColumnType::u64 || r.right.type != ColumnType::u64 ||
-      s.left.type != ColumnType::u64 || s.right.type != ColumnType::u64)
-    throw ConfigError("the GPU path takes integer (u64) columns");
-  d3g_table R{r.left.ints.data(), r.right.ints.data(), r.size(), 0, 0};
-  d3g_table S{s.left.ints.data(), s.right.ints.data(), s.size(), 0, 0};
+  // surrogate ids for byte-string columns (none: the columns are passed as they are)
+  ColumnInterner ix, iy, iz;
+  std::vector<std::uint64_t> rl_ids, rr_ids, sl_ids, sr_ids;
+  const bool bytes_x = r.left.type == ColumnType::bytes, bytes_z = s.left.type == ColumnType::bytes;
+  const bool bytes_y = r.right.type == ColumnType::bytes || s.right.type == ColumnType::bytes;
+  if (bytes_x) rl_ids = ix.intern(r.left);
+  if (bytes_z) sl_ids = iz.intern(s.left);
+  if (bytes_y) {
+    rr_ids = iy.intern(r.right);
+    sr_ids = iy.intern(s.right);
+  }
+  d3g_table R{bytes_x ? rl_ids.data() : r.left.ints.data(),
+              bytes_y ? rr_ids.data() : r.right.ints.data(), r.size(), 0, 0};
+  d3g_table S{bytes_z ? sl_ids.data() : s.left.ints.data(),
+              bytes_y ? sr_ids.data() : s.right.ints.data(), s.size(), 0, 0};
   d3g_consts k{c.t_seqR, c.t_randR, c.t_randRW, c.t_hash, c.t_map, c.t_ECs, c.t_ECd, c.w, 0};
   d3g_opts o;
   d3g_opts_default(&o);
@@ -51,7 +108,12 @@ inline JoinProjectOutput join_project(const RawTable& r, const RawTable& s,
   o.memory_budget_bytes = cfg.memory_budget_bytes;
   o.count_only = cfg.count_only;
   o.dense_mode = static_cast<int32_t>(cfg.dense_mode);
-  o.natural_keys_auto = cfg.natural_keys_auto;
+  // the flags are in engine orientation: the larger table is the engine's R
+  const bool swapped = engine_will_swap(r, s);
+  o.natural_keys_auto = (cfg.natural_keys_auto ? D3G_KEYS_AUTO : 0) |
+                        ((swapped ? bytes_z : bytes_x) ? D3G_KEYS_BYTES_X : 0) |
+                        (bytes_y ? D3G_KEYS_BYTES_Y : 0) |
+                        ((swapped ? bytes_x : bytes_z) ? D3G_KEYS_BYTES_Z : 0);
   o.declared_x = cfg.natural_keys_declared.x;
   o.declared_y = cfg.natural_keys_declared.y;
   o.declared_z = cfg.natural_keys_declared.z;
@@ -59,7 +121,8 @@ inline JoinProjectOutput join_project(const RawTable& r, const RawTable& s,
   d3g_report rep{};
   JoinProjectOutput out;
   out.result.provenance = ResultSet::Provenance::raw;   // decoded on the device
-  out.result.raw_x.type = out.result.raw_z.type = ColumnType::u64;
+  out.result.raw_x.type = r.left.type;                  // decode_result, engine.cpp:502-523
+  out.result.raw_z.type = s.left.type;
   if (cfg.count_only) {
     throw_status(d3g_join_project(context(), &R, &S, &k, &o, &rep, nullptr));
   } else {
@@ -70,6 +133,14 @@ inline JoinProjectOutput join_project(const RawTable& r, const RawTable& s,
     out.result.raw_z.ints.resize(p.n);
     throw_status(d3g_take_pairs(context(), out.result.raw_x.ints.data(),
                                 out.result.raw_z.ints.data(), p.n, 0));
+    auto to_strings = [](ColumnData& col, const ColumnInterner& in) {
+      col.strs.reserve(col.ints.size());
+      for (std::uint64_t id : col.ints) col.strs.push_back(in.value(id));
+      col.ints.clear();
+      col.ints.shrink_to_fit();
+    };
+    if (bytes_x) to_strings(out.result.raw_x, ix);
+    if (bytes_z) to_strings(out.result.raw_z, iz);
   }
   out.result.materialized = !cfg.count_only;
   out.result.count = rep.out_p;

@@ -8,6 +8,8 @@
 // Mirrors P/tests/test_engine.cpp:89-113 and acceptance criterion 1.
 // Build: make -C oracle shim (needs /root/reference); run on a B200.
 #include <cstdio>
+#include <set>
+#include <string>
 
 #include "dim3_gpu.hpp"
 #include "support.hpp"
@@ -91,6 +93,87 @@ int main() {
       }
     }
   }
+  // ColumnType::bytes columns (relation.hpp:21): the same instances with
+  // their columns turned into byte strings, one column role at a time, all of
+  // them, and with the two y columns of different types (no R row finds its
+  // y). The GPU shim interns the strings; sets, counts and the decisions of
+  // the report equal the reference's run on the same byte-string tables.
+  int bytes_runs = 0;
+  {
+    auto as_bytes = [](dim3::ColumnData& col) {
+      col.type = dim3::ColumnType::bytes;
+      for (std::uint64_t v : col.ints) col.strs.push_back("k" + std::to_string(v * 7919 % 100003));
+      col.ints.clear();
+    };
+    auto cell = [](const dim3::ColumnData& col, std::size_t i) {
+      return col.type == dim3::ColumnType::u64 ? "#" + std::to_string(col.ints[i]) : col.strs[i];
+    };
+    auto str_set = [&](const dim3::ResultSet& raw) {
+      std::set<std::pair<std::string, std::string>> out;
+      for (std::size_t i = 0; i < raw.raw_x.size(); ++i)
+        out.insert({cell(raw.raw_x, i), cell(raw.raw_z, i)});
+      return out;
+    };
+    dim3::SplitMix64 rng{77};
+    for (int it = 0; it < 6; ++it) {
+      const auto base = testsup::random_instance(rng);
+      for (int variant = 0; variant < 6; ++variant, ++bytes_runs) {
+        auto inst = base;
+        if (variant == 0 || variant == 3) as_bytes(inst.r.left);
+        if (variant == 1 || variant == 3) {
+          as_bytes(inst.r.right);
+          as_bytes(inst.s.right);
+        }
+        if (variant == 2 || variant == 3) as_bytes(inst.s.left);
+        if (variant == 4) as_bytes(inst.r.right);  // y types differ
+        if (variant == 5) as_bytes(inst.s.right);
+        for (dim3::Strategy f : {dim3::Strategy::auto_select, dim3::Strategy::hybrid,
+                                 dim3::Strategy::classical}) {
+          auto cpu = dim3::join_project(inst.r, inst.s, forced(f, false), c);
+          auto gpu = dim3::gpu::join_project(inst.r, inst.s, forced(f, false), c);
+          const auto cr = dim3::result_to_raw(cpu), gr = dim3::result_to_raw(gpu);
+          CHECK_EQ(str_set(gr), str_set(cr), "bytes: set");
+          CHECK_EQ(gr.raw_x.type, cr.raw_x.type, "bytes: x type");
+          CHECK_EQ(gr.raw_z.type, cr.raw_z.type, "bytes: z type");
+          CHECK_EQ(gpu.result.count, cpu.result.count, "bytes: count");
+          const auto &a = cpu.report, &b = gpu.report;
+          CHECK_EQ(a.strategy, b.strategy, "bytes: strategy");
+          CHECK_EQ(a.swapped, b.swapped, "bytes: swapped");
+          CHECK_EQ(a.out_j_estimate, b.out_j_estimate, "bytes: out_j_estimate");
+          CHECK_EQ(a.dropped_r, b.dropped_r, "bytes: dropped_r");
+          if (a.strategy != "classical") {
+            CHECK_EQ(a.x_card, b.x_card, "bytes: x_card");
+            CHECK_EQ(a.y_card, b.y_card, "bytes: y_card");
+            CHECK_EQ(a.z_card, b.z_card, "bytes: z_card");
+            CHECK_EQ(a.dense_z, b.dense_z, "bytes: dense_z");
+            CHECK_EQ(a.sparse_z, b.sparse_z, "bytes: sparse_z");
+            CHECK_EQ(a.pairs_dense, b.pairs_dense, "bytes: pairs_dense");
+            CHECK_EQ(a.pairs_sparse, b.pairs_sparse, "bytes: pairs_sparse");
+          }
+          auto cnt = dim3::gpu::join_project(inst.r, inst.s, forced(f, true), c);
+          CHECK_EQ(cnt.result.count, cpu.result.count, "bytes: count-only");
+        }
+      }
+      // declaring a byte-string column natural is the reference's ConfigError
+      auto inst = base;
+      as_bytes(inst.r.left);
+      as_bytes(inst.s.left);
+      // (raised inside map_tables: the classical branch, forced or chosen by
+      // the f1 gate, never gets there -- in the reference and here alike)
+      for (dim3::Strategy f : {dim3::Strategy::hybrid, dim3::Strategy::auto_select,
+                               dim3::Strategy::classical}) {
+        dim3::EngineConfig decl = forced(f, false);
+        decl.natural_keys_declared.x = true;
+        bool cpu_threw = false, gpu_threw = false;
+        try { dim3::join_project(inst.r, inst.s, decl, c); } catch (const dim3::ConfigError&) { cpu_threw = true; }
+        try { dim3::gpu::join_project(inst.r, inst.s, decl, c); } catch (const dim3::ConfigError&) { gpu_threw = true; }
+        CHECK_EQ(gpu_threw, cpu_threw, "bytes: declared natural x raises as the reference does");
+        if (f == dim3::Strategy::hybrid) CHECK_EQ(cpu_threw, true, "bytes: declared natural x -> ConfigError");
+        if (f == dim3::Strategy::classical) CHECK_EQ(cpu_threw, false, "classical ignores the skip flags");
+      }
+    }
+  }
+
   // errors map back to the reference's exception types
   bool threw = false;
   try {
@@ -106,7 +189,8 @@ int main() {
     std::fprintf(stderr, "shim FAILED: %d mismatches\n", g_fail);
     return 1;
   }
-  std::printf("shim ok: %d instances x %zu strategies, GPU == reference == oracle\n", instances,
-              sizeof(forces) / sizeof(forces[0]));
+  std::printf("shim ok: %d instances x %zu strategies, GPU == reference == oracle; %d byte-string "
+              "column runs, GPU == reference\n", instances, sizeof(forces) / sizeof(forces[0]),
+              bytes_runs);
   return 0;
 }

@@ -2098,6 +2098,15 @@ struct Mapped {
   const uint32_t *r_x = nullptr, *r_y = nullptr, *s_z = nullptr, *s_y = nullptr;
   uint64_t kept = 0, x_card = 0, y_card = 0, z_card = 0;
   uint64_t x_card_job = 0;  // the job's x card (sharded: summed local dictionaries)
+  // a declared natural-key skip the data does not allow (require_natural's
+  // ConfigError, mapping.cpp:328-338). The reference raises it inside
+  // map_tables, which its classical branch never calls (engine.cpp:386-395):
+  // the columns are dictionary-coded here and the caller raises the error
+  // unless the classical join runs (check_natural).
+  std::string natural_error;
+  void check_natural() const {
+    if (!natural_error.empty()) throw d3g::ConfigError(natural_error);
+  }
   void release_codes() {
     r_x_own.reset();
     r_y_own.reset();
@@ -2151,10 +2160,24 @@ void map_inputs(Ctx& X, const uint64_t* Rl, const uint64_t* Rr, uint64_t NR, con
   auto det = [&](int i) { return lens_job[i] > 0 && hs[i].sample_fail == 0; };
   auto fits = [&](int i) { return lens_job[i] == 0 || hs[i].max < (1ull << 32); };
   bool sx = o->declared_x != 0, sy = o->declared_y != 0, sz = o->declared_z != 0;
-  if (o->natural_keys_auto) {
-    sx = sx || det(0);
-    sy = sy || (det(1) && det(3));
-    sz = sz || det(2);
+  // columns holding surrogate ids of byte strings (ColumnType::bytes on the
+  // caller's side): never natural keys -- detect_natural_keys is false for
+  // them (mapping.cpp:284) and a declared skip is require_natural's error
+  // (mapping.cpp:328-331)
+  const bool bx = (o->natural_keys_auto & D3G_KEYS_BYTES_X) != 0,
+             by = (o->natural_keys_auto & D3G_KEYS_BYTES_Y) != 0,
+             bz = (o->natural_keys_auto & D3G_KEYS_BYTES_Z) != 0;
+  if ((bx && sx) || (by && sy) || (bz && sz)) {
+    M.natural_error = std::string("natural-key skip on column ") +
+                      (by && sy ? "y" : bz && sz ? "z" : "x") + " requires integer values";
+    sx = sx && !bx;
+    sy = sy && !by;
+    sz = sz && !bz;
+  }
+  if (o->natural_keys_auto & D3G_KEYS_AUTO) {
+    sx = sx || (!bx && det(0));
+    sy = sy || (!by && det(1) && det(3));
+    sz = sz || (!bz && det(2));
   }
   auto feasible = [&](bool ax, bool ay, bool az) {
     if (ay && (!fits(1) || !fits(3))) return false;
@@ -2163,9 +2186,15 @@ void map_inputs(Ctx& X, const uint64_t* Rl, const uint64_t* Rr, uint64_t NR, con
     return true;
   };
   if (!feasible(sx, sy, sz)) {
-    bool dx = o->declared_x != 0, dy = o->declared_y != 0, dz = o->declared_z != 0;
-    if ((sx == dx && sy == dy && sz == dz) || !feasible(dx, dy, dz))
-      throw ConfigError("natural-key skip requires integer values below 2^32");
+    bool dx = o->declared_x != 0 && !bx, dy = o->declared_y != 0 && !by,
+         dz = o->declared_z != 0 && !bz;
+    if ((sx == dx && sy == dy && sz == dz) || !feasible(dx, dy, dz)) {
+      if (M.natural_error.empty())
+        M.natural_error = "natural-key skip requires integer values below 2^32";
+      dx = dx && fits(0);
+      dy = dy && fits(1) && fits(3);
+      dz = dz && fits(2);
+    }
     sx = dx;
     sy = dy;
     sz = dz;
@@ -2710,6 +2739,7 @@ void join_project_impl(Ctx& X, const d3g_table* r, const d3g_table* s, const d3g
     bag_job = acc > (unsigned __int128)~0ull ? ~0ull : (uint64_t)acc;
   }
   if (!global_classical) decide_f1();  // delivered by map_inputs' first round trip
+  if (!classical) M.check_natural();
   const bool self_join = try_selfjoin && ident.value(X);
   const uint64_t kept = M.kept, x_card = M.x_card, y_card = M.y_card, z_card = M.z_card;
   const uint64_t x_card_job = M.x_card_job;
@@ -3176,6 +3206,7 @@ void join_aggregate_impl(Ctx& X, const d3g_valued_table* r, const d3g_valued_tab
   // map_with_fallback; the R values follow the surviving rows (m.r_kept)
   Mapped M;
   map_inputs(X, Rl, Rr, NR, Sl, Sr, NS, o, rep, /*want_kept=*/true, M);
+  M.check_natural();
   const uint64_t kept = M.kept, x_card = M.x_card, y_card = M.y_card, z_card = M.z_card;
   T.mark();  // 2
 
@@ -3771,6 +3802,7 @@ int d3g_map_tables(d3g_ctx* ctx, const d3g_table* r, const d3g_table* s, const d
     d3g_report rep{};
     Mapped M;
     map_inputs(X, Rl, Rr, NR, Sl, Sr, NS, o, &rep, /*want_kept=*/true, M);
+    M.check_natural();
     out->kept = M.kept;
     out->dropped_r = NR - M.kept;
     out->x_card = M.x_card;

@@ -144,18 +144,26 @@ class EngineConfig:
 
 
 class RawTable:
-    """Two u64 columns; row i = (left[i], right[i]) (relation.hpp:43-46).
+    """Two columns; row i = (left[i], right[i]) (relation.hpp:43-46).
 
-    Columns are numpy uint64 arrays (host) or CUDA torch tensors of int64 /
-    uint64 (device-resident input, no H2D copy)."""
+    Integer columns (ColumnType::u64) are numpy uint64 / uint32 arrays (host)
+    or CUDA torch tensors of int64 / uint64 (device-resident input, no H2D
+    copy). A column of byte strings (ColumnType::bytes, relation.hpp:21: a
+    numpy array or list of ``bytes`` / ``str``) is taken by ``join_project``,
+    which interns it into surrogate ids on the host."""
 
     def __init__(self, left=None, right=None):
         self.left = _as_col(left if left is not None else [])
         self.right = _as_col(right if right is not None else [])
         if _length(self.left) != _length(self.right):
             raise FormatError("left and right columns differ in length")
-        if _itemsize(self.left) != _itemsize(self.right):
+        if not (_is_bytes_col(self.left) or _is_bytes_col(self.right)) and \
+                _itemsize(self.left) != _itemsize(self.right):
             raise FormatError("left and right columns differ in width")
+
+    @property
+    def has_bytes(self) -> bool:
+        return _is_bytes_col(self.left) or _is_bytes_col(self.right)
 
     def size(self) -> int:
         return _length(self.left)
@@ -179,15 +187,25 @@ def _length(a) -> int:
     return int(a.shape[0]) if hasattr(a, "shape") else len(a)
 
 
+def _is_bytes_col(a) -> bool:
+    """A ColumnType::bytes column: a numpy array of bytes / str values."""
+    return isinstance(a, np.ndarray) and a.dtype.kind in "SUO"
+
+
 def _as_col(a):
     """A column as the library takes it: 64-bit (u64 values), or 32-bit for
     uint32 numpy arrays / int32 tensors (d3g_table.value_bytes = 4: half the
-    host->device bytes, widened on the GPU)."""
+    host->device bytes, widened on the GPU). Byte-string columns are kept as
+    numpy arrays of their values."""
     if _is_cuda(a):
         if a.element_size() not in (4, 8) or not a.is_contiguous():
             raise FormatError("device columns must be contiguous 32- or 64-bit tensors")
         return a
     arr = np.asarray(a)
+    if arr.dtype.kind in "SUO" and arr.size:
+        if not all(isinstance(v, (bytes, str)) for v in arr.tolist()):
+            raise FormatError("a byte-string column holds bytes or str values only")
+        return arr
     if arr.dtype == np.uint32:
         return np.ascontiguousarray(arr)
     if arr.dtype != np.uint64:
@@ -556,6 +574,8 @@ class JoinProjectOutput:
 
 
 def _table_struct(t: RawTable) -> _Table:
+    if t.has_bytes:
+        raise ConfigError("byte-string columns are taken by join_project only")
     vb = _itemsize(t.left)
     if t.on_device:
         return _Table(C.cast(C.c_void_p(t.left.data_ptr()), U64P),
@@ -586,8 +606,13 @@ def join_project(r: RawTable, s: RawTable, cfg: EngineConfig, c: CostConstants,
     if cfg.threads < 1:
         raise ConfigError("threads must be >= 1")
     ctx = ctx or default_context()
+    dec_x = dec_z = None
+    key_flags = 0
+    if r.has_bytes or s.has_bytes:
+        r, s, dec_x, dec_z, key_flags = _intern_bytes(r, s)
     rt, st = _table_struct(r), _table_struct(s)
     cs, op = _consts(c), _opts(cfg)
+    op.natural_keys_auto |= key_flags
     rep = _Report()
     pairs_p = None
     ox = oz = None
@@ -609,8 +634,62 @@ def join_project(r: RawTable, s: RawTable, cfg: EngineConfig, c: CostConstants,
         res = ResultSet(count=report.out_p, materialized=False)
     else:
         n = int(pairs.n)
-        res = ResultSet(count=n, materialized=True, raw_x=ox[:n], raw_z=oz[:n])
+        rx, rz = ox[:n], oz[:n]
+        if dec_x is not None:  # surrogate ids back to the byte strings
+            rx = dec_x[rx.astype(np.int64)]
+        if dec_z is not None:
+            rz = dec_z[rz.astype(np.int64)]
+        res = ResultSet(count=n, materialized=True, raw_x=rx, raw_z=rz)
     return JoinProjectOutput(res, report)
+
+
+KEYS_AUTO, KEYS_BYTES_X, KEYS_BYTES_Y, KEYS_BYTES_Z = 1, 2, 4, 8  # d3g_opts.natural_keys_auto bits
+
+
+def _intern_bytes(r: RawTable, s: RawTable):
+    """Byte-string columns (ColumnType::bytes) as surrogate u64 ids: equal
+    strings <-> equal ids. The device dictionary-codes the ids like the
+    reference does the strings (they are flagged D3G_KEYS_BYTES_*, in engine
+    orientation: the larger table's left column is x), and the result ids are
+    mapped back through the returned decode arrays. The two y columns share
+    one id space; when their types differ no R row finds its y
+    (Dictionary::lookup, mapping.cpp:177-189): disjoint id ranges."""
+    if r.on_device or s.on_device:
+        raise ConfigError("byte-string columns are host columns")
+
+    def ids_of(col):
+        vals, inv = np.unique(col, return_inverse=True)
+        return vals, inv.astype(np.uint64)
+
+    def widen(col):
+        return col.astype(np.uint64) if col.dtype != np.uint64 else col
+
+    bx, bz = _is_bytes_col(r.left), _is_bytes_col(s.left)
+    by_r, by_s = _is_bytes_col(r.right), _is_bytes_col(s.right)
+    dec_x = dec_z = None
+    rl, sl, rr, sr = r.left, s.left, r.right, s.right
+    if bx:
+        dec_x, rl = ids_of(rl)
+    if bz:
+        dec_z, sl = ids_of(sl)
+    if by_r and by_s:
+        both = np.concatenate([np.asarray(rr, dtype=object), np.asarray(sr, dtype=object)])
+        if both.size and not all(type(v) is type(both[0]) for v in both.tolist()):
+            raise FormatError("the y columns mix bytes and str values")
+        _, inv = np.unique(both, return_inverse=True)
+        rr, sr = inv[:len(rr)].astype(np.uint64), inv[len(rr):].astype(np.uint64)
+    elif by_r or by_s:
+        # different types never compare equal (ColumnData::value_equals)
+        ur, rr = np.unique(rr, return_inverse=True)
+        _, sr = np.unique(sr, return_inverse=True)
+        rr, sr = rr.astype(np.uint64), sr.astype(np.uint64) + np.uint64(len(ur))
+    swapped = s.size() > r.size()
+    flags = ((KEYS_BYTES_X if (bz if swapped else bx) else 0) |
+             (KEYS_BYTES_Y if (by_r or by_s) else 0) |
+             (KEYS_BYTES_Z if (bx if swapped else bz) else 0))
+    r2 = RawTable(widen(np.ascontiguousarray(rl)), widen(np.ascontiguousarray(rr)))
+    s2 = RawTable(widen(np.ascontiguousarray(sl)), widen(np.ascontiguousarray(sr)))
+    return r2, s2, dec_x, dec_z, flags
 
 
 def _to_report(rep: _Report) -> ExecutionReport:

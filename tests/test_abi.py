@@ -130,3 +130,35 @@ def test_raw_table_column_widths():
         d3.RawTable(np.array([1, 2], np.uint32), np.array([3, 4], np.uint64))
     with pytest.raises(d3.FormatError):
         d3.RawTable(np.array([-1, 2], np.int64), np.array([3, 4], np.int64))
+
+
+def test_byte_string_columns_are_interned():
+    """ColumnType::bytes columns (relation.hpp:21) become surrogate ids with
+    equal strings <-> equal ids; the y columns share one id space (disjoint
+    ranges when their types differ) and the D3G_KEYS_BYTES_* flags follow the
+    engine's orientation (the larger table's left column is x)."""
+    from paper_2206_04995_b200 import engine as E
+    r = d3.RawTable(np.array([b"a", b"b", b"a"], dtype=object), np.array([b"p", b"q", b"p"], dtype=object))
+    s = d3.RawTable(np.array([5, 6], np.uint64), np.array([b"q", b"r"], dtype=object))
+    assert r.has_bytes and s.has_bytes
+    r2, s2, dec_x, dec_z, flags = E._intern_bytes(r, s)
+    assert dec_z is None and dec_x[r2.left.astype(np.int64)].tolist() == [b"a", b"b", b"a"]
+    assert r2.right[0] == r2.right[2] != r2.right[1] and r2.right[1] == s2.right[0]
+    assert len({int(s2.right[1]), *r2.right.tolist()}) == 3
+    assert s2.left.tolist() == [5, 6] and s2.left.dtype == np.uint64
+    assert flags == E.KEYS_BYTES_X | E.KEYS_BYTES_Y
+    # the larger table is the engine's R whichever argument it is: its left
+    # column stays the engine's x
+    _, _, _, _, flags = E._intern_bytes(s, r)
+    assert flags == E.KEYS_BYTES_X | E.KEYS_BYTES_Y
+    big = d3.RawTable(np.arange(4, dtype=np.uint64), np.array([b"p"] * 4, dtype=object))
+    assert E._intern_bytes(r, big)[4] == E.KEYS_BYTES_Z | E.KEYS_BYTES_Y  # r is the engine's S
+    assert E._intern_bytes(big, r)[4] == E.KEYS_BYTES_Z | E.KEYS_BYTES_Y
+    # y columns of different types: disjoint ids
+    s3 = d3.RawTable(np.array([5, 6], np.uint64), np.array([0, 1], np.uint64))
+    r3, s4, _, _, flags = E._intern_bytes(r, s3)
+    assert not set(r3.right.tolist()) & set(s4.right.tolist()) and flags & E.KEYS_BYTES_Y
+    with pytest.raises(d3.FormatError):
+        d3.RawTable(np.array([b"a", 3], dtype=object), np.array([1, 2], np.uint64))
+    with pytest.raises(d3.ConfigError):
+        E._table_struct(r)

@@ -450,6 +450,56 @@ def test_cfg5_cold_star_segment_matches_reference(env, monkeypatch):
     torch.cuda.empty_cache()
 
 
+def test_byte_string_columns_match_integer_run():
+    """ColumnType::bytes columns (relation.hpp:21, hash_bytes keys in the
+    reference's dictionaries): each column role as byte strings, all of them,
+    and y columns of different types. The pairs decode to the strings of the
+    integer run's pairs, and counts, cards, split and dropped rows equal the
+    integer run with dictionary coding (what the reference does for bytes)."""
+    rng = SplitMix64(77)
+    enc = lambda col: np.array([b"k%d" % (int(v) * 7919 % 100003) for v in col], dtype=object)
+    for _ in range(6):
+        r, s = random_instance(rng)
+        want = oracle_pairs(r, s)
+        base = _run(r, s, d3.Strategy.hybrid, natural_keys_auto=False).report
+        for variant in range(4):
+            bx, by, bz = variant in (0, 3), variant in (1, 3), variant in (2, 3)
+            rt = d3.RawTable(enc(r[0]) if bx else r[0], enc(r[1]) if by else r[1])
+            st = d3.RawTable(enc(s[0]) if bz else s[0], enc(s[1]) if by else s[1])
+            for f in (d3.Strategy.hybrid, d3.Strategy.auto_select, d3.Strategy.classical):
+                out = d3.join_project(rt, st, d3.EngineConfig(force=f), C)
+                got = set(zip(out.result.raw_x.tolist(), out.result.raw_z.tolist()))
+                ex = {(enc([x])[0] if bx else x, enc([z])[0] if bz else z) for x, z in want}
+                assert got == ex and out.report.out_p == len(want)
+                cnt = d3.join_project(rt, st, d3.EngineConfig(force=f, count_only=True), C)
+                assert cnt.report.out_p == len(want)
+            rep = d3.join_project(rt, st, d3.EngineConfig(force=d3.Strategy.hybrid), C).report
+            # (flags in engine orientation: the larger table's left column is x)
+            sw = rep.swapped
+            assert not (rep.natural_x and (bz if sw else bx))
+            assert not (rep.natural_z and (bx if sw else bz)) and not (rep.natural_y and by)
+            if variant == 3:
+                assert (rep.x_card, rep.y_card, rep.z_card, rep.dense_z, rep.sparse_z,
+                        rep.dropped_r, rep.pairs_dense, rep.pairs_sparse) == \
+                    (base.x_card, base.y_card, base.z_card, base.dense_z, base.sparse_z,
+                     base.dropped_r, base.pairs_dense, base.pairs_sparse)
+        # y columns of different types: no R row finds its y
+        rt = d3.RawTable(r[0], enc(r[1]))
+        out = d3.join_project(rt, d3.RawTable(*s), d3.EngineConfig(force=d3.Strategy.hybrid), C)
+        assert out.report.out_p == 0 and len(out.result.raw_x) == 0
+        assert out.report.dropped_r == max(len(r[0]), len(s[0]))
+        # declaring a byte-string column natural: the reference's ConfigError
+        # (raised by map_tables, which the classical branch never calls)
+        flags = d3.SkipFlags(y=True)
+        rb, sb = d3.RawTable(r[0], enc(r[1])), d3.RawTable(s[0], enc(s[1]))
+        with pytest.raises(d3.ConfigError):
+            d3.join_project(rb, sb, d3.EngineConfig(force=d3.Strategy.hybrid,
+                                                    natural_keys_declared=flags), C)
+        out = d3.join_project(rb, sb, d3.EngineConfig(force=d3.Strategy.classical,
+                                                      natural_keys_declared=flags), C)
+        assert out.report.out_p == len(want)
+
+
 @pytest.mark.parametrize("seed", [11, 12])
 def test_hash_cold_pass_long_rows_match_bitmap_path(seed, monkeypatch):
     """The hash cold pass forced (D3G_COLD_PATH=hash) on skewed instances whose
