@@ -7,10 +7,13 @@
 //   K1 csr_bucket_hist    one read of the major codes: bucket histogram
 //                         (shared-memory privatised), and the largest bucket
 //   K2 scan               bucket starts
-//   K3 csr_bucket_scatter one read of (major, minor), one 4-byte write of the
-//                         packed key (row_low << mb | minor) into its bucket;
-//                         the ~30K bucket write frontiers stay resident in L2,
-//                         so sectors leave for DRAM full
+//   K3 two-level scatter  region_bucket_scatter (8-bit bucketing on the high
+//                         bucket bits, runs reserved by one atomic per
+//                         (tile, region)) then csr_region_scatter (one atomic
+//                         per (tile, bucket)): the packed key
+//                         (row_low << mb | minor) lands in its bucket.
+//                         (csr_bucket_scatter, one returning atomic per pair,
+//                         is kept as D3G_CSR_SCATTER=atomic for comparison)
 //   K4 csr_bucket_build   one CTA per bucket, all in shared memory: counting
 //                         sort by row_low, per-row warp bitonic sort + unique
 //                         of the minors, row degrees, bucket-local compaction
@@ -204,11 +207,92 @@ csr_region_scatter_kernel(const uint32_t* __restrict__ maj, const uint32_t* __re
   }
 }
 
-__global__ void gather_region_starts_kernel(const uint64_t* __restrict__ offs, uint32_t n_tiles,
-                                            uint64_t* __restrict__ out /* [257] */) {
+// The 8-bit bucketing pass with its runs reserved by atomics: the region
+// starts are already known (sums of the fine bucket histogram K1 took), so a
+// tile ranks itself in shared memory and reserves each digit's run with ONE
+// 64-bit atomic on that region's cursor -- no per-tile histogram pass over the
+// keys and no scan of 256 x n_tiles counts before the scatter (prims.cuh
+// bucket_pass_u32 needs both because it knows no totals). Order inside a
+// region is arbitrary: the region scatter and the bucket sort re-rank.
+__global__ void __launch_bounds__(kBucketThreads)
+region_bucket_scatter_kernel(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+                             uint64_t n, int shift,
+                             unsigned long long* __restrict__ region_cursor /* [256] */,
+                             uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out) {
+  __shared__ uint32_t s_cnt[256], s_loc[256];
+  __shared__ unsigned long long s_glb[256];
+  __shared__ uint32_t s_key[kBucketTile], s_val[kBucketTile];
+  const uint32_t t = threadIdx.x;
+  if (t < 256) s_cnt[t] = 0;
+  __syncthreads();
+  const uint64_t base = (uint64_t)blockIdx.x * kBucketTile;
+  uint32_t k[kBucketPer], v[kBucketPer], r[kBucketPer];
+#pragma unroll
+  for (int q = 0; q < kBucketPer; ++q) {
+    const uint64_t i = base + (uint64_t)q * kBucketThreads + t;
+    if (i < n) {
+      k[q] = keys[i];
+      v[q] = vals[i];
+      r[q] = atomicAdd(&s_cnt[(k[q] >> shift) & 255], 1u);
+    }
+  }
+  __syncthreads();
+  if (t < 32) {  // exclusive scan of the 256 tile counts, 8 per lane
+    uint32_t c[8], s = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      c[j] = s_cnt[t * 8 + j];
+      s += c[j];
+    }
+    uint32_t incl = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (t >= (uint32_t)o) incl += u;
+    }
+    uint32_t run = incl - s;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      s_loc[t * 8 + j] = run;
+      run += c[j];
+    }
+  }
+  if (t >= 32 && t < 288) {  // one reservation per (tile, digit)
+    const uint32_t d = t - 32;
+    if (s_cnt[d]) s_glb[d] = atomicAdd(&region_cursor[d], (unsigned long long)s_cnt[d]);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < kBucketPer; ++q) {
+    const uint64_t i = base + (uint64_t)q * kBucketThreads + t;
+    if (i < n) {
+      const uint32_t p = s_loc[(k[q] >> shift) & 255] + r[q];
+      s_key[p] = k[q];
+      s_val[p] = v[q];
+    }
+  }
+  __syncthreads();
+  const uint32_t in_tile = (uint32_t)((n - base) < (uint64_t)kBucketTile ? (n - base) : kBucketTile);
+  for (uint32_t p = t; p < in_tile; p += kBucketThreads) {
+    const uint32_t key = s_key[p], d = (key >> shift) & 255;
+    const unsigned long long g = s_glb[d] + (p - s_loc[d]);
+    keys_out[g] = key;
+    vals_out[g] = s_val[p];
+  }
+}
+
+// Region starts from the fine bucket starts: region d holds the buckets
+// [d << sub_bits, (d + 1) << sub_bits); out[d] for the host's tile list,
+// cursor[d] for the scatter's reservations.
+__global__ void region_starts_kernel(const unsigned long long* __restrict__ bstart, uint32_t nb,
+                                     int sub_bits, uint64_t* __restrict__ out /* [257] */,
+                                     unsigned long long* __restrict__ cursor /* [256] */) {
   const uint32_t d = threadIdx.x;
-  if (d < 256) out[d] = offs[(uint64_t)d * n_tiles];
-  if (d == 256) out[256] = offs[(uint64_t)256 * n_tiles];
+  if (d > 256) return;
+  const uint64_t b = (uint64_t)d << sub_bits;
+  const unsigned long long s = bstart[b < nb ? b : nb];
+  out[d] = s;
+  if (d < 256) cursor[d] = s;
 }
 
 // In-place exclusive scan of a[0..n) in shared memory by the whole CTA
@@ -495,15 +579,11 @@ inline bool build_csr_bucketed(Ctx& ctx, const uint32_t* maj, const uint32_t* mn
     DBuf<uint32_t> am = ctx.alloc<uint32_t>(n), av = ctx.alloc<uint32_t>(n);
     const uint32_t n_tiles = (uint32_t)((n + kBucketTile - 1) / kBucketTile);
     {
-      DBuf<uint32_t> hist = ctx.alloc<uint32_t>((uint64_t)256 * n_tiles);
-      DBuf<uint64_t> offs = ctx.alloc<uint64_t>((uint64_t)256 * n_tiles + 1);
-      D3G_LAUNCH(ctx, bucket_hist_kernel, n_tiles, kBucketThreads, 0, maj, n, r + sub_bits,
-                 n_tiles, hist.p);
-      exclusive_scan<uint32_t>(ctx, hist.p, (uint64_t)256 * n_tiles, offs.p);
-      D3G_LAUNCH(ctx, bucket_scatter_kernel, n_tiles, kBucketThreads, 0, maj, mnr, n,
-                 r + sub_bits, n_tiles, offs.p, am.p, av.p);
       DBuf<uint64_t> rs = ctx.alloc<uint64_t>(257);
-      D3G_LAUNCH(ctx, gather_region_starts_kernel, 1, 288, 0, offs.p, n_tiles, rs.p);
+      DBuf<unsigned long long> rcur = ctx.alloc<unsigned long long>(256);
+      D3G_LAUNCH(ctx, region_starts_kernel, 1, 288, 0, bstart.p, nb, sub_bits, rs.p, rcur.p);
+      D3G_LAUNCH(ctx, region_bucket_scatter_kernel, n_tiles, kBucketThreads, 0, maj, mnr, n,
+                 r + sub_bits, rcur.p, am.p, av.p);
       uint64_t h[257];
       ctx.to_host(h, rs.p, 257);
       std::vector<RbTile> tv;
