@@ -1148,6 +1148,42 @@ __global__ void trie_lds_kernel(const uint32_t* __restrict__ rcnt, uint64_t n, u
     atomicAdd(out_unshared, (unsigned long long)(acc_u * mult));
 }
 
+// The same accounting over several row runs in ONE launch (the pivot plan's
+// class runs: up to 64, each with its own chunking and batch multiplicity;
+// one launch per run cost more in launch gaps than in work).
+struct TrieRuns {
+  uint32_t n_runs;
+  uint32_t zc[64];     // z chunks of run q
+  uint64_t row0[64];   // its first row
+  uint64_t start[65];  // exclusive prefix of the runs' row counts
+  uint64_t mult[64];   // batches that test it
+};
+__global__ void trie_lds_runs_kernel(const uint32_t* __restrict__ rcnt, TrieRuns runs,
+                                     uint32_t sub_read, unsigned long long* __restrict__ out_shared,
+                                     unsigned long long* __restrict__ out_unshared) {
+  uint64_t acc = 0, acc_u = 0;
+  const uint64_t total = runs.start[runs.n_runs];
+  for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
+       g += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t q = 0;
+    while (q + 1 < runs.n_runs && runs.start[q + 1] <= g) ++q;
+    const uint64_t n = runs.start[q + 1] - runs.start[q], i = g - runs.start[q];
+    const uint64_t z_chunks = runs.zc[q];
+    uint64_t zc = i * z_chunks / n;
+    while (zc + 1 < z_chunks && n * (zc + 1) / z_chunks <= i) ++zc;
+    while (zc > 0 && n * zc / z_chunks > i) --zc;
+    const uint64_t z_lo = n * zc / z_chunks;
+    const uint32_t cw = rcnt[runs.row0[q] + i], c = cw & kTrieCntMask;
+    const uint32_t L = ((i - z_lo) % 32 == 0) ? 0u : (cw >> 22) & 3u;
+    acc += ((L == 0 ? sub_read : 0u) + c - (L > 1 ? L - 1 : 0u)) * runs.mult[q];
+    acc_u += (uint64_t)(sub_read + c) * runs.mult[q];
+  }
+  acc = warp_sum(acc);
+  acc_u = warp_sum(acc_u);
+  if (lane_id() == 0 && acc) atomicAdd(out_shared, (unsigned long long)acc);
+  if (lane_id() == 0 && acc_u && out_unshared) atomicAdd(out_unshared, (unsigned long long)acc_u);
+}
+
 template <int kMode, bool kTrie, bool kTab = true>
 __global__ void __launch_bounds__(kHotThreads, 1)
 dense_hot_jt_kernel(HotParams p, const uint64_t* __restrict__ dl_ptr,

@@ -1244,12 +1244,19 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
         // slice reads of every (batch, row) the kernel tests, with and without
         // the prefix sharing
         if (plan) {
-          for (uint32_t q = 0; q < n_kinds; ++q) {  // each class run, times its batches
+          TrieRuns tr{};  // each class run, times its batches: one launch
+          for (uint32_t q = 0; q < n_kinds; ++q) {
             const uint64_t rows = run_lo[q + 1] - run_lo[q];
             if (!run_mult[q] || !rows) continue;
-            D3G_LAUNCH(X, trie_lds_kernel, grid_for(rows, 256), 256, 0, rcnt.p, rows, run_zc[q],
-                       tab ? 1u : 0u, lds_units, &tallies.p[4].count, run_mult[q], run_lo[q]);
+            const uint32_t k = tr.n_runs++;
+            tr.zc[k] = run_zc[q];
+            tr.row0[k] = run_lo[q];
+            tr.mult[k] = run_mult[q];
+            tr.start[k + 1] = tr.start[k] + rows;
           }
+          if (tr.n_runs)
+            D3G_LAUNCH(X, trie_lds_runs_kernel, grid_for(tr.start[tr.n_runs], 256), 256, 0, rcnt.p,
+                       tr, tab ? 1u : 0u, lds_units, &tallies.p[4].count);
         } else {
           D3G_LAUNCH(X, trie_lds_kernel, grid_for(D, 256), 256, 0, rcnt.p, D, hp.z_chunks,
                      tab ? 1u : 0u, lds_units, &tallies.p[4].count, (uint64_t)n_batches, 0ull);
