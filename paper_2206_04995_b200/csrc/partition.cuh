@@ -52,10 +52,17 @@ __global__ void degree_scatter_kernel(const uint64_t* __restrict__ row_ptr, uint
                                       unsigned int* __restrict__ cur, uint32_t* __restrict__ out,
                                       uint64_t* __restrict__ out_ptr, uint64_t n_out,
                                       uint64_t total_ent, uint8_t* __restrict__ sp_flag) {
+  // Positions inside a degree class come from a cursor per degree. A few
+  // dozen degrees take every row, so the cursors are reserved per CTA tile
+  // (shared-memory counts, then ONE global atomic per (tile, degree)) for
+  // degrees below kSmallDeg; rarer large degrees go warp-aggregated to the
+  // global cursor. blockDim.x == 256.
+  constexpr uint32_t kSmallDeg = 256;
+  __shared__ uint32_t s_cnt[kSmallDeg], s_base[kSmallDeg];
   const uint32_t lane = lane_id();
-  const uint64_t n = r1 - r0, n_pad = (n + 31) / 32 * 32;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pad;
-       i += (uint64_t)gridDim.x * blockDim.x) {
+  const uint64_t n = r1 - r0, n_tiles = (n + blockDim.x - 1) / blockDim.x;
+  for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const uint64_t i = tile * blockDim.x + threadIdx.x;
     const uint64_t r = r0 + i;
     uint64_t d = 0;
     bool take = false, sparse = false;
@@ -66,19 +73,31 @@ __global__ void degree_scatter_kernel(const uint64_t* __restrict__ row_ptr, uint
         take = mode == 0 || (mode == 1 ? !sparse : sparse);
       }
     }
-    const uint32_t key = take ? (uint32_t)d : 0xffffffffu;
+    if (threadIdx.x < kSmallDeg) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const bool small = take && d < kSmallDeg;
+    uint32_t rank = 0, base = 0;
+    if (small) rank = atomicAdd(&s_cnt[d], 1u);
+    const uint32_t key = (take && !small) ? (uint32_t)d : 0xffffffffu;
     const uint32_t peers = __match_any_sync(0xffffffffu, key);
-    if (take) {
+    if (take && !small) {
       const int leader = __ffs(peers) - 1;
-      const uint32_t rank = __popc(peers & ((1u << lane) - 1));
-      uint32_t base = 0;
+      rank = __popc(peers & ((1u << lane) - 1));
       if ((int)lane == leader) base = atomicAdd(&cur[d], (unsigned)__popc(peers));
       base = __shfl_sync(peers, base, leader);
+    }
+    __syncthreads();
+    if (threadIdx.x < kSmallDeg && s_cnt[threadIdx.x])
+      s_base[threadIdx.x] = atomicAdd(&cur[threadIdx.x], s_cnt[threadIdx.x]);
+    __syncthreads();
+    if (take) {
+      if (small) base = s_base[d];
       const uint64_t pos = off[d] + base + rank;
       out[pos] = (uint32_t)r;
       if (out_ptr) out_ptr[pos] = ent[d] + (uint64_t)(base + rank) * d;
       if (sp_flag) sp_flag[pos] = sparse ? 1 : 0;
     }
+    __syncthreads();  // s_cnt / s_base are rewritten by the next tile
   }
   if (out_ptr && blockIdx.x == 0 && threadIdx.x == 0) out_ptr[n_out] = total_ent;
 }
