@@ -262,9 +262,11 @@ def cpu_reference_sample(cfg: int, frac: float, threads: int, tables=None, cfg5_
         # part (the swapped DenseEC walks all 1e7 S-side rows), so extrapolate
         # the MARGINAL per-x cost, the estimate most favourable to the reference.
         import numpy as np
+        # (the larger slice is run twice and its faster kernel time kept: on a
+        # shared host one disturbed run moves the marginal cost several-fold)
         x_card, runs = 10_000_000, []
         xa, xb = cfg5_slices
-        for xs in (xa, xb):
+        for xs in (xa, xb, xb):
             keep = np.asarray(r.left) < xs
             rs = O.Table(np.ascontiguousarray(np.asarray(r.left)[keep]),
                          np.ascontiguousarray(np.asarray(r.right)[keep]))
@@ -272,7 +274,7 @@ def cpu_reference_sample(cfg: int, frac: float, threads: int, tables=None, cfg5_
                                    budget_bytes=1 << 40)
             runs.append(((d["ms_estimate"] + d["ms_map"] + d["ms_csr"] + d["ms_partition"]) * 1e-3,
                          (d["ms_sparse"] + d["ms_dense"]) * 1e-3, d["out_p"]))
-        (p1, k1, _), (p2, k2, o2) = runs
+        (p1, k1, _), (p2, k2, o2) = runs[0], min(runs[1:], key=lambda t: t[1])
         marginal = max(k2 - k1, 0.0) / (xb - xa)
         est = p2 + k1 + marginal * (x_card - xa)
         return est, {"slices": "cfg5", "x_slice": f"x<{xa} and x<{xb} (marginal per-x cost)",
@@ -297,7 +299,7 @@ def _sample_text(detail):
                 "the full S (its engine swaps; the 1.25 TB panel of the whole job cannot be "
                 f"built): prep {detail['sec_prep']:.1f}s once + the marginal per-x kernel cost "
                 f"({(detail['sec_kernels'] - detail['sec_kernels_x100']) / (xb - xa) * 1e3:.2f} "
-                "ms/x) x 1e7 x values, extrapolated")
+                f"ms/x, the faster of two runs of the x<{xb} slice) x 1e7 x values, extrapolated")
     if detail.get("strategy") == "classical":
         return ("whole job through the reference's join_project(auto) -> f1 gate -> "
                 "hash_join_dedup")
@@ -326,7 +328,9 @@ def run_reference(args):
     for _ in range(args.steps):
         est, detail = cpu_reference_sample(cfg, args.cpu_frac, threads, (r, s))
         ests.append(est)
-    sec = sum(ests) / len(ests)
+    # the fastest sample: the figure most favourable to the reference (the
+    # host cores are shared; a disturbed sample only ever reads slower)
+    sec = min(ests)
     value = n_tuples / sec
     # the same reference at threads=1 (one bounded sample)
     t1_frac = args.cpu_frac / 4
