@@ -233,7 +233,8 @@ def cpu_model() -> str:
 _X_ROWS: dict = {}
 
 
-def cpu_reference_sample(cfg: int, frac: float, threads: int, tables=None, cfg5_slices=(100, 1000)):
+def cpu_reference_sample(cfg: int, frac: float, threads: int, tables=None, cfg5_slices=(100, 1000),
+                         repeat_hi: bool = False):
     """Reference prep on the whole job + reference kernels on an x-slice,
     extrapolated linearly in x. Returns (seconds_full_job_estimate, detail)."""
     from oracle import oracle as O
@@ -262,11 +263,12 @@ def cpu_reference_sample(cfg: int, frac: float, threads: int, tables=None, cfg5_
         # part (the swapped DenseEC walks all 1e7 S-side rows), so extrapolate
         # the MARGINAL per-x cost, the estimate most favourable to the reference.
         import numpy as np
-        # (the larger slice is run twice and its faster kernel time kept: on a
-        # shared host one disturbed run moves the marginal cost several-fold)
+        # (repeat_hi: the larger slice is run twice and its faster kernel time
+        # kept -- on a shared host one disturbed run moves the marginal cost
+        # several-fold; the reference arm takes the faster of its samples instead)
         x_card, runs = 10_000_000, []
         xa, xb = cfg5_slices
-        for xs in (xa, xb, xb):
+        for xs in (xa, xb, xb) if repeat_hi else (xa, xb):
             keep = np.asarray(r.left) < xs
             rs = O.Table(np.ascontiguousarray(np.asarray(r.left)[keep]),
                          np.ascontiguousarray(np.asarray(r.right)[keep]))
@@ -280,7 +282,7 @@ def cpu_reference_sample(cfg: int, frac: float, threads: int, tables=None, cfg5_
         return est, {"slices": "cfg5", "x_slice": f"x<{xa} and x<{xb} (marginal per-x cost)",
                      "x_rows": x_card, "slice_lo": xa, "slice_hi": xb,
                      "sec_prep": p2, "sec_kernels": k2, "sec_kernels_x100": k1,
-                     "est_full_s": est, "slice_out_p": o2}
+                     "est_full_s": est, "slice_out_p": o2, "repeat_hi": repeat_hi}
     x_rows = _X_ROWS.get(cfg)
     if x_rows is None:
         x_rows = O.ref_timed_sample(r, s, threads, 0, 0)["x_rows"]
@@ -299,7 +301,8 @@ def _sample_text(detail):
                 "the full S (its engine swaps; the 1.25 TB panel of the whole job cannot be "
                 f"built): prep {detail['sec_prep']:.1f}s once + the marginal per-x kernel cost "
                 f"({(detail['sec_kernels'] - detail['sec_kernels_x100']) / (xb - xa) * 1e3:.2f} "
-                f"ms/x, the faster of two runs of the x<{xb} slice) x 1e7 x values, extrapolated")
+                f"ms/x{', the faster of two runs of the larger slice' if detail.get('repeat_hi') else ''}"
+                ") x 1e7 x values, extrapolated")
     if detail.get("strategy") == "classical":
         return ("whole job through the reference's join_project(auto) -> f1 gate -> "
                 "hash_join_dedup")
@@ -649,7 +652,7 @@ def main():
             from oracle import oracle as O
             if O.ref_available():
                 threads = os.cpu_count() or 1
-                est, detail = cpu_reference_sample(cfg_id, args.cpu_frac, threads)
+                est, detail = cpu_reference_sample(cfg_id, args.cpu_frac, threads, repeat_hi=True)
                 cpu = {"value": n_tuples / est, "unit": "tuples/s", "cores": threads,
                        "kind": "reference", "cpu_model": cpu_model(),
                        "extrapolated": detail.get("strategy") != "classical",
