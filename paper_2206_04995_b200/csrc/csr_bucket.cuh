@@ -139,19 +139,39 @@ struct RbTile {
   uint32_t region;           // high bucket bits (bucket >> sub_bits)
 };
 
+// A CTA finds its tile itself: region d (pairs [starts[d], starts[d + 1]) of
+// the region-ordered arrays) is cut into tiles of kRbTile pairs, tile_prefix
+// is the exclusive prefix of the regions' tile counts (region_starts_kernel),
+// and the grid is an upper bound (n / kRbTile + 256): no tile list built on
+// the host, no round trip between the two scatter passes.
 __global__ void __launch_bounds__(kRbThreads)
 csr_region_scatter_kernel(const uint32_t* __restrict__ maj, const uint32_t* __restrict__ mnr,
-                          const RbTile* __restrict__ tiles, int r, int mb, int sub_bits,
-                          unsigned long long* __restrict__ cursor,
+                          const uint64_t* __restrict__ starts /* [257] */,
+                          const uint32_t* __restrict__ tile_prefix /* [257] */, int r, int mb,
+                          int sub_bits, unsigned long long* __restrict__ cursor,
                           uint32_t* __restrict__ packed) {
   __shared__ uint32_t s_cnt[256], s_loc[256];
   __shared__ unsigned long long s_glb[256];
   __shared__ uint32_t s_out[kRbTile];
+  __shared__ uint32_t s_tp[257];
   const uint32_t t = threadIdx.x;
-  const RbTile tl = tiles[blockIdx.x];
-  const uint32_t smask = (1u << sub_bits) - 1, rmask = (1u << r) - 1;
+  if (t < 257) s_tp[t] = tile_prefix[t];
   if (t < 256) s_cnt[t] = 0;
   __syncthreads();
+  if (blockIdx.x >= s_tp[256]) return;  // (CTA-uniform)
+  uint32_t lo = 0, hi = 256;  // the region whose tiles hold blockIdx.x
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (s_tp[mid] <= blockIdx.x) lo = mid; else hi = mid;
+  }
+  RbTile tl;
+  tl.region = lo;
+  tl.start = starts[lo] + (unsigned long long)(blockIdx.x - s_tp[lo]) * kRbTile;
+  {
+    const unsigned long long left = starts[lo + 1] - tl.start;
+    tl.len = left < (unsigned long long)kRbTile ? (uint32_t)left : (uint32_t)kRbTile;
+  }
+  const uint32_t smask = (1u << sub_bits) - 1, rmask = (1u << r) - 1;
   uint32_t key[kRbPer], sub[kRbPer], rk[kRbPer];
 #pragma unroll
   for (int q = 0; q < kRbPer; ++q) {
@@ -286,13 +306,40 @@ region_bucket_scatter_kernel(const uint32_t* __restrict__ keys, const uint32_t* 
 // cursor[d] for the scatter's reservations.
 __global__ void region_starts_kernel(const unsigned long long* __restrict__ bstart, uint32_t nb,
                                      int sub_bits, uint64_t* __restrict__ out /* [257] */,
-                                     unsigned long long* __restrict__ cursor /* [256] */) {
-  const uint32_t d = threadIdx.x;
-  if (d > 256) return;
-  const uint64_t b = (uint64_t)d << sub_bits;
-  const unsigned long long s = bstart[b < nb ? b : nb];
-  out[d] = s;
-  if (d < 256) cursor[d] = s;
+                                     unsigned long long* __restrict__ cursor /* [256] */,
+                                     uint32_t* __restrict__ tile_prefix /* [257] */) {
+  __shared__ unsigned long long s_st[257];
+  const uint32_t d = threadIdx.x;  // 288 threads
+  if (d <= 256) {
+    const uint64_t b = (uint64_t)d << sub_bits;
+    const unsigned long long s = bstart[b < nb ? b : nb];
+    s_st[d] = s;
+    out[d] = s;
+    if (d < 256) cursor[d] = s;
+  }
+  __syncthreads();
+  if (d < 32) {  // exclusive prefix of the regions' tile counts, 8 regions per lane
+    uint32_t c[8], sum = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const unsigned long long len = s_st[d * 8 + j + 1] - s_st[d * 8 + j];
+      c[j] = (uint32_t)((len + kRbTile - 1) / kRbTile);
+      sum += c[j];
+    }
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (d >= (uint32_t)o) incl += u;
+    }
+    uint32_t run = incl - sum;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      tile_prefix[d * 8 + j] = run;
+      run += c[j];
+    }
+    if (d == 31) tile_prefix[256] = run;
+  }
 }
 
 // In-place exclusive scan of a[0..n) in shared memory by the whole CTA
@@ -581,22 +628,14 @@ inline bool build_csr_bucketed(Ctx& ctx, const uint32_t* maj, const uint32_t* mn
     {
       DBuf<uint64_t> rs = ctx.alloc<uint64_t>(257);
       DBuf<unsigned long long> rcur = ctx.alloc<unsigned long long>(256);
-      D3G_LAUNCH(ctx, region_starts_kernel, 1, 288, 0, bstart.p, nb, sub_bits, rs.p, rcur.p);
+      DBuf<uint32_t> tpre = ctx.alloc<uint32_t>(257);
+      D3G_LAUNCH(ctx, region_starts_kernel, 1, 288, 0, bstart.p, nb, sub_bits, rs.p, rcur.p,
+                 tpre.p);
       D3G_LAUNCH(ctx, region_bucket_scatter_kernel, n_tiles, kBucketThreads, 0, maj, mnr, n,
                  r + sub_bits, rcur.p, am.p, av.p);
-      uint64_t h[257];
-      ctx.to_host(h, rs.p, 257);
-      std::vector<RbTile> tv;
-      tv.reserve(n / kRbTile + 257);
-      for (uint32_t d = 0; d < 256; ++d)
-        for (uint64_t p = h[d]; p < h[d + 1]; p += kRbTile)
-          tv.push_back(RbTile{p, (uint32_t)std::min<uint64_t>(kRbTile, h[d + 1] - p), d});
-      DBuf<RbTile> tiles = ctx.alloc<RbTile>(tv.size());
-      ctx.to_device(tiles.p, tv.data(), tv.size());
-      if (!tv.empty())
-        D3G_LAUNCH(ctx, csr_region_scatter_kernel, (unsigned)tv.size(), kRbThreads, 0, am.p,
-                   av.p, tiles.p, r, mb, sub_bits, cursor.p, packed.p);
-      ctx.sync();  // tv (host) is the source of the async tile copy above
+      // (every region's last tile may be partial: at most 256 more tiles than n / kRbTile)
+      D3G_LAUNCH(ctx, csr_region_scatter_kernel, (unsigned)(n / kRbTile + 257), kRbThreads, 0,
+                 am.p, av.p, rs.p, tpre.p, r, mb, sub_bits, cursor.p, packed.p);
     }
   }
   cursor.reset();
