@@ -822,7 +822,10 @@ __device__ __forceinline__ uint64_t cta_cold_x(const ColdX& s, uint64_t r0, uint
                                                const uint4* __restrict__ crec, uint64_t* s_seg0,
                                                uint32_t* s_off, uint32_t* s_wsum, uint32_t* s_tot,
                                                const volatile unsigned int* stop, uint64_t kstar,
-                                               On&& on, Step&& step) {
+                                               On&& on, Step&& step, uint32_t share = 0,
+                                               uint32_t n_shares = 1) {
+  // (share / n_shares: this CTA streams that part of every chunk -- several
+  // CTAs working on one x, dense_cold_shared_kernel)
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   uint64_t mine = 0;
   for (uint64_t yb = r0; yb < r1 && !*stop; yb += kThreads) {
@@ -839,8 +842,11 @@ __device__ __forceinline__ uint64_t cta_cold_x(const ColdX& s, uint64_t r0, uint
     // each warp streams one contiguous share of the chunk: its first segment
     // by one binary search, then the windows advance it from their masks
     constexpr uint32_t kW = kThreads / 32;
-    const uint32_t per = ((total + kW - 1) / kW + 31) & ~31u;
-    const uint32_t beg = min(total, warp * per), end = min(total, beg + per);
+    const uint32_t nw = kW * n_shares;
+    const uint32_t per = ((total + nw - 1) / nw + 31) & ~31u;
+    // (64-bit: (share * kW + warp) * per can pass 2^32 only with total near it)
+    const uint32_t beg = (uint32_t)min((uint64_t)total, (uint64_t)(share * kW + warp) * per);
+    const uint32_t end = min(total, beg + per);
     uint32_t c0 = beg < end ? seg_search(beg, n, s_off) : 0u;
     for (uint32_t tb = beg; tb < end && !*stop; tb += 32 * kColdU) {
       uint64_t t[kColdU];
@@ -1150,6 +1156,95 @@ dense_cold_overflow_kernel(const uint32_t* __restrict__ over_x, const unsigned i
           [&]() { ++dummy; });
     }
     __syncthreads();
+  }
+  flush_sp(cnt_sp, csp);
+  flush_cand(cand, ncand, ngat);
+  tally_flush(tally, cnt, sum, xr);
+}
+
+// ---- overflow tier 2, shared bitmaps: several CTAs per x ------------------------
+//
+// The x that reach the bitmap tier are few and huge (cfg5: 436 x, up to ~1M
+// candidates each): with one CTA per x the tier lasts as long as its longest
+// x. Here every x of a round owns a zeroed global bitmap and kOvShare CTAs
+// stream one share each of its candidates; atomicOr's return value makes the
+// count exact across CTAs. The star segment needs the finished bitmap, so the
+// tier is two launches: phase 0 inserts everything but the star, phase 1
+// tests the star's survivors against the bitmap. Nothing is cleared (the
+// round's bitmaps are zeroed by one memset).
+#ifndef D3G_OV_SHARE
+#define D3G_OV_SHARE 4
+#endif
+constexpr uint32_t kOvShare = D3G_OV_SHARE;
+
+template <int kMode>
+__global__ void __launch_bounds__(kOvThreads, kOvPerSm)
+dense_cold_shared_kernel(const uint32_t* __restrict__ over_x, uint32_t x_lo, uint32_t x_n,
+                         int phase, const uint64_t* __restrict__ r_ptr,
+                         const uint32_t* __restrict__ r_col, const uint64_t* __restrict__ cptr,
+                         const uint4* __restrict__ crec, const uint4* __restrict__ hz4,
+                         const uint4* __restrict__ hx4, uint64_t y_card, uint32_t var_bits,
+                         uint32_t vskip, const uint32_t* __restrict__ dl_z,
+                         uint32_t* __restrict__ gbm, uint64_t words, Decode dec, Emit em,
+                         Tally* tally, unsigned long long* __restrict__ cnt_sp,
+                         unsigned long long* __restrict__ cand = nullptr) {
+  __shared__ uint64_t s_seg0[kOvThreads];
+  __shared__ uint32_t s_off[kOvThreads];
+  __shared__ uint32_t s_wsum[2 * (kOvThreads / 32)];
+  __shared__ uint32_t s_tot[2];
+  __shared__ unsigned int s_never;  // 0: the candidate loop never stops early
+  __shared__ unsigned long long s_best;
+  extern __shared__ __align__(16) uint32_t ovdq[];  // [warps][kDQ]
+  const uint32_t warp = threadIdx.x >> 5;
+  uint32_t* dq = ovdq + warp * kDQ;
+  const uint32_t xi = blockIdx.x / kOvShare, share = blockIdx.x % kOvShare;
+  if (xi >= x_n) return;
+  if (threadIdx.x == 0) {
+    s_never = 0;
+    s_best = 0;
+  }
+  __syncthreads();
+  const uint32_t x = over_x[x_lo + xi];
+  uint32_t* bm = gbm + (uint64_t)xi * words;
+  const ColdX s = cold_x(hx4, x);
+  const uint32_t v = x_variant(s.a0.x, var_bits, vskip);
+  const uint64_t* cp = cptr + (uint64_t)v * y_card;
+  const uint64_t r0 = r_ptr[x], r1 = r_ptr[x + 1];
+  uint64_t star0 = 0;
+  uint32_t star_len = 0;
+  const uint64_t kstar =
+      kStar ? cta_star<kOvThreads>(r0, r1, r_col, cp, &s_best, star0, star_len) : ~0ull;
+  uint64_t cnt = 0, sum = 0, xr = 0, csp = 0, ncand = 0, ngat = 0;
+  uint32_t qn = 0;
+  if (phase == 0) {
+    auto ins = [&](bool ok, uint32_t key) {
+      if (!ok) return;
+      const uint32_t zl = key & kRowMask;
+      const uint32_t bit = 1u << (zl & 31);
+      if (atomicOr(&bm[zl >> 5], bit) & bit) return;
+      ++cnt;
+      if (key & kSpFlag) ++csp;
+      if (kMode != kModeCount) cold_account<kMode>(x, dl_z[zl], dec, em, sum, xr);
+    };
+    ncand += cta_cold_x<kOvThreads>(
+        s, r0, r1, r_col, cp, crec, s_seg0, s_off, s_wsum, s_tot, &s_never, kstar,
+        [&](uint32_t st, uint32_t row) {
+          ins(st == kColdSurvivor, row);
+          dq_push(dq, qn, st == kColdMaybe, row);
+        },
+        [&]() { dq_drain(dq, qn, false, s, hz4, ngat, ins); }, share, kOvShare);
+    dq_drain(dq, qn, true, s, hz4, ngat, ins);
+  } else if (star_len) {
+    auto look = [&](bool ok, uint32_t key) {
+      if (!ok) return;
+      const uint32_t zl = key & kRowMask;
+      if ((__ldcg(&bm[zl >> 5]) >> (zl & 31)) & 1u) return;
+      ++cnt;
+      if (key & kSpFlag) ++csp;
+      if (kMode != kModeCount) cold_account<kMode>(x, dl_z[zl], dec, em, sum, xr);
+    };
+    ncand += cold_star<kStarCtaU>(star0, star_len, share * (kOvThreads / 32) + warp,
+                                  kOvShare * (kOvThreads / 32), s, crec, dq, qn, hz4, ngat, look);
   }
   flush_sp(cnt_sp, csp);
   flush_cand(cand, ncand, ngat);

@@ -1420,6 +1420,26 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
           const uint32_t* ox = cta_tier ? over2_x.p : over_x.p;
           const unsigned int* on = cta_tier ? over2_n.p : over_n.p;
           const uint64_t words = (D + 31) / 32;
+          if (env_u32("D3G_OV_SHARED", 1, 0, 1)) {
+            // shared bitmaps, kOvShare CTAs per x, in rounds of at most ~1 GB
+            // of bitmaps (dense_cold_shared_kernel): insert launch, star launch
+            const uint32_t per_round = (uint32_t)std::max<uint64_t>(
+                1, std::min<uint64_t>(n_over2, (1ull << 30) / (words * 4)));
+            DBuf<uint32_t> gbm = X.alloc<uint32_t>((uint64_t)per_round * words);
+            tier("bitmap (shared)", [&] {
+              for (uint32_t lo = 0; lo < n_over2; lo += per_round) {
+                const uint32_t xn = std::min<uint32_t>(per_round, n_over2 - lo);
+                D3G_CUDA(cudaMemsetAsync(gbm.p, 0, (uint64_t)xn * words * 4, X.stream));
+                for (int phase = 0; phase < 2; ++phase)
+                  with_mode(mode, [&](auto M) {
+                    D3G_LAUNCH(X, dense_cold_shared_kernel<decltype(M)::value>, xn * kOvShare,
+                               kOvThreads, kOvSmem, ox, lo, xn, phase, in.r_ptr, in.r_col,
+                               cptr_buf.p, crec.p, hz4, reinterpret_cast<const uint4*>(hx.p), Y,
+                               var_bits, vskip, dlz, gbm.p, words, dec, em, tc, cnt_sp, cand);
+                  });
+              }
+            });
+          } else {
           const unsigned og = (unsigned)std::min<uint64_t>(
               (uint64_t)n_over2,
               (uint64_t)env_u32("D3G_OVERFLOW_CTAS", X.sm_count * kOvPerSm, 1, X.sm_count * 16));
@@ -1431,6 +1451,7 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
                        reinterpret_cast<const uint4*>(hx.p), Y, var_bits, vskip, dlz, gbm.p, words,
                        dec, em, tc, cnt_sp, touched.p, cand);
           }); });
+          }
         }
         out.cold_overflow2 = n_over2;
       } else {

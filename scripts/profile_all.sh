@@ -18,7 +18,7 @@ cap() {  # name, kernel regex, count, config
   ncu -i $o/$1.ncu-rep --page raw --csv > $o/$1.csv 2>/dev/null
 }
 cap r02_cfg5_ncu_hotpass dense_hot_jt_kernel 1 5
-cap r02_cfg5_ncu_cold "dense_cold_(hash|cta|overflow)_kernel" 3 5
+cap r02_cfg5_ncu_cold "dense_cold_(hash|cta|overflow|shared)_kernel" 4 5
 cap r02_cfg5_ncu_build "bucket_scatter|csr_region_scatter|csr_bucket_build|value_hist|dense_list_fill|row_sort_small|hx_build_rows|hot_T_from_hx|cold_hist|cold_scatter" 14 5
 cap r02_cfg2_ncu_hot_cold "dense_hot_jt_kernel|dense_cold_kernel" 2 2
 rm -f $o/r02_cfg5_ncu_build.ncu-rep $o/r02_cfg2_ncu_hot_cold.ncu-rep
