@@ -510,7 +510,7 @@ def main():
         ach_c = cold_bytes / (cold_ms * 1e-3) / 1e9
         cold_roof = {"kernel": "DenseEC P2 cold residual pass (dense_cold_kernel, or "
                                "dense_cold_hash_kernel + dense_cold_cta_kernel + "
-                               "dense_cold_overflow_kernel)",
+                               "dense_cold_shared_kernel)",
                      "bound": "hbm", "achieved": ach_c, "peak": hbm, "unit": "GB/s",
                      "frac": ach_c / hbm, "traffic": _ncu_dram_bytes(cfg_id, "cold"),
                      "work": f"16-byte candidate records x {r0.cold_candidates} + 32-byte exact "
