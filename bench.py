@@ -294,6 +294,16 @@ def cpu_reference_sample(cfg: int, frac: float, threads: int, tables=None, cfg5_
     return est, detail
 
 
+def job_config(cfg_id, mode, world, n_tuples):
+    """The `config` object of the JSON line: the same for both arms (the
+    reference arm runs our arm's config, key for key)."""
+    return {"workload": WORKLOADS[cfg_id], "mode": mode,
+            "count_only": mode != "materialize", "force": "auto",
+            "consts": "test_consts()", "parallelism": f"x-shard x{world}",
+            "l2": "256 MB buffer zeroed between steps (outside the timed device region); "
+                  f"inputs {n_tuples * 8 / 1e6:.0f} MB"}
+
+
 def _sample_text(detail):
     if detail.get("slices") == "cfg5":
         xa, xb = detail["slice_lo"], detail["slice_hi"]
@@ -354,8 +364,7 @@ def run_reference(args):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u32", "data": "synthetic (convention G)",
-        "config": {"workload": WORKLOADS[cfg], "count_only": True, "force": "auto",
-                   "consts": "test_consts()"},
+        "config": job_config(cfg, "count", world, n_tuples),
         "cpu_baseline": {"value": value, "unit": "tuples/s", "cores": threads, "kind": "reference",
                          "cpu_model": cpu_model(),
                          "extrapolated": detail.get("strategy") != "classical",
@@ -668,11 +677,7 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec_per_step * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (convention G, generated on device)",
-        "config": {"workload": WORKLOADS[cfg_id], "mode": args.mode,
-                   "count_only": args.mode != "materialize", "force": "auto",
-                   "consts": "test_consts()", "parallelism": f"x-shard x{world}",
-                   "l2": "256 MB buffer zeroed between steps (outside the timed device region); "
-                         f"inputs {n_tuples * 8 / 1e6:.0f} MB"},
+        "config": job_config(cfg_id, args.mode, world, n_tuples),
         "pairs_per_sec": total_pairs / sec_per_step, "out_p": total_pairs,
         "roofline": roof, "phases": phases_roof, "phase_ms": phase,
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
