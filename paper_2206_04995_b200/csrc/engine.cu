@@ -830,9 +830,10 @@ void run_dense_hot(Ctx& X, const DenseInputs& in, d3g::Decode dec, int mode, d3g
       // units per SM grow with the batch count: a unit that switches batch
       // reloads the batch's slice table (193 KB), so few batches want few,
       // large units (cfg2, 49 batches: 3/SM, hot 0.33 -> 0.27 ms) and many
-      // batches want finer balance (cfg5, 2442 batches: 16/SM)
+      // batches want finer balance (cfg5, 2442 batches: 8 / 12 / 16 / 24 / 32
+      // per SM -> hot 20.49 / 20.07 / 20.09 / 19.81 / 19.85 ms)
       const uint32_t u_dflt = (uint32_t)std::min<double>(
-          16.0, std::max<double>(2.0, std::round(8.0 * n_batches / X.sm_count)));
+          24.0, std::max<double>(2.0, std::round(8.0 * n_batches / X.sm_count)));
       const double per_unit = std::max(
           256.0, tested / ((double)X.sm_count * env_u32("D3G_UNITS_PER_SM", u_dflt, 1, 64)));
       for (uint32_t q = 0; q < n_kinds; ++q) {
